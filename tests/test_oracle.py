@@ -1,0 +1,294 @@
+"""Pins of the CPU oracle against things other than itself (CPU only).
+
+Each test names what fixes the expected value: brute-force enumeration of the
+definition, closed forms, the paper's worked examples (golden
+fixtures with citations), or the paper's theorems restated independently.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from conftest import golden_graph, load_golden, random_graph
+
+INF = synth.INF_I32
+
+
+# ---------------------------------------------------------------- brute force
+@pytest.mark.parametrize("directed", [True, False])
+@pytest.mark.parametrize("density", [0.3, 1.0])
+def test_fw_equals_bruteforce(rng, directed, density):
+    """FW == exhaustive simple-path enumeration (the definition), n <= 7,
+    weights including 0 and absent edges."""
+    for trial in range(25):
+        n = int(rng.integers(2, 8))
+        W = random_graph(rng, n, directed, density, lo=0, hi=6)
+        assert np.array_equal(oracle.fw(W), oracle.brute_apsp(W)), (trial, W)
+
+
+def test_fw_f64_equals_bruteforce(rng):
+    for trial in range(15):
+        n = int(rng.integers(2, 7))
+        W = random_graph(rng, n, True, 0.7, hi=1, dtype=np.float32)
+        D = oracle.fw(W)
+        B = oracle.brute_apsp(W)
+        assert np.allclose(D, B, rtol=1e-12, atol=0) and np.array_equal(np.isinf(D), np.isinf(B))
+
+
+@pytest.mark.parametrize("directed", [True, False])
+def test_dijkstra_equals_bruteforce_and_fw(rng, directed):
+    for trial in range(20):
+        n = int(rng.integers(2, 8))
+        W = random_graph(rng, n, directed, 0.6, lo=0, hi=9)
+        B = oracle.brute_apsp(W)
+        assert np.array_equal(oracle.dijkstra_rows(W, range(n)), B)
+        assert np.array_equal(oracle.dijkstra_cols(W, range(n)), B)
+    # larger: FW == all-sources Dijkstra
+    W = random_graph(rng, 120, directed, 0.5, lo=1, hi=50)
+    assert np.array_equal(oracle.fw(W), oracle.dijkstra_rows(W, range(120)))
+
+
+def test_dijkstra_pair_path(rng):
+    for trial in range(30):
+        n = int(rng.integers(2, 8))
+        W = random_graph(rng, n, True, 0.5, lo=1, hi=9)
+        s, t = rng.choice(n, 2, replace=False)
+        d, path = oracle.dijkstra_pair(W, int(s), int(t))
+        assert d == oracle.brute(W, int(s), int(t))
+        if d == INF:
+            assert path == []
+        else:
+            assert oracle.path_is_valid(W, path, s, t)
+            assert oracle.path_weight(W, path) == d
+
+
+# ---------------------------------------------------------------- closed forms
+def cycle(n, w=1):
+    W = np.full((n, n), INF, np.int32)
+    np.fill_diagonal(W, 0)
+    W[np.arange(n), (np.arange(n) + 1) % n] = w
+    return W
+
+
+def test_closed_form_directed_cycle():
+    n = 37
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    assert np.array_equal(oracle.fw(cycle(n)), ((j - i) % n).astype(np.int32))
+
+
+def test_closed_form_undirected_path():
+    n = 40
+    W = np.full((n, n), INF, np.int32)
+    np.fill_diagonal(W, 0)
+    a = np.arange(n - 1)
+    W[a, a + 1] = 1
+    W[a + 1, a] = 1
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    assert np.array_equal(oracle.fw(W), np.abs(i - j).astype(np.int32))
+
+
+def test_closed_form_uniform_complete():
+    n, c = 30, 7
+    W = np.full((n, n), c, np.int32)
+    np.fill_diagonal(W, 0)
+    assert np.array_equal(oracle.fw(W), W)
+
+
+def test_closed_form_star():
+    n = 25
+    a = np.arange(1, n) * 3 % 11 + 1
+    W = np.full((n, n), INF, np.int32)
+    np.fill_diagonal(W, 0)
+    W[0, 1:] = a
+    W[1:, 0] = a
+    D = oracle.fw(W)
+    exp = np.zeros((n, n), np.int64)
+    exp[0, 1:] = a
+    exp[1:, 0] = a
+    exp[1:, 1:] = a[:, None] + a[None, :]
+    np.fill_diagonal(exp, 0)
+    assert np.array_equal(D, exp.astype(np.int32))
+
+
+def test_closed_form_line_metric_is_fixpoint(rng):
+    x = np.sort(rng.integers(0, 1000, 50))
+    W = np.abs(x[:, None] - x[None, :]).astype(np.int32)
+    assert np.array_equal(oracle.fw(W), W)
+
+
+def test_closed_form_grid_manhattan():
+    r, c = 6, 7
+    n = r * c
+    W = np.full((n, n), INF, np.int32)
+    np.fill_diagonal(W, 0)
+    for a in range(r):
+        for b in range(c):
+            p = a * c + b
+            if b + 1 < c:
+                W[p, p + 1] = W[p + 1, p] = 1
+            if a + 1 < r:
+                W[p, p + c] = W[p + c, p] = 1
+    D = oracle.fw(W)
+    ra, ca = np.divmod(np.arange(n), c)
+    exp = np.abs(ra[:, None] - ra[None, :]) + np.abs(ca[:, None] - ca[None, :])
+    assert np.array_equal(D, exp.astype(np.int32))
+
+
+def test_fw_idempotent_metric_closure(rng):
+    W = random_graph(rng, 60, True, 0.4, lo=1, hi=20)
+    D = oracle.fw(W)
+    assert np.array_equal(oracle.fw(D), D)
+    oracle.check_invariants(D, W)
+
+
+def test_unreachable_is_inf():
+    W = np.array([[0, 5], [INF, 0]], np.int32)
+    assert np.array_equal(oracle.fw(W), W)
+
+
+# ------------------------------------------------------- paper theorems (pins)
+def test_theorem2_3_add_node_identities(rng):
+    """Theorems 2 / theo_2_back / 3, restated in numpy from the
+    paper's statements, agree with FW of the grown graph."""
+    for trial in range(20):
+        n = int(rng.integers(2, 30))
+        Wg = random_graph(rng, n + 1, True, 0.7, lo=0, hi=9).astype(np.int64)
+        Wg[Wg >= INF] = oracle.INF64
+        W = Wg[:n, :n]
+        D = oracle.to_oracle(oracle.fw(W.clip(max=INF).astype(np.int32)))
+        out_w, in_w = Wg[n, :n], Wg[:n, n]
+        row = (out_w[:, None] + D).min(axis=0)      # Thm 2: min_t d(x,t) + SPD(t,r)
+        col = (D + in_w[None, :]).min(axis=1)       # theo_2_back: min_t SPD(r,t) + d(t,x)
+        old = np.minimum(D, col[:, None] + row[None, :])  # Thm 3: min(x1, t1 + t2)
+        full = oracle.to_oracle(oracle.fw(np.where(Wg >= oracle.INF64, INF, Wg).astype(np.int32)))
+        clip = lambda a: np.minimum(a, oracle.INF64)
+        assert np.array_equal(clip(full[:n, :n]), clip(old))
+        assert np.array_equal(clip(full[n, :n]), clip(row))
+        assert np.array_equal(clip(full[:n, n]), clip(col))
+
+
+def test_golden_add_one_node():
+    g = load_golden("add_one_node.json")
+    W = np.array([[0, g["in_w"][0]], [g["out_w"][0], 0]], np.int32)
+    # new node p has index 1: W[p][0] = out (d(p,G_0)), W[0][p] = in (d(G_0,p))
+    assert oracle.fw(W).tolist() == g["expected"]
+
+
+# ---------------------------------------------------- Theorem-4 / Corollary 3
+def _remove_from(W, k):
+    keep = [i for i in range(W.shape[0]) if i != k]
+    return W[np.ix_(keep, keep)], keep
+
+
+@pytest.mark.parametrize("directed", [True, False])
+def test_need_update_removal_is_safe(rng, directed):
+    """Corollary 3: every pair NOT in need_update_list keeps its
+    distance after removing k.  Monotonicity: nothing decreases."""
+    for trial in range(60):
+        n = int(rng.integers(3, 12))
+        W = random_graph(rng, n, directed, float(rng.choice([0.3, 1.0])), lo=0, hi=6)
+        D = oracle.fw(W)
+        k = int(rng.integers(n))
+        m = oracle.need_update_removal(D, k)
+        W2, keep = _remove_from(W, k)
+        D2 = oracle.fw(W2)
+        Dk = D[np.ix_(keep, keep)]
+        mk = m[np.ix_(keep, keep)]
+        assert np.array_equal(D2[~mk], Dk[~mk])
+        assert np.all(D2 >= Dk)
+
+
+@pytest.mark.parametrize("directed", [True, False])
+def test_need_update_increase_is_safe(rng, directed):
+    for trial in range(60):
+        n = int(rng.integers(3, 12))
+        W = random_graph(rng, n, directed, 1.0, lo=1, hi=6)
+        D = oracle.fw(W)
+        u, v = (int(x) for x in rng.choice(n, 2, replace=False))
+        w_old = int(W[u, v])
+        w_new = int(rng.choice([w_old + 1, w_old + 5, INF]))
+        m = oracle.need_update_increase(D, u, v, w_old, directed)
+        W2 = W.copy()
+        W2[u, v] = w_new
+        if not directed:
+            W2[v, u] = w_new
+        D2 = oracle.fw(W2)
+        assert np.array_equal(D2[~m], D[~m])
+        assert np.all(D2 >= D)
+
+
+def test_golden_hub_remove():
+    g = load_golden("hub_remove.json")
+    W, idx = golden_graph(g)
+    D = oracle.fw(W)
+    k = idx[g["remove"]]
+    m = oracle.need_update_removal(D, k)
+    names = g["nodes"]
+    lists = {names[i]: [names[j] for j in np.nonzero(m[i])[0]] for i in range(len(names)) if m[i].any()}
+    assert lists == g["need_update_list"]
+    phi, c = oracle.cost(m, len(names))
+    assert c == g["cost"]
+    W2, keep = _remove_from(W, k)
+    D2 = oracle.fw(W2)
+    kn = [names[i] for i in keep]
+    for pair, val in g["after"].items():
+        a, b = pair.split("-")
+        assert D2[kn.index(a), kn.index(b)] == val
+
+
+def test_golden_star_avoided_remove():
+    g = load_golden("star_avoided_remove.json")
+    W, idx = golden_graph(g)
+    D = oracle.fw(W)
+    m = oracle.need_update_removal(D, idx[g["remove"]])
+    assert not m.any()
+    assert oracle.cost(m, 4)[1] == g["cost"]
+
+
+def test_remove_isolated_node_lists_empty(rng):
+    W = random_graph(rng, 9, True, 1.0, lo=1, hi=9)
+    W[4, :] = INF
+    W[:, 4] = INF
+    W[4, 4] = 0
+    assert not oracle.need_update_removal(oracle.fw(W), 4).any()
+
+
+# ------------------------------------------------------------- candidates
+def test_golden_hub_query():
+    g = load_golden("hub_query.json")
+    W, idx = golden_graph(g)
+    D = oracle.fw(W)
+    s, t = (idx[a] for a in g["query"])
+    c = oracle.candidates(D, s, t)
+    assert sorted(g["nodes"][i] for i in c) == sorted(g["candidates"])
+    d, path = oracle.dijkstra_pair(W, s, t)
+    assert d == g["dist"] and [g["nodes"][i] for i in path] == g["path"]
+
+
+def test_candidates_contain_every_shortest_path_node(rng):
+    """Every node of every shortest s-t path satisfies Theorem 4's equality
+    (S:305); on unique-path instances the set is exactly the path."""
+    for trial in range(40):
+        n = int(rng.integers(3, 8))
+        W = random_graph(rng, n, True, 0.8, lo=1, hi=20)
+        D = oracle.fw(W)
+        s, t = (int(x) for x in rng.choice(n, 2, replace=False))
+        c = set(oracle.candidates(D, s, t).tolist())
+        if D[s, t] == INF:
+            assert c == set()
+            continue
+        # enumerate simple paths and keep the shortest ones
+        best = []
+        others = [v for v in range(n) if v not in (s, t)]
+        for r in range(len(others) + 1):
+            for mid in itertools.permutations(others, r):
+                p = [s, *mid, t]
+                if oracle.path_is_valid(W, p, s, t) and oracle.path_weight(W, p) == D[s, t]:
+                    best.append(p)
+        assert best
+        for p in best:
+            assert set(p) <= c
+        if len(best) == 1:
+            assert c == set(best[0])

@@ -1,0 +1,173 @@
+"""ctypes binding of libapsp_warm.so (include/apsp_warm.h) — argument marshalling only.
+
+Every function here has the same name and meaning as its C counterpart; all
+computation happens in the library's CUDA kernels.  There is no fallback:
+if the shared library is missing or fails to load, importing this module
+raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libapsp_warm.so")
+
+APSP_I32, APSP_F32 = 0, 1
+APSP_INF_I32 = 0x3FFFFFFF
+STATUS = {
+    0: "APSP_OK", 1: "APSP_E_INVAL", 2: "APSP_E_RANGE", 3: "APSP_E_CAPACITY", 4: "APSP_E_PRECOND",
+    5: "APSP_E_CUDA", 6: "APSP_E_NCCL", 7: "APSP_E_NOMEM", 8: "APSP_E_POISONED", 9: "APSP_E_UNSUPPORTED",
+}
+OPT_FORCE_PATH, OPT_THETA, OPT_TAU, OPT_MAX_ROUNDS = 0, 1, 2, 3
+
+# exported symbols (tests check the library exports every one of them)
+SYMBOLS = [
+    "apsp_layout", "apsp_workspace_bytes", "apsp_create", "apsp_destroy", "apsp_set_option",
+    "apsp_cold_fw", "apsp_add_node", "apsp_remove_node", "apsp_update_edge", "sp_pair_query",
+    "sp_pair_query_batch", "apsp_size", "apsp_last_error", "apsp_status_string",
+    "apsp_nccl_unique_id", "apsp_kernel_launches",
+]
+
+
+class UpdateInfo(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32), ("early_exit", ctypes.c_int32), ("path", ctypes.c_int32),
+        ("rounds", ctypes.c_int32), ("affected_pairs", ctypes.c_int64),
+        ("affected_rows", ctypes.c_int64), ("max_row_affected", ctypes.c_int64),
+        ("cost", ctypes.c_double), ("n_after", ctypes.c_int64),
+    ]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class ApspError(RuntimeError):
+    def __init__(self, status, msg=""):
+        self.status = status
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2412_15122_b200.build` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    i64, i32, vp, dbl = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_double
+    P = ctypes.POINTER
+    sig = {
+        "apsp_layout": (ctypes.c_int, [i64, ctypes.c_int, ctypes.c_int, P(i64), P(i64), P(i64)]),
+        "apsp_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int, i64, ctypes.c_int]),
+        "apsp_create": (ctypes.c_int, [P(vp), ctypes.c_int, ctypes.c_int, i64, i64, vp, i64, vp, i64, vp,
+                                       ctypes.c_size_t, vp, ctypes.c_int, ctypes.c_int, vp]),
+        "apsp_destroy": (ctypes.c_int, [vp]),
+        "apsp_set_option": (ctypes.c_int, [vp, ctypes.c_int, dbl]),
+        "apsp_cold_fw": (ctypes.c_int, [vp]),
+        "apsp_add_node": (ctypes.c_int, [vp, vp, vp, P(i64), P(UpdateInfo)]),
+        "apsp_remove_node": (ctypes.c_int, [vp, i64, P(i64), P(UpdateInfo)]),
+        "apsp_update_edge": (ctypes.c_int, [vp, i64, i64, dbl, P(UpdateInfo)]),
+        "sp_pair_query": (ctypes.c_int, [vp, i64, i64, vp, P(i32), i32, P(i32), P(i32)]),
+        "sp_pair_query_batch": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, i32, vp, vp]),
+        "apsp_size": (i64, [vp]),
+        "apsp_last_error": (ctypes.c_char_p, [vp]),
+        "apsp_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+        "apsp_nccl_unique_id": (ctypes.c_int, [vp]),
+        "apsp_kernel_launches": (i64, [vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    return L
+
+
+lib = _load()
+
+
+def check(h, status):
+    if status != 0:
+        msg = lib.apsp_last_error(h).decode() if h else lib.apsp_status_string(status).decode()
+        raise ApspError(status, msg)
+
+
+# ---------------------------------------------------------------- same-name wrappers
+def apsp_layout(cap, world=1, rank=0):
+    ld, row0, rows = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    check(None, lib.apsp_layout(cap, world, rank, ctypes.byref(ld), ctypes.byref(row0), ctypes.byref(rows)))
+    return ld.value, row0.value, rows.value
+
+
+def apsp_workspace_bytes(dtype, cap, world=1):
+    return int(lib.apsp_workspace_bytes(dtype, cap, world))
+
+
+def apsp_create(dtype, directed, n, cap, W_ptr, ldw, D_ptr, ld, ws_ptr, ws_bytes, stream, rank=0,
+                world=1, nccl_id=None):
+    h = ctypes.c_void_p()
+    idbuf = None
+    if nccl_id is not None:
+        idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+    st = lib.apsp_create(ctypes.byref(h), dtype, int(directed), n, cap, W_ptr, ldw, D_ptr, ld, ws_ptr,
+                         ws_bytes, stream, rank, world, idbuf)
+    check(None, st)
+    return h
+
+
+def apsp_destroy(h):
+    check(None, lib.apsp_destroy(h))
+
+
+def apsp_set_option(h, opt, value):
+    check(h, lib.apsp_set_option(h, opt, float(value)))
+
+
+def apsp_cold_fw(h):
+    check(h, lib.apsp_cold_fw(h))
+
+
+def apsp_add_node(h, out_ptr, in_ptr):
+    x = ctypes.c_int64()
+    info = UpdateInfo()
+    check(h, lib.apsp_add_node(h, out_ptr, in_ptr, ctypes.byref(x), ctypes.byref(info)))
+    return x.value, info
+
+
+def apsp_remove_node(h, k):
+    mf = ctypes.c_int64()
+    info = UpdateInfo()
+    check(h, lib.apsp_remove_node(h, k, ctypes.byref(mf), ctypes.byref(info)))
+    return mf.value, info
+
+
+def apsp_update_edge(h, u, v, w_new):
+    info = UpdateInfo()
+    check(h, lib.apsp_update_edge(h, u, v, float(w_new), ctypes.byref(info)))
+    return info
+
+
+def sp_pair_query(h, s, t, dtype, path_cap=4096):
+    dist = ctypes.c_int32() if dtype == APSP_I32 else ctypes.c_float()
+    path = (ctypes.c_int32 * max(path_cap, 1))()
+    plen, nc = ctypes.c_int32(), ctypes.c_int32()
+    check(h, lib.sp_pair_query(h, s, t, ctypes.byref(dist), path, path_cap, ctypes.byref(plen),
+                               ctypes.byref(nc)))
+    return dist.value, list(path[: plen.value]), nc.value
+
+
+def sp_pair_query_batch(h, q, s_ptr, t_ptr, dist_ptr, paths_ptr, path_cap, lens_ptr, ncand_ptr):
+    check(h, lib.sp_pair_query_batch(h, q, s_ptr, t_ptr, dist_ptr, paths_ptr, path_cap, lens_ptr, ncand_ptr))
+
+
+def apsp_size(h):
+    return int(lib.apsp_size(h))
+
+
+def apsp_kernel_launches(h):
+    return int(lib.apsp_kernel_launches(h))
+
+
+def apsp_nccl_unique_id():
+    buf = ctypes.create_string_buffer(128)
+    check(None, lib.apsp_nccl_unique_id(buf))
+    return buf.raw

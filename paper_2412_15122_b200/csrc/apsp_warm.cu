@@ -1,0 +1,847 @@
+// apsp_warm.cu — host orchestration behind the C ABI of include/apsp_warm.h.
+//
+// Every step of the hot path runs in the sm_100a kernels of fw.cu, stream.cu,
+// sparse.cu and query.cu; this file validates arguments, takes the O(1) host
+// decisions the paper's algorithms contain (early exits, the cost gate of
+// P:196), carves the caller's workspace, and issues NCCL collectives when D
+// is row-sharded over several GPUs.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/apsp_warm.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace apsp;
+
+namespace {
+
+constexpr int64_t kTile = 128;       // FW pivot block / row-partition granule
+constexpr int kMaxSlabs = 256;       // add-node column partial slabs
+constexpr int64_t kVecs = 8;         // scratch vectors of ld elements
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct Nccl {
+  bool tried = false, ok = false;
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool load() {
+    if (tried) return ok;
+    tried = true;
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+#define SYM(name, field)                                            \
+  field = reinterpret_cast<decltype(field)>(dlsym(h, "nccl" name)); \
+  if (!field) return false;
+    SYM("GetUniqueId", GetUniqueId)
+    SYM("CommInitRank", CommInitRank)
+    SYM("CommDestroy", CommDestroy)
+    SYM("Broadcast", Broadcast)
+    SYM("AllReduce", AllReduce)
+    SYM("Send", Send)
+    SYM("Recv", Recv)
+    SYM("GroupStart", GroupStart)
+    SYM("GroupEnd", GroupEnd)
+    SYM("GetErrorString", GetErrorString)
+#undef SYM
+    ok = true;
+    return true;
+  }
+};
+Nccl g_nccl;
+
+// ------------------------------------------------------------------ workspace plan
+struct Plan {
+  int64_t ld, lcap, maxchunk;
+  size_t off_wt, off_vec, off_rowpart, off_colpart, off_rowoff, off_rowcnt, off_chg, off_prow,
+      off_pcol, off_panel, off_small, total;
+};
+
+// ld: leading dimension of D, also used for WT and every scratch vector.
+Plan make_plan(int64_t cap, int world, int64_t ld) {
+  Plan p;
+  p.ld = ld;
+  p.maxchunk = cdiv(cdiv(p.ld, 4), 256);
+  int64_t lc = cap * cap / 32;
+  p.lcap = std::min<int64_t>(std::max<int64_t>(lc, 1 << 20), (int64_t)1 << 28);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = (size_t)round_up((int64_t)(o + bytes), 256);
+    return at;
+  };
+  p.off_wt = take(sizeof(int32_t) * (size_t)cap * p.ld);
+  p.off_vec = take(sizeof(int32_t) * (size_t)kVecs * p.ld);
+  p.off_rowpart = take(sizeof(int32_t) * (size_t)p.maxchunk * p.ld);
+  p.off_colpart = take(sizeof(int32_t) * (size_t)kMaxSlabs * p.ld);
+  p.off_rowoff = take(sizeof(int64_t) * (size_t)cap);
+  p.off_rowcnt = take(sizeof(int32_t) * (size_t)cap);
+  p.off_chg = take(sizeof(int32_t) * (size_t)cap * 2);
+  p.off_prow = take(sizeof(int32_t) * (size_t)p.lcap);
+  p.off_pcol = take(sizeof(int32_t) * (size_t)p.lcap);
+  p.off_panel = take(world > 1 ? sizeof(int32_t) * (size_t)kTile * p.ld : 256);
+  p.off_small = take(64 * 1024);
+  p.total = o;
+  return p;
+}
+
+void layout_rows(int64_t cap, int world, int rank, int64_t* row0, int64_t* rows) {
+  int64_t R = world > 1 ? round_up(cdiv(cap, world), kTile) : cap;
+  int64_t r0 = std::min<int64_t>((int64_t)rank * R, cap);
+  *row0 = r0;
+  *rows = std::max<int64_t>(0, std::min<int64_t>(R, cap - r0));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ handle
+struct apsp_handle {
+  apsp_dtype dt;
+  int directed;
+  int64_t n, cap, ld;
+  void* D;
+  int64_t row0, rows;            // local row block [row0, row0 + rows)
+  int64_t R;                     // rows per rank (partition granule)
+  unsigned char* ws;
+  Plan plan;
+  cudaStream_t st;
+  int rank, world;
+  ncclComm_t comm = nullptr;
+  // options
+  int force_path = 0;
+  double theta = 0.02;
+  float tau = 1e-5f;
+  int max_rounds = 64;
+  // state
+  bool poisoned = false;
+  std::string err;
+  int64_t launches = 0;
+  void* host_small = nullptr;    // pinned host scratch for small D2H reads
+  // profiling (apsp_profile_*)
+  struct ProfRec { int cls; cudaEvent_t a, b; double work; };
+  bool prof_on = false;
+  std::vector<ProfRec> prof_pending;
+  std::vector<cudaEvent_t> ev_pool;
+  double prof_ms[APSP_K_COUNT] = {};
+  int64_t prof_cnt[APSP_K_COUNT] = {};
+  double prof_work[APSP_K_COUNT] = {};
+  cudaEvent_t ev() {
+    if (ev_pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
+  cudaError_t prof_resolve() {
+    if (prof_pending.empty()) return cudaSuccess;
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    for (auto& r : prof_pending) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, r.a, r.b);
+      prof_ms[r.cls] += ms;
+      prof_cnt[r.cls] += 1;
+      prof_work[r.cls] += r.work;
+      ev_pool.push_back(r.a);
+      ev_pool.push_back(r.b);
+    }
+    prof_pending.clear();
+    return cudaSuccess;
+  }
+
+  template <typename T> T* WT() { return reinterpret_cast<T*>(ws + plan.off_wt); }
+  template <typename T> T* vec(int idx) {
+    return reinterpret_cast<T*>(ws + plan.off_vec) + (size_t)idx * plan.ld;
+  }
+  template <typename T> T* rowpart() { return reinterpret_cast<T*>(ws + plan.off_rowpart); }
+  template <typename T> T* colpart() { return reinterpret_cast<T*>(ws + plan.off_colpart); }
+  int64_t* rowoff() { return reinterpret_cast<int64_t*>(ws + plan.off_rowoff); }
+  int* rowcnt() { return reinterpret_cast<int*>(ws + plan.off_rowcnt); }
+  int* chg(int k) { return reinterpret_cast<int*>(ws + plan.off_chg) + (size_t)k * cap; }
+  int* prow() { return reinterpret_cast<int*>(ws + plan.off_prow); }
+  int* pcol() { return reinterpret_cast<int*>(ws + plan.off_pcol); }
+  template <typename T> T* panel() { return reinterpret_cast<T*>(ws + plan.off_panel); }
+  DetectCounters* ctr() { return reinterpret_cast<DetectCounters*>(ws + plan.off_small); }
+  int* anyflag() { return reinterpret_cast<int*>(ws + plan.off_small + 256); }
+  unsigned char* small() { return ws + plan.off_small + 512; }   // query scratch etc.
+  template <typename T> T* Dl() { return reinterpret_cast<T*>(D); }
+  template <typename T> T* Drow(int64_t gi) { return Dl<T>() + (gi - row0) * ld; }
+  bool local(int64_t gi) const { return gi >= row0 && gi < row0 + rows; }
+  int owner(int64_t gi) const { return world > 1 ? (int)(gi / R) : 0; }
+  Rows active() const {
+    Rows r;
+    r.row0 = row0;
+    r.lo = std::min(row0, n);
+    r.hi = std::min(row0 + rows, n);
+    if (r.hi < r.lo) r.hi = r.lo;
+    return r;
+  }
+};
+
+namespace {
+
+apsp_status fail(apsp_handle* h, apsp_status s, const char* fmt, ...) {
+  if (h) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    h->err = buf;
+    if (s == APSP_E_CUDA || s == APSP_E_NCCL) h->poisoned = true;
+  }
+  return s;
+}
+
+// Launch a kernel class `cls` with algorithmic work `wk`; with profiling on,
+// bracket it with CUDA events on the handle's stream.
+#define PK(cls, wk, expr)                                                                 \
+  do {                                                                                    \
+    cudaEvent_t _a = nullptr;                                                             \
+    if (h->prof_on) {                                                                     \
+      _a = h->ev();                                                                       \
+      cudaEventRecord(_a, h->st);                                                         \
+    }                                                                                     \
+    cudaError_t _e = (expr);                                                              \
+    ++h->launches;                                                                        \
+    if (_e != cudaSuccess)                                                                \
+      return fail(h, APSP_E_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));       \
+    if (h->prof_on) {                                                                     \
+      cudaEvent_t _b = h->ev();                                                           \
+      cudaEventRecord(_b, h->st);                                                         \
+      h->prof_pending.push_back({(int)(cls), _a, _b, (double)(wk)});                      \
+    }                                                                                     \
+  } while (0)
+#define CK(expr) PK(APSP_K_OTHER, 0, expr)
+#define CKR(expr)                                                                         \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(h, APSP_E_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));       \
+  } while (0)
+#define NK(expr)                                                                          \
+  do {                                                                                    \
+    ncclResult_t _r = (expr);                                                             \
+    if (_r != ncclSuccess)                                                                \
+      return fail(h, APSP_E_NCCL, "%s failed: %s", #expr, g_nccl.GetErrorString(_r));    \
+  } while (0)
+#define CHECK_HANDLE(h)                                                                   \
+  do {                                                                                    \
+    if (!(h)) return APSP_E_INVAL;                                                        \
+    if ((h)->poisoned) return APSP_E_POISONED;                                            \
+  } while (0)
+
+template <typename T> ncclDataType_t nccl_type();
+template <> ncclDataType_t nccl_type<int32_t>() { return ncclInt32; }
+template <> ncclDataType_t nccl_type<float>() { return ncclFloat32; }
+
+// broadcast a length-`count` vector from the rank owning global row `gi`
+template <typename T>
+apsp_status bcast_from_owner(apsp_handle* h, T* buf, int64_t count, int64_t gi) {
+  if (h->world <= 1) return APSP_OK;
+  NK(g_nccl.Broadcast(buf, buf, (size_t)count, nccl_type<T>(), h->owner(gi), h->comm, h->st));
+  return APSP_OK;
+}
+
+// snapshot row gi of D (+ add) into out (padded to ld with INF), all ranks
+template <typename T>
+apsp_status snap_row(apsp_handle* h, int64_t gi, T add, T* out) {
+  if (h->local(gi)) CK(copy_vec<T>(h->Drow<T>(gi), h->n, h->ld, add, out, h->st));
+  return bcast_from_owner<T>(h, out, h->ld, gi);
+}
+
+// ------------------------------------------------------------------ cold FW
+// Blocked FW over the current D (the dense fallback a7 runs it on D0).
+template <typename T>
+apsp_status fw_impl(apsp_handle* h) {
+  const int64_t n = h->n, ld = h->ld;
+  Rows r = h->active();
+  const int64_t m = r.hi - r.lo;   // local active rows (local row 0 = global row0)
+  T* D = h->Dl<T>();
+  for (int64_t K0 = 0; K0 < n; K0 += kTile) {
+    const int kb = (int)std::min<int64_t>(kTile, n - K0);
+    const bool own = h->local(K0);
+    const int64_t lk = K0 - h->row0;    // local row of the pivot block (if own)
+    T* P;
+    if (own) {
+      T* rowK = D + lk * ld;
+      PK(APSP_K_FW_DIAG, (double)kb * kb * kb, fw_diag<T>(rowK + K0, ld, kb, h->st));
+      PK(APSP_K_FW_PANEL, (double)kb * kb * (n - kb), fw_row_panel<T>(rowK, ld, K0, kb, n, h->st));
+      P = rowK;
+    } else {
+      P = h->panel<T>();
+    }
+    if (h->world > 1) {
+      NK(g_nccl.Broadcast(P, P, (size_t)kb * ld, nccl_type<T>(), h->owner(K0), h->comm, h->st));
+    }
+    const int skip_ti = own ? (int)(lk / kTile) : -1;
+    if (m > 0) {
+      const double mo = (double)(m - (own ? kb : 0));   // rows outside the pivot block
+      PK(APSP_K_FW_PANEL, mo * kb * kb, fw_col_panel<T>(D, ld, m, K0, kb, P + K0, ld, skip_ti, h->st));
+      PK(APSP_K_FW_TILE, mo * (double)(n - kb) * kb,
+         fw_rest<T>(D, ld, m, n, K0, kb, P, ld, skip_ti, h->st));
+    }
+  }
+  return APSP_OK;
+}
+
+// Cold start (a1): D := W, then blocked FW.
+template <typename T>
+apsp_status cold_fw_impl(apsp_handle* h) {
+  CK(init_d<T>(h->Dl<T>(), h->ld, h->active(), h->n, h->WT<T>(), h->ld, h->st));
+  return fw_impl<T>(h);
+}
+
+// ------------------------------------------------------------------ detect + recompute
+// Shared by remove_node (skip = k, tombstone) and edge increases (skip = -1).
+// c1/r1 (and c2/r2 when undirected increase) must be set up by the caller.
+template <typename T>
+apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, const T* c2,
+                      const T* r2, bool removal, apsp_update_info* info) {
+  const int64_t n = h->n;
+  Rows r = h->active();
+  CKR(cudaMemsetAsync(h->rowcnt(), 0, sizeof(int) * h->cap, h->st));
+  CKR(cudaMemsetAsync(h->ctr(), 0, sizeof(DetectCounters), h->st));
+  PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
+     detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, h->WT<T>(), h->ld, 1,
+               h->rowoff(), h->rowcnt(), h->prow(), h->pcol(), h->plan.lcap, h->ctr(), 0, h->st));
+  if (removal) CK(tombstone<T>(h->Dl<T>(), h->ld, r, n, skip, h->WT<T>(), h->ld, h->st));
+
+  // counters -> host (|A|, Phi, max|A_i|, overflow), summed over ranks
+  unsigned long long* hs = reinterpret_cast<unsigned long long*>(h->host_small);
+  DetectCounters* hc = reinterpret_cast<DetectCounters*>(h->host_small);
+  CKR(cudaMemcpyAsync(h->host_small, h->ctr(), sizeof(DetectCounters), cudaMemcpyDeviceToHost, h->st));
+  CKR(cudaStreamSynchronize(h->st));
+  int64_t local_total = (int64_t)hc->total;
+  int64_t total = local_total, rows = hc->rows, maxrow = hc->maxrow, overflow = hc->overflow;
+  if (h->world > 1) {
+    // [total, rows, overflow] summed, maxrow by max
+    long long* v = reinterpret_cast<long long*>(h->small());
+    long long hv[4] = {(long long)total, (long long)rows, (long long)overflow, (long long)maxrow};
+    CKR(cudaMemcpyAsync(v, hv, sizeof hv, cudaMemcpyHostToDevice, h->st));
+    NK(g_nccl.AllReduce(v, v, 3, ncclInt64, ncclSum, h->comm, h->st));
+    NK(g_nccl.AllReduce(v + 3, v + 3, 1, ncclInt64, ncclMax, h->comm, h->st));
+    CKR(cudaMemcpyAsync(hs, v, sizeof hv, cudaMemcpyDeviceToHost, h->st));
+    CKR(cudaStreamSynchronize(h->st));
+    total = (int64_t)hs[0]; rows = (int64_t)hs[1]; overflow = (int64_t)hs[2]; maxrow = (int64_t)hs[3];
+  }
+  if (info) {
+    info->affected_pairs = total;
+    info->affected_rows = rows;
+    info->max_row_affected = maxrow;
+    info->cost = removal ? (n > 1 ? (double)rows / (double)(n - 1) : 0.0) : (double)rows / (double)n;
+  }
+  bool dense = h->force_path == 2 ||
+               (h->force_path == 0 && (double)total > h->theta * (double)n * (double)n) ||
+               overflow != 0;
+  if (dense) {
+    if (info) info->path = 3;
+    return fw_impl<T>(h);
+  }
+  if (info) info->path = 2;
+  if (total == 0) return APSP_OK;
+  // sparse: round 0 over all m, then rounds over A_i until no entry changes
+  if (local_total > 0)
+    PK(APSP_K_SPARSE0, 8.0 * (double)local_total * (double)n,
+       sparse_round0<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, n, h->prow(), h->pcol(),
+                        local_total, h->st));
+  int in = 0;
+  CKR(cudaMemsetAsync(h->chg(in), 1, sizeof(int) * h->cap, h->st));
+  int rounds = 1;
+  bool converged = (maxrow <= 1);
+  int* hflag = reinterpret_cast<int*>(h->host_small);
+  for (; !converged && rounds <= h->max_rounds; ++rounds) {
+    CKR(cudaMemsetAsync(h->chg(in ^ 1), 0, sizeof(int) * h->cap, h->st));
+    CKR(cudaMemsetAsync(h->anyflag(), 0, sizeof(int), h->st));
+    if (local_total > 0)
+      PK(APSP_K_SPARSE_R, 0.0, sparse_round<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, n, h->prow(), h->pcol(),
+                         local_total, h->rowoff(), h->rowcnt(), h->chg(in), h->chg(in ^ 1),
+                         h->anyflag(), h->st));
+    if (h->world > 1)
+      NK(g_nccl.AllReduce(h->anyflag(), h->anyflag(), 1, ncclInt32, ncclMax, h->comm, h->st));
+    CKR(cudaMemcpyAsync(hflag, h->anyflag(), sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    CKR(cudaStreamSynchronize(h->st));
+    if (*hflag == 0) converged = true;
+    in ^= 1;
+  }
+  if (info) info->rounds = rounds;
+  if (!converged) {
+    // still exact: every entry is a valid upper bound >= the true distance
+    if (info) info->path = 3;
+    return fw_impl<T>(h);
+  }
+  return APSP_OK;
+}
+
+// ------------------------------------------------------------------ add node
+template <typename T>
+apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, int64_t* new_index,
+                          apsp_update_info* info) {
+  const int64_t n = h->n, ld = h->ld, x = n;
+  T* ow = h->vec<T>(0);
+  T* iw = h->vec<T>(1);
+  T* col = h->vec<T>(2);
+  T* row = h->vec<T>(3);
+  CKR(cudaMemsetAsync(&h->ctr()->err, 0, sizeof(unsigned), h->st));
+  CK(validate_vec<T>(reinterpret_cast<const T*>(out_w), nullptr, n, ld, ow, &h->ctr()->err, h->st));
+  CK(validate_vec<T>(reinterpret_cast<const T*>(in_w),
+                     h->directed ? nullptr : reinterpret_cast<const T*>(out_w), n, ld, iw,
+                     &h->ctr()->err, h->st));
+  unsigned* herr = reinterpret_cast<unsigned*>(h->host_small);
+  CKR(cudaMemcpyAsync(herr, &h->ctr()->err, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+  CKR(cudaStreamSynchronize(h->st));
+  if (*herr) {
+    return fail(h, APSP_E_INVAL, "add_node: %s",
+                (*herr & 2) ? "undirected graph needs out_w == in_w" : "negative or NaN weight");
+  }
+  Rows r = h->active();
+  int nchunk = 0, nslab = 0;
+  PK(APSP_K_ADD_PASS1, 4.0 * (double)(r.hi - r.lo) * (double)n,
+     addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), h->colpart<T>(), ld, &nchunk,
+                      &nslab, kMaxSlabs, h->st));
+  CK(addnode_finish<T>(h->rowpart<T>(), nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col, row, h->st));
+  if (h->world > 1)
+    NK(g_nccl.AllReduce(row, row, (size_t)ld, nccl_type<T>(), ncclMin, h->comm, h->st));
+  PK(APSP_K_RANK1, 4.0 * (double)(r.hi - r.lo) * (double)n,
+     rank1<T>(h->Dl<T>(), ld, r, n, col, row, nullptr, nullptr, h->st));
+  CK(addnode_write<T>(h->Dl<T>(), ld, r, n, x, h->local(x) ? 1 : 0, col, row, h->WT<T>(), ld, ow,
+                      iw, h->st));
+  h->n = n + 1;
+  if (new_index) *new_index = x;
+  if (info) {
+    info->kind = 3;
+    info->path = 1;
+    info->n_after = h->n;
+  }
+  return APSP_OK;
+}
+
+// ------------------------------------------------------------------ remove node
+template <typename T>
+apsp_status remove_node_impl(apsp_handle* h, int64_t k, int64_t* moved_from, apsp_update_info* info) {
+  const int64_t n = h->n, ld = h->ld;
+  Rows r = h->active();
+  T* c1 = h->vec<T>(4);
+  T* r1 = h->vec<T>(5);
+  CK(gather_col<T>(h->Dl<T>(), ld, r, k, T(0), c1, h->st));   // t1 = SPD(i, k)
+  apsp_status s = snap_row<T>(h, k, T(0), r1);                 // t2 = SPD(k, j)
+  if (s != APSP_OK) return s;
+  if (info) info->kind = 4;
+  s = recompute<T>(h, k, c1, r1, nullptr, nullptr, true, info);
+  if (s != APSP_OK) return s;
+
+  // swap-with-last: node n-1 moves into slot k (Q7)
+  const int64_t last = n - 1;
+  T* WT = h->WT<T>();
+  const T I = Tr<T>::inf();
+  if (k != last) {
+    const bool ok_k = h->local(k), ok_l = h->local(last);
+    if (ok_k && ok_l) {
+      CK(copy_row<T>(h->Drow<T>(k), h->Drow<T>(last), n, h->st));
+    } else if (ok_k || ok_l) {
+      NK(g_nccl.GroupStart());
+      if (ok_l) NK(g_nccl.Send(h->Drow<T>(last), (size_t)n, nccl_type<T>(), h->owner(k), h->comm, h->st));
+      if (ok_k) NK(g_nccl.Recv(h->Drow<T>(k), (size_t)n, nccl_type<T>(), h->owner(last), h->comm, h->st));
+      NK(g_nccl.GroupEnd());
+    }
+    CK(copy_row<T>(WT + k * ld, WT + last * ld, n, h->st));
+    Rows rc = r;     // rows [lo, hi) with hi <= n: includes the new row k, excludes row last
+    rc.hi = std::min(rc.hi, last);
+    CK(copy_col<T>(h->Dl<T>(), ld, rc, k, last, h->st));
+    Rows rw{0, last, 0};
+    CK(copy_col<T>(WT, ld, rw, k, last, h->st));
+  }
+  // clear the vacated slot n-1
+  if (h->local(last)) CK(fill<T>(h->Drow<T>(last), n, I, h->st));
+  CK(fill_col<T>(h->Dl<T>(), ld, r, last, I, h->st));
+  CK(fill<T>(WT + last * ld, n, I, h->st));
+  Rows rw{0, n, 0};
+  CK(fill_col<T>(WT, ld, rw, last, I, h->st));
+  h->n = n - 1;
+  if (moved_from) *moved_from = (k != last) ? last : -1;
+  if (info) info->n_after = h->n;
+  return APSP_OK;
+}
+
+// ------------------------------------------------------------------ update edge
+template <typename T>
+apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp_update_info* info) {
+  const int64_t n = h->n, ld = h->ld;
+  T* WT = h->WT<T>();
+  // 8-byte read: W[u][v] (replicated WT) and D[u][v] (owner of row u)
+  T* dev2 = reinterpret_cast<T*>(h->small());
+  CKR(cudaMemcpyAsync(dev2, WT + v * ld + u, sizeof(T), cudaMemcpyDeviceToDevice, h->st));
+  if (h->local(u))
+    CKR(cudaMemcpyAsync(dev2 + 1, h->Drow<T>(u) + v, sizeof(T), cudaMemcpyDeviceToDevice, h->st));
+  if (h->world > 1)
+    NK(g_nccl.Broadcast(dev2 + 1, dev2 + 1, 1, nccl_type<T>(), h->owner(u), h->comm, h->st));
+  T* hv = reinterpret_cast<T*>(h->host_small);
+  CKR(cudaMemcpyAsync(hv, dev2, 2 * sizeof(T), cudaMemcpyDeviceToHost, h->st));
+  CKR(cudaStreamSynchronize(h->st));
+  const T w_old = hv[0], duv = hv[1];
+  if (info) info->n_after = n;
+  if (w_new == w_old) {
+    if (info) { info->kind = 0; info->early_exit = 1; }
+    return APSP_OK;
+  }
+  Rows r = h->active();
+  T* c1 = h->vec<T>(4);
+  T* r1 = h->vec<T>(5);
+  T* c2 = h->vec<T>(6);
+  T* r2 = h->vec<T>(7);
+  const bool und = !h->directed;
+  if (w_new < w_old) {
+    // ---- decrease: exact early exit iff w_new >= D[u][v] ----
+    if (info) info->kind = 1;
+    if (!(w_new < duv)) {
+      if (info) info->early_exit = 1;
+      CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
+      return APSP_OK;
+    }
+    // D'[i][j] = min(D[i][j], D[i][u] + w + D[v][j] (, D[i][v] + w + D[u][j]))
+    CK(gather_col<T>(h->Dl<T>(), ld, r, u, w_new, c1, h->st));
+    apsp_status s = snap_row<T>(h, v, T(0), r1);
+    if (s != APSP_OK) return s;
+    if (und) {
+      CK(gather_col<T>(h->Dl<T>(), ld, r, v, w_new, c2, h->st));
+      s = snap_row<T>(h, u, T(0), r2);
+      if (s != APSP_OK) return s;
+    }
+    PK(APSP_K_RANK1, 4.0 * (double)(r.hi - r.lo) * (double)n,
+       rank1<T>(h->Dl<T>(), ld, r, n, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, h->st));
+    CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
+    if (info) info->path = 1;
+    return APSP_OK;
+  }
+  // ---- increase: exact early exit iff the edge is not tight (w_old > D[u][v]) ----
+  if (info) info->kind = 2;
+  bool tight;
+  if (Tr<T>::kFloat) tight = (double)w_old <= (double)duv * (1.0 + (double)h->tau);
+  else tight = (w_old == duv);
+  if (!tight) {
+    if (info) info->early_exit = 1;
+    CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
+    return APSP_OK;
+  }
+  CK(gather_col<T>(h->Dl<T>(), ld, r, u, w_old, c1, h->st));   // D[i][u] + w_old
+  apsp_status s = snap_row<T>(h, v, T(0), r1);                  // D[v][j]
+  if (s != APSP_OK) return s;
+  if (und) {
+    CK(gather_col<T>(h->Dl<T>(), ld, r, v, w_old, c2, h->st));
+    s = snap_row<T>(h, u, T(0), r2);
+    if (s != APSP_OK) return s;
+  }
+  CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));   // W' before the D0 reset
+  return recompute<T>(h, -1, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, false, info);
+}
+
+// ------------------------------------------------------------------ query
+template <typename T>
+apsp_status query_one(apsp_handle* h, int64_t s, int64_t t, void* dist, int32_t* path,
+                      int32_t path_cap, int32_t* path_len, int32_t* n_candidates) {
+  // device scratch: [s, t, len, ncand, dist] then the path
+  int* dv = reinterpret_cast<int*>(h->small() + 1024);
+  T* ddist = reinterpret_cast<T*>(dv + 4);
+  int* dpath = dv + 8;
+  const int cap_dev = (int)((64 * 1024 - 1024 - 512 - 64) / sizeof(int)) - 8;
+  int* hv = reinterpret_cast<int*>(h->host_small);
+  hv[0] = (int)s; hv[1] = (int)t;
+  CKR(cudaMemcpyAsync(dv, hv, 2 * sizeof(int), cudaMemcpyHostToDevice, h->st));
+  PK(APSP_K_QUERY, 8.0 * (double)h->n, query_batch<T>(h->Dl<T>(), h->ld, h->WT<T>(), h->ld, h->n, 1, dv, dv + 1, ddist, dpath, cap_dev,
+                    dv + 2, dv + 3, h->tau, h->st));
+  CKR(cudaMemcpyAsync(hv, dv, 8 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  CKR(cudaStreamSynchronize(h->st));
+  const int len = hv[2], nc = hv[3];
+  std::memcpy(dist, &hv[4], sizeof(T));
+  if (n_candidates) *n_candidates = nc;
+  if (len < 0) {
+    if (path_len) *path_len = 0;
+    return fail(h, APSP_E_RANGE, "sp_pair_query: %d candidates exceed the kernel capacity %d", nc,
+                std::min(kQueryCap, cap_dev));
+  }
+  if (path_len) *path_len = len;
+  if (len > path_cap) return fail(h, APSP_E_RANGE, "sp_pair_query: path_cap %d < path length %d", path_cap, len);
+  if (len > 0) {
+    CKR(cudaMemcpyAsync(path, dpath, sizeof(int) * len, cudaMemcpyDeviceToHost, h->st));
+    CKR(cudaStreamSynchronize(h->st));
+  }
+  return APSP_OK;
+}
+
+template <typename F>
+apsp_status dispatch(apsp_dtype dt, F&& f) {
+  if (dt == APSP_I32) return f(int32_t{});
+  return f(float{});
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+apsp_status apsp_layout(int64_t cap, int world, int rank, int64_t* ld, int64_t* row0, int64_t* rows) {
+  if (cap < 1 || world < 1 || rank < 0 || rank >= world) return APSP_E_INVAL;
+  if (ld) *ld = round_up(cap, 32);
+  int64_t r0, rr;
+  layout_rows(cap, world, rank, &r0, &rr);
+  if (row0) *row0 = r0;
+  if (rows) *rows = rr;
+  return APSP_OK;
+}
+
+size_t apsp_workspace_bytes(apsp_dtype dtype, int64_t cap, int world) {
+  if ((dtype != APSP_I32 && dtype != APSP_F32) || cap < 1 || world < 1) return 0;
+  return make_plan(cap, world, round_up(cap, 32)).total;
+}
+
+const char* apsp_status_string(apsp_status s) {
+  switch (s) {
+    case APSP_OK: return "ok";
+    case APSP_E_INVAL: return "invalid argument";
+    case APSP_E_RANGE: return "out of range";
+    case APSP_E_CAPACITY: return "capacity exceeded";
+    case APSP_E_PRECOND: return "precondition violated";
+    case APSP_E_CUDA: return "CUDA error";
+    case APSP_E_NCCL: return "NCCL error";
+    case APSP_E_NOMEM: return "workspace too small";
+    case APSP_E_POISONED: return "handle poisoned by an earlier failure";
+    case APSP_E_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+apsp_status apsp_nccl_unique_id(void* out128) {
+  if (!out128) return APSP_E_INVAL;
+  if (!g_nccl.load()) return APSP_E_NCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return APSP_E_NCCL;
+  std::memcpy(out128, &id, sizeof id);
+  return APSP_OK;
+}
+
+apsp_status apsp_create(apsp_handle** out, apsp_dtype dtype, int directed, int64_t n, int64_t cap,
+                        const void* W, int64_t ldw, void* D_local, int64_t ld, void* workspace,
+                        size_t workspace_bytes, void* stream, int rank, int world,
+                        const void* nccl_id) {
+  if (!out) return APSP_E_INVAL;
+  *out = nullptr;
+  if (dtype != APSP_I32 && dtype != APSP_F32) return APSP_E_INVAL;
+  if (n < 1 || cap < n || cap > (int64_t)1 << 30 || !W || ldw < n || !D_local || !workspace)
+    return APSP_E_INVAL;
+  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_id)) return APSP_E_INVAL;
+  if (((uintptr_t)workspace & 255) || ((uintptr_t)D_local & 15)) return APSP_E_INVAL;
+  if (ld < round_up(cap, 32) || (ld & 3)) return APSP_E_INVAL;
+  Plan plan = make_plan(cap, world, ld);
+  if (workspace_bytes < plan.total) return APSP_E_NOMEM;
+
+  apsp_handle* h = new apsp_handle();
+  h->dt = dtype;
+  h->directed = directed ? 1 : 0;
+  h->n = n;
+  h->cap = cap;
+  h->ld = ld;
+  h->plan = plan;
+  h->D = D_local;
+  layout_rows(cap, world, rank, &h->row0, &h->rows);
+  h->R = world > 1 ? round_up(cdiv(cap, world), kTile) : cap;
+  h->ws = reinterpret_cast<unsigned char*>(workspace);
+  h->st = reinterpret_cast<cudaStream_t>(stream);
+  h->rank = rank;
+  h->world = world;
+  if (cudaHostAlloc(&h->host_small, 4096, cudaHostAllocDefault) != cudaSuccess) {
+    delete h;
+    return APSP_E_CUDA;
+  }
+  if (world > 1) {
+    if (!g_nccl.load()) {
+      cudaFreeHost(h->host_small);
+      delete h;
+      return APSP_E_NCCL;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof id);
+    if (g_nccl.CommInitRank(&h->comm, world, id, rank) != ncclSuccess) {
+      cudaFreeHost(h->host_small);
+      delete h;
+      return APSP_E_NCCL;
+    }
+  }
+  // WT := W^T (replicated), pads INF; validate W (diag 0, w >= 0)
+  apsp_status s = dispatch(dtype, [&](auto z) -> apsp_status {
+    using T = decltype(z);
+    CK(fill<T>(h->WT<T>(), (int64_t)cap * h->ld, Tr<T>::inf(), h->st));
+    CKR(cudaMemsetAsync(&h->ctr()->err, 0, sizeof(unsigned), h->st));
+    CK(transpose_in<T>(reinterpret_cast<const T*>(W), ldw, n, h->WT<T>(), h->ld, &h->ctr()->err, h->st));
+    unsigned* herr = reinterpret_cast<unsigned*>(h->host_small);
+    CKR(cudaMemcpyAsync(herr, &h->ctr()->err, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+    CKR(cudaStreamSynchronize(h->st));
+    if (*herr) return fail(h, APSP_E_INVAL, "create: W has %s", (*herr & 4) ? "a nonzero diagonal" : "a negative/NaN weight");
+    return APSP_OK;
+  });
+  if (s != APSP_OK) {
+    if (h->comm) g_nccl.CommDestroy(h->comm);
+    cudaFreeHost(h->host_small);
+    delete h;
+    return s;
+  }
+  *out = h;
+  return APSP_OK;
+}
+
+apsp_status apsp_destroy(apsp_handle* h) {
+  if (!h) return APSP_E_INVAL;
+  if (h->st) cudaStreamSynchronize(h->st);
+  h->prof_resolve();
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
+  if (h->comm) g_nccl.CommDestroy(h->comm);
+  if (h->host_small) cudaFreeHost(h->host_small);
+  delete h;
+  return APSP_OK;
+}
+
+apsp_status apsp_set_option(apsp_handle* h, apsp_option opt, double value) {
+  CHECK_HANDLE(h);
+  switch (opt) {
+    case APSP_OPT_FORCE_PATH:
+      if (value != 0 && value != 1 && value != 2) return APSP_E_INVAL;
+      h->force_path = (int)value;
+      return APSP_OK;
+    case APSP_OPT_THETA:
+      if (!(value >= 0)) return APSP_E_INVAL;
+      h->theta = value;
+      return APSP_OK;
+    case APSP_OPT_TAU:
+      if (!(value >= 0) || value > 0.1) return APSP_E_INVAL;
+      h->tau = (float)value;
+      return APSP_OK;
+    case APSP_OPT_MAX_ROUNDS:
+      if (!(value >= 1)) return APSP_E_INVAL;
+      h->max_rounds = (int)value;
+      return APSP_OK;
+  }
+  return APSP_E_INVAL;
+}
+
+apsp_status apsp_cold_fw(apsp_handle* h) {
+  CHECK_HANDLE(h);
+  return dispatch(h->dt, [&](auto z) { return cold_fw_impl<decltype(z)>(h); });
+}
+
+apsp_status apsp_add_node(apsp_handle* h, const void* out_w, const void* in_w, int64_t* new_index,
+                          apsp_update_info* info) {
+  CHECK_HANDLE(h);
+  if (info) std::memset(info, 0, sizeof *info);
+  if (!out_w || !in_w) return fail(h, APSP_E_INVAL, "add_node: null edge vector");
+  if (h->n >= h->cap) return fail(h, APSP_E_CAPACITY, "add_node: n == cap == %lld", (long long)h->cap);
+  return dispatch(h->dt, [&](auto z) { return add_node_impl<decltype(z)>(h, out_w, in_w, new_index, info); });
+}
+
+apsp_status apsp_remove_node(apsp_handle* h, int64_t k, int64_t* moved_from, apsp_update_info* info) {
+  CHECK_HANDLE(h);
+  if (info) std::memset(info, 0, sizeof *info);
+  if (k < 0 || k >= h->n) return fail(h, APSP_E_RANGE, "remove_node: k=%lld outside [0,%lld)", (long long)k, (long long)h->n);
+  if (h->n == 1) return fail(h, APSP_E_PRECOND, "remove_node: cannot remove the last node");
+  return dispatch(h->dt, [&](auto z) { return remove_node_impl<decltype(z)>(h, k, moved_from, info); });
+}
+
+apsp_status apsp_update_edge(apsp_handle* h, int64_t u, int64_t v, double w_new, apsp_update_info* info) {
+  CHECK_HANDLE(h);
+  if (info) std::memset(info, 0, sizeof *info);
+  if (u < 0 || u >= h->n || v < 0 || v >= h->n)
+    return fail(h, APSP_E_RANGE, "update_edge: (%lld,%lld) outside [0,%lld)", (long long)u, (long long)v, (long long)h->n);
+  if (u == v) return fail(h, APSP_E_INVAL, "update_edge: u == v (the diagonal is fixed at 0)");
+  if (std::isnan(w_new) || w_new < 0) return fail(h, APSP_E_INVAL, "update_edge: negative or NaN weight");
+  if (h->dt == APSP_I32) {
+    if (std::isfinite(w_new) && w_new != std::floor(w_new))
+      return fail(h, APSP_E_INVAL, "update_edge: non-integral weight on an int32 handle");
+    int32_t w = (w_new >= (double)APSP_INF_I32) ? APSP_INF_I32 : (int32_t)w_new;
+    return update_edge_impl<int32_t>(h, u, v, w, info);
+  }
+  float w = std::isinf(w_new) ? Tr<float>::inf() : (float)w_new;
+  return update_edge_impl<float>(h, u, v, w, info);
+}
+
+apsp_status sp_pair_query(apsp_handle* h, int64_t s, int64_t t, void* dist, int32_t* path,
+                          int32_t path_cap, int32_t* path_len, int32_t* n_candidates) {
+  CHECK_HANDLE(h);
+  if (!dist || !path_len || (path_cap > 0 && !path)) return fail(h, APSP_E_INVAL, "sp_pair_query: null output");
+  if (s < 0 || s >= h->n || t < 0 || t >= h->n) return fail(h, APSP_E_RANGE, "sp_pair_query: id out of range");
+  if (h->world > 1) return fail(h, APSP_E_UNSUPPORTED, "sp_pair_query: row-sharded queries not built yet");
+  return dispatch(h->dt, [&](auto z) {
+    return query_one<decltype(z)>(h, s, t, dist, path, path_cap, path_len, n_candidates);
+  });
+}
+
+apsp_status sp_pair_query_batch(apsp_handle* h, int32_t q, const int32_t* s, const int32_t* t,
+                                void* dist, int32_t* paths, int32_t path_cap, int32_t* path_lens,
+                                int32_t* n_cand) {
+  CHECK_HANDLE(h);
+  if (q < 0 || (q > 0 && (!s || !t || !dist || !path_lens))) return fail(h, APSP_E_INVAL, "query_batch: null argument");
+  if (path_cap > 0 && !paths) return fail(h, APSP_E_INVAL, "query_batch: null paths");
+  if (h->world > 1) return fail(h, APSP_E_UNSUPPORTED, "query_batch: row-sharded queries not built yet");
+  return dispatch(h->dt, [&](auto z) -> apsp_status {
+    using T = decltype(z);
+    PK(APSP_K_QUERY, 8.0 * (double)h->n * q, query_batch<T>(h->Dl<T>(), h->ld, h->WT<T>(), h->ld, h->n, q, s, t, reinterpret_cast<T*>(dist),
+                      paths, path_cap, path_lens, n_cand, h->tau, h->st));
+    return APSP_OK;
+  });
+}
+
+int64_t apsp_size(const apsp_handle* h) { return h ? h->n : -1; }
+
+const char* apsp_last_error(const apsp_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+int64_t apsp_kernel_launches(const apsp_handle* h) { return h ? h->launches : -1; }
+
+apsp_status apsp_profile_enable(apsp_handle* h, int on) {
+  CHECK_HANDLE(h);
+  h->prof_on = on != 0;
+  return APSP_OK;
+}
+
+apsp_status apsp_profile_reset(apsp_handle* h) {
+  CHECK_HANDLE(h);
+  CKR(h->prof_resolve());
+  for (int c = 0; c < APSP_K_COUNT; ++c) { h->prof_ms[c] = 0; h->prof_cnt[c] = 0; h->prof_work[c] = 0; }
+  return APSP_OK;
+}
+
+apsp_status apsp_profile_read(apsp_handle* h, int kernel_class, double* ms, int64_t* launches,
+                              double* work) {
+  CHECK_HANDLE(h);
+  if (kernel_class < 0 || kernel_class >= APSP_K_COUNT) return APSP_E_RANGE;
+  CKR(h->prof_resolve());
+  if (ms) *ms = h->prof_ms[kernel_class];
+  if (launches) *launches = h->prof_cnt[kernel_class];
+  if (work) *work = h->prof_work[kernel_class];
+  return APSP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,130 @@
+// common.cuh — element traits, vector access and launch helpers shared by the
+// sm_100a kernels of libapsp_warm.  Distances live in HBM row-major with a
+// 128-byte-aligned leading dimension; every streaming kernel moves 16-byte
+// vectors (int4 / float4).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define APSP_INF_I32_DEV 0x3FFFFFFF
+
+namespace apsp {
+
+// ---------------------------------------------------------------------------
+// Element traits.  int32: INF = 2^30-1, so a sum of two stored values is at
+// most 2^31-2 (no overflow) and min(.) keeps every stored value <= INF.
+// fp32: INF = +inf (inf + x = inf; weights >= 0, so NaN cannot arise).
+// ---------------------------------------------------------------------------
+template <typename T> struct Tr;
+
+template <> struct Tr<int32_t> {
+  using V4 = int4;
+  static constexpr bool kFloat = false;
+  __host__ __device__ static __forceinline__ int32_t inf() { return APSP_INF_I32_DEV; }
+  __device__ static __forceinline__ int32_t add(int32_t a, int32_t b) { return a + b; }
+  __device__ static __forceinline__ int32_t mn(int32_t a, int32_t b) { return min(a, b); }
+  // relaxation d = min(d, a + b): one VIADDMNMX on sm_100a
+  __device__ static __forceinline__ int32_t relax(int32_t d, int32_t a, int32_t b) {
+    return min(d, a + b);
+  }
+  // clamp a sum of two values back into the storable range
+  __device__ static __forceinline__ int32_t sat(int32_t a) { return min(a, APSP_INF_I32_DEV); }
+  __device__ static __forceinline__ bool fin(int32_t a) { return a < APSP_INF_I32_DEV; }
+  // "lhs == d" of Theorem 4.  lhs >= d always holds for an APSP
+  // matrix, so equality is exact for integers.
+  __device__ static __forceinline__ bool tight(int32_t lhs, int32_t d, float) { return lhs == d; }
+  // order-preserving 32-bit key for argmin (values are >= 0)
+  __device__ static __forceinline__ uint32_t key(int32_t a) { return (uint32_t)a; }
+};
+
+template <> struct Tr<float> {
+  using V4 = float4;
+  static constexpr bool kFloat = true;
+  __host__ __device__ static __forceinline__ float inf() { return __builtin_huge_valf(); }
+  __device__ static __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  __device__ static __forceinline__ float mn(float a, float b) { return fminf(a, b); }
+  __device__ static __forceinline__ float relax(float d, float a, float b) {
+    return fminf(d, __fadd_rn(a, b));
+  }
+  __device__ static __forceinline__ float sat(float a) { return a; }
+  __device__ static __forceinline__ bool fin(float a) { return a < __builtin_huge_valf(); }
+  // DESIGN.md Q4: flag iff lhs <= d * (1 + tau): ties and near-ties go to
+  // "needs update" (a false positive only costs time).
+  __device__ static __forceinline__ bool tight(float lhs, float d, float tau) {
+    return lhs <= d * (1.0f + tau);
+  }
+  // non-negative IEEE floats order like their bit patterns
+  __device__ static __forceinline__ uint32_t key(float a) { return (uint32_t)__float_as_int(a); }
+};
+
+// ---------------------------------------------------------------------------
+// 16-byte vector helpers
+// ---------------------------------------------------------------------------
+template <typename T> struct alignas(16) Vec4 { T x, y, z, w; };
+
+template <typename T>
+__device__ __forceinline__ Vec4<T> ld4(const T* p) {
+  typename Tr<T>::V4 v = *reinterpret_cast<const typename Tr<T>::V4*>(p);
+  return Vec4<T>{v.x, v.y, v.z, v.w};
+}
+// streaming load: bypass L1 allocation (the row is read once)
+template <typename T>
+__device__ __forceinline__ Vec4<T> ld4_stream(const T* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  Vec4<T> o;
+  o.x = *reinterpret_cast<T*>(&r.x);
+  o.y = *reinterpret_cast<T*>(&r.y);
+  o.z = *reinterpret_cast<T*>(&r.z);
+  o.w = *reinterpret_cast<T*>(&r.w);
+  return o;
+}
+// coherent (non-.nc) 16-byte load for data this kernel may also write
+template <typename T>
+__device__ __forceinline__ Vec4<T> ld4_cg(const T* p) {
+  int4 r;
+  asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  Vec4<T> o;
+  o.x = *reinterpret_cast<T*>(&r.x);
+  o.y = *reinterpret_cast<T*>(&r.y);
+  o.z = *reinterpret_cast<T*>(&r.z);
+  o.w = *reinterpret_cast<T*>(&r.w);
+  return o;
+}
+template <typename T>
+__device__ __forceinline__ void st4(T* p, Vec4<T> v) {
+  typename Tr<T>::V4 o;
+  o.x = v.x; o.y = v.y; o.z = v.z; o.w = v.w;
+  *reinterpret_cast<typename Tr<T>::V4*>(p) = o;
+}
+template <typename T>
+__device__ __forceinline__ T get(const Vec4<T>& v, int c) {
+  return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+}
+// replace lanes with column index >= n by INF (tail vector of a row)
+template <typename T>
+__device__ __forceinline__ Vec4<T> mask_tail(Vec4<T> v, int64_t col0, int64_t n) {
+  const T I = Tr<T>::inf();
+  if (col0 + 4 > n) {
+    if (col0 + 0 >= n) v.x = I;
+    if (col0 + 1 >= n) v.y = I;
+    if (col0 + 2 >= n) v.z = I;
+    if (col0 + 3 >= n) v.w = I;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_min(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = Tr<T>::mn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+constexpr int kNumSMs = 148;  // B200 (2 dies x 74); the host reads the real count
+
+}  // namespace apsp

@@ -1,0 +1,321 @@
+// fw.cu — tiled blocked Floyd–Warshall on sm_100a.
+//
+// The cold-start comparator of the paper and the dense
+// fallback of the removal algorithm ("If the Cost is larger than
+// hyper-parameter delta, we just use the Floyd-Warshall algorithm").
+//
+// For each pivot block K of TB=128 nodes:
+//   (1) fw_diag:  D_KK := FW closure of the 128x128 diagonal tile (one CTA,
+//                 tile resident in shared memory, one barrier per pivot).
+//   (2) panels:   D[K][J] := D_KK (x) D[K][J] and D[I][K] := D[I][K] (x) D_KK.
+//                 One min-plus product with the closed tile — exact because a
+//                 path between K and J decomposes at its last visit to K.
+//   (3) rest:     D[I][J] := min(D[I][J], D[I][K] (x) D[K][J]), I, J != K.
+// Steps (2) and (3) are the same register-tiled min-plus kernel: a 128x128
+// output tile per CTA, 256 threads x (8x8) accumulators, k staged through
+// shared memory in chunks of 32 (B tile by cp.async, A tile transposed
+// through registers so every inner-loop operand is one LDS.128).  The int32
+// relaxation min(d, a + b) is a single VIADDMNMX on sm_100a; no tensor cores
+// (min-plus is not a (+,x) contraction).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace apsp {
+
+constexpr int TB = 128;        // tile edge = pivot block
+constexpr int KC = 32;         // k chunk staged in smem
+constexpr int NTH = 256;       // threads per tile CTA
+constexpr int AST = TB + 4;    // As row stride (elements), keeps LDS.128 aligned
+
+// ---------------------------------------------------------------------------
+// (1) closure of the diagonal tile
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(1024) fw_diag_kernel(T* __restrict__ D, int64_t ld, int kb) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T (*s)[TB] = reinterpret_cast<T (*)[TB]>(smem_raw);   // 64 KB tile
+  const T I = Tr<T>::inf();
+  for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) {
+    int i = e / TB, j = e % TB;
+    s[i][j] = (i < kb && j < kb) ? D[(int64_t)i * ld + j] : I;
+  }
+  __syncthreads();
+  // Row k and column k are unchanged by pivot k (D[k][k] = 0, w >= 0), so
+  // the in-place update has no read/write race.
+  for (int k = 0; k < kb; ++k) {
+    for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) {
+      int i = e / TB, j = e % TB;
+      s[i][j] = Tr<T>::relax(s[i][j], s[i][k], s[k][j]);
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) {
+    int i = e / TB, j = e % TB;
+    if (i < kb && j < kb) D[(int64_t)i * ld + j] = s[i][j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// (2)/(3) C[I][J] = min(C[I][J], A[I][:] (x) B[:][J]) on 128x128 tiles
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+struct TileArgs {
+  void* C; int64_t ldc;          // output rows [0, m), cols [0, ncols)
+  const void* A; int64_t lda;    // m x kdepth   (rows aligned with C)
+  const void* B; int64_t ldb;    // kdepth x ncols
+  int m, ncols, kdepth;
+  int skip_ti, skip_tj;          // tile row / column excluded from this launch (-1: none)
+};
+
+template <typename T>
+__global__ void __launch_bounds__(NTH, 1) fw_tile_kernel(TileArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* As = reinterpret_cast<T*>(smem_raw);          // [2][KC][AST]   (k-major: As[k][i])
+  T* Bs = As + 2 * KC * AST;                       // [2][KC][TB]    (Bs[k][j])
+
+  const int tj = blockIdx.x, ti = blockIdx.y;
+  if (ti == a.skip_ti || tj == a.skip_tj) return;
+  T* C = reinterpret_cast<T*>(a.C);
+  const T* A = reinterpret_cast<const T*>(a.A);
+  const T* B = reinterpret_cast<const T*>(a.B);
+  const T I = Tr<T>::inf();
+
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int i0 = ti * TB, j0 = tj * TB;
+  const bool fullB = (j0 + TB <= a.ncols);
+  const bool fullA = (i0 + TB <= a.m);
+  const int nch = (a.kdepth + KC - 1) / KC;
+
+  // --- staging helpers ---
+  Vec4<T> areg[4];
+  auto load_A = [&](int kc) {
+    const int k0 = kc * KC;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int idx = tid + NTH * q;
+      int r = idx >> 3, c4 = idx & 7;
+      int kcol = k0 + c4 * 4;
+      Vec4<T> v{I, I, I, I};
+      if ((fullA || i0 + r < a.m) && kcol < a.kdepth) {
+        v = ld4<T>(A + (int64_t)(i0 + r) * a.lda + kcol);
+        v = mask_tail<T>(v, kcol, a.kdepth);
+      }
+      areg[q] = v;
+    }
+  };
+  auto store_A = [&](int buf) {
+    T* as = As + buf * KC * AST;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int idx = tid + NTH * q;
+      int r = idx >> 3, c4 = idx & 7;
+      as[(c4 * 4 + 0) * AST + r] = areg[q].x;
+      as[(c4 * 4 + 1) * AST + r] = areg[q].y;
+      as[(c4 * 4 + 2) * AST + r] = areg[q].z;
+      as[(c4 * 4 + 3) * AST + r] = areg[q].w;
+    }
+  };
+  auto load_B = [&](int kc, int buf) {
+    const int k0 = kc * KC;
+    T* bs = Bs + buf * KC * TB;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int idx = tid + NTH * q;
+      int r = idx >> 5, c4 = idx & 31;
+      int kr = k0 + r, col = j0 + c4 * 4;
+      T* dst = bs + r * TB + c4 * 4;
+      if (kr < a.kdepth && (fullB || col + 4 <= a.ncols)) {
+        cp_async16(dst, B + (int64_t)kr * a.ldb + col);
+      } else {
+        Vec4<T> v{I, I, I, I};
+        if (kr < a.kdepth && col < a.ncols) {
+          v = ld4<T>(B + (int64_t)kr * a.ldb + col);
+          v = mask_tail<T>(v, col, a.ncols);
+        }
+        st4<T>(dst, v);
+      }
+    }
+    cp_async_commit();
+  };
+
+  // --- accumulators start from C ---
+  T acc[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    int row = i0 + (r < 4 ? ty * 4 + r : 64 + ty * 4 + (r - 4));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      int col = j0 + (h == 0 ? tx * 4 : 64 + tx * 4);
+      Vec4<T> v{I, I, I, I};
+      if ((fullA || row < a.m) && (fullB || col < a.ncols)) v = ld4<T>(C + (int64_t)row * a.ldc + col);
+      acc[r][h * 4 + 0] = v.x; acc[r][h * 4 + 1] = v.y;
+      acc[r][h * 4 + 2] = v.z; acc[r][h * 4 + 3] = v.w;
+    }
+  }
+
+  load_A(0);
+  load_B(0, 0);
+  store_A(0);
+  cp_async_wait_all();
+  __syncthreads();
+
+  for (int kc = 0; kc < nch; ++kc) {
+    const int buf = kc & 1;
+    if (kc + 1 < nch) {
+      load_A(kc + 1);
+      load_B(kc + 1, buf ^ 1);
+    }
+    const T* as = As + buf * KC * AST;
+    const T* bs = Bs + buf * KC * TB;
+    if constexpr (!Tr<T>::kFloat) {
+      // int32: one VIADDMNMX per relaxation
+#pragma unroll 8
+      for (int kk = 0; kk < KC; ++kk) {
+        Vec4<T> a0 = *reinterpret_cast<const Vec4<T>*>(as + kk * AST + ty * 4);
+        Vec4<T> a1 = *reinterpret_cast<const Vec4<T>*>(as + kk * AST + 64 + ty * 4);
+        Vec4<T> b0 = *reinterpret_cast<const Vec4<T>*>(bs + kk * TB + tx * 4);
+        Vec4<T> b1 = *reinterpret_cast<const Vec4<T>*>(bs + kk * TB + 64 + tx * 4);
+        T av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        T bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[r][c] = Tr<T>::relax(acc[r][c], av[r], bv[c]);
+      }
+    } else {
+      // fp32: two pivots per step so each accumulator takes one 3-input
+      // FMNMX3 per two FADDs (1.5 instructions per relaxation)
+#pragma unroll 4
+      for (int kk = 0; kk < KC; kk += 2) {
+        Vec4<T> a0 = *reinterpret_cast<const Vec4<T>*>(as + kk * AST + ty * 4);
+        Vec4<T> a1 = *reinterpret_cast<const Vec4<T>*>(as + kk * AST + 64 + ty * 4);
+        Vec4<T> b0 = *reinterpret_cast<const Vec4<T>*>(bs + kk * TB + tx * 4);
+        Vec4<T> b1 = *reinterpret_cast<const Vec4<T>*>(bs + kk * TB + 64 + tx * 4);
+        Vec4<T> a2 = *reinterpret_cast<const Vec4<T>*>(as + (kk + 1) * AST + ty * 4);
+        Vec4<T> a3 = *reinterpret_cast<const Vec4<T>*>(as + (kk + 1) * AST + 64 + ty * 4);
+        Vec4<T> b2 = *reinterpret_cast<const Vec4<T>*>(bs + (kk + 1) * TB + tx * 4);
+        Vec4<T> b3 = *reinterpret_cast<const Vec4<T>*>(bs + (kk + 1) * TB + 64 + tx * 4);
+        T av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        T bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        T aw[8] = {a2.x, a2.y, a2.z, a2.w, a3.x, a3.y, a3.z, a3.w};
+        T bw[8] = {b2.x, b2.y, b2.z, b2.w, b3.x, b3.y, b3.z, b3.w};
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            acc[r][c] = fminf(acc[r][c], fminf(__fadd_rn(av[r], bv[c]), __fadd_rn(aw[r], bw[c])));
+      }
+    }
+    if (kc + 1 < nch) store_A(buf ^ 1);
+    cp_async_wait_all();
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    int row = i0 + (r < 4 ? ty * 4 + r : 64 + ty * 4 + (r - 4));
+    if (!(fullA || row < a.m)) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      int col = j0 + (h == 0 ? tx * 4 : 64 + tx * 4);
+      if (!(fullB || col < a.ncols)) continue;
+      Vec4<T> v{acc[r][h * 4 + 0], acc[r][h * 4 + 1], acc[r][h * 4 + 2], acc[r][h * 4 + 3]};
+      st4<T>(C + (int64_t)row * a.ldc + col, v);
+    }
+  }
+}
+
+constexpr size_t kTileSmem = sizeof(int32_t) * (2 * KC * AST + 2 * KC * TB);
+
+template <typename T>
+static cudaError_t launch_tile(const TileArgs& a, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fw_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kTileSmem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (a.m <= 0 || a.ncols <= 0) return cudaSuccess;
+  dim3 grid((a.ncols + TB - 1) / TB, (a.m + TB - 1) / TB);
+  fw_tile_kernel<T><<<grid, NTH, kTileSmem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// host-side drivers
+// ---------------------------------------------------------------------------
+template <typename T>
+cudaError_t fw_diag(T* Dkk, int64_t ld, int kb, cudaStream_t st) {
+  static bool configured = false;
+  constexpr int smem = TB * TB * sizeof(T);
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fw_diag_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  fw_diag_kernel<T><<<1, 1024, smem, st>>>(Dkk, ld, kb);
+  return cudaGetLastError();
+}
+
+// Row panel D[K][*] (all columns except the K tile) := D_KK (x) D[K][*].
+// `rowK` points at D[K0][0]; ncols = n.
+template <typename T>
+cudaError_t fw_row_panel(T* rowK, int64_t ld, int64_t K0, int kb, int64_t ncols, cudaStream_t st) {
+  TileArgs a;
+  a.C = rowK; a.ldc = ld;
+  a.A = rowK + K0; a.lda = ld;        // closed diagonal tile
+  a.B = rowK; a.ldb = ld;             // the panel itself (each CTA reads only its own tile)
+  a.m = kb; a.ncols = (int)ncols; a.kdepth = kb;
+  a.skip_ti = -1; a.skip_tj = (int)(K0 / TB);
+  return launch_tile<T>(a, st);
+}
+
+// Column panel D[rows][K] := D[rows][K] (x) D_KK for m local rows.
+// `D` = local rows base, `Dkk` = the closed diagonal tile (any ld).
+// skip_ti = the local tile row holding the diagonal tile (-1 if not local).
+template <typename T>
+cudaError_t fw_col_panel(T* D, int64_t ld, int64_t m, int64_t K0, int kb, const T* Dkk,
+                         int64_t lddk, int skip_ti, cudaStream_t st) {
+  TileArgs a;
+  a.C = D + K0; a.ldc = ld;
+  a.A = D + K0; a.lda = ld;
+  a.B = Dkk; a.ldb = lddk;
+  a.m = (int)m; a.ncols = kb; a.kdepth = kb;
+  a.skip_ti = skip_ti; a.skip_tj = -1;
+  return launch_tile<T>(a, st);
+}
+
+// Phase 3 on m local rows: D[i][j] = min(D[i][j], D[i][K] (x) P[K][j]) where
+// P is the row panel (kb x ncols, leading dimension ldp).
+template <typename T>
+cudaError_t fw_rest(T* D, int64_t ld, int64_t m, int64_t ncols, int64_t K0, int kb, const T* P,
+                    int64_t ldp, int skip_ti, cudaStream_t st) {
+  TileArgs a;
+  a.C = D; a.ldc = ld;
+  a.A = D + K0; a.lda = ld;
+  a.B = P; a.ldb = ldp;
+  a.m = (int)m; a.ncols = (int)ncols; a.kdepth = kb;
+  a.skip_ti = skip_ti; a.skip_tj = (int)(K0 / TB);
+  return launch_tile<T>(a, st);
+}
+
+#define INST(T)                                                                                  \
+  template cudaError_t fw_diag<T>(T*, int64_t, int, cudaStream_t);                               \
+  template cudaError_t fw_row_panel<T>(T*, int64_t, int64_t, int, int64_t, cudaStream_t);        \
+  template cudaError_t fw_col_panel<T>(T*, int64_t, int64_t, int64_t, int, const T*, int64_t,    \
+                                       int, cudaStream_t);                                       \
+  template cudaError_t fw_rest<T>(T*, int64_t, int64_t, int64_t, int64_t, int, const T*, int64_t, \
+                                  int, cudaStream_t);
+INST(int32_t)
+INST(float)
+#undef INST
+
+}  // namespace apsp

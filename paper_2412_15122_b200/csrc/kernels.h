@@ -1,0 +1,99 @@
+// kernels.h — host-callable launchers of the sm_100a kernels (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace apsp {
+
+// Device counters written by the detection kernel.
+struct DetectCounters {
+  unsigned long long total;   // |A|
+  unsigned int rows;          // Phi
+  unsigned int maxrow;        // max |A_i|
+  unsigned int overflow;      // list capacity exceeded
+  unsigned int err;           // validation flag (add_node inputs)
+};
+
+// ---------------- fw.cu ----------------
+template <typename T> cudaError_t fw_diag(T* Dkk, int64_t ld, int kb, cudaStream_t st);
+template <typename T>
+cudaError_t fw_row_panel(T* rowK, int64_t ld, int64_t K0, int kb, int64_t ncols, cudaStream_t st);
+template <typename T>
+cudaError_t fw_col_panel(T* D, int64_t ld, int64_t m, int64_t K0, int kb, const T* Dkk,
+                         int64_t lddk, int skip_ti, cudaStream_t st);
+template <typename T>
+cudaError_t fw_rest(T* D, int64_t ld, int64_t m, int64_t ncols, int64_t K0, int kb, const T* P,
+                    int64_t ldp, int skip_ti, cudaStream_t st);
+
+// ---------------- stream.cu ----------------
+// Row range [lo, hi) is global; D points at global row `row0` (local block).
+struct Rows {
+  int64_t lo, hi, row0;
+};
+
+template <typename T>
+cudaError_t validate_vec(const T* in, const T* in2, int64_t n, int64_t npad, T* out,
+                         unsigned int* err, cudaStream_t st);
+template <typename T>
+cudaError_t transpose_in(const T* W, int64_t ldw, int64_t n, T* WT, int64_t ldt, unsigned int* err,
+                         cudaStream_t st);
+template <typename T>
+cudaError_t fill(T* p, int64_t count, T v, cudaStream_t st);
+template <typename T>
+cudaError_t init_d(T* D, int64_t ld, Rows r, int64_t n, const T* WT, int64_t ldw, cudaStream_t st);
+template <typename T>
+cudaError_t gather_col(const T* D, int64_t ld, Rows r, int64_t col, T add, T* out, cudaStream_t st);
+template <typename T>
+cudaError_t copy_vec(const T* src, int64_t n, int64_t npad, T add, T* out, cudaStream_t st);
+template <typename T>
+cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow, const T* iw,
+                          T* rowpart, T* colpart, int64_t part_ld, int* nchunk_out, int* nslab_out,
+                          int max_slabs, cudaStream_t st);
+template <typename T>
+cudaError_t addnode_finish(const T* rowpart, int nchunk, const T* colpart, int nslab,
+                           int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col, T* row,
+                           cudaStream_t st);
+template <typename T>
+cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, const T* c2,
+                  const T* rv2, cudaStream_t st);
+template <typename T>
+cudaError_t addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xlocal,
+                          const T* col, const T* row, T* WT, int64_t ldw, const T* ow,
+                          const T* iw, cudaStream_t st);
+template <typename T>
+cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
+                   const T* c2, const T* r2, float tau, const T* WT, int64_t ldw, int reset,
+                   int64_t* rowoff, int* rowcnt, int* prow, int* pcol, int64_t lcap,
+                   DetectCounters* ctr, int grid, cudaStream_t st);
+template <typename T>
+cudaError_t tombstone(T* D, int64_t ld, Rows r, int64_t n, int64_t k, T* WT, int64_t ldw,
+                      cudaStream_t st);
+template <typename T>
+cudaError_t copy_row(T* dst, const T* src, int64_t n, cudaStream_t st);
+template <typename T>
+cudaError_t copy_col(T* D, int64_t ld, Rows r, int64_t dst_col, int64_t src_col, cudaStream_t st);
+template <typename T>
+cudaError_t fill_col(T* D, int64_t ld, Rows r, int64_t col, T v, cudaStream_t st);
+template <typename T>
+cudaError_t set_edge(T* WT, int64_t ldw, int64_t u, int64_t v, T w, int directed, cudaStream_t st);
+
+// ---------------- sparse.cu ----------------
+template <typename T>
+cudaError_t sparse_round0(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
+                          const int* prow, const int* pcol, int64_t npairs, cudaStream_t st);
+template <typename T>
+cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
+                         const int* prow, const int* pcol, int64_t npairs, const int64_t* rowoff,
+                         const int* rowcnt, const int* chg_in, int* chg_out, int* any,
+                         cudaStream_t st);
+
+// ---------------- query.cu ----------------
+constexpr int kQueryCap = 4096;
+template <typename T>
+cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int q,
+                        const int* s, const int* t, T* dist, int* paths, int path_cap,
+                        int* path_lens, int* ncand, float tau, cudaStream_t st);
+
+int num_sms();
+
+}  // namespace apsp

@@ -1,0 +1,181 @@
+// query.cu — warm-start single-pair shortest path (alg:sp_apsp).
+//
+// "It use the conclusion of Theorem 4 to exclude unnecessary nodes from node
+// i to node j, generate the candidate_node_list; then form a small graph
+// which is composed of nodes in candidate_node_list; then use Dijkstra's
+// algorithm to calculate the shortest path from node i to node j, on the
+// small graph; then translate the path into original node index."
+//
+// One CTA per query:
+//   1. candidate scan: C = {k : D[s][k] + D[k][t] == D[s][t]} over row s
+//      (contiguous) and column t (stride ld), compacted in node order with
+//      warp ballots + popc into shared memory;
+//   2. Dijkstra on the induced subgraph of C (warp 0; argmin by 64-bit
+//      (label, index) keys so ties go to the smaller node id), early
+//      stop when t is finalised; edge weights W[m][c] = WT[c][m];
+//   3. predecessor walk t -> s, written in original ids.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace apsp {
+
+constexpr int QT = 256;   // threads per query CTA
+
+template <typename T>
+__global__ void __launch_bounds__(QT) k_query(const T* __restrict__ D, int64_t ld,
+                                              const T* __restrict__ WT, int64_t ldw, int64_t n,
+                                              int q, const int* __restrict__ S,
+                                              const int* __restrict__ Tq, T* dist, int* paths,
+                                              int path_cap, int* path_lens, int* ncand, float tau) {
+  __shared__ int cid[kQueryCap];
+  __shared__ T lab[kQueryCap];
+  __shared__ short pred[kQueryCap];
+  __shared__ unsigned char done[kQueryCap];
+  __shared__ int s_cnt, s_is, s_it;
+  __shared__ int s_wcnt[QT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const T I = Tr<T>::inf();
+
+  for (int b = blockIdx.x; b < q; b += gridDim.x) {
+    const int s = S[b], t = Tq[b];
+    if (s < 0 || s >= n || t < 0 || t >= n) {
+      if (tid == 0) { path_lens[b] = -3; if (ncand) ncand[b] = 0; dist[b] = I; }
+      continue;
+    }
+    const T* Ds = D + (int64_t)s * ld;
+    const T st = Ds[t];
+    if (s == t || !Tr<T>::fin(st)) {
+      if (tid == 0) {
+        dist[b] = s == t ? T(0) : I;
+        if (s == t) {
+          if (path_cap >= 1) { paths[(int64_t)b * path_cap] = s; path_lens[b] = 1; }
+          else path_lens[b] = -1;
+        } else {
+          path_lens[b] = 0;
+        }
+        if (ncand) ncand[b] = s == t ? 1 : 0;
+      }
+      continue;
+    }
+    if (tid == 0) { s_cnt = 0; s_is = -1; s_it = -1; }
+    __syncthreads();
+
+    // ---- 1. candidate scan (Theorem 4 equality), ordered compaction ----
+    constexpr int U = 4;   // k values per thread per step (loads in flight)
+    for (int64_t base = 0; base < n; base += (int64_t)QT * U) {
+      T dsk[U], dkt[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        int64_t k = base + (int64_t)u * QT + tid;
+        dsk[u] = k < n ? Ds[k] : I;
+        dkt[u] = k < n ? D[k * ld + t] : I;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        int64_t k = base + (int64_t)u * QT + tid;
+        bool f = k < n && Tr<T>::fin(dsk[u]) && Tr<T>::fin(dkt[u]) &&
+                 Tr<T>::tight(Tr<T>::add(dsk[u], dkt[u]), st, tau);
+        unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) s_wcnt[warp] = __popc(bal);
+        __syncthreads();
+        int off = s_cnt;
+        for (int w = 0; w < warp; ++w) off += s_wcnt[w];
+        int tot = 0;
+        for (int w = 0; w < QT / 32; ++w) tot += s_wcnt[w];
+        if (f) {
+          int pos = off + __popc(bal & ((1u << lane) - 1));
+          if (pos < kQueryCap) {
+            cid[pos] = (int)k;
+            if (k == s) s_is = pos;
+            if (k == t) s_it = pos;
+          }
+        }
+        __syncthreads();
+        if (tid == 0) s_cnt += tot;
+        __syncthreads();
+      }
+    }
+    const int cnt = s_cnt;
+    if (cnt > kQueryCap || s_is < 0 || s_it < 0) {
+      if (tid == 0) { path_lens[b] = -2; if (ncand) ncand[b] = cnt; dist[b] = st; }
+      __syncthreads();
+      continue;
+    }
+
+    // ---- 2. Dijkstra on the candidate subgraph (warp 0) ----
+    if (warp == 0) {
+      for (int c = lane; c < cnt; c += 32) { lab[c] = I; pred[c] = -1; done[c] = 0; }
+      __syncwarp();
+      if (lane == 0) lab[s_is] = T(0);
+      __syncwarp();
+      for (int it = 0; it < cnt; ++it) {
+        unsigned long long best = ~0ull;
+        for (int c = lane; c < cnt; c += 32)
+          if (!done[c]) {
+            unsigned long long key = ((unsigned long long)Tr<T>::key(lab[c]) << 32) | (unsigned)c;
+            best = key < best ? key : best;
+          }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+          best = y < best ? y : best;
+        }
+        if (best == ~0ull) break;
+        const int m = (int)(best & 0xffffffffu);
+        const T lm = lab[m];
+        if (!Tr<T>::fin(lm)) break;
+        __syncwarp();
+        if (lane == 0) done[m] = 1;
+        __syncwarp();
+        if (m == s_it) break;
+        const int64_t gm = cid[m];
+        for (int c = lane; c < cnt; c += 32) {
+          if (done[c]) continue;
+          const T w = WT[(int64_t)cid[c] * ldw + gm];   // W[m][c]
+          if (!Tr<T>::fin(w)) continue;
+          const T cand = Tr<T>::add(lm, w);
+          if (cand < lab[c]) { lab[c] = cand; pred[c] = (short)m; }
+        }
+        __syncwarp();
+      }
+      // ---- 3. path t -> s ----
+      if (lane == 0) {
+        int len = 0, last = -1;
+        for (int c = s_it; c >= 0 && len <= cnt; c = (c == s_is) ? -1 : pred[c]) { ++len; last = c; }
+        dist[b] = st;
+        if (ncand) ncand[b] = cnt;
+        if (len > cnt || last != s_is) {
+          path_lens[b] = -2;       // no path through the candidates (cannot happen)
+        } else if (len > path_cap) {
+          path_lens[b] = -1;
+        } else {
+          int* out = paths + (int64_t)b * path_cap;
+          int pos = len - 1;
+          for (int c = s_it; c >= 0; c = (c == s_is) ? -1 : pred[c]) out[pos--] = cid[c];
+          path_lens[b] = len;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int q,
+                        const int* s, const int* t, T* dist, int* paths, int path_cap,
+                        int* path_lens, int* ncand, float tau, cudaStream_t st) {
+  if (q <= 0) return cudaSuccess;
+  int grid = std::min(q, num_sms() * 4);
+  k_query<T><<<grid, QT, 0, st>>>(D, ld, WT, ldw, n, q, s, t, dist, paths, path_cap, path_lens,
+                                  ncand, tau);
+  return cudaGetLastError();
+}
+
+template cudaError_t query_batch<int32_t>(const int32_t*, int64_t, const int32_t*, int64_t, int64_t,
+                                          int, const int*, const int*, int32_t*, int*, int, int*,
+                                          int*, float, cudaStream_t);
+template cudaError_t query_batch<float>(const float*, int64_t, const float*, int64_t, int64_t, int,
+                                        const int*, const int*, float*, int*, int, int*, int*,
+                                        float, cudaStream_t);
+
+}  // namespace apsp

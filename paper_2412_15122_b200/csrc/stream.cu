@@ -1,0 +1,651 @@
+// stream.cu — the O(n^2) HBM-streaming kernels of the warm-start updates.
+//
+//   addnode_pass1/finish  new node's column and row (Theorem 2, P:262-283;
+//                         theo_2_back) in ONE read pass over D:
+//                         col[i] = min_t D[i][t] + in[t]   (row reductions)
+//                         row[j] = min_t out[t] + D[t][j]  (column reductions)
+//   rank1                 D[i][j] = min(D[i][j], c[i] + r[j]) — Theorem 3's
+//                         min(x1, t1 + t2) and the same algebra
+//                         through a decreased edge; 16-byte vectors, write-back
+//                         only of changed vectors.
+//   detect                need_update_list by Theorem 4 /
+//                         Corollary 3: flags per row compacted
+//                         with warp ballots into a shared-memory bitmap, then
+//                         popc + block scan into per-row sorted column lists;
+//                         flagged entries are reset to W'[i][j] (D0).
+//   tombstone / copy_*    "Removing a node is equivalent to set the node's
+//                         distances (to and from) to other nodes to infinity"
+//                          and the swap-with-last re-index (DESIGN Q7).
+//
+// Work is laid out warp = (column chunk of 1024 columns) x (slab of rows):
+// each lane owns 8 vectors of every row of its slab, so vector operands that
+// are constant down a column (in-edges, the pivot row) live in registers and
+// every warp load instruction moves 512 contiguous bytes.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace apsp {
+
+constexpr int VPL = 8;                 // vectors per lane per row
+constexpr int CHUNK_VEC = 32 * VPL;    // vectors per warp chunk (1024 columns)
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = kNumSMs;
+  }
+  return sms;
+}
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------------------
+// validation / normalisation of caller vectors
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_validate_vec(const T* in, const T* in2, int64_t n, int64_t npad, T* out,
+                               unsigned int* err) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npad;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    T v = Tr<T>::inf();
+    if (j < n) {
+      T x = in[j];
+      if (Tr<T>::kFloat) {
+        if (!(x >= T(0))) atomicOr(err, 1u);            // negative or NaN
+      } else {
+        if (x < T(0)) atomicOr(err, 1u);
+      }
+      v = Tr<T>::kFloat ? x : (x >= Tr<T>::inf() ? Tr<T>::inf() : x);
+      if (in2) {
+        T y = in2[j];
+        T y2 = Tr<T>::kFloat ? y : (y >= Tr<T>::inf() ? Tr<T>::inf() : y);
+        if (!(y2 == v)) atomicOr(err, 2u);             // undirected asymmetry
+      }
+    }
+    out[j] = v;
+  }
+}
+template <typename T>
+cudaError_t validate_vec(const T* in, const T* in2, int64_t n, int64_t npad, T* out,
+                         unsigned int* err, cudaStream_t st) {
+  int grid = (int)std::min<int64_t>(cdiv(npad, 256), 4 * num_sms());
+  k_validate_vec<T><<<grid, 256, 0, st>>>(in, in2, n, npad, out, err);
+  return cudaGetLastError();
+}
+
+// WT[j][i] = W[i][j] (32x32 smem tiles); checks W[i][i] == 0 and w >= 0.
+template <typename T>
+__global__ void k_transpose_in(const T* W, int64_t ldw, int64_t n, T* WT, int64_t ldt,
+                               unsigned int* err) {
+  __shared__ T tile[32][33];
+  int64_t i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    int64_t i = i0 + r, j = j0 + threadIdx.x;
+    T v = Tr<T>::inf();
+    if (i < n && j < n) {
+      v = W[i * ldw + j];
+      if (!(v >= T(0))) atomicOr(err, 1u);
+      if (!Tr<T>::kFloat && v > Tr<T>::inf()) v = Tr<T>::inf();
+      if (i == j && v != T(0)) atomicOr(err, 4u);
+    }
+    tile[r][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    int64_t j = j0 + r, i = i0 + threadIdx.x;
+    if (i < n && j < n) WT[j * ldt + i] = tile[threadIdx.x][r];
+  }
+}
+template <typename T>
+cudaError_t transpose_in(const T* W, int64_t ldw, int64_t n, T* WT, int64_t ldt, unsigned int* err,
+                         cudaStream_t st) {
+  dim3 grid((unsigned)cdiv(n, 32), (unsigned)cdiv(n, 32));
+  k_transpose_in<T><<<grid, dim3(32, 8), 0, st>>>(W, ldw, n, WT, ldt, err);
+  return cudaGetLastError();
+}
+
+// D[i][j] := W[i][j] = WT[j][i] for the local rows i in [lo, hi), j < n
+// (the cold start "D := W" of blocked FW; 32x32 smem tiles).
+template <typename T>
+__global__ void k_init_d(T* D, int64_t ld, Rows r, int64_t n, const T* WT, int64_t ldw) {
+  __shared__ T tile[32][33];
+  const int64_t i0 = r.lo + blockIdx.y * 32, j0 = blockIdx.x * 32;
+  for (int rr = threadIdx.y; rr < 32; rr += blockDim.y) {
+    int64_t j = j0 + rr, i = i0 + threadIdx.x;           // read WT[j][i] coalesced over i
+    tile[rr][threadIdx.x] = (j < n && i < r.hi) ? WT[j * ldw + i] : T(0);
+  }
+  __syncthreads();
+  for (int rr = threadIdx.y; rr < 32; rr += blockDim.y) {
+    int64_t i = i0 + rr, j = j0 + threadIdx.x;
+    if (i < r.hi && j < n) D[(i - r.row0) * ld + j] = tile[threadIdx.x][rr];
+  }
+}
+template <typename T>
+cudaError_t init_d(T* D, int64_t ld, Rows r, int64_t n, const T* WT, int64_t ldw, cudaStream_t st) {
+  if (r.hi <= r.lo) return cudaSuccess;
+  dim3 grid((unsigned)cdiv(n, 32), (unsigned)cdiv(r.hi - r.lo, 32));
+  k_init_d<T><<<grid, dim3(32, 8), 0, st>>>(D, ld, r, n, WT, ldw);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void k_fill(T* p, int64_t count, T v) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x)
+    p[e] = v;
+}
+template <typename T>
+cudaError_t fill(T* p, int64_t count, T v, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  int grid = (int)std::min<int64_t>(cdiv(count, 256), 8 * num_sms());
+  k_fill<T><<<grid, 256, 0, st>>>(p, count, v);
+  return cudaGetLastError();
+}
+
+// out[i] = sat(D[i][col] + add) for the local rows (global index i)
+template <typename T>
+__global__ void k_gather_col(const T* D, int64_t ld, Rows r, int64_t col, T add, T* out) {
+  for (int64_t i = r.lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.hi;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = Tr<T>::sat(Tr<T>::add(D[(i - r.row0) * ld + col], add));
+}
+template <typename T>
+cudaError_t gather_col(const T* D, int64_t ld, Rows r, int64_t col, T add, T* out, cudaStream_t st) {
+  if (r.hi <= r.lo) return cudaSuccess;
+  int grid = (int)std::min<int64_t>(cdiv(r.hi - r.lo, 256), 4 * num_sms());
+  k_gather_col<T><<<grid, 256, 0, st>>>(D, ld, r, col, add, out);
+  return cudaGetLastError();
+}
+
+// out[j] = sat(src[j] + add) for j < n, INF for n <= j < npad
+template <typename T>
+__global__ void k_copy_vec(const T* src, int64_t n, int64_t npad, T add, T* out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npad;
+       j += (int64_t)gridDim.x * blockDim.x)
+    out[j] = j < n ? Tr<T>::sat(Tr<T>::add(src[j], add)) : Tr<T>::inf();
+}
+template <typename T>
+cudaError_t copy_vec(const T* src, int64_t n, int64_t npad, T add, T* out, cudaStream_t st) {
+  int grid = (int)std::min<int64_t>(cdiv(npad, 256), 4 * num_sms());
+  k_copy_vec<T><<<grid, 256, 0, st>>>(src, n, npad, add, out);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// add node, pass 1: one read of D -> partial new column / new row
+// ---------------------------------------------------------------------------
+struct Tiling {
+  int64_t n4;       // vectors per row
+  int nchunk;       // column chunks (1024 columns each)
+  int nslab;        // row slabs
+  int64_t slab;     // rows per slab
+  int64_t warps;
+};
+static Tiling make_tiling(int64_t n, int64_t rows, int max_slabs) {
+  Tiling t;
+  t.n4 = cdiv(n, 4);
+  t.nchunk = (int)cdiv(t.n4, CHUNK_VEC);
+  int64_t target = (int64_t)num_sms() * 32;  // ~32 resident warps per SM
+  int64_t ns = std::max<int64_t>(1, target / t.nchunk);
+  ns = std::min<int64_t>(ns, std::max<int64_t>(1, rows));
+  ns = std::min<int64_t>(ns, max_slabs);
+  t.nslab = (int)ns;
+  t.slab = cdiv(std::max<int64_t>(rows, 1), t.nslab);
+  t.warps = (int64_t)t.nchunk * t.nslab;
+  return t;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_addnode_pass1(const T* __restrict__ D, int64_t ld, Rows r,
+                                                       int64_t n, Tiling tl, const T* __restrict__ ow,
+                                                       const T* __restrict__ iw, T* rowpart,
+                                                       T* colpart, int64_t part_ld) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gw >= tl.warps) return;
+  const int chunk = (int)(gw % tl.nchunk);
+  const int slab = (int)(gw / tl.nchunk);
+  const int64_t i_lo = r.lo + slab * tl.slab;
+  const int64_t i_hi = min(r.hi, i_lo + tl.slab);
+  const T I = Tr<T>::inf();
+
+  int64_t qv[VPL];
+  Vec4<T> inw[VPL], colp[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    qv[v] = (int64_t)chunk * CHUNK_VEC + v * 32 + lane;
+    inw[v] = qv[v] < tl.n4 ? ld4<T>(iw + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+    colp[v] = Vec4<T>{I, I, I, I};
+  }
+  for (int64_t i = i_lo; i < i_hi; ++i) {
+    const T* row = D + (i - r.row0) * ld;
+    Vec4<T> d[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+      d[v] = qv[v] < tl.n4 ? mask_tail<T>(ld4_stream<T>(row + 4 * qv[v]), 4 * qv[v], n)
+                           : Vec4<T>{I, I, I, I};
+    const T oi = ow[i];
+    T rp = I;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      rp = Tr<T>::relax(rp, d[v].x, inw[v].x);
+      rp = Tr<T>::relax(rp, d[v].y, inw[v].y);
+      rp = Tr<T>::relax(rp, d[v].z, inw[v].z);
+      rp = Tr<T>::relax(rp, d[v].w, inw[v].w);
+      colp[v].x = Tr<T>::relax(colp[v].x, oi, d[v].x);
+      colp[v].y = Tr<T>::relax(colp[v].y, oi, d[v].y);
+      colp[v].z = Tr<T>::relax(colp[v].z, oi, d[v].z);
+      colp[v].w = Tr<T>::relax(colp[v].w, oi, d[v].w);
+    }
+    rp = warp_min<T>(rp);
+    if (lane == 0) rowpart[(int64_t)chunk * part_ld + i] = rp;
+  }
+#pragma unroll
+  for (int v = 0; v < VPL; ++v)
+    if (qv[v] < tl.n4) st4<T>(colpart + (int64_t)slab * part_ld + 4 * qv[v], colp[v]);
+}
+
+template <typename T>
+cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow, const T* iw,
+                          T* rowpart, T* colpart, int64_t part_ld, int* nchunk_out, int* nslab_out,
+                          int max_slabs, cudaStream_t st) {
+  Tiling tl = make_tiling(n, r.hi - r.lo, max_slabs);
+  *nchunk_out = tl.nchunk;
+  *nslab_out = tl.nslab;
+  if (r.hi <= r.lo) {
+    // no local rows: the partial row is all INF
+    cudaError_t e = fill<T>(colpart, part_ld, Tr<T>::inf(), st);
+    *nslab_out = 1;
+    return e;
+  }
+  int grid = (int)cdiv(tl.warps, 8);
+  k_addnode_pass1<T><<<grid, 256, 0, st>>>(D, ld, r, n, tl, ow, iw, rowpart, colpart, part_ld);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void k_addnode_finish(const T* rowpart, int nchunk, const T* colpart, int nslab,
+                                 int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col, T* row) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = r.lo + tid; i < r.hi; i += stride) {
+    T m = Tr<T>::inf();
+    for (int c = 0; c < nchunk; ++c) m = Tr<T>::mn(m, rowpart[(int64_t)c * part_ld + i]);
+    col[i] = Tr<T>::sat(m);
+  }
+  for (int64_t j = tid; j < npad; j += stride) {
+    T m = Tr<T>::inf();
+    if (j < n)
+      for (int s = 0; s < nslab; ++s) m = Tr<T>::mn(m, colpart[(int64_t)s * part_ld + j]);
+    row[j] = Tr<T>::sat(m);
+  }
+}
+template <typename T>
+cudaError_t addnode_finish(const T* rowpart, int nchunk, const T* colpart, int nslab,
+                           int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col, T* row,
+                           cudaStream_t st) {
+  int grid = (int)std::min<int64_t>(cdiv(std::max<int64_t>(npad, r.hi - r.lo), 256), 4 * num_sms());
+  k_addnode_finish<T><<<grid, 256, 0, st>>>(rowpart, nchunk, colpart, nslab, part_ld, r, n, npad,
+                                            col, row);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// rank-1 min-plus relaxation  D[i][j] = min(D[i][j], c[i] + r[j] (, c2[i] + r2[j]))
+// ---------------------------------------------------------------------------
+template <typename T, bool TWO>
+__global__ void __launch_bounds__(256) k_rank1(T* __restrict__ D, int64_t ld, Rows r, int64_t n,
+                                               Tiling tl, const T* __restrict__ c,
+                                               const T* __restrict__ rv, const T* __restrict__ c2,
+                                               const T* __restrict__ rv2) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gw >= tl.warps) return;
+  const int chunk = (int)(gw % tl.nchunk);
+  const int slab = (int)(gw / tl.nchunk);
+  const int64_t i_lo = r.lo + slab * tl.slab;
+  const int64_t i_hi = min(r.hi, i_lo + tl.slab);
+  const T I = Tr<T>::inf();
+
+  int64_t qv[VPL];
+  Vec4<T> a[VPL], b[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    qv[v] = (int64_t)chunk * CHUNK_VEC + v * 32 + lane;
+    a[v] = qv[v] < tl.n4 ? ld4<T>(rv + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+    if (TWO) b[v] = qv[v] < tl.n4 ? ld4<T>(rv2 + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+  }
+  for (int64_t i = i_lo; i < i_hi; ++i) {
+    const T ci = c[i];
+    const T ci2 = TWO ? c2[i] : I;
+    if (!Tr<T>::fin(ci) && !Tr<T>::fin(ci2)) continue;   // row cannot change
+    T* row = D + (i - r.row0) * ld;
+    Vec4<T> d[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+      if (qv[v] < tl.n4) d[v] = ld4_stream<T>(row + 4 * qv[v]);
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      if (qv[v] >= tl.n4) continue;
+      Vec4<T> o = d[v];
+      o.x = Tr<T>::relax(o.x, ci, a[v].x);
+      o.y = Tr<T>::relax(o.y, ci, a[v].y);
+      o.z = Tr<T>::relax(o.z, ci, a[v].z);
+      o.w = Tr<T>::relax(o.w, ci, a[v].w);
+      if (TWO) {
+        o.x = Tr<T>::relax(o.x, ci2, b[v].x);
+        o.y = Tr<T>::relax(o.y, ci2, b[v].y);
+        o.z = Tr<T>::relax(o.z, ci2, b[v].z);
+        o.w = Tr<T>::relax(o.w, ci2, b[v].w);
+      }
+      if (o.x != d[v].x || o.y != d[v].y || o.z != d[v].z || o.w != d[v].w)
+        st4<T>(row + 4 * qv[v], o);
+    }
+  }
+}
+template <typename T>
+cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, const T* c2,
+                  const T* rv2, cudaStream_t st) {
+  if (r.hi <= r.lo) return cudaSuccess;
+  Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20);
+  int grid = (int)cdiv(tl.warps, 8);
+  if (c2)
+    k_rank1<T, true><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, c2, rv2);
+  else
+    k_rank1<T, false><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, nullptr, nullptr);
+  return cudaGetLastError();
+}
+
+// new node's column / row into D, its edges into WT
+template <typename T>
+__global__ void k_addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xlocal,
+                                const T* col, const T* row, T* WT, int64_t ldw, const T* ow,
+                                const T* iw) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = r.lo + tid; i < r.hi; i += stride) D[(i - r.row0) * ld + x] = col[i];
+  if (xlocal) {
+    T* Dx = D + (x - r.row0) * ld;
+    for (int64_t j = tid; j < n; j += stride) Dx[j] = row[j];
+    if (tid == 0) Dx[x] = T(0);
+  }
+  for (int64_t t = tid; t < n; t += stride) {
+    WT[x * ldw + t] = iw[t];    // WT[x][t] = W[t][x] = in-edge t -> x
+    WT[t * ldw + x] = ow[t];    // WT[t][x] = W[x][t] = out-edge x -> t
+  }
+  if (tid == 0) WT[x * ldw + x] = T(0);
+}
+template <typename T>
+cudaError_t addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xlocal,
+                          const T* col, const T* row, T* WT, int64_t ldw, const T* ow,
+                          const T* iw, cudaStream_t st) {
+  int grid = (int)std::min<int64_t>(cdiv(n, 256), 4 * num_sms());
+  k_addnode_write<T><<<grid, 256, 0, st>>>(D, ld, r, n, x, xlocal, col, row, WT, ldw, ow, iw);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// affected-pair detection (need_update_list) with ballot/popc compaction
+// ---------------------------------------------------------------------------
+template <typename T>
+struct DetectArgs {
+  T* D; int64_t ld; Rows r; int64_t n; int64_t skip;
+  const T* c1; const T* r1; const T* c2; const T* r2; float tau;
+  const T* WT; int64_t ldw; int reset;
+  int64_t* rowoff; int* rowcnt; int* prow; int* pcol; int64_t lcap;
+  DetectCounters* ctr;
+};
+
+constexpr int DT_THREADS = 256;
+
+template <typename T, bool TWO>
+__device__ __forceinline__ unsigned flag_nibble(const Vec4<T>& d, const Vec4<T>& r1,
+                                                const Vec4<T>& r2, T c1, T c2, int64_t j0,
+                                                int64_t n, int64_t i, int64_t skip, float tau) {
+  unsigned nib = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    int64_t j = j0 + c;
+    T dj = get(d, c);
+    bool f = Tr<T>::tight(Tr<T>::add(c1, get(r1, c)), dj, tau);
+    if (TWO) f = f || Tr<T>::tight(Tr<T>::add(c2, get(r2, c)), dj, tau);
+    f = f && j < n && j != i && j != skip && Tr<T>::fin(dj);
+    nib |= (unsigned)f << c;
+  }
+  return nib;
+}
+
+template <typename T, bool TWO>
+__global__ void __launch_bounds__(DT_THREADS) k_detect(DetectArgs<T> a) {
+  extern __shared__ uint32_t bm[];   // one bit per column of the current row
+  __shared__ int s_warp[DT_THREADS / 32];
+  __shared__ long long s_base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n = a.n, n4 = (n + 3) / 4;
+  const int nwords = (int)((n + 31) / 32);
+  const T I = Tr<T>::inf();
+
+  for (int64_t i = a.r.lo + blockIdx.x; i < a.r.hi; i += gridDim.x) {
+    if (i == a.skip) continue;
+    const T c1 = a.c1[i];
+    const T c2 = TWO ? a.c2[i] : I;
+    if (!Tr<T>::fin(c1) && !Tr<T>::fin(c2)) continue;   // no pair of this row can be tight
+    T* Drow = a.D + (i - a.r.row0) * a.ld;
+    bool any = false;
+    for (int64_t base = 0; base < n4; base += 2 * DT_THREADS) {
+      const int64_t q0 = base + tid, q1 = base + DT_THREADS + tid;
+      Vec4<T> d0{I, I, I, I}, d1{I, I, I, I}, ra0{I, I, I, I}, ra1{I, I, I, I}, rb0, rb1;
+      if (q0 < n4) { d0 = ld4_stream<T>(Drow + 4 * q0); ra0 = ld4<T>(a.r1 + 4 * q0); }
+      if (q1 < n4) { d1 = ld4_stream<T>(Drow + 4 * q1); ra1 = ld4<T>(a.r1 + 4 * q1); }
+      if (TWO) {
+        rb0 = q0 < n4 ? ld4<T>(a.r2 + 4 * q0) : Vec4<T>{I, I, I, I};
+        rb1 = q1 < n4 ? ld4<T>(a.r2 + 4 * q1) : Vec4<T>{I, I, I, I};
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t q = h ? q1 : q0;
+        unsigned nib = 0;
+        if (q < n4)
+          nib = flag_nibble<T, TWO>(h ? d1 : d0, h ? ra1 : ra0, h ? rb1 : rb0, c1, c2, 4 * q, n,
+                                    i, a.skip, a.tau);
+        unsigned v = nib << (4 * (lane & 7));
+        if (__any_sync(0xffffffffu, nib)) {
+          v |= __shfl_xor_sync(0xffffffffu, v, 1);
+          v |= __shfl_xor_sync(0xffffffffu, v, 2);
+          v |= __shfl_xor_sync(0xffffffffu, v, 4);
+          any = true;
+        }
+        const int64_t word = (base + h * DT_THREADS) / 8 + warp * 4 + (lane >> 3);
+        if ((lane & 7) == 0 && word < nwords) bm[word] = v;
+      }
+    }
+    if (!__syncthreads_or(any)) continue;
+
+    // per-thread contiguous word ranges keep the emitted columns sorted
+    const int wpt = (nwords + DT_THREADS - 1) / DT_THREADS;
+    const int w0 = min(tid * wpt, nwords), w1 = min(w0 + wpt, nwords);
+    int cnt = 0;
+    for (int w = w0; w < w1; ++w) cnt += __popc(bm[w]);
+    // block exclusive scan of cnt (warp shuffles + one smem round)
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    int woff = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < DT_THREADS / 32; ++w) {
+      int sw = s_warp[w];
+      woff += (w < warp) ? sw : 0;
+      total += sw;
+    }
+    const int excl = woff + incl - cnt;
+    if (tid == 0) {
+      unsigned long long base = atomicAdd(&a.ctr->total, (unsigned long long)total);
+      a.rowoff[i] = (int64_t)base;
+      a.rowcnt[i] = total;
+      atomicAdd(&a.ctr->rows, 1u);
+      atomicMax(&a.ctr->maxrow, (unsigned)total);
+      if ((int64_t)base + total > a.lcap) atomicOr(&a.ctr->overflow, 1u);
+      s_base = (long long)base;
+    }
+    __syncthreads();
+    const int64_t base = s_base;
+    const bool store = base + total <= a.lcap;
+    int64_t pos = base + excl;
+    for (int w = w0; w < w1; ++w) {
+      uint32_t bits = bm[w];
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int64_t j = (int64_t)w * 32 + b;
+        if (store) {
+          a.pcol[pos] = (int)j;
+          a.prow[pos] = (int)i;
+        }
+        ++pos;
+        if (a.reset) Drow[j] = a.WT[j * a.ldw + i];   // D0[i][j] := W'[i][j]
+      }
+    }
+    __syncthreads();   // bm / scan storage reused by the next row
+  }
+}
+
+template <typename T>
+cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
+                   const T* c2, const T* r2, float tau, const T* WT, int64_t ldw, int reset,
+                   int64_t* rowoff, int* rowcnt, int* prow, int* pcol, int64_t lcap,
+                   DetectCounters* ctr, int grid, cudaStream_t st) {
+  if (r.hi <= r.lo) return cudaSuccess;
+  DetectArgs<T> a{D, ld, r, n, skip, c1, r1, c2, r2, tau, WT, ldw, reset,
+                  rowoff, rowcnt, prow, pcol, lcap, ctr};
+  size_t smem = sizeof(uint32_t) * (size_t)cdiv(n, 32);
+  if (grid <= 0) grid = (int)std::min<int64_t>(r.hi - r.lo, (int64_t)num_sms() * 8);
+  if (smem > 48 * 1024) {
+    auto f = c2 ? k_detect<T, true> : k_detect<T, false>;
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  if (c2)
+    k_detect<T, true><<<grid, DT_THREADS, smem, st>>>(a);
+  else
+    k_detect<T, false><<<grid, DT_THREADS, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// tombstone / swap-with-last / edge write
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_tombstone(T* D, int64_t ld, Rows r, int64_t n, int64_t k, T* WT, int64_t ldw) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const T I = Tr<T>::inf();
+  for (int64_t i = r.lo + tid; i < r.hi; i += stride)
+    if (i != k) D[(i - r.row0) * ld + k] = I;
+  if (k >= r.lo && k < r.hi) {
+    T* Dk = D + (k - r.row0) * ld;
+    for (int64_t j = tid; j < n; j += stride) Dk[j] = (j == k) ? T(0) : I;
+  }
+  for (int64_t j = tid; j < n; j += stride) {
+    WT[k * ldw + j] = (j == k) ? T(0) : I;
+    if (j != k) WT[j * ldw + k] = I;
+  }
+}
+template <typename T>
+cudaError_t tombstone(T* D, int64_t ld, Rows r, int64_t n, int64_t k, T* WT, int64_t ldw,
+                      cudaStream_t st) {
+  int grid = (int)std::min<int64_t>(cdiv(n, 256), 4 * num_sms());
+  k_tombstone<T><<<grid, 256, 0, st>>>(D, ld, r, n, k, WT, ldw);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void k_copy_row(T* dst, const T* src, int64_t n) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    dst[j] = src[j];
+}
+template <typename T>
+cudaError_t copy_row(T* dst, const T* src, int64_t n, cudaStream_t st) {
+  int grid = (int)std::min<int64_t>(cdiv(n, 256), 4 * num_sms());
+  k_copy_row<T><<<grid, 256, 0, st>>>(dst, src, n);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void k_copy_col(T* D, int64_t ld, Rows r, int64_t dst_col, int64_t src_col) {
+  for (int64_t i = r.lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.hi;
+       i += (int64_t)gridDim.x * blockDim.x)
+    D[(i - r.row0) * ld + dst_col] = D[(i - r.row0) * ld + src_col];
+}
+template <typename T>
+cudaError_t copy_col(T* D, int64_t ld, Rows r, int64_t dst_col, int64_t src_col, cudaStream_t st) {
+  if (r.hi <= r.lo) return cudaSuccess;
+  int grid = (int)std::min<int64_t>(cdiv(r.hi - r.lo, 256), 4 * num_sms());
+  k_copy_col<T><<<grid, 256, 0, st>>>(D, ld, r, dst_col, src_col);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void k_fill_col(T* D, int64_t ld, Rows r, int64_t col, T v) {
+  for (int64_t i = r.lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.hi;
+       i += (int64_t)gridDim.x * blockDim.x)
+    D[(i - r.row0) * ld + col] = v;
+}
+template <typename T>
+cudaError_t fill_col(T* D, int64_t ld, Rows r, int64_t col, T v, cudaStream_t st) {
+  if (r.hi <= r.lo) return cudaSuccess;
+  int grid = (int)std::min<int64_t>(cdiv(r.hi - r.lo, 256), 4 * num_sms());
+  k_fill_col<T><<<grid, 256, 0, st>>>(D, ld, r, col, v);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void k_set_edge(T* WT, int64_t ldw, int64_t u, int64_t v, T w, int directed) {
+  WT[v * ldw + u] = w;             // W[u][v]
+  if (!directed) WT[u * ldw + v] = w;
+}
+template <typename T>
+cudaError_t set_edge(T* WT, int64_t ldw, int64_t u, int64_t v, T w, int directed, cudaStream_t st) {
+  k_set_edge<T><<<1, 1, 0, st>>>(WT, ldw, u, v, w, directed);
+  return cudaGetLastError();
+}
+
+#define INST(T)                                                                                   \
+  template cudaError_t validate_vec<T>(const T*, const T*, int64_t, int64_t, T*, unsigned int*,    \
+                                       cudaStream_t);                                             \
+  template cudaError_t transpose_in<T>(const T*, int64_t, int64_t, T*, int64_t, unsigned int*,     \
+                                       cudaStream_t);                                             \
+  template cudaError_t fill<T>(T*, int64_t, T, cudaStream_t);                                      \
+  template cudaError_t init_d<T>(T*, int64_t, Rows, int64_t, const T*, int64_t, cudaStream_t);     \
+  template cudaError_t gather_col<T>(const T*, int64_t, Rows, int64_t, T, T*, cudaStream_t);       \
+  template cudaError_t copy_vec<T>(const T*, int64_t, int64_t, T, T*, cudaStream_t);               \
+  template cudaError_t addnode_pass1<T>(const T*, int64_t, Rows, int64_t, const T*, const T*, T*,  \
+                                        T*, int64_t, int*, int*, int, cudaStream_t);              \
+  template cudaError_t addnode_finish<T>(const T*, int, const T*, int, int64_t, Rows, int64_t,     \
+                                         int64_t, T*, T*, cudaStream_t);                          \
+  template cudaError_t rank1<T>(T*, int64_t, Rows, int64_t, const T*, const T*, const T*,          \
+                                const T*, cudaStream_t);                                          \
+  template cudaError_t addnode_write<T>(T*, int64_t, Rows, int64_t, int64_t, int, const T*,        \
+                                        const T*, T*, int64_t, const T*, const T*, cudaStream_t); \
+  template cudaError_t detect<T>(T*, int64_t, Rows, int64_t, int64_t, const T*, const T*,          \
+                                 const T*, const T*, float, const T*, int64_t, int, int64_t*,     \
+                                 int*, int*, int*, int64_t, DetectCounters*, int, cudaStream_t);  \
+  template cudaError_t tombstone<T>(T*, int64_t, Rows, int64_t, int64_t, T*, int64_t,              \
+                                    cudaStream_t);                                                \
+  template cudaError_t copy_row<T>(T*, const T*, int64_t, cudaStream_t);                           \
+  template cudaError_t copy_col<T>(T*, int64_t, Rows, int64_t, int64_t, cudaStream_t);             \
+  template cudaError_t fill_col<T>(T*, int64_t, Rows, int64_t, T, cudaStream_t);                   \
+  template cudaError_t set_edge<T>(T*, int64_t, int64_t, int64_t, T, int, cudaStream_t);
+INST(int32_t)
+INST(float)
+#undef INST
+
+}  // namespace apsp

@@ -1,0 +1,560 @@
+"""GPU parity: every hot-path call through the C ABI vs the CPU oracle.
+
+int32: bit-exact.  fp32: |g - o| <= 1e-5 |o| per entry, with 0 and inf
+matching exactly (BASELINE.json north_star).
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from conftest import golden_graph, load_golden, random_graph
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+INF = synth.INF_I32
+RTOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2412_15122_b200 as P
+    return P
+
+
+def make(P, W, directed=True, cap=None, cold=True):
+    return P.WarmAPSP(torch.from_numpy(np.ascontiguousarray(W)), directed=directed, cap=cap,
+                      cold_start=cold)
+
+
+def getD(h):
+    torch.cuda.synchronize()
+    return h.D.cpu().numpy()
+
+
+def assert_parity(G, O):
+    G = np.asarray(G)
+    O = np.asarray(O)
+    assert G.shape == O.shape
+    if np.issubdtype(G.dtype, np.integer):
+        bad = np.argwhere(G != O)
+        assert bad.size == 0, f"{len(bad)} mismatches, first {bad[:5].tolist()}: gpu {G[tuple(bad[0])]} oracle {O[tuple(bad[0])]}"
+    else:
+        Gd = G.astype(np.float64)
+        fin = np.isfinite(O)
+        assert np.array_equal(np.isfinite(Gd), fin), "inf pattern differs"
+        assert np.array_equal(Gd[O == 0] == 0, np.ones(np.count_nonzero(O == 0), bool)), "zeros differ"
+        rel = np.abs(Gd[fin] - O[fin]) / np.maximum(np.abs(O[fin]), 1e-300)
+        assert rel.max(initial=0) <= RTOL, f"max rel err {rel.max()}"
+
+
+# ------------------------------------------------------------------ cold FW (a1)
+@pytest.mark.parametrize("n", [1, 2, 5, 127, 128, 129, 255, 300, 513])
+@pytest.mark.parametrize("directed", [True, False])
+def test_cold_fw_int32(lib, rng, n, directed):
+    W = random_graph(rng, n, directed, density=0.5, lo=0, hi=40, inf_frac=0.1)
+    h = make(lib, W, directed)
+    assert_parity(getD(h), oracle.fw(W))
+
+
+def test_cold_fw_int32_bj_c1(lib):
+    W = synth.graph(synth.C1)
+    h = make(lib, W)
+    assert_parity(getD(h), oracle.fw(W))
+
+
+@pytest.mark.parametrize("n", [3, 130, 400])
+def test_cold_fw_fp32(lib, n):
+    spec = dataclasses.replace(synth.C2, n=n)
+    W = synth.graph(spec)
+    h = make(lib, W, directed=False)
+    G = getD(h)
+    assert_parity(G, oracle.fw(W))
+    assert np.array_equal(G, G.T)   # Q17: FW keeps exact symmetry
+
+
+def test_cold_fw_closed_form_cycle(lib):
+    n = 1500
+    W = np.full((n, n), INF, np.int32)
+    np.fill_diagonal(W, 0)
+    W[np.arange(n), (np.arange(n) + 1) % n] = 1
+    h = make(lib, W)
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    assert_parity(getD(h), ((j - i) % n).astype(np.int32))
+
+
+def test_cold_fw_disconnected(lib, rng):
+    W = random_graph(rng, 200, True, density=0.02, lo=1, hi=9)
+    h = make(lib, W)
+    assert_parity(getD(h), oracle.fw(W))
+
+
+# ------------------------------------------------------------------ add node (a2)
+def test_add_node_bj_c1(lib):
+    """BJ.c1: n=256, add one node with U[1,100] edges; warm == cold FW."""
+    spec = synth.C1
+    W = synth.graph(spec)
+    hg = synth.HostGraph(W, True, cap=257)
+    o, i = synth.node_edges(spec, 0, 256)
+    h = make(lib, W, cap=257)
+    x, info = h.add_node(o, i)
+    assert x == 256 and info.kind == 3 and h.n == 257
+    hg.add_node(o, i)
+    assert_parity(getD(h), oracle.fw(hg.W))
+
+
+@pytest.mark.parametrize("directed", [True, False])
+@pytest.mark.parametrize("n", [1, 7, 129, 1030])
+def test_add_node_random(lib, rng, n, directed):
+    W = random_graph(rng, n, directed, density=0.6, lo=0, hi=30, inf_frac=0.05)
+    o = rng.integers(0, 30, n).astype(np.int32)
+    o[rng.random(n) < 0.2] = INF
+    i = o.copy() if not directed else rng.integers(0, 30, n).astype(np.int32)
+    h = make(lib, W, directed, cap=n + 3)
+    h.add_node(o, i)
+    hg = synth.HostGraph(W, directed, cap=n + 3)
+    hg.add_node(o, i)
+    assert_parity(getD(h), oracle.fw(hg.W))
+
+
+def test_add_node_golden_one_node(lib):
+    g = load_golden("add_one_node.json")
+    h = make(lib, np.zeros((1, 1), np.int32), cap=2)
+    h.add_node(np.array(g["out_w"], np.int32), np.array(g["in_w"], np.int32))
+    assert getD(h).tolist() == g["expected"]
+
+
+def test_add_isolated_node_is_noop(lib, rng):
+    W = random_graph(rng, 100, True, 1.0, lo=1, hi=50)
+    h = make(lib, W, cap=101)
+    D0 = getD(h).copy()
+    h.add_node(np.full(100, INF, np.int32), np.full(100, INF, np.int32))
+    D = getD(h)
+    assert np.array_equal(D[:100, :100], D0)
+    assert np.all(D[100, :100] == INF) and np.all(D[:100, 100] == INF) and D[100, 100] == 0
+
+
+def test_add_hub_changes_every_entry(lib):
+    """Closed form: hub with edges c/4 on a complete graph of
+    uniform weight c -> every old off-diagonal distance becomes c/2."""
+    n, c = 300, 40
+    W = np.full((n, n), c, np.int32)
+    np.fill_diagonal(W, 0)
+    h = make(lib, W, cap=n + 1)
+    h.add_node(np.full(n, c // 4, np.int32), np.full(n, c // 4, np.int32))
+    D = getD(h)
+    exp = np.full((n + 1, n + 1), c // 2, np.int32)
+    exp[n, :] = c // 4
+    exp[:, n] = c // 4
+    np.fill_diagonal(exp, 0)
+    assert_parity(D, exp)
+
+
+def test_add_node_fp32_undirected(lib):
+    spec = dataclasses.replace(synth.C2, n=300)
+    W = synth.graph(spec)
+    o, i = synth.node_edges(spec, 5, 300)
+    h = make(lib, W, directed=False, cap=301)
+    h.add_node(o, i)
+    hg = synth.HostGraph(W, False, cap=301)
+    hg.add_node(o, i)
+    assert_parity(getD(h), oracle.fw(hg.W))
+
+
+def test_recursion_cold_start_by_adds(lib, rng):
+    """Algorithm 1 idea: n successive add-nodes from one node == cold FW."""
+    n = 60
+    W = random_graph(rng, n, True, 0.7, lo=1, hi=20)
+    h = make(lib, W[:1, :1], cap=n)
+    for x in range(1, n):
+        h.add_node(W[x, :x].copy(), W[:x, x].copy())
+    assert_parity(getD(h), oracle.fw(W))
+
+
+# ------------------------------------------------------------------ edge updates (a3, a4)
+def _edit(W, u, v, w, directed):
+    W2 = W.copy()
+    W2[u, v] = w
+    if not directed:
+        W2[v, u] = w
+    return W2
+
+
+@pytest.mark.parametrize("directed", [True, False])
+def test_decrease_random_and_tight(lib, rng, directed):
+    n = 260
+    W = random_graph(rng, n, directed, 1.0, lo=1, hi=100)
+    h = make(lib, W, directed)
+    for trial in range(12):
+        D = getD(h)
+        u, v = (int(x) for x in rng.choice(n, 2, replace=False))
+        w_old = int(W[u, v])
+        if trial % 2:
+            w_new = max(0, int(D[u, v]) // 2)    # tight variant: always changes entries
+        else:
+            w_new = max(0, w_old // 10)
+        if w_new >= w_old:
+            continue
+        info = h.update_edge(u, v, w_new)
+        W = _edit(W, u, v, w_new, directed)
+        assert info.kind == 1
+        assert info.early_exit == (w_new >= D[u, v])
+        assert_parity(getD(h), oracle.fw(W))
+
+
+def test_decrease_closed_form_chord(lib):
+    n = 700
+    W = np.full((n, n), INF, np.int32)
+    np.fill_diagonal(W, 0)
+    W[np.arange(n), (np.arange(n) + 1) % n] = 1
+    h = make(lib, W)
+    u, v = 10, 400
+    h.update_edge(u, v, 1)
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    exp = np.minimum((j - i) % n, (u - i) % n + 1 + (j - v) % n)
+    assert_parity(getD(h), exp.astype(np.int32))
+
+
+@pytest.mark.parametrize("directed", [True, False])
+@pytest.mark.parametrize("force", [0, 1, 2])
+def test_increase_random_and_tight(lib, rng, directed, force):
+    n = 230
+    W = random_graph(rng, n, directed, 1.0, lo=1, hi=60)
+    h = make(lib, W, directed)
+    h.set_option(0, force)
+    for trial in range(8):
+        D = getD(h)
+        if trial % 2:
+            u = int(rng.integers(n))
+            row = W[u].astype(np.int64)
+            row[u] = np.iinfo(np.int64).max
+            v = int(np.argmin(row))            # cheapest out-edge: always tight
+        else:
+            u, v = (int(x) for x in rng.choice(n, 2, replace=False))
+        w_old = int(W[u, v])
+        w_new = int(rng.choice([w_old * 10, w_old + 1, INF]))
+        info = h.update_edge(u, v, w_new)
+        tight = w_old == D[u, v]
+        mask = oracle.need_update_increase(D, u, v, w_old, directed)
+        W = _edit(W, u, v, w_new, directed)
+        assert info.kind == 2 and info.early_exit == (not tight)
+        if tight:
+            assert info.affected_pairs == mask.sum()
+            assert info.affected_rows == mask.any(axis=1).sum()
+            assert info.path == (3 if force == 2 else 2) or (force == 0 and info.path in (2, 3))
+        assert_parity(getD(h), oracle.fw(W))
+
+
+def test_increase_closed_form_cycle_cut(lib):
+    """Cycle edge u->u+1 set to INF: pairs whose arc crosses it become INF
+    (|A| = Theta(n^2), forces the dense fallback by the gate)."""
+    n = 400
+    W = np.full((n, n), INF, np.int32)
+    np.fill_diagonal(W, 0)
+    W[np.arange(n), (np.arange(n) + 1) % n] = 1
+    h = make(lib, W)
+    u = 123
+    info = h.update_edge(u, u + 1, INF)
+    W2 = _edit(W, u, u + 1, INF, True)
+    assert info.path == 3
+    assert_parity(getD(h), oracle.fw(W2))
+
+
+@pytest.mark.parametrize("force", [1, 2])
+def test_edge_updates_fp32_undirected(lib, rng, force):
+    spec = dataclasses.replace(synth.C2, n=320)
+    W = synth.graph(spec)
+    h = make(lib, W, directed=False)
+    h.set_option(0, force)
+    for trial in range(6):
+        D = getD(h)
+        u = int(rng.integers(320))
+        if trial % 2 == 0:
+            v = int(np.argmin(np.where(np.arange(320) == u, np.inf, W[u])))
+            w_new = np.float32(W[u, v] * np.float32(10))     # tight increase
+        else:
+            v = int((u + 1 + rng.integers(319)) % 320)
+            w_new = np.float32(D[u, v] * np.float32(0.5))    # tight decrease
+        h.update_edge(u, v, float(w_new))
+        W = _edit(W, u, v, w_new, False)
+        assert_parity(getD(h), oracle.fw(W))
+
+
+def test_insert_and_delete_edge(lib, rng):
+    W = random_graph(rng, 150, True, 0.1, lo=1, hi=9)
+    h = make(lib, W)
+    absent = np.argwhere((W == INF))
+    u, v = (int(x) for x in absent[len(absent) // 2])
+    h.update_edge(u, v, 3)          # insert (decrease from INF)
+    W = _edit(W, u, v, 3, True)
+    assert_parity(getD(h), oracle.fw(W))
+    h.update_edge(u, v, INF)        # delete (increase to INF)
+    W = _edit(W, u, v, INF, True)
+    assert_parity(getD(h), oracle.fw(W))
+
+
+def test_decrease_then_restore_round_trip(lib, rng):
+    W = random_graph(rng, 200, True, 1.0, lo=1, hi=100)
+    h = make(lib, W)
+    D0 = getD(h).copy()
+    u, v = 3, 77
+    h.update_edge(u, v, max(0, int(D0[u, v]) // 3))
+    h.update_edge(u, v, int(W[u, v]))
+    assert_parity(getD(h), D0)
+
+
+# ------------------------------------------------------------------ remove node (a5-a7)
+@pytest.mark.parametrize("directed", [True, False])
+@pytest.mark.parametrize("force", [0, 1, 2])
+def test_remove_random(lib, rng, directed, force):
+    n = 260
+    W = random_graph(rng, n, directed, 0.9, lo=1, hi=1000)
+    h = make(lib, W, directed)
+    h.set_option(0, force)
+    hg = synth.HostGraph(W, directed)
+    for trial in range(6):
+        D = getD(h)
+        k = int(rng.integers(hg.n))
+        mask = oracle.need_update_removal(D, k)
+        mf, info = h.remove_node(k)
+        assert mf == (hg.n - 1 if k != hg.n - 1 else -1)
+        hg.remove_node(k)
+        assert info.kind == 4
+        assert info.affected_pairs == mask.sum()
+        phi, cost = oracle.cost(mask, D.shape[0])
+        assert info.affected_rows == phi and abs(info.cost - cost) < 1e-12
+        assert_parity(getD(h), oracle.fw(hg.W))
+
+
+def test_remove_golden_hub(lib):
+    g = load_golden("hub_remove.json")
+    W, idx = golden_graph(g)
+    h = make(lib, W, directed=False)
+    mf, info = h.remove_node(idx["B"])
+    assert info.affected_pairs == 4 and info.affected_rows == 3 and info.cost == g["cost"]
+    hg = synth.HostGraph(W, False)
+    hg.remove_node(idx["B"])
+    assert_parity(getD(h), oracle.fw(hg.W))
+
+
+def test_remove_golden_star_avoided(lib):
+    g = load_golden("star_avoided_remove.json")
+    W, idx = golden_graph(g)
+    h = make(lib, W, directed=False)
+    _, info = h.remove_node(idx["C"])
+    assert info.affected_pairs == 0 and info.cost == 0.0
+
+
+def test_remove_line_metric_ties_dense(lib):
+    """Line metric: removing an interior point flags 2p(1-p)n^2 tie pairs but
+    changes no value; exercises the gate and a7."""
+    n = 301
+    x = np.arange(n) * 3
+    W = np.abs(x[:, None] - x[None, :]).astype(np.int32)
+    h = make(lib, W)
+    k = 150
+    D = getD(h)
+    mask = oracle.need_update_removal(D, k)
+    _, info = h.remove_node(k)
+    assert info.affected_pairs == mask.sum() > 0
+    hg = synth.HostGraph(W, True)
+    hg.remove_node(k)
+    assert_parity(getD(h), oracle.fw(hg.W))
+
+
+def test_remove_cycle_closed_form(lib):
+    n = 500
+    W = np.full((n, n), INF, np.int32)
+    np.fill_diagonal(W, 0)
+    W[np.arange(n), (np.arange(n) + 1) % n] = 1
+    h = make(lib, W)
+    k = n - 1   # no swap: pairs whose arc passes through k become INF
+    h.remove_node(k)
+    m = n - 1
+    i, j = np.meshgrid(np.arange(m), np.arange(m), indexing="ij")
+    exp = np.where(j >= i, j - i, INF).astype(np.int32)
+    assert_parity(getD(h), exp)
+
+
+def test_remove_then_readd_round_trip(lib, rng):
+    W = random_graph(rng, 180, True, 1.0, lo=1, hi=100)
+    h = make(lib, W)
+    D0 = getD(h).copy()
+    last = 179
+    h.remove_node(last)
+    h.add_node(W[last, :last].copy(), W[:last, last].copy())
+    assert_parity(getD(h), D0)
+
+
+@pytest.mark.parametrize("dtype", ["i32", "f32"])
+def test_remove_fp32_and_density(lib, rng, dtype):
+    if dtype == "i32":
+        spec = dataclasses.replace(synth.C3, n=400)
+    else:
+        spec = dataclasses.replace(synth.C2, n=400)
+    W = synth.graph(spec)
+    h = make(lib, W, directed=spec.directed)
+    hg = synth.HostGraph(W, spec.directed)
+    for k in (0, 399 - 1, 200):
+        h.remove_node(k)
+        hg.remove_node(k)
+        assert_parity(getD(h), oracle.fw(hg.W))
+
+
+# ------------------------------------------------------------------ sequences (BJ.c4 shape)
+def test_update_sequence_small(lib):
+    spec = dataclasses.replace(synth.C4, n=384)
+    W = synth.graph(spec)
+    cap = 384 + 16
+    hg = synth.HostGraph(W, True, cap=cap)
+    h = make(lib, W, cap=cap)
+    seq = synth.update_sequence(spec, synth.HostGraph(W, True, cap=cap), 0, 30)
+    for up in seq:
+        if up.kind == "add":
+            h.add_node(up.out_w, up.in_w)
+            hg.add_node(up.out_w, up.in_w)
+        elif up.kind == "remove":
+            h.remove_node(up.k)
+            hg.remove_node(up.k)
+        else:
+            h.update_edge(up.u, up.v, up.w_new)
+            hg.set_edge(up.u, up.v, up.w_new)
+        assert h.n == hg.n
+    assert_parity(getD(h), oracle.fw(hg.W))
+
+
+# ------------------------------------------------------------------ query (a8)
+def _check_path(W, D, s, t, dist, path):
+    if s == t:
+        assert path == [s] and dist == 0
+        return
+    if D[s, t] == INF or (np.issubdtype(np.asarray(D).dtype, np.floating) and not np.isfinite(D[s, t])):
+        assert path == []
+        return
+    assert oracle.path_is_valid(W, path, s, t)
+    pw = oracle.path_weight(W, path)
+    if np.issubdtype(np.asarray(W).dtype, np.integer):
+        assert pw == dist == D[s, t]
+    else:
+        assert abs(pw - dist) <= RTOL * abs(dist)
+
+
+def test_query_golden_hub(lib):
+    g = load_golden("hub_query.json")
+    W, idx = golden_graph(g)
+    h = make(lib, W, directed=False)
+    d, path, nc = h.query(idx["A"], idx["C"])
+    assert d == g["dist"] and [g["nodes"][i] for i in path] == g["path"] and nc == 3
+
+
+@pytest.mark.parametrize("directed", [True, False])
+def test_query_random(lib, rng, directed):
+    n = 300
+    W = random_graph(rng, n, directed, 0.3, lo=1, hi=20, inf_frac=0.0)
+    h = make(lib, W, directed)
+    D = getD(h)
+    for _ in range(40):
+        s, t = (int(x) for x in rng.integers(0, n, 2))
+        d, path, nc = h.query(s, t)
+        assert d == D[s, t]
+        _check_path(W, D, s, t, d, path)
+        if s != t and D[s, t] != INF:
+            assert nc == len(oracle.candidates(D, s, t))
+
+
+def test_query_zero_weights(lib, rng):
+    n = 40
+    W = random_graph(rng, n, True, 0.5, lo=0, hi=2)
+    h = make(lib, W)
+    D = getD(h)
+    for s in range(0, n, 3):
+        for t in range(1, n, 5):
+            d, path, _ = h.query(s, t)
+            _check_path(W, D, s, t, d, path)
+
+
+def test_query_batch_matches_single(lib, rng):
+    spec = dataclasses.replace(synth.C5, n=500)
+    W = synth.graph(spec)
+    h = make(lib, W)
+    D = getD(h)
+    s, t = synth.query_pairs(spec.seed, 500, 64)
+    dist, paths, lens, nc = h.query_batch(s, t, path_cap=32)
+    dist, paths, lens = dist.cpu().numpy(), paths.cpu().numpy(), lens.cpu().numpy()
+    for q in range(64):
+        assert dist[q] == D[s[q], t[q]]
+        p = paths[q, : lens[q]].tolist()
+        _check_path(W, D, int(s[q]), int(t[q]), dist[q], p)
+
+
+def test_query_fp32_and_cycle(lib):
+    spec = dataclasses.replace(synth.C2, n=256)
+    W = synth.graph(spec)
+    h = make(lib, W, directed=False)
+    D = getD(h)
+    for s, t in [(0, 1), (5, 200), (17, 17), (255, 3)]:
+        d, path, _ = h.query(s, t)
+        _check_path(W, D, s, t, d, path)
+    n = 300
+    C = np.full((n, n), INF, np.int32)
+    np.fill_diagonal(C, 0)
+    C[np.arange(n), (np.arange(n) + 1) % n] = 1
+    h2 = make(lib, C)
+    d, path, nc = h2.query(10, 250)
+    assert d == 240 and path == list(range(10, 251)) and nc == 241
+
+
+def test_query_unreachable(lib):
+    W = np.array([[0, 5, INF], [INF, 0, INF], [INF, INF, 0]], np.int32)
+    h = make(lib, W)
+    d, path, nc = h.query(1, 0)
+    assert d == INF and path == [] and nc == 0
+
+
+# ------------------------------------------------------------------ errors
+def test_argument_errors_leave_state(lib, rng):
+    P = lib
+    W = random_graph(rng, 50, True, 1.0, lo=1, hi=9)
+    h = make(lib, W, cap=50)
+    D0 = getD(h).copy()
+    with pytest.raises(P.ApspError) as e:
+        h.remove_node(50)
+    assert e.value.status == 2
+    with pytest.raises(P.ApspError) as e:
+        h.update_edge(3, 3, 1)
+    assert e.value.status == 1
+    with pytest.raises(P.ApspError) as e:
+        h.update_edge(3, 4, -1)
+    assert e.value.status == 1
+    with pytest.raises(P.ApspError) as e:
+        h.update_edge(3, 4, 1.5)
+    assert e.value.status == 1
+    with pytest.raises(P.ApspError) as e:
+        h.add_node(np.ones(50, np.int32), np.ones(50, np.int32))
+    assert e.value.status == 3
+    h2 = make(lib, W, cap=51)
+    bad = np.ones(50, np.int32)
+    bad[7] = -4
+    with pytest.raises(P.ApspError) as e:
+        h2.add_node(bad, np.ones(50, np.int32))
+    assert e.value.status == 1 and h2.n == 50
+    assert np.array_equal(getD(h), D0)
+    one = make(lib, np.zeros((1, 1), np.int32))
+    with pytest.raises(P.ApspError) as e:
+        one.remove_node(0)
+    assert e.value.status == 4
+
+
+def test_create_rejects_bad_W(lib):
+    P = lib
+    W = np.array([[0, 1], [-1, 0]], np.int32)
+    with pytest.raises(P.ApspError):
+        make(lib, W)
+    W = np.array([[1, 1], [1, 0]], np.int32)
+    with pytest.raises(P.ApspError):
+        make(lib, W)

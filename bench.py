@@ -1,0 +1,438 @@
+#!/usr/bin/env python
+"""bench.py — warm-start APSP update throughput on B200 (BASELINE.json metric).
+
+Metric (BJ.metric): "APSP entries updated/s per warm-start update; ms/update
+at n=32768".  Workload: BJ.c4 — n=32768 directed complete graph, int32
+weights U[1,1000], a seeded sequence of updates (1/3 add-node, 1/3
+remove-node, 1/3 edge reweight by a log-uniform factor in [0.1, 10]; DESIGN.md
+Q18).  One "step" = 64 consecutive updates of that sequence (every hot-path
+row a2-a7 the sequence exercises); entries updated per update = n_after^2.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1: launched under torch.distributed.run, one rank per GPU; D is
+row-sharded over the ranks (NCCL over NVLink inside the library), every
+rank applies the same updates, time = max over ranks.
+
+--impl reference: the CPU oracle (plain Floyd–Warshall, cold, as the paper's
+comparator) timed on the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import dataclasses
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+UPDATES_PER_STEP = 64
+METRIC = "APSP entries updated/s per warm-start update (BJ.c4 sequence)"
+UNIT = "entries/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--n", type=int, default=synth.C4.n)
+    p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-cold", action="store_true", help="skip timing one cold FW")
+    p.add_argument("--json-extra", default=None, help="write the detailed report here")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            mp = json.load(f)
+        return mp, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self, gpu_index=None):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    rows.append((int(parts[0]), float(parts[1]), float(parts[2]), parts[5:9]))
+                except ValueError:
+                    continue
+        os.unlink(self.path)
+        if gpu_index is not None:
+            sel = [r for r in rows if r[0] == gpu_index]
+            rows = sel or rows
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[3]) if v.lower().startswith("active")})
+        under = [r[1] for r in rows if r[1] > 400] or [r[1] for r in rows]
+        return {"sm_mhz": statistics.median(under), "sm_max_mhz": max(r[2] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- oracle leg
+def oracle_pivot_time(W: np.ndarray, budget_s: float = 12.0, max_pivots: int = 64):
+    """Time the CPU oracle's Floyd–Warshall (cold recompute per update) on a
+    bounded sample: `p` pivots of the full-size n x n int64 matrix.  Returns
+    (seconds per pivot, pivots timed)."""
+    import oracle
+
+    A = oracle.to_oracle(W)
+    n = A.shape[0]
+    t0 = time.perf_counter()
+    oracle.fw_raw_i64(A, 0, 1)
+    t1 = time.perf_counter() - t0
+    p = int(max(2, min(max_pivots, budget_s / max(t1, 1e-6))))
+    t0 = time.perf_counter()
+    oracle.fw_raw_i64(A, 1, 1 + p)
+    tp = (time.perf_counter() - t0) / p
+    del A
+    return tp, p, n
+
+
+def cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (cold FW per update) on the host cores."""
+    if rank != 0:
+        return
+    spec = dataclasses.replace(synth.C4, n=args.n, seed=args.seed)
+    W = synth.graph(spec)
+    n = spec.n
+    step_times = []
+    pivots = 0
+    for s in range(args.warmup + args.steps):
+        tp, p, _ = oracle_pivot_time(W, budget_s=4.0, max_pivots=16)
+        if s >= args.warmup:
+            # one step = 64 updates, each an oracle cold FW (n pivots) at n
+            step_times.append(UPDATES_PER_STEP * n * tp)
+            pivots += p
+    step_s = statistics.median(step_times)
+    value = UPDATES_PER_STEP * n * n / step_s
+    c = cores()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (seeded BJ.c4 graph, U[1,1000])",
+        "config": {"workload": "BJ.c4", "n": n, "updates_per_step": UPDATES_PER_STEP, "directed": True},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": c, "kind": "oracle",
+                         "sample": f"{pivots} Floyd-Warshall pivots of the n={n} int64 matrix timed, "
+                                   f"extrapolated x n per update (cold recompute), {UPDATES_PER_STEP} updates/step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our leg
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if world > 1:
+            import torch.distributed as dist  # noqa: F401
+        run_reference(args, rank, world)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+
+    import paper_2412_15122_b200 as P
+    from paper_2412_15122_b200 import _lib as L
+
+    spec = dataclasses.replace(synth.C4, n=args.n, seed=args.seed)
+    n0 = spec.n
+    steps_total = args.warmup + args.steps + (0 if args.no_e2e else args.steps)
+    cap = n0 + UPDATES_PER_STEP + 4 * steps_total
+    t_setup = time.perf_counter()
+    W = synth.graph(spec)
+    hg = synth.HostGraph(W, True, cap=cap)
+    seq = synth.update_sequence(spec, hg, 0, steps_total * UPDATES_PER_STEP)
+    del hg
+
+    nccl_id = None
+    if world > 1:
+        obj = [L.apsp_nccl_unique_id() if rank == 0 else None]
+        pg.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    stream = torch.cuda.current_stream(dev)
+    h = P.WarmAPSP(torch.from_numpy(W), directed=True, cap=cap, device=dev, stream=stream, rank=rank,
+                   world=world, nccl_id=nccl_id, cold_start=False)
+    del W
+
+    def barrier():
+        if pg is not None:
+            pg.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x):
+        if pg is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        return float(t.item())
+
+    # cold start: D := APSP(W) by blocked FW (a1), timed once (warm-vs-cold speedup)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    h.cold_fw()
+    e1.record(stream)
+    barrier()
+    cold_ms = max_over_ranks(e0.elapsed_time(e1))
+
+    # device-resident add-node vectors for the device-timed steps
+    dvecs = {}
+    for up in seq:
+        if up.kind == "add":
+            dvecs[up.t] = (torch.from_numpy(up.out_w).to(dev), torch.from_numpy(up.in_w).to(dev))
+    setup_s = time.perf_counter() - t_setup
+
+    per_update = []   # (kind, ms, n_after, info)
+
+    def run_step(s, record):
+        ups = seq[s * UPDATES_PER_STEP:(s + 1) * UPDATES_PER_STEP]
+        evs = []
+        infos = []
+        for up in ups:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            if up.kind == "add":
+                o, i = dvecs[up.t]
+                _, info = L.apsp_add_node(h.h, o.data_ptr(), i.data_ptr())
+            elif up.kind == "remove":
+                _, info = L.apsp_remove_node(h.h, up.k)
+            else:
+                info = L.apsp_update_edge(h.h, up.u, up.v, float(up.w_new))
+            b.record(stream)
+            evs.append((a, b))
+            infos.append((up.kind, info))
+        if record:
+            torch.cuda.synchronize(dev)
+            for (a, b), (kind, info) in zip(evs, infos):
+                per_update.append((kind, a.elapsed_time(b), info.n_after, info.as_dict()))
+
+    for s in range(args.warmup):
+        run_step(s, False)
+    torch.cuda.synchronize(dev)
+
+    # ---------------- timed region (device-resident inputs)
+    clk = ClockSampler()
+    if rank == 0:
+        clk.start()
+    L.apsp_profile_reset(h.h)
+    L.apsp_profile_enable(h.h, True)
+    launches0 = h.launches()
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for s in range(args.warmup, args.warmup + args.steps):
+        run_step(s, True)
+    t1.record(stream)
+    barrier()
+    total_ms = max_over_ranks(t0.elapsed_time(t1))
+    launches = h.launches() - launches0
+    L.apsp_profile_enable(h.h, False)
+    prof = L.apsp_profile_read(h.h)
+    clocks = clk.stop(gpu_index=None) if rank == 0 else None
+
+    entries = sum(na * na for _, _, na, _ in per_update)
+    value = entries / (total_ms / 1e3)
+    ms_per_step = total_ms / args.steps
+
+    # ---------------- e2e: public API with host buffers, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        s_lo = args.warmup + args.steps
+        pinned = {}
+        for up in seq[s_lo * UPDATES_PER_STEP:]:
+            if up.kind == "add":
+                pinned[up.t] = (torch.from_numpy(up.out_w).pin_memory(), torch.from_numpy(up.in_w).pin_memory())
+        res_host = torch.empty(cap, dtype=torch.int32).pin_memory()
+        h2d = d2h = 0
+        entries_e2e = 0
+        barrier()
+        q0 = torch.cuda.Event(enable_timing=True)
+        q1 = torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        for s in range(s_lo, s_lo + args.steps):
+            ups = seq[s * UPDATES_PER_STEP:(s + 1) * UPDATES_PER_STEP]
+            for up in ups:
+                if up.kind == "add":
+                    o, i = pinned[up.t]
+                    od = o.to(dev, non_blocking=True)
+                    idv = i.to(dev, non_blocking=True)
+                    h2d += o.numel() * 4 * 2
+                    x, info = h.add_node(od, idv)
+                elif up.kind == "remove":
+                    _, info = h.remove_node(up.k)
+                else:
+                    info = h.update_edge(up.u, up.v, up.w_new)
+                entries_e2e += info.n_after * info.n_after
+            # the step's result back to the host: row 0 of D (owner) — distances from node 0
+            nn = h.n
+            if h.row0 == 0:
+                res_host[:nn].copy_(h.D_local[0, :nn], non_blocking=True)
+                d2h += nn * 4
+        q1.record(stream)
+        barrier()
+        e2e_ms = max_over_ranks(q0.elapsed_time(q1))
+        e2e = {"value": entries_e2e / (e2e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+               "ms_per_step": e2e_ms / args.steps}
+
+    # ---------------- roofline of the dominant kernel class
+    mp, peak_kind = peaks()
+    hbm_peak = float(mp.get("hbm_gbs", 6650.0))
+    cls_ms = {k: v[0] for k, v in prof.items() if k != "other"}
+    dom = max(cls_ms, key=cls_ms.get)
+    ms_d, cnt_d, work_d = prof[dom]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get(dom)
+        except Exception:
+            traffic = None
+    if dom.startswith("fw"):
+        sm_mhz = float(mp.get("sm_max_mhz", 1965.0))
+        peak = 148 * 64 * sm_mhz * 1e6 / 1e12     # VIADDMNMX: 64 relaxations/clk/SM
+        achieved = work_d / (ms_d / 1e3) / 1e12
+        roof = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "Trelax/s",
+                "frac": achieved / peak, "traffic": traffic, "launches": cnt_d}
+    else:
+        achieved = work_d / (ms_d / 1e3) / 1e9 if ms_d > 0 else 0.0
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": traffic, "launches": cnt_d,
+                "peak_kind": f"{peak_kind} copy bandwidth"}
+    share = {k: round(v[0] / max(total_ms, 1e-9), 4) for k, v in prof.items()}
+    kern = {k: {"ms": round(v[0], 3), "launches": v[1],
+                "achieved": (round(v[2] / (v[0] / 1e3) / (1e12 if k.startswith("fw") else 1e9), 2) if v[0] > 0 else None),
+                "unit": "Trelax/s" if k.startswith("fw") else "GB/s"} for k, v in prof.items()}
+
+    # ---------------- per-type breakdown
+    by = {}
+    for kind, ms, na, info in per_update:
+        by.setdefault(kind, []).append((ms, info))
+    breakdown = {}
+    for kind, lst in by.items():
+        mss = [m for m, _ in lst]
+        breakdown[kind] = {
+            "count": len(lst), "ms_median": statistics.median(mss), "ms_mean": statistics.mean(mss),
+            "ms_max": max(mss), "early_exit": sum(i["early_exit"] for _, i in lst),
+            "paths": {str(p): sum(1 for _, i in lst if i["path"] == p) for p in sorted({i["path"] for _, i in lst})},
+            "affected_pairs_median": statistics.median([i["affected_pairs"] for _, i in lst]),
+        }
+    all_ms = [m for _, m, _, _ in per_update]
+
+    # ---------------- CPU baseline (oracle on the host cores, rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        Wc = synth.graph(spec)
+        tp, p, n = oracle_pivot_time(Wc, budget_s=12.0)
+        del Wc
+        per_update_s = n * tp
+        cpu = {"value": n * n / per_update_s, "unit": UNIT, "cores": cores(), "kind": "oracle",
+               "sample": f"{p} Floyd-Warshall pivots of the n={n} int64 oracle matrix "
+                         f"({tp * 1e3:.1f} ms/pivot), extrapolated x n: the oracle's cold recompute per update"}
+
+    n_final = h.n
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (seeded BJ.c4 graph: directed complete, U[1,1000]; seeded update sequence)",
+            "config": {"workload": "BJ.c4", "n": n0, "n_final": n_final, "updates_per_step": UPDATES_PER_STEP,
+                       "directed": True, "parallelism": f"row-shard x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (D = 4 GiB, WT = 4 GiB)",
+                       "ms_per_update_median": statistics.median(all_ms),
+                       "ms_per_update_mean": statistics.mean(all_ms),
+                       "cold_fw_ms": cold_ms, "warm_vs_cold_speedup": cold_ms / statistics.mean(all_ms)},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "kernels": kern,
+            "kernel_share": share,
+            "per_type": breakdown,
+            "setup_s": setup_s,
+        }
+        print(json.dumps(line), flush=True)
+        if args.json_extra:
+            with open(args.json_extra, "w") as f:
+                json.dump(line, f, indent=1)
+    h.close()
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

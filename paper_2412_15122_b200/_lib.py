@@ -26,8 +26,12 @@ SYMBOLS = [
     "apsp_layout", "apsp_workspace_bytes", "apsp_create", "apsp_destroy", "apsp_set_option",
     "apsp_cold_fw", "apsp_add_node", "apsp_remove_node", "apsp_update_edge", "sp_pair_query",
     "sp_pair_query_batch", "apsp_size", "apsp_last_error", "apsp_status_string",
-    "apsp_nccl_unique_id", "apsp_kernel_launches",
+    "apsp_nccl_unique_id", "apsp_kernel_launches", "apsp_profile_enable", "apsp_profile_reset",
+    "apsp_profile_read",
 ]
+# kernel classes of apsp_profile_read (apsp_kernel_class)
+K_CLASSES = ["fw_diag", "fw_panel", "fw_tile", "add_pass1", "rank1", "detect", "sparse0",
+             "sparse_r", "query", "other"]
 
 
 class UpdateInfo(ctypes.Structure):
@@ -74,6 +78,9 @@ def _load():
         "apsp_status_string": (ctypes.c_char_p, [ctypes.c_int]),
         "apsp_nccl_unique_id": (ctypes.c_int, [vp]),
         "apsp_kernel_launches": (i64, [vp]),
+        "apsp_profile_enable": (ctypes.c_int, [vp, ctypes.c_int]),
+        "apsp_profile_reset": (ctypes.c_int, [vp]),
+        "apsp_profile_read": (ctypes.c_int, [vp, ctypes.c_int, P(dbl), P(i64), P(dbl)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -171,3 +178,21 @@ def apsp_nccl_unique_id():
     buf = ctypes.create_string_buffer(128)
     check(None, lib.apsp_nccl_unique_id(buf))
     return buf.raw
+
+
+def apsp_profile_enable(h, on=True):
+    check(h, lib.apsp_profile_enable(h, int(on)))
+
+
+def apsp_profile_reset(h):
+    check(h, lib.apsp_profile_reset(h))
+
+
+def apsp_profile_read(h):
+    """{class: (ms, launches, algorithmic work)} accumulated since the last reset."""
+    out = {}
+    for c, name in enumerate(K_CLASSES):
+        ms, cnt, work = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
+        check(h, lib.apsp_profile_read(h, c, ctypes.byref(ms), ctypes.byref(cnt), ctypes.byref(work)))
+        out[name] = (ms.value, cnt.value, work.value)
+    return out

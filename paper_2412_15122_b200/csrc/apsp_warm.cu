@@ -74,16 +74,18 @@ Nccl g_nccl;
 
 // ------------------------------------------------------------------ workspace plan
 struct Plan {
-  int64_t ld, lcap, maxchunk;
+  int64_t ld, lcap, ocap, maxchunk;
   size_t off_wt, off_vec, off_rowpart, off_colpart, off_rowoff, off_rowcnt, off_chg, off_prow,
-      off_pcol, off_panel, off_small, total;
+      off_pcol, off_plb, off_popen, off_ocol, off_ocnt, off_gprow, off_gpcol, off_glb, off_gfull,
+      off_slid, off_slw, off_wnext, off_panel, off_pt, off_small, total;
+  int64_t ldpt;
 };
 
 // ld: leading dimension of D, also used for WT and every scratch vector.
 Plan make_plan(int64_t cap, int world, int64_t ld) {
   Plan p;
   p.ld = ld;
-  p.maxchunk = cdiv(cdiv(p.ld, 4), 256);
+  p.maxchunk = cdiv(cdiv(p.ld, 4), 128);   // add-node pass-1 column chunks (512 columns)
   int64_t lc = cap * cap / 32;
   p.lcap = std::min<int64_t>(std::max<int64_t>(lc, 1 << 20), (int64_t)1 << 28);
   size_t o = 0;
@@ -99,9 +101,24 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   p.off_rowoff = take(sizeof(int64_t) * (size_t)cap);
   p.off_rowcnt = take(sizeof(int32_t) * (size_t)cap);
   p.off_chg = take(sizeof(int32_t) * (size_t)cap * 2);
+  p.ocap = std::max<int64_t>(p.lcap / 4, 1 << 18);
   p.off_prow = take(sizeof(int32_t) * (size_t)p.lcap);
   p.off_pcol = take(sizeof(int32_t) * (size_t)p.lcap);
+  p.off_plb = take(sizeof(int32_t) * (size_t)p.lcap);
+  p.off_popen = take((size_t)p.lcap);
+  p.off_ocol = take(sizeof(int32_t) * (size_t)p.lcap);
+  p.off_ocnt = take(sizeof(int32_t) * (size_t)cap);
+  p.off_gprow = take(sizeof(int32_t) * (size_t)p.ocap);
+  p.off_gpcol = take(sizeof(int32_t) * (size_t)p.ocap);
+  p.off_glb = take(sizeof(int32_t) * (size_t)p.ocap);
+  p.off_gfull = take((size_t)p.ocap);
+  p.off_slid = take(sizeof(int32_t) * (size_t)cap * kSL);
+  p.off_slw = take(sizeof(int32_t) * (size_t)cap * kSL);
+  p.off_wnext = take(sizeof(int32_t) * (size_t)cap);
   p.off_panel = take(world > 1 ? sizeof(int32_t) * (size_t)kTile * p.ld : 256);
+  // transposed pivot column panel for the FW phase-3 kernel (kTile x ldpt)
+  p.ldpt = round_up(world > 1 ? round_up(cdiv(cap, world), kTile) : cap, kTile);
+  p.off_pt = take(sizeof(int32_t) * (size_t)kTile * p.ldpt);
   p.off_small = take(64 * 1024);
   p.total = o;
   return p;
@@ -185,7 +202,19 @@ struct apsp_handle {
   int* chg(int k) { return reinterpret_cast<int*>(ws + plan.off_chg) + (size_t)k * cap; }
   int* prow() { return reinterpret_cast<int*>(ws + plan.off_prow); }
   int* pcol() { return reinterpret_cast<int*>(ws + plan.off_pcol); }
+  template <typename T> T* plb() { return reinterpret_cast<T*>(ws + plan.off_plb); }
+  unsigned char* popen() { return ws + plan.off_popen; }
+  int* ocol() { return reinterpret_cast<int*>(ws + plan.off_ocol); }
+  int* ocnt() { return reinterpret_cast<int*>(ws + plan.off_ocnt); }
+  int* gprow() { return reinterpret_cast<int*>(ws + plan.off_gprow); }
+  int* gpcol() { return reinterpret_cast<int*>(ws + plan.off_gpcol); }
+  template <typename T> T* glb() { return reinterpret_cast<T*>(ws + plan.off_glb); }
+  unsigned char* gfull() { return ws + plan.off_gfull; }
+  int* slid() { return reinterpret_cast<int*>(ws + plan.off_slid); }
+  template <typename T> T* slw() { return reinterpret_cast<T*>(ws + plan.off_slw); }
+  template <typename T> T* wnext() { return reinterpret_cast<T*>(ws + plan.off_wnext); }
   template <typename T> T* panel() { return reinterpret_cast<T*>(ws + plan.off_panel); }
+  template <typename T> T* pt() { return reinterpret_cast<T*>(ws + plan.off_pt); }
   DetectCounters* ctr() { return reinterpret_cast<DetectCounters*>(ws + plan.off_small); }
   int* anyflag() { return reinterpret_cast<int*>(ws + plan.off_small + 256); }
   unsigned char* small() { return ws + plan.off_small + 512; }   // query scratch etc.
@@ -304,7 +333,7 @@ apsp_status fw_impl(apsp_handle* h) {
       const double mo = (double)(m - (own ? kb : 0));   // rows outside the pivot block
       PK(APSP_K_FW_PANEL, mo * kb * kb, fw_col_panel<T>(D, ld, m, K0, kb, P + K0, ld, skip_ti, h->st));
       PK(APSP_K_FW_TILE, mo * (double)(n - kb) * kb,
-         fw_rest<T>(D, ld, m, n, K0, kb, P, ld, skip_ti, h->st));
+         fw_rest_pt<T>(D, ld, m, n, K0, kb, P, ld, skip_ti, h->pt<T>(), h->plan.ldpt, h->st));
     }
   }
   return APSP_OK;
@@ -329,7 +358,8 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   CKR(cudaMemsetAsync(h->ctr(), 0, sizeof(DetectCounters), h->st));
   PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
      detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, h->WT<T>(), h->ld, 1,
-               h->rowoff(), h->rowcnt(), h->prow(), h->pcol(), h->plan.lcap, h->ctr(), 0, h->st));
+               h->rowoff(), h->rowcnt(), h->prow(), h->pcol(), h->plb<T>(), h->plan.lcap, h->ctr(),
+               0, h->st));
   if (removal) CK(tombstone<T>(h->Dl<T>(), h->ld, r, n, skip, h->WT<T>(), h->ld, h->st));
 
   // counters -> host (|A|, Phi, max|A_i|, overflow), summed over ranks
@@ -365,23 +395,56 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   }
   if (info) info->path = 2;
   if (total == 0) return APSP_OK;
-  // sparse: round 0 over all m, then rounds over A_i until no entry changes
+  // ---- sparse recompute (a6) ----
+  // A: shortlist pass over every listed pair: certify ties (value == lb)
   if (local_total > 0)
-    PK(APSP_K_SPARSE0, 8.0 * (double)local_total * (double)n,
-       sparse_round0<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, n, h->prow(), h->pcol(),
-                        local_total, h->st));
+    PK(APSP_K_SPARSE0, (double)local_total * kSL * 2.0 * sizeof(T),
+       sparse_short<T>(h->Dl<T>(), h->ld, h->row0, h->slid(), h->slw<T>(), h->wnext<T>(), h->prow(),
+                       h->pcol(), h->plb<T>(), local_total, h->popen(), 0, h->st));
+  CK(sparse_compact<T>(r, h->rowoff(), h->rowcnt(), h->pcol(), h->plb<T>(), h->popen(), h->ocol(),
+                       h->ocnt(), h->gprow(), h->gpcol(), h->glb<T>(), h->gfull(), h->plan.ocap,
+                       h->ctr(), h->st));
+  CKR(cudaMemcpyAsync(h->host_small, h->ctr(), sizeof(DetectCounters), cudaMemcpyDeviceToHost, h->st));
+  CKR(cudaStreamSynchronize(h->st));
+  int64_t nopen = (int64_t)hc->open_total;
+  int64_t ovf = (hc->overflow & 2u) ? 1 : 0;
+  if (h->world > 1) {
+    long long* v = reinterpret_cast<long long*>(h->small());
+    long long hv2[2] = {(long long)nopen, (long long)ovf};
+    CKR(cudaMemcpyAsync(v, hv2, sizeof hv2, cudaMemcpyHostToDevice, h->st));
+    NK(g_nccl.AllReduce(v, v, 2, ncclInt64, ncclSum, h->comm, h->st));
+    CKR(cudaMemcpyAsync(hs, v, sizeof hv2, cudaMemcpyDeviceToHost, h->st));
+    CKR(cudaStreamSynchronize(h->st));
+    ovf = (int64_t)hs[1];
+  }
+  if (info) info->rounds = 0;
+  if (ovf) {
+    if (info) info->path = 3;
+    return fw_impl<T>(h);
+  }
+  if (nopen > 0) {
+    // A2: shortlist pass over the open pairs now that certified values are final
+    CK(sparse_short<T>(h->Dl<T>(), h->ld, h->row0, h->slid(), h->slw<T>(), h->wnext<T>(),
+                       h->gprow(), h->gpcol(), h->glb<T>(), nopen, h->gfull(), 1, h->st));
+    // B: full O(n) scan for the pairs the shortlist could not settle
+    PK(APSP_K_SPARSE_R, 8.0 * (double)nopen * (double)n,
+       sparse_full<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, n, h->gprow(), h->gpcol(),
+                      h->glb<T>(), h->gfull(), nopen, h->st));
+  }
+  // rounds over the open entries of each row until no entry changes
   int in = 0;
   CKR(cudaMemsetAsync(h->chg(in), 1, sizeof(int) * h->cap, h->st));
-  int rounds = 1;
-  bool converged = (maxrow <= 1);
+  int rounds = 0;
+  bool converged = false;
   int* hflag = reinterpret_cast<int*>(h->host_small);
-  for (; !converged && rounds <= h->max_rounds; ++rounds) {
+  for (; !converged && rounds < h->max_rounds; ++rounds) {
     CKR(cudaMemsetAsync(h->chg(in ^ 1), 0, sizeof(int) * h->cap, h->st));
     CKR(cudaMemsetAsync(h->anyflag(), 0, sizeof(int), h->st));
-    if (local_total > 0)
-      PK(APSP_K_SPARSE_R, 0.0, sparse_round<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, n, h->prow(), h->pcol(),
-                         local_total, h->rowoff(), h->rowcnt(), h->chg(in), h->chg(in ^ 1),
-                         h->anyflag(), h->st));
+    if (nopen > 0)
+      PK(APSP_K_SPARSE_R, 0.0,
+         sparse_round<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->gprow(), h->gpcol(),
+                         h->glb<T>(), nopen, h->rowoff(), h->ocnt(), h->ocol(), h->chg(in),
+                         h->chg(in ^ 1), h->anyflag(), h->st));
     if (h->world > 1)
       NK(g_nccl.AllReduce(h->anyflag(), h->anyflag(), 1, ncclInt32, ncclMax, h->comm, h->st));
     CKR(cudaMemcpyAsync(hflag, h->anyflag(), sizeof(int), cudaMemcpyDeviceToHost, h->st));
@@ -431,6 +494,9 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
      rank1<T>(h->Dl<T>(), ld, r, n, col, row, nullptr, nullptr, h->st));
   CK(addnode_write<T>(h->Dl<T>(), ld, r, n, x, h->local(x) ? 1 : 0, col, row, h->WT<T>(), ld, ow,
                       iw, h->st));
+  CK(shortlist_add_bound<T>(h->wnext<T>(), ow, n, h->st));          // new in-edges x -> j
+  CK(shortlist_build<T>(h->WT<T>(), ld, n + 1, nullptr, x, x + 1, h->slid(), h->slw<T>(),
+                        h->wnext<T>(), h->st));                      // in-edges of x
   h->n = n + 1;
   if (new_index) *new_index = x;
   if (info) {
@@ -482,6 +548,7 @@ apsp_status remove_node_impl(apsp_handle* h, int64_t k, int64_t* moved_from, aps
   CK(fill<T>(WT + last * ld, n, I, h->st));
   Rows rw{0, n, 0};
   CK(fill_col<T>(WT, ld, rw, last, I, h->st));
+  CK(shortlist_remove<T>(h->slid(), h->slw<T>(), h->wnext<T>(), n, k, last, h->st));
   h->n = n - 1;
   if (moved_from) *moved_from = (k != last) ? last : -1;
   if (info) info->n_after = h->n;
@@ -521,6 +588,7 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
     if (!(w_new < duv)) {
       if (info) info->early_exit = 1;
       CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
+      CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
       return APSP_OK;
     }
     // D'[i][j] = min(D[i][j], D[i][u] + w + D[v][j] (, D[i][v] + w + D[u][j]))
@@ -535,6 +603,7 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
     PK(APSP_K_RANK1, 4.0 * (double)(r.hi - r.lo) * (double)n,
        rank1<T>(h->Dl<T>(), ld, r, n, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, h->st));
     CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
+    CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
     if (info) info->path = 1;
     return APSP_OK;
   }
@@ -546,6 +615,7 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
   if (!tight) {
     if (info) info->early_exit = 1;
     CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
+    CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
     return APSP_OK;
   }
   CK(gather_col<T>(h->Dl<T>(), ld, r, u, w_old, c1, h->st));   // D[i][u] + w_old
@@ -556,7 +626,9 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
     s = snap_row<T>(h, u, T(0), r2);
     if (s != APSP_OK) return s;
   }
-  CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));   // W' before the D0 reset
+  // W' (WT and the shortlists) before the D0 reset
+  CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
+  CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
   return recompute<T>(h, -1, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, false, info);
 }
 
@@ -699,6 +771,7 @@ apsp_status apsp_create(apsp_handle** out, apsp_dtype dtype, int directed, int64
     CK(fill<T>(h->WT<T>(), (int64_t)cap * h->ld, Tr<T>::inf(), h->st));
     CKR(cudaMemsetAsync(&h->ctr()->err, 0, sizeof(unsigned), h->st));
     CK(transpose_in<T>(reinterpret_cast<const T*>(W), ldw, n, h->WT<T>(), h->ld, &h->ctr()->err, h->st));
+    CK(shortlist_build<T>(h->WT<T>(), h->ld, n, nullptr, 0, n, h->slid(), h->slw<T>(), h->wnext<T>(), h->st));
     unsigned* herr = reinterpret_cast<unsigned*>(h->host_small);
     CKR(cudaMemcpyAsync(herr, &h->ctr()->err, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
     CKR(cudaStreamSynchronize(h->st));

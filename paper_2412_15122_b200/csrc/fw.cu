@@ -232,6 +232,155 @@ __global__ void __launch_bounds__(NTH, 1) fw_tile_kernel(TileArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Phase 3, fast path: A comes from PT, the pivot column panel stored
+// TRANSPOSED (PT[k][i] = D[i][K0 + k], rows of ldpt elements, padded with INF
+// to whole tiles), so both operand tiles arrive with 16-byte cp.async in the
+// layout the inner loop reads (As[k][i], Bs[k][j]) — no register staging and
+// no shared-memory transposes.  Out-of-range B rows/columns are zero-filled:
+// the matching A entries are INF, so INF + 0 cannot lower any output.
+// ---------------------------------------------------------------------------
+struct Tile3Args {
+  void* C; int64_t ldc;          // output rows [0, m), cols [0, ncols)
+  const void* PT; int64_t ldpt;  // kdepth (padded to TB) x round_up(m, TB)
+  const void* B; int64_t ldb;    // kdepth x ncols (row panel)
+  int m, ncols, kdepth;
+  int skip_ti, skip_tj;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(NTH, 2) fw_tile3_kernel(Tile3Args a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* As = reinterpret_cast<T*>(smem_raw);          // [2][KC][TB]
+  T* Bs = As + 2 * KC * TB;                        // [2][KC][TB]
+  const int tj = blockIdx.x, ti = blockIdx.y;
+  if (ti == a.skip_ti || tj == a.skip_tj) return;
+  T* C = reinterpret_cast<T*>(a.C);
+  const T* PT = reinterpret_cast<const T*>(a.PT);
+  const T* B = reinterpret_cast<const T*>(a.B);
+  const T I = Tr<T>::inf();
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int i0 = ti * TB, j0 = tj * TB;
+  const bool fullB = (j0 + TB <= a.ncols);
+  const bool fullA = (i0 + TB <= a.m);
+  const int nch = (a.kdepth + KC - 1) / KC;
+
+  auto load_chunk = [&](int kc, int buf) {
+    const int k0 = kc * KC;
+    T* as = As + buf * KC * TB;
+    T* bs = Bs + buf * KC * TB;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = tid + NTH * q;
+      const int r = idx >> 5, c4 = idx & 31;
+      cp_async16(as + r * TB + c4 * 4, PT + (int64_t)(k0 + r) * a.ldpt + i0 + c4 * 4);
+      const int kr = k0 + r, col = j0 + c4 * 4;
+      const T* src = B + (int64_t)kr * a.ldb + col;
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(bs + r * TB + c4 * 4);
+      const int bytes = (kr < a.kdepth && (fullB || col < a.ncols)) ? 16 : 0;
+      if (bytes == 0) src = B;   // any valid address; zero-filled
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(bytes));
+    }
+    cp_async_commit();
+  };
+
+  load_chunk(0, 0);
+  T acc[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int row = i0 + (r < 4 ? ty * 4 + r : 64 + ty * 4 + (r - 4));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int col = j0 + (h == 0 ? tx * 4 : 64 + tx * 4);
+      Vec4<T> v{I, I, I, I};
+      if ((fullA || row < a.m) && (fullB || col < a.ncols)) v = ld4<T>(C + (int64_t)row * a.ldc + col);
+      acc[r][h * 4 + 0] = v.x; acc[r][h * 4 + 1] = v.y;
+      acc[r][h * 4 + 2] = v.z; acc[r][h * 4 + 3] = v.w;
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  for (int kc = 0; kc < nch; ++kc) {
+    const int buf = kc & 1;
+    if (kc + 1 < nch) load_chunk(kc + 1, buf ^ 1);
+    const T* as = As + buf * KC * TB;
+    const T* bs = Bs + buf * KC * TB;
+    if constexpr (!Tr<T>::kFloat) {
+#pragma unroll 4
+      for (int kk = 0; kk < KC; ++kk) {
+        Vec4<T> a0 = *reinterpret_cast<const Vec4<T>*>(as + kk * TB + ty * 4);
+        Vec4<T> a1 = *reinterpret_cast<const Vec4<T>*>(as + kk * TB + 64 + ty * 4);
+        Vec4<T> b0 = *reinterpret_cast<const Vec4<T>*>(bs + kk * TB + tx * 4);
+        Vec4<T> b1 = *reinterpret_cast<const Vec4<T>*>(bs + kk * TB + 64 + tx * 4);
+        T av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        T bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[r][c] = Tr<T>::relax(acc[r][c], av[r], bv[c]);
+      }
+    } else {
+#pragma unroll 2
+      for (int kk = 0; kk < KC; kk += 2) {
+        Vec4<T> a0 = *reinterpret_cast<const Vec4<T>*>(as + kk * TB + ty * 4);
+        Vec4<T> a1 = *reinterpret_cast<const Vec4<T>*>(as + kk * TB + 64 + ty * 4);
+        Vec4<T> b0 = *reinterpret_cast<const Vec4<T>*>(bs + kk * TB + tx * 4);
+        Vec4<T> b1 = *reinterpret_cast<const Vec4<T>*>(bs + kk * TB + 64 + tx * 4);
+        Vec4<T> a2 = *reinterpret_cast<const Vec4<T>*>(as + (kk + 1) * TB + ty * 4);
+        Vec4<T> a3 = *reinterpret_cast<const Vec4<T>*>(as + (kk + 1) * TB + 64 + ty * 4);
+        Vec4<T> b2 = *reinterpret_cast<const Vec4<T>*>(bs + (kk + 1) * TB + tx * 4);
+        Vec4<T> b3 = *reinterpret_cast<const Vec4<T>*>(bs + (kk + 1) * TB + 64 + tx * 4);
+        T av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        T bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        T aw[8] = {a2.x, a2.y, a2.z, a2.w, a3.x, a3.y, a3.z, a3.w};
+        T bw[8] = {b2.x, b2.y, b2.z, b2.w, b3.x, b3.y, b3.z, b3.w};
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            acc[r][c] = fminf(acc[r][c], fminf(__fadd_rn(av[r], bv[c]), __fadd_rn(aw[r], bw[c])));
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int row = i0 + (r < 4 ? ty * 4 + r : 64 + ty * 4 + (r - 4));
+    if (!(fullA || row < a.m)) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int col = j0 + (h == 0 ? tx * 4 : 64 + tx * 4);
+      if (!(fullB || col < a.ncols)) continue;
+      Vec4<T> v{acc[r][h * 4 + 0], acc[r][h * 4 + 1], acc[r][h * 4 + 2], acc[r][h * 4 + 3]};
+      st4<T>(C + (int64_t)row * a.ldc + col, v);
+    }
+  }
+}
+
+// PT[k][i] = D[i][K0 + k] for k < kb, i < m; INF for k in [kb, TB) or i in [m, mpad)
+template <typename T>
+__global__ void fw_transpose_panel_kernel(const T* D, int64_t ld, int64_t m, int64_t K0, int kb,
+                                          T* PT, int64_t ldpt, int64_t mpad) {
+  __shared__ T tile[32][33];
+  const int64_t i0 = blockIdx.x * 32;
+  const int k0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = i0 + r;
+    const int k = k0 + threadIdx.x;
+    tile[r][threadIdx.x] = (i < m && k < kb) ? D[i * ld + K0 + k] : Tr<T>::inf();
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int k = k0 + r;
+    const int64_t i = i0 + threadIdx.x;
+    if (i < mpad) PT[(int64_t)k * ldpt + i] = tile[threadIdx.x][r];
+  }
+}
+
 constexpr size_t kTileSmem = sizeof(int32_t) * (2 * KC * AST + 2 * KC * TB);
 
 template <typename T>
@@ -307,13 +456,42 @@ cudaError_t fw_rest(T* D, int64_t ld, int64_t m, int64_t ncols, int64_t K0, int 
   return launch_tile<T>(a, st);
 }
 
+template <typename T>
+cudaError_t fw_rest_pt(T* D, int64_t ld, int64_t m, int64_t ncols, int64_t K0, int kb, const T* P,
+                       int64_t ldp, int skip_ti, T* PT, int64_t ldpt, cudaStream_t st) {
+  if (m <= 0 || ncols <= 0) return cudaSuccess;
+  const int64_t mpad = (m + TB - 1) / TB * TB;
+  if (mpad > ldpt) return cudaErrorInvalidValue;
+  fw_transpose_panel_kernel<T><<<dim3((unsigned)(mpad / 32), TB / 32), dim3(32, 8), 0, st>>>(
+      D, ld, m, K0, kb, PT, ldpt, mpad);
+  static bool configured = false;
+  constexpr size_t smem = sizeof(T) * 4 * KC * TB;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fw_tile3_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  Tile3Args a;
+  a.C = D; a.ldc = ld;
+  a.PT = PT; a.ldpt = ldpt;
+  a.B = P; a.ldb = ldp;
+  a.m = (int)m; a.ncols = (int)ncols; a.kdepth = kb;
+  a.skip_ti = skip_ti; a.skip_tj = (int)(K0 / TB);
+  dim3 grid((unsigned)((ncols + TB - 1) / TB), (unsigned)(mpad / TB));
+  fw_tile3_kernel<T><<<grid, NTH, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 #define INST(T)                                                                                  \
   template cudaError_t fw_diag<T>(T*, int64_t, int, cudaStream_t);                               \
   template cudaError_t fw_row_panel<T>(T*, int64_t, int64_t, int, int64_t, cudaStream_t);        \
   template cudaError_t fw_col_panel<T>(T*, int64_t, int64_t, int64_t, int, const T*, int64_t,    \
                                        int, cudaStream_t);                                       \
   template cudaError_t fw_rest<T>(T*, int64_t, int64_t, int64_t, int64_t, int, const T*, int64_t, \
-                                  int, cudaStream_t);
+                                  int, cudaStream_t);                                            \
+  template cudaError_t fw_rest_pt<T>(T*, int64_t, int64_t, int64_t, int64_t, int, const T*,       \
+                                     int64_t, int, T*, int64_t, cudaStream_t);
 INST(int32_t)
 INST(float)
 #undef INST

@@ -12,6 +12,7 @@ struct DetectCounters {
   unsigned int maxrow;        // max |A_i|
   unsigned int overflow;      // list capacity exceeded
   unsigned int err;           // validation flag (add_node inputs)
+  unsigned long long open_total;   // open pairs after the shortlist certification
 };
 
 // ---------------- fw.cu ----------------
@@ -24,6 +25,10 @@ cudaError_t fw_col_panel(T* D, int64_t ld, int64_t m, int64_t K0, int kb, const 
 template <typename T>
 cudaError_t fw_rest(T* D, int64_t ld, int64_t m, int64_t ncols, int64_t K0, int kb, const T* P,
                     int64_t ldp, int skip_ti, cudaStream_t st);
+
+template <typename T>
+cudaError_t fw_rest_pt(T* D, int64_t ld, int64_t m, int64_t ncols, int64_t K0, int kb, const T* P,
+                       int64_t ldp, int skip_ti, T* PT, int64_t ldpt, cudaStream_t st);
 
 // ---------------- stream.cu ----------------
 // Row range [lo, hi) is global; D points at global row `row0` (local block).
@@ -63,7 +68,7 @@ cudaError_t addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xl
 template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
                    const T* c2, const T* r2, float tau, const T* WT, int64_t ldw, int reset,
-                   int64_t* rowoff, int* rowcnt, int* prow, int* pcol, int64_t lcap,
+                   int64_t* rowoff, int* rowcnt, int* prow, int* pcol, T* plb, int64_t lcap,
                    DetectCounters* ctr, int grid, cudaStream_t st);
 template <typename T>
 cudaError_t tombstone(T* D, int64_t ld, Rows r, int64_t n, int64_t k, T* WT, int64_t ldw,
@@ -78,14 +83,37 @@ template <typename T>
 cudaError_t set_edge(T* WT, int64_t ldw, int64_t u, int64_t v, T w, int directed, cudaStream_t st);
 
 // ---------------- sparse.cu ----------------
+constexpr int kSLK = 8;               // shortlist entries per lane
+constexpr int kSL = 32 * kSLK;        // shortlist entries per node
 template <typename T>
-cudaError_t sparse_round0(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
-                          const int* prow, const int* pcol, int64_t npairs, cudaStream_t st);
+cudaError_t shortlist_build(const T* WT, int64_t ldw, int64_t n, const int* rows, int64_t r0,
+                            int64_t r1, int* SLid, T* SLw, T* wnext, cudaStream_t st);
 template <typename T>
-cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
-                         const int* prow, const int* pcol, int64_t npairs, const int64_t* rowoff,
-                         const int* rowcnt, const int* chg_in, int* chg_out, int* any,
-                         cudaStream_t st);
+cudaError_t shortlist_add_bound(T* wnext, const T* out_w, int64_t n, cudaStream_t st);
+template <typename T>
+cudaError_t shortlist_set_edge(int* SLid, T* SLw, T* wnext, int64_t u, int64_t v, T w,
+                               int directed, cudaStream_t st);
+template <typename T>
+cudaError_t shortlist_remove(int* SLid, T* SLw, T* wnext, int64_t n, int64_t k, int64_t last,
+                             cudaStream_t st);
+template <typename T>
+cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const T* SLw,
+                         const T* wnext, const int* prow, const int* pcol, const T* plb,
+                         int64_t npairs, unsigned char* out, int classify, cudaStream_t st);
+template <typename T>
+cudaError_t sparse_compact(Rows r, const int64_t* rowoff, const int* rowcnt, const int* pcol,
+                           const T* plb, const unsigned char* popen, int* ocol, int* ocnt,
+                           int* gprow, int* gpcol, T* glb, unsigned char* gfull, int64_t ocap,
+                           DetectCounters* ctr, cudaStream_t st);
+template <typename T>
+cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
+                        const int* gprow, const int* gpcol, const T* glb, const unsigned char* gfull,
+                        int64_t nopen, cudaStream_t st);
+template <typename T>
+cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw,
+                         const int* gprow, const int* gpcol, const T* glb, int64_t nopen,
+                         const int64_t* rowoff, const int* ocnt, const int* ocol, const int* chg_in,
+                         int* chg_out, int* any, cudaStream_t st);
 
 // ---------------- query.cu ----------------
 constexpr int kQueryCap = 4096;

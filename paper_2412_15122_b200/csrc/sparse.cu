@@ -3,16 +3,26 @@
 // The paper recomputes every affected source with Dijkstra ("If the Cost is
 // small, we use Dijkstra's algorithm to calculate a node's distance to other
 // nodes in the new graph").  On the GPU the work is re-expressed at
-// pair level: only the listed pairs (i, j) in A are recomputed, each from
-// the Bellman equation of its last hop,
-//     D'[i][j] = min_m D'[i][m] + W'[m][j],
-// on D0 (affected entries reset to W'[i][j], unaffected entries exact by
-// Theorem 4).  Round 0 scans all m (one streaming dot-min of row i of D with
-// row j of WT per pair); rounds r >= 1 re-relax each pair only over the
-// affected m of its own row (A_i), for rows that changed in the previous
-// round, until no entry changes.  A fixpoint of these upper bounds is the
-// exact distance; rows read only their own D row and the
-// read-only WT, so rows never race and no grid-wide sync is needed.
+// pair level: only the listed pairs (i, j) of the need_update_list are
+// recomputed, from the Bellman equation of their last hop
+//     D'[i][j] = min_m D'[i][m] + W'[m][j]                         (*)
+// on D0 (listed entries reset to W'[i][j]; unlisted entries are exact by
+// Theorem 4 / Corollary 3).  Three facts make it cheap:
+//  (a) lower bound: distances never decrease under a removal / increase, so
+//      lb = D_old[i][j] <= D'[i][j]; an upper bound that reaches lb is final.
+//      (Most listed pairs are ties — another shortest path avoids the
+//      removed element — and are certified this way.)
+//  (b) shortlist: per node j the library keeps SL(j), a set of in-edges
+//      (m, W[m][j]) and a bound wnext(j) <= W[m][j] for every in-edge NOT in
+//      SL(j).  Since D >= 0, if min over SL(j) of D[i][m] + W[m][j] is
+//      <= wnext(j), it equals the min over all m of (*) for the current D.
+//  (c) only pairs neither certified by (a) nor exact by (b) need the full
+//      O(n) scan of row i of D against row j of WT.
+// Affected m can still improve after a pair was evaluated (chains in the
+// affected set), so open pairs are re-relaxed over the open entries of their
+// own row until no entry changes.  A fixpoint of these upper bounds is the
+// exact distance.  Rows read only their own D row and the
+// read-only WT / shortlists, so rows never race and no grid sync is needed.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -20,41 +30,296 @@ namespace apsp {
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// warp per pair: est = min_m D[i][m] + WT[j][m] over all m < n
+// ---------------------------------------------------------------------------
+// shortlists: lane-local top-kSLK in-edges of node j (kSL = 32 * kSLK entries)
+// ---------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(256) k_sparse_round0(T* D, int64_t ld, int64_t row0,
-                                                       const T* __restrict__ WT, int64_t ldw,
-                                                       int64_t n, const int* __restrict__ prow,
-                                                       const int* __restrict__ pcol,
-                                                       int64_t npairs) {
+__global__ void __launch_bounds__(256) k_shortlist_build(const T* __restrict__ WT, int64_t ldw,
+                                                         int64_t n, const int* rows, int64_t r0,
+                                                         int64_t r1, int* SLid, T* SLw, T* wnext) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t n4 = (n + 3) / 4;
   const T I = Tr<T>::inf();
+  for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < r1 - r0;
+       w += nw) {
+    const int64_t j = rows ? rows[r0 + w] : r0 + w;
+    if (j < 0 || j >= n) continue;
+    const T* row = WT + j * ldw;
+    T bw[kSLK];
+    int bi[kSLK];
+#pragma unroll
+    for (int q = 0; q < kSLK; ++q) { bw[q] = I; bi[q] = -1; }
+    T rej = I;   // smallest weight this lane did not keep
+    for (int64_t m = lane; m < n; m += 32) {
+      T x = row[m];
+      if (m == j || !Tr<T>::fin(x)) continue;
+      if (x < bw[kSLK - 1]) {
+        rej = Tr<T>::mn(rej, bw[kSLK - 1]);   // the evicted maximum becomes a rejected value
+        // sorted insertion (ascending)
+        T cw = x;
+        int ci = (int)m;
+#pragma unroll
+        for (int q = 0; q < kSLK; ++q) {
+          if (cw < bw[q]) {
+            T tw = bw[q]; int ti = bi[q];
+            bw[q] = cw; bi[q] = ci;
+            cw = tw; ci = ti;
+          }
+        }
+      } else {
+        rej = Tr<T>::mn(rej, x);
+      }
+    }
+    int* oid = SLid + j * kSL;
+    T* ow = SLw + j * kSL;
+#pragma unroll
+    for (int q = 0; q < kSLK; ++q) {
+      oid[q * 32 + lane] = bi[q];
+      ow[q * 32 + lane] = bw[q];
+    }
+    rej = warp_min<T>(rej);
+    if (lane == 0) wnext[j] = rej;
+  }
+}
+
+template <typename T>
+cudaError_t shortlist_build(const T* WT, int64_t ldw, int64_t n, const int* rows, int64_t r0,
+                            int64_t r1, int* SLid, T* SLw, T* wnext, cudaStream_t st) {
+  if (r1 <= r0) return cudaSuccess;
+  int grid = (int)std::min<int64_t>(cdiv(r1 - r0, 8), (int64_t)num_sms() * 8);
+  k_shortlist_build<T><<<grid, 256, 0, st>>>(WT, ldw, n, rows, r0, r1, SLid, SLw, wnext);
+  return cudaGetLastError();
+}
+
+// A new node x adds in-edge x -> j (weight out_w[j]) to every j; it is not in
+// SL(j), so wnext(j) must cover it.
+template <typename T>
+__global__ void k_shortlist_add_edge_bound(T* wnext, const T* out_w, int64_t n) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    wnext[j] = Tr<T>::mn(wnext[j], out_w[j]);
+}
+template <typename T>
+cudaError_t shortlist_add_bound(T* wnext, const T* out_w, int64_t n, cudaStream_t st) {
+  int grid = (int)std::min<int64_t>(cdiv(n, 256), 4 * num_sms());
+  k_shortlist_add_edge_bound<T><<<grid, 256, 0, st>>>(wnext, out_w, n);
+  return cudaGetLastError();
+}
+
+// Edge u -> v now has weight w: refresh its entry in SL(v) if present,
+// otherwise make wnext(v) cover it (one warp).
+template <typename T>
+__global__ void k_shortlist_set_edge(int* SLid, T* SLw, T* wnext, int64_t u, int64_t v, T w) {
+  const int lane = threadIdx.x & 31;
+  bool found = false;
+#pragma unroll
+  for (int q = 0; q < kSLK; ++q) {
+    const int64_t e = v * kSL + q * 32 + lane;
+    if (SLid[e] == (int)u) { SLw[e] = w; found = true; }
+  }
+  found = __any_sync(0xffffffffu, found);
+  if (lane == 0 && !found) wnext[v] = Tr<T>::mn(wnext[v], w);
+}
+template <typename T>
+cudaError_t shortlist_set_edge(int* SLid, T* SLw, T* wnext, int64_t u, int64_t v, T w,
+                               int directed, cudaStream_t st) {
+  k_shortlist_set_edge<T><<<1, 32, 0, st>>>(SLid, SLw, wnext, u, v, w);
+  if (!directed) k_shortlist_set_edge<T><<<1, 32, 0, st>>>(SLid, SLw, wnext, v, u, w);
+  return cudaGetLastError();
+}
+
+// Removal of k with node `last` moving into slot k: entries naming k die
+// (weight INF), entries naming `last` are renamed k, row k takes row last.
+template <typename T>
+__global__ void k_shortlist_remove(int* SLid, T* SLw, T* wnext, int64_t n, int k, int last) {
+  const int64_t tot = n * kSL;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int id = SLid[e];
+    if (id == k) { SLid[e] = -1; SLw[e] = Tr<T>::inf(); }
+    else if (id == last && last != k) SLid[e] = k;
+  }
+}
+template <typename T>
+__global__ void k_shortlist_move_row(int* SLid, T* SLw, T* wnext, int k, int last) {
+  const int t = threadIdx.x;
+  for (int q = t; q < kSL; q += blockDim.x) {
+    int id = SLid[(int64_t)last * kSL + q];
+    SLid[(int64_t)k * kSL + q] = (id == k) ? -1 : id;   // (renamed already)
+    SLw[(int64_t)k * kSL + q] = (id == k) ? Tr<T>::inf() : SLw[(int64_t)last * kSL + q];
+  }
+  if (t == 0) wnext[k] = wnext[last];
+}
+template <typename T>
+cudaError_t shortlist_remove(int* SLid, T* SLw, T* wnext, int64_t n, int64_t k, int64_t last,
+                             cudaStream_t st) {
+  int grid = (int)std::min<int64_t>(cdiv(n * kSL, 256), 8 * num_sms());
+  k_shortlist_remove<T><<<grid, 256, 0, st>>>(SLid, SLw, wnext, n, (int)k, (int)last);
+  if (k != last) k_shortlist_move_row<T><<<1, 256, 0, st>>>(SLid, SLw, wnext, (int)k, (int)last);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// phase A / A2: shortlist evaluation of a list of pairs
+//   classify = 0 (phase A, all listed pairs):   out = 0 final (reached lb), 1 open
+//   classify = 1 (phase A2, open pairs, after A): out = 0 final,
+//            1 exact for the current D (est <= wnext), 2 needs the full scan.
+// Phase A2 must run after phase A has finished: the certified (final) values
+// of other pairs of the row are then visible, so a class-1 value is the
+// exact min of (*) over every m whose value can no longer change.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t row0,
+                                                      const int* __restrict__ SLid,
+                                                      const T* __restrict__ SLw,
+                                                      const T* __restrict__ wnext,
+                                                      const int* __restrict__ prow,
+                                                      const int* __restrict__ pcol,
+                                                      const T* __restrict__ plb, int64_t npairs,
+                                                      unsigned char* out, int classify) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t p = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); p < npairs;
        p += nw) {
     const int64_t i = prow[p], j = pcol[p];
     T* Drow = D + (i - row0) * ld;
+    const int* sid = SLid + j * kSL;
+    const T* sw = SLw + j * kSL;
+    T acc = Tr<T>::inf();
+#pragma unroll
+    for (int q = 0; q < kSLK; ++q) {
+      const int m = sid[q * 32 + lane];
+      const T w = sw[q * 32 + lane];
+      if (m >= 0) acc = Tr<T>::relax(acc, *(volatile T*)(Drow + m), w);
+    }
+    acc = warp_min<T>(acc);
+    if (lane == 0) {
+      const T lb = plb[p];
+      const T cur = *(volatile T*)(Drow + j);
+      const T v = Tr<T>::mn(acc, cur);
+      if (v < cur) Drow[j] = v;
+      unsigned char st;
+      if (v <= lb) st = 0;
+      else if (!classify || acc <= wnext[j]) st = 1;
+      else st = 2;
+      out[p] = st;
+    }
+  }
+}
+template <typename T>
+cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const T* SLw,
+                         const T* wnext, const int* prow, const int* pcol, const T* plb,
+                         int64_t npairs, unsigned char* out, int classify, cudaStream_t st) {
+  if (npairs <= 0) return cudaSuccess;
+  int grid = (int)std::min<int64_t>(cdiv(npairs, 8), (int64_t)num_sms() * 16);
+  k_sparse_short<T><<<grid, 256, 0, st>>>(D, ld, row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
+                                          out, classify);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// compaction: per affected row, the open entries (status != 0) in list order
+// -> ocol[rowoff[i] ...], ocnt[i]; and a global list of open pairs.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) k_sparse_compact(
+    Rows r, const int64_t* __restrict__ rowoff, const int* __restrict__ rowcnt,
+    const int* __restrict__ pcol, const T* __restrict__ plb, const unsigned char* __restrict__ popen,
+    int* ocol, int* ocnt, int* gprow, int* gpcol, T* glb, unsigned char* gfull, int64_t ocap,
+    DetectCounters* ctr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = r.lo + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < r.hi;
+       i += nw) {
+    const int cnt = rowcnt[i];
+    if (cnt == 0) continue;
+    const int64_t off = rowoff[i];
+    int total = 0;
+    for (int t0 = 0; t0 < cnt; t0 += 32) {
+      const int t = t0 + lane;
+      const bool f = t < cnt && popen[off + t] != 0;
+      const unsigned b = __ballot_sync(0xffffffffu, f);
+      if (f) ocol[off + total + __popc(b & ((1u << lane) - 1))] = pcol[off + t];
+      total += __popc(b);
+    }
+    if (lane == 0) ocnt[i] = total;
+    if (total == 0) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&ctr->open_total, (unsigned long long)total);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if ((int64_t)base + total > ocap) {
+      if (lane == 0) atomicOr(&ctr->overflow, 2u);
+      continue;
+    }
+    int pos = 0;
+    for (int t0 = 0; t0 < cnt; t0 += 32) {
+      const int t = t0 + lane;
+      const unsigned char s = t < cnt ? popen[off + t] : 0;
+      const bool f = s != 0;
+      const unsigned b = __ballot_sync(0xffffffffu, f);
+      if (f) {
+        const int64_t q = (int64_t)base + pos + __popc(b & ((1u << lane) - 1));
+        gprow[q] = (int)i;
+        gpcol[q] = pcol[off + t];
+        glb[q] = plb[off + t];
+        gfull[q] = 1;
+      }
+      pos += __popc(b);
+    }
+  }
+}
+template <typename T>
+cudaError_t sparse_compact(Rows r, const int64_t* rowoff, const int* rowcnt, const int* pcol,
+                           const T* plb, const unsigned char* popen, int* ocol, int* ocnt,
+                           int* gprow, int* gpcol, T* glb, unsigned char* gfull, int64_t ocap,
+                           DetectCounters* ctr, cudaStream_t st) {
+  if (r.hi <= r.lo) return cudaSuccess;
+  int grid = (int)std::min<int64_t>(cdiv(r.hi - r.lo, 8), (int64_t)num_sms() * 8);
+  k_sparse_compact<T><<<grid, 256, 0, st>>>(r, rowoff, rowcnt, pcol, plb, popen, ocol, ocnt, gprow,
+                                            gpcol, glb, gfull, ocap, ctr);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// phase B: full scan (*) for open pairs marked 2, early exit at the lower bound
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) k_sparse_full(T* D, int64_t ld, int64_t row0,
+                                                     const T* __restrict__ WT, int64_t ldw,
+                                                     int64_t n, const int* __restrict__ gprow,
+                                                     const int* __restrict__ gpcol,
+                                                     const T* __restrict__ glb,
+                                                     const unsigned char* __restrict__ gfull,
+                                                     int64_t nopen) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t n4 = (n + 3) / 4;
+  const T I = Tr<T>::inf();
+  for (int64_t p = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); p < nopen;
+       p += nw) {
+    if (gfull[p] != 2) continue;
+    const int64_t i = gprow[p], j = gpcol[p];
+    const T lb = glb[p];
+    T* Drow = D + (i - row0) * ld;
     const T* Wrow = WT + j * ldw;
     T acc = I;
-    int64_t q = lane;
-    for (; q + 32 < n4; q += 64) {
-      // two vectors per lane in flight; other warps may lower entries of this
-      // row concurrently — any value read is a valid upper bound
-      Vec4<T> d0 = ld4_cg<T>(Drow + 4 * q), d1 = ld4_cg<T>(Drow + 4 * (q + 32));
-      Vec4<T> w0 = ld4<T>(Wrow + 4 * q), w1 = ld4<T>(Wrow + 4 * (q + 32));
-      d1 = mask_tail<T>(d1, 4 * (q + 32), n);
-      w1 = mask_tail<T>(w1, 4 * (q + 32), n);
+    // warp-uniform trip count: the early-exit test below shuffles across lanes
+    for (int64_t base = 0, iter = 1; base < n4; base += 64, ++iter) {
+      const int64_t q0 = base + lane, q1 = base + 32 + lane;
+      Vec4<T> d0{I, I, I, I}, w0{I, I, I, I}, d1{I, I, I, I}, w1{I, I, I, I};
+      if (q0 < n4) {
+        d0 = mask_tail<T>(ld4_cg<T>(Drow + 4 * q0), 4 * q0, n);
+        w0 = mask_tail<T>(ld4<T>(Wrow + 4 * q0), 4 * q0, n);
+      }
+      if (q1 < n4) {
+        d1 = mask_tail<T>(ld4_cg<T>(Drow + 4 * q1), 4 * q1, n);
+        w1 = mask_tail<T>(ld4<T>(Wrow + 4 * q1), 4 * q1, n);
+      }
       acc = Tr<T>::relax(acc, d0.x, w0.x); acc = Tr<T>::relax(acc, d0.y, w0.y);
       acc = Tr<T>::relax(acc, d0.z, w0.z); acc = Tr<T>::relax(acc, d0.w, w0.w);
       acc = Tr<T>::relax(acc, d1.x, w1.x); acc = Tr<T>::relax(acc, d1.y, w1.y);
       acc = Tr<T>::relax(acc, d1.z, w1.z); acc = Tr<T>::relax(acc, d1.w, w1.w);
-    }
-    for (; q < n4; q += 32) {
-      Vec4<T> d0 = mask_tail<T>(ld4_cg<T>(Drow + 4 * q), 4 * q, n);
-      Vec4<T> w0 = mask_tail<T>(ld4<T>(Wrow + 4 * q), 4 * q, n);
-      acc = Tr<T>::relax(acc, d0.x, w0.x); acc = Tr<T>::relax(acc, d0.y, w0.y);
-      acc = Tr<T>::relax(acc, d0.z, w0.z); acc = Tr<T>::relax(acc, d0.w, w0.w);
+      if ((iter & 7) == 0 && warp_min<T>(acc) <= lb) break;   // reached the lower bound: exact
     }
     acc = warp_min<T>(acc);
     if (lane == 0) {
@@ -63,71 +328,86 @@ __global__ void __launch_bounds__(256) k_sparse_round0(T* D, int64_t ld, int64_t
     }
   }
 }
-
 template <typename T>
-cudaError_t sparse_round0(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
-                          const int* prow, const int* pcol, int64_t npairs, cudaStream_t st) {
-  if (npairs <= 0) return cudaSuccess;
-  int grid = (int)std::min<int64_t>(cdiv(npairs, 8), (int64_t)num_sms() * 8);
-  k_sparse_round0<T><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, n, prow, pcol, npairs);
+cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
+                        const int* gprow, const int* gpcol, const T* glb, const unsigned char* gfull,
+                        int64_t nopen, cudaStream_t st) {
+  if (nopen <= 0) return cudaSuccess;
+  int grid = (int)std::min<int64_t>(cdiv(nopen, 8), (int64_t)num_sms() * 8);
+  k_sparse_full<T><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, n, gprow, gpcol, glb, gfull, nopen);
   return cudaGetLastError();
 }
 
-// warp per pair of a changed row: est = min over m in A_i of D[i][m] + WT[j][m]
+// ---------------------------------------------------------------------------
+// rounds: open pair of a changed row, min over the open entries m of its row
+// ---------------------------------------------------------------------------
 template <typename T>
 __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t row0,
                                                       const T* __restrict__ WT, int64_t ldw,
-                                                      const int* __restrict__ prow,
-                                                      const int* __restrict__ pcol, int64_t npairs,
+                                                      const int* __restrict__ gprow,
+                                                      const int* __restrict__ gpcol,
+                                                      const T* __restrict__ glb, int64_t nopen,
                                                       const int64_t* __restrict__ rowoff,
-                                                      const int* __restrict__ rowcnt,
+                                                      const int* __restrict__ ocnt,
+                                                      const int* __restrict__ ocol,
                                                       const int* chg_in, int* chg_out, int* any) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t p = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); p < npairs;
+  for (int64_t p = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); p < nopen;
        p += nw) {
-    const int64_t i = prow[p];
-    const int cnt = rowcnt[i];
-    if (cnt <= 1 || !chg_in[i]) continue;      // a lone affected target is exact after round 0
-    const int64_t j = pcol[p];
-    const int64_t off = rowoff[i];
+    const int64_t i = gprow[p];
+    const int cnt = ocnt[i];
+    if (cnt <= 1 || !chg_in[i]) continue;   // a lone open entry cannot be improved by another
+    const int64_t j = gpcol[p];
     T* Drow = D + (i - row0) * ld;
+    T cur = Tr<T>::inf();
+    if (lane == 0) cur = *(volatile T*)(Drow + j);
+    cur = __shfl_sync(0xffffffffu, cur, 0);  // one value for the whole warp (others may write)
+    if (cur <= glb[p]) continue;             // already at its lower bound: final
+    const int64_t off = rowoff[i];
     const T* Wrow = WT + j * ldw;
     T acc = Tr<T>::inf();
     for (int t = lane; t < cnt; t += 32) {
-      const int64_t m = pcol[off + t];
+      const int64_t m = ocol[off + t];
       acc = Tr<T>::relax(acc, *(volatile T*)(Drow + m), Wrow[m]);
     }
     acc = warp_min<T>(acc);
-    if (lane == 0) {
-      T old = Drow[j];
-      if (acc < old) {
-        Drow[j] = acc;
-        chg_out[i] = 1;
-        *any = 1;
-      }
+    if (lane == 0 && acc < cur) {
+      Drow[j] = acc;
+      chg_out[i] = 1;
+      *any = 1;
     }
   }
 }
-
 template <typename T>
-cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
-                         const int* prow, const int* pcol, int64_t npairs, const int64_t* rowoff,
-                         const int* rowcnt, const int* chg_in, int* chg_out, int* any,
-                         cudaStream_t st) {
-  (void)n;
-  if (npairs <= 0) return cudaSuccess;
-  int grid = (int)std::min<int64_t>(cdiv(npairs, 8), (int64_t)num_sms() * 8);
-  k_sparse_round<T><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, prow, pcol, npairs, rowoff, rowcnt,
-                                          chg_in, chg_out, any);
+cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw,
+                         const int* gprow, const int* gpcol, const T* glb, int64_t nopen,
+                         const int64_t* rowoff, const int* ocnt, const int* ocol, const int* chg_in,
+                         int* chg_out, int* any, cudaStream_t st) {
+  if (nopen <= 0) return cudaSuccess;
+  int grid = (int)std::min<int64_t>(cdiv(nopen, 8), (int64_t)num_sms() * 8);
+  k_sparse_round<T><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff,
+                                          ocnt, ocol, chg_in, chg_out, any);
   return cudaGetLastError();
 }
 
-#define INST(T)                                                                                  \
-  template cudaError_t sparse_round0<T>(T*, int64_t, int64_t, const T*, int64_t, int64_t,        \
-                                        const int*, const int*, int64_t, cudaStream_t);          \
-  template cudaError_t sparse_round<T>(T*, int64_t, int64_t, const T*, int64_t, int64_t,         \
-                                       const int*, const int*, int64_t, const int64_t*,          \
+#define INST(T)                                                                                   \
+  template cudaError_t shortlist_build<T>(const T*, int64_t, int64_t, const int*, int64_t, int64_t, \
+                                          int*, T*, T*, cudaStream_t);                            \
+  template cudaError_t shortlist_add_bound<T>(T*, const T*, int64_t, cudaStream_t);                \
+  template cudaError_t shortlist_set_edge<T>(int*, T*, T*, int64_t, int64_t, T, int, cudaStream_t); \
+  template cudaError_t shortlist_remove<T>(int*, T*, T*, int64_t, int64_t, int64_t, cudaStream_t); \
+  template cudaError_t sparse_short<T>(T*, int64_t, int64_t, const int*, const T*, const T*,       \
+                                       const int*, const int*, const T*, int64_t, unsigned char*,  \
+                                       int, cudaStream_t);                                        \
+  template cudaError_t sparse_compact<T>(Rows, const int64_t*, const int*, const int*, const T*,   \
+                                         const unsigned char*, int*, int*, int*, int*, T*,         \
+                                         unsigned char*, int64_t, DetectCounters*, cudaStream_t);  \
+  template cudaError_t sparse_full<T>(T*, int64_t, int64_t, const T*, int64_t, int64_t,            \
+                                      const int*, const int*, const T*, const unsigned char*,      \
+                                      int64_t, cudaStream_t);                                     \
+  template cudaError_t sparse_round<T>(T*, int64_t, int64_t, const T*, int64_t, const int*,        \
+                                       const int*, const T*, int64_t, const int64_t*, const int*,  \
                                        const int*, const int*, int*, int*, cudaStream_t);
 INST(int32_t)
 INST(float)

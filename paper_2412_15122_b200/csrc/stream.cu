@@ -184,11 +184,12 @@ struct Tiling {
   int64_t slab;     // rows per slab
   int64_t warps;
 };
-static Tiling make_tiling(int64_t n, int64_t rows, int max_slabs) {
+static Tiling make_tiling(int64_t n, int64_t rows, int max_slabs, int chunk_vec = CHUNK_VEC,
+                          int warps_per_sm = 32) {
   Tiling t;
   t.n4 = cdiv(n, 4);
-  t.nchunk = (int)cdiv(t.n4, CHUNK_VEC);
-  int64_t target = (int64_t)num_sms() * 32;  // ~32 resident warps per SM
+  t.nchunk = (int)cdiv(t.n4, chunk_vec);
+  int64_t target = (int64_t)num_sms() * warps_per_sm;
   int64_t ns = std::max<int64_t>(1, target / t.nchunk);
   ns = std::min<int64_t>(ns, std::max<int64_t>(1, rows));
   ns = std::min<int64_t>(ns, max_slabs);
@@ -198,13 +199,24 @@ static Tiling make_tiling(int64_t n, int64_t rows, int max_slabs) {
   return t;
 }
 
+// Each warp owns a column chunk of P1_VEC vectors per row (lane: P1_V of
+// them) and a slab of rows.  Column partials (new row) stay in registers.
+// Row partials (new column) go to shared memory, one 32-row batch at a time:
+// lane l writes its partial of row r to rp[r][l]; after the batch lane l
+// reduces row l (stride 33: conflict-free).  No per-row shuffle chain, so
+// the loads of consecutive rows stay in flight.
+constexpr int P1_V = 4;
+constexpr int P1_VEC = 32 * P1_V;   // 512 columns per chunk
 template <typename T>
-__global__ void __launch_bounds__(256) k_addnode_pass1(const T* __restrict__ D, int64_t ld, Rows r,
-                                                       int64_t n, Tiling tl, const T* __restrict__ ow,
-                                                       const T* __restrict__ iw, T* rowpart,
-                                                       T* colpart, int64_t part_ld) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+__global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ D, int64_t ld, Rows r,
+                                                          int64_t n, Tiling tl,
+                                                          const T* __restrict__ ow,
+                                                          const T* __restrict__ iw, T* rowpart,
+                                                          T* colpart, int64_t part_ld) {
+  __shared__ T rp_all[8][32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T (*rp)[33] = rp_all[warp];
+  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
   if (gw >= tl.warps) return;
   const int chunk = (int)(gw % tl.nchunk);
   const int slab = (int)(gw / tl.nchunk);
@@ -212,39 +224,57 @@ __global__ void __launch_bounds__(256) k_addnode_pass1(const T* __restrict__ D, 
   const int64_t i_hi = min(r.hi, i_lo + tl.slab);
   const T I = Tr<T>::inf();
 
-  int64_t qv[VPL];
-  Vec4<T> inw[VPL], colp[VPL];
+  int64_t qv[P1_V];
+  Vec4<T> inw[P1_V], colp[P1_V];
 #pragma unroll
-  for (int v = 0; v < VPL; ++v) {
-    qv[v] = (int64_t)chunk * CHUNK_VEC + v * 32 + lane;
+  for (int v = 0; v < P1_V; ++v) {
+    qv[v] = (int64_t)chunk * P1_VEC + v * 32 + lane;
     inw[v] = qv[v] < tl.n4 ? ld4<T>(iw + 4 * qv[v]) : Vec4<T>{I, I, I, I};
     colp[v] = Vec4<T>{I, I, I, I};
   }
-  for (int64_t i = i_lo; i < i_hi; ++i) {
-    const T* row = D + (i - r.row0) * ld;
-    Vec4<T> d[VPL];
+  for (int64_t b0 = i_lo; b0 < i_hi; b0 += 32) {
+    const int nb = (int)min((int64_t)32, i_hi - b0);
+    for (int rr = 0; rr < nb; rr += 2) {
+      const bool two = rr + 1 < nb;
+      const int64_t i = b0 + rr;
+      const T* row0 = D + (i - r.row0) * ld;
+      const T* row1 = row0 + ld;
+      Vec4<T> d0[P1_V], d1[P1_V];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v)
-      d[v] = qv[v] < tl.n4 ? mask_tail<T>(ld4_stream<T>(row + 4 * qv[v]), 4 * qv[v], n)
-                           : Vec4<T>{I, I, I, I};
-    const T oi = ow[i];
-    T rp = I;
+      for (int v = 0; v < P1_V; ++v) {
+        d0[v] = qv[v] < tl.n4 ? mask_tail<T>(ld4_stream<T>(row0 + 4 * qv[v]), 4 * qv[v], n)
+                              : Vec4<T>{I, I, I, I};
+        d1[v] = (two && qv[v] < tl.n4) ? mask_tail<T>(ld4_stream<T>(row1 + 4 * qv[v]), 4 * qv[v], n)
+                                       : Vec4<T>{I, I, I, I};
+      }
+      const T o0 = ow[i];
+      const T o1 = two ? ow[i + 1] : I;
+      T p0 = I, p1 = I;
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      rp = Tr<T>::relax(rp, d[v].x, inw[v].x);
-      rp = Tr<T>::relax(rp, d[v].y, inw[v].y);
-      rp = Tr<T>::relax(rp, d[v].z, inw[v].z);
-      rp = Tr<T>::relax(rp, d[v].w, inw[v].w);
-      colp[v].x = Tr<T>::relax(colp[v].x, oi, d[v].x);
-      colp[v].y = Tr<T>::relax(colp[v].y, oi, d[v].y);
-      colp[v].z = Tr<T>::relax(colp[v].z, oi, d[v].z);
-      colp[v].w = Tr<T>::relax(colp[v].w, oi, d[v].w);
+      for (int v = 0; v < P1_V; ++v) {
+        p0 = Tr<T>::relax(p0, d0[v].x, inw[v].x); p0 = Tr<T>::relax(p0, d0[v].y, inw[v].y);
+        p0 = Tr<T>::relax(p0, d0[v].z, inw[v].z); p0 = Tr<T>::relax(p0, d0[v].w, inw[v].w);
+        p1 = Tr<T>::relax(p1, d1[v].x, inw[v].x); p1 = Tr<T>::relax(p1, d1[v].y, inw[v].y);
+        p1 = Tr<T>::relax(p1, d1[v].z, inw[v].z); p1 = Tr<T>::relax(p1, d1[v].w, inw[v].w);
+        colp[v].x = Tr<T>::relax(Tr<T>::relax(colp[v].x, o0, d0[v].x), o1, d1[v].x);
+        colp[v].y = Tr<T>::relax(Tr<T>::relax(colp[v].y, o0, d0[v].y), o1, d1[v].y);
+        colp[v].z = Tr<T>::relax(Tr<T>::relax(colp[v].z, o0, d0[v].z), o1, d1[v].z);
+        colp[v].w = Tr<T>::relax(Tr<T>::relax(colp[v].w, o0, d0[v].w), o1, d1[v].w);
+      }
+      rp[rr][lane] = p0;
+      if (two) rp[rr + 1][lane] = p1;
     }
-    rp = warp_min<T>(rp);
-    if (lane == 0) rowpart[(int64_t)chunk * part_ld + i] = rp;
+    __syncwarp();
+    if (lane < nb) {
+      T m = rp[lane][0];
+#pragma unroll 8
+      for (int t = 1; t < 32; ++t) m = Tr<T>::mn(m, rp[lane][t]);
+      rowpart[(int64_t)chunk * part_ld + b0 + lane] = m;
+    }
+    __syncwarp();
   }
 #pragma unroll
-  for (int v = 0; v < VPL; ++v)
+  for (int v = 0; v < P1_V; ++v)
     if (qv[v] < tl.n4) st4<T>(colpart + (int64_t)slab * part_ld + 4 * qv[v], colp[v]);
 }
 
@@ -252,7 +282,7 @@ template <typename T>
 cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow, const T* iw,
                           T* rowpart, T* colpart, int64_t part_ld, int* nchunk_out, int* nslab_out,
                           int max_slabs, cudaStream_t st) {
-  Tiling tl = make_tiling(n, r.hi - r.lo, max_slabs);
+  Tiling tl = make_tiling(n, r.hi - r.lo, max_slabs, P1_VEC, 48);
   *nchunk_out = tl.nchunk;
   *nslab_out = tl.nslab;
   if (r.hi <= r.lo) {
@@ -395,7 +425,7 @@ struct DetectArgs {
   T* D; int64_t ld; Rows r; int64_t n; int64_t skip;
   const T* c1; const T* r1; const T* c2; const T* r2; float tau;
   const T* WT; int64_t ldw; int reset;
-  int64_t* rowoff; int* rowcnt; int* prow; int* pcol; int64_t lcap;
+  int64_t* rowoff; int* rowcnt; int* prow; int* pcol; T* plb; int64_t lcap;
   DetectCounters* ctr;
 };
 
@@ -435,22 +465,26 @@ __global__ void __launch_bounds__(DT_THREADS) k_detect(DetectArgs<T> a) {
     if (!Tr<T>::fin(c1) && !Tr<T>::fin(c2)) continue;   // no pair of this row can be tight
     T* Drow = a.D + (i - a.r.row0) * a.ld;
     bool any = false;
-    for (int64_t base = 0; base < n4; base += 2 * DT_THREADS) {
-      const int64_t q0 = base + tid, q1 = base + DT_THREADS + tid;
-      Vec4<T> d0{I, I, I, I}, d1{I, I, I, I}, ra0{I, I, I, I}, ra1{I, I, I, I}, rb0, rb1;
-      if (q0 < n4) { d0 = ld4_stream<T>(Drow + 4 * q0); ra0 = ld4<T>(a.r1 + 4 * q0); }
-      if (q1 < n4) { d1 = ld4_stream<T>(Drow + 4 * q1); ra1 = ld4<T>(a.r1 + 4 * q1); }
-      if (TWO) {
-        rb0 = q0 < n4 ? ld4<T>(a.r2 + 4 * q0) : Vec4<T>{I, I, I, I};
-        rb1 = q1 < n4 ? ld4<T>(a.r2 + 4 * q1) : Vec4<T>{I, I, I, I};
+    constexpr int DU = 4;   // vectors per thread in flight
+    for (int64_t base = 0; base < n4; base += DU * DT_THREADS) {
+      Vec4<T> d[DU], ra[DU], rb[DU];
+#pragma unroll
+      for (int h = 0; h < DU; ++h) {
+        const int64_t q = base + h * DT_THREADS + tid;
+        d[h] = Vec4<T>{I, I, I, I};
+        ra[h] = Vec4<T>{I, I, I, I};
+        rb[h] = Vec4<T>{I, I, I, I};
+        if (q < n4) {
+          d[h] = ld4_stream<T>(Drow + 4 * q);
+          ra[h] = ld4<T>(a.r1 + 4 * q);
+          if (TWO) rb[h] = ld4<T>(a.r2 + 4 * q);
+        }
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t q = h ? q1 : q0;
+      for (int h = 0; h < DU; ++h) {
+        const int64_t q = base + h * DT_THREADS + tid;
         unsigned nib = 0;
-        if (q < n4)
-          nib = flag_nibble<T, TWO>(h ? d1 : d0, h ? ra1 : ra0, h ? rb1 : rb0, c1, c2, 4 * q, n,
-                                    i, a.skip, a.tau);
+        if (q < n4) nib = flag_nibble<T, TWO>(d[h], ra[h], rb[h], c1, c2, 4 * q, n, i, a.skip, a.tau);
         unsigned v = nib << (4 * (lane & 7));
         if (__any_sync(0xffffffffu, nib)) {
           v |= __shfl_xor_sync(0xffffffffu, v, 1);
@@ -508,6 +542,7 @@ __global__ void __launch_bounds__(DT_THREADS) k_detect(DetectArgs<T> a) {
         if (store) {
           a.pcol[pos] = (int)j;
           a.prow[pos] = (int)i;
+          a.plb[pos] = Drow[j];                         // D_old[i][j]: a lower bound of D'
         }
         ++pos;
         if (a.reset) Drow[j] = a.WT[j * a.ldw + i];   // D0[i][j] := W'[i][j]
@@ -520,11 +555,11 @@ __global__ void __launch_bounds__(DT_THREADS) k_detect(DetectArgs<T> a) {
 template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
                    const T* c2, const T* r2, float tau, const T* WT, int64_t ldw, int reset,
-                   int64_t* rowoff, int* rowcnt, int* prow, int* pcol, int64_t lcap,
+                   int64_t* rowoff, int* rowcnt, int* prow, int* pcol, T* plb, int64_t lcap,
                    DetectCounters* ctr, int grid, cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
   DetectArgs<T> a{D, ld, r, n, skip, c1, r1, c2, r2, tau, WT, ldw, reset,
-                  rowoff, rowcnt, prow, pcol, lcap, ctr};
+                  rowoff, rowcnt, prow, pcol, plb, lcap, ctr};
   size_t smem = sizeof(uint32_t) * (size_t)cdiv(n, 32);
   if (grid <= 0) grid = (int)std::min<int64_t>(r.hi - r.lo, (int64_t)num_sms() * 8);
   if (smem > 48 * 1024) {
@@ -637,7 +672,8 @@ cudaError_t set_edge(T* WT, int64_t ldw, int64_t u, int64_t v, T w, int directed
                                         const T*, T*, int64_t, const T*, const T*, cudaStream_t); \
   template cudaError_t detect<T>(T*, int64_t, Rows, int64_t, int64_t, const T*, const T*,          \
                                  const T*, const T*, float, const T*, int64_t, int, int64_t*,     \
-                                 int*, int*, int*, int64_t, DetectCounters*, int, cudaStream_t);  \
+                                 int*, int*, int*, T*, int64_t, DetectCounters*, int,             \
+                                 cudaStream_t);                                                   \
   template cudaError_t tombstone<T>(T*, int64_t, Rows, int64_t, int64_t, T*, int64_t,              \
                                     cudaStream_t);                                                \
   template cudaError_t copy_row<T>(T*, const T*, int64_t, cudaStream_t);                           \

@@ -63,6 +63,7 @@ def lib():
         L.oracle_brute_i64.argtypes = [i64, vp, i64, i64, i64]
         L.oracle_brute_f64.restype = ctypes.c_double
         L.oracle_brute_f64.argtypes = [i64, vp, i64, i64]
+        L.oracle_dijkstra_rows_i32w.argtypes = [i64, vp, i64, ctypes.c_int32, i64, vp, i64, vp, ctypes.c_int]
         L.oracle_count_shortest_i64.restype = i64
         L.oracle_count_shortest_i64.argtypes = [i64, vp, i64, i64, i64, i64]
         _lib = L
@@ -133,6 +134,19 @@ def dijkstra_rows(W, srcs):
 def dijkstra_cols(W, dsts):
     """Columns dsts of the APSP matrix (Dijkstra on the reversed graph W^T)."""
     return dijkstra_rows(np.ascontiguousarray(np.asarray(W).T), dsts).T
+
+
+def dijkstra_rows_i32(W, srcs, reverse=False):
+    """Rows (or, reverse=True, columns) srcs of the APSP matrix of an int32 W
+    (API INF sentinel), by Dijkstra reading W in place: no int64 copy of W."""
+    W = np.asarray(W)
+    assert W.dtype == np.int32 and W.strides[1] == 4
+    n = W.shape[0]
+    srcs = np.ascontiguousarray(np.asarray(srcs, np.int64))
+    out = np.empty((len(srcs), n), np.int64)
+    lib().oracle_dijkstra_rows_i32w(n, W.ctypes.data, W.strides[0] // 4, API_INF_I32, int(INF64),
+                                    srcs.ctypes.data, len(srcs), out.ctypes.data, int(reverse))
+    return from_oracle_i32(out)
 
 
 def dijkstra_pair(W, s, t):

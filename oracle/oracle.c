@@ -210,3 +210,34 @@ int64_t oracle_count_shortest_i64(int64_t n, const int64_t* W, int64_t inf, int6
   count_rec(n, W, inf, s, t, 0, target, 1u << s, &cnt);
   return cnt;
 }
+
+/* Dijkstra from each source in srcs on an int32 matrix W (row stride ld,
+ * absent edge = inf32), int64 arithmetic; rows of the APSP matrix out
+ * (count x n, int64, unreachable = inf64).  Same algorithm as
+ * oracle_dijkstra_i64, reading the int32 input in place (used for sampled
+ * checks of full-size configurations). */
+void oracle_dijkstra_rows_i32w(int64_t n, const int32_t* W, int64_t ld, int32_t inf32,
+                               int64_t inf64, const int64_t* srcs, int64_t count, int64_t* out,
+                               int reverse) {
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t q = 0; q < count; ++q) {
+    int64_t* dist = out + q * n;
+    char* done = (char*)calloc((size_t)n, 1);
+    for (int64_t v = 0; v < n; ++v) dist[v] = inf64;
+    dist[srcs[q]] = 0;
+    for (int64_t it = 0; it < n; ++it) {
+      int64_t m = -1;
+      for (int64_t v = 0; v < n; ++v)
+        if (!done[v] && dist[v] < inf64 && (m < 0 || dist[v] < dist[m])) m = v;
+      if (m < 0) break;
+      done[m] = 1;
+      for (int64_t v = 0; v < n; ++v) {
+        int32_t w = reverse ? W[v * ld + m] : W[m * ld + v];   /* reverse: edges into m */
+        if (done[v] || w >= inf32) continue;
+        int64_t cand = dist[m] + (int64_t)w;
+        if (cand < dist[v]) dist[v] = cand;
+      }
+    }
+    free(done);
+  }
+}

@@ -12,6 +12,7 @@
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -50,7 +51,10 @@ struct Nccl {
   bool load() {
     if (tried) return ok;
     tried = true;
-    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // RTLD_LOCAL: the library's NCCL symbols never interpose on the copy the
+    // host framework (torch) may have loaded; APSP_NCCL_LIB overrides the path.
+    const char* path = getenv("APSP_NCCL_LIB");
+    h = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
     if (!h) return false;
 #define SYM(name, field)                                            \
   field = reinterpret_cast<decltype(field)>(dlsym(h, "nccl" name)); \

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(QT) k_query(const T* __restrict__ D, int64_t l
   __shared__ short pred[kQueryCap];
   __shared__ unsigned char done[kQueryCap];
   __shared__ int s_cnt, s_is, s_it;
-  __shared__ int s_wcnt[QT / 32];
+  __shared__ int s_wcnt[4 * (QT / 32)];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const T I = Tr<T>::inf();
 
@@ -61,7 +61,9 @@ __global__ void __launch_bounds__(QT) k_query(const T* __restrict__ D, int64_t l
     __syncthreads();
 
     // ---- 1. candidate scan (Theorem 4 equality), ordered compaction ----
-    constexpr int U = 4;   // k values per thread per step (loads in flight)
+    // Candidates are rare (|C| ~ tens out of n), so a block-wide OR skips the
+    // compaction for almost every group of QT*U nodes.
+    constexpr int U = 4;   // nodes per thread per step (loads in flight)
     for (int64_t base = 0; base < n; base += (int64_t)QT * U) {
       T dsk[U], dkt[U];
 #pragma unroll
@@ -70,30 +72,42 @@ __global__ void __launch_bounds__(QT) k_query(const T* __restrict__ D, int64_t l
         dsk[u] = k < n ? Ds[k] : I;
         dkt[u] = k < n ? D[k * ld + t] : I;
       }
+      bool f[U];
+      bool anyf = false;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         int64_t k = base + (int64_t)u * QT + tid;
-        bool f = k < n && Tr<T>::fin(dsk[u]) && Tr<T>::fin(dkt[u]) &&
-                 Tr<T>::tight(Tr<T>::add(dsk[u], dkt[u]), st, tau);
-        unsigned bal = __ballot_sync(0xffffffffu, f);
-        if (lane == 0) s_wcnt[warp] = __popc(bal);
-        __syncthreads();
-        int off = s_cnt;
-        for (int w = 0; w < warp; ++w) off += s_wcnt[w];
-        int tot = 0;
-        for (int w = 0; w < QT / 32; ++w) tot += s_wcnt[w];
-        if (f) {
-          int pos = off + __popc(bal & ((1u << lane) - 1));
+        f[u] = k < n && Tr<T>::fin(dsk[u]) && Tr<T>::fin(dkt[u]) &&
+               Tr<T>::tight(Tr<T>::add(dsk[u], dkt[u]), st, tau);
+        anyf |= f[u];
+      }
+      if (!__syncthreads_or(anyf)) continue;
+      unsigned bal[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        bal[u] = __ballot_sync(0xffffffffu, f[u]);
+        if (lane == 0) s_wcnt[u * (QT / 32) + warp] = __popc(bal[u]);
+      }
+      __syncthreads();
+      int tot = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        int off = s_cnt + tot;
+        for (int w = 0; w < warp; ++w) off += s_wcnt[u * (QT / 32) + w];
+        for (int w = 0; w < QT / 32; ++w) tot += s_wcnt[u * (QT / 32) + w];
+        if (f[u]) {
+          const int64_t k = base + (int64_t)u * QT + tid;
+          const int pos = off + __popc(bal[u] & ((1u << lane) - 1));
           if (pos < kQueryCap) {
             cid[pos] = (int)k;
             if (k == s) s_is = pos;
             if (k == t) s_it = pos;
           }
         }
-        __syncthreads();
-        if (tid == 0) s_cnt += tot;
-        __syncthreads();
       }
+      __syncthreads();
+      if (tid == 0) s_cnt += tot;
+      __syncthreads();
     }
     const int cnt = s_cnt;
     if (cnt > kQueryCap || s_is < 0 || s_it < 0) {

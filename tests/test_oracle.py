@@ -292,3 +292,14 @@ def test_candidates_contain_every_shortest_path_node(rng):
             assert set(p) <= c
         if len(best) == 1:
             assert c == set(best[0])
+
+
+def test_dijkstra_int32_inplace_matches_bruteforce(rng):
+    """The in-place int32 Dijkstra (sampled full-size checks) against the
+    definition, rows and reversed columns, with zeros and absent edges."""
+    for trial in range(15):
+        n = int(rng.integers(2, 8))
+        W = random_graph(rng, n, True, 0.6, lo=0, hi=9)
+        B = oracle.brute_apsp(W)
+        assert np.array_equal(oracle.dijkstra_rows_i32(W, range(n)), B)
+        assert np.array_equal(oracle.dijkstra_rows_i32(W, range(n), reverse=True), B.T)

@@ -401,13 +401,13 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   if (total == 0) return APSP_OK;
   // ---- sparse recompute (a6) ----
   // A: shortlist pass over every listed pair: certify ties (value == lb)
+  CKR(cudaMemsetAsync(h->ocnt(), 0, sizeof(int) * h->cap, h->st));
   if (local_total > 0)
     PK(APSP_K_SPARSE0, (double)local_total * kSL * 2.0 * sizeof(T),
-       sparse_short<T>(h->Dl<T>(), h->ld, h->row0, h->slid(), h->slw<T>(), h->wnext<T>(), h->prow(),
-                       h->pcol(), h->plb<T>(), local_total, h->popen(), 0, h->st));
-  CK(sparse_compact<T>(r, h->rowoff(), h->rowcnt(), h->pcol(), h->plb<T>(), h->popen(), h->ocol(),
-                       h->ocnt(), h->gprow(), h->gpcol(), h->glb<T>(), h->gfull(), h->plan.ocap,
-                       h->ctr(), h->st));
+       sparse_phase_a<T>(h->Dl<T>(), h->ld, r, n, h->slid(), h->slw<T>(), h->wnext<T>(), h->rowoff(),
+                         h->rowcnt(), h->prow(), h->pcol(), h->plb<T>(), local_total, h->popen(),
+                         h->ocnt(), h->ocol(), h->gprow(), h->gpcol(), h->glb<T>(), h->gfull(),
+                         h->plan.ocap, h->ctr(), h->st));
   CKR(cudaMemcpyAsync(h->host_small, h->ctr(), sizeof(DetectCounters), cudaMemcpyDeviceToHost, h->st));
   CKR(cudaStreamSynchronize(h->st));
   int64_t nopen = (int64_t)hc->open_total;
@@ -499,8 +499,8 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   CK(addnode_write<T>(h->Dl<T>(), ld, r, n, x, h->local(x) ? 1 : 0, col, row, h->WT<T>(), ld, ow,
                       iw, h->st));
   CK(shortlist_add_bound<T>(h->wnext<T>(), ow, n, h->st));          // new in-edges x -> j
-  CK(shortlist_build<T>(h->WT<T>(), ld, n + 1, nullptr, x, x + 1, h->slid(), h->slw<T>(),
-                        h->wnext<T>(), h->st));                      // in-edges of x
+  CK(shortlist_build_one<T>(h->WT<T>(), ld, n + 1, x, h->slid(), h->slw<T>(), h->wnext<T>(),
+                            h->st));                                 // in-edges of x
   h->n = n + 1;
   if (new_index) *new_index = x;
   if (info) {

@@ -89,6 +89,9 @@ template <typename T>
 cudaError_t shortlist_build(const T* WT, int64_t ldw, int64_t n, const int* rows, int64_t r0,
                             int64_t r1, int* SLid, T* SLw, T* wnext, cudaStream_t st);
 template <typename T>
+cudaError_t shortlist_build_one(const T* WT, int64_t ldw, int64_t n, int64_t j, int* SLid, T* SLw,
+                                T* wnext, cudaStream_t st);
+template <typename T>
 cudaError_t shortlist_add_bound(T* wnext, const T* out_w, int64_t n, cudaStream_t st);
 template <typename T>
 cudaError_t shortlist_set_edge(int* SLid, T* SLw, T* wnext, int64_t u, int64_t v, T w,
@@ -100,6 +103,12 @@ template <typename T>
 cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const T* SLw,
                          const T* wnext, const int* prow, const int* pcol, const T* plb,
                          int64_t npairs, unsigned char* out, int classify, cudaStream_t st);
+template <typename T>
+cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, int64_t n, const int* SLid, const T* SLw,
+                           const T* wnext, const int64_t* rowoff, const int* rowcnt,
+                           const int* prow, const int* pcol, const T* plb, int64_t npairs,
+                           unsigned char* out, int* ocnt, int* ocol, int* gprow, int* gpcol, T* glb,
+                           unsigned char* gfull, int64_t ocap, DetectCounters* ctr, cudaStream_t st);
 template <typename T>
 cudaError_t sparse_compact(Rows r, const int64_t* rowoff, const int* rowcnt, const int* pcol,
                            const T* plb, const unsigned char* popen, int* ocol, int* ocnt,

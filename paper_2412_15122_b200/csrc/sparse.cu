@@ -91,6 +91,81 @@ cudaError_t shortlist_build(const T* WT, int64_t ldw, int64_t n, const int* rows
   return cudaGetLastError();
 }
 
+// One row, whole CTA (256 threads): each warp keeps lane-local top-kSLK of its
+// eighth of the row, then warp 0 keeps lane-local top-kSLK of those 8*kSL
+// candidates.  Every in-edge left out was rejected at one of the two stages,
+// so it is >= the min over all rejected values = wnext(j).
+template <typename T>
+__global__ void __launch_bounds__(256) k_shortlist_build_one(const T* __restrict__ WT, int64_t ldw,
+                                                             int64_t n, int64_t j, int* SLid,
+                                                             T* SLw, T* wnext) {
+  __shared__ T cw[8 * kSL];
+  __shared__ int ci[8 * kSL];
+  __shared__ T srej[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const T I = Tr<T>::inf();
+  const T* row = WT + j * ldw;
+  T bw[kSLK];
+  int bi[kSLK];
+#pragma unroll
+  for (int q = 0; q < kSLK; ++q) { bw[q] = I; bi[q] = -1; }
+  T rej = I;
+  auto insert = [&](T x, int m) {
+    if (x < bw[kSLK - 1]) {
+      rej = Tr<T>::mn(rej, bw[kSLK - 1]);
+      T cwv = x;
+      int civ = m;
+#pragma unroll
+      for (int q = 0; q < kSLK; ++q)
+        if (cwv < bw[q]) { T tw = bw[q]; int ti = bi[q]; bw[q] = cwv; bi[q] = civ; cwv = tw; civ = ti; }
+    } else {
+      rej = Tr<T>::mn(rej, x);
+    }
+  };
+  const int64_t n4 = (n + 3) / 4;
+  for (int64_t q = threadIdx.x; q < n4; q += 256) {
+    Vec4<T> v = ld4<T>(row + 4 * q);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int64_t m = 4 * q + c;
+      const T x = get(v, c);
+      if (m < n && m != j && Tr<T>::fin(x)) insert(x, (int)m);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kSLK; ++q) {
+    cw[warp * kSL + q * 32 + lane] = bw[q];
+    ci[warp * kSL + q * 32 + lane] = bi[q];
+  }
+  rej = warp_min<T>(rej);
+  if (lane == 0) srej[warp] = rej;
+  __syncthreads();
+  if (warp != 0) return;
+#pragma unroll
+  for (int q = 0; q < kSLK; ++q) { bw[q] = I; bi[q] = -1; }
+  rej = I;
+  for (int t = lane; t < 8 * kSL; t += 32)
+    if (ci[t] >= 0) insert(cw[t], ci[t]);
+  int* oid = SLid + j * kSL;
+  T* ow = SLw + j * kSL;
+#pragma unroll
+  for (int q = 0; q < kSLK; ++q) {
+    oid[q * 32 + lane] = bi[q];
+    ow[q * 32 + lane] = bw[q];
+  }
+  rej = warp_min<T>(rej);
+  if (lane == 0) {
+    for (int w = 0; w < 8; ++w) rej = Tr<T>::mn(rej, srej[w]);
+    wnext[j] = rej;
+  }
+}
+template <typename T>
+cudaError_t shortlist_build_one(const T* WT, int64_t ldw, int64_t n, int64_t j, int* SLid, T* SLw,
+                                T* wnext, cudaStream_t st) {
+  k_shortlist_build_one<T><<<1, 256, 0, st>>>(WT, ldw, n, j, SLid, SLw, wnext);
+  return cudaGetLastError();
+}
+
 // A new node x adds in-edge x -> j (weight out_w[j]) to every j; it is not in
 // SL(j), so wnext(j) must cover it.
 template <typename T>
@@ -159,6 +234,29 @@ cudaError_t shortlist_remove(int* SLid, T* SLw, T* wnext, int64_t n, int64_t k, 
   return cudaGetLastError();
 }
 
+// Open-pair bookkeeping of phase A (replaces a separate compaction pass):
+// the pair joins its row's open list (order within a row is irrelevant) and
+// the global open list consumed by phases A2/B and the rounds.
+template <typename T>
+struct OpenLists {
+  int* ocnt; int* ocol; const int64_t* rowoff;
+  int* gprow; int* gpcol; T* glb; unsigned char* gfull; int64_t ocap;
+  DetectCounters* ctr;
+  __device__ __forceinline__ void append(int64_t i, int64_t j, T lb) const {
+    const int s1 = atomicAdd(ocnt + i, 1);
+    ocol[rowoff[i] + s1] = (int)j;
+    const unsigned long long s2 = atomicAdd(&ctr->open_total, 1ull);
+    if ((int64_t)s2 < ocap) {
+      gprow[s2] = (int)i;
+      gpcol[s2] = (int)j;
+      glb[s2] = lb;
+      gfull[s2] = 1;
+    } else {
+      atomicOr(&ctr->overflow, 2u);
+    }
+  }
+};
+
 // ---------------------------------------------------------------------------
 // phase A / A2: shortlist evaluation of a list of pairs
 //   classify = 0 (phase A, all listed pairs):   out = 0 final (reached lb), 1 open
@@ -176,25 +274,32 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
                                                       const int* __restrict__ prow,
                                                       const int* __restrict__ pcol,
                                                       const T* __restrict__ plb, int64_t npairs,
-                                                      unsigned char* out, int classify) {
+                                                      unsigned char* out, int classify,
+                                                      const int* __restrict__ rowcnt, int min_cnt_skip,
+                                                      OpenLists<T> ol) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t p = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); p < npairs;
        p += nw) {
     const int64_t i = prow[p], j = pcol[p];
+    if (rowcnt && rowcnt[i] >= min_cnt_skip) continue;   // done by k_sparse_short_rows
     T* Drow = D + (i - row0) * ld;
     const int* sid = SLid + j * kSL;
     const T* sw = SLw + j * kSL;
+    const T lbp = plb[p];
     T acc = Tr<T>::inf();
+    // lane lists are ascending, so the cheapest in-edges come first: in phase
+    // A stop as soon as the warp's bound reaches lb (the value is then final)
 #pragma unroll
     for (int q = 0; q < kSLK; ++q) {
       const int m = sid[q * 32 + lane];
       const T w = sw[q * 32 + lane];
       if (m >= 0) acc = Tr<T>::relax(acc, *(volatile T*)(Drow + m), w);
+      if (!classify && (q == 0 || q == 2) && warp_min<T>(acc) <= lbp) break;
     }
     acc = warp_min<T>(acc);
     if (lane == 0) {
-      const T lb = plb[p];
+      const T lb = lbp;
       const T cur = *(volatile T*)(Drow + j);
       const T v = Tr<T>::mn(acc, cur);
       if (v < cur) Drow[j] = v;
@@ -203,17 +308,129 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
       else if (!classify || acc <= wnext[j]) st = 1;
       else st = 2;
       out[p] = st;
+      if (!classify && st != 0) ol.append(i, j, lb);
     }
   }
 }
+// Phase A for rows with many listed pairs: the CTA copies row i of D0 into
+// shared memory once (a snapshot: every value in it is a valid upper bound)
+// and evaluates all the row's pairs from it.
+template <typename T>
+__global__ void __launch_bounds__(512) k_sparse_short_rows(T* D, int64_t ld, Rows r, int64_t n,
+                                                           const int* __restrict__ SLid,
+                                                           const T* __restrict__ SLw,
+                                                           const int64_t* __restrict__ rowoff,
+                                                           const int* __restrict__ rowcnt,
+                                                           const int* __restrict__ pcol,
+                                                           const T* __restrict__ plb,
+                                                           unsigned char* out, int min_cnt,
+                                                           OpenLists<T> ol) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* srow = reinterpret_cast<T*>(smem_raw);
+  __shared__ __align__(8) unsigned long long mbar;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const unsigned bytes = (unsigned)(((n + 3) / 4) * 16);
+  const unsigned sbar = (unsigned)__cvta_generic_to_shared(&mbar);
+  const unsigned sdst = (unsigned)__cvta_generic_to_shared(srow);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::);
+  }
+  __syncthreads();
+  unsigned phase = 0;
+  for (int64_t i = r.lo + blockIdx.x; i < r.hi; i += gridDim.x) {
+    const int cnt = rowcnt[i];
+    if (cnt < min_cnt) continue;
+    T* Drow = D + (i - r.row0) * ld;
+    // TMA 1-D bulk copy of the whole row into shared memory (one thread issues it)
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(bytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              sdst),
+          "l"(Drow), "r"(bytes), "r"(sbar)
+          : "memory");
+    }
+    {
+      unsigned done = 0;
+      while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(sbar), "r"(phase)
+            : "memory");
+      }
+    }
+    phase ^= 1;
+    const int64_t off = rowoff[i];
+    for (int t = warp; t < cnt; t += nwarp) {
+      const int64_t p = off + t;
+      const int64_t j = pcol[p];
+      const int* sid = SLid + j * kSL;
+      const T* sw = SLw + j * kSL;
+      T acc = Tr<T>::inf();
+#pragma unroll
+      for (int q = 0; q < kSLK; ++q) {
+        const int m = sid[q * 32 + lane];
+        const T w = sw[q * 32 + lane];
+        if (m >= 0) acc = Tr<T>::relax(acc, srow[m], w);
+      }
+      acc = warp_min<T>(acc);
+      if (lane == 0) {
+        const T cur = srow[j];
+        const T v = Tr<T>::mn(acc, cur);
+        if (v < cur) Drow[j] = v;
+        const T lb = plb[p];
+        out[p] = v <= lb ? 0 : 1;
+        if (v > lb) ol.append(i, j, lb);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <typename T>
 cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const T* SLw,
                          const T* wnext, const int* prow, const int* pcol, const T* plb,
                          int64_t npairs, unsigned char* out, int classify, cudaStream_t st) {
   if (npairs <= 0) return cudaSuccess;
   int grid = (int)std::min<int64_t>(cdiv(npairs, 8), (int64_t)num_sms() * 16);
+  OpenLists<T> ol{};
   k_sparse_short<T><<<grid, 256, 0, st>>>(D, ld, row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
-                                          out, classify);
+                                          out, classify, nullptr, 0, ol);
+  return cudaGetLastError();
+}
+
+// Phase A over the detection lists: rows with >= kRowMin pairs use the
+// shared-memory row kernel (when the row fits), the others the pair kernel.
+constexpr int kRowMin = 1 << 30;  // row kernel off: heavy rows pin one SM (measured slower)
+template <typename T>
+cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, int64_t n, const int* SLid, const T* SLw,
+                           const T* wnext, const int64_t* rowoff, const int* rowcnt,
+                           const int* prow, const int* pcol, const T* plb, int64_t npairs,
+                           unsigned char* out, int* ocnt, int* ocol, int* gprow, int* gpcol, T* glb,
+                           unsigned char* gfull, int64_t ocap, DetectCounters* ctr, cudaStream_t st) {
+  if (npairs <= 0) return cudaSuccess;
+  OpenLists<T> ol{ocnt, ocol, rowoff, gprow, gpcol, glb, gfull, ocap, ctr};
+  const size_t smem = sizeof(T) * (size_t)((n + 3) / 4 * 4);
+  const bool rows_ok = smem <= 200 * 1024;
+  if (rows_ok) {
+    static size_t configured = 0;
+    if (configured < smem) {
+      cudaError_t e = cudaFuncSetAttribute(k_sparse_short_rows<T>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      configured = smem;
+    }
+    int grid = (int)std::min<int64_t>(r.hi - r.lo, (int64_t)num_sms() * (smem > 110 * 1024 ? 1 : 2));
+    if (grid > 0)
+      k_sparse_short_rows<T><<<grid, 512, smem, st>>>(D, ld, r, n, SLid, SLw, rowoff, rowcnt, pcol,
+                                                      plb, out, kRowMin, ol);
+  }
+  int grid = (int)std::min<int64_t>(cdiv(npairs, 8), (int64_t)num_sms() * 16);
+  k_sparse_short<T><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
+                                          out, 0, rows_ok ? rowcnt : nullptr, kRowMin, ol);
   return cudaGetLastError();
 }
 
@@ -395,11 +612,18 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
   template cudaError_t shortlist_build<T>(const T*, int64_t, int64_t, const int*, int64_t, int64_t, \
                                           int*, T*, T*, cudaStream_t);                            \
   template cudaError_t shortlist_add_bound<T>(T*, const T*, int64_t, cudaStream_t);                \
+  template cudaError_t shortlist_build_one<T>(const T*, int64_t, int64_t, int64_t, int*, T*, T*,   \
+                                              cudaStream_t);                                      \
   template cudaError_t shortlist_set_edge<T>(int*, T*, T*, int64_t, int64_t, T, int, cudaStream_t); \
   template cudaError_t shortlist_remove<T>(int*, T*, T*, int64_t, int64_t, int64_t, cudaStream_t); \
   template cudaError_t sparse_short<T>(T*, int64_t, int64_t, const int*, const T*, const T*,       \
                                        const int*, const int*, const T*, int64_t, unsigned char*,  \
                                        int, cudaStream_t);                                        \
+  template cudaError_t sparse_phase_a<T>(T*, int64_t, Rows, int64_t, const int*, const T*,         \
+                                         const T*, const int64_t*, const int*, const int*,         \
+                                         const int*, const T*, int64_t, unsigned char*, int*, int*, \
+                                         int*, int*, T*, unsigned char*, int64_t, DetectCounters*, \
+                                         cudaStream_t);                                           \
   template cudaError_t sparse_compact<T>(Rows, const int64_t*, const int*, const int*, const T*,   \
                                          const unsigned char*, int*, int*, int*, int*, T*,         \
                                          unsigned char*, int64_t, DetectCounters*, cudaStream_t);  \

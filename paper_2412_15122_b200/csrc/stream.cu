@@ -226,6 +226,8 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
 
   int64_t qv[P1_V];
   Vec4<T> inw[P1_V], colp[P1_V];
+  // does this warp's chunk contain the row's last, partially valid vector?
+  const bool tail = (n & 3) != 0 && (int64_t)(chunk + 1) * P1_VEC >= tl.n4;
 #pragma unroll
   for (int v = 0; v < P1_V; ++v) {
     qv[v] = (int64_t)chunk * P1_VEC + v * 32 + lane;
@@ -240,12 +242,22 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
       const T* row0 = D + (i - r.row0) * ld;
       const T* row1 = row0 + ld;
       Vec4<T> d0[P1_V], d1[P1_V];
+      // issue every load of both rows before touching any result (MLP = 2*P1_V)
 #pragma unroll
       for (int v = 0; v < P1_V; ++v) {
-        d0[v] = qv[v] < tl.n4 ? mask_tail<T>(ld4_stream<T>(row0 + 4 * qv[v]), 4 * qv[v], n)
-                              : Vec4<T>{I, I, I, I};
-        d1[v] = (two && qv[v] < tl.n4) ? mask_tail<T>(ld4_stream<T>(row1 + 4 * qv[v]), 4 * qv[v], n)
-                                       : Vec4<T>{I, I, I, I};
+        d0[v] = Vec4<T>{I, I, I, I};
+        d1[v] = Vec4<T>{I, I, I, I};
+        if (qv[v] < tl.n4) {
+          d0[v] = ld4_stream<T>(row0 + 4 * qv[v]);
+          if (two) d1[v] = ld4_stream<T>(row1 + 4 * qv[v]);
+        }
+      }
+      if (tail) {   // only the warp holding the row's last (partial) vector
+#pragma unroll
+        for (int v = 0; v < P1_V; ++v) {
+          d0[v] = mask_tail<T>(d0[v], 4 * qv[v], n);
+          d1[v] = mask_tail<T>(d1[v], 4 * qv[v], n);
+        }
       }
       const T o0 = ow[i];
       const T o1 = two ? ow[i + 1] : I;
@@ -431,19 +443,28 @@ struct DetectArgs {
 
 constexpr int DT_THREADS = 256;
 
+// Theorem-4 tightness of the 4 pairs of one vector: the common case (no bit)
+// costs one add + one compare per element; validity (j < n, j != i,
+// j != skip, D finite) is applied only when some bit is set.
 template <typename T, bool TWO>
 __device__ __forceinline__ unsigned flag_nibble(const Vec4<T>& d, const Vec4<T>& r1,
                                                 const Vec4<T>& r2, T c1, T c2, int64_t j0,
                                                 int64_t n, int64_t i, int64_t skip, float tau) {
-  unsigned nib = 0;
+  unsigned nib = (unsigned)Tr<T>::tight(Tr<T>::add(c1, r1.x), d.x, tau) |
+                 (unsigned)Tr<T>::tight(Tr<T>::add(c1, r1.y), d.y, tau) << 1 |
+                 (unsigned)Tr<T>::tight(Tr<T>::add(c1, r1.z), d.z, tau) << 2 |
+                 (unsigned)Tr<T>::tight(Tr<T>::add(c1, r1.w), d.w, tau) << 3;
+  if (TWO)
+    nib |= (unsigned)Tr<T>::tight(Tr<T>::add(c2, r2.x), d.x, tau) |
+           (unsigned)Tr<T>::tight(Tr<T>::add(c2, r2.y), d.y, tau) << 1 |
+           (unsigned)Tr<T>::tight(Tr<T>::add(c2, r2.z), d.z, tau) << 2 |
+           (unsigned)Tr<T>::tight(Tr<T>::add(c2, r2.w), d.w, tau) << 3;
+  if (nib) {
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    int64_t j = j0 + c;
-    T dj = get(d, c);
-    bool f = Tr<T>::tight(Tr<T>::add(c1, get(r1, c)), dj, tau);
-    if (TWO) f = f || Tr<T>::tight(Tr<T>::add(c2, get(r2, c)), dj, tau);
-    f = f && j < n && j != i && j != skip && Tr<T>::fin(dj);
-    nib |= (unsigned)f << c;
+    for (int c = 0; c < 4; ++c) {
+      const int64_t j = j0 + c;
+      if (!(j < n && j != i && j != skip && Tr<T>::fin(get(d, c)))) nib &= ~(1u << c);
+    }
   }
   return nib;
 }

@@ -100,7 +100,7 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   };
   p.off_wt = take(sizeof(int32_t) * (size_t)cap * p.ld);
   p.off_vec = take(sizeof(int32_t) * (size_t)kVecs * p.ld);
-  p.off_rowpart = take(sizeof(int32_t) * (size_t)p.maxchunk * p.ld);
+  p.off_rowpart = take(sizeof(int32_t) * (size_t)p.maxchunk * p.ld * 2);   // min and max partials
   p.off_colpart = take(sizeof(int32_t) * (size_t)kMaxSlabs * p.ld);
   p.off_rowoff = take(sizeof(int64_t) * (size_t)cap);
   p.off_rowcnt = take(sizeof(int32_t) * (size_t)cap);
@@ -488,14 +488,18 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   }
   Rows r = h->active();
   int nchunk = 0, nslab = 0;
+  T* rowpartM = h->rowpart<T>() + (size_t)h->plan.maxchunk * ld;
+  T* ceff = h->vec<T>(4);
   PK(APSP_K_ADD_PASS1, 4.0 * (double)(r.hi - r.lo) * (double)n,
-     addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), h->colpart<T>(), ld, &nchunk,
-                      &nslab, kMaxSlabs, h->st));
-  CK(addnode_finish<T>(h->rowpart<T>(), nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col, row, h->st));
+     addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
+                      &nchunk, &nslab, kMaxSlabs, h->st));
+  CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
+                       ceff, row, h->st));
   if (h->world > 1)
     NK(g_nccl.AllReduce(row, row, (size_t)ld, nccl_type<T>(), ncclMin, h->comm, h->st));
+  // rows with ceff[i] = INF provably do not change and are not read at all
   PK(APSP_K_RANK1, 4.0 * (double)(r.hi - r.lo) * (double)n,
-     rank1<T>(h->Dl<T>(), ld, r, n, col, row, nullptr, nullptr, h->st));
+     rank1<T>(h->Dl<T>(), ld, r, n, ceff, row, nullptr, nullptr, h->st));
   CK(addnode_write<T>(h->Dl<T>(), ld, r, n, x, h->local(x) ? 1 : 0, col, row, h->WT<T>(), ld, ow,
                       iw, h->st));
   CK(shortlist_add_bound<T>(h->wnext<T>(), ow, n, h->st));          // new in-edges x -> j

@@ -52,12 +52,12 @@ template <typename T>
 cudaError_t copy_vec(const T* src, int64_t n, int64_t npad, T add, T* out, cudaStream_t st);
 template <typename T>
 cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow, const T* iw,
-                          T* rowpart, T* colpart, int64_t part_ld, int* nchunk_out, int* nslab_out,
-                          int max_slabs, cudaStream_t st);
+                          T* rowpart, T* rowpartM, T* colpart, int64_t part_ld, int* nchunk_out,
+                          int* nslab_out, int max_slabs, cudaStream_t st);
 template <typename T>
-cudaError_t addnode_finish(const T* rowpart, int nchunk, const T* colpart, int nslab,
-                           int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col, T* row,
-                           cudaStream_t st);
+cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
+                           int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,
+                           T* ceff, T* row, cudaStream_t st);
 template <typename T>
 cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, const T* c2,
                   const T* rv2, cudaStream_t st);

@@ -201,21 +201,31 @@ static Tiling make_tiling(int64_t n, int64_t rows, int max_slabs, int chunk_vec 
 
 // Each warp owns a column chunk of P1_VEC vectors per row (lane: P1_V of
 // them) and a slab of rows.  Column partials (new row) stay in registers.
-// Row partials (new column) go to shared memory, one 32-row batch at a time:
-// lane l writes its partial of row r to rp[r][l]; after the batch lane l
-// reduces row l (stride 33: conflict-free).  No per-row shuffle chain, so
-// the loads of consecutive rows stay in flight.
+// Two row reductions go through shared memory, 16 rows at a time (lane l
+// writes its partial of row r to rp[r][l]; stride 33, conflict-free):
+//   col[i] = min_t D[i][t] + in[t]           (the new column, theo_2_back)
+//   M[i]   = max_t D[i][t] - out[t]          (row-skip bound for pass 2)
+// Pass 2 can change row i only if col[i] < M[i]: a change at (i, j) needs
+// col[i] + out[t*] + D[t*][j] < D[i][j] <= D[i][t*] + D[t*][j] for the t* that
+// attains row[j], i.e. col[i] < D[i][t*] - out[t*] <= M[i].
 constexpr int P1_V = 4;
 constexpr int P1_VEC = 32 * P1_V;   // 512 columns per chunk
+constexpr int P1_RB = 16;           // rows per shared-memory batch
+template <typename T>
+__device__ __forceinline__ T max_add(T m, T d, T negw) {
+  if constexpr (Tr<T>::kFloat) return fmaxf(m, __fadd_rn(d, negw));   // NaN (inf-inf) ignored
+  else return max(m, d + negw);                                        // |d + negw| <= INF
+}
 template <typename T>
 __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ D, int64_t ld, Rows r,
                                                           int64_t n, Tiling tl,
                                                           const T* __restrict__ ow,
                                                           const T* __restrict__ iw, T* rowpart,
-                                                          T* colpart, int64_t part_ld) {
-  __shared__ T rp_all[8][32][33];
+                                                          T* rowpartM, T* colpart, int64_t part_ld) {
+  __shared__ T rp_all[8][2][P1_RB][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  T (*rp)[33] = rp_all[warp];
+  T (*rp)[33] = rp_all[warp][0];
+  T (*rm)[33] = rp_all[warp][1];
   const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
   if (gw >= tl.warps) return;
   const int chunk = (int)(gw % tl.nchunk);
@@ -223,19 +233,23 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
   const int64_t i_lo = r.lo + slab * tl.slab;
   const int64_t i_hi = min(r.hi, i_lo + tl.slab);
   const T I = Tr<T>::inf();
+  const T NI = Tr<T>::kFloat ? -I : -I;   // "minus infinity" of the max reduction
 
   int64_t qv[P1_V];
-  Vec4<T> inw[P1_V], colp[P1_V];
+  Vec4<T> inw[P1_V], nout[P1_V], colp[P1_V];
   // does this warp's chunk contain the row's last, partially valid vector?
   const bool tail = (n & 3) != 0 && (int64_t)(chunk + 1) * P1_VEC >= tl.n4;
 #pragma unroll
   for (int v = 0; v < P1_V; ++v) {
     qv[v] = (int64_t)chunk * P1_VEC + v * 32 + lane;
     inw[v] = qv[v] < tl.n4 ? ld4<T>(iw + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+    Vec4<T> o = qv[v] < tl.n4 ? ld4<T>(ow + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+    // -out[t]; an absent out-edge (INF) can never give a shortcut: -INF-ish
+    nout[v] = Vec4<T>{-o.x, -o.y, -o.z, -o.w};
     colp[v] = Vec4<T>{I, I, I, I};
   }
-  for (int64_t b0 = i_lo; b0 < i_hi; b0 += 32) {
-    const int nb = (int)min((int64_t)32, i_hi - b0);
+  for (int64_t b0 = i_lo; b0 < i_hi; b0 += P1_RB) {
+    const int nb = (int)min((int64_t)P1_RB, i_hi - b0);
     for (int rr = 0; rr < nb; rr += 2) {
       const bool two = rr + 1 < nb;
       const int64_t i = b0 + rr;
@@ -261,27 +275,42 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
       }
       const T o0 = ow[i];
       const T o1 = two ? ow[i + 1] : I;
-      T p0 = I, p1 = I;
+      T p0 = I, p1 = I, m0 = NI, m1 = NI;
 #pragma unroll
       for (int v = 0; v < P1_V; ++v) {
         p0 = Tr<T>::relax(p0, d0[v].x, inw[v].x); p0 = Tr<T>::relax(p0, d0[v].y, inw[v].y);
         p0 = Tr<T>::relax(p0, d0[v].z, inw[v].z); p0 = Tr<T>::relax(p0, d0[v].w, inw[v].w);
         p1 = Tr<T>::relax(p1, d1[v].x, inw[v].x); p1 = Tr<T>::relax(p1, d1[v].y, inw[v].y);
         p1 = Tr<T>::relax(p1, d1[v].z, inw[v].z); p1 = Tr<T>::relax(p1, d1[v].w, inw[v].w);
+        m0 = max_add<T>(m0, d0[v].x, nout[v].x); m0 = max_add<T>(m0, d0[v].y, nout[v].y);
+        m0 = max_add<T>(m0, d0[v].z, nout[v].z); m0 = max_add<T>(m0, d0[v].w, nout[v].w);
+        m1 = max_add<T>(m1, d1[v].x, nout[v].x); m1 = max_add<T>(m1, d1[v].y, nout[v].y);
+        m1 = max_add<T>(m1, d1[v].z, nout[v].z); m1 = max_add<T>(m1, d1[v].w, nout[v].w);
         colp[v].x = Tr<T>::relax(Tr<T>::relax(colp[v].x, o0, d0[v].x), o1, d1[v].x);
         colp[v].y = Tr<T>::relax(Tr<T>::relax(colp[v].y, o0, d0[v].y), o1, d1[v].y);
         colp[v].z = Tr<T>::relax(Tr<T>::relax(colp[v].z, o0, d0[v].z), o1, d1[v].z);
         colp[v].w = Tr<T>::relax(Tr<T>::relax(colp[v].w, o0, d0[v].w), o1, d1[v].w);
       }
       rp[rr][lane] = p0;
-      if (two) rp[rr + 1][lane] = p1;
+      rm[rr][lane] = m0;
+      if (two) { rp[rr + 1][lane] = p1; rm[rr + 1][lane] = m1; }
     }
     __syncwarp();
-    if (lane < nb) {
-      T m = rp[lane][0];
+    {
+      const int row = lane & (P1_RB - 1);
+      if (row < nb) {
+        if (lane < P1_RB) {
+          T m = rp[row][0];
 #pragma unroll 8
-      for (int t = 1; t < 32; ++t) m = Tr<T>::mn(m, rp[lane][t]);
-      rowpart[(int64_t)chunk * part_ld + b0 + lane] = m;
+          for (int t = 1; t < 32; ++t) m = Tr<T>::mn(m, rp[row][t]);
+          rowpart[(int64_t)chunk * part_ld + b0 + row] = m;
+        } else {
+          T m = rm[row][0];
+#pragma unroll 8
+          for (int t = 1; t < 32; ++t) m = Tr<T>::kFloat ? fmaxf(m, rm[row][t]) : max(m, rm[row][t]);
+          rowpartM[(int64_t)chunk * part_ld + b0 + row] = m;
+        }
+      }
     }
     __syncwarp();
   }
@@ -292,8 +321,8 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
 
 template <typename T>
 cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow, const T* iw,
-                          T* rowpart, T* colpart, int64_t part_ld, int* nchunk_out, int* nslab_out,
-                          int max_slabs, cudaStream_t st) {
+                          T* rowpart, T* rowpartM, T* colpart, int64_t part_ld, int* nchunk_out,
+                          int* nslab_out, int max_slabs, cudaStream_t st) {
   Tiling tl = make_tiling(n, r.hi - r.lo, max_slabs, P1_VEC, 48);
   *nchunk_out = tl.nchunk;
   *nslab_out = tl.nslab;
@@ -304,19 +333,33 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
     return e;
   }
   int grid = (int)cdiv(tl.warps, 8);
-  k_addnode_pass1<T><<<grid, 256, 0, st>>>(D, ld, r, n, tl, ow, iw, rowpart, colpart, part_ld);
+  k_addnode_pass1<T><<<grid, 256, 0, st>>>(D, ld, r, n, tl, ow, iw, rowpart, rowpartM, colpart,
+                                           part_ld);
   return cudaGetLastError();
 }
 
 template <typename T>
-__global__ void k_addnode_finish(const T* rowpart, int nchunk, const T* colpart, int nslab,
-                                 int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col, T* row) {
+__global__ void k_addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
+                                 int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,
+                                 T* ceff, T* row) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = r.lo + tid; i < r.hi; i += stride) {
     T m = Tr<T>::inf();
-    for (int c = 0; c < nchunk; ++c) m = Tr<T>::mn(m, rowpart[(int64_t)c * part_ld + i]);
-    col[i] = Tr<T>::sat(m);
+    T M = -Tr<T>::inf();
+    for (int c = 0; c < nchunk; ++c) {
+      m = Tr<T>::mn(m, rowpart[(int64_t)c * part_ld + i]);
+      const T x = rowpartM[(int64_t)c * part_ld + i];
+      M = Tr<T>::kFloat ? fmaxf(M, x) : max(M, x);
+    }
+    m = Tr<T>::sat(m);
+    col[i] = m;
+    // pass 2 may skip row i unless col[i] < M[i] (fp32: with a relative
+    // margin, so rounding in d - out can only keep rows, never drop them)
+    bool keep;
+    if constexpr (Tr<T>::kFloat) keep = m < M + fabsf(M) * 1e-6f;
+    else keep = m < M;
+    ceff[i] = keep ? m : Tr<T>::inf();
   }
   for (int64_t j = tid; j < npad; j += stride) {
     T m = Tr<T>::inf();
@@ -326,12 +369,12 @@ __global__ void k_addnode_finish(const T* rowpart, int nchunk, const T* colpart,
   }
 }
 template <typename T>
-cudaError_t addnode_finish(const T* rowpart, int nchunk, const T* colpart, int nslab,
-                           int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col, T* row,
-                           cudaStream_t st) {
+cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
+                           int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,
+                           T* ceff, T* row, cudaStream_t st) {
   int grid = (int)std::min<int64_t>(cdiv(std::max<int64_t>(npad, r.hi - r.lo), 256), 4 * num_sms());
-  k_addnode_finish<T><<<grid, 256, 0, st>>>(rowpart, nchunk, colpart, nslab, part_ld, r, n, npad,
-                                            col, row);
+  k_addnode_finish<T><<<grid, 256, 0, st>>>(rowpart, rowpartM, nchunk, colpart, nslab, part_ld, r, n,
+                                            npad, col, ceff, row);
   return cudaGetLastError();
 }
 
@@ -684,9 +727,9 @@ cudaError_t set_edge(T* WT, int64_t ldw, int64_t u, int64_t v, T w, int directed
   template cudaError_t gather_col<T>(const T*, int64_t, Rows, int64_t, T, T*, cudaStream_t);       \
   template cudaError_t copy_vec<T>(const T*, int64_t, int64_t, T, T*, cudaStream_t);               \
   template cudaError_t addnode_pass1<T>(const T*, int64_t, Rows, int64_t, const T*, const T*, T*,  \
-                                        T*, int64_t, int*, int*, int, cudaStream_t);              \
-  template cudaError_t addnode_finish<T>(const T*, int, const T*, int, int64_t, Rows, int64_t,     \
-                                         int64_t, T*, T*, cudaStream_t);                          \
+                                        T*, T*, int64_t, int*, int*, int, cudaStream_t);          \
+  template cudaError_t addnode_finish<T>(const T*, const T*, int, const T*, int, int64_t, Rows,    \
+                                         int64_t, int64_t, T*, T*, T*, cudaStream_t);             \
   template cudaError_t rank1<T>(T*, int64_t, Rows, int64_t, const T*, const T*, const T*,          \
                                 const T*, cudaStream_t);                                          \
   template cudaError_t addnode_write<T>(T*, int64_t, Rows, int64_t, int64_t, int, const T*,        \

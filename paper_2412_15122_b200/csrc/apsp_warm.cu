@@ -81,7 +81,7 @@ struct Plan {
   int64_t ld, lcap, ocap, maxchunk;
   size_t off_wt, off_vec, off_rowpart, off_colpart, off_rowoff, off_rowcnt, off_chg, off_prow,
       off_pcol, off_plb, off_popen, off_ocol, off_ocnt, off_gprow, off_gpcol, off_glb, off_gfull,
-      off_slid, off_slw, off_wnext, off_panel, off_pt, off_small, total;
+      off_slid, off_slw, off_wnext, off_panel, off_pt, off_bm, off_anyrow, off_small, total;
   int64_t ldpt;
 };
 
@@ -123,6 +123,10 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   // transposed pivot column panel for the FW phase-3 kernel (kTile x ldpt)
   p.ldpt = round_up(world > 1 ? round_up(cdiv(cap, world), kTile) : cap, kTile);
   p.off_pt = take(sizeof(int32_t) * (size_t)kTile * p.ldpt);
+  // detection flag bitmap: one bit per entry of the local rows (n/8 bytes per row)
+  const int64_t rows_max = world > 1 ? round_up(cdiv(cap, world), kTile) : cap;
+  p.off_bm = take(sizeof(uint32_t) * (size_t)rows_max * cdiv(cdiv(p.ld, 4), 256) * 32);
+  p.off_anyrow = take(sizeof(int32_t) * (size_t)cap);
   p.off_small = take(64 * 1024);
   p.total = o;
   return p;
@@ -219,6 +223,8 @@ struct apsp_handle {
   template <typename T> T* wnext() { return reinterpret_cast<T*>(ws + plan.off_wnext); }
   template <typename T> T* panel() { return reinterpret_cast<T*>(ws + plan.off_panel); }
   template <typename T> T* pt() { return reinterpret_cast<T*>(ws + plan.off_pt); }
+  uint32_t* bm() { return reinterpret_cast<uint32_t*>(ws + plan.off_bm); }
+  int* anyrow() { return reinterpret_cast<int*>(ws + plan.off_anyrow); }
   DetectCounters* ctr() { return reinterpret_cast<DetectCounters*>(ws + plan.off_small); }
   int* anyflag() { return reinterpret_cast<int*>(ws + plan.off_small + 256); }
   unsigned char* small() { return ws + plan.off_small + 512; }   // query scratch etc.
@@ -363,7 +369,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
      detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, h->WT<T>(), h->ld, 1,
                h->rowoff(), h->rowcnt(), h->prow(), h->pcol(), h->plb<T>(), h->plan.lcap, h->ctr(),
-               0, h->st));
+               h->bm(), h->anyrow(), 0, h->st));
   if (removal) CK(tombstone<T>(h->Dl<T>(), h->ld, r, n, skip, h->WT<T>(), h->ld, h->st));
 
   // counters -> host (|A|, Phi, max|A_i|, overflow), summed over ranks

@@ -69,7 +69,7 @@ template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
                    const T* c2, const T* r2, float tau, const T* WT, int64_t ldw, int reset,
                    int64_t* rowoff, int* rowcnt, int* prow, int* pcol, T* plb, int64_t lcap,
-                   DetectCounters* ctr, int grid, cudaStream_t st);
+                   DetectCounters* ctr, uint32_t* bm, int* anyrow, int grid, cudaStream_t st);
 template <typename T>
 cudaError_t tombstone(T* D, int64_t ld, Rows r, int64_t n, int64_t k, T* WT, int64_t ldw,
                       cudaStream_t st);
@@ -83,7 +83,7 @@ template <typename T>
 cudaError_t set_edge(T* WT, int64_t ldw, int64_t u, int64_t v, T w, int directed, cudaStream_t st);
 
 // ---------------- sparse.cu ----------------
-constexpr int kSLK = 8;               // shortlist entries per lane
+constexpr int kSLK = 16;              // shortlist entries per lane
 constexpr int kSL = 32 * kSLK;        // shortlist entries per node
 template <typename T>
 cudaError_t shortlist_build(const T* WT, int64_t ldw, int64_t n, const int* rows, int64_t r0,

@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
       const int m = sid[q * 32 + lane];
       const T w = sw[q * 32 + lane];
       if (m >= 0) acc = Tr<T>::relax(acc, *(volatile T*)(Drow + m), w);
-      if (!classify && (q == 0 || q == 2) && warp_min<T>(acc) <= lbp) break;
+      if (!classify && (q == 0 || q == 2 || q == 6) && warp_min<T>(acc) <= lbp) break;
     }
     acc = warp_min<T>(acc);
     if (lane == 0) {
@@ -414,7 +414,7 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, int64_t n, const int* SLid,
   if (npairs <= 0) return cudaSuccess;
   OpenLists<T> ol{ocnt, ocol, rowoff, gprow, gpcol, glb, gfull, ocap, ctr};
   const size_t smem = sizeof(T) * (size_t)((n + 3) / 4 * 4);
-  const bool rows_ok = smem <= 200 * 1024;
+  const bool rows_ok = kRowMin < (1 << 30) && smem <= 200 * 1024;
   if (rows_ok) {
     static size_t configured = 0;
     if (configured < smem) {

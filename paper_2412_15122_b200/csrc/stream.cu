@@ -41,6 +41,11 @@ int num_sms() {
 }
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+#define CUDA_TRY(x)                           \
+  do {                                        \
+    cudaError_t _e = (x);                     \
+    if (_e != cudaSuccess) return _e;         \
+  } while (0)
 
 // ---------------------------------------------------------------------------
 // validation / normalisation of caller vectors
@@ -512,62 +517,78 @@ __device__ __forceinline__ unsigned flag_nibble(const Vec4<T>& d, const Vec4<T>&
   return nib;
 }
 
+// ---------------------------------------------------------------------------
+// Detection in two kernels (the launched path):
+//  (1) k_detect_stream — laid out like k_rank1: warp = (1024-column chunk) x
+//      (row slab), each lane keeps its 8 vectors of the pivot row r1 (and r2)
+//      in registers and streams the slab's rows; for every row it writes one
+//      32-bit flag word per lane (bit v*4+c <-> column 4*(chunk*256+v*32+lane)+c)
+//      and marks rows with any flag.  Pure HBM stream: 4 B read per entry, n/8
+//      bytes written per row.
+//  (2) k_detect_emit — one CTA per marked row: popcount of the row's bitmap
+//      words, block scan, one atomic for the row's list offset, then decode
+//      the flagged columns into the list (prow/pcol/plb) and reset D0.
+// ---------------------------------------------------------------------------
 template <typename T, bool TWO>
-__global__ void __launch_bounds__(DT_THREADS) k_detect(DetectArgs<T> a) {
-  extern __shared__ uint32_t bm[];   // one bit per column of the current row
+__global__ void __launch_bounds__(256) k_detect_stream(const T* __restrict__ D, int64_t ld, Rows r,
+                                                       int64_t n, int64_t skip, Tiling tl,
+                                                       const T* __restrict__ c1,
+                                                       const T* __restrict__ r1,
+                                                       const T* __restrict__ c2,
+                                                       const T* __restrict__ r2, float tau,
+                                                       uint32_t* __restrict__ bm, int64_t bmld,
+                                                       int* __restrict__ anyrow) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gw >= tl.warps) return;
+  const int chunk = (int)(gw % tl.nchunk);
+  const int slab = (int)(gw / tl.nchunk);
+  const int64_t i_lo = r.lo + slab * tl.slab;
+  const int64_t i_hi = min(r.hi, i_lo + tl.slab);
+  const T I = Tr<T>::inf();
+  int64_t qv[VPL];
+  Vec4<T> a[VPL], b[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    qv[v] = (int64_t)chunk * CHUNK_VEC + v * 32 + lane;
+    a[v] = qv[v] < tl.n4 ? ld4<T>(r1 + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+    if (TWO) b[v] = qv[v] < tl.n4 ? ld4<T>(r2 + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+  }
+  for (int64_t i = i_lo; i < i_hi; ++i) {
+    if (i == skip) continue;
+    const T ci = c1[i];
+    const T ci2 = TWO ? c2[i] : I;
+    if (!Tr<T>::fin(ci) && !Tr<T>::fin(ci2)) continue;   // no pair of this row can be tight
+    const T* row = D + (i - r.row0) * ld;
+    Vec4<T> d[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+      d[v] = qv[v] < tl.n4 ? ld4_stream<T>(row + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+    uint32_t word = 0;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+      word |= flag_nibble<T, TWO>(d[v], a[v], b[v], ci, ci2, 4 * qv[v], n, i, skip, tau) << (4 * v);
+    bm[(i - r.lo) * bmld + chunk * 32 + lane] = word;
+    if (__any_sync(0xffffffffu, word != 0) && lane == 0) anyrow[i] = 1;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(DT_THREADS) k_detect_emit(DetectArgs<T> a,
+                                                            const uint32_t* __restrict__ bm,
+                                                            int64_t bmld, int nwords,
+                                                            const int* __restrict__ anyrow) {
   __shared__ int s_warp[DT_THREADS / 32];
   __shared__ long long s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t n = a.n, n4 = (n + 3) / 4;
-  const int nwords = (int)((n + 31) / 32);
-  const T I = Tr<T>::inf();
-
   for (int64_t i = a.r.lo + blockIdx.x; i < a.r.hi; i += gridDim.x) {
-    if (i == a.skip) continue;
-    const T c1 = a.c1[i];
-    const T c2 = TWO ? a.c2[i] : I;
-    if (!Tr<T>::fin(c1) && !Tr<T>::fin(c2)) continue;   // no pair of this row can be tight
+    if (!anyrow[i]) continue;
+    const uint32_t* brow = bm + (i - a.r.lo) * bmld;
     T* Drow = a.D + (i - a.r.row0) * a.ld;
-    bool any = false;
-    constexpr int DU = 4;   // vectors per thread in flight
-    for (int64_t base = 0; base < n4; base += DU * DT_THREADS) {
-      Vec4<T> d[DU], ra[DU], rb[DU];
-#pragma unroll
-      for (int h = 0; h < DU; ++h) {
-        const int64_t q = base + h * DT_THREADS + tid;
-        d[h] = Vec4<T>{I, I, I, I};
-        ra[h] = Vec4<T>{I, I, I, I};
-        rb[h] = Vec4<T>{I, I, I, I};
-        if (q < n4) {
-          d[h] = ld4_stream<T>(Drow + 4 * q);
-          ra[h] = ld4<T>(a.r1 + 4 * q);
-          if (TWO) rb[h] = ld4<T>(a.r2 + 4 * q);
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < DU; ++h) {
-        const int64_t q = base + h * DT_THREADS + tid;
-        unsigned nib = 0;
-        if (q < n4) nib = flag_nibble<T, TWO>(d[h], ra[h], rb[h], c1, c2, 4 * q, n, i, a.skip, a.tau);
-        unsigned v = nib << (4 * (lane & 7));
-        if (__any_sync(0xffffffffu, nib)) {
-          v |= __shfl_xor_sync(0xffffffffu, v, 1);
-          v |= __shfl_xor_sync(0xffffffffu, v, 2);
-          v |= __shfl_xor_sync(0xffffffffu, v, 4);
-          any = true;
-        }
-        const int64_t word = (base + h * DT_THREADS) / 8 + warp * 4 + (lane >> 3);
-        if ((lane & 7) == 0 && word < nwords) bm[word] = v;
-      }
-    }
-    if (!__syncthreads_or(any)) continue;
-
-    // per-thread contiguous word ranges keep the emitted columns sorted
     const int wpt = (nwords + DT_THREADS - 1) / DT_THREADS;
     const int w0 = min(tid * wpt, nwords), w1 = min(w0 + wpt, nwords);
     int cnt = 0;
-    for (int w = w0; w < w1; ++w) cnt += __popc(bm[w]);
-    // block exclusive scan of cnt (warp shuffles + one smem round)
+    for (int w = w0; w < w1; ++w) cnt += __popc(brow[w]);
     int incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -579,11 +600,10 @@ __global__ void __launch_bounds__(DT_THREADS) k_detect(DetectArgs<T> a) {
     int woff = 0, total = 0;
 #pragma unroll
     for (int w = 0; w < DT_THREADS / 32; ++w) {
-      int sw = s_warp[w];
+      const int sw = s_warp[w];
       woff += (w < warp) ? sw : 0;
       total += sw;
     }
-    const int excl = woff + incl - cnt;
     if (tid == 0) {
       unsigned long long base = atomicAdd(&a.ctr->total, (unsigned long long)total);
       a.rowoff[i] = (int64_t)base;
@@ -596,23 +616,24 @@ __global__ void __launch_bounds__(DT_THREADS) k_detect(DetectArgs<T> a) {
     __syncthreads();
     const int64_t base = s_base;
     const bool store = base + total <= a.lcap;
-    int64_t pos = base + excl;
+    int64_t pos = base + woff + incl - cnt;
     for (int w = w0; w < w1; ++w) {
-      uint32_t bits = bm[w];
+      uint32_t bits = brow[w];
+      const int chunk = w >> 5, ln = w & 31;
       while (bits) {
-        const int b = __ffs(bits) - 1;
+        const int bit = __ffs(bits) - 1;
         bits &= bits - 1;
-        const int64_t j = (int64_t)w * 32 + b;
+        const int64_t j = 4 * ((int64_t)chunk * CHUNK_VEC + (bit >> 2) * 32 + ln) + (bit & 3);
         if (store) {
           a.pcol[pos] = (int)j;
           a.prow[pos] = (int)i;
-          a.plb[pos] = Drow[j];                         // D_old[i][j]: a lower bound of D'
+          a.plb[pos] = Drow[j];                          // D_old[i][j]: a lower bound of D'
         }
         ++pos;
-        if (a.reset) Drow[j] = a.WT[j * a.ldw + i];   // D0[i][j] := W'[i][j]
+        if (a.reset) Drow[j] = a.WT[j * a.ldw + i];    // D0[i][j] := W'[i][j]
       }
     }
-    __syncthreads();   // bm / scan storage reused by the next row
+    __syncthreads();   // s_warp / s_base reused by the next row
   }
 }
 
@@ -620,21 +641,23 @@ template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
                    const T* c2, const T* r2, float tau, const T* WT, int64_t ldw, int reset,
                    int64_t* rowoff, int* rowcnt, int* prow, int* pcol, T* plb, int64_t lcap,
-                   DetectCounters* ctr, int grid, cudaStream_t st) {
+                   DetectCounters* ctr, uint32_t* bm, int* anyrow, int grid, cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
   DetectArgs<T> a{D, ld, r, n, skip, c1, r1, c2, r2, tau, WT, ldw, reset,
                   rowoff, rowcnt, prow, pcol, plb, lcap, ctr};
-  size_t smem = sizeof(uint32_t) * (size_t)cdiv(n, 32);
-  if (grid <= 0) grid = (int)std::min<int64_t>(r.hi - r.lo, (int64_t)num_sms() * 8);
-  if (smem > 48 * 1024) {
-    auto f = c2 ? k_detect<T, true> : k_detect<T, false>;
-    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
+  (void)grid;
+  Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20);
+  const int64_t bmld = (int64_t)tl.nchunk * 32;
+  CUDA_TRY(cudaMemsetAsync(anyrow + r.lo, 0, sizeof(int) * (size_t)(r.hi - r.lo), st));
+  const int g1 = (int)cdiv(tl.warps, 8);
   if (c2)
-    k_detect<T, true><<<grid, DT_THREADS, smem, st>>>(a);
+    k_detect_stream<T, true><<<g1, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, c2, r2, tau, bm, bmld, anyrow);
   else
-    k_detect<T, false><<<grid, DT_THREADS, smem, st>>>(a);
+    k_detect_stream<T, false><<<g1, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, nullptr, nullptr, tau, bm,
+                                                  bmld, anyrow);
+  CUDA_TRY(cudaGetLastError());
+  const int g2 = (int)std::min<int64_t>(r.hi - r.lo, (int64_t)num_sms() * 8);
+  k_detect_emit<T><<<g2, DT_THREADS, 0, st>>>(a, bm, bmld, (int)bmld, anyrow);
   return cudaGetLastError();
 }
 
@@ -736,8 +759,8 @@ cudaError_t set_edge(T* WT, int64_t ldw, int64_t u, int64_t v, T w, int directed
                                         const T*, T*, int64_t, const T*, const T*, cudaStream_t); \
   template cudaError_t detect<T>(T*, int64_t, Rows, int64_t, int64_t, const T*, const T*,          \
                                  const T*, const T*, float, const T*, int64_t, int, int64_t*,     \
-                                 int*, int*, int*, T*, int64_t, DetectCounters*, int,             \
-                                 cudaStream_t);                                                   \
+                                 int*, int*, int*, T*, int64_t, DetectCounters*, uint32_t*, int*, \
+                                 int, cudaStream_t);                                              \
   template cudaError_t tombstone<T>(T*, int64_t, Rows, int64_t, int64_t, T*, int64_t,              \
                                     cudaStream_t);                                                \
   template cudaError_t copy_row<T>(T*, const T*, int64_t, cudaStream_t);                           \

@@ -31,7 +31,7 @@ SYMBOLS = [
 ]
 # kernel classes of apsp_profile_read (apsp_kernel_class)
 K_CLASSES = ["fw_diag", "fw_panel", "fw_tile", "add_pass1", "rank1", "detect", "sparse0",
-             "sparse_r", "query", "other"]
+             "sparse_r", "query", "other", "emit"]
 
 
 class UpdateInfo(ctypes.Structure):

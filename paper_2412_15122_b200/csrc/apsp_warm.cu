@@ -196,7 +196,11 @@ struct apsp_handle {
       ev_pool.push_back(r.b);
     }
     prof_pending.clear();
-    return cudaSuccess;
+    unsigned long long rb = 0;
+    e = cudaMemcpy(&rb, rank1_bytes(), sizeof rb, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return e;
+    prof_work[APSP_K_RANK1] += (double)rb;
+    return cudaMemset(rank1_bytes(), 0, sizeof rb);
   }
 
   template <typename T> T* WT() { return reinterpret_cast<T*>(ws + plan.off_wt); }
@@ -227,6 +231,9 @@ struct apsp_handle {
   int* anyrow() { return reinterpret_cast<int*>(ws + plan.off_anyrow); }
   DetectCounters* ctr() { return reinterpret_cast<DetectCounters*>(ws + plan.off_small); }
   int* anyflag() { return reinterpret_cast<int*>(ws + plan.off_small + 256); }
+  unsigned long long* rank1_bytes() {   // device counter of bytes the rank-1 kernel read
+    return reinterpret_cast<unsigned long long*>(ws + plan.off_small + 320);
+  }
   unsigned char* small() { return ws + plan.off_small + 512; }   // query scratch etc.
   template <typename T> T* Dl() { return reinterpret_cast<T*>(D); }
   template <typename T> T* Drow(int64_t gi) { return Dl<T>() + (gi - row0) * ld; }
@@ -367,9 +374,10 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   CKR(cudaMemsetAsync(h->rowcnt(), 0, sizeof(int) * h->cap, h->st));
   CKR(cudaMemsetAsync(h->ctr(), 0, sizeof(DetectCounters), h->st));
   PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
-     detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, h->WT<T>(), h->ld, 1,
-               h->rowoff(), h->rowcnt(), h->prow(), h->pcol(), h->plb<T>(), h->plan.lcap, h->ctr(),
-               h->bm(), h->anyrow(), 0, h->st));
+     detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, h->bm(), h->anyrow(), h->st));
+  PK(APSP_K_EMIT, 0.0,
+     detect_emit<T>(h->Dl<T>(), h->ld, r, n, h->WT<T>(), h->ld, 1, h->rowoff(), h->rowcnt(), h->prow(),
+                    h->pcol(), h->plb<T>(), h->plan.lcap, h->ctr(), h->bm(), h->anyrow(), h->st));
   if (removal) CK(tombstone<T>(h->Dl<T>(), h->ld, r, n, skip, h->WT<T>(), h->ld, h->st));
 
   // counters -> host (|A|, Phi, max|A_i|, overflow), summed over ranks
@@ -504,11 +512,11 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   if (h->world > 1)
     NK(g_nccl.AllReduce(row, row, (size_t)ld, nccl_type<T>(), ncclMin, h->comm, h->st));
   // rows with ceff[i] = INF provably do not change and are not read at all
-  PK(APSP_K_RANK1, 4.0 * (double)(r.hi - r.lo) * (double)n,
-     rank1<T>(h->Dl<T>(), ld, r, n, ceff, row, nullptr, nullptr, h->st));
+  PK(APSP_K_RANK1, 0.0,   // work: bytes actually read, counted on the device
+     rank1<T>(h->Dl<T>(), ld, r, n, ceff, row, nullptr, nullptr, h->rank1_bytes(), h->st));
   CK(addnode_write<T>(h->Dl<T>(), ld, r, n, x, h->local(x) ? 1 : 0, col, row, h->WT<T>(), ld, ow,
                       iw, h->st));
-  CK(shortlist_add_bound<T>(h->wnext<T>(), ow, n, h->st));          // new in-edges x -> j
+  CK(shortlist_add_bound<T>(h->slid(), h->slw<T>(), h->wnext<T>(), ow, n, x, h->st));  // x -> j
   CK(shortlist_build_one<T>(h->WT<T>(), ld, n + 1, x, h->slid(), h->slw<T>(), h->wnext<T>(),
                             h->st));                                 // in-edges of x
   h->n = n + 1;
@@ -614,8 +622,9 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
       s = snap_row<T>(h, u, T(0), r2);
       if (s != APSP_OK) return s;
     }
-    PK(APSP_K_RANK1, 4.0 * (double)(r.hi - r.lo) * (double)n,
-       rank1<T>(h->Dl<T>(), ld, r, n, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, h->st));
+    PK(APSP_K_RANK1, 0.0,   // work: bytes actually read, counted on the device
+       rank1<T>(h->Dl<T>(), ld, r, n, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, h->rank1_bytes(),
+                h->st));
     CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
     CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
     if (info) info->path = 1;
@@ -782,6 +791,7 @@ apsp_status apsp_create(apsp_handle** out, apsp_dtype dtype, int directed, int64
   // WT := W^T (replicated), pads INF; validate W (diag 0, w >= 0)
   apsp_status s = dispatch(dtype, [&](auto z) -> apsp_status {
     using T = decltype(z);
+    CKR(cudaMemsetAsync(h->ws + h->plan.off_small, 0, 512, h->st));   // counters, flags
     CK(fill<T>(h->WT<T>(), (int64_t)cap * h->ld, Tr<T>::inf(), h->st));
     CKR(cudaMemsetAsync(&h->ctr()->err, 0, sizeof(unsigned), h->st));
     CK(transpose_in<T>(reinterpret_cast<const T*>(W), ldw, n, h->WT<T>(), h->ld, &h->ctr()->err, h->st));

@@ -60,16 +60,18 @@ cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, cons
                            T* ceff, T* row, cudaStream_t st);
 template <typename T>
 cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, const T* c2,
-                  const T* rv2, cudaStream_t st);
+                  const T* rv2, unsigned long long* bytes_read, cudaStream_t st);
 template <typename T>
 cudaError_t addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xlocal,
                           const T* col, const T* row, T* WT, int64_t ldw, const T* ow,
                           const T* iw, cudaStream_t st);
 template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
-                   const T* c2, const T* r2, float tau, const T* WT, int64_t ldw, int reset,
-                   int64_t* rowoff, int* rowcnt, int* prow, int* pcol, T* plb, int64_t lcap,
-                   DetectCounters* ctr, uint32_t* bm, int* anyrow, int grid, cudaStream_t st);
+                   const T* c2, const T* r2, float tau, uint32_t* bm, int* anyrow, cudaStream_t st);
+template <typename T>
+cudaError_t detect_emit(T* D, int64_t ld, Rows r, int64_t n, const T* WT, int64_t ldw, int reset,
+                        int64_t* rowoff, int* rowcnt, int* prow, int* pcol, T* plb, int64_t lcap,
+                        DetectCounters* ctr, const uint32_t* bm, const int* anyrow, cudaStream_t st);
 template <typename T>
 cudaError_t tombstone(T* D, int64_t ld, Rows r, int64_t n, int64_t k, T* WT, int64_t ldw,
                       cudaStream_t st);
@@ -92,7 +94,8 @@ template <typename T>
 cudaError_t shortlist_build_one(const T* WT, int64_t ldw, int64_t n, int64_t j, int* SLid, T* SLw,
                                 T* wnext, cudaStream_t st);
 template <typename T>
-cudaError_t shortlist_add_bound(T* wnext, const T* out_w, int64_t n, cudaStream_t st);
+cudaError_t shortlist_add_bound(int* SLid, T* SLw, T* wnext, const T* out_w, int64_t n, int64_t x,
+                                cudaStream_t st);
 template <typename T>
 cudaError_t shortlist_set_edge(int* SLid, T* SLw, T* wnext, int64_t u, int64_t v, T w,
                                int directed, cudaStream_t st);

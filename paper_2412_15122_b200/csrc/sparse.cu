@@ -166,18 +166,55 @@ cudaError_t shortlist_build_one(const T* WT, int64_t ldw, int64_t n, int64_t j, 
   return cudaGetLastError();
 }
 
-// A new node x adds in-edge x -> j (weight out_w[j]) to every j; it is not in
-// SL(j), so wnext(j) must cover it.
+// Insert in-edge (m -> j, weight w) into SL(j) when it would otherwise have to
+// lower wnext(j): evict the heaviest entry instead (its weight joins the
+// excluded set, so wnext(j) = min(wnext(j), evicted)).  One warp; the caller
+// guarantees m is not already listed.
 template <typename T>
-__global__ void k_shortlist_add_edge_bound(T* wnext, const T* out_w, int64_t n) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x)
-    wnext[j] = Tr<T>::mn(wnext[j], out_w[j]);
+__device__ __forceinline__ void shortlist_insert_warp(int* SLid, T* SLw, T* wnext, int64_t j, int m,
+                                                      T w) {
+  const int lane = threadIdx.x & 31;
+  if (!(w < wnext[j])) return;   // warp-uniform: already covered by the bound
+  int* sid = SLid + j * kSL;
+  T* sw = SLw + j * kSL;
+  // warp argmax over the entries (dead entries count as +INF: evicted first)
+  T best = -Tr<T>::inf();
+  int bq = -1;
+#pragma unroll
+  for (int q = 0; q < kSLK; ++q) {
+    const int e = q * 32 + lane;
+    const T x = sid[e] < 0 ? Tr<T>::inf() : sw[e];
+    if (x > best || bq < 0) { best = x; bq = e; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const T ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+    if (ob > best || (ob == best && oq < bq)) { best = ob; bq = oq; }
+  }
+  if (lane == 0) {
+    if (w < best) {
+      if (sid[bq] >= 0) wnext[j] = Tr<T>::mn(wnext[j], best);
+      sid[bq] = m;
+      sw[bq] = w;
+    } else {
+      wnext[j] = Tr<T>::mn(wnext[j], w);
+    }
+  }
+}
+
+// A new node x adds in-edge x -> j (weight out_w[j]) to every j.
+template <typename T>
+__global__ void k_shortlist_add_edges(int* SLid, T* SLw, T* wnext, const T* out_w, int64_t n, int x) {
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t j = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); j < n; j += nw)
+    shortlist_insert_warp<T>(SLid, SLw, wnext, j, x, out_w[j]);
 }
 template <typename T>
-cudaError_t shortlist_add_bound(T* wnext, const T* out_w, int64_t n, cudaStream_t st) {
-  int grid = (int)std::min<int64_t>(cdiv(n, 256), 4 * num_sms());
-  k_shortlist_add_edge_bound<T><<<grid, 256, 0, st>>>(wnext, out_w, n);
+cudaError_t shortlist_add_bound(int* SLid, T* SLw, T* wnext, const T* out_w, int64_t n, int64_t x,
+                                cudaStream_t st) {
+  int grid = (int)std::min<int64_t>(cdiv(n, 8), 8 * num_sms());
+  k_shortlist_add_edges<T><<<grid, 256, 0, st>>>(SLid, SLw, wnext, out_w, n, (int)x);
   return cudaGetLastError();
 }
 
@@ -193,7 +230,7 @@ __global__ void k_shortlist_set_edge(int* SLid, T* SLw, T* wnext, int64_t u, int
     if (SLid[e] == (int)u) { SLw[e] = w; found = true; }
   }
   found = __any_sync(0xffffffffu, found);
-  if (lane == 0 && !found) wnext[v] = Tr<T>::mn(wnext[v], w);
+  if (!found) shortlist_insert_warp<T>(SLid, SLw, wnext, v, (int)u, w);
 }
 template <typename T>
 cudaError_t shortlist_set_edge(int* SLid, T* SLw, T* wnext, int64_t u, int64_t v, T w,
@@ -611,7 +648,8 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
 #define INST(T)                                                                                   \
   template cudaError_t shortlist_build<T>(const T*, int64_t, int64_t, const int*, int64_t, int64_t, \
                                           int*, T*, T*, cudaStream_t);                            \
-  template cudaError_t shortlist_add_bound<T>(T*, const T*, int64_t, cudaStream_t);                \
+  template cudaError_t shortlist_add_bound<T>(int*, T*, T*, const T*, int64_t, int64_t,            \
+                                              cudaStream_t);                                      \
   template cudaError_t shortlist_build_one<T>(const T*, int64_t, int64_t, int64_t, int*, T*, T*,   \
                                               cudaStream_t);                                      \
   template cudaError_t shortlist_set_edge<T>(int*, T*, T*, int64_t, int64_t, T, int, cudaStream_t); \

@@ -390,7 +390,8 @@ template <typename T, bool TWO>
 __global__ void __launch_bounds__(256) k_rank1(T* __restrict__ D, int64_t ld, Rows r, int64_t n,
                                                Tiling tl, const T* __restrict__ c,
                                                const T* __restrict__ rv, const T* __restrict__ c2,
-                                               const T* __restrict__ rv2) {
+                                               const T* __restrict__ rv2,
+                                               unsigned long long* __restrict__ bytes_read) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (gw >= tl.warps) return;
@@ -408,10 +409,12 @@ __global__ void __launch_bounds__(256) k_rank1(T* __restrict__ D, int64_t ld, Ro
     a[v] = qv[v] < tl.n4 ? ld4<T>(rv + 4 * qv[v]) : Vec4<T>{I, I, I, I};
     if (TWO) b[v] = qv[v] < tl.n4 ? ld4<T>(rv2 + 4 * qv[v]) : Vec4<T>{I, I, I, I};
   }
+  int64_t rows_read = 0;
   for (int64_t i = i_lo; i < i_hi; ++i) {
     const T ci = c[i];
     const T ci2 = TWO ? c2[i] : I;
     if (!Tr<T>::fin(ci) && !Tr<T>::fin(ci2)) continue;   // row cannot change
+    ++rows_read;
     T* row = D + (i - r.row0) * ld;
     Vec4<T> d[VPL];
 #pragma unroll
@@ -435,17 +438,21 @@ __global__ void __launch_bounds__(256) k_rank1(T* __restrict__ D, int64_t ld, Ro
         st4<T>(row + 4 * qv[v], o);
     }
   }
+  if (bytes_read && lane == 0 && rows_read) {
+    const int64_t cols = min((int64_t)CHUNK_VEC * 4, n - (int64_t)chunk * CHUNK_VEC * 4);
+    atomicAdd(bytes_read, (unsigned long long)(rows_read * cols * (int64_t)sizeof(T)));
+  }
 }
 template <typename T>
 cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, const T* c2,
-                  const T* rv2, cudaStream_t st) {
+                  const T* rv2, unsigned long long* bytes_read, cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
   Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20);
   int grid = (int)cdiv(tl.warps, 8);
   if (c2)
-    k_rank1<T, true><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, c2, rv2);
+    k_rank1<T, true><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, c2, rv2, bytes_read);
   else
-    k_rank1<T, false><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, nullptr, nullptr);
+    k_rank1<T, false><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, nullptr, nullptr, bytes_read);
   return cudaGetLastError();
 }
 
@@ -639,13 +646,8 @@ __global__ void __launch_bounds__(DT_THREADS) k_detect_emit(DetectArgs<T> a,
 
 template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
-                   const T* c2, const T* r2, float tau, const T* WT, int64_t ldw, int reset,
-                   int64_t* rowoff, int* rowcnt, int* prow, int* pcol, T* plb, int64_t lcap,
-                   DetectCounters* ctr, uint32_t* bm, int* anyrow, int grid, cudaStream_t st) {
+                   const T* c2, const T* r2, float tau, uint32_t* bm, int* anyrow, cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
-  DetectArgs<T> a{D, ld, r, n, skip, c1, r1, c2, r2, tau, WT, ldw, reset,
-                  rowoff, rowcnt, prow, pcol, plb, lcap, ctr};
-  (void)grid;
   Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20);
   const int64_t bmld = (int64_t)tl.nchunk * 32;
   CUDA_TRY(cudaMemsetAsync(anyrow + r.lo, 0, sizeof(int) * (size_t)(r.hi - r.lo), st));
@@ -655,7 +657,18 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
   else
     k_detect_stream<T, false><<<g1, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, nullptr, nullptr, tau, bm,
                                                   bmld, anyrow);
-  CUDA_TRY(cudaGetLastError());
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t detect_emit(T* D, int64_t ld, Rows r, int64_t n, const T* WT, int64_t ldw, int reset,
+                        int64_t* rowoff, int* rowcnt, int* prow, int* pcol, T* plb, int64_t lcap,
+                        DetectCounters* ctr, const uint32_t* bm, const int* anyrow, cudaStream_t st) {
+  if (r.hi <= r.lo) return cudaSuccess;
+  Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20);
+  const int64_t bmld = (int64_t)tl.nchunk * 32;
+  DetectArgs<T> a{D, ld, r, n, -1, nullptr, nullptr, nullptr, nullptr, 0.f, WT, ldw, reset,
+                  rowoff, rowcnt, prow, pcol, plb, lcap, ctr};
   const int g2 = (int)std::min<int64_t>(r.hi - r.lo, (int64_t)num_sms() * 8);
   k_detect_emit<T><<<g2, DT_THREADS, 0, st>>>(a, bm, bmld, (int)bmld, anyrow);
   return cudaGetLastError();
@@ -754,13 +767,14 @@ cudaError_t set_edge(T* WT, int64_t ldw, int64_t u, int64_t v, T w, int directed
   template cudaError_t addnode_finish<T>(const T*, const T*, int, const T*, int, int64_t, Rows,    \
                                          int64_t, int64_t, T*, T*, T*, cudaStream_t);             \
   template cudaError_t rank1<T>(T*, int64_t, Rows, int64_t, const T*, const T*, const T*,          \
-                                const T*, cudaStream_t);                                          \
+                                const T*, unsigned long long*, cudaStream_t);                     \
   template cudaError_t addnode_write<T>(T*, int64_t, Rows, int64_t, int64_t, int, const T*,        \
                                         const T*, T*, int64_t, const T*, const T*, cudaStream_t); \
   template cudaError_t detect<T>(T*, int64_t, Rows, int64_t, int64_t, const T*, const T*,          \
-                                 const T*, const T*, float, const T*, int64_t, int, int64_t*,     \
-                                 int*, int*, int*, T*, int64_t, DetectCounters*, uint32_t*, int*, \
-                                 int, cudaStream_t);                                              \
+                                 const T*, const T*, float, uint32_t*, int*, cudaStream_t);       \
+  template cudaError_t detect_emit<T>(T*, int64_t, Rows, int64_t, const T*, int64_t, int,          \
+                                      int64_t*, int*, int*, int*, T*, int64_t, DetectCounters*,    \
+                                      const uint32_t*, const int*, cudaStream_t);                 \
   template cudaError_t tombstone<T>(T*, int64_t, Rows, int64_t, int64_t, T*, int64_t,              \
                                     cudaStream_t);                                                \
   template cudaError_t copy_row<T>(T*, const T*, int64_t, cudaStream_t);                           \

@@ -358,6 +358,7 @@ def main():
         try:
             with open(tpath) as f:
                 traffic = json.load(f).get(dom)
+            traffic = traffic if isinstance(traffic, (int, float)) else None
         except Exception:
             traffic = None
     if dom.startswith("fw"):

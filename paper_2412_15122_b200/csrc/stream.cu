@@ -536,15 +536,17 @@ __device__ __forceinline__ unsigned flag_nibble(const Vec4<T>& d, const Vec4<T>&
 //      words, block scan, one atomic for the row's list offset, then decode
 //      the flagged columns into the list (prow/pcol/plb) and reset D0.
 // ---------------------------------------------------------------------------
+constexpr int DS_V = 4;              // vectors per lane per row
+constexpr int DS_VEC = 32 * DS_V;    // vectors per chunk (512 columns)
 template <typename T, bool TWO>
-__global__ void __launch_bounds__(256) k_detect_stream(const T* __restrict__ D, int64_t ld, Rows r,
-                                                       int64_t n, int64_t skip, Tiling tl,
-                                                       const T* __restrict__ c1,
-                                                       const T* __restrict__ r1,
-                                                       const T* __restrict__ c2,
-                                                       const T* __restrict__ r2, float tau,
-                                                       uint32_t* __restrict__ bm, int64_t bmld,
-                                                       int* __restrict__ anyrow) {
+__global__ void __launch_bounds__(256, 2) k_detect_stream(const T* __restrict__ D, int64_t ld, Rows r,
+                                                          int64_t n, int64_t skip, Tiling tl,
+                                                          const T* __restrict__ c1,
+                                                          const T* __restrict__ r1,
+                                                          const T* __restrict__ c2,
+                                                          const T* __restrict__ r2, float tau,
+                                                          uint16_t* __restrict__ bm, int64_t bmld,
+                                                          int* __restrict__ anyrow) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (gw >= tl.warps) return;
@@ -553,36 +555,51 @@ __global__ void __launch_bounds__(256) k_detect_stream(const T* __restrict__ D, 
   const int64_t i_lo = r.lo + slab * tl.slab;
   const int64_t i_hi = min(r.hi, i_lo + tl.slab);
   const T I = Tr<T>::inf();
-  int64_t qv[VPL];
-  Vec4<T> a[VPL], b[VPL];
+  int64_t qv[DS_V];
+  Vec4<T> a[DS_V], b[DS_V];
 #pragma unroll
-  for (int v = 0; v < VPL; ++v) {
-    qv[v] = (int64_t)chunk * CHUNK_VEC + v * 32 + lane;
+  for (int v = 0; v < DS_V; ++v) {
+    qv[v] = (int64_t)chunk * DS_VEC + v * 32 + lane;
     a[v] = qv[v] < tl.n4 ? ld4<T>(r1 + 4 * qv[v]) : Vec4<T>{I, I, I, I};
     if (TWO) b[v] = qv[v] < tl.n4 ? ld4<T>(r2 + 4 * qv[v]) : Vec4<T>{I, I, I, I};
   }
-  for (int64_t i = i_lo; i < i_hi; ++i) {
-    if (i == skip) continue;
-    const T ci = c1[i];
-    const T ci2 = TWO ? c2[i] : I;
-    if (!Tr<T>::fin(ci) && !Tr<T>::fin(ci2)) continue;   // no pair of this row can be tight
-    const T* row = D + (i - r.row0) * ld;
-    Vec4<T> d[VPL];
+  for (int64_t i0 = i_lo; i0 < i_hi; i0 += 2) {
+    // two rows in flight per lane; a row that cannot be tight is not read
+    bool act[2];
+    T ci[2], cj[2];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v)
-      d[v] = qv[v] < tl.n4 ? ld4_stream<T>(row + 4 * qv[v]) : Vec4<T>{I, I, I, I};
-    uint32_t word = 0;
+    for (int h = 0; h < 2; ++h) {
+      const int64_t i = i0 + h;
+      ci[h] = (i < i_hi) ? c1[i] : I;
+      cj[h] = (TWO && i < i_hi) ? c2[i] : I;
+      act[h] = i < i_hi && i != skip && (Tr<T>::fin(ci[h]) || Tr<T>::fin(cj[h]));
+    }
+    Vec4<T> d[2][DS_V];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v)
-      word |= flag_nibble<T, TWO>(d[v], a[v], b[v], ci, ci2, 4 * qv[v], n, i, skip, tau) << (4 * v);
-    bm[(i - r.lo) * bmld + chunk * 32 + lane] = word;
-    if (__any_sync(0xffffffffu, word != 0) && lane == 0) anyrow[i] = 1;
+    for (int h = 0; h < 2; ++h) {
+      const T* row = D + (i0 + h - r.row0) * ld;
+#pragma unroll
+      for (int v = 0; v < DS_V; ++v)
+        d[h][v] = (act[h] && qv[v] < tl.n4) ? ld4_stream<T>(row + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (!act[h]) continue;
+      const int64_t i = i0 + h;
+      unsigned word = 0;
+#pragma unroll
+      for (int v = 0; v < DS_V; ++v)
+        word |= flag_nibble<T, TWO>(d[h][v], a[v], b[v], ci[h], cj[h], 4 * qv[v], n, i, skip, tau)
+                << (4 * v);
+      bm[(i - r.lo) * bmld + chunk * 32 + lane] = (uint16_t)word;
+      if (__any_sync(0xffffffffu, word != 0) && lane == 0) anyrow[i] = 1;
+    }
   }
 }
 
 template <typename T>
 __global__ void __launch_bounds__(DT_THREADS) k_detect_emit(DetectArgs<T> a,
-                                                            const uint32_t* __restrict__ bm,
+                                                            const uint16_t* __restrict__ bm,
                                                             int64_t bmld, int nwords,
                                                             const int* __restrict__ anyrow) {
   __shared__ int s_warp[DT_THREADS / 32];
@@ -590,7 +607,7 @@ __global__ void __launch_bounds__(DT_THREADS) k_detect_emit(DetectArgs<T> a,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int64_t i = a.r.lo + blockIdx.x; i < a.r.hi; i += gridDim.x) {
     if (!anyrow[i]) continue;
-    const uint32_t* brow = bm + (i - a.r.lo) * bmld;
+    const uint16_t* brow = bm + (i - a.r.lo) * bmld;
     T* Drow = a.D + (i - a.r.row0) * a.ld;
     const int wpt = (nwords + DT_THREADS - 1) / DT_THREADS;
     const int w0 = min(tid * wpt, nwords), w1 = min(w0 + wpt, nwords);
@@ -630,7 +647,7 @@ __global__ void __launch_bounds__(DT_THREADS) k_detect_emit(DetectArgs<T> a,
       while (bits) {
         const int bit = __ffs(bits) - 1;
         bits &= bits - 1;
-        const int64_t j = 4 * ((int64_t)chunk * CHUNK_VEC + (bit >> 2) * 32 + ln) + (bit & 3);
+        const int64_t j = 4 * ((int64_t)chunk * DS_VEC + (bit >> 2) * 32 + ln) + (bit & 3);
         if (store) {
           a.pcol[pos] = (int)j;
           a.prow[pos] = (int)i;
@@ -646,9 +663,10 @@ __global__ void __launch_bounds__(DT_THREADS) k_detect_emit(DetectArgs<T> a,
 
 template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
-                   const T* c2, const T* r2, float tau, uint32_t* bm, int* anyrow, cudaStream_t st) {
+                   const T* c2, const T* r2, float tau, uint32_t* bm32, int* anyrow, cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
-  Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20);
+  uint16_t* bm = reinterpret_cast<uint16_t*>(bm32);
+  Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20, DS_VEC, 32);
   const int64_t bmld = (int64_t)tl.nchunk * 32;
   CUDA_TRY(cudaMemsetAsync(anyrow + r.lo, 0, sizeof(int) * (size_t)(r.hi - r.lo), st));
   const int g1 = (int)cdiv(tl.warps, 8);
@@ -665,12 +683,13 @@ cudaError_t detect_emit(T* D, int64_t ld, Rows r, int64_t n, const T* WT, int64_
                         int64_t* rowoff, int* rowcnt, int* prow, int* pcol, T* plb, int64_t lcap,
                         DetectCounters* ctr, const uint32_t* bm, const int* anyrow, cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
-  Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20);
+  Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20, DS_VEC, 32);
   const int64_t bmld = (int64_t)tl.nchunk * 32;
   DetectArgs<T> a{D, ld, r, n, -1, nullptr, nullptr, nullptr, nullptr, 0.f, WT, ldw, reset,
                   rowoff, rowcnt, prow, pcol, plb, lcap, ctr};
   const int g2 = (int)std::min<int64_t>(r.hi - r.lo, (int64_t)num_sms() * 8);
-  k_detect_emit<T><<<g2, DT_THREADS, 0, st>>>(a, bm, bmld, (int)bmld, anyrow);
+  k_detect_emit<T><<<g2, DT_THREADS, 0, st>>>(a, reinterpret_cast<const uint16_t*>(bm), bmld,
+                                              (int)bmld, anyrow);
   return cudaGetLastError();
 }
 

@@ -91,7 +91,8 @@ typedef enum {
 
 /* Statistics of one update. */
 typedef struct {
-  int32_t kind;        /* 0 no-op, 1 edge decrease, 2 edge increase, 3 add node, 4 remove node */
+  int32_t kind;        /* 0 no-op, 1 edge decrease, 2 edge increase, 3 add node, 4 remove node,
+                          5 edge modified by remove + re-add (apsp_modify_edge_readd) */
   int32_t early_exit;  /* 1: an O(1) tightness test proved no distance changes */
   int32_t path;        /* 0 none, 1 rank-1 relaxation, 2 sparse recompute, 3 dense FW */
   int32_t rounds;      /* sparse-recompute rounds run (path 2) */
@@ -170,6 +171,21 @@ apsp_status apsp_remove_node(apsp_handle* h, int64_t k, int64_t* moved_from,
 apsp_status apsp_update_edge(apsp_handle* h, int64_t u, int64_t v, double w_new,
                              apsp_update_info* info);
 
+/* Edge modification by the paper's own algorithm (alg:APSPmodify):
+ * "It firstly remove a node associated with the edge from the graph, then add
+ * the node back, with the edge being updated ... it calculates which node is
+ * cheaper to remove, then remove the cheaper one."  The removal cost of both
+ * endpoints is Definition 1 (Phi/(N-1), need_update_lists counted
+ * on the GPU); ties go to the smaller index.  The chosen endpoint
+ * is removed (remove_node), re-added with its edge vectors including the
+ * edited edge (add_node), and swapped back into its original slot so node
+ * ids are stable.  Same result as apsp_update_edge (D is unique); this is the
+ * paper-faithful composition, kept for comparison.  info->kind = 5,
+ * info->cost = the removed endpoint's cost, *removed = that endpoint (may be
+ * NULL).  Errors as apsp_update_edge; E_PRECOND when n < 3. */
+apsp_status apsp_modify_edge_readd(apsp_handle* h, int64_t u, int64_t v, double w_new,
+                                   int64_t* removed, apsp_update_info* info);
+
 /* Warm single-pair shortest path (alg:sp_apsp): candidate_node_list
  * by Theorem 4 (nodes k with D[s][k] + D[k][t] = D[s][t]), then Dijkstra on
  * the induced small graph, path in original ids.
@@ -189,6 +205,10 @@ apsp_status sp_pair_query(apsp_handle* h, int64_t s, int64_t t, void* dist, int3
 apsp_status sp_pair_query_batch(apsp_handle* h, int32_t q, const int32_t* s, const int32_t* t,
                                 void* dist, int32_t* paths, int32_t path_cap,
                                 int32_t* path_lens, int32_t* n_cand);
+
+/* Current weight w(u -> v) (host, 4 bytes of the handle's dtype; INF if
+ * absent).  Synchronises the stream.  E_RANGE for ids outside [0, n). */
+apsp_status apsp_get_weight(apsp_handle* h, int64_t u, int64_t v, void* w);
 
 /* Current node count n. */
 int64_t apsp_size(const apsp_handle* h);

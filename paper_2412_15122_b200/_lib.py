@@ -27,7 +27,7 @@ SYMBOLS = [
     "apsp_cold_fw", "apsp_add_node", "apsp_remove_node", "apsp_update_edge", "sp_pair_query",
     "sp_pair_query_batch", "apsp_size", "apsp_last_error", "apsp_status_string",
     "apsp_nccl_unique_id", "apsp_kernel_launches", "apsp_profile_enable", "apsp_profile_reset",
-    "apsp_profile_read",
+    "apsp_profile_read", "apsp_modify_edge_readd", "apsp_get_weight",
 ]
 # kernel classes of apsp_profile_read (apsp_kernel_class)
 K_CLASSES = ["fw_diag", "fw_panel", "fw_tile", "add_pass1", "rank1", "detect", "sparse0",
@@ -71,9 +71,11 @@ def _load():
         "apsp_add_node": (ctypes.c_int, [vp, vp, vp, P(i64), P(UpdateInfo)]),
         "apsp_remove_node": (ctypes.c_int, [vp, i64, P(i64), P(UpdateInfo)]),
         "apsp_update_edge": (ctypes.c_int, [vp, i64, i64, dbl, P(UpdateInfo)]),
+        "apsp_modify_edge_readd": (ctypes.c_int, [vp, i64, i64, dbl, P(i64), P(UpdateInfo)]),
         "sp_pair_query": (ctypes.c_int, [vp, i64, i64, vp, P(i32), i32, P(i32), P(i32)]),
         "sp_pair_query_batch": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, i32, vp, vp]),
         "apsp_size": (i64, [vp]),
+        "apsp_get_weight": (ctypes.c_int, [vp, i64, i64, vp]),
         "apsp_last_error": (ctypes.c_char_p, [vp]),
         "apsp_status_string": (ctypes.c_char_p, [ctypes.c_int]),
         "apsp_nccl_unique_id": (ctypes.c_int, [vp]),
@@ -153,6 +155,13 @@ def apsp_update_edge(h, u, v, w_new):
     return info
 
 
+def apsp_modify_edge_readd(h, u, v, w_new):
+    removed = ctypes.c_int64(-1)
+    info = UpdateInfo()
+    check(h, lib.apsp_modify_edge_readd(h, u, v, float(w_new), ctypes.byref(removed), ctypes.byref(info)))
+    return removed.value, info
+
+
 def sp_pair_query(h, s, t, dtype, path_cap=4096):
     dist = ctypes.c_int32() if dtype == APSP_I32 else ctypes.c_float()
     path = (ctypes.c_int32 * max(path_cap, 1))()
@@ -164,6 +173,12 @@ def sp_pair_query(h, s, t, dtype, path_cap=4096):
 
 def sp_pair_query_batch(h, q, s_ptr, t_ptr, dist_ptr, paths_ptr, path_cap, lens_ptr, ncand_ptr):
     check(h, lib.sp_pair_query_batch(h, q, s_ptr, t_ptr, dist_ptr, paths_ptr, path_cap, lens_ptr, ncand_ptr))
+
+
+def apsp_get_weight(h, u, v, dtype):
+    w = ctypes.c_int32() if dtype == APSP_I32 else ctypes.c_float()
+    check(h, lib.apsp_get_weight(h, u, v, ctypes.byref(w)))
+    return w.value
 
 
 def apsp_size(h):

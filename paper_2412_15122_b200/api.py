@@ -103,6 +103,15 @@ class WarmAPSP:
     def update_edge(self, u, v, w_new):
         return L.apsp_update_edge(self.h, int(u), int(v), float(w_new))
 
+    def modify_edge_readd(self, u, v, w_new):
+        """The paper's alg:APSPmodify: remove the cheaper endpoint,
+        re-add it with the edited edge.  Returns (removed endpoint, info)."""
+        return L.apsp_modify_edge_readd(self.h, int(u), int(v), float(w_new))
+
+    def weight(self, u, v):
+        """Current w(u -> v) as held on the device (WT)."""
+        return L.apsp_get_weight(self.h, int(u), int(v), self.cdtype)
+
     def query(self, s, t, path_cap=4096):
         return L.sp_pair_query(self.h, int(s), int(t), self.cdtype, path_cap)
 

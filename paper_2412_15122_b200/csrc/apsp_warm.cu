@@ -655,6 +655,113 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
   return recompute<T>(h, -1, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, false, info);
 }
 
+// ------------------------------------------------------------------ f1: paper-faithful modify
+// Definition 1's Phi for removing node k: rows with a non-empty need_update_list
+// (P:184-194), counted from the detection bitmap's row marks.
+template <typename T>
+apsp_status removal_phi(apsp_handle* h, int64_t k, int64_t* phi) {
+  const int64_t n = h->n, ld = h->ld;
+  Rows r = h->active();
+  T* c1 = h->vec<T>(4);
+  T* r1 = h->vec<T>(5);
+  CK(gather_col<T>(h->Dl<T>(), ld, r, k, T(0), c1, h->st));
+  apsp_status s = snap_row<T>(h, k, T(0), r1);
+  if (s != APSP_OK) return s;
+  PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
+     detect<T>(h->Dl<T>(), ld, r, n, k, c1, r1, nullptr, nullptr, h->tau, h->bm(), h->anyrow(), h->st));
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(h->small() + 128);
+  CKR(cudaMemsetAsync(cnt, 0, sizeof *cnt, h->st));
+  CK(count_nonzero(h->anyrow() + r.lo, r.hi - r.lo, cnt, h->st));
+  if (h->world > 1)
+    NK(g_nccl.AllReduce(cnt, cnt, 1, ncclUint64, ncclSum, h->comm, h->st));
+  unsigned long long* hv = reinterpret_cast<unsigned long long*>(h->host_small);
+  CKR(cudaMemcpyAsync(hv, cnt, sizeof *cnt, cudaMemcpyDeviceToHost, h->st));
+  CKR(cudaStreamSynchronize(h->st));
+  *phi = (int64_t)*hv;
+  return APSP_OK;
+}
+
+// Exchange the ids of nodes p and q (rows and columns of D and WT, shortlists).
+template <typename T>
+apsp_status swap_nodes(apsp_handle* h, int64_t p, int64_t q) {
+  const int64_t n = h->n, ld = h->ld;
+  const bool lp = h->local(p), lq = h->local(q);
+  if (lp && lq) {
+    CK(swap_vecs<T>(h->Drow<T>(p), h->Drow<T>(q), n, h->st));
+  } else if (lp || lq) {
+    T* mine = lp ? h->Drow<T>(p) : h->Drow<T>(q);
+    const int peer = h->owner(lp ? q : p);
+    T* tmp = h->panel<T>();
+    NK(g_nccl.GroupStart());
+    NK(g_nccl.Send(mine, (size_t)n, nccl_type<T>(), peer, h->comm, h->st));
+    NK(g_nccl.Recv(tmp, (size_t)n, nccl_type<T>(), peer, h->comm, h->st));
+    NK(g_nccl.GroupEnd());
+    CK(copy_row<T>(mine, tmp, n, h->st));
+  }
+  CK(swap_cols<T>(h->Dl<T>(), ld, h->active(), p, q, h->st));
+  T* WT = h->WT<T>();
+  CK(swap_vecs<T>(WT + p * ld, WT + q * ld, n, h->st));
+  Rows rw{0, n, 0};
+  CK(swap_cols<T>(WT, ld, rw, p, q, h->st));
+  CK(shortlist_swap<T>(h->slid(), h->slw<T>(), h->wnext<T>(), n, p, q, h->st));
+  return APSP_OK;
+}
+
+template <typename T>
+apsp_status modify_readd_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, int64_t* removed,
+                              apsp_update_info* info) {
+  const int64_t n = h->n, ld = h->ld;
+  T* WT = h->WT<T>();
+  T* hv = reinterpret_cast<T*>(h->host_small);
+  CKR(cudaMemcpyAsync(hv, WT + v * ld + u, sizeof(T), cudaMemcpyDeviceToHost, h->st));
+  CKR(cudaStreamSynchronize(h->st));
+  if (info) info->n_after = n;
+  if (hv[0] == w_new) {
+    if (info) { info->kind = 0; info->early_exit = 1; }
+    return APSP_OK;
+  }
+  // "it calculates which node is cheaper to remove, then remove the cheaper one"
+  int64_t phi_u = 0, phi_v = 0;
+  apsp_status s = removal_phi<T>(h, u, &phi_u);
+  if (s != APSP_OK) return s;
+  s = removal_phi<T>(h, v, &phi_v);
+  if (s != APSP_OK) return s;
+  const int64_t p = (phi_u < phi_v || (phi_u == phi_v && u < v)) ? u : v;
+  const int64_t other = p == u ? v : u;
+  // p's edge vectors with the edited edge: out[t] = W[p][t], in[t] = W[t][p]
+  T* so = h->vec<T>(2);
+  T* si = h->vec<T>(3);
+  Rows rw{0, n, 0};
+  CK(gather_col<T>(WT, ld, rw, p, T(0), so, h->st));
+  CK(copy_vec<T>(WT + p * ld, n, ld, T(0), si, h->st));
+  if (!h->directed || p == u) CK(vec_set_move<T>(so, other, w_new, -1, 0, h->st));
+  if (!h->directed || p == v) CK(vec_set_move<T>(si, other, w_new, -1, 0, h->st));
+  const int64_t last = n - 1;
+  if (p != last) {   // after the removal node `last` lives in slot p
+    CK(vec_set_move<T>(so, -1, T(0), p, last, h->st));
+    CK(vec_set_move<T>(si, -1, T(0), p, last, h->st));
+  }
+  int64_t mf = -1;
+  apsp_update_info rinfo;
+  std::memset(&rinfo, 0, sizeof rinfo);
+  s = remove_node_impl<T>(h, p, &mf, &rinfo);
+  if (s != APSP_OK) return s;
+  int64_t x = -1;
+  s = add_node_impl<T>(h, so, si, &x, nullptr);
+  if (s != APSP_OK) return s;
+  if (p != last) {
+    s = swap_nodes<T>(h, p, x);   // restore the original ids
+    if (s != APSP_OK) return s;
+  }
+  if (removed) *removed = p;
+  if (info) {
+    *info = rinfo;
+    info->kind = 5;
+    info->n_after = h->n;
+  }
+  return APSP_OK;
+}
+
 // ------------------------------------------------------------------ query
 template <typename T>
 apsp_status query_one(apsp_handle* h, int64_t s, int64_t t, void* dist, int32_t* path,
@@ -885,6 +992,25 @@ apsp_status apsp_update_edge(apsp_handle* h, int64_t u, int64_t v, double w_new,
   return update_edge_impl<float>(h, u, v, w, info);
 }
 
+apsp_status apsp_modify_edge_readd(apsp_handle* h, int64_t u, int64_t v, double w_new,
+                                   int64_t* removed, apsp_update_info* info) {
+  CHECK_HANDLE(h);
+  if (info) std::memset(info, 0, sizeof *info);
+  if (u < 0 || u >= h->n || v < 0 || v >= h->n)
+    return fail(h, APSP_E_RANGE, "modify_edge_readd: (%lld,%lld) outside [0,%lld)", (long long)u, (long long)v, (long long)h->n);
+  if (u == v) return fail(h, APSP_E_INVAL, "modify_edge_readd: u == v");
+  if (std::isnan(w_new) || w_new < 0) return fail(h, APSP_E_INVAL, "modify_edge_readd: negative or NaN weight");
+  if (h->n < 3) return fail(h, APSP_E_PRECOND, "modify_edge_readd: needs n >= 3");
+  if (h->dt == APSP_I32) {
+    if (std::isfinite(w_new) && w_new != std::floor(w_new))
+      return fail(h, APSP_E_INVAL, "modify_edge_readd: non-integral weight on an int32 handle");
+    int32_t w = (w_new >= (double)APSP_INF_I32) ? APSP_INF_I32 : (int32_t)w_new;
+    return modify_readd_impl<int32_t>(h, u, v, w, removed, info);
+  }
+  float w = std::isinf(w_new) ? Tr<float>::inf() : (float)w_new;
+  return modify_readd_impl<float>(h, u, v, w, removed, info);
+}
+
 apsp_status sp_pair_query(apsp_handle* h, int64_t s, int64_t t, void* dist, int32_t* path,
                           int32_t path_cap, int32_t* path_len, int32_t* n_candidates) {
   CHECK_HANDLE(h);
@@ -909,6 +1035,18 @@ apsp_status sp_pair_query_batch(apsp_handle* h, int32_t q, const int32_t* s, con
                       paths, path_cap, path_lens, n_cand, h->tau, h->st));
     return APSP_OK;
   });
+}
+
+apsp_status apsp_get_weight(apsp_handle* h, int64_t u, int64_t v, void* w) {
+  CHECK_HANDLE(h);
+  if (!w) return fail(h, APSP_E_INVAL, "get_weight: null output");
+  if (u < 0 || u >= h->n || v < 0 || v >= h->n) return fail(h, APSP_E_RANGE, "get_weight: id out of range");
+  const size_t es = 4;
+  CKR(cudaMemcpyAsync(h->host_small, h->ws + h->plan.off_wt + (size_t)(v * h->ld + u) * es, es,
+                      cudaMemcpyDeviceToHost, h->st));
+  CKR(cudaStreamSynchronize(h->st));
+  std::memcpy(w, h->host_small, es);
+  return APSP_OK;
 }
 
 int64_t apsp_size(const apsp_handle* h) { return h ? h->n : -1; }

@@ -83,6 +83,16 @@ template <typename T>
 cudaError_t fill_col(T* D, int64_t ld, Rows r, int64_t col, T v, cudaStream_t st);
 template <typename T>
 cudaError_t set_edge(T* WT, int64_t ldw, int64_t u, int64_t v, T w, int directed, cudaStream_t st);
+cudaError_t count_nonzero(const int* a, int64_t m, unsigned long long* out, cudaStream_t st);
+template <typename T>
+cudaError_t vec_set_move(T* v, int64_t set_i, T set_v, int64_t dst, int64_t src, cudaStream_t st);
+template <typename T>
+cudaError_t swap_vecs(T* a, T* b, int64_t n, cudaStream_t st);
+template <typename T>
+cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream_t st);
+template <typename T>
+cudaError_t shortlist_swap(int* SLid, T* SLw, T* wnext, int64_t n, int64_t p, int64_t q,
+                           cudaStream_t st);
 
 // ---------------- sparse.cu ----------------
 constexpr int kSLK = 16;              // shortlist entries per lane

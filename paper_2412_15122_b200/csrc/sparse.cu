@@ -294,6 +294,45 @@ struct OpenLists {
   }
 };
 
+// Swap the ids of nodes p and q in every shortlist (rows and entries).
+template <typename T>
+__global__ void k_shortlist_swap(int* SLid, T* SLw, T* wnext, int64_t n, int p, int q) {
+  const int64_t tot = n * kSL;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / kSL;
+    if (row == p || row == q) continue;
+    const int id = SLid[e];
+    if (id == p) SLid[e] = q;
+    else if (id == q) SLid[e] = p;
+  }
+}
+template <typename T>
+__global__ void k_shortlist_swap_rows(int* SLid, T* SLw, T* wnext, int p, int q) {
+  for (int t = threadIdx.x; t < kSL; t += blockDim.x) {
+    const int64_t a = (int64_t)p * kSL + t, b = (int64_t)q * kSL + t;
+    int ia = SLid[a], ib = SLid[b];
+    T wa = SLw[a], wb = SLw[b];
+    ia = ia == p ? q : ia == q ? p : ia;
+    ib = ib == p ? q : ib == q ? p : ib;
+    SLid[a] = ib; SLw[a] = wb;
+    SLid[b] = ia; SLw[b] = wa;
+  }
+  if (threadIdx.x == 0) {
+    T x = wnext[p];
+    wnext[p] = wnext[q];
+    wnext[q] = x;
+  }
+}
+template <typename T>
+cudaError_t shortlist_swap(int* SLid, T* SLw, T* wnext, int64_t n, int64_t p, int64_t q,
+                           cudaStream_t st) {
+  int grid = (int)std::min<int64_t>(cdiv(n * kSL, 256), 8 * num_sms());
+  k_shortlist_swap<T><<<grid, 256, 0, st>>>(SLid, SLw, wnext, n, (int)p, (int)q);
+  k_shortlist_swap_rows<T><<<1, 256, 0, st>>>(SLid, SLw, wnext, (int)p, (int)q);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // phase A / A2: shortlist evaluation of a list of pairs
 //   classify = 0 (phase A, all listed pairs):   out = 0 final (reached lb), 1 open
@@ -653,6 +692,7 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
   template cudaError_t shortlist_build_one<T>(const T*, int64_t, int64_t, int64_t, int*, T*, T*,   \
                                               cudaStream_t);                                      \
   template cudaError_t shortlist_set_edge<T>(int*, T*, T*, int64_t, int64_t, T, int, cudaStream_t); \
+  template cudaError_t shortlist_swap<T>(int*, T*, T*, int64_t, int64_t, int64_t, cudaStream_t);    \
   template cudaError_t shortlist_remove<T>(int*, T*, T*, int64_t, int64_t, int64_t, cudaStream_t); \
   template cudaError_t sparse_short<T>(T*, int64_t, int64_t, const int*, const T*, const T*,       \
                                        const int*, const int*, const T*, int64_t, unsigned char*,  \

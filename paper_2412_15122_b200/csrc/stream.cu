@@ -772,6 +772,69 @@ cudaError_t set_edge(T* WT, int64_t ldw, int64_t u, int64_t v, T w, int directed
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// helpers of the paper-faithful edge modification (remove + re-add + swap)
+// ---------------------------------------------------------------------------
+__global__ void k_count_nonzero(const int* a, int64_t m, unsigned long long* out) {
+  unsigned c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += a[i] != 0;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+cudaError_t count_nonzero(const int* a, int64_t m, unsigned long long* out, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  int grid = (int)std::min<int64_t>(cdiv(m, 256), 2 * num_sms());
+  k_count_nonzero<<<grid, 256, 0, st>>>(a, m, out);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void k_set_move(T* v, int64_t set_i, T set_v, int64_t dst, int64_t src) {
+  if (set_i >= 0) v[set_i] = set_v;
+  if (dst >= 0) v[dst] = v[src];
+}
+template <typename T>
+cudaError_t vec_set_move(T* v, int64_t set_i, T set_v, int64_t dst, int64_t src, cudaStream_t st) {
+  k_set_move<T><<<1, 1, 0, st>>>(v, set_i, set_v, dst, src);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void k_swap_vecs(T* a, T* b, int64_t n) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    T x = a[j];
+    a[j] = b[j];
+    b[j] = x;
+  }
+}
+template <typename T>
+cudaError_t swap_vecs(T* a, T* b, int64_t n, cudaStream_t st) {
+  int grid = (int)std::min<int64_t>(cdiv(n, 256), 4 * num_sms());
+  k_swap_vecs<T><<<grid, 256, 0, st>>>(a, b, n);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void k_swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q) {
+  for (int64_t i = r.lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.hi;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    T* row = D + (i - r.row0) * ld;
+    T x = row[p];
+    row[p] = row[q];
+    row[q] = x;
+  }
+}
+template <typename T>
+cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream_t st) {
+  if (r.hi <= r.lo) return cudaSuccess;
+  int grid = (int)std::min<int64_t>(cdiv(r.hi - r.lo, 256), 4 * num_sms());
+  k_swap_cols<T><<<grid, 256, 0, st>>>(D, ld, r, p, q);
+  return cudaGetLastError();
+}
+
 #define INST(T)                                                                                   \
   template cudaError_t validate_vec<T>(const T*, const T*, int64_t, int64_t, T*, unsigned int*,    \
                                        cudaStream_t);                                             \
@@ -799,7 +862,10 @@ cudaError_t set_edge(T* WT, int64_t ldw, int64_t u, int64_t v, T w, int directed
   template cudaError_t copy_row<T>(T*, const T*, int64_t, cudaStream_t);                           \
   template cudaError_t copy_col<T>(T*, int64_t, Rows, int64_t, int64_t, cudaStream_t);             \
   template cudaError_t fill_col<T>(T*, int64_t, Rows, int64_t, T, cudaStream_t);                   \
-  template cudaError_t set_edge<T>(T*, int64_t, int64_t, int64_t, T, int, cudaStream_t);
+  template cudaError_t set_edge<T>(T*, int64_t, int64_t, int64_t, T, int, cudaStream_t);        \
+  template cudaError_t vec_set_move<T>(T*, int64_t, T, int64_t, int64_t, cudaStream_t);           \
+  template cudaError_t swap_vecs<T>(T*, T*, int64_t, cudaStream_t);                               \
+  template cudaError_t swap_cols<T>(T*, int64_t, Rows, int64_t, int64_t, cudaStream_t);
 INST(int32_t)
 INST(float)
 #undef INST

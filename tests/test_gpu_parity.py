@@ -558,3 +558,42 @@ def test_create_rejects_bad_W(lib):
     W = np.array([[1, 1], [1, 0]], np.int32)
     with pytest.raises(P.ApspError):
         make(lib, W)
+
+
+# ------------------------------------------------------------------ f1: paper's modify (remove + re-add)
+@pytest.mark.parametrize("directed", [True, False])
+def test_modify_edge_readd_matches_oracle_and_direct(lib, rng, directed):
+    """alg:APSPmodify: remove the cheaper endpoint (Definition 1),
+    re-add it with the edited edge, ids restored; == oracle == direct update."""
+    n = 200
+    W = random_graph(rng, n, directed, 0.9, lo=1, hi=80)
+    a = make(lib, W, directed)
+    b = make(lib, W, directed)
+    for trial in range(8):
+        u, v = (int(x) for x in rng.choice(n, 2, replace=False))
+        if trial == 3:
+            u, v = n - 1, 0          # the endpoint may be the last node (no swap)
+        w_old = int(W[u, v])
+        w_new = min(INF, int(rng.choice([max(0, w_old // 3), w_old * 5, INF, w_old + 1])))
+        removed, info = a.modify_edge_readd(u, v, w_new)
+        assert a.weight(u, v) == w_new
+        b.update_edge(u, v, w_new)
+        W = _edit(W, u, v, w_new, directed)
+        if w_new != w_old:
+            assert info.kind == 5 and removed in (u, v)
+            assert a.n == n
+        Da = getD(a)
+        assert_parity(Da, oracle.fw(W))
+        assert np.array_equal(Da, getD(b))
+
+
+def test_modify_edge_readd_fp32(lib, rng):
+    spec = dataclasses.replace(synth.C2, n=150)
+    W = synth.graph(spec)
+    h = make(lib, W, directed=False)
+    for trial in range(4):
+        u, v = (int(x) for x in rng.choice(150, 2, replace=False))
+        w_new = np.float32(W[u, v] * np.float32(rng.choice([0.1, 10.0])))
+        h.modify_edge_readd(u, v, float(w_new))
+        W = _edit(W, u, v, w_new, False)
+        assert_parity(getD(h), oracle.fw(W))

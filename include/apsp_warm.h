@@ -86,7 +86,10 @@ typedef enum {
   APSP_OPT_FORCE_PATH = 0,  /* 0 auto, 1 sparse (a6), 2 dense (a7) — mirrors S:192 */
   APSP_OPT_THETA = 1,       /* gate: dense iff |A| > theta * n^2 (default 0.02)      */
   APSP_OPT_TAU = 2,         /* fp32 tie tolerance tau (default 1e-5), Q4   */
-  APSP_OPT_MAX_ROUNDS = 3   /* sparse rounds before switching to dense (default 64)  */
+  APSP_OPT_MAX_ROUNDS = 3,  /* sparse rounds before switching to dense (default 64)  */
+  APSP_OPT_ROW_DELTA = 4    /* > 0: use the paper's own gate instead — dense FW iff
+                               Definition 1's cost Phi/(N-1) > delta;
+                               0 (default): the pair-level gate of APSP_OPT_THETA    */
 } apsp_option;
 
 /* Statistics of one update. */

@@ -159,6 +159,7 @@ struct apsp_handle {
   double theta = 0.02;
   float tau = 1e-5f;
   int max_rounds = 64;
+  double row_delta = 0.0;        // > 0: the paper's Definition-1 gate (ablation)
   // state
   bool poisoned = false;
   std::string err;
@@ -404,9 +405,11 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     info->max_row_affected = maxrow;
     info->cost = removal ? (n > 1 ? (double)rows / (double)(n - 1) : 0.0) : (double)rows / (double)n;
   }
-  bool dense = h->force_path == 2 ||
-               (h->force_path == 0 && (double)total > h->theta * (double)n * (double)n) ||
-               overflow != 0;
+  const double cost = info ? info->cost
+                            : (removal ? (n > 1 ? (double)rows / (double)(n - 1) : 0.0) : (double)rows / n);
+  const bool gate = h->row_delta > 0 ? cost > h->row_delta   // paper: "Cost larger than delta"
+                                     : (double)total > h->theta * (double)n * (double)n;
+  bool dense = h->force_path == 2 || (h->force_path == 0 && gate) || overflow != 0;
   if (dense) {
     if (info) info->path = 3;
     return fw_impl<T>(h);
@@ -455,20 +458,25 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   int rounds = 0;
   bool converged = false;
   int* hflag = reinterpret_cast<int*>(h->host_small);
-  for (; !converged && rounds < h->max_rounds; ++rounds) {
-    CKR(cudaMemsetAsync(h->chg(in ^ 1), 0, sizeof(int) * h->cap, h->st));
-    CKR(cudaMemsetAsync(h->anyflag(), 0, sizeof(int), h->st));
-    if (nopen > 0)
-      PK(APSP_K_SPARSE_R, 0.0,
-         sparse_round<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->gprow(), h->gpcol(),
-                         h->glb<T>(), nopen, h->rowoff(), h->ocnt(), h->ocol(), h->chg(in),
-                         h->chg(in ^ 1), h->anyflag(), h->st));
+  // rounds are enqueued in batches of 4 between host convergence checks; a
+  // round after convergence only reads the (all-zero) row-change flags
+  while (!converged && rounds < h->max_rounds) {
+    const int batch = std::min(4, h->max_rounds - rounds);
+    for (int b = 0; b < batch; ++b, ++rounds) {
+      CKR(cudaMemsetAsync(h->chg(in ^ 1), 0, sizeof(int) * h->cap, h->st));
+      if (b == batch - 1) CKR(cudaMemsetAsync(h->anyflag(), 0, sizeof(int), h->st));
+      if (nopen > 0)
+        PK(APSP_K_SPARSE_R, 0.0,
+           sparse_round<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->gprow(), h->gpcol(),
+                           h->glb<T>(), nopen, h->rowoff(), h->ocnt(), h->ocol(), h->chg(in),
+                           h->chg(in ^ 1), h->anyflag(), h->st));
+      in ^= 1;
+    }
     if (h->world > 1)
       NK(g_nccl.AllReduce(h->anyflag(), h->anyflag(), 1, ncclInt32, ncclMax, h->comm, h->st));
     CKR(cudaMemcpyAsync(hflag, h->anyflag(), sizeof(int), cudaMemcpyDeviceToHost, h->st));
     CKR(cudaStreamSynchronize(h->st));
-    if (*hflag == 0) converged = true;
-    in ^= 1;
+    if (*hflag == 0) converged = true;   // the batch's last round changed nothing
   }
   if (info) info->rounds = rounds;
   if (!converged) {
@@ -948,6 +956,10 @@ apsp_status apsp_set_option(apsp_handle* h, apsp_option opt, double value) {
     case APSP_OPT_MAX_ROUNDS:
       if (!(value >= 1)) return APSP_E_INVAL;
       h->max_rounds = (int)value;
+      return APSP_OK;
+    case APSP_OPT_ROW_DELTA:
+      if (!(value >= 0) || value > 1) return APSP_E_INVAL;
+      h->row_delta = value;
       return APSP_OK;
   }
   return APSP_E_INVAL;

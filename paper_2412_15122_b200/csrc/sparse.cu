@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
       const int m = sid[q * 32 + lane];
       const T w = sw[q * 32 + lane];
       if (m >= 0) acc = Tr<T>::relax(acc, *(volatile T*)(Drow + m), w);
-      if (!classify && (q == 0 || q == 2 || q == 6) && warp_min<T>(acc) <= lbp) break;
+      if (!classify && (q == 0 || q == 2 || q == 6) && Tr<T>::at_lb(warp_min<T>(acc), lbp)) break;
     }
     acc = warp_min<T>(acc);
     if (lane == 0) {
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
       const T v = Tr<T>::mn(acc, cur);
       if (v < cur) Drow[j] = v;
       unsigned char st;
-      if (v <= lb) st = 0;
+      if (Tr<T>::at_lb(v, lb)) st = 0;
       else if (!classify || acc <= wnext[j]) st = 1;
       else st = 2;
       out[p] = st;
@@ -458,8 +458,9 @@ __global__ void __launch_bounds__(512) k_sparse_short_rows(T* D, int64_t ld, Row
         const T v = Tr<T>::mn(acc, cur);
         if (v < cur) Drow[j] = v;
         const T lb = plb[p];
-        out[p] = v <= lb ? 0 : 1;
-        if (v > lb) ol.append(i, j, lb);
+        const bool fin_ = Tr<T>::at_lb(v, lb);
+        out[p] = fin_ ? 0 : 1;
+        if (!fin_) ol.append(i, j, lb);
       }
     }
     __syncthreads();
@@ -612,7 +613,7 @@ __global__ void __launch_bounds__(256) k_sparse_full(T* D, int64_t ld, int64_t r
       acc = Tr<T>::relax(acc, d0.z, w0.z); acc = Tr<T>::relax(acc, d0.w, w0.w);
       acc = Tr<T>::relax(acc, d1.x, w1.x); acc = Tr<T>::relax(acc, d1.y, w1.y);
       acc = Tr<T>::relax(acc, d1.z, w1.z); acc = Tr<T>::relax(acc, d1.w, w1.w);
-      if ((iter & 7) == 0 && warp_min<T>(acc) <= lb) break;   // reached the lower bound: exact
+      if ((iter & 7) == 0 && Tr<T>::at_lb(warp_min<T>(acc), lb)) break;   // reached the lower bound
     }
     acc = warp_min<T>(acc);
     if (lane == 0) {
@@ -656,7 +657,7 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
     T cur = Tr<T>::inf();
     if (lane == 0) cur = *(volatile T*)(Drow + j);
     cur = __shfl_sync(0xffffffffu, cur, 0);  // one value for the whole warp (others may write)
-    if (cur <= glb[p]) continue;             // already at its lower bound: final
+    if (Tr<T>::at_lb(cur, glb[p])) continue;   // already at its lower bound: final
     const int64_t off = rowoff[i];
     const T* Wrow = WT + j * ldw;
     T acc = Tr<T>::inf();

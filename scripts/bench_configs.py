@@ -159,8 +159,33 @@ def c5():
     emit("c5", "query_single", [t4], n)
 
 
+def c4f1():
+    """f1 ablation at BJ.c4's size: the paper's edge modification (remove the
+    cheaper endpoint + re-add) vs the direct decrease/increase path,
+    on the same random reweights (factor in [0.1, 10]) and on tight edges."""
+    spec = synth.C4
+    n = spec.n
+    W = synth.graph(spec)
+    h = P.WarmAPSP(torch.from_numpy(W), directed=True)
+    D0 = h.D_local[:n, :n].clone()
+    del h
+    hg = synth.HostGraph.__new__(synth.HostGraph)
+    hg.buf, hg.n, hg.inf, hg.directed, hg.dtype = W, n, INF, True, W.dtype
+    edges = []
+    for t in range(3):
+        u, v = synth.random_edge(spec.seed, 1000 + t, hg)
+        edges.append(("random", u, v, synth.new_weight(W[u, v], synth.reweight_factor(spec.seed, 1000 + t), W.dtype)))
+    for t in range(2):
+        u = 31 + 977 * t
+        v = tight_in(W, u)
+        edges.append(("tight_x10", u, v, int(W[u, v]) * 10))
+    for kind, u, v, w in edges:
+        repeat_update("c4", f"modify_readd_{kind}", W, True, D0, lambda h: h.modify_edge_readd(u, v, w)[1], R=2)
+        repeat_update("c4", f"update_edge_{kind}", W, True, D0, lambda h: h.update_edge(u, v, w), R=2)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["c1", "c2", "c3", "c5"]
+    which = sys.argv[1:] or ["c1", "c2", "c3", "c5", "c4f1"]
     for c in which:
         globals()[c]()
         torch.cuda.empty_cache()

@@ -597,3 +597,24 @@ def test_modify_edge_readd_fp32(lib, rng):
         h.modify_edge_readd(u, v, float(w_new))
         W = _edit(W, u, v, w_new, False)
         assert_parity(getD(h), oracle.fw(W))
+
+
+def test_row_delta_gate_paper_definition1(lib, rng):
+    """f4 ablation: the paper's gate (dense FW iff Definition 1's cost > delta,
+    P:184-196) picks the path; results are identical either way."""
+    n = 220
+    W = random_graph(rng, n, True, 1.0, lo=1, hi=100)
+    a = make(lib, W)
+    b = make(lib, W)
+    a.set_option(4, 0.01)     # cost ~0.5 > 0.01 -> dense
+    b.set_option(4, 1.0)      # never above 1 -> sparse
+    hg = synth.HostGraph(W, True)
+    for k in (3, 100, 0):
+        _, ia = a.remove_node(k)
+        _, ib = b.remove_node(k)
+        hg.remove_node(k)
+        assert ia.cost == ib.cost and ia.cost > 0.01
+        assert ia.path == 3 and ib.path == 2
+        Da = getD(a)
+        assert np.array_equal(Da, getD(b))
+        assert_parity(Da, oracle.fw(hg.W))

@@ -64,6 +64,10 @@ def lib():
         L.oracle_brute_f64.restype = ctypes.c_double
         L.oracle_brute_f64.argtypes = [i64, vp, i64, i64]
         L.oracle_dijkstra_rows_i32w.argtypes = [i64, vp, i64, ctypes.c_int32, i64, vp, i64, vp, ctypes.c_int]
+        L.oracle_fw_minimax_i64.argtypes = [i64, vp, i64]
+        L.oracle_fw_minimax_f64.argtypes = [i64, vp]
+        L.oracle_brute_minimax_i64.restype = i64
+        L.oracle_brute_minimax_i64.argtypes = [i64, vp, i64, i64, i64]
         L.oracle_count_shortest_i64.restype = i64
         L.oracle_count_shortest_i64.argtypes = [i64, vp, i64, i64, i64, i64]
         _lib = L
@@ -110,6 +114,40 @@ def fw(W):
         return from_oracle_i32(A)
     lib().oracle_fw_f64(n, A.ctypes.data)
     return A
+
+
+def fw_minimax(W):
+    """All-pairs minimax (bottleneck) distances by FW with (+) -> max."""
+    A = to_oracle(W)
+    n = A.shape[0]
+    if is_int(W):
+        lib().oracle_fw_minimax_i64(n, A.ctypes.data, int(INF64))
+        return from_oracle_i32(A)
+    lib().oracle_fw_minimax_f64(n, A.ctypes.data)
+    return A
+
+
+def brute_minimax_apsp(W):
+    """Exhaustive simple-path enumeration of the minimax distance (n <= 12)."""
+    A = to_oracle(W)
+    n = A.shape[0]
+    out = np.zeros((n, n), np.int64)
+    for s_ in range(n):
+        for t in range(n):
+            r = lib().oracle_brute_minimax_i64(n, A.ctypes.data, int(INF64), s_, t)
+            out[s_, t] = API_INF_I32 if r >= INF64 else r
+    return out.astype(np.int32)
+
+
+def need_update_removal_minimax(D, k):
+    """Theorem 4 with (+) -> max: pair (i, j) listed iff max(D[i][k], D[k][j]) == D[i][j]."""
+    A = to_oracle(D)
+    lhs = np.maximum(A[:, k][:, None], A[k, :][None, :])
+    m = (lhs == A) & _fin(A)
+    m[k, :] = False
+    m[:, k] = False
+    np.fill_diagonal(m, False)
+    return m
 
 
 def fw_raw_i64(A64, k0, k1):

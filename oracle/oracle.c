@@ -241,3 +241,56 @@ void oracle_dijkstra_rows_i32w(int64_t n, const int32_t* W, int64_t ld, int32_t 
     free(done);
   }
 }
+
+/* ---------------- minimax (bottleneck) paths, §6 ----------------
+ * "The algorithms can be revised to solve the all pairs minimax path problem":
+ * the cost of a path is its largest edge weight; MD(s,t) = min over paths of
+ * that maximum.  Same textbook loops with (+) replaced by max. */
+void oracle_fw_minimax_i64(int64_t n, int64_t* D, int64_t inf) {
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t* Dk = D + k * n;
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t dik = D[i * n + k];
+      if (dik >= inf) continue;
+      int64_t* Di = D + i * n;
+      for (int64_t j = 0; j < n; ++j) {
+        int64_t cand = dik > Dk[j] ? dik : Dk[j];
+        if (cand < Di[j]) Di[j] = cand;
+      }
+    }
+  }
+}
+
+void oracle_fw_minimax_f64(int64_t n, double* D) {
+  for (int64_t k = 0; k < n; ++k) {
+    const double* Dk = D + k * n;
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+      double dik = D[i * n + k];
+      double* Di = D + i * n;
+      for (int64_t j = 0; j < n; ++j) {
+        double cand = dik > Dk[j] ? dik : Dk[j];
+        if (cand < Di[j]) Di[j] = cand;
+      }
+    }
+  }
+}
+
+static void brute_mm_rec(int64_t n, const int64_t* W, int64_t inf, int64_t cur, int64_t t,
+                         int64_t mx, unsigned vis, int64_t* best) {
+  if (cur == t) { if (mx < *best) *best = mx; return; }
+  for (int64_t v = 0; v < n; ++v) {
+    if (vis & (1u << v)) continue;
+    int64_t w = W[cur * n + v];
+    if (w >= inf) continue;
+    brute_mm_rec(n, W, inf, v, t, mx > w ? mx : w, vis | (1u << v), best);
+  }
+}
+/* min over simple s->t paths of the max edge weight (n <= 12); 0 for s == t */
+int64_t oracle_brute_minimax_i64(int64_t n, const int64_t* W, int64_t inf, int64_t s, int64_t t) {
+  int64_t best = inf;
+  if (n > 12) return -1;
+  brute_mm_rec(n, W, inf, s, t, 0, 1u << s, &best);
+  return best;
+}

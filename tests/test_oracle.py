@@ -303,3 +303,63 @@ def test_dijkstra_int32_inplace_matches_bruteforce(rng):
         B = oracle.brute_apsp(W)
         assert np.array_equal(oracle.dijkstra_rows_i32(W, range(n)), B)
         assert np.array_equal(oracle.dijkstra_rows_i32(W, range(n), reverse=True), B.T)
+
+
+# ------------------------------------------------------ f2: minimax semiring
+@pytest.mark.parametrize("directed", [True, False])
+def test_minimax_fw_equals_bruteforce(rng, directed):
+    """Minimax FW == min over simple paths of the max edge (definition)."""
+    for trial in range(25):
+        n = int(rng.integers(2, 8))
+        W = random_graph(rng, n, directed, float(rng.choice([0.4, 1.0])), lo=0, hi=9)
+        assert np.array_equal(oracle.fw_minimax(W), oracle.brute_minimax_apsp(W)), (trial, W)
+
+
+def test_minimax_equals_mst_path_max(rng):
+    """Undirected minimax distance = the largest edge on the minimum spanning
+    tree path (a classical property; MST by a plain Prim, independent of FW)."""
+    n = 40
+    W = random_graph(rng, n, False, 1.0, lo=1, hi=500)
+    Wd = W.astype(np.int64)
+    intree = np.zeros(n, bool)
+    intree[0] = True
+    adj = {i: [] for i in range(n)}
+    best = Wd[0].copy()
+    parent = np.zeros(n, int)
+    for _ in range(n - 1):
+        cand = np.where(intree, np.iinfo(np.int64).max, best)
+        v = int(np.argmin(cand))
+        intree[v] = True
+        adj[v].append((parent[v], Wd[v, parent[v]]))
+        adj[parent[v]].append((v, Wd[v, parent[v]]))
+        upd = (~intree) & (Wd[v] < best)
+        best[upd] = Wd[v][upd]
+        parent[upd] = v
+    exp = np.zeros((n, n), np.int64)
+    for s in range(n):
+        stack = [(s, 0)]
+        seen = {s}
+        while stack:
+            x, mx = stack.pop()
+            exp[s, x] = mx
+            for y, w in adj[x]:
+                if y not in seen:
+                    seen.add(y)
+                    stack.append((y, max(mx, w)))
+    assert np.array_equal(oracle.fw_minimax(W), exp.astype(np.int32))
+
+
+def test_minimax_need_update_is_safe(rng):
+    """Theorem 4 carries over to minimax: unlisted pairs keep their distance."""
+    for trial in range(40):
+        n = int(rng.integers(3, 11))
+        W = random_graph(rng, n, True, 1.0, lo=0, hi=7)
+        D = oracle.fw_minimax(W)
+        k = int(rng.integers(n))
+        m = oracle.need_update_removal_minimax(D, k)
+        W2, keep = _remove_from(W, k)
+        D2 = oracle.fw_minimax(W2)
+        Dk = D[np.ix_(keep, keep)]
+        mk = m[np.ix_(keep, keep)]
+        assert np.array_equal(D2[~mk], Dk[~mk])
+        assert np.all(D2 >= Dk)

@@ -87,9 +87,16 @@ typedef enum {
   APSP_OPT_THETA = 1,       /* gate: dense iff |A| > theta * n^2 (default 0.02)      */
   APSP_OPT_TAU = 2,         /* fp32 tie tolerance tau (default 1e-5), Q4   */
   APSP_OPT_MAX_ROUNDS = 3,  /* sparse rounds before switching to dense (default 64)  */
-  APSP_OPT_ROW_DELTA = 4    /* > 0: use the paper's own gate instead — dense FW iff
+  APSP_OPT_ROW_DELTA = 4,   /* > 0: use the paper's own gate instead — dense FW iff
                                Definition 1's cost Phi/(N-1) > delta;
                                0 (default): the pair-level gate of APSP_OPT_THETA    */
+  APSP_OPT_SEMIRING = 5     /* path algebra: 0 (default) shortest path, D = min over
+                               paths of the summed weights; 1 minimax / bottleneck
+                               path, D = min over paths of the largest weight (PAPER.md
+                               §6: "The algorithms can be revised to solve
+                               the all pairs minimax path problem").  Every call then
+                               uses that algebra; D is NOT converted: set it before
+                               apsp_cold_fw (or fill D with the matching matrix).    */
 } apsp_option;
 
 /* Statistics of one update. */

@@ -23,7 +23,7 @@ class WarmAPSP:
     """
 
     def __init__(self, W, directed=True, cap=None, device=None, stream=None, rank=0, world=1,
-                 nccl_id=None, cold_start=True):
+                 nccl_id=None, cold_start=True, semiring="shortest"):
         W = torch.as_tensor(W)
         if W.dtype not in _DT:
             raise TypeError("W must be int32 or float32")
@@ -46,6 +46,11 @@ class WarmAPSP:
                                    self.D_local.data_ptr(), self.ld, self.workspace.data_ptr(), nbytes,
                                    self.stream.cuda_stream, rank, world, nccl_id)
             del Wd
+        if semiring not in ("shortest", "minimax"):
+            raise ValueError("semiring must be 'shortest' or 'minimax'")
+        self.semiring = semiring
+        if semiring == "minimax":
+            L.apsp_set_option(self.h, L.OPT_SEMIRING, 1)
         if cold_start:
             self.cold_fw()
 

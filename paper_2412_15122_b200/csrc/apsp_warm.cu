@@ -160,6 +160,7 @@ struct apsp_handle {
   float tau = 1e-5f;
   int max_rounds = 64;
   double row_delta = 0.0;        // > 0: the paper's Definition-1 gate (ablation)
+  int sr = 0;                    // path algebra: 0 shortest path, 1 minimax
   // state
   bool poisoned = false;
   std::string err;
@@ -337,8 +338,8 @@ apsp_status fw_impl(apsp_handle* h) {
     T* P;
     if (own) {
       T* rowK = D + lk * ld;
-      PK(APSP_K_FW_DIAG, (double)kb * kb * kb, fw_diag<T>(rowK + K0, ld, kb, h->st));
-      PK(APSP_K_FW_PANEL, (double)kb * kb * (n - kb), fw_row_panel<T>(rowK, ld, K0, kb, n, h->st));
+      PK(APSP_K_FW_DIAG, (double)kb * kb * kb, fw_diag<T>(rowK + K0, ld, kb, h->sr, h->st));
+      PK(APSP_K_FW_PANEL, (double)kb * kb * (n - kb), fw_row_panel<T>(rowK, ld, K0, kb, n, h->sr, h->st));
       P = rowK;
     } else {
       P = h->panel<T>();
@@ -349,9 +350,9 @@ apsp_status fw_impl(apsp_handle* h) {
     const int skip_ti = own ? (int)(lk / kTile) : -1;
     if (m > 0) {
       const double mo = (double)(m - (own ? kb : 0));   // rows outside the pivot block
-      PK(APSP_K_FW_PANEL, mo * kb * kb, fw_col_panel<T>(D, ld, m, K0, kb, P + K0, ld, skip_ti, h->st));
+      PK(APSP_K_FW_PANEL, mo * kb * kb, fw_col_panel<T>(D, ld, m, K0, kb, P + K0, ld, skip_ti, h->sr, h->st));
       PK(APSP_K_FW_TILE, mo * (double)(n - kb) * kb,
-         fw_rest_pt<T>(D, ld, m, n, K0, kb, P, ld, skip_ti, h->pt<T>(), h->plan.ldpt, h->st));
+         fw_rest_pt<T>(D, ld, m, n, K0, kb, P, ld, skip_ti, h->pt<T>(), h->plan.ldpt, h->sr, h->st));
     }
   }
   return APSP_OK;
@@ -375,7 +376,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   CKR(cudaMemsetAsync(h->rowcnt(), 0, sizeof(int) * h->cap, h->st));
   CKR(cudaMemsetAsync(h->ctr(), 0, sizeof(DetectCounters), h->st));
   PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
-     detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, h->bm(), h->anyrow(), h->st));
+     detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, h->bm(), h->anyrow(), h->sr, h->st));
   PK(APSP_K_EMIT, 0.0,
      detect_emit<T>(h->Dl<T>(), h->ld, r, n, h->WT<T>(), h->ld, 1, h->rowoff(), h->rowcnt(), h->prow(),
                     h->pcol(), h->plb<T>(), h->plan.lcap, h->ctr(), h->bm(), h->anyrow(), h->st));
@@ -424,7 +425,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
        sparse_phase_a<T>(h->Dl<T>(), h->ld, r, n, h->slid(), h->slw<T>(), h->wnext<T>(), h->rowoff(),
                          h->rowcnt(), h->prow(), h->pcol(), h->plb<T>(), local_total, h->popen(),
                          h->ocnt(), h->ocol(), h->gprow(), h->gpcol(), h->glb<T>(), h->gfull(),
-                         h->plan.ocap, h->ctr(), h->st));
+                         h->plan.ocap, h->ctr(), h->sr, h->st));
   CKR(cudaMemcpyAsync(h->host_small, h->ctr(), sizeof(DetectCounters), cudaMemcpyDeviceToHost, h->st));
   CKR(cudaStreamSynchronize(h->st));
   int64_t nopen = (int64_t)hc->open_total;
@@ -446,11 +447,11 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   if (nopen > 0) {
     // A2: shortlist pass over the open pairs now that certified values are final
     CK(sparse_short<T>(h->Dl<T>(), h->ld, h->row0, h->slid(), h->slw<T>(), h->wnext<T>(),
-                       h->gprow(), h->gpcol(), h->glb<T>(), nopen, h->gfull(), 1, h->st));
+                       h->gprow(), h->gpcol(), h->glb<T>(), nopen, h->gfull(), 1, h->sr, h->st));
     // B: full O(n) scan for the pairs the shortlist could not settle
     PK(APSP_K_SPARSE_R, 8.0 * (double)nopen * (double)n,
        sparse_full<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, n, h->gprow(), h->gpcol(),
-                      h->glb<T>(), h->gfull(), nopen, h->st));
+                      h->glb<T>(), h->gfull(), nopen, h->sr, h->st));
   }
   // rounds over the open entries of each row until no entry changes
   int in = 0;
@@ -469,7 +470,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
         PK(APSP_K_SPARSE_R, 0.0,
            sparse_round<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->gprow(), h->gpcol(),
                            h->glb<T>(), nopen, h->rowoff(), h->ocnt(), h->ocol(), h->chg(in),
-                           h->chg(in ^ 1), h->anyflag(), h->st));
+                           h->chg(in ^ 1), h->anyflag(), h->sr, h->st));
       in ^= 1;
     }
     if (h->world > 1)
@@ -514,14 +515,14 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   T* ceff = h->vec<T>(4);
   PK(APSP_K_ADD_PASS1, 4.0 * (double)(r.hi - r.lo) * (double)n,
      addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
-                      &nchunk, &nslab, kMaxSlabs, h->st));
+                      &nchunk, &nslab, kMaxSlabs, h->sr, h->st));
   CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
                        ceff, row, h->st));
   if (h->world > 1)
     NK(g_nccl.AllReduce(row, row, (size_t)ld, nccl_type<T>(), ncclMin, h->comm, h->st));
   // rows with ceff[i] = INF provably do not change and are not read at all
   PK(APSP_K_RANK1, 0.0,   // work: bytes actually read, counted on the device
-     rank1<T>(h->Dl<T>(), ld, r, n, ceff, row, nullptr, nullptr, h->rank1_bytes(), h->st));
+     rank1<T>(h->Dl<T>(), ld, r, n, ceff, row, nullptr, nullptr, h->rank1_bytes(), h->sr, h->st));
   CK(addnode_write<T>(h->Dl<T>(), ld, r, n, x, h->local(x) ? 1 : 0, col, row, h->WT<T>(), ld, ow,
                       iw, h->st));
   CK(shortlist_add_bound<T>(h->slid(), h->slw<T>(), h->wnext<T>(), ow, n, x, h->st));  // x -> j
@@ -544,7 +545,7 @@ apsp_status remove_node_impl(apsp_handle* h, int64_t k, int64_t* moved_from, aps
   Rows r = h->active();
   T* c1 = h->vec<T>(4);
   T* r1 = h->vec<T>(5);
-  CK(gather_col<T>(h->Dl<T>(), ld, r, k, T(0), c1, h->st));   // t1 = SPD(i, k)
+  CK(gather_col<T>(h->Dl<T>(), ld, r, k, T(0), c1, h->sr, h->st));   // t1 = SPD(i, k)
   apsp_status s = snap_row<T>(h, k, T(0), r1);                 // t2 = SPD(k, j)
   if (s != APSP_OK) return s;
   if (info) info->kind = 4;
@@ -622,17 +623,17 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
       return APSP_OK;
     }
     // D'[i][j] = min(D[i][j], D[i][u] + w + D[v][j] (, D[i][v] + w + D[u][j]))
-    CK(gather_col<T>(h->Dl<T>(), ld, r, u, w_new, c1, h->st));
+    CK(gather_col<T>(h->Dl<T>(), ld, r, u, w_new, c1, h->sr, h->st));
     apsp_status s = snap_row<T>(h, v, T(0), r1);
     if (s != APSP_OK) return s;
     if (und) {
-      CK(gather_col<T>(h->Dl<T>(), ld, r, v, w_new, c2, h->st));
+      CK(gather_col<T>(h->Dl<T>(), ld, r, v, w_new, c2, h->sr, h->st));
       s = snap_row<T>(h, u, T(0), r2);
       if (s != APSP_OK) return s;
     }
     PK(APSP_K_RANK1, 0.0,   // work: bytes actually read, counted on the device
        rank1<T>(h->Dl<T>(), ld, r, n, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, h->rank1_bytes(),
-                h->st));
+                h->sr, h->st));
     CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
     CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
     if (info) info->path = 1;
@@ -649,11 +650,11 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
     CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
     return APSP_OK;
   }
-  CK(gather_col<T>(h->Dl<T>(), ld, r, u, w_old, c1, h->st));   // D[i][u] + w_old
+  CK(gather_col<T>(h->Dl<T>(), ld, r, u, w_old, c1, h->sr, h->st));   // D[i][u] + w_old
   apsp_status s = snap_row<T>(h, v, T(0), r1);                  // D[v][j]
   if (s != APSP_OK) return s;
   if (und) {
-    CK(gather_col<T>(h->Dl<T>(), ld, r, v, w_old, c2, h->st));
+    CK(gather_col<T>(h->Dl<T>(), ld, r, v, w_old, c2, h->sr, h->st));
     s = snap_row<T>(h, u, T(0), r2);
     if (s != APSP_OK) return s;
   }
@@ -672,11 +673,11 @@ apsp_status removal_phi(apsp_handle* h, int64_t k, int64_t* phi) {
   Rows r = h->active();
   T* c1 = h->vec<T>(4);
   T* r1 = h->vec<T>(5);
-  CK(gather_col<T>(h->Dl<T>(), ld, r, k, T(0), c1, h->st));
+  CK(gather_col<T>(h->Dl<T>(), ld, r, k, T(0), c1, h->sr, h->st));
   apsp_status s = snap_row<T>(h, k, T(0), r1);
   if (s != APSP_OK) return s;
   PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
-     detect<T>(h->Dl<T>(), ld, r, n, k, c1, r1, nullptr, nullptr, h->tau, h->bm(), h->anyrow(), h->st));
+     detect<T>(h->Dl<T>(), ld, r, n, k, c1, r1, nullptr, nullptr, h->tau, h->bm(), h->anyrow(), h->sr, h->st));
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(h->small() + 128);
   CKR(cudaMemsetAsync(cnt, 0, sizeof *cnt, h->st));
   CK(count_nonzero(h->anyrow() + r.lo, r.hi - r.lo, cnt, h->st));
@@ -740,7 +741,7 @@ apsp_status modify_readd_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, int
   T* so = h->vec<T>(2);
   T* si = h->vec<T>(3);
   Rows rw{0, n, 0};
-  CK(gather_col<T>(WT, ld, rw, p, T(0), so, h->st));
+  CK(gather_col<T>(WT, ld, rw, p, T(0), so, h->sr, h->st));
   CK(copy_vec<T>(WT + p * ld, n, ld, T(0), si, h->st));
   if (!h->directed || p == u) CK(vec_set_move<T>(so, other, w_new, -1, 0, h->st));
   if (!h->directed || p == v) CK(vec_set_move<T>(si, other, w_new, -1, 0, h->st));
@@ -783,7 +784,7 @@ apsp_status query_one(apsp_handle* h, int64_t s, int64_t t, void* dist, int32_t*
   hv[0] = (int)s; hv[1] = (int)t;
   CKR(cudaMemcpyAsync(dv, hv, 2 * sizeof(int), cudaMemcpyHostToDevice, h->st));
   PK(APSP_K_QUERY, 8.0 * (double)h->n, query_batch<T>(h->Dl<T>(), h->ld, h->WT<T>(), h->ld, h->n, 1, dv, dv + 1, ddist, dpath, cap_dev,
-                    dv + 2, dv + 3, h->tau, h->st));
+                    dv + 2, dv + 3, h->tau, h->sr, h->st));
   CKR(cudaMemcpyAsync(hv, dv, 8 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
   CKR(cudaStreamSynchronize(h->st));
   const int len = hv[2], nc = hv[3];
@@ -957,6 +958,10 @@ apsp_status apsp_set_option(apsp_handle* h, apsp_option opt, double value) {
       if (!(value >= 1)) return APSP_E_INVAL;
       h->max_rounds = (int)value;
       return APSP_OK;
+    case APSP_OPT_SEMIRING:
+      if (value != 0 && value != 1) return APSP_E_INVAL;
+      h->sr = (int)value;
+      return APSP_OK;
     case APSP_OPT_ROW_DELTA:
       if (!(value >= 0) || value > 1) return APSP_E_INVAL;
       h->row_delta = value;
@@ -1044,7 +1049,7 @@ apsp_status sp_pair_query_batch(apsp_handle* h, int32_t q, const int32_t* s, con
   return dispatch(h->dt, [&](auto z) -> apsp_status {
     using T = decltype(z);
     PK(APSP_K_QUERY, 8.0 * (double)h->n * q, query_batch<T>(h->Dl<T>(), h->ld, h->WT<T>(), h->ld, h->n, q, s, t, reinterpret_cast<T*>(dist),
-                      paths, path_cap, path_lens, n_cand, h->tau, h->st));
+                      paths, path_cap, path_lens, n_cand, h->tau, h->sr, h->st));
     return APSP_OK;
   });
 }

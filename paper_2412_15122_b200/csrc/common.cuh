@@ -15,9 +15,14 @@ namespace apsp {
 // most 2^31-2 (no overflow) and min(.) keeps every stored value <= INF.
 // fp32: INF = +inf (inf + x = inf; weights >= 0, so NaN cannot arise).
 // ---------------------------------------------------------------------------
-template <typename T> struct Tr;
+// SR selects the path algebra (§6): 0 = shortest path,
+// the (min, +) semiring of the paper's body; 1 = minimax / bottleneck path,
+// (min, max) — "The algorithms can be revised to solve the all pairs minimax
+// path problem".  Only add/relax/sat/tight differ; 0 stays the identity of
+// the path composition in both (weights are >= 0).
+template <typename T, int SR = 0> struct Tr;
 
-template <> struct Tr<int32_t> {
+template <> struct Tr<int32_t, 0> {
   using V4 = int4;
   static constexpr bool kFloat = false;
   __host__ __device__ static __forceinline__ int32_t inf() { return APSP_INF_I32_DEV; }
@@ -39,7 +44,7 @@ template <> struct Tr<int32_t> {
   __device__ static __forceinline__ bool at_lb(int32_t v, int32_t lb) { return v <= lb; }
 };
 
-template <> struct Tr<float> {
+template <> struct Tr<float, 0> {
   using V4 = float4;
   static constexpr bool kFloat = true;
   __host__ __device__ static __forceinline__ float inf() { return __builtin_huge_valf(); }
@@ -60,6 +65,15 @@ template <> struct Tr<float> {
   // within 2^-21 relative of the lower bound: the true value lies in [lb, v],
   // so stopping here errs by <= 5e-7 relative (fp32 bar 1e-5)
   __device__ static __forceinline__ bool at_lb(float v, float lb) { return v <= lb + lb * 0x1p-21f; }
+};
+
+// minimax: a path's cost is its largest edge; max is exact in int32 and fp32
+template <typename T> struct Tr<T, 1> : Tr<T, 0> {
+  using B = Tr<T, 0>;
+  __device__ static __forceinline__ T add(T a, T b) { return a > b ? a : b; }
+  __device__ static __forceinline__ T relax(T d, T a, T b) { return B::mn(d, a > b ? a : b); }
+  __device__ static __forceinline__ T sat(T a) { return a; }
+  __device__ static __forceinline__ bool tight(T lhs, T d, float) { return lhs == d; }
 };
 
 // ---------------------------------------------------------------------------

@@ -30,7 +30,7 @@ constexpr int AST = TB + 4;    // As row stride (elements), keeps LDS.128 aligne
 // ---------------------------------------------------------------------------
 // (1) closure of the diagonal tile
 // ---------------------------------------------------------------------------
-template <typename T>
+template <typename T, int SR>
 __global__ void __launch_bounds__(1024) fw_diag_kernel(T* __restrict__ D, int64_t ld, int kb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T (*s)[TB] = reinterpret_cast<T (*)[TB]>(smem_raw);   // 64 KB tile
@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(1024) fw_diag_kernel(T* __restrict__ D, int64_
   for (int k = 0; k < kb; ++k) {
     for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) {
       int i = e / TB, j = e % TB;
-      s[i][j] = Tr<T>::relax(s[i][j], s[i][k], s[k][j]);
+      s[i][j] = Tr<T, SR>::relax(s[i][j], s[i][k], s[k][j]);
     }
     __syncthreads();
   }
@@ -73,7 +73,7 @@ struct TileArgs {
   int skip_ti, skip_tj;          // tile row / column excluded from this launch (-1: none)
 };
 
-template <typename T>
+template <typename T, int SR>
 __global__ void __launch_bounds__(NTH, 1) fw_tile_kernel(TileArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* As = reinterpret_cast<T*>(smem_raw);          // [2][KC][AST]   (k-major: As[k][i])
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(NTH, 1) fw_tile_kernel(TileArgs a) {
     }
     const T* as = As + buf * KC * AST;
     const T* bs = Bs + buf * KC * TB;
-    if constexpr (!Tr<T>::kFloat) {
+    if constexpr (!(Tr<T>::kFloat && SR == 0)) {
       // int32: one VIADDMNMX per relaxation
 #pragma unroll 8
       for (int kk = 0; kk < KC; ++kk) {
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(NTH, 1) fw_tile_kernel(TileArgs a) {
 #pragma unroll
         for (int r = 0; r < 8; ++r)
 #pragma unroll
-          for (int c = 0; c < 8; ++c) acc[r][c] = Tr<T>::relax(acc[r][c], av[r], bv[c]);
+          for (int c = 0; c < 8; ++c) acc[r][c] = Tr<T, SR>::relax(acc[r][c], av[r], bv[c]);
       }
     } else {
       // fp32: two pivots per step so each accumulator takes one 3-input
@@ -248,7 +248,7 @@ struct Tile3Args {
   int skip_ti, skip_tj;
 };
 
-template <typename T>
+template <typename T, int SR>
 __global__ void __launch_bounds__(NTH, 2) fw_tile3_kernel(Tile3Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* As = reinterpret_cast<T*>(smem_raw);          // [2][KC][TB]
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(NTH, 2) fw_tile3_kernel(Tile3Args a) {
     if (kc + 1 < nch) load_chunk(kc + 1, buf ^ 1);
     const T* as = As + buf * KC * TB;
     const T* bs = Bs + buf * KC * TB;
-    if constexpr (!Tr<T>::kFloat) {
+    if constexpr (!(Tr<T>::kFloat && SR == 0)) {
 #pragma unroll 4
       for (int kk = 0; kk < KC; ++kk) {
         Vec4<T> a0 = *reinterpret_cast<const Vec4<T>*>(as + kk * TB + ty * 4);
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(NTH, 2) fw_tile3_kernel(Tile3Args a) {
 #pragma unroll
         for (int r = 0; r < 8; ++r)
 #pragma unroll
-          for (int c = 0; c < 8; ++c) acc[r][c] = Tr<T>::relax(acc[r][c], av[r], bv[c]);
+          for (int c = 0; c < 8; ++c) acc[r][c] = Tr<T, SR>::relax(acc[r][c], av[r], bv[c]);
       }
     } else {
 #pragma unroll 2
@@ -383,48 +383,56 @@ __global__ void fw_transpose_panel_kernel(const T* D, int64_t ld, int64_t m, int
 
 constexpr size_t kTileSmem = sizeof(int32_t) * (2 * KC * AST + 2 * KC * TB);
 
-template <typename T>
-static cudaError_t launch_tile(const TileArgs& a, cudaStream_t st) {
+template <typename T, int SR>
+static cudaError_t launch_tile_sr(const TileArgs& a, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(fw_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(fw_tile_kernel<T, SR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kTileSmem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   if (a.m <= 0 || a.ncols <= 0) return cudaSuccess;
   dim3 grid((a.ncols + TB - 1) / TB, (a.m + TB - 1) / TB);
-  fw_tile_kernel<T><<<grid, NTH, kTileSmem, st>>>(a);
+  fw_tile_kernel<T, SR><<<grid, NTH, kTileSmem, st>>>(a);
   return cudaGetLastError();
+}
+template <typename T>
+static cudaError_t launch_tile(const TileArgs& a, int sr, cudaStream_t st) {
+  return sr ? launch_tile_sr<T, 1>(a, st) : launch_tile_sr<T, 0>(a, st);
 }
 
 // ---------------------------------------------------------------------------
 // host-side drivers
 // ---------------------------------------------------------------------------
-template <typename T>
-cudaError_t fw_diag(T* Dkk, int64_t ld, int kb, cudaStream_t st) {
+template <typename T, int SR>
+static cudaError_t fw_diag_sr(T* Dkk, int64_t ld, int kb, cudaStream_t st) {
   static bool configured = false;
   constexpr int smem = TB * TB * sizeof(T);
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(fw_diag_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(fw_diag_kernel<T, SR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  fw_diag_kernel<T><<<1, 1024, smem, st>>>(Dkk, ld, kb);
+  fw_diag_kernel<T, SR><<<1, 1024, smem, st>>>(Dkk, ld, kb);
   return cudaGetLastError();
+}
+template <typename T>
+cudaError_t fw_diag(T* Dkk, int64_t ld, int kb, int sr, cudaStream_t st) {
+  return sr ? fw_diag_sr<T, 1>(Dkk, ld, kb, st) : fw_diag_sr<T, 0>(Dkk, ld, kb, st);
 }
 
 // Row panel D[K][*] (all columns except the K tile) := D_KK (x) D[K][*].
 // `rowK` points at D[K0][0]; ncols = n.
 template <typename T>
-cudaError_t fw_row_panel(T* rowK, int64_t ld, int64_t K0, int kb, int64_t ncols, cudaStream_t st) {
+cudaError_t fw_row_panel(T* rowK, int64_t ld, int64_t K0, int kb, int64_t ncols, int sr, cudaStream_t st) {
   TileArgs a;
   a.C = rowK; a.ldc = ld;
   a.A = rowK + K0; a.lda = ld;        // closed diagonal tile
   a.B = rowK; a.ldb = ld;             // the panel itself (each CTA reads only its own tile)
   a.m = kb; a.ncols = (int)ncols; a.kdepth = kb;
   a.skip_ti = -1; a.skip_tj = (int)(K0 / TB);
-  return launch_tile<T>(a, st);
+  return launch_tile<T>(a, sr, st);
 }
 
 // Column panel D[rows][K] := D[rows][K] (x) D_KK for m local rows.
@@ -432,45 +440,34 @@ cudaError_t fw_row_panel(T* rowK, int64_t ld, int64_t K0, int kb, int64_t ncols,
 // skip_ti = the local tile row holding the diagonal tile (-1 if not local).
 template <typename T>
 cudaError_t fw_col_panel(T* D, int64_t ld, int64_t m, int64_t K0, int kb, const T* Dkk,
-                         int64_t lddk, int skip_ti, cudaStream_t st) {
+                         int64_t lddk, int skip_ti, int sr, cudaStream_t st) {
   TileArgs a;
   a.C = D + K0; a.ldc = ld;
   a.A = D + K0; a.lda = ld;
   a.B = Dkk; a.ldb = lddk;
   a.m = (int)m; a.ncols = kb; a.kdepth = kb;
   a.skip_ti = skip_ti; a.skip_tj = -1;
-  return launch_tile<T>(a, st);
+  return launch_tile<T>(a, sr, st);
 }
 
 // Phase 3 on m local rows: D[i][j] = min(D[i][j], D[i][K] (x) P[K][j]) where
 // P is the row panel (kb x ncols, leading dimension ldp).
-template <typename T>
-cudaError_t fw_rest(T* D, int64_t ld, int64_t m, int64_t ncols, int64_t K0, int kb, const T* P,
-                    int64_t ldp, int skip_ti, cudaStream_t st) {
-  TileArgs a;
-  a.C = D; a.ldc = ld;
-  a.A = D + K0; a.lda = ld;
-  a.B = P; a.ldb = ldp;
-  a.m = (int)m; a.ncols = (int)ncols; a.kdepth = kb;
-  a.skip_ti = skip_ti; a.skip_tj = (int)(K0 / TB);
-  return launch_tile<T>(a, st);
-}
 
 template <typename T>
 cudaError_t fw_rest_pt(T* D, int64_t ld, int64_t m, int64_t ncols, int64_t K0, int kb, const T* P,
-                       int64_t ldp, int skip_ti, T* PT, int64_t ldpt, cudaStream_t st) {
+                       int64_t ldp, int skip_ti, T* PT, int64_t ldpt, int sr, cudaStream_t st) {
   if (m <= 0 || ncols <= 0) return cudaSuccess;
   const int64_t mpad = (m + TB - 1) / TB * TB;
   if (mpad > ldpt) return cudaErrorInvalidValue;
   fw_transpose_panel_kernel<T><<<dim3((unsigned)(mpad / 32), TB / 32), dim3(32, 8), 0, st>>>(
       D, ld, m, K0, kb, PT, ldpt, mpad);
-  static bool configured = false;
+  static bool configured[2] = {false, false};
   constexpr size_t smem = sizeof(T) * 4 * KC * TB;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(fw_tile3_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+  if (!configured[sr ? 1 : 0]) {
+    cudaError_t e = cudaFuncSetAttribute(sr ? fw_tile3_kernel<T, 1> : fw_tile3_kernel<T, 0>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured[sr ? 1 : 0] = true;
   }
   Tile3Args a;
   a.C = D; a.ldc = ld;
@@ -479,19 +476,20 @@ cudaError_t fw_rest_pt(T* D, int64_t ld, int64_t m, int64_t ncols, int64_t K0, i
   a.m = (int)m; a.ncols = (int)ncols; a.kdepth = kb;
   a.skip_ti = skip_ti; a.skip_tj = (int)(K0 / TB);
   dim3 grid((unsigned)((ncols + TB - 1) / TB), (unsigned)(mpad / TB));
-  fw_tile3_kernel<T><<<grid, NTH, smem, st>>>(a);
+  if (sr)
+    fw_tile3_kernel<T, 1><<<grid, NTH, smem, st>>>(a);
+  else
+    fw_tile3_kernel<T, 0><<<grid, NTH, smem, st>>>(a);
   return cudaGetLastError();
 }
 
 #define INST(T)                                                                                  \
-  template cudaError_t fw_diag<T>(T*, int64_t, int, cudaStream_t);                               \
-  template cudaError_t fw_row_panel<T>(T*, int64_t, int64_t, int, int64_t, cudaStream_t);        \
+  template cudaError_t fw_diag<T>(T*, int64_t, int, int, cudaStream_t);                          \
+  template cudaError_t fw_row_panel<T>(T*, int64_t, int64_t, int, int64_t, int, cudaStream_t);   \
   template cudaError_t fw_col_panel<T>(T*, int64_t, int64_t, int64_t, int, const T*, int64_t,    \
-                                       int, cudaStream_t);                                       \
-  template cudaError_t fw_rest<T>(T*, int64_t, int64_t, int64_t, int64_t, int, const T*, int64_t, \
-                                  int, cudaStream_t);                                            \
+                                       int, int, cudaStream_t);                                  \
   template cudaError_t fw_rest_pt<T>(T*, int64_t, int64_t, int64_t, int64_t, int, const T*,       \
-                                     int64_t, int, T*, int64_t, cudaStream_t);
+                                     int64_t, int, T*, int64_t, int, cudaStream_t);
 INST(int32_t)
 INST(float)
 #undef INST

@@ -15,20 +15,17 @@ struct DetectCounters {
   unsigned long long open_total;   // open pairs after the shortlist certification
 };
 
-// ---------------- fw.cu ----------------
-template <typename T> cudaError_t fw_diag(T* Dkk, int64_t ld, int kb, cudaStream_t st);
+// ---------------- fw.cu ----------------  (sr: 0 shortest path, 1 minimax)
+template <typename T> cudaError_t fw_diag(T* Dkk, int64_t ld, int kb, int sr, cudaStream_t st);
 template <typename T>
-cudaError_t fw_row_panel(T* rowK, int64_t ld, int64_t K0, int kb, int64_t ncols, cudaStream_t st);
+cudaError_t fw_row_panel(T* rowK, int64_t ld, int64_t K0, int kb, int64_t ncols, int sr,
+                         cudaStream_t st);
 template <typename T>
 cudaError_t fw_col_panel(T* D, int64_t ld, int64_t m, int64_t K0, int kb, const T* Dkk,
-                         int64_t lddk, int skip_ti, cudaStream_t st);
-template <typename T>
-cudaError_t fw_rest(T* D, int64_t ld, int64_t m, int64_t ncols, int64_t K0, int kb, const T* P,
-                    int64_t ldp, int skip_ti, cudaStream_t st);
-
+                         int64_t lddk, int skip_ti, int sr, cudaStream_t st);
 template <typename T>
 cudaError_t fw_rest_pt(T* D, int64_t ld, int64_t m, int64_t ncols, int64_t K0, int kb, const T* P,
-                       int64_t ldp, int skip_ti, T* PT, int64_t ldpt, cudaStream_t st);
+                       int64_t ldp, int skip_ti, T* PT, int64_t ldpt, int sr, cudaStream_t st);
 
 // ---------------- stream.cu ----------------
 // Row range [lo, hi) is global; D points at global row `row0` (local block).
@@ -47,27 +44,29 @@ cudaError_t fill(T* p, int64_t count, T v, cudaStream_t st);
 template <typename T>
 cudaError_t init_d(T* D, int64_t ld, Rows r, int64_t n, const T* WT, int64_t ldw, cudaStream_t st);
 template <typename T>
-cudaError_t gather_col(const T* D, int64_t ld, Rows r, int64_t col, T add, T* out, cudaStream_t st);
+cudaError_t gather_col(const T* D, int64_t ld, Rows r, int64_t col, T add, T* out, int sr,
+                       cudaStream_t st);
 template <typename T>
 cudaError_t copy_vec(const T* src, int64_t n, int64_t npad, T add, T* out, cudaStream_t st);
 template <typename T>
 cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow, const T* iw,
                           T* rowpart, T* rowpartM, T* colpart, int64_t part_ld, int* nchunk_out,
-                          int* nslab_out, int max_slabs, cudaStream_t st);
+                          int* nslab_out, int max_slabs, int sr, cudaStream_t st);
 template <typename T>
 cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
                            int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,
                            T* ceff, T* row, cudaStream_t st);
 template <typename T>
 cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, const T* c2,
-                  const T* rv2, unsigned long long* bytes_read, cudaStream_t st);
+                  const T* rv2, unsigned long long* bytes_read, int sr, cudaStream_t st);
 template <typename T>
 cudaError_t addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xlocal,
                           const T* col, const T* row, T* WT, int64_t ldw, const T* ow,
                           const T* iw, cudaStream_t st);
 template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
-                   const T* c2, const T* r2, float tau, uint32_t* bm, int* anyrow, cudaStream_t st);
+                   const T* c2, const T* r2, float tau, uint32_t* bm, int* anyrow, int sr,
+                   cudaStream_t st);
 template <typename T>
 cudaError_t detect_emit(T* D, int64_t ld, Rows r, int64_t n, const T* WT, int64_t ldw, int reset,
                         int64_t* rowoff, int* rowcnt, int* prow, int* pcol, T* plb, int64_t lcap,
@@ -115,13 +114,14 @@ cudaError_t shortlist_remove(int* SLid, T* SLw, T* wnext, int64_t n, int64_t k, 
 template <typename T>
 cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const T* SLw,
                          const T* wnext, const int* prow, const int* pcol, const T* plb,
-                         int64_t npairs, unsigned char* out, int classify, cudaStream_t st);
+                         int64_t npairs, unsigned char* out, int classify, int sr, cudaStream_t st);
 template <typename T>
 cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, int64_t n, const int* SLid, const T* SLw,
                            const T* wnext, const int64_t* rowoff, const int* rowcnt,
                            const int* prow, const int* pcol, const T* plb, int64_t npairs,
                            unsigned char* out, int* ocnt, int* ocol, int* gprow, int* gpcol, T* glb,
-                           unsigned char* gfull, int64_t ocap, DetectCounters* ctr, cudaStream_t st);
+                           unsigned char* gfull, int64_t ocap, DetectCounters* ctr, int sr,
+                           cudaStream_t st);
 template <typename T>
 cudaError_t sparse_compact(Rows r, const int64_t* rowoff, const int* rowcnt, const int* pcol,
                            const T* plb, const unsigned char* popen, int* ocol, int* ocnt,
@@ -130,19 +130,19 @@ cudaError_t sparse_compact(Rows r, const int64_t* rowoff, const int* rowcnt, con
 template <typename T>
 cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
                         const int* gprow, const int* gpcol, const T* glb, const unsigned char* gfull,
-                        int64_t nopen, cudaStream_t st);
+                        int64_t nopen, int sr, cudaStream_t st);
 template <typename T>
 cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw,
                          const int* gprow, const int* gpcol, const T* glb, int64_t nopen,
                          const int64_t* rowoff, const int* ocnt, const int* ocol, const int* chg_in,
-                         int* chg_out, int* any, cudaStream_t st);
+                         int* chg_out, int* any, int sr, cudaStream_t st);
 
 // ---------------- query.cu ----------------
 constexpr int kQueryCap = 4096;
 template <typename T>
 cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int q,
                         const int* s, const int* t, T* dist, int* paths, int path_cap,
-                        int* path_lens, int* ncand, float tau, cudaStream_t st);
+                        int* path_lens, int* ncand, float tau, int sr, cudaStream_t st);
 
 int num_sms();
 

@@ -21,7 +21,7 @@ namespace apsp {
 
 constexpr int QT = 256;   // threads per query CTA
 
-template <typename T>
+template <typename T, int SR>
 __global__ void __launch_bounds__(QT) k_query(const T* __restrict__ D, int64_t ld,
                                               const T* __restrict__ WT, int64_t ldw, int64_t n,
                                               int q, const int* __restrict__ S,
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(QT) k_query(const T* __restrict__ D, int64_t l
       for (int u = 0; u < U; ++u) {
         int64_t k = base + (int64_t)u * QT + tid;
         f[u] = k < n && Tr<T>::fin(dsk[u]) && Tr<T>::fin(dkt[u]) &&
-               Tr<T>::tight(Tr<T>::add(dsk[u], dkt[u]), st, tau);
+               Tr<T, SR>::tight(Tr<T, SR>::add(dsk[u], dkt[u]), st, tau);
         anyf |= f[u];
       }
       if (!__syncthreads_or(anyf)) continue;
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(QT) k_query(const T* __restrict__ D, int64_t l
           if (done[c]) continue;
           const T w = WT[(int64_t)cid[c] * ldw + gm];   // W[m][c]
           if (!Tr<T>::fin(w)) continue;
-          const T cand = Tr<T>::add(lm, w);
+          const T cand = Tr<T, SR>::add(lm, w);
           if (cand < lab[c]) { lab[c] = cand; pred[c] = (short)m; }
         }
         __syncwarp();
@@ -177,19 +177,23 @@ __global__ void __launch_bounds__(QT) k_query(const T* __restrict__ D, int64_t l
 template <typename T>
 cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int q,
                         const int* s, const int* t, T* dist, int* paths, int path_cap,
-                        int* path_lens, int* ncand, float tau, cudaStream_t st) {
+                        int* path_lens, int* ncand, float tau, int sr, cudaStream_t st) {
   if (q <= 0) return cudaSuccess;
   int grid = std::min(q, num_sms() * 4);
-  k_query<T><<<grid, QT, 0, st>>>(D, ld, WT, ldw, n, q, s, t, dist, paths, path_cap, path_lens,
-                                  ncand, tau);
+  if (sr)
+    k_query<T, 1><<<grid, QT, 0, st>>>(D, ld, WT, ldw, n, q, s, t, dist, paths, path_cap, path_lens,
+                                       ncand, tau);
+  else
+    k_query<T, 0><<<grid, QT, 0, st>>>(D, ld, WT, ldw, n, q, s, t, dist, paths, path_cap, path_lens,
+                                       ncand, tau);
   return cudaGetLastError();
 }
 
 template cudaError_t query_batch<int32_t>(const int32_t*, int64_t, const int32_t*, int64_t, int64_t,
                                           int, const int*, const int*, int32_t*, int*, int, int*,
-                                          int*, float, cudaStream_t);
+                                          int*, float, int, cudaStream_t);
 template cudaError_t query_batch<float>(const float*, int64_t, const float*, int64_t, int64_t, int,
                                         const int*, const int*, float*, int*, int, int*, int*,
-                                        float, cudaStream_t);
+                                        float, int, cudaStream_t);
 
 }  // namespace apsp

@@ -342,7 +342,7 @@ cudaError_t shortlist_swap(int* SLid, T* SLw, T* wnext, int64_t n, int64_t p, in
 // of other pairs of the row are then visible, so a class-1 value is the
 // exact min of (*) over every m whose value can no longer change.
 // ---------------------------------------------------------------------------
-template <typename T>
+template <typename T, int SR>
 __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t row0,
                                                       const int* __restrict__ SLid,
                                                       const T* __restrict__ SLw,
@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
     for (int q = 0; q < kSLK; ++q) {
       const int m = sid[q * 32 + lane];
       const T w = sw[q * 32 + lane];
-      if (m >= 0) acc = Tr<T>::relax(acc, *(volatile T*)(Drow + m), w);
+      if (m >= 0) acc = Tr<T, SR>::relax(acc, *(volatile T*)(Drow + m), w);
       if (!classify && (q == 0 || q == 2 || q == 6) && Tr<T>::at_lb(warp_min<T>(acc), lbp)) break;
     }
     acc = warp_min<T>(acc);
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
 // Phase A for rows with many listed pairs: the CTA copies row i of D0 into
 // shared memory once (a snapshot: every value in it is a valid upper bound)
 // and evaluates all the row's pairs from it.
-template <typename T>
+template <typename T, int SR>
 __global__ void __launch_bounds__(512) k_sparse_short_rows(T* D, int64_t ld, Rows r, int64_t n,
                                                            const int* __restrict__ SLid,
                                                            const T* __restrict__ SLw,
@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(512) k_sparse_short_rows(T* D, int64_t ld, Row
       for (int q = 0; q < kSLK; ++q) {
         const int m = sid[q * 32 + lane];
         const T w = sw[q * 32 + lane];
-        if (m >= 0) acc = Tr<T>::relax(acc, srow[m], w);
+        if (m >= 0) acc = Tr<T, SR>::relax(acc, srow[m], w);
       }
       acc = warp_min<T>(acc);
       if (lane == 0) {
@@ -470,12 +470,16 @@ __global__ void __launch_bounds__(512) k_sparse_short_rows(T* D, int64_t ld, Row
 template <typename T>
 cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const T* SLw,
                          const T* wnext, const int* prow, const int* pcol, const T* plb,
-                         int64_t npairs, unsigned char* out, int classify, cudaStream_t st) {
+                         int64_t npairs, unsigned char* out, int classify, int sr, cudaStream_t st) {
   if (npairs <= 0) return cudaSuccess;
   int grid = (int)std::min<int64_t>(cdiv(npairs, 8), (int64_t)num_sms() * 16);
   OpenLists<T> ol{};
-  k_sparse_short<T><<<grid, 256, 0, st>>>(D, ld, row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
-                                          out, classify, nullptr, 0, ol);
+  if (sr)
+    k_sparse_short<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
+                                               out, classify, nullptr, 0, ol);
+  else
+    k_sparse_short<T, 0><<<grid, 256, 0, st>>>(D, ld, row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
+                                               out, classify, nullptr, 0, ol);
   return cudaGetLastError();
 }
 
@@ -487,7 +491,8 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, int64_t n, const int* SLid,
                            const T* wnext, const int64_t* rowoff, const int* rowcnt,
                            const int* prow, const int* pcol, const T* plb, int64_t npairs,
                            unsigned char* out, int* ocnt, int* ocol, int* gprow, int* gpcol, T* glb,
-                           unsigned char* gfull, int64_t ocap, DetectCounters* ctr, cudaStream_t st) {
+                           unsigned char* gfull, int64_t ocap, DetectCounters* ctr, int sr,
+                           cudaStream_t st) {
   if (npairs <= 0) return cudaSuccess;
   OpenLists<T> ol{ocnt, ocol, rowoff, gprow, gpcol, glb, gfull, ocap, ctr};
   const size_t smem = sizeof(T) * (size_t)((n + 3) / 4 * 4);
@@ -495,19 +500,29 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, int64_t n, const int* SLid,
   if (rows_ok) {
     static size_t configured = 0;
     if (configured < smem) {
-      cudaError_t e = cudaFuncSetAttribute(k_sparse_short_rows<T>,
+      cudaError_t e = cudaFuncSetAttribute(k_sparse_short_rows<T, 0>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_sparse_short_rows<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
       if (e != cudaSuccess) return e;
       configured = smem;
     }
     int grid = (int)std::min<int64_t>(r.hi - r.lo, (int64_t)num_sms() * (smem > 110 * 1024 ? 1 : 2));
-    if (grid > 0)
-      k_sparse_short_rows<T><<<grid, 512, smem, st>>>(D, ld, r, n, SLid, SLw, rowoff, rowcnt, pcol,
-                                                      plb, out, kRowMin, ol);
+    if (grid > 0 && sr)
+      k_sparse_short_rows<T, 1><<<grid, 512, smem, st>>>(D, ld, r, n, SLid, SLw, rowoff, rowcnt, pcol,
+                                                         plb, out, kRowMin, ol);
+    else if (grid > 0)
+      k_sparse_short_rows<T, 0><<<grid, 512, smem, st>>>(D, ld, r, n, SLid, SLw, rowoff, rowcnt, pcol,
+                                                         plb, out, kRowMin, ol);
   }
   int grid = (int)std::min<int64_t>(cdiv(npairs, 8), (int64_t)num_sms() * 16);
-  k_sparse_short<T><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
-                                          out, 0, rows_ok ? rowcnt : nullptr, kRowMin, ol);
+  if (sr)
+    k_sparse_short<T, 1><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
+                                               out, 0, rows_ok ? rowcnt : nullptr, kRowMin, ol);
+  else
+    k_sparse_short<T, 0><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
+                                               out, 0, rows_ok ? rowcnt : nullptr, kRowMin, ol);
   return cudaGetLastError();
 }
 
@@ -577,7 +592,7 @@ cudaError_t sparse_compact(Rows r, const int64_t* rowoff, const int* rowcnt, con
 // ---------------------------------------------------------------------------
 // phase B: full scan (*) for open pairs marked 2, early exit at the lower bound
 // ---------------------------------------------------------------------------
-template <typename T>
+template <typename T, int SR>
 __global__ void __launch_bounds__(256) k_sparse_full(T* D, int64_t ld, int64_t row0,
                                                      const T* __restrict__ WT, int64_t ldw,
                                                      int64_t n, const int* __restrict__ gprow,
@@ -609,10 +624,10 @@ __global__ void __launch_bounds__(256) k_sparse_full(T* D, int64_t ld, int64_t r
         d1 = mask_tail<T>(ld4_cg<T>(Drow + 4 * q1), 4 * q1, n);
         w1 = mask_tail<T>(ld4<T>(Wrow + 4 * q1), 4 * q1, n);
       }
-      acc = Tr<T>::relax(acc, d0.x, w0.x); acc = Tr<T>::relax(acc, d0.y, w0.y);
-      acc = Tr<T>::relax(acc, d0.z, w0.z); acc = Tr<T>::relax(acc, d0.w, w0.w);
-      acc = Tr<T>::relax(acc, d1.x, w1.x); acc = Tr<T>::relax(acc, d1.y, w1.y);
-      acc = Tr<T>::relax(acc, d1.z, w1.z); acc = Tr<T>::relax(acc, d1.w, w1.w);
+      acc = Tr<T, SR>::relax(acc, d0.x, w0.x); acc = Tr<T, SR>::relax(acc, d0.y, w0.y);
+      acc = Tr<T, SR>::relax(acc, d0.z, w0.z); acc = Tr<T, SR>::relax(acc, d0.w, w0.w);
+      acc = Tr<T, SR>::relax(acc, d1.x, w1.x); acc = Tr<T, SR>::relax(acc, d1.y, w1.y);
+      acc = Tr<T, SR>::relax(acc, d1.z, w1.z); acc = Tr<T, SR>::relax(acc, d1.w, w1.w);
       if ((iter & 7) == 0 && Tr<T>::at_lb(warp_min<T>(acc), lb)) break;   // reached the lower bound
     }
     acc = warp_min<T>(acc);
@@ -625,17 +640,20 @@ __global__ void __launch_bounds__(256) k_sparse_full(T* D, int64_t ld, int64_t r
 template <typename T>
 cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
                         const int* gprow, const int* gpcol, const T* glb, const unsigned char* gfull,
-                        int64_t nopen, cudaStream_t st) {
+                        int64_t nopen, int sr, cudaStream_t st) {
   if (nopen <= 0) return cudaSuccess;
   int grid = (int)std::min<int64_t>(cdiv(nopen, 8), (int64_t)num_sms() * 8);
-  k_sparse_full<T><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, n, gprow, gpcol, glb, gfull, nopen);
+  if (sr)
+    k_sparse_full<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, n, gprow, gpcol, glb, gfull, nopen);
+  else
+    k_sparse_full<T, 0><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, n, gprow, gpcol, glb, gfull, nopen);
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
 // rounds: open pair of a changed row, min over the open entries m of its row
 // ---------------------------------------------------------------------------
-template <typename T>
+template <typename T, int SR>
 __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t row0,
                                                       const T* __restrict__ WT, int64_t ldw,
                                                       const int* __restrict__ gprow,
@@ -663,7 +681,7 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
     T acc = Tr<T>::inf();
     for (int t = lane; t < cnt; t += 32) {
       const int64_t m = ocol[off + t];
-      acc = Tr<T>::relax(acc, *(volatile T*)(Drow + m), Wrow[m]);
+      acc = Tr<T, SR>::relax(acc, *(volatile T*)(Drow + m), Wrow[m]);
     }
     acc = warp_min<T>(acc);
     if (lane == 0 && acc < cur) {
@@ -677,11 +695,15 @@ template <typename T>
 cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw,
                          const int* gprow, const int* gpcol, const T* glb, int64_t nopen,
                          const int64_t* rowoff, const int* ocnt, const int* ocol, const int* chg_in,
-                         int* chg_out, int* any, cudaStream_t st) {
+                         int* chg_out, int* any, int sr, cudaStream_t st) {
   if (nopen <= 0) return cudaSuccess;
   int grid = (int)std::min<int64_t>(cdiv(nopen, 8), (int64_t)num_sms() * 8);
-  k_sparse_round<T><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff,
-                                          ocnt, ocol, chg_in, chg_out, any);
+  if (sr)
+    k_sparse_round<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff,
+                                               ocnt, ocol, chg_in, chg_out, any);
+  else
+    k_sparse_round<T, 0><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff,
+                                               ocnt, ocol, chg_in, chg_out, any);
   return cudaGetLastError();
 }
 
@@ -697,21 +719,21 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
   template cudaError_t shortlist_remove<T>(int*, T*, T*, int64_t, int64_t, int64_t, cudaStream_t); \
   template cudaError_t sparse_short<T>(T*, int64_t, int64_t, const int*, const T*, const T*,       \
                                        const int*, const int*, const T*, int64_t, unsigned char*,  \
-                                       int, cudaStream_t);                                        \
+                                       int, int, cudaStream_t);                                   \
   template cudaError_t sparse_phase_a<T>(T*, int64_t, Rows, int64_t, const int*, const T*,         \
                                          const T*, const int64_t*, const int*, const int*,         \
                                          const int*, const T*, int64_t, unsigned char*, int*, int*, \
                                          int*, int*, T*, unsigned char*, int64_t, DetectCounters*, \
-                                         cudaStream_t);                                           \
+                                         int, cudaStream_t);                                      \
   template cudaError_t sparse_compact<T>(Rows, const int64_t*, const int*, const int*, const T*,   \
                                          const unsigned char*, int*, int*, int*, int*, T*,         \
                                          unsigned char*, int64_t, DetectCounters*, cudaStream_t);  \
   template cudaError_t sparse_full<T>(T*, int64_t, int64_t, const T*, int64_t, int64_t,            \
                                       const int*, const int*, const T*, const unsigned char*,      \
-                                      int64_t, cudaStream_t);                                     \
+                                      int64_t, int, cudaStream_t);                                \
   template cudaError_t sparse_round<T>(T*, int64_t, int64_t, const T*, int64_t, const int*,        \
                                        const int*, const T*, int64_t, const int64_t*, const int*,  \
-                                       const int*, const int*, int*, int*, cudaStream_t);
+                                       const int*, const int*, int*, int*, int, cudaStream_t);
 INST(int32_t)
 INST(float)
 #undef INST

@@ -151,17 +151,21 @@ cudaError_t fill(T* p, int64_t count, T v, cudaStream_t st) {
 }
 
 // out[i] = sat(D[i][col] + add) for the local rows (global index i)
-template <typename T>
+template <typename T, int SR>
 __global__ void k_gather_col(const T* D, int64_t ld, Rows r, int64_t col, T add, T* out) {
   for (int64_t i = r.lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.hi;
        i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = Tr<T>::sat(Tr<T>::add(D[(i - r.row0) * ld + col], add));
+    out[i] = Tr<T, SR>::sat(Tr<T, SR>::add(D[(i - r.row0) * ld + col], add));
 }
 template <typename T>
-cudaError_t gather_col(const T* D, int64_t ld, Rows r, int64_t col, T add, T* out, cudaStream_t st) {
+cudaError_t gather_col(const T* D, int64_t ld, Rows r, int64_t col, T add, T* out, int sr,
+                       cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
   int grid = (int)std::min<int64_t>(cdiv(r.hi - r.lo, 256), 4 * num_sms());
-  k_gather_col<T><<<grid, 256, 0, st>>>(D, ld, r, col, add, out);
+  if (sr)
+    k_gather_col<T, 1><<<grid, 256, 0, st>>>(D, ld, r, col, add, out);
+  else
+    k_gather_col<T, 0><<<grid, 256, 0, st>>>(D, ld, r, col, add, out);
   return cudaGetLastError();
 }
 
@@ -216,12 +220,17 @@ static Tiling make_tiling(int64_t n, int64_t rows, int max_slabs, int chunk_vec 
 constexpr int P1_V = 4;
 constexpr int P1_VEC = 32 * P1_V;   // 512 columns per chunk
 constexpr int P1_RB = 16;           // rows per shared-memory batch
-template <typename T>
-__device__ __forceinline__ T max_add(T m, T d, T negw) {
-  if constexpr (Tr<T>::kFloat) return fmaxf(m, __fadd_rn(d, negw));   // NaN (inf-inf) ignored
-  else return max(m, d + negw);                                        // |d + negw| <= INF
+// Row-skip term of pass 1.  Shortest path: M = max_t d - out[t] (w = -out).
+// Minimax: a change at (i, j) needs max(col[i], out[t*]) < D[i][t*] for the
+// t* attaining row[j] (since D[i][j] <= max(D[i][t*], D[t*][j]) and
+// D[t*][j] < D[i][j]); so M = max_t {D[i][t] : out[t] < D[i][t]} (w = out).
+template <typename T, int SR>
+__device__ __forceinline__ T max_add(T m, T d, T w) {
+  if constexpr (SR == 1) return (w < d && d > m) ? d : m;
+  else if constexpr (Tr<T>::kFloat) return fmaxf(m, __fadd_rn(d, w));   // NaN (inf-inf) ignored
+  else return max(m, d + w);                                            // |d + w| <= INF
 }
-template <typename T>
+template <typename T, int SR>
 __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ D, int64_t ld, Rows r,
                                                           int64_t n, Tiling tl,
                                                           const T* __restrict__ ow,
@@ -249,8 +258,9 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
     qv[v] = (int64_t)chunk * P1_VEC + v * 32 + lane;
     inw[v] = qv[v] < tl.n4 ? ld4<T>(iw + 4 * qv[v]) : Vec4<T>{I, I, I, I};
     Vec4<T> o = qv[v] < tl.n4 ? ld4<T>(ow + 4 * qv[v]) : Vec4<T>{I, I, I, I};
-    // -out[t]; an absent out-edge (INF) can never give a shortcut: -INF-ish
-    nout[v] = Vec4<T>{-o.x, -o.y, -o.z, -o.w};
+    // shortest path: -out[t] (an absent out-edge, INF, can never give a
+    // shortcut: -INF); minimax: out[t] itself (see max_add)
+    nout[v] = SR ? o : Vec4<T>{-o.x, -o.y, -o.z, -o.w};
     colp[v] = Vec4<T>{I, I, I, I};
   }
   for (int64_t b0 = i_lo; b0 < i_hi; b0 += P1_RB) {
@@ -283,18 +293,18 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
       T p0 = I, p1 = I, m0 = NI, m1 = NI;
 #pragma unroll
       for (int v = 0; v < P1_V; ++v) {
-        p0 = Tr<T>::relax(p0, d0[v].x, inw[v].x); p0 = Tr<T>::relax(p0, d0[v].y, inw[v].y);
-        p0 = Tr<T>::relax(p0, d0[v].z, inw[v].z); p0 = Tr<T>::relax(p0, d0[v].w, inw[v].w);
-        p1 = Tr<T>::relax(p1, d1[v].x, inw[v].x); p1 = Tr<T>::relax(p1, d1[v].y, inw[v].y);
-        p1 = Tr<T>::relax(p1, d1[v].z, inw[v].z); p1 = Tr<T>::relax(p1, d1[v].w, inw[v].w);
-        m0 = max_add<T>(m0, d0[v].x, nout[v].x); m0 = max_add<T>(m0, d0[v].y, nout[v].y);
-        m0 = max_add<T>(m0, d0[v].z, nout[v].z); m0 = max_add<T>(m0, d0[v].w, nout[v].w);
-        m1 = max_add<T>(m1, d1[v].x, nout[v].x); m1 = max_add<T>(m1, d1[v].y, nout[v].y);
-        m1 = max_add<T>(m1, d1[v].z, nout[v].z); m1 = max_add<T>(m1, d1[v].w, nout[v].w);
-        colp[v].x = Tr<T>::relax(Tr<T>::relax(colp[v].x, o0, d0[v].x), o1, d1[v].x);
-        colp[v].y = Tr<T>::relax(Tr<T>::relax(colp[v].y, o0, d0[v].y), o1, d1[v].y);
-        colp[v].z = Tr<T>::relax(Tr<T>::relax(colp[v].z, o0, d0[v].z), o1, d1[v].z);
-        colp[v].w = Tr<T>::relax(Tr<T>::relax(colp[v].w, o0, d0[v].w), o1, d1[v].w);
+        p0 = Tr<T, SR>::relax(p0, d0[v].x, inw[v].x); p0 = Tr<T, SR>::relax(p0, d0[v].y, inw[v].y);
+        p0 = Tr<T, SR>::relax(p0, d0[v].z, inw[v].z); p0 = Tr<T, SR>::relax(p0, d0[v].w, inw[v].w);
+        p1 = Tr<T, SR>::relax(p1, d1[v].x, inw[v].x); p1 = Tr<T, SR>::relax(p1, d1[v].y, inw[v].y);
+        p1 = Tr<T, SR>::relax(p1, d1[v].z, inw[v].z); p1 = Tr<T, SR>::relax(p1, d1[v].w, inw[v].w);
+        m0 = max_add<T, SR>(m0, d0[v].x, nout[v].x); m0 = max_add<T, SR>(m0, d0[v].y, nout[v].y);
+        m0 = max_add<T, SR>(m0, d0[v].z, nout[v].z); m0 = max_add<T, SR>(m0, d0[v].w, nout[v].w);
+        m1 = max_add<T, SR>(m1, d1[v].x, nout[v].x); m1 = max_add<T, SR>(m1, d1[v].y, nout[v].y);
+        m1 = max_add<T, SR>(m1, d1[v].z, nout[v].z); m1 = max_add<T, SR>(m1, d1[v].w, nout[v].w);
+        colp[v].x = Tr<T, SR>::relax(Tr<T, SR>::relax(colp[v].x, o0, d0[v].x), o1, d1[v].x);
+        colp[v].y = Tr<T, SR>::relax(Tr<T, SR>::relax(colp[v].y, o0, d0[v].y), o1, d1[v].y);
+        colp[v].z = Tr<T, SR>::relax(Tr<T, SR>::relax(colp[v].z, o0, d0[v].z), o1, d1[v].z);
+        colp[v].w = Tr<T, SR>::relax(Tr<T, SR>::relax(colp[v].w, o0, d0[v].w), o1, d1[v].w);
       }
       rp[rr][lane] = p0;
       rm[rr][lane] = m0;
@@ -327,7 +337,7 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
 template <typename T>
 cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow, const T* iw,
                           T* rowpart, T* rowpartM, T* colpart, int64_t part_ld, int* nchunk_out,
-                          int* nslab_out, int max_slabs, cudaStream_t st) {
+                          int* nslab_out, int max_slabs, int sr, cudaStream_t st) {
   Tiling tl = make_tiling(n, r.hi - r.lo, max_slabs, P1_VEC, 48);
   *nchunk_out = tl.nchunk;
   *nslab_out = tl.nslab;
@@ -338,8 +348,12 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
     return e;
   }
   int grid = (int)cdiv(tl.warps, 8);
-  k_addnode_pass1<T><<<grid, 256, 0, st>>>(D, ld, r, n, tl, ow, iw, rowpart, rowpartM, colpart,
-                                           part_ld);
+  if (sr)
+    k_addnode_pass1<T, 1><<<grid, 256, 0, st>>>(D, ld, r, n, tl, ow, iw, rowpart, rowpartM, colpart,
+                                                part_ld);
+  else
+    k_addnode_pass1<T, 0><<<grid, 256, 0, st>>>(D, ld, r, n, tl, ow, iw, rowpart, rowpartM, colpart,
+                                                part_ld);
   return cudaGetLastError();
 }
 
@@ -386,7 +400,7 @@ cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, cons
 // ---------------------------------------------------------------------------
 // rank-1 min-plus relaxation  D[i][j] = min(D[i][j], c[i] + r[j] (, c2[i] + r2[j]))
 // ---------------------------------------------------------------------------
-template <typename T, bool TWO>
+template <typename T, bool TWO, int SR>
 __global__ void __launch_bounds__(256) k_rank1(T* __restrict__ D, int64_t ld, Rows r, int64_t n,
                                                Tiling tl, const T* __restrict__ c,
                                                const T* __restrict__ rv, const T* __restrict__ c2,
@@ -424,15 +438,15 @@ __global__ void __launch_bounds__(256) k_rank1(T* __restrict__ D, int64_t ld, Ro
     for (int v = 0; v < VPL; ++v) {
       if (qv[v] >= tl.n4) continue;
       Vec4<T> o = d[v];
-      o.x = Tr<T>::relax(o.x, ci, a[v].x);
-      o.y = Tr<T>::relax(o.y, ci, a[v].y);
-      o.z = Tr<T>::relax(o.z, ci, a[v].z);
-      o.w = Tr<T>::relax(o.w, ci, a[v].w);
+      o.x = Tr<T, SR>::relax(o.x, ci, a[v].x);
+      o.y = Tr<T, SR>::relax(o.y, ci, a[v].y);
+      o.z = Tr<T, SR>::relax(o.z, ci, a[v].z);
+      o.w = Tr<T, SR>::relax(o.w, ci, a[v].w);
       if (TWO) {
-        o.x = Tr<T>::relax(o.x, ci2, b[v].x);
-        o.y = Tr<T>::relax(o.y, ci2, b[v].y);
-        o.z = Tr<T>::relax(o.z, ci2, b[v].z);
-        o.w = Tr<T>::relax(o.w, ci2, b[v].w);
+        o.x = Tr<T, SR>::relax(o.x, ci2, b[v].x);
+        o.y = Tr<T, SR>::relax(o.y, ci2, b[v].y);
+        o.z = Tr<T, SR>::relax(o.z, ci2, b[v].z);
+        o.w = Tr<T, SR>::relax(o.w, ci2, b[v].w);
       }
       if (o.x != d[v].x || o.y != d[v].y || o.z != d[v].z || o.w != d[v].w)
         st4<T>(row + 4 * qv[v], o);
@@ -445,14 +459,18 @@ __global__ void __launch_bounds__(256) k_rank1(T* __restrict__ D, int64_t ld, Ro
 }
 template <typename T>
 cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, const T* c2,
-                  const T* rv2, unsigned long long* bytes_read, cudaStream_t st) {
+                  const T* rv2, unsigned long long* bytes_read, int sr, cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
   Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20);
   int grid = (int)cdiv(tl.warps, 8);
-  if (c2)
-    k_rank1<T, true><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, c2, rv2, bytes_read);
+  if (c2 && sr)
+    k_rank1<T, true, 1><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, c2, rv2, bytes_read);
+  else if (c2)
+    k_rank1<T, true, 0><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, c2, rv2, bytes_read);
+  else if (sr)
+    k_rank1<T, false, 1><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, nullptr, nullptr, bytes_read);
   else
-    k_rank1<T, false><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, nullptr, nullptr, bytes_read);
+    k_rank1<T, false, 0><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, nullptr, nullptr, bytes_read);
   return cudaGetLastError();
 }
 
@@ -501,19 +519,19 @@ constexpr int DT_THREADS = 256;
 // Theorem-4 tightness of the 4 pairs of one vector: the common case (no bit)
 // costs one add + one compare per element; validity (j < n, j != i,
 // j != skip, D finite) is applied only when some bit is set.
-template <typename T, bool TWO>
+template <typename T, bool TWO, int SR>
 __device__ __forceinline__ unsigned flag_nibble(const Vec4<T>& d, const Vec4<T>& r1,
                                                 const Vec4<T>& r2, T c1, T c2, int64_t j0,
                                                 int64_t n, int64_t i, int64_t skip, float tau) {
-  unsigned nib = (unsigned)Tr<T>::tight(Tr<T>::add(c1, r1.x), d.x, tau) |
-                 (unsigned)Tr<T>::tight(Tr<T>::add(c1, r1.y), d.y, tau) << 1 |
-                 (unsigned)Tr<T>::tight(Tr<T>::add(c1, r1.z), d.z, tau) << 2 |
-                 (unsigned)Tr<T>::tight(Tr<T>::add(c1, r1.w), d.w, tau) << 3;
+  unsigned nib = (unsigned)Tr<T, SR>::tight(Tr<T, SR>::add(c1, r1.x), d.x, tau) |
+                 (unsigned)Tr<T, SR>::tight(Tr<T, SR>::add(c1, r1.y), d.y, tau) << 1 |
+                 (unsigned)Tr<T, SR>::tight(Tr<T, SR>::add(c1, r1.z), d.z, tau) << 2 |
+                 (unsigned)Tr<T, SR>::tight(Tr<T, SR>::add(c1, r1.w), d.w, tau) << 3;
   if (TWO)
-    nib |= (unsigned)Tr<T>::tight(Tr<T>::add(c2, r2.x), d.x, tau) |
-           (unsigned)Tr<T>::tight(Tr<T>::add(c2, r2.y), d.y, tau) << 1 |
-           (unsigned)Tr<T>::tight(Tr<T>::add(c2, r2.z), d.z, tau) << 2 |
-           (unsigned)Tr<T>::tight(Tr<T>::add(c2, r2.w), d.w, tau) << 3;
+    nib |= (unsigned)Tr<T, SR>::tight(Tr<T, SR>::add(c2, r2.x), d.x, tau) |
+           (unsigned)Tr<T, SR>::tight(Tr<T, SR>::add(c2, r2.y), d.y, tau) << 1 |
+           (unsigned)Tr<T, SR>::tight(Tr<T, SR>::add(c2, r2.z), d.z, tau) << 2 |
+           (unsigned)Tr<T, SR>::tight(Tr<T, SR>::add(c2, r2.w), d.w, tau) << 3;
   if (nib) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -538,7 +556,7 @@ __device__ __forceinline__ unsigned flag_nibble(const Vec4<T>& d, const Vec4<T>&
 // ---------------------------------------------------------------------------
 constexpr int DS_V = 4;              // vectors per lane per row
 constexpr int DS_VEC = 32 * DS_V;    // vectors per chunk (512 columns)
-template <typename T, bool TWO>
+template <typename T, bool TWO, int SR>
 __global__ void __launch_bounds__(256, 2) k_detect_stream(const T* __restrict__ D, int64_t ld, Rows r,
                                                           int64_t n, int64_t skip, Tiling tl,
                                                           const T* __restrict__ c1,
@@ -589,7 +607,7 @@ __global__ void __launch_bounds__(256, 2) k_detect_stream(const T* __restrict__ 
       unsigned word = 0;
 #pragma unroll
       for (int v = 0; v < DS_V; ++v)
-        word |= flag_nibble<T, TWO>(d[h][v], a[v], b[v], ci[h], cj[h], 4 * qv[v], n, i, skip, tau)
+        word |= flag_nibble<T, TWO, SR>(d[h][v], a[v], b[v], ci[h], cj[h], 4 * qv[v], n, i, skip, tau)
                 << (4 * v);
       bm[(i - r.lo) * bmld + chunk * 32 + lane] = (uint16_t)word;
       if (__any_sync(0xffffffffu, word != 0) && lane == 0) anyrow[i] = 1;
@@ -663,18 +681,24 @@ __global__ void __launch_bounds__(DT_THREADS) k_detect_emit(DetectArgs<T> a,
 
 template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
-                   const T* c2, const T* r2, float tau, uint32_t* bm32, int* anyrow, cudaStream_t st) {
+                   const T* c2, const T* r2, float tau, uint32_t* bm32, int* anyrow, int sr,
+                   cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
   uint16_t* bm = reinterpret_cast<uint16_t*>(bm32);
   Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20, DS_VEC, 32);
   const int64_t bmld = (int64_t)tl.nchunk * 32;
   CUDA_TRY(cudaMemsetAsync(anyrow + r.lo, 0, sizeof(int) * (size_t)(r.hi - r.lo), st));
   const int g1 = (int)cdiv(tl.warps, 8);
-  if (c2)
-    k_detect_stream<T, true><<<g1, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, c2, r2, tau, bm, bmld, anyrow);
+  if (c2 && sr)
+    k_detect_stream<T, true, 1><<<g1, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, c2, r2, tau, bm, bmld, anyrow);
+  else if (c2)
+    k_detect_stream<T, true, 0><<<g1, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, c2, r2, tau, bm, bmld, anyrow);
+  else if (sr)
+    k_detect_stream<T, false, 1><<<g1, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, nullptr, nullptr, tau, bm,
+                                                     bmld, anyrow);
   else
-    k_detect_stream<T, false><<<g1, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, nullptr, nullptr, tau, bm,
-                                                  bmld, anyrow);
+    k_detect_stream<T, false, 0><<<g1, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, nullptr, nullptr, tau, bm,
+                                                     bmld, anyrow);
   return cudaGetLastError();
 }
 
@@ -842,18 +866,18 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
                                        cudaStream_t);                                             \
   template cudaError_t fill<T>(T*, int64_t, T, cudaStream_t);                                      \
   template cudaError_t init_d<T>(T*, int64_t, Rows, int64_t, const T*, int64_t, cudaStream_t);     \
-  template cudaError_t gather_col<T>(const T*, int64_t, Rows, int64_t, T, T*, cudaStream_t);       \
+  template cudaError_t gather_col<T>(const T*, int64_t, Rows, int64_t, T, T*, int, cudaStream_t);  \
   template cudaError_t copy_vec<T>(const T*, int64_t, int64_t, T, T*, cudaStream_t);               \
   template cudaError_t addnode_pass1<T>(const T*, int64_t, Rows, int64_t, const T*, const T*, T*,  \
-                                        T*, T*, int64_t, int*, int*, int, cudaStream_t);          \
+                                        T*, T*, int64_t, int*, int*, int, int, cudaStream_t);     \
   template cudaError_t addnode_finish<T>(const T*, const T*, int, const T*, int, int64_t, Rows,    \
                                          int64_t, int64_t, T*, T*, T*, cudaStream_t);             \
   template cudaError_t rank1<T>(T*, int64_t, Rows, int64_t, const T*, const T*, const T*,          \
-                                const T*, unsigned long long*, cudaStream_t);                     \
+                                const T*, unsigned long long*, int, cudaStream_t);                \
   template cudaError_t addnode_write<T>(T*, int64_t, Rows, int64_t, int64_t, int, const T*,        \
                                         const T*, T*, int64_t, const T*, const T*, cudaStream_t); \
   template cudaError_t detect<T>(T*, int64_t, Rows, int64_t, int64_t, const T*, const T*,          \
-                                 const T*, const T*, float, uint32_t*, int*, cudaStream_t);       \
+                                 const T*, const T*, float, uint32_t*, int*, int, cudaStream_t);  \
   template cudaError_t detect_emit<T>(T*, int64_t, Rows, int64_t, const T*, int64_t, int,          \
                                       int64_t*, int*, int*, int*, T*, int64_t, DetectCounters*,    \
                                       const uint32_t*, const int*, cudaStream_t);                 \

@@ -143,6 +143,28 @@ apsp_status apsp_create(apsp_handle** out, apsp_dtype dtype, int directed, int64
                         void* workspace, size_t workspace_bytes, void* stream, int rank,
                         int world, const void* nccl_id);
 
+/* In-process rank group: the row-sharded path with every rank
+ * a host THREAD of one process, all ranks on the calling threads' current
+ * device.  Used to exercise the multi-rank code (partition, owner broadcasts,
+ * reductions, swap-with-last across ranks) bit-for-bit on fewer GPUs than
+ * ranks; production multi-GPU runs use apsp_create with NCCL.  A collective
+ * is a host rendezvous of all ranks followed by device-to-device copies (and,
+ * for reductions, one kernel) ordered against each rank's stream with CUDA
+ * events — no kernel ever waits on another kernel.  The group owns 8 MiB of
+ * device scratch (the one device allocation the library makes).
+ *   apsp_local_group_create: world in [1, 16]; *group receives the group.
+ *   apsp_create_local: as apsp_create with world = the group's size and the
+ *     group in place of the NCCL id; every rank's thread calls every API
+ *     function with identical arguments (SPMD), concurrently.
+ *   apsp_local_group_destroy: after every handle of the group is destroyed.
+ * Errors: E_INVAL (bad world / null), E_CUDA (scratch allocation). */
+apsp_status apsp_local_group_create(int world, void** group);
+apsp_status apsp_local_group_destroy(void* group);
+apsp_status apsp_create_local(apsp_handle** out, apsp_dtype dtype, int directed, int64_t n,
+                              int64_t cap, const void* W, int64_t ldw, void* D_local, int64_t ld,
+                              void* workspace, size_t workspace_bytes, void* stream, int rank,
+                              void* group);
+
 apsp_status apsp_destroy(apsp_handle* h);
 
 apsp_status apsp_set_option(apsp_handle* h, apsp_option opt, double value);

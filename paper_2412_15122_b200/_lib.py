@@ -28,6 +28,7 @@ SYMBOLS = [
     "sp_pair_query_batch", "apsp_size", "apsp_last_error", "apsp_status_string",
     "apsp_nccl_unique_id", "apsp_kernel_launches", "apsp_profile_enable", "apsp_profile_reset",
     "apsp_profile_read", "apsp_modify_edge_readd", "apsp_get_weight",
+    "apsp_local_group_create", "apsp_local_group_destroy", "apsp_create_local",
 ]
 # kernel classes of apsp_profile_read (apsp_kernel_class)
 K_CLASSES = ["fw_diag", "fw_panel", "fw_tile", "add_pass1", "rank1", "detect", "sparse0",
@@ -65,6 +66,10 @@ def _load():
         "apsp_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int, i64, ctypes.c_int]),
         "apsp_create": (ctypes.c_int, [P(vp), ctypes.c_int, ctypes.c_int, i64, i64, vp, i64, vp, i64, vp,
                                        ctypes.c_size_t, vp, ctypes.c_int, ctypes.c_int, vp]),
+        "apsp_local_group_create": (ctypes.c_int, [ctypes.c_int, P(vp)]),
+        "apsp_local_group_destroy": (ctypes.c_int, [vp]),
+        "apsp_create_local": (ctypes.c_int, [P(vp), ctypes.c_int, ctypes.c_int, i64, i64, vp, i64, vp, i64,
+                                             vp, ctypes.c_size_t, vp, ctypes.c_int, vp]),
         "apsp_destroy": (ctypes.c_int, [vp]),
         "apsp_set_option": (ctypes.c_int, [vp, ctypes.c_int, dbl]),
         "apsp_cold_fw": (ctypes.c_int, [vp]),
@@ -120,6 +125,24 @@ def apsp_create(dtype, directed, n, cap, W_ptr, ldw, D_ptr, ld, ws_ptr, ws_bytes
     st = lib.apsp_create(ctypes.byref(h), dtype, int(directed), n, cap, W_ptr, ldw, D_ptr, ld, ws_ptr,
                          ws_bytes, stream, rank, world, idbuf)
     check(None, st)
+    return h
+
+
+def apsp_local_group_create(world):
+    g = ctypes.c_void_p()
+    check(None, lib.apsp_local_group_create(world, ctypes.byref(g)))
+    return g
+
+
+def apsp_local_group_destroy(g):
+    check(None, lib.apsp_local_group_destroy(g))
+
+
+def apsp_create_local(dtype, directed, n, cap, W_ptr, ldw, D_ptr, ld, ws_ptr, ws_bytes, stream, rank,
+                      group):
+    h = ctypes.c_void_p()
+    check(None, lib.apsp_create_local(ctypes.byref(h), dtype, int(directed), n, cap, W_ptr, ldw, D_ptr, ld,
+                                      ws_ptr, ws_bytes, stream, rank, group))
     return h
 
 

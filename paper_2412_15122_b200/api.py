@@ -23,7 +23,7 @@ class WarmAPSP:
     """
 
     def __init__(self, W, directed=True, cap=None, device=None, stream=None, rank=0, world=1,
-                 nccl_id=None, cold_start=True, semiring="shortest"):
+                 nccl_id=None, cold_start=True, semiring="shortest", local_group=None):
         W = torch.as_tensor(W)
         if W.dtype not in _DT:
             raise TypeError("W must be int32 or float32")
@@ -42,9 +42,17 @@ class WarmAPSP:
             nbytes = L.apsp_workspace_bytes(self.cdtype, cap, world)
             self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
             Wd = W.to(self.device).contiguous()
-            self.h = L.apsp_create(self.cdtype, self.directed, n, cap, Wd.data_ptr(), Wd.stride(0),
-                                   self.D_local.data_ptr(), self.ld, self.workspace.data_ptr(), nbytes,
-                                   self.stream.cuda_stream, rank, world, nccl_id)
+            # the copy ran on torch's current stream; the library reads W on its own
+            self.stream.wait_stream(torch.cuda.current_stream(self.device))
+            if local_group is not None:   # in-process rank group (apsp_create_local)
+                self.h = L.apsp_create_local(self.cdtype, self.directed, n, cap, Wd.data_ptr(),
+                                             Wd.stride(0), self.D_local.data_ptr(), self.ld,
+                                             self.workspace.data_ptr(), nbytes, self.stream.cuda_stream,
+                                             rank, local_group)
+            else:
+                self.h = L.apsp_create(self.cdtype, self.directed, n, cap, Wd.data_ptr(), Wd.stride(0),
+                                       self.D_local.data_ptr(), self.ld, self.workspace.data_ptr(), nbytes,
+                                       self.stream.cuda_stream, rank, world, nccl_id)
             del Wd
         if semiring not in ("shortest", "minimax"):
             raise ValueError("semiring must be 'shortest' or 'minimax'")
@@ -128,10 +136,13 @@ class WarmAPSP:
         paths = torch.full((q, max(path_cap, 1)), -1, dtype=torch.int32, device=self.device)
         lens = torch.empty(q, dtype=torch.int32, device=self.device)
         nc = torch.empty(q, dtype=torch.int32, device=self.device)
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
         L.sp_pair_query_batch(self.h, q, s.data_ptr(), t.data_ptr(), dist.data_ptr(), paths.data_ptr(),
                               path_cap, lens.data_ptr(), nc.data_ptr())
         return dist, paths, lens, nc
 
     def _vec(self, v):
         v = torch.as_tensor(v if not isinstance(v, np.ndarray) else np.ascontiguousarray(v))
-        return v.to(device=self.device, dtype=self.dtype).contiguous()
+        v = v.to(device=self.device, dtype=self.dtype).contiguous()
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        return v

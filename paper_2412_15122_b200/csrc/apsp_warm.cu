@@ -5,7 +5,6 @@
 // decisions the paper's algorithms contain (early exits, the cost gate of
 // P:196), carves the caller's workspace, and issues NCCL collectives when D
 // is row-sharded over several GPUs.
-#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -19,6 +18,7 @@
 
 #include "../../include/apsp_warm.h"
 #include "common.cuh"
+#include "comm.h"
 #include "kernels.h"
 
 using namespace apsp;
@@ -28,60 +28,19 @@ namespace {
 constexpr int64_t kTile = 128;       // FW pivot block / row-partition granule
 constexpr int kMaxSlabs = 256;       // add-node column partial slabs
 constexpr int64_t kVecs = 8;         // scratch vectors of ld elements
+constexpr int kQueryChunk = 32;      // sharded queries per column all-gather
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// ------------------------------------------------------------------ NCCL (dlopen)
-struct Nccl {
-  bool tried = false, ok = false;
-  void* h = nullptr;
-  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*GroupStart)() = nullptr;
-  ncclResult_t (*GroupEnd)() = nullptr;
-  const char* (*GetErrorString)(ncclResult_t) = nullptr;
-  bool load() {
-    if (tried) return ok;
-    tried = true;
-    // RTLD_LOCAL: the library's NCCL symbols never interpose on the copy the
-    // host framework (torch) may have loaded; APSP_NCCL_LIB overrides the path.
-    const char* path = getenv("APSP_NCCL_LIB");
-    h = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
-    if (!h) return false;
-#define SYM(name, field)                                            \
-  field = reinterpret_cast<decltype(field)>(dlsym(h, "nccl" name)); \
-  if (!field) return false;
-    SYM("GetUniqueId", GetUniqueId)
-    SYM("CommInitRank", CommInitRank)
-    SYM("CommDestroy", CommDestroy)
-    SYM("Broadcast", Broadcast)
-    SYM("AllReduce", AllReduce)
-    SYM("Send", Send)
-    SYM("Recv", Recv)
-    SYM("GroupStart", GroupStart)
-    SYM("GroupEnd", GroupEnd)
-    SYM("GetErrorString", GetErrorString)
-#undef SYM
-    ok = true;
-    return true;
-  }
-};
-Nccl g_nccl;
 
 // ------------------------------------------------------------------ workspace plan
 struct Plan {
   int64_t ld, lcap, ocap, maxchunk;
   size_t off_wt, off_vec, off_rowpart, off_colpart, off_rowoff, off_rowcnt, off_chg, off_prow,
       off_pcol, off_plb, off_popen, off_ocol, off_ocnt, off_gprow, off_gpcol, off_glb, off_gfull,
-      off_slid, off_slw, off_wnext, off_panel, off_pt, off_bm, off_anyrow, off_small, total;
+      off_slid, off_slw, off_wnext, off_panel, off_pt, off_bm, off_anyrow, off_qsend, off_qcol,
+      off_small, total;
   int64_t ldpt;
 };
 
@@ -127,6 +86,9 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   const int64_t rows_max = world > 1 ? round_up(cdiv(cap, world), kTile) : cap;
   p.off_bm = take(sizeof(uint32_t) * (size_t)rows_max * cdiv(cdiv(p.ld, 4), 256) * 32);
   p.off_anyrow = take(sizeof(int32_t) * (size_t)cap);
+  // sharded queries: this rank's slices of kQueryChunk columns, and all ranks' (all-gathered)
+  p.off_qsend = take(world > 1 ? sizeof(int32_t) * (size_t)kQueryChunk * rows_max : 256);
+  p.off_qcol = take(world > 1 ? sizeof(int32_t) * (size_t)kQueryChunk * rows_max * world : 256);
   p.off_small = take(64 * 1024);
   p.total = o;
   return p;
@@ -153,7 +115,7 @@ struct apsp_handle {
   Plan plan;
   cudaStream_t st;
   int rank, world;
-  ncclComm_t comm = nullptr;
+  Comm* comm = nullptr;          // world > 1: NCCL or in-process group (comm.h)
   // options
   int force_path = 0;
   double theta = 0.02;
@@ -230,6 +192,8 @@ struct apsp_handle {
   template <typename T> T* panel() { return reinterpret_cast<T*>(ws + plan.off_panel); }
   template <typename T> T* pt() { return reinterpret_cast<T*>(ws + plan.off_pt); }
   uint32_t* bm() { return reinterpret_cast<uint32_t*>(ws + plan.off_bm); }
+  template <typename T> T* qsend() { return reinterpret_cast<T*>(ws + plan.off_qsend); }
+  template <typename T> T* qcol() { return reinterpret_cast<T*>(ws + plan.off_qcol); }
   int* anyrow() { return reinterpret_cast<int*>(ws + plan.off_anyrow); }
   DetectCounters* ctr() { return reinterpret_cast<DetectCounters*>(ws + plan.off_small); }
   int* anyflag() { return reinterpret_cast<int*>(ws + plan.off_small + 256); }
@@ -294,9 +258,9 @@ apsp_status fail(apsp_handle* h, apsp_status s, const char* fmt, ...) {
   } while (0)
 #define NK(expr)                                                                          \
   do {                                                                                    \
-    ncclResult_t _r = (expr);                                                             \
-    if (_r != ncclSuccess)                                                                \
-      return fail(h, APSP_E_NCCL, "%s failed: %s", #expr, g_nccl.GetErrorString(_r));    \
+    int _r = (expr);                                                                      \
+    if (_r != 0)                                                                          \
+      return fail(h, APSP_E_NCCL, "%s failed: %s", #expr, h->comm->errstr(_r));          \
   } while (0)
 #define CHECK_HANDLE(h)                                                                   \
   do {                                                                                    \
@@ -312,7 +276,7 @@ template <> ncclDataType_t nccl_type<float>() { return ncclFloat32; }
 template <typename T>
 apsp_status bcast_from_owner(apsp_handle* h, T* buf, int64_t count, int64_t gi) {
   if (h->world <= 1) return APSP_OK;
-  NK(g_nccl.Broadcast(buf, buf, (size_t)count, nccl_type<T>(), h->owner(gi), h->comm, h->st));
+  NK(h->comm->bcast(buf, (size_t)count, nccl_type<T>(), h->owner(gi), h->st));
   return APSP_OK;
 }
 
@@ -345,7 +309,7 @@ apsp_status fw_impl(apsp_handle* h) {
       P = h->panel<T>();
     }
     if (h->world > 1) {
-      NK(g_nccl.Broadcast(P, P, (size_t)kb * ld, nccl_type<T>(), h->owner(K0), h->comm, h->st));
+      NK(h->comm->bcast(P, (size_t)kb * ld, nccl_type<T>(), h->owner(K0), h->st));
     }
     const int skip_ti = own ? (int)(lk / kTile) : -1;
     if (m > 0) {
@@ -394,8 +358,8 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     long long* v = reinterpret_cast<long long*>(h->small());
     long long hv[4] = {(long long)total, (long long)rows, (long long)overflow, (long long)maxrow};
     CKR(cudaMemcpyAsync(v, hv, sizeof hv, cudaMemcpyHostToDevice, h->st));
-    NK(g_nccl.AllReduce(v, v, 3, ncclInt64, ncclSum, h->comm, h->st));
-    NK(g_nccl.AllReduce(v + 3, v + 3, 1, ncclInt64, ncclMax, h->comm, h->st));
+    NK(h->comm->allreduce(v, 3, ncclInt64, ncclSum, h->st));
+    NK(h->comm->allreduce(v + 3, 1, ncclInt64, ncclMax, h->st));
     CKR(cudaMemcpyAsync(hs, v, sizeof hv, cudaMemcpyDeviceToHost, h->st));
     CKR(cudaStreamSynchronize(h->st));
     total = (int64_t)hs[0]; rows = (int64_t)hs[1]; overflow = (int64_t)hs[2]; maxrow = (int64_t)hs[3];
@@ -434,7 +398,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     long long* v = reinterpret_cast<long long*>(h->small());
     long long hv2[2] = {(long long)nopen, (long long)ovf};
     CKR(cudaMemcpyAsync(v, hv2, sizeof hv2, cudaMemcpyHostToDevice, h->st));
-    NK(g_nccl.AllReduce(v, v, 2, ncclInt64, ncclSum, h->comm, h->st));
+    NK(h->comm->allreduce(v, 2, ncclInt64, ncclSum, h->st));
     CKR(cudaMemcpyAsync(hs, v, sizeof hv2, cudaMemcpyDeviceToHost, h->st));
     CKR(cudaStreamSynchronize(h->st));
     ovf = (int64_t)hs[1];
@@ -474,7 +438,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
       in ^= 1;
     }
     if (h->world > 1)
-      NK(g_nccl.AllReduce(h->anyflag(), h->anyflag(), 1, ncclInt32, ncclMax, h->comm, h->st));
+      NK(h->comm->allreduce(h->anyflag(), 1, ncclInt32, ncclMax, h->st));
     CKR(cudaMemcpyAsync(hflag, h->anyflag(), sizeof(int), cudaMemcpyDeviceToHost, h->st));
     CKR(cudaStreamSynchronize(h->st));
     if (*hflag == 0) converged = true;   // the batch's last round changed nothing
@@ -519,7 +483,7 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
                        ceff, row, h->st));
   if (h->world > 1)
-    NK(g_nccl.AllReduce(row, row, (size_t)ld, nccl_type<T>(), ncclMin, h->comm, h->st));
+    NK(h->comm->allreduce(row, (size_t)ld, nccl_type<T>(), ncclMin, h->st));
   // rows with ceff[i] = INF provably do not change and are not read at all
   PK(APSP_K_RANK1, 0.0,   // work: bytes actually read, counted on the device
      rank1<T>(h->Dl<T>(), ld, r, n, ceff, row, nullptr, nullptr, h->rank1_bytes(), h->sr, h->st));
@@ -561,10 +525,9 @@ apsp_status remove_node_impl(apsp_handle* h, int64_t k, int64_t* moved_from, aps
     if (ok_k && ok_l) {
       CK(copy_row<T>(h->Drow<T>(k), h->Drow<T>(last), n, h->st));
     } else if (ok_k || ok_l) {
-      NK(g_nccl.GroupStart());
-      if (ok_l) NK(g_nccl.Send(h->Drow<T>(last), (size_t)n, nccl_type<T>(), h->owner(k), h->comm, h->st));
-      if (ok_k) NK(g_nccl.Recv(h->Drow<T>(k), (size_t)n, nccl_type<T>(), h->owner(last), h->comm, h->st));
-      NK(g_nccl.GroupEnd());
+      P2POp op = ok_l ? P2POp{1, h->Drow<T>(last), (size_t)n, nccl_type<T>(), h->owner(k)}
+                      : P2POp{0, h->Drow<T>(k), (size_t)n, nccl_type<T>(), h->owner(last)};
+      NK(h->comm->sendrecv(&op, 1, h->st));
     }
     CK(copy_row<T>(WT + k * ld, WT + last * ld, n, h->st));
     Rows rc = r;     // rows [lo, hi) with hi <= n: includes the new row k, excludes row last
@@ -597,7 +560,7 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
   if (h->local(u))
     CKR(cudaMemcpyAsync(dev2 + 1, h->Drow<T>(u) + v, sizeof(T), cudaMemcpyDeviceToDevice, h->st));
   if (h->world > 1)
-    NK(g_nccl.Broadcast(dev2 + 1, dev2 + 1, 1, nccl_type<T>(), h->owner(u), h->comm, h->st));
+    NK(h->comm->bcast(dev2 + 1, 1, nccl_type<T>(), h->owner(u), h->st));
   T* hv = reinterpret_cast<T*>(h->host_small);
   CKR(cudaMemcpyAsync(hv, dev2, 2 * sizeof(T), cudaMemcpyDeviceToHost, h->st));
   CKR(cudaStreamSynchronize(h->st));
@@ -682,7 +645,7 @@ apsp_status removal_phi(apsp_handle* h, int64_t k, int64_t* phi) {
   CKR(cudaMemsetAsync(cnt, 0, sizeof *cnt, h->st));
   CK(count_nonzero(h->anyrow() + r.lo, r.hi - r.lo, cnt, h->st));
   if (h->world > 1)
-    NK(g_nccl.AllReduce(cnt, cnt, 1, ncclUint64, ncclSum, h->comm, h->st));
+    NK(h->comm->allreduce(cnt, 1, ncclUint64, ncclSum, h->st));
   unsigned long long* hv = reinterpret_cast<unsigned long long*>(h->host_small);
   CKR(cudaMemcpyAsync(hv, cnt, sizeof *cnt, cudaMemcpyDeviceToHost, h->st));
   CKR(cudaStreamSynchronize(h->st));
@@ -701,10 +664,8 @@ apsp_status swap_nodes(apsp_handle* h, int64_t p, int64_t q) {
     T* mine = lp ? h->Drow<T>(p) : h->Drow<T>(q);
     const int peer = h->owner(lp ? q : p);
     T* tmp = h->panel<T>();
-    NK(g_nccl.GroupStart());
-    NK(g_nccl.Send(mine, (size_t)n, nccl_type<T>(), peer, h->comm, h->st));
-    NK(g_nccl.Recv(tmp, (size_t)n, nccl_type<T>(), peer, h->comm, h->st));
-    NK(g_nccl.GroupEnd());
+    P2POp ops[2] = {{1, mine, (size_t)n, nccl_type<T>(), peer}, {0, tmp, (size_t)n, nccl_type<T>(), peer}};
+    NK(h->comm->sendrecv(ops, 2, h->st));
     CK(copy_row<T>(mine, tmp, n, h->st));
   }
   CK(swap_cols<T>(h->Dl<T>(), ld, h->active(), p, q, h->st));
@@ -772,6 +733,41 @@ apsp_status modify_readd_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, int
 }
 
 // ------------------------------------------------------------------ query
+// Batched queries on device arrays.  world == 1: one kernel.  world > 1 (row-
+// sharded D, f3 of SURVEY §8(f)): per chunk of kQueryChunk queries, gather the
+// column-t slices of every rank (one all-gather), let the owner of row s answer,
+// and all-reduce(sum) the outputs (non-owners contribute zeros).  No rank
+// gathers whole rows; WT is replicated, so the Dijkstra step is local.
+template <typename T>
+apsp_status query_dispatch(apsp_handle* h, int q, const int* s, const int* t, T* dist, int* paths,
+                           int path_cap, int* lens, int* ncand) {
+  const int64_t n = h->n, ld = h->ld;
+  if (h->world <= 1) {
+    PK(APSP_K_QUERY, 8.0 * (double)n * q,
+       query_batch<T>(h->Dl<T>(), ld, h->WT<T>(), ld, n, q, s, t, dist, paths, path_cap, lens, ncand,
+                      h->tau, h->sr, h->st));
+    return APSP_OK;
+  }
+  Rows r = h->active();
+  const int64_t R = h->R;
+  for (int b0 = 0; b0 < q; b0 += kQueryChunk) {
+    const int c = std::min(kQueryChunk, q - b0);
+    CK(query_colslice<T>(h->Dl<T>(), ld, r.hi - r.lo, R, n, t + b0, c, h->qsend<T>(), h->st));
+    NK(h->comm->allgather(h->qsend<T>(), h->qcol<T>(), (size_t)c * R, nccl_type<T>(), h->st));
+    int* pb = path_cap > 0 ? paths + (int64_t)b0 * path_cap : paths;
+    PK(APSP_K_QUERY, 8.0 * (double)n * c,
+       query_batch<T>(h->Dl<T>(), ld, h->WT<T>(), ld, n, c, s + b0, t + b0, dist + b0, pb, path_cap,
+                      lens + b0, ncand ? ncand + b0 : nullptr, h->tau, h->sr, h->st, h->qcol<T>(), R,
+                      h->row0, r.hi - r.lo));
+    NK(h->comm->allreduce(dist + b0, (size_t)c, nccl_type<T>(), ncclSum, h->st));
+    NK(h->comm->allreduce(lens + b0, (size_t)c, ncclInt32, ncclSum, h->st));
+    if (ncand) NK(h->comm->allreduce(ncand + b0, (size_t)c, ncclInt32, ncclSum, h->st));
+    if (path_cap > 0)
+      NK(h->comm->allreduce(pb, (size_t)c * path_cap, ncclInt32, ncclSum, h->st));
+  }
+  return APSP_OK;
+}
+
 template <typename T>
 apsp_status query_one(apsp_handle* h, int64_t s, int64_t t, void* dist, int32_t* path,
                       int32_t path_cap, int32_t* path_len, int32_t* n_candidates) {
@@ -783,8 +779,8 @@ apsp_status query_one(apsp_handle* h, int64_t s, int64_t t, void* dist, int32_t*
   int* hv = reinterpret_cast<int*>(h->host_small);
   hv[0] = (int)s; hv[1] = (int)t;
   CKR(cudaMemcpyAsync(dv, hv, 2 * sizeof(int), cudaMemcpyHostToDevice, h->st));
-  PK(APSP_K_QUERY, 8.0 * (double)h->n, query_batch<T>(h->Dl<T>(), h->ld, h->WT<T>(), h->ld, h->n, 1, dv, dv + 1, ddist, dpath, cap_dev,
-                    dv + 2, dv + 3, h->tau, h->sr, h->st));
+  apsp_status qs = query_dispatch<T>(h, 1, dv, dv + 1, ddist, dpath, cap_dev, dv + 2, dv + 3);
+  if (qs != APSP_OK) return qs;
   CKR(cudaMemcpyAsync(hv, dv, 8 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
   CKR(cudaStreamSynchronize(h->st));
   const int len = hv[2], nc = hv[3];
@@ -850,23 +846,25 @@ const char* apsp_status_string(apsp_status s) {
 
 apsp_status apsp_nccl_unique_id(void* out128) {
   if (!out128) return APSP_E_INVAL;
-  if (!g_nccl.load()) return APSP_E_NCCL;
-  ncclUniqueId id;
-  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return APSP_E_NCCL;
-  std::memcpy(out128, &id, sizeof id);
-  return APSP_OK;
+  return nccl_unique_id(out128) ? APSP_OK : APSP_E_NCCL;
 }
 
-apsp_status apsp_create(apsp_handle** out, apsp_dtype dtype, int directed, int64_t n, int64_t cap,
+}  // extern "C"
+
+namespace {
+
+// Shared by apsp_create (NCCL) and apsp_create_local (in-process group):
+// exactly one of nccl_id / group is used when world > 1.
+apsp_status create_impl(apsp_handle** out, apsp_dtype dtype, int directed, int64_t n, int64_t cap,
                         const void* W, int64_t ldw, void* D_local, int64_t ld, void* workspace,
                         size_t workspace_bytes, void* stream, int rank, int world,
-                        const void* nccl_id) {
+                        const void* nccl_id, LocalGroup* group) {
   if (!out) return APSP_E_INVAL;
   *out = nullptr;
   if (dtype != APSP_I32 && dtype != APSP_F32) return APSP_E_INVAL;
   if (n < 1 || cap < n || cap > (int64_t)1 << 30 || !W || ldw < n || !D_local || !workspace)
     return APSP_E_INVAL;
-  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_id)) return APSP_E_INVAL;
+  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_id && !group)) return APSP_E_INVAL;
   if (((uintptr_t)workspace & 255) || ((uintptr_t)D_local & 15)) return APSP_E_INVAL;
   if (ld < round_up(cap, 32) || (ld & 3)) return APSP_E_INVAL;
   Plan plan = make_plan(cap, world, ld);
@@ -891,14 +889,9 @@ apsp_status apsp_create(apsp_handle** out, apsp_dtype dtype, int directed, int64
     return APSP_E_CUDA;
   }
   if (world > 1) {
-    if (!g_nccl.load()) {
-      cudaFreeHost(h->host_small);
-      delete h;
-      return APSP_E_NCCL;
-    }
-    ncclUniqueId id;
-    std::memcpy(&id, nccl_id, sizeof id);
-    if (g_nccl.CommInitRank(&h->comm, world, id, rank) != ncclSuccess) {
+    int err = 0;
+    h->comm = group ? make_local_comm(group, rank) : make_nccl_comm(nccl_id, world, rank, &err);
+    if (!h->comm) {
       cudaFreeHost(h->host_small);
       delete h;
       return APSP_E_NCCL;
@@ -919,7 +912,7 @@ apsp_status apsp_create(apsp_handle** out, apsp_dtype dtype, int directed, int64
     return APSP_OK;
   });
   if (s != APSP_OK) {
-    if (h->comm) g_nccl.CommDestroy(h->comm);
+    delete h->comm;
     cudaFreeHost(h->host_small);
     delete h;
     return s;
@@ -928,12 +921,50 @@ apsp_status apsp_create(apsp_handle** out, apsp_dtype dtype, int directed, int64
   return APSP_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+apsp_status apsp_create(apsp_handle** out, apsp_dtype dtype, int directed, int64_t n, int64_t cap,
+                        const void* W, int64_t ldw, void* D_local, int64_t ld, void* workspace,
+                        size_t workspace_bytes, void* stream, int rank, int world,
+                        const void* nccl_id) {
+  return create_impl(out, dtype, directed, n, cap, W, ldw, D_local, ld, workspace, workspace_bytes,
+                     stream, rank, world, nccl_id, nullptr);
+}
+
+apsp_status apsp_local_group_create(int world, void** group) {
+  if (!group) return APSP_E_INVAL;
+  *group = nullptr;
+  if (world < 1 || world > 16) return APSP_E_INVAL;
+  LocalGroup* g = local_group_create(world);
+  if (!g) return APSP_E_CUDA;
+  *group = g;
+  return APSP_OK;
+}
+
+apsp_status apsp_local_group_destroy(void* group) {
+  if (!group) return APSP_E_INVAL;
+  local_group_destroy(reinterpret_cast<LocalGroup*>(group));
+  return APSP_OK;
+}
+
+apsp_status apsp_create_local(apsp_handle** out, apsp_dtype dtype, int directed, int64_t n,
+                              int64_t cap, const void* W, int64_t ldw, void* D_local, int64_t ld,
+                              void* workspace, size_t workspace_bytes, void* stream, int rank,
+                              void* group) {
+  if (!group) return APSP_E_INVAL;
+  LocalGroup* g = reinterpret_cast<LocalGroup*>(group);
+  return create_impl(out, dtype, directed, n, cap, W, ldw, D_local, ld, workspace, workspace_bytes,
+                     stream, rank, local_group_world(g), nullptr, g);
+}
+
 apsp_status apsp_destroy(apsp_handle* h) {
   if (!h) return APSP_E_INVAL;
   if (h->st) cudaStreamSynchronize(h->st);
   h->prof_resolve();
   for (auto e : h->ev_pool) cudaEventDestroy(e);
-  if (h->comm) g_nccl.CommDestroy(h->comm);
+  delete h->comm;
   if (h->host_small) cudaFreeHost(h->host_small);
   delete h;
   return APSP_OK;
@@ -1033,7 +1064,6 @@ apsp_status sp_pair_query(apsp_handle* h, int64_t s, int64_t t, void* dist, int3
   CHECK_HANDLE(h);
   if (!dist || !path_len || (path_cap > 0 && !path)) return fail(h, APSP_E_INVAL, "sp_pair_query: null output");
   if (s < 0 || s >= h->n || t < 0 || t >= h->n) return fail(h, APSP_E_RANGE, "sp_pair_query: id out of range");
-  if (h->world > 1) return fail(h, APSP_E_UNSUPPORTED, "sp_pair_query: row-sharded queries not built yet");
   return dispatch(h->dt, [&](auto z) {
     return query_one<decltype(z)>(h, s, t, dist, path, path_cap, path_len, n_candidates);
   });
@@ -1045,12 +1075,9 @@ apsp_status sp_pair_query_batch(apsp_handle* h, int32_t q, const int32_t* s, con
   CHECK_HANDLE(h);
   if (q < 0 || (q > 0 && (!s || !t || !dist || !path_lens))) return fail(h, APSP_E_INVAL, "query_batch: null argument");
   if (path_cap > 0 && !paths) return fail(h, APSP_E_INVAL, "query_batch: null paths");
-  if (h->world > 1) return fail(h, APSP_E_UNSUPPORTED, "query_batch: row-sharded queries not built yet");
   return dispatch(h->dt, [&](auto z) -> apsp_status {
     using T = decltype(z);
-    PK(APSP_K_QUERY, 8.0 * (double)h->n * q, query_batch<T>(h->Dl<T>(), h->ld, h->WT<T>(), h->ld, h->n, q, s, t, reinterpret_cast<T*>(dist),
-                      paths, path_cap, path_lens, n_cand, h->tau, h->sr, h->st));
-    return APSP_OK;
+    return query_dispatch<T>(h, q, s, t, reinterpret_cast<T*>(dist), paths, path_cap, path_lens, n_cand);
   });
 }
 

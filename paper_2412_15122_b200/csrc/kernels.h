@@ -142,7 +142,13 @@ constexpr int kQueryCap = 4096;
 template <typename T>
 cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int q,
                         const int* s, const int* t, T* dist, int* paths, int path_cap,
-                        int* path_lens, int* ncand, float tau, int sr, cudaStream_t st);
+                        int* path_lens, int* ncand, float tau, int sr, cudaStream_t st,
+                        const T* colbuf = nullptr, int64_t R = 0, int64_t row0 = 0,
+                        int64_t rows = 0);
+// sharded queries: out[b * R + i] = D[row0 + i][t_b] (INF beyond the local rows)
+template <typename T>
+cudaError_t query_colslice(const T* D, int64_t ld, int64_t rows, int64_t R, int64_t n,
+                           const int* t, int qc, T* out, cudaStream_t st);
 
 int num_sms();
 

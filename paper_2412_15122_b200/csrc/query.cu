@@ -14,6 +14,15 @@
 //      (label, index) keys so ties go to the smaller node id), early
 //      stop when t is finalised; edge weights W[m][c] = WT[c][m];
 //   3. predecessor walk t -> s, written in original ids.
+//
+// Row-sharded mode (world > 1): D is split by rows, so
+// row s lives on one rank and column t is spread over all of them.  The host
+// first gathers, for a chunk of QC queries, every rank's slice of each column
+// t (k_query_colslice + one all-gather of QC x R entries per rank); then the
+// rank owning row s runs the query exactly as above, reading D[k][t] from the
+// gathered slices, while the other ranks write zeros, and one all-reduce(sum)
+// of the outputs leaves every rank with the owner's answer.  WT is replicated,
+// so the Dijkstra step needs no communication.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -21,12 +30,22 @@ namespace apsp {
 
 constexpr int QT = 256;   // threads per query CTA
 
+// Sharded-mode description (sh.colbuf == nullptr: single GPU, D holds every row).
+template <typename T>
+struct QShard {
+  const T* colbuf;   // gathered column slices: colbuf[(r * qc + b) * R + i] = D[r*R + i][t_b]
+  int64_t R;         // rows per rank
+  int64_t row0, rows;   // this rank's rows (D points at global row row0)
+  int qc;            // queries in this chunk
+};
+
 template <typename T, int SR>
 __global__ void __launch_bounds__(QT) k_query(const T* __restrict__ D, int64_t ld,
                                               const T* __restrict__ WT, int64_t ldw, int64_t n,
                                               int q, const int* __restrict__ S,
                                               const int* __restrict__ Tq, T* dist, int* paths,
-                                              int path_cap, int* path_lens, int* ncand, float tau) {
+                                              int path_cap, int* path_lens, int* ncand, float tau,
+                                              QShard<T> sh) {
   __shared__ int cid[kQueryCap];
   __shared__ T lab[kQueryCap];
   __shared__ short pred[kQueryCap];
@@ -38,11 +57,24 @@ __global__ void __launch_bounds__(QT) k_query(const T* __restrict__ D, int64_t l
 
   for (int b = blockIdx.x; b < q; b += gridDim.x) {
     const int s = S[b], t = Tq[b];
-    if (s < 0 || s >= n || t < 0 || t >= n) {
+    const bool bad = s < 0 || s >= n || t < 0 || t >= n;
+    if (sh.colbuf) {
+      // sharded: the owner of row s answers (rank 0 answers invalid pairs);
+      // every other rank contributes zeros to the all-reduce(sum)
+      const bool mine = bad ? sh.row0 == 0 : (s >= sh.row0 && s < sh.row0 + sh.rows);
+      if (!mine) {
+        if (tid == 0) { path_lens[b] = 0; if (ncand) ncand[b] = 0; dist[b] = T(0); }
+        for (int c = tid; c < path_cap; c += QT) paths[(int64_t)b * path_cap + c] = 0;
+        continue;
+      }
+      for (int c = tid; c < path_cap; c += QT) paths[(int64_t)b * path_cap + c] = -1;
+      __syncthreads();
+    }
+    if (bad) {
       if (tid == 0) { path_lens[b] = -3; if (ncand) ncand[b] = 0; dist[b] = I; }
       continue;
     }
-    const T* Ds = D + (int64_t)s * ld;
+    const T* Ds = D + ((int64_t)s - sh.row0) * ld;
     const T st = Ds[t];
     if (s == t || !Tr<T>::fin(st)) {
       if (tid == 0) {
@@ -70,7 +102,12 @@ __global__ void __launch_bounds__(QT) k_query(const T* __restrict__ D, int64_t l
       for (int u = 0; u < U; ++u) {
         int64_t k = base + (int64_t)u * QT + tid;
         dsk[u] = k < n ? Ds[k] : I;
-        dkt[u] = k < n ? D[k * ld + t] : I;
+        if (sh.colbuf) {
+          const int64_t r = k / sh.R;
+          dkt[u] = k < n ? sh.colbuf[(r * sh.qc + b) * sh.R + (k - r * sh.R)] : I;
+        } else {
+          dkt[u] = k < n ? D[k * ld + t] : I;
+        }
       }
       bool f[U];
       bool anyf = false;
@@ -174,26 +211,58 @@ __global__ void __launch_bounds__(QT) k_query(const T* __restrict__ D, int64_t l
   }
 }
 
+// out[b * R + i] = D[row0 + i][t_b] for local rows i < rows, INF for i in [rows, R)
+// (also for an out-of-range t_b).  One warp per (query, 32-row group): the
+// column entries are 4-byte strided reads, so this is sector-bound (32 B per
+// entry) — 2·qc·R sectors, small next to the candidate scan's row stream.
 template <typename T>
-cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int q,
-                        const int* s, const int* t, T* dist, int* paths, int path_cap,
-                        int* path_lens, int* ncand, float tau, int sr, cudaStream_t st) {
-  if (q <= 0) return cudaSuccess;
-  int grid = std::min(q, num_sms() * 4);
-  if (sr)
-    k_query<T, 1><<<grid, QT, 0, st>>>(D, ld, WT, ldw, n, q, s, t, dist, paths, path_cap, path_lens,
-                                       ncand, tau);
-  else
-    k_query<T, 0><<<grid, QT, 0, st>>>(D, ld, WT, ldw, n, q, s, t, dist, paths, path_cap, path_lens,
-                                       ncand, tau);
+__global__ void k_query_colslice(const T* __restrict__ D, int64_t ld, int64_t rows, int64_t R,
+                                 int64_t n, const int* __restrict__ Tq, int qc, T* __restrict__ out) {
+  const int64_t total = (int64_t)qc * R;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(e / R);
+    const int64_t i = e - (int64_t)b * R;
+    const int t = Tq[b];
+    out[e] = (i < rows && t >= 0 && t < n) ? D[i * ld + t] : Tr<T>::inf();
+  }
+}
+
+template <typename T>
+cudaError_t query_colslice(const T* D, int64_t ld, int64_t rows, int64_t R, int64_t n,
+                           const int* t, int qc, T* out, cudaStream_t st) {
+  const int64_t total = (int64_t)qc * R;
+  if (total <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+  k_query_colslice<T><<<blocks, 256, 0, st>>>(D, ld, rows, R, n, t, qc, out);
   return cudaGetLastError();
 }
 
-template cudaError_t query_batch<int32_t>(const int32_t*, int64_t, const int32_t*, int64_t, int64_t,
-                                          int, const int*, const int*, int32_t*, int*, int, int*,
-                                          int*, float, int, cudaStream_t);
-template cudaError_t query_batch<float>(const float*, int64_t, const float*, int64_t, int64_t, int,
-                                        const int*, const int*, float*, int*, int, int*, int*,
-                                        float, int, cudaStream_t);
+template <typename T>
+cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int q,
+                        const int* s, const int* t, T* dist, int* paths, int path_cap,
+                        int* path_lens, int* ncand, float tau, int sr, cudaStream_t st,
+                        const T* colbuf, int64_t R, int64_t row0, int64_t rows) {
+  if (q <= 0) return cudaSuccess;
+  int grid = std::min(q, num_sms() * 4);
+  QShard<T> sh{colbuf, R, colbuf ? row0 : 0, rows, q};
+  if (sr)
+    k_query<T, 1><<<grid, QT, 0, st>>>(D, ld, WT, ldw, n, q, s, t, dist, paths, path_cap, path_lens,
+                                       ncand, tau, sh);
+  else
+    k_query<T, 0><<<grid, QT, 0, st>>>(D, ld, WT, ldw, n, q, s, t, dist, paths, path_cap, path_lens,
+                                       ncand, tau, sh);
+  return cudaGetLastError();
+}
+
+#define INST(T)                                                                                  \
+  template cudaError_t query_batch<T>(const T*, int64_t, const T*, int64_t, int64_t, int,       \
+                                      const int*, const int*, T*, int*, int, int*, int*, float,  \
+                                      int, cudaStream_t, const T*, int64_t, int64_t, int64_t);   \
+  template cudaError_t query_colslice<T>(const T*, int64_t, int64_t, int64_t, int64_t,          \
+                                         const int*, int, T*, cudaStream_t);
+INST(int32_t)
+INST(float)
+#undef INST
 
 }  // namespace apsp

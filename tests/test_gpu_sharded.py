@@ -1,0 +1,268 @@
+"""Row-sharded path of the library on ONE GPU: world 2/3/4.
+
+Every rank is a host thread driving its own handle and stream through the C
+ABI (apsp_create_local): the library's multi-rank code — the capacity row
+partition, owner broadcasts of pivot rows and FW panels, all-reduce(min) of
+the add-node row, counter all-reduces, swap-with-last across ranks, the
+sharded query's column all-gather — runs for real, with the in-process
+transport standing in for NCCL (collectives are event-ordered device copies;
+no kernel waits on another kernel).  Requirements (SURVEY §8(c-2) item 11,
+§8(e) "Test"): the gathered int32 D after every update is bit-identical to
+the oracle's cold APSP of the mutated graph (so also to world 1), the update
+statistics agree across ranks and with world 1, and sharded queries return
+the same answers on every rank.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from conftest import random_graph
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2412_15122_b200 as P
+    return P
+
+
+def run_ranks(world, fn, timeout=300):
+    out, errs = [None] * world, []
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            out[r] = fn(r)
+        except BaseException as e:   # noqa: BLE001 - reported below
+            errs.append((r, e))
+
+    ths = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(world)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout)
+    assert not any(t.is_alive() for t in ths), "a rank hung"
+    if errs:
+        raise errs[0][1]
+    return out
+
+
+def build_script(W, directed, cap, rng, dtype):
+    """Updates (identical on every rank) and the expected D after each one
+    (None for option changes)."""
+    hg = synth.HostGraph(W, directed, cap=cap)
+    ops, expect = [], []
+
+    def rec(op):
+        ops.append(op)
+        expect.append(oracle.fw(hg.W) if op[0] != "force" else None)
+
+    def scaled(w, f):
+        assert w != hg.inf
+        return max(int(int(w) * f), 1) if dtype == np.int32 else np.float32(float(w) * f)
+
+    def present_from(u, v):
+        while hg.weight(u, v) == hg.inf:
+            v -= 1
+        return u, v
+
+    # removal whose swap-with-last crosses ranks (k on rank 0, n-1 on the last active rank)
+    hg.remove_node(5)
+    rec(("remove", 5))
+    # add a node at index n
+    m = hg.n
+    o = rng.integers(1, 60, size=m).astype(dtype)
+    i = o.copy() if not directed else rng.integers(1, 60, size=m).astype(dtype)
+    hg.add_node(o, i)
+    rec(("add", o, i))
+    # decrease (rank-1 through the edge)
+    u, v = present_from(3, hg.n - 2)
+    w = scaled(hg.weight(u, v), 0.25)
+    hg.set_edge(u, v, w)
+    rec(("edge", u, v, float(w)))
+    # increases of tight edges: sparse path, then the forced dense (FW on D0) path
+    for force in (1, 2):
+        D, Wc = expect[-1], hg.W
+        tight = [(a, b) for a in range(3, hg.n) for b in range(hg.n)
+                 if a != b and Wc[a, b] != hg.inf and Wc[a, b] == D[a, b]]
+        a, b = tight[int(rng.integers(len(tight)))]
+        w = scaled(Wc[a, b], 10)
+        rec(("force", force))
+        hg.set_edge(a, b, w)
+        rec(("edge", a, b, float(w)))
+    rec(("force", 0))
+    # remove the last node (no swap), then a node in the middle of the range
+    hg.remove_node(hg.n - 1)
+    rec(("remove", hg.n))
+    k = min(300, hg.n - 3)
+    hg.remove_node(k)
+    rec(("remove", k))
+    # the paper's edge modification (remove the cheaper endpoint, re-add, swap back)
+    u, v = present_from(7, hg.n - 4)
+    w = scaled(hg.weight(u, v), 3)
+    hg.set_edge(u, v, w)
+    rec(("readd", u, v, float(w)))
+    return ops, expect, hg
+
+
+def apply(h, op):
+    kind = op[0]
+    if kind == "remove":
+        return h.remove_node(op[1])[1].as_dict()
+    if kind == "add":
+        return h.add_node(op[1], op[2])[1].as_dict()
+    if kind == "edge":
+        return h.update_edge(op[1], op[2], op[3]).as_dict()
+    if kind == "readd":
+        return h.modify_edge_readd(op[1], op[2], op[3])[1].as_dict()
+    if kind == "force":
+        h.set_option(0, op[1])   # APSP_OPT_FORCE_PATH
+        return None
+    raise ValueError(kind)
+
+
+def gather(parts, n):
+    rows = [p for p in parts if p.shape[0]]
+    return np.concatenate(rows, axis=0)[:n, :n] if rows else np.zeros((0, 0))
+
+
+@pytest.mark.parametrize("world,cap,n,directed,dtype", [
+    (2, 512, 430, True, np.int32),
+    (3, 640, 600, True, np.int32),
+    (4, 1024, 700, True, np.int32),     # rank 3 owns no live row until the graph grows
+    (2, 512, 400, False, np.float32),
+])
+def test_sharded_updates_equal_oracle(P, world, cap, n, directed, dtype):
+    rng = np.random.default_rng(world * 1000 + n)
+    W = random_graph(rng, n, directed, density=0.95, lo=1, hi=40, dtype=dtype, inf_frac=0.0)
+    ops, expect, hg = build_script(W, directed, cap, rng, dtype)
+    qs, qt = synth.query_pairs(7, hg.n, 96)
+    qs[:4] = [0, 1, hg.n - 1, 2]
+    qt[:4] = [0, hg.n - 1, 3, 2]
+    g = P._lib.apsp_local_group_create(world)
+
+    def rank(r):
+        st = torch.cuda.Stream()
+        h = P.WarmAPSP(torch.from_numpy(np.ascontiguousarray(W)), directed=directed, cap=cap,
+                       device="cuda:0", stream=st, rank=r, world=world, local_group=g)
+        snaps, infos = [], []
+        torch.cuda.synchronize()
+        snaps.append(h.D.cpu().numpy().copy())
+        for op in ops:
+            infos.append(apply(h, op))
+            st.synchronize()
+            snaps.append(h.D.cpu().numpy().copy() if op[0] != "force" else None)
+        dist, paths, lens, nc = h.query_batch(qs, qt, path_cap=128)
+        one = h.query(int(qs[5]), int(qt[5]))
+        st.synchronize()
+        res = (snaps, infos, dist.cpu().numpy(), paths.cpu().numpy(), lens.cpu().numpy(),
+               nc.cpu().numpy(), one, (h.row0, h.rows))
+        h.close()
+        return res
+
+    try:
+        res = run_ranks(world, rank)
+    finally:
+        torch.cuda.synchronize()
+        P._lib.apsp_local_group_destroy(g)
+    # the same script on one GPU without sharding: identical statistics
+    h1 = P.WarmAPSP(torch.from_numpy(np.ascontiguousarray(W)), directed=directed, cap=cap)
+    infos1 = [apply(h1, op) for op in ops]
+    d1b, _, l1b, _ = h1.query_batch(qs, qt, path_cap=128)
+    torch.cuda.synchronize()
+    assert infos1 == res[0][1], "sharded update statistics differ from world 1"
+    assert np.array_equal(d1b.cpu().numpy(), res[0][2])
+    assert np.array_equal(l1b.cpu().numpy(), res[0][4])
+    h1.close()
+
+    # D after cold FW, then after every update
+    D0 = gather([res[r][0][0] for r in range(world)], n)
+    assert_eq(D0, oracle.fw(W), dtype)
+    for j, (op, exp) in enumerate(zip(ops, expect)):
+        if exp is None:
+            continue
+        Dj = gather([res[r][0][j + 1] for r in range(world)], exp.shape[0])
+        assert_eq(Dj, exp, dtype, f"after op {j} {op[0]}")
+        infos = [res[r][1][j] for r in range(world)]
+        assert all(i == infos[0] for i in infos), f"ranks disagree on update info after {op[0]}"
+
+    # sharded queries: identical on every rank, and correct
+    Df = expect[-1]
+    Wf = hg.W
+    for r in range(1, world):
+        for a, b in zip(res[0][2:6], res[r][2:6]):
+            assert np.array_equal(a, b), f"rank {r} query outputs differ from rank 0"
+        assert res[r][6] == res[0][6]
+    dist, paths, lens = res[0][2], res[0][3], res[0][4]
+    for q, (s, t) in enumerate(zip(qs, qt)):
+        if dtype == np.int32:
+            assert dist[q] == Df[s, t]
+        else:
+            assert abs(float(dist[q]) - Df[s, t]) <= 1e-5 * Df[s, t]
+        L = int(lens[q])
+        assert L >= 1, f"query {q} ({s},{t}) path_len {L}"
+        path = [int(x) for x in paths[q, :L]]
+        assert oracle.path_is_valid(Wf, path, s, t)
+        pw = oracle.path_weight(Wf, path)
+        assert (pw == Df[s, t]) if dtype == np.int32 else abs(pw - Df[s, t]) <= 1e-5 * Df[s, t]
+        assert all(x == -1 for x in paths[q, L:]), "sharded paths are -1 padded"
+    d1, p1, _ = res[0][6]
+    assert p1 == [int(x) for x in paths[5, :lens[5]]] and d1 == dist[5]
+
+
+def test_sharded_world1_equivalence_and_ranks_zero_rows(P):
+    """world 4 with cap 1024 and n 300: ranks 2 and 3 own no live row; cold FW
+    and a growth sequence of adds that reaches rank 2's rows stay bit-exact."""
+    rng = np.random.default_rng(4)
+    n, cap, world = 300, 1024, 4
+    W = random_graph(rng, n, True, density=1.0, lo=1, hi=30)
+    hg = synth.HostGraph(W, True, cap=cap)
+    adds = []
+    for _ in range(220):   # 300 -> 520: crosses into rank 2's block [512, 768)
+        m = hg.n
+        o = rng.integers(1, 40, size=m).astype(np.int32)
+        i = rng.integers(1, 40, size=m).astype(np.int32)
+        hg.add_node(o, i)
+        adds.append((o, i))
+    g = P._lib.apsp_local_group_create(world)
+
+    def rank(r):
+        st = torch.cuda.Stream()
+        h = P.WarmAPSP(torch.from_numpy(W), directed=True, cap=cap, device="cuda:0", stream=st,
+                       rank=r, world=world, local_group=g)
+        for o, i in adds:
+            h.add_node(o, i)
+        h.remove_node(513)       # k and n-1 both on rank 2
+        h.remove_node(2)         # k on rank 0, n-1 on rank 2
+        st.synchronize()
+        D = h.D.cpu().numpy().copy()
+        h.close()
+        return D
+
+    try:
+        parts = run_ranks(world, rank)
+    finally:
+        torch.cuda.synchronize()
+        P._lib.apsp_local_group_destroy(g)
+    hg.remove_node(513)
+    hg.remove_node(2)
+    assert_eq(gather(parts, hg.n), oracle.fw(hg.W), np.int32)
+
+
+def assert_eq(G, O, dtype, what=""):
+    assert G.shape == O.shape, what
+    if dtype == np.int32:
+        bad = np.argwhere(G != O)
+        assert bad.size == 0, f"{what}: {len(bad)} mismatches, first {bad[:4].tolist()}"
+    else:
+        fin = np.isfinite(O)
+        assert np.array_equal(np.isfinite(G), fin), what
+        rel = np.abs(G[fin].astype(np.float64) - O[fin]) / np.maximum(np.abs(O[fin]), 1e-300)
+        assert rel.max(initial=0) <= 1e-5, f"{what}: max rel err {rel.max()}"

@@ -40,7 +40,8 @@ struct Plan {
   size_t off_wt, off_vec, off_rowpart, off_colpart, off_rowoff, off_rowcnt, off_chg, off_prow,
       off_pcol, off_plb, off_popen, off_ocol, off_ocnt, off_gprow, off_gpcol, off_glb, off_gfull,
       off_slid, off_slw, off_wnext, off_panel, off_pt, off_bm, off_anyrow, off_qsend, off_qcol,
-      off_small, total;
+      off_qids, off_qdsv, off_qlab, off_qpred, off_qpath, off_qdone, off_qcnt, off_small, total;
+  int qcap, qbatch;
   int64_t ldpt;
 };
 
@@ -89,6 +90,17 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   // sharded queries: this rank's slices of kQueryChunk columns, and all ranks' (all-gathered)
   p.off_qsend = take(world > 1 ? sizeof(int32_t) * (size_t)kQueryChunk * rows_max : 256);
   p.off_qcol = take(world > 1 ? sizeof(int32_t) * (size_t)kQueryChunk * rows_max * world : 256);
+  // query scratch: qbatch slots of qcap candidates (|C| <= n <= cap)
+  p.qcap = (int)std::min<int64_t>(kQueryCap, cap);
+  p.qbatch = world > 1 ? kQueryChunk : kQueryBatch;
+  const size_t qe = (size_t)p.qcap * p.qbatch;
+  p.off_qids = take(4 * qe);
+  p.off_qdsv = take(4 * qe);
+  p.off_qlab = take(4 * qe);
+  p.off_qpred = take(4 * qe);
+  p.off_qpath = take(4 * qe);
+  p.off_qdone = take(qe);
+  p.off_qcnt = take(sizeof(int32_t) * (size_t)p.qbatch);
   p.off_small = take(64 * 1024);
   p.total = o;
   return p;
@@ -194,6 +206,19 @@ struct apsp_handle {
   uint32_t* bm() { return reinterpret_cast<uint32_t*>(ws + plan.off_bm); }
   template <typename T> T* qsend() { return reinterpret_cast<T*>(ws + plan.off_qsend); }
   template <typename T> T* qcol() { return reinterpret_cast<T*>(ws + plan.off_qcol); }
+  QueryScratch qscratch() {
+    QueryScratch q;
+    q.ids = reinterpret_cast<int*>(ws + plan.off_qids);
+    q.dsv = ws + plan.off_qdsv;
+    q.lab = ws + plan.off_qlab;
+    q.pred = reinterpret_cast<int*>(ws + plan.off_qpred);
+    q.path = reinterpret_cast<int*>(ws + plan.off_qpath);
+    q.done = ws + plan.off_qdone;
+    q.cnt = reinterpret_cast<int*>(ws + plan.off_qcnt);
+    q.qcap = plan.qcap;
+    q.batch = plan.qbatch;
+    return q;
+  }
   int* anyrow() { return reinterpret_cast<int*>(ws + plan.off_anyrow); }
   DetectCounters* ctr() { return reinterpret_cast<DetectCounters*>(ws + plan.off_small); }
   int* anyflag() { return reinterpret_cast<int*>(ws + plan.off_small + 256); }
@@ -745,7 +770,7 @@ apsp_status query_dispatch(apsp_handle* h, int q, const int* s, const int* t, T*
   if (h->world <= 1) {
     PK(APSP_K_QUERY, 8.0 * (double)n * q,
        query_batch<T>(h->Dl<T>(), ld, h->WT<T>(), ld, n, q, s, t, dist, paths, path_cap, lens, ncand,
-                      h->tau, h->sr, h->st));
+                      h->tau, h->sr, h->st, h->qscratch()));
     return APSP_OK;
   }
   Rows r = h->active();
@@ -757,8 +782,8 @@ apsp_status query_dispatch(apsp_handle* h, int q, const int* s, const int* t, T*
     int* pb = path_cap > 0 ? paths + (int64_t)b0 * path_cap : paths;
     PK(APSP_K_QUERY, 8.0 * (double)n * c,
        query_batch<T>(h->Dl<T>(), ld, h->WT<T>(), ld, n, c, s + b0, t + b0, dist + b0, pb, path_cap,
-                      lens + b0, ncand ? ncand + b0 : nullptr, h->tau, h->sr, h->st, h->qcol<T>(), R,
-                      h->row0, r.hi - r.lo));
+                      lens + b0, ncand ? ncand + b0 : nullptr, h->tau, h->sr, h->st, h->qscratch(),
+                      h->qcol<T>(), R, h->row0, r.hi - r.lo));
     NK(h->comm->allreduce(dist + b0, (size_t)c, nccl_type<T>(), ncclSum, h->st));
     NK(h->comm->allreduce(lens + b0, (size_t)c, ncclInt32, ncclSum, h->st));
     if (ncand) NK(h->comm->allreduce(ncand + b0, (size_t)c, ncclInt32, ncclSum, h->st));
@@ -789,7 +814,7 @@ apsp_status query_one(apsp_handle* h, int64_t s, int64_t t, void* dist, int32_t*
   if (len < 0) {
     if (path_len) *path_len = 0;
     return fail(h, APSP_E_RANGE, "sp_pair_query: %d candidates exceed the kernel capacity %d", nc,
-                std::min(kQueryCap, cap_dev));
+                std::min(h->plan.qcap, cap_dev));
   }
   if (path_len) *path_len = len;
   if (len > path_cap) return fail(h, APSP_E_RANGE, "sp_pair_query: path_cap %d < path length %d", path_cap, len);

@@ -138,13 +138,25 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
                          int* chg_out, int* any, int sr, cudaStream_t st);
 
 // ---------------- query.cu ----------------
-constexpr int kQueryCap = 4096;
+constexpr int kQueryCap = 4096;    // max |C| per query (min(kQueryCap, cap) per handle)
+constexpr int kQueryBatch = 1024;  // queries per scan/solve launch pair
+// per-query device scratch, `batch` slots of `qcap` entries each (workspace)
+struct QueryScratch {
+  int* ids;             // candidate ids
+  void* dsv;            // D[s][id], the handle's element type
+  void* lab;            // Dijkstra labels (element type)
+  int* pred;
+  int* path;
+  unsigned char* done;
+  int* cnt;             // |C| per slot
+  int qcap, batch;
+};
 template <typename T>
 cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int q,
                         const int* s, const int* t, T* dist, int* paths, int path_cap,
                         int* path_lens, int* ncand, float tau, int sr, cudaStream_t st,
-                        const T* colbuf = nullptr, int64_t R = 0, int64_t row0 = 0,
-                        int64_t rows = 0);
+                        const QueryScratch& qs, const T* colbuf = nullptr, int64_t R = 0,
+                        int64_t row0 = 0, int64_t rows = 0);
 // sharded queries: out[b * R + i] = D[row0 + i][t_b] (INF beyond the local rows)
 template <typename T>
 cudaError_t query_colslice(const T* D, int64_t ld, int64_t rows, int64_t R, int64_t n,

@@ -6,31 +6,52 @@
 // algorithm to calculate the shortest path from node i to node j, on the
 // small graph; then translate the path into original node index."
 //
-// One CTA per query:
-//   1. candidate scan: C = {k : D[s][k] + D[k][t] == D[s][t]} over row s
-//      (contiguous) and column t (stride ld), compacted in node order with
-//      warp ballots + popc into shared memory;
-//   2. Dijkstra on the induced subgraph of C (warp 0; argmin by 64-bit
-//      (label, index) keys so ties go to the smaller node id), early
-//      stop when t is finalised; edge weights W[m][c] = WT[c][m];
-//   3. predecessor walk t -> s, written in original ids.
+// Two kernels per chunk of queries:
+//   k_query_scan  — the candidate_node_list C = {k : D[s][k] + D[k][t] ==
+//                   D[s][t]}.  Grid (node chunks x queries), so even ONE query
+//                   spreads its scan of row s (contiguous) and column t
+//                   (stride ld: one 32-byte sector per entry, ~128 B of DRAM
+//                   traffic measured — this column is what bounds the query)
+//                   over every SM.  Candidates are rare (|C| ~ tens of n),
+//                   appended with one warp-aggregated atomic per warp that
+//                   found any, together with D[s][k].
+//   k_query_solve — one warp per query: Dijkstra on the small graph induced by
+//                   C, ties to the smaller node id, early stop at t,
+//                   path in original ids.  The append order of C is arbitrary,
+//                   so every tie-break compares node ids, never positions.
 //
-// Row-sharded mode (world > 1): D is split by rows, so
-// row s lives on one rank and column t is spread over all of them.  The host
-// first gathers, for a chunk of QC queries, every rank's slice of each column
-// t (k_query_colslice + one all-gather of QC x R entries per rank); then the
-// rank owning row s runs the query exactly as above, reading D[k][t] from the
-// gathered slices, while the other ranks write zeros, and one all-reduce(sum)
-// of the outputs leaves every rank with the owner's answer.  WT is replicated,
-// so the Dijkstra step needs no communication.
+// Dijkstra's labels on the small graph are known in advance: for k in C a
+// whole shortest s->k path lies in C (each node y on it has D[s][y] + D[y][t]
+// <= D[s][k] + D[k][t] = D[s][t]), so the label Dijkstra settles k with is
+// D[s][k], which the scan read.  With positive weights Dijkstra therefore
+// settles C in (D[s][k], id) order, and the predecessor it records for k is the
+// first m in that order with D[s][m] + W[m][k] == D[s][k].  For int32 shortest
+// paths the kernel computes exactly that tree, hop by hop backwards from t
+// (one parallel pass over C per hop instead of one sequential Dijkstra
+// iteration per candidate), identical to Dijkstra's output.  With zero-weight
+// edges (Q2) every hop still satisfies the equality, so a walk that reaches s
+// is a shortest path (though possibly another tie than Dijkstra's); a walk that
+// finds no predecessor ordered before the current node falls back to the
+// sequential Dijkstra.  fp32 (tolerant equality, Q4) and minimax always run
+// the sequential Dijkstra.
+//
+// Row-sharded mode (world > 1): D is split by rows,
+// so row s lives on one rank and column t is spread over all of them.  The
+// host first gathers, for a chunk of queries, every rank's slice of each
+// column t (k_query_colslice + one all-gather); then the rank owning row s
+// answers exactly as above, reading D[k][t] from the gathered slices, while
+// the other ranks write zeros, and one all-reduce(sum) of the outputs leaves
+// every rank with the owner's answer.  WT is replicated, so the small-graph
+// Dijkstra needs no communication.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace apsp {
 
-constexpr int QT = 256;   // threads per query CTA
+constexpr int QS_T = 256;   // scan threads
+constexpr int QS_U = 4;     // nodes per thread per step (loads in flight)
 
-// Sharded-mode description (sh.colbuf == nullptr: single GPU, D holds every row).
+// Sharded-mode description (colbuf == nullptr: single GPU, D holds every row).
 template <typename T>
 struct QShard {
   const T* colbuf;   // gathered column slices: colbuf[(r * qc + b) * R + i] = D[r*R + i][t_b]
@@ -39,20 +60,106 @@ struct QShard {
   int qc;            // queries in this chunk
 };
 
+template <typename T>
+__device__ __forceinline__ T ld_col(const T* D, int64_t ld, int64_t k, int t, int b,
+                                    const QShard<T>& sh) {
+  if (sh.colbuf) {
+    const int64_t r = k / sh.R;
+    return sh.colbuf[(r * sh.qc + b) * sh.R + (k - r * sh.R)];
+  }
+  return __ldg(D + k * ld + t);
+}
+
 template <typename T, int SR>
-__global__ void __launch_bounds__(QT) k_query(const T* __restrict__ D, int64_t ld,
-                                              const T* __restrict__ WT, int64_t ldw, int64_t n,
-                                              int q, const int* __restrict__ S,
-                                              const int* __restrict__ Tq, T* dist, int* paths,
-                                              int path_cap, int* path_lens, int* ncand, float tau,
-                                              QShard<T> sh) {
-  __shared__ int cid[kQueryCap];
-  __shared__ T lab[kQueryCap];
-  __shared__ short pred[kQueryCap];
-  __shared__ unsigned char done[kQueryCap];
-  __shared__ int s_cnt, s_is, s_it;
-  __shared__ int s_wcnt[4 * (QT / 32)];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+__global__ void __launch_bounds__(QS_T) k_query_scan(const T* __restrict__ D, int64_t ld, int64_t n,
+                                                     const int* __restrict__ S,
+                                                     const int* __restrict__ Tq, int64_t chunk,
+                                                     int* __restrict__ cand, T* __restrict__ cand_d,
+                                                     int qcap, int* __restrict__ cnt, float tau,
+                                                     QShard<T> sh) {
+  const int b = blockIdx.y;
+  const int s = S[b], t = Tq[b];
+  if (s < 0 || s >= n || t < 0 || t >= n || s == t) return;
+  if (sh.colbuf && !(s >= sh.row0 && s < sh.row0 + sh.rows)) return;
+  const T* Ds = D + ((int64_t)s - sh.row0) * ld;
+  const T st = Ds[t];
+  if (!Tr<T>::fin(st)) return;
+  const int lane = threadIdx.x & 31;
+  const T I = Tr<T>::inf();
+  const int64_t k0 = (int64_t)blockIdx.x * chunk, k1 = min(n, k0 + chunk);
+  int* out = cand + (int64_t)b * qcap;
+  T* outd = cand_d + (int64_t)b * qcap;
+  for (int64_t base = k0; base < k1; base += (int64_t)QS_T * QS_U) {
+    T dsk[QS_U], dkt[QS_U];
+#pragma unroll
+    for (int u = 0; u < QS_U; ++u) {
+      const int64_t k = base + (int64_t)u * QS_T + threadIdx.x;
+      dsk[u] = k < k1 ? Ds[k] : I;
+      dkt[u] = k < k1 ? ld_col<T>(D, ld, k, t, b, sh) : I;
+    }
+#pragma unroll
+    for (int u = 0; u < QS_U; ++u) {
+      const int64_t k = base + (int64_t)u * QS_T + threadIdx.x;
+      const bool f = k < k1 && Tr<T>::fin(dsk[u]) && Tr<T>::fin(dkt[u]) &&
+                     Tr<T, SR>::tight(Tr<T, SR>::add(dsk[u], dkt[u]), st, tau);
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (bal) {
+        int pos0 = 0;
+        if (lane == 0) pos0 = atomicAdd(cnt + b, __popc(bal));
+        pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+        const int pos = pos0 + __popc(bal & ((1u << lane) - 1));
+        if (f && pos < qcap) { out[pos] = (int)k; outd[pos] = dsk[u]; }
+      }
+    }
+  }
+}
+
+// shared memory of k_query_solve (one warp per CTA); candidate sets larger
+// than kSmall use the per-query global scratch instead
+constexpr int kSmall = 512;
+template <typename T>
+struct QSolveSmem {
+  int ids[kSmall];
+  T dsv[kSmall];   // D[s][ids[x]]
+  T lab[kSmall];
+  int pred[kSmall];
+  int path[kSmall];
+  unsigned char done[kSmall];
+};
+
+// per-query global scratch (slot b of the chunk, qcap entries each)
+template <typename T>
+struct QScratch {
+  int* ids;            // candidate ids (written by the scan)
+  T* dsv;              // D[s][id] (written by the scan)
+  T* lab;
+  int* pred;
+  int* path;
+  unsigned char* done;
+  int qcap;
+};
+
+__device__ __forceinline__ void warp_argmin(unsigned long long& key, int& pos) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long k2 = __shfl_xor_sync(0xffffffffu, key, o);
+    const int p2 = __shfl_xor_sync(0xffffffffu, pos, o);
+    if (k2 < key) { key = k2; pos = p2; }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ unsigned long long qkey(T v, int id) {
+  return ((unsigned long long)Tr<T>::key(v) << 32) | (unsigned)id;
+}
+
+template <typename T, int SR>
+__global__ void __launch_bounds__(32) k_query_solve(
+    const T* __restrict__ D, int64_t ld, const T* __restrict__ WT, int64_t ldw, int64_t n, int q,
+    const int* __restrict__ S, const int* __restrict__ Tq, const int* __restrict__ cnt,
+    QScratch<T> gs, T* dist, int* paths, int path_cap, int* path_lens, int* ncand, QShard<T> sh) {
+  __shared__ QSolveSmem<T> sm;
+  const int lane = threadIdx.x;
   const T I = Tr<T>::inf();
 
   for (int b = blockIdx.x; b < q; b += gridDim.x) {
@@ -63,21 +170,20 @@ __global__ void __launch_bounds__(QT) k_query(const T* __restrict__ D, int64_t l
       // every other rank contributes zeros to the all-reduce(sum)
       const bool mine = bad ? sh.row0 == 0 : (s >= sh.row0 && s < sh.row0 + sh.rows);
       if (!mine) {
-        if (tid == 0) { path_lens[b] = 0; if (ncand) ncand[b] = 0; dist[b] = T(0); }
-        for (int c = tid; c < path_cap; c += QT) paths[(int64_t)b * path_cap + c] = 0;
+        if (lane == 0) { path_lens[b] = 0; if (ncand) ncand[b] = 0; dist[b] = T(0); }
+        for (int c = lane; c < path_cap; c += 32) paths[(int64_t)b * path_cap + c] = 0;
         continue;
       }
-      for (int c = tid; c < path_cap; c += QT) paths[(int64_t)b * path_cap + c] = -1;
-      __syncthreads();
+      for (int c = lane; c < path_cap; c += 32) paths[(int64_t)b * path_cap + c] = -1;
+      __syncwarp();
     }
     if (bad) {
-      if (tid == 0) { path_lens[b] = -3; if (ncand) ncand[b] = 0; dist[b] = I; }
+      if (lane == 0) { path_lens[b] = -3; if (ncand) ncand[b] = 0; dist[b] = I; }
       continue;
     }
-    const T* Ds = D + ((int64_t)s - sh.row0) * ld;
-    const T st = Ds[t];
+    const T st = D[((int64_t)s - sh.row0) * ld + t];
     if (s == t || !Tr<T>::fin(st)) {
-      if (tid == 0) {
+      if (lane == 0) {
         dist[b] = s == t ? T(0) : I;
         if (s == t) {
           if (path_cap >= 1) { paths[(int64_t)b * path_cap] = s; path_lens[b] = 1; }
@@ -89,132 +195,122 @@ __global__ void __launch_bounds__(QT) k_query(const T* __restrict__ D, int64_t l
       }
       continue;
     }
-    if (tid == 0) { s_cnt = 0; s_is = -1; s_it = -1; }
-    __syncthreads();
-
-    // ---- 1. candidate scan (Theorem 4 equality), ordered compaction ----
-    // Candidates are rare (|C| ~ tens out of n), so a block-wide OR skips the
-    // compaction for almost every group of QT*U nodes.
-    constexpr int U = 4;   // nodes per thread per step (loads in flight)
-    for (int64_t base = 0; base < n; base += (int64_t)QT * U) {
-      T dsk[U], dkt[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        int64_t k = base + (int64_t)u * QT + tid;
-        dsk[u] = k < n ? Ds[k] : I;
-        if (sh.colbuf) {
-          const int64_t r = k / sh.R;
-          dkt[u] = k < n ? sh.colbuf[(r * sh.qc + b) * sh.R + (k - r * sh.R)] : I;
-        } else {
-          dkt[u] = k < n ? D[k * ld + t] : I;
-        }
-      }
-      bool f[U];
-      bool anyf = false;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        int64_t k = base + (int64_t)u * QT + tid;
-        f[u] = k < n && Tr<T>::fin(dsk[u]) && Tr<T>::fin(dkt[u]) &&
-               Tr<T, SR>::tight(Tr<T, SR>::add(dsk[u], dkt[u]), st, tau);
-        anyf |= f[u];
-      }
-      if (!__syncthreads_or(anyf)) continue;
-      unsigned bal[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        bal[u] = __ballot_sync(0xffffffffu, f[u]);
-        if (lane == 0) s_wcnt[u * (QT / 32) + warp] = __popc(bal[u]);
-      }
-      __syncthreads();
-      int tot = 0;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        int off = s_cnt + tot;
-        for (int w = 0; w < warp; ++w) off += s_wcnt[u * (QT / 32) + w];
-        for (int w = 0; w < QT / 32; ++w) tot += s_wcnt[u * (QT / 32) + w];
-        if (f[u]) {
-          const int64_t k = base + (int64_t)u * QT + tid;
-          const int pos = off + __popc(bal[u] & ((1u << lane) - 1));
-          if (pos < kQueryCap) {
-            cid[pos] = (int)k;
-            if (k == s) s_is = pos;
-            if (k == t) s_it = pos;
-          }
-        }
-      }
-      __syncthreads();
-      if (tid == 0) s_cnt += tot;
-      __syncthreads();
+    const int c = cnt[b];
+    if (c > gs.qcap) {
+      if (lane == 0) { path_lens[b] = -2; if (ncand) ncand[b] = c; dist[b] = st; }
+      continue;
     }
-    const int cnt = s_cnt;
-    if (cnt > kQueryCap || s_is < 0 || s_it < 0) {
-      if (tid == 0) { path_lens[b] = -2; if (ncand) ncand[b] = cnt; dist[b] = st; }
-      __syncthreads();
+    const int64_t slot = (int64_t)b * gs.qcap;
+    const bool small = c <= kSmall;
+    int* ids = small ? sm.ids : gs.ids + slot;
+    T* dsv = small ? sm.dsv : gs.dsv + slot;
+    T* lab = small ? sm.lab : gs.lab + slot;
+    int* pred = small ? sm.pred : gs.pred + slot;
+    int* path = small ? sm.path : gs.path + slot;
+    unsigned char* done = small ? sm.done : gs.done + slot;
+    int is = -1, it = -1;
+    for (int x = lane; x < c; x += 32) {
+      const int id = gs.ids[slot + x];
+      const T d = gs.dsv[slot + x];
+      if (small) { ids[x] = id; dsv[x] = d; }
+      if (id == s) is = x;
+      if (id == t) it = x;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      is = max(is, __shfl_xor_sync(0xffffffffu, is, o));
+      it = max(it, __shfl_xor_sync(0xffffffffu, it, o));
+    }
+    __syncwarp();
+    if (is < 0 || it < 0) {   // cannot happen: s and t satisfy the equality
+      if (lane == 0) { path_lens[b] = -2; if (ncand) ncand[b] = c; dist[b] = st; }
       continue;
     }
 
-    // ---- 2. Dijkstra on the candidate subgraph (warp 0) ----
-    if (warp == 0) {
-      for (int c = lane; c < cnt; c += 32) { lab[c] = I; pred[c] = -1; done[c] = 0; }
-      __syncwarp();
-      if (lane == 0) lab[s_is] = T(0);
-      __syncwarp();
-      for (int it = 0; it < cnt; ++it) {
+    int len = -1;   // path length found (path[] holds it backwards, t first)
+    if (SR == 0 && !Tr<T>::kFloat) {
+      // ---- predecessor walk with the known labels (int32 shortest path) ----
+      int cur = it, hops = 0;
+      if (lane == 0) path[0] = it;
+      while (cur != is && hops < c) {
+        const T dc = dsv[cur];
+        const unsigned long long kc = qkey<T>(dc, ids[cur]);
+        const T* wrow = WT + (int64_t)ids[cur] * ldw;   // W[m][cur] = WT[cur][m]
         unsigned long long best = ~0ull;
-        for (int c = lane; c < cnt; c += 32)
-          if (!done[c]) {
-            unsigned long long key = ((unsigned long long)Tr<T>::key(lab[c]) << 32) | (unsigned)c;
-            best = key < best ? key : best;
+        int bpos = -1;
+        for (int x = lane; x < c; x += 32) {
+          const unsigned long long kx = qkey<T>(dsv[x], ids[x]);
+          if (kx < kc) {
+            const T w = wrow[ids[x]];
+            if (Tr<T>::fin(w) && Tr<T>::add(dsv[x], w) == dc && kx < best) { best = kx; bpos = x; }
           }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
-          best = y < best ? y : best;
         }
-        if (best == ~0ull) break;
-        const int m = (int)(best & 0xffffffffu);
+        warp_argmin(best, bpos);
+        if (bpos < 0) break;   // no settled predecessor: a zero-weight hop (see above)
+        cur = bpos;
+        ++hops;
+        if (lane == 0) path[hops] = cur;
+      }
+      if (cur == is) len = hops + 1;
+      __syncwarp();
+    }
+    if (len < 0) {
+      // ---- Dijkstra on the candidate subgraph ----
+      for (int x = lane; x < c; x += 32) { lab[x] = I; pred[x] = -1; done[x] = 0; }
+      __syncwarp();
+      if (lane == 0) lab[is] = T(0);
+      __syncwarp();
+      for (int iter = 0; iter < c; ++iter) {
+        unsigned long long best = ~0ull;
+        int m = -1;
+        for (int x = lane; x < c; x += 32)
+          if (!done[x]) {
+            const unsigned long long key = qkey<T>(lab[x], ids[x]);
+            if (key < best) { best = key; m = x; }
+          }
+        warp_argmin(best, m);
+        if (m < 0) break;
         const T lm = lab[m];
         if (!Tr<T>::fin(lm)) break;
         __syncwarp();
         if (lane == 0) done[m] = 1;
         __syncwarp();
-        if (m == s_it) break;
-        const int64_t gm = cid[m];
-        for (int c = lane; c < cnt; c += 32) {
-          if (done[c]) continue;
-          const T w = WT[(int64_t)cid[c] * ldw + gm];   // W[m][c]
+        if (m == it) break;
+        const int64_t gm = ids[m];
+        for (int x = lane; x < c; x += 32) {
+          if (done[x]) continue;
+          const T w = WT[(int64_t)ids[x] * ldw + gm];   // W[m][x]
           if (!Tr<T>::fin(w)) continue;
-          const T cand = Tr<T, SR>::add(lm, w);
-          if (cand < lab[c]) { lab[c] = cand; pred[c] = (short)m; }
+          const T cd = Tr<T, SR>::add(lm, w);
+          if (cd < lab[x]) { lab[x] = cd; pred[x] = m; }
         }
         __syncwarp();
       }
-      // ---- 3. path t -> s ----
       if (lane == 0) {
-        int len = 0, last = -1;
-        for (int c = s_it; c >= 0 && len <= cnt; c = (c == s_is) ? -1 : pred[c]) { ++len; last = c; }
-        dist[b] = st;
-        if (ncand) ncand[b] = cnt;
-        if (len > cnt || last != s_is) {
-          path_lens[b] = -2;       // no path through the candidates (cannot happen)
-        } else if (len > path_cap) {
-          path_lens[b] = -1;
-        } else {
-          int* out = paths + (int64_t)b * path_cap;
-          int pos = len - 1;
-          for (int c = s_it; c >= 0; c = (c == s_is) ? -1 : pred[c]) out[pos--] = cid[c];
-          path_lens[b] = len;
-        }
+        int l = 0, last = -1;
+        for (int x = it; x >= 0 && l < c; x = (x == is) ? -1 : pred[x]) { path[l++] = x; last = x; }
+        len = last == is ? l : -1;
       }
+      len = __shfl_sync(0xffffffffu, len, 0);
     }
-    __syncthreads();
+    // ---- output: the path s -> t in original ids ----
+    __syncwarp();
+    if (lane == 0) {
+      dist[b] = st;
+      if (ncand) ncand[b] = c;
+      path_lens[b] = len < 0 ? -2 : (len > path_cap ? -1 : len);
+    }
+    if (len > 0 && len <= path_cap) {
+      int* o = paths + (int64_t)b * path_cap;
+      for (int x = lane; x < len; x += 32) o[x] = ids[path[len - 1 - x]];
+    }
+    __syncwarp();
   }
 }
 
 // out[b * R + i] = D[row0 + i][t_b] for local rows i < rows, INF for i in [rows, R)
-// (also for an out-of-range t_b).  One warp per (query, 32-row group): the
-// column entries are 4-byte strided reads, so this is sector-bound (32 B per
-// entry) — 2·qc·R sectors, small next to the candidate scan's row stream.
+// (also for an out-of-range t_b).  4-byte strided reads: sector-bound (32 B per
+// entry), the sharded counterpart of the scan's column reads.
 template <typename T>
 __global__ void k_query_colslice(const T* __restrict__ D, int64_t ld, int64_t rows, int64_t R,
                                  int64_t n, const int* __restrict__ Tq, int qc, T* __restrict__ out) {
@@ -238,27 +334,59 @@ cudaError_t query_colslice(const T* D, int64_t ld, int64_t rows, int64_t R, int6
   return cudaGetLastError();
 }
 
+template <typename T, int SR>
+cudaError_t query_launch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int q,
+                         const int* s, const int* t, T* dist, int* paths, int path_cap,
+                         int* path_lens, int* ncand, float tau, cudaStream_t st, QShard<T> sh,
+                         const QueryScratch& qs) {
+  cudaError_t e = cudaMemsetAsync(qs.cnt, 0, sizeof(int) * q, st);
+  if (e != cudaSuccess) return e;
+  // node chunks: >= 4 CTAs per SM over the whole grid, >= 1 step per CTA
+  const int64_t step = (int64_t)QS_T * QS_U;
+  const int64_t steps = (n + step - 1) / step;
+  int64_t nch = std::max<int64_t>(1, ((int64_t)num_sms() * 4 + q - 1) / q);
+  nch = std::min(nch, steps);
+  const int64_t chunk = (steps + nch - 1) / nch * step;
+  nch = (n + chunk - 1) / chunk;
+  T* cand_d = reinterpret_cast<T*>(qs.dsv);
+  k_query_scan<T, SR><<<dim3((unsigned)nch, (unsigned)q), QS_T, 0, st>>>(
+      D, ld, n, s, t, chunk, qs.ids, cand_d, qs.qcap, qs.cnt, tau, sh);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  QScratch<T> gs{qs.ids, cand_d, reinterpret_cast<T*>(qs.lab), qs.pred, qs.path, qs.done, qs.qcap};
+  const int grid = std::min(q, num_sms() * 16);
+  k_query_solve<T, SR><<<grid, 32, 0, st>>>(D, ld, WT, ldw, n, q, s, t, qs.cnt, gs, dist, paths,
+                                            path_cap, path_lens, ncand, sh);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int q,
                         const int* s, const int* t, T* dist, int* paths, int path_cap,
                         int* path_lens, int* ncand, float tau, int sr, cudaStream_t st,
-                        const T* colbuf, int64_t R, int64_t row0, int64_t rows) {
+                        const QueryScratch& qs, const T* colbuf, int64_t R, int64_t row0,
+                        int64_t rows) {
   if (q <= 0) return cudaSuccess;
-  int grid = std::min(q, num_sms() * 4);
-  QShard<T> sh{colbuf, R, colbuf ? row0 : 0, rows, q};
-  if (sr)
-    k_query<T, 1><<<grid, QT, 0, st>>>(D, ld, WT, ldw, n, q, s, t, dist, paths, path_cap, path_lens,
-                                       ncand, tau, sh);
-  else
-    k_query<T, 0><<<grid, QT, 0, st>>>(D, ld, WT, ldw, n, q, s, t, dist, paths, path_cap, path_lens,
-                                       ncand, tau, sh);
-  return cudaGetLastError();
+  if (colbuf && q > qs.batch) return cudaErrorInvalidValue;   // the host chunks sharded batches
+  for (int b0 = 0; b0 < q; b0 += qs.batch) {
+    const int c = std::min(qs.batch, q - b0);
+    QShard<T> sh{colbuf, R, colbuf ? row0 : 0, rows, c};
+    int* pb = path_cap > 0 ? paths + (int64_t)b0 * path_cap : paths;
+    int* nc = ncand ? ncand + b0 : nullptr;
+    cudaError_t e = sr ? query_launch<T, 1>(D, ld, WT, ldw, n, c, s + b0, t + b0, dist + b0, pb, path_cap,
+                                            path_lens + b0, nc, tau, st, sh, qs)
+                       : query_launch<T, 0>(D, ld, WT, ldw, n, c, s + b0, t + b0, dist + b0, pb, path_cap,
+                                            path_lens + b0, nc, tau, st, sh, qs);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 #define INST(T)                                                                                  \
   template cudaError_t query_batch<T>(const T*, int64_t, const T*, int64_t, int64_t, int,       \
                                       const int*, const int*, T*, int*, int, int*, int*, float,  \
-                                      int, cudaStream_t, const T*, int64_t, int64_t, int64_t);   \
+                                      int, cudaStream_t, const QueryScratch&, const T*, int64_t, \
+                                      int64_t, int64_t);                                         \
   template cudaError_t query_colslice<T>(const T*, int64_t, int64_t, int64_t, int64_t,          \
                                          const int*, int, T*, cudaStream_t);
 INST(int32_t)

@@ -39,7 +39,7 @@ struct Plan {
   int64_t ld, lcap, ocap, maxchunk;
   size_t off_wt, off_vec, off_rowpart, off_colpart, off_rowoff, off_rowcnt, off_chg, off_prow,
       off_pcol, off_plb, off_popen, off_ocol, off_ocnt, off_gprow, off_gpcol, off_glb, off_gfull,
-      off_slid, off_slw, off_wnext, off_panel, off_pt, off_bm, off_anyrow, off_qsend, off_qcol,
+      off_srow, off_scol, off_slb, off_slid, off_slw, off_wnext, off_panel, off_pt, off_anyrow, off_qsend, off_qcol,
       off_qids, off_qdsv, off_qlab, off_qpred, off_qpath, off_qdone, off_qcnt, off_small, total;
   int qcap, qbatch;
   int64_t ldpt;
@@ -76,6 +76,9 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   p.off_gpcol = take(sizeof(int32_t) * (size_t)p.ocap);
   p.off_glb = take(sizeof(int32_t) * (size_t)p.ocap);
   p.off_gfull = take((size_t)p.ocap);
+  p.off_srow = take(sizeof(int32_t) * (size_t)p.lcap);   // staging list of the detection pass
+  p.off_scol = take(sizeof(int32_t) * (size_t)p.lcap);
+  p.off_slb = take(sizeof(int32_t) * (size_t)p.lcap);
   p.off_slid = take(sizeof(int32_t) * (size_t)cap * kSL);
   p.off_slw = take(sizeof(int32_t) * (size_t)cap * kSL);
   p.off_wnext = take(sizeof(int32_t) * (size_t)cap);
@@ -83,9 +86,7 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   // transposed pivot column panel for the FW phase-3 kernel (kTile x ldpt)
   p.ldpt = round_up(world > 1 ? round_up(cdiv(cap, world), kTile) : cap, kTile);
   p.off_pt = take(sizeof(int32_t) * (size_t)kTile * p.ldpt);
-  // detection flag bitmap: one bit per entry of the local rows (n/8 bytes per row)
   const int64_t rows_max = world > 1 ? round_up(cdiv(cap, world), kTile) : cap;
-  p.off_bm = take(sizeof(uint32_t) * (size_t)rows_max * cdiv(cdiv(p.ld, 4), 256) * 32);
   p.off_anyrow = take(sizeof(int32_t) * (size_t)cap);
   // sharded queries: this rank's slices of kQueryChunk columns, and all ranks' (all-gathered)
   p.off_qsend = take(world > 1 ? sizeof(int32_t) * (size_t)kQueryChunk * rows_max : 256);
@@ -198,12 +199,14 @@ struct apsp_handle {
   int* gpcol() { return reinterpret_cast<int*>(ws + plan.off_gpcol); }
   template <typename T> T* glb() { return reinterpret_cast<T*>(ws + plan.off_glb); }
   unsigned char* gfull() { return ws + plan.off_gfull; }
+  int* srow() { return reinterpret_cast<int*>(ws + plan.off_srow); }
+  int* scol() { return reinterpret_cast<int*>(ws + plan.off_scol); }
+  template <typename T> T* slb() { return reinterpret_cast<T*>(ws + plan.off_slb); }
   int* slid() { return reinterpret_cast<int*>(ws + plan.off_slid); }
   template <typename T> T* slw() { return reinterpret_cast<T*>(ws + plan.off_slw); }
   template <typename T> T* wnext() { return reinterpret_cast<T*>(ws + plan.off_wnext); }
   template <typename T> T* panel() { return reinterpret_cast<T*>(ws + plan.off_panel); }
   template <typename T> T* pt() { return reinterpret_cast<T*>(ws + plan.off_pt); }
-  uint32_t* bm() { return reinterpret_cast<uint32_t*>(ws + plan.off_bm); }
   template <typename T> T* qsend() { return reinterpret_cast<T*>(ws + plan.off_qsend); }
   template <typename T> T* qcol() { return reinterpret_cast<T*>(ws + plan.off_qcol); }
   QueryScratch qscratch() {
@@ -364,11 +367,17 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   Rows r = h->active();
   CKR(cudaMemsetAsync(h->rowcnt(), 0, sizeof(int) * h->cap, h->st));
   CKR(cudaMemsetAsync(h->ctr(), 0, sizeof(DetectCounters), h->st));
+  // one streaming pass appends the need_update_list; then per-row slices,
+  // Phi / max|A_i| and the D0 reset (W'[i][j]) of the listed pairs
+  CKR(cudaMemsetAsync(h->ocnt(), 0, sizeof(int) * h->cap, h->st));   // scatter cursors
   PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
-     detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, h->bm(), h->anyrow(), h->sr, h->st));
+     detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, 1, nullptr, h->rowcnt(),
+               h->srow(), h->scol(), h->slb<T>(), h->plan.lcap, h->ctr(), h->WT<T>(), h->ld, h->sr,
+               h->st));
   PK(APSP_K_EMIT, 0.0,
-     detect_emit<T>(h->Dl<T>(), h->ld, r, n, h->WT<T>(), h->ld, 1, h->rowoff(), h->rowcnt(), h->prow(),
-                    h->pcol(), h->plb<T>(), h->plan.lcap, h->ctr(), h->bm(), h->anyrow(), h->st));
+     detect_lists<T>(h->Dl<T>(), h->ld, r, h->WT<T>(), h->ld, h->rowcnt(), h->rowoff(), h->srow(),
+                     h->scol(), h->slb<T>(), h->ocnt(), h->prow(), h->pcol(), h->plb<T>(), h->plan.lcap,
+                     h->ctr(), h->st));
   if (removal) CK(tombstone<T>(h->Dl<T>(), h->ld, r, n, skip, h->WT<T>(), h->ld, h->st));
 
   // counters -> host (|A|, Phi, max|A_i|, overflow), summed over ranks
@@ -376,8 +385,9 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   DetectCounters* hc = reinterpret_cast<DetectCounters*>(h->host_small);
   CKR(cudaMemcpyAsync(h->host_small, h->ctr(), sizeof(DetectCounters), cudaMemcpyDeviceToHost, h->st));
   CKR(cudaStreamSynchronize(h->st));
-  int64_t local_total = (int64_t)hc->total;
-  int64_t total = local_total, rows = hc->rows, maxrow = hc->maxrow, overflow = hc->overflow;
+  int64_t local_total = std::min<int64_t>((int64_t)hc->total, h->plan.lcap);
+  const bool local_overflow = hc->overflow != 0;
+  int64_t total = (int64_t)hc->total, rows = hc->rows, maxrow = hc->maxrow, overflow = hc->overflow;
   if (h->world > 1) {
     // [total, rows, overflow] summed, maxrow by max
     long long* v = reinterpret_cast<long long*>(h->small());
@@ -402,6 +412,10 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   bool dense = h->force_path == 2 || (h->force_path == 0 && gate) || overflow != 0;
   if (dense) {
     if (info) info->path = 3;
+    if (local_overflow)   // the list missed pairs: reset every flagged entry in place
+      PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
+         detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, 2, nullptr, nullptr, nullptr,
+                   nullptr, nullptr, 0, nullptr, h->WT<T>(), h->ld, h->sr, h->st));
     return fw_impl<T>(h);
   }
   if (info) info->path = 2;
@@ -665,7 +679,8 @@ apsp_status removal_phi(apsp_handle* h, int64_t k, int64_t* phi) {
   apsp_status s = snap_row<T>(h, k, T(0), r1);
   if (s != APSP_OK) return s;
   PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
-     detect<T>(h->Dl<T>(), ld, r, n, k, c1, r1, nullptr, nullptr, h->tau, h->bm(), h->anyrow(), h->sr, h->st));
+     detect<T>(h->Dl<T>(), ld, r, n, k, c1, r1, nullptr, nullptr, h->tau, 0, h->anyrow(), nullptr,
+               nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0, h->sr, h->st));
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(h->small() + 128);
   CKR(cudaMemsetAsync(cnt, 0, sizeof *cnt, h->st));
   CK(count_nonzero(h->anyrow() + r.lo, r.hi - r.lo, cnt, h->st));

@@ -13,6 +13,7 @@ struct DetectCounters {
   unsigned int overflow;      // list capacity exceeded
   unsigned int err;           // validation flag (add_node inputs)
   unsigned long long open_total;   // open pairs after the shortlist certification
+  unsigned long long rowbase;      // cursor of the per-row open-list slices
 };
 
 // ---------------- fw.cu ----------------  (sr: 0 shortest path, 1 minimax)
@@ -63,14 +64,18 @@ template <typename T>
 cudaError_t addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xlocal,
                           const T* col, const T* row, T* WT, int64_t ldw, const T* ow,
                           const T* iw, cudaStream_t st);
+// mode 0: mark rows with flags (anyrow); 1: append the need_update_list
+// (prow/pcol/plb, rowcnt, ctr->total/overflow); 2: reset flagged entries in place
 template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
-                   const T* c2, const T* r2, float tau, uint32_t* bm, int* anyrow, int sr,
-                   cudaStream_t st);
+                   const T* c2, const T* r2, float tau, int mode, int* anyrow, int* rowcnt,
+                   int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr, const T* WT,
+                   int64_t ldw, int sr, cudaStream_t st);
 template <typename T>
-cudaError_t detect_emit(T* D, int64_t ld, Rows r, int64_t n, const T* WT, int64_t ldw, int reset,
-                        int64_t* rowoff, int* rowcnt, int* prow, int* pcol, T* plb, int64_t lcap,
-                        DetectCounters* ctr, const uint32_t* bm, const int* anyrow, cudaStream_t st);
+cudaError_t detect_lists(T* D, int64_t ld, Rows r, const T* WT, int64_t ldw, const int* rowcnt,
+                         int64_t* rowoff, const int* srow, const int* scol, const T* slb, int* cur,
+                         int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr,
+                         cudaStream_t st);
 template <typename T>
 cudaError_t tombstone(T* D, int64_t ld, Rows r, int64_t n, int64_t k, T* WT, int64_t ldw,
                       cudaStream_t st);

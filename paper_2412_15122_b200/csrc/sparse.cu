@@ -351,14 +351,12 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
                                                       const int* __restrict__ pcol,
                                                       const T* __restrict__ plb, int64_t npairs,
                                                       unsigned char* out, int classify,
-                                                      const int* __restrict__ rowcnt, int min_cnt_skip,
                                                       OpenLists<T> ol) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t p = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); p < npairs;
        p += nw) {
     const int64_t i = prow[p], j = pcol[p];
-    if (rowcnt && rowcnt[i] >= min_cnt_skip) continue;   // done by k_sparse_short_rows
     T* Drow = D + (i - row0) * ld;
     const int* sid = SLid + j * kSL;
     const T* sw = SLw + j * kSL;
@@ -388,84 +386,6 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
     }
   }
 }
-// Phase A for rows with many listed pairs: the CTA copies row i of D0 into
-// shared memory once (a snapshot: every value in it is a valid upper bound)
-// and evaluates all the row's pairs from it.
-template <typename T, int SR>
-__global__ void __launch_bounds__(512) k_sparse_short_rows(T* D, int64_t ld, Rows r, int64_t n,
-                                                           const int* __restrict__ SLid,
-                                                           const T* __restrict__ SLw,
-                                                           const int64_t* __restrict__ rowoff,
-                                                           const int* __restrict__ rowcnt,
-                                                           const int* __restrict__ pcol,
-                                                           const T* __restrict__ plb,
-                                                           unsigned char* out, int min_cnt,
-                                                           OpenLists<T> ol) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* srow = reinterpret_cast<T*>(smem_raw);
-  __shared__ __align__(8) unsigned long long mbar;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  const unsigned bytes = (unsigned)(((n + 3) / 4) * 16);
-  const unsigned sbar = (unsigned)__cvta_generic_to_shared(&mbar);
-  const unsigned sdst = (unsigned)__cvta_generic_to_shared(srow);
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::);
-  }
-  __syncthreads();
-  unsigned phase = 0;
-  for (int64_t i = r.lo + blockIdx.x; i < r.hi; i += gridDim.x) {
-    const int cnt = rowcnt[i];
-    if (cnt < min_cnt) continue;
-    T* Drow = D + (i - r.row0) * ld;
-    // TMA 1-D bulk copy of the whole row into shared memory (one thread issues it)
-    if (threadIdx.x == 0) {
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(bytes)
-                   : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              sdst),
-          "l"(Drow), "r"(bytes), "r"(sbar)
-          : "memory");
-    }
-    {
-      unsigned done = 0;
-      while (!done) {
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-            : "=r"(done)
-            : "r"(sbar), "r"(phase)
-            : "memory");
-      }
-    }
-    phase ^= 1;
-    const int64_t off = rowoff[i];
-    for (int t = warp; t < cnt; t += nwarp) {
-      const int64_t p = off + t;
-      const int64_t j = pcol[p];
-      const int* sid = SLid + j * kSL;
-      const T* sw = SLw + j * kSL;
-      T acc = Tr<T>::inf();
-#pragma unroll
-      for (int q = 0; q < kSLK; ++q) {
-        const int m = sid[q * 32 + lane];
-        const T w = sw[q * 32 + lane];
-        if (m >= 0) acc = Tr<T, SR>::relax(acc, srow[m], w);
-      }
-      acc = warp_min<T>(acc);
-      if (lane == 0) {
-        const T cur = srow[j];
-        const T v = Tr<T>::mn(acc, cur);
-        if (v < cur) Drow[j] = v;
-        const T lb = plb[p];
-        const bool fin_ = Tr<T>::at_lb(v, lb);
-        out[p] = fin_ ? 0 : 1;
-        if (!fin_) ol.append(i, j, lb);
-      }
-    }
-    __syncthreads();
-  }
-}
 
 template <typename T>
 cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const T* SLw,
@@ -476,16 +396,15 @@ cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const 
   OpenLists<T> ol{};
   if (sr)
     k_sparse_short<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
-                                               out, classify, nullptr, 0, ol);
+                                               out, classify, ol);
   else
     k_sparse_short<T, 0><<<grid, 256, 0, st>>>(D, ld, row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
-                                               out, classify, nullptr, 0, ol);
+                                               out, classify, ol);
   return cudaGetLastError();
 }
 
-// Phase A over the detection lists: rows with >= kRowMin pairs use the
-// shared-memory row kernel (when the row fits), the others the pair kernel.
-constexpr int kRowMin = 1 << 30;  // row kernel off: heavy rows pin one SM (measured slower)
+// Phase A over the detection list (pairs in any order: the list is appended
+// by the detection stream; every pair reads only its own row).
 template <typename T>
 cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, int64_t n, const int* SLid, const T* SLw,
                            const T* wnext, const int64_t* rowoff, const int* rowcnt,
@@ -495,34 +414,13 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, int64_t n, const int* SLid,
                            cudaStream_t st) {
   if (npairs <= 0) return cudaSuccess;
   OpenLists<T> ol{ocnt, ocol, rowoff, gprow, gpcol, glb, gfull, ocap, ctr};
-  const size_t smem = sizeof(T) * (size_t)((n + 3) / 4 * 4);
-  const bool rows_ok = kRowMin < (1 << 30) && smem <= 200 * 1024;
-  if (rows_ok) {
-    static size_t configured = 0;
-    if (configured < smem) {
-      cudaError_t e = cudaFuncSetAttribute(k_sparse_short_rows<T, 0>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_sparse_short_rows<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-      if (e != cudaSuccess) return e;
-      configured = smem;
-    }
-    int grid = (int)std::min<int64_t>(r.hi - r.lo, (int64_t)num_sms() * (smem > 110 * 1024 ? 1 : 2));
-    if (grid > 0 && sr)
-      k_sparse_short_rows<T, 1><<<grid, 512, smem, st>>>(D, ld, r, n, SLid, SLw, rowoff, rowcnt, pcol,
-                                                         plb, out, kRowMin, ol);
-    else if (grid > 0)
-      k_sparse_short_rows<T, 0><<<grid, 512, smem, st>>>(D, ld, r, n, SLid, SLw, rowoff, rowcnt, pcol,
-                                                         plb, out, kRowMin, ol);
-  }
   int grid = (int)std::min<int64_t>(cdiv(npairs, 8), (int64_t)num_sms() * 16);
   if (sr)
     k_sparse_short<T, 1><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
-                                               out, 0, rows_ok ? rowcnt : nullptr, kRowMin, ol);
+                                               out, 0, ol);
   else
     k_sparse_short<T, 0><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
-                                               out, 0, rows_ok ? rowcnt : nullptr, kRowMin, ol);
+                                               out, 0, ol);
   return cudaGetLastError();
 }
 

@@ -505,17 +505,6 @@ cudaError_t addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xl
 // ---------------------------------------------------------------------------
 // affected-pair detection (need_update_list) with ballot/popc compaction
 // ---------------------------------------------------------------------------
-template <typename T>
-struct DetectArgs {
-  T* D; int64_t ld; Rows r; int64_t n; int64_t skip;
-  const T* c1; const T* r1; const T* c2; const T* r2; float tau;
-  const T* WT; int64_t ldw; int reset;
-  int64_t* rowoff; int* rowcnt; int* prow; int* pcol; T* plb; int64_t lcap;
-  DetectCounters* ctr;
-};
-
-constexpr int DT_THREADS = 256;
-
 // Theorem-4 tightness of the 4 pairs of one vector: the common case (no bit)
 // costs one add + one compare per element; validity (j < n, j != i,
 // j != skip, D finite) is applied only when some bit is set.
@@ -543,29 +532,99 @@ __device__ __forceinline__ unsigned flag_nibble(const Vec4<T>& d, const Vec4<T>&
 }
 
 // ---------------------------------------------------------------------------
-// Detection in two kernels (the launched path):
-//  (1) k_detect_stream — laid out like k_rank1: warp = (1024-column chunk) x
-//      (row slab), each lane keeps its 8 vectors of the pivot row r1 (and r2)
-//      in registers and streams the slab's rows; for every row it writes one
-//      32-bit flag word per lane (bit v*4+c <-> column 4*(chunk*256+v*32+lane)+c)
-//      and marks rows with any flag.  Pure HBM stream: 4 B read per entry, n/8
-//      bytes written per row.
-//  (2) k_detect_emit — one CTA per marked row: popcount of the row's bitmap
-//      words, block scan, one atomic for the row's list offset, then decode
-//      the flagged columns into the list (prow/pcol/plb) and reset D0.
+// k_detect_stream — the detection pass, laid out like k_rank1: warp =
+// (512-column chunk) x (row slab); each lane keeps its 4 vectors of the pivot
+// row r1 (and r2) in registers and streams the slab's rows, two rows in
+// flight.  Per row and lane a 16-bit flag word (bit v*4+c <-> column
+// 4*(chunk*128 + v*32 + lane) + c).  What happens to the flags:
+//   MODE 0 (count): mark rows with any flag (anyrow) — Definition 1's Phi.
+//   MODE 1 (emit):  append the flagged pairs (i, j, D_old[i][j]) to the
+//                   need_update_list with one warp-aggregated atomic per
+//                   (row, chunk) that has flags, and count them per row.
+//                   Flags are rare (|A| ~ 27n of n^2), so the pass stays a
+//                   pure HBM stream: 4 B read per entry, 12 B written per pair.
+//   MODE 2 (reset): D0[i][j] := W'[i][j] in place for every flagged pair (the
+//                   recovery pass when the list overflowed and FW follows).
+// Columns are owned by one warp, so rewriting D inside the pass is race-free.
 // ---------------------------------------------------------------------------
 constexpr int DS_V = 4;              // vectors per lane per row
 constexpr int DS_VEC = 32 * DS_V;    // vectors per chunk (512 columns)
-template <typename T, bool TWO, int SR>
-__global__ void __launch_bounds__(256, 2) k_detect_stream(const T* __restrict__ D, int64_t ld, Rows r,
+
+template <typename T>
+struct DetectOut {
+  int* anyrow;               // MODE 0
+  int* rowcnt;               // MODE 1: pairs per row
+  int* prow; int* pcol; T* plb; int64_t lcap;   // MODE 1: the (staging) list
+  DetectCounters* ctr;       // MODE 1: total (list cursor), overflow
+  const T* WT; int64_t ldw;  // MODE 2
+};
+
+// MODE 1 staging: the hot loop only queues, per lane with flags, its 16-bit
+// flag word and (row - slab start, lane) in shared memory; a flush decodes the
+// queue into pairs, re-reads D_old[i][j] (D is not written in this pass) and
+// appends them to the global list with ONE atomic on the list cursor per
+// flush (a single hot address otherwise hit once per (row, chunk) with flags).
+constexpr int DS_Q = 256;   // queued lane words per warp (>= 32: one row always fits)
+struct DetectQueue {
+  unsigned rl[DS_Q];        // (row - slab start) << 5 | lane
+  unsigned short w[DS_Q];   // flag word: bit v*4+c <-> column 4*(chunk*128 + v*32 + lane) + c
+};
+template <typename T>
+__device__ __forceinline__ void detect_flush(const DetectQueue& Q, int cnt, const T* D, int64_t ld,
+                                             int64_t row0, int64_t i_lo, int chunk,
+                                             const DetectOut<T>& o, int lane) {
+  if (cnt == 0) return;
+  __syncwarp();
+  // lane e takes queue entries e, e+32, ...: count its pairs, scan, one atomic
+  int mine = 0;
+  for (int e = lane; e < cnt; e += 32) mine += __popc((unsigned)Q.w[e]);
+  int incl = mine;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  const int tot = __shfl_sync(0xffffffffu, incl, 31);
+  unsigned long long base = 0;
+  if (lane == 0) {
+    base = atomicAdd(&o.ctr->total, (unsigned long long)tot);
+    if ((int64_t)(base + tot) > o.lcap) atomicOr(&o.ctr->overflow, 1u);
+  }
+  base = __shfl_sync(0xffffffffu, base, 0);
+  int64_t pos = (int64_t)base + incl - mine;
+  for (int e = lane; e < cnt; e += 32) {
+    unsigned w = Q.w[e];
+    const unsigned rl = Q.rl[e];
+    const int64_t i = i_lo + (rl >> 5);
+    const int ln = (int)(rl & 31u);
+    const T* Drow = D + (i - row0) * ld;
+    while (w) {
+      const int bit = __ffs(w) - 1;
+      w &= w - 1;
+      const int64_t j = 4 * ((int64_t)chunk * DS_VEC + (bit >> 2) * 32 + ln) + (bit & 3);
+      if (pos < o.lcap) {
+        o.prow[pos] = (int)i;
+        o.pcol[pos] = (int)j;
+        o.plb[pos] = Drow[j];   // D_old[i][j]: a lower bound of D'
+      }
+      ++pos;
+    }
+  }
+  __syncwarp();
+}
+
+template <typename T, bool TWO, int SR, int MODE>
+__global__ void __launch_bounds__(256, 2) k_detect_stream(T* __restrict__ D, int64_t ld, Rows r,
                                                           int64_t n, int64_t skip, Tiling tl,
                                                           const T* __restrict__ c1,
                                                           const T* __restrict__ r1,
                                                           const T* __restrict__ c2,
                                                           const T* __restrict__ r2, float tau,
-                                                          uint16_t* __restrict__ bm, int64_t bmld,
-                                                          int* __restrict__ anyrow) {
+                                                          DetectOut<T> o) {
+  __shared__ DetectQueue sq[MODE == 1 ? 8 : 1];
   const int lane = threadIdx.x & 31;
+  DetectQueue& Q = sq[MODE == 1 ? (threadIdx.x >> 5) : 0];
+  int qcnt = 0;   // MODE 1: queued lane words (warp-uniform)
   const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (gw >= tl.warps) return;
   const int chunk = (int)(gw % tl.nchunk);
@@ -582,23 +641,27 @@ __global__ void __launch_bounds__(256, 2) k_detect_stream(const T* __restrict__ 
     if (TWO) b[v] = qv[v] < tl.n4 ? ld4<T>(r2 + 4 * qv[v]) : Vec4<T>{I, I, I, I};
   }
   for (int64_t i0 = i_lo; i0 < i_hi; i0 += 2) {
-    // two rows in flight per lane; a row that cannot be tight is not read
+    // two rows in flight per lane; the row loads are issued first (their
+    // predicate needs no memory), the column snapshot c1[i] after them
     bool act[2];
     T ci[2], cj[2];
+    Vec4<T> d[2][DS_V];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t i = i0 + h;
+      act[h] = i < i_hi && i != skip;
+      const T* row = D + (i - r.row0) * ld;
+#pragma unroll
+      for (int v = 0; v < DS_V; ++v)
+        d[h][v] = (act[h] && qv[v] < tl.n4) ? ld4_stream<T>(row + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int64_t i = i0 + h;
       ci[h] = (i < i_hi) ? c1[i] : I;
       cj[h] = (TWO && i < i_hi) ? c2[i] : I;
-      act[h] = i < i_hi && i != skip && (Tr<T>::fin(ci[h]) || Tr<T>::fin(cj[h]));
-    }
-    Vec4<T> d[2][DS_V];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const T* row = D + (i0 + h - r.row0) * ld;
-#pragma unroll
-      for (int v = 0; v < DS_V; ++v)
-        d[h][v] = (act[h] && qv[v] < tl.n4) ? ld4_stream<T>(row + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+      // a row that cannot be tight (no path through the element) has no flags
+      act[h] = act[h] && (Tr<T>::fin(ci[h]) || Tr<T>::fin(cj[h]));
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -609,111 +672,128 @@ __global__ void __launch_bounds__(256, 2) k_detect_stream(const T* __restrict__ 
       for (int v = 0; v < DS_V; ++v)
         word |= flag_nibble<T, TWO, SR>(d[h][v], a[v], b[v], ci[h], cj[h], 4 * qv[v], n, i, skip, tau)
                 << (4 * v);
-      bm[(i - r.lo) * bmld + chunk * 32 + lane] = (uint16_t)word;
-      if (__any_sync(0xffffffffu, word != 0) && lane == 0) anyrow[i] = 1;
+      if (!__any_sync(0xffffffffu, word != 0)) continue;
+      if (MODE == 0) {
+        if (lane == 0) o.anyrow[i] = 1;
+      } else if (MODE == 1) {
+        const int tot = __reduce_add_sync(0xffffffffu, (unsigned)__popc(word));
+        if (lane == 0) atomicAdd(o.rowcnt + i, tot);
+        if (qcnt + 32 > DS_Q) {
+          detect_flush<T>(Q, qcnt, D, ld, r.row0, i_lo, chunk, o, lane);
+          qcnt = 0;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, word != 0);
+        if (word) {
+          const int qp = qcnt + __popc(bal & ((1u << lane) - 1));
+          Q.rl[qp] = (unsigned)(i - i_lo) << 5 | (unsigned)lane;
+          Q.w[qp] = (unsigned short)word;
+        }
+        qcnt += __popc(bal);
+      } else {
+        T* row = D + (i - r.row0) * ld;
+#pragma unroll
+        for (int v = 0; v < DS_V; ++v)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if ((word >> (4 * v + c)) & 1u) {
+              const int64_t j = 4 * qv[v] + c;
+              row[j] = o.WT[j * o.ldw + i];   // D0[i][j] := W'[i][j]
+            }
+      }
     }
+  }
+  if (MODE == 1) detect_flush<T>(Q, qcnt, D, ld, r.row0, i_lo, chunk, o, lane);
+}
+
+// Per row of the list: rowoff[i] (a slice of rowcnt[i] slots for the row's
+// open pairs), Phi (rows with a non-empty list) and max |A_i|.
+__global__ void k_detect_rows(Rows r, const int* __restrict__ rowcnt, int64_t* rowoff,
+                              DetectCounters* ctr) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = r.lo + (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; i0 < r.hi;
+       i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + lane;
+    const int c = i < r.hi ? rowcnt[i] : 0;
+    int incl = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    const unsigned nz = __ballot_sync(0xffffffffu, c > 0);
+    const unsigned mx = __reduce_max_sync(0xffffffffu, (unsigned)c);
+    unsigned long long base = 0;
+    if (lane == 0 && tot) {
+      base = atomicAdd(&ctr->rowbase, (unsigned long long)tot);
+      atomicAdd(&ctr->rows, (unsigned)__popc(nz));
+      atomicMax(&ctr->maxrow, mx);
+    }
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (c > 0) rowoff[i] = (int64_t)base + incl - c;
   }
 }
 
+// Group the staged list by row (counting sort on rowoff, the row's slot cursor
+// in `cur`) and reset D0[i][j] := W'[i][j] for every listed pair: phase A then
+// walks the pairs row by row (the row's D entries stay hot in L2).
 template <typename T>
-__global__ void __launch_bounds__(DT_THREADS) k_detect_emit(DetectArgs<T> a,
-                                                            const uint16_t* __restrict__ bm,
-                                                            int64_t bmld, int nwords,
-                                                            const int* __restrict__ anyrow) {
-  __shared__ int s_warp[DT_THREADS / 32];
-  __shared__ long long s_base;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int64_t i = a.r.lo + blockIdx.x; i < a.r.hi; i += gridDim.x) {
-    if (!anyrow[i]) continue;
-    const uint16_t* brow = bm + (i - a.r.lo) * bmld;
-    T* Drow = a.D + (i - a.r.row0) * a.ld;
-    const int wpt = (nwords + DT_THREADS - 1) / DT_THREADS;
-    const int w0 = min(tid * wpt, nwords), w1 = min(w0 + wpt, nwords);
-    int cnt = 0;
-    for (int w = w0; w < w1; ++w) cnt += __popc(brow[w]);
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    int woff = 0, total = 0;
-#pragma unroll
-    for (int w = 0; w < DT_THREADS / 32; ++w) {
-      const int sw = s_warp[w];
-      woff += (w < warp) ? sw : 0;
-      total += sw;
-    }
-    if (tid == 0) {
-      unsigned long long base = atomicAdd(&a.ctr->total, (unsigned long long)total);
-      a.rowoff[i] = (int64_t)base;
-      a.rowcnt[i] = total;
-      atomicAdd(&a.ctr->rows, 1u);
-      atomicMax(&a.ctr->maxrow, (unsigned)total);
-      if ((int64_t)base + total > a.lcap) atomicOr(&a.ctr->overflow, 1u);
-      s_base = (long long)base;
-    }
-    __syncthreads();
-    const int64_t base = s_base;
-    const bool store = base + total <= a.lcap;
-    int64_t pos = base + woff + incl - cnt;
-    for (int w = w0; w < w1; ++w) {
-      uint32_t bits = brow[w];
-      const int chunk = w >> 5, ln = w & 31;
-      while (bits) {
-        const int bit = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const int64_t j = 4 * ((int64_t)chunk * DS_VEC + (bit >> 2) * 32 + ln) + (bit & 3);
-        if (store) {
-          a.pcol[pos] = (int)j;
-          a.prow[pos] = (int)i;
-          a.plb[pos] = Drow[j];                          // D_old[i][j]: a lower bound of D'
-        }
-        ++pos;
-        if (a.reset) Drow[j] = a.WT[j * a.ldw + i];    // D0[i][j] := W'[i][j]
-      }
-    }
-    __syncthreads();   // s_warp / s_base reused by the next row
+__global__ void k_scatter_pairs(T* D, int64_t ld, int64_t row0, const T* __restrict__ WT, int64_t ldw,
+                                const int* __restrict__ srow, const int* __restrict__ scol,
+                                const T* __restrict__ slb, const int64_t* __restrict__ rowoff,
+                                int* cur, int* prow, int* pcol, T* plb, const DetectCounters* ctr,
+                                int64_t lcap) {
+  const int64_t np = min((int64_t)ctr->total, lcap);
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int i = srow[p], j = scol[p];
+    const int64_t q = rowoff[i] + atomicAdd(cur + i, 1);
+    prow[q] = i;
+    pcol[q] = j;
+    plb[q] = slb[p];
+    D[((int64_t)i - row0) * ld + j] = WT[(int64_t)j * ldw + i];
   }
 }
 
 template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
-                   const T* c2, const T* r2, float tau, uint32_t* bm32, int* anyrow, int sr,
-                   cudaStream_t st) {
+                   const T* c2, const T* r2, float tau, int mode, int* anyrow, int* rowcnt,
+                   int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr, const T* WT,
+                   int64_t ldw, int sr, cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
-  uint16_t* bm = reinterpret_cast<uint16_t*>(bm32);
-  Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20, DS_VEC, 32);
-  const int64_t bmld = (int64_t)tl.nchunk * 32;
-  CUDA_TRY(cudaMemsetAsync(anyrow + r.lo, 0, sizeof(int) * (size_t)(r.hi - r.lo), st));
-  const int g1 = (int)cdiv(tl.warps, 8);
-  if (c2 && sr)
-    k_detect_stream<T, true, 1><<<g1, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, c2, r2, tau, bm, bmld, anyrow);
-  else if (c2)
-    k_detect_stream<T, true, 0><<<g1, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, c2, r2, tau, bm, bmld, anyrow);
-  else if (sr)
-    k_detect_stream<T, false, 1><<<g1, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, nullptr, nullptr, tau, bm,
-                                                     bmld, anyrow);
-  else
-    k_detect_stream<T, false, 0><<<g1, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, nullptr, nullptr, tau, bm,
-                                                     bmld, anyrow);
+  Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20, DS_VEC, 64);   // 64 warps/SM: 4 waves (measured best)
+  if (tl.slab >= (1 << 26)) return cudaErrorInvalidValue;   // MODE-1 queue packing
+  if (mode == 0) CUDA_TRY(cudaMemsetAsync(anyrow + r.lo, 0, sizeof(int) * (size_t)(r.hi - r.lo), st));
+  DetectOut<T> o{anyrow, rowcnt, prow, pcol, plb, lcap, ctr, WT, ldw};
+  const int g = (int)cdiv(tl.warps, 8);
+#define LAUNCH(TWO, SR, MODE)                                                                    \
+  k_detect_stream<T, TWO, SR, MODE><<<g, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, c2, r2, tau, o)
+#define BY_MODE(TWO, SR)                 \
+  if (mode == 0) LAUNCH(TWO, SR, 0);     \
+  else if (mode == 1) LAUNCH(TWO, SR, 1); \
+  else LAUNCH(TWO, SR, 2);
+  if (c2 && sr) { BY_MODE(true, 1) }
+  else if (c2) { BY_MODE(true, 0) }
+  else if (sr) { BY_MODE(false, 1) }
+  else { BY_MODE(false, 0) }
+#undef BY_MODE
+#undef LAUNCH
   return cudaGetLastError();
 }
 
+// After a MODE-1 pass: per-row slices, Phi, max|A_i|, then the row grouping
+// of the staged list and the D0 reset.  `cur` (cap ints) must be zero.
 template <typename T>
-cudaError_t detect_emit(T* D, int64_t ld, Rows r, int64_t n, const T* WT, int64_t ldw, int reset,
-                        int64_t* rowoff, int* rowcnt, int* prow, int* pcol, T* plb, int64_t lcap,
-                        DetectCounters* ctr, const uint32_t* bm, const int* anyrow, cudaStream_t st) {
+cudaError_t detect_lists(T* D, int64_t ld, Rows r, const T* WT, int64_t ldw, const int* rowcnt,
+                         int64_t* rowoff, const int* srow, const int* scol, const T* slb, int* cur,
+                         int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr,
+                         cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
-  Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20, DS_VEC, 32);
-  const int64_t bmld = (int64_t)tl.nchunk * 32;
-  DetectArgs<T> a{D, ld, r, n, -1, nullptr, nullptr, nullptr, nullptr, 0.f, WT, ldw, reset,
-                  rowoff, rowcnt, prow, pcol, plb, lcap, ctr};
-  const int g2 = (int)std::min<int64_t>(r.hi - r.lo, (int64_t)num_sms() * 8);
-  k_detect_emit<T><<<g2, DT_THREADS, 0, st>>>(a, reinterpret_cast<const uint16_t*>(bm), bmld,
-                                              (int)bmld, anyrow);
+  const int g = (int)std::min<int64_t>(cdiv(r.hi - r.lo, 256), 2 * num_sms());
+  k_detect_rows<<<g, 256, 0, st>>>(r, rowcnt, rowoff, ctr);
+  CUDA_TRY(cudaGetLastError());
+  k_scatter_pairs<T><<<num_sms() * 8, 256, 0, st>>>(D, ld, r.row0, WT, ldw, srow, scol, slb, rowoff,
+                                                    cur, prow, pcol, plb, ctr, lcap);
   return cudaGetLastError();
 }
 
@@ -877,10 +957,11 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
   template cudaError_t addnode_write<T>(T*, int64_t, Rows, int64_t, int64_t, int, const T*,        \
                                         const T*, T*, int64_t, const T*, const T*, cudaStream_t); \
   template cudaError_t detect<T>(T*, int64_t, Rows, int64_t, int64_t, const T*, const T*,          \
-                                 const T*, const T*, float, uint32_t*, int*, int, cudaStream_t);  \
-  template cudaError_t detect_emit<T>(T*, int64_t, Rows, int64_t, const T*, int64_t, int,          \
-                                      int64_t*, int*, int*, int*, T*, int64_t, DetectCounters*,    \
-                                      const uint32_t*, const int*, cudaStream_t);                 \
+                                 const T*, const T*, float, int, int*, int*, int*, int*, T*,      \
+                                 int64_t, DetectCounters*, const T*, int64_t, int, cudaStream_t); \
+  template cudaError_t detect_lists<T>(T*, int64_t, Rows, const T*, int64_t, const int*, int64_t*, \
+                                       const int*, const int*, const T*, int*, int*, int*, T*,     \
+                                       int64_t, DetectCounters*, cudaStream_t);                    \
   template cudaError_t tombstone<T>(T*, int64_t, Rows, int64_t, int64_t, T*, int64_t,              \
                                     cudaStream_t);                                                \
   template cudaError_t copy_row<T>(T*, const T*, int64_t, cudaStream_t);                           \

@@ -127,6 +127,8 @@ struct apsp_handle {
   unsigned char* ws;
   Plan plan;
   cudaStream_t st;
+  cudaStream_t st2 = nullptr;    // side stream: shortlist upkeep overlapped with the D passes
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int rank, world;
   Comm* comm = nullptr;          // world > 1: NCCL or in-process group (comm.h)
   // options
@@ -278,6 +280,14 @@ apsp_status fail(apsp_handle* h, apsp_status s, const char* fmt, ...) {
     }                                                                                     \
   } while (0)
 #define CK(expr) PK(APSP_K_OTHER, 0, expr)
+// a launch on the side stream (not bracketed by the profiling events)
+#define CK2(expr)                                                                         \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    ++h->launches;                                                                        \
+    if (_e != cudaSuccess)                                                                \
+      return fail(h, APSP_E_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));       \
+  } while (0)
 #define CKR(expr)                                                                         \
   do {                                                                                    \
     cudaError_t _e = (expr);                                                              \
@@ -512,6 +522,14 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
     return fail(h, APSP_E_INVAL, "add_node: %s",
                 (*herr & 2) ? "undirected graph needs out_w == in_w" : "negative or NaN weight");
   }
+  // shortlist upkeep needs only the validated edge vectors: it runs on the
+  // side stream while pass 1 / rank-1 stream D (joined before returning)
+  CKR(cudaEventRecord(h->ev_fork, h->st));
+  CKR(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
+  CK2(shortlist_add_bound<T>(h->slid(), h->slw<T>(), h->wnext<T>(), ow, n, x, h->st2));  // x -> j
+  CK2(shortlist_build_one<T>(iw, 0, n + 1, x, h->slid(), h->slw<T>(), h->wnext<T>(),
+                             h->st2));   // in-edges of x: row x of WT is in_w
+  CKR(cudaEventRecord(h->ev_join, h->st2));
   Rows r = h->active();
   int nchunk = 0, nslab = 0;
   T* rowpartM = h->rowpart<T>() + (size_t)h->plan.maxchunk * ld;
@@ -528,9 +546,7 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
      rank1<T>(h->Dl<T>(), ld, r, n, ceff, row, nullptr, nullptr, h->rank1_bytes(), h->sr, h->st));
   CK(addnode_write<T>(h->Dl<T>(), ld, r, n, x, h->local(x) ? 1 : 0, col, row, h->WT<T>(), ld, ow,
                       iw, h->st));
-  CK(shortlist_add_bound<T>(h->slid(), h->slw<T>(), h->wnext<T>(), ow, n, x, h->st));  // x -> j
-  CK(shortlist_build_one<T>(h->WT<T>(), ld, n + 1, x, h->slid(), h->slw<T>(), h->wnext<T>(),
-                            h->st));                                 // in-edges of x
+  CKR(cudaStreamWaitEvent(h->st, h->ev_join, 0));   // shortlist upkeep (side stream) done
   h->n = n + 1;
   if (new_index) *new_index = x;
   if (info) {
@@ -893,6 +909,18 @@ apsp_status apsp_nccl_unique_id(void* out128) {
 
 namespace {
 
+// Frees everything a handle owns (never the caller's memory).
+void release_handle(apsp_handle* h) {
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
+  for (auto& r : h->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  if (h->st2) { cudaStreamSynchronize(h->st2); cudaStreamDestroy(h->st2); }
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  delete h->comm;
+  if (h->host_small) cudaFreeHost(h->host_small);
+  delete h;
+}
+
 // Shared by apsp_create (NCCL) and apsp_create_local (in-process group):
 // exactly one of nccl_id / group is used when world > 1.
 apsp_status create_impl(apsp_handle** out, apsp_dtype dtype, int directed, int64_t n, int64_t cap,
@@ -928,12 +956,18 @@ apsp_status create_impl(apsp_handle** out, apsp_dtype dtype, int directed, int64
     delete h;
     return APSP_E_CUDA;
   }
+  if (cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    cudaFreeHost(h->host_small);
+    delete h;
+    return APSP_E_CUDA;
+  }
   if (world > 1) {
     int err = 0;
     h->comm = group ? make_local_comm(group, rank) : make_nccl_comm(nccl_id, world, rank, &err);
     if (!h->comm) {
-      cudaFreeHost(h->host_small);
-      delete h;
+      release_handle(h);
       return APSP_E_NCCL;
     }
   }
@@ -952,9 +986,7 @@ apsp_status create_impl(apsp_handle** out, apsp_dtype dtype, int directed, int64
     return APSP_OK;
   });
   if (s != APSP_OK) {
-    delete h->comm;
-    cudaFreeHost(h->host_small);
-    delete h;
+    release_handle(h);
     return s;
   }
   *out = h;
@@ -1003,10 +1035,7 @@ apsp_status apsp_destroy(apsp_handle* h) {
   if (!h) return APSP_E_INVAL;
   if (h->st) cudaStreamSynchronize(h->st);
   h->prof_resolve();
-  for (auto e : h->ev_pool) cudaEventDestroy(e);
-  delete h->comm;
-  if (h->host_small) cudaFreeHost(h->host_small);
-  delete h;
+  release_handle(h);
   return APSP_OK;
 }
 

@@ -244,12 +244,21 @@ cudaError_t shortlist_set_edge(int* SLid, T* SLw, T* wnext, int64_t u, int64_t v
 // (weight INF), entries naming `last` are renamed k, row k takes row last.
 template <typename T>
 __global__ void k_shortlist_remove(int* SLid, T* SLw, T* wnext, int64_t n, int k, int last) {
-  const int64_t tot = n * kSL;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+  const int64_t tot4 = n * kSL / 4;   // kSL is a multiple of 4: 16-byte id vectors
+  int4* ids4 = reinterpret_cast<int4*>(SLid);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot4;
        e += (int64_t)gridDim.x * blockDim.x) {
-    int id = SLid[e];
-    if (id == k) { SLid[e] = -1; SLw[e] = Tr<T>::inf(); }
-    else if (id == last && last != k) SLid[e] = k;
+    int4 v = ids4[e];
+    const bool hk = v.x == k || v.y == k || v.z == k || v.w == k;
+    const bool hl = last != k && (v.x == last || v.y == last || v.z == last || v.w == last);
+    if (!hk && !hl) continue;   // the common case: one 16-byte read
+    int* id = &v.x;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (id[c] == k) { id[c] = -1; SLw[4 * e + c] = Tr<T>::inf(); }
+      else if (hl && id[c] == last) id[c] = k;
+    }
+    ids4[e] = v;
   }
 }
 template <typename T>
@@ -265,7 +274,7 @@ __global__ void k_shortlist_move_row(int* SLid, T* SLw, T* wnext, int k, int las
 template <typename T>
 cudaError_t shortlist_remove(int* SLid, T* SLw, T* wnext, int64_t n, int64_t k, int64_t last,
                              cudaStream_t st) {
-  int grid = (int)std::min<int64_t>(cdiv(n * kSL, 256), 8 * num_sms());
+  int grid = (int)std::min<int64_t>(cdiv(n * kSL / 4, 256), 16 * num_sms());
   k_shortlist_remove<T><<<grid, 256, 0, st>>>(SLid, SLw, wnext, n, (int)k, (int)last);
   if (k != last) k_shortlist_move_row<T><<<1, 256, 0, st>>>(SLid, SLw, wnext, (int)k, (int)last);
   return cudaGetLastError();

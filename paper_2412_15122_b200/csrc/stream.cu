@@ -357,43 +357,68 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
   return cudaGetLastError();
 }
 
+// Reduce the pass-1 partials: col[i] / M[i] over the nchunk column chunks,
+// row[j] over the nslab row slabs.  CTA = 8 warps x 32 consecutive indices:
+// warp g reduces partials g, g+8, ... (coalesced 128-byte rows of the
+// partial arrays), then the 8 warp results meet in shared memory.
 template <typename T>
-__global__ void k_addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
-                                 int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,
-                                 T* ceff, T* row) {
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = r.lo + tid; i < r.hi; i += stride) {
+__global__ void __launch_bounds__(256) k_addnode_finish(const T* rowpart, const T* rowpartM,
+                                                        int nchunk, const T* colpart, int nslab,
+                                                        int64_t part_ld, Rows r, int64_t n,
+                                                        int64_t npad, int64_t ntile_i, T* col,
+                                                        T* ceff, T* row) {
+  __shared__ T sm[8][32], sM[8][32];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  if (blockIdx.x < ntile_i) {
+    const int64_t i = r.lo + (int64_t)blockIdx.x * 32 + lane;
     T m = Tr<T>::inf();
     T M = -Tr<T>::inf();
-    for (int c = 0; c < nchunk; ++c) {
-      m = Tr<T>::mn(m, rowpart[(int64_t)c * part_ld + i]);
-      const T x = rowpartM[(int64_t)c * part_ld + i];
-      M = Tr<T>::kFloat ? fmaxf(M, x) : max(M, x);
+    if (i < r.hi)
+      for (int c = g; c < nchunk; c += 8) {
+        m = Tr<T>::mn(m, rowpart[(int64_t)c * part_ld + i]);
+        const T x = rowpartM[(int64_t)c * part_ld + i];
+        M = Tr<T>::kFloat ? fmaxf(M, x) : max(M, x);
+      }
+    sm[g][lane] = m;
+    sM[g][lane] = M;
+    __syncthreads();
+    if (g == 0 && i < r.hi) {
+#pragma unroll
+      for (int q = 1; q < 8; ++q) {
+        m = Tr<T>::mn(m, sm[q][lane]);
+        M = Tr<T>::kFloat ? fmaxf(M, sM[q][lane]) : max(M, sM[q][lane]);
+      }
+      m = Tr<T>::sat(m);
+      col[i] = m;
+      // pass 2 may skip row i unless col[i] < M[i] (fp32: with a relative
+      // margin, so rounding in d - out can only keep rows, never drop them)
+      bool keep;
+      if constexpr (Tr<T>::kFloat) keep = m < M + fabsf(M) * 1e-6f;
+      else keep = m < M;
+      ceff[i] = keep ? m : Tr<T>::inf();
     }
-    m = Tr<T>::sat(m);
-    col[i] = m;
-    // pass 2 may skip row i unless col[i] < M[i] (fp32: with a relative
-    // margin, so rounding in d - out can only keep rows, never drop them)
-    bool keep;
-    if constexpr (Tr<T>::kFloat) keep = m < M + fabsf(M) * 1e-6f;
-    else keep = m < M;
-    ceff[i] = keep ? m : Tr<T>::inf();
-  }
-  for (int64_t j = tid; j < npad; j += stride) {
+  } else {
+    const int64_t j = (int64_t)(blockIdx.x - ntile_i) * 32 + lane;
     T m = Tr<T>::inf();
     if (j < n)
-      for (int s = 0; s < nslab; ++s) m = Tr<T>::mn(m, colpart[(int64_t)s * part_ld + j]);
-    row[j] = Tr<T>::sat(m);
+      for (int s = g; s < nslab; s += 8) m = Tr<T>::mn(m, colpart[(int64_t)s * part_ld + j]);
+    sm[g][lane] = m;
+    __syncthreads();
+    if (g == 0 && j < npad) {
+#pragma unroll
+      for (int q = 1; q < 8; ++q) m = Tr<T>::mn(m, sm[q][lane]);
+      row[j] = Tr<T>::sat(m);
+    }
   }
 }
 template <typename T>
 cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
                            int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,
                            T* ceff, T* row, cudaStream_t st) {
-  int grid = (int)std::min<int64_t>(cdiv(std::max<int64_t>(npad, r.hi - r.lo), 256), 4 * num_sms());
-  k_addnode_finish<T><<<grid, 256, 0, st>>>(rowpart, rowpartM, nchunk, colpart, nslab, part_ld, r, n,
-                                            npad, col, ceff, row);
+  const int64_t ti = cdiv(std::max<int64_t>(r.hi - r.lo, 0), 32), tj = cdiv(npad, 32);
+  if (ti + tj == 0) return cudaSuccess;
+  k_addnode_finish<T><<<(unsigned)(ti + tj), 256, 0, st>>>(rowpart, rowpartM, nchunk, colpart, nslab,
+                                                           part_ld, r, n, npad, ti, col, ceff, row);
   return cudaGetLastError();
 }
 

@@ -205,7 +205,8 @@ def main():
 
     spec = dataclasses.replace(synth.C4, n=args.n, seed=args.seed)
     n0 = spec.n
-    steps_total = args.warmup + args.steps + (0 if args.no_e2e else args.steps)
+    # warm-up, timed, e2e and profiled steps each consume their own updates
+    steps_total = args.warmup + 2 * args.steps + (0 if args.no_e2e else args.steps)
     cap = n0 + UPDATES_PER_STEP + 4 * steps_total
     t_setup = time.perf_counter()
     W = synth.graph(spec)
@@ -284,8 +285,6 @@ def main():
     clk = ClockSampler()
     if rank == 0:
         clk.start()
-    L.apsp_profile_reset(h.h)
-    L.apsp_profile_enable(h.h, True)
     launches0 = h.launches()
     barrier()
     t0 = torch.cuda.Event(enable_timing=True)
@@ -297,9 +296,8 @@ def main():
     barrier()
     total_ms = max_over_ranks(t0.elapsed_time(t1))
     launches = h.launches() - launches0
-    L.apsp_profile_enable(h.h, False)
-    prof = L.apsp_profile_read(h.h)
     clocks = clk.stop(gpu_index=None) if rank == 0 else None
+
 
     entries = sum(na * na for _, _, na, _ in per_update)
     value = entries / (total_ms / 1e3)
@@ -346,6 +344,23 @@ def main():
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
                "ms_per_step": e2e_ms / args.steps}
 
+    # ---------------- profiled pass (not the timed one): the library brackets
+    # every kernel with CUDA events on its stream -> per-class time and work
+    L.apsp_profile_reset(h.h)
+    L.apsp_profile_enable(h.h, True)
+    barrier()
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    s_prof = args.warmup + args.steps + (0 if args.no_e2e else args.steps)
+    for s in range(s_prof, s_prof + args.steps):
+        run_step(s, False)
+    p1.record(stream)
+    barrier()
+    prof_total_ms = max_over_ranks(p0.elapsed_time(p1))
+    L.apsp_profile_enable(h.h, False)
+    prof = L.apsp_profile_read(h.h)
+
     # ---------------- roofline of the dominant kernel class
     mp, peak_kind = peaks()
     hbm_peak = float(mp.get("hbm_gbs", 6650.0))
@@ -372,7 +387,7 @@ def main():
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": traffic, "launches": cnt_d,
                 "peak_kind": f"{peak_kind} copy bandwidth"}
-    share = {k: round(v[0] / max(total_ms, 1e-9), 4) for k, v in prof.items()}
+    share = {k: round(v[0] / max(prof_total_ms, 1e-9), 4) for k, v in prof.items()}
     kern = {k: {"ms": round(v[0], 3), "launches": v[1],
                 "achieved": (round(v[2] / (v[0] / 1e3) / (1e12 if k.startswith("fw") else 1e9), 2) if v[0] > 0 else None),
                 "unit": "Trelax/s" if k.startswith("fw") else "GB/s"} for k, v in prof.items()}

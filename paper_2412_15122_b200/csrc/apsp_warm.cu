@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/apsp_warm.h"
@@ -230,7 +231,30 @@ struct apsp_handle {
   unsigned long long* rank1_bytes() {   // device counter of bytes the rank-1 kernel read
     return reinterpret_cast<unsigned long long*>(ws + plan.off_small + 320);
   }
+  unsigned* wmin_dev() {   // accumulator of the smallest edge weight (bits of a T >= 0)
+    return reinterpret_cast<unsigned*>(ws + plan.off_small + 384);
+  }
   unsigned char* small() { return ws + plan.off_small + 512; }   // query scratch etc.
+  // host copy: the smallest weight of any edge present since creation, as the
+  // bits of a T >= 0 (~0u: none).  A lower bound of every distance between
+  // distinct nodes (removals and increases only remove weights).
+  unsigned wmin_bits = ~0u;
+  template <typename T> T wmin() const {
+    if (wmin_bits == ~0u) return T(0);
+    if constexpr (std::is_same<T, float>::value) { float f; std::memcpy(&f, &wmin_bits, 4); return f; }
+    else return (T)wmin_bits;
+  }
+  template <typename T> void fold_wmin(T w) {   // host code: no device traits here
+    unsigned b;
+    if constexpr (std::is_same<T, float>::value) {
+      if (!(w >= 0.0f) || std::isinf(w)) return;
+      std::memcpy(&b, &w, 4);
+    } else {
+      if (w < 0 || w >= APSP_INF_I32) return;
+      b = (unsigned)w;
+    }
+    wmin_bits = std::min(wmin_bits, b);
+  }
   template <typename T> T* Dl() { return reinterpret_cast<T*>(D); }
   template <typename T> T* Drow(int64_t gi) { return Dl<T>() + (gi - row0) * ld; }
   bool local(int64_t gi) const { return gi >= row0 && gi < row0 + rows; }
@@ -511,17 +535,21 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   T* col = h->vec<T>(2);
   T* row = h->vec<T>(3);
   CKR(cudaMemsetAsync(&h->ctr()->err, 0, sizeof(unsigned), h->st));
-  CK(validate_vec<T>(reinterpret_cast<const T*>(out_w), nullptr, n, ld, ow, &h->ctr()->err, h->st));
+  CKR(cudaMemsetAsync(h->wmin_dev(), 0xff, sizeof(unsigned), h->st));
+  CK(validate_vec<T>(reinterpret_cast<const T*>(out_w), nullptr, n, ld, ow, &h->ctr()->err, h->wmin_dev(),
+                     h->st));
   CK(validate_vec<T>(reinterpret_cast<const T*>(in_w),
                      h->directed ? nullptr : reinterpret_cast<const T*>(out_w), n, ld, iw,
-                     &h->ctr()->err, h->st));
+                     &h->ctr()->err, h->wmin_dev(), h->st));
   unsigned* herr = reinterpret_cast<unsigned*>(h->host_small);
   CKR(cudaMemcpyAsync(herr, &h->ctr()->err, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+  CKR(cudaMemcpyAsync(herr + 1, h->wmin_dev(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
   CKR(cudaStreamSynchronize(h->st));
   if (*herr) {
     return fail(h, APSP_E_INVAL, "add_node: %s",
                 (*herr & 2) ? "undirected graph needs out_w == in_w" : "negative or NaN weight");
   }
+  h->wmin_bits = std::min(h->wmin_bits, herr[1]);
   // shortlist upkeep needs only the validated edge vectors: it runs on the
   // side stream while pass 1 / rank-1 stream D (joined before returning)
   CKR(cudaEventRecord(h->ev_fork, h->st));
@@ -625,6 +653,7 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
     if (info) { info->kind = 0; info->early_exit = 1; }
     return APSP_OK;
   }
+  h->fold_wmin<T>(w_new);
   Rows r = h->active();
   T* c1 = h->vec<T>(4);
   T* r1 = h->vec<T>(5);
@@ -801,7 +830,7 @@ apsp_status query_dispatch(apsp_handle* h, int q, const int* s, const int* t, T*
   if (h->world <= 1) {
     PK(APSP_K_QUERY, 8.0 * (double)n * q,
        query_batch<T>(h->Dl<T>(), ld, h->WT<T>(), ld, n, q, s, t, dist, paths, path_cap, lens, ncand,
-                      h->tau, h->sr, h->st, h->qscratch()));
+                      h->tau, h->sr, h->st, h->qscratch(), h->wmin<T>()));
     return APSP_OK;
   }
   Rows r = h->active();
@@ -814,7 +843,7 @@ apsp_status query_dispatch(apsp_handle* h, int q, const int* s, const int* t, T*
     PK(APSP_K_QUERY, 8.0 * (double)n * c,
        query_batch<T>(h->Dl<T>(), ld, h->WT<T>(), ld, n, c, s + b0, t + b0, dist + b0, pb, path_cap,
                       lens + b0, ncand ? ncand + b0 : nullptr, h->tau, h->sr, h->st, h->qscratch(),
-                      h->qcol<T>(), R, h->row0, r.hi - r.lo));
+                      h->wmin<T>(), h->qcol<T>(), R, h->row0, r.hi - r.lo));
     NK(h->comm->allreduce(dist + b0, (size_t)c, nccl_type<T>(), ncclSum, h->st));
     NK(h->comm->allreduce(lens + b0, (size_t)c, ncclInt32, ncclSum, h->st));
     if (ncand) NK(h->comm->allreduce(ncand + b0, (size_t)c, ncclInt32, ncclSum, h->st));
@@ -977,12 +1006,16 @@ apsp_status create_impl(apsp_handle** out, apsp_dtype dtype, int directed, int64
     CKR(cudaMemsetAsync(h->ws + h->plan.off_small, 0, 512, h->st));   // counters, flags
     CK(fill<T>(h->WT<T>(), (int64_t)cap * h->ld, Tr<T>::inf(), h->st));
     CKR(cudaMemsetAsync(&h->ctr()->err, 0, sizeof(unsigned), h->st));
-    CK(transpose_in<T>(reinterpret_cast<const T*>(W), ldw, n, h->WT<T>(), h->ld, &h->ctr()->err, h->st));
+    CKR(cudaMemsetAsync(h->wmin_dev(), 0xff, sizeof(unsigned), h->st));
+    CK(transpose_in<T>(reinterpret_cast<const T*>(W), ldw, n, h->WT<T>(), h->ld, &h->ctr()->err,
+                       h->wmin_dev(), h->st));
     CK(shortlist_build<T>(h->WT<T>(), h->ld, n, nullptr, 0, n, h->slid(), h->slw<T>(), h->wnext<T>(), h->st));
     unsigned* herr = reinterpret_cast<unsigned*>(h->host_small);
     CKR(cudaMemcpyAsync(herr, &h->ctr()->err, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+    CKR(cudaMemcpyAsync(herr + 1, h->wmin_dev(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
     CKR(cudaStreamSynchronize(h->st));
     if (*herr) return fail(h, APSP_E_INVAL, "create: W has %s", (*herr & 4) ? "a nonzero diagonal" : "a negative/NaN weight");
+    h->wmin_bits = herr[1];
     return APSP_OK;
   });
   if (s != APSP_OK) {

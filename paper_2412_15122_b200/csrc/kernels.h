@@ -36,10 +36,10 @@ struct Rows {
 
 template <typename T>
 cudaError_t validate_vec(const T* in, const T* in2, int64_t n, int64_t npad, T* out,
-                         unsigned int* err, cudaStream_t st);
+                         unsigned int* err, unsigned* wmin_bits, cudaStream_t st);
 template <typename T>
 cudaError_t transpose_in(const T* W, int64_t ldw, int64_t n, T* WT, int64_t ldt, unsigned int* err,
-                         cudaStream_t st);
+                         unsigned* wmin_bits, cudaStream_t st);
 template <typename T>
 cudaError_t fill(T* p, int64_t count, T v, cudaStream_t st);
 template <typename T>
@@ -160,7 +160,7 @@ template <typename T>
 cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int q,
                         const int* s, const int* t, T* dist, int* paths, int path_cap,
                         int* path_lens, int* ncand, float tau, int sr, cudaStream_t st,
-                        const QueryScratch& qs, const T* colbuf = nullptr, int64_t R = 0,
+                        const QueryScratch& qs, T wmin, const T* colbuf = nullptr, int64_t R = 0,
                         int64_t row0 = 0, int64_t rows = 0);
 // sharded queries: out[b * R + i] = D[row0 + i][t_b] (INF beyond the local rows)
 template <typename T>

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(QS_T) k_query_scan(const T* __restrict__ D, in
                                                      const int* __restrict__ Tq, int64_t chunk,
                                                      int* __restrict__ cand, T* __restrict__ cand_d,
                                                      int qcap, int* __restrict__ cnt, float tau,
-                                                     QShard<T> sh) {
+                                                     T wmin, QShard<T> sh) {
   const int b = blockIdx.y;
   const int s = S[b], t = Tq[b];
   if (s < 0 || s >= n || t < 0 || t >= n || s == t) return;
@@ -89,13 +89,26 @@ __global__ void __launch_bounds__(QS_T) k_query_scan(const T* __restrict__ D, in
   const int64_t k0 = (int64_t)blockIdx.x * chunk, k1 = min(n, k0 + chunk);
   int* out = cand + (int64_t)b * qcap;
   T* outd = cand_d + (int64_t)b * qcap;
+  // Column t is the expensive read (one sector per entry), so it is read only
+  // for k that can pass the test: D[k][t] >= 0, and for k != t a path of at
+  // least one edge, so D[k][t] >= wmin (the smallest edge weight present since
+  // creation).  Hence k needs D[s][k] <= D[s][t] - wmin (int32 shortest path;
+  // fp32: D[s][k] <= D[s][t](1+tau); minimax: D[s][k] <= D[s][t]).
+  T lim;
+  if (SR == 1) lim = st;
+  else if (Tr<T>::kFloat) lim = st * (1.0f + tau);
+  else lim = st - wmin;
   for (int64_t base = k0; base < k1; base += (int64_t)QS_T * QS_U) {
     T dsk[QS_U], dkt[QS_U];
 #pragma unroll
     for (int u = 0; u < QS_U; ++u) {
       const int64_t k = base + (int64_t)u * QS_T + threadIdx.x;
       dsk[u] = k < k1 ? Ds[k] : I;
-      dkt[u] = k < k1 ? ld_col<T>(D, ld, k, t, b, sh) : I;
+    }
+#pragma unroll
+    for (int u = 0; u < QS_U; ++u) {
+      const int64_t k = base + (int64_t)u * QS_T + threadIdx.x;
+      dkt[u] = (k < k1 && (dsk[u] <= lim || k == t)) ? ld_col<T>(D, ld, k, t, b, sh) : I;
     }
 #pragma unroll
     for (int u = 0; u < QS_U; ++u) {
@@ -338,7 +351,7 @@ template <typename T, int SR>
 cudaError_t query_launch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int q,
                          const int* s, const int* t, T* dist, int* paths, int path_cap,
                          int* path_lens, int* ncand, float tau, cudaStream_t st, QShard<T> sh,
-                         const QueryScratch& qs) {
+                         const QueryScratch& qs, T wmin) {
   cudaError_t e = cudaMemsetAsync(qs.cnt, 0, sizeof(int) * q, st);
   if (e != cudaSuccess) return e;
   // node chunks: >= 4 CTAs per SM over the whole grid, >= 1 step per CTA
@@ -350,7 +363,7 @@ cudaError_t query_launch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64
   nch = (n + chunk - 1) / chunk;
   T* cand_d = reinterpret_cast<T*>(qs.dsv);
   k_query_scan<T, SR><<<dim3((unsigned)nch, (unsigned)q), QS_T, 0, st>>>(
-      D, ld, n, s, t, chunk, qs.ids, cand_d, qs.qcap, qs.cnt, tau, sh);
+      D, ld, n, s, t, chunk, qs.ids, cand_d, qs.qcap, qs.cnt, tau, wmin, sh);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   QScratch<T> gs{qs.ids, cand_d, reinterpret_cast<T*>(qs.lab), qs.pred, qs.path, qs.done, qs.qcap};
@@ -364,7 +377,7 @@ template <typename T>
 cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int q,
                         const int* s, const int* t, T* dist, int* paths, int path_cap,
                         int* path_lens, int* ncand, float tau, int sr, cudaStream_t st,
-                        const QueryScratch& qs, const T* colbuf, int64_t R, int64_t row0,
+                        const QueryScratch& qs, T wmin, const T* colbuf, int64_t R, int64_t row0,
                         int64_t rows) {
   if (q <= 0) return cudaSuccess;
   if (colbuf && q > qs.batch) return cudaErrorInvalidValue;   // the host chunks sharded batches
@@ -374,9 +387,9 @@ cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_
     int* pb = path_cap > 0 ? paths + (int64_t)b0 * path_cap : paths;
     int* nc = ncand ? ncand + b0 : nullptr;
     cudaError_t e = sr ? query_launch<T, 1>(D, ld, WT, ldw, n, c, s + b0, t + b0, dist + b0, pb, path_cap,
-                                            path_lens + b0, nc, tau, st, sh, qs)
+                                            path_lens + b0, nc, tau, st, sh, qs, wmin)
                        : query_launch<T, 0>(D, ld, WT, ldw, n, c, s + b0, t + b0, dist + b0, pb, path_cap,
-                                            path_lens + b0, nc, tau, st, sh, qs);
+                                            path_lens + b0, nc, tau, st, sh, qs, wmin);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -385,7 +398,7 @@ cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_
 #define INST(T)                                                                                  \
   template cudaError_t query_batch<T>(const T*, int64_t, const T*, int64_t, int64_t, int,       \
                                       const int*, const int*, T*, int*, int, int*, int*, float,  \
-                                      int, cudaStream_t, const QueryScratch&, const T*, int64_t, \
+                                      int, cudaStream_t, const QueryScratch&, T, const T*, int64_t, \
                                       int64_t, int64_t);                                         \
   template cudaError_t query_colslice<T>(const T*, int64_t, int64_t, int64_t, int64_t,          \
                                          const int*, int, T*, cudaStream_t);

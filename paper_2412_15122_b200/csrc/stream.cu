@@ -50,11 +50,21 @@ static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // ---------------------------------------------------------------------------
 // validation / normalisation of caller vectors
 // ---------------------------------------------------------------------------
+// Smallest edge weight seen, as the bit pattern of a non-negative T (ordered
+// like the value for int32 and for IEEE floats >= 0): a lower bound of every
+// distance between distinct nodes, used to prune query candidates.
+template <typename T>
+__device__ __forceinline__ void wmin_fold(unsigned* wmin_bits, T v, bool valid) {
+  unsigned b = valid ? (Tr<T>::kFloat ? (unsigned)__float_as_int((float)v) : (unsigned)v) : ~0u;
+  b = __reduce_min_sync(0xffffffffu, b);
+  if ((threadIdx.x & 31) == 0 && b != ~0u) atomicMin(wmin_bits, b);
+}
+
 template <typename T>
 __global__ void k_validate_vec(const T* in, const T* in2, int64_t n, int64_t npad, T* out,
-                               unsigned int* err) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npad;
-       j += (int64_t)gridDim.x * blockDim.x) {
+                               unsigned int* err, unsigned* wmin_bits) {
+  for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < npad; j0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = j0 + threadIdx.x;
     T v = Tr<T>::inf();
     if (j < n) {
       T x = in[j];
@@ -70,21 +80,22 @@ __global__ void k_validate_vec(const T* in, const T* in2, int64_t n, int64_t npa
         if (!(y2 == v)) atomicOr(err, 2u);             // undirected asymmetry
       }
     }
-    out[j] = v;
+    if (wmin_bits) wmin_fold<T>(wmin_bits, v, j < n && v >= T(0) && Tr<T>::fin(v));
+    if (j < npad) out[j] = v;
   }
 }
 template <typename T>
 cudaError_t validate_vec(const T* in, const T* in2, int64_t n, int64_t npad, T* out,
-                         unsigned int* err, cudaStream_t st) {
+                         unsigned int* err, unsigned* wmin_bits, cudaStream_t st) {
   int grid = (int)std::min<int64_t>(cdiv(npad, 256), 4 * num_sms());
-  k_validate_vec<T><<<grid, 256, 0, st>>>(in, in2, n, npad, out, err);
+  k_validate_vec<T><<<grid, 256, 0, st>>>(in, in2, n, npad, out, err, wmin_bits);
   return cudaGetLastError();
 }
 
 // WT[j][i] = W[i][j] (32x32 smem tiles); checks W[i][i] == 0 and w >= 0.
 template <typename T>
 __global__ void k_transpose_in(const T* W, int64_t ldw, int64_t n, T* WT, int64_t ldt,
-                               unsigned int* err) {
+                               unsigned int* err, unsigned* wmin_bits) {
   __shared__ T tile[32][33];
   int64_t i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
@@ -96,6 +107,7 @@ __global__ void k_transpose_in(const T* W, int64_t ldw, int64_t n, T* WT, int64_
       if (!Tr<T>::kFloat && v > Tr<T>::inf()) v = Tr<T>::inf();
       if (i == j && v != T(0)) atomicOr(err, 4u);
     }
+    wmin_fold<T>(wmin_bits, v, i < n && j < n && i != j && v >= T(0) && Tr<T>::fin(v));
     tile[r][threadIdx.x] = v;
   }
   __syncthreads();
@@ -106,9 +118,9 @@ __global__ void k_transpose_in(const T* W, int64_t ldw, int64_t n, T* WT, int64_
 }
 template <typename T>
 cudaError_t transpose_in(const T* W, int64_t ldw, int64_t n, T* WT, int64_t ldt, unsigned int* err,
-                         cudaStream_t st) {
+                         unsigned* wmin_bits, cudaStream_t st) {
   dim3 grid((unsigned)cdiv(n, 32), (unsigned)cdiv(n, 32));
-  k_transpose_in<T><<<grid, dim3(32, 8), 0, st>>>(W, ldw, n, WT, ldt, err);
+  k_transpose_in<T><<<grid, dim3(32, 8), 0, st>>>(W, ldw, n, WT, ldt, err, wmin_bits);
   return cudaGetLastError();
 }
 
@@ -965,10 +977,10 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
 }
 
 #define INST(T)                                                                                   \
-  template cudaError_t validate_vec<T>(const T*, const T*, int64_t, int64_t, T*, unsigned int*,    \
+  template cudaError_t validate_vec<T>(const T*, const T*, int64_t, int64_t, T*, unsigned int*, unsigned*,    \
                                        cudaStream_t);                                             \
   template cudaError_t transpose_in<T>(const T*, int64_t, int64_t, T*, int64_t, unsigned int*,     \
-                                       cudaStream_t);                                             \
+                                       unsigned*, cudaStream_t);                                  \
   template cudaError_t fill<T>(T*, int64_t, T, cudaStream_t);                                      \
   template cudaError_t init_d<T>(T*, int64_t, Rows, int64_t, const T*, int64_t, cudaStream_t);     \
   template cudaError_t gather_col<T>(const T*, int64_t, Rows, int64_t, T, T*, int, cudaStream_t);  \

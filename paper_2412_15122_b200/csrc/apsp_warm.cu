@@ -399,129 +399,105 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
                       const T* r2, bool removal, apsp_update_info* info) {
   const int64_t n = h->n;
   Rows r = h->active();
+  const int64_t lcap = h->plan.lcap, ocap = h->plan.ocap;
   CKR(cudaMemsetAsync(h->rowcnt(), 0, sizeof(int) * h->cap, h->st));
   CKR(cudaMemsetAsync(h->ctr(), 0, sizeof(DetectCounters), h->st));
-  // one streaming pass appends the need_update_list; then per-row slices,
-  // Phi / max|A_i| and the D0 reset (W'[i][j]) of the listed pairs
   CKR(cudaMemsetAsync(h->ocnt(), 0, sizeof(int) * h->cap, h->st));   // scatter cursors
+  // one streaming pass appends the need_update_list; then per-row slices,
+  // Phi / max|A_i|, the row grouping and the D0 reset (W'[i][j])
   PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
      detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, 1, nullptr, h->rowcnt(),
-               h->srow(), h->scol(), h->slb<T>(), h->plan.lcap, h->ctr(), h->WT<T>(), h->ld, h->sr,
-               h->st));
+               h->srow(), h->scol(), h->slb<T>(), lcap, h->ctr(), h->WT<T>(), h->ld, h->sr, h->st));
   PK(APSP_K_EMIT, 0.0,
      detect_lists<T>(h->Dl<T>(), h->ld, r, h->WT<T>(), h->ld, h->rowcnt(), h->rowoff(), h->srow(),
-                     h->scol(), h->slb<T>(), h->ocnt(), h->prow(), h->pcol(), h->plb<T>(), h->plan.lcap,
+                     h->scol(), h->slb<T>(), h->ocnt(), h->prow(), h->pcol(), h->plb<T>(), lcap,
                      h->ctr(), h->st));
   if (removal) CK(tombstone<T>(h->Dl<T>(), h->ld, r, n, skip, h->WT<T>(), h->ld, h->st));
 
-  // counters -> host (|A|, Phi, max|A_i|, overflow), summed over ranks
-  unsigned long long* hs = reinterpret_cast<unsigned long long*>(h->host_small);
-  DetectCounters* hc = reinterpret_cast<DetectCounters*>(h->host_small);
-  CKR(cudaMemcpyAsync(h->host_small, h->ctr(), sizeof(DetectCounters), cudaMemcpyDeviceToHost, h->st));
-  CKR(cudaStreamSynchronize(h->st));
-  int64_t local_total = std::min<int64_t>((int64_t)hc->total, h->plan.lcap);
-  const bool local_overflow = hc->overflow != 0;
-  int64_t total = (int64_t)hc->total, rows = hc->rows, maxrow = hc->maxrow, overflow = hc->overflow;
-  if (h->world > 1) {
-    // [total, rows, overflow] summed, maxrow by max
-    long long* v = reinterpret_cast<long long*>(h->small());
-    long long hv[4] = {(long long)total, (long long)rows, (long long)overflow, (long long)maxrow};
-    CKR(cudaMemcpyAsync(v, hv, sizeof hv, cudaMemcpyHostToDevice, h->st));
-    NK(h->comm->allreduce(v, 3, ncclInt64, ncclSum, h->st));
-    NK(h->comm->allreduce(v + 3, 1, ncclInt64, ncclMax, h->st));
-    CKR(cudaMemcpyAsync(hs, v, sizeof hv, cudaMemcpyDeviceToHost, h->st));
-    CKR(cudaStreamSynchronize(h->st));
-    total = (int64_t)hs[0]; rows = (int64_t)hs[1]; overflow = (int64_t)hs[2]; maxrow = (int64_t)hs[3];
+  // ---- sparse recompute (a6), enqueued without a host round trip: the pair
+  // counts stay on the device, and the kernels do nothing if a list
+  // overflowed.  Every value they write is a walk length of G' (>= the new
+  // distance), so if the gate below picks the dense path after all, FW on
+  // the result is still exact.
+  const bool try_sparse = h->force_path != 2;
+  int in = 0, rounds = 0;
+  auto enqueue_rounds = [&](int batch) -> apsp_status {
+    for (int b = 0; b < batch; ++b, ++rounds) {
+      CKR(cudaMemsetAsync(h->chg(in ^ 1), 0, sizeof(int) * h->cap, h->st));
+      if (b == batch - 1) CKR(cudaMemsetAsync(h->anyflag(), 0, sizeof(int), h->st));
+      PK(APSP_K_SPARSE_R, 0.0,
+         sparse_round<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->gprow(), h->gpcol(),
+                         h->glb<T>(), ocap, h->rowoff(), h->ocnt(), h->ocol(), h->chg(in),
+                         h->chg(in ^ 1), h->anyflag(), h->sr, h->ctr(), h->st));
+      in ^= 1;
+    }
+    return APSP_OK;
+  };
+  if (try_sparse) {
+    CKR(cudaMemsetAsync(h->ocnt(), 0, sizeof(int) * h->cap, h->st));
+    // A: shortlist certification of every listed pair (ties reach lb)
+    PK(APSP_K_SPARSE0, 0.0,
+       sparse_phase_a<T>(h->Dl<T>(), h->ld, r, n, h->slid(), h->slw<T>(), h->wnext<T>(), h->rowoff(),
+                         h->rowcnt(), h->prow(), h->pcol(), h->plb<T>(), lcap, h->popen(), h->ocnt(),
+                         h->ocol(), h->gprow(), h->gpcol(), h->glb<T>(), h->gfull(), ocap, h->ctr(),
+                         h->sr, h->st));
+    // A2: whole-shortlist pass over the open pairs, now that certified values are final
+    CK(sparse_short<T>(h->Dl<T>(), h->ld, h->row0, h->slid(), h->slw<T>(), h->wnext<T>(), h->gprow(),
+                       h->gpcol(), h->glb<T>(), ocap, h->gfull(), 1, h->sr, h->ctr(), h->st));
+    // B: full O(n) scan for the pairs the shortlist could not settle
+    PK(APSP_K_SPARSE_R, 0.0,
+       sparse_full<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, n, h->gprow(), h->gpcol(),
+                      h->glb<T>(), h->gfull(), ocap, h->sr, h->ctr(), h->st));
+    // rounds over the open entries of each row, a first batch of 4
+    CKR(cudaMemsetAsync(h->chg(in), 1, sizeof(int) * h->cap, h->st));
+    apsp_status s = enqueue_rounds(std::min(4, h->max_rounds));
+    if (s != APSP_OK) return s;
   }
+
+  // ---- the one host read of this update: counters (summed over ranks) ----
+  long long* v = reinterpret_cast<long long*>(h->small());
+  CK(pack_counters(h->ctr(), h->anyflag(), v, h->st));   // total rows ovf1 ovf2 any | maxrow
+  if (h->world > 1) {
+    NK(h->comm->allreduce(v, 5, ncclInt64, ncclSum, h->st));
+    NK(h->comm->allreduce(v + 5, 1, ncclInt64, ncclMax, h->st));
+  }
+  long long* hv = reinterpret_cast<long long*>(h->host_small);
+  CKR(cudaMemcpyAsync(hv, v, 6 * sizeof(long long), cudaMemcpyDeviceToHost, h->st));
+  CKR(cudaStreamSynchronize(h->st));
+  const int64_t total = hv[0], rows = hv[1], maxrow = hv[5];
+  const bool overflow = hv[2] != 0 || hv[3] != 0;   // a list overflowed on some rank
+  bool changed = hv[4] != 0;
   if (info) {
     info->affected_pairs = total;
     info->affected_rows = rows;
     info->max_row_affected = maxrow;
     info->cost = removal ? (n > 1 ? (double)rows / (double)(n - 1) : 0.0) : (double)rows / (double)n;
   }
-  const double cost = info ? info->cost
-                            : (removal ? (n > 1 ? (double)rows / (double)(n - 1) : 0.0) : (double)rows / n);
+  const double cost = removal ? (n > 1 ? (double)rows / (double)(n - 1) : 0.0) : (double)rows / n;
   const bool gate = h->row_delta > 0 ? cost > h->row_delta   // paper: "Cost larger than delta"
                                      : (double)total > h->theta * (double)n * (double)n;
-  bool dense = h->force_path == 2 || (h->force_path == 0 && gate) || overflow != 0;
+  bool dense = h->force_path == 2 || (h->force_path == 0 && gate) || overflow;
+  // rounds until no entry changes (rarely more than the first batch)
+  while (!dense && changed && rounds < h->max_rounds) {
+    apsp_status s = enqueue_rounds(std::min(4, h->max_rounds - rounds));
+    if (s != APSP_OK) return s;
+    if (h->world > 1) NK(h->comm->allreduce(h->anyflag(), 1, ncclInt32, ncclMax, h->st));
+    int* hflag = reinterpret_cast<int*>(h->host_small);
+    CKR(cudaMemcpyAsync(hflag, h->anyflag(), sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    CKR(cudaStreamSynchronize(h->st));
+    changed = *hflag != 0;
+  }
+  if (info) info->rounds = rounds;
+  if (!dense && changed) dense = true;   // not converged: every entry is still a valid upper bound
   if (dense) {
     if (info) info->path = 3;
-    if (local_overflow)   // the list missed pairs: reset every flagged entry in place
+    if (hv[2] != 0)   // the need_update_list missed pairs: reset every flagged entry in place
       PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
          detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, 2, nullptr, nullptr, nullptr,
                    nullptr, nullptr, 0, nullptr, h->WT<T>(), h->ld, h->sr, h->st));
     return fw_impl<T>(h);
   }
   if (info) info->path = 2;
-  if (total == 0) return APSP_OK;
-  // ---- sparse recompute (a6) ----
-  // A: shortlist pass over every listed pair: certify ties (value == lb)
-  CKR(cudaMemsetAsync(h->ocnt(), 0, sizeof(int) * h->cap, h->st));
-  if (local_total > 0)
-    PK(APSP_K_SPARSE0, (double)local_total * kSL * 2.0 * sizeof(T),
-       sparse_phase_a<T>(h->Dl<T>(), h->ld, r, n, h->slid(), h->slw<T>(), h->wnext<T>(), h->rowoff(),
-                         h->rowcnt(), h->prow(), h->pcol(), h->plb<T>(), local_total, h->popen(),
-                         h->ocnt(), h->ocol(), h->gprow(), h->gpcol(), h->glb<T>(), h->gfull(),
-                         h->plan.ocap, h->ctr(), h->sr, h->st));
-  CKR(cudaMemcpyAsync(h->host_small, h->ctr(), sizeof(DetectCounters), cudaMemcpyDeviceToHost, h->st));
-  CKR(cudaStreamSynchronize(h->st));
-  int64_t nopen = (int64_t)hc->open_total;
-  int64_t ovf = (hc->overflow & 2u) ? 1 : 0;
-  if (h->world > 1) {
-    long long* v = reinterpret_cast<long long*>(h->small());
-    long long hv2[2] = {(long long)nopen, (long long)ovf};
-    CKR(cudaMemcpyAsync(v, hv2, sizeof hv2, cudaMemcpyHostToDevice, h->st));
-    NK(h->comm->allreduce(v, 2, ncclInt64, ncclSum, h->st));
-    CKR(cudaMemcpyAsync(hs, v, sizeof hv2, cudaMemcpyDeviceToHost, h->st));
-    CKR(cudaStreamSynchronize(h->st));
-    ovf = (int64_t)hs[1];
-  }
-  if (info) info->rounds = 0;
-  if (ovf) {
-    if (info) info->path = 3;
-    return fw_impl<T>(h);
-  }
-  if (nopen > 0) {
-    // A2: shortlist pass over the open pairs now that certified values are final
-    CK(sparse_short<T>(h->Dl<T>(), h->ld, h->row0, h->slid(), h->slw<T>(), h->wnext<T>(),
-                       h->gprow(), h->gpcol(), h->glb<T>(), nopen, h->gfull(), 1, h->sr, h->st));
-    // B: full O(n) scan for the pairs the shortlist could not settle
-    PK(APSP_K_SPARSE_R, 8.0 * (double)nopen * (double)n,
-       sparse_full<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, n, h->gprow(), h->gpcol(),
-                      h->glb<T>(), h->gfull(), nopen, h->sr, h->st));
-  }
-  // rounds over the open entries of each row until no entry changes
-  int in = 0;
-  CKR(cudaMemsetAsync(h->chg(in), 1, sizeof(int) * h->cap, h->st));
-  int rounds = 0;
-  bool converged = false;
-  int* hflag = reinterpret_cast<int*>(h->host_small);
-  // rounds are enqueued in batches of 4 between host convergence checks; a
-  // round after convergence only reads the (all-zero) row-change flags
-  while (!converged && rounds < h->max_rounds) {
-    const int batch = std::min(4, h->max_rounds - rounds);
-    for (int b = 0; b < batch; ++b, ++rounds) {
-      CKR(cudaMemsetAsync(h->chg(in ^ 1), 0, sizeof(int) * h->cap, h->st));
-      if (b == batch - 1) CKR(cudaMemsetAsync(h->anyflag(), 0, sizeof(int), h->st));
-      if (nopen > 0)
-        PK(APSP_K_SPARSE_R, 0.0,
-           sparse_round<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->gprow(), h->gpcol(),
-                           h->glb<T>(), nopen, h->rowoff(), h->ocnt(), h->ocol(), h->chg(in),
-                           h->chg(in ^ 1), h->anyflag(), h->sr, h->st));
-      in ^= 1;
-    }
-    if (h->world > 1)
-      NK(h->comm->allreduce(h->anyflag(), 1, ncclInt32, ncclMax, h->st));
-    CKR(cudaMemcpyAsync(hflag, h->anyflag(), sizeof(int), cudaMemcpyDeviceToHost, h->st));
-    CKR(cudaStreamSynchronize(h->st));
-    if (*hflag == 0) converged = true;   // the batch's last round changed nothing
-  }
-  if (info) info->rounds = rounds;
-  if (!converged) {
-    // still exact: every entry is a valid upper bound >= the true distance
-    if (info) info->path = 3;
-    return fw_impl<T>(h);
-  }
   return APSP_OK;
 }
 

@@ -119,7 +119,7 @@ cudaError_t shortlist_remove(int* SLid, T* SLw, T* wnext, int64_t n, int64_t k, 
 template <typename T>
 cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const T* SLw,
                          const T* wnext, const int* prow, const int* pcol, const T* plb,
-                         int64_t npairs, unsigned char* out, int classify, int sr, cudaStream_t st);
+                         int64_t npairs, unsigned char* out, int classify, int sr, const DetectCounters* dc, cudaStream_t st);
 template <typename T>
 cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, int64_t n, const int* SLid, const T* SLw,
                            const T* wnext, const int64_t* rowoff, const int* rowcnt,
@@ -135,12 +135,12 @@ cudaError_t sparse_compact(Rows r, const int64_t* rowoff, const int* rowcnt, con
 template <typename T>
 cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
                         const int* gprow, const int* gpcol, const T* glb, const unsigned char* gfull,
-                        int64_t nopen, int sr, cudaStream_t st);
+                        int64_t nopen, int sr, const DetectCounters* dc, cudaStream_t st);
 template <typename T>
 cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw,
                          const int* gprow, const int* gpcol, const T* glb, int64_t nopen,
                          const int64_t* rowoff, const int* ocnt, const int* ocol, const int* chg_in,
-                         int* chg_out, int* any, int sr, cudaStream_t st);
+                         int* chg_out, int* any, int sr, const DetectCounters* dc, cudaStream_t st);
 
 // ---------------- query.cu ----------------
 constexpr int kQueryCap = 4096;    // max |C| per query (min(kQueryCap, cap) per handle)
@@ -167,6 +167,7 @@ template <typename T>
 cudaError_t query_colslice(const T* D, int64_t ld, int64_t rows, int64_t R, int64_t n,
                            const int* t, int qc, T* out, cudaStream_t st);
 
+cudaError_t pack_counters(const DetectCounters* c, const int* any, long long* v, cudaStream_t st);
 int num_sms();
 
 }  // namespace apsp

@@ -351,6 +351,19 @@ cudaError_t shortlist_swap(int* SLid, T* SLw, T* wnext, int64_t n, int64_t p, in
 // of other pairs of the row are then visible, so a class-1 value is the
 // exact min of (*) over every m whose value can no longer change.
 // ---------------------------------------------------------------------------
+constexpr int kPhaseASteps = 3;   // phase A: at most 3 x 32 shortlist entries per pair
+
+// Pair counts live on the device (the host reads them once per update, after
+// the sparse recompute): which = 0, the need_update_list (nothing to do if it
+// overflowed: some flagged entries were never reset); 1, the open pairs
+// (nothing to do if either list overflowed — the dense path follows).
+__device__ __forceinline__ int64_t device_count(const DetectCounters* dc, int64_t cap, int which) {
+  if (!dc) return cap;
+  if (dc->overflow & (which ? 3u : 1u)) return 0;
+  const int64_t c = (int64_t)(which ? dc->open_total : dc->total);
+  return c < cap ? c : cap;
+}
+
 template <typename T, int SR>
 __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t row0,
                                                       const int* __restrict__ SLid,
@@ -360,9 +373,10 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
                                                       const int* __restrict__ pcol,
                                                       const T* __restrict__ plb, int64_t npairs,
                                                       unsigned char* out, int classify,
-                                                      OpenLists<T> ol) {
+                                                      OpenLists<T> ol, const DetectCounters* dc) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  npairs = device_count(dc, npairs, classify ? 1 : 0);
   for (int64_t p = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); p < npairs;
        p += nw) {
     const int64_t i = prow[p], j = pcol[p];
@@ -371,14 +385,19 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
     const T* sw = SLw + j * kSL;
     const T lbp = plb[p];
     T acc = Tr<T>::inf();
-    // lane lists are ascending, so the cheapest in-edges come first: in phase
-    // A stop as soon as the warp's bound reaches lb (the value is then final)
+    // lane lists are ascending, so the cheapest in-edges come first.  Phase A
+    // only certifies: it stops as soon as the warp's bound reaches lb (the
+    // value is then final), and after kPhaseASteps steps a pair that has not
+    // is left open — A2 evaluates the whole shortlist once the certified
+    // values are in place.  (A pair that certifies does so almost always in
+    // the first step; scanning all 512 entries for the ~1/3 of pairs that
+    // never do was ~90% of phase A's time.)
 #pragma unroll
     for (int q = 0; q < kSLK; ++q) {
       const int m = sid[q * 32 + lane];
       const T w = sw[q * 32 + lane];
       if (m >= 0) acc = Tr<T, SR>::relax(acc, *(volatile T*)(Drow + m), w);
-      if (!classify && (q == 0 || q == 2 || q == 6) && Tr<T>::at_lb(warp_min<T>(acc), lbp)) break;
+      if (!classify && (Tr<T>::at_lb(warp_min<T>(acc), lbp) || q == kPhaseASteps - 1)) break;
     }
     acc = warp_min<T>(acc);
     if (lane == 0) {
@@ -399,16 +418,17 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
 template <typename T>
 cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const T* SLw,
                          const T* wnext, const int* prow, const int* pcol, const T* plb,
-                         int64_t npairs, unsigned char* out, int classify, int sr, cudaStream_t st) {
+                         int64_t npairs, unsigned char* out, int classify, int sr,
+                         const DetectCounters* dc, cudaStream_t st) {
   if (npairs <= 0) return cudaSuccess;
   int grid = (int)std::min<int64_t>(cdiv(npairs, 8), (int64_t)num_sms() * 16);
   OpenLists<T> ol{};
   if (sr)
     k_sparse_short<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
-                                               out, classify, ol);
+                                               out, classify, ol, dc);
   else
     k_sparse_short<T, 0><<<grid, 256, 0, st>>>(D, ld, row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
-                                               out, classify, ol);
+                                               out, classify, ol, dc);
   return cudaGetLastError();
 }
 
@@ -426,10 +446,10 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, int64_t n, const int* SLid,
   int grid = (int)std::min<int64_t>(cdiv(npairs, 8), (int64_t)num_sms() * 16);
   if (sr)
     k_sparse_short<T, 1><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
-                                               out, 0, ol);
+                                               out, 0, ol, ctr);
   else
     k_sparse_short<T, 0><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
-                                               out, 0, ol);
+                                               out, 0, ol, ctr);
   return cudaGetLastError();
 }
 
@@ -506,10 +526,11 @@ __global__ void __launch_bounds__(256) k_sparse_full(T* D, int64_t ld, int64_t r
                                                      const int* __restrict__ gpcol,
                                                      const T* __restrict__ glb,
                                                      const unsigned char* __restrict__ gfull,
-                                                     int64_t nopen) {
+                                                     int64_t nopen, const DetectCounters* dc) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t n4 = (n + 3) / 4;
+  nopen = device_count(dc, nopen, 1);
   const T I = Tr<T>::inf();
   for (int64_t p = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); p < nopen;
        p += nw) {
@@ -547,13 +568,13 @@ __global__ void __launch_bounds__(256) k_sparse_full(T* D, int64_t ld, int64_t r
 template <typename T>
 cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
                         const int* gprow, const int* gpcol, const T* glb, const unsigned char* gfull,
-                        int64_t nopen, int sr, cudaStream_t st) {
+                        int64_t nopen, int sr, const DetectCounters* dc, cudaStream_t st) {
   if (nopen <= 0) return cudaSuccess;
   int grid = (int)std::min<int64_t>(cdiv(nopen, 8), (int64_t)num_sms() * 8);
   if (sr)
-    k_sparse_full<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, n, gprow, gpcol, glb, gfull, nopen);
+    k_sparse_full<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, n, gprow, gpcol, glb, gfull, nopen, dc);
   else
-    k_sparse_full<T, 0><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, n, gprow, gpcol, glb, gfull, nopen);
+    k_sparse_full<T, 0><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, n, gprow, gpcol, glb, gfull, nopen, dc);
   return cudaGetLastError();
 }
 
@@ -569,9 +590,11 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
                                                       const int64_t* __restrict__ rowoff,
                                                       const int* __restrict__ ocnt,
                                                       const int* __restrict__ ocol,
-                                                      const int* chg_in, int* chg_out, int* any) {
+                                                      const int* chg_in, int* chg_out, int* any,
+                                                      const DetectCounters* dc) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  nopen = device_count(dc, nopen, 1);
   for (int64_t p = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); p < nopen;
        p += nw) {
     const int64_t i = gprow[p];
@@ -602,15 +625,15 @@ template <typename T>
 cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw,
                          const int* gprow, const int* gpcol, const T* glb, int64_t nopen,
                          const int64_t* rowoff, const int* ocnt, const int* ocol, const int* chg_in,
-                         int* chg_out, int* any, int sr, cudaStream_t st) {
+                         int* chg_out, int* any, int sr, const DetectCounters* dc, cudaStream_t st) {
   if (nopen <= 0) return cudaSuccess;
   int grid = (int)std::min<int64_t>(cdiv(nopen, 8), (int64_t)num_sms() * 8);
   if (sr)
     k_sparse_round<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff,
-                                               ocnt, ocol, chg_in, chg_out, any);
+                                               ocnt, ocol, chg_in, chg_out, any, dc);
   else
     k_sparse_round<T, 0><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff,
-                                               ocnt, ocol, chg_in, chg_out, any);
+                                               ocnt, ocol, chg_in, chg_out, any, dc);
   return cudaGetLastError();
 }
 
@@ -626,7 +649,7 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
   template cudaError_t shortlist_remove<T>(int*, T*, T*, int64_t, int64_t, int64_t, cudaStream_t); \
   template cudaError_t sparse_short<T>(T*, int64_t, int64_t, const int*, const T*, const T*,       \
                                        const int*, const int*, const T*, int64_t, unsigned char*,  \
-                                       int, int, cudaStream_t);                                   \
+                                       int, int, const DetectCounters*, cudaStream_t);            \
   template cudaError_t sparse_phase_a<T>(T*, int64_t, Rows, int64_t, const int*, const T*,         \
                                          const T*, const int64_t*, const int*, const int*,         \
                                          const int*, const T*, int64_t, unsigned char*, int*, int*, \
@@ -637,10 +660,11 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
                                          unsigned char*, int64_t, DetectCounters*, cudaStream_t);  \
   template cudaError_t sparse_full<T>(T*, int64_t, int64_t, const T*, int64_t, int64_t,            \
                                       const int*, const int*, const T*, const unsigned char*,      \
-                                      int64_t, int, cudaStream_t);                                \
+                                      int64_t, int, const DetectCounters*, cudaStream_t);         \
   template cudaError_t sparse_round<T>(T*, int64_t, int64_t, const T*, int64_t, const int*,        \
                                        const int*, const T*, int64_t, const int64_t*, const int*,  \
-                                       const int*, const int*, int*, int*, int, cudaStream_t);
+                                       const int*, const int*, int*, int*, int,                    \
+                                       const DetectCounters*, cudaStream_t);
 INST(int32_t)
 INST(float)
 #undef INST

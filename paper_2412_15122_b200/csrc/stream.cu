@@ -916,6 +916,21 @@ cudaError_t set_edge(T* WT, int64_t ldw, int64_t u, int64_t v, T w, int directed
 // ---------------------------------------------------------------------------
 // helpers of the paper-faithful edge modification (remove + re-add + swap)
 // ---------------------------------------------------------------------------
+// The counters one update reports / gates on, as int64 for a sum/max all-reduce:
+// v = [|A|, Phi, list overflow, open-list overflow, rounds still changing | max|A_i|]
+__global__ void k_pack_counters(const DetectCounters* c, const int* any, long long* v) {
+  v[0] = (long long)c->total;
+  v[1] = (long long)c->rows;
+  v[2] = (c->overflow & 1u) ? 1 : 0;
+  v[3] = (c->overflow & 2u) ? 1 : 0;
+  v[4] = *any ? 1 : 0;
+  v[5] = (long long)c->maxrow;
+}
+cudaError_t pack_counters(const DetectCounters* c, const int* any, long long* v, cudaStream_t st) {
+  k_pack_counters<<<1, 1, 0, st>>>(c, any, v);
+  return cudaGetLastError();
+}
+
 __global__ void k_count_nonzero(const int* a, int64_t m, unsigned long long* out) {
   unsigned c = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;

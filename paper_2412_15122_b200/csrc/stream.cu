@@ -54,10 +54,18 @@ static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // like the value for int32 and for IEEE floats >= 0): a lower bound of every
 // distance between distinct nodes, used to prune query candidates.
 template <typename T>
-__device__ __forceinline__ void wmin_fold(unsigned* wmin_bits, T v, bool valid) {
-  unsigned b = valid ? (Tr<T>::kFloat ? (unsigned)__float_as_int((float)v) : (unsigned)v) : ~0u;
+__device__ __forceinline__ unsigned wmin_key(T v, bool valid) {
+  return valid ? (Tr<T>::kFloat ? (unsigned)__float_as_int((float)v) : (unsigned)v) : ~0u;
+}
+// warp-reduce, then one atomic per warp only if it would lower the current
+// value (after the first few warps almost none do: one hot address otherwise)
+__device__ __forceinline__ void wmin_fold_bits(unsigned* wmin_bits, unsigned b) {
   b = __reduce_min_sync(0xffffffffu, b);
-  if ((threadIdx.x & 31) == 0 && b != ~0u) atomicMin(wmin_bits, b);
+  if ((threadIdx.x & 31) == 0 && b != ~0u && b < *(volatile unsigned*)wmin_bits) atomicMin(wmin_bits, b);
+}
+template <typename T>
+__device__ __forceinline__ void wmin_fold(unsigned* wmin_bits, T v, bool valid) {
+  wmin_fold_bits(wmin_bits, wmin_key<T>(v, valid));
 }
 
 template <typename T>
@@ -98,6 +106,7 @@ __global__ void k_transpose_in(const T* W, int64_t ldw, int64_t n, T* WT, int64_
                                unsigned int* err, unsigned* wmin_bits) {
   __shared__ T tile[32][33];
   int64_t i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  unsigned wk = ~0u;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     int64_t i = i0 + r, j = j0 + threadIdx.x;
     T v = Tr<T>::inf();
@@ -107,9 +116,10 @@ __global__ void k_transpose_in(const T* W, int64_t ldw, int64_t n, T* WT, int64_
       if (!Tr<T>::kFloat && v > Tr<T>::inf()) v = Tr<T>::inf();
       if (i == j && v != T(0)) atomicOr(err, 4u);
     }
-    wmin_fold<T>(wmin_bits, v, i < n && j < n && i != j && v >= T(0) && Tr<T>::fin(v));
+    wk = min(wk, wmin_key<T>(v, i < n && j < n && i != j && v >= T(0) && Tr<T>::fin(v)));
     tile[r][threadIdx.x] = v;
   }
+  wmin_fold_bits(wmin_bits, wk);
   __syncthreads();
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     int64_t j = j0 + r, i = i0 + threadIdx.x;

@@ -367,6 +367,31 @@ def test_remove_line_metric_ties_dense(lib):
     assert_parity(getD(h), oracle.fw(hg.W))
 
 
+@pytest.mark.parametrize("force", [0, 1])
+def test_list_overflow_recovers_through_dense(lib, force):
+    """|A| ~ n^2/2 > the need_update_list capacity (max(cap^2/32, 2^20) pairs):
+    the detection pass cannot list every pair, so the flagged entries are reset
+    in place by a second pass (MODE 2) and blocked FW runs on D0 — also when
+    the sparse path is forced.  Directed removal and undirected increase (the
+    two-term detection)."""
+    n = 2048
+    x = np.arange(n) * 3
+    W = np.abs(x[:, None] - x[None, :]).astype(np.int32)
+    h = make(lib, W)
+    h.set_option(0, force)
+    _, info = h.remove_node(n // 2)
+    assert info.affected_pairs > (1 << 20) and info.path == 3
+    hg = synth.HostGraph(W, True)
+    hg.remove_node(n // 2)
+    assert_parity(getD(h), oracle.fw(hg.W))
+    hu = make(lib, W, directed=False)
+    hu.set_option(0, force)
+    p = n // 2
+    info = hu.update_edge(p, p + 1, 30)   # tight edge of the line: every crossing pair is flagged
+    assert info.affected_pairs > (1 << 20) and info.path == 3
+    assert_parity(getD(hu), oracle.fw(_edit(W, p, p + 1, 30, False)))
+
+
 def test_remove_cycle_closed_form(lib):
     n = 500
     W = np.full((n, n), INF, np.int32)

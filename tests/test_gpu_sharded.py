@@ -266,3 +266,11 @@ def assert_eq(G, O, dtype, what=""):
         assert np.array_equal(np.isfinite(G), fin), what
         rel = np.abs(G[fin].astype(np.float64) - O[fin]) / np.maximum(np.abs(O[fin]), 1e-300)
         assert rel.max(initial=0) <= 1e-5, f"{what}: max rel err {rel.max()}"
+
+
+def test_nccl_transport_loads(P):
+    """The production transport: libnccl is dlopen()ed and hands out an id
+    (a communicator needs one GPU per rank, so it is not created here)."""
+    a = P._lib.apsp_nccl_unique_id()
+    b = P._lib.apsp_nccl_unique_id()
+    assert len(a) == 128 and a != b

@@ -420,16 +420,23 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   // distance), so if the gate below picks the dense path after all, FW on
   // the result is still exact.
   const bool try_sparse = h->force_path != 2;
-  int in = 0, rounds = 0;
+  // Rounds are frontier-based Bellman-Ford over each row's open entries: round
+  // r relaxes every open pair of a row through the entries of that row that
+  // changed in round r-1 (round 0: all open entries).  Frontier lists live in
+  // the row slices of the (now free) staging list, counts in chg(0)/chg(1).
+  int rounds = 0;
+  int* fcol[2] = {h->srow(), h->scol()};
   auto enqueue_rounds = [&](int batch) -> apsp_status {
     for (int b = 0; b < batch; ++b, ++rounds) {
-      CKR(cudaMemsetAsync(h->chg(in ^ 1), 0, sizeof(int) * h->cap, h->st));
+      const int o = rounds & 1;
+      const int* fin_c = rounds == 0 ? h->ocnt() : h->chg(o ^ 1);
+      const int* fin_l = rounds == 0 ? h->ocol() : fcol[o ^ 1];
+      CKR(cudaMemsetAsync(h->chg(o), 0, sizeof(int) * h->cap, h->st));
       if (b == batch - 1) CKR(cudaMemsetAsync(h->anyflag(), 0, sizeof(int), h->st));
       PK(APSP_K_SPARSE_R, 0.0,
          sparse_round<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->gprow(), h->gpcol(),
-                         h->glb<T>(), ocap, h->rowoff(), h->ocnt(), h->ocol(), h->chg(in),
-                         h->chg(in ^ 1), h->anyflag(), h->sr, h->ctr(), h->st));
-      in ^= 1;
+                         h->glb<T>(), ocap, h->rowoff(), fin_c, fin_l, h->chg(o), fcol[o],
+                         h->anyflag(), h->sr, h->ctr(), h->st));
     }
     return APSP_OK;
   };
@@ -449,7 +456,6 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
        sparse_full<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, n, h->gprow(), h->gpcol(),
                       h->glb<T>(), h->gfull(), ocap, h->sr, h->ctr(), h->st));
     // rounds over the open entries of each row, a first batch of 4
-    CKR(cudaMemsetAsync(h->chg(in), 1, sizeof(int) * h->cap, h->st));
     apsp_status s = enqueue_rounds(std::min(4, h->max_rounds));
     if (s != APSP_OK) return s;
   }
@@ -477,9 +483,12 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   const bool gate = h->row_delta > 0 ? cost > h->row_delta   // paper: "Cost larger than delta"
                                      : (double)total > h->theta * (double)n * (double)n;
   bool dense = h->force_path == 2 || (h->force_path == 0 && gate) || overflow;
-  // rounds until no entry changes (rarely more than the first batch)
+  // rounds until no entry changes (rarely more than the first batch); later
+  // batches double (a round whose frontier is empty costs one small launch)
+  int batch = 4;
   while (!dense && changed && rounds < h->max_rounds) {
-    apsp_status s = enqueue_rounds(std::min(4, h->max_rounds - rounds));
+    batch *= 2;
+    apsp_status s = enqueue_rounds(std::min(batch, h->max_rounds - rounds));
     if (s != APSP_OK) return s;
     if (h->world > 1) NK(h->comm->allreduce(h->anyflag(), 1, ncclInt32, ncclMax, h->st));
     int* hflag = reinterpret_cast<int*>(h->host_small);

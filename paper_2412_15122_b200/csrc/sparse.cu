@@ -588,9 +588,9 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
                                                       const int* __restrict__ gpcol,
                                                       const T* __restrict__ glb, int64_t nopen,
                                                       const int64_t* __restrict__ rowoff,
-                                                      const int* __restrict__ ocnt,
-                                                      const int* __restrict__ ocol,
-                                                      const int* chg_in, int* chg_out, int* any,
+                                                      const int* __restrict__ fcnt_in,
+                                                      const int* __restrict__ fcol_in,
+                                                      int* fcnt_out, int* fcol_out, int* any,
                                                       const DetectCounters* dc) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -598,8 +598,8 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
   for (int64_t p = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); p < nopen;
        p += nw) {
     const int64_t i = gprow[p];
-    const int cnt = ocnt[i];
-    if (cnt <= 1 || !chg_in[i]) continue;   // a lone open entry cannot be improved by another
+    const int cnt = fcnt_in[i];
+    if (cnt == 0) continue;   // nothing in row i changed last round
     const int64_t j = gpcol[p];
     T* Drow = D + (i - row0) * ld;
     T cur = Tr<T>::inf();
@@ -610,13 +610,13 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
     const T* Wrow = WT + j * ldw;
     T acc = Tr<T>::inf();
     for (int t = lane; t < cnt; t += 32) {
-      const int64_t m = ocol[off + t];
+      const int64_t m = fcol_in[off + t];
       acc = Tr<T, SR>::relax(acc, *(volatile T*)(Drow + m), Wrow[m]);
     }
     acc = warp_min<T>(acc);
     if (lane == 0 && acc < cur) {
       Drow[j] = acc;
-      chg_out[i] = 1;
+      fcol_out[off + atomicAdd(fcnt_out + i, 1)] = (int)j;   // j changed: next round's frontier
       *any = 1;
     }
   }
@@ -624,16 +624,17 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
 template <typename T>
 cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw,
                          const int* gprow, const int* gpcol, const T* glb, int64_t nopen,
-                         const int64_t* rowoff, const int* ocnt, const int* ocol, const int* chg_in,
-                         int* chg_out, int* any, int sr, const DetectCounters* dc, cudaStream_t st) {
+                         const int64_t* rowoff, const int* fcnt_in, const int* fcol_in,
+                         int* fcnt_out, int* fcol_out, int* any, int sr, const DetectCounters* dc,
+                         cudaStream_t st) {
   if (nopen <= 0) return cudaSuccess;
   int grid = (int)std::min<int64_t>(cdiv(nopen, 8), (int64_t)num_sms() * 8);
   if (sr)
     k_sparse_round<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff,
-                                               ocnt, ocol, chg_in, chg_out, any, dc);
+                                               fcnt_in, fcol_in, fcnt_out, fcol_out, any, dc);
   else
     k_sparse_round<T, 0><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff,
-                                               ocnt, ocol, chg_in, chg_out, any, dc);
+                                               fcnt_in, fcol_in, fcnt_out, fcol_out, any, dc);
   return cudaGetLastError();
 }
 
@@ -663,7 +664,7 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
                                       int64_t, int, const DetectCounters*, cudaStream_t);         \
   template cudaError_t sparse_round<T>(T*, int64_t, int64_t, const T*, int64_t, const int*,        \
                                        const int*, const T*, int64_t, const int64_t*, const int*,  \
-                                       const int*, const int*, int*, int*, int,                    \
+                                       const int*, int*, int*, int*, int,                          \
                                        const DetectCounters*, cudaStream_t);
 INST(int32_t)
 INST(float)

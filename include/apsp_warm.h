@@ -34,8 +34,9 @@
  *   All device work is enqueued on the handle's stream (a cudaStream_t passed
  *   as void*).  Calls that need a host decision synchronise that stream:
  *   add_node (argument validation flag, 4 B), update_edge (the 8-byte read of
- *   W[u][v], D[u][v]), remove_node and edge increases (|A|, Phi, max|A_i| for
- *   the gate, and one 4-byte flag per sparse round), sp_pair_query (result).
+ *   W[u][v], D[u][v]), remove_node and edge increases (one read of |A|, Phi,
+ *   max|A_i| and the round flag after the sparse recompute was enqueued, plus
+ *   one 4-byte flag per further batch of rounds), sp_pair_query (result).
  *   cold_fw and update_edge decreases after the early-exit test are
  *   asynchronous.  One handle per stream; handles are not thread-safe.
  *
@@ -282,6 +283,17 @@ apsp_status apsp_profile_enable(apsp_handle* h, int on);
 apsp_status apsp_profile_reset(apsp_handle* h);
 apsp_status apsp_profile_read(apsp_handle* h, int kernel_class, double* ms, int64_t* launches,
                               double* work);
+
+/* Roofline denominators measured on the current device:
+ *   kind 0: int32 relaxations/s (d = min(d, a + b), one VIADDMNMX each)
+ *   kind 1: fp32 relaxations/s (FADD, FADD, FMNMX3 per two)
+ *   kind 2: int16x2 relaxations/s (VIADDMNMX.S16x2; reference only)
+ *   kind 3: HBM read bytes/s over buf[0, bytes) (device; >= 1 GiB to exceed L2)
+ *   kind 4: HBM read+write bytes/s, buf updated in place (contents destroyed)
+ * buf: device memory (kinds 0-2 only need 4 bytes, never written).  Best of 5
+ * launches after 2 warm-ups, CUDA events on `stream`; synchronises it.
+ * Errors: E_INVAL (bad kind, null buf/rate), E_CUDA. */
+apsp_status apsp_microbench(int kind, void* buf, size_t bytes, void* stream, double* rate);
 
 #ifdef __cplusplus
 }

@@ -28,7 +28,7 @@ SYMBOLS = [
     "sp_pair_query_batch", "apsp_size", "apsp_last_error", "apsp_status_string",
     "apsp_nccl_unique_id", "apsp_kernel_launches", "apsp_profile_enable", "apsp_profile_reset",
     "apsp_profile_read", "apsp_modify_edge_readd", "apsp_get_weight",
-    "apsp_local_group_create", "apsp_local_group_destroy", "apsp_create_local",
+    "apsp_local_group_create", "apsp_local_group_destroy", "apsp_create_local", "apsp_microbench",
 ]
 # kernel classes of apsp_profile_read (apsp_kernel_class)
 K_CLASSES = ["fw_diag", "fw_panel", "fw_tile", "add_pass1", "rank1", "detect", "sparse0",
@@ -70,6 +70,7 @@ def _load():
         "apsp_local_group_destroy": (ctypes.c_int, [vp]),
         "apsp_create_local": (ctypes.c_int, [P(vp), ctypes.c_int, ctypes.c_int, i64, i64, vp, i64, vp, i64,
                                              vp, ctypes.c_size_t, vp, ctypes.c_int, vp]),
+        "apsp_microbench": (ctypes.c_int, [ctypes.c_int, vp, ctypes.c_size_t, vp, P(dbl)]),
         "apsp_destroy": (ctypes.c_int, [vp]),
         "apsp_set_option": (ctypes.c_int, [vp, ctypes.c_int, dbl]),
         "apsp_cold_fw": (ctypes.c_int, [vp]),
@@ -144,6 +145,14 @@ def apsp_create_local(dtype, directed, n, cap, W_ptr, ldw, D_ptr, ld, ws_ptr, ws
     check(None, lib.apsp_create_local(ctypes.byref(h), dtype, int(directed), n, cap, W_ptr, ldw, D_ptr, ld,
                                       ws_ptr, ws_bytes, stream, rank, group))
     return h
+
+
+def apsp_microbench(kind, buf_ptr, nbytes, stream):
+    """K13 roofline denominators (apsp_warm.h): 0 int32 / 1 fp32 / 2 int16x2
+    relaxations per second, 3 HBM read / 4 read+write bytes per second."""
+    r = ctypes.c_double()
+    check(None, lib.apsp_microbench(kind, buf_ptr, nbytes, stream, ctypes.byref(r)))
+    return r.value
 
 
 def apsp_destroy(h):

@@ -1186,6 +1186,14 @@ const char* apsp_last_error(const apsp_handle* h) { return h ? h->err.c_str() : 
 
 int64_t apsp_kernel_launches(const apsp_handle* h) { return h ? h->launches : -1; }
 
+apsp_status apsp_microbench(int kind, void* buf, size_t bytes, void* stream, double* rate) {
+  if (!rate || kind < 0 || kind > 4) return APSP_E_INVAL;
+  const double r = microbench(kind, buf, bytes, reinterpret_cast<cudaStream_t>(stream));
+  if (r < 0) return r == -1.0 ? APSP_E_INVAL : APSP_E_CUDA;
+  *rate = r;
+  return APSP_OK;
+}
+
 apsp_status apsp_profile_enable(apsp_handle* h, int on) {
   CHECK_HANDLE(h);
   h->prof_on = on != 0;

@@ -169,6 +169,7 @@ cudaError_t query_colslice(const T* D, int64_t ld, int64_t rows, int64_t R, int6
                            const int* t, int qc, T* out, cudaStream_t st);
 
 cudaError_t pack_counters(const DetectCounters* c, const int* any, long long* v, cudaStream_t st);
+double microbench(int kind, void* buf, size_t bytes, cudaStream_t st);   // microbench.cu
 int num_sms();
 
 }  // namespace apsp

@@ -643,3 +643,22 @@ def test_row_delta_gate_paper_definition1(lib, rng):
         Da = getD(a)
         assert np.array_equal(Da, getD(b))
         assert_parity(Da, oracle.fw(hg.W))
+
+
+def test_microbench_denominators(lib):
+    """K13: the measured relaxation and HBM rates are in the
+    range the B200 can deliver (one VIADDMNMX per int32 relaxation: 64/clk/SM
+    at <= 1.965 GHz on 148 SMs; HBM3e <= 8 TB/s)."""
+    L = lib._lib
+    buf = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    r32 = L.apsp_microbench(0, buf.data_ptr(), 4, st)
+    f32 = L.apsp_microbench(1, buf.data_ptr(), 4, st)
+    s16 = L.apsp_microbench(2, buf.data_ptr(), 4, st)
+    rd = L.apsp_microbench(3, buf.data_ptr(), buf.numel(), st)
+    rmw = L.apsp_microbench(4, buf.data_ptr(), buf.numel(), st)
+    assert 5e12 < r32 <= 148 * 64 * 1.97e9 * 1.02
+    assert f32 > 5e12 and s16 > r32
+    assert 2e12 < rd < 8.5e12 and 2e12 < rmw < 8.5e12
+    with pytest.raises(lib._lib.ApspError):
+        L.apsp_microbench(9, buf.data_ptr(), 4, st)

@@ -91,13 +91,19 @@ typedef enum {
   APSP_OPT_ROW_DELTA = 4,   /* > 0: use the paper's own gate instead — dense FW iff
                                Definition 1's cost Phi/(N-1) > delta;
                                0 (default): the pair-level gate of APSP_OPT_THETA    */
-  APSP_OPT_SEMIRING = 5     /* path algebra: 0 (default) shortest path, D = min over
+  APSP_OPT_SEMIRING = 5,    /* path algebra: 0 (default) shortest path, D = min over
                                paths of the summed weights; 1 minimax / bottleneck
                                path, D = min over paths of the largest weight (PAPER.md
                                §6: "The algorithms can be revised to solve
                                the all pairs minimax path problem").  Every call then
                                uses that algebra; D is NOT converted: set it before
                                apsp_cold_fw (or fill D with the matching matrix).    */
+  APSP_OPT_FW16 = 6         /* 1 (default): blocked FW on int32 shortest-path handles
+                               on one GPU runs on a packed int16x2 copy of D (two
+                               relaxations per VIADDMNMX.S16x2), exact for every
+                               distance < 0x3FFF; if any entry saturates it finishes
+                               in int32 — results are identical either way.
+                               0: always int32.                                       */
 } apsp_option;
 
 /* Statistics of one update. */

@@ -19,7 +19,7 @@ STATUS = {
     0: "APSP_OK", 1: "APSP_E_INVAL", 2: "APSP_E_RANGE", 3: "APSP_E_CAPACITY", 4: "APSP_E_PRECOND",
     5: "APSP_E_CUDA", 6: "APSP_E_NCCL", 7: "APSP_E_NOMEM", 8: "APSP_E_POISONED", 9: "APSP_E_UNSUPPORTED",
 }
-OPT_FORCE_PATH, OPT_THETA, OPT_TAU, OPT_MAX_ROUNDS, OPT_ROW_DELTA, OPT_SEMIRING = 0, 1, 2, 3, 4, 5
+OPT_FORCE_PATH, OPT_THETA, OPT_TAU, OPT_MAX_ROUNDS, OPT_ROW_DELTA, OPT_SEMIRING, OPT_FW16 = 0, 1, 2, 3, 4, 5, 6
 
 # exported symbols (tests check the library exports every one of them)
 SYMBOLS = [

@@ -41,7 +41,8 @@ struct Plan {
   size_t off_wt, off_vec, off_rowpart, off_colpart, off_rowoff, off_rowcnt, off_chg, off_prow,
       off_pcol, off_plb, off_popen, off_ocol, off_ocnt, off_gprow, off_gpcol, off_glb, off_gfull,
       off_srow, off_scol, off_slb, off_slid, off_slw, off_wnext, off_panel, off_pt, off_anyrow, off_qsend, off_qcol,
-      off_qids, off_qdsv, off_qlab, off_qpred, off_qpath, off_qdone, off_qcnt, off_small, total;
+      off_qids, off_qdsv, off_qlab, off_qpred, off_qpath, off_qdone, off_qcnt, off_p16, off_ptd, off_small,
+      total;
   int qcap, qbatch;
   int64_t ldpt;
 };
@@ -103,6 +104,10 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   p.off_qpath = take(4 * qe);
   p.off_qdone = take(qe);
   p.off_qcnt = take(sizeof(int32_t) * (size_t)p.qbatch);
+  // int16x2 FW (one GPU): packed copy of D (two columns per word) + the
+  // transposed diagonal tile
+  p.off_p16 = take(world == 1 ? sizeof(uint16_t) * (size_t)cap * p.ld : 256);
+  p.off_ptd = take(sizeof(uint32_t) * (size_t)kTile * kTile);
   p.off_small = take(64 * 1024);
   p.total = o;
   return p;
@@ -137,6 +142,8 @@ struct apsp_handle {
   double theta = 0.02;
   float tau = 1e-5f;
   int max_rounds = 64;
+  int fw16 = 1;                  // int16x2 FW when exact (int32 shortest path, one GPU)
+  int last_fw16 = 0;             // 1: the last FW ran packed, 2: it fell back to int32
   double row_delta = 0.0;        // > 0: the paper's Definition-1 gate (ablation)
   int sr = 0;                    // path algebra: 0 shortest path, 1 minimax
   // state
@@ -231,6 +238,9 @@ struct apsp_handle {
   unsigned long long* rank1_bytes() {   // device counter of bytes the rank-1 kernel read
     return reinterpret_cast<unsigned long long*>(ws + plan.off_small + 320);
   }
+  unsigned* fw16_flag() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 392); }
+  uint32_t* p16() { return reinterpret_cast<uint32_t*>(ws + plan.off_p16); }
+  uint32_t* ptd() { return reinterpret_cast<uint32_t*>(ws + plan.off_ptd); }
   unsigned* wmin_dev() {   // accumulator of the smallest edge weight (bits of a T >= 0)
     return reinterpret_cast<unsigned*>(ws + plan.off_small + 384);
   }
@@ -352,7 +362,32 @@ apsp_status snap_row(apsp_handle* h, int64_t gi, T add, T* out) {
 // ------------------------------------------------------------------ cold FW
 // Blocked FW over the current D (the dense fallback a7 runs it on D0).
 template <typename T>
+apsp_status fw_impl_elem(apsp_handle* h);
+
+// Blocked FW: the int16x2 path first where it is exact, the element-type
+// path otherwise (and whenever an entry saturated).
+template <typename T>
 apsp_status fw_impl(apsp_handle* h) {
+  if constexpr (std::is_same<T, int32_t>::value) {
+    if (h->fw16 && h->sr == 0 && h->world == 1) {
+      const int64_t n = h->n;
+      PK(APSP_K_FW_TILE, (double)n * n * n,
+         fw16(h->Dl<int32_t>(), h->ld, h->active().hi - h->active().lo, n, h->p16(),
+              h->pt<uint32_t>(), h->plan.ldpt, h->ptd(), h->fw16_flag(), h->st));
+      unsigned* hf = reinterpret_cast<unsigned*>(h->host_small);
+      CKR(cudaMemcpyAsync(hf, h->fw16_flag(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+      CKR(cudaStreamSynchronize(h->st));
+      h->last_fw16 = *hf ? 2 : 1;
+      if (!*hf) return APSP_OK;
+      // some distance is >= 0x3FFF or infinite: finish in int32 (exact from any
+      // matrix of walk lengths, which D still is)
+    }
+  }
+  return fw_impl_elem<T>(h);
+}
+
+template <typename T>
+apsp_status fw_impl_elem(apsp_handle* h) {
   const int64_t n = h->n, ld = h->ld;
   Rows r = h->active();
   const int64_t m = r.hi - r.lo;   // local active rows (local row 0 = global row0)
@@ -1079,6 +1114,10 @@ apsp_status apsp_set_option(apsp_handle* h, apsp_option opt, double value) {
     case APSP_OPT_SEMIRING:
       if (value != 0 && value != 1) return APSP_E_INVAL;
       h->sr = (int)value;
+      return APSP_OK;
+    case APSP_OPT_FW16:
+      if (value != 0 && value != 1) return APSP_E_INVAL;
+      h->fw16 = (int)value;
       return APSP_OK;
     case APSP_OPT_ROW_DELTA:
       if (!(value >= 0) || value > 1) return APSP_E_INVAL;

@@ -8,6 +8,13 @@
 
 #define APSP_INF_I32_DEV 0x3FFFFFFF
 
+// return a CUDA error from a host launcher
+#define CUDA_TRY(x)                           \
+  do {                                        \
+    cudaError_t _e = (x);                     \
+    if (_e != cudaSuccess) return _e;         \
+  } while (0)
+
 namespace apsp {
 
 // ---------------------------------------------------------------------------
@@ -65,6 +72,19 @@ template <> struct Tr<float, 0> {
   // within 2^-21 relative of the lower bound: the true value lies in [lb, v],
   // so stopping here errs by <= 5e-7 relative (fp32 bar 1e-5)
   __device__ static __forceinline__ bool at_lb(float v, float lb) { return v <= lb + lb * 0x1p-21f; }
+};
+
+// Packed pair of int16 distances (two adjacent columns per 32-bit word), the
+// element of the int16x2 Floyd–Warshall (fw.cu): INF = 0x3FFF in each half, so
+// a sum of two stored halves is <= 32766 (no overflow) and
+// __viaddmin_s16x2 = VIADDMNMX.S16x2 relaxes both columns in one instruction.
+template <> struct Tr<uint32_t, 0> {
+  using V4 = uint4;
+  static constexpr bool kFloat = false;
+  __host__ __device__ static __forceinline__ uint32_t inf() { return 0x3FFF3FFFu; }
+  __device__ static __forceinline__ uint32_t relax(uint32_t d, uint32_t a, uint32_t b) {
+    return __viaddmin_s16x2(a, b, d);
+  }
 };
 
 // minimax: a path's cost is its largest edge; max is exact in int32 and fp32

@@ -483,6 +483,178 @@ cudaError_t fw_rest_pt(T* D, int64_t ld, int64_t m, int64_t ncols, int64_t K0, i
   return cudaGetLastError();
 }
 
+// ===========================================================================
+// int16x2 blocked FW (int32 API, shortest path, one GPU).
+//
+// The int32 relaxation is one VIADDMNMX per pair; VIADDMNMX.S16x2 relaxes two
+// int16 pairs per instruction (K13: 2x the int32 rate).  The FW runs on a
+// packed copy P of D (two columns per word) with every value saturated at
+// SAT = 0x3FFF: stored values stay <= SAT (each update is a min with the old
+// value) and a sum of two is <= 32766, so nothing overflows.  Every entry whose
+// true distance is < SAT comes out exact (an induction over the pivots: the
+// shortest restricted path's sub-paths are shorter, hence exact; any candidate
+// through a saturated value is >= SAT); every other entry comes out == SAT.
+// Back-conversion writes the exact entries and raises a flag on any SAT, and
+// the caller then re-runs the int32 FW on D (whose unconverted entries are
+// still walk lengths, so the result is exact either way).
+//
+// Per pivot block K the same three phases as above, all on packed words:
+//   (1) closure of the diagonal tile (one CTA, packed in shared memory);
+//   (2) row panel D[K][*] := D_KK (x) D[K][*], column panel D[*][K] :=
+//       D[*][K] (x) D_KK — fw_tile3_kernel<uint32_t> with A = a transposed,
+//       half-replicated copy (PT[k][i] = D[i][k] in both halves);
+//   (3) D[I][J] := min(D[I][J], D[I][K] (x) D[K][J]) — fw_tile3_kernel<uint32_t>
+//       on 128-row x 256-column tiles (128 words).
+// Recomputing the K tiles inside (2)/(3) is harmless: D_KK is closed.
+// ===========================================================================
+constexpr uint32_t kSat16 = 0x3FFFu;
+__device__ __forceinline__ uint32_t half16(uint32_t w, int hi) { return hi ? (w >> 16) : (w & 0xFFFFu); }
+__device__ __forceinline__ uint32_t rep16(uint32_t v) { return v | (v << 16); }
+
+// P[i][w] = (sat(D[i][2w]), sat(D[i][2w+1])), columns >= n saturated
+__global__ void k_d32_to_p16(const int32_t* __restrict__ D, int64_t ld, int64_t m, int64_t n,
+                             uint32_t* __restrict__ P, int64_t ldw) {
+  const int64_t tot = m * ldw;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / ldw, w = e - i * ldw, j = 2 * w;
+    const uint32_t lo = j < n ? (uint32_t)min(D[i * ld + j], (int32_t)kSat16) : kSat16;
+    const uint32_t hi = j + 1 < n ? (uint32_t)min(D[i * ld + j + 1], (int32_t)kSat16) : kSat16;
+    P[e] = lo | (hi << 16);
+  }
+}
+
+// D[i][j] := P value where it is < SAT; flag any saturated off-diagonal entry
+__global__ void k_p16_to_d32(const uint32_t* __restrict__ P, int64_t ldw, int64_t m, int64_t n,
+                             int64_t row0, int32_t* __restrict__ D, int64_t ld, unsigned* flag) {
+  const int64_t tot = m * n;
+  unsigned f = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    const uint32_t v = half16(P[i * ldw + (j >> 1)], (int)(j & 1));
+    if (v < kSat16) D[i * ld + j] = (int32_t)v;
+    else f = 1;
+  }
+  if (__any_sync(0xffffffffu, f) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
+// closure of the kb x kb diagonal tile at P (word pointer of its top-left)
+__global__ void __launch_bounds__(1024) k_p16_diag(uint32_t* __restrict__ P, int64_t ldw, int kb) {
+  __shared__ uint32_t s[TB][TB / 2];
+  for (int e = threadIdx.x; e < TB * TB / 2; e += blockDim.x) {
+    const int i = e / (TB / 2), w = e % (TB / 2);
+    uint32_t v = rep16(kSat16);
+    if (i < kb) {
+      const uint32_t x = P[(int64_t)i * ldw + w];
+      const uint32_t lo = 2 * w < kb ? (x & 0xFFFFu) : kSat16;
+      const uint32_t hi = 2 * w + 1 < kb ? (x >> 16) : kSat16;
+      v = lo | (hi << 16);
+    }
+    s[i][w] = v;
+  }
+  __syncthreads();
+  // row k and column k do not change at pivot k (D[k][k] = 0): in place
+  for (int k = 0; k < kb; ++k) {
+    for (int e = threadIdx.x; e < TB * TB / 2; e += blockDim.x) {
+      const int i = e / (TB / 2), w = e % (TB / 2);
+      s[i][w] = __viaddmin_s16x2(rep16(half16(s[i][k >> 1], k & 1)), s[k][w], s[i][w]);
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < TB * TB / 2; e += blockDim.x) {
+    const int i = e / (TB / 2), w = e % (TB / 2);
+    if (i < kb && 2 * w < kb) {
+      uint32_t v = s[i][w];
+      if (2 * w + 1 >= kb) v = (v & 0xFFFFu) | (P[(int64_t)i * ldw + w] & 0xFFFF0000u);   // keep the neighbour column
+      P[(int64_t)i * ldw + w] = v;
+    }
+  }
+}
+
+// PT[k][i] = rep(D[i][K0 + k]) for k < kb, i < m; rep(SAT) elsewhere (i < mpad, k < TB)
+__global__ void k_p16_transpose_rep(const uint32_t* __restrict__ P, int64_t ldw, int64_t m, int64_t K0,
+                                    int kb, uint32_t* __restrict__ PT, int64_t ldpt, int64_t mpad) {
+  __shared__ uint32_t tile[32][33];
+  const int64_t i0 = blockIdx.x * 32;
+  const int k0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = i0 + r;
+    const int k = k0 + threadIdx.x;
+    uint32_t v = kSat16;
+    if (i < m && k < kb) {
+      const int64_t c = K0 + k;
+      v = half16(P[i * ldw + (c >> 1)], (int)(c & 1));
+    }
+    tile[r][threadIdx.x] = rep16(v);
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int k = k0 + r;
+    const int64_t i = i0 + threadIdx.x;
+    if (i < mpad) PT[(int64_t)k * ldpt + i] = tile[threadIdx.x][r];
+  }
+}
+
+static cudaError_t tile3_p16(uint32_t* C, int64_t ldc, const uint32_t* PT, int64_t ldpt, const uint32_t* B,
+                             int64_t ldb, int64_t m, int64_t ncols, int kdepth, int skip_ti, cudaStream_t st) {
+  static bool configured = false;
+  constexpr size_t smem = sizeof(uint32_t) * 4 * KC * TB;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fw_tile3_kernel<uint32_t, 0>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (m <= 0 || ncols <= 0) return cudaSuccess;
+  Tile3Args a;
+  a.C = C; a.ldc = ldc;
+  a.PT = PT; a.ldpt = ldpt;
+  a.B = B; a.ldb = ldb;
+  a.m = (int)m; a.ncols = (int)ncols; a.kdepth = kdepth;
+  a.skip_ti = skip_ti; a.skip_tj = -1;
+  const int64_t mpad = (m + TB - 1) / TB * TB;
+  dim3 grid((unsigned)((ncols + TB - 1) / TB), (unsigned)(mpad / TB));
+  fw_tile3_kernel<uint32_t, 0><<<grid, NTH, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t fw16(int32_t* D, int64_t ld, int64_t m, int64_t n, uint32_t* P, uint32_t* PT, int64_t ldpt,
+                 uint32_t* PTd, unsigned* flag, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return cudaSuccess;
+  const int64_t ldw = ld / 2;                 // words per packed row
+  const int64_t nw = (n + 1) / 2;             // words holding columns [0, n)
+  const int64_t mpad = (m + TB - 1) / TB * TB;
+  if (mpad > ldpt || (ld & 1)) return cudaErrorInvalidValue;
+  const int g = num_sms() * 8;
+  k_d32_to_p16<<<g, 256, 0, st>>>(D, ld, m, n, P, ldw);
+  CUDA_TRY(cudaGetLastError());
+  for (int64_t K0 = 0; K0 < n; K0 += TB) {
+    const int kb = (int)std::min<int64_t>(TB, n - K0);
+    uint32_t* rowK = P + K0 * ldw;
+    // (1) diagonal tile
+    k_p16_diag<<<1, 1024, 0, st>>>(rowK + K0 / 2, ldw, kb);
+    CUDA_TRY(cudaGetLastError());
+    // (2) row panel with A = the closed tile, column panel with A = its old values
+    k_p16_transpose_rep<<<dim3(TB / 32, TB / 32), dim3(32, 8), 0, st>>>(rowK, ldw, kb, K0, kb, PTd, TB, TB);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(tile3_p16(rowK, ldw, PTd, TB, rowK, ldw, kb, nw, kb, -1, st));
+    k_p16_transpose_rep<<<dim3((unsigned)(mpad / 32), TB / 32), dim3(32, 8), 0, st>>>(P, ldw, m, K0, kb, PT,
+                                                                                      ldpt, mpad);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(tile3_p16(P + K0 / 2, ldw, PT, ldpt, rowK + K0 / 2, ldw, m, (kb + 1) / 2, kb,
+                       (int)(K0 / TB), st));
+    // (3) the rest, A = the updated column panel
+    k_p16_transpose_rep<<<dim3((unsigned)(mpad / 32), TB / 32), dim3(32, 8), 0, st>>>(P, ldw, m, K0, kb, PT,
+                                                                                      ldpt, mpad);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(tile3_p16(P, ldw, PT, ldpt, rowK, ldw, m, nw, kb, (int)(K0 / TB), st));
+  }
+  CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(unsigned), st));
+  k_p16_to_d32<<<g, 256, 0, st>>>(P, ldw, m, n, 0, D, ld, flag);
+  return cudaGetLastError();
+}
+
 #define INST(T)                                                                                  \
   template cudaError_t fw_diag<T>(T*, int64_t, int, int, cudaStream_t);                          \
   template cudaError_t fw_row_panel<T>(T*, int64_t, int64_t, int, int64_t, int, cudaStream_t);   \

@@ -28,6 +28,13 @@ template <typename T>
 cudaError_t fw_rest_pt(T* D, int64_t ld, int64_t m, int64_t ncols, int64_t K0, int kb, const T* P,
                        int64_t ldp, int skip_ti, T* PT, int64_t ldpt, int sr, cudaStream_t st);
 
+// int16x2 blocked FW of an int32 shortest-path D (one GPU): exact for every
+// entry whose distance is < 0x3FFF; *flag (device) = 1 if any entry saturated
+// (the caller then runs the int32 FW).  P: packed copy (m x ld/2 words),
+// PT: TB x ldpt words, PTd: TB x TB words.
+cudaError_t fw16(int32_t* D, int64_t ld, int64_t m, int64_t n, uint32_t* P, uint32_t* PT, int64_t ldpt,
+                 uint32_t* PTd, unsigned* flag, cudaStream_t st);
+
 // ---------------- stream.cu ----------------
 // Row range [lo, hi) is global; D points at global row `row0` (local block).
 struct Rows {

@@ -41,11 +41,6 @@ int num_sms() {
 }
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
-#define CUDA_TRY(x)                           \
-  do {                                        \
-    cudaError_t _e = (x);                     \
-    if (_e != cudaSuccess) return _e;         \
-  } while (0)
 
 // ---------------------------------------------------------------------------
 // validation / normalisation of caller vectors

@@ -662,3 +662,34 @@ def test_microbench_denominators(lib):
     assert 2e12 < rd < 8.5e12 and 2e12 < rmw < 8.5e12
     with pytest.raises(lib._lib.ApspError):
         L.apsp_microbench(9, buf.data_ptr(), 4, st)
+
+
+@pytest.mark.parametrize("n,lo,hi,inf_frac", [
+    (300, 1, 60, 0.0),         # packed path, ragged tiles (n odd multiple of nothing)
+    (513, 0, 9, 0.3),          # zero weights + absent edges: unreachable pairs saturate -> int32 finish
+    (257, 9000, 16000, 0.0),   # distances >= 0x3FFF: saturate -> int32 finish
+    (1000, 1, 1000, 0.05),
+])
+def test_fw16_packed_equals_int32_and_oracle(lib, rng, n, lo, hi, inf_frac):
+    """APSP_OPT_FW16: the int16x2 blocked FW (exact below 0x3FFF, int32 finish
+    otherwise) gives the same D as the int32 FW and the oracle."""
+    W = random_graph(rng, n, True, density=1.0, lo=lo, hi=hi, inf_frac=inf_frac)
+    h16 = make(lib, W)                      # default: packed
+    h32 = make(lib, W, cold=False)
+    h32.set_option(lib._lib.OPT_FW16, 0)
+    h32.cold_fw()
+    D16, D32 = getD(h16), getD(h32)
+    assert np.array_equal(D16, D32)
+    assert_parity(D16, oracle.fw(W))
+
+
+def test_fw16_dense_fallback_of_a_removal(lib, rng):
+    """a7 through the packed FW: a forced-dense removal equals the oracle."""
+    W = random_graph(rng, 700, True, density=0.9, lo=1, hi=50)
+    h = make(lib, W)
+    h.set_option(0, 2)
+    _, info = h.remove_node(123)
+    assert info.path == 3
+    hg = synth.HostGraph(W, True)
+    hg.remove_node(123)
+    assert_parity(getD(h), oracle.fw(hg.W))

@@ -106,7 +106,7 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   p.off_qcnt = take(sizeof(int32_t) * (size_t)p.qbatch);
   // int16x2 FW (one GPU): packed copy of D (two columns per word) + the
   // transposed diagonal tile
-  p.off_p16 = take(world == 1 ? sizeof(uint16_t) * (size_t)cap * p.ld : 256);
+  p.off_p16 = take(sizeof(uint16_t) * (size_t)rows_max * p.ld);
   p.off_ptd = take(sizeof(uint32_t) * (size_t)kTile * kTile);
   p.off_small = take(64 * 1024);
   p.total = o;
@@ -364,21 +364,66 @@ apsp_status snap_row(apsp_handle* h, int64_t gi, T add, T* out) {
 template <typename T>
 apsp_status fw_impl_elem(apsp_handle* h);
 
+// int16x2 blocked FW (fw.cu) over the packed copy of this rank's rows, with the
+// same pivot schedule and panel broadcast as fw_impl_elem.  Sets *saturated
+// (summed over ranks) when some entry reached 0x3FFF: D then holds the exact
+// entries below it and walk lengths elsewhere.
+apsp_status fw16_impl(apsp_handle* h, bool* saturated) {
+  const int64_t n = h->n, ld = h->ld;
+  Rows r = h->active();
+  const int64_t m = r.hi - r.lo;
+  uint32_t* P = h->p16();
+  uint32_t* PT = h->pt<uint32_t>();
+  CK(p16_from_d32(h->Dl<int32_t>(), ld, m, n, P, h->st));
+  for (int64_t K0 = 0; K0 < n; K0 += kTile) {
+    const int kb = (int)std::min<int64_t>(kTile, n - K0);
+    const bool own = h->local(K0);
+    const int64_t lk = K0 - h->row0;
+    uint32_t* panel;
+    if (own) {
+      uint32_t* rowK = P + lk * (ld / 2);
+      PK(APSP_K_FW_DIAG, (double)kb * kb * kb, p16_diag(rowK + K0 / 2, ld, kb, h->st));
+      CK(p16_transpose_rep(rowK, ld, kb, K0, kb, h->ptd(), kTile, h->st));
+      PK(APSP_K_FW_PANEL, (double)kb * kb * (n - kb),
+         p16_tile3(rowK, ld, h->ptd(), kTile, rowK, kb, n, kb, -1, h->st));
+      panel = rowK;
+    } else {
+      panel = h->panel<uint32_t>();
+    }
+    if (h->world > 1)
+      NK(h->comm->bcast(panel, (size_t)kb * (ld / 2), ncclUint32, h->owner(K0), h->st));
+    const int skip_ti = own ? (int)(lk / kTile) : -1;
+    if (m > 0) {
+      const double mo = (double)(m - (own ? kb : 0));
+      CK(p16_transpose_rep(P, ld, m, K0, kb, PT, h->plan.ldpt, h->st));   // old column panel
+      PK(APSP_K_FW_PANEL, mo * kb * kb,
+         p16_tile3(P + K0 / 2, ld, PT, h->plan.ldpt, panel + K0 / 2, m, kb, kb, skip_ti, h->st));
+      CK(p16_transpose_rep(P, ld, m, K0, kb, PT, h->plan.ldpt, h->st));   // updated column panel
+      PK(APSP_K_FW_TILE, mo * (double)(n - kb) * kb,
+         p16_tile3(P, ld, PT, h->plan.ldpt, panel, m, n, kb, skip_ti, h->st));
+    }
+  }
+  CKR(cudaMemsetAsync(h->fw16_flag(), 0, sizeof(unsigned), h->st));
+  CK(p16_to_d32(P, ld, m, n, h->Dl<int32_t>(), h->fw16_flag(), h->st));
+  if (h->world > 1) NK(h->comm->allreduce(h->fw16_flag(), 1, ncclUint32, ncclMax, h->st));
+  unsigned* hf = reinterpret_cast<unsigned*>(h->host_small);
+  CKR(cudaMemcpyAsync(hf, h->fw16_flag(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+  CKR(cudaStreamSynchronize(h->st));
+  *saturated = *hf != 0;
+  return APSP_OK;
+}
+
 // Blocked FW: the int16x2 path first where it is exact, the element-type
 // path otherwise (and whenever an entry saturated).
 template <typename T>
 apsp_status fw_impl(apsp_handle* h) {
   if constexpr (std::is_same<T, int32_t>::value) {
-    if (h->fw16 && h->sr == 0 && h->world == 1) {
-      const int64_t n = h->n;
-      PK(APSP_K_FW_TILE, (double)n * n * n,
-         fw16(h->Dl<int32_t>(), h->ld, h->active().hi - h->active().lo, n, h->p16(),
-              h->pt<uint32_t>(), h->plan.ldpt, h->ptd(), h->fw16_flag(), h->st));
-      unsigned* hf = reinterpret_cast<unsigned*>(h->host_small);
-      CKR(cudaMemcpyAsync(hf, h->fw16_flag(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
-      CKR(cudaStreamSynchronize(h->st));
-      h->last_fw16 = *hf ? 2 : 1;
-      if (!*hf) return APSP_OK;
+    if (h->fw16 && h->sr == 0) {
+      bool saturated = false;
+      apsp_status s = fw16_impl(h, &saturated);
+      if (s != APSP_OK) return s;
+      h->last_fw16 = saturated ? 2 : 1;
+      if (!saturated) return APSP_OK;
       // some distance is >= 0x3FFF or infinite: finish in int32 (exact from any
       // matrix of walk lengths, which D still is)
     }

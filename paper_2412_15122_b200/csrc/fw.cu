@@ -619,40 +619,36 @@ static cudaError_t tile3_p16(uint32_t* C, int64_t ldc, const uint32_t* PT, int64
   return cudaGetLastError();
 }
 
-cudaError_t fw16(int32_t* D, int64_t ld, int64_t m, int64_t n, uint32_t* P, uint32_t* PT, int64_t ldpt,
-                 uint32_t* PTd, unsigned* flag, cudaStream_t st) {
-  if (m <= 0 || n <= 0) return cudaSuccess;
-  const int64_t ldw = ld / 2;                 // words per packed row
-  const int64_t nw = (n + 1) / 2;             // words holding columns [0, n)
-  const int64_t mpad = (m + TB - 1) / TB * TB;
-  if (mpad > ldpt || (ld & 1)) return cudaErrorInvalidValue;
-  const int g = num_sms() * 8;
-  k_d32_to_p16<<<g, 256, 0, st>>>(D, ld, m, n, P, ldw);
-  CUDA_TRY(cudaGetLastError());
-  for (int64_t K0 = 0; K0 < n; K0 += TB) {
-    const int kb = (int)std::min<int64_t>(TB, n - K0);
-    uint32_t* rowK = P + K0 * ldw;
-    // (1) diagonal tile
-    k_p16_diag<<<1, 1024, 0, st>>>(rowK + K0 / 2, ldw, kb);
-    CUDA_TRY(cudaGetLastError());
-    // (2) row panel with A = the closed tile, column panel with A = its old values
-    k_p16_transpose_rep<<<dim3(TB / 32, TB / 32), dim3(32, 8), 0, st>>>(rowK, ldw, kb, K0, kb, PTd, TB, TB);
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(tile3_p16(rowK, ldw, PTd, TB, rowK, ldw, kb, nw, kb, -1, st));
-    k_p16_transpose_rep<<<dim3((unsigned)(mpad / 32), TB / 32), dim3(32, 8), 0, st>>>(P, ldw, m, K0, kb, PT,
-                                                                                      ldpt, mpad);
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(tile3_p16(P + K0 / 2, ldw, PT, ldpt, rowK + K0 / 2, ldw, m, (kb + 1) / 2, kb,
-                       (int)(K0 / TB), st));
-    // (3) the rest, A = the updated column panel
-    k_p16_transpose_rep<<<dim3((unsigned)(mpad / 32), TB / 32), dim3(32, 8), 0, st>>>(P, ldw, m, K0, kb, PT,
-                                                                                      ldpt, mpad);
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(tile3_p16(P, ldw, PT, ldpt, rowK, ldw, m, nw, kb, (int)(K0 / TB), st));
-  }
-  CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(unsigned), st));
-  k_p16_to_d32<<<g, 256, 0, st>>>(P, ldw, m, n, 0, D, ld, flag);
+// ---- launchers (the per-pivot host loop is fw16_impl in apsp_warm.cu, which
+// also broadcasts the packed row panel when D is row-sharded) ----
+cudaError_t p16_from_d32(const int32_t* D, int64_t ld, int64_t m, int64_t n, uint32_t* P, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  k_d32_to_p16<<<num_sms() * 8, 256, 0, st>>>(D, ld, m, n, P, ld / 2);
   return cudaGetLastError();
+}
+cudaError_t p16_to_d32(const uint32_t* P, int64_t ld, int64_t m, int64_t n, int32_t* D, unsigned* flag,
+                       cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  k_p16_to_d32<<<num_sms() * 8, 256, 0, st>>>(P, ld / 2, m, n, 0, D, ld, flag);
+  return cudaGetLastError();
+}
+cudaError_t p16_diag(uint32_t* Pkk, int64_t ld, int kb, cudaStream_t st) {
+  k_p16_diag<<<1, 1024, 0, st>>>(Pkk, ld / 2, kb);
+  return cudaGetLastError();
+}
+cudaError_t p16_transpose_rep(const uint32_t* P, int64_t ld, int64_t m, int64_t K0, int kb, uint32_t* PT,
+                              int64_t ldpt, cudaStream_t st) {
+  const int64_t mpad = (m + TB - 1) / TB * TB;
+  if (mpad == 0) return cudaSuccess;
+  if (mpad > ldpt) return cudaErrorInvalidValue;
+  k_p16_transpose_rep<<<dim3((unsigned)(mpad / 32), TB / 32), dim3(32, 8), 0, st>>>(P, ld / 2, m, K0, kb, PT,
+                                                                                    ldpt, mpad);
+  return cudaGetLastError();
+}
+cudaError_t p16_tile3(uint32_t* C, int64_t ld, const uint32_t* PT, int64_t ldpt, const uint32_t* B, int64_t m,
+                      int64_t n, int kdepth, int skip_ti, cudaStream_t st) {
+  // C and B rows are packed rows of D (ld/2 words); n = columns of D covered
+  return tile3_p16(C, ld / 2, PT, ldpt, B, ld / 2, m, (n + 1) / 2, kdepth, skip_ti, st);
 }
 
 #define INST(T)                                                                                  \

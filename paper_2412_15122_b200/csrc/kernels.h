@@ -28,12 +28,20 @@ template <typename T>
 cudaError_t fw_rest_pt(T* D, int64_t ld, int64_t m, int64_t ncols, int64_t K0, int kb, const T* P,
                        int64_t ldp, int skip_ti, T* PT, int64_t ldpt, int sr, cudaStream_t st);
 
-// int16x2 blocked FW of an int32 shortest-path D (one GPU): exact for every
-// entry whose distance is < 0x3FFF; *flag (device) = 1 if any entry saturated
-// (the caller then runs the int32 FW).  P: packed copy (m x ld/2 words),
-// PT: TB x ldpt words, PTd: TB x TB words.
-cudaError_t fw16(int32_t* D, int64_t ld, int64_t m, int64_t n, uint32_t* P, uint32_t* PT, int64_t ldpt,
-                 uint32_t* PTd, unsigned* flag, cudaStream_t st);
+// int16x2 blocked FW of an int32 shortest-path D (fw.cu): packed copy P of the
+// local rows (two columns per 32-bit word, row stride ld/2 words), values
+// saturated at 0x3FFF.  ld = D's leading dimension in int32 elements.
+cudaError_t p16_from_d32(const int32_t* D, int64_t ld, int64_t m, int64_t n, uint32_t* P, cudaStream_t st);
+// D := P where < 0x3FFF; *flag |= 1 if any of the m x n entries saturated
+cudaError_t p16_to_d32(const uint32_t* P, int64_t ld, int64_t m, int64_t n, int32_t* D, unsigned* flag,
+                       cudaStream_t st);
+cudaError_t p16_diag(uint32_t* Pkk, int64_t ld, int kb, cudaStream_t st);
+// PT[k][i] = D[i][K0 + k] in both halves (k < kb, i < m), INF padding to TB x round_up(m, 128)
+cudaError_t p16_transpose_rep(const uint32_t* P, int64_t ld, int64_t m, int64_t K0, int kb, uint32_t* PT,
+                              int64_t ldpt, cudaStream_t st);
+// C[i][j] = min(C[i][j], min_k PT[k][i] + B[k][j]) for i < m, j < n (packed rows)
+cudaError_t p16_tile3(uint32_t* C, int64_t ld, const uint32_t* PT, int64_t ldpt, const uint32_t* B, int64_t m,
+                      int64_t n, int kdepth, int skip_ti, cudaStream_t st);
 
 // ---------------- stream.cu ----------------
 // Row range [lo, hi) is global; D points at global row `row0` (local block).

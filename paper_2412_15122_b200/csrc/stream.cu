@@ -612,8 +612,7 @@ struct DetectQueue {
   unsigned short w[DS_Q];   // flag word: bit v*4+c <-> column 4*(chunk*128 + v*32 + lane) + c
 };
 template <typename T>
-__device__ __forceinline__ void detect_flush(const DetectQueue& Q, int cnt, const T* D, int64_t ld,
-                                             int64_t row0, int64_t i_lo, int chunk,
+__device__ __forceinline__ void detect_flush(const DetectQueue& Q, int cnt, int64_t i_lo, int chunk,
                                              const DetectOut<T>& o, int lane) {
   if (cnt == 0) return;
   __syncwarp();
@@ -639,15 +638,13 @@ __device__ __forceinline__ void detect_flush(const DetectQueue& Q, int cnt, cons
     const unsigned rl = Q.rl[e];
     const int64_t i = i_lo + (rl >> 5);
     const int ln = (int)(rl & 31u);
-    const T* Drow = D + (i - row0) * ld;
     while (w) {
       const int bit = __ffs(w) - 1;
       w &= w - 1;
       const int64_t j = 4 * ((int64_t)chunk * DS_VEC + (bit >> 2) * 32 + ln) + (bit & 3);
       if (pos < o.lcap) {
         o.prow[pos] = (int)i;
-        o.pcol[pos] = (int)j;
-        o.plb[pos] = Drow[j];   // D_old[i][j]: a lower bound of D'
+        o.pcol[pos] = (int)j;   // D_old[i][j] (the lower bound) is read by the scatter
       }
       ++pos;
     }
@@ -721,7 +718,7 @@ __global__ void __launch_bounds__(256, 2) k_detect_stream(T* __restrict__ D, int
         const int tot = __reduce_add_sync(0xffffffffu, (unsigned)__popc(word));
         if (lane == 0) atomicAdd(o.rowcnt + i, tot);
         if (qcnt + 32 > DS_Q) {
-          detect_flush<T>(Q, qcnt, D, ld, r.row0, i_lo, chunk, o, lane);
+          detect_flush<T>(Q, qcnt, i_lo, chunk, o, lane);
           qcnt = 0;
         }
         const unsigned bal = __ballot_sync(0xffffffffu, word != 0);
@@ -744,7 +741,7 @@ __global__ void __launch_bounds__(256, 2) k_detect_stream(T* __restrict__ D, int
       }
     }
   }
-  if (MODE == 1) detect_flush<T>(Q, qcnt, D, ld, r.row0, i_lo, chunk, o, lane);
+  if (MODE == 1) detect_flush<T>(Q, qcnt, i_lo, chunk, o, lane);
 }
 
 // Per row of the list: rowoff[i] (a slice of rowcnt[i] slots for the row's
@@ -790,10 +787,11 @@ __global__ void k_scatter_pairs(T* D, int64_t ld, int64_t row0, const T* __restr
        p += (int64_t)gridDim.x * blockDim.x) {
     const int i = srow[p], j = scol[p];
     const int64_t q = rowoff[i] + atomicAdd(cur + i, 1);
+    T* d = D + ((int64_t)i - row0) * ld + j;
     prow[q] = i;
     pcol[q] = j;
-    plb[q] = slb[p];
-    D[((int64_t)i - row0) * ld + j] = WT[(int64_t)j * ldw + i];
+    plb[q] = *d;                               // D_old[i][j]: a lower bound of D'
+    *d = WT[(int64_t)j * ldw + i];             // D0[i][j] := W'[i][j]
   }
 }
 

@@ -168,7 +168,38 @@ def worker(rank, world, port, W, cap, adds, removes, q):
             Wfull[:, last] = INF
             n -= 1
         D = gather_rows(Dl, row0, rows, n, world)
-        q.put((rank, ok_fw, D, int(cnt.item()) if removes else 0))
+        # ---- sharded queries: all-gather of every rank's column-t slices, the
+        # owner of row s answers (candidates + predecessor walk), the others
+        # contribute zeros to an all-reduce(sum) of the outputs
+        qs, qt = synth.query_pairs(3, n, 24)
+        m = max(0, min(rows, n - row0))
+        cols = np.full((len(qs), R), INF, np.int64)
+        for b, t in enumerate(qt):
+            cols[b, :m] = Dl[:m, t]
+        parts = [torch.zeros_like(torch.from_numpy(cols)) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(cols))
+        colfull = torch.cat(parts, dim=1).numpy()[:, :n]   # D[k][t_b], k < n
+        PCAP = 64
+        out = np.zeros((len(qs), 2 + PCAP), np.int64)      # dist, |C|, path (+1 so 0 = empty)
+        Wq = np.minimum(Wfull[:n, :n], INF)
+        for b, (s_, t_) in enumerate(zip(qs, qt)):
+            if owner(s_) != rank:
+                continue
+            drow = Dl[s_ - row0, :n]
+            dst = drow[t_]
+            cand = np.nonzero((drow + colfull[b] == dst) & (drow < INF) & (colfull[b] < INF))[0]
+            path, cur = [t_], t_
+            while cur != s_:   # predecessor walk: first m in (D[s][m], m) order with an exact last hop
+                ok = [c for c in cand if (drow[c], c) < (drow[cur], cur) and Wq[c, cur] < INF
+                      and drow[c] + Wq[c, cur] == drow[cur]]
+                cur = min(ok, key=lambda c: (drow[c], c))
+                path.append(cur)
+            path = path[::-1]
+            out[b, 0], out[b, 1] = dst, len(cand)
+            out[b, 2:2 + len(path)] = np.array(path) + 1
+        tq = torch.from_numpy(out)
+        dist.all_reduce(tq)
+        q.put((rank, ok_fw, D, int(cnt.item()) if removes else 0, (qs, qt, tq.numpy())))
     finally:
         dist.destroy_process_group()
 
@@ -210,6 +241,13 @@ def test_row_sharded_protocol_world2(n, cap):
     for p in procs:
         p.join(timeout=60)
     exp = oracle.to_oracle(oracle.fw(hg.W)).clip(max=INF)
-    for rank, ok_fw, D, cnt in res:
+    Wf = hg.W
+    for rank, ok_fw, D, cnt, (qs, qt, out) in res:
         assert ok_fw, f"rank {rank}: sharded cold FW != oracle"
         assert np.array_equal(np.minimum(D, INF), exp), f"rank {rank}: sharded updates != oracle"
+        assert np.array_equal(out, res[0][4][2]), "ranks disagree on the sharded query outputs"
+        for b, (s_, t_) in enumerate(zip(qs, qt)):
+            assert out[b, 0] == exp[s_, t_]
+            assert out[b, 1] == len(oracle.candidates(exp, s_, t_))
+            path = [int(x) - 1 for x in out[b, 2:] if x > 0]
+            assert oracle.path_is_valid(Wf, path, s_, t_) and oracle.path_weight(Wf, path) == exp[s_, t_]

@@ -368,7 +368,7 @@ apsp_status fw_impl_elem(apsp_handle* h);
 // same pivot schedule and panel broadcast as fw_impl_elem.  Sets *saturated
 // (summed over ranks) when some entry reached 0x3FFF: D then holds the exact
 // entries below it and walk lengths elsewhere.
-apsp_status fw16_impl(apsp_handle* h, bool* saturated) {
+apsp_status fw16_impl(apsp_handle* h, int64_t skip, bool* saturated) {
   const int64_t n = h->n, ld = h->ld;
   Rows r = h->active();
   const int64_t m = r.hi - r.lo;
@@ -404,7 +404,7 @@ apsp_status fw16_impl(apsp_handle* h, bool* saturated) {
     }
   }
   CKR(cudaMemsetAsync(h->fw16_flag(), 0, sizeof(unsigned), h->st));
-  CK(p16_to_d32(P, ld, m, n, h->Dl<int32_t>(), h->fw16_flag(), h->st));
+  CK(p16_to_d32(P, ld, m, n, h->row0, skip, h->Dl<int32_t>(), h->fw16_flag(), h->st));
   if (h->world > 1) NK(h->comm->allreduce(h->fw16_flag(), 1, ncclUint32, ncclMax, h->st));
   unsigned* hf = reinterpret_cast<unsigned*>(h->host_small);
   CKR(cudaMemcpyAsync(hf, h->fw16_flag(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
@@ -415,12 +415,13 @@ apsp_status fw16_impl(apsp_handle* h, bool* saturated) {
 
 // Blocked FW: the int16x2 path first where it is exact, the element-type
 // path otherwise (and whenever an entry saturated).
+// `skip`: a tombstoned node (its row and column are INF and stay so), or -1.
 template <typename T>
-apsp_status fw_impl(apsp_handle* h) {
+apsp_status fw_impl(apsp_handle* h, int64_t skip = -1) {
   if constexpr (std::is_same<T, int32_t>::value) {
     if (h->fw16 && h->sr == 0) {
       bool saturated = false;
-      apsp_status s = fw16_impl(h, &saturated);
+      apsp_status s = fw16_impl(h, skip, &saturated);
       if (s != APSP_OK) return s;
       h->last_fw16 = saturated ? 2 : 1;
       if (!saturated) return APSP_OK;
@@ -584,7 +585,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
       PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
          detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, 2, nullptr, nullptr, nullptr,
                    nullptr, nullptr, 0, nullptr, h->WT<T>(), h->ld, h->sr, h->st));
-    return fw_impl<T>(h);
+    return fw_impl<T>(h, removal ? skip : -1);
   }
   if (info) info->path = 2;
   return APSP_OK;

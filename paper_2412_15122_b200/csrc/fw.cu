@@ -524,14 +524,18 @@ __global__ void k_d32_to_p16(const int32_t* __restrict__ D, int64_t ld, int64_t 
   }
 }
 
-// D[i][j] := P value where it is < SAT; flag any saturated off-diagonal entry
+// D[i][j] := P value where it is < SAT; flag any other saturated entry.  Row and
+// column `skip` (a tombstoned node: INF in D already, isolated in the graph)
+// are neither written nor flagged.
 __global__ void k_p16_to_d32(const uint32_t* __restrict__ P, int64_t ldw, int64_t m, int64_t n,
-                             int64_t row0, int32_t* __restrict__ D, int64_t ld, unsigned* flag) {
+                             int64_t row0, int32_t* __restrict__ D, int64_t ld, int64_t skip,
+                             unsigned* flag) {
   const int64_t tot = m * n;
   unsigned f = 0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / n, j = e - i * n;
+    if (i + row0 == skip || j == skip) continue;
     const uint32_t v = half16(P[i * ldw + (j >> 1)], (int)(j & 1));
     if (v < kSat16) D[i * ld + j] = (int32_t)v;
     else f = 1;
@@ -626,10 +630,10 @@ cudaError_t p16_from_d32(const int32_t* D, int64_t ld, int64_t m, int64_t n, uin
   k_d32_to_p16<<<num_sms() * 8, 256, 0, st>>>(D, ld, m, n, P, ld / 2);
   return cudaGetLastError();
 }
-cudaError_t p16_to_d32(const uint32_t* P, int64_t ld, int64_t m, int64_t n, int32_t* D, unsigned* flag,
-                       cudaStream_t st) {
+cudaError_t p16_to_d32(const uint32_t* P, int64_t ld, int64_t m, int64_t n, int64_t row0, int64_t skip,
+                       int32_t* D, unsigned* flag, cudaStream_t st) {
   if (m <= 0) return cudaSuccess;
-  k_p16_to_d32<<<num_sms() * 8, 256, 0, st>>>(P, ld / 2, m, n, 0, D, ld, flag);
+  k_p16_to_d32<<<num_sms() * 8, 256, 0, st>>>(P, ld / 2, m, n, row0, D, ld, skip, flag);
   return cudaGetLastError();
 }
 cudaError_t p16_diag(uint32_t* Pkk, int64_t ld, int kb, cudaStream_t st) {

@@ -33,8 +33,9 @@ cudaError_t fw_rest_pt(T* D, int64_t ld, int64_t m, int64_t ncols, int64_t K0, i
 // saturated at 0x3FFF.  ld = D's leading dimension in int32 elements.
 cudaError_t p16_from_d32(const int32_t* D, int64_t ld, int64_t m, int64_t n, uint32_t* P, cudaStream_t st);
 // D := P where < 0x3FFF; *flag |= 1 if any of the m x n entries saturated
-cudaError_t p16_to_d32(const uint32_t* P, int64_t ld, int64_t m, int64_t n, int32_t* D, unsigned* flag,
-                       cudaStream_t st);
+// (row / column `skip`, a tombstoned node, excluded; -1: none)
+cudaError_t p16_to_d32(const uint32_t* P, int64_t ld, int64_t m, int64_t n, int64_t row0, int64_t skip,
+                       int32_t* D, unsigned* flag, cudaStream_t st);
 cudaError_t p16_diag(uint32_t* Pkk, int64_t ld, int kb, cudaStream_t st);
 // PT[k][i] = D[i][K0 + k] in both halves (k < kb, i < m), INF padding to TB x round_up(m, 128)
 cudaError_t p16_transpose_rep(const uint32_t* P, int64_t ld, int64_t m, int64_t K0, int kb, uint32_t* PT,

@@ -144,6 +144,7 @@ struct apsp_handle {
   int max_rounds = 64;
   int fw16 = 1;                  // int16x2 FW when exact (int32 shortest path, one GPU)
   int last_fw16 = 0;             // 1: the last FW ran packed, 2: it fell back to int32
+  bool mirror_built = false;     // the int16 mirror was built (or invalidated) from D
   double row_delta = 0.0;        // > 0: the paper's Definition-1 gate (ablation)
   int sr = 0;                    // path algebra: 0 shortest path, 1 minimax
   // state
@@ -239,6 +240,12 @@ struct apsp_handle {
     return reinterpret_cast<unsigned long long*>(ws + plan.off_small + 320);
   }
   unsigned* fw16_flag() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 392); }
+  unsigned* mirror_flag() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 396); }
+  // int16 mirror of D (kernels.h): int32 handles only; lives in the packed-FW buffer
+  template <typename T> Mirror mirror() {
+    if constexpr (std::is_same<T, int32_t>::value) return Mirror{reinterpret_cast<uint16_t*>(p16()), mirror_flag()};
+    else return Mirror{nullptr, mirror_flag()};
+  }
   uint32_t* p16() { return reinterpret_cast<uint32_t*>(ws + plan.off_p16); }
   uint32_t* ptd() { return reinterpret_cast<uint32_t*>(ws + plan.off_ptd); }
   unsigned* wmin_dev() {   // accumulator of the smallest edge weight (bits of a T >= 0)
@@ -364,6 +371,24 @@ apsp_status snap_row(apsp_handle* h, int64_t gi, T add, T* out) {
 template <typename T>
 apsp_status fw_impl_elem(apsp_handle* h);
 
+// (Re)build the int16 mirror from D: at the first update of a handle whose D
+// the caller filled (warm start), and after an int32 FW.  Mirror flag = 0 iff
+// every finite distance is < 0x3FFF (on every rank).
+template <typename T>
+apsp_status mirror_rebuild(apsp_handle* h) {
+  if constexpr (std::is_same<T, int32_t>::value) {
+    CKR(cudaMemsetAsync(h->mirror_flag(), 0, sizeof(unsigned), h->st));
+    CK(mirror_build(h->Dl<int32_t>(), h->ld, h->active(), h->n, h->mirror<int32_t>(), h->st));
+    if (h->world > 1) NK(h->comm->allreduce(h->mirror_flag(), 1, ncclUint32, ncclMax, h->st));
+  }
+  h->mirror_built = true;
+  return APSP_OK;
+}
+template <typename T>
+apsp_status ensure_mirror(apsp_handle* h) {
+  return h->mirror_built ? APSP_OK : mirror_rebuild<T>(h);
+}
+
 // int16x2 blocked FW (fw.cu) over the packed copy of this rank's rows, with the
 // same pivot schedule and panel broadcast as fw_impl_elem.  Sets *saturated
 // (summed over ranks) when some entry reached 0x3FFF: D then holds the exact
@@ -424,12 +449,18 @@ apsp_status fw_impl(apsp_handle* h, int64_t skip = -1) {
       apsp_status s = fw16_impl(h, skip, &saturated);
       if (s != APSP_OK) return s;
       h->last_fw16 = saturated ? 2 : 1;
-      if (!saturated) return APSP_OK;
+      if (!saturated) {   // the packed buffer now holds sat16(D): the mirror is valid
+        CKR(cudaMemsetAsync(h->mirror_flag(), 0, sizeof(unsigned), h->st));
+        h->mirror_built = true;
+        return APSP_OK;
+      }
       // some distance is >= 0x3FFF or infinite: finish in int32 (exact from any
       // matrix of walk lengths, which D still is)
     }
   }
-  return fw_impl_elem<T>(h);
+  apsp_status s = fw_impl_elem<T>(h);
+  if (s != APSP_OK) return s;
+  return mirror_rebuild<T>(h);   // the packed buffer was work space (or never mirrored D)
 }
 
 template <typename T>
@@ -488,7 +519,8 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   // Phi / max|A_i|, the row grouping and the D0 reset (W'[i][j])
   PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
      detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, 1, nullptr, h->rowcnt(),
-               h->srow(), h->scol(), h->slb<T>(), lcap, h->ctr(), h->WT<T>(), h->ld, h->sr, h->st));
+               h->srow(), h->scol(), h->slb<T>(), lcap, h->ctr(), h->WT<T>(), h->ld, h->sr,
+               h->mirror<T>(), h->st));
   PK(APSP_K_EMIT, 0.0,
      detect_lists<T>(h->Dl<T>(), h->ld, r, h->WT<T>(), h->ld, h->rowcnt(), h->rowoff(), h->srow(),
                      h->scol(), h->slb<T>(), h->ocnt(), h->prow(), h->pcol(), h->plb<T>(), lcap,
@@ -584,10 +616,12 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     if (hv[2] != 0)   // the need_update_list missed pairs: reset every flagged entry in place
       PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
          detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, 2, nullptr, nullptr, nullptr,
-                   nullptr, nullptr, 0, nullptr, h->WT<T>(), h->ld, h->sr, h->st));
+                   nullptr, nullptr, 0, nullptr, h->WT<T>(), h->ld, h->sr, h->mirror<T>(), h->st));
     return fw_impl<T>(h, removal ? skip : -1);
   }
   if (info) info->path = 2;
+  if (total > 0)   // the sparse kernels wrote D on listed pairs only
+    CK(mirror_pairs(h->Dl<T>(), h->ld, h->row0, h->prow(), h->pcol(), h->ctr(), lcap, h->mirror<T>(), h->st));
   return APSP_OK;
 }
 
@@ -595,6 +629,10 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
 template <typename T>
 apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, int64_t* new_index,
                           apsp_update_info* info) {
+  {
+    apsp_status ms = ensure_mirror<T>(h);
+    if (ms != APSP_OK) return ms;
+  }
   const int64_t n = h->n, ld = h->ld, x = n;
   T* ow = h->vec<T>(0);
   T* iw = h->vec<T>(1);
@@ -630,16 +668,20 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   T* ceff = h->vec<T>(4);
   PK(APSP_K_ADD_PASS1, 4.0 * (double)(r.hi - r.lo) * (double)n,
      addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
-                      &nchunk, &nslab, kMaxSlabs, h->sr, h->st));
+                      &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), h->st));
   CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
                        ceff, row, h->st));
   if (h->world > 1)
     NK(h->comm->allreduce(row, (size_t)ld, nccl_type<T>(), ncclMin, h->st));
   // rows with ceff[i] = INF provably do not change and are not read at all
   PK(APSP_K_RANK1, 0.0,   // work: bytes actually read, counted on the device
-     rank1<T>(h->Dl<T>(), ld, r, n, ceff, row, nullptr, nullptr, h->rank1_bytes(), h->sr, h->st));
+     rank1<T>(h->Dl<T>(), ld, r, n, ceff, row, nullptr, nullptr, h->rank1_bytes(), h->sr, h->mirror<T>(),
+              h->st));
   CK(addnode_write<T>(h->Dl<T>(), ld, r, n, x, h->local(x) ? 1 : 0, col, row, h->WT<T>(), ld, ow,
                       iw, h->st));
+  Rows rx = r;   // the active rows after the add (row x joins them if it is local)
+  if (h->local(x)) rx.hi = x + 1;
+  CK(mirror_cross(h->Dl<T>(), ld, rx, n + 1, x, x, h->mirror<T>(), h->st));
   CKR(cudaStreamWaitEvent(h->st, h->ev_join, 0));   // shortlist upkeep (side stream) done
   h->n = n + 1;
   if (new_index) *new_index = x;
@@ -654,6 +696,10 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
 // ------------------------------------------------------------------ remove node
 template <typename T>
 apsp_status remove_node_impl(apsp_handle* h, int64_t k, int64_t* moved_from, apsp_update_info* info) {
+  {
+    apsp_status ms = ensure_mirror<T>(h);
+    if (ms != APSP_OK) return ms;
+  }
   const int64_t n = h->n, ld = h->ld;
   Rows r = h->active();
   T* c1 = h->vec<T>(4);
@@ -692,6 +738,9 @@ apsp_status remove_node_impl(apsp_handle* h, int64_t k, int64_t* moved_from, aps
   Rows rw{0, n, 0};
   CK(fill_col<T>(WT, ld, rw, last, I, h->st));
   CK(shortlist_remove<T>(h->slid(), h->slw<T>(), h->wnext<T>(), n, k, last, h->st));
+  // the int16 mirror of the rows / columns the tombstone and the move rewrote
+  CK(mirror_cross(h->Dl<T>(), ld, r, n, k, k, h->mirror<T>(), h->st));
+  if (k != last) CK(mirror_cross(h->Dl<T>(), ld, r, n, last, last, h->mirror<T>(), h->st));
   h->n = n - 1;
   if (moved_from) *moved_from = (k != last) ? last : -1;
   if (info) info->n_after = h->n;
@@ -701,6 +750,10 @@ apsp_status remove_node_impl(apsp_handle* h, int64_t k, int64_t* moved_from, aps
 // ------------------------------------------------------------------ update edge
 template <typename T>
 apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp_update_info* info) {
+  {
+    apsp_status ms = ensure_mirror<T>(h);
+    if (ms != APSP_OK) return ms;
+  }
   const int64_t n = h->n, ld = h->ld;
   T* WT = h->WT<T>();
   // 8-byte read: W[u][v] (replicated WT) and D[u][v] (owner of row u)
@@ -746,7 +799,7 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
     }
     PK(APSP_K_RANK1, 0.0,   // work: bytes actually read, counted on the device
        rank1<T>(h->Dl<T>(), ld, r, n, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, h->rank1_bytes(),
-                h->sr, h->st));
+                h->sr, h->mirror<T>(), h->st));
     CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
     CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
     if (info) info->path = 1;
@@ -791,7 +844,7 @@ apsp_status removal_phi(apsp_handle* h, int64_t k, int64_t* phi) {
   if (s != APSP_OK) return s;
   PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
      detect<T>(h->Dl<T>(), ld, r, n, k, c1, r1, nullptr, nullptr, h->tau, 0, h->anyrow(), nullptr,
-               nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0, h->sr, h->st));
+               nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0, h->sr, h->mirror<T>(), h->st));
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(h->small() + 128);
   CKR(cudaMemsetAsync(cnt, 0, sizeof *cnt, h->st));
   CK(count_nonzero(h->anyrow() + r.lo, r.hi - r.lo, cnt, h->st));
@@ -825,12 +878,18 @@ apsp_status swap_nodes(apsp_handle* h, int64_t p, int64_t q) {
   Rows rw{0, n, 0};
   CK(swap_cols<T>(WT, ld, rw, p, q, h->st));
   CK(shortlist_swap<T>(h->slid(), h->slw<T>(), h->wnext<T>(), n, p, q, h->st));
+  CK(mirror_cross(h->Dl<T>(), ld, h->active(), n, p, p, h->mirror<T>(), h->st));
+  CK(mirror_cross(h->Dl<T>(), ld, h->active(), n, q, q, h->mirror<T>(), h->st));
   return APSP_OK;
 }
 
 template <typename T>
 apsp_status modify_readd_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, int64_t* removed,
                               apsp_update_info* info) {
+  {
+    apsp_status ms = ensure_mirror<T>(h);
+    if (ms != APSP_OK) return ms;
+  }
   const int64_t n = h->n, ld = h->ld;
   T* WT = h->WT<T>();
   T* hv = reinterpret_cast<T*>(h->host_small);
@@ -1070,6 +1129,7 @@ apsp_status create_impl(apsp_handle** out, apsp_dtype dtype, int directed, int64
   apsp_status s = dispatch(dtype, [&](auto z) -> apsp_status {
     using T = decltype(z);
     CKR(cudaMemsetAsync(h->ws + h->plan.off_small, 0, 512, h->st));   // counters, flags
+    CKR(cudaMemsetAsync(h->mirror_flag(), 0xff, sizeof(unsigned), h->st));   // no mirror yet
     CK(fill<T>(h->WT<T>(), (int64_t)cap * h->ld, Tr<T>::inf(), h->st));
     CKR(cudaMemsetAsync(&h->ctr()->err, 0, sizeof(unsigned), h->st));
     CKR(cudaMemsetAsync(h->wmin_dev(), 0xff, sizeof(unsigned), h->st));

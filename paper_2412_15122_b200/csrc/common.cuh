@@ -157,6 +157,41 @@ __device__ __forceinline__ Vec4<T> mask_tail(Vec4<T> v, int64_t col0, int64_t n)
   return v;
 }
 
+// ---------------------------------------------------------------------------
+// int16 mirror of int32 D (kernels.h: struct Mirror)
+// ---------------------------------------------------------------------------
+constexpr int32_t kSat16i = 0x3FFF;
+__device__ __forceinline__ uint16_t sat16(int32_t v) { return (uint16_t)min(v, kSat16i); }
+// 4 mirrored values: an 8-byte streaming load, then (separately, so that every
+// load of a batch is issued before the first result is waited for) the
+// conversion that reads 0x3FFF back as INF
+// 8 mirrored values in one 16-byte streaming load (two Vec4 worth)
+__device__ __forceinline__ uint4 mload8(const uint16_t* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+// Column groups of a lane in a 512-column chunk.  int32 rows: vector v holds
+// columns 4*(chunk*128 + v*32 + lane) + [0, 4).  Mirror rows are read 16 bytes
+// (8 columns) at a time, so vectors 2q and 2q+1 are the halves of load q:
+// columns 8*(chunk*64 + q*32 + lane) + [0, 8) — the same 512 columns per warp.
+__device__ __forceinline__ int64_t group_of(bool m16, int chunk, int v, int lane) {
+  return m16 ? 2 * ((int64_t)chunk * 64 + (v >> 1) * 32 + lane) + (v & 1)
+             : (int64_t)chunk * 128 + v * 32 + lane;
+}
+__device__ __forceinline__ uint2 mload4(const uint16_t* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ Vec4<T> mconv4(uint2 r) {
+  auto cv = [](unsigned x) -> T { return x == (unsigned)kSat16i ? Tr<T>::inf() : (T)x; };
+  return Vec4<T>{cv(r.x & 0xFFFFu), cv(r.x >> 16), cv(r.y & 0xFFFFu), cv(r.y >> 16)};
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_min(T v) {
 #pragma unroll

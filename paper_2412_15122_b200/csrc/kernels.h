@@ -5,6 +5,16 @@
 
 namespace apsp {
 
+// int16 mirror of an int32 D (same element indexing, ld int16 per row): every
+// value v stored as min(v, 0x3FFF), INF as 0x3FFF.  It is exact — and the two
+// O(n^2) streaming passes (add-node pass 1, detection) read it at half the
+// bytes — while *flag == 0, i.e. while every finite distance is < 0x3FFF.
+// Writers of D keep it in step and raise *flag on a finite value >= 0x3FFF.
+struct Mirror {
+  uint16_t* m;      // nullptr: no mirror (fp32 handles)
+  unsigned* flag;   // 0: m mirrors D exactly
+};
+
 // Device counters written by the detection kernel.
 struct DetectCounters {
   unsigned long long total;   // |A|
@@ -68,14 +78,14 @@ cudaError_t copy_vec(const T* src, int64_t n, int64_t npad, T add, T* out, cudaS
 template <typename T>
 cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow, const T* iw,
                           T* rowpart, T* rowpartM, T* colpart, int64_t part_ld, int* nchunk_out,
-                          int* nslab_out, int max_slabs, int sr, cudaStream_t st);
+                          int* nslab_out, int max_slabs, int sr, Mirror M, cudaStream_t st);
 template <typename T>
 cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
                            int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,
                            T* ceff, T* row, cudaStream_t st);
 template <typename T>
 cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, const T* c2,
-                  const T* rv2, unsigned long long* bytes_read, int sr, cudaStream_t st);
+                  const T* rv2, unsigned long long* bytes_read, int sr, Mirror M, cudaStream_t st);
 template <typename T>
 cudaError_t addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xlocal,
                           const T* col, const T* row, T* WT, int64_t ldw, const T* ow,
@@ -86,7 +96,7 @@ template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
                    const T* c2, const T* r2, float tau, int mode, int* anyrow, int* rowcnt,
                    int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr, const T* WT,
-                   int64_t ldw, int sr, cudaStream_t st);
+                   int64_t ldw, int sr, Mirror M, cudaStream_t st);
 template <typename T>
 cudaError_t detect_lists(T* D, int64_t ld, Rows r, const T* WT, int64_t ldw, const int* rowcnt,
                          int64_t* rowoff, const int* srow, const int* scol, const T* slb, int* cur,
@@ -184,6 +194,19 @@ template <typename T>
 cudaError_t query_colslice(const T* D, int64_t ld, int64_t rows, int64_t R, int64_t n,
                            const int* t, int qc, T* out, cudaStream_t st);
 
+// int16 mirror upkeep (stream.cu): build from D (flag must be 0 before), re-sync
+// the listed pairs / one row and one column (-1: none) after D changed there
+cudaError_t mirror_build(const int32_t* D, int64_t ld, Rows r, int64_t n, Mirror M, cudaStream_t st);
+cudaError_t mirror_pairs(const int32_t* D, int64_t ld, int64_t row0, const int* prow, const int* pcol,
+                         const DetectCounters* ctr, int64_t lcap, Mirror M, cudaStream_t st);
+cudaError_t mirror_cross(const int32_t* D, int64_t ld, Rows r, int64_t n, int64_t row, int64_t col, Mirror M,
+                         cudaStream_t st);
+// fp32 handles have no mirror
+inline cudaError_t mirror_pairs(const float*, int64_t, int64_t, const int*, const int*, const DetectCounters*,
+                                int64_t, Mirror, cudaStream_t) { return cudaSuccess; }
+inline cudaError_t mirror_cross(const float*, int64_t, Rows, int64_t, int64_t, int64_t, Mirror, cudaStream_t) {
+  return cudaSuccess;
+}
 cudaError_t pack_counters(const DetectCounters* c, const int* any, long long* v, cudaStream_t st);
 double microbench(int kind, void* buf, size_t bytes, cudaStream_t st);   // microbench.cu
 int num_sms();

@@ -21,6 +21,8 @@
 // each lane owns 8 vectors of every row of its slab, so vector operands that
 // are constant down a column (in-edges, the pivot row) live in registers and
 // every warp load instruction moves 512 contiguous bytes.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -234,6 +236,74 @@ static Tiling make_tiling(int64_t n, int64_t rows, int max_slabs, int chunk_vec 
 // Pass 2 can change row i only if col[i] < M[i]: a change at (i, j) needs
 // col[i] + out[t*] + D[t*][j] < D[i][j] <= D[i][t*] + D[t*][j] for the t* that
 // attains row[j], i.e. col[i] < D[i][t*] - out[t*] <= M[i].
+// ---------------------------------------------------------------------------
+// int16 mirror upkeep (kernels.h: struct Mirror)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mput(const Mirror& M, int64_t idx, int32_t v) {
+  M.m[idx] = sat16(v);
+  if (v >= kSat16i && v < APSP_INF_I32_DEV) *M.flag = 1u;   // not representable: mirror off
+}
+__device__ __forceinline__ void mput(const Mirror&, int64_t, float) {}
+
+// M := sat16(D) over the local rows' first n columns; *flag must be 0 on entry
+__global__ void k_mirror_build(const int32_t* __restrict__ D, int64_t ld, Rows r, int64_t n, Mirror M) {
+  const int64_t m = r.hi - r.lo, n4 = (n + 3) / 4;
+  const int64_t tot = m * n4;
+  bool bad = false;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t li = (r.lo - r.row0) + e / n4, c = 4 * (e % n4);
+    const int4 v = *reinterpret_cast<const int4*>(D + li * ld + c);
+    const int vv[4] = {v.x, v.y, v.z, v.w};
+    unsigned w[2] = {0, 0};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      bad |= c + q < n && vv[q] >= kSat16i && vv[q] < APSP_INF_I32_DEV;
+      w[q >> 1] |= (unsigned)sat16(vv[q]) << (16 * (q & 1));
+    }
+    *reinterpret_cast<uint2*>(M.m + li * ld + c) = make_uint2(w[0], w[1]);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *M.flag = 1u;
+}
+// M[i][j] := sat16(D[i][j]) for the listed pairs (the sparse recompute's writes)
+__global__ void k_mirror_pairs(const int32_t* __restrict__ D, int64_t ld, int64_t row0,
+                               const int* __restrict__ prow, const int* __restrict__ pcol,
+                               const DetectCounters* ctr, int64_t lcap, Mirror M) {
+  const int64_t np = min((int64_t)ctr->total, lcap);
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t idx = ((int64_t)prow[p] - row0) * ld + pcol[p];
+    mput(M, idx, D[idx]);
+  }
+}
+// M := sat16(D) on local row `row` (if local) and on column `col` (-1: none)
+__global__ void k_mirror_cross(const int32_t* __restrict__ D, int64_t ld, Rows r, int64_t n, int64_t row,
+                               int64_t col, Mirror M) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (row >= r.lo && row < r.hi)
+    for (int64_t j = tid; j < n; j += stride) mput(M, (row - r.row0) * ld + j, D[(row - r.row0) * ld + j]);
+  if (col >= 0)
+    for (int64_t i = r.lo + tid; i < r.hi; i += stride) mput(M, (i - r.row0) * ld + col, D[(i - r.row0) * ld + col]);
+}
+
+cudaError_t mirror_build(const int32_t* D, int64_t ld, Rows r, int64_t n, Mirror M, cudaStream_t st) {
+  if (r.hi <= r.lo) return cudaSuccess;
+  k_mirror_build<<<num_sms() * 8, 256, 0, st>>>(D, ld, r, n, M);
+  return cudaGetLastError();
+}
+cudaError_t mirror_pairs(const int32_t* D, int64_t ld, int64_t row0, const int* prow, const int* pcol,
+                         const DetectCounters* ctr, int64_t lcap, Mirror M, cudaStream_t st) {
+  k_mirror_pairs<<<num_sms() * 8, 256, 0, st>>>(D, ld, row0, prow, pcol, ctr, lcap, M);
+  return cudaGetLastError();
+}
+cudaError_t mirror_cross(const int32_t* D, int64_t ld, Rows r, int64_t n, int64_t row, int64_t col, Mirror M,
+                         cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>(cdiv(std::max<int64_t>(n, r.hi - r.lo), 256), 4 * num_sms());
+  k_mirror_cross<<<grid, 256, 0, st>>>(D, ld, r, n, row, col, M);
+  return cudaGetLastError();
+}
+
 constexpr int P1_V = 4;
 constexpr int P1_VEC = 32 * P1_V;   // 512 columns per chunk
 constexpr int P1_RB = 16;           // rows per shared-memory batch
@@ -252,7 +322,10 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
                                                           int64_t n, Tiling tl,
                                                           const T* __restrict__ ow,
                                                           const T* __restrict__ iw, T* rowpart,
-                                                          T* rowpartM, T* colpart, int64_t part_ld) {
+                                                          T* rowpartM, T* colpart, int64_t part_ld,
+                                                          Mirror M) {
+  const uint16_t* mm = M.m;
+  const bool m16 = mm != nullptr && *(volatile unsigned*)M.flag == 0u;
   __shared__ T rp_all[8][2][P1_RB][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   T (*rp)[33] = rp_all[warp][0];
@@ -272,7 +345,7 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
   const bool tail = (n & 3) != 0 && (int64_t)(chunk + 1) * P1_VEC >= tl.n4;
 #pragma unroll
   for (int v = 0; v < P1_V; ++v) {
-    qv[v] = (int64_t)chunk * P1_VEC + v * 32 + lane;
+    qv[v] = group_of(m16, chunk, v, lane);   // P1_VEC == 128: the 512-column chunk
     inw[v] = qv[v] < tl.n4 ? ld4<T>(iw + 4 * qv[v]) : Vec4<T>{I, I, I, I};
     Vec4<T> o = qv[v] < tl.n4 ? ld4<T>(ow + 4 * qv[v]) : Vec4<T>{I, I, I, I};
     // shortest path: -out[t] (an absent out-edge, INF, can never give a
@@ -282,22 +355,9 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
   }
   for (int64_t b0 = i_lo; b0 < i_hi; b0 += P1_RB) {
     const int nb = (int)min((int64_t)P1_RB, i_hi - b0);
-    for (int rr = 0; rr < nb; rr += 2) {
-      const bool two = rr + 1 < nb;
+    // rows b0 + rr and b0 + rr + 1 (if two): partials into rp / rm, column partials
+    auto body = [&](Vec4<T> (&d0)[P1_V], Vec4<T> (&d1)[P1_V], int rr, bool two) {
       const int64_t i = b0 + rr;
-      const T* row0 = D + (i - r.row0) * ld;
-      const T* row1 = row0 + ld;
-      Vec4<T> d0[P1_V], d1[P1_V];
-      // issue every load of both rows before touching any result (MLP = 2*P1_V)
-#pragma unroll
-      for (int v = 0; v < P1_V; ++v) {
-        d0[v] = Vec4<T>{I, I, I, I};
-        d1[v] = Vec4<T>{I, I, I, I};
-        if (qv[v] < tl.n4) {
-          d0[v] = ld4_stream<T>(row0 + 4 * qv[v]);
-          if (two) d1[v] = ld4_stream<T>(row1 + 4 * qv[v]);
-        }
-      }
       if (tail) {   // only the warp holding the row's last (partial) vector
 #pragma unroll
         for (int v = 0; v < P1_V; ++v) {
@@ -326,6 +386,56 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
       rp[rr][lane] = p0;
       rm[rr][lane] = m0;
       if (two) { rp[rr + 1][lane] = p1; rm[rr + 1][lane] = m1; }
+    };
+    if (m16) {
+      // the int16 mirror: 16-byte loads of 8 columns, four rows in flight
+      // (the same bytes in flight per lane as two int32 rows)
+      const uint4 sat = make_uint4(0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu);
+      for (int rr = 0; rr < nb; rr += 4) {
+        uint4 w[4][P1_V / 2];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const uint16_t* mrow = mm + (b0 + rr + h - r.row0) * ld;
+#pragma unroll
+          for (int q = 0; q < P1_V / 2; ++q)
+            w[h][q] = (rr + h < nb && qv[2 * q] < tl.n4) ? mload8(mrow + 4 * qv[2 * q]) : sat;
+        }
+#pragma unroll
+        for (int hh = 0; hh < 4; hh += 2) {
+          if (rr + hh < nb) {
+            Vec4<T> d0[P1_V], d1[P1_V];
+#pragma unroll
+            for (int q = 0; q < P1_V / 2; ++q) {
+              d0[2 * q] = mconv4<T>(make_uint2(w[hh][q].x, w[hh][q].y));
+              d0[2 * q + 1] = mconv4<T>(make_uint2(w[hh][q].z, w[hh][q].w));
+              d1[2 * q] = mconv4<T>(make_uint2(w[hh + 1][q].x, w[hh + 1][q].y));
+              d1[2 * q + 1] = mconv4<T>(make_uint2(w[hh + 1][q].z, w[hh + 1][q].w));
+            }
+#pragma unroll
+            for (int v = 0; v < P1_V; ++v)
+              if (qv[v] >= tl.n4) { d0[v] = Vec4<T>{I, I, I, I}; d1[v] = Vec4<T>{I, I, I, I}; }
+            body(d0, d1, rr + hh, rr + hh + 1 < nb);
+          }
+        }
+      }
+    } else {
+      for (int rr = 0; rr < nb; rr += 2) {
+        const bool two = rr + 1 < nb;
+        const T* row0 = D + (b0 + rr - r.row0) * ld;
+        const T* row1 = row0 + ld;
+        Vec4<T> d0[P1_V], d1[P1_V];
+        // issue every load of both rows before touching any result (MLP = 2*P1_V)
+#pragma unroll
+        for (int v = 0; v < P1_V; ++v) {
+          d0[v] = Vec4<T>{I, I, I, I};
+          d1[v] = Vec4<T>{I, I, I, I};
+          if (qv[v] < tl.n4) {
+            d0[v] = ld4_stream<T>(row0 + 4 * qv[v]);
+            if (two) d1[v] = ld4_stream<T>(row1 + 4 * qv[v]);
+          }
+        }
+        body(d0, d1, rr, two);
+      }
     }
     __syncwarp();
     {
@@ -354,7 +464,7 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
 template <typename T>
 cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow, const T* iw,
                           T* rowpart, T* rowpartM, T* colpart, int64_t part_ld, int* nchunk_out,
-                          int* nslab_out, int max_slabs, int sr, cudaStream_t st) {
+                          int* nslab_out, int max_slabs, int sr, Mirror M, cudaStream_t st) {
   Tiling tl = make_tiling(n, r.hi - r.lo, max_slabs, P1_VEC, 48);
   *nchunk_out = tl.nchunk;
   *nslab_out = tl.nslab;
@@ -367,10 +477,10 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
   int grid = (int)cdiv(tl.warps, 8);
   if (sr)
     k_addnode_pass1<T, 1><<<grid, 256, 0, st>>>(D, ld, r, n, tl, ow, iw, rowpart, rowpartM, colpart,
-                                                part_ld);
+                                                part_ld, M);
   else
     k_addnode_pass1<T, 0><<<grid, 256, 0, st>>>(D, ld, r, n, tl, ow, iw, rowpart, rowpartM, colpart,
-                                                part_ld);
+                                                part_ld, M);
   return cudaGetLastError();
 }
 
@@ -447,7 +557,8 @@ __global__ void __launch_bounds__(256) k_rank1(T* __restrict__ D, int64_t ld, Ro
                                                Tiling tl, const T* __restrict__ c,
                                                const T* __restrict__ rv, const T* __restrict__ c2,
                                                const T* __restrict__ rv2,
-                                               unsigned long long* __restrict__ bytes_read) {
+                                               unsigned long long* __restrict__ bytes_read,
+                                               Mirror M) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (gw >= tl.warps) return;
@@ -490,8 +601,13 @@ __global__ void __launch_bounds__(256) k_rank1(T* __restrict__ D, int64_t ld, Ro
         o.z = Tr<T, SR>::relax(o.z, ci2, b[v].z);
         o.w = Tr<T, SR>::relax(o.w, ci2, b[v].w);
       }
-      if (o.x != d[v].x || o.y != d[v].y || o.z != d[v].z || o.w != d[v].w)
+      if (o.x != d[v].x || o.y != d[v].y || o.z != d[v].z || o.w != d[v].w) {
         st4<T>(row + 4 * qv[v], o);
+        if (M.m) {
+          const int64_t idx = (i - r.row0) * ld + 4 * qv[v];
+          mput(M, idx, o.x); mput(M, idx + 1, o.y); mput(M, idx + 2, o.z); mput(M, idx + 3, o.w);
+        }
+      }
     }
   }
   if (bytes_read && lane == 0 && rows_read) {
@@ -501,18 +617,18 @@ __global__ void __launch_bounds__(256) k_rank1(T* __restrict__ D, int64_t ld, Ro
 }
 template <typename T>
 cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, const T* c2,
-                  const T* rv2, unsigned long long* bytes_read, int sr, cudaStream_t st) {
+                  const T* rv2, unsigned long long* bytes_read, int sr, Mirror M, cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
   Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20);
   int grid = (int)cdiv(tl.warps, 8);
   if (c2 && sr)
-    k_rank1<T, true, 1><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, c2, rv2, bytes_read);
+    k_rank1<T, true, 1><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, c2, rv2, bytes_read, M);
   else if (c2)
-    k_rank1<T, true, 0><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, c2, rv2, bytes_read);
+    k_rank1<T, true, 0><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, c2, rv2, bytes_read, M);
   else if (sr)
-    k_rank1<T, false, 1><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, nullptr, nullptr, bytes_read);
+    k_rank1<T, false, 1><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, nullptr, nullptr, bytes_read, M);
   else
-    k_rank1<T, false, 0><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, nullptr, nullptr, bytes_read);
+    k_rank1<T, false, 0><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, nullptr, nullptr, bytes_read, M);
   return cudaGetLastError();
 }
 
@@ -599,6 +715,7 @@ struct DetectOut {
   int* prow; int* pcol; T* plb; int64_t lcap;   // MODE 1: the (staging) list
   DetectCounters* ctr;       // MODE 1: total (list cursor), overflow
   const T* WT; int64_t ldw;  // MODE 2
+  Mirror M;                  // read instead of D while M.flag == 0 (modes 0, 1)
 };
 
 // MODE 1 staging: the hot loop only queues, per lane with flags, its 16-bit
@@ -609,11 +726,11 @@ struct DetectOut {
 constexpr int DS_Q = 256;   // queued lane words per warp (>= 32: one row always fits)
 struct DetectQueue {
   unsigned rl[DS_Q];        // (row - slab start) << 5 | lane
-  unsigned short w[DS_Q];   // flag word: bit v*4+c <-> column 4*(chunk*128 + v*32 + lane) + c
+  unsigned short w[DS_Q];   // flag word: bit v*4+c <-> column 4*group_of(m16, chunk, v, lane) + c
 };
 template <typename T>
 __device__ __forceinline__ void detect_flush(const DetectQueue& Q, int cnt, int64_t i_lo, int chunk,
-                                             const DetectOut<T>& o, int lane) {
+                                             bool m16, const DetectOut<T>& o, int lane) {
   if (cnt == 0) return;
   __syncwarp();
   // lane e takes queue entries e, e+32, ...: count its pairs, scan, one atomic
@@ -641,7 +758,7 @@ __device__ __forceinline__ void detect_flush(const DetectQueue& Q, int cnt, int6
     while (w) {
       const int bit = __ffs(w) - 1;
       w &= w - 1;
-      const int64_t j = 4 * ((int64_t)chunk * DS_VEC + (bit >> 2) * 32 + ln) + (bit & 3);
+      const int64_t j = 4 * group_of(m16, chunk, bit >> 2, ln) + (bit & 3);
       if (pos < o.lcap) {
         o.prow[pos] = (int)i;
         o.pcol[pos] = (int)j;   // D_old[i][j] (the lower bound) is read by the scatter
@@ -650,6 +767,15 @@ __device__ __forceinline__ void detect_flush(const DetectQueue& Q, int cnt, int6
     }
   }
   __syncwarp();
+}
+
+// Modes 0/1 of the shortest-path detection on an int32 D read the int16
+// mirror (k_detect_p16) while it is valid; decided on the device (the flag
+// is only known there), each of the two kernels exits when the other applies.
+template <typename T, int SR, int MODE>
+__device__ __forceinline__ bool detect_uses_mirror(const Mirror& M) {
+  return MODE != 2 && SR == 0 && std::is_same<T, int32_t>::value && M.m != nullptr &&
+         *(volatile unsigned*)M.flag == 0u;
 }
 
 template <typename T, bool TWO, int SR, int MODE>
@@ -664,6 +790,11 @@ __global__ void __launch_bounds__(256, 2) k_detect_stream(T* __restrict__ D, int
   const int lane = threadIdx.x & 31;
   DetectQueue& Q = sq[MODE == 1 ? (threadIdx.x >> 5) : 0];
   int qcnt = 0;   // MODE 1: queued lane words (warp-uniform)
+  // MODE 2 rewrites D in place, so it always reads D itself
+  // While the int16 mirror is valid, k_detect_p16 (launched next to this
+  // kernel) does the shortest-path detection on it and this kernel exits.
+  if (detect_uses_mirror<T, SR, MODE>(o.M)) return;
+  const bool m16 = false;
   const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (gw >= tl.warps) return;
   const int chunk = (int)(gw % tl.nchunk);
@@ -675,25 +806,13 @@ __global__ void __launch_bounds__(256, 2) k_detect_stream(T* __restrict__ D, int
   Vec4<T> a[DS_V], b[DS_V];
 #pragma unroll
   for (int v = 0; v < DS_V; ++v) {
-    qv[v] = (int64_t)chunk * DS_VEC + v * 32 + lane;
+    qv[v] = group_of(m16, chunk, v, lane);   // DS_VEC == 128: the 512-column chunk
     a[v] = qv[v] < tl.n4 ? ld4<T>(r1 + 4 * qv[v]) : Vec4<T>{I, I, I, I};
     if (TWO) b[v] = qv[v] < tl.n4 ? ld4<T>(r2 + 4 * qv[v]) : Vec4<T>{I, I, I, I};
   }
-  for (int64_t i0 = i_lo; i0 < i_hi; i0 += 2) {
-    // two rows in flight per lane; the row loads are issued first (their
-    // predicate needs no memory), the column snapshot c1[i] after them
-    bool act[2];
+  // rows i0, i0 + 1 (values in d, act = in range and not the skipped row)
+  auto process2 = [&](int64_t i0, Vec4<T> (&d)[2][DS_V], bool (&act)[2]) {
     T ci[2], cj[2];
-    Vec4<T> d[2][DS_V];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t i = i0 + h;
-      act[h] = i < i_hi && i != skip;
-      const T* row = D + (i - r.row0) * ld;
-#pragma unroll
-      for (int v = 0; v < DS_V; ++v)
-        d[h][v] = (act[h] && qv[v] < tl.n4) ? ld4_stream<T>(row + 4 * qv[v]) : Vec4<T>{I, I, I, I};
-    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int64_t i = i0 + h;
@@ -718,7 +837,7 @@ __global__ void __launch_bounds__(256, 2) k_detect_stream(T* __restrict__ D, int
         const int tot = __reduce_add_sync(0xffffffffu, (unsigned)__popc(word));
         if (lane == 0) atomicAdd(o.rowcnt + i, tot);
         if (qcnt + 32 > DS_Q) {
-          detect_flush<T>(Q, qcnt, i_lo, chunk, o, lane);
+          detect_flush<T>(Q, qcnt, i_lo, chunk, m16, o, lane);
           qcnt = 0;
         }
         const unsigned bal = __ballot_sync(0xffffffffu, word != 0);
@@ -740,8 +859,140 @@ __global__ void __launch_bounds__(256, 2) k_detect_stream(T* __restrict__ D, int
             }
       }
     }
-  }
-  if (MODE == 1) detect_flush<T>(Q, qcnt, i_lo, chunk, o, lane);
+  };
+    for (int64_t i0 = i_lo; i0 < i_hi; i0 += 2) {
+      // two rows in flight per lane; the row loads are issued first (their
+      // predicate needs no memory), the column snapshot c1[i] after them
+      bool act[2];
+      Vec4<T> d[2][DS_V];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t i = i0 + h;
+        act[h] = i < i_hi && i != skip;
+        const T* row = D + (i - r.row0) * ld;
+#pragma unroll
+        for (int v = 0; v < DS_V; ++v)
+          d[h][v] = (act[h] && qv[v] < tl.n4) ? ld4_stream<T>(row + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+      }
+      process2(i0, d, act);
+    }
+  if (MODE == 1) detect_flush<T>(Q, qcnt, i_lo, chunk, m16, o, lane);
+}
+
+// k_detect_stream on the int16 mirror in packed int16x2 arithmetic (modes 0
+// and 1, shortest path, int32 D).  A kernel of its own so that its smaller
+// register footprint gives 3 CTAs per SM: four rows of 16-byte loads in flight
+// per lane and 24 warps per SM keep the halved byte stream at HBM speed.
+template <typename T, bool TWO, int MODE>
+__global__ void __launch_bounds__(256, 3) k_detect_p16(T* __restrict__ D, int64_t ld, Rows r, int64_t n,
+                                                       int64_t skip, Tiling tl, const T* __restrict__ c1,
+                                                       const T* __restrict__ r1, const T* __restrict__ c2,
+                                                       const T* __restrict__ r2, float tau, DetectOut<T> o) {
+  if (!detect_uses_mirror<T, 0, MODE>(o.M)) return;
+  __shared__ DetectQueue sq[MODE == 1 ? 8 : 1];
+  const int lane = threadIdx.x & 31;
+  DetectQueue& Q = sq[MODE == 1 ? (threadIdx.x >> 5) : 0];
+  int qcnt = 0;   // MODE 1: queued lane words (warp-uniform)
+  const bool m16 = true;
+  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gw >= tl.warps) return;
+  const int chunk = (int)(gw % tl.nchunk);
+  const int slab = (int)(gw / tl.nchunk);
+  const int64_t i_lo = r.lo + slab * tl.slab;
+  const int64_t i_hi = min(r.hi, i_lo + tl.slab);
+  const T I = Tr<T>::inf();
+  int64_t qv[DS_V];
+#pragma unroll
+  for (int v = 0; v < DS_V; ++v) qv[v] = group_of(true, chunk, v, lane);
+    // The int16 mirror, tested in packed int16x2 arithmetic: D[i][j] is tight
+    // iff D[i][j] == c + r (c = D[i][k], r = D[k][j]).  Since D[i][j] <= c + r
+    // always holds, min(c + (r - 1), D[i][j]) differs from D[i][j] exactly for
+    // the tight entries: one VIADDMNMX.S16x2 and one LOP3 per two entries.
+    // Saturated operands (0x3FFF, i.e. INF) can only make c + r - 1 >= D, so
+    // they never flag except where r == 0 or c == 0 (j == k, i == k: filtered
+    // with the other validity tests).  Sums stay <= 32765: no overflow.
+    uint32_t rw[DS_V * 2], rw2[TWO ? DS_V * 2 : 1];
+#pragma unroll
+    for (int q = 0; q < DS_V * 2; ++q) {   // word q = columns 4*qv[q/2] + 2*(q&1) + {0,1}
+      const int64_t j0 = 4 * qv[q >> 1] + 2 * (q & 1);
+      auto sm1 = [&](const T* rv, int64_t j) -> uint32_t {   // sat16(r) - 1 (0xFFFF for r == 0)
+        return j < 4 * tl.n4 ? (uint32_t)((int)sat16((int32_t)rv[j]) - 1) & 0xFFFFu : 0x3FFEu;
+      };
+      rw[q] = sm1(r1, j0) | (sm1(r1, j0 + 1) << 16);
+      if (TWO) rw2[q] = sm1(r2, j0) | (sm1(r2, j0 + 1) << 16);
+    }
+    unsigned vmask = 0;   // this lane's columns with j < n and j != skip
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+      const int64_t j = 4 * qv[b >> 2] + (b & 3);
+      if (j < n && j != skip) vmask |= 1u << b;
+    }
+    const uint4 sat = make_uint4(0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu);
+    for (int64_t i0 = i_lo; i0 < i_hi; i0 += 4) {
+      uint4 w[4][DS_V / 2];
+      bool a4[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int64_t i = i0 + h;
+        a4[h] = i < i_hi && i != skip;
+        const uint16_t* mrow = o.M.m + (i - r.row0) * ld;
+#pragma unroll
+        for (int q = 0; q < DS_V / 2; ++q)
+          w[h][q] = (a4[h] && qv[2 * q] < tl.n4) ? mload8(mrow + 4 * qv[2 * q]) : sat;
+      }
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int64_t i = i0 + h;
+        const T ci = (i < i_hi) ? c1[i] : I;
+        const T cj = (TWO && i < i_hi) ? c2[i] : I;
+        const bool act = a4[h] && (Tr<T>::fin(ci) || Tr<T>::fin(cj));
+        const uint32_t cr = (uint32_t)sat16((int32_t)ci) * 0x10001u;
+        const uint32_t cr2 = TWO ? (uint32_t)sat16((int32_t)cj) * 0x10001u : 0u;
+        const uint32_t dw[DS_V * 2] = {w[h][0].x, w[h][0].y, w[h][0].z, w[h][0].w,
+                                       w[h][1].x, w[h][1].y, w[h][1].z, w[h][1].w};
+        uint32_t x[DS_V * 2], any = 0;
+#pragma unroll
+        for (int q = 0; q < DS_V * 2; ++q) {
+          x[q] = __viaddmin_s16x2(cr, rw[q], dw[q]) ^ dw[q];
+          if (TWO) x[q] |= __viaddmin_s16x2(cr2, rw2[q], dw[q]) ^ dw[q];
+          any |= x[q];
+        }
+        if (!__any_sync(0xffffffffu, act && any != 0)) continue;
+        // flag word: bit 2q+hf <-> half hf of word q nonzero (SWAR: bit 15 /
+        // 31 of t is set iff the half is nonzero), then the static validity
+        // mask (j < n, j != skip) and column i (the diagonal).  An entry with
+        // D == INF cannot flag here: D[i][j] <= c + r, so c, r finite forces
+        // D finite, and a saturated c or r only flags where r == 0 or c == 0.
+        unsigned word = 0;
+#pragma unroll
+        for (int q = 0; q < DS_V * 2; ++q) {
+          const uint32_t t = x[q] | ((x[q] & 0x7FFF7FFFu) + 0x7FFF7FFFu);
+          word |= (((t >> 15) & 1u) | ((t >> 30) & 2u)) << (2 * q);
+        }
+        word &= vmask;
+        if ((i >> 9) == chunk && ((i >> 3) & 31) == lane) word &= ~(1u << (((i >> 8) & 1) * 8 + (i & 7)));
+        if (!act) word = 0;
+        if (!__any_sync(0xffffffffu, word != 0)) continue;
+        if (MODE == 0) {
+          if (lane == 0) o.anyrow[i] = 1;
+        } else {
+          const int tot = __reduce_add_sync(0xffffffffu, (unsigned)__popc(word));
+          if (lane == 0) atomicAdd(o.rowcnt + i, tot);
+          if (qcnt + 32 > DS_Q) {
+            detect_flush<T>(Q, qcnt, i_lo, chunk, m16, o, lane);
+            qcnt = 0;
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, word != 0);
+          if (word) {
+            const int qp = qcnt + __popc(bal & ((1u << lane) - 1));
+            Q.rl[qp] = (unsigned)(i - i_lo) << 5 | (unsigned)lane;
+            Q.w[qp] = (unsigned short)word;
+          }
+          qcnt += __popc(bal);
+        }
+      }
+    }
+  if (MODE == 1) detect_flush<T>(Q, qcnt, i_lo, chunk, m16, o, lane);
 }
 
 // Per row of the list: rowoff[i] (a slice of rowcnt[i] slots for the row's
@@ -799,15 +1050,21 @@ template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
                    const T* c2, const T* r2, float tau, int mode, int* anyrow, int* rowcnt,
                    int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr, const T* WT,
-                   int64_t ldw, int sr, cudaStream_t st) {
+                   int64_t ldw, int sr, Mirror M, cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
   Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20, DS_VEC, 64);   // 64 warps/SM: 4 waves (measured best)
   if (tl.slab >= (1 << 26)) return cudaErrorInvalidValue;   // MODE-1 queue packing
   if (mode == 0) CUDA_TRY(cudaMemsetAsync(anyrow + r.lo, 0, sizeof(int) * (size_t)(r.hi - r.lo), st));
-  DetectOut<T> o{anyrow, rowcnt, prow, pcol, plb, lcap, ctr, WT, ldw};
+  DetectOut<T> o{anyrow, rowcnt, prow, pcol, plb, lcap, ctr, WT, ldw, M};
   const int g = (int)cdiv(tl.warps, 8);
 #define LAUNCH(TWO, SR, MODE)                                                                    \
-  k_detect_stream<T, TWO, SR, MODE><<<g, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, c2, r2, tau, o)
+  do {                                                                                           \
+    if (SR == 0 && MODE != 2 && M.m)                                                             \
+      k_detect_p16<T, TWO, (MODE == 2 ? 0 : MODE)><<<g, 256, 0, st>>>(D, ld, r, n, skip, tl, c1,  \
+                                                                       r1, c2, r2, tau, o);     \
+    k_detect_stream<T, TWO, SR, MODE><<<g, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, c2, r2,  \
+                                                         tau, o);                                \
+  } while (0)
 #define BY_MODE(TWO, SR)                 \
   if (mode == 0) LAUNCH(TWO, SR, 0);     \
   else if (mode == 1) LAUNCH(TWO, SR, 1); \
@@ -1004,16 +1261,18 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
   template cudaError_t gather_col<T>(const T*, int64_t, Rows, int64_t, T, T*, int, cudaStream_t);  \
   template cudaError_t copy_vec<T>(const T*, int64_t, int64_t, T, T*, cudaStream_t);               \
   template cudaError_t addnode_pass1<T>(const T*, int64_t, Rows, int64_t, const T*, const T*, T*,  \
-                                        T*, T*, int64_t, int*, int*, int, int, cudaStream_t);     \
+                                        T*, T*, int64_t, int*, int*, int, int, Mirror,            \
+                                        cudaStream_t);                                            \
   template cudaError_t addnode_finish<T>(const T*, const T*, int, const T*, int, int64_t, Rows,    \
                                          int64_t, int64_t, T*, T*, T*, cudaStream_t);             \
   template cudaError_t rank1<T>(T*, int64_t, Rows, int64_t, const T*, const T*, const T*,          \
-                                const T*, unsigned long long*, int, cudaStream_t);                \
+                                const T*, unsigned long long*, int, Mirror, cudaStream_t);        \
   template cudaError_t addnode_write<T>(T*, int64_t, Rows, int64_t, int64_t, int, const T*,        \
                                         const T*, T*, int64_t, const T*, const T*, cudaStream_t); \
   template cudaError_t detect<T>(T*, int64_t, Rows, int64_t, int64_t, const T*, const T*,          \
                                  const T*, const T*, float, int, int*, int*, int*, int*, T*,      \
-                                 int64_t, DetectCounters*, const T*, int64_t, int, cudaStream_t); \
+                                 int64_t, DetectCounters*, const T*, int64_t, int, Mirror,        \
+                                 cudaStream_t);                                                   \
   template cudaError_t detect_lists<T>(T*, int64_t, Rows, const T*, int64_t, const int*, int64_t*, \
                                        const int*, const int*, const T*, int*, int*, int*, T*,     \
                                        int64_t, DetectCounters*, cudaStream_t);                    \

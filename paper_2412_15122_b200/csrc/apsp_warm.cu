@@ -241,6 +241,7 @@ struct apsp_handle {
   }
   unsigned* fw16_flag() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 392); }
   unsigned* mirror_flag() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 396); }
+  unsigned* pass1_uncertain() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 400); }
   // int16 mirror of D (kernels.h): int32 handles only; lives in the packed-FW buffer
   template <typename T> Mirror mirror() {
     if constexpr (std::is_same<T, int32_t>::value) return Mirror{reinterpret_cast<uint16_t*>(p16()), mirror_flag()};
@@ -666,11 +667,26 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   int nchunk = 0, nslab = 0;
   T* rowpartM = h->rowpart<T>() + (size_t)h->plan.maxchunk * ld;
   T* ceff = h->vec<T>(4);
-  PK(APSP_K_ADD_PASS1, 4.0 * (double)(r.hi - r.lo) * (double)n,
+  // Pass 1: on the int16 mirror in packed arithmetic when it is valid
+  // (shortest path, int32), else — or if a new-row/column value came out
+  // >= 0x3FFF — in int32.  The choice is made on the device: each launch
+  // below exits when it does not apply (gate flags, stream order).
+  const bool try_packed = std::is_same<T, int32_t>::value && h->sr == 0;
+  unsigned* unc = h->pass1_uncertain();
+  if (try_packed) {
+    CKR(cudaMemsetAsync(unc, 0, sizeof(unsigned), h->st));
+    PK(APSP_K_ADD_PASS1, 2.0 * (double)(r.hi - r.lo) * (double)n,
+       addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
+                        &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), unc, 1, h->st));
+    CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
+                         ceff, row, 1, h->mirror<T>(), unc, h->st));
+  }
+  PK(APSP_K_ADD_PASS1, try_packed ? 0.0 : 4.0 * (double)(r.hi - r.lo) * (double)n,
      addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
-                      &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), h->st));
+                      &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), try_packed ? unc : nullptr, 0,
+                      h->st));
   CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
-                       ceff, row, h->st));
+                       ceff, row, try_packed ? 2 : 0, h->mirror<T>(), unc, h->st));
   if (h->world > 1)
     NK(h->comm->allreduce(row, (size_t)ld, nccl_type<T>(), ncclMin, h->st));
   // rows with ceff[i] = INF provably do not change and are not read at all

@@ -78,11 +78,13 @@ cudaError_t copy_vec(const T* src, int64_t n, int64_t npad, T add, T* out, cudaS
 template <typename T>
 cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow, const T* iw,
                           T* rowpart, T* rowpartM, T* colpart, int64_t part_ld, int* nchunk_out,
-                          int* nslab_out, int max_slabs, int sr, Mirror M, cudaStream_t st);
+                          int* nslab_out, int max_slabs, int sr, Mirror M, const unsigned* uncertain, int packed,
+                          cudaStream_t st);
 template <typename T>
 cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
                            int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,
-                           T* ceff, T* row, cudaStream_t st);
+                           T* ceff, T* row, int gate, Mirror M, unsigned* uncertain,
+                           cudaStream_t st);
 template <typename T>
 cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, const T* c2,
                   const T* rv2, unsigned long long* bytes_read, int sr, Mirror M, cudaStream_t st);

@@ -317,15 +317,153 @@ __device__ __forceinline__ T max_add(T m, T d, T w) {
   else if constexpr (Tr<T>::kFloat) return fmaxf(m, __fadd_rn(d, w));   // NaN (inf-inf) ignored
   else return max(m, d + w);                                            // |d + w| <= INF
 }
+// Add-node pass 1 on the int16 mirror in packed int16x2 arithmetic (shortest
+// path, int32 D, mirror valid).  Per lane 16 columns = 8 packed words; per word
+//   p    = min(p, D + in)          VIADDMNMX.S16x2   (new column, theo_2_back)
+//   colp = min(colp, out_i + D)    VIADDMNMX.S16x2   (new row, Theorem 2)
+//   m    = max(m, D - out)         VIADDMNMX.S16x2 (max form)   (row-skip bound)
+//   inf |= (D == INF) & (out finite)   VIMNMX.S16x2 + LOP3
+// All operands are saturated at 0x3FFF, so every partial below 0x3FFF is exact
+// and every other one is ">= 0x3FFF": the finish kernel flags the add
+// "uncertain" if a final new-row/column value is >= 0x3FFF, and the int32
+// pass then redoes it.  m is an upper bound of max(D - out) (a saturated out
+// only lowers D - out; a saturated D with a finite out sets inf -> no skip),
+// which keeps the row skip of pass 2 safe.
+template <typename T, int SR>
+__device__ __forceinline__ bool pass1_packed_done(const Mirror& M, const unsigned* uncertain) {
+  return SR == 0 && std::is_same<T, int32_t>::value && M.m != nullptr &&
+         *(volatile unsigned*)M.flag == 0u && (uncertain == nullptr || *(volatile unsigned*)uncertain == 0u);
+}
+template <typename T, int SR>
+__device__ __forceinline__ bool pass1_packed_runs(const Mirror& M) {
+  return SR == 0 && std::is_same<T, int32_t>::value && M.m != nullptr && *(volatile unsigned*)M.flag == 0u;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256, 2) k_addnode_pass1_p16(Rows r, int64_t ld, int64_t n, Tiling tl,
+                                                              const T* __restrict__ ow,
+                                                              const T* __restrict__ iw, T* rowpart,
+                                                              T* rowpartM, T* colpart, int64_t part_ld,
+                                                              Mirror M) {
+  if (!pass1_packed_runs<T, 0>(M)) return;
+  __shared__ T rp_all[8][2][P1_RB][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T (*rp)[33] = rp_all[warp][0];
+  T (*rm)[33] = rp_all[warp][1];
+  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
+  if (gw >= tl.warps) return;
+  const int chunk = (int)(gw % tl.nchunk);
+  const int slab = (int)(gw / tl.nchunk);
+  const int64_t i_lo = r.lo + slab * tl.slab;
+  const int64_t i_hi = min(r.hi, i_lo + tl.slab);
+  const T I = Tr<T>::inf();
+  constexpr uint32_t SAT2 = 0x3FFF3FFFu;
+  int64_t qv[P1_V];
+  // satnf: 0x3FFE where out is finite, 0x3FFF where it is not, so that
+  // min(D, satnf) != D exactly for a saturated D with a finite out
+  uint32_t in2[8], nout2[8], satnf[8], colp2[8];
+  const bool tail = (int64_t)(chunk + 1) * P1_VEC * 4 > n;   // chunk holds columns >= n
+#pragma unroll
+  for (int v = 0; v < P1_V; ++v) qv[v] = group_of(true, chunk, v, lane);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int64_t j0 = 4 * qv[q >> 1] + 2 * (q & 1);
+    uint32_t a = 0, b = 0, c = 0;
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      const int64_t j = j0 + hf;
+      const uint32_t iv = j < n ? (uint32_t)sat16((int32_t)iw[j]) : 0x3FFFu;
+      const uint32_t ov = j < n ? (uint32_t)sat16((int32_t)ow[j]) : 0x3FFFu;
+      a |= iv << (16 * hf);
+      b |= ((0x10000u - ov) & 0xFFFFu) << (16 * hf);   // -out as int16
+      c |= (ov < 0x3FFFu ? 0x3FFEu : 0x3FFFu) << (16 * hf);
+    }
+    in2[q] = a; nout2[q] = b; satnf[q] = c; colp2[q] = SAT2;
+  }
+  const uint4 sat = make_uint4(SAT2, SAT2, SAT2, SAT2);
+  for (int64_t b0 = i_lo; b0 < i_hi; b0 += P1_RB) {
+    const int nb = (int)min((int64_t)P1_RB, i_hi - b0);
+    for (int rr = 0; rr < nb; rr += 4) {
+      uint4 w[4][2];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const uint16_t* mrow = M.m + (b0 + rr + h - r.row0) * ld;
+#pragma unroll
+        for (int l = 0; l < 2; ++l)
+          w[h][l] = (rr + h < nb && qv[2 * l] < tl.n4) ? mload8(mrow + 4 * qv[2 * l]) : sat;
+      }
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        if (rr + h >= nb) break;
+        const int64_t i = b0 + rr + h;
+        const uint32_t orep = (uint32_t)sat16((int32_t)ow[i]) * 0x10001u;
+        uint32_t dw[8] = {w[h][0].x, w[h][0].y, w[h][0].z, w[h][0].w,
+                          w[h][1].x, w[h][1].y, w[h][1].z, w[h][1].w};
+        if (tail) {   // the row's last chunk: columns >= n hold no mirrored value
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int64_t j0 = 4 * qv[q >> 1] + 2 * (q & 1);
+            const uint32_t pm = (j0 < n ? 0u : 0xFFFFu) | (j0 + 1 < n ? 0u : 0xFFFF0000u);
+            dw[q] = (dw[q] & ~pm) | (SAT2 & pm);
+          }
+        }
+        uint32_t p2 = SAT2, m2 = 0xC001C001u /* -16383 */, inf = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          p2 = __viaddmin_s16x2(dw[q], in2[q], p2);
+          m2 = __viaddmax_s16x2(dw[q], nout2[q], m2);
+          inf |= __vmins2(dw[q], satnf[q]) ^ dw[q];
+          colp2[q] = __viaddmin_s16x2(orep, dw[q], colp2[q]);
+        }
+        const int pl = (int)min(p2 & 0xFFFFu, p2 >> 16);   // >= 0x3FFF: ">= SAT"
+        const int ml = max((int)(short)(m2 & 0xFFFFu), (int)(short)(m2 >> 16));
+        rp[rr + h][lane] = (T)pl;
+        rm[rr + h][lane] = inf ? I : (T)ml;
+      }
+    }
+    __syncwarp();
+    {
+      const int row = lane & (P1_RB - 1);
+      if (row < nb) {
+        if (lane < P1_RB) {
+          T m = rp[row][0];
+#pragma unroll 8
+          for (int t = 1; t < 32; ++t) m = Tr<T>::mn(m, rp[row][t]);
+          rowpart[(int64_t)chunk * part_ld + b0 + row] = m;
+        } else {
+          T m = rm[row][0];
+#pragma unroll 8
+          for (int t = 1; t < 32; ++t) m = max(m, rm[row][t]);
+          rowpartM[(int64_t)chunk * part_ld + b0 + row] = m;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // column partials of the new row, as int32 (>= 0x3FFF kept as 0x3FFF: ">= SAT")
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int64_t j0 = 4 * qv[q >> 1] + 2 * (q & 1);
+    if (j0 < 4 * tl.n4) {
+      T* dst = colpart + (int64_t)slab * part_ld + j0;
+      dst[0] = (T)(colp2[q] & 0xFFFFu);
+      dst[1] = (T)(colp2[q] >> 16);
+    }
+  }
+}
+
 template <typename T, int SR>
 __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ D, int64_t ld, Rows r,
                                                           int64_t n, Tiling tl,
                                                           const T* __restrict__ ow,
                                                           const T* __restrict__ iw, T* rowpart,
                                                           T* rowpartM, T* colpart, int64_t part_ld,
-                                                          Mirror M) {
-  const uint16_t* mm = M.m;
-  const bool m16 = mm != nullptr && *(volatile unsigned*)M.flag == 0u;
+                                                          Mirror M, const unsigned* uncertain) {
+  // The packed pass (k_addnode_pass1_p16) handled this add unless the mirror
+  // is invalid, the algebra is minimax, or a result came out >= 0x3FFF.
+  if (pass1_packed_done<T, SR>(M, uncertain)) return;
+  const uint16_t* mm = nullptr;
+  const bool m16 = false;
   __shared__ T rp_all[8][2][P1_RB][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   T (*rp)[33] = rp_all[warp][0];
@@ -464,7 +602,8 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
 template <typename T>
 cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow, const T* iw,
                           T* rowpart, T* rowpartM, T* colpart, int64_t part_ld, int* nchunk_out,
-                          int* nslab_out, int max_slabs, int sr, Mirror M, cudaStream_t st) {
+                          int* nslab_out, int max_slabs, int sr, Mirror M, const unsigned* uncertain,
+                          int packed, cudaStream_t st) {
   Tiling tl = make_tiling(n, r.hi - r.lo, max_slabs, P1_VEC, 48);
   *nchunk_out = tl.nchunk;
   *nslab_out = tl.nslab;
@@ -477,10 +616,13 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
   int grid = (int)cdiv(tl.warps, 8);
   if (sr)
     k_addnode_pass1<T, 1><<<grid, 256, 0, st>>>(D, ld, r, n, tl, ow, iw, rowpart, rowpartM, colpart,
-                                                part_ld, M);
-  else
+                                                part_ld, M, uncertain);
+  else if (packed)   // on the mirror (exits unless it is valid)
+    k_addnode_pass1_p16<T><<<grid, 256, 0, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
+                                                 part_ld, M);
+  else   // int32 (exits if the packed pass ran and came out certain)
     k_addnode_pass1<T, 0><<<grid, 256, 0, st>>>(D, ld, r, n, tl, ow, iw, rowpart, rowpartM, colpart,
-                                                part_ld, M);
+                                                part_ld, M, uncertain);
   return cudaGetLastError();
 }
 
@@ -488,12 +630,18 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
 // row[j] over the nslab row slabs.  CTA = 8 warps x 32 consecutive indices:
 // warp g reduces partials g, g+8, ... (coalesced 128-byte rows of the
 // partial arrays), then the 8 warp results meet in shared memory.
+// gate 0: always; 1: only after the packed pass ran (mirror valid) — then a
+// new-row/column value >= 0x3FFF sets *uncertain; 2: only if the packed pass
+// did not run or was uncertain.
 template <typename T>
 __global__ void __launch_bounds__(256) k_addnode_finish(const T* rowpart, const T* rowpartM,
                                                         int nchunk, const T* colpart, int nslab,
                                                         int64_t part_ld, Rows r, int64_t n,
                                                         int64_t npad, int64_t ntile_i, T* col,
-                                                        T* ceff, T* row) {
+                                                        T* ceff, T* row, int gate, Mirror M,
+                                                        unsigned* uncertain) {
+  if (gate == 1 && !pass1_packed_runs<T, 0>(M)) return;
+  if (gate == 2 && pass1_packed_done<T, 0>(M, uncertain)) return;
   __shared__ T sm[8][32], sM[8][32];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   if (blockIdx.x < ntile_i) {
@@ -516,6 +664,7 @@ __global__ void __launch_bounds__(256) k_addnode_finish(const T* rowpart, const 
         M = Tr<T>::kFloat ? fmaxf(M, sM[q][lane]) : max(M, sM[q][lane]);
       }
       m = Tr<T>::sat(m);
+      if (gate == 1 && m >= (T)kSat16i) *uncertain = 1u;
       col[i] = m;
       // pass 2 may skip row i unless col[i] < M[i] (fp32: with a relative
       // margin, so rounding in d - out can only keep rows, never drop them)
@@ -534,6 +683,7 @@ __global__ void __launch_bounds__(256) k_addnode_finish(const T* rowpart, const 
     if (g == 0 && j < npad) {
 #pragma unroll
       for (int q = 1; q < 8; ++q) m = Tr<T>::mn(m, sm[q][lane]);
+      if (gate == 1 && j < n && m >= (T)kSat16i) *uncertain = 1u;
       row[j] = Tr<T>::sat(m);
     }
   }
@@ -541,11 +691,12 @@ __global__ void __launch_bounds__(256) k_addnode_finish(const T* rowpart, const 
 template <typename T>
 cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
                            int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,
-                           T* ceff, T* row, cudaStream_t st) {
+                           T* ceff, T* row, int gate, Mirror M, unsigned* uncertain, cudaStream_t st) {
   const int64_t ti = cdiv(std::max<int64_t>(r.hi - r.lo, 0), 32), tj = cdiv(npad, 32);
   if (ti + tj == 0) return cudaSuccess;
   k_addnode_finish<T><<<(unsigned)(ti + tj), 256, 0, st>>>(rowpart, rowpartM, nchunk, colpart, nslab,
-                                                           part_ld, r, n, npad, ti, col, ceff, row);
+                                                           part_ld, r, n, npad, ti, col, ceff, row,
+                                                           gate, M, uncertain);
   return cudaGetLastError();
 }
 
@@ -1262,9 +1413,10 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
   template cudaError_t copy_vec<T>(const T*, int64_t, int64_t, T, T*, cudaStream_t);               \
   template cudaError_t addnode_pass1<T>(const T*, int64_t, Rows, int64_t, const T*, const T*, T*,  \
                                         T*, T*, int64_t, int*, int*, int, int, Mirror,            \
-                                        cudaStream_t);                                            \
+                                        const unsigned*, int, cudaStream_t);                      \
   template cudaError_t addnode_finish<T>(const T*, const T*, int, const T*, int, int64_t, Rows,    \
-                                         int64_t, int64_t, T*, T*, T*, cudaStream_t);             \
+                                         int64_t, int64_t, T*, T*, T*, int, Mirror, unsigned*,    \
+                                         cudaStream_t);                                           \
   template cudaError_t rank1<T>(T*, int64_t, Rows, int64_t, const T*, const T*, const T*,          \
                                 const T*, unsigned long long*, int, Mirror, cudaStream_t);        \
   template cudaError_t addnode_write<T>(T*, int64_t, Rows, int64_t, int64_t, int, const T*,        \

@@ -176,6 +176,14 @@ apsp_status apsp_destroy(apsp_handle* h);
 
 apsp_status apsp_set_option(apsp_handle* h, apsp_option opt, double value);
 
+/* D was written by the caller (a warm start from a known APSP matrix):
+ * re-derive the library's internal image of it (the int16 mirror the O(n^2)
+ * passes read on int32 handles).  Optional — the first update
+ * that needs it does it otherwise, inside that update's time.  Asynchronous.
+ * D must not be modified by the caller after an update call without calling
+ * this (or apsp_cold_fw) again. */
+apsp_status apsp_sync_distances(apsp_handle* h);
+
 /* Cold start: D := APSP(W) by tiled blocked Floyd–Warshall (the comparator of
  * P:74/P:93/P:224).  Asynchronous. */
 apsp_status apsp_cold_fw(apsp_handle* h);

@@ -29,6 +29,7 @@ SYMBOLS = [
     "apsp_nccl_unique_id", "apsp_kernel_launches", "apsp_profile_enable", "apsp_profile_reset",
     "apsp_profile_read", "apsp_modify_edge_readd", "apsp_get_weight",
     "apsp_local_group_create", "apsp_local_group_destroy", "apsp_create_local", "apsp_microbench",
+    "apsp_sync_distances",
 ]
 # kernel classes of apsp_profile_read (apsp_kernel_class)
 K_CLASSES = ["fw_diag", "fw_panel", "fw_tile", "add_pass1", "rank1", "detect", "sparse0",
@@ -74,6 +75,7 @@ def _load():
         "apsp_destroy": (ctypes.c_int, [vp]),
         "apsp_set_option": (ctypes.c_int, [vp, ctypes.c_int, dbl]),
         "apsp_cold_fw": (ctypes.c_int, [vp]),
+        "apsp_sync_distances": (ctypes.c_int, [vp]),
         "apsp_add_node": (ctypes.c_int, [vp, vp, vp, P(i64), P(UpdateInfo)]),
         "apsp_remove_node": (ctypes.c_int, [vp, i64, P(i64), P(UpdateInfo)]),
         "apsp_update_edge": (ctypes.c_int, [vp, i64, i64, dbl, P(UpdateInfo)]),
@@ -161,6 +163,10 @@ def apsp_destroy(h):
 
 def apsp_set_option(h, opt, value):
     check(h, lib.apsp_set_option(h, opt, float(value)))
+
+
+def apsp_sync_distances(h):
+    check(h, lib.apsp_sync_distances(h))
 
 
 def apsp_cold_fw(h):

@@ -81,6 +81,12 @@ class WarmAPSP:
         Dfull = torch.as_tensor(Dfull)
         lo, hi = min(self.row0, n), min(self.row0 + self.rows, n)
         self.D_local[: hi - lo, :n].copy_(Dfull[lo:hi, :n])
+        self.sync_distances()
+
+    def sync_distances(self):
+        """D_local was written directly: let the library re-derive its image of it."""
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        L.apsp_sync_distances(self.h)
 
     def close(self):
         if getattr(self, "h", None):

@@ -766,10 +766,6 @@ apsp_status remove_node_impl(apsp_handle* h, int64_t k, int64_t* moved_from, aps
 // ------------------------------------------------------------------ update edge
 template <typename T>
 apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp_update_info* info) {
-  {
-    apsp_status ms = ensure_mirror<T>(h);
-    if (ms != APSP_OK) return ms;
-  }
   const int64_t n = h->n, ld = h->ld;
   T* WT = h->WT<T>();
   // 8-byte read: W[u][v] (replicated WT) and D[u][v] (owner of row u)
@@ -843,6 +839,10 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
   // W' (WT and the shortlists) before the D0 reset
   CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
   CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
+  {   // the detection pass reads the int16 mirror (early exits and decreases do not)
+    apsp_status ms = ensure_mirror<T>(h);
+    if (ms != APSP_OK) return ms;
+  }
   return recompute<T>(h, -1, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, false, info);
 }
 
@@ -1247,6 +1247,11 @@ apsp_status apsp_set_option(apsp_handle* h, apsp_option opt, double value) {
       return APSP_OK;
   }
   return APSP_E_INVAL;
+}
+
+apsp_status apsp_sync_distances(apsp_handle* h) {
+  CHECK_HANDLE(h);
+  return dispatch(h->dt, [&](auto z) { return mirror_rebuild<decltype(z)>(h); });
 }
 
 apsp_status apsp_cold_fw(apsp_handle* h) {

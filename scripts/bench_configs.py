@@ -54,6 +54,7 @@ def emit(cfg, what, ms_list, n, extra=None):
 def fresh(W, directed, D0, cap=None):
     h = P.WarmAPSP(torch.from_numpy(W), directed=directed, cap=cap, cold_start=False)
     h.D_local[: D0.shape[0], : D0.shape[1]].copy_(D0)
+    h.sync_distances()   # warm start: not part of the timed update
     return h
 
 

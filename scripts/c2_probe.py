@@ -27,6 +27,7 @@ for rep in range(4):
     h.close()
     h = P.WarmAPSP(torch.from_numpy(W), directed=False, cold_start=False)
     h.D_local.copy_(D0)
+    h.sync_distances()
     torch.cuda.synchronize()
     L.apsp_profile_enable(h.h, rep == 3)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

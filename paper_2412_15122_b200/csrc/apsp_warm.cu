@@ -373,14 +373,15 @@ template <typename T>
 apsp_status fw_impl_elem(apsp_handle* h);
 
 // (Re)build the int16 mirror from D: at the first update of a handle whose D
-// the caller filled (warm start), and after an int32 FW.  Mirror flag = 0 iff
-// every finite distance is < 0x3FFF (on every rank).
+// the caller filled (warm start), and after an int32 FW.  Mirror flag bit 0
+// set iff some finite local distance is >= 0x3FFF, bit 1 iff some local entry
+// is INF (stream.cu: kMirrorOff, kMirrorInf).
 template <typename T>
 apsp_status mirror_rebuild(apsp_handle* h) {
   if constexpr (std::is_same<T, int32_t>::value) {
     CKR(cudaMemsetAsync(h->mirror_flag(), 0, sizeof(unsigned), h->st));
+    // per rank: each rank's readers stream only its own rows
     CK(mirror_build(h->Dl<int32_t>(), h->ld, h->active(), h->n, h->mirror<int32_t>(), h->st));
-    if (h->world > 1) NK(h->comm->allreduce(h->mirror_flag(), 1, ncclUint32, ncclMax, h->st));
   }
   h->mirror_built = true;
   return APSP_OK;
@@ -754,9 +755,13 @@ apsp_status remove_node_impl(apsp_handle* h, int64_t k, int64_t* moved_from, aps
   Rows rw{0, n, 0};
   CK(fill_col<T>(WT, ld, rw, last, I, h->st));
   CK(shortlist_remove<T>(h->slid(), h->slw<T>(), h->wnext<T>(), n, k, last, h->st));
-  // the int16 mirror of the rows / columns the tombstone and the move rewrote
-  CK(mirror_cross(h->Dl<T>(), ld, r, n, k, k, h->mirror<T>(), h->st));
-  if (k != last) CK(mirror_cross(h->Dl<T>(), ld, r, n, last, last, h->mirror<T>(), h->st));
+  // the int16 mirror of row / column k (the tombstone and the move rewrote
+  // them); slot `last` is no longer active (a later add re-derives it)
+  if (k != last) {
+    Rows ra = r;
+    ra.hi = std::min(ra.hi, last);
+    CK(mirror_cross(h->Dl<T>(), ld, ra, last, k, k, h->mirror<T>(), h->st));
+  }
   h->n = n - 1;
   if (moved_from) *moved_from = (k != last) ? last : -1;
   if (info) info->n_after = h->n;

@@ -239,52 +239,70 @@ static Tiling make_tiling(int64_t n, int64_t rows, int max_slabs, int chunk_vec 
 // ---------------------------------------------------------------------------
 // int16 mirror upkeep (kernels.h: struct Mirror)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void mput(const Mirror& M, int64_t idx, int32_t v) {
+// Mirror flag bits: kMirrorOff — some finite distance is >= 0x3FFF (M is not
+// an exact image of D); kMirrorInf — some active entry is INF (readers then
+// need their INF tests).  mput returns the bits the write raises; callers OR
+// them per thread and post them once per warp (mirror_post).
+constexpr unsigned kMirrorOff = 1u, kMirrorInf = 2u;
+__device__ __forceinline__ unsigned mput(const Mirror& M, int64_t idx, int32_t v) {
   M.m[idx] = sat16(v);
-  if (v >= kSat16i && v < APSP_INF_I32_DEV) *M.flag = 1u;   // not representable: mirror off
+  return v >= APSP_INF_I32_DEV ? kMirrorInf : (v >= kSat16i ? kMirrorOff : 0u);
 }
-__device__ __forceinline__ void mput(const Mirror&, int64_t, float) {}
+__device__ __forceinline__ unsigned mput(const Mirror&, int64_t, float) { return 0u; }
+__device__ __forceinline__ void mirror_post(const Mirror& M, unsigned bits) {
+  bits = __reduce_or_sync(0xffffffffu, bits);
+  if ((threadIdx.x & 31) == 0 && bits && (bits & ~*(volatile unsigned*)M.flag)) atomicOr(M.flag, bits);
+}
 
 // M := sat16(D) over the local rows' first n columns; *flag must be 0 on entry
 __global__ void k_mirror_build(const int32_t* __restrict__ D, int64_t ld, Rows r, int64_t n, Mirror M) {
   const int64_t m = r.hi - r.lo, n4 = (n + 3) / 4;
   const int64_t tot = m * n4;
-  bool bad = false;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
-       e += (int64_t)gridDim.x * blockDim.x) {
+  unsigned bits = 0;
+  for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x; e0 < tot; e0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = e0 + threadIdx.x;
+    if (e >= tot) continue;
     const int64_t li = (r.lo - r.row0) + e / n4, c = 4 * (e % n4);
     const int4 v = *reinterpret_cast<const int4*>(D + li * ld + c);
     const int vv[4] = {v.x, v.y, v.z, v.w};
     unsigned w[2] = {0, 0};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      bad |= c + q < n && vv[q] >= kSat16i && vv[q] < APSP_INF_I32_DEV;
+      if (c + q < n)
+        bits |= vv[q] >= APSP_INF_I32_DEV ? kMirrorInf : (vv[q] >= kSat16i ? kMirrorOff : 0u);
       w[q >> 1] |= (unsigned)sat16(vv[q]) << (16 * (q & 1));
     }
     *reinterpret_cast<uint2*>(M.m + li * ld + c) = make_uint2(w[0], w[1]);
   }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *M.flag = 1u;
+  mirror_post(M, bits);
 }
 // M[i][j] := sat16(D[i][j]) for the listed pairs (the sparse recompute's writes)
 __global__ void k_mirror_pairs(const int32_t* __restrict__ D, int64_t ld, int64_t row0,
                                const int* __restrict__ prow, const int* __restrict__ pcol,
                                const DetectCounters* ctr, int64_t lcap, Mirror M) {
   const int64_t np = min((int64_t)ctr->total, lcap);
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t idx = ((int64_t)prow[p] - row0) * ld + pcol[p];
-    mput(M, idx, D[idx]);
+  unsigned bits = 0;
+  for (int64_t p0 = blockIdx.x * (int64_t)blockDim.x; p0 < np; p0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = p0 + threadIdx.x;
+    if (p < np) {
+      const int64_t idx = ((int64_t)prow[p] - row0) * ld + pcol[p];
+      bits |= mput(M, idx, D[idx]);
+    }
   }
+  mirror_post(M, bits);
 }
 // M := sat16(D) on local row `row` (if local) and on column `col` (-1: none)
 __global__ void k_mirror_cross(const int32_t* __restrict__ D, int64_t ld, Rows r, int64_t n, int64_t row,
                                int64_t col, Mirror M) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned bits = 0;
   if (row >= r.lo && row < r.hi)
-    for (int64_t j = tid; j < n; j += stride) mput(M, (row - r.row0) * ld + j, D[(row - r.row0) * ld + j]);
+    for (int64_t j = tid; j < n; j += stride) bits |= mput(M, (row - r.row0) * ld + j, D[(row - r.row0) * ld + j]);
   if (col >= 0)
-    for (int64_t i = r.lo + tid; i < r.hi; i += stride) mput(M, (i - r.row0) * ld + col, D[(i - r.row0) * ld + col]);
+    for (int64_t i = r.lo + tid; i < r.hi; i += stride)
+      if (i != col) bits |= mput(M, (i - r.row0) * ld + col, D[(i - r.row0) * ld + col]);
+  mirror_post(M, bits);
 }
 
 cudaError_t mirror_build(const int32_t* D, int64_t ld, Rows r, int64_t n, Mirror M, cudaStream_t st) {
@@ -332,11 +350,13 @@ __device__ __forceinline__ T max_add(T m, T d, T w) {
 template <typename T, int SR>
 __device__ __forceinline__ bool pass1_packed_done(const Mirror& M, const unsigned* uncertain) {
   return SR == 0 && std::is_same<T, int32_t>::value && M.m != nullptr &&
-         *(volatile unsigned*)M.flag == 0u && (uncertain == nullptr || *(volatile unsigned*)uncertain == 0u);
+         (*(volatile unsigned*)M.flag & kMirrorOff) == 0u &&
+         (uncertain == nullptr || *(volatile unsigned*)uncertain == 0u);
 }
 template <typename T, int SR>
 __device__ __forceinline__ bool pass1_packed_runs(const Mirror& M) {
-  return SR == 0 && std::is_same<T, int32_t>::value && M.m != nullptr && *(volatile unsigned*)M.flag == 0u;
+  return SR == 0 && std::is_same<T, int32_t>::value && M.m != nullptr &&
+         (*(volatile unsigned*)M.flag & kMirrorOff) == 0u;
 }
 
 template <typename T>
@@ -346,6 +366,7 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1_p16(Rows r, int64_t ld
                                                               T* rowpartM, T* colpart, int64_t part_ld,
                                                               Mirror M) {
   if (!pass1_packed_runs<T, 0>(M)) return;
+  const bool has_inf = (*(volatile unsigned*)M.flag & kMirrorInf) != 0u;
   __shared__ T rp_all[8][2][P1_RB][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   T (*rp)[33] = rp_all[warp][0];
@@ -408,12 +429,21 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1_p16(Rows r, int64_t ld
           }
         }
         uint32_t p2 = SAT2, m2 = 0xC001C001u /* -16383 */, inf = 0;
+        if (has_inf) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          p2 = __viaddmin_s16x2(dw[q], in2[q], p2);
-          m2 = __viaddmax_s16x2(dw[q], nout2[q], m2);
-          inf |= __vmins2(dw[q], satnf[q]) ^ dw[q];
-          colp2[q] = __viaddmin_s16x2(orep, dw[q], colp2[q]);
+          for (int q = 0; q < 8; ++q) {
+            p2 = __viaddmin_s16x2(dw[q], in2[q], p2);
+            m2 = __viaddmax_s16x2(dw[q], nout2[q], m2);
+            inf |= __vmins2(dw[q], satnf[q]) ^ dw[q];
+            colp2[q] = __viaddmin_s16x2(orep, dw[q], colp2[q]);
+          }
+        } else {   // no INF among the active entries (the common dense case)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            p2 = __viaddmin_s16x2(dw[q], in2[q], p2);
+            m2 = __viaddmax_s16x2(dw[q], nout2[q], m2);
+            colp2[q] = __viaddmin_s16x2(orep, dw[q], colp2[q]);
+          }
         }
         const int pl = (int)min(p2 & 0xFFFFu, p2 >> 16);   // >= 0x3FFF: ">= SAT"
         const int ml = max((int)(short)(m2 & 0xFFFFu), (int)(short)(m2 >> 16));
@@ -728,6 +758,7 @@ __global__ void __launch_bounds__(256) k_rank1(T* __restrict__ D, int64_t ld, Ro
     if (TWO) b[v] = qv[v] < tl.n4 ? ld4<T>(rv2 + 4 * qv[v]) : Vec4<T>{I, I, I, I};
   }
   int64_t rows_read = 0;
+  unsigned mbits = 0;
   for (int64_t i = i_lo; i < i_hi; ++i) {
     const T ci = c[i];
     const T ci2 = TWO ? c2[i] : I;
@@ -756,11 +787,12 @@ __global__ void __launch_bounds__(256) k_rank1(T* __restrict__ D, int64_t ld, Ro
         st4<T>(row + 4 * qv[v], o);
         if (M.m) {
           const int64_t idx = (i - r.row0) * ld + 4 * qv[v];
-          mput(M, idx, o.x); mput(M, idx + 1, o.y); mput(M, idx + 2, o.z); mput(M, idx + 3, o.w);
+          mbits |= mput(M, idx, o.x) | mput(M, idx + 1, o.y) | mput(M, idx + 2, o.z) | mput(M, idx + 3, o.w);
         }
       }
     }
   }
+  if (M.m) mirror_post(M, mbits);
   if (bytes_read && lane == 0 && rows_read) {
     const int64_t cols = min((int64_t)CHUNK_VEC * 4, n - (int64_t)chunk * CHUNK_VEC * 4);
     atomicAdd(bytes_read, (unsigned long long)(rows_read * cols * (int64_t)sizeof(T)));
@@ -926,7 +958,7 @@ __device__ __forceinline__ void detect_flush(const DetectQueue& Q, int cnt, int6
 template <typename T, int SR, int MODE>
 __device__ __forceinline__ bool detect_uses_mirror(const Mirror& M) {
   return MODE != 2 && SR == 0 && std::is_same<T, int32_t>::value && M.m != nullptr &&
-         *(volatile unsigned*)M.flag == 0u;
+         (*(volatile unsigned*)M.flag & kMirrorOff) == 0u;
 }
 
 template <typename T, bool TWO, int SR, int MODE>

@@ -145,6 +145,11 @@ struct apsp_handle {
   int fw16 = 1;                  // int16x2 FW when exact (int32 shortest path, one GPU)
   int last_fw16 = 0;             // 1: the last FW ran packed, 2: it fell back to int32
   bool mirror_built = false;     // the int16 mirror was built (or invalidated) from D
+  bool mirror_hint = false;      // last observed mirror state was "valid" (profile accounting only)
+  // bytes per entry the O(n^2) streams read: 2 on the valid int16 mirror, else 4
+  template <typename T> double stream_bytes() const {
+    return (std::is_same<T, int32_t>::value && sr == 0 && mirror_hint) ? 2.0 : 4.0;
+  }
   double row_delta = 0.0;        // > 0: the paper's Definition-1 gate (ablation)
   int sr = 0;                    // path algebra: 0 shortest path, 1 minimax
   // state
@@ -382,6 +387,7 @@ apsp_status mirror_rebuild(apsp_handle* h) {
     CKR(cudaMemsetAsync(h->mirror_flag(), 0, sizeof(unsigned), h->st));
     // per rank: each rank's readers stream only its own rows
     CK(mirror_build(h->Dl<int32_t>(), h->ld, h->active(), h->n, h->mirror<int32_t>(), h->st));
+    h->mirror_hint = true;   // corrected at the next host read of the flag
   }
   h->mirror_built = true;
   return APSP_OK;
@@ -454,6 +460,7 @@ apsp_status fw_impl(apsp_handle* h, int64_t skip = -1) {
       if (!saturated) {   // the packed buffer now holds sat16(D): the mirror is valid
         CKR(cudaMemsetAsync(h->mirror_flag(), 0, sizeof(unsigned), h->st));
         h->mirror_built = true;
+        h->mirror_hint = true;
         return APSP_OK;
       }
       // some distance is >= 0x3FFF or infinite: finish in int32 (exact from any
@@ -519,7 +526,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   CKR(cudaMemsetAsync(h->ocnt(), 0, sizeof(int) * h->cap, h->st));   // scatter cursors
   // one streaming pass appends the need_update_list; then per-row slices,
   // Phi / max|A_i|, the row grouping and the D0 reset (W'[i][j])
-  PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
+  PK(APSP_K_DETECT, h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n,
      detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, 1, nullptr, h->rowcnt(),
                h->srow(), h->scol(), h->slb<T>(), lcap, h->ctr(), h->WT<T>(), h->ld, h->sr,
                h->mirror<T>(), h->st));
@@ -584,7 +591,10 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   }
   long long* hv = reinterpret_cast<long long*>(h->host_small);
   CKR(cudaMemcpyAsync(hv, v, 6 * sizeof(long long), cudaMemcpyDeviceToHost, h->st));
+  unsigned* hmf = reinterpret_cast<unsigned*>(h->host_small) + 16;
+  CKR(cudaMemcpyAsync(hmf, h->mirror_flag(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
   CKR(cudaStreamSynchronize(h->st));
+  h->mirror_hint = (*hmf & 1u) == 0u;
   const int64_t total = hv[0], rows = hv[1], maxrow = hv[5];
   const bool overflow = hv[2] != 0 || hv[3] != 0;   // a list overflowed on some rank
   bool changed = hv[4] != 0;
@@ -650,7 +660,9 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   unsigned* herr = reinterpret_cast<unsigned*>(h->host_small);
   CKR(cudaMemcpyAsync(herr, &h->ctr()->err, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
   CKR(cudaMemcpyAsync(herr + 1, h->wmin_dev(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+  CKR(cudaMemcpyAsync(herr + 2, h->mirror_flag(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
   CKR(cudaStreamSynchronize(h->st));
+  h->mirror_hint = (herr[2] & 1u) == 0u;
   if (*herr) {
     return fail(h, APSP_E_INVAL, "add_node: %s",
                 (*herr & 2) ? "undirected graph needs out_w == in_w" : "negative or NaN weight");
@@ -676,13 +688,13 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   unsigned* unc = h->pass1_uncertain();
   if (try_packed) {
     CKR(cudaMemsetAsync(unc, 0, sizeof(unsigned), h->st));
-    PK(APSP_K_ADD_PASS1, 2.0 * (double)(r.hi - r.lo) * (double)n,
+    PK(APSP_K_ADD_PASS1, h->mirror_hint ? 2.0 * (double)(r.hi - r.lo) * (double)n : 0.0,
        addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
                         &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), unc, 1, h->st));
     CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
                          ceff, row, 1, h->mirror<T>(), unc, h->st));
   }
-  PK(APSP_K_ADD_PASS1, try_packed ? 0.0 : 4.0 * (double)(r.hi - r.lo) * (double)n,
+  PK(APSP_K_ADD_PASS1, try_packed && h->mirror_hint ? 0.0 : 4.0 * (double)(r.hi - r.lo) * (double)n,
      addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
                       &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), try_packed ? unc : nullptr, 0,
                       h->st));
@@ -863,7 +875,7 @@ apsp_status removal_phi(apsp_handle* h, int64_t k, int64_t* phi) {
   CK(gather_col<T>(h->Dl<T>(), ld, r, k, T(0), c1, h->sr, h->st));
   apsp_status s = snap_row<T>(h, k, T(0), r1);
   if (s != APSP_OK) return s;
-  PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
+  PK(APSP_K_DETECT, h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n,
      detect<T>(h->Dl<T>(), ld, r, n, k, c1, r1, nullptr, nullptr, h->tau, 0, h->anyrow(), nullptr,
                nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0, h->sr, h->mirror<T>(), h->st));
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(h->small() + 128);

@@ -367,16 +367,13 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1_p16(Rows r, int64_t ld
                                                               Mirror M) {
   if (!pass1_packed_runs<T, 0>(M)) return;
   const bool has_inf = (*(volatile unsigned*)M.flag & kMirrorInf) != 0u;
-  __shared__ T rp_all[8][2][P1_RB][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  T (*rp)[33] = rp_all[warp][0];
-  T (*rm)[33] = rp_all[warp][1];
   const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
   if (gw >= tl.warps) return;
   const int chunk = (int)(gw % tl.nchunk);
   const int slab = (int)(gw / tl.nchunk);
   const int64_t i_lo = r.lo + slab * tl.slab;
-  const int64_t i_hi = min(r.hi, i_lo + tl.slab);
+  const int rows = (int)max((int64_t)0, min(r.hi, i_lo + tl.slab) - i_lo);
   const T I = Tr<T>::inf();
   constexpr uint32_t SAT2 = 0x3FFF3FFFu;
   int64_t qv[P1_V];
@@ -401,74 +398,63 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1_p16(Rows r, int64_t ld
     }
     in2[q] = a; nout2[q] = b; satnf[q] = c; colp2[q] = SAT2;
   }
+  // this lane's two 16-byte column groups of row i_lo; rows are ld apart
+  const bool ok0 = qv[0] < tl.n4, ok1 = qv[2] < tl.n4;
+  const uint16_t* m0 = M.m + (i_lo - r.row0) * ld + 4 * qv[0];
+  const uint16_t* m1 = M.m + (i_lo - r.row0) * ld + 4 * qv[2];
+  const T* owr = ow + i_lo;
+  T* rp_out = rowpart + (int64_t)chunk * part_ld + i_lo;
+  T* rm_out = rowpartM + (int64_t)chunk * part_ld + i_lo;
   const uint4 sat = make_uint4(SAT2, SAT2, SAT2, SAT2);
-  for (int64_t b0 = i_lo; b0 < i_hi; b0 += P1_RB) {
-    const int nb = (int)min((int64_t)P1_RB, i_hi - b0);
-    for (int rr = 0; rr < nb; rr += 4) {
-      uint4 w[4][2];
+  for (int rr = 0; rr < rows; rr += 4) {
+    uint4 w[4][2];
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const uint16_t* mrow = M.m + (b0 + rr + h - r.row0) * ld;
+    for (int h = 0; h < 4; ++h) {
+      const bool in = rr + h < rows;
+      w[h][0] = (in && ok0) ? mload8(m0 + (int64_t)(rr + h) * ld) : sat;
+      w[h][1] = (in && ok1) ? mload8(m1 + (int64_t)(rr + h) * ld) : sat;
+    }
 #pragma unroll
-        for (int l = 0; l < 2; ++l)
-          w[h][l] = (rr + h < nb && qv[2 * l] < tl.n4) ? mload8(mrow + 4 * qv[2 * l]) : sat;
+    for (int h = 0; h < 4; ++h) {
+      if (rr + h >= rows) break;
+      const uint32_t orep = (uint32_t)sat16((int32_t)owr[rr + h]) * 0x10001u;
+      uint32_t dw[8] = {w[h][0].x, w[h][0].y, w[h][0].z, w[h][0].w,
+                        w[h][1].x, w[h][1].y, w[h][1].z, w[h][1].w};
+      if (tail) {   // the row's last chunk: columns >= n hold no mirrored value
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int64_t j0 = 4 * qv[q >> 1] + 2 * (q & 1);
+          const uint32_t pm = (j0 < n ? 0u : 0xFFFFu) | (j0 + 1 < n ? 0u : 0xFFFF0000u);
+          dw[q] = (dw[q] & ~pm) | (SAT2 & pm);
+        }
       }
+      uint32_t p2 = SAT2, m2 = 0xC001C001u /* -16383 */, inf = 0;
+      if (has_inf) {
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        if (rr + h >= nb) break;
-        const int64_t i = b0 + rr + h;
-        const uint32_t orep = (uint32_t)sat16((int32_t)ow[i]) * 0x10001u;
-        uint32_t dw[8] = {w[h][0].x, w[h][0].y, w[h][0].z, w[h][0].w,
-                          w[h][1].x, w[h][1].y, w[h][1].z, w[h][1].w};
-        if (tail) {   // the row's last chunk: columns >= n hold no mirrored value
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int64_t j0 = 4 * qv[q >> 1] + 2 * (q & 1);
-            const uint32_t pm = (j0 < n ? 0u : 0xFFFFu) | (j0 + 1 < n ? 0u : 0xFFFF0000u);
-            dw[q] = (dw[q] & ~pm) | (SAT2 & pm);
-          }
+        for (int q = 0; q < 8; ++q) {
+          p2 = __viaddmin_s16x2(dw[q], in2[q], p2);
+          m2 = __viaddmax_s16x2(dw[q], nout2[q], m2);
+          inf |= __vmins2(dw[q], satnf[q]) ^ dw[q];
+          colp2[q] = __viaddmin_s16x2(orep, dw[q], colp2[q]);
         }
-        uint32_t p2 = SAT2, m2 = 0xC001C001u /* -16383 */, inf = 0;
-        if (has_inf) {
+      } else {   // no INF among the active entries (the common dense case)
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            p2 = __viaddmin_s16x2(dw[q], in2[q], p2);
-            m2 = __viaddmax_s16x2(dw[q], nout2[q], m2);
-            inf |= __vmins2(dw[q], satnf[q]) ^ dw[q];
-            colp2[q] = __viaddmin_s16x2(orep, dw[q], colp2[q]);
-          }
-        } else {   // no INF among the active entries (the common dense case)
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            p2 = __viaddmin_s16x2(dw[q], in2[q], p2);
-            m2 = __viaddmax_s16x2(dw[q], nout2[q], m2);
-            colp2[q] = __viaddmin_s16x2(orep, dw[q], colp2[q]);
-          }
+        for (int q = 0; q < 8; ++q) {
+          p2 = __viaddmin_s16x2(dw[q], in2[q], p2);
+          m2 = __viaddmax_s16x2(dw[q], nout2[q], m2);
+          colp2[q] = __viaddmin_s16x2(orep, dw[q], colp2[q]);
         }
-        const int pl = (int)min(p2 & 0xFFFFu, p2 >> 16);   // >= 0x3FFF: ">= SAT"
-        const int ml = max((int)(short)(m2 & 0xFFFFu), (int)(short)(m2 >> 16));
-        rp[rr + h][lane] = (T)pl;
-        rm[rr + h][lane] = inf ? I : (T)ml;
+      }
+      // row reductions over the warp: one REDUX each (>= 0x3FFF: ">= SAT")
+      const int pl = (int)min(p2 & 0xFFFFu, p2 >> 16);
+      const int ml = inf ? (int)I : max((int)(short)(m2 & 0xFFFFu), (int)(short)(m2 >> 16));
+      const int pr = (int)__reduce_min_sync(0xffffffffu, (unsigned)pl);
+      const int mr = __reduce_max_sync(0xffffffffu, ml);
+      if (lane == 0) {
+        rp_out[rr + h] = (T)pr;
+        rm_out[rr + h] = (T)mr;
       }
     }
-    __syncwarp();
-    {
-      const int row = lane & (P1_RB - 1);
-      if (row < nb) {
-        if (lane < P1_RB) {
-          T m = rp[row][0];
-#pragma unroll 8
-          for (int t = 1; t < 32; ++t) m = Tr<T>::mn(m, rp[row][t]);
-          rowpart[(int64_t)chunk * part_ld + b0 + row] = m;
-        } else {
-          T m = rm[row][0];
-#pragma unroll 8
-          for (int t = 1; t < 32; ++t) m = max(m, rm[row][t]);
-          rowpartM[(int64_t)chunk * part_ld + b0 + row] = m;
-        }
-      }
-    }
-    __syncwarp();
   }
   // column partials of the new row, as int32 (>= 0x3FFF kept as 0x3FFF: ">= SAT")
 #pragma unroll
@@ -1111,36 +1097,39 @@ __global__ void __launch_bounds__(256, 3) k_detect_p16(T* __restrict__ D, int64_
       if (j < n && j != skip) vmask |= 1u << b;
     }
     const uint4 sat = make_uint4(0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu);
-    for (int64_t i0 = i_lo; i0 < i_hi; i0 += 4) {
+    const int rows = (int)max((int64_t)0, i_hi - i_lo);
+    const bool ok0 = qv[0] < tl.n4, ok1 = qv[2] < tl.n4;
+    const uint16_t* mb0 = o.M.m + (i_lo - r.row0) * ld + 4 * qv[0];
+    const uint16_t* mb1 = o.M.m + (i_lo - r.row0) * ld + 4 * qv[2];
+    const int rskip = (skip >= i_lo && skip < i_hi) ? (int)(skip - i_lo) : -1;
+    // column i of row i (the diagonal) in this lane's bits, per row: i >> 9 is
+    // the chunk, (i >> 3) & 31 the lane, ((i >> 8) & 1) * 8 + (i & 7) the bit
+    for (int rr = 0; rr < rows; rr += 4) {
       uint4 w[4][DS_V / 2];
-      bool a4[4];
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
-        const int64_t i = i0 + h;
-        a4[h] = i < i_hi && i != skip;
-        const uint16_t* mrow = o.M.m + (i - r.row0) * ld;
-#pragma unroll
-        for (int q = 0; q < DS_V / 2; ++q)
-          w[h][q] = (a4[h] && qv[2 * q] < tl.n4) ? mload8(mrow + 4 * qv[2 * q]) : sat;
+        const bool in = rr + h < rows && rr + h != rskip;
+        w[h][0] = (in && ok0) ? mload8(mb0 + (int64_t)(rr + h) * ld) : sat;
+        w[h][1] = (in && ok1) ? mload8(mb1 + (int64_t)(rr + h) * ld) : sat;
       }
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
-        const int64_t i = i0 + h;
-        const T ci = (i < i_hi) ? c1[i] : I;
-        const T cj = (TWO && i < i_hi) ? c2[i] : I;
-        const bool act = a4[h] && (Tr<T>::fin(ci) || Tr<T>::fin(cj));
+        if (rr + h >= rows) break;
+        const T ci = c1[i_lo + rr + h];
+        const T cj = TWO ? c2[i_lo + rr + h] : I;
+        const bool act = rr + h != rskip && (Tr<T>::fin(ci) || Tr<T>::fin(cj));
         const uint32_t cr = (uint32_t)sat16((int32_t)ci) * 0x10001u;
         const uint32_t cr2 = TWO ? (uint32_t)sat16((int32_t)cj) * 0x10001u : 0u;
         const uint32_t dw[DS_V * 2] = {w[h][0].x, w[h][0].y, w[h][0].z, w[h][0].w,
                                        w[h][1].x, w[h][1].y, w[h][1].z, w[h][1].w};
-        uint32_t x[DS_V * 2], any = 0;
+        uint32_t any = 0;
 #pragma unroll
         for (int q = 0; q < DS_V * 2; ++q) {
-          x[q] = __viaddmin_s16x2(cr, rw[q], dw[q]) ^ dw[q];
-          if (TWO) x[q] |= __viaddmin_s16x2(cr2, rw2[q], dw[q]) ^ dw[q];
-          any |= x[q];
+          any |= __viaddmin_s16x2(cr, rw[q], dw[q]) ^ dw[q];
+          if (TWO) any |= __viaddmin_s16x2(cr2, rw2[q], dw[q]) ^ dw[q];
         }
         if (!__any_sync(0xffffffffu, act && any != 0)) continue;
+        const int64_t i = i_lo + rr + h;
         // flag word: bit 2q+hf <-> half hf of word q nonzero (SWAR: bit 15 /
         // 31 of t is set iff the half is nonzero), then the static validity
         // mask (j < n, j != skip) and column i (the diagonal).  An entry with
@@ -1149,7 +1138,9 @@ __global__ void __launch_bounds__(256, 3) k_detect_p16(T* __restrict__ D, int64_
         unsigned word = 0;
 #pragma unroll
         for (int q = 0; q < DS_V * 2; ++q) {
-          const uint32_t t = x[q] | ((x[q] & 0x7FFF7FFFu) + 0x7FFF7FFFu);
+          uint32_t x = __viaddmin_s16x2(cr, rw[q], dw[q]) ^ dw[q];
+          if (TWO) x |= __viaddmin_s16x2(cr2, rw2[q], dw[q]) ^ dw[q];
+          const uint32_t t = x | ((x & 0x7FFF7FFFu) + 0x7FFF7FFFu);
           word |= (((t >> 15) & 1u) | ((t >> 30) & 2u)) << (2 * q);
         }
         word &= vmask;

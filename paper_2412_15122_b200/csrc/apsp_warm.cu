@@ -742,38 +742,19 @@ apsp_status remove_node_impl(apsp_handle* h, int64_t k, int64_t* moved_from, aps
 
   // swap-with-last: node n-1 moves into slot k (Q7)
   const int64_t last = n - 1;
-  T* WT = h->WT<T>();
-  const T I = Tr<T>::inf();
+  int row_copy = 0;
   if (k != last) {
     const bool ok_k = h->local(k), ok_l = h->local(last);
     if (ok_k && ok_l) {
-      CK(copy_row<T>(h->Drow<T>(k), h->Drow<T>(last), n, h->st));
-    } else if (ok_k || ok_l) {
+      row_copy = 1;
+    } else if (ok_k || ok_l) {   // the row crosses ranks: it arrives in row k first
       P2POp op = ok_l ? P2POp{1, h->Drow<T>(last), (size_t)n, nccl_type<T>(), h->owner(k)}
                       : P2POp{0, h->Drow<T>(k), (size_t)n, nccl_type<T>(), h->owner(last)};
       NK(h->comm->sendrecv(&op, 1, h->st));
     }
-    CK(copy_row<T>(WT + k * ld, WT + last * ld, n, h->st));
-    Rows rc = r;     // rows [lo, hi) with hi <= n: includes the new row k, excludes row last
-    rc.hi = std::min(rc.hi, last);
-    CK(copy_col<T>(h->Dl<T>(), ld, rc, k, last, h->st));
-    Rows rw{0, last, 0};
-    CK(copy_col<T>(WT, ld, rw, k, last, h->st));
   }
-  // clear the vacated slot n-1
-  if (h->local(last)) CK(fill<T>(h->Drow<T>(last), n, I, h->st));
-  CK(fill_col<T>(h->Dl<T>(), ld, r, last, I, h->st));
-  CK(fill<T>(WT + last * ld, n, I, h->st));
-  Rows rw{0, n, 0};
-  CK(fill_col<T>(WT, ld, rw, last, I, h->st));
+  CK(move_last<T>(h->Dl<T>(), ld, r, n, k, row_copy, h->WT<T>(), ld, h->mirror<T>(), h->st));
   CK(shortlist_remove<T>(h->slid(), h->slw<T>(), h->wnext<T>(), n, k, last, h->st));
-  // the int16 mirror of row / column k (the tombstone and the move rewrote
-  // them); slot `last` is no longer active (a later add re-derives it)
-  if (k != last) {
-    Rows ra = r;
-    ra.hi = std::min(ra.hi, last);
-    CK(mirror_cross(h->Dl<T>(), ld, ra, last, k, k, h->mirror<T>(), h->st));
-  }
   h->n = n - 1;
   if (moved_from) *moved_from = (k != last) ? last : -1;
   if (info) info->n_after = h->n;

@@ -109,6 +109,12 @@ cudaError_t tombstone(T* D, int64_t ld, Rows r, int64_t n, int64_t k, T* WT, int
                       cudaStream_t st);
 template <typename T>
 cudaError_t copy_row(T* dst, const T* src, int64_t n, cudaStream_t st);
+// swap-with-last after a removal: node n-1 into slot k of D (local rows r) and
+// WT, slot n-1 cleared, the mirror of row / column k re-derived.  row_copy = 0
+// when row n-1 lives on another rank (it was exchanged into row k already).
+template <typename T>
+cudaError_t move_last(T* D, int64_t ld, Rows r, int64_t n, int64_t k, int row_copy, T* WT, int64_t ldw,
+                      Mirror M, cudaStream_t st);
 template <typename T>
 cudaError_t copy_col(T* D, int64_t ld, Rows r, int64_t dst_col, int64_t src_col, cudaStream_t st);
 template <typename T>

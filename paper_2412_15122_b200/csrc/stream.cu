@@ -1295,6 +1295,69 @@ cudaError_t tombstone(T* D, int64_t ld, Rows r, int64_t n, int64_t k, T* WT, int
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// swap-with-last after a removal (Q7), two launches instead of nine:
+// node `last` moves into slot k of D (local rows r) and of WT (all rows).
+// Copy: row k := row last (if both local; else the row already arrived by a
+// point-to-point exchange), column k := column last for the other rows,
+// D[k][k] = WT[k][k] = 0.  Reads (row / column last) and writes (row / column
+// k) are disjoint, so one launch suffices.  Clear: row / column last := INF,
+// then the int16 mirror of row / column k is re-derived.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_move_last_copy(T* D, int64_t ld, Rows r, int64_t k, int64_t last, int row_copy, T* WT,
+                                 int64_t ldw) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool kl = k >= r.lo && k < r.hi;
+  for (int64_t j = tid; j < last; j += stride) {
+    if (j == k) continue;
+    if (row_copy) D[(k - r.row0) * ld + j] = D[(last - r.row0) * ld + j];
+    WT[k * ldw + j] = WT[last * ldw + j];
+    WT[j * ldw + k] = WT[j * ldw + last];
+  }
+  for (int64_t i = r.lo + tid; i < min(r.hi, last); i += stride)
+    if (i != k) D[(i - r.row0) * ld + k] = D[(i - r.row0) * ld + last];
+  if (tid == 0) {
+    if (kl) D[(k - r.row0) * ld + k] = T(0);
+    WT[k * ldw + k] = T(0);
+  }
+}
+template <typename T>
+__global__ void k_move_last_clear(T* D, int64_t ld, Rows r, int64_t k, int64_t last, int64_t n, T* WT,
+                                  int64_t ldw, Mirror M) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const T I = Tr<T>::inf();
+  if (last >= r.lo && last < r.hi)
+    for (int64_t j = tid; j < n; j += stride) D[(last - r.row0) * ld + j] = I;
+  for (int64_t i = r.lo + tid; i < r.hi; i += stride) D[(i - r.row0) * ld + last] = I;
+  for (int64_t j = tid; j < n; j += stride) {
+    WT[last * ldw + j] = I;
+    WT[j * ldw + last] = I;
+  }
+  if (M.m && k != last) {   // the mirror of row / column k over the remaining nodes [0, last)
+    unsigned bits = 0;
+    if (k >= r.lo && k < r.hi)
+      for (int64_t j = tid; j < last; j += stride) bits |= mput(M, (k - r.row0) * ld + j, D[(k - r.row0) * ld + j]);
+    for (int64_t i = r.lo + tid; i < min(r.hi, last); i += stride)
+      if (i != k) bits |= mput(M, (i - r.row0) * ld + k, D[(i - r.row0) * ld + k]);
+    mirror_post(M, bits);
+  }
+}
+template <typename T>
+cudaError_t move_last(T* D, int64_t ld, Rows r, int64_t n, int64_t k, int row_copy, T* WT, int64_t ldw,
+                      Mirror M, cudaStream_t st) {
+  const int64_t last = n - 1;
+  const int grid = (int)std::min<int64_t>(cdiv(n, 256), 4 * num_sms());
+  if (k != last) {
+    k_move_last_copy<T><<<grid, 256, 0, st>>>(D, ld, r, k, last, row_copy, WT, ldw);
+    CUDA_TRY(cudaGetLastError());
+  }
+  k_move_last_clear<T><<<grid, 256, 0, st>>>(D, ld, r, k, last, n, WT, ldw, M);
+  return cudaGetLastError();
+}
+
 template <typename T>
 __global__ void k_copy_row(T* dst, const T* src, int64_t n) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
@@ -1454,6 +1517,8 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
   template cudaError_t tombstone<T>(T*, int64_t, Rows, int64_t, int64_t, T*, int64_t,              \
                                     cudaStream_t);                                                \
   template cudaError_t copy_row<T>(T*, const T*, int64_t, cudaStream_t);                           \
+  template cudaError_t move_last<T>(T*, int64_t, Rows, int64_t, int64_t, int, T*, int64_t, Mirror,  \
+                                    cudaStream_t);                                                \
   template cudaError_t copy_col<T>(T*, int64_t, Rows, int64_t, int64_t, cudaStream_t);             \
   template cudaError_t fill_col<T>(T*, int64_t, Rows, int64_t, T, cudaStream_t);                   \
   template cudaError_t set_edge<T>(T*, int64_t, int64_t, int64_t, T, int, cudaStream_t);        \

@@ -33,6 +33,72 @@ static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // ---------------------------------------------------------------------------
 // shortlists: lane-local top-kSLK in-edges of node j (kSL = 32 * kSLK entries)
 // ---------------------------------------------------------------------------
+// Sort SL(j) ascending by weight (dead entries carry INF and sink to the end):
+// a warp-level bitonic network on the 512 entries in place in global memory
+// (__syncwarp orders the warp's accesses between stages).  Phase A then finds
+// the cheapest in-edges — the likeliest last hops of a tie — in the first
+// positions.  Runs at build and after every insertion / weight refresh.
+template <typename T>
+__device__ void sl_sort_warp(int* sid, T* sw) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  for (int k = 2; k <= kSL; k <<= 1)
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+#pragma unroll 4
+      for (int t = 0; t < kSL / 32; ++t) {
+        const int i = t * 32 + lane, l = i ^ jj;
+        if (l > i) {
+          const T a = sw[i], b = sw[l];
+          const bool up = (i & k) == 0;
+          if ((a > b) == up && a != b) {
+            const int ia = sid[i], ib = sid[l];
+            sw[i] = b; sw[l] = a;
+            sid[i] = ib; sid[l] = ia;
+          }
+        }
+      }
+      __syncwarp();
+    }
+}
+
+// Replace slot `bq` of a sorted SL(j) by (m, w) keeping the live entries in
+// ascending order (dead entries — INF — may sit anywhere): p = the first live
+// entry heavier than w; the entries between p and bq shift by one.  One warp,
+// two passes over the 512 entries (a full re-sort per insertion was too heavy
+// for the add-node side stream).
+template <typename T>
+__device__ void sl_place_warp(int* sid, T* sw, int bq, int m, T w) {
+  const int lane = threadIdx.x & 31;
+  int p = kSL;
+#pragma unroll 4
+  for (int t = 0; t < kSL / 32; ++t) {
+    const int e = t * 32 + lane;
+    if (e != bq && sid[e] >= 0 && sw[e] > w) p = min(p, e);
+  }
+  p = __reduce_min_sync(0xffffffffu, p);
+  // target slot of (m, w): before p if p <= bq (shift [p, bq) right), else
+  // just before p after shifting (bq, p) left; p == kSL means "at the end"
+  const int lo = p <= bq ? p : bq + 1, hi = p <= bq ? bq : p;   // moved range [lo, hi)
+  const int dst = p <= bq ? p : p - 1;
+  const int dir = p <= bq ? 1 : -1;
+  int ids[kSL / 32];
+  T ws[kSL / 32];
+#pragma unroll
+  for (int t = 0; t < kSL / 32; ++t) {
+    const int e = t * 32 + lane;
+    if (e >= lo && e < hi) { ids[t] = sid[e]; ws[t] = sw[e]; }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < kSL / 32; ++t) {
+    const int e = t * 32 + lane;
+    if (e >= lo && e < hi) { sid[e + dir] = ids[t]; sw[e + dir] = ws[t]; }
+  }
+  __syncwarp();
+  if (lane == 0) { sid[dst] = m; sw[dst] = w; }
+  __syncwarp();
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_shortlist_build(const T* __restrict__ WT, int64_t ldw,
                                                          int64_t n, const int* rows, int64_t r0,
@@ -77,6 +143,7 @@ __global__ void __launch_bounds__(256) k_shortlist_build(const T* __restrict__ W
       oid[q * 32 + lane] = bi[q];
       ow[q * 32 + lane] = bw[q];
     }
+    sl_sort_warp<T>(oid, ow);
     rej = warp_min<T>(rej);
     if (lane == 0) wnext[j] = rej;
   }
@@ -153,6 +220,7 @@ __global__ void __launch_bounds__(256) k_shortlist_build_one(const T* __restrict
     oid[q * 32 + lane] = bi[q];
     ow[q * 32 + lane] = bw[q];
   }
+  sl_sort_warp<T>(oid, ow);
   rej = warp_min<T>(rej);
   if (lane == 0) {
     for (int w = 0; w < 8; ++w) rej = Tr<T>::mn(rej, srej[w]);
@@ -192,14 +260,11 @@ __device__ __forceinline__ void shortlist_insert_warp(int* SLid, T* SLw, T* wnex
     const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
     if (ob > best || (ob == best && oq < bq)) { best = ob; bq = oq; }
   }
-  if (lane == 0) {
-    if (w < best) {
-      if (sid[bq] >= 0) wnext[j] = Tr<T>::mn(wnext[j], best);
-      sid[bq] = m;
-      sw[bq] = w;
-    } else {
-      wnext[j] = Tr<T>::mn(wnext[j], w);
-    }
+  if (w < best) {   // warp-uniform (best is the warp's): evict slot bq
+    if (lane == 0 && sid[bq] >= 0) wnext[j] = Tr<T>::mn(wnext[j], best);
+    sl_place_warp<T>(sid, sw, bq, m, w);
+  } else if (lane == 0) {
+    wnext[j] = Tr<T>::mn(wnext[j], w);
   }
 }
 
@@ -223,14 +288,15 @@ cudaError_t shortlist_add_bound(int* SLid, T* SLw, T* wnext, const T* out_w, int
 template <typename T>
 __global__ void k_shortlist_set_edge(int* SLid, T* SLw, T* wnext, int64_t u, int64_t v, T w) {
   const int lane = threadIdx.x & 31;
-  bool found = false;
+  int at = -1;
 #pragma unroll
   for (int q = 0; q < kSLK; ++q) {
-    const int64_t e = v * kSL + q * 32 + lane;
-    if (SLid[e] == (int)u) { SLw[e] = w; found = true; }
+    const int e = q * 32 + lane;
+    if (SLid[v * kSL + e] == (int)u) at = e;
   }
-  found = __any_sync(0xffffffffu, found);
-  if (!found) shortlist_insert_warp<T>(SLid, SLw, wnext, v, (int)u, w);
+  at = __reduce_max_sync(0xffffffffu, at);
+  if (at >= 0) sl_place_warp<T>(SLid + v * kSL, SLw + v * kSL, at, (int)u, w);   // re-place the entry
+  else shortlist_insert_warp<T>(SLid, SLw, wnext, v, (int)u, w);
 }
 template <typename T>
 cudaError_t shortlist_set_edge(int* SLid, T* SLw, T* wnext, int64_t u, int64_t v, T w,
@@ -351,7 +417,7 @@ cudaError_t shortlist_swap(int* SLid, T* SLw, T* wnext, int64_t n, int64_t p, in
 // of other pairs of the row are then visible, so a class-1 value is the
 // exact min of (*) over every m whose value can no longer change.
 // ---------------------------------------------------------------------------
-constexpr int kPhaseASteps = 3;   // phase A: at most 3 x 32 shortlist entries per pair
+constexpr int kPhaseASteps = 3;   // phase A: sorted shortlist positions 0-7, 8-39, 40-71
 
 // Pair counts live on the device (the host reads them once per update, after
 // the sparse recompute): which = 0, the need_update_list (nothing to do if it
@@ -385,19 +451,32 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
     const T* sw = SLw + j * kSL;
     const T lbp = plb[p];
     T acc = Tr<T>::inf();
-    // lane lists are ascending, so the cheapest in-edges come first.  Phase A
-    // only certifies: it stops as soon as the warp's bound reaches lb (the
-    // value is then final), and after kPhaseASteps steps a pair that has not
+    // Phase A only certifies: it walks SL(j) in ascending weight order (the
+    // list is kept sorted) and stops as soon as the warp's bound reaches lb
+    // (the value is then final); after kPhaseASteps stages a pair that has not
     // is left open — A2 evaluates the whole shortlist once the certified
-    // values are in place.  (A pair that certifies does so almost always in
-    // the first step; scanning all 512 entries for the ~1/3 of pairs that
-    // never do was ~90% of phase A's time.)
+    // values are in place.  (A pair that certifies almost always does so on
+    // one of its cheapest few in-edges; scanning all 512 entries for the pairs
+    // that never do was ~90% of phase A's time.)
+    if (!classify) {
+      // SL(j) is sorted ascending: positions 0-7 first (8 gathers — most ties
+      // certify on the cheapest few in-edges), then 8-39, then 40-71
 #pragma unroll
-    for (int q = 0; q < kSLK; ++q) {
-      const int m = sid[q * 32 + lane];
-      const T w = sw[q * 32 + lane];
-      if (m >= 0) acc = Tr<T, SR>::relax(acc, *(volatile T*)(Drow + m), w);
-      if (!classify && (Tr<T>::at_lb(warp_min<T>(acc), lbp) || q == kPhaseASteps - 1)) break;
+      for (int st = 0; st < kPhaseASteps; ++st) {
+        const int e = st == 0 ? lane : 8 + 32 * (st - 1) + lane;
+        if (st > 0 || lane < 8) {
+          const int m = sid[e];
+          if (m >= 0) acc = Tr<T, SR>::relax(acc, *(volatile T*)(Drow + m), sw[e]);
+        }
+        if (Tr<T>::at_lb(warp_min<T>(acc), lbp)) break;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < kSLK; ++q) {
+        const int m = sid[q * 32 + lane];
+        const T w = sw[q * 32 + lane];
+        if (m >= 0) acc = Tr<T, SR>::relax(acc, *(volatile T*)(Drow + m), w);
+      }
     }
     acc = warp_min<T>(acc);
     if (lane == 0) {

@@ -511,6 +511,89 @@ cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const 
   return cudaGetLastError();
 }
 
+// Phase A, one lane per pair (32 pairs per warp in flight: the stage is a
+// chain of dependent gathers — pair, shortlist, D[i][m], D[i][j] — so the
+// pairs a warp overlaps set its speed).  Each lane walks SL(j) in ascending
+// weight order, 8 entries per batch (ids and weights as two 16-byte loads
+// each, then 8 independent gathers of D[i][m]), and stops at the first batch
+// whose running bound reaches lb (certified); after kPhaseABatches batches
+// the pair is left open for A2, which evaluates the whole shortlist.
+constexpr int kPhaseABatches = 9;   // sorted positions 0-71
+
+template <typename T, int SR>
+__global__ void __launch_bounds__(256) k_sparse_phase_a(T* D, int64_t ld, int64_t row0,
+                                                        const int* __restrict__ SLid,
+                                                        const T* __restrict__ SLw,
+                                                        const int* __restrict__ prow,
+                                                        const int* __restrict__ pcol,
+                                                        const T* __restrict__ plb, int64_t npairs,
+                                                        unsigned char* out, OpenLists<T> ol,
+                                                        const DetectCounters* dc) {
+  const int lane = threadIdx.x & 31;
+  npairs = device_count(dc, npairs, 0);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < npairs;
+       base += stride) {
+    const int64_t p = base + lane;
+    const bool valid = p < npairs;
+    int64_t i = 0, j = 0;
+    T lb = Tr<T>::inf(), acc = Tr<T>::inf();
+    bool open = false;
+    if (valid) {
+      i = prow[p];
+      j = pcol[p];
+      lb = plb[p];
+      const T* Drow = D + (i - row0) * ld;
+      const int4* sid = reinterpret_cast<const int4*>(SLid + j * kSL);
+      const int4* sw = reinterpret_cast<const int4*>(SLw + j * kSL);
+      open = true;
+      for (int b = 0; b < kPhaseABatches; ++b) {
+        const int4 m0 = sid[2 * b], m1 = sid[2 * b + 1];
+        const int4 w0 = sw[2 * b], w1 = sw[2 * b + 1];
+        const int m[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+        const int wi[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+        T dv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dv[q] = m[q] >= 0 ? *(volatile const T*)(Drow + m[q]) : Tr<T>::inf();
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (m[q] >= 0) {
+            T w;
+            memcpy(&w, &wi[q], sizeof(T));
+            acc = Tr<T, SR>::relax(acc, dv[q], w);
+          }
+        if (Tr<T>::at_lb(acc, lb)) { open = false; break; }
+      }
+      T* Dw = D + (i - row0) * ld + j;
+      const T cur = *(volatile T*)Dw;
+      const T v = Tr<T>::mn(acc, cur);
+      if (v < cur) *Dw = v;
+      open = !Tr<T>::at_lb(v, lb);
+      out[p] = open ? 1 : 0;
+    }
+    // open-pair lists: per-row slot by atomic, the global slot warp-aggregated
+    const unsigned bal = __ballot_sync(0xffffffffu, open);
+    if (bal) {
+      unsigned long long g0 = 0;
+      if (lane == __ffs(bal) - 1) g0 = atomicAdd(&ol.ctr->open_total, (unsigned long long)__popc(bal));
+      g0 = __shfl_sync(0xffffffffu, g0, __ffs(bal) - 1);
+      if (open) {
+        const int s1 = atomicAdd(ol.ocnt + i, 1);
+        ol.ocol[ol.rowoff[i] + s1] = (int)j;
+        const unsigned long long s2 = g0 + __popc(bal & ((1u << lane) - 1));
+        if ((int64_t)s2 < ol.ocap) {
+          ol.gprow[s2] = (int)i;
+          ol.gpcol[s2] = (int)j;
+          ol.glb[s2] = lb;
+          ol.gfull[s2] = 1;
+        } else {
+          atomicOr(&ol.ctr->overflow, 2u);
+        }
+      }
+    }
+  }
+}
+
 // Phase A over the detection list (pairs in any order: the list is appended
 // by the detection stream; every pair reads only its own row).
 template <typename T>
@@ -522,13 +605,14 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, int64_t n, const int* SLid,
                            cudaStream_t st) {
   if (npairs <= 0) return cudaSuccess;
   OpenLists<T> ol{ocnt, ocol, rowoff, gprow, gpcol, glb, gfull, ocap, ctr};
-  int grid = (int)std::min<int64_t>(cdiv(npairs, 8), (int64_t)num_sms() * 16);
+  // npairs is the capacity bound (the device count decides): full occupancy
+  int grid = (int)std::min<int64_t>(cdiv(npairs, 256), (int64_t)num_sms() * 8);
   if (sr)
-    k_sparse_short<T, 1><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
-                                               out, 0, ol, ctr);
+    k_sparse_phase_a<T, 1><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, prow, pcol, plb, npairs, out,
+                                                 ol, ctr);
   else
-    k_sparse_short<T, 0><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
-                                               out, 0, ol, ctr);
+    k_sparse_phase_a<T, 0><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, prow, pcol, plb, npairs, out,
+                                                 ol, ctr);
   return cudaGetLastError();
 }
 

@@ -212,6 +212,14 @@ struct Tiling {
   int64_t slab;     // rows per slab
   int64_t warps;
 };
+// Tuning override for the streaming tilings (warps per SM the grid targets),
+// read once from the environment; used only to measure alternatives.
+static int tune_wps(const char* name, int dflt) {
+  const char* v = getenv(name);
+  const int x = v ? atoi(v) : 0;
+  return x > 0 ? x : dflt;
+}
+
 static Tiling make_tiling(int64_t n, int64_t rows, int max_slabs, int chunk_vec = CHUNK_VEC,
                           int warps_per_sm = 32) {
   Tiling t;
@@ -620,7 +628,7 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
                           T* rowpart, T* rowpartM, T* colpart, int64_t part_ld, int* nchunk_out,
                           int* nslab_out, int max_slabs, int sr, Mirror M, const unsigned* uncertain,
                           int packed, cudaStream_t st) {
-  Tiling tl = make_tiling(n, r.hi - r.lo, max_slabs, P1_VEC, 48);
+  Tiling tl = make_tiling(n, r.hi - r.lo, max_slabs, P1_VEC, tune_wps("APSP_TUNE_P1_WPS", 16));
   *nchunk_out = tl.nchunk;
   *nslab_out = tl.nslab;
   if (r.hi <= r.lo) {
@@ -1226,7 +1234,7 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
                    int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr, const T* WT,
                    int64_t ldw, int sr, Mirror M, cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
-  Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20, DS_VEC, 64);   // 64 warps/SM: 4 waves (measured best)
+  Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20, DS_VEC, tune_wps("APSP_TUNE_DET_WPS", 192));   // 64 warps/SM: 4 waves (measured best)
   if (tl.slab >= (1 << 26)) return cudaErrorInvalidValue;   // MODE-1 queue packing
   if (mode == 0) CUDA_TRY(cudaMemsetAsync(anyrow + r.lo, 0, sizeof(int) * (size_t)(r.hi - r.lo), st));
   DetectOut<T> o{anyrow, rowcnt, prow, pcol, plb, lcap, ctr, WT, ldw, M};

@@ -39,8 +39,8 @@ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 struct Plan {
   int64_t ld, lcap, ocap, maxchunk;
   size_t off_wt, off_vec, off_rowpart, off_colpart, off_rowoff, off_rowcnt, off_chg, off_prow,
-      off_pcol, off_plb, off_popen, off_ocol, off_ocnt, off_gprow, off_gpcol, off_glb, off_gfull,
-      off_srow, off_scol, off_slb, off_slid, off_slw, off_wnext, off_panel, off_pt, off_anyrow, off_qsend, off_qcol,
+      off_pcol, off_ocol, off_ocnt, off_gprow, off_gpcol, off_glb, off_gfull,
+      off_srow, off_scol, off_slid, off_slw, off_wnext, off_panel, off_pt, off_anyrow, off_qsend, off_qcol,
       off_qids, off_qdsv, off_qlab, off_qpred, off_qpath, off_qdone, off_qcnt, off_p16, off_ptd, off_small,
       total;
   int qcap, qbatch;
@@ -70,8 +70,6 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   p.ocap = std::max<int64_t>(p.lcap / 4, 1 << 18);
   p.off_prow = take(sizeof(int32_t) * (size_t)p.lcap);
   p.off_pcol = take(sizeof(int32_t) * (size_t)p.lcap);
-  p.off_plb = take(sizeof(int32_t) * (size_t)p.lcap);
-  p.off_popen = take((size_t)p.lcap);
   p.off_ocol = take(sizeof(int32_t) * (size_t)p.lcap);
   p.off_ocnt = take(sizeof(int32_t) * (size_t)cap);
   p.off_gprow = take(sizeof(int32_t) * (size_t)p.ocap);
@@ -80,7 +78,6 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   p.off_gfull = take((size_t)p.ocap);
   p.off_srow = take(sizeof(int32_t) * (size_t)p.lcap);   // staging list of the detection pass
   p.off_scol = take(sizeof(int32_t) * (size_t)p.lcap);
-  p.off_slb = take(sizeof(int32_t) * (size_t)p.lcap);
   p.off_slid = take(sizeof(int32_t) * (size_t)cap * kSL);
   p.off_slw = take(sizeof(int32_t) * (size_t)cap * kSL);
   p.off_wnext = take(sizeof(int32_t) * (size_t)cap);
@@ -207,8 +204,6 @@ struct apsp_handle {
   int* chg(int k) { return reinterpret_cast<int*>(ws + plan.off_chg) + (size_t)k * cap; }
   int* prow() { return reinterpret_cast<int*>(ws + plan.off_prow); }
   int* pcol() { return reinterpret_cast<int*>(ws + plan.off_pcol); }
-  template <typename T> T* plb() { return reinterpret_cast<T*>(ws + plan.off_plb); }
-  unsigned char* popen() { return ws + plan.off_popen; }
   int* ocol() { return reinterpret_cast<int*>(ws + plan.off_ocol); }
   int* ocnt() { return reinterpret_cast<int*>(ws + plan.off_ocnt); }
   int* gprow() { return reinterpret_cast<int*>(ws + plan.off_gprow); }
@@ -217,7 +212,6 @@ struct apsp_handle {
   unsigned char* gfull() { return ws + plan.off_gfull; }
   int* srow() { return reinterpret_cast<int*>(ws + plan.off_srow); }
   int* scol() { return reinterpret_cast<int*>(ws + plan.off_scol); }
-  template <typename T> T* slb() { return reinterpret_cast<T*>(ws + plan.off_slb); }
   int* slid() { return reinterpret_cast<int*>(ws + plan.off_slid); }
   template <typename T> T* slw() { return reinterpret_cast<T*>(ws + plan.off_slw); }
   template <typename T> T* wnext() { return reinterpret_cast<T*>(ws + plan.off_wnext); }
@@ -523,17 +517,13 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   const int64_t lcap = h->plan.lcap, ocap = h->plan.ocap;
   CKR(cudaMemsetAsync(h->rowcnt(), 0, sizeof(int) * h->cap, h->st));
   CKR(cudaMemsetAsync(h->ctr(), 0, sizeof(DetectCounters), h->st));
-  CKR(cudaMemsetAsync(h->ocnt(), 0, sizeof(int) * h->cap, h->st));   // scatter cursors
-  // one streaming pass appends the need_update_list; then per-row slices,
-  // Phi / max|A_i|, the row grouping and the D0 reset (W'[i][j])
+  // one streaming pass appends the need_update_list; then the per-row slices
+  // of the open lists and Phi / max|A_i|
   PK(APSP_K_DETECT, h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n,
      detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, 1, nullptr, h->rowcnt(),
-               h->srow(), h->scol(), h->slb<T>(), lcap, h->ctr(), h->WT<T>(), h->ld, h->sr,
+               h->srow(), h->scol(), nullptr, lcap, h->ctr(), h->WT<T>(), h->ld, h->sr,
                h->mirror<T>(), h->st));
-  PK(APSP_K_EMIT, 0.0,
-     detect_lists<T>(h->Dl<T>(), h->ld, r, h->WT<T>(), h->ld, h->rowcnt(), h->rowoff(), h->srow(),
-                     h->scol(), h->slb<T>(), h->ocnt(), h->prow(), h->pcol(), h->plb<T>(), lcap,
-                     h->ctr(), h->st));
+  PK(APSP_K_EMIT, 0.0, detect_lists(r, h->rowcnt(), h->rowoff(), h->ctr(), h->st));
   if (removal) CK(tombstone<T>(h->Dl<T>(), h->ld, r, n, skip, h->WT<T>(), h->ld, h->st));
 
   // ---- sparse recompute (a6), enqueued without a host round trip: the pair
@@ -545,9 +535,9 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   // Rounds are frontier-based Bellman-Ford over each row's open entries: round
   // r relaxes every open pair of a row through the entries of that row that
   // changed in round r-1 (round 0: all open entries).  Frontier lists live in
-  // the row slices of the (now free) staging list, counts in chg(0)/chg(1).
+  // the row slices of two spare pair-list buffers, counts in chg(0)/chg(1).
   int rounds = 0;
-  int* fcol[2] = {h->srow(), h->scol()};
+  int* fcol[2] = {h->prow(), h->pcol()};
   auto enqueue_rounds = [&](int batch) -> apsp_status {
     for (int b = 0; b < batch; ++b, ++rounds) {
       const int o = rounds & 1;
@@ -564,12 +554,12 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   };
   if (try_sparse) {
     CKR(cudaMemsetAsync(h->ocnt(), 0, sizeof(int) * h->cap, h->st));
-    // A: shortlist certification of every listed pair (ties reach lb)
+    // A: every listed entry rewritten with a walk length of G' (stale entries
+    // skipped by the detection predicate), certified where it reaches lb
     PK(APSP_K_SPARSE0, 0.0,
-       sparse_phase_a<T>(h->Dl<T>(), h->ld, r, n, h->slid(), h->slw<T>(), h->wnext<T>(), h->rowoff(),
-                         h->rowcnt(), h->prow(), h->pcol(), h->plb<T>(), lcap, h->popen(), h->ocnt(),
-                         h->ocol(), h->gprow(), h->gpcol(), h->glb<T>(), h->gfull(), ocap, h->ctr(),
-                         h->sr, h->st));
+       sparse_phase_a<T>(h->Dl<T>(), h->ld, r, h->slid(), h->slw<T>(), h->rowoff(), h->srow(), h->scol(),
+                         lcap, c1, r1, c2, r2, h->tau, h->ocnt(), h->ocol(), h->gprow(), h->gpcol(),
+                         h->glb<T>(), h->gfull(), ocap, h->ctr(), h->sr, h->st));
     // A2: whole-shortlist pass over the open pairs, now that certified values are final
     CK(sparse_short<T>(h->Dl<T>(), h->ld, h->row0, h->slid(), h->slw<T>(), h->wnext<T>(), h->gprow(),
                        h->gpcol(), h->glb<T>(), ocap, h->gfull(), 1, h->sr, h->ctr(), h->st));
@@ -629,11 +619,14 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
       PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
          detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, 2, nullptr, nullptr, nullptr,
                    nullptr, nullptr, 0, nullptr, h->WT<T>(), h->ld, h->sr, h->mirror<T>(), h->st));
+    else if (!try_sparse)   // no phase A ran: the listed entries still hold D_old
+      CK(reset_pairs<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->srow(), h->scol(), h->ctr(), lcap,
+                        h->st));
     return fw_impl<T>(h, removal ? skip : -1);
   }
   if (info) info->path = 2;
   if (total > 0)   // the sparse kernels wrote D on listed pairs only
-    CK(mirror_pairs(h->Dl<T>(), h->ld, h->row0, h->prow(), h->pcol(), h->ctr(), lcap, h->mirror<T>(), h->st));
+    CK(mirror_pairs(h->Dl<T>(), h->ld, h->row0, h->srow(), h->scol(), h->ctr(), lcap, h->mirror<T>(), h->st));
   return APSP_OK;
 }
 

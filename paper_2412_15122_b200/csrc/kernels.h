@@ -99,11 +99,12 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
                    const T* c2, const T* r2, float tau, int mode, int* anyrow, int* rowcnt,
                    int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr, const T* WT,
                    int64_t ldw, int sr, Mirror M, cudaStream_t st);
-template <typename T>
-cudaError_t detect_lists(T* D, int64_t ld, Rows r, const T* WT, int64_t ldw, const int* rowcnt,
-                         int64_t* rowoff, const int* srow, const int* scol, const T* slb, int* cur,
-                         int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr,
+cudaError_t detect_lists(Rows r, const int* rowcnt, int64_t* rowoff, DetectCounters* ctr,
                          cudaStream_t st);
+// D[i][j] := W'[i][j] on every listed pair (the dense path without the sparse kernels)
+template <typename T>
+cudaError_t reset_pairs(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, const int* srow,
+                        const int* scol, const DetectCounters* ctr, int64_t lcap, cudaStream_t st);
 template <typename T>
 cudaError_t tombstone(T* D, int64_t ld, Rows r, int64_t n, int64_t k, T* WT, int64_t ldw,
                       cudaStream_t st);
@@ -155,17 +156,11 @@ cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const 
                          const T* wnext, const int* prow, const int* pcol, const T* plb,
                          int64_t npairs, unsigned char* out, int classify, int sr, const DetectCounters* dc, cudaStream_t st);
 template <typename T>
-cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, int64_t n, const int* SLid, const T* SLw,
-                           const T* wnext, const int64_t* rowoff, const int* rowcnt,
-                           const int* prow, const int* pcol, const T* plb, int64_t npairs,
-                           unsigned char* out, int* ocnt, int* ocol, int* gprow, int* gpcol, T* glb,
-                           unsigned char* gfull, int64_t ocap, DetectCounters* ctr, int sr,
-                           cudaStream_t st);
-template <typename T>
-cudaError_t sparse_compact(Rows r, const int64_t* rowoff, const int* rowcnt, const int* pcol,
-                           const T* plb, const unsigned char* popen, int* ocol, int* ocnt,
-                           int* gprow, int* gpcol, T* glb, unsigned char* gfull, int64_t ocap,
-                           DetectCounters* ctr, cudaStream_t st);
+cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* SLw,
+                           const int64_t* rowoff, const int* srow, const int* scol, int64_t npairs,
+                           const T* c1, const T* r1, const T* c2, const T* r2, float tau, int* ocnt,
+                           int* ocol, int* gprow, int* gpcol, T* glb, unsigned char* gfull, int64_t ocap,
+                           DetectCounters* ctr, int sr, cudaStream_t st);
 template <typename T>
 cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
                         const int* gprow, const int* gpcol, const T* glb, const unsigned char* gfull,

@@ -511,23 +511,31 @@ cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const 
   return cudaGetLastError();
 }
 
-// Phase A, one lane per pair (32 pairs per warp in flight: the stage is a
-// chain of dependent gathers — pair, shortlist, D[i][m], D[i][j] — so the
-// pairs a warp overlaps set its speed).  Each lane walks SL(j) in ascending
-// weight order, 8 entries per batch (ids and weights as two 16-byte loads
-// each, then 8 independent gathers of D[i][m]), and stops at the first batch
-// whose running bound reaches lb (certified); after kPhaseABatches batches
-// the pair is left open for A2, which evaluates the whole shortlist.
+// Phase A, one lane per pair, straight off the detection list (32 pairs per
+// warp in flight: the stage is a chain of dependent gathers — pair, shortlist,
+// D[i][m] — so the pairs a warp overlaps set its speed).  Nothing has been
+// reset: every listed entry still holds D_old, which is the pair's lower
+// bound lb (read here; only this lane writes (i, j)) but is stale as a
+// candidate.  A stale D[i][m] is recognised by the detection predicate itself
+// (same function of the same values: m's entry is listed iff it still tests
+// tight against the pivot snapshots) and skipped; an entry another lane has
+// already rewritten holds a walk length of G' and is used.  Skipping only
+// weakens the bound, so the value written — min over the usable candidates,
+// INF if none — is a walk length of G' (>= the new distance) either way.
+// Each lane walks SL(j) in ascending weight order, 8 entries per batch, and
+// stops at the first batch whose bound reaches lb (certified); after
+// kPhaseABatches batches the pair is left open for A2 / B / the rounds.
 constexpr int kPhaseABatches = 9;   // sorted positions 0-71
 
-template <typename T, int SR>
+template <typename T, int SR, bool TWO>
 __global__ void __launch_bounds__(256) k_sparse_phase_a(T* D, int64_t ld, int64_t row0,
                                                         const int* __restrict__ SLid,
                                                         const T* __restrict__ SLw,
-                                                        const int* __restrict__ prow,
-                                                        const int* __restrict__ pcol,
-                                                        const T* __restrict__ plb, int64_t npairs,
-                                                        unsigned char* out, OpenLists<T> ol,
+                                                        const int* __restrict__ srow,
+                                                        const int* __restrict__ scol, int64_t npairs,
+                                                        const T* __restrict__ c1, const T* __restrict__ r1,
+                                                        const T* __restrict__ c2, const T* __restrict__ r2,
+                                                        float tau, OpenLists<T> ol,
                                                         const DetectCounters* dc) {
   const int lane = threadIdx.x & 31;
   npairs = device_count(dc, npairs, 0);
@@ -535,41 +543,44 @@ __global__ void __launch_bounds__(256) k_sparse_phase_a(T* D, int64_t ld, int64_
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < npairs;
        base += stride) {
     const int64_t p = base + lane;
-    const bool valid = p < npairs;
     int64_t i = 0, j = 0;
     T lb = Tr<T>::inf(), acc = Tr<T>::inf();
     bool open = false;
-    if (valid) {
-      i = prow[p];
-      j = pcol[p];
-      lb = plb[p];
-      const T* Drow = D + (i - row0) * ld;
+    if (p < npairs) {
+      i = srow[p];
+      j = scol[p];
+      T* Drow = D + (i - row0) * ld;
       const int4* sid = reinterpret_cast<const int4*>(SLid + j * kSL);
       const int4* sw = reinterpret_cast<const int4*>(SLw + j * kSL);
-      open = true;
+      lb = *(volatile T*)(Drow + j);   // D_old[i][j]
+      const T ci = c1[i], cj = TWO ? c2[i] : Tr<T>::inf();
       for (int b = 0; b < kPhaseABatches; ++b) {
         const int4 m0 = sid[2 * b], m1 = sid[2 * b + 1];
         const int4 w0 = sw[2 * b], w1 = sw[2 * b + 1];
         const int m[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
         const int wi[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-        T dv[8];
+        T dv[8], rv[8], rv2[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) dv[q] = m[q] >= 0 ? *(volatile const T*)(Drow + m[q]) : Tr<T>::inf();
+        for (int q = 0; q < 8; ++q) {
+          const int mq = m[q] >= 0 ? m[q] : 0;
+          dv[q] = m[q] >= 0 ? *(volatile const T*)(Drow + mq) : Tr<T>::inf();
+          rv[q] = r1[mq];
+          if (TWO) rv2[q] = r2[mq];
+        }
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (m[q] >= 0) {
+        for (int q = 0; q < 8; ++q) {
+          bool stale = Tr<T, SR>::tight(Tr<T, SR>::add(ci, rv[q]), dv[q], tau);
+          if (TWO) stale = stale || Tr<T, SR>::tight(Tr<T, SR>::add(cj, rv2[q]), dv[q], tau);
+          if (m[q] >= 0 && !stale) {
             T w;
             memcpy(&w, &wi[q], sizeof(T));
             acc = Tr<T, SR>::relax(acc, dv[q], w);
           }
-        if (Tr<T>::at_lb(acc, lb)) { open = false; break; }
+        }
+        if (Tr<T>::at_lb(acc, lb)) break;
       }
-      T* Dw = D + (i - row0) * ld + j;
-      const T cur = *(volatile T*)Dw;
-      const T v = Tr<T>::mn(acc, cur);
-      if (v < cur) *Dw = v;
-      open = !Tr<T>::at_lb(v, lb);
-      out[p] = open ? 1 : 0;
+      Drow[j] = acc;   // unconditionally: D_old is not an upper bound of D'
+      open = !Tr<T>::at_lb(acc, lb);
     }
     // open-pair lists: per-row slot by atomic, the global slot warp-aggregated
     const unsigned bal = __ballot_sync(0xffffffffu, open);
@@ -594,88 +605,25 @@ __global__ void __launch_bounds__(256) k_sparse_phase_a(T* D, int64_t ld, int64_
   }
 }
 
-// Phase A over the detection list (pairs in any order: the list is appended
-// by the detection stream; every pair reads only its own row).
+// Phase A over the detection list (pairs in append order; every pair reads
+// and writes only its own row).
 template <typename T>
-cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, int64_t n, const int* SLid, const T* SLw,
-                           const T* wnext, const int64_t* rowoff, const int* rowcnt,
-                           const int* prow, const int* pcol, const T* plb, int64_t npairs,
-                           unsigned char* out, int* ocnt, int* ocol, int* gprow, int* gpcol, T* glb,
-                           unsigned char* gfull, int64_t ocap, DetectCounters* ctr, int sr,
-                           cudaStream_t st) {
+cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* SLw,
+                           const int64_t* rowoff, const int* srow, const int* scol, int64_t npairs,
+                           const T* c1, const T* r1, const T* c2, const T* r2, float tau, int* ocnt,
+                           int* ocol, int* gprow, int* gpcol, T* glb, unsigned char* gfull, int64_t ocap,
+                           DetectCounters* ctr, int sr, cudaStream_t st) {
   if (npairs <= 0) return cudaSuccess;
   OpenLists<T> ol{ocnt, ocol, rowoff, gprow, gpcol, glb, gfull, ocap, ctr};
   // npairs is the capacity bound (the device count decides): full occupancy
   int grid = (int)std::min<int64_t>(cdiv(npairs, 256), (int64_t)num_sms() * 8);
-  if (sr)
-    k_sparse_phase_a<T, 1><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, prow, pcol, plb, npairs, out,
-                                                 ol, ctr);
-  else
-    k_sparse_phase_a<T, 0><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, prow, pcol, plb, npairs, out,
-                                                 ol, ctr);
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// compaction: per affected row, the open entries (status != 0) in list order
-// -> ocol[rowoff[i] ...], ocnt[i]; and a global list of open pairs.
-// ---------------------------------------------------------------------------
-template <typename T>
-__global__ void __launch_bounds__(256) k_sparse_compact(
-    Rows r, const int64_t* __restrict__ rowoff, const int* __restrict__ rowcnt,
-    const int* __restrict__ pcol, const T* __restrict__ plb, const unsigned char* __restrict__ popen,
-    int* ocol, int* ocnt, int* gprow, int* gpcol, T* glb, unsigned char* gfull, int64_t ocap,
-    DetectCounters* ctr) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t i = r.lo + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < r.hi;
-       i += nw) {
-    const int cnt = rowcnt[i];
-    if (cnt == 0) continue;
-    const int64_t off = rowoff[i];
-    int total = 0;
-    for (int t0 = 0; t0 < cnt; t0 += 32) {
-      const int t = t0 + lane;
-      const bool f = t < cnt && popen[off + t] != 0;
-      const unsigned b = __ballot_sync(0xffffffffu, f);
-      if (f) ocol[off + total + __popc(b & ((1u << lane) - 1))] = pcol[off + t];
-      total += __popc(b);
-    }
-    if (lane == 0) ocnt[i] = total;
-    if (total == 0) continue;
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(&ctr->open_total, (unsigned long long)total);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if ((int64_t)base + total > ocap) {
-      if (lane == 0) atomicOr(&ctr->overflow, 2u);
-      continue;
-    }
-    int pos = 0;
-    for (int t0 = 0; t0 < cnt; t0 += 32) {
-      const int t = t0 + lane;
-      const unsigned char s = t < cnt ? popen[off + t] : 0;
-      const bool f = s != 0;
-      const unsigned b = __ballot_sync(0xffffffffu, f);
-      if (f) {
-        const int64_t q = (int64_t)base + pos + __popc(b & ((1u << lane) - 1));
-        gprow[q] = (int)i;
-        gpcol[q] = pcol[off + t];
-        glb[q] = plb[off + t];
-        gfull[q] = 1;
-      }
-      pos += __popc(b);
-    }
-  }
-}
-template <typename T>
-cudaError_t sparse_compact(Rows r, const int64_t* rowoff, const int* rowcnt, const int* pcol,
-                           const T* plb, const unsigned char* popen, int* ocol, int* ocnt,
-                           int* gprow, int* gpcol, T* glb, unsigned char* gfull, int64_t ocap,
-                           DetectCounters* ctr, cudaStream_t st) {
-  if (r.hi <= r.lo) return cudaSuccess;
-  int grid = (int)std::min<int64_t>(cdiv(r.hi - r.lo, 8), (int64_t)num_sms() * 8);
-  k_sparse_compact<T><<<grid, 256, 0, st>>>(r, rowoff, rowcnt, pcol, plb, popen, ocol, ocnt, gprow,
-                                            gpcol, glb, gfull, ocap, ctr);
+#define PA(SRV, TWOV)                                                                              \
+  k_sparse_phase_a<T, SRV, TWOV><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, srow, scol, npairs, \
+                                                       c1, r1, c2, r2, tau, ol, ctr)
+  const bool two = c2 != nullptr;
+  if (sr) { if (two) PA(1, true); else PA(1, false); }
+  else { if (two) PA(0, true); else PA(0, false); }
+#undef PA
   return cudaGetLastError();
 }
 
@@ -814,14 +762,11 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
   template cudaError_t sparse_short<T>(T*, int64_t, int64_t, const int*, const T*, const T*,       \
                                        const int*, const int*, const T*, int64_t, unsigned char*,  \
                                        int, int, const DetectCounters*, cudaStream_t);            \
-  template cudaError_t sparse_phase_a<T>(T*, int64_t, Rows, int64_t, const int*, const T*,         \
-                                         const T*, const int64_t*, const int*, const int*,         \
-                                         const int*, const T*, int64_t, unsigned char*, int*, int*, \
-                                         int*, int*, T*, unsigned char*, int64_t, DetectCounters*, \
-                                         int, cudaStream_t);                                      \
-  template cudaError_t sparse_compact<T>(Rows, const int64_t*, const int*, const int*, const T*,   \
-                                         const unsigned char*, int*, int*, int*, int*, T*,         \
-                                         unsigned char*, int64_t, DetectCounters*, cudaStream_t);  \
+  template cudaError_t sparse_phase_a<T>(T*, int64_t, Rows, const int*, const T*, const int64_t*,  \
+                                         const int*, const int*, int64_t, const T*, const T*,      \
+                                         const T*, const T*, float, int*, int*, int*, int*, T*,    \
+                                         unsigned char*, int64_t, DetectCounters*, int,            \
+                                         cudaStream_t);                                            \
   template cudaError_t sparse_full<T>(T*, int64_t, int64_t, const T*, int64_t, int64_t,            \
                                       const int*, const int*, const T*, const unsigned char*,      \
                                       int64_t, int, const DetectCounters*, cudaStream_t);         \

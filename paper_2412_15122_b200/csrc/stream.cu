@@ -938,7 +938,7 @@ __device__ __forceinline__ void detect_flush(const DetectQueue& Q, int cnt, int6
       const int64_t j = 4 * group_of(m16, chunk, bit >> 2, ln) + (bit & 3);
       if (pos < o.lcap) {
         o.prow[pos] = (int)i;
-        o.pcol[pos] = (int)j;   // D_old[i][j] (the lower bound) is read by the scatter
+        o.pcol[pos] = (int)j;   // D_old[i][j] (the lower bound) is read by phase A
       }
       ++pos;
     }
@@ -1206,28 +1206,6 @@ __global__ void k_detect_rows(Rows r, const int* __restrict__ rowcnt, int64_t* r
   }
 }
 
-// Group the staged list by row (counting sort on rowoff, the row's slot cursor
-// in `cur`) and reset D0[i][j] := W'[i][j] for every listed pair: phase A then
-// walks the pairs row by row (the row's D entries stay hot in L2).
-template <typename T>
-__global__ void k_scatter_pairs(T* D, int64_t ld, int64_t row0, const T* __restrict__ WT, int64_t ldw,
-                                const int* __restrict__ srow, const int* __restrict__ scol,
-                                const T* __restrict__ slb, const int64_t* __restrict__ rowoff,
-                                int* cur, int* prow, int* pcol, T* plb, const DetectCounters* ctr,
-                                int64_t lcap) {
-  const int64_t np = min((int64_t)ctr->total, lcap);
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const int i = srow[p], j = scol[p];
-    const int64_t q = rowoff[i] + atomicAdd(cur + i, 1);
-    T* d = D + ((int64_t)i - row0) * ld + j;
-    prow[q] = i;
-    pcol[q] = j;
-    plb[q] = *d;                               // D_old[i][j]: a lower bound of D'
-    *d = WT[(int64_t)j * ldw + i];             // D0[i][j] := W'[i][j]
-  }
-}
-
 template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
                    const T* c2, const T* r2, float tau, int mode, int* anyrow, int* rowcnt,
@@ -1262,17 +1240,35 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
 
 // After a MODE-1 pass: per-row slices, Phi, max|A_i|, then the row grouping
 // of the staged list and the D0 reset.  `cur` (cap ints) must be zero.
+// D0[i][j] := W'[i][j] for every listed pair: only when the dense path runs
+// without the sparse kernels (forced); otherwise phase A rewrites every
+// listed entry itself (sparse.cu).
 template <typename T>
-cudaError_t detect_lists(T* D, int64_t ld, Rows r, const T* WT, int64_t ldw, const int* rowcnt,
-                         int64_t* rowoff, const int* srow, const int* scol, const T* slb, int* cur,
-                         int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr,
+__global__ void k_reset_pairs(T* D, int64_t ld, int64_t row0, const T* __restrict__ WT, int64_t ldw,
+                              const int* __restrict__ srow, const int* __restrict__ scol,
+                              const DetectCounters* ctr, int64_t lcap) {
+  const int64_t np = min((int64_t)ctr->total, lcap);
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int i = srow[p], j = scol[p];
+    D[((int64_t)i - row0) * ld + j] = WT[(int64_t)j * ldw + i];
+  }
+}
+
+template <typename T>
+cudaError_t reset_pairs(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, const int* srow,
+                        const int* scol, const DetectCounters* ctr, int64_t lcap, cudaStream_t st) {
+  k_reset_pairs<T><<<num_sms() * 8, 256, 0, st>>>(D, ld, row0, WT, ldw, srow, scol, ctr, lcap);
+  return cudaGetLastError();
+}
+
+// Per-row slices of the open lists: rowoff = prefix of the per-row counts,
+// plus Phi (rows with pairs) and max |A_i|.
+cudaError_t detect_lists(Rows r, const int* rowcnt, int64_t* rowoff, DetectCounters* ctr,
                          cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
   const int g = (int)std::min<int64_t>(cdiv(r.hi - r.lo, 256), 2 * num_sms());
   k_detect_rows<<<g, 256, 0, st>>>(r, rowcnt, rowoff, ctr);
-  CUDA_TRY(cudaGetLastError());
-  k_scatter_pairs<T><<<num_sms() * 8, 256, 0, st>>>(D, ld, r.row0, WT, ldw, srow, scol, slb, rowoff,
-                                                    cur, prow, pcol, plb, ctr, lcap);
   return cudaGetLastError();
 }
 
@@ -1519,9 +1515,8 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
                                  const T*, const T*, float, int, int*, int*, int*, int*, T*,      \
                                  int64_t, DetectCounters*, const T*, int64_t, int, Mirror,        \
                                  cudaStream_t);                                                   \
-  template cudaError_t detect_lists<T>(T*, int64_t, Rows, const T*, int64_t, const int*, int64_t*, \
-                                       const int*, const int*, const T*, int*, int*, int*, T*,     \
-                                       int64_t, DetectCounters*, cudaStream_t);                    \
+  template cudaError_t reset_pairs<T>(T*, int64_t, int64_t, const T*, int64_t, const int*,         \
+                                      const int*, const DetectCounters*, int64_t, cudaStream_t);  \
   template cudaError_t tombstone<T>(T*, int64_t, Rows, int64_t, int64_t, T*, int64_t,              \
                                     cudaStream_t);                                                \
   template cudaError_t copy_row<T>(T*, const T*, int64_t, cudaStream_t);                           \

@@ -66,7 +66,7 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   p.off_colpart = take(sizeof(int32_t) * (size_t)kMaxSlabs * p.ld);
   p.off_rowoff = take(sizeof(int64_t) * (size_t)cap);
   p.off_rowcnt = take(sizeof(int32_t) * (size_t)cap);
-  p.off_chg = take(sizeof(int32_t) * (size_t)cap * 2);
+  p.off_chg = take(sizeof(int32_t) * (size_t)(cap + 32) * 2);   // + the round's frontier total
   p.ocap = std::max<int64_t>(p.lcap / 4, 1 << 18);
   p.off_prow = take(sizeof(int32_t) * (size_t)p.lcap);
   p.off_pcol = take(sizeof(int32_t) * (size_t)p.lcap);
@@ -201,7 +201,8 @@ struct apsp_handle {
   template <typename T> T* colpart() { return reinterpret_cast<T*>(ws + plan.off_colpart); }
   int64_t* rowoff() { return reinterpret_cast<int64_t*>(ws + plan.off_rowoff); }
   int* rowcnt() { return reinterpret_cast<int*>(ws + plan.off_rowcnt); }
-  int* chg(int k) { return reinterpret_cast<int*>(ws + plan.off_chg) + (size_t)k * cap; }
+  // round frontier counts per row; chg(k)[cap] = their total
+  int* chg(int k) { return reinterpret_cast<int*>(ws + plan.off_chg) + (size_t)k * (cap + 32); }
   int* prow() { return reinterpret_cast<int*>(ws + plan.off_prow); }
   int* pcol() { return reinterpret_cast<int*>(ws + plan.off_pcol); }
   int* ocol() { return reinterpret_cast<int*>(ws + plan.off_ocol); }
@@ -543,12 +544,12 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
       const int o = rounds & 1;
       const int* fin_c = rounds == 0 ? h->ocnt() : h->chg(o ^ 1);
       const int* fin_l = rounds == 0 ? h->ocol() : fcol[o ^ 1];
-      CKR(cudaMemsetAsync(h->chg(o), 0, sizeof(int) * h->cap, h->st));
+      CKR(cudaMemsetAsync(h->chg(o), 0, sizeof(int) * (h->cap + 1), h->st));
       if (b == batch - 1) CKR(cudaMemsetAsync(h->anyflag(), 0, sizeof(int), h->st));
       PK(APSP_K_SPARSE_R, 0.0,
          sparse_round<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->gprow(), h->gpcol(),
-                         h->glb<T>(), ocap, h->rowoff(), fin_c, fin_l, h->chg(o), fcol[o],
-                         h->anyflag(), h->sr, h->ctr(), h->st));
+                         h->glb<T>(), ocap, h->rowoff(), fin_c, rounds == 0 ? nullptr : fin_c + h->cap,
+                         fin_l, h->chg(o), h->chg(o) + h->cap, fcol[o], h->anyflag(), h->sr, h->ctr(), h->st));
     }
     return APSP_OK;
   };

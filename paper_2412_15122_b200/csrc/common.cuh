@@ -199,6 +199,17 @@ __device__ __forceinline__ T warp_min(T v) {
   return v;
 }
 
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+  if constexpr (std::is_same<T, int32_t>::value) {
+    return __reduce_max_sync(0xffffffffu, v);
+  } else {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+  }
+}
+
 constexpr int kNumSMs = 148;  // B200 (2 dies x 74); the host reads the real count
 
 }  // namespace apsp

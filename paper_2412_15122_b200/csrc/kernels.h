@@ -168,9 +168,9 @@ cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw
 template <typename T>
 cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw,
                          const int* gprow, const int* gpcol, const T* glb, int64_t nopen,
-                         const int64_t* rowoff, const int* fcnt_in, const int* fcol_in,
-                         int* fcnt_out, int* fcol_out, int* any, int sr, const DetectCounters* dc,
-                         cudaStream_t st);
+                         const int64_t* rowoff, const int* fcnt_in, const int* ftot_in, const int* fcol_in,
+                         int* fcnt_out, int* ftot_out, int* fcol_out, int* any, int sr,
+                         const DetectCounters* dc, cudaStream_t st);
 
 // ---------------- query.cu ----------------
 constexpr int kQueryCap = 4096;    // max |C| per query (min(kQueryCap, cap) per handle)

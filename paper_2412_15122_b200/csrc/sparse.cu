@@ -471,11 +471,20 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
         if (Tr<T>::at_lb(warp_min<T>(acc), lbp)) break;
       }
     } else {
+      // the whole shortlist, in ascending weight order, stopping once no
+      // later entry can improve: every later live entry weighs >= the
+      // heaviest live one seen (SL(j) is sorted) and D >= 0, so D + w >= w
+      // (minimax: max(D, w) >= w) — the result is min over all of SL(j)
+      T wseen = T(0);
 #pragma unroll
       for (int q = 0; q < kSLK; ++q) {
         const int m = sid[q * 32 + lane];
         const T w = sw[q * 32 + lane];
-        if (m >= 0) acc = Tr<T, SR>::relax(acc, *(volatile T*)(Drow + m), w);
+        if (m >= 0) {
+          acc = Tr<T, SR>::relax(acc, *(volatile T*)(Drow + m), w);
+          wseen = w > wseen ? w : wseen;
+        }
+        if ((q & 1) && q + 1 < kSLK && __any_sync(0xffffffffu, acc <= warp_max<T>(wseen))) break;
       }
     }
     acc = warp_min<T>(acc);
@@ -559,25 +568,36 @@ __global__ void __launch_bounds__(256) k_sparse_phase_a(T* D, int64_t ld, int64_
         const int4 w0 = sw[2 * b], w1 = sw[2 * b + 1];
         const int m[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
         const int wi[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-        T dv[8], rv[8], rv2[8];
+        // the first batch in two steps: the 2 cheapest in-edges certify most
+        // pairs, so the other 6 gathers are issued only when they did not
+        bool done = false;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int mq = m[q] >= 0 ? m[q] : 0;
-          dv[q] = m[q] >= 0 ? *(volatile const T*)(Drow + mq) : Tr<T>::inf();
-          rv[q] = r1[mq];
-          if (TWO) rv2[q] = r2[mq];
-        }
+        for (int h = 0; h < 2; ++h) {
+          const int q0 = h == 0 ? 0 : (b == 0 ? 2 : 8), q1 = h == 0 ? (b == 0 ? 2 : 8) : 8;
+          if (q0 >= q1) continue;
+          T dv[8], rv[8], rv2[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          bool stale = Tr<T, SR>::tight(Tr<T, SR>::add(ci, rv[q]), dv[q], tau);
-          if (TWO) stale = stale || Tr<T, SR>::tight(Tr<T, SR>::add(cj, rv2[q]), dv[q], tau);
-          if (m[q] >= 0 && !stale) {
-            T w;
-            memcpy(&w, &wi[q], sizeof(T));
-            acc = Tr<T, SR>::relax(acc, dv[q], w);
+          for (int q = 0; q < 8; ++q) {
+            if (q < q0 || q >= q1) continue;
+            const int mq = m[q] >= 0 ? m[q] : 0;
+            dv[q] = m[q] >= 0 ? *(volatile const T*)(Drow + mq) : Tr<T>::inf();
+            rv[q] = r1[mq];
+            if (TWO) rv2[q] = r2[mq];
           }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (q < q0 || q >= q1) continue;
+            bool stale = Tr<T, SR>::tight(Tr<T, SR>::add(ci, rv[q]), dv[q], tau);
+            if (TWO) stale = stale || Tr<T, SR>::tight(Tr<T, SR>::add(cj, rv2[q]), dv[q], tau);
+            if (m[q] >= 0 && !stale) {
+              T w;
+              memcpy(&w, &wi[q], sizeof(T));
+              acc = Tr<T, SR>::relax(acc, dv[q], w);
+            }
+          }
+          if (Tr<T>::at_lb(acc, lb)) { done = true; break; }
         }
-        if (Tr<T>::at_lb(acc, lb)) break;
+        if (done) break;
       }
       Drow[j] = acc;   // unconditionally: D_old is not an upper bound of D'
       open = !Tr<T>::at_lb(acc, lb);
@@ -700,9 +720,12 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
                                                       const T* __restrict__ glb, int64_t nopen,
                                                       const int64_t* __restrict__ rowoff,
                                                       const int* __restrict__ fcnt_in,
+                                                      const int* __restrict__ ftot_in,
                                                       const int* __restrict__ fcol_in,
-                                                      int* fcnt_out, int* fcol_out, int* any,
+                                                      int* fcnt_out, int* ftot_out, int* fcol_out, int* any,
                                                       const DetectCounters* dc) {
+  // an empty frontier (nothing changed last round): the round is a no-op
+  if (ftot_in && *(volatile const int*)ftot_in == 0) return;
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   nopen = device_count(dc, nopen, 1);
@@ -717,17 +740,25 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
     if (lane == 0) cur = *(volatile T*)(Drow + j);
     cur = __shfl_sync(0xffffffffu, cur, 0);  // one value for the whole warp (others may write)
     if (Tr<T>::at_lb(cur, glb[p])) continue;   // already at its lower bound: final
-    const int64_t off = rowoff[i];
     const T* Wrow = WT + j * ldw;
+    const int* fl = fcol_in + rowoff[i];
     T acc = Tr<T>::inf();
-    for (int t = lane; t < cnt; t += 32) {
-      const int64_t m = fcol_in[off + t];
+    int t = lane;
+    for (; t + 32 < cnt; t += 64) {   // two gathers in flight per lane
+      const int64_t m0 = fl[t], m1 = fl[t + 32];
+      const T d0 = *(volatile T*)(Drow + m0), d1 = *(volatile T*)(Drow + m1);
+      const T w0 = Wrow[m0], w1 = Wrow[m1];
+      acc = Tr<T, SR>::relax(Tr<T, SR>::relax(acc, d0, w0), d1, w1);
+    }
+    if (t < cnt) {
+      const int64_t m = fl[t];
       acc = Tr<T, SR>::relax(acc, *(volatile T*)(Drow + m), Wrow[m]);
     }
     acc = warp_min<T>(acc);
     if (lane == 0 && acc < cur) {
       Drow[j] = acc;
-      fcol_out[off + atomicAdd(fcnt_out + i, 1)] = (int)j;   // j changed: next round's frontier
+      fcol_out[rowoff[i] + atomicAdd(fcnt_out + i, 1)] = (int)j;   // j changed: next round's frontier
+      atomicAdd(ftot_out, 1);
       *any = 1;
     }
   }
@@ -735,17 +766,19 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
 template <typename T>
 cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw,
                          const int* gprow, const int* gpcol, const T* glb, int64_t nopen,
-                         const int64_t* rowoff, const int* fcnt_in, const int* fcol_in,
-                         int* fcnt_out, int* fcol_out, int* any, int sr, const DetectCounters* dc,
-                         cudaStream_t st) {
+                         const int64_t* rowoff, const int* fcnt_in, const int* ftot_in, const int* fcol_in,
+                         int* fcnt_out, int* ftot_out, int* fcol_out, int* any, int sr,
+                         const DetectCounters* dc, cudaStream_t st) {
   if (nopen <= 0) return cudaSuccess;
   int grid = (int)std::min<int64_t>(cdiv(nopen, 8), (int64_t)num_sms() * 8);
   if (sr)
     k_sparse_round<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff,
-                                               fcnt_in, fcol_in, fcnt_out, fcol_out, any, dc);
+                                               fcnt_in, ftot_in, fcol_in, fcnt_out, ftot_out, fcol_out, any,
+                                               dc);
   else
     k_sparse_round<T, 0><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff,
-                                               fcnt_in, fcol_in, fcnt_out, fcol_out, any, dc);
+                                               fcnt_in, ftot_in, fcol_in, fcnt_out, ftot_out, fcol_out, any,
+                                               dc);
   return cudaGetLastError();
 }
 
@@ -772,7 +805,7 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
                                       int64_t, int, const DetectCounters*, cudaStream_t);         \
   template cudaError_t sparse_round<T>(T*, int64_t, int64_t, const T*, int64_t, const int*,        \
                                        const int*, const T*, int64_t, const int64_t*, const int*,  \
-                                       const int*, int*, int*, int*, int,                          \
+                                       const int*, const int*, int*, int*, int*, int*, int,        \
                                        const DetectCounters*, cudaStream_t);
 INST(int32_t)
 INST(float)

@@ -98,12 +98,18 @@ typedef enum {
                                the all pairs minimax path problem").  Every call then
                                uses that algebra; D is NOT converted: set it before
                                apsp_cold_fw (or fill D with the matching matrix).    */
-  APSP_OPT_FW16 = 6         /* 1 (default): blocked FW on int32 shortest-path handles
+  APSP_OPT_FW16 = 6,        /* 1 (default): blocked FW on int32 shortest-path handles
                                on one GPU runs on a packed int16x2 copy of D (two
                                relaxations per VIADDMNMX.S16x2), exact for every
                                distance < 0x3FFF; if any entry saturates it finishes
                                in int32 — results are identical either way.
                                0: always int32.                                       */
+  APSP_OPT_MIRROR8 = 7      /* 1 (default): on int32 shortest-path handles the two
+                               O(n^2) streaming passes (add-node pass 1, detection)
+                               read an int8 copy of D while every finite distance is
+                               < 0x7F, else an int16 copy while every one is < 0x3FFF,
+                               else D itself; results are identical on every path.
+                               0: never int8 (int16 / int32 only).                    */
 } apsp_option;
 
 /* Statistics of one update. */
@@ -183,6 +189,14 @@ apsp_status apsp_set_option(apsp_handle* h, apsp_option opt, double value);
  * D must not be modified by the caller after an update call without calling
  * this (or apsp_cold_fw) again. */
 apsp_status apsp_sync_distances(apsp_handle* h);
+
+/* Width in bits (8 or 16) of the saturated copy of D the O(n^2) streaming
+ * passes read (APSP_OPT_MIRROR8), as last observed by the
+ * host (the validity flag is read at each update's host synchronisation);
+ * 0 when they read D itself (fp32 / minimax handles, no copy built yet, or the
+ * copy was invalidated by a distance at or above its saturation value).
+ * Returns -1 for a null handle.  Never blocks. */
+int32_t apsp_mirror_width(const apsp_handle* h);
 
 /* Cold start: D := APSP(W) by tiled blocked Floyd–Warshall (the comparator of
  * P:74/P:93/P:224).  Asynchronous. */

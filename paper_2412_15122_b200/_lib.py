@@ -19,7 +19,7 @@ STATUS = {
     0: "APSP_OK", 1: "APSP_E_INVAL", 2: "APSP_E_RANGE", 3: "APSP_E_CAPACITY", 4: "APSP_E_PRECOND",
     5: "APSP_E_CUDA", 6: "APSP_E_NCCL", 7: "APSP_E_NOMEM", 8: "APSP_E_POISONED", 9: "APSP_E_UNSUPPORTED",
 }
-OPT_FORCE_PATH, OPT_THETA, OPT_TAU, OPT_MAX_ROUNDS, OPT_ROW_DELTA, OPT_SEMIRING, OPT_FW16 = 0, 1, 2, 3, 4, 5, 6
+OPT_FORCE_PATH, OPT_THETA, OPT_TAU, OPT_MAX_ROUNDS, OPT_ROW_DELTA, OPT_SEMIRING, OPT_FW16, OPT_MIRROR8 = range(8)
 
 # exported symbols (tests check the library exports every one of them)
 SYMBOLS = [
@@ -29,7 +29,7 @@ SYMBOLS = [
     "apsp_nccl_unique_id", "apsp_kernel_launches", "apsp_profile_enable", "apsp_profile_reset",
     "apsp_profile_read", "apsp_modify_edge_readd", "apsp_get_weight",
     "apsp_local_group_create", "apsp_local_group_destroy", "apsp_create_local", "apsp_microbench",
-    "apsp_sync_distances",
+    "apsp_sync_distances", "apsp_mirror_width",
 ]
 # kernel classes of apsp_profile_read (apsp_kernel_class)
 K_CLASSES = ["fw_diag", "fw_panel", "fw_tile", "add_pass1", "rank1", "detect", "sparse0",
@@ -76,6 +76,7 @@ def _load():
         "apsp_set_option": (ctypes.c_int, [vp, ctypes.c_int, dbl]),
         "apsp_cold_fw": (ctypes.c_int, [vp]),
         "apsp_sync_distances": (ctypes.c_int, [vp]),
+        "apsp_mirror_width": (ctypes.c_int32, [vp]),
         "apsp_add_node": (ctypes.c_int, [vp, vp, vp, P(i64), P(UpdateInfo)]),
         "apsp_remove_node": (ctypes.c_int, [vp, i64, P(i64), P(UpdateInfo)]),
         "apsp_update_edge": (ctypes.c_int, [vp, i64, i64, dbl, P(UpdateInfo)]),
@@ -167,6 +168,10 @@ def apsp_set_option(h, opt, value):
 
 def apsp_sync_distances(h):
     check(h, lib.apsp_sync_distances(h))
+
+
+def apsp_mirror_width(h):
+    return int(lib.apsp_mirror_width(h))
 
 
 def apsp_cold_fw(h):

@@ -88,6 +88,11 @@ class WarmAPSP:
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         L.apsp_sync_distances(self.h)
 
+    @property
+    def mirror_width(self):
+        """Bits per entry of D's saturated copy the O(n^2) passes read (8, 16; 0: D itself)."""
+        return L.apsp_mirror_width(self.h)
+
     def close(self):
         if getattr(self, "h", None):
             L.apsp_destroy(self.h)

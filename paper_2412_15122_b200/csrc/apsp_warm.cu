@@ -41,7 +41,7 @@ struct Plan {
   size_t off_wt, off_vec, off_rowpart, off_colpart, off_rowoff, off_rowcnt, off_chg, off_prow,
       off_pcol, off_ocol, off_ocnt, off_gprow, off_gpcol, off_glb, off_gfull,
       off_srow, off_scol, off_slid, off_slw, off_wnext, off_panel, off_pt, off_anyrow, off_qsend, off_qcol,
-      off_qids, off_qdsv, off_qlab, off_qpred, off_qpath, off_qdone, off_qcnt, off_p16, off_ptd, off_small,
+      off_qids, off_qdsv, off_qlab, off_qpred, off_qpath, off_qdone, off_qcnt, off_p16, off_p8, off_ptd, off_small,
       total;
   int qcap, qbatch;
   int64_t ldpt;
@@ -104,6 +104,7 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   // int16x2 FW (one GPU): packed copy of D (two columns per word) + the
   // transposed diagonal tile
   p.off_p16 = take(sizeof(uint16_t) * (size_t)rows_max * p.ld);
+  p.off_p8 = take((size_t)rows_max * p.ld);   // the int8 mirror (int32 handles)
   p.off_ptd = take(sizeof(uint32_t) * (size_t)kTile * kTile);
   p.off_small = take(64 * 1024);
   p.total = o;
@@ -143,9 +144,13 @@ struct apsp_handle {
   int last_fw16 = 0;             // 1: the last FW ran packed, 2: it fell back to int32
   bool mirror_built = false;     // the int16 mirror was built (or invalidated) from D
   bool mirror_hint = false;      // last observed mirror state was "valid" (profile accounting only)
-  // bytes per entry the O(n^2) streams read: 2 on the valid int16 mirror, else 4
+  int mirror_level = 16;         // width of the mirror: 8 or 16 bits
+  int mirror8 = 1;               // APSP_OPT_MIRROR8: try the int8 width at each build
+  bool mirror8_failed = false;   // an int8 build found a distance >= 0x7F: int16 from then on
+  // bytes per entry the O(n^2) streams read: 1 / 2 on a valid int8 / int16 mirror, else 4
   template <typename T> double stream_bytes() const {
-    return (std::is_same<T, int32_t>::value && sr == 0 && mirror_hint) ? 2.0 : 4.0;
+    if (!(std::is_same<T, int32_t>::value && sr == 0 && mirror_hint)) return 4.0;
+    return mirror_level == 8 ? 1.0 : 2.0;
   }
   double row_delta = 0.0;        // > 0: the paper's Definition-1 gate (ablation)
   int sr = 0;                    // path algebra: 0 shortest path, 1 minimax
@@ -242,10 +247,15 @@ struct apsp_handle {
   unsigned* fw16_flag() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 392); }
   unsigned* mirror_flag() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 396); }
   unsigned* pass1_uncertain() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 400); }
-  // int16 mirror of D (kernels.h): int32 handles only; lives in the packed-FW buffer
+  // saturated mirror of D (kernels.h), int32 handles only: int8 (own buffer)
+  // or int16 (in the packed-FW buffer), the width picked at the last build
   template <typename T> Mirror mirror() {
-    if constexpr (std::is_same<T, int32_t>::value) return Mirror{reinterpret_cast<uint16_t*>(p16()), mirror_flag()};
-    else return Mirror{nullptr, mirror_flag()};
+    if constexpr (std::is_same<T, int32_t>::value) {
+      if (mirror_level == 8) return Mirror{nullptr, ws + plan.off_p8, mirror_flag()};
+      return Mirror{reinterpret_cast<uint16_t*>(p16()), nullptr, mirror_flag()};
+    } else {
+      return Mirror{nullptr, nullptr, mirror_flag()};
+    }
   }
   uint32_t* p16() { return reinterpret_cast<uint32_t*>(ws + plan.off_p16); }
   uint32_t* ptd() { return reinterpret_cast<uint32_t*>(ws + plan.off_ptd); }
@@ -376,20 +386,55 @@ apsp_status fw_impl_elem(apsp_handle* h);
 // the caller filled (warm start), and after an int32 FW.  Mirror flag bit 0
 // set iff some finite local distance is >= 0x3FFF, bit 1 iff some local entry
 // is INF (stream.cu: kMirrorOff, kMirrorInf).
+// The int8 width is tried first (unless an earlier int8 build failed): if some
+// finite distance is >= 0x7F the build is redone at int16 (one host read of
+// the flag; builds are rare — warm start, after an int32 FW).
+bool try_mirror8(const apsp_handle* h) { return h->mirror8 && !h->mirror8_failed && h->sr == 0; }
+
+// read the mirror flag; if the int8 build came out invalid, fall back to int16
+// for the rest of the handle's life (returns true if the caller must build it)
+apsp_status mirror8_settle(apsp_handle* h, bool* need16) {
+  unsigned* hf = reinterpret_cast<unsigned*>(h->host_small);
+  CKR(cudaMemcpyAsync(hf, h->mirror_flag(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+  CKR(cudaStreamSynchronize(h->st));
+  *need16 = (*hf & 1u) != 0u;
+  if (*need16) {
+    h->mirror8_failed = true;
+    h->mirror_level = 16;
+  }
+  return APSP_OK;
+}
+
 template <typename T>
 apsp_status mirror_rebuild(apsp_handle* h) {
   if constexpr (std::is_same<T, int32_t>::value) {
-    CKR(cudaMemsetAsync(h->mirror_flag(), 0, sizeof(unsigned), h->st));
-    // per rank: each rank's readers stream only its own rows
-    CK(mirror_build(h->Dl<int32_t>(), h->ld, h->active(), h->n, h->mirror<int32_t>(), h->st));
+    bool need16 = true;
+    if (try_mirror8(h)) {
+      h->mirror_level = 8;
+      CKR(cudaMemsetAsync(h->mirror_flag(), 0, sizeof(unsigned), h->st));
+      CK(mirror_build(h->Dl<int32_t>(), h->ld, h->active(), h->n, h->mirror<int32_t>(), h->st));
+      apsp_status s = mirror8_settle(h, &need16);
+      if (s != APSP_OK) return s;
+    }
+    if (need16) {
+      h->mirror_level = 16;
+      CKR(cudaMemsetAsync(h->mirror_flag(), 0, sizeof(unsigned), h->st));
+      // per rank: each rank's readers stream only its own rows
+      CK(mirror_build(h->Dl<int32_t>(), h->ld, h->active(), h->n, h->mirror<int32_t>(), h->st));
+    }
     h->mirror_hint = true;   // corrected at the next host read of the flag
   }
   h->mirror_built = true;
   return APSP_OK;
 }
+// Build the mirror if it was never built — or if it is the int8 one and the
+// host has seen it invalidated (a distance reached 0x7F): rebuilt once, it is
+// the int16 one from then on (an invalid int16 mirror stays invalid until a
+// FW or apsp_sync_distances rebuilds it: its distances are >= 0x3FFF).
 template <typename T>
 apsp_status ensure_mirror(apsp_handle* h) {
-  return h->mirror_built ? APSP_OK : mirror_rebuild<T>(h);
+  const bool stale8 = h->mirror_built && h->mirror_level == 8 && !h->mirror_hint;
+  return (h->mirror_built && !stale8) ? APSP_OK : mirror_rebuild<T>(h);
 }
 
 // int16x2 blocked FW (fw.cu) over the packed copy of this rank's rows, with the
@@ -452,7 +497,17 @@ apsp_status fw_impl(apsp_handle* h, int64_t skip = -1) {
       apsp_status s = fw16_impl(h, skip, &saturated);
       if (s != APSP_OK) return s;
       h->last_fw16 = saturated ? 2 : 1;
-      if (!saturated) {   // the packed buffer now holds sat16(D): the mirror is valid
+      if (!saturated) {   // the packed buffer now holds sat16(D): the int16 mirror is valid
+        bool need16 = true;
+        if (try_mirror8(h)) {   // narrow it to int8 if every distance is < 0x7F
+          h->mirror_level = 8;
+          CKR(cudaMemsetAsync(h->mirror_flag(), 0, sizeof(unsigned), h->st));
+          CK(mirror8_from_p16(h->p16(), h->ld, h->active().hi - h->active().lo, h->n, h->mirror<int32_t>(),
+                              h->st));
+          apsp_status s2 = mirror8_settle(h, &need16);
+          if (s2 != APSP_OK) return s2;
+        }
+        if (need16) h->mirror_level = 16;
         CKR(cudaMemsetAsync(h->mirror_flag(), 0, sizeof(unsigned), h->st));
         h->mirror_built = true;
         h->mirror_hint = true;
@@ -682,7 +737,7 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   unsigned* unc = h->pass1_uncertain();
   if (try_packed) {
     CKR(cudaMemsetAsync(unc, 0, sizeof(unsigned), h->st));
-    PK(APSP_K_ADD_PASS1, h->mirror_hint ? 2.0 * (double)(r.hi - r.lo) * (double)n : 0.0,
+    PK(APSP_K_ADD_PASS1, h->mirror_hint ? h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n : 0.0,
        addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
                         &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), unc, 1, h->st));
     CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
@@ -1233,12 +1288,24 @@ apsp_status apsp_set_option(apsp_handle* h, apsp_option opt, double value) {
       if (value != 0 && value != 1) return APSP_E_INVAL;
       h->fw16 = (int)value;
       return APSP_OK;
+    case APSP_OPT_MIRROR8:   // takes effect at the next mirror build
+      if (value != 0 && value != 1) return APSP_E_INVAL;
+      h->mirror8 = (int)value;
+      h->mirror8_failed = false;
+      if (!value && h->mirror_level == 8) h->mirror_built = false;   // rebuild at int16
+      return APSP_OK;
     case APSP_OPT_ROW_DELTA:
       if (!(value >= 0) || value > 1) return APSP_E_INVAL;
       h->row_delta = value;
       return APSP_OK;
   }
   return APSP_E_INVAL;
+}
+
+int32_t apsp_mirror_width(const apsp_handle* h) {
+  if (!h) return -1;
+  if (h->dt != APSP_I32 || h->sr != 0 || !h->mirror_built || !h->mirror_hint) return 0;
+  return h->mirror_level;
 }
 
 apsp_status apsp_sync_distances(apsp_handle* h) {

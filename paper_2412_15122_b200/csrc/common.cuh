@@ -181,6 +181,24 @@ __device__ __forceinline__ int64_t group_of(bool m16, int chunk, int v, int lane
   return m16 ? 2 * ((int64_t)chunk * 64 + (v >> 1) * 32 + lane) + (v & 1)
              : (int64_t)chunk * 128 + v * 32 + lane;
 }
+// int8 mirror: 8 values in one 8-byte streaming load, widened to the int16x2
+// words the packed arithmetic uses (halves 0..0x7F)
+constexpr int32_t kSat8i = 0x7F;
+__device__ __forceinline__ uint2 mload8b(const uint8_t* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 widen8(uint2 b) {
+  return make_uint4(__byte_perm(b.x, 0u, 0x4140), __byte_perm(b.x, 0u, 0x4342),
+                    __byte_perm(b.y, 0u, 0x4140), __byte_perm(b.y, 0u, 0x4342));
+}
+// int16x2 word with halves <= 0x7F: halves equal to 0x7F (int8 INF) -> 0x3FFF
+__device__ __forceinline__ uint32_t inf8to16(uint32_t x) {
+  const uint32_t t = x ^ 0x007F007Fu;   // zero half <-> INF
+  const uint32_t nz = (t | ((t & 0x7FFF7FFFu) + 0x7FFF7FFFu)) & 0x80008000u;
+  return x | (((~nz & 0x80008000u) >> 15) * 0x3FFFu);
+}
 __device__ __forceinline__ uint2 mload4(const uint16_t* p) {
   uint2 r;
   asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));

@@ -5,14 +5,18 @@
 
 namespace apsp {
 
-// int16 mirror of an int32 D (same element indexing, ld int16 per row): every
-// value v stored as min(v, 0x3FFF), INF as 0x3FFF.  It is exact — and the two
-// O(n^2) streaming passes (add-node pass 1, detection) read it at half the
-// bytes — while *flag == 0, i.e. while every finite distance is < 0x3FFF.
-// Writers of D keep it in step and raise *flag on a finite value >= 0x3FFF.
+// Saturated mirror of an int32 D (same element indexing, ld elements per row)
+// at one of two widths: int16 (m: v stored as min(v, 0x3FFF), INF as 0x3FFF)
+// or int8 (m8: min(v, 0x7F), INF as 0x7F).  It is exact — and the two O(n^2)
+// streaming passes (add-node pass 1, detection) read it at a half / a quarter
+// of the bytes — while bit 0 of *flag is clear, i.e. while every finite
+// distance is below the width's saturation value.  Writers of D keep it in
+// step and raise the bit on a finite value at or above it.  At most one of m,
+// m8 is set (the host picks the width when it builds the mirror).
 struct Mirror {
-  uint16_t* m;      // nullptr: no mirror (fp32 handles)
-  unsigned* flag;   // 0: m mirrors D exactly
+  uint16_t* m;      // int16 level (nullptr: not this width / no mirror)
+  uint8_t* m8;      // int8 level
+  unsigned* flag;   // bit 0 clear: the mirror images D exactly
 };
 
 // Device counters written by the detection kernel.
@@ -200,6 +204,8 @@ cudaError_t query_colslice(const T* D, int64_t ld, int64_t rows, int64_t R, int6
 // int16 mirror upkeep (stream.cu): build from D (flag must be 0 before), re-sync
 // the listed pairs / one row and one column (-1: none) after D changed there
 cudaError_t mirror_build(const int32_t* D, int64_t ld, Rows r, int64_t n, Mirror M, cudaStream_t st);
+// int8 mirror from the packed int16 buffer (after a packed FW left sat16(D) there)
+cudaError_t mirror8_from_p16(const uint32_t* P, int64_t ld, int64_t m, int64_t n, Mirror M, cudaStream_t st);
 cudaError_t mirror_pairs(const int32_t* D, int64_t ld, int64_t row0, const int* prow, const int* pcol,
                          const DetectCounters* ctr, int64_t lcap, Mirror M, cudaStream_t st);
 cudaError_t mirror_cross(const int32_t* D, int64_t ld, Rows r, int64_t n, int64_t row, int64_t col, Mirror M,

@@ -253,9 +253,14 @@ static Tiling make_tiling(int64_t n, int64_t rows, int max_slabs, int chunk_vec 
 // them per thread and post them once per warp (mirror_post).
 constexpr unsigned kMirrorOff = 1u, kMirrorInf = 2u;
 __device__ __forceinline__ unsigned mput(const Mirror& M, int64_t idx, int32_t v) {
+  if (M.m8) {
+    M.m8[idx] = (uint8_t)min(v, kSat8i);
+    return v >= APSP_INF_I32_DEV ? kMirrorInf : (v >= kSat8i ? kMirrorOff : 0u);
+  }
   M.m[idx] = sat16(v);
   return v >= APSP_INF_I32_DEV ? kMirrorInf : (v >= kSat16i ? kMirrorOff : 0u);
 }
+__device__ __forceinline__ bool has_mirror(const Mirror& M) { return M.m != nullptr || M.m8 != nullptr; }
 __device__ __forceinline__ unsigned mput(const Mirror&, int64_t, float) { return 0u; }
 __device__ __forceinline__ void mirror_post(const Mirror& M, unsigned bits) {
   bits = __reduce_or_sync(0xffffffffu, bits);
@@ -273,16 +278,47 @@ __global__ void k_mirror_build(const int32_t* __restrict__ D, int64_t ld, Rows r
     const int64_t li = (r.lo - r.row0) + e / n4, c = 4 * (e % n4);
     const int4 v = *reinterpret_cast<const int4*>(D + li * ld + c);
     const int vv[4] = {v.x, v.y, v.z, v.w};
-    unsigned w[2] = {0, 0};
+    const int32_t satv = M.m8 ? kSat8i : kSat16i;
+    unsigned w[2] = {0, 0}, b8 = 0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (c + q < n)
-        bits |= vv[q] >= APSP_INF_I32_DEV ? kMirrorInf : (vv[q] >= kSat16i ? kMirrorOff : 0u);
+        bits |= vv[q] >= APSP_INF_I32_DEV ? kMirrorInf : (vv[q] >= satv ? kMirrorOff : 0u);
       w[q >> 1] |= (unsigned)sat16(vv[q]) << (16 * (q & 1));
+      b8 |= (unsigned)min(vv[q], kSat8i) << (8 * q);
     }
-    *reinterpret_cast<uint2*>(M.m + li * ld + c) = make_uint2(w[0], w[1]);
+    if (M.m8) *reinterpret_cast<uint32_t*>(M.m8 + li * ld + c) = b8;
+    else *reinterpret_cast<uint2*>(M.m + li * ld + c) = make_uint2(w[0], w[1]);
   }
   mirror_post(M, bits);
+}
+// M8 := the int8 image of the packed int16 buffer P (sat16(D) after a packed
+// FW): a half h becomes min(h, 0x7F); 0x3FFF (INF or saturated) stays INF-like
+__global__ void k_mirror8_from_p16(const uint32_t* __restrict__ P, int64_t ld, int64_t m, int64_t n,
+                                   Mirror M) {
+  const int64_t n4 = (n + 3) / 4, tot = m * n4;
+  unsigned bits = 0;
+  for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x; e0 < tot; e0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = e0 + threadIdx.x;
+    if (e >= tot) continue;
+    const int64_t li = e / n4, c = 4 * (e % n4);
+    const uint2 v = *reinterpret_cast<const uint2*>(P + li * (ld / 2) + c / 2);
+    const unsigned h[4] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16};
+    unsigned b8 = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (c + q < n)
+        bits |= h[q] >= (unsigned)kSat16i ? kMirrorInf : (h[q] >= (unsigned)kSat8i ? kMirrorOff : 0u);
+      b8 |= min(h[q], (unsigned)kSat8i) << (8 * q);
+    }
+    *reinterpret_cast<uint32_t*>(M.m8 + li * ld + c) = b8;
+  }
+  mirror_post(M, bits);
+}
+cudaError_t mirror8_from_p16(const uint32_t* P, int64_t ld, int64_t m, int64_t n, Mirror M, cudaStream_t st) {
+  if (m <= 0 || !M.m8) return cudaSuccess;
+  k_mirror8_from_p16<<<num_sms() * 8, 256, 0, st>>>(P, ld, m, n, M);
+  return cudaGetLastError();
 }
 // M[i][j] := sat16(D[i][j]) for the listed pairs (the sparse recompute's writes)
 __global__ void k_mirror_pairs(const int32_t* __restrict__ D, int64_t ld, int64_t row0,
@@ -357,23 +393,46 @@ __device__ __forceinline__ T max_add(T m, T d, T w) {
 // which keeps the row skip of pass 2 safe.
 template <typename T, int SR>
 __device__ __forceinline__ bool pass1_packed_done(const Mirror& M, const unsigned* uncertain) {
-  return SR == 0 && std::is_same<T, int32_t>::value && M.m != nullptr &&
+  return SR == 0 && std::is_same<T, int32_t>::value && has_mirror(M) &&
          (*(volatile unsigned*)M.flag & kMirrorOff) == 0u &&
          (uncertain == nullptr || *(volatile unsigned*)uncertain == 0u);
 }
 template <typename T, int SR>
 __device__ __forceinline__ bool pass1_packed_runs(const Mirror& M) {
-  return SR == 0 && std::is_same<T, int32_t>::value && M.m != nullptr &&
+  return SR == 0 && std::is_same<T, int32_t>::value && has_mirror(M) &&
          (*(volatile unsigned*)M.flag & kMirrorOff) == 0u;
 }
 
-template <typename T>
+// The packed readers at either mirror width (EW bytes per value): a column
+// group (8 values) is one 16-byte (int16) or 8-byte (int8) load, widened to
+// four int16x2 words; int8 reads keep twice as many rows in flight.
+template <int EW> struct MW;
+template <> struct MW<2> {
+  using E = uint16_t;
+  using Raw = uint4;
+  static constexpr int kRows = 4;
+  __device__ static __forceinline__ const E* base(const Mirror& M) { return M.m; }
+  __device__ static __forceinline__ Raw load(const E* p) { return mload8(p); }
+  __device__ static __forceinline__ Raw sat() { return make_uint4(0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu); }
+  __device__ static __forceinline__ uint4 widen(Raw r) { return r; }
+};
+template <> struct MW<1> {
+  using E = uint8_t;
+  using Raw = uint2;
+  static constexpr int kRows = 8;
+  __device__ static __forceinline__ const E* base(const Mirror& M) { return M.m8; }
+  __device__ static __forceinline__ Raw load(const E* p) { return mload8b(p); }
+  __device__ static __forceinline__ Raw sat() { return make_uint2(0x7F7F7F7Fu, 0x7F7F7F7Fu); }
+  __device__ static __forceinline__ uint4 widen(Raw r) { return widen8(r); }
+};
+
+template <typename T, int EW>
 __global__ void __launch_bounds__(256, 2) k_addnode_pass1_p16(Rows r, int64_t ld, int64_t n, Tiling tl,
                                                               const T* __restrict__ ow,
                                                               const T* __restrict__ iw, T* rowpart,
                                                               T* rowpartM, T* colpart, int64_t part_ld,
                                                               Mirror M) {
-  if (!pass1_packed_runs<T, 0>(M)) return;
+  if (!pass1_packed_runs<T, 0>(M) || MW<EW>::base(M) == nullptr) return;
   const bool has_inf = (*(volatile unsigned*)M.flag & kMirrorInf) != 0u;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
@@ -408,26 +467,31 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1_p16(Rows r, int64_t ld
   }
   // this lane's two 16-byte column groups of row i_lo; rows are ld apart
   const bool ok0 = qv[0] < tl.n4, ok1 = qv[2] < tl.n4;
-  const uint16_t* m0 = M.m + (i_lo - r.row0) * ld + 4 * qv[0];
-  const uint16_t* m1 = M.m + (i_lo - r.row0) * ld + 4 * qv[2];
+  using W = MW<EW>;
+  constexpr int RB = W::kRows;
+  const typename W::E* m0 = W::base(M) + (i_lo - r.row0) * ld + 4 * qv[0];
+  const typename W::E* m1 = W::base(M) + (i_lo - r.row0) * ld + 4 * qv[2];
   const T* owr = ow + i_lo;
   T* rp_out = rowpart + (int64_t)chunk * part_ld + i_lo;
   T* rm_out = rowpartM + (int64_t)chunk * part_ld + i_lo;
-  const uint4 sat = make_uint4(SAT2, SAT2, SAT2, SAT2);
-  for (int rr = 0; rr < rows; rr += 4) {
-    uint4 w[4][2];
+  for (int rr = 0; rr < rows; rr += RB) {
+    typename W::Raw w[RB][2];
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
+    for (int h = 0; h < RB; ++h) {
       const bool in = rr + h < rows;
-      w[h][0] = (in && ok0) ? mload8(m0 + (int64_t)(rr + h) * ld) : sat;
-      w[h][1] = (in && ok1) ? mload8(m1 + (int64_t)(rr + h) * ld) : sat;
+      w[h][0] = (in && ok0) ? W::load(m0 + (int64_t)(rr + h) * ld) : W::sat();
+      w[h][1] = (in && ok1) ? W::load(m1 + (int64_t)(rr + h) * ld) : W::sat();
     }
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
+    for (int h = 0; h < RB; ++h) {
       if (rr + h >= rows) break;
       const uint32_t orep = (uint32_t)sat16((int32_t)owr[rr + h]) * 0x10001u;
-      uint32_t dw[8] = {w[h][0].x, w[h][0].y, w[h][0].z, w[h][0].w,
-                        w[h][1].x, w[h][1].y, w[h][1].z, w[h][1].w};
+      const uint4 u0 = W::widen(w[h][0]), u1 = W::widen(w[h][1]);
+      uint32_t dw[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+      if (EW == 1 && has_inf) {   // int8 INF (0x7F) reads as the int16 INF (0x3FFF)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dw[q] = inf8to16(dw[q]);
+      }
       if (tail) {   // the row's last chunk: columns >= n hold no mirrored value
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -472,6 +536,127 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1_p16(Rows r, int64_t ld
       T* dst = colpart + (int64_t)slab * part_ld + j0;
       dst[0] = (T)(colp2[q] & 0xFFFFu);
       dst[1] = (T)(colp2[q] >> 16);
+    }
+  }
+}
+
+// Add-node pass 1 on the int8 mirror: the arithmetic of k_addnode_pass1_p16
+// on widened words, with a warp owning 1024 columns of a row (lane l: the
+// 16-column groups at 16 l and 512 + 16 l) so that the per-row work — the two
+// warp reductions, the out[i] operand — is spread over twice the columns; the
+// per-row results are kept by lane (row & 31) and stored 32 rows at a time.
+constexpr int P8A_RB = 8;   // rows in flight per lane (one CTA of 8 warps per SM: 64 KB in flight)
+template <typename T>
+__global__ void __launch_bounds__(256, 1) k_addnode_pass1_p8(Rows r, int64_t ld, int64_t n, Tiling tl,
+                                                             const T* __restrict__ ow,
+                                                             const T* __restrict__ iw, T* rowpart,
+                                                             T* rowpartM, T* colpart, int64_t part_ld,
+                                                             Mirror M) {
+  if (!pass1_packed_runs<T, 0>(M) || M.m8 == nullptr) return;
+  const bool has_inf = (*(volatile unsigned*)M.flag & kMirrorInf) != 0u;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gw >= tl.warps) return;
+  const int chunk = (int)(gw % tl.nchunk);
+  const int slab = (int)(gw / tl.nchunk);
+  const int64_t i_lo = r.lo + slab * tl.slab;
+  const int rows = (int)max((int64_t)0, min(r.hi, i_lo + tl.slab) - i_lo);
+  constexpr uint32_t SAT2 = 0x3FFF3FFFu;
+  const int64_t g0 = (int64_t)chunk * 1024 + 16 * lane;
+  // word q (0..15): columns g0 + (q >> 3) * 512 + (q & 7) * 2 + {0, 1}
+  auto colq = [&](int q) -> int64_t { return g0 + (q >> 3) * 512 + (q & 7) * 2; };
+  uint32_t in2[16], nout2[16], colp2[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    uint32_t a = 0, b = 0;
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      const int64_t j = colq(q) + hf;
+      const uint32_t iv = j < n ? (uint32_t)sat16((int32_t)iw[j]) : 0x3FFFu;
+      const uint32_t ov = j < n ? (uint32_t)sat16((int32_t)ow[j]) : 0x3FFFu;
+      a |= iv << (16 * hf);
+      b |= ((0x10000u - ov) & 0xFFFFu) << (16 * hf);   // -out as int16
+    }
+    in2[q] = a; nout2[q] = b; colp2[q] = SAT2;
+  }
+  const bool tail = (int64_t)(chunk + 1) * 1024 > n;   // this chunk holds columns >= n
+  const bool ok0 = g0 < n, ok1 = g0 + 512 < n;
+  const uint8_t* mb = M.m8 + (i_lo - r.row0) * ld + g0;
+  const uint4 satb = make_uint4(0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu);
+  T* rp_out = rowpart + (int64_t)chunk * part_ld + i_lo;
+  T* rm_out = rowpartM + (int64_t)chunk * part_ld + i_lo;
+  for (int rr = 0; rr < rows; rr += 32) {
+    const int r32 = min(32, rows - rr);
+    // out[i] of the 32 rows, one per lane; the row results, kept by lane (row & 31)
+    const uint32_t ol = lane < r32 ? (uint32_t)sat16((int32_t)ow[i_lo + rr + lane]) * 0x10001u : SAT2;
+    int keep_p = 0, keep_m = 0;
+    for (int hb = 0; hb < r32; hb += P8A_RB) {
+      uint4 w[P8A_RB][2];
+#pragma unroll
+      for (int h = 0; h < P8A_RB; ++h) {
+        const bool in = hb + h < r32;
+        const uint8_t* p = mb + (int64_t)(rr + hb + h) * ld;
+        w[h][0] = (in && ok0) ? mload8(reinterpret_cast<const uint16_t*>(p)) : satb;
+        w[h][1] = (in && ok1) ? mload8(reinterpret_cast<const uint16_t*>(p + 512)) : satb;
+      }
+#pragma unroll
+      for (int h = 0; h < P8A_RB; ++h) {
+        if (hb + h >= r32) break;
+        const uint32_t orep = __shfl_sync(0xffffffffu, ol, hb + h);
+        uint32_t dw[16];
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          const uint4 b = w[h][g];
+          const uint4 lo = widen8(make_uint2(b.x, b.y)), hi = widen8(make_uint2(b.z, b.w));
+          dw[8 * g + 0] = lo.x; dw[8 * g + 1] = lo.y; dw[8 * g + 2] = lo.z; dw[8 * g + 3] = lo.w;
+          dw[8 * g + 4] = hi.x; dw[8 * g + 5] = hi.y; dw[8 * g + 6] = hi.z; dw[8 * g + 7] = hi.w;
+        }
+        if (has_inf) {   // int8 INF (0x7F) reads as the int16 INF (0x3FFF)
+#pragma unroll
+          for (int q = 0; q < 16; ++q) dw[q] = inf8to16(dw[q]);
+        }
+        if (tail) {   // columns >= n hold no mirrored value
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int64_t j0 = colq(q);
+            const uint32_t pm = (j0 < n ? 0u : 0xFFFFu) | (j0 + 1 < n ? 0u : 0xFFFF0000u);
+            dw[q] = (dw[q] & ~pm) | (SAT2 & pm);
+          }
+        }
+        uint32_t p2 = SAT2, m2 = 0xC001C001u /* -16383 */, inf = 0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          p2 = __viaddmin_s16x2(dw[q], in2[q], p2);
+          m2 = __viaddmax_s16x2(dw[q], nout2[q], m2);
+          colp2[q] = __viaddmin_s16x2(orep, dw[q], colp2[q]);
+        }
+        if (has_inf) {   // D == INF with a finite out: no row skip (see k_addnode_pass1_p16)
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const uint32_t satnf = ((nout2[q] & 0xFFFFu) == 0xC001u ? 0x3FFFu : 0x3FFEu) |
+                                   ((nout2[q] >> 16) == 0xC001u ? 0x3FFF0000u : 0x3FFE0000u);
+            inf |= __vmins2(dw[q], satnf) ^ dw[q];
+          }
+        }
+        const int pl = (int)min(p2 & 0xFFFFu, p2 >> 16);
+        const int ml = inf ? (int)Tr<T>::inf() : max((int)(short)(m2 & 0xFFFFu), (int)(short)(m2 >> 16));
+        const int pr = (int)__reduce_min_sync(0xffffffffu, (unsigned)pl);
+        const int mr = __reduce_max_sync(0xffffffffu, ml);
+        if (lane == hb + h) { keep_p = pr; keep_m = mr; }
+      }
+    }
+    if (lane < r32) {
+      rp_out[rr + lane] = (T)keep_p;
+      rm_out[rr + lane] = (T)keep_m;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int64_t j0 = colq(q);
+    if (j0 < n) {
+      T* dst = colpart + (int64_t)slab * part_ld + j0;
+      dst[0] = (T)(colp2[q] & 0xFFFFu);
+      if (j0 + 1 < n) dst[1] = (T)(colp2[q] >> 16);
     }
   }
 }
@@ -628,7 +813,9 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
                           T* rowpart, T* rowpartM, T* colpart, int64_t part_ld, int* nchunk_out,
                           int* nslab_out, int max_slabs, int sr, Mirror M, const unsigned* uncertain,
                           int packed, cudaStream_t st) {
-  Tiling tl = make_tiling(n, r.hi - r.lo, max_slabs, P1_VEC, tune_wps("APSP_TUNE_P1_WPS", 16));
+  const bool p8 = packed && !sr && M.m8 != nullptr;   // int8 mirror: 1024-column chunks
+  Tiling tl = p8 ? make_tiling(n, r.hi - r.lo, max_slabs, 256, tune_wps("APSP_TUNE_P8_WPS", 8))
+                 : make_tiling(n, r.hi - r.lo, max_slabs, P1_VEC, tune_wps("APSP_TUNE_P1_WPS", 16));
   *nchunk_out = tl.nchunk;
   *nslab_out = tl.nslab;
   if (r.hi <= r.lo) {
@@ -641,9 +828,12 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
   if (sr)
     k_addnode_pass1<T, 1><<<grid, 256, 0, st>>>(D, ld, r, n, tl, ow, iw, rowpart, rowpartM, colpart,
                                                 part_ld, M, uncertain);
-  else if (packed)   // on the mirror (exits unless it is valid)
-    k_addnode_pass1_p16<T><<<grid, 256, 0, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
-                                                 part_ld, M);
+  else if (p8)   // on the mirror (exits unless it is valid)
+    k_addnode_pass1_p8<T><<<grid, 256, 0, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
+                                                part_ld, M);
+  else if (packed)
+    k_addnode_pass1_p16<T, 2><<<grid, 256, 0, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
+                                                    part_ld, M);
   else   // int32 (exits if the packed pass ran and came out certain)
     k_addnode_pass1<T, 0><<<grid, 256, 0, st>>>(D, ld, r, n, tl, ow, iw, rowpart, rowpartM, colpart,
                                                 part_ld, M, uncertain);
@@ -779,14 +969,14 @@ __global__ void __launch_bounds__(256) k_rank1(T* __restrict__ D, int64_t ld, Ro
       }
       if (o.x != d[v].x || o.y != d[v].y || o.z != d[v].z || o.w != d[v].w) {
         st4<T>(row + 4 * qv[v], o);
-        if (M.m) {
+        if (has_mirror(M)) {
           const int64_t idx = (i - r.row0) * ld + 4 * qv[v];
           mbits |= mput(M, idx, o.x) | mput(M, idx + 1, o.y) | mput(M, idx + 2, o.z) | mput(M, idx + 3, o.w);
         }
       }
     }
   }
-  if (M.m) mirror_post(M, mbits);
+  if (has_mirror(M)) mirror_post(M, mbits);
   if (bytes_read && lane == 0 && rows_read) {
     const int64_t cols = min((int64_t)CHUNK_VEC * 4, n - (int64_t)chunk * CHUNK_VEC * 4);
     atomicAdd(bytes_read, (unsigned long long)(rows_read * cols * (int64_t)sizeof(T)));
@@ -901,13 +1091,27 @@ struct DetectOut {
 // appends them to the global list with ONE atomic on the list cursor per
 // flush (a single hot address otherwise hit once per (row, chunk) with flags).
 constexpr int DS_Q = 256;   // queued lane words per warp (>= 32: one row always fits)
-struct DetectQueue {
-  unsigned rl[DS_Q];        // (row - slab start) << 5 | lane
-  unsigned short w[DS_Q];   // flag word: bit v*4+c <-> column 4*group_of(m16, chunk, v, lane) + c
+template <typename WT>
+struct DetectQueueT {
+  unsigned rl[DS_Q];   // (row - slab start) << 5 | lane
+  WT w[DS_Q];          // flag word; its bit -> column mapping belongs to the kernel
 };
+// int32 / int16 readers: bit v*4+c <-> column 4*group_of(m16, chunk, v, lane) + c
+using DetectQueue = DetectQueueT<unsigned short>;
+
+template <typename T, typename WT, typename ColOf>
+__device__ __forceinline__ void detect_flush_q(const DetectQueueT<WT>& Q, int cnt, int64_t i_lo,
+                                               const DetectOut<T>& o, int lane, ColOf col_of);
 template <typename T>
 __device__ __forceinline__ void detect_flush(const DetectQueue& Q, int cnt, int64_t i_lo, int chunk,
                                              bool m16, const DetectOut<T>& o, int lane) {
+  detect_flush_q<T>(Q, cnt, i_lo, o, lane, [&](int bit, int ln) -> int64_t {
+    return 4 * group_of(m16, chunk, bit >> 2, ln) + (bit & 3);
+  });
+}
+template <typename T, typename WT, typename ColOf>
+__device__ __forceinline__ void detect_flush_q(const DetectQueueT<WT>& Q, int cnt, int64_t i_lo,
+                                               const DetectOut<T>& o, int lane, ColOf col_of) {
   if (cnt == 0) return;
   __syncwarp();
   // lane e takes queue entries e, e+32, ...: count its pairs, scan, one atomic
@@ -935,7 +1139,7 @@ __device__ __forceinline__ void detect_flush(const DetectQueue& Q, int cnt, int6
     while (w) {
       const int bit = __ffs(w) - 1;
       w &= w - 1;
-      const int64_t j = 4 * group_of(m16, chunk, bit >> 2, ln) + (bit & 3);
+      const int64_t j = col_of(bit, ln);
       if (pos < o.lcap) {
         o.prow[pos] = (int)i;
         o.pcol[pos] = (int)j;   // D_old[i][j] (the lower bound) is read by phase A
@@ -951,7 +1155,7 @@ __device__ __forceinline__ void detect_flush(const DetectQueue& Q, int cnt, int6
 // is only known there), each of the two kernels exits when the other applies.
 template <typename T, int SR, int MODE>
 __device__ __forceinline__ bool detect_uses_mirror(const Mirror& M) {
-  return MODE != 2 && SR == 0 && std::is_same<T, int32_t>::value && M.m != nullptr &&
+  return MODE != 2 && SR == 0 && std::is_same<T, int32_t>::value && has_mirror(M) &&
          (*(volatile unsigned*)M.flag & kMirrorOff) == 0u;
 }
 
@@ -972,8 +1176,10 @@ __global__ void __launch_bounds__(256, 2) k_detect_stream(T* __restrict__ D, int
   // kernel) does the shortest-path detection on it and this kernel exits.
   if (detect_uses_mirror<T, SR, MODE>(o.M)) return;
   const bool m16 = false;
-  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (gw >= tl.warps) return;
+  // grid-stride over the (chunk, slab) tasks: with a mirror present this
+  // kernel is usually the no-op twin of the packed one, launched small
+  for (int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); gw < tl.warps;
+       gw += (int64_t)gridDim.x * (blockDim.x >> 5)) {
   const int chunk = (int)(gw % tl.nchunk);
   const int slab = (int)(gw / tl.nchunk);
   const int64_t i_lo = r.lo + slab * tl.slab;
@@ -1054,18 +1260,20 @@ __global__ void __launch_bounds__(256, 2) k_detect_stream(T* __restrict__ D, int
       process2(i0, d, act);
     }
   if (MODE == 1) detect_flush<T>(Q, qcnt, i_lo, chunk, m16, o, lane);
+  qcnt = 0;
+  }
 }
 
 // k_detect_stream on the int16 mirror in packed int16x2 arithmetic (modes 0
 // and 1, shortest path, int32 D).  A kernel of its own so that its smaller
 // register footprint gives 3 CTAs per SM: four rows of 16-byte loads in flight
 // per lane and 24 warps per SM keep the halved byte stream at HBM speed.
-template <typename T, bool TWO, int MODE>
+template <typename T, bool TWO, int MODE, int EW>
 __global__ void __launch_bounds__(256, 3) k_detect_p16(T* __restrict__ D, int64_t ld, Rows r, int64_t n,
                                                        int64_t skip, Tiling tl, const T* __restrict__ c1,
                                                        const T* __restrict__ r1, const T* __restrict__ c2,
                                                        const T* __restrict__ r2, float tau, DetectOut<T> o) {
-  if (!detect_uses_mirror<T, 0, MODE>(o.M)) return;
+  if (!detect_uses_mirror<T, 0, MODE>(o.M) || MW<EW>::base(o.M) == nullptr) return;
   __shared__ DetectQueue sq[MODE == 1 ? 8 : 1];
   const int lane = threadIdx.x & 31;
   DetectQueue& Q = sq[MODE == 1 ? (threadIdx.x >> 5) : 0];
@@ -1104,32 +1312,35 @@ __global__ void __launch_bounds__(256, 3) k_detect_p16(T* __restrict__ D, int64_
       const int64_t j = 4 * qv[b >> 2] + (b & 3);
       if (j < n && j != skip) vmask |= 1u << b;
     }
-    const uint4 sat = make_uint4(0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu);
+    // int8 mirror: INF reads as 0x7F, not 0x3FFF — no test changes: an INF
+    // D[i][j] has c or r INF (D <= c + r), and then c + r - 1 >= 0x3FFE > 0x7F
+    using W = MW<EW>;
+    constexpr int RB = W::kRows;
     const int rows = (int)max((int64_t)0, i_hi - i_lo);
     const bool ok0 = qv[0] < tl.n4, ok1 = qv[2] < tl.n4;
-    const uint16_t* mb0 = o.M.m + (i_lo - r.row0) * ld + 4 * qv[0];
-    const uint16_t* mb1 = o.M.m + (i_lo - r.row0) * ld + 4 * qv[2];
+    const typename W::E* mb0 = W::base(o.M) + (i_lo - r.row0) * ld + 4 * qv[0];
+    const typename W::E* mb1 = W::base(o.M) + (i_lo - r.row0) * ld + 4 * qv[2];
     const int rskip = (skip >= i_lo && skip < i_hi) ? (int)(skip - i_lo) : -1;
     // column i of row i (the diagonal) in this lane's bits, per row: i >> 9 is
     // the chunk, (i >> 3) & 31 the lane, ((i >> 8) & 1) * 8 + (i & 7) the bit
-    for (int rr = 0; rr < rows; rr += 4) {
-      uint4 w[4][DS_V / 2];
+    for (int rr = 0; rr < rows; rr += RB) {
+      typename W::Raw w[RB][DS_V / 2];
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
+      for (int h = 0; h < RB; ++h) {
         const bool in = rr + h < rows && rr + h != rskip;
-        w[h][0] = (in && ok0) ? mload8(mb0 + (int64_t)(rr + h) * ld) : sat;
-        w[h][1] = (in && ok1) ? mload8(mb1 + (int64_t)(rr + h) * ld) : sat;
+        w[h][0] = (in && ok0) ? W::load(mb0 + (int64_t)(rr + h) * ld) : W::sat();
+        w[h][1] = (in && ok1) ? W::load(mb1 + (int64_t)(rr + h) * ld) : W::sat();
       }
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
+      for (int h = 0; h < RB; ++h) {
         if (rr + h >= rows) break;
         const T ci = c1[i_lo + rr + h];
         const T cj = TWO ? c2[i_lo + rr + h] : I;
         const bool act = rr + h != rskip && (Tr<T>::fin(ci) || Tr<T>::fin(cj));
         const uint32_t cr = (uint32_t)sat16((int32_t)ci) * 0x10001u;
         const uint32_t cr2 = TWO ? (uint32_t)sat16((int32_t)cj) * 0x10001u : 0u;
-        const uint32_t dw[DS_V * 2] = {w[h][0].x, w[h][0].y, w[h][0].z, w[h][0].w,
-                                       w[h][1].x, w[h][1].y, w[h][1].z, w[h][1].w};
+        const uint4 u0 = W::widen(w[h][0]), u1 = W::widen(w[h][1]);
+        const uint32_t dw[DS_V * 2] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
         uint32_t any = 0;
 #pragma unroll
         for (int q = 0; q < DS_V * 2; ++q) {
@@ -1206,6 +1417,140 @@ __global__ void k_detect_rows(Rows r, const int* __restrict__ rowcnt, int64_t* r
   }
 }
 
+// Detection on the int8 mirror (modes 0/1, shortest path, int32 D) in SWAR
+// byte arithmetic — the int8 stream is too cheap in bytes for the widen +
+// VIADDMNMX form, which made it ALU-bound.  Per byte, with s = c + r (every
+// value <= 0x7F, so s <= 0xFE: no carry between bytes) and d the mirrored
+// D[i][j]: D <= c + r gives s >= d in every byte (an INF d = 0x7F needs c or
+// r INF, then s >= 0x7F), so u = s - d has no borrows either, and the entry is
+// tight iff its byte of u is 0.  Per 4 entries:
+//   u = c + r - d,  v = c + (r - 0x01010101) - d (= u - 0x01010101)   IADD3 x2
+//   acc |= v & ~u                                                     LOP3
+// (the classic exact "some byte is zero" test); only a batch of rows whose
+// acc has a byte flag set recomputes the exact per-byte flags.  A warp owns
+// 1024 columns of a row: lane l the 16-byte groups at 16 l and 512 + 16 l.
+// Row k (the removed node) is given c = INF: then u >= 0x7F - ... never 0
+// there (its d equals r), and the diagonal is masked in the rare path.
+constexpr int P8_RB = 4;   // rows per batch (two 16-byte loads each in flight)
+template <typename T, bool TWO, int MODE>
+__global__ void __launch_bounds__(256, 3) k_detect_p8(Rows r, int64_t ld, int64_t n, int64_t skip, Tiling tl,
+                                                      const T* __restrict__ c1, const T* __restrict__ r1,
+                                                      const T* __restrict__ c2, const T* __restrict__ r2,
+                                                      DetectOut<T> o) {
+  if (!detect_uses_mirror<T, 0, MODE>(o.M) || o.M.m8 == nullptr) return;
+  __shared__ DetectQueueT<unsigned> sq[MODE == 1 ? 8 : 1];
+  const int lane = threadIdx.x & 31;
+  DetectQueueT<unsigned>& Q = sq[MODE == 1 ? (threadIdx.x >> 5) : 0];
+  int qcnt = 0;
+  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gw >= tl.warps) return;
+  const int chunk = (int)(gw % tl.nchunk);
+  const int slab = (int)(gw / tl.nchunk);
+  const int64_t i_lo = r.lo + slab * tl.slab;
+  const int64_t i_hi = min(r.hi, i_lo + tl.slab);
+  const int rows = (int)max((int64_t)0, i_hi - i_lo);
+  // this lane's columns: g0 + [0, 16) and g0 + 512 + [0, 16)
+  const int64_t g0 = (int64_t)chunk * 1024 + 16 * lane;
+  auto col_of = [&](int bit, int ln) -> int64_t {
+    return (int64_t)chunk * 1024 + 16 * ln + (bit >> 4) * 512 + (bit & 15);
+  };
+  auto s8 = [](T v) -> uint32_t { return (uint32_t)min((int32_t)v, kSat8i); };
+  uint32_t rw[8], rwm[8], rw2[TWO ? 8 : 1], rwm2[TWO ? 8 : 1];
+  unsigned vmask = 0;   // bit b <-> column col_of(b, lane): j < n and j != skip
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    uint32_t a = 0, b = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int bit = (q >> 2) * 16 + (q & 3) * 4 + e;
+      const int64_t j = g0 + (q >> 2) * 512 + (q & 3) * 4 + e;
+      a |= (j < n ? s8(r1[j]) : (uint32_t)kSat8i) << (8 * e);
+      if (TWO) b |= (j < n ? s8(r2[j]) : (uint32_t)kSat8i) << (8 * e);
+      if (j < n && j != skip) vmask |= 1u << bit;
+    }
+    rw[q] = a;
+    rwm[q] = a - 0x01010101u;
+    if (TWO) { rw2[q] = b; rwm2[q] = b - 0x01010101u; }
+  }
+  const bool ok0 = g0 < n, ok1 = g0 + 512 < n;   // n is a multiple of 4, ld of 32: groups are in the row
+  const uint8_t* mb = o.M.m8 + (i_lo - r.row0) * ld + g0;
+  const uint4 satv = make_uint4(0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu);
+  for (int rr = 0; rr < rows; rr += 32) {
+    // the pivot column for 32 rows, one per lane (INF on row k: never tight)
+    const int64_t il = i_lo + rr + lane;
+    const bool inr = rr + lane < rows;
+    const uint32_t cl = (inr && il != skip) ? s8(c1[il]) * 0x01010101u : 0x7F7F7F7Fu;
+    const uint32_t cl2 = TWO ? ((inr && il != skip) ? s8(c2[il]) * 0x01010101u : 0x7F7F7F7Fu) : 0u;
+    const int r32 = min(32, rows - rr);
+    for (int hb = 0; hb < r32; hb += P8_RB) {
+      uint4 w[P8_RB][2];
+#pragma unroll
+      for (int h = 0; h < P8_RB; ++h) {
+        const bool in = hb + h < r32;
+        const uint8_t* p = mb + (int64_t)(rr + hb + h) * ld;
+        w[h][0] = (in && ok0) ? mload8(reinterpret_cast<const uint16_t*>(p)) : satv;
+        w[h][1] = (in && ok1) ? mload8(reinterpret_cast<const uint16_t*>(p + 512)) : satv;
+      }
+#pragma unroll
+      for (int h = 0; h < P8_RB; ++h) {
+        if (hb + h >= r32) break;
+        const uint32_t cw = __shfl_sync(0xffffffffu, cl, hb + h);
+        const uint32_t cw2 = TWO ? __shfl_sync(0xffffffffu, cl2, hb + h) : 0u;
+        const uint32_t d[8] = {w[h][0].x, w[h][0].y, w[h][0].z, w[h][0].w,
+                               w[h][1].x, w[h][1].y, w[h][1].z, w[h][1].w};
+        uint32_t acc = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          acc |= (cw + rwm[q] - d[q]) & ~(cw + rw[q] - d[q]);
+          if (TWO) acc |= (cw2 + rwm2[q] - d[q]) & ~(cw2 + rw2[q] - d[q]);
+        }
+        if (!__any_sync(0xffffffffu, (acc & 0x80808080u) != 0u)) continue;
+        // some lane has a tight entry in this row: exact per-byte flags of the
+        // words that have a zero byte (the test above is exact per word)
+        const int64_t i = i_lo + rr + hb + h;
+        unsigned word = 0;
+        if (acc & 0x80808080u) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            uint32_t u = cw + rw[q] - d[q];
+            uint32_t z = ~(u | ((u & 0x7F7F7F7Fu) + 0x7F7F7F7Fu)) & 0x80808080u;   // exact zero bytes
+            if (TWO) {
+              u = cw2 + rw2[q] - d[q];
+              z |= ~(u | ((u & 0x7F7F7F7Fu) + 0x7F7F7F7Fu)) & 0x80808080u;
+            }
+            // bytes 0..3 -> bits 4q' .. 4q'+3 of this lane's 16-column half
+            const uint32_t nib = ((((z >> 7) & 0x01010101u) * 0x01020408u) >> 24) & 0xFu;
+            word |= nib << ((q >> 2) * 16 + (q & 3) * 4);
+          }
+          word &= vmask;
+          const int64_t di = i - g0;   // the diagonal j == i
+          if (di >= 0 && di < 16) word &= ~(1u << di);
+          else if (di >= 512 && di < 528) word &= ~(1u << (di - 512 + 16));
+        }
+        if (!__any_sync(0xffffffffu, word != 0)) continue;
+        if (MODE == 0) {
+          if (lane == 0) o.anyrow[i] = 1;
+        } else {
+          const int tot = __reduce_add_sync(0xffffffffu, (unsigned)__popc(word));
+          if (lane == 0) atomicAdd(o.rowcnt + i, tot);
+          if (qcnt + 32 > DS_Q) {
+            detect_flush_q<T>(Q, qcnt, i_lo, o, lane, col_of);
+            qcnt = 0;
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, word != 0);
+          if (word) {
+            const int qp = qcnt + __popc(bal & ((1u << lane) - 1));
+            Q.rl[qp] = (unsigned)(i - i_lo) << 5 | (unsigned)lane;
+            Q.w[qp] = word;
+          }
+          qcnt += __popc(bal);
+        }
+      }
+    }
+  }
+  if (MODE == 1) detect_flush_q<T>(Q, qcnt, i_lo, o, lane, col_of);
+}
+
 template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
                    const T* c2, const T* r2, float tau, int mode, int* anyrow, int* rowcnt,
@@ -1217,13 +1562,23 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
   if (mode == 0) CUDA_TRY(cudaMemsetAsync(anyrow + r.lo, 0, sizeof(int) * (size_t)(r.hi - r.lo), st));
   DetectOut<T> o{anyrow, rowcnt, prow, pcol, plb, lcap, ctr, WT, ldw, M};
   const int g = (int)cdiv(tl.warps, 8);
+  // int8 mirror: 1024-column chunks
+  const Tiling tl8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256, tune_wps("APSP_TUNE_DET8_WPS", 64));
+  const int g8 = (int)cdiv(tl8.warps, 8);
+  // the int32 twin exits when a packed kernel applies (decided on the device):
+  // with a mirror it is launched at its residency (2 CTAs per SM) and strides
+  const bool packed = sr == 0 && mode != 2 && (M.m8 || M.m);
+  const int gs = packed ? std::min(g, 2 * num_sms()) : g;
 #define LAUNCH(TWO, SR, MODE)                                                                    \
   do {                                                                                           \
-    if (SR == 0 && MODE != 2 && M.m)                                                             \
-      k_detect_p16<T, TWO, (MODE == 2 ? 0 : MODE)><<<g, 256, 0, st>>>(D, ld, r, n, skip, tl, c1,  \
-                                                                       r1, c2, r2, tau, o);     \
-    k_detect_stream<T, TWO, SR, MODE><<<g, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, c2, r2,  \
-                                                         tau, o);                                \
+    if (SR == 0 && MODE != 2 && M.m8)                                                            \
+      k_detect_p8<T, TWO, (MODE == 2 ? 0 : MODE)><<<g8, 256, 0, st>>>(r, ld, n, skip, tl8, c1, r1, \
+                                                                      c2, r2, o);                \
+    else if (SR == 0 && MODE != 2 && M.m)                                                        \
+      k_detect_p16<T, TWO, (MODE == 2 ? 0 : MODE), 2><<<g, 256, 0, st>>>(D, ld, r, n, skip, tl,   \
+                                                                          c1, r1, c2, r2, tau, o); \
+    k_detect_stream<T, TWO, SR, MODE><<<gs, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, c2, r2, \
+                                                          tau, o);                               \
   } while (0)
 #define BY_MODE(TWO, SR)                 \
   if (mode == 0) LAUNCH(TWO, SR, 0);     \
@@ -1340,7 +1695,7 @@ __global__ void k_move_last_clear(T* D, int64_t ld, Rows r, int64_t k, int64_t l
     WT[last * ldw + j] = I;
     WT[j * ldw + last] = I;
   }
-  if (M.m && k != last) {   // the mirror of row / column k over the remaining nodes [0, last)
+  if (has_mirror(M) && k != last) {   // the mirror of row / column k over the remaining nodes [0, last)
     unsigned bits = 0;
     if (k >= r.lo && k < r.hi)
       for (int64_t j = tid; j < last; j += stride) bits |= mput(M, (k - r.row0) * ld + j, D[(k - r.row0) * ld + j]);

@@ -52,6 +52,6 @@ for r in range(reps):
     ms, _ = timed(lambda: h.add_node(od, idv))
     ad.append(ms)
 prof_add = {k: (round(v[0], 3), v[1]) for k, v in L.apsp_profile_read(h.h).items() if v[1]}
-print(json.dumps({"n": n, "remove_ms": [round(x[0], 4) for x in rm],
+print(json.dumps({"n": n, "mirror_width": h.mirror_width, "remove_ms": [round(x[0], 4) for x in rm],
                   "remove_stats": [x[1:] for x in rm], "remove_profile_ms": prof,
                   "add_ms": [round(x, 4) for x in ad], "add_profile_ms": prof_add}))

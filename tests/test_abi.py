@@ -14,7 +14,7 @@ HEADER = os.path.join(ROOT, "include", "apsp_warm.h")
 def declared_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    names = re.findall(r"^\s*(?:apsp_status|size_t|int64_t|const char\*)\s+(\w+)\s*\(", src, flags=re.M)
+    names = re.findall(r"^\s*(?:apsp_status|size_t|int64_t|int32_t|const char\*)\s+(\w+)\s*\(", src, flags=re.M)
     return sorted(set(names))
 
 

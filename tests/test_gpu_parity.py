@@ -693,3 +693,101 @@ def test_fw16_dense_fallback_of_a_removal(lib, rng):
     hg = synth.HostGraph(W, True)
     hg.remove_node(123)
     assert_parity(getD(h), oracle.fw(hg.W))
+
+
+# ------------------------------------------------------------------ mirror widths (§4.7)
+def _apply(h, hg, up):
+    if up.kind == "add":
+        h.add_node(up.out_w, up.in_w)
+        hg.add_node(up.out_w, up.in_w)
+    elif up.kind == "remove":
+        h.remove_node(up.k)
+        hg.remove_node(up.k)
+    else:
+        h.update_edge(up.u, up.v, up.w_new)
+        hg.set_edge(up.u, up.v, up.w_new)
+
+
+@pytest.mark.parametrize("mirror8", [1, 0])
+def test_mirror_width_sequence(lib, mirror8):
+    """BJ.c4-shaped sequence (distances < 0x7F): the streaming passes read the
+    int8 copy of D (or, with APSP_OPT_MIRROR8 = 0, the int16 one); D equals
+    the oracle after every update either way."""
+    spec = dataclasses.replace(synth.C4, n=520)
+    W = synth.graph(spec)
+    cap = 520 + 24
+    hg = synth.HostGraph(W, True, cap=cap)
+    h = make(lib, W, cap=cap, cold=False)
+    h.set_option(lib._lib.OPT_MIRROR8, mirror8)
+    h.cold_fw()
+    seq = synth.update_sequence(spec, synth.HostGraph(W, True, cap=cap), 0, 24)
+    for t, up in enumerate(seq):
+        _apply(h, hg, up)
+        assert h.mirror_width == (8 if mirror8 else 16)
+        if t % 6 == 5:
+            assert_parity(getD(h), oracle.fw(hg.W))
+    assert_parity(getD(h), oracle.fw(hg.W))
+
+
+@pytest.mark.parametrize("force", [0, 1])
+def test_mirror8_invalidated_by_a_removal(lib, force):
+    """Removing a hub pushes distances along a chain of weight-10 edges from 2
+    up to 10*(n-2) >= 0x7F: the int8 copy is invalidated, the updates that
+    follow read D (exact), and the next build of the copy is int16."""
+    n = 90
+    W = np.full((n, n), INF, np.int32)
+    np.fill_diagonal(W, 0)
+    hub = n - 1
+    for i in range(n - 1):
+        W[i, hub] = W[hub, i] = 1
+        if i + 1 < n - 1:
+            W[i, i + 1] = W[i + 1, i] = 10
+    hg = synth.HostGraph(W, True, cap=n + 4)
+    h = make(lib, W, cap=n + 4)
+    rng = np.random.default_rng(5)
+    o = np.full(n, INF, np.int32)
+    o[3] = 1
+    i = o.copy()
+    h.add_node(o, i)   # first update: builds the copy (int8: every distance <= 3)
+    hg.add_node(o, i)
+    assert h.mirror_width == 8
+    h.set_option(0, force)
+    h.remove_node(hub)
+    hg.remove_node(hub)
+    assert_parity(getD(h), oracle.fw(hg.W))
+    for _ in range(4):   # further updates on the invalidated / rebuilt copy
+        u, v = (int(x) for x in rng.choice(hg.n, 2, replace=False))
+        w = int(rng.integers(1, 40))
+        h.update_edge(u, v, w)
+        hg.set_edge(u, v, w)
+        assert_parity(getD(h), oracle.fw(hg.W))
+    assert h.mirror_width in (0, 16)
+    h.sync_distances()   # rebuild: int8 failed once, so int16 now
+    assert h.mirror_width == 16
+    k = int(rng.integers(0, hg.n))
+    h.remove_node(k)
+    hg.remove_node(k)
+    assert_parity(getD(h), oracle.fw(hg.W))
+
+
+def test_mirror8_invalidated_by_an_add(lib, rng):
+    """A new node whose edges weigh 500 writes distances >= 0x7F through the
+    rank-1 pass: the int8 copy is invalidated; later updates stay exact."""
+    spec = dataclasses.replace(synth.C4, n=300)
+    W = synth.graph(spec)
+    hg = synth.HostGraph(W, True, cap=310)
+    h = make(lib, W, cap=310)
+    o, i = synth.node_edges(spec, 1, 300)
+    h.add_node(o, i)
+    hg.add_node(o, i)
+    assert h.mirror_width == 8
+    o2 = np.full(hg.n, 500, np.int32)
+    h.add_node(o2, o2)
+    hg.add_node(o2, o2)
+    assert_parity(getD(h), oracle.fw(hg.W))
+    for k in (5, 17, -1):
+        k = k % hg.n
+        h.remove_node(k)
+        hg.remove_node(k)
+        assert_parity(getD(h), oracle.fw(hg.W))
+    assert h.mirror_width in (0, 16)

@@ -58,12 +58,7 @@ __global__ void __launch_bounds__(1024) fw_diag_kernel(T* __restrict__ D, int64_
 // ---------------------------------------------------------------------------
 // (2)/(3) C[I][J] = min(C[I][J], A[I][:] (x) B[:][J]) on 128x128 tiles
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { cp_async_wait<0>(); }   // common.cuh
 
 struct TileArgs {
   void* C; int64_t ldc;          // output rows [0, m), cols [0, ncols)

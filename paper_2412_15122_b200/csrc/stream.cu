@@ -541,37 +541,79 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1_p16(Rows r, int64_t ld
 }
 
 // Add-node pass 1 on the int8 mirror: the arithmetic of k_addnode_pass1_p16
-// on widened words, with a warp owning 1024 columns of a row (lane l: the
-// 16-column groups at 16 l and 512 + 16 l) so that the per-row work — the two
-// warp reductions, the out[i] operand — is spread over twice the columns; the
-// per-row results are kept by lane (row & 31) and stored 32 rows at a time.
-constexpr int P8A_RB = 8;   // rows in flight per lane (one CTA of 8 warps per SM: 64 KB in flight)
+// on widened words.  A lane owns 16 consecutive columns (16 bytes per row)
+// and streams them through a private shared-memory ring with per-thread
+// async copies (cp.async, 16 bytes per row; kP8S stages of kP8R rows in
+// flight; each thread reads back only its own bytes, so cp.async.wait_group
+// alone orders the ring).  Per row the pass costs half a PRMT (widening) and
+// 1.5 VIADDMNMX.S16x2 per entry, so the per-row bookkeeping is what decides
+// its speed: the row results (new-column value p, row-skip bound m) are not
+// reduced across the warp row by row but kept per lane, two rows per word
+// (int16 halves), for kP8G rows, then reduce-scattered across the 32 lanes
+// in one butterfly (log steps, halving the words each step) — ~2 shuffles and
+// mins per row instead of two warp reductions, two extractions and two
+// single-lane stores.
+#ifndef P8_MINB
+#define P8_MINB 2   // 2 CTAs (16 warps) per SM: 128 registers, no spills (measured best)
+#endif
+#ifndef P8_S
+#define P8_S 4
+#endif
+constexpr int kP8R = 4, kP8S = P8_S, kP8G = 16;   // rows per stage, stages, rows per reduction group
+// reduce-scatter of 8 words (16 rows, 2 per word) over the warp: lane l ends
+// with the reduction over all lanes of word 4*b4 + 2*b3 + b2 (b = bits of l)
+template <bool MAX>
+__device__ __forceinline__ uint32_t p8_reduce_scatter(const uint32_t (&w)[8], int lane) {
+  auto op = [](uint32_t a, uint32_t b) { return MAX ? __vmaxs2(a, b) : __vmins2(a, b); };
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  uint32_t k4[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t keep = b4 ? w[i + 4] : w[i], send = b4 ? w[i] : w[i + 4];
+    k4[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+  }
+  uint32_t k2[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const uint32_t keep = b3 ? k4[i + 2] : k4[i], send = b3 ? k4[i] : k4[i + 2];
+    k2[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+  }
+  uint32_t k1;
+  {
+    const uint32_t keep = b2 ? k2[1] : k2[0], send = b2 ? k2[0] : k2[1];
+    k1 = op(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+  }
+  k1 = op(k1, __shfl_xor_sync(0xffffffffu, k1, 2));
+  return op(k1, __shfl_xor_sync(0xffffffffu, k1, 1));
+}
+
 template <typename T>
-__global__ void __launch_bounds__(256, 1) k_addnode_pass1_p8(Rows r, int64_t ld, int64_t n, Tiling tl,
+__global__ void __launch_bounds__(256, P8_MINB) k_addnode_pass1_p8(Rows r, int64_t ld, int64_t n, Tiling tl,
                                                              const T* __restrict__ ow,
                                                              const T* __restrict__ iw, T* rowpart,
                                                              T* rowpartM, T* colpart, int64_t part_ld,
                                                              Mirror M) {
   if (!pass1_packed_runs<T, 0>(M) || M.m8 == nullptr) return;
+  extern __shared__ uint4 ring_raw[];   // [warp][stage][row][lane]: 64 KB per CTA
+  auto ring = reinterpret_cast<uint4 (*)[kP8S][kP8R][32]>(ring_raw);
   const bool has_inf = (*(volatile unsigned*)M.flag & kMirrorInf) != 0u;
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
   if (gw >= tl.warps) return;
   const int chunk = (int)(gw % tl.nchunk);
   const int slab = (int)(gw / tl.nchunk);
   const int64_t i_lo = r.lo + slab * tl.slab;
+  // may be 0: the slab still writes its (all-SAT) new-row partials
   const int rows = (int)max((int64_t)0, min(r.hi, i_lo + tl.slab) - i_lo);
   constexpr uint32_t SAT2 = 0x3FFF3FFFu;
-  const int64_t g0 = (int64_t)chunk * 1024 + 16 * lane;
-  // word q (0..15): columns g0 + (q >> 3) * 512 + (q & 7) * 2 + {0, 1}
-  auto colq = [&](int q) -> int64_t { return g0 + (q >> 3) * 512 + (q & 7) * 2; };
-  uint32_t in2[16], nout2[16], colp2[16];
+  const int64_t g0 = (int64_t)chunk * 512 + 16 * lane;   // word q: columns g0 + 2q, g0 + 2q + 1
+  uint32_t in2[8], nout2[8], colp2[8];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
+  for (int q = 0; q < 8; ++q) {
     uint32_t a = 0, b = 0;
 #pragma unroll
     for (int hf = 0; hf < 2; ++hf) {
-      const int64_t j = colq(q) + hf;
+      const int64_t j = g0 + 2 * q + hf;
       const uint32_t iv = j < n ? (uint32_t)sat16((int32_t)iw[j]) : 0x3FFFu;
       const uint32_t ov = j < n ? (uint32_t)sat16((int32_t)ow[j]) : 0x3FFFu;
       a |= iv << (16 * hf);
@@ -579,80 +621,115 @@ __global__ void __launch_bounds__(256, 1) k_addnode_pass1_p8(Rows r, int64_t ld,
     }
     in2[q] = a; nout2[q] = b; colp2[q] = SAT2;
   }
-  const bool tail = (int64_t)(chunk + 1) * 1024 > n;   // this chunk holds columns >= n
-  const bool ok0 = g0 < n, ok1 = g0 + 512 < n;
-  const uint8_t* mb = M.m8 + (i_lo - r.row0) * ld + g0;
-  const uint4 satb = make_uint4(0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu);
+  const bool tail = (int64_t)(chunk + 1) * 512 > n;   // this chunk holds columns >= n (replaced)
+  // a lane whose group starts beyond n copies the row's first group (in bounds)
+  const uint8_t* base = M.m8 + (i_lo - r.row0) * ld + (g0 < n ? g0 : 0);
   T* rp_out = rowpart + (int64_t)chunk * part_ld + i_lo;
   T* rm_out = rowpartM + (int64_t)chunk * part_ld + i_lo;
-  for (int rr = 0; rr < rows; rr += 32) {
-    const int r32 = min(32, rows - rr);
-    // out[i] of the 32 rows, one per lane; the row results, kept by lane (row & 31)
-    const uint32_t ol = lane < r32 ? (uint32_t)sat16((int32_t)ow[i_lo + rr + lane]) * 0x10001u : SAT2;
-    int keep_p = 0, keep_m = 0;
-    for (int hb = 0; hb < r32; hb += P8A_RB) {
-      uint4 w[P8A_RB][2];
+  const int nst = (rows + kP8R - 1) / kP8R;
+  auto issue = [&](int s) {   // stage s -> ring slot s % kP8S (rows past the slab: its last row)
+    if (s < nst) {
 #pragma unroll
-      for (int h = 0; h < P8A_RB; ++h) {
-        const bool in = hb + h < r32;
-        const uint8_t* p = mb + (int64_t)(rr + hb + h) * ld;
-        w[h][0] = (in && ok0) ? mload8(reinterpret_cast<const uint16_t*>(p)) : satb;
-        w[h][1] = (in && ok1) ? mload8(reinterpret_cast<const uint16_t*>(p + 512)) : satb;
-      }
+      for (int h = 0; h < kP8R; ++h)
+        cp_async16(&ring[warp][s % kP8S][h][lane], base + (int64_t)min(s * kP8R + h, rows - 1) * ld);
+    }
+    cp_async_commit();   // (an empty group past the end keeps the wait count uniform)
+  };
+  auto out_of = [&](int row) -> uint32_t {   // out[i] of a row, replicated in both halves
+    return row < rows ? (uint32_t)sat16((int32_t)ow[i_lo + row]) * 0x10001u : SAT2;
+  };
+  // the common case (no INF entry, no column >= n in this chunk) has a loop
+  // of its own: the INF and tail fix-ups would otherwise hold registers
+  auto run = [&](auto special) {
+    constexpr bool SPECIAL = decltype(special)::value;
 #pragma unroll
-      for (int h = 0; h < P8A_RB; ++h) {
-        if (hb + h >= r32) break;
-        const uint32_t orep = __shfl_sync(0xffffffffu, ol, hb + h);
-        uint32_t dw[16];
+    for (int s = 0; s < kP8S - 1; ++s) issue(s);
+    uint32_t onext = out_of(lane & (kP8G - 1));   // group 0's out[i], lane l < kP8G: row l
+    for (int g0r = 0; g0r < rows; g0r += kP8G) {
+      const uint32_t ocur = onext;
+      onext = out_of(g0r + kP8G + (lane & (kP8G - 1)));   // next group's, in flight meanwhile
+      uint32_t pw[kP8G / 2], mw[kP8G / 2];   // row results, two rows per word
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          const uint4 b = w[h][g];
-          const uint4 lo = widen8(make_uint2(b.x, b.y)), hi = widen8(make_uint2(b.z, b.w));
-          dw[8 * g + 0] = lo.x; dw[8 * g + 1] = lo.y; dw[8 * g + 2] = lo.z; dw[8 * g + 3] = lo.w;
-          dw[8 * g + 4] = hi.x; dw[8 * g + 5] = hi.y; dw[8 * g + 6] = hi.z; dw[8 * g + 7] = hi.w;
-        }
-        if (has_inf) {   // int8 INF (0x7F) reads as the int16 INF (0x3FFF)
+      for (int sg = 0; sg < kP8G / kP8R; ++sg) {
+        const int s = g0r / kP8R + sg;
+        issue(s + kP8S - 1);
+        cp_async_wait<kP8S - 1>();   // this thread's copies of stage s have landed
+        uint32_t prow[kP8R], mrow[kP8R];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) dw[q] = inf8to16(dw[q]);
-        }
-        if (tail) {   // columns >= n hold no mirrored value
+        for (int h = 0; h < kP8R; ++h) {
+          const uint32_t orep = __shfl_sync(0xffffffffu, ocur, sg * kP8R + h);
+          const uint4 wv = ring[warp][s % kP8S][h][lane];
+          const uint4 lo = widen8(make_uint2(wv.x, wv.y)), hi = widen8(make_uint2(wv.z, wv.w));
+          uint32_t dw[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+          if (SPECIAL && has_inf) {   // int8 INF (0x7F) reads as the int16 INF (0x3FFF)
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int64_t j0 = colq(q);
-            const uint32_t pm = (j0 < n ? 0u : 0xFFFFu) | (j0 + 1 < n ? 0u : 0xFFFF0000u);
-            dw[q] = (dw[q] & ~pm) | (SAT2 & pm);
+            for (int q = 0; q < 8; ++q) dw[q] = inf8to16(dw[q]);
+          }
+          if (SPECIAL && tail) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int64_t j0 = g0 + 2 * q;
+              const uint32_t pm = (j0 < n ? 0u : 0xFFFFu) | (j0 + 1 < n ? 0u : 0xFFFF0000u);
+              dw[q] = (dw[q] & ~pm) | (SAT2 & pm);
+            }
+          }
+          uint32_t pa = SAT2, pb = SAT2, ma = 0xC001C001u /* -16383 */, mb = 0xC001C001u;
+#pragma unroll
+          for (int q = 0; q < 8; q += 2) {
+            pa = __viaddmin_s16x2(dw[q], in2[q], pa);
+            pb = __viaddmin_s16x2(dw[q + 1], in2[q + 1], pb);
+            ma = __viaddmax_s16x2(dw[q], nout2[q], ma);
+            mb = __viaddmax_s16x2(dw[q + 1], nout2[q + 1], mb);
+            colp2[q] = __viaddmin_s16x2(orep, dw[q], colp2[q]);
+            colp2[q + 1] = __viaddmin_s16x2(orep, dw[q + 1], colp2[q + 1]);
+          }
+          prow[h] = __vmins2(pa, pb);
+          mrow[h] = __vmaxs2(ma, mb);
+          if (SPECIAL && has_inf) {   // D == INF with a finite out: no row skip (k_addnode_pass1_p16)
+            uint32_t inf = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const uint32_t satnf = ((nout2[q] & 0xFFFFu) == 0xC001u ? 0x3FFFu : 0x3FFEu) |
+                                     ((nout2[q] >> 16) == 0xC001u ? 0x3FFF0000u : 0x3FFE0000u);
+              inf |= __vmins2(dw[q], satnf) ^ dw[q];
+            }
+            if (inf) mrow[h] = 0x7FFF7FFFu;   // 0x7FFF: "no skip" (written back as INF)
           }
         }
-        uint32_t p2 = SAT2, m2 = 0xC001C001u /* -16383 */, inf = 0;
+        // fold each row's two halves and pair rows: word = (row 2k, row 2k + 1)
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          p2 = __viaddmin_s16x2(dw[q], in2[q], p2);
-          m2 = __viaddmax_s16x2(dw[q], nout2[q], m2);
-          colp2[q] = __viaddmin_s16x2(orep, dw[q], colp2[q]);
+        for (int h = 0; h < kP8R; h += 2) {
+          const uint32_t pl = __byte_perm(prow[h], prow[h + 1], 0x5410);
+          const uint32_t ph = __byte_perm(prow[h], prow[h + 1], 0x7632);
+          const uint32_t ml = __byte_perm(mrow[h], mrow[h + 1], 0x5410);
+          const uint32_t mh = __byte_perm(mrow[h], mrow[h + 1], 0x7632);
+          pw[(sg * kP8R + h) / 2] = __vmins2(pl, ph);
+          mw[(sg * kP8R + h) / 2] = __vmaxs2(ml, mh);
         }
-        if (has_inf) {   // D == INF with a finite out: no row skip (see k_addnode_pass1_p16)
+      }
+      // rows g0r + 2 wi, g0r + 2 wi + 1 (wi = 4 b4 + 2 b3 + b2) reduced over the warp
+      const uint32_t pr = p8_reduce_scatter<false>(pw, lane);
+      const uint32_t mr = p8_reduce_scatter<true>(mw, lane);
+      if ((lane & 3) == 0) {
+        const int wi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+        const int ra = g0r + 2 * wi;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const uint32_t satnf = ((nout2[q] & 0xFFFFu) == 0xC001u ? 0x3FFFu : 0x3FFEu) |
-                                   ((nout2[q] >> 16) == 0xC001u ? 0x3FFF0000u : 0x3FFE0000u);
-            inf |= __vmins2(dw[q], satnf) ^ dw[q];
+        for (int e = 0; e < 2; ++e) {
+          if (ra + e < rows) {
+            const int mv = (int)(short)(mr >> (16 * e));
+            rp_out[ra + e] = (T)((pr >> (16 * e)) & 0xFFFFu);
+            rm_out[ra + e] = mv == 0x7FFF ? Tr<T>::inf() : (T)mv;
           }
         }
-        const int pl = (int)min(p2 & 0xFFFFu, p2 >> 16);
-        const int ml = inf ? (int)Tr<T>::inf() : max((int)(short)(m2 & 0xFFFFu), (int)(short)(m2 >> 16));
-        const int pr = (int)__reduce_min_sync(0xffffffffu, (unsigned)pl);
-        const int mr = __reduce_max_sync(0xffffffffu, ml);
-        if (lane == hb + h) { keep_p = pr; keep_m = mr; }
       }
     }
-    if (lane < r32) {
-      rp_out[rr + lane] = (T)keep_p;
-      rm_out[rr + lane] = (T)keep_m;
-    }
-  }
+  };
+  if (has_inf || tail) run(std::true_type{});
+  else run(std::false_type{});
+  cp_async_wait<0>();
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const int64_t j0 = colq(q);
+  for (int q = 0; q < 8; ++q) {
+    const int64_t j0 = g0 + 2 * q;
     if (j0 < n) {
       T* dst = colpart + (int64_t)slab * part_ld + j0;
       dst[0] = (T)(colp2[q] & 0xFFFFu);
@@ -814,7 +891,7 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
                           int* nslab_out, int max_slabs, int sr, Mirror M, const unsigned* uncertain,
                           int packed, cudaStream_t st) {
   const bool p8 = packed && !sr && M.m8 != nullptr;   // int8 mirror: 1024-column chunks
-  Tiling tl = p8 ? make_tiling(n, r.hi - r.lo, max_slabs, 256, tune_wps("APSP_TUNE_P8_WPS", 8))
+  Tiling tl = p8 ? make_tiling(n, r.hi - r.lo, max_slabs, 128, tune_wps("APSP_TUNE_P8_WPS", 144))
                  : make_tiling(n, r.hi - r.lo, max_slabs, P1_VEC, tune_wps("APSP_TUNE_P1_WPS", 16));
   *nchunk_out = tl.nchunk;
   *nslab_out = tl.nslab;
@@ -828,9 +905,16 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
   if (sr)
     k_addnode_pass1<T, 1><<<grid, 256, 0, st>>>(D, ld, r, n, tl, ow, iw, rowpart, rowpartM, colpart,
                                                 part_ld, M, uncertain);
-  else if (p8)   // on the mirror (exits unless it is valid)
-    k_addnode_pass1_p8<T><<<grid, 256, 0, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
-                                                part_ld, M);
+  else if (p8) {   // on the mirror (exits unless it is valid)
+    constexpr int smem = 8 * kP8S * kP8R * 32 * 16;
+    static bool attr = false;
+    if (!attr) {
+      CUDA_TRY(cudaFuncSetAttribute(k_addnode_pass1_p8<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = true;
+    }
+    k_addnode_pass1_p8<T><<<grid, 256, smem, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
+                                                   part_ld, M);
+  }
   else if (packed)
     k_addnode_pass1_p16<T, 2><<<grid, 256, 0, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
                                                     part_ld, M);

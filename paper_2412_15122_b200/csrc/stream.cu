@@ -1515,7 +1515,8 @@ __global__ void k_detect_rows(Rows r, const int* __restrict__ rowcnt, int64_t* r
 // 1024 columns of a row: lane l the 16-byte groups at 16 l and 512 + 16 l.
 // Row k (the removed node) is given c = INF: then u >= 0x7F - ... never 0
 // there (its d equals r), and the diagonal is masked in the rare path.
-constexpr int P8_RB = 4;   // rows per batch (two 16-byte loads each in flight)
+constexpr int kD8R = 2, kD8S = 3;   // ring: rows per stage, stages (6 KB per warp; 3 CTAs per SM)
+constexpr int kD8Smem = 8 * kD8S * kD8R * 2 * 32 * 16;
 template <typename T, bool TWO, int MODE>
 __global__ void __launch_bounds__(256, 3) k_detect_p8(Rows r, int64_t ld, int64_t n, int64_t skip, Tiling tl,
                                                       const T* __restrict__ c1, const T* __restrict__ r1,
@@ -1556,32 +1557,48 @@ __global__ void __launch_bounds__(256, 3) k_detect_p8(Rows r, int64_t ld, int64_
     rwm[q] = a - 0x01010101u;
     if (TWO) { rw2[q] = b; rwm2[q] = b - 0x01010101u; }
   }
-  const bool ok0 = g0 < n, ok1 = g0 + 512 < n;   // n is a multiple of 4, ld of 32: groups are in the row
-  const uint8_t* mb = o.M.m8 + (i_lo - r.row0) * ld + g0;
-  const uint4 satv = make_uint4(0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu);
-  for (int rr = 0; rr < rows; rr += 32) {
-    // the pivot column for 32 rows, one per lane (INF on row k: never tight)
-    const int64_t il = i_lo + rr + lane;
-    const bool inr = rr + lane < rows;
-    const uint32_t cl = (inr && il != skip) ? s8(c1[il]) * 0x01010101u : 0x7F7F7F7Fu;
-    const uint32_t cl2 = TWO ? ((inr && il != skip) ? s8(c2[il]) * 0x01010101u : 0x7F7F7F7Fu) : 0u;
-    const int r32 = min(32, rows - rr);
-    for (int hb = 0; hb < r32; hb += P8_RB) {
-      uint4 w[P8_RB][2];
+  // the rows stream through a per-warp shared-memory ring of per-thread async
+  // copies (each lane copies, and later reads, exactly its own 2 x 16 bytes per
+  // row): kD8S stages of kD8R rows stay in flight while the warp computes.  A
+  // lane whose group lies beyond n copies the row's first group (in bounds;
+  // those columns are masked out).
+  extern __shared__ uint4 dring_raw[];
+  auto ring = reinterpret_cast<uint4 (*)[kD8S][kD8R][2][32]>(dring_raw) + (threadIdx.x >> 5);
+  const uint8_t* mb = o.M.m8 + (i_lo - r.row0) * ld;
+  const int64_t off0 = g0 < n ? g0 : 0, off1 = g0 + 512 < n ? g0 + 512 : 0;
+  const int nst = (rows + kD8R - 1) / kD8R;
+  auto issue = [&](int st) {
+    if (st < nst) {
 #pragma unroll
-      for (int h = 0; h < P8_RB; ++h) {
-        const bool in = hb + h < r32;
-        const uint8_t* p = mb + (int64_t)(rr + hb + h) * ld;
-        w[h][0] = (in && ok0) ? mload8(reinterpret_cast<const uint16_t*>(p)) : satv;
-        w[h][1] = (in && ok1) ? mload8(reinterpret_cast<const uint16_t*>(p + 512)) : satv;
+      for (int h = 0; h < kD8R; ++h) {
+        const uint8_t* p = mb + (int64_t)min(st * kD8R + h, rows - 1) * ld;
+        cp_async16(&(*ring)[st % kD8S][h][0][lane], p + off0);
+        cp_async16(&(*ring)[st % kD8S][h][1][lane], p + off1);
       }
+    }
+    cp_async_commit();
+  };
 #pragma unroll
-      for (int h = 0; h < P8_RB; ++h) {
-        if (hb + h >= r32) break;
-        const uint32_t cw = __shfl_sync(0xffffffffu, cl, hb + h);
-        const uint32_t cw2 = TWO ? __shfl_sync(0xffffffffu, cl2, hb + h) : 0u;
-        const uint32_t d[8] = {w[h][0].x, w[h][0].y, w[h][0].z, w[h][0].w,
-                               w[h][1].x, w[h][1].y, w[h][1].z, w[h][1].w};
+  for (int st = 0; st < kD8S - 1; ++st) issue(st);
+  uint32_t cl = 0, cl2 = 0;
+  for (int st = 0; st < nst; ++st) {
+    issue(st + kD8S - 1);
+    cp_async_wait<kD8S - 1>();
+#pragma unroll
+    for (int h = 0; h < kD8R; ++h) {
+      const int rr = st * kD8R + h;
+      if (rr >= rows) break;   // warp-uniform
+      if ((rr & 31) == 0) {    // the pivot column for the next 32 rows, one per lane (INF on row k)
+        const int64_t il = i_lo + rr + lane;
+        const bool inr = rr + lane < rows;
+        cl = (inr && il != skip) ? s8(c1[il]) * 0x01010101u : 0x7F7F7F7Fu;
+        if (TWO) cl2 = (inr && il != skip) ? s8(c2[il]) * 0x01010101u : 0x7F7F7F7Fu;
+      }
+      {
+        const uint32_t cw = __shfl_sync(0xffffffffu, cl, rr & 31);
+        const uint32_t cw2 = TWO ? __shfl_sync(0xffffffffu, cl2, rr & 31) : 0u;
+        const uint4 w0 = (*ring)[st % kD8S][h][0][lane], w1 = (*ring)[st % kD8S][h][1][lane];
+        const uint32_t d[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
         uint32_t acc = 0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -1591,7 +1608,7 @@ __global__ void __launch_bounds__(256, 3) k_detect_p8(Rows r, int64_t ld, int64_
         if (!__any_sync(0xffffffffu, (acc & 0x80808080u) != 0u)) continue;
         // some lane has a tight entry in this row: exact per-byte flags of the
         // words that have a zero byte (the test above is exact per word)
-        const int64_t i = i_lo + rr + hb + h;
+        const int64_t i = i_lo + rr;
         unsigned word = 0;
         if (acc & 0x80808080u) {
 #pragma unroll
@@ -1655,9 +1672,13 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
   const int gs = packed ? std::min(g, 2 * num_sms()) : g;
 #define LAUNCH(TWO, SR, MODE)                                                                    \
   do {                                                                                           \
-    if (SR == 0 && MODE != 2 && M.m8)                                                            \
-      k_detect_p8<T, TWO, (MODE == 2 ? 0 : MODE)><<<g8, 256, 0, st>>>(r, ld, n, skip, tl8, c1, r1, \
-                                                                      c2, r2, o);                \
+    if (SR == 0 && MODE != 2 && M.m8) {                                                          \
+      auto kp8 = k_detect_p8<T, TWO, (MODE == 2 ? 0 : MODE)>;                                    \
+      static const cudaError_t attr =                                                            \
+          cudaFuncSetAttribute(kp8, cudaFuncAttributeMaxDynamicSharedMemorySize, kD8Smem);        \
+      CUDA_TRY(attr);                                                                            \
+      kp8<<<g8, 256, kD8Smem, st>>>(r, ld, n, skip, tl8, c1, r1, c2, r2, o);                     \
+    }                                                                                            \
     else if (SR == 0 && MODE != 2 && M.m)                                                        \
       k_detect_p16<T, TWO, (MODE == 2 ? 0 : MODE), 2><<<g, 256, 0, st>>>(D, ld, r, n, skip, tl,   \
                                                                           c1, r1, c2, r2, tau, o); \

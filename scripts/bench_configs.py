@@ -64,9 +64,10 @@ def repeat_update(cfg, what, W, directed, D0, op, R=5, flush=False, cap=None):
         h = fresh(W, directed, D0, cap)
         t, info = timed(lambda: op(h), flush)
         ms.append(t)
+        mw = h.mirror_width   # width of D's copy the streaming passes read (8 / 16; 0: D)
         del h
     d = info.as_dict() if hasattr(info, "as_dict") else {}
-    emit(cfg, what, ms, W.shape[0], {"info": d, "l2_flushed": flush})
+    emit(cfg, what, ms, W.shape[0], {"info": d, "l2_flushed": flush, "mirror_width": mw})
 
 
 def cold(cfg, W, directed, R=3):
@@ -144,10 +145,10 @@ def c5():
     v += v >= u
     ms = []
     t1, info = timed(lambda: h.update_edge(u, v, int(W[u, v]) * 10))
-    emit("c5", "increase_x10_random", [t1], n, {"info": info.as_dict()})
+    emit("c5", "increase_x10_random", [t1], n, {"info": info.as_dict(), "mirror_width": h.mirror_width})
     vt = tight_in(W, u)
     t2, info = timed(lambda: h.update_edge(u, vt, int(W[u, vt]) * 10))
-    emit("c5", "increase_x10_tight", [t2], n, {"info": info.as_dict()})
+    emit("c5", "increase_x10_tight", [t2], n, {"info": info.as_dict(), "mirror_width": h.mirror_width})
     s, tt = synth.query_pairs(spec.seed, n, 1024)
     sd, td = torch.from_numpy(s).cuda(), torch.from_numpy(tt).cuda()
     for rep in range(3):

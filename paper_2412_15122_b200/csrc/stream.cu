@@ -1008,6 +1008,8 @@ __global__ void __launch_bounds__(256) k_rank1(T* __restrict__ D, int64_t ld, Ro
                                                const T* __restrict__ rv2,
                                                unsigned long long* __restrict__ bytes_read,
                                                Mirror M) {
+  // k_rank1_p8 (launched first) did the update while the int8 mirror is valid
+  if (SR == 0 && M.m8 != nullptr && (*(volatile unsigned*)M.flag & kMirrorOff) == 0u) return;
   const int lane = threadIdx.x & 31;
   const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (gw >= tl.warps) return;
@@ -1066,12 +1068,161 @@ __global__ void __launch_bounds__(256) k_rank1(T* __restrict__ D, int64_t ld, Ro
     atomicAdd(bytes_read, (unsigned long long)(rows_read * cols * (int64_t)sizeof(T)));
   }
 }
+// Rank-1 pass on the int8 mirror (shortest path, int32 D, mirror valid):
+// D[i][j] = min(D[i][j], c[i] + r[j] (, c2[i] + r2[j])).  While the mirror is
+// valid it images D exactly (0x7F = INF), so D itself is never read: a row
+// that can change (c[i] finite) is read as 1 KB of bytes per 1024 columns
+// instead of 4 KB, and only the entries that change are written (D and the
+// mirror).  Rows are found 32 at a time (one c load per lane, a ballot).
+// The int32 k_rank1 launched after it exits while the mirror is still valid;
+// if this pass wrote a distance >= 0x7F (mirror now off) the int32 pass runs
+// too — harmless, the update is idempotent.
+template <bool TWO>
+__global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, int64_t ld, Rows r, int64_t n,
+                                                     Tiling tl, const int32_t* __restrict__ c,
+                                                     const int32_t* __restrict__ rv, const int32_t* __restrict__ c2,
+                                                     const int32_t* __restrict__ rv2,
+                                                     unsigned long long* __restrict__ bytes_read, Mirror M) {
+  if (M.m8 == nullptr || (*(volatile unsigned*)M.flag & kMirrorOff)) return;
+  // No INF entry: min(d, c + r) in packed int16x2 is exact — d <= 0x7E, and
+  // a saturated c + r (>= 0x3FFF) exceeds every finite d.  With INF entries
+  // (0x7F) a finite c + r >= 0x3FFF could still lower one: per-entry int32.
+  const bool has_inf = (*(volatile unsigned*)M.flag & kMirrorInf) != 0u;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gw >= tl.warps) return;
+  const int chunk = (int)(gw % tl.nchunk);
+  const int slab = (int)(gw / tl.nchunk);
+  const int64_t i_lo = r.lo + slab * tl.slab;
+  const int64_t i_hi = min(r.hi, i_lo + tl.slab);
+  const int32_t I = APSP_INF_I32_DEV;
+  const int64_t g0 = (int64_t)chunk * 1024 + 16 * lane;   // columns g0 + [0,16) and g0 + 512 + [0,16)
+  auto colj = [&](int e) -> int64_t { return g0 + (e >> 4) * 512 + (e & 15); };
+  uint32_t r2[16], r2b[TWO ? 16 : 1];   // word q: columns colj(2q), colj(2q + 1), saturated at 0x3FFF
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    uint32_t a = 0, b = 0;
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      const int64_t j = colj(2 * q + hf);
+      a |= (uint32_t)(j < n ? sat16(rv[j]) : 0x3FFF) << (16 * hf);
+      if (TWO) b |= (uint32_t)(j < n ? sat16(rv2[j]) : 0x3FFF) << (16 * hf);
+    }
+    r2[q] = a;
+    if (TWO) r2b[q] = b;
+  }
+  const bool ok0 = g0 < n, ok1 = g0 + 512 < n;
+  int64_t rows_read = 0;
+  unsigned mbits = 0;
+  for (int64_t ib = i_lo; ib < i_hi; ib += 32) {
+    const int64_t il = ib + lane;
+    const int32_t cl = il < i_hi ? c[il] : I;
+    const int32_t cl2 = TWO ? (il < i_hi ? c2[il] : I) : I;
+    unsigned live = __ballot_sync(0xffffffffu, cl < I || (TWO && cl2 < I));   // rows that can change
+    while (live) {
+      constexpr int kR8 = 4;   // up to 4 live rows at a time: their loads fly together
+      int bs[kR8];
+      uint4 wv[kR8][2];
+#pragma unroll
+      for (int t = 0; t < kR8; ++t) {
+        bs[t] = live ? __ffs(live) - 1 : -1;
+        if (live) live &= live - 1;
+        const uint8_t* mrow = M.m8 + (ib + max(bs[t], 0) - r.row0) * ld;
+        const bool v = bs[t] >= 0;
+        wv[t][0] = (v && ok0) ? mload8(reinterpret_cast<const uint16_t*>(mrow + g0)) : make_uint4(0, 0, 0, 0);
+        wv[t][1] = (v && ok1) ? mload8(reinterpret_cast<const uint16_t*>(mrow + g0 + 512)) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int t = 0; t < kR8; ++t) {
+        if (bs[t] < 0) break;   // warp-uniform
+        const int64_t i = ib + bs[t];
+        const int32_t ci = __shfl_sync(0xffffffffu, cl, bs[t]);
+        const int32_t ci2 = TWO ? __shfl_sync(0xffffffffu, cl2, bs[t]) : I;
+        ++rows_read;
+        int32_t* drow = D + (i - r.row0) * ld;
+        uint8_t* mrow = M.m8 + (i - r.row0) * ld;
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          const int64_t jg = g0 + 512 * g;
+          const uint4 wb = wv[t][g];
+          if (!has_inf) {
+            const uint32_t cw = (uint32_t)sat16(ci) * 0x10001u, cw2 = (uint32_t)sat16(ci2) * 0x10001u;
+            const uint4 lo = widen8(make_uint2(wb.x, wb.y)), hi = widen8(make_uint2(wb.z, wb.w));
+            const uint32_t d[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+            uint32_t o[8], diff = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              o[q] = __viaddmin_s16x2(cw, r2[8 * g + q], d[q]);
+              if (TWO) o[q] = __viaddmin_s16x2(cw2, r2b[8 * g + q], o[q]);
+              diff |= o[q] ^ d[q];
+            }
+            if (!diff) continue;
+            if (jg + 16 <= n) {   // rewrite the half: 64 bytes of D, 16 mirror bytes
+              int4* dst = reinterpret_cast<int4*>(drow + jg);
+              uint32_t mw[4];
+              uint32_t big = 0;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t a = o[2 * q], b = o[2 * q + 1];
+                dst[q] = make_int4((int)(a & 0xFFFFu), (int)(a >> 16), (int)(b & 0xFFFFu), (int)(b >> 16));
+                const uint32_t sa = __vmins2(a, 0x007F007Fu), sb = __vmins2(b, 0x007F007Fu);   // sat8
+                mw[q] = __byte_perm(sa, sb, 0x6420);
+                big |= __vcmpgeu2(a, 0x007F007Fu) | __vcmpgeu2(b, 0x007F007Fu);
+              }
+              *reinterpret_cast<uint4*>(mrow + jg) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+              if (big) mbits |= kMirrorOff;   // a distance >= 0x7F: the int8 mirror is no longer exact
+            } else {   // the row's ragged end: element stores below n
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                if (jg + e < n) {
+                  const int32_t v = (int32_t)((o[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
+                  drow[jg + e] = v;
+                  mbits |= mput(M, (i - r.row0) * ld + jg + e, v);
+                }
+            }
+          } else {   // INF entries present: exact int32 per entry
+            const uint32_t wd[4] = {wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int64_t j = jg + e;
+              if (j >= n) break;
+              const int32_t d8 = (int32_t)((wd[e >> 2] >> (8 * (e & 3))) & 0xFFu);
+              const int32_t dv = d8 == kSat8i ? I : d8;
+              int32_t nv = min(I, ci + rv[j]);
+              if (TWO) nv = min(nv, min(I, ci2 + rv2[j]));
+              if (nv < dv) {
+                drow[j] = nv;
+                mbits |= mput(M, (i - r.row0) * ld + j, nv);
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  mirror_post(M, mbits);
+  if (bytes_read && lane == 0 && rows_read) {
+    const int64_t cols = min((int64_t)1024, n - (int64_t)chunk * 1024);
+    atomicAdd(bytes_read, (unsigned long long)(rows_read * cols));
+  }
+}
+
 template <typename T>
 cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, const T* c2,
                   const T* rv2, unsigned long long* bytes_read, int sr, Mirror M, cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
   Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20);
   int grid = (int)cdiv(tl.warps, 8);
+  if constexpr (std::is_same<T, int32_t>::value) {
+    if (!sr && M.m8) {   // the int8 twin first (the int32 kernel then exits while M stays valid)
+      const Tiling t8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256, tune_wps("APSP_TUNE_R8_WPS", 32));
+      const int g8 = (int)cdiv(t8.warps, 8);
+      if (c2)
+        k_rank1_p8<true><<<g8, 256, 0, st>>>(D, ld, r, n, t8, c, rv, c2, rv2, bytes_read, M);
+      else
+        k_rank1_p8<false><<<g8, 256, 0, st>>>(D, ld, r, n, t8, c, rv, nullptr, nullptr, bytes_read, M);
+    }
+  }
   if (c2 && sr)
     k_rank1<T, true, 1><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, c2, rv2, bytes_read, M);
   else if (c2)

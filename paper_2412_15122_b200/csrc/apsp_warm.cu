@@ -565,6 +565,17 @@ apsp_status cold_fw_impl(apsp_handle* h) {
 // ------------------------------------------------------------------ detect + recompute
 // Shared by remove_node (skip = k, tombstone) and edge increases (skip = -1).
 // c1/r1 (and c2/r2 when undirected increase) must be set up by the caller.
+// Removal of node k: SL upkeep (drop k's entries, node n-1 takes slot k) on
+// the side stream; remove_node_impl joins it (ev_join) before returning.
+template <typename T>
+apsp_status fork_shortlist_remove(apsp_handle* h, int64_t k) {
+  CKR(cudaEventRecord(h->ev_fork, h->st));
+  CKR(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
+  CK2(shortlist_remove<T>(h->slid(), h->slw<T>(), h->wnext<T>(), h->n, k, h->n - 1, h->st2));
+  CKR(cudaEventRecord(h->ev_join, h->st2));
+  return APSP_OK;
+}
+
 template <typename T>
 apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, const T* c2,
                       const T* r2, bool removal, apsp_update_info* info) {
@@ -615,10 +626,16 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     PK(APSP_K_SPARSE0, 0.0,
        sparse_phase_a<T>(h->Dl<T>(), h->ld, r, h->slid(), h->slw<T>(), h->rowoff(), h->srow(), h->scol(),
                          lcap, c1, r1, c2, r2, h->tau, h->ocnt(), h->ocol(), h->gprow(), h->gpcol(),
-                         h->glb<T>(), h->gfull(), ocap, h->ctr(), h->sr, h->st));
+                         h->glb<T>(), h->gfull(), ocap, h->ctr(), h->sr, h->mirror<T>(), h->st));
     // A2: whole-shortlist pass over the open pairs, now that certified values are final
     CK(sparse_short<T>(h->Dl<T>(), h->ld, h->row0, h->slid(), h->slw<T>(), h->wnext<T>(), h->gprow(),
                        h->gpcol(), h->glb<T>(), ocap, h->gfull(), 1, h->sr, h->ctr(), h->st));
+    // the removal's shortlist upkeep needs nothing after A2 (the last reader of
+    // SL): it runs on the side stream, joined before the update returns
+    if (removal) {
+      apsp_status s2 = fork_shortlist_remove<T>(h, skip);
+      if (s2 != APSP_OK) return s2;
+    }
     // B: full O(n) scan for the pairs the shortlist could not settle
     PK(APSP_K_SPARSE_R, 0.0,
        sparse_full<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, n, h->gprow(), h->gpcol(),
@@ -628,6 +645,10 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     if (s != APSP_OK) return s;
   }
 
+  if (removal && !try_sparse) {
+    apsp_status s2 = fork_shortlist_remove<T>(h, skip);
+    if (s2 != APSP_OK) return s2;
+  }
   // ---- the one host read of this update: counters (summed over ranks) ----
   long long* v = reinterpret_cast<long long*>(h->small());
   CK(pack_counters(h->ctr(), h->anyflag(), v, h->st));   // total rows ovf1 ovf2 any | maxrow
@@ -681,8 +702,9 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     return fw_impl<T>(h, removal ? skip : -1);
   }
   if (info) info->path = 2;
-  if (total > 0)   // the sparse kernels wrote D on listed pairs only
-    CK(mirror_pairs(h->Dl<T>(), h->ld, h->row0, h->srow(), h->scol(), h->ctr(), lcap, h->mirror<T>(), h->st));
+  if (total > 0)   // phase A mirrored its final values; A2 / B / the rounds changed open pairs only
+    CK(mirror_pairs(h->Dl<T>(), h->ld, h->row0, h->gprow(), h->gpcol(), h->ctr(), ocap, 1, h->mirror<T>(),
+                    h->st));
   return APSP_OK;
 }
 
@@ -803,7 +825,7 @@ apsp_status remove_node_impl(apsp_handle* h, int64_t k, int64_t* moved_from, aps
     }
   }
   CK(move_last<T>(h->Dl<T>(), ld, r, n, k, row_copy, h->WT<T>(), ld, h->mirror<T>(), h->st));
-  CK(shortlist_remove<T>(h->slid(), h->slw<T>(), h->wnext<T>(), n, k, last, h->st));
+  CKR(cudaStreamWaitEvent(h->st, h->ev_join, 0));   // shortlist upkeep (side stream, forked in recompute)
   h->n = n - 1;
   if (moved_from) *moved_from = (k != last) ? last : -1;
   if (info) info->n_after = h->n;

@@ -164,7 +164,7 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
                            const int64_t* rowoff, const int* srow, const int* scol, int64_t npairs,
                            const T* c1, const T* r1, const T* c2, const T* r2, float tau, int* ocnt,
                            int* ocol, int* gprow, int* gpcol, T* glb, unsigned char* gfull, int64_t ocap,
-                           DetectCounters* ctr, int sr, cudaStream_t st);
+                           DetectCounters* ctr, int sr, Mirror M, cudaStream_t st);
 template <typename T>
 cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
                         const int* gprow, const int* gpcol, const T* glb, const unsigned char* gfull,
@@ -206,13 +206,15 @@ cudaError_t query_colslice(const T* D, int64_t ld, int64_t rows, int64_t R, int6
 cudaError_t mirror_build(const int32_t* D, int64_t ld, Rows r, int64_t n, Mirror M, cudaStream_t st);
 // int8 mirror from the packed int16 buffer (after a packed FW left sat16(D) there)
 cudaError_t mirror8_from_p16(const uint32_t* P, int64_t ld, int64_t m, int64_t n, Mirror M, cudaStream_t st);
+// M := sat(D) on the listed pairs: the need_update_list (open == 0, ctr->total
+// entries) or the open-pair list (open == 1, ctr->open_total entries)
 cudaError_t mirror_pairs(const int32_t* D, int64_t ld, int64_t row0, const int* prow, const int* pcol,
-                         const DetectCounters* ctr, int64_t lcap, Mirror M, cudaStream_t st);
+                         const DetectCounters* ctr, int64_t lcap, int open, Mirror M, cudaStream_t st);
 cudaError_t mirror_cross(const int32_t* D, int64_t ld, Rows r, int64_t n, int64_t row, int64_t col, Mirror M,
                          cudaStream_t st);
 // fp32 handles have no mirror
 inline cudaError_t mirror_pairs(const float*, int64_t, int64_t, const int*, const int*, const DetectCounters*,
-                                int64_t, Mirror, cudaStream_t) { return cudaSuccess; }
+                                int64_t, int, Mirror, cudaStream_t) { return cudaSuccess; }
 inline cudaError_t mirror_cross(const float*, int64_t, Rows, int64_t, int64_t, int64_t, Mirror, cudaStream_t) {
   return cudaSuccess;
 }

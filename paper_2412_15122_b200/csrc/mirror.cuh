@@ -1,0 +1,31 @@
+// mirror.cuh — device-side upkeep of the saturated mirror of D (kernels.h:
+// struct Mirror), shared by the streaming and the sparse kernels.
+#pragma once
+#include "common.cuh"
+#include "kernels.h"
+
+namespace apsp {
+
+// Mirror flag bits: kMirrorOff — some finite distance is at or above the
+// width's saturation value (M is not an exact image of D); kMirrorInf — some
+// active entry is INF (readers then need their INF tests).  mput returns the
+// bits the write raises; callers OR them per thread and post them once per
+// warp (mirror_post).
+constexpr unsigned kMirrorOff = 1u, kMirrorInf = 2u;
+__device__ __forceinline__ unsigned mput(const Mirror& M, int64_t idx, int32_t v) {
+  if (M.m8) {
+    M.m8[idx] = (uint8_t)min(v, kSat8i);
+    return v >= APSP_INF_I32_DEV ? kMirrorInf : (v >= kSat8i ? kMirrorOff : 0u);
+  }
+  M.m[idx] = sat16(v);
+  return v >= APSP_INF_I32_DEV ? kMirrorInf : (v >= kSat16i ? kMirrorOff : 0u);
+}
+__device__ __forceinline__ bool has_mirror(const Mirror& M) { return M.m != nullptr || M.m8 != nullptr; }
+__device__ __forceinline__ unsigned mput(const Mirror&, int64_t, float) { return 0u; }
+__device__ __forceinline__ void mirror_post(const Mirror& M, unsigned bits) {
+  bits = __reduce_or_sync(0xffffffffu, bits);
+  if ((threadIdx.x & 31) == 0 && bits && (bits & ~*(volatile unsigned*)M.flag)) atomicOr(M.flag, bits);
+}
+
+
+}  // namespace apsp

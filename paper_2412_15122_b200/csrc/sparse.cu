@@ -25,6 +25,7 @@
 // read-only WT / shortlists, so rows never race and no grid sync is needed.
 #include "common.cuh"
 #include "kernels.h"
+#include "mirror.cuh"
 
 namespace apsp {
 
@@ -545,8 +546,9 @@ __global__ void __launch_bounds__(256) k_sparse_phase_a(T* D, int64_t ld, int64_
                                                         const T* __restrict__ c1, const T* __restrict__ r1,
                                                         const T* __restrict__ c2, const T* __restrict__ r2,
                                                         float tau, OpenLists<T> ol,
-                                                        const DetectCounters* dc) {
+                                                        const DetectCounters* dc, Mirror M) {
   const int lane = threadIdx.x & 31;
+  unsigned mbits = 0;   // mirror flag bits raised by this thread's writes
   npairs = device_count(dc, npairs, 0);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < npairs;
@@ -601,6 +603,8 @@ __global__ void __launch_bounds__(256) k_sparse_phase_a(T* D, int64_t ld, int64_
       }
       Drow[j] = acc;   // unconditionally: D_old is not an upper bound of D'
       open = !Tr<T>::at_lb(acc, lb);
+      // a final value goes to the mirror now; open ones after the last round
+      if (!open && (M.m || M.m8)) mbits |= mput(M, (i - row0) * ld + j, acc);
     }
     // open-pair lists: per-row slot by atomic, the global slot warp-aggregated
     const unsigned bal = __ballot_sync(0xffffffffu, open);
@@ -623,6 +627,7 @@ __global__ void __launch_bounds__(256) k_sparse_phase_a(T* D, int64_t ld, int64_
       }
     }
   }
+  if (M.m || M.m8) mirror_post(M, mbits);
 }
 
 // Phase A over the detection list (pairs in append order; every pair reads
@@ -632,14 +637,14 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
                            const int64_t* rowoff, const int* srow, const int* scol, int64_t npairs,
                            const T* c1, const T* r1, const T* c2, const T* r2, float tau, int* ocnt,
                            int* ocol, int* gprow, int* gpcol, T* glb, unsigned char* gfull, int64_t ocap,
-                           DetectCounters* ctr, int sr, cudaStream_t st) {
+                           DetectCounters* ctr, int sr, Mirror M, cudaStream_t st) {
   if (npairs <= 0) return cudaSuccess;
   OpenLists<T> ol{ocnt, ocol, rowoff, gprow, gpcol, glb, gfull, ocap, ctr};
   // npairs is the capacity bound (the device count decides): full occupancy
   int grid = (int)std::min<int64_t>(cdiv(npairs, 256), (int64_t)num_sms() * 8);
 #define PA(SRV, TWOV)                                                                              \
   k_sparse_phase_a<T, SRV, TWOV><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, srow, scol, npairs, \
-                                                       c1, r1, c2, r2, tau, ol, ctr)
+                                                       c1, r1, c2, r2, tau, ol, ctr, M)
   const bool two = c2 != nullptr;
   if (sr) { if (two) PA(1, true); else PA(1, false); }
   else { if (two) PA(0, true); else PA(0, false); }
@@ -798,7 +803,7 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
   template cudaError_t sparse_phase_a<T>(T*, int64_t, Rows, const int*, const T*, const int64_t*,  \
                                          const int*, const int*, int64_t, const T*, const T*,      \
                                          const T*, const T*, float, int*, int*, int*, int*, T*,    \
-                                         unsigned char*, int64_t, DetectCounters*, int,            \
+                                         unsigned char*, int64_t, DetectCounters*, int, Mirror,    \
                                          cudaStream_t);                                            \
   template cudaError_t sparse_full<T>(T*, int64_t, int64_t, const T*, int64_t, int64_t,            \
                                       const int*, const int*, const T*, const unsigned char*,      \

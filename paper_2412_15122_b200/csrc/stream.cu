@@ -25,6 +25,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "mirror.cuh"
 
 namespace apsp {
 
@@ -247,26 +248,7 @@ static Tiling make_tiling(int64_t n, int64_t rows, int max_slabs, int chunk_vec 
 // ---------------------------------------------------------------------------
 // int16 mirror upkeep (kernels.h: struct Mirror)
 // ---------------------------------------------------------------------------
-// Mirror flag bits: kMirrorOff — some finite distance is >= 0x3FFF (M is not
-// an exact image of D); kMirrorInf — some active entry is INF (readers then
-// need their INF tests).  mput returns the bits the write raises; callers OR
-// them per thread and post them once per warp (mirror_post).
-constexpr unsigned kMirrorOff = 1u, kMirrorInf = 2u;
-__device__ __forceinline__ unsigned mput(const Mirror& M, int64_t idx, int32_t v) {
-  if (M.m8) {
-    M.m8[idx] = (uint8_t)min(v, kSat8i);
-    return v >= APSP_INF_I32_DEV ? kMirrorInf : (v >= kSat8i ? kMirrorOff : 0u);
-  }
-  M.m[idx] = sat16(v);
-  return v >= APSP_INF_I32_DEV ? kMirrorInf : (v >= kSat16i ? kMirrorOff : 0u);
-}
-__device__ __forceinline__ bool has_mirror(const Mirror& M) { return M.m != nullptr || M.m8 != nullptr; }
-__device__ __forceinline__ unsigned mput(const Mirror&, int64_t, float) { return 0u; }
-__device__ __forceinline__ void mirror_post(const Mirror& M, unsigned bits) {
-  bits = __reduce_or_sync(0xffffffffu, bits);
-  if ((threadIdx.x & 31) == 0 && bits && (bits & ~*(volatile unsigned*)M.flag)) atomicOr(M.flag, bits);
-}
-
+// (flag bits, mput, mirror_post: mirror.cuh)
 // M := sat16(D) over the local rows' first n columns; *flag must be 0 on entry
 __global__ void k_mirror_build(const int32_t* __restrict__ D, int64_t ld, Rows r, int64_t n, Mirror M) {
   const int64_t m = r.hi - r.lo, n4 = (n + 3) / 4;
@@ -323,8 +305,8 @@ cudaError_t mirror8_from_p16(const uint32_t* P, int64_t ld, int64_t m, int64_t n
 // M[i][j] := sat16(D[i][j]) for the listed pairs (the sparse recompute's writes)
 __global__ void k_mirror_pairs(const int32_t* __restrict__ D, int64_t ld, int64_t row0,
                                const int* __restrict__ prow, const int* __restrict__ pcol,
-                               const DetectCounters* ctr, int64_t lcap, Mirror M) {
-  const int64_t np = min((int64_t)ctr->total, lcap);
+                               const DetectCounters* ctr, int64_t lcap, int open, Mirror M) {
+  const int64_t np = min((int64_t)(open ? ctr->open_total : ctr->total), lcap);
   unsigned bits = 0;
   for (int64_t p0 = blockIdx.x * (int64_t)blockDim.x; p0 < np; p0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = p0 + threadIdx.x;
@@ -355,8 +337,8 @@ cudaError_t mirror_build(const int32_t* D, int64_t ld, Rows r, int64_t n, Mirror
   return cudaGetLastError();
 }
 cudaError_t mirror_pairs(const int32_t* D, int64_t ld, int64_t row0, const int* prow, const int* pcol,
-                         const DetectCounters* ctr, int64_t lcap, Mirror M, cudaStream_t st) {
-  k_mirror_pairs<<<num_sms() * 8, 256, 0, st>>>(D, ld, row0, prow, pcol, ctr, lcap, M);
+                         const DetectCounters* ctr, int64_t lcap, int open, Mirror M, cudaStream_t st) {
+  k_mirror_pairs<<<num_sms() * (open ? 2 : 8), 256, 0, st>>>(D, ld, row0, prow, pcol, ctr, lcap, open, M);
   return cudaGetLastError();
 }
 cudaError_t mirror_cross(const int32_t* D, int64_t ld, Rows r, int64_t n, int64_t row, int64_t col, Mirror M,

@@ -565,6 +565,12 @@ apsp_status cold_fw_impl(apsp_handle* h) {
 // ------------------------------------------------------------------ detect + recompute
 // Shared by remove_node (skip = k, tombstone) and edge increases (skip = -1).
 // c1/r1 (and c2/r2 when undirected increase) must be set up by the caller.
+// The int8 mirror is valid as of this update's host read of its flag (valid
+// only where no kernel that writes D/the mirror ran since that read).
+inline bool mirror8_known_valid(const apsp_handle* h) {
+  return h->mirror_built && h->mirror_level == 8 && h->mirror_hint && h->sr == 0;
+}
+
 // Removal of node k: SL upkeep (drop k's entries, node n-1 takes slot k) on
 // the side stream; remove_node_impl joins it (ev_join) before returning.
 template <typename T>
@@ -776,7 +782,7 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   // rows with ceff[i] = INF provably do not change and are not read at all
   PK(APSP_K_RANK1, 0.0,   // work: bytes actually read, counted on the device
      rank1<T>(h->Dl<T>(), ld, r, n, ceff, row, nullptr, nullptr, h->rank1_bytes(), h->sr, h->mirror<T>(),
-              h->st));
+              h->st, mirror8_known_valid(h) ? 0 : 1));
   CK(addnode_write<T>(h->Dl<T>(), ld, r, n, x, h->local(x) ? 1 : 0, col, row, h->WT<T>(), ld, ow,
                       iw, h->st));
   Rows rx = r;   // the active rows after the add (row x joins them if it is local)

@@ -90,8 +90,11 @@ cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, cons
                            T* ceff, T* row, int gate, Mirror M, unsigned* uncertain,
                            cudaStream_t st);
 template <typename T>
+// twin = 0: the caller knows the int8 mirror is valid (its flag was read since
+// the last write that could change it), so only the int8 pass is launched
 cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, const T* c2,
-                  const T* rv2, unsigned long long* bytes_read, int sr, Mirror M, cudaStream_t st);
+                  const T* rv2, unsigned long long* bytes_read, int sr, Mirror M, cudaStream_t st,
+                  int twin = 1);
 template <typename T>
 cudaError_t addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xlocal,
                           const T* col, const T* row, T* WT, int64_t ldw, const T* ow,

@@ -872,7 +872,7 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
                           T* rowpart, T* rowpartM, T* colpart, int64_t part_ld, int* nchunk_out,
                           int* nslab_out, int max_slabs, int sr, Mirror M, const unsigned* uncertain,
                           int packed, cudaStream_t st) {
-  const bool p8 = packed && !sr && M.m8 != nullptr;   // int8 mirror: 1024-column chunks
+  const bool p8 = packed && !sr && M.m8 != nullptr;   // int8 mirror: 512-column chunks
   Tiling tl = p8 ? make_tiling(n, r.hi - r.lo, max_slabs, 128, tune_wps("APSP_TUNE_P8_WPS", 144))
                  : make_tiling(n, r.hi - r.lo, max_slabs, P1_VEC, tune_wps("APSP_TUNE_P1_WPS", 16));
   *nchunk_out = tl.nchunk;
@@ -924,8 +924,11 @@ __global__ void __launch_bounds__(256) k_addnode_finish(const T* rowpart, const 
   if (gate == 2 && pass1_packed_done<T, 0>(M, uncertain)) return;
   __shared__ T sm[8][32], sM[8][32];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  if (blockIdx.x < ntile_i) {
-    const int64_t i = r.lo + (int64_t)blockIdx.x * 32 + lane;
+  // grid-stride over the 32-index tiles (a small grid: the gated twin's exit is cheap)
+  for (int64_t tile = blockIdx.x; tile < ntile_i + (npad + 31) / 32; tile += gridDim.x) {
+  __syncthreads();   // sm / sM reuse across tiles
+  if (tile < ntile_i) {
+    const int64_t i = r.lo + tile * 32 + lane;
     T m = Tr<T>::inf();
     T M = -Tr<T>::inf();
     if (i < r.hi)
@@ -954,7 +957,7 @@ __global__ void __launch_bounds__(256) k_addnode_finish(const T* rowpart, const 
       ceff[i] = keep ? m : Tr<T>::inf();
     }
   } else {
-    const int64_t j = (int64_t)(blockIdx.x - ntile_i) * 32 + lane;
+    const int64_t j = (tile - ntile_i) * 32 + lane;
     T m = Tr<T>::inf();
     if (j < n)
       for (int s = g; s < nslab; s += 8) m = Tr<T>::mn(m, colpart[(int64_t)s * part_ld + j]);
@@ -967,6 +970,7 @@ __global__ void __launch_bounds__(256) k_addnode_finish(const T* rowpart, const 
       row[j] = Tr<T>::sat(m);
     }
   }
+  }
 }
 template <typename T>
 cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
@@ -974,7 +978,7 @@ cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, cons
                            T* ceff, T* row, int gate, Mirror M, unsigned* uncertain, cudaStream_t st) {
   const int64_t ti = cdiv(std::max<int64_t>(r.hi - r.lo, 0), 32), tj = cdiv(npad, 32);
   if (ti + tj == 0) return cudaSuccess;
-  k_addnode_finish<T><<<(unsigned)(ti + tj), 256, 0, st>>>(rowpart, rowpartM, nchunk, colpart, nslab,
+  k_addnode_finish<T><<<(unsigned)std::min<int64_t>(ti + tj, 4 * num_sms()), 256, 0, st>>>(rowpart, rowpartM, nchunk, colpart, nslab,
                                                            part_ld, r, n, npad, ti, col, ceff, row,
                                                            gate, M, uncertain);
   return cudaGetLastError();
@@ -1191,7 +1195,8 @@ __global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, in
 
 template <typename T>
 cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, const T* c2,
-                  const T* rv2, unsigned long long* bytes_read, int sr, Mirror M, cudaStream_t st) {
+                  const T* rv2, unsigned long long* bytes_read, int sr, Mirror M, cudaStream_t st,
+                  int twin) {
   if (r.hi <= r.lo) return cudaSuccess;
   Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20);
   int grid = (int)cdiv(tl.warps, 8);
@@ -1203,6 +1208,7 @@ cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, 
         k_rank1_p8<true><<<g8, 256, 0, st>>>(D, ld, r, n, t8, c, rv, c2, rv2, bytes_read, M);
       else
         k_rank1_p8<false><<<g8, 256, 0, st>>>(D, ld, r, n, t8, c, rv, nullptr, nullptr, bytes_read, M);
+      if (!twin) return cudaGetLastError();
     }
   }
   if (c2 && sr)
@@ -1746,15 +1752,19 @@ __global__ void __launch_bounds__(256, 3) k_detect_p8(Rows r, int64_t ld, int64_
         if (acc & 0x80808080u) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            uint32_t u = cw + rw[q] - d[q];
-            uint32_t z = ~(u | ((u & 0x7F7F7F7Fu) + 0x7F7F7F7Fu)) & 0x80808080u;   // exact zero bytes
-            if (TWO) {
-              u = cw2 + rw2[q] - d[q];
-              z |= ~(u | ((u & 0x7F7F7F7Fu) + 0x7F7F7F7Fu)) & 0x80808080u;
+            // the exact per-word test again; only a word that has a zero byte
+            // (about one per flagged row in a 1024-column chunk) is decoded
+            const uint32_t u = cw + rw[q] - d[q];
+            uint32_t t = (cw + rwm[q] - d[q]) & ~u;
+            const uint32_t u2 = TWO ? cw2 + rw2[q] - d[q] : 0u;
+            if (TWO) t |= (cw2 + rwm2[q] - d[q]) & ~u2;
+            if (t & 0x80808080u) {
+              uint32_t z = ~(u | ((u & 0x7F7F7F7Fu) + 0x7F7F7F7Fu)) & 0x80808080u;   // exact zero bytes
+              if (TWO) z |= ~(u2 | ((u2 & 0x7F7F7F7Fu) + 0x7F7F7F7Fu)) & 0x80808080u;
+              // bytes 0..3 -> bits 4q' .. 4q'+3 of this lane's 16-column half
+              const uint32_t nib = ((((z >> 7) & 0x01010101u) * 0x01020408u) >> 24) & 0xFu;
+              word |= nib << ((q >> 2) * 16 + (q & 3) * 4);
             }
-            // bytes 0..3 -> bits 4q' .. 4q'+3 of this lane's 16-column half
-            const uint32_t nib = ((((z >> 7) & 0x01010101u) * 0x01020408u) >> 24) & 0xFu;
-            word |= nib << ((q >> 2) * 16 + (q & 3) * 4);
           }
           word &= vmask;
           const int64_t di = i - g0;   // the diagonal j == i
@@ -2101,7 +2111,7 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
                                          int64_t, int64_t, T*, T*, T*, int, Mirror, unsigned*,    \
                                          cudaStream_t);                                           \
   template cudaError_t rank1<T>(T*, int64_t, Rows, int64_t, const T*, const T*, const T*,          \
-                                const T*, unsigned long long*, int, Mirror, cudaStream_t);        \
+                                const T*, unsigned long long*, int, Mirror, cudaStream_t, int);        \
   template cudaError_t addnode_write<T>(T*, int64_t, Rows, int64_t, int64_t, int, const T*,        \
                                         const T*, T*, int64_t, const T*, const T*, cudaStream_t); \
   template cudaError_t detect<T>(T*, int64_t, Rows, int64_t, int64_t, const T*, const T*,          \

@@ -775,7 +775,10 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
                          int* fcnt_out, int* ftot_out, int* fcol_out, int* any, int sr,
                          const DetectCounters* dc, cudaStream_t st) {
   if (nopen <= 0) return cudaSuccess;
-  int grid = (int)std::min<int64_t>(cdiv(nopen, 8), (int64_t)num_sms() * 8);
+  // round 0 relaxes every open pair through its row's open entries; later
+  // rounds only the pairs whose row changed (often none: a small grid keeps
+  // the no-op round cheap)
+  int grid = (int)std::min<int64_t>(cdiv(nopen, 8), (int64_t)num_sms() * (ftot_in ? 2 : 8));
   if (sr)
     k_sparse_round<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff,
                                                fcnt_in, ftot_in, fcol_in, fcnt_out, ftot_out, fcol_out, any,

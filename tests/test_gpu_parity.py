@@ -791,3 +791,37 @@ def test_mirror8_invalidated_by_an_add(lib, rng):
         hg.remove_node(k)
         assert_parity(getD(h), oracle.fw(hg.W))
     assert h.mirror_width in (0, 16)
+
+
+@pytest.mark.parametrize("n,directed", [(1003, True), (1003, False), (517, True), (33, False)])
+def test_mirror8_ragged_sizes(lib, rng, n, directed):
+    """The int8 readers (detection, pass 1, rank-1) on sizes that end inside a
+    16-column group and a 512/1024-column chunk, directed and undirected (two
+    pivot terms), with absent edges (INF entries): every update kind, parity
+    after each."""
+    W = random_graph(rng, n, directed, density=0.7, lo=1, hi=25, inf_frac=0.05)
+    cap = n + 4
+    hg = synth.HostGraph(W, directed, cap=cap)
+    h = make(lib, W, directed, cap=cap)
+    for step in range(6):
+        kind = step % 3
+        if kind == 0:
+            o = rng.integers(1, 25, hg.n).astype(np.int32)
+            o[rng.random(hg.n) < 0.1] = INF
+            i = o.copy() if not directed else rng.integers(1, 25, hg.n).astype(np.int32)
+            h.add_node(o, i)
+            hg.add_node(o, i)
+        elif kind == 1:
+            k = int(rng.integers(0, hg.n))
+            h.remove_node(k)
+            hg.remove_node(k)
+        else:   # a tight edge increase (Theorem 4's affected set is non-empty)
+            u = int(rng.integers(0, hg.n))
+            row = np.where(np.arange(hg.n) == u, INF, hg.W[u, :hg.n]).astype(np.int64)
+            v = int(np.argmin(row))
+            if row[v] < INF:
+                w = int(row[v]) * 3 + 1
+                h.update_edge(u, v, w)
+                hg.set_edge(u, v, w)
+        assert h.mirror_width == 8
+        assert_parity(getD(h), oracle.fw(hg.W))

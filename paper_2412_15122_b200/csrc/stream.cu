@@ -1654,10 +1654,19 @@ __global__ void k_detect_rows(Rows r, const int* __restrict__ rowcnt, int64_t* r
 // 1024 columns of a row: lane l the 16-byte groups at 16 l and 512 + 16 l.
 // Row k (the removed node) is given c = INF: then u >= 0x7F - ... never 0
 // there (its d equals r), and the diagonal is masked in the rare path.
-constexpr int kD8R = 2, kD8S = 3;   // ring: rows per stage, stages (6 KB per warp; 3 CTAs per SM)
+#ifndef D8_R
+#define D8_R 2
+#endif
+#ifndef D8_S
+#define D8_S 3
+#endif
+#ifndef D8_MINB
+#define D8_MINB 3
+#endif
+constexpr int kD8R = D8_R, kD8S = D8_S;   // ring: rows per stage, stages (6 KB per warp; 3 CTAs per SM)
 constexpr int kD8Smem = 8 * kD8S * kD8R * 2 * 32 * 16;
 template <typename T, bool TWO, int MODE>
-__global__ void __launch_bounds__(256, 3) k_detect_p8(Rows r, int64_t ld, int64_t n, int64_t skip, Tiling tl,
+__global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, int64_t n, int64_t skip, Tiling tl,
                                                       const T* __restrict__ c1, const T* __restrict__ r1,
                                                       const T* __restrict__ c2, const T* __restrict__ r2,
                                                       DetectOut<T> o) {
@@ -1807,7 +1816,7 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
   DetectOut<T> o{anyrow, rowcnt, prow, pcol, plb, lcap, ctr, WT, ldw, M};
   const int g = (int)cdiv(tl.warps, 8);
   // int8 mirror: 1024-column chunks
-  const Tiling tl8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256, tune_wps("APSP_TUNE_DET8_WPS", 64));
+  const Tiling tl8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256, tune_wps("APSP_TUNE_DET8_WPS", 128));
   const int g8 = (int)cdiv(tl8.warps, 8);
   // the int32 twin exits when a packed kernel applies (decided on the device):
   // with a mirror it is launched at its residency (2 CTAs per SM) and strides

@@ -66,7 +66,7 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   p.off_colpart = take(sizeof(int32_t) * (size_t)kMaxSlabs * p.ld);
   p.off_rowoff = take(sizeof(int64_t) * (size_t)cap);
   p.off_rowcnt = take(sizeof(int32_t) * (size_t)cap);
-  p.off_chg = take(sizeof(int32_t) * (size_t)(cap + 32) * 2);   // + the round's frontier total
+  p.off_chg = take(sizeof(int32_t) * (size_t)(cap + 32) * 4);   // 4 rounds' counts + frontier totals
   p.ocap = std::max<int64_t>(p.lcap / 4, 1 << 18);
   p.off_prow = take(sizeof(int32_t) * (size_t)p.lcap);
   p.off_pcol = take(sizeof(int32_t) * (size_t)p.lcap);
@@ -382,9 +382,9 @@ apsp_status snap_row(apsp_handle* h, int64_t gi, T add, T* out) {
 template <typename T>
 apsp_status fw_impl_elem(apsp_handle* h);
 
-// (Re)build the int16 mirror from D: at the first update of a handle whose D
+// (Re)build the mirror of D: at the first update of a handle whose D
 // the caller filled (warm start), and after an int32 FW.  Mirror flag bit 0
-// set iff some finite local distance is >= 0x3FFF, bit 1 iff some local entry
+// set iff some finite local distance is >= the saturation value, bit 1 iff some local entry
 // is INF (stream.cu: kMirrorOff, kMirrorInf).
 // The int8 width is tried first (unless an earlier int8 build failed): if some
 // finite distance is >= 0x7F the build is redone at int16 (one host read of
@@ -588,8 +588,16 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   const int64_t n = h->n;
   Rows r = h->active();
   const int64_t lcap = h->plan.lcap, ocap = h->plan.ocap;
-  CKR(cudaMemsetAsync(h->rowcnt(), 0, sizeof(int) * h->cap, h->st));
-  CKR(cudaMemsetAsync(h->ctr(), 0, sizeof(DetectCounters), h->st));
+  {   // every per-update counter in one launch: per-row counts, the counters,
+      // the open-list cursors, the first four rounds' frontier counts, the flag
+    ZeroSet z{};
+    z.add(h->rowcnt(), h->cap);
+    z.add(reinterpret_cast<int*>(h->ctr()), (int64_t)(sizeof(DetectCounters) / sizeof(int)));
+    z.add(h->ocnt(), h->cap);
+    for (int q = 0; q < 4; ++q) z.add(h->chg(q), h->cap + 1);
+    z.add(h->anyflag(), 1);
+    CK(zero_set(z, h->st));
+  }
   // one streaming pass appends the need_update_list; then the per-row slices
   // of the open lists and Phi / max|A_i|
   PK(APSP_K_DETECT, h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n,
@@ -608,25 +616,29 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   // Rounds are frontier-based Bellman-Ford over each row's open entries: round
   // r relaxes every open pair of a row through the entries of that row that
   // changed in round r-1 (round 0: all open entries).  Frontier lists live in
-  // the row slices of two spare pair-list buffers, counts in chg(0)/chg(1).
+  // the row slices of two spare pair-list buffers; counts (and, at [cap], the
+  // round's total of changes) in chg(r % 4) — zeroed with the counters for
+  // rounds 0-3, by a memset for later ones.  "Converged" = the last round of
+  // a batch changed nothing: its total, read with the counters.
   int rounds = 0;
   int* fcol[2] = {h->prow(), h->pcol()};
+  int* last_total = h->anyflag();   // no round enqueued: 0
   auto enqueue_rounds = [&](int batch) -> apsp_status {
     for (int b = 0; b < batch; ++b, ++rounds) {
-      const int o = rounds & 1;
-      const int* fin_c = rounds == 0 ? h->ocnt() : h->chg(o ^ 1);
-      const int* fin_l = rounds == 0 ? h->ocol() : fcol[o ^ 1];
-      CKR(cudaMemsetAsync(h->chg(o), 0, sizeof(int) * (h->cap + 1), h->st));
-      if (b == batch - 1) CKR(cudaMemsetAsync(h->anyflag(), 0, sizeof(int), h->st));
+      const int o = rounds & 3, oi = (rounds + 3) & 3;
+      const int* fin_c = rounds == 0 ? h->ocnt() : h->chg(oi);
+      const int* fin_l = rounds == 0 ? h->ocol() : fcol[(rounds & 1) ^ 1];
+      if (rounds >= 4) CKR(cudaMemsetAsync(h->chg(o), 0, sizeof(int) * (h->cap + 1), h->st));
       PK(APSP_K_SPARSE_R, 0.0,
          sparse_round<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->gprow(), h->gpcol(),
                          h->glb<T>(), ocap, h->rowoff(), fin_c, rounds == 0 ? nullptr : fin_c + h->cap,
-                         fin_l, h->chg(o), h->chg(o) + h->cap, fcol[o], h->anyflag(), h->sr, h->ctr(), h->st));
+                         fin_l, h->chg(o), h->chg(o) + h->cap, fcol[rounds & 1], h->anyflag(), h->sr, h->ctr(),
+                         h->st));
+      last_total = h->chg(o) + h->cap;
     }
     return APSP_OK;
   };
   if (try_sparse) {
-    CKR(cudaMemsetAsync(h->ocnt(), 0, sizeof(int) * h->cap, h->st));
     // A: every listed entry rewritten with a walk length of G' (stale entries
     // skipped by the detection predicate), certified where it reaches lb
     PK(APSP_K_SPARSE0, 0.0,
@@ -657,7 +669,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   }
   // ---- the one host read of this update: counters (summed over ranks) ----
   long long* v = reinterpret_cast<long long*>(h->small());
-  CK(pack_counters(h->ctr(), h->anyflag(), v, h->st));   // total rows ovf1 ovf2 any | maxrow
+  CK(pack_counters(h->ctr(), last_total, v, h->st));   // total rows ovf1 ovf2 changed | maxrow
   if (h->world > 1) {
     NK(h->comm->allreduce(v, 5, ncclInt64, ncclSum, h->st));
     NK(h->comm->allreduce(v + 5, 1, ncclInt64, ncclMax, h->st));
@@ -688,9 +700,9 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     batch *= 2;
     apsp_status s = enqueue_rounds(std::min(batch, h->max_rounds - rounds));
     if (s != APSP_OK) return s;
-    if (h->world > 1) NK(h->comm->allreduce(h->anyflag(), 1, ncclInt32, ncclMax, h->st));
+    if (h->world > 1) NK(h->comm->allreduce(last_total, 1, ncclInt32, ncclMax, h->st));
     int* hflag = reinterpret_cast<int*>(h->host_small);
-    CKR(cudaMemcpyAsync(hflag, h->anyflag(), sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    CKR(cudaMemcpyAsync(hflag, last_total, sizeof(int), cudaMemcpyDeviceToHost, h->st));
     CKR(cudaStreamSynchronize(h->st));
     changed = *hflag != 0;
   }

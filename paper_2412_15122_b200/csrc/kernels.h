@@ -222,6 +222,14 @@ inline cudaError_t mirror_cross(const float*, int64_t, Rows, int64_t, int64_t, i
   return cudaSuccess;
 }
 cudaError_t pack_counters(const DetectCounters* c, const int* any, long long* v, cudaStream_t st);
+// zero up to 8 int buffers in one launch
+struct ZeroSet {
+  int* p[8];
+  int64_t n[8];
+  int k;
+  void add(int* ptr, int64_t count) { p[k] = ptr; n[k] = count; ++k; }
+};
+cudaError_t zero_set(const ZeroSet& z, cudaStream_t st);
 double microbench(int kind, void* buf, size_t bytes, cudaStream_t st);   // microbench.cu
 int num_sms();
 

@@ -2044,6 +2044,19 @@ cudaError_t pack_counters(const DetectCounters* c, const int* any, long long* v,
   return cudaGetLastError();
 }
 
+__global__ void k_zero_set(ZeroSet z) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int b = 0; b < z.k; ++b)
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < z.n[b]; e += stride) z.p[b][e] = 0;
+}
+cudaError_t zero_set(const ZeroSet& z, cudaStream_t st) {
+  int64_t most = 1;
+  for (int b = 0; b < z.k; ++b) most = std::max(most, z.n[b]);
+  const int grid = (int)std::min<int64_t>(cdiv(most, 256), 2 * num_sms());
+  k_zero_set<<<grid, 256, 0, st>>>(z);
+  return cudaGetLastError();
+}
+
 __global__ void k_count_nonzero(const int* a, int64_t m, unsigned long long* out) {
   unsigned c = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;

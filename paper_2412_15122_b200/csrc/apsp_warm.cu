@@ -742,10 +742,8 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   CKR(cudaMemsetAsync(&h->ctr()->err, 0, sizeof(unsigned), h->st));
   CKR(cudaMemsetAsync(h->wmin_dev(), 0xff, sizeof(unsigned), h->st));
   CK(validate_vec<T>(reinterpret_cast<const T*>(out_w), nullptr, n, ld, ow, &h->ctr()->err, h->wmin_dev(),
-                     h->st));
-  CK(validate_vec<T>(reinterpret_cast<const T*>(in_w),
-                     h->directed ? nullptr : reinterpret_cast<const T*>(out_w), n, ld, iw,
-                     &h->ctr()->err, h->wmin_dev(), h->st));
+                     h->st, reinterpret_cast<const T*>(in_w),
+                     h->directed ? nullptr : reinterpret_cast<const T*>(out_w), iw));   // both vectors, one launch
   unsigned* herr = reinterpret_cast<unsigned*>(h->host_small);
   CKR(cudaMemcpyAsync(herr, &h->ctr()->err, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
   CKR(cudaMemcpyAsync(herr + 1, h->wmin_dev(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
@@ -796,10 +794,8 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
      rank1<T>(h->Dl<T>(), ld, r, n, ceff, row, nullptr, nullptr, h->rank1_bytes(), h->sr, h->mirror<T>(),
               h->st, mirror8_known_valid(h) ? 0 : 1));
   CK(addnode_write<T>(h->Dl<T>(), ld, r, n, x, h->local(x) ? 1 : 0, col, row, h->WT<T>(), ld, ow,
-                      iw, h->st));
-  Rows rx = r;   // the active rows after the add (row x joins them if it is local)
-  if (h->local(x)) rx.hi = x + 1;
-  CK(mirror_cross(h->Dl<T>(), ld, rx, n + 1, x, x, h->mirror<T>(), h->st));
+                      iw, h->mirror<T>(), h->st));
+  // (addnode_write mirrored the new row / column)
   CKR(cudaStreamWaitEvent(h->st, h->ev_join, 0));   // shortlist upkeep (side stream) done
   h->n = n + 1;
   if (new_index) *new_index = x;

@@ -65,8 +65,10 @@ struct Rows {
 };
 
 template <typename T>
+// (inb, in2b, outb): an optional second vector validated in the same launch
 cudaError_t validate_vec(const T* in, const T* in2, int64_t n, int64_t npad, T* out,
-                         unsigned int* err, unsigned* wmin_bits, cudaStream_t st);
+                         unsigned int* err, unsigned* wmin_bits, cudaStream_t st, const T* inb = nullptr,
+                         const T* in2b = nullptr, T* outb = nullptr);
 template <typename T>
 cudaError_t transpose_in(const T* W, int64_t ldw, int64_t n, T* WT, int64_t ldt, unsigned int* err,
                          unsigned* wmin_bits, cudaStream_t st);
@@ -98,7 +100,7 @@ cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, 
 template <typename T>
 cudaError_t addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xlocal,
                           const T* col, const T* row, T* WT, int64_t ldw, const T* ow,
-                          const T* iw, cudaStream_t st);
+                          const T* iw, Mirror M, cudaStream_t st);
 // mode 0: mark rows with flags (anyrow); 1: append the need_update_list
 // (prow/pcol/plb, rowcnt, ctr->total/overflow); 2: reset flagged entries in place
 template <typename T>

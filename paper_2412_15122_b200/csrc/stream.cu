@@ -68,7 +68,9 @@ __device__ __forceinline__ void wmin_fold(unsigned* wmin_bits, T v, bool valid) 
 
 template <typename T>
 __global__ void k_validate_vec(const T* in, const T* in2, int64_t n, int64_t npad, T* out,
-                               unsigned int* err, unsigned* wmin_bits) {
+                               unsigned int* err, unsigned* wmin_bits, const T* inb, const T* in2b,
+                               T* outb) {
+  if (blockIdx.y == 1) { in = inb; in2 = in2b; out = outb; }   // the second vector of a pair
   for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < npad; j0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = j0 + threadIdx.x;
     T v = Tr<T>::inf();
@@ -92,9 +94,11 @@ __global__ void k_validate_vec(const T* in, const T* in2, int64_t n, int64_t npa
 }
 template <typename T>
 cudaError_t validate_vec(const T* in, const T* in2, int64_t n, int64_t npad, T* out,
-                         unsigned int* err, unsigned* wmin_bits, cudaStream_t st) {
-  int grid = (int)std::min<int64_t>(cdiv(npad, 256), 4 * num_sms());
-  k_validate_vec<T><<<grid, 256, 0, st>>>(in, in2, n, npad, out, err, wmin_bits);
+                         unsigned int* err, unsigned* wmin_bits, cudaStream_t st, const T* inb,
+                         const T* in2b, T* outb) {
+  const int grid = (int)std::min<int64_t>(cdiv(npad, 256), 4 * num_sms());
+  k_validate_vec<T><<<dim3(grid, inb ? 2 : 1), 256, 0, st>>>(in, in2, n, npad, out, err, wmin_bits, inb, in2b,
+                                                            outb);
   return cudaGetLastError();
 }
 
@@ -1226,15 +1230,27 @@ cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, 
 template <typename T>
 __global__ void k_addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xlocal,
                                 const T* col, const T* row, T* WT, int64_t ldw, const T* ow,
-                                const T* iw) {
+                                const T* iw, Mirror M) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = r.lo + tid; i < r.hi; i += stride) D[(i - r.row0) * ld + x] = col[i];
+  const bool mir = has_mirror(M);   // the new row / column go to the mirror as well
+  unsigned mbits = 0;
+  for (int64_t i = r.lo + tid; i < r.hi; i += stride) {
+    D[(i - r.row0) * ld + x] = col[i];
+    if (mir) mbits |= mput(M, (i - r.row0) * ld + x, col[i]);
+  }
   if (xlocal) {
     T* Dx = D + (x - r.row0) * ld;
-    for (int64_t j = tid; j < n; j += stride) Dx[j] = row[j];
-    if (tid == 0) Dx[x] = T(0);
+    for (int64_t j = tid; j < n; j += stride) {
+      Dx[j] = row[j];
+      if (mir) mbits |= mput(M, (x - r.row0) * ld + j, row[j]);
+    }
+    if (tid == 0) {
+      Dx[x] = T(0);
+      if (mir) mbits |= mput(M, (x - r.row0) * ld + x, T(0));
+    }
   }
+  if (mir) mirror_post(M, mbits);
   for (int64_t t = tid; t < n; t += stride) {
     WT[x * ldw + t] = iw[t];    // WT[x][t] = W[t][x] = in-edge t -> x
     WT[t * ldw + x] = ow[t];    // WT[t][x] = W[x][t] = out-edge x -> t
@@ -1244,9 +1260,9 @@ __global__ void k_addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, 
 template <typename T>
 cudaError_t addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xlocal,
                           const T* col, const T* row, T* WT, int64_t ldw, const T* ow,
-                          const T* iw, cudaStream_t st) {
+                          const T* iw, Mirror M, cudaStream_t st) {
   int grid = (int)std::min<int64_t>(cdiv(n, 256), 4 * num_sms());
-  k_addnode_write<T><<<grid, 256, 0, st>>>(D, ld, r, n, x, xlocal, col, row, WT, ldw, ow, iw);
+  k_addnode_write<T><<<grid, 256, 0, st>>>(D, ld, r, n, x, xlocal, col, row, WT, ldw, ow, iw, M);
   return cudaGetLastError();
 }
 
@@ -2119,7 +2135,7 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
 
 #define INST(T)                                                                                   \
   template cudaError_t validate_vec<T>(const T*, const T*, int64_t, int64_t, T*, unsigned int*, unsigned*,    \
-                                       cudaStream_t);                                             \
+                                       cudaStream_t, const T*, const T*, T*);                                             \
   template cudaError_t transpose_in<T>(const T*, int64_t, int64_t, T*, int64_t, unsigned int*,     \
                                        unsigned*, cudaStream_t);                                  \
   template cudaError_t fill<T>(T*, int64_t, T, cudaStream_t);                                      \
@@ -2135,7 +2151,7 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
   template cudaError_t rank1<T>(T*, int64_t, Rows, int64_t, const T*, const T*, const T*,          \
                                 const T*, unsigned long long*, int, Mirror, cudaStream_t, int);        \
   template cudaError_t addnode_write<T>(T*, int64_t, Rows, int64_t, int64_t, int, const T*,        \
-                                        const T*, T*, int64_t, const T*, const T*, cudaStream_t); \
+                                        const T*, T*, int64_t, const T*, const T*, Mirror, cudaStream_t); \
   template cudaError_t detect<T>(T*, int64_t, Rows, int64_t, int64_t, const T*, const T*,          \
                                  const T*, const T*, float, int, int*, int*, int*, int*, T*,      \
                                  int64_t, DetectCounters*, const T*, int64_t, int, Mirror,        \

@@ -1936,57 +1936,48 @@ cudaError_t tombstone(T* D, int64_t ld, Rows r, int64_t n, int64_t k, T* WT, int
 // k) are disjoint, so one launch suffices.  Clear: row / column last := INF,
 // then the int16 mirror of row / column k is re-derived.
 // ---------------------------------------------------------------------------
+// Swap-with-last after a removal, one launch: node `last` moves into slot k
+// (row/column of D and WT, mirror of row/column k), then row/column `last`
+// become INF.  Every copied element is copied, cleared and mirrored by the
+// same thread, in that order, so no element is read after another thread
+// overwrote it (row k / column k of D and WT were tombstoned before).
 template <typename T>
-__global__ void k_move_last_copy(T* D, int64_t ld, Rows r, int64_t k, int64_t last, int row_copy, T* WT,
-                                 int64_t ldw) {
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const bool kl = k >= r.lo && k < r.hi;
-  for (int64_t j = tid; j < last; j += stride) {
-    if (j == k) continue;
-    if (row_copy) D[(k - r.row0) * ld + j] = D[(last - r.row0) * ld + j];
-    WT[k * ldw + j] = WT[last * ldw + j];
-    WT[j * ldw + k] = WT[j * ldw + last];
-  }
-  for (int64_t i = r.lo + tid; i < min(r.hi, last); i += stride)
-    if (i != k) D[(i - r.row0) * ld + k] = D[(i - r.row0) * ld + last];
-  if (tid == 0) {
-    if (kl) D[(k - r.row0) * ld + k] = T(0);
-    WT[k * ldw + k] = T(0);
-  }
-}
-template <typename T>
-__global__ void k_move_last_clear(T* D, int64_t ld, Rows r, int64_t k, int64_t last, int64_t n, T* WT,
-                                  int64_t ldw, Mirror M) {
+__global__ void k_move_last(T* D, int64_t ld, Rows r, int64_t k, int64_t last, int64_t n, int row_copy,
+                            T* WT, int64_t ldw, Mirror M) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const T I = Tr<T>::inf();
-  if (last >= r.lo && last < r.hi)
-    for (int64_t j = tid; j < n; j += stride) D[(last - r.row0) * ld + j] = I;
-  for (int64_t i = r.lo + tid; i < r.hi; i += stride) D[(i - r.row0) * ld + last] = I;
-  for (int64_t j = tid; j < n; j += stride) {
+  const bool kl = k >= r.lo && k < r.hi, ll = last >= r.lo && last < r.hi;
+  const bool mv = k != last, mir = has_mirror(M) && mv;
+  unsigned bits = 0;
+  for (int64_t j = tid; j < n; j += stride) {   // row k <- row last; WT row/col k <- last
+    if (mv && j < last && j != k) {
+      if (row_copy) D[(k - r.row0) * ld + j] = D[(last - r.row0) * ld + j];
+      WT[k * ldw + j] = WT[last * ldw + j];
+      WT[j * ldw + k] = WT[j * ldw + last];
+    }
+    if (ll) D[(last - r.row0) * ld + j] = I;
     WT[last * ldw + j] = I;
     WT[j * ldw + last] = I;
+    if (mir && kl && j < last) bits |= mput(M, (k - r.row0) * ld + j, j == k ? T(0) : D[(k - r.row0) * ld + j]);
   }
-  if (has_mirror(M) && k != last) {   // the mirror of row / column k over the remaining nodes [0, last)
-    unsigned bits = 0;
-    if (k >= r.lo && k < r.hi)
-      for (int64_t j = tid; j < last; j += stride) bits |= mput(M, (k - r.row0) * ld + j, D[(k - r.row0) * ld + j]);
-    for (int64_t i = r.lo + tid; i < min(r.hi, last); i += stride)
-      if (i != k) bits |= mput(M, (i - r.row0) * ld + k, D[(i - r.row0) * ld + k]);
-    mirror_post(M, bits);
+  for (int64_t i = r.lo + tid; i < r.hi; i += stride) {   // column k <- column last
+    T* Di = D + (i - r.row0) * ld;
+    if (mv && i < last && i != k) Di[k] = Di[last];
+    Di[last] = I;
+    if (mir && i < last && i != k) bits |= mput(M, (i - r.row0) * ld + k, Di[k]);
   }
+  if (tid == 0 && mv) {
+    if (kl) D[(k - r.row0) * ld + k] = T(0);
+    WT[k * ldw + k] = T(0);
+  }
+  if (mir) mirror_post(M, bits);
 }
 template <typename T>
 cudaError_t move_last(T* D, int64_t ld, Rows r, int64_t n, int64_t k, int row_copy, T* WT, int64_t ldw,
                       Mirror M, cudaStream_t st) {
-  const int64_t last = n - 1;
   const int grid = (int)std::min<int64_t>(cdiv(n, 256), 4 * num_sms());
-  if (k != last) {
-    k_move_last_copy<T><<<grid, 256, 0, st>>>(D, ld, r, k, last, row_copy, WT, ldw);
-    CUDA_TRY(cudaGetLastError());
-  }
-  k_move_last_clear<T><<<grid, 256, 0, st>>>(D, ld, r, k, last, n, WT, ldw, M);
+  k_move_last<T><<<grid, 256, 0, st>>>(D, ld, r, k, n - 1, n, row_copy, WT, ldw, M);
   return cudaGetLastError();
 }
 

@@ -371,6 +371,21 @@ apsp_status bcast_from_owner(apsp_handle* h, T* buf, int64_t count, int64_t gi) 
 }
 
 // snapshot row gi of D (+ add) into out (padded to ld with INF), all ranks
+// Pivot snapshots: c[i] = D[i][col] + add over the local rows and r = row `ri`
+// of D (every rank) — one launch on one GPU, gather + broadcast otherwise.
+template <typename T>
+apsp_status snap_row(apsp_handle* h, int64_t gi, T add, T* out);
+template <typename T>
+apsp_status snap_pivots(apsp_handle* h, int64_t col, T add, T* c, int64_t ri, T* rout) {
+  if (h->world == 1) {
+    CK(gather_col_row<T>(h->Dl<T>(), h->ld, h->active(), col, add, c, h->Drow<T>(ri), h->n, h->ld, rout,
+                         h->sr, h->st));
+    return APSP_OK;
+  }
+  CK(gather_col<T>(h->Dl<T>(), h->ld, h->active(), col, add, c, h->sr, h->st));
+  return snap_row<T>(h, ri, T(0), rout);
+}
+
 template <typename T>
 apsp_status snap_row(apsp_handle* h, int64_t gi, T add, T* out) {
   if (h->local(gi)) CK(copy_vec<T>(h->Drow<T>(gi), h->n, h->ld, add, out, h->st));
@@ -818,8 +833,7 @@ apsp_status remove_node_impl(apsp_handle* h, int64_t k, int64_t* moved_from, aps
   Rows r = h->active();
   T* c1 = h->vec<T>(4);
   T* r1 = h->vec<T>(5);
-  CK(gather_col<T>(h->Dl<T>(), ld, r, k, T(0), c1, h->sr, h->st));   // t1 = SPD(i, k)
-  apsp_status s = snap_row<T>(h, k, T(0), r1);                 // t2 = SPD(k, j)
+  apsp_status s = snap_pivots<T>(h, k, T(0), c1, k, r1);   // t1 = SPD(i, k), t2 = SPD(k, j)
   if (s != APSP_OK) return s;
   if (info) info->kind = 4;
   s = recompute<T>(h, k, c1, r1, nullptr, nullptr, true, info);
@@ -884,12 +898,10 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
       return APSP_OK;
     }
     // D'[i][j] = min(D[i][j], D[i][u] + w + D[v][j] (, D[i][v] + w + D[u][j]))
-    CK(gather_col<T>(h->Dl<T>(), ld, r, u, w_new, c1, h->sr, h->st));
-    apsp_status s = snap_row<T>(h, v, T(0), r1);
+    apsp_status s = snap_pivots<T>(h, u, w_new, c1, v, r1);
     if (s != APSP_OK) return s;
     if (und) {
-      CK(gather_col<T>(h->Dl<T>(), ld, r, v, w_new, c2, h->sr, h->st));
-      s = snap_row<T>(h, u, T(0), r2);
+      s = snap_pivots<T>(h, v, w_new, c2, u, r2);
       if (s != APSP_OK) return s;
     }
     PK(APSP_K_RANK1, 0.0,   // work: bytes actually read, counted on the device
@@ -911,12 +923,10 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
     CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
     return APSP_OK;
   }
-  CK(gather_col<T>(h->Dl<T>(), ld, r, u, w_old, c1, h->sr, h->st));   // D[i][u] + w_old
-  apsp_status s = snap_row<T>(h, v, T(0), r1);                  // D[v][j]
+  apsp_status s = snap_pivots<T>(h, u, w_old, c1, v, r1);   // D[i][u] + w_old, D[v][j]
   if (s != APSP_OK) return s;
   if (und) {
-    CK(gather_col<T>(h->Dl<T>(), ld, r, v, w_old, c2, h->sr, h->st));
-    s = snap_row<T>(h, u, T(0), r2);
+    s = snap_pivots<T>(h, v, w_old, c2, u, r2);
     if (s != APSP_OK) return s;
   }
   // W' (WT and the shortlists) before the D0 reset

@@ -80,6 +80,9 @@ template <typename T>
 cudaError_t gather_col(const T* D, int64_t ld, Rows r, int64_t col, T add, T* out, int sr,
                        cudaStream_t st);
 template <typename T>
+cudaError_t gather_col_row(const T* D, int64_t ld, Rows r, int64_t col, T add, T* cout, const T* rsrc,
+                           int64_t n, int64_t npad, T* rout, int sr, cudaStream_t st);
+template <typename T>
 cudaError_t copy_vec(const T* src, int64_t n, int64_t npad, T add, T* out, cudaStream_t st);
 template <typename T>
 cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow, const T* iw,

@@ -194,6 +194,27 @@ cudaError_t gather_col(const T* D, int64_t ld, Rows r, int64_t col, T add, T* ou
 }
 
 // out[j] = sat(src[j] + add) for j < n, INF for n <= j < npad
+// gather_col and copy_vec of a pivot row in one launch (one GPU: the row is local)
+template <typename T, int SR>
+__global__ void k_gather_col_row(const T* D, int64_t ld, Rows r, int64_t col, T add, T* cout,
+                                 const T* rsrc, int64_t n, int64_t npad, T* rout) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = r.lo + tid; i < r.hi; i += stride)
+    cout[i] = Tr<T, SR>::sat(Tr<T, SR>::add(D[(i - r.row0) * ld + col], add));
+  for (int64_t j = tid; j < npad; j += stride) rout[j] = j < n ? rsrc[j] : Tr<T>::inf();
+}
+template <typename T>
+cudaError_t gather_col_row(const T* D, int64_t ld, Rows r, int64_t col, T add, T* cout, const T* rsrc,
+                           int64_t n, int64_t npad, T* rout, int sr, cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>(cdiv(std::max<int64_t>(r.hi - r.lo, npad), 256), 4 * num_sms());
+  if (sr)
+    k_gather_col_row<T, 1><<<grid, 256, 0, st>>>(D, ld, r, col, add, cout, rsrc, n, npad, rout);
+  else
+    k_gather_col_row<T, 0><<<grid, 256, 0, st>>>(D, ld, r, col, add, cout, rsrc, n, npad, rout);
+  return cudaGetLastError();
+}
+
 template <typename T>
 __global__ void k_copy_vec(const T* src, int64_t n, int64_t npad, T add, T* out) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npad;
@@ -2132,6 +2153,8 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
   template cudaError_t fill<T>(T*, int64_t, T, cudaStream_t);                                      \
   template cudaError_t init_d<T>(T*, int64_t, Rows, int64_t, const T*, int64_t, cudaStream_t);     \
   template cudaError_t gather_col<T>(const T*, int64_t, Rows, int64_t, T, T*, int, cudaStream_t);  \
+  template cudaError_t gather_col_row<T>(const T*, int64_t, Rows, int64_t, T, T*, const T*, int64_t,     \
+                                         int64_t, T*, int, cudaStream_t);                               \
   template cudaError_t copy_vec<T>(const T*, int64_t, int64_t, T, T*, cudaStream_t);               \
   template cudaError_t addnode_pass1<T>(const T*, int64_t, Rows, int64_t, const T*, const T*, T*,  \
                                         T*, T*, int64_t, int*, int*, int, int, Mirror,            \

@@ -132,7 +132,7 @@ struct apsp_handle {
   Plan plan;
   cudaStream_t st;
   cudaStream_t st2 = nullptr;    // side stream: shortlist upkeep overlapped with the D passes
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_row = nullptr;
   int rank, world;
   Comm* comm = nullptr;          // world > 1: NCCL or in-process group (comm.h)
   // options
@@ -247,6 +247,8 @@ struct apsp_handle {
   unsigned* fw16_flag() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 392); }
   unsigned* mirror_flag() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 396); }
   unsigned* pass1_uncertain() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 400); }
+  unsigned* addrow_full() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 404); }
+  int* addrow_count() { return reinterpret_cast<int*>(ws + plan.off_small + 408); }
   // saturated mirror of D (kernels.h), int32 handles only: int8 (own buffer)
   // or int16 (in the packed-FW buffer), the width picked at the last build
   template <typename T> Mirror mirror() {
@@ -774,6 +776,17 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   // side stream while pass 1 / rank-1 stream D (joined before returning)
   CKR(cudaEventRecord(h->ev_fork, h->st));
   CKR(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
+  // the new row from the few rows that can attain it (one GPU, int8 mirror
+  // valid as read above): on the side stream, under pass 1
+  bool srow = false;
+  if constexpr (std::is_same<T, int32_t>::value) srow = h->world == 1 && mirror8_known_valid(h);
+  if constexpr (std::is_same<T, int32_t>::value) {
+    if (srow) {
+      CK2(addrow_s(ow, n, h->mirror<T>().m8, ld, h->row0, row, ld, reinterpret_cast<int*>(h->vec<T>(5)),
+                   h->addrow_count(), h->addrow_full(), (int)ld, h->st2));
+      CKR(cudaEventRecord(h->ev_row, h->st2));
+    }
+  }
   CK2(shortlist_add_bound<T>(h->slid(), h->slw<T>(), h->wnext<T>(), ow, n, x, h->st2));  // x -> j
   CK2(shortlist_build_one<T>(iw, 0, n + 1, x, h->slid(), h->slw<T>(), h->wnext<T>(),
                              h->st2));   // in-edges of x: row x of WT is in_w
@@ -792,9 +805,10 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
     CKR(cudaMemsetAsync(unc, 0, sizeof(unsigned), h->st));
     PK(APSP_K_ADD_PASS1, h->mirror_hint ? h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n : 0.0,
        addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
-                        &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), unc, 1, h->st));
+                        &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), unc, 1, h->st, srow ? 0 : 1));
+    if (srow) CKR(cudaStreamWaitEvent(h->st, h->ev_row, 0));   // the side stream's new row
     CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
-                         ceff, row, 1, h->mirror<T>(), unc, h->st));
+                         ceff, row, 1, h->mirror<T>(), unc, h->st, srow ? h->addrow_full() : nullptr));
   }
   PK(APSP_K_ADD_PASS1, try_packed && h->mirror_hint ? 0.0 : 4.0 * (double)(r.hi - r.lo) * (double)n,
      addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
@@ -1179,6 +1193,7 @@ void release_handle(apsp_handle* h) {
   if (h->st2) { cudaStreamSynchronize(h->st2); cudaStreamDestroy(h->st2); }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->ev_row) cudaEventDestroy(h->ev_row);
   delete h->comm;
   if (h->host_small) cudaFreeHost(h->host_small);
   delete h;
@@ -1221,7 +1236,8 @@ apsp_status create_impl(apsp_handle** out, apsp_dtype dtype, int directed, int64
   }
   if (cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_row, cudaEventDisableTiming) != cudaSuccess) {
     cudaFreeHost(h->host_small);
     delete h;
     return APSP_E_CUDA;

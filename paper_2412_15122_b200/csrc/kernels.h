@@ -88,12 +88,16 @@ template <typename T>
 cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow, const T* iw,
                           T* rowpart, T* rowpartM, T* colpart, int64_t part_ld, int* nchunk_out,
                           int* nslab_out, int max_slabs, int sr, Mirror M, const unsigned* uncertain, int packed,
-                          cudaStream_t st);
+                          cudaStream_t st, int colp = 1, const unsigned* full = nullptr);
+// The new row of an add from the rows S = {t : out[t] <= Rb} (int8 mirror, one GPU):
+// *full = 1 when the shortcut does not apply (pass 1 must compute the row)
+cudaError_t addrow_s(const int32_t* ow, int64_t n, const uint8_t* m8, int64_t ld, int64_t row0, int32_t* row,
+                     int64_t npad, int* slist, int* scount, unsigned* full, int limit, cudaStream_t st);
 template <typename T>
 cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
                            int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,
                            T* ceff, T* row, int gate, Mirror M, unsigned* uncertain,
-                           cudaStream_t st);
+                           cudaStream_t st, const unsigned* row_full = nullptr);   // see addrow_s
 template <typename T>
 // twin = 0: the caller knows the int8 mirror is valid (its flag was read since
 // the last write that could change it), so only the int8 pass is launched

@@ -594,13 +594,16 @@ __device__ __forceinline__ uint32_t p8_reduce_scatter(const uint32_t (&w)[8], in
   return op(k1, __shfl_xor_sync(0xffffffffu, k1, 1));
 }
 
-template <typename T>
+// COLP = false: the new row is not computed here (k_addrow does it from the
+// few rows that can attain it); `full` (nullable) gates a launch on a flag.
+template <typename T, bool COLP>
 __global__ void __launch_bounds__(256, P8_MINB) k_addnode_pass1_p8(Rows r, int64_t ld, int64_t n, Tiling tl,
                                                              const T* __restrict__ ow,
                                                              const T* __restrict__ iw, T* rowpart,
                                                              T* rowpartM, T* colpart, int64_t part_ld,
-                                                             Mirror M) {
+                                                             Mirror M, const unsigned* full) {
   if (!pass1_packed_runs<T, 0>(M) || M.m8 == nullptr) return;
+  if (full && *(volatile const unsigned*)full == 0u) return;
   extern __shared__ uint4 ring_raw[];   // [warp][stage][row][lane]: 64 KB per CTA
   auto ring = reinterpret_cast<uint4 (*)[kP8S][kP8R][32]>(ring_raw);
   const bool has_inf = (*(volatile unsigned*)M.flag & kMirrorInf) != 0u;
@@ -651,10 +654,10 @@ __global__ void __launch_bounds__(256, P8_MINB) k_addnode_pass1_p8(Rows r, int64
     constexpr bool SPECIAL = decltype(special)::value;
 #pragma unroll
     for (int s = 0; s < kP8S - 1; ++s) issue(s);
-    uint32_t onext = out_of(lane & (kP8G - 1));   // group 0's out[i], lane l < kP8G: row l
+    uint32_t onext = COLP ? out_of(lane & (kP8G - 1)) : 0u;   // group 0's out[i], lane l < kP8G: row l
     for (int g0r = 0; g0r < rows; g0r += kP8G) {
       const uint32_t ocur = onext;
-      onext = out_of(g0r + kP8G + (lane & (kP8G - 1)));   // next group's, in flight meanwhile
+      if (COLP) onext = out_of(g0r + kP8G + (lane & (kP8G - 1)));   // next group's, in flight meanwhile
       uint32_t pw[kP8G / 2], mw[kP8G / 2];   // row results, two rows per word
 #pragma unroll
       for (int sg = 0; sg < kP8G / kP8R; ++sg) {
@@ -664,7 +667,7 @@ __global__ void __launch_bounds__(256, P8_MINB) k_addnode_pass1_p8(Rows r, int64
         uint32_t prow[kP8R], mrow[kP8R];
 #pragma unroll
         for (int h = 0; h < kP8R; ++h) {
-          const uint32_t orep = __shfl_sync(0xffffffffu, ocur, sg * kP8R + h);
+          const uint32_t orep = COLP ? __shfl_sync(0xffffffffu, ocur, sg * kP8R + h) : 0u;
           const uint4 wv = ring[warp][s % kP8S][h][lane];
           const uint4 lo = widen8(make_uint2(wv.x, wv.y)), hi = widen8(make_uint2(wv.z, wv.w));
           uint32_t dw[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
@@ -687,8 +690,10 @@ __global__ void __launch_bounds__(256, P8_MINB) k_addnode_pass1_p8(Rows r, int64
             pb = __viaddmin_s16x2(dw[q + 1], in2[q + 1], pb);
             ma = __viaddmax_s16x2(dw[q], nout2[q], ma);
             mb = __viaddmax_s16x2(dw[q + 1], nout2[q + 1], mb);
-            colp2[q] = __viaddmin_s16x2(orep, dw[q], colp2[q]);
-            colp2[q + 1] = __viaddmin_s16x2(orep, dw[q + 1], colp2[q + 1]);
+            if (COLP) {
+              colp2[q] = __viaddmin_s16x2(orep, dw[q], colp2[q]);
+              colp2[q + 1] = __viaddmin_s16x2(orep, dw[q + 1], colp2[q + 1]);
+            }
           }
           prow[h] = __vmins2(pa, pb);
           mrow[h] = __vmaxs2(ma, mb);
@@ -734,6 +739,7 @@ __global__ void __launch_bounds__(256, P8_MINB) k_addnode_pass1_p8(Rows r, int64
   if (has_inf || tail) run(std::true_type{});
   else run(std::false_type{});
   cp_async_wait<0>();
+  if (!COLP) return;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int64_t j0 = g0 + 2 * q;
@@ -743,6 +749,116 @@ __global__ void __launch_bounds__(256, P8_MINB) k_addnode_pass1_p8(Rows r, int64
       if (j0 + 1 < n) dst[1] = (T)(colp2[q] >> 16);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// The new row of an add, from the rows that can attain it (int8 mirror valid,
+// one GPU).  row[j] = min_t out[t] + D[t][j] is attained at a t* with
+// out[t*] <= row[j] <= Rb, where Rb = out[t0] + max_j D[t0][j] bounds every
+// row[j] (t0: the cheapest out-edge).  So S = {t : out[t] <= Rb} contains
+// every minimiser and the min over S is exact — typically a few hundred rows
+// (out ~ U[1,1000] and distances < 0x7F).  k_addrow_setup (one CTA) finds t0,
+// Rb and S; k_addrow reduces the |S| mirror rows; both run on the side
+// stream under pass 1.  Where the bound is useless (row t0 holds an INF) S is
+// every row with a finite out-edge — still exact, just a longer reduction.
+// *full stays 0 (the finish kernel keeps this row).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_addrow_setup(const int32_t* __restrict__ ow, int64_t n,
+                                                       const uint8_t* __restrict__ m8, int64_t ld,
+                                                       int64_t row0, int32_t* row, int64_t npad, int* slist,
+                                                       int* scount, unsigned* full, int limit) {
+  __shared__ int32_t sv[32];
+  __shared__ int si[32];
+  __shared__ int cnt;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int32_t I = APSP_INF_I32_DEV;
+  for (int64_t j = tid; j < npad; j += blockDim.x) row[j] = I;
+  // t0 = argmin out (smallest index among ties)
+  int32_t bv = I;
+  int bi = -1;
+  for (int64_t t = tid; t < n; t += blockDim.x)
+    if (ow[t] < bv) { bv = ow[t]; bi = (int)t; }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int32_t v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (v2 < bv || (v2 == bv && i2 >= 0 && (bi < 0 || i2 < bi))) { bv = v2; bi = i2; }
+  }
+  if (lane == 0) { sv[warp] = bv; si[warp] = bi; }
+  if (tid == 0) cnt = 0;
+  __syncthreads();
+  if (warp == 0) {
+    bv = sv[lane]; bi = si[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int32_t v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (v2 < bv || (v2 == bv && i2 >= 0 && (bi < 0 || i2 < bi))) { bv = v2; bi = i2; }
+    }
+    if (lane == 0) { sv[0] = bv; si[0] = bi; }
+  }
+  __syncthreads();
+  const int32_t omin = sv[0];
+  const int t0 = si[0];
+  __syncthreads();
+  if (omin >= I || t0 < 0) {   // no out-edge: the new row is all INF
+    if (tid == 0) { *scount = 0; *full = 0u; }
+    return;
+  }
+  // Rb = out[t0] + max_j D[t0][j] (INF if row t0 has an INF entry)
+  int32_t mx = 0;
+  const uint8_t* mr = m8 + ((int64_t)t0 - row0) * ld;
+  for (int64_t j = tid; j < n; j += blockDim.x) mx = max(mx, (int32_t)mr[j]);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0) sv[warp] = mx;
+  __syncthreads();
+  if (warp == 0) {
+    mx = __reduce_max_sync(0xffffffffu, sv[lane]);
+    if (lane == 0) sv[0] = mx;
+  }
+  __syncthreads();
+  mx = sv[0];
+  const int32_t rb = mx >= kSat8i ? I - 1 : omin + mx;   // INF in row t0: every finite out-edge
+  for (int64_t t = tid; t < n; t += blockDim.x)
+    if (ow[t] <= rb) slist[atomicAdd(&cnt, 1)] = (int)t;   // (at most n <= ld entries)
+  __syncthreads();
+  if (tid == 0) { *scount = cnt; *full = 0u; }
+}
+// row[j] = min over t in S of out[t] + D[t][j] (the mirror is exact: 0x7F = INF);
+// blockIdx.y splits S, atomicMin merges
+__global__ void __launch_bounds__(256) k_addrow(const int32_t* __restrict__ ow, const int* __restrict__ slist,
+                                                const int* __restrict__ scount, const unsigned* __restrict__ full,
+                                                const uint8_t* __restrict__ m8, int64_t ld, int64_t row0,
+                                                int64_t n, int32_t* row) {
+  if (*full) return;
+  const int cnt = *scount;
+  const int64_t j0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  if (j0 >= n) return;
+  const int s0 = (int)((int64_t)cnt * blockIdx.y / gridDim.y), s1 = (int)((int64_t)cnt * (blockIdx.y + 1) / gridDim.y);
+  const int32_t I = APSP_INF_I32_DEV;
+  int32_t acc[4] = {I, I, I, I};
+#pragma unroll 4
+  for (int s = s0; s < s1; ++s) {
+    const int t = slist[s];
+    const int32_t o = ow[t];
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(m8 + ((int64_t)t - row0) * ld + j0);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int32_t d = (int32_t)((w >> (8 * e)) & 0xFFu);
+      if (d != kSat8i) acc[e] = min(acc[e], o + d);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    if (j0 + e < n && acc[e] < I) atomicMin(row + j0 + e, acc[e]);
+}
+cudaError_t addrow_s(const int32_t* ow, int64_t n, const uint8_t* m8, int64_t ld, int64_t row0, int32_t* row,
+                     int64_t npad, int* slist, int* scount, unsigned* full, int limit, cudaStream_t st) {
+  k_addrow_setup<<<1, 1024, 0, st>>>(ow, n, m8, ld, row0, row, npad, slist, scount, full, limit);
+  CUDA_TRY(cudaGetLastError());
+  const dim3 grid((unsigned)cdiv(cdiv(n, 4), 256), 16);
+  k_addrow<<<grid, 256, 0, st>>>(ow, slist, scount, full, m8, ld, row0, n, row);
+  return cudaGetLastError();
 }
 
 template <typename T, int SR>
@@ -896,7 +1012,7 @@ template <typename T>
 cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow, const T* iw,
                           T* rowpart, T* rowpartM, T* colpart, int64_t part_ld, int* nchunk_out,
                           int* nslab_out, int max_slabs, int sr, Mirror M, const unsigned* uncertain,
-                          int packed, cudaStream_t st) {
+                          int packed, cudaStream_t st, int colp, const unsigned* full) {
   const bool p8 = packed && !sr && M.m8 != nullptr;   // int8 mirror: 512-column chunks
   Tiling tl = p8 ? make_tiling(n, r.hi - r.lo, max_slabs, 128, tune_wps("APSP_TUNE_P8_WPS", 144))
                  : make_tiling(n, r.hi - r.lo, max_slabs, P1_VEC, tune_wps("APSP_TUNE_P1_WPS", 16));
@@ -914,13 +1030,18 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
                                                 part_ld, M, uncertain);
   else if (p8) {   // on the mirror (exits unless it is valid)
     constexpr int smem = 8 * kP8S * kP8R * 32 * 16;
-    static bool attr = false;
-    if (!attr) {
-      CUDA_TRY(cudaFuncSetAttribute(k_addnode_pass1_p8<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr = true;
-    }
-    k_addnode_pass1_p8<T><<<grid, 256, smem, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
-                                                   part_ld, M);
+    static const cudaError_t a1 =
+        cudaFuncSetAttribute(k_addnode_pass1_p8<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    static const cudaError_t a0 =
+        cudaFuncSetAttribute(k_addnode_pass1_p8<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    CUDA_TRY(a1);
+    CUDA_TRY(a0);
+    if (colp)
+      k_addnode_pass1_p8<T, true><<<grid, 256, smem, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
+                                                           part_ld, M, full);
+    else
+      k_addnode_pass1_p8<T, false><<<grid, 256, smem, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
+                                                            part_ld, M, nullptr);
   }
   else if (packed)
     k_addnode_pass1_p16<T, 2><<<grid, 256, 0, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
@@ -944,7 +1065,7 @@ __global__ void __launch_bounds__(256) k_addnode_finish(const T* rowpart, const 
                                                         int64_t part_ld, Rows r, int64_t n,
                                                         int64_t npad, int64_t ntile_i, T* col,
                                                         T* ceff, T* row, int gate, Mirror M,
-                                                        unsigned* uncertain) {
+                                                        unsigned* uncertain, const unsigned* row_full) {
   if (gate == 1 && !pass1_packed_runs<T, 0>(M)) return;
   if (gate == 2 && pass1_packed_done<T, 0>(M, uncertain)) return;
   __shared__ T sm[8][32], sM[8][32];
@@ -982,6 +1103,8 @@ __global__ void __launch_bounds__(256) k_addnode_finish(const T* rowpart, const 
       ceff[i] = keep ? m : Tr<T>::inf();
     }
   } else {
+    // row_full == 0: the new row was already computed from the cheapest out-rows (k_addrow)
+    if (row_full && *(volatile const unsigned*)row_full == 0u) continue;
     const int64_t j = (tile - ntile_i) * 32 + lane;
     T m = Tr<T>::inf();
     if (j < n)
@@ -1000,12 +1123,13 @@ __global__ void __launch_bounds__(256) k_addnode_finish(const T* rowpart, const 
 template <typename T>
 cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
                            int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,
-                           T* ceff, T* row, int gate, Mirror M, unsigned* uncertain, cudaStream_t st) {
+                           T* ceff, T* row, int gate, Mirror M, unsigned* uncertain, cudaStream_t st,
+                           const unsigned* row_full) {
   const int64_t ti = cdiv(std::max<int64_t>(r.hi - r.lo, 0), 32), tj = cdiv(npad, 32);
   if (ti + tj == 0) return cudaSuccess;
   k_addnode_finish<T><<<(unsigned)std::min<int64_t>(ti + tj, 4 * num_sms()), 256, 0, st>>>(rowpart, rowpartM, nchunk, colpart, nslab,
                                                            part_ld, r, n, npad, ti, col, ceff, row,
-                                                           gate, M, uncertain);
+                                                           gate, M, uncertain, row_full);
   return cudaGetLastError();
 }
 
@@ -2158,10 +2282,10 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
   template cudaError_t copy_vec<T>(const T*, int64_t, int64_t, T, T*, cudaStream_t);               \
   template cudaError_t addnode_pass1<T>(const T*, int64_t, Rows, int64_t, const T*, const T*, T*,  \
                                         T*, T*, int64_t, int*, int*, int, int, Mirror,            \
-                                        const unsigned*, int, cudaStream_t);                      \
+                                        const unsigned*, int, cudaStream_t, int, const unsigned*);                      \
   template cudaError_t addnode_finish<T>(const T*, const T*, int, const T*, int, int64_t, Rows,    \
                                          int64_t, int64_t, T*, T*, T*, int, Mirror, unsigned*,    \
-                                         cudaStream_t);                                           \
+                                         cudaStream_t, const unsigned*);                                           \
   template cudaError_t rank1<T>(T*, int64_t, Rows, int64_t, const T*, const T*, const T*,          \
                                 const T*, unsigned long long*, int, Mirror, cudaStream_t, int);        \
   template cudaError_t addnode_write<T>(T*, int64_t, Rows, int64_t, int64_t, int, const T*,        \

@@ -410,11 +410,10 @@ __device__ __forceinline__ bool pass1_packed_runs(const Mirror& M) {
          (*(volatile unsigned*)M.flag & kMirrorOff) == 0u;
 }
 
-// The packed readers at either mirror width (EW bytes per value): a column
-// group (8 values) is one 16-byte (int16) or 8-byte (int8) load, widened to
-// four int16x2 words; int8 reads keep twice as many rows in flight.
-template <int EW> struct MW;
-template <> struct MW<2> {
+// The int16-mirror readers: a column group (8 values) is one 16-byte load,
+// four int16x2 words.  (The int8 mirror has readers of its own: k_detect_p8,
+// k_addnode_pass1_p8, k_rank1_p8.)
+struct MW16 {
   using E = uint16_t;
   using Raw = uint4;
   static constexpr int kRows = 4;
@@ -423,23 +422,14 @@ template <> struct MW<2> {
   __device__ static __forceinline__ Raw sat() { return make_uint4(0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu); }
   __device__ static __forceinline__ uint4 widen(Raw r) { return r; }
 };
-template <> struct MW<1> {
-  using E = uint8_t;
-  using Raw = uint2;
-  static constexpr int kRows = 8;
-  __device__ static __forceinline__ const E* base(const Mirror& M) { return M.m8; }
-  __device__ static __forceinline__ Raw load(const E* p) { return mload8b(p); }
-  __device__ static __forceinline__ Raw sat() { return make_uint2(0x7F7F7F7Fu, 0x7F7F7F7Fu); }
-  __device__ static __forceinline__ uint4 widen(Raw r) { return widen8(r); }
-};
 
-template <typename T, int EW>
+template <typename T>
 __global__ void __launch_bounds__(256, 2) k_addnode_pass1_p16(Rows r, int64_t ld, int64_t n, Tiling tl,
                                                               const T* __restrict__ ow,
                                                               const T* __restrict__ iw, T* rowpart,
                                                               T* rowpartM, T* colpart, int64_t part_ld,
                                                               Mirror M) {
-  if (!pass1_packed_runs<T, 0>(M) || MW<EW>::base(M) == nullptr) return;
+  if (!pass1_packed_runs<T, 0>(M) || M.m == nullptr) return;
   const bool has_inf = (*(volatile unsigned*)M.flag & kMirrorInf) != 0u;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
@@ -474,7 +464,7 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1_p16(Rows r, int64_t ld
   }
   // this lane's two 16-byte column groups of row i_lo; rows are ld apart
   const bool ok0 = qv[0] < tl.n4, ok1 = qv[2] < tl.n4;
-  using W = MW<EW>;
+  using W = MW16;
   constexpr int RB = W::kRows;
   const typename W::E* m0 = W::base(M) + (i_lo - r.row0) * ld + 4 * qv[0];
   const typename W::E* m1 = W::base(M) + (i_lo - r.row0) * ld + 4 * qv[2];
@@ -495,10 +485,6 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1_p16(Rows r, int64_t ld
       const uint32_t orep = (uint32_t)sat16((int32_t)owr[rr + h]) * 0x10001u;
       const uint4 u0 = W::widen(w[h][0]), u1 = W::widen(w[h][1]);
       uint32_t dw[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-      if (EW == 1 && has_inf) {   // int8 INF (0x7F) reads as the int16 INF (0x3FFF)
-#pragma unroll
-        for (int q = 0; q < 8; ++q) dw[q] = inf8to16(dw[q]);
-      }
       if (tail) {   // the row's last chunk: columns >= n hold no mirrored value
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -1044,7 +1030,7 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
                                                             part_ld, M, nullptr);
   }
   else if (packed)
-    k_addnode_pass1_p16<T, 2><<<grid, 256, 0, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
+    k_addnode_pass1_p16<T><<<grid, 256, 0, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
                                                     part_ld, M);
   else   // int32 (exits if the packed pass ran and came out certain)
     k_addnode_pass1<T, 0><<<grid, 256, 0, st>>>(D, ld, r, n, tl, ow, iw, rowpart, rowpartM, colpart,
@@ -1652,12 +1638,12 @@ __global__ void __launch_bounds__(256, 2) k_detect_stream(T* __restrict__ D, int
 // and 1, shortest path, int32 D).  A kernel of its own so that its smaller
 // register footprint gives 3 CTAs per SM: four rows of 16-byte loads in flight
 // per lane and 24 warps per SM keep the halved byte stream at HBM speed.
-template <typename T, bool TWO, int MODE, int EW>
+template <typename T, bool TWO, int MODE>
 __global__ void __launch_bounds__(256, 3) k_detect_p16(T* __restrict__ D, int64_t ld, Rows r, int64_t n,
                                                        int64_t skip, Tiling tl, const T* __restrict__ c1,
                                                        const T* __restrict__ r1, const T* __restrict__ c2,
                                                        const T* __restrict__ r2, float tau, DetectOut<T> o) {
-  if (!detect_uses_mirror<T, 0, MODE>(o.M) || MW<EW>::base(o.M) == nullptr) return;
+  if (!detect_uses_mirror<T, 0, MODE>(o.M) || o.M.m == nullptr) return;
   __shared__ DetectQueue sq[MODE == 1 ? 8 : 1];
   const int lane = threadIdx.x & 31;
   DetectQueue& Q = sq[MODE == 1 ? (threadIdx.x >> 5) : 0];
@@ -1698,7 +1684,7 @@ __global__ void __launch_bounds__(256, 3) k_detect_p16(T* __restrict__ D, int64_
     }
     // int8 mirror: INF reads as 0x7F, not 0x3FFF — no test changes: an INF
     // D[i][j] has c or r INF (D <= c + r), and then c + r - 1 >= 0x3FFE > 0x7F
-    using W = MW<EW>;
+    using W = MW16;
     constexpr int RB = W::kRows;
     const int rows = (int)max((int64_t)0, i_hi - i_lo);
     const bool ok0 = qv[0] < tl.n4, ok1 = qv[2] < tl.n4;
@@ -1993,7 +1979,7 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
       kp8<<<g8, 256, kD8Smem, st>>>(r, ld, n, skip, tl8, c1, r1, c2, r2, o);                     \
     }                                                                                            \
     else if (SR == 0 && MODE != 2 && M.m)                                                        \
-      k_detect_p16<T, TWO, (MODE == 2 ? 0 : MODE), 2><<<g, 256, 0, st>>>(D, ld, r, n, skip, tl,   \
+      k_detect_p16<T, TWO, (MODE == 2 ? 0 : MODE)><<<g, 256, 0, st>>>(D, ld, r, n, skip, tl,   \
                                                                           c1, r1, c2, r2, tau, o); \
     k_detect_stream<T, TWO, SR, MODE><<<gs, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, c2, r2, \
                                                           tau, o);                               \

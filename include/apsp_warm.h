@@ -183,9 +183,11 @@ apsp_status apsp_destroy(apsp_handle* h);
 apsp_status apsp_set_option(apsp_handle* h, apsp_option opt, double value);
 
 /* D was written by the caller (a warm start from a known APSP matrix):
- * re-derive the library's internal image of it (the int16 mirror the O(n^2)
- * passes read on int32 handles).  Optional — the first update
- * that needs it does it otherwise, inside that update's time.  Asynchronous.
+ * re-derive the library's internal image of it (the int8 / int16 mirror the
+ * O(n^2) passes read on int32 handles).  Optional — the first
+ * update that needs it does it otherwise, inside that update's time.
+ * Synchronises the stream once when it tries the int8 width (one 4-byte read
+ * of the validity flag), else asynchronous.
  * D must not be modified by the caller after an update call without calling
  * this (or apsp_cold_fw) again. */
 apsp_status apsp_sync_distances(apsp_handle* h);
@@ -303,7 +305,7 @@ typedef enum {
   APSP_K_SPARSE_R = 7,   /* sparse recompute, rounds >= 1             work: bytes       */
   APSP_K_QUERY = 8,      /* single-pair queries                       work: bytes       */
   APSP_K_OTHER = 9,      /* snapshots, tombstone, swap, small kernels work: bytes       */
-  APSP_K_EMIT = 10,      /* detection list emission (+ D0 reset)      work: bytes       */
+  APSP_K_EMIT = 10,      /* detection list: per-row slices, Phi        work: bytes       */
   APSP_K_COUNT = 11
 } apsp_kernel_class;
 

@@ -142,7 +142,7 @@ struct apsp_handle {
   int max_rounds = 64;
   int fw16 = 1;                  // int16x2 FW when exact (int32 shortest path, one GPU)
   int last_fw16 = 0;             // 1: the last FW ran packed, 2: it fell back to int32
-  bool mirror_built = false;     // the int16 mirror was built (or invalidated) from D
+  bool mirror_built = false;     // the mirror was built (or invalidated) from D
   bool mirror_hint = false;      // last observed mirror state was "valid" (profile accounting only)
   int mirror_level = 16;         // width of the mirror: 8 or 16 bits
   int mirror8 = 1;               // APSP_OPT_MIRROR8: try the int8 width at each build
@@ -795,7 +795,7 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   int nchunk = 0, nslab = 0;
   T* rowpartM = h->rowpart<T>() + (size_t)h->plan.maxchunk * ld;
   T* ceff = h->vec<T>(4);
-  // Pass 1: on the int16 mirror in packed arithmetic when it is valid
+  // Pass 1: on the int8 / int16 mirror in packed arithmetic when it is valid
   // (shortest path, int32), else — or if a new-row/column value came out
   // >= 0x3FFF — in int32.  The choice is made on the device: each launch
   // below exits when it does not apply (gate flags, stream order).
@@ -943,10 +943,10 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
     s = snap_pivots<T>(h, v, w_old, c2, u, r2);
     if (s != APSP_OK) return s;
   }
-  // W' (WT and the shortlists) before the D0 reset
+  // W' (WT and the shortlists) before the recompute reads them
   CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
   CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
-  {   // the detection pass reads the int16 mirror (early exits and decreases do not)
+  {   // the detection pass reads the mirror (early exits and decreases do not)
     apsp_status ms = ensure_mirror<T>(h);
     if (ms != APSP_OK) return ms;
   }

@@ -158,7 +158,7 @@ __device__ __forceinline__ Vec4<T> mask_tail(Vec4<T> v, int64_t col0, int64_t n)
 }
 
 // ---------------------------------------------------------------------------
-// int16 mirror of int32 D (kernels.h: struct Mirror)
+// saturated mirror of int32 D, int16 / int8 (kernels.h: struct Mirror)
 // ---------------------------------------------------------------------------
 constexpr int32_t kSat16i = 0x3FFF;
 __device__ __forceinline__ uint16_t sat16(int32_t v) { return (uint16_t)min(v, kSat16i); }

@@ -109,7 +109,8 @@ cudaError_t addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xl
                           const T* col, const T* row, T* WT, int64_t ldw, const T* ow,
                           const T* iw, Mirror M, cudaStream_t st);
 // mode 0: mark rows with flags (anyrow); 1: append the need_update_list
-// (prow/pcol/plb, rowcnt, ctr->total/overflow); 2: reset flagged entries in place
+// (pairs to prow/pcol, rowcnt, ctr->total/overflow; plb unused); 2: reset
+// flagged entries to W' in place
 template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
                    const T* c2, const T* r2, float tau, int mode, int* anyrow, int* rowcnt,
@@ -213,7 +214,7 @@ template <typename T>
 cudaError_t query_colslice(const T* D, int64_t ld, int64_t rows, int64_t R, int64_t n,
                            const int* t, int qc, T* out, cudaStream_t st);
 
-// int16 mirror upkeep (stream.cu): build from D (flag must be 0 before), re-sync
+// mirror upkeep (stream.cu): build from D (flag must be 0 before), re-sync
 // the listed pairs / one row and one column (-1: none) after D changed there
 cudaError_t mirror_build(const int32_t* D, int64_t ld, Rows r, int64_t n, Mirror M, cudaStream_t st);
 // int8 mirror from the packed int16 buffer (after a packed FW left sat16(D) there)

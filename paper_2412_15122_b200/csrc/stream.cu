@@ -271,7 +271,7 @@ static Tiling make_tiling(int64_t n, int64_t rows, int max_slabs, int chunk_vec 
 // col[i] + out[t*] + D[t*][j] < D[i][j] <= D[i][t*] + D[t*][j] for the t* that
 // attains row[j], i.e. col[i] < D[i][t*] - out[t*] <= M[i].
 // ---------------------------------------------------------------------------
-// int16 mirror upkeep (kernels.h: struct Mirror)
+// mirror upkeep, int8 or int16 (kernels.h: struct Mirror; mirror.cuh)
 // ---------------------------------------------------------------------------
 // (flag bits, mput, mirror_post: mirror.cuh)
 // M := sat16(D) over the local rows' first n columns; *flag must be 0 on entry
@@ -1997,8 +1997,6 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
   return cudaGetLastError();
 }
 
-// After a MODE-1 pass: per-row slices, Phi, max|A_i|, then the row grouping
-// of the staged list and the D0 reset.  `cur` (cap ints) must be zero.
 // D0[i][j] := W'[i][j] for every listed pair: only when the dense path runs
 // without the sparse kernels (forced); otherwise phase A rewrites every
 // listed entry itself (sparse.cu).
@@ -2059,13 +2057,7 @@ cudaError_t tombstone(T* D, int64_t ld, Rows r, int64_t n, int64_t k, T* WT, int
 }
 
 // ---------------------------------------------------------------------------
-// swap-with-last after a removal (Q7), two launches instead of nine:
-// node `last` moves into slot k of D (local rows r) and of WT (all rows).
-// Copy: row k := row last (if both local; else the row already arrived by a
-// point-to-point exchange), column k := column last for the other rows,
-// D[k][k] = WT[k][k] = 0.  Reads (row / column last) and writes (row / column
-// k) are disjoint, so one launch suffices.  Clear: row / column last := INF,
-// then the int16 mirror of row / column k is re-derived.
+// swap-with-last after a removal (Q7)
 // ---------------------------------------------------------------------------
 // Swap-with-last after a removal, one launch: node `last` moves into slot k
 // (row/column of D and WT, mirror of row/column k), then row/column `last`

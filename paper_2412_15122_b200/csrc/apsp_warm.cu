@@ -28,6 +28,7 @@ namespace {
 
 constexpr int64_t kTile = 128;       // FW pivot block / row-partition granule
 constexpr int kMaxSlabs = 256;       // add-node column partial slabs
+constexpr int kAddColLimit = 2048;   // columns the add-node gathers may read per row (else the stream)
 constexpr int64_t kVecs = 8;         // scratch vectors of ld elements
 constexpr int kQueryChunk = 32;      // sharded queries per column all-gather
 
@@ -249,6 +250,10 @@ struct apsp_handle {
   unsigned* pass1_uncertain() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 400); }
   unsigned* addrow_full() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 404); }
   int* addrow_count() { return reinterpret_cast<int*>(ws + plan.off_small + 408); }
+  int* addcol_ucount() { return reinterpret_cast<int*>(ws + plan.off_small + 412); }
+  int32_t* addcol_th2() { return reinterpret_cast<int32_t*>(ws + plan.off_small + 416); }
+  unsigned* addcol_full() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 420); }
+  int* addcol_fbcount() { return reinterpret_cast<int*>(ws + plan.off_small + 424); }
   // saturated mirror of D (kernels.h), int32 handles only: int8 (own buffer)
   // or int16 (in the packed-FW buffer), the width picked at the last build
   template <typename T> Mirror mirror() {
@@ -803,12 +808,23 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   unsigned* unc = h->pass1_uncertain();
   if (try_packed) {
     CKR(cudaMemsetAsync(unc, 0, sizeof(unsigned), h->st));
-    PK(APSP_K_ADD_PASS1, h->mirror_hint ? h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n : 0.0,
+    const unsigned* cfull = nullptr;
+    if constexpr (std::is_same<T, int32_t>::value) {
+      if (srow) {   // the new row first (side stream), then col / the skip bound by gathers
+        CKR(cudaStreamWaitEvent(h->st, h->ev_row, 0));
+        PK(APSP_K_ADD_PASS1, 0.0,
+           addcol_g(r, h->mirror<T>().m8, ld, n, iw, ow, row, reinterpret_cast<int*>(h->vec<T>(5)),
+                    h->addcol_ucount(), h->addcol_th2(), h->addcol_full(), kAddColLimit, col, ceff, h->vec<T>(6),
+                    reinterpret_cast<int*>(h->vec<T>(7)), h->addcol_fbcount(), h->st));
+        cfull = h->addcol_full();
+      }
+    }
+    // the streaming pass (gated off when the gathers did it)
+    PK(APSP_K_ADD_PASS1, h->mirror_hint && !srow ? h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n : 0.0,
        addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
-                        &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), unc, 1, h->st, srow ? 0 : 1));
-    if (srow) CKR(cudaStreamWaitEvent(h->st, h->ev_row, 0));   // the side stream's new row
+                        &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), unc, 1, h->st, srow ? 0 : 1, cfull));
     CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
-                         ceff, row, 1, h->mirror<T>(), unc, h->st, srow ? h->addrow_full() : nullptr));
+                         ceff, row, 1, h->mirror<T>(), unc, h->st, srow ? h->addrow_full() : nullptr, cfull));
   }
   PK(APSP_K_ADD_PASS1, try_packed && h->mirror_hint ? 0.0 : 4.0 * (double)(r.hi - r.lo) * (double)n,
      addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,

@@ -93,11 +93,18 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
 // *full = 1 when the shortcut does not apply (pass 1 must compute the row)
 cudaError_t addrow_s(const int32_t* ow, int64_t n, const uint8_t* m8, int64_t ld, int64_t row0, int32_t* row,
                      int64_t npad, int* slist, int* scount, unsigned* full, int limit, cudaStream_t st);
+// The new column and the row-skip bound of an add by gathers over the few
+// columns that matter (after addrow_s: needs the new row).  *ufull = 1: |U|
+// exceeded `limit`, pass 1 + the finish kernel must compute them instead.
+cudaError_t addcol_g(Rows r, const uint8_t* m8, int64_t ld, int64_t n, const int32_t* iw, const int32_t* ow,
+                     const int32_t* row, int* ulist, int* ucount, int32_t* th2, unsigned* ufull, int limit,
+                     int32_t* col, int32_t* ceff, int32_t* mprime, int* fb_list, int* fb_count, cudaStream_t st);
 template <typename T>
 cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
                            int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,
                            T* ceff, T* row, int gate, Mirror M, unsigned* uncertain,
-                           cudaStream_t st, const unsigned* row_full = nullptr);   // see addrow_s
+                           cudaStream_t st, const unsigned* row_full = nullptr,   // see addrow_s
+                           const unsigned* col_full = nullptr);                   // see addcol_g
 template <typename T>
 // twin = 0: the caller knows the int8 mirror is valid (its flag was read since
 // the last write that could change it), so only the int8 pass is launched

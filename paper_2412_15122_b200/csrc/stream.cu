@@ -594,145 +594,148 @@ __global__ void __launch_bounds__(256, P8_MINB) k_addnode_pass1_p8(Rows r, int64
   auto ring = reinterpret_cast<uint4 (*)[kP8S][kP8R][32]>(ring_raw);
   const bool has_inf = (*(volatile unsigned*)M.flag & kMirrorInf) != 0u;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
-  if (gw >= tl.warps) return;
-  const int chunk = (int)(gw % tl.nchunk);
-  const int slab = (int)(gw / tl.nchunk);
-  const int64_t i_lo = r.lo + slab * tl.slab;
-  // may be 0: the slab still writes its (all-SAT) new-row partials
-  const int rows = (int)max((int64_t)0, min(r.hi, i_lo + tl.slab) - i_lo);
-  constexpr uint32_t SAT2 = 0x3FFF3FFFu;
-  const int64_t g0 = (int64_t)chunk * 512 + 16 * lane;   // word q: columns g0 + 2q, g0 + 2q + 1
-  uint32_t in2[8], nout2[8], colp2[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    uint32_t a = 0, b = 0;
-#pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
-      const int64_t j = g0 + 2 * q + hf;
-      const uint32_t iv = j < n ? (uint32_t)sat16((int32_t)iw[j]) : 0x3FFFu;
-      const uint32_t ov = j < n ? (uint32_t)sat16((int32_t)ow[j]) : 0x3FFFu;
-      a |= iv << (16 * hf);
-      b |= ((0x10000u - ov) & 0xFFFFu) << (16 * hf);   // -out as int16
+  // grid-stride over the (chunk, slab) tasks (a launch gated off exits cheaply
+  // on a small grid; the normal launch has one task per warp)
+  for (int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; gw < tl.warps;
+       gw += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int chunk = (int)(gw % tl.nchunk);
+    const int slab = (int)(gw / tl.nchunk);
+    const int64_t i_lo = r.lo + slab * tl.slab;
+    // may be 0: the slab still writes its (all-SAT) new-row partials
+    const int rows = (int)max((int64_t)0, min(r.hi, i_lo + tl.slab) - i_lo);
+    constexpr uint32_t SAT2 = 0x3FFF3FFFu;
+    const int64_t g0 = (int64_t)chunk * 512 + 16 * lane;   // word q: columns g0 + 2q, g0 + 2q + 1
+    uint32_t in2[8], nout2[8], colp2[8];
+  #pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uint32_t a = 0, b = 0;
+  #pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        const int64_t j = g0 + 2 * q + hf;
+        const uint32_t iv = j < n ? (uint32_t)sat16((int32_t)iw[j]) : 0x3FFFu;
+        const uint32_t ov = j < n ? (uint32_t)sat16((int32_t)ow[j]) : 0x3FFFu;
+        a |= iv << (16 * hf);
+        b |= ((0x10000u - ov) & 0xFFFFu) << (16 * hf);   // -out as int16
+      }
+      in2[q] = a; nout2[q] = b; colp2[q] = SAT2;
     }
-    in2[q] = a; nout2[q] = b; colp2[q] = SAT2;
-  }
-  const bool tail = (int64_t)(chunk + 1) * 512 > n;   // this chunk holds columns >= n (replaced)
-  // a lane whose group starts beyond n copies the row's first group (in bounds)
-  const uint8_t* base = M.m8 + (i_lo - r.row0) * ld + (g0 < n ? g0 : 0);
-  T* rp_out = rowpart + (int64_t)chunk * part_ld + i_lo;
-  T* rm_out = rowpartM + (int64_t)chunk * part_ld + i_lo;
-  const int nst = (rows + kP8R - 1) / kP8R;
-  auto issue = [&](int s) {   // stage s -> ring slot s % kP8S (rows past the slab: its last row)
-    if (s < nst) {
-#pragma unroll
-      for (int h = 0; h < kP8R; ++h)
-        cp_async16(&ring[warp][s % kP8S][h][lane], base + (int64_t)min(s * kP8R + h, rows - 1) * ld);
-    }
-    cp_async_commit();   // (an empty group past the end keeps the wait count uniform)
-  };
-  auto out_of = [&](int row) -> uint32_t {   // out[i] of a row, replicated in both halves
-    return row < rows ? (uint32_t)sat16((int32_t)ow[i_lo + row]) * 0x10001u : SAT2;
-  };
-  // the common case (no INF entry, no column >= n in this chunk) has a loop
-  // of its own: the INF and tail fix-ups would otherwise hold registers
-  auto run = [&](auto special) {
-    constexpr bool SPECIAL = decltype(special)::value;
-#pragma unroll
-    for (int s = 0; s < kP8S - 1; ++s) issue(s);
-    uint32_t onext = COLP ? out_of(lane & (kP8G - 1)) : 0u;   // group 0's out[i], lane l < kP8G: row l
-    for (int g0r = 0; g0r < rows; g0r += kP8G) {
-      const uint32_t ocur = onext;
-      if (COLP) onext = out_of(g0r + kP8G + (lane & (kP8G - 1)));   // next group's, in flight meanwhile
-      uint32_t pw[kP8G / 2], mw[kP8G / 2];   // row results, two rows per word
-#pragma unroll
-      for (int sg = 0; sg < kP8G / kP8R; ++sg) {
-        const int s = g0r / kP8R + sg;
-        issue(s + kP8S - 1);
-        cp_async_wait<kP8S - 1>();   // this thread's copies of stage s have landed
-        uint32_t prow[kP8R], mrow[kP8R];
-#pragma unroll
-        for (int h = 0; h < kP8R; ++h) {
-          const uint32_t orep = COLP ? __shfl_sync(0xffffffffu, ocur, sg * kP8R + h) : 0u;
-          const uint4 wv = ring[warp][s % kP8S][h][lane];
-          const uint4 lo = widen8(make_uint2(wv.x, wv.y)), hi = widen8(make_uint2(wv.z, wv.w));
-          uint32_t dw[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-          if (SPECIAL && has_inf) {   // int8 INF (0x7F) reads as the int16 INF (0x3FFF)
-#pragma unroll
-            for (int q = 0; q < 8; ++q) dw[q] = inf8to16(dw[q]);
-          }
-          if (SPECIAL && tail) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const int64_t j0 = g0 + 2 * q;
-              const uint32_t pm = (j0 < n ? 0u : 0xFFFFu) | (j0 + 1 < n ? 0u : 0xFFFF0000u);
-              dw[q] = (dw[q] & ~pm) | (SAT2 & pm);
+    const bool tail = (int64_t)(chunk + 1) * 512 > n;   // this chunk holds columns >= n (replaced)
+    // a lane whose group starts beyond n copies the row's first group (in bounds)
+    const uint8_t* base = M.m8 + (i_lo - r.row0) * ld + (g0 < n ? g0 : 0);
+    T* rp_out = rowpart + (int64_t)chunk * part_ld + i_lo;
+    T* rm_out = rowpartM + (int64_t)chunk * part_ld + i_lo;
+    const int nst = (rows + kP8R - 1) / kP8R;
+    auto issue = [&](int s) {   // stage s -> ring slot s % kP8S (rows past the slab: its last row)
+      if (s < nst) {
+  #pragma unroll
+        for (int h = 0; h < kP8R; ++h)
+          cp_async16(&ring[warp][s % kP8S][h][lane], base + (int64_t)min(s * kP8R + h, rows - 1) * ld);
+      }
+      cp_async_commit();   // (an empty group past the end keeps the wait count uniform)
+    };
+    auto out_of = [&](int row) -> uint32_t {   // out[i] of a row, replicated in both halves
+      return row < rows ? (uint32_t)sat16((int32_t)ow[i_lo + row]) * 0x10001u : SAT2;
+    };
+    // the common case (no INF entry, no column >= n in this chunk) has a loop
+    // of its own: the INF and tail fix-ups would otherwise hold registers
+    auto run = [&](auto special) {
+      constexpr bool SPECIAL = decltype(special)::value;
+  #pragma unroll
+      for (int s = 0; s < kP8S - 1; ++s) issue(s);
+      uint32_t onext = COLP ? out_of(lane & (kP8G - 1)) : 0u;   // group 0's out[i], lane l < kP8G: row l
+      for (int g0r = 0; g0r < rows; g0r += kP8G) {
+        const uint32_t ocur = onext;
+        if (COLP) onext = out_of(g0r + kP8G + (lane & (kP8G - 1)));   // next group's, in flight meanwhile
+        uint32_t pw[kP8G / 2], mw[kP8G / 2];   // row results, two rows per word
+  #pragma unroll
+        for (int sg = 0; sg < kP8G / kP8R; ++sg) {
+          const int s = g0r / kP8R + sg;
+          issue(s + kP8S - 1);
+          cp_async_wait<kP8S - 1>();   // this thread's copies of stage s have landed
+          uint32_t prow[kP8R], mrow[kP8R];
+  #pragma unroll
+          for (int h = 0; h < kP8R; ++h) {
+            const uint32_t orep = COLP ? __shfl_sync(0xffffffffu, ocur, sg * kP8R + h) : 0u;
+            const uint4 wv = ring[warp][s % kP8S][h][lane];
+            const uint4 lo = widen8(make_uint2(wv.x, wv.y)), hi = widen8(make_uint2(wv.z, wv.w));
+            uint32_t dw[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+            if (SPECIAL && has_inf) {   // int8 INF (0x7F) reads as the int16 INF (0x3FFF)
+  #pragma unroll
+              for (int q = 0; q < 8; ++q) dw[q] = inf8to16(dw[q]);
+            }
+            if (SPECIAL && tail) {
+  #pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const int64_t j0 = g0 + 2 * q;
+                const uint32_t pm = (j0 < n ? 0u : 0xFFFFu) | (j0 + 1 < n ? 0u : 0xFFFF0000u);
+                dw[q] = (dw[q] & ~pm) | (SAT2 & pm);
+              }
+            }
+            uint32_t pa = SAT2, pb = SAT2, ma = 0xC001C001u /* -16383 */, mb = 0xC001C001u;
+  #pragma unroll
+            for (int q = 0; q < 8; q += 2) {
+              pa = __viaddmin_s16x2(dw[q], in2[q], pa);
+              pb = __viaddmin_s16x2(dw[q + 1], in2[q + 1], pb);
+              ma = __viaddmax_s16x2(dw[q], nout2[q], ma);
+              mb = __viaddmax_s16x2(dw[q + 1], nout2[q + 1], mb);
+              if (COLP) {
+                colp2[q] = __viaddmin_s16x2(orep, dw[q], colp2[q]);
+                colp2[q + 1] = __viaddmin_s16x2(orep, dw[q + 1], colp2[q + 1]);
+              }
+            }
+            prow[h] = __vmins2(pa, pb);
+            mrow[h] = __vmaxs2(ma, mb);
+            if (SPECIAL && has_inf) {   // D == INF with a finite out: no row skip (k_addnode_pass1_p16)
+              uint32_t inf = 0;
+  #pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const uint32_t satnf = ((nout2[q] & 0xFFFFu) == 0xC001u ? 0x3FFFu : 0x3FFEu) |
+                                       ((nout2[q] >> 16) == 0xC001u ? 0x3FFF0000u : 0x3FFE0000u);
+                inf |= __vmins2(dw[q], satnf) ^ dw[q];
+              }
+              if (inf) mrow[h] = 0x7FFF7FFFu;   // 0x7FFF: "no skip" (written back as INF)
             }
           }
-          uint32_t pa = SAT2, pb = SAT2, ma = 0xC001C001u /* -16383 */, mb = 0xC001C001u;
-#pragma unroll
-          for (int q = 0; q < 8; q += 2) {
-            pa = __viaddmin_s16x2(dw[q], in2[q], pa);
-            pb = __viaddmin_s16x2(dw[q + 1], in2[q + 1], pb);
-            ma = __viaddmax_s16x2(dw[q], nout2[q], ma);
-            mb = __viaddmax_s16x2(dw[q + 1], nout2[q + 1], mb);
-            if (COLP) {
-              colp2[q] = __viaddmin_s16x2(orep, dw[q], colp2[q]);
-              colp2[q + 1] = __viaddmin_s16x2(orep, dw[q + 1], colp2[q + 1]);
-            }
-          }
-          prow[h] = __vmins2(pa, pb);
-          mrow[h] = __vmaxs2(ma, mb);
-          if (SPECIAL && has_inf) {   // D == INF with a finite out: no row skip (k_addnode_pass1_p16)
-            uint32_t inf = 0;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const uint32_t satnf = ((nout2[q] & 0xFFFFu) == 0xC001u ? 0x3FFFu : 0x3FFEu) |
-                                     ((nout2[q] >> 16) == 0xC001u ? 0x3FFF0000u : 0x3FFE0000u);
-              inf |= __vmins2(dw[q], satnf) ^ dw[q];
-            }
-            if (inf) mrow[h] = 0x7FFF7FFFu;   // 0x7FFF: "no skip" (written back as INF)
+          // fold each row's two halves and pair rows: word = (row 2k, row 2k + 1)
+  #pragma unroll
+          for (int h = 0; h < kP8R; h += 2) {
+            const uint32_t pl = __byte_perm(prow[h], prow[h + 1], 0x5410);
+            const uint32_t ph = __byte_perm(prow[h], prow[h + 1], 0x7632);
+            const uint32_t ml = __byte_perm(mrow[h], mrow[h + 1], 0x5410);
+            const uint32_t mh = __byte_perm(mrow[h], mrow[h + 1], 0x7632);
+            pw[(sg * kP8R + h) / 2] = __vmins2(pl, ph);
+            mw[(sg * kP8R + h) / 2] = __vmaxs2(ml, mh);
           }
         }
-        // fold each row's two halves and pair rows: word = (row 2k, row 2k + 1)
-#pragma unroll
-        for (int h = 0; h < kP8R; h += 2) {
-          const uint32_t pl = __byte_perm(prow[h], prow[h + 1], 0x5410);
-          const uint32_t ph = __byte_perm(prow[h], prow[h + 1], 0x7632);
-          const uint32_t ml = __byte_perm(mrow[h], mrow[h + 1], 0x5410);
-          const uint32_t mh = __byte_perm(mrow[h], mrow[h + 1], 0x7632);
-          pw[(sg * kP8R + h) / 2] = __vmins2(pl, ph);
-          mw[(sg * kP8R + h) / 2] = __vmaxs2(ml, mh);
+        // rows g0r + 2 wi, g0r + 2 wi + 1 (wi = 4 b4 + 2 b3 + b2) reduced over the warp
+        const uint32_t pr = p8_reduce_scatter<false>(pw, lane);
+        const uint32_t mr = p8_reduce_scatter<true>(mw, lane);
+        if ((lane & 3) == 0) {
+          const int wi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+          const int ra = g0r + 2 * wi;
+  #pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            if (ra + e < rows) {
+              const int mv = (int)(short)(mr >> (16 * e));
+              rp_out[ra + e] = (T)((pr >> (16 * e)) & 0xFFFFu);
+              rm_out[ra + e] = mv == 0x7FFF ? Tr<T>::inf() : (T)mv;
+            }
+          }
         }
       }
-      // rows g0r + 2 wi, g0r + 2 wi + 1 (wi = 4 b4 + 2 b3 + b2) reduced over the warp
-      const uint32_t pr = p8_reduce_scatter<false>(pw, lane);
-      const uint32_t mr = p8_reduce_scatter<true>(mw, lane);
-      if ((lane & 3) == 0) {
-        const int wi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-        const int ra = g0r + 2 * wi;
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          if (ra + e < rows) {
-            const int mv = (int)(short)(mr >> (16 * e));
-            rp_out[ra + e] = (T)((pr >> (16 * e)) & 0xFFFFu);
-            rm_out[ra + e] = mv == 0x7FFF ? Tr<T>::inf() : (T)mv;
-          }
-        }
+    };
+    if (has_inf || tail) run(std::true_type{});
+    else run(std::false_type{});
+    cp_async_wait<0>();
+    if (!COLP) continue;
+  #pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t j0 = g0 + 2 * q;
+      if (j0 < n) {
+        T* dst = colpart + (int64_t)slab * part_ld + j0;
+        dst[0] = (T)(colp2[q] & 0xFFFFu);
+        if (j0 + 1 < n) dst[1] = (T)(colp2[q] >> 16);
       }
-    }
-  };
-  if (has_inf || tail) run(std::true_type{});
-  else run(std::false_type{});
-  cp_async_wait<0>();
-  if (!COLP) return;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int64_t j0 = g0 + 2 * q;
-    if (j0 < n) {
-      T* dst = colpart + (int64_t)slab * part_ld + j0;
-      dst[0] = (T)(colp2[q] & 0xFFFFu);
-      if (j0 + 1 < n) dst[1] = (T)(colp2[q] >> 16);
     }
   }
 }
@@ -838,6 +841,154 @@ __global__ void __launch_bounds__(256) k_addrow(const int32_t* __restrict__ ow, 
   for (int e = 0; e < 4; ++e)
     if (j0 + e < n && acc[e] < I) atomicMin(row + j0 + e, acc[e]);
 }
+// ---------------------------------------------------------------------------
+// The new column and the row-skip bound of an add by gathers instead of a
+// pass over the mirror (int8 mirror valid, one GPU).
+//   col[i] = min_t D[i][t] + in[t]: over S1 = {t : in[t] <= th} it is an upper
+//     bound col1[i]; if col1[i] <= th2 (the smallest in[t] above th), no t
+//     outside S1 can do better (D >= 0): exact.  Rows not certified get a
+//     full-row scan (k_addcol_rows).  th = min in + 3.
+//   M'[i] = max_{t in S2} D[i][t] - out[t], S2 = {t : out[t] <= R}, R = max_j
+//     row[j] (the new row, computed first): a change at (i, j) needs col[i] <
+//     D[i][t*] - out[t*] for the t* attaining row[j], and out[t*] <= row[j]
+//     <= R — so rows with col[i] >= M'[i] do not change.
+// Both sets are gathered together: U = S1 u S2 (an extra candidate never
+// breaks either bound).  If |U| > limit, *ufull is set and the streaming
+// pass 1 does it instead.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_addcol_sets(const int32_t* __restrict__ iw,
+                                                      const int32_t* __restrict__ ow,
+                                                      const int32_t* __restrict__ row, int64_t n, int delta,
+                                                      int* ulist, int* ucount, int32_t* th2_out, unsigned* ufull,
+                                                      int limit) {
+  __shared__ int32_t red[32];
+  __shared__ int cnt;
+  __shared__ int32_t th2s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int32_t I = APSP_INF_I32_DEV;
+  auto block_red = [&](int32_t v, bool mx) -> int32_t {
+    v = mx ? __reduce_max_sync(0xffffffffu, v) : __reduce_min_sync(0xffffffffu, v);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    int32_t w = red[lane];
+    w = mx ? __reduce_max_sync(0xffffffffu, w) : __reduce_min_sync(0xffffffffu, w);
+    __syncthreads();
+    return w;
+  };
+  int32_t mn = I, mx = 0;
+  for (int64_t t = tid; t < n; t += blockDim.x) {
+    mn = min(mn, iw[t]);
+    if (row[t] < I) mx = max(mx, row[t]);
+  }
+  const int32_t in_min = block_red(mn, false);
+  const int32_t R = block_red(mx, true);   // max finite entry of the new row
+  const int32_t th = in_min >= I ? I : min(I - 1, in_min + delta);
+  if (tid == 0) { cnt = 0; th2s = I; }
+  __syncthreads();
+  int32_t t2 = I;
+  for (int64_t t = tid; t < n; t += blockDim.x) {
+    const int32_t a = iw[t], b = ow[t];
+    if (a > th && a < t2) t2 = a;
+    if (a <= th || b <= R) {
+      const int q = atomicAdd(&cnt, 1);
+      if (q < limit) ulist[q] = (int)t;
+    }
+  }
+  t2 = __reduce_min_sync(0xffffffffu, t2);
+  if (lane == 0) atomicMin(&th2s, t2);
+  __syncthreads();
+  if (tid == 0) {
+    *ucount = min(cnt, limit);
+    *th2_out = th2s;
+    *ufull = cnt > limit ? 1u : 0u;
+  }
+}
+// one warp per row: col1 / M' over U; certified rows get col and ceff, the
+// others are listed for k_addcol_rows (M' kept in mprime)
+__global__ void __launch_bounds__(256) k_addcol_gather(Rows r, const uint8_t* __restrict__ m8, int64_t ld,
+                                                       const int* __restrict__ ulist, const int* __restrict__ ucount,
+                                                       const unsigned* __restrict__ ufull,
+                                                       const int32_t* __restrict__ iw, const int32_t* __restrict__ ow,
+                                                       const int32_t* __restrict__ th2p, int32_t* col, int32_t* ceff,
+                                                       int32_t* mprime, int* fb_list, int* fb_count) {
+  if (*ufull) return;
+  const int lane = threadIdx.x & 31;
+  const int cnt = *ucount;
+  const int32_t th2 = *th2p, I = APSP_INF_I32_DEV;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = r.lo + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < r.hi; i += nw) {
+    const uint8_t* mrow = m8 + (i - r.row0) * ld;
+    int32_t p = I, m = INT_MIN;
+#pragma unroll 4
+    for (int k = lane; k < cnt; k += 32) {
+      const int t = ulist[k];
+      const int32_t d8 = mrow[t];
+      const int32_t a = iw[t], b = ow[t];
+      if (d8 != kSat8i) {
+        if (a < I) p = min(p, d8 + a);
+        if (b < I) m = max(m, d8 - b);
+      } else if (b < I) {
+        m = I;   // an INF entry with a finite out: never skip (as in pass 1)
+      }
+    }
+    p = __reduce_min_sync(0xffffffffu, p);
+    m = __reduce_max_sync(0xffffffffu, m);
+    if (lane == 0) {
+      if (p <= th2) {
+        col[i] = p;
+        ceff[i] = p < m ? p : I;
+      } else {
+        mprime[i] = m;
+        fb_list[atomicAdd(fb_count, 1)] = (int)i;
+      }
+    }
+  }
+}
+// the rows col1 could not certify: a full-row min over the mirror (block per row)
+__global__ void __launch_bounds__(256) k_addcol_rows(Rows r, const uint8_t* __restrict__ m8, int64_t ld, int64_t n,
+                                                     const int32_t* __restrict__ iw, const unsigned* __restrict__ ufull,
+                                                     const int* __restrict__ fb_list, const int* __restrict__ fb_count,
+                                                     const int32_t* __restrict__ mprime, int32_t* col, int32_t* ceff) {
+  if (*ufull) return;
+  __shared__ int32_t red[8];
+  const int cnt = *fb_count;
+  const int32_t I = APSP_INF_I32_DEV;
+  for (int f = blockIdx.x; f < cnt; f += gridDim.x) {
+    const int64_t i = fb_list[f];
+    const uint8_t* mrow = m8 + (i - r.row0) * ld;
+    int32_t p = I;
+    for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
+      const int32_t d8 = mrow[t], a = iw[t];
+      if (d8 != kSat8i && a < I) p = min(p, d8 + a);
+    }
+    p = __reduce_min_sync(0xffffffffu, p);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < 8; ++w) p = min(p, red[w]);
+      p = min(p, red[0]);
+      col[i] = p;
+      ceff[i] = p < mprime[i] ? p : I;
+    }
+    __syncthreads();
+  }
+}
+cudaError_t addcol_g(Rows r, const uint8_t* m8, int64_t ld, int64_t n, const int32_t* iw, const int32_t* ow,
+                     const int32_t* row, int* ulist, int* ucount, int32_t* th2, unsigned* ufull, int limit,
+                     int32_t* col, int32_t* ceff, int32_t* mprime, int* fb_list, int* fb_count, cudaStream_t st) {
+  CUDA_TRY(cudaMemsetAsync(fb_count, 0, sizeof(int), st));
+  k_addcol_sets<<<1, 1024, 0, st>>>(iw, ow, row, n, 3, ulist, ucount, th2, ufull, limit);
+  CUDA_TRY(cudaGetLastError());
+  if (r.hi > r.lo) {
+    const int grid = (int)std::min<int64_t>(cdiv(r.hi - r.lo, 8), (int64_t)num_sms() * 16);
+    k_addcol_gather<<<grid, 256, 0, st>>>(r, m8, ld, ulist, ucount, ufull, iw, ow, th2, col, ceff, mprime,
+                                          fb_list, fb_count);
+    CUDA_TRY(cudaGetLastError());
+    k_addcol_rows<<<num_sms(), 256, 0, st>>>(r, m8, ld, n, iw, ufull, fb_list, fb_count, mprime, col, ceff);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t addrow_s(const int32_t* ow, int64_t n, const uint8_t* m8, int64_t ld, int64_t row0, int32_t* row,
                      int64_t npad, int* slist, int* scount, unsigned* full, int limit, cudaStream_t st) {
   k_addrow_setup<<<1, 1024, 0, st>>>(ow, n, m8, ld, row0, row, npad, slist, scount, full, limit);
@@ -1022,12 +1173,15 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
         cudaFuncSetAttribute(k_addnode_pass1_p8<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     CUDA_TRY(a1);
     CUDA_TRY(a0);
+    // a launch gated on `full` usually exits: a persistent-size grid (the
+    // kernel strides over the tasks)
+    const int g = full ? std::min(grid, 2 * num_sms()) : grid;
     if (colp)
-      k_addnode_pass1_p8<T, true><<<grid, 256, smem, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
-                                                           part_ld, M, full);
+      k_addnode_pass1_p8<T, true><<<g, 256, smem, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
+                                                        part_ld, M, full);
     else
-      k_addnode_pass1_p8<T, false><<<grid, 256, smem, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
-                                                            part_ld, M, nullptr);
+      k_addnode_pass1_p8<T, false><<<g, 256, smem, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
+                                                         part_ld, M, full);
   }
   else if (packed)
     k_addnode_pass1_p16<T><<<grid, 256, 0, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
@@ -1051,7 +1205,8 @@ __global__ void __launch_bounds__(256) k_addnode_finish(const T* rowpart, const 
                                                         int64_t part_ld, Rows r, int64_t n,
                                                         int64_t npad, int64_t ntile_i, T* col,
                                                         T* ceff, T* row, int gate, Mirror M,
-                                                        unsigned* uncertain, const unsigned* row_full) {
+                                                        unsigned* uncertain, const unsigned* row_full,
+                                                        const unsigned* col_full) {
   if (gate == 1 && !pass1_packed_runs<T, 0>(M)) return;
   if (gate == 2 && pass1_packed_done<T, 0>(M, uncertain)) return;
   __shared__ T sm[8][32], sM[8][32];
@@ -1060,6 +1215,8 @@ __global__ void __launch_bounds__(256) k_addnode_finish(const T* rowpart, const 
   for (int64_t tile = blockIdx.x; tile < ntile_i + (npad + 31) / 32; tile += gridDim.x) {
   __syncthreads();   // sm / sM reuse across tiles
   if (tile < ntile_i) {
+    // col_full == 0: the new column was gathered (k_addcol_gather)
+    if (col_full && *(volatile const unsigned*)col_full == 0u) continue;
     const int64_t i = r.lo + tile * 32 + lane;
     T m = Tr<T>::inf();
     T M = -Tr<T>::inf();
@@ -1110,12 +1267,12 @@ template <typename T>
 cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
                            int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,
                            T* ceff, T* row, int gate, Mirror M, unsigned* uncertain, cudaStream_t st,
-                           const unsigned* row_full) {
+                           const unsigned* row_full, const unsigned* col_full) {
   const int64_t ti = cdiv(std::max<int64_t>(r.hi - r.lo, 0), 32), tj = cdiv(npad, 32);
   if (ti + tj == 0) return cudaSuccess;
   k_addnode_finish<T><<<(unsigned)std::min<int64_t>(ti + tj, 4 * num_sms()), 256, 0, st>>>(rowpart, rowpartM, nchunk, colpart, nslab,
                                                            part_ld, r, n, npad, ti, col, ceff, row,
-                                                           gate, M, uncertain, row_full);
+                                                           gate, M, uncertain, row_full, col_full);
   return cudaGetLastError();
 }
 
@@ -2263,7 +2420,7 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
                                         const unsigned*, int, cudaStream_t, int, const unsigned*);                      \
   template cudaError_t addnode_finish<T>(const T*, const T*, int, const T*, int, int64_t, Rows,    \
                                          int64_t, int64_t, T*, T*, T*, int, Mirror, unsigned*,    \
-                                         cudaStream_t, const unsigned*);                                           \
+                                         cudaStream_t, const unsigned*, const unsigned*);                                           \
   template cudaError_t rank1<T>(T*, int64_t, Rows, int64_t, const T*, const T*, const T*,          \
                                 const T*, unsigned long long*, int, Mirror, cudaStream_t, int);        \
   template cudaError_t addnode_write<T>(T*, int64_t, Rows, int64_t, int64_t, int, const T*,        \

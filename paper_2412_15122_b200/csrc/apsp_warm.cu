@@ -248,12 +248,15 @@ struct apsp_handle {
   unsigned* fw16_flag() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 392); }
   unsigned* mirror_flag() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 396); }
   unsigned* pass1_uncertain() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 400); }
-  unsigned* addrow_full() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 404); }
-  int* addrow_count() { return reinterpret_cast<int*>(ws + plan.off_small + 408); }
-  int* addcol_ucount() { return reinterpret_cast<int*>(ws + plan.off_small + 412); }
-  int32_t* addcol_th2() { return reinterpret_cast<int32_t*>(ws + plan.off_small + 416); }
-  unsigned* addcol_full() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 420); }
-  int* addcol_fbcount() { return reinterpret_cast<int*>(ws + plan.off_small + 424); }
+  // the add-node shortcuts' scratch words (small + 404 ... 463)
+  AddScratch add_scratch() {
+    unsigned char* b = ws + plan.off_small;
+    return AddScratch{reinterpret_cast<unsigned long long*>(b + 448), reinterpret_cast<unsigned*>(b + 404),
+                      reinterpret_cast<int*>(b + 408), reinterpret_cast<int*>(b + 412),
+                      reinterpret_cast<int*>(b + 416), reinterpret_cast<int*>(b + 420),
+                      reinterpret_cast<int*>(b + 424), reinterpret_cast<int*>(b + 428),
+                      reinterpret_cast<unsigned*>(b + 432), reinterpret_cast<unsigned*>(b + 436)};
+  }
   // saturated mirror of D (kernels.h), int32 handles only: int8 (own buffer)
   // or int16 (in the packed-FW buffer), the width picked at the last build
   template <typename T> Mirror mirror() {
@@ -761,11 +764,13 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   T* iw = h->vec<T>(1);
   T* col = h->vec<T>(2);
   T* row = h->vec<T>(3);
-  CKR(cudaMemsetAsync(&h->ctr()->err, 0, sizeof(unsigned), h->st));
-  CKR(cudaMemsetAsync(h->wmin_dev(), 0xff, sizeof(unsigned), h->st));
+  const AddScratch as = h->add_scratch();
+  CK(add_init(as, &h->ctr()->err, h->wmin_dev(), h->st));
   CK(validate_vec<T>(reinterpret_cast<const T*>(out_w), nullptr, n, ld, ow, &h->ctr()->err, h->wmin_dev(),
                      h->st, reinterpret_cast<const T*>(in_w),
-                     h->directed ? nullptr : reinterpret_cast<const T*>(out_w), iw));   // both vectors, one launch
+                     h->directed ? nullptr : reinterpret_cast<const T*>(out_w), iw,   // both vectors, one launch
+                     std::is_same<T, int32_t>::value ? as.argmin_out : nullptr,
+                     std::is_same<T, int32_t>::value ? as.in_min : nullptr));
   unsigned* herr = reinterpret_cast<unsigned*>(h->host_small);
   CKR(cudaMemcpyAsync(herr, &h->ctr()->err, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
   CKR(cudaMemcpyAsync(herr + 1, h->wmin_dev(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
@@ -787,8 +792,8 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   if constexpr (std::is_same<T, int32_t>::value) srow = h->world == 1 && mirror8_known_valid(h);
   if constexpr (std::is_same<T, int32_t>::value) {
     if (srow) {
-      CK2(addrow_s(ow, n, h->mirror<T>().m8, ld, h->row0, row, ld, reinterpret_cast<int*>(h->vec<T>(5)),
-                   h->addrow_count(), h->addrow_full(), (int)ld, h->st2));
+      CK2(addrow_s(as, ow, n, h->mirror<T>().m8, ld, h->row0, row, ld, reinterpret_cast<int*>(h->vec<T>(5)),
+                   h->st2));
       CKR(cudaEventRecord(h->ev_row, h->st2));
     }
   }
@@ -813,10 +818,9 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
       if (srow) {   // the new row first (side stream), then col / the skip bound by gathers
         CKR(cudaStreamWaitEvent(h->st, h->ev_row, 0));
         PK(APSP_K_ADD_PASS1, 0.0,
-           addcol_g(r, h->mirror<T>().m8, ld, n, iw, ow, row, reinterpret_cast<int*>(h->vec<T>(5)),
-                    h->addcol_ucount(), h->addcol_th2(), h->addcol_full(), kAddColLimit, col, ceff, h->vec<T>(6),
-                    reinterpret_cast<int*>(h->vec<T>(7)), h->addcol_fbcount(), h->st));
-        cfull = h->addcol_full();
+           addcol_g(as, r, h->mirror<T>().m8, ld, n, iw, ow, reinterpret_cast<int*>(h->vec<T>(5)), kAddColLimit,
+                    col, ceff, h->vec<T>(6), reinterpret_cast<int*>(h->vec<T>(7)), h->st));
+        cfull = as.ufull;
       }
     }
     // the streaming pass (gated off when the gathers did it)
@@ -824,7 +828,7 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
        addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
                         &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), unc, 1, h->st, srow ? 0 : 1, cfull));
     CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
-                         ceff, row, 1, h->mirror<T>(), unc, h->st, srow ? h->addrow_full() : nullptr, cfull));
+                         ceff, row, 1, h->mirror<T>(), unc, h->st, srow ? as.rfull : nullptr, cfull));
   }
   PK(APSP_K_ADD_PASS1, try_packed && h->mirror_hint ? 0.0 : 4.0 * (double)(r.hi - r.lo) * (double)n,
      addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,

@@ -68,7 +68,8 @@ template <typename T>
 // (inb, in2b, outb): an optional second vector validated in the same launch
 cudaError_t validate_vec(const T* in, const T* in2, int64_t n, int64_t npad, T* out,
                          unsigned int* err, unsigned* wmin_bits, cudaStream_t st, const T* inb = nullptr,
-                         const T* in2b = nullptr, T* outb = nullptr);
+                         const T* in2b = nullptr, T* outb = nullptr, unsigned long long* argmin0 = nullptr,
+                         unsigned* min1 = nullptr);
 template <typename T>
 cudaError_t transpose_in(const T* W, int64_t ldw, int64_t n, T* WT, int64_t ldt, unsigned int* err,
                          unsigned* wmin_bits, cudaStream_t st);
@@ -89,16 +90,19 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
                           T* rowpart, T* rowpartM, T* colpart, int64_t part_ld, int* nchunk_out,
                           int* nslab_out, int max_slabs, int sr, Mirror M, const unsigned* uncertain, int packed,
                           cudaStream_t st, int colp = 1, const unsigned* full = nullptr);
-// The new row of an add from the rows S = {t : out[t] <= Rb} (int8 mirror, one GPU):
-// *full = 1 when the shortcut does not apply (pass 1 must compute the row)
-cudaError_t addrow_s(const int32_t* ow, int64_t n, const uint8_t* m8, int64_t ld, int64_t row0, int32_t* row,
-                     int64_t npad, int* slist, int* scount, unsigned* full, int limit, cudaStream_t st);
-// The new column and the row-skip bound of an add by gathers over the few
-// columns that matter (after addrow_s: needs the new row).  *ufull = 1: |U|
-// exceeded `limit`, pass 1 + the finish kernel must compute them instead.
-cudaError_t addcol_g(Rows r, const uint8_t* m8, int64_t ld, int64_t n, const int32_t* iw, const int32_t* ow,
-                     const int32_t* row, int* ulist, int* ucount, int32_t* th2, unsigned* ufull, int limit,
-                     int32_t* col, int32_t* ceff, int32_t* mprime, int* fb_list, int* fb_count, cudaStream_t st);
+// Add-node shortcuts (int8 mirror, one GPU): scratch words, the new row from
+// the rows that can attain it, then the new column / skip bound by gathers
+struct AddScratch {
+  unsigned long long* argmin_out; unsigned* in_min; int* s_count; int* u_count; int* th2; int* fb_count;
+  int* rmax; int* rb; unsigned* ufull; unsigned* rfull;
+};
+cudaError_t add_init(const AddScratch& a, unsigned* err, unsigned* wmin, cudaStream_t st);
+cudaError_t addrow_s(const AddScratch& a, const int32_t* ow, int64_t n, const uint8_t* m8, int64_t ld, int64_t row0,
+                     int32_t* row, int64_t npad, int* slist, cudaStream_t st);
+// *a.ufull = 1 when |U| exceeded `limit`: pass 1 + the finish kernel compute col instead
+cudaError_t addcol_g(const AddScratch& a, Rows r, const uint8_t* m8, int64_t ld, int64_t n, const int32_t* iw,
+                     const int32_t* ow, int* ulist, int limit, int32_t* col, int32_t* ceff, int32_t* mprime,
+                     int* fb_list, cudaStream_t st);
 template <typename T>
 cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
                            int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,

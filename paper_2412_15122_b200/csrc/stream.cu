@@ -69,8 +69,12 @@ __device__ __forceinline__ void wmin_fold(unsigned* wmin_bits, T v, bool valid) 
 template <typename T>
 __global__ void k_validate_vec(const T* in, const T* in2, int64_t n, int64_t npad, T* out,
                                unsigned int* err, unsigned* wmin_bits, const T* inb, const T* in2b,
-                               T* outb) {
+                               T* outb, unsigned long long* argmin0, unsigned* min1) {
   if (blockIdx.y == 1) { in = inb; in2 = in2b; out = outb; }   // the second vector of a pair
+  // (argmin0: (value << 32 | index) of the first vector's minimum; min1: the
+  // second vector's minimum — int32 add-node shortcut, values >= 0)
+  unsigned long long am = ~0ull;
+  unsigned m1 = ~0u;
   for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < npad; j0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = j0 + threadIdx.x;
     T v = Tr<T>::inf();
@@ -90,15 +94,30 @@ __global__ void k_validate_vec(const T* in, const T* in2, int64_t n, int64_t npa
     }
     if (wmin_bits) wmin_fold<T>(wmin_bits, v, j < n && v >= T(0) && Tr<T>::fin(v));
     if (j < npad) out[j] = v;
+    if constexpr (!Tr<T>::kFloat) {
+      if (j < n && v >= T(0)) {
+        am = min(am, (unsigned long long)(unsigned)v << 32 | (unsigned long long)j);
+        m1 = min(m1, (unsigned)v);
+      }
+    }
+  }
+  if (argmin0 && blockIdx.y == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) am = min(am, __shfl_xor_sync(0xffffffffu, am, o));
+    if ((threadIdx.x & 31) == 0 && am != ~0ull) atomicMin(argmin0, am);
+  }
+  if (min1 && blockIdx.y == 1) {
+    m1 = __reduce_min_sync(0xffffffffu, m1);
+    if ((threadIdx.x & 31) == 0 && m1 != ~0u) atomicMin(min1, m1);
   }
 }
 template <typename T>
 cudaError_t validate_vec(const T* in, const T* in2, int64_t n, int64_t npad, T* out,
                          unsigned int* err, unsigned* wmin_bits, cudaStream_t st, const T* inb,
-                         const T* in2b, T* outb) {
+                         const T* in2b, T* outb, unsigned long long* argmin0, unsigned* min1) {
   const int grid = (int)std::min<int64_t>(cdiv(npad, 256), 4 * num_sms());
   k_validate_vec<T><<<dim3(grid, inb ? 2 : 1), 256, 0, st>>>(in, in2, n, npad, out, err, wmin_bits, inb, in2b,
-                                                            outb);
+                                                            outb, argmin0, min1);
   return cudaGetLastError();
 }
 
@@ -752,74 +771,55 @@ __global__ void __launch_bounds__(256, P8_MINB) k_addnode_pass1_p8(Rows r, int64
 // every row with a finite out-edge — still exact, just a longer reduction.
 // *full stays 0 (the finish kernel keeps this row).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_addrow_setup(const int32_t* __restrict__ ow, int64_t n,
-                                                       const uint8_t* __restrict__ m8, int64_t ld,
-                                                       int64_t row0, int32_t* row, int64_t npad, int* slist,
-                                                       int* scount, unsigned* full, int limit) {
-  __shared__ int32_t sv[32];
-  __shared__ int si[32];
-  __shared__ int cnt;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// (AddScratch: kernels.h — the add's shortcut scratch words, set by k_add_init)
+__global__ void k_add_init(AddScratch a, unsigned* err, unsigned* wmin) {
+  *a.argmin_out = ~0ull; *a.in_min = ~0u; *a.s_count = 0; *a.u_count = 0; *a.th2 = 0x7F7F7F7F;
+  *a.fb_count = 0; *a.rmax = 0; *a.ufull = 0u; *a.rfull = 0u;
+  *err = 0u; *wmin = ~0u;
+}
+cudaError_t add_init(const AddScratch& a, unsigned* err, unsigned* wmin, cudaStream_t st) {
+  k_add_init<<<1, 1, 0, st>>>(a, err, wmin);
+  return cudaGetLastError();
+}
+// Rb = out[t0] + max_j D[t0][j] (t0 = the cheapest out-edge; INF in row t0:
+// every finite out); one CTA reads the 1 KB... n bytes of mirror row t0
+__global__ void __launch_bounds__(1024) k_addrow_bound(AddScratch a, const uint8_t* __restrict__ m8, int64_t ld,
+                                                       int64_t row0, int64_t n) {
+  __shared__ int32_t red[32];
+  const unsigned long long am = *a.argmin_out;
   const int32_t I = APSP_INF_I32_DEV;
-  for (int64_t j = tid; j < npad; j += blockDim.x) row[j] = I;
-  // t0 = argmin out (smallest index among ties)
-  int32_t bv = I;
-  int bi = -1;
-  for (int64_t t = tid; t < n; t += blockDim.x)
-    if (ow[t] < bv) { bv = ow[t]; bi = (int)t; }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const int32_t v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-    const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (v2 < bv || (v2 == bv && i2 >= 0 && (bi < 0 || i2 < bi))) { bv = v2; bi = i2; }
-  }
-  if (lane == 0) { sv[warp] = bv; si[warp] = bi; }
-  if (tid == 0) cnt = 0;
-  __syncthreads();
-  if (warp == 0) {
-    bv = sv[lane]; bi = si[lane];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const int32_t v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (v2 < bv || (v2 == bv && i2 >= 0 && (bi < 0 || i2 < bi))) { bv = v2; bi = i2; }
-    }
-    if (lane == 0) { sv[0] = bv; si[0] = bi; }
-  }
-  __syncthreads();
-  const int32_t omin = sv[0];
-  const int t0 = si[0];
-  __syncthreads();
-  if (omin >= I || t0 < 0) {   // no out-edge: the new row is all INF
-    if (tid == 0) { *scount = 0; *full = 0u; }
+  if (am == ~0ull || (int32_t)(am >> 32) >= I) {   // no out-edge: S is empty
+    if (threadIdx.x == 0) *a.rb = -1;
     return;
   }
-  // Rb = out[t0] + max_j D[t0][j] (INF if row t0 has an INF entry)
+  const int32_t omin = (int32_t)(am >> 32);
+  const int64_t t0 = (int64_t)(am & 0xFFFFFFFFull);
+  const uint8_t* mr = m8 + (t0 - row0) * ld;
   int32_t mx = 0;
-  const uint8_t* mr = m8 + ((int64_t)t0 - row0) * ld;
-  for (int64_t j = tid; j < n; j += blockDim.x) mx = max(mx, (int32_t)mr[j]);
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) mx = max(mx, (int32_t)mr[j]);
   mx = __reduce_max_sync(0xffffffffu, mx);
-  if (lane == 0) sv[warp] = mx;
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
   __syncthreads();
-  if (warp == 0) {
-    mx = __reduce_max_sync(0xffffffffu, sv[lane]);
-    if (lane == 0) sv[0] = mx;
+  if (threadIdx.x < 32) {
+    mx = __reduce_max_sync(0xffffffffu, threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0);
+    if (threadIdx.x == 0) *a.rb = mx >= kSat8i ? I - 1 : omin + mx;
   }
-  __syncthreads();
-  mx = sv[0];
-  const int32_t rb = mx >= kSat8i ? I - 1 : omin + mx;   // INF in row t0: every finite out-edge
-  for (int64_t t = tid; t < n; t += blockDim.x)
-    if (ow[t] <= rb) slist[atomicAdd(&cnt, 1)] = (int)t;   // (at most n <= ld entries)
-  __syncthreads();
-  if (tid == 0) { *scount = cnt; *full = 0u; }
+}
+// S = {t : out[t] <= Rb}; row := INF
+__global__ void k_addrow_compact(AddScratch a, const int32_t* __restrict__ ow, int64_t n, int64_t npad, int* slist,
+                                 int32_t* row) {
+  const int32_t rb = *a.rb, I = APSP_INF_I32_DEV;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < npad; t += (int64_t)gridDim.x * blockDim.x) {
+    row[t] = I;
+    if (t < n && ow[t] <= rb) slist[atomicAdd(a.s_count, 1)] = (int)t;
+  }
 }
 // row[j] = min over t in S of out[t] + D[t][j] (the mirror is exact: 0x7F = INF);
 // blockIdx.y splits S, atomicMin merges
 __global__ void __launch_bounds__(256) k_addrow(const int32_t* __restrict__ ow, const int* __restrict__ slist,
-                                                const int* __restrict__ scount, const unsigned* __restrict__ full,
+                                                const int* __restrict__ scount,
                                                 const uint8_t* __restrict__ m8, int64_t ld, int64_t row0,
                                                 int64_t n, int32_t* row) {
-  if (*full) return;
   const int cnt = *scount;
   const int64_t j0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
   if (j0 >= n) return;
@@ -856,65 +856,40 @@ __global__ void __launch_bounds__(256) k_addrow(const int32_t* __restrict__ ow, 
 // breaks either bound).  If |U| > limit, *ufull is set and the streaming
 // pass 1 does it instead.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_addcol_sets(const int32_t* __restrict__ iw,
-                                                      const int32_t* __restrict__ ow,
-                                                      const int32_t* __restrict__ row, int64_t n, int delta,
-                                                      int* ulist, int* ucount, int32_t* th2_out, unsigned* ufull,
-                                                      int limit) {
-  __shared__ int32_t red[32];
-  __shared__ int cnt;
-  __shared__ int32_t th2s;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// U = {t : in[t] <= th || out[t] <= R}, th = min in + delta; th2 = the
+// smallest in[t] above th (the certification threshold of col1)
+__global__ void k_addcol_sets(AddScratch a, const int32_t* __restrict__ iw, const int32_t* __restrict__ ow,
+                              int64_t n, int delta, int* ulist, int limit) {
   const int32_t I = APSP_INF_I32_DEV;
-  auto block_red = [&](int32_t v, bool mx) -> int32_t {
-    v = mx ? __reduce_max_sync(0xffffffffu, v) : __reduce_min_sync(0xffffffffu, v);
-    if (lane == 0) red[warp] = v;
-    __syncthreads();
-    int32_t w = red[lane];
-    w = mx ? __reduce_max_sync(0xffffffffu, w) : __reduce_min_sync(0xffffffffu, w);
-    __syncthreads();
-    return w;
-  };
-  int32_t mn = I, mx = 0;
-  for (int64_t t = tid; t < n; t += blockDim.x) {
-    mn = min(mn, iw[t]);
-    if (row[t] < I) mx = max(mx, row[t]);
-  }
-  const int32_t in_min = block_red(mn, false);
-  const int32_t R = block_red(mx, true);   // max finite entry of the new row
-  const int32_t th = in_min >= I ? I : min(I - 1, in_min + delta);
-  if (tid == 0) { cnt = 0; th2s = I; }
-  __syncthreads();
-  int32_t t2 = I;
-  for (int64_t t = tid; t < n; t += blockDim.x) {
-    const int32_t a = iw[t], b = ow[t];
-    if (a > th && a < t2) t2 = a;
-    if (a <= th || b <= R) {
-      const int q = atomicAdd(&cnt, 1);
+  const unsigned imn = *a.in_min;
+  const int32_t th = imn >= (unsigned)I ? I : min(I - 1, (int32_t)imn + delta);
+  const int32_t R = *a.rmax;
+  int32_t t2 = 0x7F7F7F7F;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t x = iw[t], y = ow[t];
+    if (x > th && x < t2) t2 = x;
+    if (x <= th || y <= R) {
+      const int q = atomicAdd(a.u_count, 1);
       if (q < limit) ulist[q] = (int)t;
     }
   }
   t2 = __reduce_min_sync(0xffffffffu, t2);
-  if (lane == 0) atomicMin(&th2s, t2);
-  __syncthreads();
-  if (tid == 0) {
-    *ucount = min(cnt, limit);
-    *th2_out = th2s;
-    *ufull = cnt > limit ? 1u : 0u;
-  }
+  if ((threadIdx.x & 31) == 0 && t2 < 0x7F7F7F7F) atomicMin(a.th2, t2);
 }
 // one warp per row: col1 / M' over U; certified rows get col and ceff, the
 // others are listed for k_addcol_rows (M' kept in mprime)
-__global__ void __launch_bounds__(256) k_addcol_gather(Rows r, const uint8_t* __restrict__ m8, int64_t ld,
-                                                       const int* __restrict__ ulist, const int* __restrict__ ucount,
-                                                       const unsigned* __restrict__ ufull,
+__global__ void __launch_bounds__(256) k_addcol_gather(AddScratch a, Rows r, const uint8_t* __restrict__ m8,
+                                                       int64_t ld, const int* __restrict__ ulist, int limit,
                                                        const int32_t* __restrict__ iw, const int32_t* __restrict__ ow,
-                                                       const int32_t* __restrict__ th2p, int32_t* col, int32_t* ceff,
-                                                       int32_t* mprime, int* fb_list, int* fb_count) {
-  if (*ufull) return;
+                                                       int32_t* col, int32_t* ceff, int32_t* mprime, int* fb_list) {
+  const int cnt = *a.u_count;
+  if (cnt > limit) {   // too many columns: the streaming pass does it
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.ufull = 1u;
+    return;
+  }
   const int lane = threadIdx.x & 31;
-  const int cnt = *ucount;
-  const int32_t th2 = *th2p, I = APSP_INF_I32_DEV;
+  const int32_t th2 = *a.th2, I = APSP_INF_I32_DEV;
+  int* fb_count = a.fb_count;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t i = r.lo + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < r.hi; i += nw) {
     const uint8_t* mrow = m8 + (i - r.row0) * ld;
@@ -945,13 +920,13 @@ __global__ void __launch_bounds__(256) k_addcol_gather(Rows r, const uint8_t* __
   }
 }
 // the rows col1 could not certify: a full-row min over the mirror (block per row)
-__global__ void __launch_bounds__(256) k_addcol_rows(Rows r, const uint8_t* __restrict__ m8, int64_t ld, int64_t n,
-                                                     const int32_t* __restrict__ iw, const unsigned* __restrict__ ufull,
-                                                     const int* __restrict__ fb_list, const int* __restrict__ fb_count,
+__global__ void __launch_bounds__(256) k_addcol_rows(AddScratch a, Rows r, const uint8_t* __restrict__ m8, int64_t ld,
+                                                     int64_t n, const int32_t* __restrict__ iw,
+                                                     const int* __restrict__ fb_list,
                                                      const int32_t* __restrict__ mprime, int32_t* col, int32_t* ceff) {
-  if (*ufull) return;
+  if (*a.ufull) return;
   __shared__ int32_t red[8];
-  const int cnt = *fb_count;
+  const int cnt = *a.fb_count;
   const int32_t I = APSP_INF_I32_DEV;
   for (int f = blockIdx.x; f < cnt; f += gridDim.x) {
     const int64_t i = fb_list[f];
@@ -973,28 +948,40 @@ __global__ void __launch_bounds__(256) k_addcol_rows(Rows r, const uint8_t* __re
     __syncthreads();
   }
 }
-cudaError_t addcol_g(Rows r, const uint8_t* m8, int64_t ld, int64_t n, const int32_t* iw, const int32_t* ow,
-                     const int32_t* row, int* ulist, int* ucount, int32_t* th2, unsigned* ufull, int limit,
-                     int32_t* col, int32_t* ceff, int32_t* mprime, int* fb_list, int* fb_count, cudaStream_t st) {
-  CUDA_TRY(cudaMemsetAsync(fb_count, 0, sizeof(int), st));
-  k_addcol_sets<<<1, 1024, 0, st>>>(iw, ow, row, n, 3, ulist, ucount, th2, ufull, limit);
+cudaError_t addcol_g(const AddScratch& a, Rows r, const uint8_t* m8, int64_t ld, int64_t n, const int32_t* iw,
+                     const int32_t* ow, int* ulist, int limit, int32_t* col, int32_t* ceff, int32_t* mprime,
+                     int* fb_list, cudaStream_t st) {
+  const int g = (int)std::min<int64_t>(cdiv(n, 256), 2 * num_sms());
+  k_addcol_sets<<<g, 256, 0, st>>>(a, iw, ow, n, 3, ulist, limit);
   CUDA_TRY(cudaGetLastError());
   if (r.hi > r.lo) {
     const int grid = (int)std::min<int64_t>(cdiv(r.hi - r.lo, 8), (int64_t)num_sms() * 16);
-    k_addcol_gather<<<grid, 256, 0, st>>>(r, m8, ld, ulist, ucount, ufull, iw, ow, th2, col, ceff, mprime,
-                                          fb_list, fb_count);
+    k_addcol_gather<<<grid, 256, 0, st>>>(a, r, m8, ld, ulist, limit, iw, ow, col, ceff, mprime, fb_list);
     CUDA_TRY(cudaGetLastError());
-    k_addcol_rows<<<num_sms(), 256, 0, st>>>(r, m8, ld, n, iw, ufull, fb_list, fb_count, mprime, col, ceff);
+    k_addcol_rows<<<num_sms(), 256, 0, st>>>(a, r, m8, ld, n, iw, fb_list, mprime, col, ceff);
   }
   return cudaGetLastError();
 }
 
-cudaError_t addrow_s(const int32_t* ow, int64_t n, const uint8_t* m8, int64_t ld, int64_t row0, int32_t* row,
-                     int64_t npad, int* slist, int* scount, unsigned* full, int limit, cudaStream_t st) {
-  k_addrow_setup<<<1, 1024, 0, st>>>(ow, n, m8, ld, row0, row, npad, slist, scount, full, limit);
+// max finite entry of the new row (the S2 bound of the gathers)
+__global__ void k_row_max(const int32_t* __restrict__ row, int64_t n, int* rmax) {
+  int32_t m = 0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    if (row[j] < APSP_INF_I32_DEV) m = max(m, row[j]);
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(rmax, m);
+}
+cudaError_t addrow_s(const AddScratch& a, const int32_t* ow, int64_t n, const uint8_t* m8, int64_t ld, int64_t row0,
+                     int32_t* row, int64_t npad, int* slist, cudaStream_t st) {
+  k_addrow_bound<<<1, 1024, 0, st>>>(a, m8, ld, row0, n);
+  CUDA_TRY(cudaGetLastError());
+  const int g = (int)std::min<int64_t>(cdiv(npad, 256), 2 * num_sms());
+  k_addrow_compact<<<g, 256, 0, st>>>(a, ow, n, npad, slist, row);
   CUDA_TRY(cudaGetLastError());
   const dim3 grid((unsigned)cdiv(cdiv(n, 4), 256), 16);
-  k_addrow<<<grid, 256, 0, st>>>(ow, slist, scount, full, m8, ld, row0, n, row);
+  k_addrow<<<grid, 256, 0, st>>>(ow, slist, a.s_count, m8, ld, row0, n, row);
+  CUDA_TRY(cudaGetLastError());
+  k_row_max<<<(int)std::min<int64_t>(cdiv(n, 256), 2 * num_sms()), 256, 0, st>>>(row, n, a.rmax);
   return cudaGetLastError();
 }
 
@@ -2406,7 +2393,7 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
 
 #define INST(T)                                                                                   \
   template cudaError_t validate_vec<T>(const T*, const T*, int64_t, int64_t, T*, unsigned int*, unsigned*,    \
-                                       cudaStream_t, const T*, const T*, T*);                                             \
+                                       cudaStream_t, const T*, const T*, T*, unsigned long long*, unsigned*);                                             \
   template cudaError_t transpose_in<T>(const T*, int64_t, int64_t, T*, int64_t, unsigned int*,     \
                                        unsigned*, cudaStream_t);                                  \
   template cudaError_t fill<T>(T*, int64_t, T, cudaStream_t);                                      \

@@ -825,3 +825,28 @@ def test_mirror8_ragged_sizes(lib, rng, n, directed):
                 hg.set_edge(u, v, w)
         assert h.mirror_width == 8
         assert_parity(getD(h), oracle.fw(hg.W))
+
+
+def test_add_node_gather_fallbacks(lib, rng):
+    """The add-node shortcuts' fallbacks on the int8 mirror: (1) columns with
+    the cheapest in-edges are unreachable from most rows (col1 uncertified:
+    full-row scans); (2) every in-edge equally cheap, so the gathered column
+    set exceeds its limit (the streaming pass 1 runs)."""
+    n = 2600
+    W = random_graph(rng, n, True, density=0.02, lo=1, hi=9)
+    W[:, :10] = INF            # nodes 0-9: no in-edges
+    np.fill_diagonal(W, 0)
+    hg = synth.HostGraph(W, True, cap=n + 3)
+    h = make(lib, W, cap=n + 3)
+    o = rng.integers(1, 9, n).astype(np.int32)
+    i = np.full(n, 60, np.int32)
+    i[:10] = 1                 # cheapest in-edges from the unreachable nodes
+    h.add_node(o, i)
+    hg.add_node(o, i)
+    assert h.mirror_width == 8
+    assert_parity(getD(h), oracle.fw(hg.W))
+    o2 = rng.integers(1, 9, hg.n).astype(np.int32)
+    i2 = np.full(hg.n, 3, np.int32)   # all equal: |U| = n > 2048
+    h.add_node(o2, i2)
+    hg.add_node(o2, i2)
+    assert_parity(getD(h), oracle.fw(hg.W))

@@ -536,9 +536,12 @@ cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const 
 // stops at the first batch whose bound reaches lb (certified); after
 // kPhaseABatches batches the pair is left open for A2 / B / the rounds.
 constexpr int kPhaseABatches = 9;   // sorted positions 0-71
+#ifndef PA_MINB
+#define PA_MINB 4   // 4 CTAs per SM (64 registers, no spills): latency-bound, occupancy wins
+#endif
 
 template <typename T, int SR, bool TWO>
-__global__ void __launch_bounds__(256) k_sparse_phase_a(T* D, int64_t ld, int64_t row0,
+__global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_a(T* D, int64_t ld, int64_t row0,
                                                         const int* __restrict__ SLid,
                                                         const T* __restrict__ SLw,
                                                         const int* __restrict__ srow,

@@ -894,7 +894,7 @@ __global__ void __launch_bounds__(256) k_addcol_gather(AddScratch a, Rows r, con
   for (int64_t i = r.lo + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < r.hi; i += nw) {
     const uint8_t* mrow = m8 + (i - r.row0) * ld;
     int32_t p = I, m = INT_MIN;
-#pragma unroll 4
+#pragma unroll 16
     for (int k = lane; k < cnt; k += 32) {
       const int t = ulist[k];
       const int32_t d8 = mrow[t];

@@ -159,7 +159,8 @@ struct apsp_handle {
   bool poisoned = false;
   std::string err;
   int64_t launches = 0;
-  void* host_small = nullptr;    // pinned host scratch for small D2H reads
+  void* host_small = nullptr;    // pinned, mapped host scratch for small D2H reads
+  void* host_small_dev = nullptr;   // its device address
   // profiling (apsp_profile_*)
   struct ProfRec { int cls; cudaEvent_t a, b; double work; };
   bool prof_on = false;
@@ -700,9 +701,13 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     NK(h->comm->allreduce(v + 5, 1, ncclInt64, ncclMax, h->st));
   }
   long long* hv = reinterpret_cast<long long*>(h->host_small);
-  CKR(cudaMemcpyAsync(hv, v, 6 * sizeof(long long), cudaMemcpyDeviceToHost, h->st));
-  unsigned* hmf = reinterpret_cast<unsigned*>(h->host_small) + 16;
-  CKR(cudaMemcpyAsync(hmf, h->mirror_flag(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+  unsigned* hmf = reinterpret_cast<unsigned*>(h->host_small) + 12;
+  {
+    ReadSet rs{};
+    rs.add(v, 6 * sizeof(long long));
+    rs.add(h->mirror_flag(), sizeof(unsigned));
+    CK(readback(rs, h->host_small_dev, h->st));
+  }
   CKR(cudaStreamSynchronize(h->st));
   h->mirror_hint = (*hmf & 1u) == 0u;
   const int64_t total = hv[0], rows = hv[1], maxrow = hv[5];
@@ -772,9 +777,13 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
                      std::is_same<T, int32_t>::value ? as.argmin_out : nullptr,
                      std::is_same<T, int32_t>::value ? as.in_min : nullptr));
   unsigned* herr = reinterpret_cast<unsigned*>(h->host_small);
-  CKR(cudaMemcpyAsync(herr, &h->ctr()->err, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
-  CKR(cudaMemcpyAsync(herr + 1, h->wmin_dev(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
-  CKR(cudaMemcpyAsync(herr + 2, h->mirror_flag(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+  {
+    ReadSet rs{};
+    rs.add(&h->ctr()->err, sizeof(unsigned));
+    rs.add(h->wmin_dev(), sizeof(unsigned));
+    rs.add(h->mirror_flag(), sizeof(unsigned));
+    CK(readback(rs, h->host_small_dev, h->st));
+  }
   CKR(cudaStreamSynchronize(h->st));
   h->mirror_hint = (herr[2] & 1u) == 0u;
   if (*herr) {
@@ -907,7 +916,11 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
   if (h->world > 1)
     NK(h->comm->bcast(dev2 + 1, 1, nccl_type<T>(), h->owner(u), h->st));
   T* hv = reinterpret_cast<T*>(h->host_small);
-  CKR(cudaMemcpyAsync(hv, dev2, 2 * sizeof(T), cudaMemcpyDeviceToHost, h->st));
+  {
+    ReadSet rs{};
+    rs.add(dev2, 2 * sizeof(T));
+    CK(readback(rs, h->host_small_dev, h->st));
+  }
   CKR(cudaStreamSynchronize(h->st));
   const T w_old = hv[0], duv = hv[1];
   if (info) info->n_after = n;
@@ -1250,7 +1263,11 @@ apsp_status create_impl(apsp_handle** out, apsp_dtype dtype, int directed, int64
   h->st = reinterpret_cast<cudaStream_t>(stream);
   h->rank = rank;
   h->world = world;
-  if (cudaHostAlloc(&h->host_small, 4096, cudaHostAllocDefault) != cudaSuccess) {
+  // mapped: small host reads are written by a kernel (k_readback) instead of
+  // separate device-to-host copies
+  if (cudaHostAlloc(&h->host_small, 4096, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(&h->host_small_dev, h->host_small, 0) != cudaSuccess) {
+    if (h->host_small) cudaFreeHost(h->host_small);
     delete h;
     return APSP_E_CUDA;
   }

@@ -243,6 +243,15 @@ inline cudaError_t mirror_cross(const float*, int64_t, Rows, int64_t, int64_t, i
   return cudaSuccess;
 }
 cudaError_t pack_counters(const DetectCounters* c, const int* any, long long* v, cudaStream_t st);
+// small device values to (mapped) host memory in one launch: the pieces are
+// packed back to back, 4-byte words, in the order added
+struct ReadSet {
+  const void* p[8];
+  int bytes[8];
+  int k;
+  void add(const void* ptr, int nbytes) { p[k] = ptr; bytes[k] = nbytes; ++k; }
+};
+cudaError_t readback(const ReadSet& rs, void* dst_dev, cudaStream_t st);
 // zero up to 8 int buffers in one launch
 struct ZeroSet {
   int* p[8];

@@ -2318,6 +2318,20 @@ cudaError_t pack_counters(const DetectCounters* c, const int* any, long long* v,
   return cudaGetLastError();
 }
 
+__global__ void k_readback(ReadSet rs, unsigned* dst) {
+  int off = 0;
+  for (int b = 0; b < rs.k; ++b) {
+    const unsigned* src = reinterpret_cast<const unsigned*>(rs.p[b]);
+    const int w = rs.bytes[b] / 4;
+    for (int e = threadIdx.x; e < w; e += blockDim.x) dst[off + e] = *(volatile const unsigned*)(src + e);
+    off += w;
+  }
+}
+cudaError_t readback(const ReadSet& rs, void* dst_dev, cudaStream_t st) {
+  k_readback<<<1, 32, 0, st>>>(rs, reinterpret_cast<unsigned*>(dst_dev));
+  return cudaGetLastError();
+}
+
 __global__ void k_zero_set(ZeroSet z) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int b = 0; b < z.k; ++b)

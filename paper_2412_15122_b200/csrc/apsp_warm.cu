@@ -29,6 +29,7 @@ namespace {
 constexpr int64_t kTile = 128;       // FW pivot block / row-partition granule
 constexpr int kMaxSlabs = 256;       // add-node column partial slabs
 constexpr int kAddColLimit = 2048;   // columns the add-node gathers may read per row (else the stream)
+constexpr int64_t kAddShortcutMinN = 4096;   // the add-node shortcuts from this n on
 constexpr int64_t kVecs = 8;         // scratch vectors of ld elements
 constexpr int kQueryChunk = 32;      // sharded queries per column all-gather
 
@@ -798,7 +799,8 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   // the new row from the few rows that can attain it (one GPU, int8 mirror
   // valid as read above): on the side stream, under pass 1
   bool srow = false;
-  if constexpr (std::is_same<T, int32_t>::value) srow = h->world == 1 && mirror8_known_valid(h);
+  // (small graphs: the one streaming pass costs less than the shortcuts' extra launches)
+  if constexpr (std::is_same<T, int32_t>::value) srow = h->world == 1 && n >= kAddShortcutMinN && mirror8_known_valid(h);
   if constexpr (std::is_same<T, int32_t>::value) {
     if (srow) {
       CK2(addrow_s(as, ow, n, h->mirror<T>().m8, ld, h->row0, row, ld, reinterpret_cast<int*>(h->vec<T>(5)),

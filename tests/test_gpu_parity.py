@@ -827,26 +827,43 @@ def test_mirror8_ragged_sizes(lib, rng, n, directed):
         assert_parity(getD(h), oracle.fw(hg.W))
 
 
+def _sampled_rows_cols(h, W, idx):
+    torch.cuda.synchronize()
+    it = torch.as_tensor(np.asarray(idx), device=h.D_local.device, dtype=torch.long)
+    got_r = h.D.index_select(0, it).cpu().numpy()
+    got_c = h.D.index_select(1, it).cpu().numpy().T
+    assert np.array_equal(got_r, oracle.dijkstra_rows_i32(W, idx))
+    assert np.array_equal(got_c, oracle.dijkstra_rows_i32(W, idx, reverse=True))
+
+
 def test_add_node_gather_fallbacks(lib, rng):
-    """The add-node shortcuts' fallbacks on the int8 mirror: (1) columns with
-    the cheapest in-edges are unreachable from most rows (col1 uncertified:
-    full-row scans); (2) every in-edge equally cheap, so the gathered column
-    set exceeds its limit (the streaming pass 1 runs)."""
-    n = 2600
-    W = random_graph(rng, n, True, density=0.02, lo=1, hi=9)
+    """The add-node shortcuts (n >= 4096, int8 mirror) and their fallbacks:
+    (1) the columns with the cheapest in-edges are unreachable from most rows
+    (col1 uncertified: full-row scans); (2) every in-edge equally cheap, so the
+    gathered column set exceeds its limit (the streaming pass 1 runs).
+    Sampled rows / columns (the new node's included) against Dijkstra on the
+    host graph, and the whole matrix against a cold FW of the same graph."""
+    n = 4200
+    W = random_graph(rng, n, True, density=0.01, lo=1, hi=9)
     W[:, :10] = INF            # nodes 0-9: no in-edges
     np.fill_diagonal(W, 0)
     hg = synth.HostGraph(W, True, cap=n + 3)
     h = make(lib, W, cap=n + 3)
+    assert h.mirror_width == 8
     o = rng.integers(1, 9, n).astype(np.int32)
     i = np.full(n, 60, np.int32)
     i[:10] = 1                 # cheapest in-edges from the unreachable nodes
     h.add_node(o, i)
     hg.add_node(o, i)
-    assert h.mirror_width == 8
-    assert_parity(getD(h), oracle.fw(hg.W))
     o2 = rng.integers(1, 9, hg.n).astype(np.int32)
     i2 = np.full(hg.n, 3, np.int32)   # all equal: |U| = n > 2048
     h.add_node(o2, i2)
     hg.add_node(o2, i2)
-    assert_parity(getD(h), oracle.fw(hg.W))
+    o3 = rng.integers(1, 40, hg.n).astype(np.int32)   # the ordinary case
+    i3 = rng.integers(1, 40, hg.n).astype(np.int32)
+    h.add_node(o3, i3)
+    hg.add_node(o3, i3)
+    idx = np.concatenate([rng.choice(n, 12, replace=False), [0, 5, n, n + 1, n + 2]])
+    _sampled_rows_cols(h, hg.W, idx)
+    cold = make(lib, hg.W, cap=n + 3)
+    assert np.array_equal(getD(h), getD(cold))

@@ -847,7 +847,7 @@ __global__ void __launch_bounds__(256) k_addrow(const int32_t* __restrict__ ow, 
 //   col[i] = min_t D[i][t] + in[t]: over S1 = {t : in[t] <= th} it is an upper
 //     bound col1[i]; if col1[i] <= th2 (the smallest in[t] above th), no t
 //     outside S1 can do better (D >= 0): exact.  Rows not certified get a
-//     full-row scan (k_addcol_rows).  th = min in + 3.
+//     full-row scan (k_addcol_rows).  th = min in + 2.
 //   M'[i] = max_{t in S2} D[i][t] - out[t], S2 = {t : out[t] <= R}, R = max_j
 //     row[j] (the new row, computed first): a change at (i, j) needs col[i] <
 //     D[i][t*] - out[t*] for the t* attaining row[j], and out[t*] <= row[j]
@@ -952,7 +952,8 @@ cudaError_t addcol_g(const AddScratch& a, Rows r, const uint8_t* m8, int64_t ld,
                      const int32_t* ow, int* ulist, int limit, int32_t* col, int32_t* ceff, int32_t* mprime,
                      int* fb_list, cudaStream_t st) {
   const int g = (int)std::min<int64_t>(cdiv(n, 256), 2 * num_sms());
-  k_addcol_sets<<<g, 256, 0, st>>>(a, iw, ow, n, 3, ulist, limit);
+  static const int delta = tune_wps("APSP_TUNE_ADDCOL_DELTA", 2);   // th = min in + delta (measured)
+  k_addcol_sets<<<g, 256, 0, st>>>(a, iw, ow, n, delta, ulist, limit);
   CUDA_TRY(cudaGetLastError());
   if (r.hi > r.lo) {
     const int grid = (int)std::min<int64_t>(cdiv(r.hi - r.lo, 8), (int64_t)num_sms() * 16);

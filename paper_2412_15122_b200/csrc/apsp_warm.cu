@@ -623,6 +623,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     z.add(h->ocnt(), h->cap);
     for (int q = 0; q < 4; ++q) z.add(h->chg(q), h->cap + 1);
     z.add(h->anyflag(), 1);
+    z.add(h->anyrow(), h->cap);   // the rounds' per-row open minima (keys)
     CK(zero_set(z, h->st));
   }
   // one streaming pass appends the need_update_list; then the per-row slices
@@ -660,7 +661,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
          sparse_round<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->gprow(), h->gpcol(),
                          h->glb<T>(), ocap, h->rowoff(), fin_c, rounds == 0 ? nullptr : fin_c + h->cap,
                          fin_l, h->chg(o), h->chg(o) + h->cap, fcol[rounds & 1], h->anyflag(), h->sr, h->ctr(),
-                         h->st));
+                         h->st, reinterpret_cast<unsigned*>(h->anyrow()), h->wmin<T>()));
       last_total = h->chg(o) + h->cap;
     }
     return APSP_OK;
@@ -685,6 +686,8 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     PK(APSP_K_SPARSE_R, 0.0,
        sparse_full<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, n, h->gprow(), h->gpcol(),
                       h->glb<T>(), h->gfull(), ocap, h->sr, h->ctr(), h->st));
+    CK(open_rowmin<T>(h->Dl<T>(), h->ld, h->row0, h->gprow(), h->gpcol(), ocap,
+                      reinterpret_cast<unsigned*>(h->anyrow()), h->ctr(), h->st));
     // rounds over the open entries of each row, a first batch of 4
     apsp_status s = enqueue_rounds(std::min(4, h->max_rounds));
     if (s != APSP_OK) return s;

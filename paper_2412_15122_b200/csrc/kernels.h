@@ -198,7 +198,11 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
                          const int* gprow, const int* gpcol, const T* glb, int64_t nopen,
                          const int64_t* rowoff, const int* fcnt_in, const int* ftot_in, const int* fcol_in,
                          int* fcnt_out, int* ftot_out, int* fcol_out, int* any, int sr,
-                         const DetectCounters* dc, cudaStream_t st);
+                         const DetectCounters* dc, cudaStream_t st, unsigned* rowkey = nullptr, T wmin = T(0));
+// per-row minimum of the open pairs' current values (after A2 / B), as keys
+template <typename T>
+cudaError_t open_rowmin(const T* D, int64_t ld, int64_t row0, const int* gprow, const int* gpcol, int64_t nopen,
+                        unsigned* rowkey, const DetectCounters* dc, cudaStream_t st);
 
 // ---------------- query.cu ----------------
 constexpr int kQueryCap = 4096;    // max |C| per query (min(kQueryCap, cap) per handle)
@@ -246,18 +250,28 @@ cudaError_t pack_counters(const DetectCounters* c, const int* any, long long* v,
 // small device values to (mapped) host memory in one launch: the pieces are
 // packed back to back, 4-byte words, in the order added
 struct ReadSet {
-  const void* p[8];
-  int bytes[8];
+  static constexpr int kMax = 8;
+  const void* p[kMax];
+  int bytes[kMax];
   int k;
-  void add(const void* ptr, int nbytes) { p[k] = ptr; bytes[k] = nbytes; ++k; }
+  void add(const void* ptr, int nbytes) {
+    if (k < kMax) { p[k] = ptr; bytes[k] = nbytes; ++k; }
+    else overflow = true;
+  }
+  bool overflow;
 };
 cudaError_t readback(const ReadSet& rs, void* dst_dev, cudaStream_t st);
-// zero up to 8 int buffers in one launch
+// zero up to 12 int buffers in one launch
 struct ZeroSet {
-  int* p[8];
-  int64_t n[8];
+  static constexpr int kMax = 12;
+  int* p[kMax];
+  int64_t n[kMax];
   int k;
-  void add(int* ptr, int64_t count) { p[k] = ptr; n[k] = count; ++k; }
+  void add(int* ptr, int64_t count) {
+    if (k < kMax) { p[k] = ptr; n[k] = count; ++k; }
+    else overflow = true;
+  }
+  bool overflow;
 };
 cudaError_t zero_set(const ZeroSet& z, cudaStream_t st);
 double microbench(int kind, void* buf, size_t bytes, cudaStream_t st);   // microbench.cu

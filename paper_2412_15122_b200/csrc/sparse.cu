@@ -720,6 +720,40 @@ cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw
 // ---------------------------------------------------------------------------
 // rounds: open pair of a changed row, min over the open entries m of its row
 // ---------------------------------------------------------------------------
+// Per-row minimum of the open entries' current values, kept as a key that
+// atomicMax orders like the value's min (values are >= 0: int32 and IEEE
+// floats order like their bits; ~bits reverses it; key 0 = "none").
+template <typename T>
+__device__ __forceinline__ unsigned open_key(T v) {
+  unsigned b;
+  memcpy(&b, &v, 4);
+  return ~b;
+}
+template <typename T>
+__device__ __forceinline__ T open_min(unsigned key) {
+  const unsigned b = ~key;
+  T v;
+  memcpy(&v, &b, 4);
+  return v;
+}
+template <typename T>
+__global__ void k_open_rowmin(const T* __restrict__ D, int64_t ld, int64_t row0, const int* __restrict__ gprow,
+                              const int* __restrict__ gpcol, int64_t nopen, unsigned* rowkey,
+                              const DetectCounters* dc) {
+  nopen = device_count(dc, nopen, 1);
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nopen; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = gprow[p];
+    atomicMax(rowkey + i, open_key<T>(D[(i - row0) * ld + gpcol[p]]));
+  }
+}
+template <typename T>
+cudaError_t open_rowmin(const T* D, int64_t ld, int64_t row0, const int* gprow, const int* gpcol, int64_t nopen,
+                        unsigned* rowkey, const DetectCounters* dc, cudaStream_t st) {
+  if (nopen <= 0) return cudaSuccess;
+  k_open_rowmin<T><<<2 * num_sms(), 256, 0, st>>>(D, ld, row0, gprow, gpcol, nopen, rowkey, dc);
+  return cudaGetLastError();
+}
+
 template <typename T, int SR>
 __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t row0,
                                                       const T* __restrict__ WT, int64_t ldw,
@@ -731,7 +765,7 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
                                                       const int* __restrict__ ftot_in,
                                                       const int* __restrict__ fcol_in,
                                                       int* fcnt_out, int* ftot_out, int* fcol_out, int* any,
-                                                      const DetectCounters* dc) {
+                                                      const DetectCounters* dc, unsigned* rowkey, T wmin) {
   // an empty frontier (nothing changed last round): the round is a no-op
   if (ftot_in && *(volatile const int*)ftot_in == 0) return;
   const int lane = threadIdx.x & 31;
@@ -748,6 +782,9 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
     if (lane == 0) cur = *(volatile T*)(Drow + j);
     cur = __shfl_sync(0xffffffffu, cur, 0);  // one value for the whole warp (others may write)
     if (Tr<T>::at_lb(cur, glb[p])) continue;   // already at its lower bound: final
+    // no open entry of the row can lower it: every one is >= the row's
+    // smallest open value and every weight >= wmin
+    if (rowkey && cur <= Tr<T, SR>::add(open_min<T>(rowkey[i]), wmin)) continue;
     const T* Wrow = WT + j * ldw;
     const int* fl = fcol_in + rowoff[i];
     T acc = Tr<T>::inf();
@@ -767,6 +804,7 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
       Drow[j] = acc;
       fcol_out[rowoff[i] + atomicAdd(fcnt_out + i, 1)] = (int)j;   // j changed: next round's frontier
       atomicAdd(ftot_out, 1);
+      if (rowkey) atomicMax(rowkey + i, open_key<T>(acc));
       *any = 1;
     }
   }
@@ -776,7 +814,7 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
                          const int* gprow, const int* gpcol, const T* glb, int64_t nopen,
                          const int64_t* rowoff, const int* fcnt_in, const int* ftot_in, const int* fcol_in,
                          int* fcnt_out, int* ftot_out, int* fcol_out, int* any, int sr,
-                         const DetectCounters* dc, cudaStream_t st) {
+                         const DetectCounters* dc, cudaStream_t st, unsigned* rowkey, T wmin) {
   if (nopen <= 0) return cudaSuccess;
   // round 0 relaxes every open pair through its row's open entries; later
   // rounds only the pairs whose row changed (often none: a small grid keeps
@@ -785,11 +823,11 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
   if (sr)
     k_sparse_round<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff,
                                                fcnt_in, ftot_in, fcol_in, fcnt_out, ftot_out, fcol_out, any,
-                                               dc);
+                                               dc, rowkey, wmin);
   else
     k_sparse_round<T, 0><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff,
                                                fcnt_in, ftot_in, fcol_in, fcnt_out, ftot_out, fcol_out, any,
-                                               dc);
+                                               dc, rowkey, wmin);
   return cudaGetLastError();
 }
 
@@ -814,10 +852,12 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
   template cudaError_t sparse_full<T>(T*, int64_t, int64_t, const T*, int64_t, int64_t,            \
                                       const int*, const int*, const T*, const unsigned char*,      \
                                       int64_t, int, const DetectCounters*, cudaStream_t);         \
+  template cudaError_t open_rowmin<T>(const T*, int64_t, int64_t, const int*, const int*, int64_t,      \
+                                      unsigned*, const DetectCounters*, cudaStream_t);             \
   template cudaError_t sparse_round<T>(T*, int64_t, int64_t, const T*, int64_t, const int*,        \
                                        const int*, const T*, int64_t, const int64_t*, const int*,  \
                                        const int*, const int*, int*, int*, int*, int*, int,        \
-                                       const DetectCounters*, cudaStream_t);
+                                       const DetectCounters*, cudaStream_t, unsigned*, T);
 INST(int32_t)
 INST(float)
 #undef INST

@@ -2329,6 +2329,7 @@ __global__ void k_readback(ReadSet rs, unsigned* dst) {
   }
 }
 cudaError_t readback(const ReadSet& rs, void* dst_dev, cudaStream_t st) {
+  if (rs.overflow) return cudaErrorInvalidValue;
   k_readback<<<1, 32, 0, st>>>(rs, reinterpret_cast<unsigned*>(dst_dev));
   return cudaGetLastError();
 }
@@ -2339,6 +2340,7 @@ __global__ void k_zero_set(ZeroSet z) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < z.n[b]; e += stride) z.p[b][e] = 0;
 }
 cudaError_t zero_set(const ZeroSet& z, cudaStream_t st) {
+  if (z.overflow) return cudaErrorInvalidValue;   // more buffers than the set holds
   int64_t most = 1;
   for (int b = 0; b < z.k; ++b) most = std::max(most, z.n[b]);
   const int grid = (int)std::min<int64_t>(cdiv(most, 256), 2 * num_sms());

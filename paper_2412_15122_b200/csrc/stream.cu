@@ -1002,135 +1002,138 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   T (*rp)[33] = rp_all[warp][0];
   T (*rm)[33] = rp_all[warp][1];
-  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
-  if (gw >= tl.warps) return;
-  const int chunk = (int)(gw % tl.nchunk);
-  const int slab = (int)(gw / tl.nchunk);
-  const int64_t i_lo = r.lo + slab * tl.slab;
-  const int64_t i_hi = min(r.hi, i_lo + tl.slab);
-  const T I = Tr<T>::inf();
-  const T NI = Tr<T>::kFloat ? -I : -I;   // "minus infinity" of the max reduction
+  // grid-stride over the tasks: launched next to a packed pass, this kernel
+  // usually exits at once, so it is launched small
+  for (int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; gw < tl.warps;
+       gw += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int chunk = (int)(gw % tl.nchunk);
+    const int slab = (int)(gw / tl.nchunk);
+    const int64_t i_lo = r.lo + slab * tl.slab;
+    const int64_t i_hi = min(r.hi, i_lo + tl.slab);
+    const T I = Tr<T>::inf();
+    const T NI = Tr<T>::kFloat ? -I : -I;   // "minus infinity" of the max reduction
 
-  int64_t qv[P1_V];
-  Vec4<T> inw[P1_V], nout[P1_V], colp[P1_V];
-  // does this warp's chunk contain the row's last, partially valid vector?
-  const bool tail = (n & 3) != 0 && (int64_t)(chunk + 1) * P1_VEC >= tl.n4;
-#pragma unroll
-  for (int v = 0; v < P1_V; ++v) {
-    qv[v] = group_of(m16, chunk, v, lane);   // P1_VEC == 128: the 512-column chunk
-    inw[v] = qv[v] < tl.n4 ? ld4<T>(iw + 4 * qv[v]) : Vec4<T>{I, I, I, I};
-    Vec4<T> o = qv[v] < tl.n4 ? ld4<T>(ow + 4 * qv[v]) : Vec4<T>{I, I, I, I};
-    // shortest path: -out[t] (an absent out-edge, INF, can never give a
-    // shortcut: -INF); minimax: out[t] itself (see max_add)
-    nout[v] = SR ? o : Vec4<T>{-o.x, -o.y, -o.z, -o.w};
-    colp[v] = Vec4<T>{I, I, I, I};
-  }
-  for (int64_t b0 = i_lo; b0 < i_hi; b0 += P1_RB) {
-    const int nb = (int)min((int64_t)P1_RB, i_hi - b0);
-    // rows b0 + rr and b0 + rr + 1 (if two): partials into rp / rm, column partials
-    auto body = [&](Vec4<T> (&d0)[P1_V], Vec4<T> (&d1)[P1_V], int rr, bool two) {
-      const int64_t i = b0 + rr;
-      if (tail) {   // only the warp holding the row's last (partial) vector
-#pragma unroll
+    int64_t qv[P1_V];
+    Vec4<T> inw[P1_V], nout[P1_V], colp[P1_V];
+    // does this warp's chunk contain the row's last, partially valid vector?
+    const bool tail = (n & 3) != 0 && (int64_t)(chunk + 1) * P1_VEC >= tl.n4;
+  #pragma unroll
+    for (int v = 0; v < P1_V; ++v) {
+      qv[v] = group_of(m16, chunk, v, lane);   // P1_VEC == 128: the 512-column chunk
+      inw[v] = qv[v] < tl.n4 ? ld4<T>(iw + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+      Vec4<T> o = qv[v] < tl.n4 ? ld4<T>(ow + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+      // shortest path: -out[t] (an absent out-edge, INF, can never give a
+      // shortcut: -INF); minimax: out[t] itself (see max_add)
+      nout[v] = SR ? o : Vec4<T>{-o.x, -o.y, -o.z, -o.w};
+      colp[v] = Vec4<T>{I, I, I, I};
+    }
+    for (int64_t b0 = i_lo; b0 < i_hi; b0 += P1_RB) {
+      const int nb = (int)min((int64_t)P1_RB, i_hi - b0);
+      // rows b0 + rr and b0 + rr + 1 (if two): partials into rp / rm, column partials
+      auto body = [&](Vec4<T> (&d0)[P1_V], Vec4<T> (&d1)[P1_V], int rr, bool two) {
+        const int64_t i = b0 + rr;
+        if (tail) {   // only the warp holding the row's last (partial) vector
+  #pragma unroll
+          for (int v = 0; v < P1_V; ++v) {
+            d0[v] = mask_tail<T>(d0[v], 4 * qv[v], n);
+            d1[v] = mask_tail<T>(d1[v], 4 * qv[v], n);
+          }
+        }
+        const T o0 = ow[i];
+        const T o1 = two ? ow[i + 1] : I;
+        T p0 = I, p1 = I, m0 = NI, m1 = NI;
+  #pragma unroll
         for (int v = 0; v < P1_V; ++v) {
-          d0[v] = mask_tail<T>(d0[v], 4 * qv[v], n);
-          d1[v] = mask_tail<T>(d1[v], 4 * qv[v], n);
+          p0 = Tr<T, SR>::relax(p0, d0[v].x, inw[v].x); p0 = Tr<T, SR>::relax(p0, d0[v].y, inw[v].y);
+          p0 = Tr<T, SR>::relax(p0, d0[v].z, inw[v].z); p0 = Tr<T, SR>::relax(p0, d0[v].w, inw[v].w);
+          p1 = Tr<T, SR>::relax(p1, d1[v].x, inw[v].x); p1 = Tr<T, SR>::relax(p1, d1[v].y, inw[v].y);
+          p1 = Tr<T, SR>::relax(p1, d1[v].z, inw[v].z); p1 = Tr<T, SR>::relax(p1, d1[v].w, inw[v].w);
+          m0 = max_add<T, SR>(m0, d0[v].x, nout[v].x); m0 = max_add<T, SR>(m0, d0[v].y, nout[v].y);
+          m0 = max_add<T, SR>(m0, d0[v].z, nout[v].z); m0 = max_add<T, SR>(m0, d0[v].w, nout[v].w);
+          m1 = max_add<T, SR>(m1, d1[v].x, nout[v].x); m1 = max_add<T, SR>(m1, d1[v].y, nout[v].y);
+          m1 = max_add<T, SR>(m1, d1[v].z, nout[v].z); m1 = max_add<T, SR>(m1, d1[v].w, nout[v].w);
+          colp[v].x = Tr<T, SR>::relax(Tr<T, SR>::relax(colp[v].x, o0, d0[v].x), o1, d1[v].x);
+          colp[v].y = Tr<T, SR>::relax(Tr<T, SR>::relax(colp[v].y, o0, d0[v].y), o1, d1[v].y);
+          colp[v].z = Tr<T, SR>::relax(Tr<T, SR>::relax(colp[v].z, o0, d0[v].z), o1, d1[v].z);
+          colp[v].w = Tr<T, SR>::relax(Tr<T, SR>::relax(colp[v].w, o0, d0[v].w), o1, d1[v].w);
         }
-      }
-      const T o0 = ow[i];
-      const T o1 = two ? ow[i + 1] : I;
-      T p0 = I, p1 = I, m0 = NI, m1 = NI;
-#pragma unroll
-      for (int v = 0; v < P1_V; ++v) {
-        p0 = Tr<T, SR>::relax(p0, d0[v].x, inw[v].x); p0 = Tr<T, SR>::relax(p0, d0[v].y, inw[v].y);
-        p0 = Tr<T, SR>::relax(p0, d0[v].z, inw[v].z); p0 = Tr<T, SR>::relax(p0, d0[v].w, inw[v].w);
-        p1 = Tr<T, SR>::relax(p1, d1[v].x, inw[v].x); p1 = Tr<T, SR>::relax(p1, d1[v].y, inw[v].y);
-        p1 = Tr<T, SR>::relax(p1, d1[v].z, inw[v].z); p1 = Tr<T, SR>::relax(p1, d1[v].w, inw[v].w);
-        m0 = max_add<T, SR>(m0, d0[v].x, nout[v].x); m0 = max_add<T, SR>(m0, d0[v].y, nout[v].y);
-        m0 = max_add<T, SR>(m0, d0[v].z, nout[v].z); m0 = max_add<T, SR>(m0, d0[v].w, nout[v].w);
-        m1 = max_add<T, SR>(m1, d1[v].x, nout[v].x); m1 = max_add<T, SR>(m1, d1[v].y, nout[v].y);
-        m1 = max_add<T, SR>(m1, d1[v].z, nout[v].z); m1 = max_add<T, SR>(m1, d1[v].w, nout[v].w);
-        colp[v].x = Tr<T, SR>::relax(Tr<T, SR>::relax(colp[v].x, o0, d0[v].x), o1, d1[v].x);
-        colp[v].y = Tr<T, SR>::relax(Tr<T, SR>::relax(colp[v].y, o0, d0[v].y), o1, d1[v].y);
-        colp[v].z = Tr<T, SR>::relax(Tr<T, SR>::relax(colp[v].z, o0, d0[v].z), o1, d1[v].z);
-        colp[v].w = Tr<T, SR>::relax(Tr<T, SR>::relax(colp[v].w, o0, d0[v].w), o1, d1[v].w);
-      }
-      rp[rr][lane] = p0;
-      rm[rr][lane] = m0;
-      if (two) { rp[rr + 1][lane] = p1; rm[rr + 1][lane] = m1; }
-    };
-    if (m16) {
-      // the int16 mirror: 16-byte loads of 8 columns, four rows in flight
-      // (the same bytes in flight per lane as two int32 rows)
-      const uint4 sat = make_uint4(0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu);
-      for (int rr = 0; rr < nb; rr += 4) {
-        uint4 w[4][P1_V / 2];
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const uint16_t* mrow = mm + (b0 + rr + h - r.row0) * ld;
-#pragma unroll
-          for (int q = 0; q < P1_V / 2; ++q)
-            w[h][q] = (rr + h < nb && qv[2 * q] < tl.n4) ? mload8(mrow + 4 * qv[2 * q]) : sat;
-        }
-#pragma unroll
-        for (int hh = 0; hh < 4; hh += 2) {
-          if (rr + hh < nb) {
-            Vec4<T> d0[P1_V], d1[P1_V];
-#pragma unroll
-            for (int q = 0; q < P1_V / 2; ++q) {
-              d0[2 * q] = mconv4<T>(make_uint2(w[hh][q].x, w[hh][q].y));
-              d0[2 * q + 1] = mconv4<T>(make_uint2(w[hh][q].z, w[hh][q].w));
-              d1[2 * q] = mconv4<T>(make_uint2(w[hh + 1][q].x, w[hh + 1][q].y));
-              d1[2 * q + 1] = mconv4<T>(make_uint2(w[hh + 1][q].z, w[hh + 1][q].w));
+        rp[rr][lane] = p0;
+        rm[rr][lane] = m0;
+        if (two) { rp[rr + 1][lane] = p1; rm[rr + 1][lane] = m1; }
+      };
+      if (m16) {
+        // the int16 mirror: 16-byte loads of 8 columns, four rows in flight
+        // (the same bytes in flight per lane as two int32 rows)
+        const uint4 sat = make_uint4(0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu);
+        for (int rr = 0; rr < nb; rr += 4) {
+          uint4 w[4][P1_V / 2];
+  #pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const uint16_t* mrow = mm + (b0 + rr + h - r.row0) * ld;
+  #pragma unroll
+            for (int q = 0; q < P1_V / 2; ++q)
+              w[h][q] = (rr + h < nb && qv[2 * q] < tl.n4) ? mload8(mrow + 4 * qv[2 * q]) : sat;
+          }
+  #pragma unroll
+          for (int hh = 0; hh < 4; hh += 2) {
+            if (rr + hh < nb) {
+              Vec4<T> d0[P1_V], d1[P1_V];
+  #pragma unroll
+              for (int q = 0; q < P1_V / 2; ++q) {
+                d0[2 * q] = mconv4<T>(make_uint2(w[hh][q].x, w[hh][q].y));
+                d0[2 * q + 1] = mconv4<T>(make_uint2(w[hh][q].z, w[hh][q].w));
+                d1[2 * q] = mconv4<T>(make_uint2(w[hh + 1][q].x, w[hh + 1][q].y));
+                d1[2 * q + 1] = mconv4<T>(make_uint2(w[hh + 1][q].z, w[hh + 1][q].w));
+              }
+  #pragma unroll
+              for (int v = 0; v < P1_V; ++v)
+                if (qv[v] >= tl.n4) { d0[v] = Vec4<T>{I, I, I, I}; d1[v] = Vec4<T>{I, I, I, I}; }
+              body(d0, d1, rr + hh, rr + hh + 1 < nb);
             }
-#pragma unroll
-            for (int v = 0; v < P1_V; ++v)
-              if (qv[v] >= tl.n4) { d0[v] = Vec4<T>{I, I, I, I}; d1[v] = Vec4<T>{I, I, I, I}; }
-            body(d0, d1, rr + hh, rr + hh + 1 < nb);
+          }
+        }
+      } else {
+        for (int rr = 0; rr < nb; rr += 2) {
+          const bool two = rr + 1 < nb;
+          const T* row0 = D + (b0 + rr - r.row0) * ld;
+          const T* row1 = row0 + ld;
+          Vec4<T> d0[P1_V], d1[P1_V];
+          // issue every load of both rows before touching any result (MLP = 2*P1_V)
+  #pragma unroll
+          for (int v = 0; v < P1_V; ++v) {
+            d0[v] = Vec4<T>{I, I, I, I};
+            d1[v] = Vec4<T>{I, I, I, I};
+            if (qv[v] < tl.n4) {
+              d0[v] = ld4_stream<T>(row0 + 4 * qv[v]);
+              if (two) d1[v] = ld4_stream<T>(row1 + 4 * qv[v]);
+            }
+          }
+          body(d0, d1, rr, two);
+        }
+      }
+      __syncwarp();
+      {
+        const int row = lane & (P1_RB - 1);
+        if (row < nb) {
+          if (lane < P1_RB) {
+            T m = rp[row][0];
+  #pragma unroll 8
+            for (int t = 1; t < 32; ++t) m = Tr<T>::mn(m, rp[row][t]);
+            rowpart[(int64_t)chunk * part_ld + b0 + row] = m;
+          } else {
+            T m = rm[row][0];
+  #pragma unroll 8
+            for (int t = 1; t < 32; ++t) m = Tr<T>::kFloat ? fmaxf(m, rm[row][t]) : max(m, rm[row][t]);
+            rowpartM[(int64_t)chunk * part_ld + b0 + row] = m;
           }
         }
       }
-    } else {
-      for (int rr = 0; rr < nb; rr += 2) {
-        const bool two = rr + 1 < nb;
-        const T* row0 = D + (b0 + rr - r.row0) * ld;
-        const T* row1 = row0 + ld;
-        Vec4<T> d0[P1_V], d1[P1_V];
-        // issue every load of both rows before touching any result (MLP = 2*P1_V)
-#pragma unroll
-        for (int v = 0; v < P1_V; ++v) {
-          d0[v] = Vec4<T>{I, I, I, I};
-          d1[v] = Vec4<T>{I, I, I, I};
-          if (qv[v] < tl.n4) {
-            d0[v] = ld4_stream<T>(row0 + 4 * qv[v]);
-            if (two) d1[v] = ld4_stream<T>(row1 + 4 * qv[v]);
-          }
-        }
-        body(d0, d1, rr, two);
-      }
+      __syncwarp();
     }
-    __syncwarp();
-    {
-      const int row = lane & (P1_RB - 1);
-      if (row < nb) {
-        if (lane < P1_RB) {
-          T m = rp[row][0];
-#pragma unroll 8
-          for (int t = 1; t < 32; ++t) m = Tr<T>::mn(m, rp[row][t]);
-          rowpart[(int64_t)chunk * part_ld + b0 + row] = m;
-        } else {
-          T m = rm[row][0];
-#pragma unroll 8
-          for (int t = 1; t < 32; ++t) m = Tr<T>::kFloat ? fmaxf(m, rm[row][t]) : max(m, rm[row][t]);
-          rowpartM[(int64_t)chunk * part_ld + b0 + row] = m;
-        }
-      }
-    }
-    __syncwarp();
+  #pragma unroll
+    for (int v = 0; v < P1_V; ++v)
+      if (qv[v] < tl.n4) st4<T>(colpart + (int64_t)slab * part_ld + 4 * qv[v], colp[v]);
   }
-#pragma unroll
-  for (int v = 0; v < P1_V; ++v)
-    if (qv[v] < tl.n4) st4<T>(colpart + (int64_t)slab * part_ld + 4 * qv[v], colp[v]);
 }
 
 template <typename T>
@@ -1175,8 +1178,8 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
     k_addnode_pass1_p16<T><<<grid, 256, 0, st>>>(r, ld, n, tl, ow, iw, rowpart, rowpartM, colpart,
                                                     part_ld, M);
   else   // int32 (exits if the packed pass ran and came out certain)
-    k_addnode_pass1<T, 0><<<grid, 256, 0, st>>>(D, ld, r, n, tl, ow, iw, rowpart, rowpartM, colpart,
-                                                part_ld, M, uncertain);
+    k_addnode_pass1<T, 0><<<uncertain ? std::min(grid, 2 * num_sms()) : grid, 256, 0, st>>>(
+        D, ld, r, n, tl, ow, iw, rowpart, rowpartM, colpart, part_ld, M, uncertain);
   return cudaGetLastError();
 }
 
@@ -1258,7 +1261,7 @@ cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, cons
                            const unsigned* row_full, const unsigned* col_full) {
   const int64_t ti = cdiv(std::max<int64_t>(r.hi - r.lo, 0), 32), tj = cdiv(npad, 32);
   if (ti + tj == 0) return cudaSuccess;
-  k_addnode_finish<T><<<(unsigned)std::min<int64_t>(ti + tj, 4 * num_sms()), 256, 0, st>>>(rowpart, rowpartM, nchunk, colpart, nslab,
+  k_addnode_finish<T><<<(unsigned)std::min<int64_t>(ti + tj, (gate == 2 ? 1 : 4) * num_sms()), 256, 0, st>>>(rowpart, rowpartM, nchunk, colpart, nslab,
                                                            part_ld, r, n, npad, ti, col, ceff, row,
                                                            gate, M, uncertain, row_full, col_full);
   return cudaGetLastError();

@@ -553,6 +553,13 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_a(T* D, int64_t l
   const int lane = threadIdx.x & 31;
   unsigned mbits = 0;   // mirror flag bits raised by this thread's writes
   npairs = device_count(dc, npairs, 0);
+  // the gathers read the int8 mirror while it is valid (exact; a quarter of
+  // the bytes).  An entry this kernel rewrites meanwhile reads as its old
+  // value (stale: skipped by the test below), its new final value, or 0x7F
+  // (INF: skipped) if that is >= 0x7F — each case only weakens the bound.
+  const uint8_t* M8 = nullptr;
+  if constexpr (std::is_same<T, int32_t>::value && SR == 0)
+    if (M.m8 && (*(volatile unsigned*)M.flag & 1u) == 0u) M8 = M.m8;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < npairs;
        base += stride) {
@@ -564,6 +571,7 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_a(T* D, int64_t l
       i = srow[p];
       j = scol[p];
       T* Drow = D + (i - row0) * ld;
+      const uint8_t* Mrow = M8 ? M8 + (i - row0) * ld : nullptr;
       const int4* sid = reinterpret_cast<const int4*>(SLid + j * kSL);
       const int4* sw = reinterpret_cast<const int4*>(SLw + j * kSL);
       lb = *(volatile T*)(Drow + j);   // D_old[i][j]
@@ -585,7 +593,12 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_a(T* D, int64_t l
           for (int q = 0; q < 8; ++q) {
             if (q < q0 || q >= q1) continue;
             const int mq = m[q] >= 0 ? m[q] : 0;
-            dv[q] = m[q] >= 0 ? *(volatile const T*)(Drow + mq) : Tr<T>::inf();
+            if (Mrow) {
+              const int32_t b8 = Mrow[mq];
+              dv[q] = (m[q] >= 0 && b8 != kSat8i) ? (T)b8 : Tr<T>::inf();
+            } else {
+              dv[q] = m[q] >= 0 ? *(volatile const T*)(Drow + mq) : Tr<T>::inf();
+            }
             rv[q] = r1[mq];
             if (TWO) rv2[q] = r2[mq];
           }

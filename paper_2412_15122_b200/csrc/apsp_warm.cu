@@ -803,11 +803,16 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   // valid as read above): on the side stream, under pass 1
   bool srow = false;
   // (small graphs: the one streaming pass costs less than the shortcuts' extra launches)
-  if constexpr (std::is_same<T, int32_t>::value) srow = h->world == 1 && n >= kAddShortcutMinN && mirror8_known_valid(h);
+  if constexpr (std::is_same<T, int32_t>::value)
+    srow = h->world == 1 && n >= kAddShortcutMinN && h->plan.maxchunk >= 2 && mirror8_known_valid(h);
   if constexpr (std::is_same<T, int32_t>::value) {
     if (srow) {
+      // scratch: the (value, minimiser) row and the minimiser flags live in the
+      // pass-1 partial buffer (unused unless the gathers fall back to pass 1,
+      // which runs after they are consumed)
       CK2(addrow_s(as, ow, n, h->mirror<T>().m8, ld, h->row0, row, ld, reinterpret_cast<int*>(h->vec<T>(5)),
-                   h->st2));
+                   reinterpret_cast<unsigned long long*>(h->rowpart<T>()),
+                   reinterpret_cast<int*>(h->rowpart<T>()) + 2 * ld, h->st2));
       CKR(cudaEventRecord(h->ev_row, h->st2));
     }
   }
@@ -832,8 +837,9 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
       if (srow) {   // the new row first (side stream), then col / the skip bound by gathers
         CKR(cudaStreamWaitEvent(h->st, h->ev_row, 0));
         PK(APSP_K_ADD_PASS1, 0.0,
-           addcol_g(as, r, h->mirror<T>().m8, ld, n, iw, ow, reinterpret_cast<int*>(h->vec<T>(5)), kAddColLimit,
-                    col, ceff, h->vec<T>(6), reinterpret_cast<int*>(h->vec<T>(7)), h->st));
+           addcol_g(as, r, h->mirror<T>().m8, ld, n, iw, ow, reinterpret_cast<int*>(h->rowpart<T>()) + 2 * ld,
+                    reinterpret_cast<int*>(h->vec<T>(5)), kAddColLimit, col, ceff, h->vec<T>(6),
+                    reinterpret_cast<int*>(h->vec<T>(7)), h->st));
         cfull = as.ufull;
       }
     }

@@ -98,11 +98,12 @@ struct AddScratch {
 };
 cudaError_t add_init(const AddScratch& a, unsigned* err, unsigned* wmin, cudaStream_t st);
 cudaError_t addrow_s(const AddScratch& a, const int32_t* ow, int64_t n, const uint8_t* m8, int64_t ld, int64_t row0,
-                     int32_t* row, int64_t npad, int* slist, cudaStream_t st);
+                     int32_t* row, int64_t npad, int* slist, unsigned long long* packed, int* tflag,
+                     cudaStream_t st);
 // *a.ufull = 1 when |U| exceeded `limit`: pass 1 + the finish kernel compute col instead
 cudaError_t addcol_g(const AddScratch& a, Rows r, const uint8_t* m8, int64_t ld, int64_t n, const int32_t* iw,
-                     const int32_t* ow, int* ulist, int limit, int32_t* col, int32_t* ceff, int32_t* mprime,
-                     int* fb_list, cudaStream_t st);
+                     const int32_t* ow, const int* tflag, int* ulist, int limit, int32_t* col, int32_t* ceff,
+                     int32_t* mprime, int* fb_list, cudaStream_t st);
 template <typename T>
 cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
                            int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,

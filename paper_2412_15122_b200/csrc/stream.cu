@@ -805,12 +805,14 @@ __global__ void __launch_bounds__(1024) k_addrow_bound(AddScratch a, const uint8
     if (threadIdx.x == 0) *a.rb = mx >= kSat8i ? I - 1 : omin + mx;
   }
 }
-// S = {t : out[t] <= Rb}; row := INF
+// S = {t : out[t] <= Rb}; the packed (value, minimiser) row := none; the
+// minimiser flags := 0
 __global__ void k_addrow_compact(AddScratch a, const int32_t* __restrict__ ow, int64_t n, int64_t npad, int* slist,
-                                 int32_t* row) {
-  const int32_t rb = *a.rb, I = APSP_INF_I32_DEV;
+                                 unsigned long long* packed, int* tflag) {
+  const int32_t rb = *a.rb;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < npad; t += (int64_t)gridDim.x * blockDim.x) {
-    row[t] = I;
+    packed[t] = ~0ull;
+    tflag[t] = 0;
     if (t < n && ow[t] <= rb) slist[atomicAdd(a.s_count, 1)] = (int)t;
   }
 }
@@ -819,13 +821,14 @@ __global__ void k_addrow_compact(AddScratch a, const int32_t* __restrict__ ow, i
 __global__ void __launch_bounds__(256) k_addrow(const int32_t* __restrict__ ow, const int* __restrict__ slist,
                                                 const int* __restrict__ scount,
                                                 const uint8_t* __restrict__ m8, int64_t ld, int64_t row0,
-                                                int64_t n, int32_t* row) {
+                                                int64_t n, unsigned long long* packed) {
   const int cnt = *scount;
   const int64_t j0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
   if (j0 >= n) return;
   const int s0 = (int)((int64_t)cnt * blockIdx.y / gridDim.y), s1 = (int)((int64_t)cnt * (blockIdx.y + 1) / gridDim.y);
   const int32_t I = APSP_INF_I32_DEV;
   int32_t acc[4] = {I, I, I, I};
+  int tt[4] = {0, 0, 0, 0};
 #pragma unroll 4
   for (int s = s0; s < s1; ++s) {
     const int t = slist[s];
@@ -834,12 +837,26 @@ __global__ void __launch_bounds__(256) k_addrow(const int32_t* __restrict__ ow, 
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int32_t d = (int32_t)((w >> (8 * e)) & 0xFFu);
-      if (d != kSat8i) acc[e] = min(acc[e], o + d);
+      if (d != kSat8i && o + d < acc[e]) { acc[e] = o + d; tt[e] = t; }
     }
   }
 #pragma unroll
-  for (int e = 0; e < 4; ++e)
-    if (j0 + e < n && acc[e] < I) atomicMin(row + j0 + e, acc[e]);
+  for (int e = 0; e < 4; ++e)   // (value, minimiser): the min value, any minimiser
+    if (j0 + e < n && acc[e] < I)
+      atomicMin(packed + j0 + e, (unsigned long long)(unsigned)acc[e] << 32 | (unsigned)tt[e]);
+}
+// row[j] := the min; the minimisers T* = {t*(j)} are flagged for the gathers
+__global__ void k_addrow_final(const unsigned long long* __restrict__ packed, int64_t npad, int32_t* row,
+                               int* tflag) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npad; j += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long v = packed[j];
+    if (v == ~0ull) {
+      row[j] = APSP_INF_I32_DEV;
+    } else {
+      row[j] = (int32_t)(v >> 32);
+      tflag[(int)(v & 0xFFFFFFFFull)] = 1;
+    }
+  }
 }
 // ---------------------------------------------------------------------------
 // The new column and the row-skip bound of an add by gathers instead of a
@@ -848,27 +865,26 @@ __global__ void __launch_bounds__(256) k_addrow(const int32_t* __restrict__ ow, 
 //     bound col1[i]; if col1[i] <= th2 (the smallest in[t] above th), no t
 //     outside S1 can do better (D >= 0): exact.  Rows not certified get a
 //     full-row scan (k_addcol_rows).  th = min in + 2.
-//   M'[i] = max_{t in S2} D[i][t] - out[t], S2 = {t : out[t] <= R}, R = max_j
-//     row[j] (the new row, computed first): a change at (i, j) needs col[i] <
-//     D[i][t*] - out[t*] for the t* attaining row[j], and out[t*] <= row[j]
-//     <= R — so rows with col[i] >= M'[i] do not change.
-// Both sets are gathered together: U = S1 u S2 (an extra candidate never
+//   M'[i] = max_{t in T*} D[i][t] - out[t], T* = one minimiser t*(j) of each
+//     new-row entry (recorded by k_addrow): a change at (i, j) needs col[i] <
+//     D[i][t*] - out[t*] for a t* attaining row[j] — so rows with col[i] >=
+//     M'[i] do not change.
+// Both sets are gathered together: U = S1 u T* (an extra candidate never
 // breaks either bound).  If |U| > limit, *ufull is set and the streaming
 // pass 1 does it instead.
 // ---------------------------------------------------------------------------
-// U = {t : in[t] <= th || out[t] <= R}, th = min in + delta; th2 = the
+// U = {t : in[t] <= th || t in T*}, th = min in + delta; th2 = the
 // smallest in[t] above th (the certification threshold of col1)
-__global__ void k_addcol_sets(AddScratch a, const int32_t* __restrict__ iw, const int32_t* __restrict__ ow,
+__global__ void k_addcol_sets(AddScratch a, const int32_t* __restrict__ iw, const int* __restrict__ tflag,
                               int64_t n, int delta, int* ulist, int limit) {
   const int32_t I = APSP_INF_I32_DEV;
   const unsigned imn = *a.in_min;
   const int32_t th = imn >= (unsigned)I ? I : min(I - 1, (int32_t)imn + delta);
-  const int32_t R = *a.rmax;
   int32_t t2 = 0x7F7F7F7F;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t x = iw[t], y = ow[t];
+    const int32_t x = iw[t];
     if (x > th && x < t2) t2 = x;
-    if (x <= th || y <= R) {
+    if (x <= th || tflag[t]) {
       const int q = atomicAdd(a.u_count, 1);
       if (q < limit) ulist[q] = (int)t;
     }
@@ -949,11 +965,11 @@ __global__ void __launch_bounds__(256) k_addcol_rows(AddScratch a, Rows r, const
   }
 }
 cudaError_t addcol_g(const AddScratch& a, Rows r, const uint8_t* m8, int64_t ld, int64_t n, const int32_t* iw,
-                     const int32_t* ow, int* ulist, int limit, int32_t* col, int32_t* ceff, int32_t* mprime,
-                     int* fb_list, cudaStream_t st) {
+                     const int32_t* ow, const int* tflag, int* ulist, int limit, int32_t* col, int32_t* ceff,
+                     int32_t* mprime, int* fb_list, cudaStream_t st) {
   const int g = (int)std::min<int64_t>(cdiv(n, 256), 2 * num_sms());
   static const int delta = tune_wps("APSP_TUNE_ADDCOL_DELTA", 2);   // th = min in + delta (measured)
-  k_addcol_sets<<<g, 256, 0, st>>>(a, iw, ow, n, delta, ulist, limit);
+  k_addcol_sets<<<g, 256, 0, st>>>(a, iw, tflag, n, delta, ulist, limit);
   CUDA_TRY(cudaGetLastError());
   if (r.hi > r.lo) {
     const int grid = (int)std::min<int64_t>(cdiv(r.hi - r.lo, 8), (int64_t)num_sms() * 16);
@@ -964,25 +980,18 @@ cudaError_t addcol_g(const AddScratch& a, Rows r, const uint8_t* m8, int64_t ld,
   return cudaGetLastError();
 }
 
-// max finite entry of the new row (the S2 bound of the gathers)
-__global__ void k_row_max(const int32_t* __restrict__ row, int64_t n, int* rmax) {
-  int32_t m = 0;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
-    if (row[j] < APSP_INF_I32_DEV) m = max(m, row[j]);
-  m = __reduce_max_sync(0xffffffffu, m);
-  if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(rmax, m);
-}
 cudaError_t addrow_s(const AddScratch& a, const int32_t* ow, int64_t n, const uint8_t* m8, int64_t ld, int64_t row0,
-                     int32_t* row, int64_t npad, int* slist, cudaStream_t st) {
+                     int32_t* row, int64_t npad, int* slist, unsigned long long* packed, int* tflag,
+                     cudaStream_t st) {
   k_addrow_bound<<<1, 1024, 0, st>>>(a, m8, ld, row0, n);
   CUDA_TRY(cudaGetLastError());
   const int g = (int)std::min<int64_t>(cdiv(npad, 256), 2 * num_sms());
-  k_addrow_compact<<<g, 256, 0, st>>>(a, ow, n, npad, slist, row);
+  k_addrow_compact<<<g, 256, 0, st>>>(a, ow, n, npad, slist, packed, tflag);
   CUDA_TRY(cudaGetLastError());
   const dim3 grid((unsigned)cdiv(cdiv(n, 4), 256), 16);
-  k_addrow<<<grid, 256, 0, st>>>(ow, slist, a.s_count, m8, ld, row0, n, row);
+  k_addrow<<<grid, 256, 0, st>>>(ow, slist, a.s_count, m8, ld, row0, n, packed);
   CUDA_TRY(cudaGetLastError());
-  k_row_max<<<(int)std::min<int64_t>(cdiv(n, 256), 2 * num_sms()), 256, 0, st>>>(row, n, a.rmax);
+  k_addrow_final<<<g, 256, 0, st>>>(packed, npad, row, tflag);
   return cudaGetLastError();
 }
 

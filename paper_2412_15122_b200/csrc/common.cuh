@@ -162,10 +162,7 @@ __device__ __forceinline__ Vec4<T> mask_tail(Vec4<T> v, int64_t col0, int64_t n)
 // ---------------------------------------------------------------------------
 constexpr int32_t kSat16i = 0x3FFF;
 __device__ __forceinline__ uint16_t sat16(int32_t v) { return (uint16_t)min(v, kSat16i); }
-// 4 mirrored values: an 8-byte streaming load, then (separately, so that every
-// load of a batch is issued before the first result is waited for) the
-// conversion that reads 0x3FFF back as INF
-// 8 mirrored values in one 16-byte streaming load (two Vec4 worth)
+// 8 int16 mirrored values (or 16 int8 ones) in one 16-byte streaming load
 __device__ __forceinline__ uint4 mload8(const uint16_t* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -181,14 +178,9 @@ __device__ __forceinline__ int64_t group_of(bool m16, int chunk, int v, int lane
   return m16 ? 2 * ((int64_t)chunk * 64 + (v >> 1) * 32 + lane) + (v & 1)
              : (int64_t)chunk * 128 + v * 32 + lane;
 }
-// int8 mirror: 8 values in one 8-byte streaming load, widened to the int16x2
-// words the packed arithmetic uses (halves 0..0x7F)
+// int8 mirror: 8 values widened to the int16x2 words the packed arithmetic
+// uses (halves 0..0x7F)
 constexpr int32_t kSat8i = 0x7F;
-__device__ __forceinline__ uint2 mload8b(const uint8_t* p) {
-  uint2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
-  return r;
-}
 __device__ __forceinline__ uint4 widen8(uint2 b) {
   return make_uint4(__byte_perm(b.x, 0u, 0x4140), __byte_perm(b.x, 0u, 0x4342),
                     __byte_perm(b.y, 0u, 0x4140), __byte_perm(b.y, 0u, 0x4342));
@@ -199,58 +191,10 @@ __device__ __forceinline__ uint32_t inf8to16(uint32_t x) {
   const uint32_t nz = (t | ((t & 0x7FFF7FFFu) + 0x7FFF7FFFu)) & 0x80008000u;
   return x | (((~nz & 0x80008000u) >> 15) * 0x3FFFu);
 }
-__device__ __forceinline__ uint2 mload4(const uint16_t* p) {
-  uint2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
-  return r;
-}
-template <typename T>
-__device__ __forceinline__ Vec4<T> mconv4(uint2 r) {
-  auto cv = [](unsigned x) -> T { return x == (unsigned)kSat16i ? Tr<T>::inf() : (T)x; };
-  return Vec4<T>{cv(r.x & 0xFFFFu), cv(r.x >> 16), cv(r.y & 0xFFFFu), cv(r.y >> 16)};
-}
 
-// ---------------------------------------------------------------------------
-// mbarrier + bulk copy (cp.async.bulk, the 1-D TMA path: UBLKCP) for the
-// streaming kernels' shared-memory rings
-// ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// global -> shared bulk copy of `bytes` (multiple of 16, both ends 16-byte
-// aligned); completes `bytes` of the barrier's transaction count
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
 // per-thread async copies (LDGSTS): 16 bytes global -> shared, no registers
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");

@@ -1005,7 +1005,6 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
   // The packed pass (k_addnode_pass1_p16) handled this add unless the mirror
   // is invalid, the algebra is minimax, or a result came out >= 0x3FFF.
   if (pass1_packed_done<T, SR>(M, uncertain)) return;
-  const uint16_t* mm = nullptr;
   const bool m16 = false;
   __shared__ T rp_all[8][2][P1_RB][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1070,55 +1069,22 @@ __global__ void __launch_bounds__(256, 2) k_addnode_pass1(const T* __restrict__ 
         rm[rr][lane] = m0;
         if (two) { rp[rr + 1][lane] = p1; rm[rr + 1][lane] = m1; }
       };
-      if (m16) {
-        // the int16 mirror: 16-byte loads of 8 columns, four rows in flight
-        // (the same bytes in flight per lane as two int32 rows)
-        const uint4 sat = make_uint4(0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu, 0x3FFF3FFFu);
-        for (int rr = 0; rr < nb; rr += 4) {
-          uint4 w[4][P1_V / 2];
-  #pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const uint16_t* mrow = mm + (b0 + rr + h - r.row0) * ld;
-  #pragma unroll
-            for (int q = 0; q < P1_V / 2; ++q)
-              w[h][q] = (rr + h < nb && qv[2 * q] < tl.n4) ? mload8(mrow + 4 * qv[2 * q]) : sat;
-          }
-  #pragma unroll
-          for (int hh = 0; hh < 4; hh += 2) {
-            if (rr + hh < nb) {
-              Vec4<T> d0[P1_V], d1[P1_V];
-  #pragma unroll
-              for (int q = 0; q < P1_V / 2; ++q) {
-                d0[2 * q] = mconv4<T>(make_uint2(w[hh][q].x, w[hh][q].y));
-                d0[2 * q + 1] = mconv4<T>(make_uint2(w[hh][q].z, w[hh][q].w));
-                d1[2 * q] = mconv4<T>(make_uint2(w[hh + 1][q].x, w[hh + 1][q].y));
-                d1[2 * q + 1] = mconv4<T>(make_uint2(w[hh + 1][q].z, w[hh + 1][q].w));
-              }
-  #pragma unroll
-              for (int v = 0; v < P1_V; ++v)
-                if (qv[v] >= tl.n4) { d0[v] = Vec4<T>{I, I, I, I}; d1[v] = Vec4<T>{I, I, I, I}; }
-              body(d0, d1, rr + hh, rr + hh + 1 < nb);
-            }
+      for (int rr = 0; rr < nb; rr += 2) {
+        const bool two = rr + 1 < nb;
+        const T* row0 = D + (b0 + rr - r.row0) * ld;
+        const T* row1 = row0 + ld;
+        Vec4<T> d0[P1_V], d1[P1_V];
+        // issue every load of both rows before touching any result (MLP = 2*P1_V)
+#pragma unroll
+        for (int v = 0; v < P1_V; ++v) {
+          d0[v] = Vec4<T>{I, I, I, I};
+          d1[v] = Vec4<T>{I, I, I, I};
+          if (qv[v] < tl.n4) {
+            d0[v] = ld4_stream<T>(row0 + 4 * qv[v]);
+            if (two) d1[v] = ld4_stream<T>(row1 + 4 * qv[v]);
           }
         }
-      } else {
-        for (int rr = 0; rr < nb; rr += 2) {
-          const bool two = rr + 1 < nb;
-          const T* row0 = D + (b0 + rr - r.row0) * ld;
-          const T* row1 = row0 + ld;
-          Vec4<T> d0[P1_V], d1[P1_V];
-          // issue every load of both rows before touching any result (MLP = 2*P1_V)
-  #pragma unroll
-          for (int v = 0; v < P1_V; ++v) {
-            d0[v] = Vec4<T>{I, I, I, I};
-            d1[v] = Vec4<T>{I, I, I, I};
-            if (qv[v] < tl.n4) {
-              d0[v] = ld4_stream<T>(row0 + 4 * qv[v]);
-              if (two) d1[v] = ld4_stream<T>(row1 + 4 * qv[v]);
-            }
-          }
-          body(d0, d1, rr, two);
-        }
+        body(d0, d1, rr, two);
       }
       __syncwarp();
       {

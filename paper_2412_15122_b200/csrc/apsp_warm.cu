@@ -661,7 +661,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
          sparse_round<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->gprow(), h->gpcol(),
                          h->glb<T>(), ocap, h->rowoff(), fin_c, rounds == 0 ? nullptr : fin_c + h->cap,
                          fin_l, h->chg(o), h->chg(o) + h->cap, fcol[rounds & 1], h->anyflag(), h->sr, h->ctr(),
-                         h->st, reinterpret_cast<unsigned*>(h->anyrow()), h->wmin<T>()));
+                         h->st, reinterpret_cast<unsigned*>(h->anyrow()), h->wmin<T>(), h->mirror<T>()));
       last_total = h->chg(o) + h->cap;
     }
     return APSP_OK;
@@ -675,7 +675,8 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
                          h->glb<T>(), h->gfull(), ocap, h->ctr(), h->sr, h->mirror<T>(), h->st));
     // A2: whole-shortlist pass over the open pairs, now that certified values are final
     CK(sparse_short<T>(h->Dl<T>(), h->ld, h->row0, h->slid(), h->slw<T>(), h->wnext<T>(), h->gprow(),
-                       h->gpcol(), h->glb<T>(), ocap, h->gfull(), 1, h->sr, h->ctr(), h->st));
+                       h->gpcol(), h->glb<T>(), ocap, h->gfull(), 1, h->sr, h->ctr(), h->st, h->mirror<T>(),
+                       removal ? skip : -1));
     // the removal's shortlist upkeep needs nothing after A2 (the last reader of
     // SL): it runs on the side stream, joined before the update returns
     if (removal) {
@@ -685,7 +686,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     // B: full O(n) scan for the pairs the shortlist could not settle
     PK(APSP_K_SPARSE_R, 0.0,
        sparse_full<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, n, h->gprow(), h->gpcol(),
-                      h->glb<T>(), h->gfull(), ocap, h->sr, h->ctr(), h->st));
+                      h->glb<T>(), h->gfull(), ocap, h->sr, h->ctr(), h->st, h->mirror<T>()));
     CK(open_rowmin<T>(h->Dl<T>(), h->ld, h->row0, h->gprow(), h->gpcol(), ocap,
                       reinterpret_cast<unsigned*>(h->anyrow()), h->ctr(), h->st));
     // rounds over the open entries of each row, a first batch of 4
@@ -754,9 +755,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     return fw_impl<T>(h, removal ? skip : -1);
   }
   if (info) info->path = 2;
-  if (total > 0)   // phase A mirrored its final values; A2 / B / the rounds changed open pairs only
-    CK(mirror_pairs(h->Dl<T>(), h->ld, h->row0, h->gprow(), h->gpcol(), h->ctr(), ocap, 1, h->mirror<T>(),
-                    h->st));
+  // (the sparse kernels mirrored every value they wrote)
   return APSP_OK;
 }
 

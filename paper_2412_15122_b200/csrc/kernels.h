@@ -183,7 +183,8 @@ cudaError_t shortlist_remove(int* SLid, T* SLw, T* wnext, int64_t n, int64_t k, 
 template <typename T>
 cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const T* SLw,
                          const T* wnext, const int* prow, const int* pcol, const T* plb,
-                         int64_t npairs, unsigned char* out, int classify, int sr, const DetectCounters* dc, cudaStream_t st);
+                         int64_t npairs, unsigned char* out, int classify, int sr, const DetectCounters* dc, cudaStream_t st,
+                         Mirror M = Mirror{nullptr, nullptr, nullptr}, int64_t skip = -1);
 template <typename T>
 cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* SLw,
                            const int64_t* rowoff, const int* srow, const int* scol, int64_t npairs,
@@ -193,13 +194,15 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
 template <typename T>
 cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
                         const int* gprow, const int* gpcol, const T* glb, const unsigned char* gfull,
-                        int64_t nopen, int sr, const DetectCounters* dc, cudaStream_t st);
+                        int64_t nopen, int sr, const DetectCounters* dc, cudaStream_t st,
+                        Mirror M = Mirror{nullptr, nullptr, nullptr});
 template <typename T>
 cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw,
                          const int* gprow, const int* gpcol, const T* glb, int64_t nopen,
                          const int64_t* rowoff, const int* fcnt_in, const int* ftot_in, const int* fcol_in,
                          int* fcnt_out, int* ftot_out, int* fcol_out, int* any, int sr,
-                         const DetectCounters* dc, cudaStream_t st, unsigned* rowkey = nullptr, T wmin = T(0));
+                         const DetectCounters* dc, cudaStream_t st, unsigned* rowkey = nullptr, T wmin = T(0),
+                         Mirror M = Mirror{nullptr, nullptr, nullptr});
 // per-row minimum of the open pairs' current values (after A2 / B), as keys
 template <typename T>
 cudaError_t open_rowmin(const T* D, int64_t ld, int64_t row0, const int* gprow, const int* gpcol, int64_t nopen,

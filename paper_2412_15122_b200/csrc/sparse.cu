@@ -440,14 +440,23 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
                                                       const int* __restrict__ pcol,
                                                       const T* __restrict__ plb, int64_t npairs,
                                                       unsigned char* out, int classify,
-                                                      OpenLists<T> ol, const DetectCounters* dc) {
+                                                      OpenLists<T> ol, const DetectCounters* dc, Mirror M,
+                                                      int64_t skip) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   npairs = device_count(dc, npairs, classify ? 1 : 0);
+  // A2 gathers from the int8 mirror: every listed entry was mirrored by phase
+  // A (final or not, a walk length of G'), later writes are mirrored too, and
+  // 0x7F reads as INF — each value read is >= the current D entry, so e is an
+  // upper bound and e <= wnext(j) still proves no m outside SL(j) does better
+  const uint8_t* M8 = nullptr;
+  if constexpr (std::is_same<T, int32_t>::value && SR == 0) M8 = M.m8;
+  unsigned mbits = 0;
   for (int64_t p = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); p < npairs;
        p += nw) {
     const int64_t i = prow[p], j = pcol[p];
     T* Drow = D + (i - row0) * ld;
+    const uint8_t* Mrow = M8 ? M8 + (i - row0) * ld : nullptr;
     const int* sid = SLid + j * kSL;
     const T* sw = SLw + j * kSL;
     const T lbp = plb[p];
@@ -482,7 +491,14 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
         const int m = sid[q * 32 + lane];
         const T w = sw[q * 32 + lane];
         if (m >= 0) {
-          acc = Tr<T, SR>::relax(acc, *(volatile T*)(Drow + m), w);
+          T d;
+          if (Mrow) {   // (column `skip` — the removed node — is tombstoned in D, not in the mirror)
+            const int32_t b8 = Mrow[m];
+            d = (b8 == kSat8i || m == skip) ? Tr<T>::inf() : (T)b8;
+          } else {
+            d = *(volatile T*)(Drow + m);
+          }
+          acc = Tr<T, SR>::relax(acc, d, w);
           wseen = w > wseen ? w : wseen;
         }
         if ((q & 1) && q + 1 < kSLK && __any_sync(0xffffffffu, acc <= warp_max<T>(wseen))) break;
@@ -493,7 +509,10 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
       const T lb = lbp;
       const T cur = *(volatile T*)(Drow + j);
       const T v = Tr<T>::mn(acc, cur);
-      if (v < cur) Drow[j] = v;
+      if (v < cur) {
+        Drow[j] = v;
+        if (M.m || M.m8) mbits |= mput(M, (i - row0) * ld + j, v);
+      }
       unsigned char st;
       if (Tr<T>::at_lb(v, lb)) st = 0;
       else if (!classify || acc <= wnext[j]) st = 1;
@@ -502,22 +521,23 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
       if (!classify && st != 0) ol.append(i, j, lb);
     }
   }
+  if (M.m || M.m8) mirror_post(M, mbits);
 }
 
 template <typename T>
 cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const T* SLw,
                          const T* wnext, const int* prow, const int* pcol, const T* plb,
                          int64_t npairs, unsigned char* out, int classify, int sr,
-                         const DetectCounters* dc, cudaStream_t st) {
+                         const DetectCounters* dc, cudaStream_t st, Mirror M, int64_t skip) {
   if (npairs <= 0) return cudaSuccess;
   int grid = (int)std::min<int64_t>(cdiv(npairs, 8), (int64_t)num_sms() * 16);
   OpenLists<T> ol{};
   if (sr)
     k_sparse_short<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
-                                               out, classify, ol, dc);
+                                               out, classify, ol, dc, M, skip);
   else
     k_sparse_short<T, 0><<<grid, 256, 0, st>>>(D, ld, row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
-                                               out, classify, ol, dc);
+                                               out, classify, ol, dc, M, skip);
   return cudaGetLastError();
 }
 
@@ -619,8 +639,9 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_a(T* D, int64_t l
       }
       Drow[j] = acc;   // unconditionally: D_old is not an upper bound of D'
       open = !Tr<T>::at_lb(acc, lb);
-      // a final value goes to the mirror now; open ones after the last round
-      if (!open && (M.m || M.m8)) mbits |= mput(M, (i - row0) * ld + j, acc);
+      // every listed value goes to the mirror now (A2 reads it); later
+      // writes (A2, B, the rounds) are mirrored as they happen
+      if (M.m || M.m8) mbits |= mput(M, (i - row0) * ld + j, acc);
     }
     // open-pair lists: per-row slot by atomic, the global slot warp-aggregated
     const unsigned bal = __ballot_sync(0xffffffffu, open);
@@ -678,8 +699,9 @@ __global__ void __launch_bounds__(256) k_sparse_full(T* D, int64_t ld, int64_t r
                                                      const int* __restrict__ gpcol,
                                                      const T* __restrict__ glb,
                                                      const unsigned char* __restrict__ gfull,
-                                                     int64_t nopen, const DetectCounters* dc) {
+                                                     int64_t nopen, const DetectCounters* dc, Mirror M) {
   const int lane = threadIdx.x & 31;
+  unsigned mbits = 0;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t n4 = (n + 3) / 4;
   nopen = device_count(dc, nopen, 1);
@@ -713,20 +735,24 @@ __global__ void __launch_bounds__(256) k_sparse_full(T* D, int64_t ld, int64_t r
     acc = warp_min<T>(acc);
     if (lane == 0) {
       T old = Drow[j];
-      if (acc < old) Drow[j] = acc;
+      if (acc < old) {
+        Drow[j] = acc;
+        if (M.m || M.m8) mbits |= mput(M, (i - row0) * ld + j, acc);
+      }
     }
   }
+  if (M.m || M.m8) mirror_post(M, mbits);
 }
 template <typename T>
 cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
                         const int* gprow, const int* gpcol, const T* glb, const unsigned char* gfull,
-                        int64_t nopen, int sr, const DetectCounters* dc, cudaStream_t st) {
+                        int64_t nopen, int sr, const DetectCounters* dc, cudaStream_t st, Mirror M) {
   if (nopen <= 0) return cudaSuccess;
   int grid = (int)std::min<int64_t>(cdiv(nopen, 8), (int64_t)num_sms() * 8);
   if (sr)
-    k_sparse_full<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, n, gprow, gpcol, glb, gfull, nopen, dc);
+    k_sparse_full<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, n, gprow, gpcol, glb, gfull, nopen, dc, M);
   else
-    k_sparse_full<T, 0><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, n, gprow, gpcol, glb, gfull, nopen, dc);
+    k_sparse_full<T, 0><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, n, gprow, gpcol, glb, gfull, nopen, dc, M);
   return cudaGetLastError();
 }
 
@@ -778,7 +804,9 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
                                                       const int* __restrict__ ftot_in,
                                                       const int* __restrict__ fcol_in,
                                                       int* fcnt_out, int* ftot_out, int* fcol_out, int* any,
-                                                      const DetectCounters* dc, unsigned* rowkey, T wmin) {
+                                                      const DetectCounters* dc, unsigned* rowkey, T wmin,
+                                                      Mirror M) {
+  unsigned mbits = 0;
   // an empty frontier (nothing changed last round): the round is a no-op
   if (ftot_in && *(volatile const int*)ftot_in == 0) return;
   const int lane = threadIdx.x & 31;
@@ -815,19 +843,21 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
     acc = warp_min<T>(acc);
     if (lane == 0 && acc < cur) {
       Drow[j] = acc;
+      if (M.m || M.m8) mbits |= mput(M, (i - row0) * ld + j, acc);
       fcol_out[rowoff[i] + atomicAdd(fcnt_out + i, 1)] = (int)j;   // j changed: next round's frontier
       atomicAdd(ftot_out, 1);
       if (rowkey) atomicMax(rowkey + i, open_key<T>(acc));
       *any = 1;
     }
   }
+  if (M.m || M.m8) mirror_post(M, mbits);
 }
 template <typename T>
 cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw,
                          const int* gprow, const int* gpcol, const T* glb, int64_t nopen,
                          const int64_t* rowoff, const int* fcnt_in, const int* ftot_in, const int* fcol_in,
                          int* fcnt_out, int* ftot_out, int* fcol_out, int* any, int sr,
-                         const DetectCounters* dc, cudaStream_t st, unsigned* rowkey, T wmin) {
+                         const DetectCounters* dc, cudaStream_t st, unsigned* rowkey, T wmin, Mirror M) {
   if (nopen <= 0) return cudaSuccess;
   // round 0 relaxes every open pair through its row's open entries; later
   // rounds only the pairs whose row changed (often none: a small grid keeps
@@ -836,11 +866,11 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
   if (sr)
     k_sparse_round<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff,
                                                fcnt_in, ftot_in, fcol_in, fcnt_out, ftot_out, fcol_out, any,
-                                               dc, rowkey, wmin);
+                                               dc, rowkey, wmin, M);
   else
     k_sparse_round<T, 0><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff,
                                                fcnt_in, ftot_in, fcol_in, fcnt_out, ftot_out, fcol_out, any,
-                                               dc, rowkey, wmin);
+                                               dc, rowkey, wmin, M);
   return cudaGetLastError();
 }
 
@@ -856,7 +886,7 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
   template cudaError_t shortlist_remove<T>(int*, T*, T*, int64_t, int64_t, int64_t, cudaStream_t); \
   template cudaError_t sparse_short<T>(T*, int64_t, int64_t, const int*, const T*, const T*,       \
                                        const int*, const int*, const T*, int64_t, unsigned char*,  \
-                                       int, int, const DetectCounters*, cudaStream_t);            \
+                                       int, int, const DetectCounters*, cudaStream_t, Mirror, int64_t);            \
   template cudaError_t sparse_phase_a<T>(T*, int64_t, Rows, const int*, const T*, const int64_t*,  \
                                          const int*, const int*, int64_t, const T*, const T*,      \
                                          const T*, const T*, float, int*, int*, int*, int*, T*,    \
@@ -864,13 +894,13 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
                                          cudaStream_t);                                            \
   template cudaError_t sparse_full<T>(T*, int64_t, int64_t, const T*, int64_t, int64_t,            \
                                       const int*, const int*, const T*, const unsigned char*,      \
-                                      int64_t, int, const DetectCounters*, cudaStream_t);         \
+                                      int64_t, int, const DetectCounters*, cudaStream_t, Mirror);         \
   template cudaError_t open_rowmin<T>(const T*, int64_t, int64_t, const int*, const int*, int64_t,      \
                                       unsigned*, const DetectCounters*, cudaStream_t);             \
   template cudaError_t sparse_round<T>(T*, int64_t, int64_t, const T*, int64_t, const int*,        \
                                        const int*, const T*, int64_t, const int64_t*, const int*,  \
                                        const int*, const int*, int*, int*, int*, int*, int,        \
-                                       const DetectCounters*, cudaStream_t, unsigned*, T);
+                                       const DetectCounters*, cudaStream_t, unsigned*, T, Mirror);
 INST(int32_t)
 INST(float)
 #undef INST

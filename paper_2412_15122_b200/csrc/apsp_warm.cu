@@ -142,6 +142,7 @@ struct apsp_handle {
   double theta = 0.02;
   float tau = 1e-5f;
   int max_rounds = 64;
+  int rounds_hint = 2;           // rounds the last sparse recompute needed (its first batch)
   int fw16 = 1;                  // int16x2 FW when exact (int32 shortest path, one GPU)
   int last_fw16 = 0;             // 1: the last FW ran packed, 2: it fell back to int32
   bool mirror_built = false;     // the mirror was built (or invalidated) from D
@@ -690,7 +691,9 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     CK(open_rowmin<T>(h->Dl<T>(), h->ld, h->row0, h->gprow(), h->gpcol(), ocap,
                       reinterpret_cast<unsigned*>(h->anyrow()), h->ctr(), h->st));
     // rounds over the open entries of each row, a first batch of 4
-    apsp_status s = enqueue_rounds(std::min(4, h->max_rounds));
+    // the first batch is enqueued blind: as many rounds as the previous
+    // recompute needed (at least 2: round 1 finding nothing proves convergence)
+    apsp_status s = enqueue_rounds(std::min(std::max(2, h->rounds_hint), h->max_rounds));
     if (s != APSP_OK) return s;
   }
 
@@ -730,7 +733,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   bool dense = h->force_path == 2 || (h->force_path == 0 && gate) || overflow;
   // rounds until no entry changes (rarely more than the first batch); later
   // batches double (a round whose frontier is empty costs one small launch)
-  int batch = 4;
+  int batch = std::max(2, rounds);
   while (!dense && changed && rounds < h->max_rounds) {
     batch *= 2;
     apsp_status s = enqueue_rounds(std::min(batch, h->max_rounds - rounds));
@@ -742,6 +745,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     changed = *hflag != 0;
   }
   if (info) info->rounds = rounds;
+  if (try_sparse && !dense && !changed) h->rounds_hint = rounds;   // converged within `rounds`
   if (!dense && changed) dense = true;   // not converged: every entry is still a valid upper bound
   if (dense) {
     if (info) info->path = 3;

@@ -846,19 +846,31 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
         cfull = as.ufull;
       }
     }
-    // the streaming pass (gated off when the gathers did it)
-    PK(APSP_K_ADD_PASS1, h->mirror_hint && !srow ? h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n : 0.0,
-       addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
-                        &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), unc, 1, h->st, srow ? 0 : 1, cfull));
-    CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
-                         ceff, row, 1, h->mirror<T>(), unc, h->st, srow ? as.rfull : nullptr, cfull));
+    if (srow) {
+      // fallback of the gathers (|U| over its limit, *cfull set): the int32
+      // pass — exact, so no int16 uncertainty to resolve — and the finish of
+      // the column; both exit at once otherwise (grid-stride, small grids)
+      CK(addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
+                          &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), cfull, 0, h->st));
+      CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
+                           ceff, row, 0, h->mirror<T>(), unc, h->st, as.rfull, cfull));
+    } else {
+      // the streaming pass on the mirror ...
+      PK(APSP_K_ADD_PASS1, h->mirror_hint ? h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n : 0.0,
+         addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
+                          &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), unc, 1, h->st));
+      CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
+                           ceff, row, 1, h->mirror<T>(), unc, h->st));
+    }
   }
-  PK(APSP_K_ADD_PASS1, try_packed && h->mirror_hint ? 0.0 : 4.0 * (double)(r.hi - r.lo) * (double)n,
-     addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
-                      &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), try_packed ? unc : nullptr, 0,
-                      h->st));
-  CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
-                       ceff, row, try_packed ? 2 : 0, h->mirror<T>(), unc, h->st));
+  if (!srow) {   // ... or in int32 (gated on the packed pass' outcome when it ran)
+    PK(APSP_K_ADD_PASS1, try_packed && h->mirror_hint ? 0.0 : 4.0 * (double)(r.hi - r.lo) * (double)n,
+       addnode_pass1<T>(h->Dl<T>(), ld, r, n, ow, iw, h->rowpart<T>(), rowpartM, h->colpart<T>(), ld,
+                        &nchunk, &nslab, kMaxSlabs, h->sr, h->mirror<T>(), try_packed ? unc : nullptr, 0,
+                        h->st));
+    CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
+                         ceff, row, try_packed ? 2 : 0, h->mirror<T>(), unc, h->st));
+  }
   if (h->world > 1)
     NK(h->comm->allreduce(row, (size_t)ld, nccl_type<T>(), ncclMin, h->st));
   // rows with ceff[i] = INF provably do not change and are not read at all

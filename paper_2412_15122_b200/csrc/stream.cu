@@ -258,7 +258,8 @@ struct Tiling {
   int64_t warps;
 };
 // Tuning override for the streaming tilings (warps per SM the grid targets),
-// read once from the environment; used only to measure alternatives.
+// from the environment (callers keep it in a static: read once); used only
+// to measure alternatives.
 static int tune_wps(const char* name, int dflt) {
   const char* v = getenv(name);
   const int x = v ? atoi(v) : 0;
@@ -1117,8 +1118,9 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
                           int* nslab_out, int max_slabs, int sr, Mirror M, const unsigned* uncertain,
                           int packed, cudaStream_t st, int colp, const unsigned* full) {
   const bool p8 = packed && !sr && M.m8 != nullptr;   // int8 mirror: 512-column chunks
-  Tiling tl = p8 ? make_tiling(n, r.hi - r.lo, max_slabs, 128, tune_wps("APSP_TUNE_P8_WPS", 144))
-                 : make_tiling(n, r.hi - r.lo, max_slabs, P1_VEC, tune_wps("APSP_TUNE_P1_WPS", 16));
+  static const int wps8 = tune_wps("APSP_TUNE_P8_WPS", 144), wps16 = tune_wps("APSP_TUNE_P1_WPS", 16);
+  Tiling tl = p8 ? make_tiling(n, r.hi - r.lo, max_slabs, 128, wps8)
+                 : make_tiling(n, r.hi - r.lo, max_slabs, P1_VEC, wps16);
   *nchunk_out = tl.nchunk;
   *nslab_out = tl.nslab;
   if (r.hi <= r.lo) {
@@ -1460,7 +1462,8 @@ cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, 
   int grid = (int)cdiv(tl.warps, 8);
   if constexpr (std::is_same<T, int32_t>::value) {
     if (!sr && M.m8) {   // the int8 twin first (the int32 kernel then exits while M stays valid)
-      const Tiling t8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256, tune_wps("APSP_TUNE_R8_WPS", 32));
+      static const int wps = tune_wps("APSP_TUNE_R8_WPS", 32);
+      const Tiling t8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256, wps);
       const int g8 = (int)cdiv(t8.warps, 8);
       if (c2)
         k_rank1_p8<true><<<g8, 256, 0, st>>>(D, ld, r, n, t8, c, rv, c2, rv2, bytes_read, M);
@@ -2080,13 +2083,14 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
                    int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr, const T* WT,
                    int64_t ldw, int sr, Mirror M, cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
-  Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20, DS_VEC, tune_wps("APSP_TUNE_DET_WPS", 192));   // 64 warps/SM: 4 waves (measured best)
+  static const int wps = tune_wps("APSP_TUNE_DET_WPS", 192), wps8 = tune_wps("APSP_TUNE_DET8_WPS", 128);
+  Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20, DS_VEC, wps);   // (measured best)
   if (tl.slab >= (1 << 26)) return cudaErrorInvalidValue;   // MODE-1 queue packing
   if (mode == 0) CUDA_TRY(cudaMemsetAsync(anyrow + r.lo, 0, sizeof(int) * (size_t)(r.hi - r.lo), st));
   DetectOut<T> o{anyrow, rowcnt, prow, pcol, plb, lcap, ctr, WT, ldw, M};
   const int g = (int)cdiv(tl.warps, 8);
   // int8 mirror: 1024-column chunks
-  const Tiling tl8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256, tune_wps("APSP_TUNE_DET8_WPS", 128));
+  const Tiling tl8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256, wps8);
   const int g8 = (int)cdiv(tl8.warps, 8);
   // the int32 twin exits when a packed kernel applies (decided on the device):
   // with a mirror it is launched at its residency (2 CTAs per SM) and strides

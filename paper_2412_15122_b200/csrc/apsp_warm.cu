@@ -42,7 +42,7 @@ struct Plan {
   int64_t ld, lcap, ocap, maxchunk;
   size_t off_wt, off_vec, off_rowpart, off_colpart, off_rowoff, off_rowcnt, off_chg, off_prow,
       off_pcol, off_ocol, off_ocnt, off_gprow, off_gpcol, off_glb, off_gfull,
-      off_srow, off_scol, off_slid, off_slw, off_wnext, off_panel, off_pt, off_anyrow, off_qsend, off_qcol,
+      off_srow, off_scol, off_slid, off_slw, off_wnext, off_slscr, off_panel, off_pt, off_anyrow, off_qsend, off_qcol,
       off_qids, off_qdsv, off_qlab, off_qpred, off_qpath, off_qdone, off_qcnt, off_p16, off_p8, off_ptd, off_small,
       total;
   int qcap, qbatch;
@@ -83,6 +83,7 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   p.off_slid = take(sizeof(int32_t) * (size_t)cap * kSL);
   p.off_slw = take(sizeof(int32_t) * (size_t)cap * kSL);
   p.off_wnext = take(sizeof(int32_t) * (size_t)cap);
+  p.off_slscr = take(kSLScratch);
   p.off_panel = take(world > 1 ? sizeof(int32_t) * (size_t)kTile * p.ld : 256);
   // transposed pivot column panel for the FW phase-3 kernel (kTile x ldpt)
   p.ldpt = round_up(world > 1 ? round_up(cdiv(cap, world), kTile) : cap, kTile);
@@ -225,6 +226,7 @@ struct apsp_handle {
   int* slid() { return reinterpret_cast<int*>(ws + plan.off_slid); }
   template <typename T> T* slw() { return reinterpret_cast<T*>(ws + plan.off_slw); }
   template <typename T> T* wnext() { return reinterpret_cast<T*>(ws + plan.off_wnext); }
+  void* slscr() { return ws + plan.off_slscr; }
   template <typename T> T* panel() { return reinterpret_cast<T*>(ws + plan.off_panel); }
   template <typename T> T* pt() { return reinterpret_cast<T*>(ws + plan.off_pt); }
   template <typename T> T* qsend() { return reinterpret_cast<T*>(ws + plan.off_qsend); }
@@ -807,7 +809,8 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   bool srow = false;
   // (small graphs: the one streaming pass costs less than the shortcuts' extra launches)
   if constexpr (std::is_same<T, int32_t>::value)
-    srow = h->world == 1 && n >= kAddShortcutMinN && h->plan.maxchunk >= 2 && mirror8_known_valid(h);
+    srow = h->world == 1 && n >= kAddShortcutMinN && n < (int64_t(1) << 24) && h->plan.maxchunk >= 2 &&
+           mirror8_known_valid(h);   // (k_addrow packs t in 24 bits)
   if constexpr (std::is_same<T, int32_t>::value) {
     if (srow) {
       // scratch: the (value, minimiser) row and the minimiser flags live in the
@@ -820,7 +823,7 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
     }
   }
   CK2(shortlist_add_bound<T>(h->slid(), h->slw<T>(), h->wnext<T>(), ow, n, x, h->st2));  // x -> j
-  CK2(shortlist_build_one<T>(iw, 0, n + 1, x, h->slid(), h->slw<T>(), h->wnext<T>(),
+  CK2(shortlist_build_one<T>(iw, 0, n + 1, x, h->slid(), h->slw<T>(), h->wnext<T>(), h->slscr(),
                              h->st2));   // in-edges of x: row x of WT is in_w
   CKR(cudaEventRecord(h->ev_join, h->st2));
   Rows r = h->active();

@@ -165,12 +165,14 @@ cudaError_t shortlist_swap(int* SLid, T* SLw, T* wnext, int64_t n, int64_t p, in
 // ---------------- sparse.cu ----------------
 constexpr int kSLK = 16;              // shortlist entries per lane
 constexpr int kSL = 32 * kSLK;        // shortlist entries per node
+constexpr int kSLG = 32;              // shortlist_build_one: partial lists (CTAs) at most
+constexpr size_t kSLScratch = (size_t)kSLG * kSL * 8 + (size_t)kSLG * 4;   // its scratch bytes
 template <typename T>
 cudaError_t shortlist_build(const T* WT, int64_t ldw, int64_t n, const int* rows, int64_t r0,
                             int64_t r1, int* SLid, T* SLw, T* wnext, cudaStream_t st);
 template <typename T>
 cudaError_t shortlist_build_one(const T* WT, int64_t ldw, int64_t n, int64_t j, int* SLid, T* SLw,
-                                T* wnext, cudaStream_t st);
+                                T* wnext, void* scratch /* kSLScratch bytes */, cudaStream_t st);
 template <typename T>
 cudaError_t shortlist_add_bound(int* SLid, T* SLw, T* wnext, const T* out_w, int64_t n, int64_t x,
                                 cudaStream_t st);

@@ -34,31 +34,57 @@ static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // ---------------------------------------------------------------------------
 // shortlists: lane-local top-kSLK in-edges of node j (kSL = 32 * kSLK entries)
 // ---------------------------------------------------------------------------
-// Sort SL(j) ascending by weight (dead entries carry INF and sink to the end):
-// a warp-level bitonic network on the 512 entries in place in global memory
-// (__syncwarp orders the warp's accesses between stages).  Phase A then finds
-// the cheapest in-edges — the likeliest last hops of a tie — in the first
-// positions.  Runs at build and after every insertion / weight refresh.
+// Sort SL(j) ascending by (weight, id) (dead entries — id -1, INF — sink to
+// the end): a warp-level bitonic network on the 512 entries held in registers
+// (entry t * 32 + lane in slot t of the lane), compare-exchanges across slots
+// in-register and across lanes by shuffles.  Phase A then finds the cheapest
+// in-edges — the likeliest last hops of a tie — in the first positions.  Runs
+// at build (the previous in-global-memory network was latency-bound: ~100 us
+// per list on the add-node side stream).
 template <typename T>
-__device__ void sl_sort_warp(int* sid, T* sw) {
+__device__ __forceinline__ bool sl_less(T wa, int ia, T wb, int ib) {
+  return wa < wb || (wa == wb && ia < ib);
+}
+template <typename T, int TJ>
+__device__ __forceinline__ void sl_stage_slots(T (&w)[kSLK], int (&id)[kSLK], int k, int lane) {
+#pragma unroll
+  for (int t = 0; t < kSLK; ++t) {
+    if ((t & TJ) == 0) {
+      const int t2 = t | TJ;
+      const bool up = (((t << 5) | lane) & k) == 0;
+      const bool sw = up ? sl_less(w[t2], id[t2], w[t], id[t]) : sl_less(w[t], id[t], w[t2], id[t2]);
+      if (sw) {
+        const T tw = w[t]; w[t] = w[t2]; w[t2] = tw;
+        const int ti = id[t]; id[t] = id[t2]; id[t2] = ti;
+      }
+    }
+  }
+}
+template <typename T>
+__device__ void sl_sort_regs(T (&w)[kSLK], int (&id)[kSLK]) {
+  static_assert(kSLK == 16, "slot stages below are written for 16 slots per lane");
   const int lane = threadIdx.x & 31;
-  __syncwarp();
   for (int k = 2; k <= kSL; k <<= 1)
     for (int jj = k >> 1; jj > 0; jj >>= 1) {
-#pragma unroll 4
-      for (int t = 0; t < kSL / 32; ++t) {
-        const int i = t * 32 + lane, l = i ^ jj;
-        if (l > i) {
-          const T a = sw[i], b = sw[l];
-          const bool up = (i & k) == 0;
-          if ((a > b) == up && a != b) {
-            const int ia = sid[i], ib = sid[l];
-            sw[i] = b; sw[l] = a;
-            sid[i] = ib; sid[l] = ia;
-          }
+      if (jj >= 32) {
+        switch (jj >> 5) {
+          case 1: sl_stage_slots<T, 1>(w, id, k, lane); break;
+          case 2: sl_stage_slots<T, 2>(w, id, k, lane); break;
+          case 4: sl_stage_slots<T, 4>(w, id, k, lane); break;
+          default: sl_stage_slots<T, 8>(w, id, k, lane); break;
+        }
+      } else {
+        const bool lower = (lane & jj) == 0;
+#pragma unroll
+        for (int t = 0; t < kSLK; ++t) {
+          const T ow = __shfl_xor_sync(0xffffffffu, w[t], jj);
+          const int oi = __shfl_xor_sync(0xffffffffu, id[t], jj);
+          const bool up = (((t << 5) | lane) & k) == 0;
+          // the lower index of the pair keeps the min when ascending, else the max
+          const bool take = (lower == up) ? sl_less(ow, oi, w[t], id[t]) : sl_less(w[t], id[t], ow, oi);
+          if (take) { w[t] = ow; id[t] = oi; }
         }
       }
-      __syncwarp();
     }
 }
 
@@ -137,6 +163,7 @@ __global__ void __launch_bounds__(256) k_shortlist_build(const T* __restrict__ W
         rej = Tr<T>::mn(rej, x);
       }
     }
+    sl_sort_regs<T>(bw, bi);
     int* oid = SLid + j * kSL;
     T* ow = SLw + j * kSL;
 #pragma unroll
@@ -144,7 +171,6 @@ __global__ void __launch_bounds__(256) k_shortlist_build(const T* __restrict__ W
       oid[q * 32 + lane] = bi[q];
       ow[q * 32 + lane] = bw[q];
     }
-    sl_sort_warp<T>(oid, ow);
     rej = warp_min<T>(rej);
     if (lane == 0) wnext[j] = rej;
   }
@@ -159,79 +185,157 @@ cudaError_t shortlist_build(const T* WT, int64_t ldw, int64_t n, const int* rows
   return cudaGetLastError();
 }
 
-// One row, whole CTA (256 threads): each warp keeps lane-local top-kSLK of its
-// eighth of the row, then warp 0 keeps lane-local top-kSLK of those 8*kSL
-// candidates.  Every in-edge left out was rejected at one of the two stages,
-// so it is >= the min over all rejected values = wnext(j).
+// SL(x) of one node (the add-node side stream): the kSL cheapest in-edges by
+// (weight, id), exactly, and wnext = the smallest weight left out.  Two
+// kernels instead of one CTA walking the row (that was latency-bound at ~117
+// us for n = 32768):
+//   k_sl_one_part  — CTA g sorts kSLC-entry chunks of the row in shared memory
+//                    (bitonic) and keeps a running sorted top-kSL: merged as
+//                    min(run[i], chunk[kSL-1-i]) (a bitonic sequence holding the
+//                    kSL smallest of both) + a bitonic merge.  Writes its list
+//                    and the min of everything it discarded.
+//   k_sl_one_merge — one CTA merges the <= kSLG lists pairwise the same way.
+// Every in-edge left out was discarded at one step, so it is >= the min over
+// all discarded values = wnext(j).
+constexpr int kSLC = 1024;   // chunk (one entry per thread)
 template <typename T>
-__global__ void __launch_bounds__(256) k_shortlist_build_one(const T* __restrict__ WT, int64_t ldw,
-                                                             int64_t n, int64_t j, int* SLid,
-                                                             T* SLw, T* wnext) {
-  __shared__ T cw[8 * kSL];
-  __shared__ int ci[8 * kSL];
-  __shared__ T srej[8];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const T I = Tr<T>::inf();
-  const T* row = WT + j * ldw;
-  T bw[kSLK];
-  int bi[kSLK];
-#pragma unroll
-  for (int q = 0; q < kSLK; ++q) { bw[q] = I; bi[q] = -1; }
-  T rej = I;
-  auto insert = [&](T x, int m) {
-    if (x < bw[kSLK - 1]) {
-      rej = Tr<T>::mn(rej, bw[kSLK - 1]);
-      T cwv = x;
-      int civ = m;
-#pragma unroll
-      for (int q = 0; q < kSLK; ++q)
-        if (cwv < bw[q]) { T tw = bw[q]; int ti = bi[q]; bw[q] = cwv; bi[q] = civ; cwv = tw; civ = ti; }
-    } else {
-      rej = Tr<T>::mn(rej, x);
+__device__ __forceinline__ void sl_cx(T* w, int* id, int lo, int hi) {   // ascending compare-exchange
+  const T a = w[lo], b = w[hi];
+  const int ia = id[lo], ib = id[hi];
+  if (sl_less(b, ib, a, ia)) { w[lo] = b; w[hi] = a; id[lo] = ib; id[hi] = ia; }
+}
+// bitonic merge of `lists` bitonic sequences of kSL entries each, list q at
+// w + q * stride (ascending); all threads of the CTA
+template <typename T>
+__device__ void sl_merge_lists(T* w, int* id, int lists, int stride) {
+  for (int jj = kSL / 2; jj > 0; jj >>= 1) {
+    for (int idx = threadIdx.x; idx < lists * (kSL / 2); idx += blockDim.x) {
+      const int q = idx / (kSL / 2), t = idx % (kSL / 2);
+      const int lo = (t / jj) * 2 * jj + (t % jj);
+      sl_cx(w + q * stride, id + q * stride, lo, lo + jj);
     }
-  };
-  const int64_t n4 = (n + 3) / 4;
-  for (int64_t q = threadIdx.x; q < n4; q += 256) {
-    Vec4<T> v = ld4<T>(row + 4 * q);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int64_t m = 4 * q + c;
-      const T x = get(v, c);
-      if (m < n && m != j && Tr<T>::fin(x)) insert(x, (int)m);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < kSLK; ++q) {
-    cw[warp * kSL + q * 32 + lane] = bw[q];
-    ci[warp * kSL + q * 32 + lane] = bi[q];
-  }
-  rej = warp_min<T>(rej);
-  if (lane == 0) srej[warp] = rej;
-  __syncthreads();
-  if (warp != 0) return;
-#pragma unroll
-  for (int q = 0; q < kSLK; ++q) { bw[q] = I; bi[q] = -1; }
-  rej = I;
-  for (int t = lane; t < 8 * kSL; t += 32)
-    if (ci[t] >= 0) insert(cw[t], ci[t]);
-  int* oid = SLid + j * kSL;
-  T* ow = SLw + j * kSL;
-#pragma unroll
-  for (int q = 0; q < kSLK; ++q) {
-    oid[q * 32 + lane] = bi[q];
-    ow[q * 32 + lane] = bw[q];
-  }
-  sl_sort_warp<T>(oid, ow);
-  rej = warp_min<T>(rej);
-  if (lane == 0) {
-    for (int w = 0; w < 8; ++w) rej = Tr<T>::mn(rej, srej[w]);
-    wnext[j] = rej;
+    __syncthreads();
   }
 }
 template <typename T>
+__device__ __forceinline__ T sl_block_min(T v, T* red) {
+  v = warp_min<T>(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : Tr<T>::inf();
+    v = warp_min<T>(v);
+  }
+  return v;   // valid in thread 0
+}
+template <typename T>
+__global__ void __launch_bounds__(kSLC) k_sl_one_part(const T* __restrict__ row, int64_t n, int64_t j,
+                                                      T* cw_out, int* ci_out, T* rej_out) {
+  __shared__ T cw[kSLC], rw[kSL];
+  __shared__ int ci[kSLC], ri[kSL];
+  __shared__ T red[32];
+  const int tid = threadIdx.x;
+  const T I = Tr<T>::inf();
+  T rej = I;
+  bool first = true;
+  for (int64_t c0 = (int64_t)blockIdx.x * kSLC; c0 < n; c0 += (int64_t)gridDim.x * kSLC) {
+    const int64_t e = c0 + tid;
+    const T x = e < n ? row[e] : I;
+    const bool ok = e < n && e != j && Tr<T>::fin(x);
+    cw[tid] = ok ? x : I;
+    ci[tid] = ok ? (int)e : -1;
+    __syncthreads();
+    for (int k = 2; k <= kSLC; k <<= 1)
+      for (int jj = k >> 1; jj > 0; jj >>= 1) {
+        const int l = tid ^ jj;
+        if (l > tid) {
+          if ((tid & k) == 0) sl_cx(cw, ci, tid, l);
+          else sl_cx(cw, ci, l, tid);
+        }
+        __syncthreads();
+      }
+    if (tid >= kSL) rej = Tr<T>::mn(rej, cw[tid]);   // the upper half of the chunk is discarded
+    if (first) {
+      if (tid < kSL) { rw[tid] = cw[tid]; ri[tid] = ci[tid]; }
+      __syncthreads();
+    } else {
+      if (tid < kSL) {
+        const T a = rw[tid], b = cw[kSL - 1 - tid];
+        const int ia = ri[tid], ib = ci[kSL - 1 - tid];
+        const bool bl = sl_less(b, ib, a, ia);
+        rej = Tr<T>::mn(rej, bl ? a : b);
+        if (bl) { rw[tid] = b; ri[tid] = ib; }
+      }
+      __syncthreads();
+      sl_merge_lists<T>(rw, ri, 1, 0);
+    }
+    first = false;
+  }
+  if (first && tid < kSL) { rw[tid] = I; ri[tid] = -1; }   // (no chunk: launched with fewer CTAs)
+  if (tid < kSL) {
+    cw_out[(int64_t)blockIdx.x * kSL + tid] = rw[tid];
+    ci_out[(int64_t)blockIdx.x * kSL + tid] = ri[tid];
+  }
+  rej = sl_block_min<T>(rej, red);
+  if (tid == 0) rej_out[blockIdx.x] = rej;
+}
+template <typename T>
+__global__ void __launch_bounds__(kSLC) k_sl_one_merge(const T* __restrict__ cw_in, const int* __restrict__ ci_in,
+                                                       const T* __restrict__ rej_in, int G, int Gp, int64_t j,
+                                                       int* SLid, T* SLw, T* wnext) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  T* w = reinterpret_cast<T*>(sm_raw);
+  int* id = reinterpret_cast<int*>(sm_raw + sizeof(T) * (size_t)Gp * kSL);
+  __shared__ T red[32];
+  const int tid = threadIdx.x;
+  const T I = Tr<T>::inf();
+  T rej = tid < G ? rej_in[tid] : I;
+  for (int e = tid; e < Gp * kSL; e += blockDim.x) {
+    const bool ok = e < G * kSL;
+    w[e] = ok ? cw_in[e] : I;
+    id[e] = ok ? ci_in[e] : -1;
+  }
+  __syncthreads();
+  for (int s = 1; s < Gp; s <<= 1) {   // lists q (multiples of 2s) absorb lists q + s
+    const int lists = Gp / (2 * s);
+    for (int idx = tid; idx < lists * kSL; idx += blockDim.x) {
+      const int q = (idx / kSL) * 2 * s, i = idx % kSL;
+      const int pa = q * kSL + i, pb = (q + s) * kSL + (kSL - 1 - i);
+      const bool bl = sl_less(w[pb], id[pb], w[pa], id[pa]);
+      rej = Tr<T>::mn(rej, bl ? w[pa] : w[pb]);
+      if (bl) { w[pa] = w[pb]; id[pa] = id[pb]; }
+    }
+    __syncthreads();
+    sl_merge_lists<T>(w, id, lists, 2 * s * kSL);
+  }
+  if (tid < kSL) {
+    SLid[j * kSL + tid] = id[tid];
+    SLw[j * kSL + tid] = w[tid];
+  }
+  rej = sl_block_min<T>(rej, red);
+  if (tid == 0) wnext[j] = rej;
+}
+template <typename T>
 cudaError_t shortlist_build_one(const T* WT, int64_t ldw, int64_t n, int64_t j, int* SLid, T* SLw,
-                                T* wnext, cudaStream_t st) {
-  k_shortlist_build_one<T><<<1, 256, 0, st>>>(WT, ldw, n, j, SLid, SLw, wnext);
+                                T* wnext, void* scratch, cudaStream_t st) {
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(kSLG, cdiv(n, kSLC)));
+  int Gp = 1;
+  while (Gp < G) Gp <<= 1;
+  T* cw = reinterpret_cast<T*>(scratch);
+  int* ci = reinterpret_cast<int*>(cw + (size_t)kSLG * kSL);
+  T* rj = reinterpret_cast<T*>(ci + (size_t)kSLG * kSL);
+  k_sl_one_part<T><<<G, kSLC, 0, st>>>(WT + j * ldw, n, j, cw, ci, rj);
+  CUDA_TRY(cudaGetLastError());
+  const size_t smem = (sizeof(T) + sizeof(int)) * (size_t)Gp * kSL;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_sl_one_merge<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)((sizeof(int32_t) + sizeof(int)) * (size_t)kSLG * kSL)));
+    CUDA_TRY(cudaFuncSetAttribute(k_sl_one_merge<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)((sizeof(float) + sizeof(int)) * (size_t)kSLG * kSL)));
+    attr = true;
+  }
+  k_sl_one_merge<T><<<1, kSLC, smem, st>>>(cw, ci, rj, G, Gp, j, SLid, SLw, wnext);
   return cudaGetLastError();
 }
 
@@ -879,7 +983,7 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
                                           int*, T*, T*, cudaStream_t);                            \
   template cudaError_t shortlist_add_bound<T>(int*, T*, T*, const T*, int64_t, int64_t,            \
                                               cudaStream_t);                                      \
-  template cudaError_t shortlist_build_one<T>(const T*, int64_t, int64_t, int64_t, int*, T*, T*,   \
+  template cudaError_t shortlist_build_one<T>(const T*, int64_t, int64_t, int64_t, int*, T*, T*, void*, \
                                               cudaStream_t);                                      \
   template cudaError_t shortlist_set_edge<T>(int*, T*, T*, int64_t, int64_t, T, int, cudaStream_t); \
   template cudaError_t shortlist_swap<T>(int*, T*, T*, int64_t, int64_t, int64_t, cudaStream_t);    \

@@ -810,12 +810,12 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   // (small graphs: the one streaming pass costs less than the shortcuts' extra launches)
   if constexpr (std::is_same<T, int32_t>::value)
     srow = h->world == 1 && n >= kAddShortcutMinN && n < (int64_t(1) << 24) && h->plan.maxchunk >= 2 &&
-           mirror8_known_valid(h);   // (k_addrow packs t in 24 bits)
+           2 * kAddColLimit <= ld && mirror8_known_valid(h);   // (k_addrow packs t in 24 bits)
   if constexpr (std::is_same<T, int32_t>::value) {
     if (srow) {
-      // scratch: the (value, minimiser) row and the minimiser flags live in the
-      // pass-1 partial buffer (unused unless the gathers fall back to pass 1,
-      // which runs after they are consumed)
+      // scratch: the (value, minimiser) row, the minimiser flags and U's in /
+      // out lists live in the pass-1 partial buffer (4 ld words: unused unless
+      // the gathers fall back to pass 1, which runs after they are consumed)
       CK2(addrow_s(as, ow, n, h->mirror<T>().m8, ld, h->row0, row, ld, reinterpret_cast<int*>(h->vec<T>(5)),
                    reinterpret_cast<unsigned long long*>(h->rowpart<T>()),
                    reinterpret_cast<int*>(h->rowpart<T>()) + 2 * ld, h->st2));
@@ -844,8 +844,9 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
         CKR(cudaStreamWaitEvent(h->st, h->ev_row, 0));
         PK(APSP_K_ADD_PASS1, 0.0,
            addcol_g(as, r, h->mirror<T>().m8, ld, n, iw, ow, reinterpret_cast<int*>(h->rowpart<T>()) + 2 * ld,
-                    reinterpret_cast<int*>(h->vec<T>(5)), kAddColLimit, col, ceff, h->vec<T>(6),
-                    reinterpret_cast<int*>(h->vec<T>(7)), h->st));
+                    reinterpret_cast<int*>(h->vec<T>(5)), reinterpret_cast<int*>(h->rowpart<T>()) + 3 * ld,
+                    kAddColLimit, col, ceff, h->vec<T>(6),
+                    reinterpret_cast<int*>(h->vec<T>(7)), h->wmin<int32_t>(), h->st));
         cfull = as.ufull;
       }
     }

@@ -163,6 +163,13 @@ __device__ __forceinline__ Vec4<T> mask_tail(Vec4<T> v, int64_t col0, int64_t n)
 constexpr int32_t kSat16i = 0x3FFF;
 __device__ __forceinline__ uint16_t sat16(int32_t v) { return (uint16_t)min(v, kSat16i); }
 // 8 int16 mirrored values (or 16 int8 ones) in one 16-byte streaming load
+// One byte of a random gather, cached in L2 only: an L1 miss would fill a
+// whole 128-byte line (4 sectors from DRAM) for the one byte used.
+__device__ __forceinline__ uint32_t ldg_byte_l2(const uint8_t* p) {
+  uint32_t v;
+  asm("ld.global.cg.u8 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ uint4 mload8(const uint16_t* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"

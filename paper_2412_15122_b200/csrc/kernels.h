@@ -102,8 +102,9 @@ cudaError_t addrow_s(const AddScratch& a, const int32_t* ow, int64_t n, const ui
                      cudaStream_t st);
 // *a.ufull = 1 when |U| exceeded `limit`: pass 1 + the finish kernel compute col instead
 cudaError_t addcol_g(const AddScratch& a, Rows r, const uint8_t* m8, int64_t ld, int64_t n, const int32_t* iw,
-                     const int32_t* ow, const int* tflag, int* ulist, int limit, int32_t* col, int32_t* ceff,
-                     int32_t* mprime, int* fb_list, cudaStream_t st);
+                     const int32_t* ow, const int* tflag, int* ulist, int* uaux /* 2 * limit */, int limit,
+                     int32_t* col, int32_t* ceff, int32_t* mprime, int* fb_list,
+                     int32_t wmin /* <= every edge weight */, cudaStream_t st);
 template <typename T>
 cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
                            int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,

@@ -660,6 +660,11 @@ cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const 
 // stops at the first batch whose bound reaches lb (certified); after
 // kPhaseABatches batches the pair is left open for A2 / B / the rounds.
 constexpr int kPhaseABatches = 9;   // sorted positions 0-71
+static int pa_tune(const char* name, int dflt) {   // measurement override (read once)
+  const char* v = getenv(name);
+  const int x = v ? atoi(v) : 0;
+  return x > 0 ? x : dflt;
+}
 #ifndef PA_MINB
 #define PA_MINB 4   // 4 CTAs per SM (64 registers, no spills): latency-bound, occupancy wins
 #endif
@@ -673,7 +678,7 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_a(T* D, int64_t l
                                                         const T* __restrict__ c1, const T* __restrict__ r1,
                                                         const T* __restrict__ c2, const T* __restrict__ r2,
                                                         float tau, OpenLists<T> ol,
-                                                        const DetectCounters* dc, Mirror M) {
+                                                        const DetectCounters* dc, Mirror M, int nbatch) {
   const int lane = threadIdx.x & 31;
   unsigned mbits = 0;   // mirror flag bits raised by this thread's writes
   npairs = device_count(dc, npairs, 0);
@@ -700,7 +705,7 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_a(T* D, int64_t l
       const int4* sw = reinterpret_cast<const int4*>(SLw + j * kSL);
       lb = *(volatile T*)(Drow + j);   // D_old[i][j]
       const T ci = c1[i], cj = TWO ? c2[i] : Tr<T>::inf();
-      for (int b = 0; b < kPhaseABatches; ++b) {
+      for (int b = 0; b < nbatch; ++b) {
         const int4 m0 = sid[2 * b], m1 = sid[2 * b + 1];
         const int4 w0 = sw[2 * b], w1 = sw[2 * b + 1];
         const int m[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
@@ -785,7 +790,8 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
   int grid = (int)std::min<int64_t>(cdiv(npairs, 256), (int64_t)num_sms() * 8);
 #define PA(SRV, TWOV)                                                                              \
   k_sparse_phase_a<T, SRV, TWOV><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, srow, scol, npairs, \
-                                                       c1, r1, c2, r2, tau, ol, ctr, M)
+                                                       c1, r1, c2, r2, tau, ol, ctr, M, nb)
+  static const int nb = std::min(kSL / 8, pa_tune("APSP_TUNE_PA_BATCHES", kPhaseABatches));
   const bool two = c2 != nullptr;
   if (sr) { if (two) PA(1, true); else PA(1, false); }
   else { if (two) PA(0, true); else PA(0, false); }

@@ -866,9 +866,11 @@ __global__ void k_addrow_final(const unsigned long long* __restrict__ packed, in
 // The new column and the row-skip bound of an add by gathers instead of a
 // pass over the mirror (int8 mirror valid, one GPU).
 //   col[i] = min_t D[i][t] + in[t]: over S1 = {t : in[t] <= th} it is an upper
-//     bound col1[i]; if col1[i] <= th2 (the smallest in[t] above th), no t
-//     outside S1 can do better (D >= 0): exact.  Rows not certified get a
-//     full-row scan (k_addcol_rows).  th = min in + 2.
+//     bound col1[i]; a t outside S1 costs D[i][t] + in[t] >= wmin + th2 (th2:
+//     the smallest in[t] above th; wmin <= every edge weight, so D[i][t] >=
+//     wmin for t != i), or in[i] for t = i (D[i][i] = 0).  So col1[i] <=
+//     min(th2 + wmin, in[i] if i is outside S1) is exact.  Rows not certified
+//     get a full-row scan (k_addcol_rows).  th = min in + delta.
 //   M'[i] = max_{t in T*} D[i][t] - out[t], T* = one minimiser t*(j) of each
 //     new-row entry (recorded by k_addrow): a change at (i, j) needs col[i] <
 //     D[i][t*] - out[t*] for a t* attaining row[j] — so rows with col[i] >=
@@ -879,8 +881,9 @@ __global__ void k_addrow_final(const unsigned long long* __restrict__ packed, in
 // ---------------------------------------------------------------------------
 // U = {t : in[t] <= th || t in T*}, th = min in + delta; th2 = the
 // smallest in[t] above th (the certification threshold of col1)
-__global__ void k_addcol_sets(AddScratch a, const int32_t* __restrict__ iw, const int* __restrict__ tflag,
-                              int64_t n, int delta, int* ulist, int limit) {
+__global__ void k_addcol_sets(AddScratch a, const int32_t* __restrict__ iw, const int32_t* __restrict__ ow,
+                              const int* __restrict__ tflag, int64_t n, int delta, int* ulist, int* uin, int* uout,
+                              int limit) {
   const int32_t I = APSP_INF_I32_DEV;
   const unsigned imn = *a.in_min;
   const int32_t th = imn >= (unsigned)I ? I : min(I - 1, (int32_t)imn + delta);
@@ -890,18 +893,23 @@ __global__ void k_addcol_sets(AddScratch a, const int32_t* __restrict__ iw, cons
     if (x > th && x < t2) t2 = x;
     if (x <= th || tflag[t]) {
       const int q = atomicAdd(a.u_count, 1);
-      if (q < limit) ulist[q] = (int)t;
+      if (q < limit) { ulist[q] = (int)t; uin[q] = x; uout[q] = ow[t]; }
     }
   }
   t2 = __reduce_min_sync(0xffffffffu, t2);
   if ((threadIdx.x & 31) == 0 && t2 < 0x7F7F7F7F) atomicMin(a.th2, t2);
 }
 // one warp per row: col1 / M' over U; certified rows get col and ceff, the
-// others are listed for k_addcol_rows (M' kept in mprime)
+// others are listed for k_addcol_rows (M' kept in mprime).  U's (t, in[t],
+// out[t]) come from coalesced lists; the byte gathers of a row are issued as
+// one batch before any is used (the gathers are latency-bound, not bandwidth).
+constexpr int kGB = 8;   // gathers in flight per lane
 __global__ void __launch_bounds__(256) k_addcol_gather(AddScratch a, Rows r, const uint8_t* __restrict__ m8,
-                                                       int64_t ld, const int* __restrict__ ulist, int limit,
-                                                       const int32_t* __restrict__ iw, const int32_t* __restrict__ ow,
-                                                       int32_t* col, int32_t* ceff, int32_t* mprime, int* fb_list) {
+                                                       int64_t ld, const int* __restrict__ ulist,
+                                                       const int* __restrict__ uin, const int* __restrict__ uout,
+                                                       int limit, const int32_t* __restrict__ iw,
+                                                       int32_t* col, int32_t* ceff, int32_t* mprime, int* fb_list,
+                                                       int delta, int32_t wmin) {
   const int cnt = *a.u_count;
   if (cnt > limit) {   // too many columns: the streaming pass does it
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.ufull = 1u;
@@ -909,27 +917,40 @@ __global__ void __launch_bounds__(256) k_addcol_gather(AddScratch a, Rows r, con
   }
   const int lane = threadIdx.x & 31;
   const int32_t th2 = *a.th2, I = APSP_INF_I32_DEV;
+  const unsigned imn = *a.in_min;
+  const int32_t th = imn >= (unsigned)I ? I : min(I - 1, (int32_t)imn + delta);
+  // certification threshold (see above); th2 unset: every finite in[t] is in S1
+  const int32_t thr0 = th2 == 0x7F7F7F7F ? INT_MAX : (int32_t)min((int64_t)th2 + wmin, (int64_t)I);
   int* fb_count = a.fb_count;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t i = r.lo + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < r.hi; i += nw) {
     const uint8_t* mrow = m8 + (i - r.row0) * ld;
     int32_t p = I, m = INT_MIN;
-#pragma unroll 16
-    for (int k = lane; k < cnt; k += 32) {
-      const int t = ulist[k];
-      const int32_t d8 = mrow[t];
-      const int32_t a = iw[t], b = ow[t];
-      if (d8 != kSat8i) {
-        if (a < I) p = min(p, d8 + a);
-        if (b < I) m = max(m, d8 - b);
-      } else if (b < I) {
-        m = I;   // an INF entry with a finite out: never skip (as in pass 1)
+    for (int k0 = 0; k0 < cnt; k0 += 32 * kGB) {
+      int t[kGB];
+      int32_t d[kGB];
+#pragma unroll
+      for (int q = 0; q < kGB; ++q) {
+        const int k = k0 + 32 * q + lane;
+        t[q] = k < cnt ? __ldg(ulist + k) : -1;
+      }
+#pragma unroll
+      for (int q = 0; q < kGB; ++q) d[q] = t[q] >= 0 ? (int32_t)ldg_byte_l2(mrow + t[q]) : kSat8i;
+#pragma unroll
+      for (int q = 0; q < kGB; ++q) {
+        const int k = k0 + 32 * q + lane;
+        const int32_t av = k < cnt ? __ldg(uin + k) : I, bv = k < cnt ? __ldg(uout + k) : I;
+        const bool fin = d[q] != kSat8i;
+        if (fin && av < I) p = min(p, d[q] + av);
+        // an INF entry with a finite out: never skip (as in pass 1)
+        if (bv < I) m = max(m, fin ? d[q] - bv : I);
       }
     }
     p = __reduce_min_sync(0xffffffffu, p);
     m = __reduce_max_sync(0xffffffffu, m);
     if (lane == 0) {
-      if (p <= th2) {
+      const int32_t ii = iw[i];
+      if (p <= (ii > th ? min(thr0, ii) : thr0)) {
         col[i] = p;
         ceff[i] = p < m ? p : I;
       } else {
@@ -952,7 +973,17 @@ __global__ void __launch_bounds__(256) k_addcol_rows(AddScratch a, Rows r, const
     const int64_t i = fb_list[f];
     const uint8_t* mrow = m8 + (i - r.row0) * ld;
     int32_t p = I;
-    for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
+    const int64_t n4 = n >> 2;   // 4 mirror bytes per load (rows are 4-byte aligned: ld % 4 == 0)
+#pragma unroll 4
+    for (int64_t q = threadIdx.x; q < n4; q += blockDim.x) {
+      const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(mrow) + q);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int32_t d8 = (int32_t)((w >> (8 * e)) & 0xFFu), a = __ldg(iw + 4 * q + e);
+        if (d8 != kSat8i && a < I) p = min(p, d8 + a);
+      }
+    }
+    for (int64_t t = 4 * n4 + threadIdx.x; t < n; t += blockDim.x) {
       const int32_t d8 = mrow[t], a = iw[t];
       if (d8 != kSat8i && a < I) p = min(p, d8 + a);
     }
@@ -969,15 +1000,16 @@ __global__ void __launch_bounds__(256) k_addcol_rows(AddScratch a, Rows r, const
   }
 }
 cudaError_t addcol_g(const AddScratch& a, Rows r, const uint8_t* m8, int64_t ld, int64_t n, const int32_t* iw,
-                     const int32_t* ow, const int* tflag, int* ulist, int limit, int32_t* col, int32_t* ceff,
-                     int32_t* mprime, int* fb_list, cudaStream_t st) {
+                     const int32_t* ow, const int* tflag, int* ulist, int* uaux, int limit, int32_t* col,
+                     int32_t* ceff, int32_t* mprime, int* fb_list, int32_t wmin, cudaStream_t st) {
   const int g = (int)std::min<int64_t>(cdiv(n, 256), 2 * num_sms());
   static const int delta = tune_wps("APSP_TUNE_ADDCOL_DELTA", 2);   // th = min in + delta (measured)
-  k_addcol_sets<<<g, 256, 0, st>>>(a, iw, tflag, n, delta, ulist, limit);
+  k_addcol_sets<<<g, 256, 0, st>>>(a, iw, ow, tflag, n, delta, ulist, uaux, uaux + limit, limit);
   CUDA_TRY(cudaGetLastError());
   if (r.hi > r.lo) {
     const int grid = (int)std::min<int64_t>(cdiv(r.hi - r.lo, 8), (int64_t)num_sms() * 16);
-    k_addcol_gather<<<grid, 256, 0, st>>>(a, r, m8, ld, ulist, limit, iw, ow, col, ceff, mprime, fb_list);
+    k_addcol_gather<<<grid, 256, 0, st>>>(a, r, m8, ld, ulist, uaux, uaux + limit, limit, iw, col, ceff, mprime,
+                                          fb_list, delta, wmin);
     CUDA_TRY(cudaGetLastError());
     k_addcol_rows<<<num_sms(), 256, 0, st>>>(a, r, m8, ld, n, iw, fb_list, mprime, col, ceff);
   }

@@ -776,6 +776,137 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_a(T* D, int64_t l
   if (M.m || M.m8) mirror_post(M, mbits);
 }
 
+// Phase A with a per-warp work queue: the same per-pair computation as
+// k_sparse_phase_a, one gather step per loop iteration (step 0: the 2
+// cheapest in-edges, step 1: the other 6 of the first batch, then one 8-entry
+// batch per step), and a lane whose pair is finished takes the next pair of
+// the warp's chunk at once.  In the one-pair-per-lane kernel a warp runs as
+// many steps as its slowest lane (ncu: ~6 batches per 32 pairs where the
+// average pair needs ~1.3); here a warp runs ~sum(steps)/32.
+constexpr int kPAChunk = 8;   // pairs per warp chunk = 32 * kPAChunk
+template <typename T, int SR, bool TWO>
+__global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_aq(T* D, int64_t ld, int64_t row0,
+                                                         const int* __restrict__ SLid,
+                                                         const T* __restrict__ SLw,
+                                                         const int* __restrict__ srow,
+                                                         const int* __restrict__ scol, int64_t npairs,
+                                                         const T* __restrict__ c1, const T* __restrict__ r1,
+                                                         const T* __restrict__ c2, const T* __restrict__ r2,
+                                                         float tau, OpenLists<T> ol,
+                                                         const DetectCounters* dc, Mirror M, int nbatch) {
+  const int lane = threadIdx.x & 31;
+  unsigned mbits = 0;
+  npairs = device_count(dc, npairs, 0);
+  const uint8_t* M8 = nullptr;
+  if constexpr (std::is_same<T, int32_t>::value && SR == 0)
+    if (M.m8 && (*(volatile unsigned*)M.flag & 1u) == 0u) M8 = M.m8;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  constexpr int64_t CH = 32 * kPAChunk;
+  for (int64_t c0 = wid * CH; c0 < npairs; c0 += nw * CH) {
+    const int64_t cend = c0 + CH < npairs ? c0 + CH : npairs;
+    int64_t next = c0;   // warp-uniform
+    bool busy = false;
+    int i = 0, j = 0, b = 0, h = 0;
+    T lb = Tr<T>::inf(), acc = Tr<T>::inf(), ci = Tr<T>::inf(), cj = Tr<T>::inf();
+    int m[8], wi[8];
+    while (true) {
+      const unsigned need = __ballot_sync(0xffffffffu, !busy);
+      if (need) {
+        const int64_t mine = next + __popc(need & ((1u << lane) - 1));
+        if (!busy && mine < cend) {
+          busy = true;
+          i = srow[mine];
+          j = scol[mine];
+          lb = *(volatile T*)(D + (int64_t)(i - row0) * ld + j);   // D_old[i][j]
+          ci = c1[i];
+          cj = TWO ? c2[i] : Tr<T>::inf();
+          acc = Tr<T>::inf();
+          b = 0;
+          h = 0;
+        }
+        next += __popc(need);
+      }
+      if (!__any_sync(0xffffffffu, busy)) break;
+      bool fin = false;
+      if (busy) {
+        if (h == 0) {   // a new batch: its 8 sorted shortlist entries
+          const int4* sid = reinterpret_cast<const int4*>(SLid + (int64_t)j * kSL) + 2 * b;
+          const int4* sw = reinterpret_cast<const int4*>(SLw + (int64_t)j * kSL) + 2 * b;
+          const int4 m0 = sid[0], m1 = sid[1], w0 = sw[0], w1 = sw[1];
+          m[0] = m0.x; m[1] = m0.y; m[2] = m0.z; m[3] = m0.w; m[4] = m1.x; m[5] = m1.y; m[6] = m1.z; m[7] = m1.w;
+          wi[0] = w0.x; wi[1] = w0.y; wi[2] = w0.z; wi[3] = w0.w; wi[4] = w1.x; wi[5] = w1.y; wi[6] = w1.z;
+          wi[7] = w1.w;
+        }
+        const int q0 = h == 0 ? 0 : 2, q1 = (b == 0 && h == 0) ? 2 : 8;
+        const T* Drow = D + (int64_t)(i - row0) * ld;
+        const uint8_t* Mrow = M8 ? M8 + (int64_t)(i - row0) * ld : nullptr;
+        T dv[8], rv[8], rv2[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q < q0 || q >= q1) continue;
+          const int mq = m[q] >= 0 ? m[q] : 0;
+          if (Mrow) {
+            const int32_t b8 = Mrow[mq];
+            dv[q] = (m[q] >= 0 && b8 != kSat8i) ? (T)b8 : Tr<T>::inf();
+          } else {
+            dv[q] = m[q] >= 0 ? *(volatile const T*)(Drow + mq) : Tr<T>::inf();
+          }
+          rv[q] = r1[mq];
+          if (TWO) rv2[q] = r2[mq];
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q < q0 || q >= q1) continue;
+          bool stale = Tr<T, SR>::tight(Tr<T, SR>::add(ci, rv[q]), dv[q], tau);
+          if (TWO) stale = stale || Tr<T, SR>::tight(Tr<T, SR>::add(cj, rv2[q]), dv[q], tau);
+          if (m[q] >= 0 && !stale) {
+            T w;
+            memcpy(&w, &wi[q], sizeof(T));
+            acc = Tr<T, SR>::relax(acc, dv[q], w);
+          }
+        }
+        if (Tr<T>::at_lb(acc, lb)) {
+          fin = true;
+        } else if (b == 0 && h == 0) {
+          h = 1;
+        } else {
+          ++b;
+          h = 0;
+          fin = b >= nbatch;
+        }
+      }
+      bool open = false;
+      if (fin) {
+        D[(int64_t)(i - row0) * ld + j] = acc;   // unconditionally: D_old is not an upper bound of D'
+        open = !Tr<T>::at_lb(acc, lb);
+        if (M.m || M.m8) mbits |= mput(M, (int64_t)(i - row0) * ld + j, acc);
+        busy = false;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, open);
+      if (bal) {
+        unsigned long long g0 = 0;
+        if (lane == __ffs(bal) - 1) g0 = atomicAdd(&ol.ctr->open_total, (unsigned long long)__popc(bal));
+        g0 = __shfl_sync(0xffffffffu, g0, __ffs(bal) - 1);
+        if (open) {
+          const int s1 = atomicAdd(ol.ocnt + i, 1);
+          ol.ocol[ol.rowoff[i] + s1] = j;
+          const unsigned long long s2 = g0 + __popc(bal & ((1u << lane) - 1));
+          if ((int64_t)s2 < ol.ocap) {
+            ol.gprow[s2] = i;
+            ol.gpcol[s2] = j;
+            ol.glb[s2] = lb;
+            ol.gfull[s2] = 1;
+          } else {
+            atomicOr(&ol.ctr->overflow, 2u);
+          }
+        }
+      }
+    }
+  }
+  if (M.m || M.m8) mirror_post(M, mbits);
+}
+
 // Phase A over the detection list (pairs in append order; every pair reads
 // and writes only its own row).
 template <typename T>
@@ -789,9 +920,16 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
   // npairs is the capacity bound (the device count decides): full occupancy
   int grid = (int)std::min<int64_t>(cdiv(npairs, 256), (int64_t)num_sms() * 8);
 #define PA(SRV, TWOV)                                                                              \
-  k_sparse_phase_a<T, SRV, TWOV><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, srow, scol, npairs, \
-                                                       c1, r1, c2, r2, tau, ol, ctr, M, nb)
+  do {                                                                                             \
+    if (queue)                                                                                     \
+      k_sparse_phase_aq<T, SRV, TWOV><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, srow, scol,  \
+                                                            npairs, c1, r1, c2, r2, tau, ol, ctr, M, nb); \
+    else                                                                                           \
+      k_sparse_phase_a<T, SRV, TWOV><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, srow, scol,   \
+                                                           npairs, c1, r1, c2, r2, tau, ol, ctr, M, nb); \
+  } while (0)
   static const int nb = std::min(kSL / 8, pa_tune("APSP_TUNE_PA_BATCHES", kPhaseABatches));
+  static const bool queue = pa_tune("APSP_TUNE_PA_QUEUE", 1) == 1;   // 2: the one-pair-per-lane kernel
   const bool two = c2 != nullptr;
   if (sr) { if (two) PA(1, true); else PA(1, false); }
   else { if (two) PA(0, true); else PA(0, false); }

@@ -837,7 +837,7 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   const bool try_packed = std::is_same<T, int32_t>::value && h->sr == 0;
   unsigned* unc = h->pass1_uncertain();
   if (try_packed) {
-    CKR(cudaMemsetAsync(unc, 0, sizeof(unsigned), h->st));
+    if (!srow) CKR(cudaMemsetAsync(unc, 0, sizeof(unsigned), h->st));   // (the gather path never reads it)
     const unsigned* cfull = nullptr;
     if constexpr (std::is_same<T, int32_t>::value) {
       if (srow) {   // the new row first (side stream), then col / the skip bound by gathers

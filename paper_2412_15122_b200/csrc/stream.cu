@@ -1212,6 +1212,9 @@ __global__ void __launch_bounds__(256) k_addnode_finish(const T* rowpart, const 
                                                         const unsigned* col_full) {
   if (gate == 1 && !pass1_packed_runs<T, 0>(M)) return;
   if (gate == 2 && pass1_packed_done<T, 0>(M, uncertain)) return;
+  if (row_full && col_full && *(volatile const unsigned*)row_full == 0u &&
+      *(volatile const unsigned*)col_full == 0u)
+    return;   // both the row and the column came from the shortcuts
   __shared__ T sm[8][32], sM[8][32];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   // grid-stride over the 32-index tiles (a small grid: the gated twin's exit is cheap)

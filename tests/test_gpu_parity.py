@@ -867,3 +867,42 @@ def test_add_node_gather_fallbacks(lib, rng):
     _sampled_rows_cols(h, hg.W, idx)
     cold = make(lib, hg.W, cap=n + 3)
     assert np.array_equal(getD(h), getD(cold))
+
+
+def test_new_node_shortlist_then_removals(lib, rng):
+    """The new node's shortlist SL(x) (exact top-512 in-edges by (weight, id),
+    built over 1024-entry chunks — n = 4100 ends inside a chunk) used by later
+    removals that list pairs in column x: (1) fewer than 512 finite in-edges
+    (dead entries) and zero weights (wmin = 0 in the column certification);
+    (2) every in-edge finite.  Sampled rows / columns against Dijkstra on the
+    host graph and the whole matrix against a cold FW of the final graph."""
+    n = 4100
+    W = random_graph(rng, n, True, density=0.02, lo=1, hi=9)
+    hg = synth.HostGraph(W, True, cap=n + 3)
+    h = make(lib, W, cap=n + 3)
+    assert h.mirror_width == 8
+    o = rng.integers(1, 9, n).astype(np.int32)
+    i = np.full(n, INF, np.int32)
+    fin = rng.choice(n, 300, replace=False)
+    i[fin] = rng.integers(1, 9, 300)
+    i[fin[:5]] = 0
+    o[rng.choice(n, 4, replace=False)] = 0
+    h.add_node(o, i)
+    hg.add_node(o, i)
+    for _ in range(3):
+        k = int(rng.integers(0, hg.n - 1))
+        h.remove_node(k)
+        hg.remove_node(k)
+    o2 = rng.integers(1, 12, hg.n).astype(np.int32)
+    i2 = rng.integers(1, 12, hg.n).astype(np.int32)
+    h.add_node(o2, i2)
+    hg.add_node(o2, i2)
+    for _ in range(2):
+        k = int(rng.integers(0, hg.n - 1))
+        h.remove_node(k)
+        hg.remove_node(k)
+    m = hg.n
+    idx = np.concatenate([rng.choice(m, 10, replace=False), [m - 1, m - 2]])
+    _sampled_rows_cols(h, hg.W[:m, :m], idx)
+    cold = make(lib, hg.W[:m, :m], cap=m + 1)
+    assert np.array_equal(getD(h), getD(cold))

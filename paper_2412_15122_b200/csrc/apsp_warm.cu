@@ -785,6 +785,29 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
                      h->directed ? nullptr : reinterpret_cast<const T*>(out_w), iw,   // both vectors, one launch
                      std::is_same<T, int32_t>::value ? as.argmin_out : nullptr,
                      std::is_same<T, int32_t>::value ? as.in_min : nullptr));
+  // the new row from the few rows that can attain it (one GPU, int8 mirror
+  // valid): on the side stream, launched before the validation read so it
+  // overlaps the host round trip (it writes scratch only; a rejected call
+  // waits for it before returning, and if that read shows the mirror
+  // invalidated the shortcuts are dropped)
+  bool srow = false;
+  // (small graphs: the one streaming pass costs less than the shortcuts' extra launches)
+  if constexpr (std::is_same<T, int32_t>::value)
+    srow = h->world == 1 && n >= kAddShortcutMinN && n < (int64_t(1) << 24) && h->plan.maxchunk >= 2 &&
+           2 * kAddColLimit <= ld && mirror8_known_valid(h);   // (k_addrow packs t in 24 bits)
+  if constexpr (std::is_same<T, int32_t>::value) {
+    if (srow) {
+      CKR(cudaEventRecord(h->ev_fork, h->st));
+      CKR(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
+      // scratch: the (value, minimiser) row, the minimiser flags and U's in /
+      // out lists live in the pass-1 partial buffer (4 ld words: unused unless
+      // the gathers fall back to pass 1, which runs after they are consumed)
+      CK2(addrow_s(as, ow, n, h->mirror<T>().m8, ld, h->row0, row, ld, reinterpret_cast<int*>(h->vec<T>(5)),
+                   reinterpret_cast<unsigned long long*>(h->rowpart<T>()),
+                   reinterpret_cast<int*>(h->rowpart<T>()) + 2 * ld, h->st2));
+      CKR(cudaEventRecord(h->ev_row, h->st2));
+    }
+  }
   unsigned* herr = reinterpret_cast<unsigned*>(h->host_small);
   {
     ReadSet rs{};
@@ -796,32 +819,21 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   CKR(cudaStreamSynchronize(h->st));
   h->mirror_hint = (herr[2] & 1u) == 0u;
   if (*herr) {
+    if (srow) CKR(cudaStreamSynchronize(h->st2));   // the scratch is free again
     return fail(h, APSP_E_INVAL, "add_node: %s",
                 (*herr & 2) ? "undirected graph needs out_w == in_w" : "negative or NaN weight");
   }
   h->wmin_bits = std::min(h->wmin_bits, herr[1]);
+  if (srow && !mirror8_known_valid(h)) {
+    // the flag read just now says the int8 mirror was invalidated since the
+    // last host read: no shortcuts; the row chain's scratch must be free first
+    srow = false;
+    CKR(cudaStreamWaitEvent(h->st, h->ev_row, 0));
+  }
   // shortlist upkeep needs only the validated edge vectors: it runs on the
   // side stream while pass 1 / rank-1 stream D (joined before returning)
   CKR(cudaEventRecord(h->ev_fork, h->st));
   CKR(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
-  // the new row from the few rows that can attain it (one GPU, int8 mirror
-  // valid as read above): on the side stream, under pass 1
-  bool srow = false;
-  // (small graphs: the one streaming pass costs less than the shortcuts' extra launches)
-  if constexpr (std::is_same<T, int32_t>::value)
-    srow = h->world == 1 && n >= kAddShortcutMinN && n < (int64_t(1) << 24) && h->plan.maxchunk >= 2 &&
-           2 * kAddColLimit <= ld && mirror8_known_valid(h);   // (k_addrow packs t in 24 bits)
-  if constexpr (std::is_same<T, int32_t>::value) {
-    if (srow) {
-      // scratch: the (value, minimiser) row, the minimiser flags and U's in /
-      // out lists live in the pass-1 partial buffer (4 ld words: unused unless
-      // the gathers fall back to pass 1, which runs after they are consumed)
-      CK2(addrow_s(as, ow, n, h->mirror<T>().m8, ld, h->row0, row, ld, reinterpret_cast<int*>(h->vec<T>(5)),
-                   reinterpret_cast<unsigned long long*>(h->rowpart<T>()),
-                   reinterpret_cast<int*>(h->rowpart<T>()) + 2 * ld, h->st2));
-      CKR(cudaEventRecord(h->ev_row, h->st2));
-    }
-  }
   CK2(shortlist_add_bound<T>(h->slid(), h->slw<T>(), h->wnext<T>(), ow, n, x, h->st2));  // x -> j
   CK2(shortlist_build_one<T>(iw, 0, n + 1, x, h->slid(), h->slw<T>(), h->wnext<T>(), h->slscr(),
                              h->st2));   // in-edges of x: row x of WT is in_w

@@ -950,15 +950,20 @@ template <typename T>
 apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp_update_info* info) {
   const int64_t n = h->n, ld = h->ld;
   T* WT = h->WT<T>();
-  // 8-byte read: W[u][v] (replicated WT) and D[u][v] (owner of row u)
-  T* dev2 = reinterpret_cast<T*>(h->small());
-  CKR(cudaMemcpyAsync(dev2, WT + v * ld + u, sizeof(T), cudaMemcpyDeviceToDevice, h->st));
-  if (h->local(u))
-    CKR(cudaMemcpyAsync(dev2 + 1, h->Drow<T>(u) + v, sizeof(T), cudaMemcpyDeviceToDevice, h->st));
-  if (h->world > 1)
-    NK(h->comm->bcast(dev2 + 1, 1, nccl_type<T>(), h->owner(u), h->st));
+  // 8-byte read: W[u][v] (replicated WT) and D[u][v] (owner of row u) —
+  // one GPU: both words straight into the mapped host buffer by one kernel
   T* hv = reinterpret_cast<T*>(h->host_small);
-  {
+  if (h->world == 1) {
+    ReadSet rs{};
+    rs.add(WT + v * ld + u, sizeof(T));
+    rs.add(h->Drow<T>(u) + v, sizeof(T));
+    CK(readback(rs, h->host_small_dev, h->st));
+  } else {
+    T* dev2 = reinterpret_cast<T*>(h->small());
+    CKR(cudaMemcpyAsync(dev2, WT + v * ld + u, sizeof(T), cudaMemcpyDeviceToDevice, h->st));
+    if (h->local(u))
+      CKR(cudaMemcpyAsync(dev2 + 1, h->Drow<T>(u) + v, sizeof(T), cudaMemcpyDeviceToDevice, h->st));
+    NK(h->comm->bcast(dev2 + 1, 1, nccl_type<T>(), h->owner(u), h->st));
     ReadSet rs{};
     rs.add(dev2, 2 * sizeof(T));
     CK(readback(rs, h->host_small_dev, h->st));

@@ -1500,7 +1500,7 @@ cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, 
   int grid = (int)cdiv(tl.warps, 8);
   if constexpr (std::is_same<T, int32_t>::value) {
     if (!sr && M.m8) {   // the int8 twin first (the int32 kernel then exits while M stays valid)
-      static const int wps = tune_wps("APSP_TUNE_R8_WPS", 32);
+      static const int wps = tune_wps("APSP_TUNE_R8_WPS", 16);   // (measured: 16 -> 29 us, 32 -> 32 us at BJ.c4)
       const Tiling t8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256, wps);
       const int g8 = (int)cdiv(t8.warps, 8);
       if (c2)

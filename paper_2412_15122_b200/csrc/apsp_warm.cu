@@ -253,6 +253,8 @@ struct apsp_handle {
   unsigned* fw16_flag() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 392); }
   unsigned* mirror_flag() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 396); }
   unsigned* pass1_uncertain() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 400); }
+  unsigned* mirror_epoch_word() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 472); }
+  unsigned mirror_epoch = 0;     // per-launch epochs of the rank-1 gate (Mirror::epoch)
   // the add-node shortcuts' scratch words (small + 404 ... 463)
   AddScratch add_scratch() {
     unsigned char* b = ws + plan.off_small;
@@ -266,8 +268,9 @@ struct apsp_handle {
   // or int16 (in the packed-FW buffer), the width picked at the last build
   template <typename T> Mirror mirror() {
     if constexpr (std::is_same<T, int32_t>::value) {
-      if (mirror_level == 8) return Mirror{nullptr, ws + plan.off_p8, mirror_flag()};
-      return Mirror{reinterpret_cast<uint16_t*>(p16()), nullptr, mirror_flag()};
+      if (mirror_level == 8)
+        return Mirror{nullptr, ws + plan.off_p8, mirror_flag(), mirror_epoch_word(), ++mirror_epoch};
+      return Mirror{reinterpret_cast<uint16_t*>(p16()), nullptr, mirror_flag(), mirror_epoch_word(), ++mirror_epoch};
     } else {
       return Mirror{nullptr, nullptr, mirror_flag()};
     }

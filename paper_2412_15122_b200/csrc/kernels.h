@@ -17,6 +17,11 @@ struct Mirror {
   uint16_t* m;      // int16 level (nullptr: not this width / no mirror)
   uint8_t* m8;      // int8 level
   unsigned* flag;   // bit 0 clear: the mirror images D exactly
+  // k_rank1_p8's launch gate: a launch that raises bit 0 itself first stores
+  // its `epoch` (unique per launch, from the host) in *ep, so its own later
+  // CTAs still see the pre-launch state (rows left un-relaxed otherwise)
+  unsigned* ep = nullptr;
+  unsigned epoch = 0;
 };
 
 // Device counters written by the detection kernel.

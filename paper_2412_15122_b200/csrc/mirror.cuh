@@ -20,6 +20,11 @@ __device__ __forceinline__ unsigned mput(const Mirror& M, int64_t idx, int32_t v
   M.m[idx] = sat16(v);
   return v >= APSP_INF_I32_DEV ? kMirrorInf : (v >= kSat16i ? kMirrorOff : 0u);
 }
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ bool has_mirror(const Mirror& M) { return M.m != nullptr || M.m8 != nullptr; }
 __device__ __forceinline__ unsigned mput(const Mirror&, int64_t, float) { return 0u; }
 __device__ __forceinline__ void mirror_post(const Mirror& M, unsigned bits) {

@@ -837,12 +837,12 @@ __global__ void __launch_bounds__(256) k_addrow(AddScratch a, const int32_t* __r
   for (int s = s0; s < s1; ++s) {
     const int t = slist[s];
     const int32_t o = ow[t];
-    const unsigned long long lo = (unsigned long long)(min(o - omin, 255) << 24 | t);
+    const unsigned long long lo = (unsigned long long)(((unsigned)min(o - omin, 255) << 24) | (unsigned)t);
     const uint32_t w = *reinterpret_cast<const uint32_t*>(m8 + ((int64_t)t - row0) * ld + j0);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int32_t d = (int32_t)((w >> (8 * e)) & 0xFFu);
-      if (d != kSat8i) acc[e] = min(acc[e], (unsigned long long)(unsigned)(o + d) << 32 | lo);
+      if (d != kSat8i) acc[e] = min(acc[e], (unsigned long long)(unsigned)min(o + d, APSP_INF_I32_DEV) << 32 | lo);
     }
   }
 #pragma unroll
@@ -941,7 +941,7 @@ __global__ void __launch_bounds__(256) k_addcol_gather(AddScratch a, Rows r, con
         const int k = k0 + 32 * q + lane;
         const int32_t av = k < cnt ? __ldg(uin + k) : I, bv = k < cnt ? __ldg(uout + k) : I;
         const bool fin = d[q] != kSat8i;
-        if (fin && av < I) p = min(p, d[q] + av);
+        if (fin && av < I) p = min(p, min(d[q] + av, I));
         // an INF entry with a finite out: never skip (as in pass 1)
         if (bv < I) m = max(m, fin ? d[q] - bv : I);
       }
@@ -980,12 +980,12 @@ __global__ void __launch_bounds__(256) k_addcol_rows(AddScratch a, Rows r, const
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int32_t d8 = (int32_t)((w >> (8 * e)) & 0xFFu), a = __ldg(iw + 4 * q + e);
-        if (d8 != kSat8i && a < I) p = min(p, d8 + a);
+        if (d8 != kSat8i && a < I) p = min(p, min(d8 + a, I));
       }
     }
     for (int64_t t = 4 * n4 + threadIdx.x; t < n; t += blockDim.x) {
       const int32_t d8 = mrow[t], a = iw[t];
-      if (d8 != kSat8i && a < I) p = min(p, d8 + a);
+      if (d8 != kSat8i && a < I) p = min(p, min(d8 + a, I));
     }
     p = __reduce_min_sync(0xffffffffu, p);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;
@@ -1367,7 +1367,12 @@ __global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, in
                                                      const int32_t* __restrict__ rv, const int32_t* __restrict__ c2,
                                                      const int32_t* __restrict__ rv2,
                                                      unsigned long long* __restrict__ bytes_read, Mirror M) {
-  if (M.m8 == nullptr || (*(volatile unsigned*)M.flag & kMirrorOff)) return;
+  if (M.m8 == nullptr) return;
+  {   // the gate is the flag as it was before this launch: bit 0 raised by this
+      // launch's own CTAs (they store the epoch first) does not count
+    const unsigned f0 = ld_acquire(M.flag);
+    if ((f0 & kMirrorOff) && (M.ep == nullptr || *(volatile unsigned*)M.ep != M.epoch)) return;
+  }
   // No INF entry: min(d, c + r) in packed int16x2 is exact — d <= 0x7E, and
   // a saturated c + r (>= 0x3FFF) exceeds every finite d.  With INF entries
   // (0x7F) a finite c + r >= 0x3FFF could still lower one: per-entry int32.
@@ -1484,7 +1489,14 @@ __global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, in
       }
     }
   }
-  mirror_post(M, mbits);
+  mbits = __reduce_or_sync(0xffffffffu, mbits);
+  if (lane == 0 && (mbits & ~*(volatile unsigned*)M.flag)) {
+    if ((mbits & kMirrorOff) && M.ep) {
+      atomicExch(M.ep, M.epoch);   // before the bit: a CTA that sees the bit sees the epoch
+      __threadfence();
+    }
+    atomicOr(M.flag, mbits);
+  }
   if (bytes_read && lane == 0 && rows_read) {
     const int64_t cols = min((int64_t)1024, n - (int64_t)chunk * 1024);
     atomicAdd(bytes_read, (unsigned long long)(rows_read * cols));

@@ -906,3 +906,35 @@ def test_new_node_shortlist_then_removals(lib, rng):
     _sampled_rows_cols(h, hg.W[:m, :m], idx)
     cold = make(lib, hg.W[:m, :m], cap=m + 1)
     assert np.array_equal(getD(h), getD(cold))
+
+
+def test_add_node_heavy_out_edges_to_unreachable(lib, rng):
+    """ADVICE r1 (two bugs on the add-node shortcut path, n >= 4096, int8
+    mirror): nodes 0-9 have no in-edges, so the new node's row there is its
+    own out-edge out[j] ~ U[1,1000] (>= omin + 128 for most j: the minimiser
+    key must not sign-extend), and rank-1 then writes distances >= 0x7F into
+    columns 0-9 of every row — the int8 mirror goes invalid during the rank-1
+    launch, whose later CTAs must still relax their rows.  Whole matrix vs the
+    oracle's cold FW of the same graph; then a removal and a second add on the
+    (now int16) mirror."""
+    n = 4200
+    W = random_graph(rng, n, True, density=0.02, lo=1, hi=9)
+    W[:, :10] = INF            # nodes 0-9: no in-edges
+    np.fill_diagonal(W, 0)
+    hg = synth.HostGraph(W, True, cap=n + 3)
+    h = make(lib, W, cap=n + 3)
+    assert h.mirror_width == 8
+    o = rng.integers(1, 1001, n).astype(np.int32)
+    o[rng.choice(np.arange(10, n), 3, replace=False)] = 1     # omin = 1, outside 0-9
+    i = rng.integers(1, 40, n).astype(np.int32)
+    h.add_node(o, i)
+    hg.add_node(o, i)
+    assert_parity(getD(h), oracle.fw(hg.W))
+    k = int(rng.integers(10, hg.n - 1))
+    h.remove_node(k)
+    hg.remove_node(k)
+    o2 = rng.integers(1, 1001, hg.n).astype(np.int32)
+    i2 = rng.integers(1, 1001, hg.n).astype(np.int32)
+    h.add_node(o2, i2)
+    hg.add_node(o2, i2)
+    assert_parity(getD(h), oracle.fw(hg.W[:hg.n, :hg.n]))

@@ -54,6 +54,10 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-cold", action="store_true", help="skip timing one cold FW")
     p.add_argument("--json-extra", default=None, help="write the detailed report here")
+    p.add_argument("--no-verify", action="store_true", help="skip the post-run oracle check")
+    p.add_argument("--no-int32", action="store_true",
+                   help="skip the profiled pass on the int32 streams (APSP_OPT_MIRROR=0)")
+    p.add_argument("--verify-samples", type=int, default=16)
     return p.parse_args()
 
 
@@ -177,6 +181,62 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- post-run check
+def final_check(h, hg, seq, rank, world, pg, dev, samples=16):
+    """Sampled rows and columns of the final D (every update of the run applied)
+    against oracle Dijkstra on the host graph: the ids the last updates touched
+    (x, the moved slot, u, v) plus random ones.  Rows / column slices are
+    gathered from their owners when D is sharded; rank 0 compares."""
+    import torch
+
+    n = h.n
+    ids = []
+    for up in reversed(seq):
+        cand = {"add": [up.n_before], "remove": [up.k], "reweight": [up.u, up.v]}[up.kind]
+        ids += [x for x in cand if 0 <= x < n and x not in ids]
+        if len(ids) >= samples // 2:
+            break
+    rng = np.random.default_rng(7)
+    for x in rng.permutation(n):
+        if len(ids) >= samples:
+            break
+        if int(x) not in ids:
+            ids.append(int(x))
+    ids = np.asarray(ids[:samples], np.int64)
+    torch.cuda.synchronize(dev)
+    lo, hi = min(h.row0, n), min(h.row0 + h.rows, n)
+    it = torch.as_tensor(ids, device=dev)
+    cols_local = h.D.index_select(1, it).cpu().numpy()          # (hi - lo) x samples
+    mine = [(int(i), h.D[int(i) - lo].cpu().numpy()) for i in ids if lo <= i < hi]
+    if world > 1:
+        got_c, got_r = [None] * world, [None] * world
+        pg.all_gather_object(got_c, (lo, cols_local))
+        pg.all_gather_object(got_r, mine)
+    else:
+        got_c, got_r = [(lo, cols_local)], [mine]
+    if rank != 0:
+        return None
+    import oracle   # test infrastructure: the checker, never on the product path
+
+    C = np.full((n, len(ids)), -1, np.int64)
+    for l0, blk in got_c:
+        C[l0:l0 + blk.shape[0]] = blk
+    R = dict(x for part in got_r for x in part)
+    Rm = np.stack([R[int(i)] for i in ids])
+    t0 = time.perf_counter()
+    Wv = hg.W
+    exp_r = oracle.dijkstra_rows_i32(Wv, ids)
+    WT = np.ascontiguousarray(Wv.T)
+    exp_c = oracle.dijkstra_rows_i32(WT, ids).T
+    del WT
+    dt = time.perf_counter() - t0
+    bad_r = int(np.count_nonzero(Rm != exp_r))
+    bad_c = int(np.count_nonzero(C != exp_c))
+    return {"ok": bad_r == 0 and bad_c == 0, "n": n, "updates_applied": len(seq), "rows": len(ids),
+            "cols": len(ids), "ids": ids.tolist(), "mismatches": bad_r + bad_c,
+            "oracle": "Dijkstra rows + columns (transposed W) on the host graph", "oracle_s": round(dt, 2)}
+
+
 # ----------------------------------------------------------------------------- our leg
 def main():
     args = parse()
@@ -206,12 +266,16 @@ def main():
     spec = dataclasses.replace(synth.C4, n=args.n, seed=args.seed)
     n0 = spec.n
     # warm-up, timed, e2e and profiled steps each consume their own updates
-    steps_total = args.warmup + 2 * args.steps + (0 if args.no_e2e else args.steps)
+    steps_total = (args.warmup + 2 * args.steps + (0 if args.no_e2e else args.steps) +
+                   (0 if args.no_int32 else args.steps))
     cap = n0 + UPDATES_PER_STEP + 4 * steps_total
     t_setup = time.perf_counter()
     W = synth.graph(spec)
     hg = synth.HostGraph(W, True, cap=cap)
     seq = synth.update_sequence(spec, hg, 0, steps_total * UPDATES_PER_STEP)
+    # hg now holds W after every update the run applies: the post-run check
+    # compares the GPU's final state with the oracle on it (rank 0 keeps it)
+    hg_final = hg if rank == 0 else None
     del hg
 
     nccl_id = None
@@ -361,6 +425,25 @@ def main():
     L.apsp_profile_enable(h.h, False)
     prof = L.apsp_profile_read(h.h)
 
+    # ---------------- profiled pass on the 4-byte streams: the same kind of
+    # steps with the saturated mirror switched off (APSP_OPT_MIRROR = 0), so
+    # detection, add-node pass 1 and rank-1 stream the int32 D itself at
+    # SURVEY §8(d-4)'s 4 bytes per entry (after every timed number is taken)
+    prof32 = None
+    if not args.no_int32:
+        L.apsp_set_option(h.h, L.OPT_MIRROR, 0)
+        s32 = s_prof + args.steps
+        run_step(s32, False)     # the first update after the switch drops the mirror
+        torch.cuda.synchronize(dev)
+        L.apsp_profile_reset(h.h)
+        L.apsp_profile_enable(h.h, True)
+        barrier()
+        for s in range(s32 + 1, s32 + args.steps):
+            run_step(s, False)
+        barrier()
+        L.apsp_profile_enable(h.h, False)
+        prof32 = L.apsp_profile_read(h.h)
+
     # ---------------- K13: the roofline denominators measured on this device
     k13 = None
     try:
@@ -407,6 +490,25 @@ def main():
         if k13 and k13.get("hbm_read_gbs"):   # the same kernel against the measured read-only stream
             roof["k13_read_gbs"] = k13["hbm_read_gbs"]
             roof["frac_of_k13_read"] = achieved / k13["hbm_read_gbs"]
+    roof["basis"] = ("algorithmic bytes of the stream the kernel reads: the int8 mirror of D (1 B/entry) "
+                     "while every distance is < 0x7F, else int16 (2 B) or D itself (4 B); DESIGN.md §6")
+    roof32 = None
+    if prof32 is not None:
+        # the dominant O(n^2) stream class with the mirror off, on §8(d-4)'s 4 B/entry
+        cand = {k: v for k, v in prof32.items() if k in ("detect", "add_pass1", "rank1") and v[0] > 0}
+        if cand:
+            d32 = max(cand, key=lambda k: cand[k][0])
+            ms32, c32, w32 = prof32[d32]
+            a32 = w32 / (ms32 / 1e3) / 1e9
+            roof32 = {"bound": "hbm", "kernel": d32, "achieved": a32, "peak": hbm_peak, "unit": "GB/s",
+                      "frac": a32 / hbm_peak, "traffic": None, "launches": c32,
+                      "peak_kind": f"{peak_kind} copy bandwidth",
+                      "basis": "int32 D, 4 B per entry read (SURVEY §8(d-4)); APSP_OPT_MIRROR = 0",
+                      "classes": {k: {"ms": round(v[0], 3), "launches": v[1],
+                                      "achieved_gbs": round(v[2] / (v[0] / 1e3) / 1e9, 1) if v[0] > 0 else None}
+                                  for k, v in prof32.items() if v[1] > 0}}
+            if k13 and k13.get("hbm_read_gbs"):
+                roof32["frac_of_k13_read"] = a32 / k13["hbm_read_gbs"]
     share = {k: round(v[0] / max(prof_total_ms, 1e-9), 4) for k, v in prof.items()}
     kern = {k: {"ms": round(v[0], 3), "launches": v[1],
                 "achieved": (round(v[2] / (v[0] / 1e3) / (1e12 if k.startswith("fw") else 1e9), 2) if v[0] > 0 else None),
@@ -438,6 +540,11 @@ def main():
                "sample": f"{p} Floyd-Warshall pivots of the n={n} int64 oracle matrix "
                          f"({tp * 1e3:.1f} ms/pivot), extrapolated x n: the oracle's cold recompute per update"}
 
+    # ---------------- post-run check of the final state (test infrastructure,
+    # outside every timed region): sampled rows / columns of the GPU's D after
+    # all the updates vs oracle Dijkstra on the host graph
+    verify = None if args.no_verify else final_check(h, hg_final, seq, rank, world, pg, dev,
+                                                      args.verify_samples)
     n_final = h.n
     if rank == 0:
         line = {
@@ -452,6 +559,7 @@ def main():
                        "ms_per_update_mean": statistics.mean(all_ms),
                        "cold_fw_ms": cold_ms, "warm_vs_cold_speedup": cold_ms / statistics.mean(all_ms)},
             "roofline": roof,
+            "roofline_int32": roof32,
             "k13": k13,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -461,12 +569,15 @@ def main():
             "kernel_share": share,
             "per_type": breakdown,
             "setup_s": setup_s,
+            "verify": verify,
         }
         print(json.dumps(line), flush=True)
         if args.json_extra:
             with open(args.json_extra, "w") as f:
                 json.dump(line, f, indent=1)
     h.close()
+    if verify is not None and not verify["ok"]:
+        sys.exit(3)   # the reported number was taken on a wrong state
     if pg is not None:
         pg.destroy_process_group()
 

@@ -104,12 +104,17 @@ typedef enum {
                                distance < 0x3FFF; if any entry saturates it finishes
                                in int32 — results are identical either way.
                                0: always int32.                                       */
-  APSP_OPT_MIRROR8 = 7      /* 1 (default): on int32 shortest-path handles the two
+  APSP_OPT_MIRROR8 = 7,     /* 1 (default): on int32 shortest-path handles the two
                                O(n^2) streaming passes (add-node pass 1, detection)
                                read an int8 copy of D while every finite distance is
                                < 0x7F, else an int16 copy while every one is < 0x3FFF,
                                else D itself; results are identical on every path.
                                0: never int8 (int16 / int32 only).                    */
+  APSP_OPT_MIRROR = 8       /* 1 (default): keep the saturated mirror of APSP_OPT_MIRROR8.
+                               0: no mirror at all — every O(n^2) pass streams the
+                               int32 D itself (4 bytes per entry, SURVEY §8(d-4)'s
+                               byte basis); for measuring the 4-byte streams.  Results
+                               are identical.  Takes effect at the next update.       */
 } apsp_option;
 
 /* Statistics of one update. */
@@ -268,6 +273,22 @@ apsp_status sp_pair_query(apsp_handle* h, int64_t s, int64_t t, void* dist, int3
 apsp_status sp_pair_query_batch(apsp_handle* h, int32_t q, const int32_t* s, const int32_t* t,
                                 void* dist, int32_t* paths, int32_t path_cap,
                                 int32_t* path_lens, int32_t* n_cand);
+
+/* TEST / DIAGNOSTIC export of the need_update_list of a
+ * prospective update, computed by the same snapshot + detection kernels the
+ * update runs, WITHOUT applying the update (D, WT and n are unchanged):
+ *   kind 4: removal of node a — pairs (i, j), i, j != a, D[i][j] < INF, with
+ *           D[i][a] + D[a][j] == D[i][j] (Corollary 3);
+ *   kind 2: increase of edge (a, b) — pairs with D[i][a] + w(a,b) + D[b][j] ==
+ *           D[i][j] (undirected: or D[i][b] + w + D[a][j] == D[i][j]), w the
+ *           current weight (Theorem 4's edge analogue); fp32 uses
+ *           the tolerant test of APSP_OPT_TAU (Q4).
+ * rows/cols (host, cap entries each) receive the pairs in global ids, in the
+ * kernel's flush order (unsorted); *count = |A| (only min(|A|, cap) written).
+ * Multi-GPU: each rank returns the pairs of its own rows.  Synchronises.
+ * Errors: E_INVAL (bad kind, null output, u == v), E_RANGE (ids). */
+apsp_status apsp_need_update_list(apsp_handle* h, int32_t kind, int64_t a, int64_t b, int32_t* rows,
+                                  int32_t* cols, int64_t cap, int64_t* count);
 
 /* Current weight w(u -> v) (host, 4 bytes of the handle's dtype; INF if
  * absent).  Synchronises the stream.  E_RANGE for ids outside [0, n). */

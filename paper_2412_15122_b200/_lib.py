@@ -19,7 +19,8 @@ STATUS = {
     0: "APSP_OK", 1: "APSP_E_INVAL", 2: "APSP_E_RANGE", 3: "APSP_E_CAPACITY", 4: "APSP_E_PRECOND",
     5: "APSP_E_CUDA", 6: "APSP_E_NCCL", 7: "APSP_E_NOMEM", 8: "APSP_E_POISONED", 9: "APSP_E_UNSUPPORTED",
 }
-OPT_FORCE_PATH, OPT_THETA, OPT_TAU, OPT_MAX_ROUNDS, OPT_ROW_DELTA, OPT_SEMIRING, OPT_FW16, OPT_MIRROR8 = range(8)
+(OPT_FORCE_PATH, OPT_THETA, OPT_TAU, OPT_MAX_ROUNDS, OPT_ROW_DELTA, OPT_SEMIRING, OPT_FW16, OPT_MIRROR8,
+ OPT_MIRROR) = range(9)
 
 # exported symbols (tests check the library exports every one of them)
 SYMBOLS = [
@@ -29,7 +30,7 @@ SYMBOLS = [
     "apsp_nccl_unique_id", "apsp_kernel_launches", "apsp_profile_enable", "apsp_profile_reset",
     "apsp_profile_read", "apsp_modify_edge_readd", "apsp_get_weight",
     "apsp_local_group_create", "apsp_local_group_destroy", "apsp_create_local", "apsp_microbench",
-    "apsp_sync_distances", "apsp_mirror_width",
+    "apsp_sync_distances", "apsp_mirror_width", "apsp_need_update_list",
 ]
 # kernel classes of apsp_profile_read (apsp_kernel_class)
 K_CLASSES = ["fw_diag", "fw_panel", "fw_tile", "add_pass1", "rank1", "detect", "sparse0",
@@ -85,6 +86,7 @@ def _load():
         "sp_pair_query_batch": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, i32, vp, vp]),
         "apsp_size": (i64, [vp]),
         "apsp_get_weight": (ctypes.c_int, [vp, i64, i64, vp]),
+        "apsp_need_update_list": (ctypes.c_int, [vp, i32, i64, i64, vp, vp, i64, P(i64)]),
         "apsp_last_error": (ctypes.c_char_p, [vp]),
         "apsp_status_string": (ctypes.c_char_p, [ctypes.c_int]),
         "apsp_nccl_unique_id": (ctypes.c_int, [vp]),
@@ -222,6 +224,20 @@ def apsp_get_weight(h, u, v, dtype):
     w = ctypes.c_int32() if dtype == APSP_I32 else ctypes.c_float()
     check(h, lib.apsp_get_weight(h, u, v, ctypes.byref(w)))
     return w.value
+
+
+def apsp_need_update_list(h, kind, a, b, cap):
+    """(rows, cols, |A|) of a prospective removal (kind 4, node a) or edge
+    increase (kind 2, edge (a, b)); test / diagnostic export (apsp_warm.h)."""
+    import numpy as np
+
+    rows = np.empty(max(cap, 1), np.int32)
+    cols = np.empty(max(cap, 1), np.int32)
+    cnt = ctypes.c_int64()
+    check(h, lib.apsp_need_update_list(h, kind, a, b, rows.ctypes.data, cols.ctypes.data, cap,
+                                       ctypes.byref(cnt)))
+    m = min(cnt.value, cap)
+    return rows[:m], cols[:m], cnt.value
 
 
 def apsp_size(h):

@@ -132,6 +132,17 @@ class WarmAPSP:
         re-add it with the edited edge.  Returns (removed endpoint, info)."""
         return L.apsp_modify_edge_readd(self.h, int(u), int(v), float(w_new))
 
+    def need_update_list(self, kind, a, b=-1, cap=None):
+        """Test export: the affected pairs (rows, cols) a removal of node a
+        (kind 'remove') or an increase of edge (a, b) (kind 'increase') would
+        list, by the library's own detection kernels; nothing is applied."""
+        k = {"remove": 4, "increase": 2}[kind]
+        n = self.n
+        cap = n * n if cap is None else int(cap)
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        r, c, cnt = L.apsp_need_update_list(self.h, k, int(a), int(b), cap)
+        return r, c, cnt
+
     def weight(self, u, v):
         """Current w(u -> v) as held on the device (WT)."""
         return L.apsp_get_weight(self.h, int(u), int(v), self.cdtype)

@@ -150,6 +150,7 @@ struct apsp_handle {
   bool mirror_hint = false;      // last observed mirror state was "valid" (profile accounting only)
   int mirror_level = 16;         // width of the mirror: 8 or 16 bits
   int mirror8 = 1;               // APSP_OPT_MIRROR8: try the int8 width at each build
+  int use_mirror = 1;            // APSP_OPT_MIRROR: 0 = no mirror, the streams read D (4 B/entry)
   bool mirror8_failed = false;   // an int8 build found a distance >= 0x7F: int16 from then on
   // bytes per entry the O(n^2) streams read: 1 / 2 on a valid int8 / int16 mirror, else 4
   template <typename T> double stream_bytes() const {
@@ -268,6 +269,7 @@ struct apsp_handle {
   // or int16 (in the packed-FW buffer), the width picked at the last build
   template <typename T> Mirror mirror() {
     if constexpr (std::is_same<T, int32_t>::value) {
+      if (!use_mirror) return Mirror{nullptr, nullptr, mirror_flag()};
       if (mirror_level == 8)
         return Mirror{nullptr, ws + plan.off_p8, mirror_flag(), mirror_epoch_word(), ++mirror_epoch};
       return Mirror{reinterpret_cast<uint16_t*>(p16()), nullptr, mirror_flag(), mirror_epoch_word(), ++mirror_epoch};
@@ -441,6 +443,12 @@ apsp_status mirror8_settle(apsp_handle* h, bool* need16) {
 template <typename T>
 apsp_status mirror_rebuild(apsp_handle* h) {
   if constexpr (std::is_same<T, int32_t>::value) {
+    if (!h->use_mirror) {   // APSP_OPT_MIRROR = 0: the streams read D itself
+      CKR(cudaMemsetAsync(h->mirror_flag(), 0xff, sizeof(unsigned), h->st));
+      h->mirror_hint = false;
+      h->mirror_built = true;
+      return APSP_OK;
+    }
     bool need16 = true;
     if (try_mirror8(h)) {
       h->mirror_level = 8;
@@ -530,6 +538,7 @@ apsp_status fw_impl(apsp_handle* h, int64_t skip = -1) {
       apsp_status s = fw16_impl(h, skip, &saturated);
       if (s != APSP_OK) return s;
       h->last_fw16 = saturated ? 2 : 1;
+      if (!saturated && !h->use_mirror) return mirror_rebuild<T>(h);
       if (!saturated) {   // the packed buffer now holds sat16(D): the int16 mirror is valid
         bool need16 = true;
         if (try_mirror8(h)) {   // narrow it to int8 if every distance is < 0x7F
@@ -849,7 +858,7 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   // (shortest path, int32), else — or if a new-row/column value came out
   // >= 0x3FFF — in int32.  The choice is made on the device: each launch
   // below exits when it does not apply (gate flags, stream order).
-  const bool try_packed = std::is_same<T, int32_t>::value && h->sr == 0;
+  const bool try_packed = std::is_same<T, int32_t>::value && h->sr == 0 && h->use_mirror;
   unsigned* unc = h->pass1_uncertain();
   if (try_packed) {
     if (!srow) CKR(cudaMemsetAsync(unc, 0, sizeof(unsigned), h->st));   // (the gather path never reads it)
@@ -1216,6 +1225,59 @@ apsp_status query_one(apsp_handle* h, int64_t s, int64_t t, void* dist, int32_t*
   return APSP_OK;
 }
 
+// ------------------------------------------------------------------ test export
+// The need_update_list of a prospective update, by the same snapshot and
+// detection launches the update itself runs (MODE 1), without applying it.
+template <typename T>
+apsp_status need_list_impl(apsp_handle* h, int kind, int64_t a, int64_t b, int32_t* rows, int32_t* cols,
+                           int64_t cap, int64_t* count) {
+  {
+    apsp_status ms = ensure_mirror<T>(h);
+    if (ms != APSP_OK) return ms;
+  }
+  const int64_t n = h->n;
+  Rows r = h->active();
+  T* c1 = h->vec<T>(4);
+  T* r1 = h->vec<T>(5);
+  T* c2 = h->vec<T>(6);
+  T* r2 = h->vec<T>(7);
+  const bool und = kind == 2 && !h->directed;
+  int64_t skip = -1;
+  apsp_status s;
+  if (kind == 4) {
+    skip = a;
+    s = snap_pivots<T>(h, a, T(0), c1, a, r1);
+  } else {
+    T* hv = reinterpret_cast<T*>(h->host_small);
+    CKR(cudaMemcpyAsync(hv, h->WT<T>() + b * h->ld + a, sizeof(T), cudaMemcpyDeviceToHost, h->st));
+    CKR(cudaStreamSynchronize(h->st));
+    const T w_old = hv[0];
+    s = snap_pivots<T>(h, a, w_old, c1, b, r1);
+    if (s == APSP_OK && und) s = snap_pivots<T>(h, b, w_old, c2, a, r2);
+  }
+  if (s != APSP_OK) return s;
+  ZeroSet z{};
+  z.add(h->rowcnt(), h->cap);
+  z.add(reinterpret_cast<int*>(h->ctr()), (int64_t)(sizeof(DetectCounters) / sizeof(int)));
+  CK(zero_set(z, h->st));
+  PK(APSP_K_DETECT, h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n,
+     detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, h->tau, 1, nullptr,
+               h->rowcnt(), h->srow(), h->scol(), nullptr, h->plan.lcap, h->ctr(), h->WT<T>(), h->ld, h->sr,
+               h->mirror<T>(), h->st));
+  unsigned long long tot = 0;
+  CKR(cudaMemcpyAsync(h->host_small, &h->ctr()->total, sizeof tot, cudaMemcpyDeviceToHost, h->st));
+  CKR(cudaStreamSynchronize(h->st));
+  std::memcpy(&tot, h->host_small, sizeof tot);
+  *count = (int64_t)tot;
+  const int64_t m = std::min<int64_t>(std::min<int64_t>((int64_t)tot, h->plan.lcap), cap);
+  if (m > 0) {
+    CKR(cudaMemcpyAsync(rows, h->srow(), sizeof(int32_t) * (size_t)m, cudaMemcpyDeviceToHost, h->st));
+    CKR(cudaMemcpyAsync(cols, h->scol(), sizeof(int32_t) * (size_t)m, cudaMemcpyDeviceToHost, h->st));
+    CKR(cudaStreamSynchronize(h->st));
+  }
+  return APSP_OK;
+}
+
 template <typename F>
 apsp_status dispatch(apsp_dtype dt, F&& f) {
   if (dt == APSP_I32) return f(int32_t{});
@@ -1443,6 +1505,11 @@ apsp_status apsp_set_option(apsp_handle* h, apsp_option opt, double value) {
       h->mirror8_failed = false;
       if (!value && h->mirror_level == 8) h->mirror_built = false;   // rebuild at int16
       return APSP_OK;
+    case APSP_OPT_MIRROR:   // takes effect at the next update (rebuilt, or dropped)
+      if (value != 0 && value != 1) return APSP_E_INVAL;
+      h->use_mirror = (int)value;
+      h->mirror_built = false;
+      return APSP_OK;
     case APSP_OPT_ROW_DELTA:
       if (!(value >= 0) || value > 1) return APSP_E_INVAL;
       h->row_delta = value;
@@ -1552,6 +1619,17 @@ apsp_status apsp_get_weight(apsp_handle* h, int64_t u, int64_t v, void* w) {
   CKR(cudaStreamSynchronize(h->st));
   std::memcpy(w, h->host_small, es);
   return APSP_OK;
+}
+
+apsp_status apsp_need_update_list(apsp_handle* h, int32_t kind, int64_t a, int64_t b, int32_t* rows,
+                                  int32_t* cols, int64_t cap, int64_t* count) {
+  CHECK_HANDLE(h);
+  if (!count || cap < 0 || (cap > 0 && (!rows || !cols)) || (kind != 2 && kind != 4))
+    return fail(h, APSP_E_INVAL, "need_update_list: bad argument");
+  if (a < 0 || a >= h->n || (kind == 2 && (b < 0 || b >= h->n)))
+    return fail(h, APSP_E_RANGE, "need_update_list: id out of range");
+  if (kind == 2 && a == b) return fail(h, APSP_E_INVAL, "need_update_list: u == v");
+  return dispatch(h->dt, [&](auto z) { return need_list_impl<decltype(z)>(h, kind, a, b, rows, cols, cap, count); });
 }
 
 int64_t apsp_size(const apsp_handle* h) { return h ? h->n : -1; }

@@ -26,6 +26,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "mirror.cuh"
+#include "tma.cuh"
 
 namespace apsp {
 
@@ -1987,7 +1988,8 @@ __global__ void k_detect_rows(Rows r, const int* __restrict__ rowcnt, int64_t* r
 #define D8_MINB 3
 #endif
 constexpr int kD8R = D8_R, kD8S = D8_S;   // ring: rows per stage, stages (6 KB per warp; 3 CTAs per SM)
-constexpr int kD8Smem = 8 * kD8S * kD8R * 2 * 32 * 16;
+using D8Ring = WarpRing<kD8S, kD8R, 1024>;
+constexpr int kD8Smem = 8 * D8Ring::kBytes;
 template <typename T, bool TWO, int MODE>
 __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, int64_t n, int64_t skip, Tiling tl,
                                                       const T* __restrict__ c1, const T* __restrict__ r1,
@@ -2028,33 +2030,27 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
     rwm[q] = a - 0x01010101u;
     if (TWO) { rw2[q] = b; rwm2[q] = b - 0x01010101u; }
   }
-  // the rows stream through a per-warp shared-memory ring of per-thread async
-  // copies (each lane copies, and later reads, exactly its own 2 x 16 bytes per
-  // row): kD8S stages of kD8R rows stay in flight while the warp computes.  A
-  // lane whose group lies beyond n copies the row's first group (in bounds;
-  // those columns are masked out).
-  extern __shared__ uint4 dring_raw[];
-  auto ring = reinterpret_cast<uint4 (*)[kD8S][kD8R][2][32]>(dring_raw) + (threadIdx.x >> 5);
-  const uint8_t* mb = o.M.m8 + (i_lo - r.row0) * ld;
-  const int64_t off0 = g0 < n ? g0 : 0, off1 = g0 + 512 < n ? g0 + 512 : 0;
+  // the rows stream through a per-warp shared-memory ring filled by bulk
+  // copies (TMA, tma.cuh): lane 0 copies the chunk's 1024 contiguous mirror
+  // bytes of each row (fewer on the row's ragged end; the bytes past n are
+  // masked out) and kD8S - 1 stages of kD8R rows stay in flight while the warp
+  // computes.  Lane l then reads bytes [16 l, 16 l + 16) and [512 + 16 l, ...).
+  extern __shared__ __align__(128) uint8_t dring_raw[];
+  D8Ring ring;
+  ring.init(dring_raw + (threadIdx.x >> 5) * D8Ring::kBytes, lane);
+  const uint8_t* mb = o.M.m8 + (i_lo - r.row0) * ld + (int64_t)chunk * 1024;
+  const unsigned cbytes = (unsigned)((min((int64_t)1024, n - (int64_t)chunk * 1024) + 15) & ~15);
   const int nst = (rows + kD8R - 1) / kD8R;
   auto issue = [&](int st) {
-    if (st < nst) {
-#pragma unroll
-      for (int h = 0; h < kD8R; ++h) {
-        const uint8_t* p = mb + (int64_t)min(st * kD8R + h, rows - 1) * ld;
-        cp_async16(&(*ring)[st % kD8S][h][0][lane], p + off0);
-        cp_async16(&(*ring)[st % kD8S][h][1][lane], p + off1);
-      }
-    }
-    cp_async_commit();
+    if (st < nst)
+      ring.issue(st, cbytes, lane, [&](int h) { return mb + (int64_t)min(st * kD8R + h, rows - 1) * ld; });
   };
 #pragma unroll
   for (int st = 0; st < kD8S - 1; ++st) issue(st);
   uint32_t cl = 0, cl2 = 0;
   for (int st = 0; st < nst; ++st) {
     issue(st + kD8S - 1);
-    cp_async_wait<kD8S - 1>();
+    ring.wait(st);
 #pragma unroll
     for (int h = 0; h < kD8R; ++h) {
       const int rr = st * kD8R + h;
@@ -2068,7 +2064,8 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
       {
         const uint32_t cw = __shfl_sync(0xffffffffu, cl, rr & 31);
         const uint32_t cw2 = TWO ? __shfl_sync(0xffffffffu, cl2, rr & 31) : 0u;
-        const uint4 w0 = (*ring)[st % kD8S][h][0][lane], w1 = (*ring)[st % kD8S][h][1][lane];
+        const uint4 w0 = reinterpret_cast<const uint4*>(ring.row(st, h))[lane];
+        const uint4 w1 = reinterpret_cast<const uint4*>(ring.row(st, h))[32 + lane];
         const uint32_t d[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
         uint32_t acc = 0;
 #pragma unroll

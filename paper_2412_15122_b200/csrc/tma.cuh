@@ -1,0 +1,111 @@
+// tma.cuh — bulk-copy (TMA) row rings for the O(n^2) streaming kernels.
+//
+// A warp streams the rows of its (column chunk, row slab) task through a ring
+// of S stages x R rows x CB bytes in shared memory.  One lane issues every
+// copy with cp.async.bulk (SASS UBLKCP: the TMA engine moves the bytes, no
+// register or issue slot of the warp is spent per 16 bytes) and arms the
+// stage's mbarrier with the expected byte count; the warp then waits on the
+// barrier's phase bit and reads the rows from shared memory.  The stage being
+// refilled was consumed by the same warp one iteration earlier: a __syncwarp
+// plus a generic->async proxy fence order those reads before the refill.
+#pragma once
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace apsp {
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+// barrier inits (and prior generic smem writes) visible to the async proxy
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// global -> shared bulk copy of `bytes` (multiple of 16, both addresses
+// 16-byte aligned), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// the same with an L2 eviction hint: the row is read once (evict_first)
+__device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                                uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+      "%4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// Per-warp ring: S stages of R rows of CB bytes, plus S mbarriers.
+// Shared-memory bytes per warp: ring_bytes<S, R, CB>().
+template <int S, int R, int CB>
+struct WarpRing {
+  static constexpr int kStageBytes = R * CB;
+  static constexpr int kBytes = S * kStageBytes + S * 8;
+  uint8_t* buf;    // S * R * CB bytes, 128-byte aligned
+  uint64_t* bar;   // S barriers (after the data)
+
+  __device__ __forceinline__ void init(uint8_t* base, int lane) {
+    buf = base;
+    bar = reinterpret_cast<uint64_t*>(base + S * kStageBytes);
+    if (lane == 0) {
+#pragma unroll
+      for (int s = 0; s < S; ++s) mbar_init(bar + s, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+  }
+  __device__ __forceinline__ uint8_t* row(int stage, int h) const {
+    return buf + (stage % S) * kStageBytes + h * CB;
+  }
+  // lane 0: refill stage `stage` with rows src(h), h < R, `bytes` each.  The
+  // caller's lanes finished reading the slot (the last use of it) before.
+  template <typename Src>
+  __device__ __forceinline__ void issue(int stage, unsigned bytes, int lane, Src src) {
+    __syncwarp();
+    if (lane == 0) {
+      fence_proxy_async();
+      uint64_t* b = bar + stage % S;
+      mbar_expect_tx(b, R * bytes);
+#pragma unroll
+      for (int h = 0; h < R; ++h) bulk_g2s(row(stage, h), src(h), bytes, b);
+    }
+  }
+  __device__ __forceinline__ void wait(int stage) const { mbar_wait(bar + stage % S, (unsigned)(stage / S) & 1u); }
+};
+
+}  // namespace apsp

@@ -121,18 +121,50 @@ def test_bj_c3_remove_sparse_equals_dense(P):
     check_sampled_i32(h, np.ascontiguousarray(hg.W), rows, rows[:8])
 
 
-def test_bj_c4_sequence_warm_equals_cold(P):
-    """BJ.c4 launch configuration (n=32768, cap headroom, the bench's update
-    sequence): after 12 updates GPU warm == GPU cold FW on the mutated W,
-    bit-exact, and sampled rows/columns match the oracle."""
+def _touched(up, n_before):
+    """Node ids an update wrote (u, v, x and the moved slot)."""
+    if up.kind == "add":
+        return [n_before]                       # x
+    if up.kind == "remove":
+        return [up.k] if up.k < n_before - 1 else []   # slot k now holds node n-1
+    return [up.u, up.v]
+
+
+def check_sampled_i32_fast(h, hg, ids):
+    """Rows and columns `ids` of the GPU D against oracle Dijkstra on the host
+    graph (columns: Dijkstra on a transposed copy, a forward scan)."""
+    n = hg.n
+    Wv = hg.W
+    exp_r = oracle.dijkstra_rows_i32(Wv, ids)
+    WT = np.ascontiguousarray(Wv.T)
+    exp_c = oracle.dijkstra_rows_i32(WT, ids)
+    del WT
+    assert np.array_equal(rows_of(h, ids), exp_r)
+    assert np.array_equal(cols_of(h, ids), exp_c)
+    assert exp_r.shape == (len(ids), n)
+
+
+def test_bj_c4_sequence_64_updates_sampled_and_warm_equals_cold(P):
+    """BJ.c4 in the bench's launch configuration (n=32768, the bench's cap and
+    update sequence, seed 1): 64 updates (22 adds, 21 removals, 21 reweights),
+    then 4 tight reweights (an increase of a cheapest out-edge x10, which runs
+    detection + the sparse recompute, and a decrease to half the distance,
+    which runs rank-1).  At t = 1, 8, 32, 64 and at the end: >= 64 rows and
+    >= 64 columns — every id the recent updates touched (u, v, x, the moved
+    slot) plus random ones — against oracle Dijkstra on the mutated host W
+    (SURVEY §8(c-4)).  At the end GPU warm == GPU cold FW, bit-exact."""
     spec = synth.C4
-    cap = spec.n + 64
+    cap = spec.n + 64 + 4 * 23      # bench.py's cap (3 + 2*5 + 5 steps)
     W = synth.graph(spec)
     hg = synth.HostGraph(W, True, cap=cap)
-    seq = synth.update_sequence(spec, synth.HostGraph(W, True, cap=cap), 0, 12)
+    seq = synth.update_sequence(spec, synth.HostGraph(W, True, cap=cap), 0, 64)
     h = P.WarmAPSP(torch.from_numpy(W), directed=True, cap=cap)
     del W
-    for up in seq:
+    rng = np.random.default_rng(4)
+    touched = []
+    checks = {1, 8, 32, 64}
+    for t, up in enumerate(seq, start=1):
+        nb = hg.n
         if up.kind == "add":
             h.add_node(up.out_w, up.in_w)
             hg.add_node(up.out_w, up.in_w)
@@ -142,15 +174,37 @@ def test_bj_c4_sequence_warm_equals_cold(P):
         else:
             h.update_edge(up.u, up.v, up.w_new)
             hg.set_edge(up.u, up.v, up.w_new)
+        touched = [x for x in _touched(up, nb) if x < hg.n] + [x for x in touched if x < hg.n]
+        if t in checks:
+            ids = list(dict.fromkeys(touched))[:32]
+            ids += [int(x) for x in rng.choice(hg.n, 64 - len(ids), replace=False) if int(x) not in ids]
+            check_sampled_i32_fast(h, hg, np.asarray(ids, np.int64))
+    # tight reweights: detection + sparse recompute, and rank-1
+    Dn = None
+    for q in range(2):
+        u = int(rng.integers(hg.n))
+        row = hg.W[u].astype(np.int64)
+        row[u] = INF
+        v = int(np.argmin(row))
+        info = h.update_edge(u, v, int(hg.W[u, v]) * 10)
+        assert info.kind == 2 and info.early_exit == 0 and info.path in (2, 3)
+        hg.set_edge(u, v, int(hg.W[u, v]) * 10)
+        u2, v2 = synth.random_edge(spec.seed, 1000 + q, hg)
+        d = int(rows_of(h, [u2])[0, v2])
+        w = max(0, d // 2)
+        info = h.update_edge(u2, v2, w)
+        assert info.kind == 1 and info.early_exit == 0 and info.path == 1
+        hg.set_edge(u2, v2, w)
+        touched = [u, v, u2, v2] + touched
+    ids = list(dict.fromkeys(x for x in touched if x < hg.n))[:32]
+    ids += [int(x) for x in rng.choice(hg.n, 64 - len(ids), replace=False) if int(x) not in ids]
+    check_sampled_i32_fast(h, hg, np.asarray(ids, np.int64))
     Wn = np.ascontiguousarray(hg.W)
     warm = h.D.clone()
     del h
     torch.cuda.empty_cache()
     c = P.WarmAPSP(torch.from_numpy(Wn), directed=True)
     assert torch.equal(warm, c.D)
-    rng = np.random.default_rng(4)
-    rows = rng.choice(Wn.shape[0], 8, replace=False)
-    check_sampled_i32(c, Wn, rows, rows[:4])
 
 
 def test_bj_c5_fw_increase_and_1024_queries(P):

@@ -467,6 +467,7 @@ def _check_path(W, D, s, t, dist, path):
         assert pw == dist == D[s, t]
     else:
         assert abs(pw - dist) <= RTOL * abs(dist)
+        assert abs(dist - D[s, t]) <= RTOL * abs(D[s, t])
 
 
 def test_query_golden_hub(lib):
@@ -482,11 +483,12 @@ def test_query_random(lib, rng, directed):
     n = 300
     W = random_graph(rng, n, directed, 0.3, lo=1, hi=20, inf_frac=0.0)
     h = make(lib, W, directed)
-    D = getD(h)
+    D = oracle.fw(W)                      # the oracle's matrix, not the GPU's
     for _ in range(40):
         s, t = (int(x) for x in rng.integers(0, n, 2))
         d, path, nc = h.query(s, t)
-        assert d == D[s, t]
+        dd, _ = oracle.dijkstra_pair(W, s, t)
+        assert d == D[s, t] == (0 if s == t else dd)
         _check_path(W, D, s, t, d, path)
         if s != t and D[s, t] != INF:
             assert nc == len(oracle.candidates(D, s, t))
@@ -496,7 +498,7 @@ def test_query_zero_weights(lib, rng):
     n = 40
     W = random_graph(rng, n, True, 0.5, lo=0, hi=2)
     h = make(lib, W)
-    D = getD(h)
+    D = oracle.fw(W)
     for s in range(0, n, 3):
         for t in range(1, n, 5):
             d, path, _ = h.query(s, t)
@@ -507,7 +509,7 @@ def test_query_batch_matches_single(lib, rng):
     spec = dataclasses.replace(synth.C5, n=500)
     W = synth.graph(spec)
     h = make(lib, W)
-    D = getD(h)
+    D = oracle.fw(W)
     s, t = synth.query_pairs(spec.seed, 500, 64)
     dist, paths, lens, nc = h.query_batch(s, t, path_cap=32)
     dist, paths, lens = dist.cpu().numpy(), paths.cpu().numpy(), lens.cpu().numpy()
@@ -521,9 +523,12 @@ def test_query_fp32_and_cycle(lib):
     spec = dataclasses.replace(synth.C2, n=256)
     W = synth.graph(spec)
     h = make(lib, W, directed=False)
-    D = getD(h)
+    D = oracle.fw(W)                      # fp64
     for s, t in [(0, 1), (5, 200), (17, 17), (255, 3)]:
         d, path, _ = h.query(s, t)
+        if s != t:
+            dd, _ = oracle.dijkstra_pair(W, s, t)
+            assert abs(d - dd) <= RTOL * dd
         _check_path(W, D, s, t, d, path)
     n = 300
     C = np.full((n, n), INF, np.int32)
@@ -842,7 +847,7 @@ def test_add_node_gather_fallbacks(lib, rng):
     (col1 uncertified: full-row scans); (2) every in-edge equally cheap, so the
     gathered column set exceeds its limit (the streaming pass 1 runs).
     Sampled rows / columns (the new node's included) against Dijkstra on the
-    host graph, and the whole matrix against a cold FW of the same graph."""
+    host graph, and the whole matrix against the oracle's FW of the same graph."""
     n = 4200
     W = random_graph(rng, n, True, density=0.01, lo=1, hi=9)
     W[:, :10] = INF            # nodes 0-9: no in-edges
@@ -865,8 +870,7 @@ def test_add_node_gather_fallbacks(lib, rng):
     hg.add_node(o3, i3)
     idx = np.concatenate([rng.choice(n, 12, replace=False), [0, 5, n, n + 1, n + 2]])
     _sampled_rows_cols(h, hg.W, idx)
-    cold = make(lib, hg.W, cap=n + 3)
-    assert np.array_equal(getD(h), getD(cold))
+    assert_parity(getD(h), oracle.fw(hg.W))
 
 
 def test_new_node_shortlist_then_removals(lib, rng):
@@ -875,7 +879,7 @@ def test_new_node_shortlist_then_removals(lib, rng):
     removals that list pairs in column x: (1) fewer than 512 finite in-edges
     (dead entries) and zero weights (wmin = 0 in the column certification);
     (2) every in-edge finite.  Sampled rows / columns against Dijkstra on the
-    host graph and the whole matrix against a cold FW of the final graph."""
+    host graph and the whole matrix against the oracle's FW of the final graph."""
     n = 4100
     W = random_graph(rng, n, True, density=0.02, lo=1, hi=9)
     hg = synth.HostGraph(W, True, cap=n + 3)
@@ -904,8 +908,7 @@ def test_new_node_shortlist_then_removals(lib, rng):
     m = hg.n
     idx = np.concatenate([rng.choice(m, 10, replace=False), [m - 1, m - 2]])
     _sampled_rows_cols(h, hg.W[:m, :m], idx)
-    cold = make(lib, hg.W[:m, :m], cap=m + 1)
-    assert np.array_equal(getD(h), getD(cold))
+    assert_parity(getD(h), oracle.fw(hg.W[:m, :m]))
 
 
 def test_add_node_heavy_out_edges_to_unreachable(lib, rng):
@@ -937,4 +940,126 @@ def test_add_node_heavy_out_edges_to_unreachable(lib, rng):
     i2 = rng.integers(1, 1001, hg.n).astype(np.int32)
     h.add_node(o2, i2)
     hg.add_node(o2, i2)
+    assert_parity(getD(h), oracle.fw(hg.W[:hg.n, :hg.n]))
+
+
+# ------------------------------------------------ detection, set for set (§8(c-1))
+def _pairs(r, c):
+    return set(zip(np.asarray(r).tolist(), np.asarray(c).tolist()))
+
+
+def _mask_pairs(m):
+    i, j = np.nonzero(m)
+    return set(zip(i.tolist(), j.tolist()))
+
+
+def _tight_edge(W, D, rng, directed=True):
+    """An edge (u, v) with W[u][v] == D[u][v] (tight: on a shortest path)."""
+    n = W.shape[0]
+    for _ in range(1000):
+        u = int(rng.integers(n))
+        row = np.where((np.arange(n) != u) & (W[u] < INF) & (W[u] == D[u]), 1, 0)
+        if row.any():
+            v = int(rng.choice(np.nonzero(row)[0]))
+            return u, v
+    raise AssertionError("no tight edge")
+
+
+@pytest.mark.parametrize("n,directed,hi,mirror", [
+    (300, True, 9, 1),        # int8 mirror
+    (1100, True, 9, 1),       # int8, several 1024-column chunks + a ragged one
+    (700, False, 9, 1),
+    (1100, True, 4000, 1),    # distances >= 0x7F: int16 mirror
+    (1100, True, 9, 0),       # no mirror: the int32 stream (4 B/entry)
+    (2100, False, 60, 0),
+])
+def test_need_update_list_set_for_set_int32(lib, rng, n, directed, hi, mirror):
+    """The GPU's need_update_list (the detection kernels the updates run,
+    exported by apsp_need_update_list) equals the oracle's definitional
+    predicate set for set (Corollary 3 / Theorem 4): removals of
+    random nodes and increases of tight edges (undirected: both orientations)."""
+    W = random_graph(rng, n, directed, density=0.3, lo=1, hi=hi, inf_frac=0.02)
+    h = make(lib, W, directed)
+    h.set_option(lib._lib.OPT_MIRROR, mirror)
+    D = oracle.fw(W)
+    assert np.array_equal(getD(h), D)
+    for k in rng.choice(n, 3, replace=False):
+        r, c, cnt = h.need_update_list("remove", int(k))
+        assert cnt == len(r)
+        exp = _mask_pairs(oracle.need_update_removal(D, int(k)))
+        assert _pairs(r, c) == exp and cnt == len(exp)
+    if mirror:
+        assert h.mirror_width == (8 if D[D < INF].max() < 0x7F else 16)
+    else:
+        assert h.mirror_width == 0
+    for _ in range(3):
+        u, v = _tight_edge(W, D, rng)
+        r, c, cnt = h.need_update_list("increase", u, v)
+        exp = _mask_pairs(oracle.need_update_increase(D, u, v, int(W[u, v]), directed))
+        assert _pairs(r, c) == exp and cnt == len(exp)
+    assert np.array_equal(getD(h), D)      # nothing was applied
+
+
+def test_need_update_list_fp32_bracketed(lib, rng):
+    """fp32 detection uses the tolerant test (Q4): the GPU set holds
+    every exactly tight pair of the fp64 oracle (tau = 0) and nothing outside
+    the oracle's set at a slightly looser tau (what is unique is compared, the
+    rest checked valid)."""
+    n = 600
+    W = random_graph(rng, n, False, density=0.5, hi=1, dtype=np.float32)
+    h = make(lib, W, directed=False)
+    D = oracle.fw(W)
+    for k in rng.choice(n, 3, replace=False):
+        r, c, _ = h.need_update_list("remove", int(k))
+        got = _pairs(r, c)
+        assert _mask_pairs(oracle.need_update_removal(D, int(k), tau=0.0)) <= got
+        assert got <= _mask_pairs(oracle.need_update_removal(D, int(k), tau=3e-5))
+    u = 5
+    row = np.where(np.arange(n) == u, np.inf, W[u].astype(np.float64))
+    v = int(np.argmin(row))                  # the cheapest out-edge is tight
+    r, c, _ = h.need_update_list("increase", u, v)
+    got = _pairs(r, c)
+    assert _mask_pairs(oracle.need_update_increase(D, u, v, float(W[u, v]), False, tau=0.0)) <= got
+    assert got <= _mask_pairs(oracle.need_update_increase(D, u, v, float(W[u, v]), False, tau=3e-5))
+
+
+def test_need_update_list_minimax_set_for_set(lib, rng):
+    """Minimax handles (f2): the detection predicate with + -> max, set for set."""
+    n = 500
+    W = random_graph(rng, n, True, density=0.2, lo=1, hi=30)
+    h = make(lib, W, cold=False)
+    h.set_option(lib._lib.OPT_SEMIRING, 1)
+    h.cold_fw()
+    D = oracle.fw_minimax(W)
+    assert np.array_equal(getD(h), D)
+    for k in rng.choice(n, 3, replace=False):
+        r, c, _ = h.need_update_list("remove", int(k))
+        assert _pairs(r, c) == _mask_pairs(oracle.need_update_removal_minimax(D, int(k)))
+
+
+def test_int32_streams_without_mirror_match_oracle(lib, rng):
+    """APSP_OPT_MIRROR = 0 (every O(n^2) pass streams the int32 D, the byte
+    basis of SURVEY §8(d-4)): a mixed update sequence stays bit-exact."""
+    n = 1500
+    W = random_graph(rng, n, True, density=0.5, lo=1, hi=50)
+    hg = synth.HostGraph(W, True, cap=n + 8)
+    h = make(lib, W, cap=n + 8)
+    h.set_option(lib._lib.OPT_MIRROR, 0)
+    for t in range(9):
+        if t % 3 == 0:
+            o = rng.integers(1, 50, hg.n).astype(np.int32)
+            i = rng.integers(1, 50, hg.n).astype(np.int32)
+            h.add_node(o, i)
+            hg.add_node(o, i)
+        elif t % 3 == 1:
+            k = int(rng.integers(hg.n))
+            h.remove_node(k)
+            hg.remove_node(k)
+        else:
+            Dn = getD(h)
+            u, v = _tight_edge(hg.W[:hg.n, :hg.n], Dn, rng)
+            w = int(hg.W[u, v]) * 4
+            h.update_edge(u, v, w)
+            hg.set_edge(u, v, w)
+        assert h.mirror_width == 0
     assert_parity(getD(h), oracle.fw(hg.W[:hg.n, :hg.n]))

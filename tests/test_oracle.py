@@ -363,3 +363,144 @@ def test_minimax_need_update_is_safe(rng):
         mk = m[np.ix_(keep, keep)]
         assert np.array_equal(D2[~mk], Dk[~mk])
         assert np.all(D2 >= Dk)
+
+
+# ------------------------------------------- pins added in round 2
+def _py_brute(W, combine):
+    """Independent pure-Python enumeration of every simple path (n <= 6): the
+    definition of the APSP matrix with the path cost folded by
+    `combine` (sum: shortest path; max: minimax).  Floats in fp64."""
+    W = np.asarray(W, np.float64)
+    n = W.shape[0]
+    out = np.full((n, n), np.inf)
+    for s in range(n):
+        out[s, s] = 0.0
+        for t in range(n):
+            if t == s:
+                continue
+            others = [v for v in range(n) if v not in (s, t)]
+            for r in range(len(others) + 1):
+                for mid in itertools.permutations(others, r):
+                    p = [s, *mid, t]
+                    c = 0.0
+                    for a, b in zip(p[:-1], p[1:]):
+                        c = combine(c, W[a, b])
+                    out[s, t] = min(out[s, t], c)
+    return out
+
+
+def _float_graph(rng, n, directed):
+    W = random_graph(rng, n, directed, 0.6, hi=1, dtype=np.float32)
+    z = rng.random((n, n)) < 0.15           # some zero-weight edges
+    if not directed:
+        z = np.triu(z, 1)
+        z = z | z.T
+    W = np.where(z & np.isfinite(W), np.float32(0), W).astype(np.float32)
+    np.fill_diagonal(W, 0)
+    return W
+
+
+@pytest.mark.parametrize("directed", [True, False])
+def test_dijkstra_f64_rows_and_pair_equal_python_bruteforce(rng, directed):
+    """oracle_dijkstra_rows_f64 / oracle_dijkstra_f64 (the fp32 full-size
+    checkers) against an independent enumeration of simple paths, float
+    weights with zeros and absent edges (+inf)."""
+    for trial in range(20):
+        n = int(rng.integers(2, 7))
+        W = _float_graph(rng, n, directed)
+        B = _py_brute(W, lambda c, w: c + w)
+        D = oracle.dijkstra_rows(W, range(n))
+        assert np.array_equal(np.isinf(D), np.isinf(B))
+        fin = np.isfinite(B)
+        assert np.allclose(D[fin], B[fin], rtol=1e-12, atol=0)
+        assert np.allclose(oracle.dijkstra_cols(W, range(n))[fin], B[fin], rtol=1e-12, atol=0)
+        s, t = (int(x) for x in rng.choice(n, 2, replace=False))
+        d, path = oracle.dijkstra_pair(W, s, t)
+        if np.isinf(B[s, t]):
+            assert np.isinf(d) and path == []
+        else:
+            assert abs(d - B[s, t]) <= 1e-12 * max(B[s, t], 1e-300)
+            assert oracle.path_is_valid(W, path, s, t)
+            assert abs(oracle.path_weight(W, path) - d) <= 1e-12 * max(d, 1e-300)
+
+
+@pytest.mark.parametrize("directed", [True, False])
+def test_fw_minimax_f64_equals_python_bruteforce(rng, directed):
+    """oracle_fw_minimax_f64 against the independent enumeration with the
+    path cost = its largest edge; exact (max/min need no rounding)."""
+    for trial in range(20):
+        n = int(rng.integers(2, 7))
+        W = _float_graph(rng, n, directed)
+        assert np.array_equal(oracle.fw_minimax(W), _py_brute(W, max))
+
+
+def _arc_crosses(n, i, j, a):
+    """On the directed unit cycle the i -> j path is i, i+1, ..., j: it uses
+    edge a -> a+1 iff a lies in [i, j) cyclically."""
+    return (a - i) % n < (j - i) % n
+
+
+def test_need_update_increase_exact_on_cycle():
+    """Exact set (not only safety): on the directed unit cycle every pair has a
+    unique shortest path, so raising edge u -> u+1 lists exactly the pairs
+    whose arc crosses it (SURVEY §8(c-4) a4 closed form)."""
+    n = 23
+    D = oracle.fw(cycle(n))
+    for u in (0, 7, n - 1):
+        v = (u + 1) % n
+        m = oracle.need_update_increase(D, u, v, 1, directed=True)
+        exp = np.array([[i != j and _arc_crosses(n, i, j, u) for j in range(n)] for i in range(n)])
+        assert np.array_equal(m, exp)
+
+
+def test_need_update_increase_exact_on_undirected_path():
+    """Undirected unit path: edge {u, u+1} lies on the unique i - j path iff
+    min(i, j) <= u < max(i, j); both orientations are tested (DESIGN Q10)."""
+    n = 19
+    W = np.full((n, n), INF, np.int32)
+    np.fill_diagonal(W, 0)
+    a = np.arange(n - 1)
+    W[a, a + 1] = 1
+    W[a + 1, a] = 1
+    D = oracle.fw(W)
+    for u in (0, 5, n - 2):
+        m = oracle.need_update_increase(D, u, u + 1, 1, directed=False)
+        i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+        exp = (np.minimum(i, j) <= u) & (u < np.maximum(i, j))
+        assert np.array_equal(m, exp)
+
+
+def test_need_update_removal_exact_on_cycle():
+    """Removing k from the directed unit cycle lists exactly the pairs i, j != k
+    whose arc passes through k as an interior node (Corollary 3, unique paths)."""
+    n = 21
+    D = oracle.fw(cycle(n))
+    for k in (0, 9, n - 1):
+        m = oracle.need_update_removal(D, k)
+        exp = np.array([[i != j and i != k and j != k and (k - i) % n < (j - i) % n for j in range(n)]
+                        for i in range(n)])
+        assert np.array_equal(m, exp)
+        assert oracle.cost(m, n)[0] == n - 2     # every other source loses some target
+
+
+def test_need_update_removal_minimax_exact_on_increasing_path():
+    """Minimax predicate, exact set: undirected path whose edge weights grow
+    along it (w(a, a+1) = a + 1), so D[i][j] = max(i, j) off the diagonal.
+    Removing k lists (i, j), both != k, iff max(D[i][k], D[k][j]) =
+    max(i, j, k) equals max(i, j), i.e. iff max(i, j) > k: pairs straddling k
+    and pairs beyond it (a detour through k costs no more than their own
+    bottleneck edge — the ties the minimax algebra makes frequent, SURVEY
+    f2); pairs below k are not listed (the detour's edge k is heavier)."""
+    n = 15
+    W = np.full((n, n), INF, np.int32)
+    np.fill_diagonal(W, 0)
+    a = np.arange(n - 1)
+    W[a, a + 1] = a + 1
+    W[a + 1, a] = a + 1
+    D = oracle.fw_minimax(W)
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    assert np.array_equal(D, np.where(i == j, 0, np.maximum(i, j)).astype(np.int32))
+    for k in (1, 7, n - 2):
+        m = oracle.need_update_removal_minimax(D, k)
+        exp = (np.maximum(i, j) > k) & (i != j) & (i != k) & (j != k)
+        assert np.array_equal(m, exp)

@@ -30,6 +30,8 @@
 
 namespace apsp {
 
+constexpr int DS_V = 4;              // vectors per lane per row (detection / rank-1 on D)
+constexpr int DS_VEC = 32 * DS_V;    // vectors per chunk (512 columns)
 constexpr int VPL = 8;                 // vectors per lane per row
 constexpr int CHUNK_VEC = 32 * VPL;    // vectors per warp chunk (1024 columns)
 
@@ -1286,72 +1288,150 @@ cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, cons
 // ---------------------------------------------------------------------------
 // rank-1 min-plus relaxation  D[i][j] = min(D[i][j], c[i] + r[j] (, c2[i] + r2[j]))
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ int32_t bits32(int32_t v) { return v; }
+__device__ __forceinline__ int32_t bits32(float v) { return __float_as_int(v); }
+template <typename T> __device__ __forceinline__ T from_bits32(int32_t b);
+template <> __device__ __forceinline__ int32_t from_bits32<int32_t>(int32_t b) { return b; }
+template <> __device__ __forceinline__ float from_bits32<float>(int32_t b) { return __int_as_float(b); }
+
+// Warp-uniform iterator over the rows i in [lo, hi) that can change in a
+// rank-1 pass (c[i] or c2[i] finite): one ballot per 32 rows, the next group's
+// c values loaded a group ahead.  next() returns the row and its c values.
+template <typename T, bool TWO>
+struct LiveRows {
+  const T* c;
+  const T* c2;
+  int64_t g, cur, hi;
+  unsigned mask;
+  T nx, nx2, cx, cx2;
+  __device__ __forceinline__ void load(int lane) {
+    const int64_t i = g + lane;
+    nx = i < hi ? c[i] : Tr<T>::inf();
+    nx2 = (TWO && i < hi) ? c2[i] : Tr<T>::inf();
+  }
+  __device__ __forceinline__ void init(const T* c_, const T* c2_, int64_t lo, int64_t hi_, int lane) {
+    c = c_; c2 = c2_; g = lo; hi = hi_; mask = 0u; cur = lo;
+    if (g < hi) load(lane);
+  }
+  // -1 at the end; *ci / *ci2 = c[i] / c2[i] (warp-uniform)
+  __device__ __forceinline__ int64_t next(int lane, T* ci, T* ci2) {
+    while (mask == 0u) {
+      if (g >= hi) return -1;
+      mask = __ballot_sync(0xffffffffu, Tr<T>::fin(nx) || (TWO && Tr<T>::fin(nx2)));
+      cur = g;
+      cx = nx;
+      cx2 = nx2;
+      g += 32;
+      if (g < hi) load(lane);
+    }
+    const int b = __ffs(mask) - 1;
+    mask &= mask - 1u;
+    *ci = __shfl_sync(0xffffffffu, cx, b);
+    *ci2 = TWO ? __shfl_sync(0xffffffffu, cx2, b) : Tr<T>::inf();
+    return cur + b;
+  }
+};
+
+// The rank-1 pass on D itself (int32 / fp32, either algebra).  A warp owns a
+// 512-column chunk of a row slab; the rows that can change (LiveRows) arrive
+// through a per-warp TMA ring, one 2 KB row per stage, kR1S - 1 rows ahead;
+// only the 16-byte vectors that change are written back (D, and the mirror
+// when there is one).
+constexpr int kR1S = 4;
+using R1Ring = WarpRing<kR1S, 1, DS_VEC * 16>;
+struct R1Meta { int64_t i; int32_t c, c2; };   // per stage: the row and its c values (bit patterns)
+constexpr int kR1Smem = 8 * (R1Ring::kBytes + kR1S * (int)sizeof(R1Meta));
 template <typename T, bool TWO, int SR>
-__global__ void __launch_bounds__(256) k_rank1(T* __restrict__ D, int64_t ld, Rows r, int64_t n,
-                                               Tiling tl, const T* __restrict__ c,
-                                               const T* __restrict__ rv, const T* __restrict__ c2,
-                                               const T* __restrict__ rv2,
-                                               unsigned long long* __restrict__ bytes_read,
-                                               Mirror M) {
+__global__ void __launch_bounds__(256, 3) k_rank1(T* __restrict__ D, int64_t ld, Rows r, int64_t n,
+                                                  Tiling tl, const T* __restrict__ c,
+                                                  const T* __restrict__ rv, const T* __restrict__ c2,
+                                                  const T* __restrict__ rv2,
+                                                  unsigned long long* __restrict__ bytes_read,
+                                                  Mirror M) {
   // k_rank1_p8 (launched first) did the update while the int8 mirror is valid
   if (SR == 0 && M.m8 != nullptr && (*(volatile unsigned*)M.flag & kMirrorOff) == 0u) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (gw >= tl.warps) return;
-  const int chunk = (int)(gw % tl.nchunk);
-  const int slab = (int)(gw / tl.nchunk);
-  const int64_t i_lo = r.lo + slab * tl.slab;
-  const int64_t i_hi = min(r.hi, i_lo + tl.slab);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  extern __shared__ __align__(128) uint8_t r1_raw[];
+  R1Ring ring;
+  ring.init(r1_raw + warp * R1Ring::kBytes, lane);
+  R1Meta* meta = reinterpret_cast<R1Meta*>(r1_raw + 8 * R1Ring::kBytes) + warp * kR1S;
   const T I = Tr<T>::inf();
-
-  int64_t qv[VPL];
-  Vec4<T> a[VPL], b[VPL];
-#pragma unroll
-  for (int v = 0; v < VPL; ++v) {
-    qv[v] = (int64_t)chunk * CHUNK_VEC + v * 32 + lane;
-    a[v] = qv[v] < tl.n4 ? ld4<T>(rv + 4 * qv[v]) : Vec4<T>{I, I, I, I};
-    if (TWO) b[v] = qv[v] < tl.n4 ? ld4<T>(rv2 + 4 * qv[v]) : Vec4<T>{I, I, I, I};
-  }
-  int64_t rows_read = 0;
+  int64_t base = 0, rows_read = 0;
   unsigned mbits = 0;
-  for (int64_t i = i_lo; i < i_hi; ++i) {
-    const T ci = c[i];
-    const T ci2 = TWO ? c2[i] : I;
-    if (!Tr<T>::fin(ci) && !Tr<T>::fin(ci2)) continue;   // row cannot change
-    ++rows_read;
-    T* row = D + (i - r.row0) * ld;
-    Vec4<T> d[VPL];
+  for (int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; gw < tl.warps;
+       gw += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int chunk = (int)(gw % tl.nchunk);
+    const int slab = (int)(gw / tl.nchunk);
+    const int64_t i_lo = r.lo + slab * tl.slab;
+    const int64_t i_hi = min(r.hi, i_lo + tl.slab);
+    int64_t qv[DS_V];
+    Vec4<T> a[DS_V], b[DS_V];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v)
-      if (qv[v] < tl.n4) d[v] = ld4_stream<T>(row + 4 * qv[v]);
-#pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      if (qv[v] >= tl.n4) continue;
-      Vec4<T> o = d[v];
-      o.x = Tr<T, SR>::relax(o.x, ci, a[v].x);
-      o.y = Tr<T, SR>::relax(o.y, ci, a[v].y);
-      o.z = Tr<T, SR>::relax(o.z, ci, a[v].z);
-      o.w = Tr<T, SR>::relax(o.w, ci, a[v].w);
-      if (TWO) {
-        o.x = Tr<T, SR>::relax(o.x, ci2, b[v].x);
-        o.y = Tr<T, SR>::relax(o.y, ci2, b[v].y);
-        o.z = Tr<T, SR>::relax(o.z, ci2, b[v].z);
-        o.w = Tr<T, SR>::relax(o.w, ci2, b[v].w);
+    for (int v = 0; v < DS_V; ++v) {
+      qv[v] = (int64_t)chunk * DS_VEC + v * 32 + lane;
+      a[v] = qv[v] < tl.n4 ? ld4<T>(rv + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+      if (TWO) b[v] = qv[v] < tl.n4 ? ld4<T>(rv2 + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+    }
+    const unsigned cbytes =
+        (unsigned)((min((int64_t)DS_VEC * 4, n - (int64_t)chunk * DS_VEC * 4) * (int64_t)sizeof(T) + 15) & ~15);
+    T* dchunk = D + (int64_t)chunk * DS_VEC * 4 - r.row0 * ld;   // + i * ld: row i's chunk
+    LiveRows<T, TWO> it;
+    it.init(c, c2, i_lo, i_hi, lane);
+    int64_t issued = 0;
+    auto produce = [&]() {
+      T ci, ci2;
+      const int64_t i = it.next(lane, &ci, &ci2);
+      if (i < 0) return;
+      if (lane == 0) {
+        R1Meta& m = meta[(base + issued) % kR1S];
+        m.i = i;
+        m.c = bits32(ci);
+        m.c2 = bits32(ci2);
       }
-      if (o.x != d[v].x || o.y != d[v].y || o.z != d[v].z || o.w != d[v].w) {
-        st4<T>(row + 4 * qv[v], o);
-        if (has_mirror(M)) {
-          const int64_t idx = (i - r.row0) * ld + 4 * qv[v];
-          mbits |= mput(M, idx, o.x) | mput(M, idx + 1, o.y) | mput(M, idx + 2, o.z) | mput(M, idx + 3, o.w);
+      ring.issue((int)(base + issued), cbytes, lane, [&](int) { return dchunk + i * ld; });
+      ++issued;
+    };
+    for (int k = 0; k < kR1S - 1; ++k) produce();
+    for (int64_t st = 0; st < issued; ++st) {
+      produce();
+      ring.wait((int)(base + st));
+      const R1Meta m = meta[(base + st) % kR1S];
+      const T ci = from_bits32<T>(m.c), ci2 = from_bits32<T>(m.c2);
+      const uint8_t* srow = ring.row((int)(base + st), 0);
+      T* row = dchunk + m.i * ld;
+      ++rows_read;
+#pragma unroll
+      for (int v = 0; v < DS_V; ++v) {
+        if (qv[v] >= tl.n4) continue;
+        const Vec4<T> d = ld4<T>(reinterpret_cast<const T*>(srow + 512 * v + 16 * lane));
+        Vec4<T> o = d;
+        o.x = Tr<T, SR>::relax(o.x, ci, a[v].x);
+        o.y = Tr<T, SR>::relax(o.y, ci, a[v].y);
+        o.z = Tr<T, SR>::relax(o.z, ci, a[v].z);
+        o.w = Tr<T, SR>::relax(o.w, ci, a[v].w);
+        if (TWO) {
+          o.x = Tr<T, SR>::relax(o.x, ci2, b[v].x);
+          o.y = Tr<T, SR>::relax(o.y, ci2, b[v].y);
+          o.z = Tr<T, SR>::relax(o.z, ci2, b[v].z);
+          o.w = Tr<T, SR>::relax(o.w, ci2, b[v].w);
+        }
+        if (o.x != d.x || o.y != d.y || o.z != d.z || o.w != d.w) {
+          st4<T>(row + 128 * v + 4 * lane, o);
+          if (has_mirror(M)) {
+            const int64_t idx = (m.i - r.row0) * ld + 4 * qv[v];
+            mbits |= mput(M, idx, o.x) | mput(M, idx + 1, o.y) | mput(M, idx + 2, o.z) | mput(M, idx + 3, o.w);
+          }
         }
       }
     }
+    base += issued;
+    if (bytes_read && lane == 0 && issued) {
+      const int64_t cols = min((int64_t)DS_VEC * 4, n - (int64_t)chunk * DS_VEC * 4);
+      atomicAdd(bytes_read, (unsigned long long)(issued * cols * (int64_t)sizeof(T)));
+    }
   }
+  (void)rows_read;
   if (has_mirror(M)) mirror_post(M, mbits);
-  if (bytes_read && lane == 0 && rows_read) {
-    const int64_t cols = min((int64_t)CHUNK_VEC * 4, n - (int64_t)chunk * CHUNK_VEC * 4);
-    atomicAdd(bytes_read, (unsigned long long)(rows_read * cols * (int64_t)sizeof(T)));
-  }
 }
 // Rank-1 pass on the int8 mirror (shortest path, int32 D, mirror valid):
 // D[i][j] = min(D[i][j], c[i] + r[j] (, c2[i] + r2[j])).  While the mirror is
@@ -1523,14 +1603,30 @@ cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, 
       if (!twin) return cudaGetLastError();
     }
   }
-  if (c2 && sr)
-    k_rank1<T, true, 1><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, c2, rv2, bytes_read, M);
-  else if (c2)
-    k_rank1<T, true, 0><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, c2, rv2, bytes_read, M);
-  else if (sr)
-    k_rank1<T, false, 1><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, nullptr, nullptr, bytes_read, M);
-  else
-    k_rank1<T, false, 0><<<grid, 256, 0, st>>>(D, ld, r, n, tl, c, rv, nullptr, nullptr, bytes_read, M);
+  // 512-column chunks, one task per warp at 24 warps per SM (a launch next to
+  // the int8 twin usually exits at once; the grid is then at residency anyway)
+  tl = make_tiling(n, r.hi - r.lo, 1 << 20, DS_VEC, 24);
+  grid = (int)cdiv(tl.warps, 8);
+  // (every variant's smem attribute once: the four kernels share one pointer type)
+  static const cudaError_t attr = [] {
+    cudaError_t e = cudaFuncSetAttribute(k_rank1<T, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kR1Smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_rank1<T, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kR1Smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_rank1<T, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kR1Smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_rank1<T, false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kR1Smem);
+    return e;
+  }();
+  CUDA_TRY(attr);
+  auto launch = [&](auto kern, const T* cc2, const T* rr2) -> cudaError_t {
+    kern<<<grid, 256, kR1Smem, st>>>(D, ld, r, n, tl, c, rv, cc2, rr2, bytes_read, M);
+    return cudaGetLastError();
+  };
+  if (c2 && sr) return launch(k_rank1<T, true, 1>, c2, rv2);
+  if (c2) return launch(k_rank1<T, true, 0>, c2, rv2);
+  if (sr) return launch(k_rank1<T, false, 1>, (const T*)nullptr, (const T*)nullptr);
+  return launch(k_rank1<T, false, 0>, (const T*)nullptr, (const T*)nullptr);
   return cudaGetLastError();
 }
 
@@ -1619,8 +1715,6 @@ __device__ __forceinline__ unsigned flag_nibble(const Vec4<T>& d, const Vec4<T>&
 //                   recovery pass when the list overflowed and FW follows).
 // Columns are owned by one warp, so rewriting D inside the pass is race-free.
 // ---------------------------------------------------------------------------
-constexpr int DS_V = 4;              // vectors per lane per row
-constexpr int DS_VEC = 32 * DS_V;    // vectors per chunk (512 columns)
 
 template <typename T>
 struct DetectOut {
@@ -1706,6 +1800,10 @@ __device__ __forceinline__ bool detect_uses_mirror(const Mirror& M) {
          (*(volatile unsigned*)M.flag & kMirrorOff) == 0u;
 }
 
+constexpr int kDSS = 3, kDSR = 2;   // TMA ring of the 4-byte detection stream: stages, rows per stage
+using DSRing = WarpRing<kDSS, kDSR, DS_VEC * 16>;   // 2 KB per row (512 columns)
+constexpr int kDSSmem = 8 * DSRing::kBytes;
+
 template <typename T, bool TWO, int SR, int MODE>
 __global__ void __launch_bounds__(256, 2) k_detect_stream(T* __restrict__ D, int64_t ld, Rows r,
                                                           int64_t n, int64_t skip, Tiling tl,
@@ -1723,6 +1821,14 @@ __global__ void __launch_bounds__(256, 2) k_detect_stream(T* __restrict__ D, int
   // kernel) does the shortest-path detection on it and this kernel exits.
   if (detect_uses_mirror<T, SR, MODE>(o.M)) return;
   const bool m16 = false;
+  // rows arrive through a per-warp TMA ring (tma.cuh): lane 0 bulk-copies the
+  // chunk's 2 KB of each row, kDSS - 1 stages of kDSR rows ahead; lane l reads
+  // its vector v at byte 512 v + 16 l.  `base` counts the ring's stages over
+  // the warp's tasks (the barriers' phases run on across tasks).
+  extern __shared__ __align__(128) uint8_t ds_raw[];
+  DSRing ring;
+  ring.init(ds_raw + (threadIdx.x >> 5) * DSRing::kBytes, lane);
+  int base = 0;
   // grid-stride over the (chunk, slab) tasks: with a mirror present this
   // kernel is usually the no-op twin of the packed one, launched small
   for (int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); gw < tl.warps;
@@ -1790,22 +1896,36 @@ __global__ void __launch_bounds__(256, 2) k_detect_stream(T* __restrict__ D, int
       }
     }
   };
-    for (int64_t i0 = i_lo; i0 < i_hi; i0 += 2) {
-      // two rows in flight per lane; the row loads are issued first (their
-      // predicate needs no memory), the column snapshot c1[i] after them
-      bool act[2];
-      Vec4<T> d[2][DS_V];
+    const int rows = (int)max((int64_t)0, i_hi - i_lo);
+    const int nst = (rows + kDSR - 1) / kDSR;
+    const T* db = D + (i_lo - r.row0) * ld + (int64_t)chunk * DS_VEC * 4;
+    const unsigned cbytes =
+        (unsigned)((min((int64_t)DS_VEC * 4, n - (int64_t)chunk * DS_VEC * 4) * (int64_t)sizeof(T) + 15) & ~15);
+    auto issue = [&](int st) {
+      if (st < nst)
+        ring.issue(base + st, cbytes, lane,
+                   [&](int h) { return db + (int64_t)min(st * kDSR + h, rows - 1) * ld; });
+    };
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t i = i0 + h;
+    for (int st = 0; st < kDSS - 1; ++st) issue(st);
+    for (int st = 0; st < nst; ++st) {
+      issue(st + kDSS - 1);
+      ring.wait(base + st);
+      bool act[kDSR];
+      Vec4<T> d[kDSR][DS_V];
+#pragma unroll
+      for (int h = 0; h < kDSR; ++h) {
+        const int64_t i = i_lo + st * kDSR + h;
         act[h] = i < i_hi && i != skip;
-        const T* row = D + (i - r.row0) * ld;
+        const uint8_t* row = ring.row(base + st, h);
 #pragma unroll
         for (int v = 0; v < DS_V; ++v)
-          d[h][v] = (act[h] && qv[v] < tl.n4) ? ld4_stream<T>(row + 4 * qv[v]) : Vec4<T>{I, I, I, I};
+          d[h][v] = (act[h] && qv[v] < tl.n4) ? ld4<T>(reinterpret_cast<const T*>(row + 512 * v + 16 * lane))
+                                              : Vec4<T>{I, I, I, I};
       }
-      process2(i0, d, act);
+      process2(i_lo + st * kDSR, d, act);
     }
+    base += nst;
   if (MODE == 1) detect_flush<T>(Q, qcnt, i_lo, chunk, m16, o, lane);
   qcnt = 0;
   }
@@ -2155,8 +2275,13 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
     else if (SR == 0 && MODE != 2 && M.m)                                                        \
       k_detect_p16<T, TWO, (MODE == 2 ? 0 : MODE)><<<g, 256, 0, st>>>(D, ld, r, n, skip, tl,   \
                                                                           c1, r1, c2, r2, tau, o); \
-    k_detect_stream<T, TWO, SR, MODE><<<gs, 256, 0, st>>>(D, ld, r, n, skip, tl, c1, r1, c2, r2, \
-                                                          tau, o);                               \
+    {                                                                                            \
+      auto kds = k_detect_stream<T, TWO, SR, MODE>;                                              \
+      static const cudaError_t attr2 =                                                           \
+          cudaFuncSetAttribute(kds, cudaFuncAttributeMaxDynamicSharedMemorySize, kDSSmem);        \
+      CUDA_TRY(attr2);                                                                           \
+      kds<<<gs, 256, kDSSmem, st>>>(D, ld, r, n, skip, tl, c1, r1, c2, r2, tau, o);              \
+    }                                                                                            \
   } while (0)
 #define BY_MODE(TWO, SR)                 \
   if (mode == 0) LAUNCH(TWO, SR, 0);     \

@@ -75,7 +75,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 template <int S, int R, int CB>
 struct WarpRing {
   static constexpr int kStageBytes = R * CB;
-  static constexpr int kBytes = S * kStageBytes + S * 8;
+  // per-warp footprint, rounded to 128 bytes so that every warp's ring (and
+  // each row in it) stays 16-byte aligned for the bulk copies
+  static constexpr int kBytes = (S * kStageBytes + S * 8 + 127) / 128 * 128;
   uint8_t* buf;    // S * R * CB bytes, 128-byte aligned
   uint64_t* bar;   // S barriers (after the data)
 
@@ -106,6 +108,54 @@ struct WarpRing {
     }
   }
   __device__ __forceinline__ void wait(int stage) const { mbar_wait(bar + stage % S, (unsigned)(stage / S) & 1u); }
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// CTA-wide ring: the CTA's warps cover adjacent column chunks of the SAME
+// rows, so one bulk copy of CB bytes per row feeds all of them (a larger copy
+// per TMA operation than a per-warp ring of one warp's chunk).  One thread
+// produces; every warp consumes each stage and releases it through the
+// stage's `empty` barrier (one arrival per warp), which the producer waits on
+// before refilling the slot (the ordering the release/acquire pair gives; no
+// proxy fence is needed for reads followed by an async-proxy refill).
+template <int S, int CB>
+struct CtaRing {
+  static constexpr int kBytes = (S * CB + 2 * S * 8 + 127) / 128 * 128;
+  uint8_t* buf;
+  uint64_t* full;
+  uint64_t* empty;
+  // every thread of the CTA calls this (it ends with __syncthreads)
+  __device__ __forceinline__ void init(uint8_t* base, int nwarps) {
+    buf = base;
+    full = reinterpret_cast<uint64_t*>(base + S * CB);
+    empty = full + S;
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        mbar_init(full + s, 1);
+        mbar_init(empty + s, nwarps);
+      }
+      fence_barrier_init();
+    }
+    __syncthreads();
+  }
+  __device__ __forceinline__ const uint8_t* row(int stage) const { return buf + (stage % S) * CB; }
+  // the producer thread only: stage `stage` := `bytes` from src
+  __device__ __forceinline__ void produce(int stage, const void* src, unsigned bytes) {
+    const int s = stage % S;
+    if (stage >= S) mbar_wait(empty + s, (unsigned)(stage / S - 1) & 1u);
+    mbar_expect_tx(full + s, bytes);
+    bulk_g2s(buf + s * CB, src, bytes, full + s);
+  }
+  __device__ __forceinline__ void wait(int stage) const { mbar_wait(full + stage % S, (unsigned)(stage / S) & 1u); }
+  // every warp, after its last read of the stage
+  __device__ __forceinline__ void release(int stage, int lane) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + stage % S);
+  }
 };
 
 }  // namespace apsp

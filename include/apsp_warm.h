@@ -110,11 +110,16 @@ typedef enum {
                                < 0x7F, else an int16 copy while every one is < 0x3FFF,
                                else D itself; results are identical on every path.
                                0: never int8 (int16 / int32 only).                    */
-  APSP_OPT_MIRROR = 8       /* 1 (default): keep the saturated mirror of APSP_OPT_MIRROR8.
+  APSP_OPT_MIRROR = 8,      /* 1 (default): keep the saturated mirror of APSP_OPT_MIRROR8.
                                0: no mirror at all — every O(n^2) pass streams the
                                int32 D itself (4 bytes per entry, SURVEY §8(d-4)'s
                                byte basis); for measuring the 4-byte streams.  Results
                                are identical.  Takes effect at the next update.       */
+  APSP_OPT_FUSED = 9        /* 1 (default): removals and directed edge increases on the
+                               int8 mirror run detection and the first phase of the
+                               sparse recompute in ONE pass, each row of the mirror
+                               staged whole in shared memory (n up to ~36K); 0: the
+                               separate kernels.  Results are identical.             */
 } apsp_option;
 
 /* Statistics of one update. */

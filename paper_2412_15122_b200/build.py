@@ -21,7 +21,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libapsp_warm.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["fw.cu", "stream.cu", "sparse.cu", "query.cu", "comm.cu", "microbench.cu", "apsp_warm.cu"]
+SOURCES = ["fw.cu", "stream.cu", "sparse.cu", "fused.cu", "query.cu", "comm.cu", "microbench.cu", "apsp_warm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
                 "-I" + os.path.join(ROOT, "include"), "-Xptxas", "-v"] + os.environ.get("APSP_NVCC_EXTRA", "").split()

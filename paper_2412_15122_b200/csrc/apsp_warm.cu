@@ -43,8 +43,9 @@ struct Plan {
   size_t off_wt, off_vec, off_rowpart, off_colpart, off_rowoff, off_rowcnt, off_chg, off_prow,
       off_pcol, off_ocol, off_ocnt, off_gprow, off_gpcol, off_glb, off_gfull,
       off_srow, off_scol, off_slid, off_slw, off_wnext, off_slscr, off_panel, off_pt, off_anyrow, off_qsend, off_qcol,
-      off_qids, off_qdsv, off_qlab, off_qpred, off_qpath, off_qdone, off_qcnt, off_p16, off_p8, off_ptd, off_small,
-      total;
+      off_qids, off_qdsv, off_qlab, off_qpred, off_qpath, off_qdone, off_qcnt, off_p16, off_p8, off_mt, off_ptd,
+      off_small, total;
+  int64_t ldt;   // row stride of the transposed int8 mirror (bytes >= local rows)
   int qcap, qbatch;
   int64_t ldpt;
 };
@@ -108,6 +109,8 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   // transposed diagonal tile
   p.off_p16 = take(sizeof(uint16_t) * (size_t)rows_max * p.ld);
   p.off_p8 = take((size_t)rows_max * p.ld);   // the int8 mirror (int32 handles)
+  p.ldt = round_up(rows_max, 128);
+  p.off_mt = take((size_t)cap * p.ldt);       // its transpose (column j of D = row j)
   p.off_ptd = take(sizeof(uint32_t) * (size_t)kTile * kTile);
   p.off_small = take(64 * 1024);
   p.total = o;
@@ -151,6 +154,7 @@ struct apsp_handle {
   int mirror_level = 16;         // width of the mirror: 8 or 16 bits
   int mirror8 = 1;               // APSP_OPT_MIRROR8: try the int8 width at each build
   int use_mirror = 1;            // APSP_OPT_MIRROR: 0 = no mirror, the streams read D (4 B/entry)
+  int fused = 1;                 // APSP_OPT_FUSED: detection + phase A in one pass (fused.cu)
   bool mirror8_failed = false;   // an int8 build found a distance >= 0x7F: int16 from then on
   // bytes per entry the O(n^2) streams read: 1 / 2 on a valid int8 / int16 mirror, else 4
   template <typename T> double stream_bytes() const {
@@ -271,7 +275,8 @@ struct apsp_handle {
     if constexpr (std::is_same<T, int32_t>::value) {
       if (!use_mirror) return Mirror{nullptr, nullptr, mirror_flag()};
       if (mirror_level == 8)
-        return Mirror{nullptr, ws + plan.off_p8, mirror_flag(), mirror_epoch_word(), ++mirror_epoch};
+        return Mirror{nullptr, ws + plan.off_p8, mirror_flag(), mirror_epoch_word(), ++mirror_epoch,
+                      ws + plan.off_mt, ld, plan.ldt};
       return Mirror{reinterpret_cast<uint16_t*>(p16()), nullptr, mirror_flag(), mirror_epoch_word(), ++mirror_epoch};
     } else {
       return Mirror{nullptr, nullptr, mirror_flag()};
@@ -624,6 +629,14 @@ apsp_status fork_shortlist_remove(apsp_handle* h, int64_t k) {
   return APSP_OK;
 }
 
+// The fused detection + phase A kernel (fused.cu) applies: int32 shortest
+// path, the int8 mirror known valid, one pivot term (removal or a directed
+// increase), and a row of the mirror fits in shared memory.
+template <typename T>
+bool use_fused(const apsp_handle* h, bool two) {
+  return std::is_same<T, int32_t>::value && !two && mirror8_known_valid(h) && h->fused && fused_stages(h->n) > 0;
+}
+
 template <typename T>
 apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, const T* c2,
                       const T* r2, bool removal, apsp_update_info* info) {
@@ -641,21 +654,37 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     z.add(h->anyrow(), h->cap);   // the rounds' per-row open minima (keys)
     CK(zero_set(z, h->st));
   }
-  // one streaming pass appends the need_update_list; then the per-row slices
-  // of the open lists and Phi / max|A_i|
-  PK(APSP_K_DETECT, h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n,
-     detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, 1, nullptr, h->rowcnt(),
-               h->srow(), h->scol(), nullptr, lcap, h->ctr(), h->WT<T>(), h->ld, h->sr,
-               h->mirror<T>(), h->st));
-  PK(APSP_K_EMIT, 0.0, detect_lists(r, h->rowcnt(), h->rowoff(), h->ctr(), h->st));
-  if (removal) CK(tombstone<T>(h->Dl<T>(), h->ld, r, n, skip, h->WT<T>(), h->ld, h->st));
-
   // ---- sparse recompute (a6), enqueued without a host round trip: the pair
   // counts stay on the device, and the kernels do nothing if a list
   // overflowed.  Every value they write is a walk length of G' (>= the new
   // distance), so if the gate below picks the dense path after all, FW on
   // the result is still exact.
   const bool try_sparse = h->force_path != 2;
+  const bool fused = use_fused<T>(h, c2 != nullptr) && try_sparse;
+  if (fused) {
+    // detection + phase A in one pass over the int8 mirror (fused.cu); the
+    // pairs it could not buffer get the stand-alone phase A below
+    PK(APSP_K_DETECT, (double)(r.hi - r.lo) * (double)n,
+       detect_fix_p8(reinterpret_cast<int32_t*>(h->Dl<T>()), h->ld, r, n, skip,
+                     reinterpret_cast<const int32_t*>(c1), reinterpret_cast<const int32_t*>(r1), h->slid(),
+                     reinterpret_cast<const int32_t*>(h->slw<T>()), h->mirror<T>(), h->rowcnt(), h->srow(),
+                     h->scol(), lcap, h->ctr(), 0, h->st));
+    PK(APSP_K_EMIT, 0.0, detect_lists(r, h->rowcnt(), h->rowoff(), h->ctr(), h->st));
+    if (removal) CK(tombstone<T>(h->Dl<T>(), h->ld, r, n, skip, h->WT<T>(), h->ld, h->st));
+    PK(APSP_K_SPARSE0, 0.0,
+       sparse_phase_a<T>(h->Dl<T>(), h->ld, r, h->slid(), h->slw<T>(), h->rowoff(), h->srow(), h->scol(),
+                         lcap, c1, r1, c2, r2, h->tau, h->ocnt(), h->ocol(), h->gprow(), h->gpcol(),
+                         h->glb<T>(), h->gfull(), ocap, h->ctr(), h->sr, h->mirror<T>(), h->st, 2));
+  } else {
+    // one streaming pass appends the need_update_list; then the per-row slices
+    // of the open lists and Phi / max|A_i|
+    PK(APSP_K_DETECT, h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n,
+       detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, 1, nullptr, h->rowcnt(),
+                 h->srow(), h->scol(), nullptr, lcap, h->ctr(), h->WT<T>(), h->ld, h->sr,
+                 h->mirror<T>(), h->st));
+    PK(APSP_K_EMIT, 0.0, detect_lists(r, h->rowcnt(), h->rowoff(), h->ctr(), h->st));
+    if (removal) CK(tombstone<T>(h->Dl<T>(), h->ld, r, n, skip, h->WT<T>(), h->ld, h->st));
+  }
   // Rounds are frontier-based Bellman-Ford over each row's open entries: round
   // r relaxes every open pair of a row through the entries of that row that
   // changed in round r-1 (round 0: all open entries).  Frontier lists live in
@@ -684,6 +713,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   if (try_sparse) {
     // A: every listed entry rewritten with a walk length of G' (stale entries
     // skipped by the detection predicate), certified where it reaches lb
+    if (!fused)
     PK(APSP_K_SPARSE0, 0.0,
        sparse_phase_a<T>(h->Dl<T>(), h->ld, r, h->slid(), h->slw<T>(), h->rowoff(), h->srow(), h->scol(),
                          lcap, c1, r1, c2, r2, h->tau, h->ocnt(), h->ocol(), h->gprow(), h->gpcol(),
@@ -770,6 +800,10 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     else if (!try_sparse)   // no phase A ran: the listed entries still hold D_old
       CK(reset_pairs<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->srow(), h->scol(), h->ctr(), lcap,
                         h->st));
+    // the sparse kernels' values are walk lengths of G' but may exceed a
+    // listed pair's own edge: FW needs D0 <= W' too (one O(n^2) pass, against
+    // the O(n^3) FW that follows)
+    if (try_sparse) CK(min_with_w<T>(h->Dl<T>(), h->ld, r, n, h->WT<T>(), h->ld, h->st));
     return fw_impl<T>(h, removal ? skip : -1);
   }
   if (info) info->path = 2;
@@ -870,7 +904,8 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
            addcol_g(as, r, h->mirror<T>().m8, ld, n, iw, ow, reinterpret_cast<int*>(h->rowpart<T>()) + 2 * ld,
                     reinterpret_cast<int*>(h->vec<T>(5)), reinterpret_cast<int*>(h->rowpart<T>()) + 3 * ld,
                     kAddColLimit, col, ceff, h->vec<T>(6),
-                    reinterpret_cast<int*>(h->vec<T>(7)), h->wmin<int32_t>(), h->st));
+                    reinterpret_cast<int*>(h->vec<T>(7)), h->wmin<int32_t>(), h->st, h->mirror<T>().mt,
+                    h->plan.ldt));
         cfull = as.ufull;
       }
     }
@@ -1260,10 +1295,18 @@ apsp_status need_list_impl(apsp_handle* h, int kind, int64_t a, int64_t b, int32
   z.add(h->rowcnt(), h->cap);
   z.add(reinterpret_cast<int*>(h->ctr()), (int64_t)(sizeof(DetectCounters) / sizeof(int)));
   CK(zero_set(z, h->st));
-  PK(APSP_K_DETECT, h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n,
-     detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, h->tau, 1, nullptr,
-               h->rowcnt(), h->srow(), h->scol(), nullptr, h->plan.lcap, h->ctr(), h->WT<T>(), h->ld, h->sr,
-               h->mirror<T>(), h->st));
+  if (use_fused<T>(h, und)) {   // the kernel the update would run, every pair on the list
+    PK(APSP_K_DETECT, (double)(r.hi - r.lo) * (double)n,
+       detect_fix_p8(reinterpret_cast<int32_t*>(h->Dl<T>()), h->ld, r, n, skip,
+                     reinterpret_cast<const int32_t*>(c1), reinterpret_cast<const int32_t*>(r1), h->slid(),
+                     reinterpret_cast<const int32_t*>(h->slw<T>()), h->mirror<T>(), h->rowcnt(), h->srow(),
+                     h->scol(), h->plan.lcap, h->ctr(), 1, h->st));
+  } else {
+    PK(APSP_K_DETECT, h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n,
+       detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, h->tau, 1,
+                 nullptr, h->rowcnt(), h->srow(), h->scol(), nullptr, h->plan.lcap, h->ctr(), h->WT<T>(), h->ld,
+                 h->sr, h->mirror<T>(), h->st));
+  }
   unsigned long long tot = 0;
   CKR(cudaMemcpyAsync(h->host_small, &h->ctr()->total, sizeof tot, cudaMemcpyDeviceToHost, h->st));
   CKR(cudaStreamSynchronize(h->st));
@@ -1509,6 +1552,10 @@ apsp_status apsp_set_option(apsp_handle* h, apsp_option opt, double value) {
       if (value != 0 && value != 1) return APSP_E_INVAL;
       h->use_mirror = (int)value;
       h->mirror_built = false;
+      return APSP_OK;
+    case APSP_OPT_FUSED:
+      if (value != 0 && value != 1) return APSP_E_INVAL;
+      h->fused = (int)value;
       return APSP_OK;
     case APSP_OPT_ROW_DELTA:
       if (!(value >= 0) || value > 1) return APSP_E_INVAL;

@@ -22,6 +22,12 @@ struct Mirror {
   // CTAs still see the pre-launch state (rows left un-relaxed otherwise)
   unsigned* ep = nullptr;
   unsigned epoch = 0;
+  // int8 level only: the transposed copy MT[j][li] = m8[li][j] (li = local row),
+  // kept in step by every writer of m8, so that a COLUMN of D is a contiguous
+  // row of MT (the add-node column reads it).  nullptr: none.
+  uint8_t* mt = nullptr;
+  int64_t ld = 0;    // row stride of m / m8 (elements)
+  int64_t ldt = 0;   // row stride of mt (bytes >= local rows)
 };
 
 // Device counters written by the detection kernel.
@@ -33,6 +39,7 @@ struct DetectCounters {
   unsigned int err;           // validation flag (add_node inputs)
   unsigned long long open_total;   // open pairs after the shortlist certification
   unsigned long long rowbase;      // cursor of the per-row open-list slices
+  unsigned long long spill;        // fused detection + phase A: pairs left on the global list
 };
 
 // ---------------- fw.cu ----------------  (sr: 0 shortest path, 1 minimax)
@@ -109,7 +116,8 @@ cudaError_t addrow_s(const AddScratch& a, const int32_t* ow, int64_t n, const ui
 cudaError_t addcol_g(const AddScratch& a, Rows r, const uint8_t* m8, int64_t ld, int64_t n, const int32_t* iw,
                      const int32_t* ow, const int* tflag, int* ulist, int* uaux /* 2 * limit */, int limit,
                      int32_t* col, int32_t* ceff, int32_t* mprime, int* fb_list,
-                     int32_t wmin /* <= every edge weight */, cudaStream_t st);
+                     int32_t wmin /* <= every edge weight */, cudaStream_t st,
+                     const uint8_t* mt = nullptr, int64_t ldt = 0 /* the transposed mirror, if any */);
 template <typename T>
 cudaError_t addnode_finish(const T* rowpart, const T* rowpartM, int nchunk, const T* colpart,
                            int nslab, int64_t part_ld, Rows r, int64_t n, int64_t npad, T* col,
@@ -137,6 +145,8 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
 cudaError_t detect_lists(Rows r, const int* rowcnt, int64_t* rowoff, DetectCounters* ctr,
                          cudaStream_t st);
 // D[i][j] := W'[i][j] on every listed pair (the dense path without the sparse kernels)
+template <typename T>
+cudaError_t min_with_w(T* D, int64_t ld, Rows r, int64_t n, const T* WT, int64_t ldw, cudaStream_t st);
 template <typename T>
 cudaError_t reset_pairs(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, const int* srow,
                         const int* scol, const DetectCounters* ctr, int64_t lcap, cudaStream_t st);
@@ -198,7 +208,8 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
                            const int64_t* rowoff, const int* srow, const int* scol, int64_t npairs,
                            const T* c1, const T* r1, const T* c2, const T* r2, float tau, int* ocnt,
                            int* ocol, int* gprow, int* gpcol, T* glb, unsigned char* gfull, int64_t ocap,
-                           DetectCounters* ctr, int sr, Mirror M, cudaStream_t st);
+                           DetectCounters* ctr, int sr, Mirror M, cudaStream_t st,
+                           int list = 0 /* 0: the need_update_list, 2: the fused kernel's spills */);
 template <typename T>
 cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
                         const int* gprow, const int* gpcol, const T* glb, const unsigned char* gfull,
@@ -288,5 +299,16 @@ struct ZeroSet {
 cudaError_t zero_set(const ZeroSet& z, cudaStream_t st);
 double microbench(int kind, void* buf, size_t bytes, cudaStream_t st);   // microbench.cu
 int num_sms();
+// ---------------- fused.cu ----------------
+// Detection + phase A in one pass over the int8 mirror (removal, or a directed
+// edge increase: c1 = D[:, u] (+ w), r1 = D[v, :]); rows are staged whole in
+// shared memory: fused_stages(n) > 0 iff a row of n bytes fits.
+int fused_stages(int64_t n);
+// Outputs: rowcnt[i] = |A_i|, ctr->total = |A|, and on (srow, scol) with
+// count ctr->spill the pairs it did not certify (all of them if export_only).
+cudaError_t detect_fix_p8(int32_t* D, int64_t ld, Rows r, int64_t n, int64_t skip, const int32_t* c1,
+                          const int32_t* r1, const int* SLid, const int32_t* SLw, Mirror M, int* rowcnt,
+                          int* srow, int* scol, int64_t lcap, DetectCounters* ctr, int export_only,
+                          cudaStream_t st);
 
 }  // namespace apsp

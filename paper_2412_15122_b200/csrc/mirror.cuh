@@ -12,9 +12,18 @@ namespace apsp {
 // bits the write raises; callers OR them per thread and post them once per
 // warp (mirror_post).
 constexpr unsigned kMirrorOff = 1u, kMirrorInf = 2u;
+// the transposed byte of m8[li][j] (no-op without MT)
+__device__ __forceinline__ void mput_t(const Mirror& M, int64_t li, int64_t j, uint8_t b) {
+  if (M.mt) M.mt[j * M.ldt + li] = b;
+}
 __device__ __forceinline__ unsigned mput(const Mirror& M, int64_t idx, int32_t v) {
   if (M.m8) {
-    M.m8[idx] = (uint8_t)min(v, kSat8i);
+    const uint8_t b = (uint8_t)min(v, kSat8i);
+    M.m8[idx] = b;
+    if (M.mt) {
+      const int64_t li = idx / M.ld;
+      mput_t(M, li, idx - li * M.ld, b);
+    }
     return v >= APSP_INF_I32_DEV ? kMirrorInf : (v >= kSat8i ? kMirrorOff : 0u);
   }
   M.m[idx] = sat16(v);

@@ -528,10 +528,12 @@ constexpr int kPhaseASteps = 3;   // phase A: sorted shortlist positions 0-7, 8-
 // the sparse recompute): which = 0, the need_update_list (nothing to do if it
 // overflowed: some flagged entries were never reset); 1, the open pairs
 // (nothing to do if either list overflowed — the dense path follows).
+// which = 2: the pairs the fused detection + phase A kernel spilled to the
+// global list (fused.cu).
 __device__ __forceinline__ int64_t device_count(const DetectCounters* dc, int64_t cap, int which) {
   if (!dc) return cap;
-  if (dc->overflow & (which ? 3u : 1u)) return 0;
-  const int64_t c = (int64_t)(which ? dc->open_total : dc->total);
+  if (dc->overflow & (which == 1 ? 3u : 1u)) return 0;
+  const int64_t c = (int64_t)(which == 1 ? dc->open_total : which == 2 ? dc->spill : dc->total);
   return c < cap ? c : cap;
 }
 
@@ -678,10 +680,11 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_a(T* D, int64_t l
                                                         const T* __restrict__ c1, const T* __restrict__ r1,
                                                         const T* __restrict__ c2, const T* __restrict__ r2,
                                                         float tau, OpenLists<T> ol,
-                                                        const DetectCounters* dc, Mirror M, int nbatch) {
+                                                        const DetectCounters* dc, Mirror M, int nbatch,
+                                                        int list) {
   const int lane = threadIdx.x & 31;
   unsigned mbits = 0;   // mirror flag bits raised by this thread's writes
-  npairs = device_count(dc, npairs, 0);
+  npairs = device_count(dc, npairs, list);
   // the gathers read the int8 mirror while it is valid (exact; a quarter of
   // the bytes).  An entry this kernel rewrites meanwhile reads as its old
   // value (stale: skipped by the test below), its new final value, or 0x7F
@@ -793,10 +796,11 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_aq(T* D, int64_t 
                                                          const T* __restrict__ c1, const T* __restrict__ r1,
                                                          const T* __restrict__ c2, const T* __restrict__ r2,
                                                          float tau, OpenLists<T> ol,
-                                                         const DetectCounters* dc, Mirror M, int nbatch) {
+                                                         const DetectCounters* dc, Mirror M, int nbatch,
+                                                         int list) {
   const int lane = threadIdx.x & 31;
   unsigned mbits = 0;
-  npairs = device_count(dc, npairs, 0);
+  npairs = device_count(dc, npairs, list);
   const uint8_t* M8 = nullptr;
   if constexpr (std::is_same<T, int32_t>::value && SR == 0)
     if (M.m8 && (*(volatile unsigned*)M.flag & 1u) == 0u) M8 = M.m8;
@@ -914,7 +918,7 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
                            const int64_t* rowoff, const int* srow, const int* scol, int64_t npairs,
                            const T* c1, const T* r1, const T* c2, const T* r2, float tau, int* ocnt,
                            int* ocol, int* gprow, int* gpcol, T* glb, unsigned char* gfull, int64_t ocap,
-                           DetectCounters* ctr, int sr, Mirror M, cudaStream_t st) {
+                           DetectCounters* ctr, int sr, Mirror M, cudaStream_t st, int list) {
   if (npairs <= 0) return cudaSuccess;
   OpenLists<T> ol{ocnt, ocol, rowoff, gprow, gpcol, glb, gfull, ocap, ctr};
   // npairs is the capacity bound (the device count decides): full occupancy
@@ -923,10 +927,10 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
   do {                                                                                             \
     if (queue)                                                                                     \
       k_sparse_phase_aq<T, SRV, TWOV><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, srow, scol,  \
-                                                            npairs, c1, r1, c2, r2, tau, ol, ctr, M, nb); \
+                                                            npairs, c1, r1, c2, r2, tau, ol, ctr, M, nb, list); \
     else                                                                                           \
       k_sparse_phase_a<T, SRV, TWOV><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, srow, scol,   \
-                                                           npairs, c1, r1, c2, r2, tau, ol, ctr, M, nb); \
+                                                           npairs, c1, r1, c2, r2, tau, ol, ctr, M, nb, list); \
   } while (0)
   static const int nb = std::min(kSL / 8, pa_tune("APSP_TUNE_PA_BATCHES", kPhaseABatches));
   static const bool queue = pa_tune("APSP_TUNE_PA_QUEUE", 1) == 1;   // 2: the one-pair-per-lane kernel
@@ -1139,7 +1143,7 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
                                          const int*, const int*, int64_t, const T*, const T*,      \
                                          const T*, const T*, float, int*, int*, int*, int*, T*,    \
                                          unsigned char*, int64_t, DetectCounters*, int, Mirror,    \
-                                         cudaStream_t);                                            \
+                                         cudaStream_t, int);                                       \
   template cudaError_t sparse_full<T>(T*, int64_t, int64_t, const T*, int64_t, int64_t,            \
                                       const int*, const int*, const T*, const unsigned char*,      \
                                       int64_t, int, const DetectCounters*, cudaStream_t, Mirror);         \

@@ -322,6 +322,7 @@ __global__ void k_mirror_build(const int32_t* __restrict__ D, int64_t ld, Rows r
   }
   mirror_post(M, bits);
 }
+static cudaError_t mirror_transpose(Mirror M, int64_t m, int64_t n, cudaStream_t st);
 // M8 := the int8 image of the packed int16 buffer P (sat16(D) after a packed
 // FW): a half h becomes min(h, 0x7F); 0x3FFF (INF or saturated) stays INF-like
 __global__ void k_mirror8_from_p16(const uint32_t* __restrict__ P, int64_t ld, int64_t m, int64_t n,
@@ -348,7 +349,8 @@ __global__ void k_mirror8_from_p16(const uint32_t* __restrict__ P, int64_t ld, i
 cudaError_t mirror8_from_p16(const uint32_t* P, int64_t ld, int64_t m, int64_t n, Mirror M, cudaStream_t st) {
   if (m <= 0 || !M.m8) return cudaSuccess;
   k_mirror8_from_p16<<<num_sms() * 8, 256, 0, st>>>(P, ld, m, n, M);
-  return cudaGetLastError();
+  CUDA_TRY(cudaGetLastError());
+  return mirror_transpose(M, m, n, st);
 }
 // M[i][j] := sat16(D[i][j]) for the listed pairs (the sparse recompute's writes)
 __global__ void k_mirror_pairs(const int32_t* __restrict__ D, int64_t ld, int64_t row0,
@@ -379,10 +381,33 @@ __global__ void k_mirror_cross(const int32_t* __restrict__ D, int64_t ld, Rows r
   mirror_post(M, bits);
 }
 
+// MT[j][li] := M8[li][j] for the m local rows and n columns (after a full
+// build of the int8 mirror), 32 x 32-byte tiles through shared memory
+__global__ void k_mirror_transpose(Mirror M, int64_t m, int64_t n) {
+  __shared__ uint8_t tile[32][33];
+  const int64_t l0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  for (int rr = threadIdx.y; rr < 32; rr += blockDim.y) {
+    const int64_t li = l0 + rr, j = j0 + threadIdx.x;
+    tile[rr][threadIdx.x] = (li < m && j < n) ? M.m8[li * M.ld + j] : (uint8_t)kSat8i;
+  }
+  __syncthreads();
+  for (int rr = threadIdx.y; rr < 32; rr += blockDim.y) {
+    const int64_t j = j0 + rr, li = l0 + threadIdx.x;
+    if (j < n && li < m) M.mt[j * M.ldt + li] = tile[threadIdx.x][rr];
+  }
+}
+static cudaError_t mirror_transpose(Mirror M, int64_t m, int64_t n, cudaStream_t st) {
+  if (!M.m8 || !M.mt || m <= 0) return cudaSuccess;
+  dim3 grid((unsigned)cdiv(n, 32), (unsigned)cdiv(m, 32));
+  k_mirror_transpose<<<grid, dim3(32, 8), 0, st>>>(M, m, n);
+  return cudaGetLastError();
+}
+
 cudaError_t mirror_build(const int32_t* D, int64_t ld, Rows r, int64_t n, Mirror M, cudaStream_t st) {
   if (r.hi <= r.lo) return cudaSuccess;
   k_mirror_build<<<num_sms() * 8, 256, 0, st>>>(D, ld, r, n, M);
-  return cudaGetLastError();
+  CUDA_TRY(cudaGetLastError());
+  return mirror_transpose(M, r.hi - r.row0, n, st);   // (rows before r.lo are not active: r.lo == r.row0)
 }
 cudaError_t mirror_pairs(const int32_t* D, int64_t ld, int64_t row0, const int* prow, const int* pcol,
                          const DetectCounters* ctr, int64_t lcap, int open, Mirror M, cudaStream_t st) {
@@ -963,6 +988,77 @@ __global__ void __launch_bounds__(256) k_addcol_gather(AddScratch a, Rows r, con
     }
   }
 }
+// The same from the transposed mirror MT (column t of D = row t of MT): a
+// thread owns 4 consecutive local rows and streams the |U| rows of MT at its
+// 4 bytes — |U| x m bytes, coalesced, instead of |U| one-byte sector gathers
+// per row (which cost ~85 B of DRAM each, measured).  U's (t, in[t], out[t])
+// are staged in shared memory.
+constexpr int kAddColMax = 2048;   // |U| limit (= kAddColLimit of the host)
+constexpr int kACQ = 64, kACY = 8;   // row quads per CTA (256 rows), slices of U
+__global__ void __launch_bounds__(kACQ * kACY) k_addcol_mt(AddScratch a, Rows r, const uint8_t* __restrict__ mt,
+                                                           int64_t ldt, const int* __restrict__ ulist,
+                                                           const int* __restrict__ uin, const int* __restrict__ uout,
+                                                           int limit, const int32_t* __restrict__ iw, int32_t* col,
+                                                           int32_t* ceff, int32_t* mprime, int* fb_list, int delta,
+                                                           int32_t wmin) {
+  __shared__ int su[kAddColMax], sin_[kAddColMax], sout[kAddColMax];
+  __shared__ int rp[kACY][kACQ][4], rm[kACY][kACQ][4];
+  const int cnt = *a.u_count;
+  if (cnt > limit) {   // too many columns: the streaming pass does it
+    if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) *a.ufull = 1u;
+    return;
+  }
+  const int tid = threadIdx.y * kACQ + threadIdx.x;
+  for (int k = tid; k < cnt; k += kACQ * kACY) { su[k] = ulist[k]; sin_[k] = uin[k]; sout[k] = uout[k]; }
+  __syncthreads();
+  const int32_t I = APSP_INF_I32_DEV;
+  const int64_t m = r.hi - r.lo, lbase = r.lo - r.row0;   // local rows [lbase, lbase + m)
+  // thread (x, y): rows lbase + 4 (256 blockIdx.x / 4 + x) + [0, 4), U entries y, y + kACY, ...
+  const int64_t q = (int64_t)blockIdx.x * kACQ + threadIdx.x;
+  const int64_t l0 = lbase + 4 * q;
+  int32_t p[4] = {I, I, I, I}, mx[4] = {INT_MIN, INT_MIN, INT_MIN, INT_MIN};
+  if (4 * q < m) {
+#pragma unroll 4
+    for (int k = threadIdx.y; k < cnt; k += kACY) {
+      const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(mt + (int64_t)su[k] * ldt + l0));
+      const int32_t av = sin_[k], bv = sout[k];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int32_t d = (int32_t)((w >> (8 * e)) & 0xFFu);
+        const bool fin = d != kSat8i;
+        if (fin && av < I) p[e] = min(p[e], min(d + av, I));
+        // an INF entry with a finite out: never skip (as in pass 1)
+        if (bv < I) mx[e] = max(mx[e], fin ? d - bv : I);
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) { rp[threadIdx.y][threadIdx.x][e] = p[e]; rm[threadIdx.y][threadIdx.x][e] = mx[e]; }
+  __syncthreads();
+  if (threadIdx.y != 0 || 4 * q >= m) return;
+#pragma unroll
+  for (int y = 1; y < kACY; ++y)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { p[e] = min(p[e], rp[y][threadIdx.x][e]); mx[e] = max(mx[e], rm[y][threadIdx.x][e]); }
+  const int32_t th2 = *a.th2;
+  const unsigned imn = *a.in_min;
+  const int32_t th = imn >= (unsigned)I ? I : min(I - 1, (int32_t)imn + delta);
+  const int32_t thr0 = th2 == 0x7F7F7F7F ? INT_MAX : (int32_t)min((int64_t)th2 + wmin, (int64_t)I);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (4 * q + e >= m) break;
+    const int64_t i = r.row0 + l0 + e;
+    const int32_t ii = iw[i];
+    if (p[e] <= (ii > th ? min(thr0, ii) : thr0)) {
+      col[i] = p[e];
+      ceff[i] = p[e] < mx[e] ? p[e] : I;
+    } else {
+      mprime[i] = mx[e];
+      fb_list[atomicAdd(a.fb_count, 1)] = (int)i;
+    }
+  }
+}
+
 // the rows col1 could not certify: a full-row min over the mirror (block per row)
 __global__ void __launch_bounds__(256) k_addcol_rows(AddScratch a, Rows r, const uint8_t* __restrict__ m8, int64_t ld,
                                                      int64_t n, const int32_t* __restrict__ iw,
@@ -1004,12 +1100,19 @@ __global__ void __launch_bounds__(256) k_addcol_rows(AddScratch a, Rows r, const
 }
 cudaError_t addcol_g(const AddScratch& a, Rows r, const uint8_t* m8, int64_t ld, int64_t n, const int32_t* iw,
                      const int32_t* ow, const int* tflag, int* ulist, int* uaux, int limit, int32_t* col,
-                     int32_t* ceff, int32_t* mprime, int* fb_list, int32_t wmin, cudaStream_t st) {
+                     int32_t* ceff, int32_t* mprime, int* fb_list, int32_t wmin, cudaStream_t st,
+                     const uint8_t* mt, int64_t ldt) {
   const int g = (int)std::min<int64_t>(cdiv(n, 256), 2 * num_sms());
   static const int delta = tune_wps("APSP_TUNE_ADDCOL_DELTA", 2);   // th = min in + delta (measured)
   k_addcol_sets<<<g, 256, 0, st>>>(a, iw, ow, tflag, n, delta, ulist, uaux, uaux + limit, limit);
   CUDA_TRY(cudaGetLastError());
-  if (r.hi > r.lo) {
+  if (r.hi > r.lo && mt && limit <= kAddColMax && ((r.lo - r.row0) & 3) == 0 && (ldt & 3) == 0) {
+    const int grid = (int)cdiv(cdiv(r.hi - r.lo, 4), kACQ);
+    k_addcol_mt<<<grid, dim3(kACQ, kACY), 0, st>>>(a, r, mt, ldt, ulist, uaux, uaux + limit, limit, iw, col, ceff,
+                                                   mprime, fb_list, delta, wmin);
+    CUDA_TRY(cudaGetLastError());
+    k_addcol_rows<<<num_sms(), 256, 0, st>>>(a, r, m8, ld, n, iw, fb_list, mprime, col, ceff);
+  } else if (r.hi > r.lo) {
     const int grid = (int)std::min<int64_t>(cdiv(r.hi - r.lo, 8), (int64_t)num_sms() * 16);
     k_addcol_gather<<<grid, 256, 0, st>>>(a, r, m8, ld, ulist, uaux, uaux + limit, limit, iw, col, ceff, mprime,
                                           fb_list, delta, wmin);
@@ -1541,6 +1644,17 @@ __global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, in
               }
               *reinterpret_cast<uint4*>(mrow + jg) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
               if (big) mbits |= kMirrorOff;   // a distance >= 0x7F: the int8 mirror is no longer exact
+              if (M.mt) {   // the changed bytes into the transposed copy
+                const uint32_t ow[4] = {wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const uint32_t x = mw[q] ^ ow[q];
+                  if (!x) continue;
+#pragma unroll
+                  for (int e = 0; e < 4; ++e)
+                    if ((x >> (8 * e)) & 0xFFu) mput_t(M, i - r.row0, jg + 4 * q + e, (uint8_t)(mw[q] >> (8 * e)));
+                }
+              }
             } else {   // the row's ragged end: element stores below n
 #pragma unroll
               for (int e = 0; e < 16; ++e)
@@ -2026,7 +2140,9 @@ __global__ void __launch_bounds__(256, 3) k_detect_p16(T* __restrict__ D, int64_
         for (int q = 0; q < DS_V * 2; ++q) {
           uint32_t x = __viaddmin_s16x2(cr, rw[q], dw[q]) ^ dw[q];
           if (TWO) x |= __viaddmin_s16x2(cr2, rw2[q], dw[q]) ^ dw[q];
-          const uint32_t t = x | ((x & 0x7FFF7FFFu) + 0x7FFF7FFFu);
+          // not an INF entry (d == 0x3FFF tests tight where c is INF and r is 0)
+          const uint32_t dn = dw[q] ^ 0x3FFF3FFFu;
+          const uint32_t t = (x | ((x & 0x7FFF7FFFu) + 0x7FFF7FFFu)) & (dn | ((dn & 0x7FFF7FFFu) + 0x7FFF7FFFu));
           word |= (((t >> 15) & 1u) | ((t >> 30) & 2u)) << (2 * q);
         }
         word &= vmask;
@@ -2210,6 +2326,10 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
             if (t & 0x80808080u) {
               uint32_t z = ~(u | ((u & 0x7F7F7F7Fu) + 0x7F7F7F7Fu)) & 0x80808080u;   // exact zero bytes
               if (TWO) z |= ~(u2 | ((u2 & 0x7F7F7F7Fu) + 0x7F7F7F7Fu)) & 0x80808080u;
+              // minus the INF entries (d == 0x7F with c INF and r == 0 tests
+              // tight; INF pairs are never listed, Q5)
+              const uint32_t dq = d[q] ^ 0x7F7F7F7Fu;
+              z &= dq | ((dq & 0x7F7F7F7Fu) + 0x7F7F7F7Fu);
               // bytes 0..3 -> bits 4q' .. 4q'+3 of this lane's 16-column half
               const uint32_t nib = ((((z >> 7) & 0x01010101u) * 0x01020408u) >> 24) & 0xFu;
               word |= nib << ((q >> 2) * 16 + (q & 3) * 4);
@@ -2315,6 +2435,37 @@ template <typename T>
 cudaError_t reset_pairs(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, const int* srow,
                         const int* scol, const DetectCounters* ctr, int64_t lcap, cudaStream_t st) {
   k_reset_pairs<T><<<num_sms() * 8, 256, 0, st>>>(D, ld, row0, WT, ldw, srow, scol, ctr, lcap);
+  return cudaGetLastError();
+}
+
+// D[i][j] := min(D[i][j], W'[i][j]) over the local rows (W' = WT transposed,
+// 32x32 shared-memory tiles) — before a dense fallback that follows the
+// sparse kernels: their values are walk lengths of G' but may exceed the
+// listed pair's direct edge (phase A looks at the cheapest in-edges of j
+// only), and FW(D0) is exact only when D0 <= W' as well.
+template <typename T>
+__global__ void k_min_with_w(T* D, int64_t ld, Rows r, int64_t n, const T* __restrict__ WT, int64_t ldw) {
+  __shared__ T tile[32][33];
+  const int64_t i0 = r.lo + blockIdx.y * 32, j0 = blockIdx.x * 32;
+  for (int rr = threadIdx.y; rr < 32; rr += blockDim.y) {
+    const int64_t j = j0 + rr, i = i0 + threadIdx.x;   // WT[j][i], coalesced over i
+    tile[rr][threadIdx.x] = (j < n && i < r.hi) ? WT[j * ldw + i] : Tr<T>::inf();
+  }
+  __syncthreads();
+  for (int rr = threadIdx.y; rr < 32; rr += blockDim.y) {
+    const int64_t i = i0 + rr, j = j0 + threadIdx.x;
+    if (i < r.hi && j < n) {
+      T* p = D + (i - r.row0) * ld + j;
+      const T w = tile[threadIdx.x][rr];
+      if (w < *p) *p = w;
+    }
+  }
+}
+template <typename T>
+cudaError_t min_with_w(T* D, int64_t ld, Rows r, int64_t n, const T* WT, int64_t ldw, cudaStream_t st) {
+  if (r.hi <= r.lo) return cudaSuccess;
+  dim3 grid((unsigned)cdiv(n, 32), (unsigned)cdiv(r.hi - r.lo, 32));
+  k_min_with_w<T><<<grid, dim3(32, 8), 0, st>>>(D, ld, r, n, WT, ldw);
   return cudaGetLastError();
 }
 
@@ -2587,6 +2738,7 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
                                  const T*, const T*, float, int, int*, int*, int*, int*, T*,      \
                                  int64_t, DetectCounters*, const T*, int64_t, int, Mirror,        \
                                  cudaStream_t);                                                   \
+  template cudaError_t min_with_w<T>(T*, int64_t, Rows, int64_t, const T*, int64_t, cudaStream_t);  \
   template cudaError_t reset_pairs<T>(T*, int64_t, int64_t, const T*, int64_t, const int*,         \
                                       const int*, const DetectCounters*, int64_t, cudaStream_t);  \
   template cudaError_t tombstone<T>(T*, int64_t, Rows, int64_t, int64_t, T*, int64_t,              \

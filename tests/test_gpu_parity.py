@@ -979,6 +979,10 @@ def test_need_update_list_set_for_set_int32(lib, rng, n, directed, hi, mirror):
     predicate set for set (Corollary 3 / Theorem 4): removals of
     random nodes and increases of tight edges (undirected: both orientations)."""
     W = random_graph(rng, n, directed, density=0.3, lo=1, hi=hi, inf_frac=0.02)
+    W[10:, :10] = INF          # nodes 0-9 reachable only among themselves: INF
+    if not directed:           # rows / columns (increases inside 0-9 must not
+        W[:10, 10:] = INF      # list the INF pairs, DESIGN.md Q5)
+    np.fill_diagonal(W, 0)
     h = make(lib, W, directed)
     h.set_option(lib._lib.OPT_MIRROR, mirror)
     D = oracle.fw(W)
@@ -992,8 +996,15 @@ def test_need_update_list_set_for_set_int32(lib, rng, n, directed, hi, mirror):
         assert h.mirror_width == (8 if D[D < INF].max() < 0x7F else 16)
     else:
         assert h.mirror_width == 0
-    for _ in range(3):
-        u, v = _tight_edge(W, D, rng)
+    for t in range(4):
+        if t == 0:   # an edge inside the 0-9 island
+            sub = W[:10, :10]
+            cand = [(a, b) for a in range(10) for b in range(10) if a != b and sub[a, b] < INF and sub[a, b] == D[a, b]]
+            if not cand:
+                continue
+            u, v = cand[0]
+        else:
+            u, v = _tight_edge(W, D, rng)
         r, c, cnt = h.need_update_list("increase", u, v)
         exp = _mask_pairs(oracle.need_update_increase(D, u, v, int(W[u, v]), directed))
         assert _pairs(r, c) == exp and cnt == len(exp)
@@ -1063,3 +1074,58 @@ def test_int32_streams_without_mirror_match_oracle(lib, rng):
             hg.set_edge(u, v, w)
         assert h.mirror_width == 0
     assert_parity(getD(h), oracle.fw(hg.W[:hg.n, :hg.n]))
+
+
+@pytest.mark.parametrize("fused", [1, 0])
+def test_fused_detect_phase_a_with_spills(lib, rng, fused):
+    """The fused detection + phase A kernel (fused.cu, removals on the int8
+    mirror) against the separate kernels and the oracle: a line metric with
+    repeated positions (every pair through the middle is a tie, so rows list
+    far more pairs than a stage's buffer holds and spill to the stand-alone
+    phase A), the sparse path forced; then random removals on a random graph.
+    Bit-exact vs the oracle's FW after every removal."""
+    n = 2500
+    x = np.sort(rng.integers(0, 100, n))
+    W = np.abs(x[:, None] - x[None, :]).astype(np.int32)
+    hg = synth.HostGraph(W, True)
+    h = make(lib, W)
+    h.set_option(lib._lib.OPT_FUSED, fused)
+    h.set_option(lib._lib.OPT_FORCE_PATH, 1)
+    assert h.mirror_width == 8
+    k = n // 2
+    _, info = h.remove_node(k)
+    hg.remove_node(k)
+    # (rows list more pairs than a stage buffer: the spill path ran; the gate
+    # may still finish densely — the sparse kernels' output is exact input)
+    assert info.path in (2, 3) and info.max_row_affected > 1024
+    assert_parity(getD(h), oracle.fw(hg.W))
+    W2 = random_graph(rng, 1800, True, density=0.05, lo=1, hi=9)
+    hg2 = synth.HostGraph(W2, True)
+    h2 = make(lib, W2)
+    h2.set_option(lib._lib.OPT_FUSED, fused)
+    for _ in range(4):
+        k = int(rng.integers(hg2.n))
+        h2.remove_node(k)
+        hg2.remove_node(k)
+        assert_parity(getD(h2), oracle.fw(hg2.W))
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.float32])
+def test_gate_dense_after_sparse_kernels(lib, rng, dtype):
+    """The default gate picks the dense FW AFTER the sparse kernels already ran
+    (|A| > theta n^2): a line metric with repeated positions, middle node
+    removed (every pair across it is a tie, |A| ~ n^2 / 2).  The sparse
+    kernels' values may exceed a listed pair's own edge (phase A reads the
+    cheapest in-edges of j only), so the fallback takes min(D, W') first —
+    without it this case came out too large.  Bit-exact
+    (int32) / 1e-5 (fp32) vs the oracle."""
+    n = 1500
+    x = np.sort(rng.integers(0, 60, n)).astype(np.float64)
+    W = np.abs(x[:, None] - x[None, :])
+    W = W.astype(np.int32) if dtype == np.int32 else (W * 0.125).astype(np.float32)
+    hg = synth.HostGraph(W, True)
+    h = make(lib, W)
+    _, info = h.remove_node(n // 2)
+    hg.remove_node(n // 2)
+    assert info.path == 3
+    assert_parity(getD(h), oracle.fw(hg.W))

@@ -115,11 +115,12 @@ typedef enum {
                                int32 D itself (4 bytes per entry, SURVEY §8(d-4)'s
                                byte basis); for measuring the 4-byte streams.  Results
                                are identical.  Takes effect at the next update.       */
-  APSP_OPT_FUSED = 9        /* 1 (default): removals and directed edge increases on the
-                               int8 mirror run detection and the first phase of the
-                               sparse recompute in ONE pass, each row of the mirror
-                               staged whole in shared memory (n up to ~36K); 0: the
-                               separate kernels.  Results are identical.             */
+  APSP_OPT_FUSED = 9        /* 1: removals and directed edge increases on the int8
+                               mirror run detection and the first phase of the sparse
+                               recompute in ONE pass, each row of the mirror staged
+                               whole in shared memory (n up to ~36K).  0 (default): the
+                               separate kernels, measured faster at BJ.c4 (DESIGN.md
+                               §11).  Results are identical.                          */
 } apsp_option;
 
 /* Statistics of one update. */
@@ -266,8 +267,12 @@ apsp_status apsp_modify_edge_readd(apsp_handle* h, int64_t u, int64_t v, double 
  *   path (host, path_cap int32) = s ... t; *path_len = its length
  *   (1 for s == t, 0 if unreachable); *n_candidates (may be NULL) = |C|.
  * E_RANGE: s/t out of range, or path_cap too small (*path_len then holds the
- * needed length), or |C| above the kernel's candidate capacity (4096).
- * Synchronises the stream. */
+ * needed length).  A candidate set larger than the batch scratch (4096) is
+ * answered by a second pass that computes every candidate's predecessor at
+ * once (one GPU, shortest path; e.g. the directed unit cycle, whose path
+ * has n nodes); only multi-GPU or minimax queries beyond 4096 candidates, or
+ * zero-weight ties that leave the large set without a chain, still return
+ * E_RANGE.  Synchronises the stream. */
 apsp_status sp_pair_query(apsp_handle* h, int64_t s, int64_t t, void* dist, int32_t* path,
                           int32_t path_cap, int32_t* path_len, int32_t* n_candidates);
 

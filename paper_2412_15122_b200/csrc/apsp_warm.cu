@@ -44,7 +44,7 @@ struct Plan {
       off_pcol, off_ocol, off_ocnt, off_gprow, off_gpcol, off_glb, off_gfull,
       off_srow, off_scol, off_slid, off_slw, off_wnext, off_slscr, off_panel, off_pt, off_anyrow, off_qsend, off_qcol,
       off_qids, off_qdsv, off_qlab, off_qpred, off_qpath, off_qdone, off_qcnt, off_p16, off_p8, off_mt, off_ptd,
-      off_small, total;
+      off_small, off_qbits, off_qbpred, off_qbout, total;
   int64_t ldt;   // row stride of the transposed int8 mirror (bytes >= local rows)
   int qcap, qbatch;
   int64_t ldpt;
@@ -105,6 +105,11 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   p.off_qpath = take(4 * qe);
   p.off_qdone = take(qe);
   p.off_qcnt = take(sizeof(int32_t) * (size_t)p.qbatch);
+  // a single query whose candidate set exceeds qcap (query_big): bitmap,
+  // predecessors, [length, path] (one GPU)
+  p.off_qbits = take(sizeof(uint32_t) * (size_t)(cap / 32 + 1));
+  p.off_qbpred = take(sizeof(int32_t) * (size_t)cap);
+  p.off_qbout = take(sizeof(int32_t) * (size_t)(cap + 4));
   // int16x2 FW (one GPU): packed copy of D (two columns per word) + the
   // transposed diagonal tile
   p.off_p16 = take(sizeof(uint16_t) * (size_t)rows_max * p.ld);
@@ -154,7 +159,8 @@ struct apsp_handle {
   int mirror_level = 16;         // width of the mirror: 8 or 16 bits
   int mirror8 = 1;               // APSP_OPT_MIRROR8: try the int8 width at each build
   int use_mirror = 1;            // APSP_OPT_MIRROR: 0 = no mirror, the streams read D (4 B/entry)
-  int fused = 1;                 // APSP_OPT_FUSED: detection + phase A in one pass (fused.cu)
+  int fused = 0;                 // APSP_OPT_FUSED: detection + phase A in one pass (fused.cu; off:
+                                 // measured slower than the separate kernels)
   bool mirror8_failed = false;   // an int8 build found a distance >= 0x7F: int16 from then on
   // bytes per entry the O(n^2) streams read: 1 / 2 on a valid int8 / int16 mirror, else 4
   template <typename T> double stream_bytes() const {
@@ -259,6 +265,9 @@ struct apsp_handle {
   unsigned* mirror_flag() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 396); }
   unsigned* pass1_uncertain() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 400); }
   unsigned* mirror_epoch_word() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 472); }
+  alignas(64) unsigned char tmap8[128];   // CUtensorMap of the int8 mirror (detection's TMA)
+  bool tmap8_ok = false;
+  const void* tmap8_ptr() const { return tmap8_ok ? tmap8 : nullptr; }
   unsigned mirror_epoch = 0;     // per-launch epochs of the rank-1 gate (Mirror::epoch)
   // the add-node shortcuts' scratch words (small + 404 ... 463)
   AddScratch add_scratch() {
@@ -637,23 +646,28 @@ bool use_fused(const apsp_handle* h, bool two) {
   return std::is_same<T, int32_t>::value && !two && mirror8_known_valid(h) && h->fused && fused_stages(h->n) > 0;
 }
 
+// Every per-update counter of the recompute: per-row counts, the counters,
+// the open-list cursors, the first four rounds' frontier counts, the flag.
+ZeroSet recompute_zero_set(apsp_handle* h) {
+  ZeroSet z{};
+  z.add(h->rowcnt(), h->cap);
+  z.add(reinterpret_cast<int*>(h->ctr()), (int64_t)(sizeof(DetectCounters) / sizeof(int)));
+  z.add(h->ocnt(), h->cap);
+  for (int q = 0; q < 4; ++q) z.add(h->chg(q), h->cap + 1);
+  z.add(h->anyflag(), 1);
+  z.add(h->anyrow(), h->cap);   // the rounds' per-row open minima (keys)
+  return z;
+}
+
+// prepped: the counters were zeroed — and for a removal WT tombstoned — by the
+// update's first launch (update_prep, one GPU)
 template <typename T>
 apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, const T* c2,
-                      const T* r2, bool removal, apsp_update_info* info) {
+                      const T* r2, bool removal, apsp_update_info* info, bool prepped = false) {
   const int64_t n = h->n;
   Rows r = h->active();
   const int64_t lcap = h->plan.lcap, ocap = h->plan.ocap;
-  {   // every per-update counter in one launch: per-row counts, the counters,
-      // the open-list cursors, the first four rounds' frontier counts, the flag
-    ZeroSet z{};
-    z.add(h->rowcnt(), h->cap);
-    z.add(reinterpret_cast<int*>(h->ctr()), (int64_t)(sizeof(DetectCounters) / sizeof(int)));
-    z.add(h->ocnt(), h->cap);
-    for (int q = 0; q < 4; ++q) z.add(h->chg(q), h->cap + 1);
-    z.add(h->anyflag(), 1);
-    z.add(h->anyrow(), h->cap);   // the rounds' per-row open minima (keys)
-    CK(zero_set(z, h->st));
-  }
+  if (!prepped) CK(zero_set(recompute_zero_set(h), h->st));
   // ---- sparse recompute (a6), enqueued without a host round trip: the pair
   // counts stay on the device, and the kernels do nothing if a list
   // overflowed.  Every value they write is a walk length of G' (>= the new
@@ -668,22 +682,26 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
        detect_fix_p8(reinterpret_cast<int32_t*>(h->Dl<T>()), h->ld, r, n, skip,
                      reinterpret_cast<const int32_t*>(c1), reinterpret_cast<const int32_t*>(r1), h->slid(),
                      reinterpret_cast<const int32_t*>(h->slw<T>()), h->mirror<T>(), h->rowcnt(), h->srow(),
-                     h->scol(), lcap, h->ctr(), 0, h->st));
+                     h->scol(), h->prow(), h->pcol(), lcap, h->ctr(), 0, h->st));
     PK(APSP_K_EMIT, 0.0, detect_lists(r, h->rowcnt(), h->rowoff(), h->ctr(), h->st));
-    if (removal) CK(tombstone<T>(h->Dl<T>(), h->ld, r, n, skip, h->WT<T>(), h->ld, h->st));
+    if (removal && !prepped) CK(tombstone<T>(h->Dl<T>(), h->ld, r, n, skip, h->WT<T>(), h->ld, h->st));
+    // the pairs it did not certify: their bounds into D, onto the open lists
     PK(APSP_K_SPARSE0, 0.0,
-       sparse_phase_a<T>(h->Dl<T>(), h->ld, r, h->slid(), h->slw<T>(), h->rowoff(), h->srow(), h->scol(),
-                         lcap, c1, r1, c2, r2, h->tau, h->ocnt(), h->ocol(), h->gprow(), h->gpcol(),
-                         h->glb<T>(), h->gfull(), ocap, h->ctr(), h->sr, h->mirror<T>(), h->st, 2));
+       defer_apply(reinterpret_cast<int32_t*>(h->Dl<T>()), h->ld, h->row0, h->srow(), h->scol(), h->prow(),
+                   h->pcol(), lcap, h->ocnt(), h->ocol(), h->rowoff(), h->gprow(), h->gpcol(),
+                   reinterpret_cast<int32_t*>(h->glb<T>()), h->gfull(), ocap, h->ctr(), h->mirror<T>(), h->st));
   } else {
     // one streaming pass appends the need_update_list; then the per-row slices
     // of the open lists and Phi / max|A_i|
     PK(APSP_K_DETECT, h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n,
        detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, 1, nullptr, h->rowcnt(),
                  h->srow(), h->scol(), nullptr, lcap, h->ctr(), h->WT<T>(), h->ld, h->sr,
-                 h->mirror<T>(), h->st));
+                 h->mirror<T>(), h->st, h->tmap8_ptr()));
     PK(APSP_K_EMIT, 0.0, detect_lists(r, h->rowcnt(), h->rowoff(), h->ctr(), h->st));
-    if (removal) CK(tombstone<T>(h->Dl<T>(), h->ld, r, n, skip, h->WT<T>(), h->ld, h->st));
+    // (prepped: WT was tombstoned by update_prep; D's row and column of the
+    // removed node are only read again by the dense path, which tombstones
+    // them itself, or overwritten by the swap-with-last)
+    if (removal && !prepped) CK(tombstone<T>(h->Dl<T>(), h->ld, r, n, skip, h->WT<T>(), h->ld, h->st));
   }
   // Rounds are frontier-based Bellman-Ford over each row's open entries: round
   // r relaxes every open pair of a row through the entries of that row that
@@ -746,15 +764,15 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     if (s2 != APSP_OK) return s2;
   }
   // ---- the one host read of this update: counters (summed over ranks) ----
-  long long* v = reinterpret_cast<long long*>(h->small());
-  CK(pack_counters(h->ctr(), last_total, v, h->st));   // total rows ovf1 ovf2 changed | maxrow
-  if (h->world > 1) {
-    NK(h->comm->allreduce(v, 5, ncclInt64, ncclSum, h->st));
-    NK(h->comm->allreduce(v + 5, 1, ncclInt64, ncclMax, h->st));
-  }
   long long* hv = reinterpret_cast<long long*>(h->host_small);
   unsigned* hmf = reinterpret_cast<unsigned*>(h->host_small) + 12;
-  {
+  if (h->world == 1) {   // packed straight into mapped host memory
+    CK(pack_to_host(h->ctr(), last_total, h->mirror_flag(), h->host_small_dev, h->st));
+  } else {
+    long long* v = reinterpret_cast<long long*>(h->small());
+    CK(pack_counters(h->ctr(), last_total, v, h->st));   // total rows ovf1 ovf2 changed | maxrow
+    NK(h->comm->allreduce(v, 5, ncclInt64, ncclSum, h->st));
+    NK(h->comm->allreduce(v + 5, 1, ncclInt64, ncclMax, h->st));
     ReadSet rs{};
     rs.add(v, 6 * sizeof(long long));
     rs.add(h->mirror_flag(), sizeof(unsigned));
@@ -793,6 +811,8 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   if (!dense && changed) dense = true;   // not converged: every entry is still a valid upper bound
   if (dense) {
     if (info) info->path = 3;
+    if (removal && prepped)   // FW needs the removed node's row and column of D at INF
+      CK(tombstone<T>(h->Dl<T>(), h->ld, r, n, skip, h->WT<T>(), h->ld, h->st));
     if (hv[2] != 0)   // the need_update_list missed pairs: reset every flagged entry in place
       PK(APSP_K_DETECT, 4.0 * (double)(r.hi - r.lo) * (double)n,
          detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, 2, nullptr, nullptr, nullptr,
@@ -965,10 +985,17 @@ apsp_status remove_node_impl(apsp_handle* h, int64_t k, int64_t* moved_from, aps
   Rows r = h->active();
   T* c1 = h->vec<T>(4);
   T* r1 = h->vec<T>(5);
-  apsp_status s = snap_pivots<T>(h, k, T(0), c1, k, r1);   // t1 = SPD(i, k), t2 = SPD(k, j)
-  if (s != APSP_OK) return s;
+  apsp_status s;
+  const bool prep = h->world == 1;
+  if (prep) {   // counters, snapshots t1 = SPD(i, k), t2 = SPD(k, j), WT tombstone: one launch
+    CK(update_prep<T>(h->Dl<T>(), ld, r, k, T(0), c1, h->Drow<T>(k), n, ld, r1, recompute_zero_set(h), h->WT<T>(),
+                      ld, k, h->sr, h->st));
+  } else {
+    s = snap_pivots<T>(h, k, T(0), c1, k, r1);   // t1 = SPD(i, k), t2 = SPD(k, j)
+    if (s != APSP_OK) return s;
+  }
   if (info) info->kind = 4;
-  s = recompute<T>(h, k, c1, r1, nullptr, nullptr, true, info);
+  s = recompute<T>(h, k, c1, r1, nullptr, nullptr, true, info, prep);
   if (s != APSP_OK) return s;
 
   // swap-with-last: node n-1 moves into slot k (Q7)
@@ -1064,8 +1091,15 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
     CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
     return APSP_OK;
   }
-  apsp_status s = snap_pivots<T>(h, u, w_old, c1, v, r1);   // D[i][u] + w_old, D[v][j]
-  if (s != APSP_OK) return s;
+  apsp_status s;
+  const bool prep = h->world == 1;
+  if (prep) {   // counters and the snapshots D[i][u] + w_old, D[v][j]: one launch
+    CK(update_prep<T>(h->Dl<T>(), ld, r, u, w_old, c1, h->Drow<T>(v), n, ld, r1, recompute_zero_set(h), WT, ld,
+                      -1, h->sr, h->st));
+  } else {
+    s = snap_pivots<T>(h, u, w_old, c1, v, r1);   // D[i][u] + w_old, D[v][j]
+    if (s != APSP_OK) return s;
+  }
   if (und) {
     s = snap_pivots<T>(h, v, w_old, c2, u, r2);
     if (s != APSP_OK) return s;
@@ -1077,7 +1111,7 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
     apsp_status ms = ensure_mirror<T>(h);
     if (ms != APSP_OK) return ms;
   }
-  return recompute<T>(h, -1, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, false, info);
+  return recompute<T>(h, -1, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, false, info, prep);
 }
 
 // ------------------------------------------------------------------ f1: paper-faithful modify
@@ -1094,7 +1128,7 @@ apsp_status removal_phi(apsp_handle* h, int64_t k, int64_t* phi) {
   if (s != APSP_OK) return s;
   PK(APSP_K_DETECT, h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n,
      detect<T>(h->Dl<T>(), ld, r, n, k, c1, r1, nullptr, nullptr, h->tau, 0, h->anyrow(), nullptr,
-               nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0, h->sr, h->mirror<T>(), h->st));
+               nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0, h->sr, h->mirror<T>(), h->st, h->tmap8_ptr()));
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(h->small() + 128);
   CKR(cudaMemsetAsync(cnt, 0, sizeof *cnt, h->st));
   CK(count_nonzero(h->anyrow() + r.lo, r.hi - r.lo, cnt, h->st));
@@ -1246,9 +1280,29 @@ apsp_status query_one(apsp_handle* h, int64_t s, int64_t t, void* dist, int32_t*
   const int len = hv[2], nc = hv[3];
   std::memcpy(dist, &hv[4], sizeof(T));
   if (n_candidates) *n_candidates = nc;
+  if (len < 0 && nc > std::min(h->plan.qcap, cap_dev) && h->world == 1 && h->sr == 0) {
+    // more candidates than the batch scratch holds: every candidate's
+    // predecessor at once, then the walk (query.cu: query_big)
+    int* out = reinterpret_cast<int*>(h->ws + h->plan.off_qbout);
+    CK(query_big<T>(h->Dl<T>(), h->ld, h->WT<T>(), h->ld, h->n, (int)s, (int)t,
+                    reinterpret_cast<unsigned*>(h->ws + h->plan.off_qbits),
+                    reinterpret_cast<int*>(h->ws + h->plan.off_qbpred), out + 2, out + 3, (int)h->cap, h->tau,
+                    h->wmin<T>(), h->st));
+    CKR(cudaMemcpyAsync(hv, out + 3, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    CKR(cudaStreamSynchronize(h->st));
+    const int blen = hv[0];
+    if (blen > 0) {
+      if (path_len) *path_len = blen;
+      if (blen > path_cap)
+        return fail(h, APSP_E_RANGE, "sp_pair_query: path_cap %d < path length %d", path_cap, blen);
+      CKR(cudaMemcpyAsync(path, out + 4, sizeof(int) * blen, cudaMemcpyDeviceToHost, h->st));
+      CKR(cudaStreamSynchronize(h->st));
+      return APSP_OK;
+    }
+  }
   if (len < 0) {
     if (path_len) *path_len = 0;
-    return fail(h, APSP_E_RANGE, "sp_pair_query: %d candidates exceed the kernel capacity %d", nc,
+    return fail(h, APSP_E_RANGE, "sp_pair_query: no path from the %d candidates (capacity %d)", nc,
                 std::min(h->plan.qcap, cap_dev));
   }
   if (path_len) *path_len = len;
@@ -1300,12 +1354,12 @@ apsp_status need_list_impl(apsp_handle* h, int kind, int64_t a, int64_t b, int32
        detect_fix_p8(reinterpret_cast<int32_t*>(h->Dl<T>()), h->ld, r, n, skip,
                      reinterpret_cast<const int32_t*>(c1), reinterpret_cast<const int32_t*>(r1), h->slid(),
                      reinterpret_cast<const int32_t*>(h->slw<T>()), h->mirror<T>(), h->rowcnt(), h->srow(),
-                     h->scol(), h->plan.lcap, h->ctr(), 1, h->st));
+                     h->scol(), h->prow(), h->pcol(), h->plan.lcap, h->ctr(), 1, h->st));
   } else {
     PK(APSP_K_DETECT, h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n,
        detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, h->tau, 1,
                  nullptr, h->rowcnt(), h->srow(), h->scol(), nullptr, h->plan.lcap, h->ctr(), h->WT<T>(), h->ld,
-                 h->sr, h->mirror<T>(), h->st));
+                 h->sr, h->mirror<T>(), h->st, h->tmap8_ptr()));
   }
   unsigned long long tot = 0;
   CKR(cudaMemcpyAsync(h->host_small, &h->ctr()->total, sizeof tot, cudaMemcpyDeviceToHost, h->st));
@@ -1453,6 +1507,11 @@ apsp_status create_impl(apsp_handle** out, apsp_dtype dtype, int directed, int64
     CK(transpose_in<T>(reinterpret_cast<const T*>(W), ldw, n, h->WT<T>(), h->ld, &h->ctr()->err,
                        h->wmin_dev(), h->st));
     CK(shortlist_build<T>(h->WT<T>(), h->ld, n, nullptr, 0, n, h->slid(), h->slw<T>(), h->wnext<T>(), h->st));
+    if (std::is_same<T, int32_t>::value && h->rows > 0) {   // the int8 detection's tensor map (fixed buffer)
+      const int64_t rows_max = world > 1 ? round_up(cdiv(cap, world), kTile) : cap;
+      CKR(detect8_tensor_map(h->tmap8, h->ws + h->plan.off_p8, h->ld, rows_max));
+      h->tmap8_ok = true;
+    }
     unsigned* herr = reinterpret_cast<unsigned*>(h->host_small);
     CKR(cudaMemcpyAsync(herr, &h->ctr()->err, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
     CKR(cudaMemcpyAsync(herr + 1, h->wmin_dev(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));

@@ -141,7 +141,12 @@ template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
                    const T* c2, const T* r2, float tau, int mode, int* anyrow, int* rowcnt,
                    int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr, const T* WT,
-                   int64_t ldw, int sr, Mirror M, cudaStream_t st);
+                   int64_t ldw, int sr, Mirror M, cudaStream_t st,
+                   const void* tmap8 = nullptr /* host CUtensorMap of the int8 mirror (detect8_tensor_map) */);
+// The 2-D tensor map the int8 detection's TMA copies use: the int8 mirror m8
+// as a uint32 tensor of `rows` x ld / 4 words (row stride ld bytes), boxes of
+// 256 words x the kernel's rows per stage.  out: 128-byte CUtensorMap.
+cudaError_t detect8_tensor_map(void* out, const uint8_t* m8, int64_t ld, int64_t rows);
 cudaError_t detect_lists(Rows r, const int* rowcnt, int64_t* rowoff, DetectCounters* ctr,
                          cudaStream_t st);
 // D[i][j] := W'[i][j] on every listed pair (the dense path without the sparse kernels)
@@ -241,6 +246,12 @@ struct QueryScratch {
   int* cnt;             // |C| per slot
   int qcap, batch;
 };
+// One query with a candidate set beyond the batch scratch (one GPU, shortest
+// path): bits (n bits), pred (n ints), cnt (1 int) scratch; out[0] = path
+// length (-2: not found), path (<= cap ids) in out + 1.
+template <typename T>
+cudaError_t query_big(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int s, int t, unsigned* bits,
+                      int* pred, int* cnt, int* out, int cap, float tau, T wmin, cudaStream_t st);
 template <typename T>
 cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int q,
                         const int* s, const int* t, T* dist, int* paths, int path_cap,
@@ -297,6 +308,15 @@ struct ZeroSet {
   bool overflow;
 };
 cudaError_t zero_set(const ZeroSet& z, cudaStream_t st);
+// zero z, the pivot snapshots cout[i] = sat(D[i][col] + add) (local rows) and
+// rout = rsrc (if non-null), and tombstone node `tomb` (>= 0) in WT: one launch
+template <typename T>
+cudaError_t update_prep(const T* D, int64_t ld, Rows r, int64_t col, T add, T* cout, const T* rsrc, int64_t n,
+                        int64_t npad, T* rout, const ZeroSet& z, T* WT, int64_t ldw, int64_t tomb, int sr,
+                        cudaStream_t st);
+// the counters pack_counters packs, plus the mirror flag, into mapped host memory
+cudaError_t pack_to_host(const DetectCounters* c, const int* any, const unsigned* mflag, void* host_dev,
+                         cudaStream_t st);
 double microbench(int kind, void* buf, size_t bytes, cudaStream_t st);   // microbench.cu
 int num_sms();
 // ---------------- fused.cu ----------------
@@ -304,11 +324,18 @@ int num_sms();
 // edge increase: c1 = D[:, u] (+ w), r1 = D[v, :]); rows are staged whole in
 // shared memory: fused_stages(n) > 0 iff a row of n bytes fits.
 int fused_stages(int64_t n);
-// Outputs: rowcnt[i] = |A_i|, ctr->total = |A|, and on (srow, scol) with
-// count ctr->spill the pairs it did not certify (all of them if export_only).
+// Outputs: rowcnt[i] = |A_i|, ctr->total = |A|, and on (srow, scol, sacc, slb)
+// with count ctr->spill the pairs it did not certify with their bound and
+// D_old (all pairs, no bounds, if export_only).  defer_apply then writes
+// those bounds and appends the pairs to the open lists (rowoff from
+// detect_lists).
 cudaError_t detect_fix_p8(int32_t* D, int64_t ld, Rows r, int64_t n, int64_t skip, const int32_t* c1,
                           const int32_t* r1, const int* SLid, const int32_t* SLw, Mirror M, int* rowcnt,
-                          int* srow, int* scol, int64_t lcap, DetectCounters* ctr, int export_only,
-                          cudaStream_t st);
+                          int* srow, int* scol, int* sacc, int* slb, int64_t lcap, DetectCounters* ctr,
+                          int export_only, cudaStream_t st);
+cudaError_t defer_apply(int32_t* D, int64_t ld, int64_t row0, const int* srow, const int* scol, const int* sacc,
+                        const int* slb, int64_t lcap, int* ocnt, int* ocol, const int64_t* rowoff, int* gprow,
+                        int* gpcol, int32_t* glb, unsigned char* gfull, int64_t ocap, DetectCounters* ctr, Mirror M,
+                        cudaStream_t st);
 
 }  // namespace apsp

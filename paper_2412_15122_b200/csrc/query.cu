@@ -395,7 +395,109 @@ cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_
   return cudaSuccess;
 }
 
+// ---------------------------------------------------------------------------
+// Queries whose candidate set exceeds the per-query scratch (|C| > qcap, e.g.
+// the directed unit cycle, where C is the whole arc and the path has n
+// nodes): the same predecessor tree as the walk above, computed for every
+// candidate at once instead of hop by hop.
+//   k_qbig_bits: C as a bitmap (the scan's test, no capacity);
+//   k_qbig_pred: for each k in C (one warp), pred[k] = the first m in
+//     (D[s][m], id) order with m in C, key(m) < key(k) and D[s][m] + W[m][k]
+//     == D[s][k] (fp32: the tolerant test of Q4) — row k of WT and row s of D
+//     are read contiguously;
+//   k_qbig_walk: t, pred[t], ... until s (one thread), the path written
+//     forward.  Positive weights make the keys strictly decrease, so the walk
+//     ends at s within |C| hops (R3); a zero-weight tie can leave a node
+//     without a predecessor, and the walk then reports failure (-2).
+// Shortest-path algebra only (minimax: -2 as before).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_qbig_bits(const T* __restrict__ D, int64_t ld, int64_t n, int s, int t, unsigned* bits,
+                            int* cnt, float tau, T wmin) {
+  const T* Ds = D + (int64_t)s * ld;
+  const T st = Ds[t];
+  T lim;
+  if (Tr<T>::kFloat) lim = st * (1.0f + tau);
+  else lim = st - wmin;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < (n + 31) / 32;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    unsigned m = 0;
+    for (int e = 0; e < 32; ++e) {
+      const int64_t k = 32 * w + e;
+      if (k >= n) break;
+      const T dsk = Ds[k];
+      if (!Tr<T>::fin(dsk) || !(dsk <= lim || k == t)) continue;
+      const T dkt = D[k * ld + t];
+      if (Tr<T>::fin(dkt) && Tr<T>::tight(Tr<T>::add(dsk, dkt), st, tau)) m |= 1u << e;
+    }
+    bits[w] = m;
+    if (m) atomicAdd(cnt, __popc(m));
+  }
+}
+template <typename T>
+__global__ void k_qbig_pred(const T* __restrict__ D, int64_t ld, const T* __restrict__ WT, int64_t ldw, int64_t n,
+                            int s, const unsigned* __restrict__ bits, int* pred, float tau) {
+  const int lane = threadIdx.x & 31;
+  const T* Ds = D + (int64_t)s * ld;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t k = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); k < n; k += nw) {
+    if (!((bits[k >> 5] >> (k & 31)) & 1u) || k == s) continue;   // warp-uniform
+    const T dk = Ds[k];
+    const unsigned long long kk = ((unsigned long long)Tr<T>::key(dk) << 32) | (unsigned)k;
+    const T* wrow = WT + k * ldw;   // W[m][k] = WT[k][m]
+    unsigned long long best = ~0ull;
+    for (int64_t m = lane; m < n; m += 32) {
+      if (!((bits[m >> 5] >> (m & 31)) & 1u)) continue;
+      const T dm = Ds[m];
+      const unsigned long long km = ((unsigned long long)Tr<T>::key(dm) << 32) | (unsigned)m;
+      if (km >= kk || km >= best) continue;
+      const T w = wrow[m];
+      if (!Tr<T>::fin(w)) continue;
+      const T via = Tr<T>::add(dm, w);
+      const bool eq = Tr<T>::kFloat ? Tr<T>::tight(via, dk, tau) : via == dk;
+      if (eq) best = km;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (lane == 0) pred[k] = best == ~0ull ? -1 : (int)(best & 0xFFFFFFFFull);
+  }
+}
+// out[0] = path length (or -2: no chain to s), path written forward into out + 1
+__global__ void k_qbig_walk(int s, int t, const int* __restrict__ pred, int64_t n, int* out, int cap) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int len = 1;
+  int cur = t;
+  while (cur != s && len <= n) {
+    cur = pred[cur];
+    if (cur < 0) { out[0] = -2; return; }
+    ++len;
+  }
+  if (cur != s) { out[0] = -2; return; }
+  out[0] = len;
+  if (len > cap) return;
+  cur = t;
+  for (int x = len - 1; x >= 0; --x) {
+    out[1 + x] = cur;
+    if (x) cur = pred[cur];
+  }
+}
+template <typename T>
+cudaError_t query_big(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int s, int t, unsigned* bits,
+                      int* pred, int* cnt, int* out, int cap, float tau, T wmin, cudaStream_t st) {
+  CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int), st));
+  const int wwords = (int)((n + 31) / 32);
+  k_qbig_bits<T><<<std::max(1, std::min((wwords + 255) / 256, num_sms() * 4)), 256, 0, st>>>(D, ld, n, s, t, bits,
+                                                                                            cnt, tau, wmin);
+  CUDA_TRY(cudaGetLastError());
+  k_qbig_pred<T><<<num_sms() * 8, 256, 0, st>>>(D, ld, WT, ldw, n, s, bits, pred, tau);
+  CUDA_TRY(cudaGetLastError());
+  k_qbig_walk<<<1, 32, 0, st>>>(s, t, pred, n, out, cap);
+  return cudaGetLastError();
+}
+
 #define INST(T)                                                                                  \
+  template cudaError_t query_big<T>(const T*, int64_t, const T*, int64_t, int64_t, int, int, unsigned*, int*, \
+                                    int*, int*, int, float, T, cudaStream_t);                    \
   template cudaError_t query_batch<T>(const T*, int64_t, const T*, int64_t, int64_t, int,       \
                                       const int*, const int*, T*, int*, int, int*, int*, float,  \
                                       int, cudaStream_t, const QueryScratch&, T, const T*, int64_t, \

@@ -749,11 +749,15 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_a(T* D, int64_t l
         }
         if (done) break;
       }
-      Drow[j] = acc;   // unconditionally: D_old is not an upper bound of D'
+      // D_old is not an upper bound of D': every listed entry gets acc — a
+      // write only where it differs (a certified pair, acc == lb, already
+      // holds it; mirrors included: A2 reads them; later writes — A2, B, the
+      // rounds — are mirrored as they happen)
+      if (acc != lb) {
+        Drow[j] = acc;
+        if (M.m || M.m8) mbits |= mput(M, (i - row0) * ld + j, acc);
+      }
       open = !Tr<T>::at_lb(acc, lb);
-      // every listed value goes to the mirror now (A2 reads it); later
-      // writes (A2, B, the rounds) are mirrored as they happen
-      if (M.m || M.m8) mbits |= mput(M, (i - row0) * ld + j, acc);
     }
     // open-pair lists: per-row slot by atomic, the global slot warp-aggregated
     const unsigned bal = __ballot_sync(0xffffffffu, open);
@@ -822,9 +826,18 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_aq(T* D, int64_t 
           busy = true;
           i = srow[mine];
           j = scol[mine];
-          lb = *(volatile T*)(D + (int64_t)(i - row0) * ld + j);   // D_old[i][j]
           ci = c1[i];
           cj = TWO ? c2[i] : Tr<T>::inf();
+          // D_old[i][j]: an integer listed pair is exactly tight, D_old = c1[i] +
+          // r1[j] (or the c2 + r2 term; D_old <= both), read from the pivot
+          // vectors (L2-resident) instead of a DRAM gather of D; fp32 pairs are
+          // listed with a tolerance, so D itself is read
+          if constexpr (!Tr<T>::kFloat) {
+            lb = Tr<T, SR>::add(ci, r1[j]);
+            if (TWO) lb = Tr<T>::mn(lb, Tr<T, SR>::add(cj, r2[j]));
+          } else {
+            lb = *(volatile T*)(D + (int64_t)(i - row0) * ld + j);
+          }
           acc = Tr<T>::inf();
           b = 0;
           h = 0;
@@ -882,9 +895,11 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_aq(T* D, int64_t 
       }
       bool open = false;
       if (fin) {
-        D[(int64_t)(i - row0) * ld + j] = acc;   // unconditionally: D_old is not an upper bound of D'
+        if (acc != lb) {   // D_old is not an upper bound of D' (a certified pair already holds acc)
+          D[(int64_t)(i - row0) * ld + j] = acc;
+          if (M.m || M.m8) mbits |= mput(M, (int64_t)(i - row0) * ld + j, acc);
+        }
         open = !Tr<T>::at_lb(acc, lb);
-        if (M.m || M.m8) mbits |= mput(M, (int64_t)(i - row0) * ld + j, acc);
         busy = false;
       }
       const unsigned bal = __ballot_sync(0xffffffffu, open);

@@ -226,6 +226,44 @@ __global__ void k_gather_col_row(const T* D, int64_t ld, Rows r, int64_t col, T 
     cout[i] = Tr<T, SR>::sat(Tr<T, SR>::add(D[(i - r.row0) * ld + col], add));
   for (int64_t j = tid; j < npad; j += stride) rout[j] = j < n ? rsrc[j] : Tr<T>::inf();
 }
+// The first launch of a removal / tight increase (one GPU): the update's
+// counters zeroed (z), the pivot snapshots (column col + add, row rsrc), and
+// for a removal the tombstone of node `tomb` in WT (W' has no edge into or
+// out of it; nothing before the recompute reads WT, and D's row / column of
+// the node are overwritten by the swap-with-last, or tombstoned by the dense
+// path) — independent writes, one grid-stride pass.
+template <typename T, int SR>
+__global__ void k_update_prep(const T* D, int64_t ld, Rows r, int64_t col, T add, T* cout, const T* rsrc,
+                              int64_t n, int64_t npad, T* rout, ZeroSet z, T* WT, int64_t ldw, int64_t tomb) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int b = 0; b < z.k; ++b)
+    for (int64_t e = tid; e < z.n[b]; e += stride) z.p[b][e] = 0;
+  for (int64_t i = r.lo + tid; i < r.hi; i += stride)
+    cout[i] = Tr<T, SR>::sat(Tr<T, SR>::add(D[(i - r.row0) * ld + col], add));
+  if (rsrc)
+    for (int64_t j = tid; j < npad; j += stride) rout[j] = j < n ? rsrc[j] : Tr<T>::inf();
+  if (tomb >= 0)
+    for (int64_t j = tid; j < n; j += stride) {
+      WT[tomb * ldw + j] = (j == tomb) ? T(0) : Tr<T>::inf();
+      if (j != tomb) WT[j * ldw + tomb] = Tr<T>::inf();
+    }
+}
+template <typename T>
+cudaError_t update_prep(const T* D, int64_t ld, Rows r, int64_t col, T add, T* cout, const T* rsrc, int64_t n,
+                        int64_t npad, T* rout, const ZeroSet& z, T* WT, int64_t ldw, int64_t tomb, int sr,
+                        cudaStream_t st) {
+  if (z.overflow) return cudaErrorInvalidValue;
+  int64_t most = std::max<int64_t>(std::max<int64_t>(r.hi - r.lo, npad), 1);
+  for (int b = 0; b < z.k; ++b) most = std::max(most, z.n[b]);
+  const int grid = (int)std::min<int64_t>(cdiv(most, 256), 4 * num_sms());
+  if (sr)
+    k_update_prep<T, 1><<<grid, 256, 0, st>>>(D, ld, r, col, add, cout, rsrc, n, npad, rout, z, WT, ldw, tomb);
+  else
+    k_update_prep<T, 0><<<grid, 256, 0, st>>>(D, ld, r, col, add, cout, rsrc, n, npad, rout, z, WT, ldw, tomb);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t gather_col_row(const T* D, int64_t ld, Rows r, int64_t col, T add, T* cout, const T* rsrc,
                            int64_t n, int64_t npad, T* rout, int sr, cudaStream_t st) {
@@ -1871,7 +1909,7 @@ __device__ __forceinline__ void detect_flush_q(const DetectQueueT<WT>& Q, int cn
   __syncwarp();
   // lane e takes queue entries e, e+32, ...: count its pairs, scan, one atomic
   int mine = 0;
-  for (int e = lane; e < cnt; e += 32) mine += __popc((unsigned)Q.w[e]);
+  for (int e = lane; e < cnt; e += 32) mine += __popcll((unsigned long long)Q.w[e]);
   int incl = mine;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
@@ -1887,12 +1925,12 @@ __device__ __forceinline__ void detect_flush_q(const DetectQueueT<WT>& Q, int cn
   base = __shfl_sync(0xffffffffu, base, 0);
   int64_t pos = (int64_t)base + incl - mine;
   for (int e = lane; e < cnt; e += 32) {
-    unsigned w = Q.w[e];
+    unsigned long long w = Q.w[e];
     const unsigned rl = Q.rl[e];
     const int64_t i = i_lo + (rl >> 5);
     const int ln = (int)(rl & 31u);
     while (w) {
-      const int bit = __ffs(w) - 1;
+      const int bit = __ffsll(w) - 1;
       w &= w - 1;
       const int64_t j = col_of(bit, ln);
       if (pos < o.lcap) {
@@ -2223,14 +2261,20 @@ __global__ void k_detect_rows(Rows r, const int* __restrict__ rowcnt, int64_t* r
 #ifndef D8_MINB
 #define D8_MINB 3
 #endif
-constexpr int kD8R = D8_R, kD8S = D8_S;   // ring: rows per stage, stages (6 KB per warp; 3 CTAs per SM)
+// A warp owns a 1024-column chunk of a row slab; lane l the 16-byte groups at
+// 16 l and 512 + 16 l.  Rows arrive through a per-warp TMA ring: one 2-D
+// tensor copy (the mirror as a uint32 tensor of local rows x ld / 4 words, box
+// 256 words x kD8R rows) fills a stage — kD8R KB per copy (one 1 KB bulk copy
+// per row was bound by the TMA engine's per-copy cost: 4.7 TB/s, against
+// 7.0 TB/s for 2 KB copies, scripts/tma_probe.cu).
+constexpr int kD8R = D8_R, kD8S = D8_S;   // ring: rows per stage, stages
 using D8Ring = WarpRing<kD8S, kD8R, 1024>;
 constexpr int kD8Smem = 8 * D8Ring::kBytes;
 template <typename T, bool TWO, int MODE>
 __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, int64_t n, int64_t skip, Tiling tl,
                                                       const T* __restrict__ c1, const T* __restrict__ r1,
                                                       const T* __restrict__ c2, const T* __restrict__ r2,
-                                                      DetectOut<T> o) {
+                                                      DetectOut<T> o, const __grid_constant__ CUtensorMap tm) {
   if (!detect_uses_mirror<T, 0, MODE>(o.M) || o.M.m8 == nullptr) return;
   __shared__ DetectQueueT<unsigned> sq[MODE == 1 ? 8 : 1];
   const int lane = threadIdx.x & 31;
@@ -2249,7 +2293,7 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
     return (int64_t)chunk * 1024 + 16 * ln + (bit >> 4) * 512 + (bit & 15);
   };
   auto s8 = [](T v) -> uint32_t { return (uint32_t)min((int32_t)v, kSat8i); };
-  uint32_t rw[8], rwm[8], rw2[TWO ? 8 : 1], rwm2[TWO ? 8 : 1];
+  uint32_t rw[8], rw2[TWO ? 8 : 1];
   unsigned vmask = 0;   // bit b <-> column col_of(b, lane): j < n and j != skip
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
@@ -2263,23 +2307,16 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
       if (j < n && j != skip) vmask |= 1u << bit;
     }
     rw[q] = a;
-    rwm[q] = a - 0x01010101u;
-    if (TWO) { rw2[q] = b; rwm2[q] = b - 0x01010101u; }
+    if (TWO) rw2[q] = b;
   }
-  // the rows stream through a per-warp shared-memory ring filled by bulk
-  // copies (TMA, tma.cuh): lane 0 copies the chunk's 1024 contiguous mirror
-  // bytes of each row (fewer on the row's ragged end; the bytes past n are
-  // masked out) and kD8S - 1 stages of kD8R rows stay in flight while the warp
-  // computes.  Lane l then reads bytes [16 l, 16 l + 16) and [512 + 16 l, ...).
   extern __shared__ __align__(128) uint8_t dring_raw[];
   D8Ring ring;
   ring.init(dring_raw + (threadIdx.x >> 5) * D8Ring::kBytes, lane);
-  const uint8_t* mb = o.M.m8 + (i_lo - r.row0) * ld + (int64_t)chunk * 1024;
-  const unsigned cbytes = (unsigned)((min((int64_t)1024, n - (int64_t)chunk * 1024) + 15) & ~15);
+  // tensor coordinates: (word column, local row)
+  const int cw0 = chunk * 256, rl0 = (int)(i_lo - r.row0);
   const int nst = (rows + kD8R - 1) / kD8R;
   auto issue = [&](int st) {
-    if (st < nst)
-      ring.issue(st, cbytes, lane, [&](int h) { return mb + (int64_t)min(st * kD8R + h, rows - 1) * ld; });
+    if (st < nst) ring.issue_box(st, &tm, cw0, rl0 + st * kD8R, lane);
   };
 #pragma unroll
   for (int st = 0; st < kD8S - 1; ++st) issue(st);
@@ -2297,67 +2334,70 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
         cl = (inr && il != skip) ? s8(c1[il]) * 0x01010101u : 0x7F7F7F7Fu;
         if (TWO) cl2 = (inr && il != skip) ? s8(c2[il]) * 0x01010101u : 0x7F7F7F7Fu;
       }
-      {
-        const uint32_t cw = __shfl_sync(0xffffffffu, cl, rr & 31);
-        const uint32_t cw2 = TWO ? __shfl_sync(0xffffffffu, cl2, rr & 31) : 0u;
-        const uint4 w0 = reinterpret_cast<const uint4*>(ring.row(st, h))[lane];
-        const uint4 w1 = reinterpret_cast<const uint4*>(ring.row(st, h))[32 + lane];
-        const uint32_t d[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-        uint32_t acc = 0;
+      const uint32_t cw = __shfl_sync(0xffffffffu, cl, rr & 31);
+      const uint32_t cw2 = TWO ? __shfl_sync(0xffffffffu, cl2, rr & 31) : 0u;
+      const uint4* rp = reinterpret_cast<const uint4*>(ring.row(st, h));
+      const uint4 w0 = rp[lane], w1 = rp[32 + lane];
+      const uint32_t d[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+      // every byte <= 0x7F and D <= c + r: no carries or borrows between
+      // bytes; the entry is tight iff its byte of u = c + r - d is 0 (the
+      // classic exact zero-byte test: (u - 0x01010101) & ~u)
+      uint32_t acc = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t u = cw + rw[q] - d[q];
+        acc |= (u - 0x01010101u) & ~u;
+        if (TWO) {
+          const uint32_t u2 = cw2 + rw2[q] - d[q];
+          acc |= (u2 - 0x01010101u) & ~u2;
+        }
+      }
+      if (!__any_sync(0xffffffffu, (acc & 0x80808080u) != 0u)) continue;
+      // some lane has a tight entry in this row: exact per-byte flags of the
+      // words that have a zero byte (the test above is exact per word)
+      const int64_t i = i_lo + rr;
+      unsigned word = 0;
+      if (acc & 0x80808080u) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          acc |= (cw + rwm[q] - d[q]) & ~(cw + rw[q] - d[q]);
-          if (TWO) acc |= (cw2 + rwm2[q] - d[q]) & ~(cw2 + rw2[q] - d[q]);
-        }
-        if (!__any_sync(0xffffffffu, (acc & 0x80808080u) != 0u)) continue;
-        // some lane has a tight entry in this row: exact per-byte flags of the
-        // words that have a zero byte (the test above is exact per word)
-        const int64_t i = i_lo + rr;
-        unsigned word = 0;
-        if (acc & 0x80808080u) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            // the exact per-word test again; only a word that has a zero byte
-            // (about one per flagged row in a 1024-column chunk) is decoded
-            const uint32_t u = cw + rw[q] - d[q];
-            uint32_t t = (cw + rwm[q] - d[q]) & ~u;
-            const uint32_t u2 = TWO ? cw2 + rw2[q] - d[q] : 0u;
-            if (TWO) t |= (cw2 + rwm2[q] - d[q]) & ~u2;
-            if (t & 0x80808080u) {
-              uint32_t z = ~(u | ((u & 0x7F7F7F7Fu) + 0x7F7F7F7Fu)) & 0x80808080u;   // exact zero bytes
-              if (TWO) z |= ~(u2 | ((u2 & 0x7F7F7F7Fu) + 0x7F7F7F7Fu)) & 0x80808080u;
-              // minus the INF entries (d == 0x7F with c INF and r == 0 tests
-              // tight; INF pairs are never listed, Q5)
-              const uint32_t dq = d[q] ^ 0x7F7F7F7Fu;
-              z &= dq | ((dq & 0x7F7F7F7Fu) + 0x7F7F7F7Fu);
-              // bytes 0..3 -> bits 4q' .. 4q'+3 of this lane's 16-column half
-              const uint32_t nib = ((((z >> 7) & 0x01010101u) * 0x01020408u) >> 24) & 0xFu;
-              word |= nib << ((q >> 2) * 16 + (q & 3) * 4);
-            }
+          const uint32_t u = cw + rw[q] - d[q];
+          uint32_t t = (u - 0x01010101u) & ~u;
+          const uint32_t u2 = TWO ? cw2 + rw2[q] - d[q] : 0u;
+          if (TWO) t |= (u2 - 0x01010101u) & ~u2;
+          if (t & 0x80808080u) {
+            uint32_t z = ~(u | ((u & 0x7F7F7F7Fu) + 0x7F7F7F7Fu)) & 0x80808080u;   // exact zero bytes
+            if (TWO) z |= ~(u2 | ((u2 & 0x7F7F7F7Fu) + 0x7F7F7F7Fu)) & 0x80808080u;
+            // minus the INF entries (d == 0x7F with c INF and r == 0 tests
+            // tight; INF pairs are never listed, Q5)
+            const uint32_t dq = d[q] ^ 0x7F7F7F7Fu;
+            z &= dq | ((dq & 0x7F7F7F7Fu) + 0x7F7F7F7Fu);
+            // bytes 0..3 -> bits 4q' .. 4q'+3 of this lane's 16-column half
+            const uint32_t nib = ((((z >> 7) & 0x01010101u) * 0x01020408u) >> 24) & 0xFu;
+            word |= nib << ((q >> 2) * 16 + (q & 3) * 4);
           }
-          word &= vmask;
-          const int64_t di = i - g0;   // the diagonal j == i
-          if (di >= 0 && di < 16) word &= ~(1u << di);
-          else if (di >= 512 && di < 528) word &= ~(1u << (di - 512 + 16));
         }
-        if (!__any_sync(0xffffffffu, word != 0)) continue;
-        if (MODE == 0) {
-          if (lane == 0) o.anyrow[i] = 1;
-        } else {
-          const int tot = __reduce_add_sync(0xffffffffu, (unsigned)__popc(word));
-          if (lane == 0) atomicAdd(o.rowcnt + i, tot);
-          if (qcnt + 32 > DS_Q) {
-            detect_flush_q<T>(Q, qcnt, i_lo, o, lane, col_of);
-            qcnt = 0;
-          }
-          const unsigned bal = __ballot_sync(0xffffffffu, word != 0);
-          if (word) {
-            const int qp = qcnt + __popc(bal & ((1u << lane) - 1));
-            Q.rl[qp] = (unsigned)(i - i_lo) << 5 | (unsigned)lane;
-            Q.w[qp] = word;
-          }
-          qcnt += __popc(bal);
+        word &= vmask;
+        const int64_t di = i - g0;   // the diagonal j == i
+        if (di >= 0 && di < 16) word &= ~(1u << di);
+        else if (di >= 512 && di < 528) word &= ~(1u << (di - 512 + 16));
+      }
+      if (!__any_sync(0xffffffffu, word != 0)) continue;
+      if (MODE == 0) {
+        if (lane == 0) o.anyrow[i] = 1;
+      } else {
+        const int tot = __reduce_add_sync(0xffffffffu, (unsigned)__popc(word));
+        if (lane == 0) atomicAdd(o.rowcnt + i, tot);
+        if (qcnt + 32 > DS_Q) {
+          detect_flush_q<T>(Q, qcnt, i_lo, o, lane, col_of);
+          qcnt = 0;
         }
+        const unsigned bal = __ballot_sync(0xffffffffu, word != 0);
+        if (word) {
+          const int qp = qcnt + __popc(bal & ((1u << lane) - 1));
+          Q.rl[qp] = (unsigned)(i - i_lo) << 5 | (unsigned)lane;
+          Q.w[qp] = word;
+        }
+        qcnt += __popc(bal);
       }
     }
   }
@@ -2368,9 +2408,9 @@ template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
                    const T* c2, const T* r2, float tau, int mode, int* anyrow, int* rowcnt,
                    int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr, const T* WT,
-                   int64_t ldw, int sr, Mirror M, cudaStream_t st) {
+                   int64_t ldw, int sr, Mirror M, cudaStream_t st, const void* tmap8) {
   if (r.hi <= r.lo) return cudaSuccess;
-  static const int wps = tune_wps("APSP_TUNE_DET_WPS", 192), wps8 = tune_wps("APSP_TUNE_DET8_WPS", 128);
+  static const int wps = tune_wps("APSP_TUNE_DET_WPS", 192), wps8 = tune_wps("APSP_TUNE_DET8_WPS", 8 * D8_MINB);
   Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20, DS_VEC, wps);   // (measured best)
   if (tl.slab >= (1 << 26)) return cudaErrorInvalidValue;   // MODE-1 queue packing
   if (mode == 0) CUDA_TRY(cudaMemsetAsync(anyrow + r.lo, 0, sizeof(int) * (size_t)(r.hi - r.lo), st));
@@ -2390,7 +2430,9 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
       static const cudaError_t attr =                                                            \
           cudaFuncSetAttribute(kp8, cudaFuncAttributeMaxDynamicSharedMemorySize, kD8Smem);        \
       CUDA_TRY(attr);                                                                            \
-      kp8<<<g8, 256, kD8Smem, st>>>(r, ld, n, skip, tl8, c1, r1, c2, r2, o);                     \
+      if (!tmap8) return cudaErrorInvalidValue;                                                  \
+      kp8<<<g8, 256, kD8Smem, st>>>(r, ld, n, skip, tl8, c1, r1, c2, r2, o,                      \
+                                   *reinterpret_cast<const CUtensorMap*>(tmap8));                \
     }                                                                                            \
     else if (SR == 0 && MODE != 2 && M.m)                                                        \
       k_detect_p16<T, TWO, (MODE == 2 ? 0 : MODE)><<<g, 256, 0, st>>>(D, ld, r, n, skip, tl,   \
@@ -2414,6 +2456,30 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
 #undef BY_MODE
 #undef LAUNCH
   return cudaGetLastError();
+}
+
+cudaError_t detect8_tensor_map(void* out, const uint8_t* m8, int64_t ld, int64_t rows) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+    encode = reinterpret_cast<Encode>(fn);
+  }
+  if ((ld & 15) || ((uintptr_t)m8 & 15) || rows < 1) return cudaErrorInvalidValue;
+  const cuuint64_t dims[2] = {(cuuint64_t)(ld / 4), (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld};   // bytes between rows
+  const cuuint32_t box[2] = {256, (cuuint32_t)kD8R};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
+                            const_cast<uint8_t*>(m8), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 // D0[i][j] := W'[i][j] for every listed pair: only when the dense path runs
@@ -2623,6 +2689,24 @@ cudaError_t pack_counters(const DetectCounters* c, const int* any, long long* v,
   k_pack_counters<<<1, 1, 0, st>>>(c, any, v);
   return cudaGetLastError();
 }
+// one GPU: the same six words straight into mapped host memory, plus the
+// mirror flag after them (host[12] as unsigned) — the update's one host read
+__global__ void k_pack_to_host(const DetectCounters* c, const int* any, const unsigned* mflag,
+                               volatile long long* host) {
+  host[0] = (long long)c->total;
+  host[1] = (long long)c->rows;
+  host[2] = (c->overflow & 1u) ? 1 : 0;
+  host[3] = (c->overflow & 2u) ? 1 : 0;
+  host[4] = *any ? 1 : 0;
+  host[5] = (long long)c->maxrow;
+  reinterpret_cast<volatile unsigned*>(host)[12] = *(volatile const unsigned*)mflag;
+  __threadfence_system();
+}
+cudaError_t pack_to_host(const DetectCounters* c, const int* any, const unsigned* mflag, void* host_dev,
+                         cudaStream_t st) {
+  k_pack_to_host<<<1, 1, 0, st>>>(c, any, mflag, reinterpret_cast<volatile long long*>(host_dev));
+  return cudaGetLastError();
+}
 
 __global__ void k_readback(ReadSet rs, unsigned* dst) {
   int off = 0;
@@ -2721,6 +2805,8 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
   template cudaError_t fill<T>(T*, int64_t, T, cudaStream_t);                                      \
   template cudaError_t init_d<T>(T*, int64_t, Rows, int64_t, const T*, int64_t, cudaStream_t);     \
   template cudaError_t gather_col<T>(const T*, int64_t, Rows, int64_t, T, T*, int, cudaStream_t);  \
+  template cudaError_t update_prep<T>(const T*, int64_t, Rows, int64_t, T, T*, const T*, int64_t, int64_t, T*, \
+                                      const ZeroSet&, T*, int64_t, int64_t, int, cudaStream_t);   \
   template cudaError_t gather_col_row<T>(const T*, int64_t, Rows, int64_t, T, T*, const T*, int64_t,     \
                                          int64_t, T*, int, cudaStream_t);                               \
   template cudaError_t copy_vec<T>(const T*, int64_t, int64_t, T, T*, cudaStream_t);               \
@@ -2737,7 +2823,7 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
   template cudaError_t detect<T>(T*, int64_t, Rows, int64_t, int64_t, const T*, const T*,          \
                                  const T*, const T*, float, int, int*, int*, int*, int*, T*,      \
                                  int64_t, DetectCounters*, const T*, int64_t, int, Mirror,        \
-                                 cudaStream_t);                                                   \
+                                 cudaStream_t, const void*);                                      \
   template cudaError_t min_with_w<T>(T*, int64_t, Rows, int64_t, const T*, int64_t, cudaStream_t);  \
   template cudaError_t reset_pairs<T>(T*, int64_t, int64_t, const T*, int64_t, const int*,         \
                                       const int*, const DetectCounters*, int64_t, cudaStream_t);  \

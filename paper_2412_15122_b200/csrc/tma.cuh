@@ -9,6 +9,7 @@
 // refilled was consumed by the same warp one iteration earlier: a __syncwarp
 // plus a generic->async proxy fence order those reads before the refill.
 #pragma once
+#include <cuda.h>   // CUtensorMap (the type only; maps are encoded on the host)
 #include <stdint.h>
 
 #include "common.cuh"
@@ -45,6 +46,15 @@ __device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, unsi
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
       "%4;" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+// 2-D tiled tensor copy: the box at (c0, c1) of the tensor `map` describes
+// -> shared memory, completion counted on `bar` (SASS UTMALDG)
+__device__ __forceinline__ void tensor2d_g2s(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -105,6 +115,16 @@ struct WarpRing {
       mbar_expect_tx(b, R * bytes);
 #pragma unroll
       for (int h = 0; h < R; ++h) bulk_g2s(row(stage, h), src(h), bytes, b);
+    }
+  }
+  // lane 0: refill stage `stage` with one 2-D tensor box (R rows of CB bytes)
+  __device__ __forceinline__ void issue_box(int stage, const CUtensorMap* map, int c0, int c1, int lane) {
+    __syncwarp();
+    if (lane == 0) {
+      fence_proxy_async();
+      uint64_t* b = bar + stage % S;
+      mbar_expect_tx(b, R * CB);
+      tensor2d_g2s(row(stage, 0), map, c0, c1, b);
     }
   }
   __device__ __forceinline__ void wait(int stage) const { mbar_wait(bar + stage % S, (unsigned)(stage / S) & 1u); }

@@ -250,3 +250,7 @@ def test_closed_form_cycle_at_65536(P):
     for i in rng.choice(n, 16, replace=False):
         got = rows_of(h, [int(i)])[0]
         assert np.array_equal(got, ((np.arange(n) - i) % n).astype(np.int32))
+    # the query with the largest candidate set there is: C = all n nodes, the
+    # path s = 0, 1, ..., n - 1 (no |C| cap)
+    d, path, nc = h.query(0, n - 1, path_cap=n)
+    assert d == n - 1 and nc == n and path == list(range(n))

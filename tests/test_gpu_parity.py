@@ -1129,3 +1129,38 @@ def test_gate_dense_after_sparse_kernels(lib, rng, dtype):
     hg.remove_node(n // 2)
     assert info.path == 3
     assert_parity(getD(h), oracle.fw(hg.W))
+
+
+def test_need_update_list_fused_export_set_for_set(lib, rng):
+    """The fused kernel's own list (APSP_OPT_FUSED=1, export mode) against the
+    oracle's predicate, removals and directed increases."""
+    n = 1300
+    W = random_graph(rng, n, True, density=0.3, lo=1, hi=9, inf_frac=0.02)
+    h = make(lib, W)
+    h.set_option(lib._lib.OPT_FUSED, 1)
+    D = oracle.fw(W)
+    for k in rng.choice(n, 3, replace=False):
+        r, c, cnt = h.need_update_list("remove", int(k))
+        assert _pairs(r, c) == _mask_pairs(oracle.need_update_removal(D, int(k))) and cnt == len(r)
+    u, v = _tight_edge(W, D, rng)
+    r, c, _ = h.need_update_list("increase", u, v)
+    assert _pairs(r, c) == _mask_pairs(oracle.need_update_increase(D, u, v, int(W[u, v]), True))
+
+
+def test_query_candidate_set_beyond_scratch(lib):
+    """|C| > 4096 (the batch scratch): the directed unit cycle, s = 0, t = n-1 —
+    C is the whole arc and the path has n nodes (SURVEY §8(c-4) a8
+    closed form).  Also a query in the other direction and a short one."""
+    n = 5000
+    C = np.full((n, n), INF, np.int32)
+    np.fill_diagonal(C, 0)
+    C[np.arange(n), (np.arange(n) + 1) % n] = 1
+    h = make(lib, C)
+    d, path, nc = h.query(0, n - 1, path_cap=n)
+    assert d == n - 1 and nc == n and path == list(range(n))
+    d, path, nc = h.query(4500, 4200, path_cap=n)
+    assert d == (4200 - 4500) % n and path == [(4500 + k) % n for k in range(d + 1)]
+    d, path, _ = h.query(10, 15)
+    assert d == 5 and path == list(range(10, 16))
+    with pytest.raises(lib.ApspError):   # path_cap too small: E_RANGE, needed length reported
+        h.query(0, n - 1, path_cap=100)

@@ -6,6 +6,7 @@
 // P:196), carves the caller's workspace, and issues NCCL collectives when D
 // is row-sharded over several GPUs.
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX: named ranges per API call (free without a tool attached)
 
 #include <algorithm>
 #include <cstdarg>
@@ -26,6 +27,12 @@ using namespace apsp;
 
 namespace {
 
+// one NVTX range per C-ABI call (profilers show the update types on the timeline)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 constexpr int64_t kTile = 128;       // FW pivot block / row-partition granule
 constexpr int kMaxSlabs = 256;       // add-node column partial slabs
 constexpr int kAddColLimit = 2048;   // columns the add-node gathers may read per row (else the stream)
@@ -44,7 +51,7 @@ struct Plan {
       off_pcol, off_ocol, off_ocnt, off_gprow, off_gpcol, off_glb, off_gfull,
       off_srow, off_scol, off_slid, off_slw, off_wnext, off_slscr, off_panel, off_pt, off_anyrow, off_qsend, off_qcol,
       off_qids, off_qdsv, off_qlab, off_qpred, off_qpath, off_qdone, off_qcnt, off_p16, off_p8, off_mt, off_ptd,
-      off_small, off_qbits, off_qbpred, off_qbout, total;
+      off_small, off_qbits, off_qbpred, off_qbout, off_qhit, total;
   int64_t ldt;   // row stride of the transposed int8 mirror (bytes >= local rows)
   int qcap, qbatch;
   int64_t ldpt;
@@ -91,11 +98,13 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   p.off_pt = take(sizeof(int32_t) * (size_t)kTile * p.ldpt);
   const int64_t rows_max = world > 1 ? round_up(cdiv(cap, world), kTile) : cap;
   p.off_anyrow = take(sizeof(int32_t) * (size_t)cap);
-  // sharded queries: this rank's slices of kQueryChunk columns, and all ranks' (all-gathered)
-  p.off_qsend = take(world > 1 ? sizeof(int32_t) * (size_t)kQueryChunk * rows_max : 256);
-  p.off_qcol = take(world > 1 ? sizeof(int32_t) * (size_t)kQueryChunk * rows_max * world : 256);
   // query scratch: qbatch slots of qcap candidates (|C| <= n <= cap)
   p.qcap = (int)std::min<int64_t>(kQueryCap, cap);
+  // sharded queries (f3, gather-free): rows s of a chunk of queries (qsend),
+  // this rank's hit lists and every rank's (qcol, all-gathered)
+  p.off_qsend = take(world > 1 ? sizeof(int32_t) * (size_t)kQueryChunk * p.ld : 256);
+  p.off_qhit = take(world > 1 ? sizeof(int32_t) * (size_t)kQueryChunk * (p.qcap + 1) : 256);
+  p.off_qcol = take(world > 1 ? sizeof(int32_t) * (size_t)kQueryChunk * (p.qcap + 1) * world : 256);
   p.qbatch = world > 1 ? kQueryChunk : kQueryBatch;
   const size_t qe = (size_t)p.qcap * p.qbatch;
   p.off_qids = take(4 * qe);
@@ -1243,21 +1252,24 @@ apsp_status query_dispatch(apsp_handle* h, int q, const int* s, const int* t, T*
     return APSP_OK;
   }
   Rows r = h->active();
-  const int64_t R = h->R;
+  const int hcap = h->plan.qcap;
+  int* hits = reinterpret_cast<int*>(h->ws + h->plan.off_qhit);
+  int* allhits = reinterpret_cast<int*>(h->ws + h->plan.off_qcol);
+  T* rowbuf = h->qsend<T>();
   for (int b0 = 0; b0 < q; b0 += kQueryChunk) {
     const int c = std::min(kQueryChunk, q - b0);
-    CK(query_colslice<T>(h->Dl<T>(), ld, r.hi - r.lo, R, n, t + b0, c, h->qsend<T>(), h->st));
-    NK(h->comm->allgather(h->qsend<T>(), h->qcol<T>(), (size_t)c * R, nccl_type<T>(), h->st));
+    // rows s to every rank, the local candidate tests, the hit lists to every
+    // rank; then every rank solves (identical answers, no output exchange)
+    CK(query_rowsend<T>(h->Dl<T>(), ld, h->row0, r.hi - r.lo, n, s + b0, c, rowbuf, ld, h->st));
+    NK(h->comm->allreduce(rowbuf, (size_t)c * ld, nccl_type<T>(), ncclSum, h->st));
+    PK(APSP_K_QUERY, 8.0 * (double)(r.hi - r.lo) * c,
+       query_localscan<T>(h->Dl<T>(), ld, h->row0, r.hi - r.lo, n, s + b0, t + b0, c, rowbuf, ld, hits, hcap,
+                          h->tau, h->sr, h->wmin<T>(), h->st));
+    NK(h->comm->allgather(hits, allhits, (size_t)c * (hcap + 1), ncclInt32, h->st));
     int* pb = path_cap > 0 ? paths + (int64_t)b0 * path_cap : paths;
-    PK(APSP_K_QUERY, 8.0 * (double)n * c,
-       query_batch<T>(h->Dl<T>(), ld, h->WT<T>(), ld, n, c, s + b0, t + b0, dist + b0, pb, path_cap,
-                      lens + b0, ncand ? ncand + b0 : nullptr, h->tau, h->sr, h->st, h->qscratch(),
-                      h->wmin<T>(), h->qcol<T>(), R, h->row0, r.hi - r.lo));
-    NK(h->comm->allreduce(dist + b0, (size_t)c, nccl_type<T>(), ncclSum, h->st));
-    NK(h->comm->allreduce(lens + b0, (size_t)c, ncclInt32, ncclSum, h->st));
-    if (ncand) NK(h->comm->allreduce(ncand + b0, (size_t)c, ncclInt32, ncclSum, h->st));
-    if (path_cap > 0)
-      NK(h->comm->allreduce(pb, (size_t)c * path_cap, ncclInt32, ncclSum, h->st));
+    CK(query_solve_sharded<T>(h->Dl<T>(), ld, h->WT<T>(), ld, n, c, s + b0, t + b0, dist + b0, pb, path_cap,
+                              lens + b0, ncand ? ncand + b0 : nullptr, h->tau, h->sr, allhits, h->world, hcap,
+                              rowbuf, ld, h->qscratch(), h->st));
   }
   return APSP_OK;
 }
@@ -1637,12 +1649,14 @@ apsp_status apsp_sync_distances(apsp_handle* h) {
 
 apsp_status apsp_cold_fw(apsp_handle* h) {
   CHECK_HANDLE(h);
+  NvtxRange nvtx_("apsp_cold_fw");
   return dispatch(h->dt, [&](auto z) { return cold_fw_impl<decltype(z)>(h); });
 }
 
 apsp_status apsp_add_node(apsp_handle* h, const void* out_w, const void* in_w, int64_t* new_index,
                           apsp_update_info* info) {
   CHECK_HANDLE(h);
+  NvtxRange nvtx_("apsp_add_node");
   if (info) std::memset(info, 0, sizeof *info);
   if (!out_w || !in_w) return fail(h, APSP_E_INVAL, "add_node: null edge vector");
   if (h->n >= h->cap) return fail(h, APSP_E_CAPACITY, "add_node: n == cap == %lld", (long long)h->cap);
@@ -1651,6 +1665,7 @@ apsp_status apsp_add_node(apsp_handle* h, const void* out_w, const void* in_w, i
 
 apsp_status apsp_remove_node(apsp_handle* h, int64_t k, int64_t* moved_from, apsp_update_info* info) {
   CHECK_HANDLE(h);
+  NvtxRange nvtx_("apsp_remove_node");
   if (info) std::memset(info, 0, sizeof *info);
   if (k < 0 || k >= h->n) return fail(h, APSP_E_RANGE, "remove_node: k=%lld outside [0,%lld)", (long long)k, (long long)h->n);
   if (h->n == 1) return fail(h, APSP_E_PRECOND, "remove_node: cannot remove the last node");
@@ -1659,6 +1674,7 @@ apsp_status apsp_remove_node(apsp_handle* h, int64_t k, int64_t* moved_from, aps
 
 apsp_status apsp_update_edge(apsp_handle* h, int64_t u, int64_t v, double w_new, apsp_update_info* info) {
   CHECK_HANDLE(h);
+  NvtxRange nvtx_("apsp_update_edge");
   if (info) std::memset(info, 0, sizeof *info);
   if (u < 0 || u >= h->n || v < 0 || v >= h->n)
     return fail(h, APSP_E_RANGE, "update_edge: (%lld,%lld) outside [0,%lld)", (long long)u, (long long)v, (long long)h->n);
@@ -1677,6 +1693,7 @@ apsp_status apsp_update_edge(apsp_handle* h, int64_t u, int64_t v, double w_new,
 apsp_status apsp_modify_edge_readd(apsp_handle* h, int64_t u, int64_t v, double w_new,
                                    int64_t* removed, apsp_update_info* info) {
   CHECK_HANDLE(h);
+  NvtxRange nvtx_("apsp_modify_edge_readd");
   if (info) std::memset(info, 0, sizeof *info);
   if (u < 0 || u >= h->n || v < 0 || v >= h->n)
     return fail(h, APSP_E_RANGE, "modify_edge_readd: (%lld,%lld) outside [0,%lld)", (long long)u, (long long)v, (long long)h->n);
@@ -1696,6 +1713,7 @@ apsp_status apsp_modify_edge_readd(apsp_handle* h, int64_t u, int64_t v, double 
 apsp_status sp_pair_query(apsp_handle* h, int64_t s, int64_t t, void* dist, int32_t* path,
                           int32_t path_cap, int32_t* path_len, int32_t* n_candidates) {
   CHECK_HANDLE(h);
+  NvtxRange nvtx_("sp_pair_query");
   if (!dist || !path_len || (path_cap > 0 && !path)) return fail(h, APSP_E_INVAL, "sp_pair_query: null output");
   if (s < 0 || s >= h->n || t < 0 || t >= h->n) return fail(h, APSP_E_RANGE, "sp_pair_query: id out of range");
   return dispatch(h->dt, [&](auto z) {
@@ -1707,6 +1725,7 @@ apsp_status sp_pair_query_batch(apsp_handle* h, int32_t q, const int32_t* s, con
                                 void* dist, int32_t* paths, int32_t path_cap, int32_t* path_lens,
                                 int32_t* n_cand) {
   CHECK_HANDLE(h);
+  NvtxRange nvtx_("sp_pair_query_batch");
   if (q < 0 || (q > 0 && (!s || !t || !dist || !path_lens))) return fail(h, APSP_E_INVAL, "query_batch: null argument");
   if (path_cap > 0 && !paths) return fail(h, APSP_E_INVAL, "query_batch: null paths");
   return dispatch(h->dt, [&](auto z) -> apsp_status {

@@ -259,6 +259,22 @@ cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_
                         const QueryScratch& qs, T wmin, const T* colbuf = nullptr, int64_t R = 0,
                         int64_t row0 = 0, int64_t rows = 0);
 // sharded queries: out[b * R + i] = D[row0 + i][t_b] (INF beyond the local rows)
+// Gather-free sharded queries (f3): row s of each query to every rank
+// (rowsend + all-reduce sum), the local candidate tests (localscan: per query
+// hcap + 1 ints, count then ids), the hit lists all-gathered, then every rank
+// merges them and solves (solve_sharded) — identical answers on every rank.
+template <typename T>
+cudaError_t query_rowsend(const T* D, int64_t ld, int64_t row0, int64_t rows, int64_t n, const int* s, int qc,
+                          T* rowbuf, int64_t ldr, cudaStream_t st);
+template <typename T>
+cudaError_t query_localscan(const T* D, int64_t ld, int64_t row0, int64_t rows, int64_t n, const int* s,
+                            const int* t, int qc, const T* rowbuf, int64_t ldr, int* hits, int hcap, float tau,
+                            int sr, T wmin, cudaStream_t st);
+template <typename T>
+cudaError_t query_solve_sharded(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int qc, const int* s,
+                                const int* t, T* dist, int* paths, int path_cap, int* path_lens, int* ncand,
+                                float tau, int sr, const int* allhits, int world, int hcap, const T* rowbuf,
+                                int64_t ldr, const QueryScratch& qs, cudaStream_t st);
 template <typename T>
 cudaError_t query_colslice(const T* D, int64_t ld, int64_t rows, int64_t R, int64_t n,
                            const int* t, int qc, T* out, cudaStream_t st);

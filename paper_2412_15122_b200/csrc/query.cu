@@ -36,13 +36,14 @@
 // the sequential Dijkstra.
 //
 // Row-sharded mode (world > 1): D is split by rows,
-// so row s lives on one rank and column t is spread over all of them.  The
-// host first gathers, for a chunk of queries, every rank's slice of each
-// column t (k_query_colslice + one all-gather); then the rank owning row s
-// answers exactly as above, reading D[k][t] from the gathered slices, while
-// the other ranks write zeros, and one all-reduce(sum) of the outputs leaves
-// every rank with the owner's answer.  WT is replicated, so the small-graph
-// Dijkstra needs no communication.
+// so row s lives on one rank and column t is spread over all of them.  For a
+// chunk of queries: row s of each query goes to every rank (the owner writes
+// it, the others zeros, one all-reduce(sum)); every rank tests the candidates
+// k among ITS rows — D[s][k] from the shared row, D[k][t] local — and keeps
+// the hits; one all-gather of the hit lists (|C| ids per query, no column
+// data) gives every rank the candidate set, and every rank solves the small
+// graph itself (WT is replicated), so the answer is on every rank without a
+// further exchange.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -58,6 +59,8 @@ struct QShard {
   int64_t R;         // rows per rank
   int64_t row0, rows;   // this rank's rows (D points at global row row0)
   int qc;            // queries in this chunk
+  const T* rowbuf;   // gather-free mode: row s_b of every query (rowbuf[b * ldr + j]); every rank solves
+  int64_t ldr;
 };
 
 template <typename T>
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(32) k_query_solve(
   for (int b = blockIdx.x; b < q; b += gridDim.x) {
     const int s = S[b], t = Tq[b];
     const bool bad = s < 0 || s >= n || t < 0 || t >= n;
-    if (sh.colbuf) {
+    if (sh.colbuf && !sh.rowbuf) {
       // sharded: the owner of row s answers (rank 0 answers invalid pairs);
       // every other rank contributes zeros to the all-reduce(sum)
       const bool mine = bad ? sh.row0 == 0 : (s >= sh.row0 && s < sh.row0 + sh.rows);
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(32) k_query_solve(
       if (lane == 0) { path_lens[b] = -3; if (ncand) ncand[b] = 0; dist[b] = I; }
       continue;
     }
-    const T st = D[((int64_t)s - sh.row0) * ld + t];
+    const T st = sh.rowbuf ? sh.rowbuf[(int64_t)b * sh.ldr + t] : D[((int64_t)s - sh.row0) * ld + t];
     if (s == t || !Tr<T>::fin(st)) {
       if (lane == 0) {
         dist[b] = s == t ? T(0) : I;
@@ -337,6 +340,80 @@ __global__ void k_query_colslice(const T* __restrict__ D, int64_t ld, int64_t ro
   }
 }
 
+// ---- gather-free sharded queries (f3) -------------------------------------
+// rowbuf[b * ldr + j] = D[s_b][j] if this rank owns row s_b, else 0 (summed
+// over the ranks next)
+template <typename T>
+__global__ void k_query_rowsend(const T* __restrict__ D, int64_t ld, int64_t row0, int64_t rows, int64_t n,
+                                const int* __restrict__ S, int qc, T* rowbuf, int64_t ldr) {
+  const int b = blockIdx.y;
+  const int s = S[b];
+  const bool mine = s >= row0 && s < row0 + rows && s < n;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < ldr; j += (int64_t)gridDim.x * blockDim.x)
+    rowbuf[b * ldr + j] = (mine && j < n) ? D[((int64_t)s - row0) * ld + j] : T(0);
+}
+// hits[b * (hcap + 1)] = |C ∩ local rows| of query b, then their ids (global)
+template <typename T, int SR>
+__global__ void k_query_localscan(const T* __restrict__ D, int64_t ld, int64_t row0, int64_t rows, int64_t n,
+                                  const int* __restrict__ S, const int* __restrict__ Tq, const T* __restrict__ rowbuf,
+                                  int64_t ldr, int* hits, int hcap, float tau, T wmin) {
+  const int b = blockIdx.y;
+  const int s = S[b], t = Tq[b];
+  int* out = hits + (int64_t)b * (hcap + 1);
+  if (s < 0 || s >= n || t < 0 || t >= n || s == t) return;
+  const T* Rs = rowbuf + (int64_t)b * ldr;
+  const T st = Rs[t];
+  if (!Tr<T>::fin(st)) return;
+  T lim;
+  if (SR == 1) lim = st;
+  else if (Tr<T>::kFloat) lim = st * (1.0f + tau);
+  else lim = st - wmin;
+  const int lane = threadIdx.x & 31;
+  const int64_t hi = min(rows, n - row0);
+  for (int64_t l0 = blockIdx.x * (int64_t)blockDim.x; l0 < hi; l0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = l0 + threadIdx.x;
+    const int64_t k = row0 + l;
+    bool f = false;
+    if (l < hi) {
+      const T dsk = Rs[k];
+      if (Tr<T>::fin(dsk) && (dsk <= lim || k == t)) {
+        const T dkt = D[l * ld + t];
+        f = Tr<T>::fin(dkt) && Tr<T, SR>::tight(Tr<T, SR>::add(dsk, dkt), st, tau);
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (bal) {
+      int pos0 = 0;
+      if (lane == 0) pos0 = atomicAdd(out, __popc(bal));
+      pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+      const int pos = pos0 + __popc(bal & ((1u << lane) - 1));
+      if (f && pos < hcap) out[1 + pos] = (int)k;
+    }
+  }
+}
+// the candidate set of query b from every rank's hits -> the solve's scratch
+// (ids, D[s][id], |C|); |C| > qcap is left to the solve's capacity check
+template <typename T>
+__global__ void k_query_mergehits(const int* __restrict__ all, int world, int qc, int hcap, const T* __restrict__ rowbuf,
+                                  int64_t ldr, int* ids, T* dsv, int qcap, int* cnt) {
+  const int b = blockIdx.x;
+  int base = 0;
+  for (int rk = 0; rk < world; ++rk) {
+    const int* h = all + ((int64_t)rk * qc + b) * (hcap + 1);
+    const int c = min(h[0], hcap);
+    for (int x = threadIdx.x; x < c; x += blockDim.x) {
+      const int pos = base + x;
+      if (pos < qcap) {
+        const int k = h[1 + x];
+        ids[(int64_t)b * qcap + pos] = k;
+        dsv[(int64_t)b * qcap + pos] = rowbuf[(int64_t)b * ldr + k];
+      }
+    }
+    base += h[0];
+  }
+  if (threadIdx.x == 0) cnt[b] = base;
+}
+
 template <typename T>
 cudaError_t query_colslice(const T* D, int64_t ld, int64_t rows, int64_t R, int64_t n,
                            const int* t, int qc, T* out, cudaStream_t st) {
@@ -373,6 +450,49 @@ cudaError_t query_launch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64
   return cudaGetLastError();
 }
 
+// Gather-free sharded chunk (qc <= qs.batch queries): phases 1 and 2 of f3
+// (the caller runs the two collectives between them and solve_sharded).
+template <typename T>
+cudaError_t query_rowsend(const T* D, int64_t ld, int64_t row0, int64_t rows, int64_t n, const int* s, int qc,
+                          T* rowbuf, int64_t ldr, cudaStream_t st) {
+  const int bx = (int)std::min<int64_t>((ldr + 255) / 256, 64);
+  k_query_rowsend<T><<<dim3(bx, qc), 256, 0, st>>>(D, ld, row0, rows, n, s, qc, rowbuf, ldr);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t query_localscan(const T* D, int64_t ld, int64_t row0, int64_t rows, int64_t n, const int* s,
+                            const int* t, int qc, const T* rowbuf, int64_t ldr, int* hits, int hcap, float tau,
+                            int sr, T wmin, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(hits, 0, sizeof(int) * (size_t)qc * (hcap + 1), st);
+  if (e != cudaSuccess) return e;
+  const int bx = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 255) / 256, (int64_t)num_sms() * 4 / std::max(qc, 1) + 1));
+  if (sr)
+    k_query_localscan<T, 1><<<dim3(bx, qc), 256, 0, st>>>(D, ld, row0, rows, n, s, t, rowbuf, ldr, hits, hcap, tau, wmin);
+  else
+    k_query_localscan<T, 0><<<dim3(bx, qc), 256, 0, st>>>(D, ld, row0, rows, n, s, t, rowbuf, ldr, hits, hcap, tau, wmin);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t query_solve_sharded(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int qc, const int* s,
+                                const int* t, T* dist, int* paths, int path_cap, int* path_lens, int* ncand,
+                                float tau, int sr, const int* allhits, int world, int hcap, const T* rowbuf,
+                                int64_t ldr, const QueryScratch& qs, cudaStream_t st) {
+  T* cand_d = reinterpret_cast<T*>(qs.dsv);
+  k_query_mergehits<T><<<qc, 256, 0, st>>>(allhits, world, qc, hcap, rowbuf, ldr, qs.ids, cand_d, qs.qcap, qs.cnt);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  QScratch<T> gs{qs.ids, cand_d, reinterpret_cast<T*>(qs.lab), qs.pred, qs.path, qs.done, qs.qcap};
+  QShard<T> sh{nullptr, 0, 0, 0, qc, rowbuf, ldr};
+  const int grid = std::min(qc, num_sms() * 16);
+  if (sr)
+    k_query_solve<T, 1><<<grid, 32, 0, st>>>(D, ld, WT, ldw, n, qc, s, t, qs.cnt, gs, dist, paths, path_cap,
+                                             path_lens, ncand, sh);
+  else
+    k_query_solve<T, 0><<<grid, 32, 0, st>>>(D, ld, WT, ldw, n, qc, s, t, qs.cnt, gs, dist, paths, path_cap,
+                                             path_lens, ncand, sh);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int q,
                         const int* s, const int* t, T* dist, int* paths, int path_cap,
@@ -383,7 +503,7 @@ cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_
   if (colbuf && q > qs.batch) return cudaErrorInvalidValue;   // the host chunks sharded batches
   for (int b0 = 0; b0 < q; b0 += qs.batch) {
     const int c = std::min(qs.batch, q - b0);
-    QShard<T> sh{colbuf, R, colbuf ? row0 : 0, rows, c};
+    QShard<T> sh{colbuf, R, colbuf ? row0 : 0, rows, c, nullptr, 0};
     int* pb = path_cap > 0 ? paths + (int64_t)b0 * path_cap : paths;
     int* nc = ncand ? ncand + b0 : nullptr;
     cudaError_t e = sr ? query_launch<T, 1>(D, ld, WT, ldw, n, c, s + b0, t + b0, dist + b0, pb, path_cap,
@@ -503,7 +623,14 @@ cudaError_t query_big(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t 
                                       int, cudaStream_t, const QueryScratch&, T, const T*, int64_t, \
                                       int64_t, int64_t);                                         \
   template cudaError_t query_colslice<T>(const T*, int64_t, int64_t, int64_t, int64_t,          \
-                                         const int*, int, T*, cudaStream_t);
+                                         const int*, int, T*, cudaStream_t);                     \
+  template cudaError_t query_rowsend<T>(const T*, int64_t, int64_t, int64_t, int64_t, const int*, int, T*, \
+                                        int64_t, cudaStream_t);                                  \
+  template cudaError_t query_localscan<T>(const T*, int64_t, int64_t, int64_t, int64_t, const int*, const int*, \
+                                          int, const T*, int64_t, int*, int, float, int, T, cudaStream_t); \
+  template cudaError_t query_solve_sharded<T>(const T*, int64_t, const T*, int64_t, int64_t, int, const int*, \
+                                              const int*, T*, int*, int, int*, int*, float, int, const int*, int, \
+                                              int, const T*, int64_t, const QueryScratch&, cudaStream_t);
 INST(int32_t)
 INST(float)
 #undef INST

@@ -598,11 +598,13 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
         const T w = sw[q * 32 + lane];
         if (m >= 0) {
           T d;
-          if (Mrow) {   // (column `skip` — the removed node — is tombstoned in D, not in the mirror)
+          // column `skip` (the removed node) is not tombstoned in the mirror,
+          // nor yet in D (the swap-with-last overwrites it): read as INF
+          if (Mrow) {
             const int32_t b8 = Mrow[m];
             d = (b8 == kSat8i || m == skip) ? Tr<T>::inf() : (T)b8;
           } else {
-            d = *(volatile T*)(Drow + m);
+            d = m == skip ? Tr<T>::inf() : *(volatile T*)(Drow + m);
           }
           acc = Tr<T, SR>::relax(acc, d, w);
           wseen = w > wseen ? w : wseen;

@@ -2410,7 +2410,7 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
                    int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr, const T* WT,
                    int64_t ldw, int sr, Mirror M, cudaStream_t st, const void* tmap8) {
   if (r.hi <= r.lo) return cudaSuccess;
-  static const int wps = tune_wps("APSP_TUNE_DET_WPS", 192), wps8 = tune_wps("APSP_TUNE_DET8_WPS", 8 * D8_MINB);
+  static const int wps = tune_wps("APSP_TUNE_DET_WPS", 192), wps8 = tune_wps("APSP_TUNE_DET8_WPS", 128);
   Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20, DS_VEC, wps);   // (measured best)
   if (tl.slab >= (1 << 26)) return cudaErrorInvalidValue;   // MODE-1 queue packing
   if (mode == 0) CUDA_TRY(cudaMemsetAsync(anyrow + r.lo, 0, sizeof(int) * (size_t)(r.hi - r.lo), st));

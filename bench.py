@@ -354,8 +354,10 @@ def main():
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
+    torch.cuda.nvtx.range_push("timed")   # (ncu --nvtx --nvtx-include "timed/": the timed region's launches)
     for s in range(args.warmup, args.warmup + args.steps):
         run_step(s, True)
+    torch.cuda.nvtx.range_pop()
     t1.record(stream)
     barrier()
     total_ms = max_over_ranks(t0.elapsed_time(t1))

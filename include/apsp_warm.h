@@ -115,12 +115,17 @@ typedef enum {
                                int32 D itself (4 bytes per entry, SURVEY §8(d-4)'s
                                byte basis); for measuring the 4-byte streams.  Results
                                are identical.  Takes effect at the next update.       */
-  APSP_OPT_FUSED = 9        /* 1: removals and directed edge increases on the int8
+  APSP_OPT_FUSED = 9,       /* 1: removals and directed edge increases on the int8
                                mirror run detection and the first phase of the sparse
                                recompute in ONE pass, each row of the mirror staged
                                whole in shared memory (n up to ~36K).  0 (default): the
                                separate kernels, measured faster at BJ.c4 (DESIGN.md
                                §11).  Results are identical.                          */
+  APSP_OPT_HEAVY = 10       /* Sparse recompute, one GPU: a row with at least this many
+                               open pairs skips the frontier rounds and is resolved
+                               from the other rows once they are final (at most 32
+                               rows per update).  0 (default):
+                               max(512, n/8); -1: never.  Results are identical.      */
 } apsp_option;
 
 /* Statistics of one update. */

@@ -20,7 +20,7 @@ STATUS = {
     5: "APSP_E_CUDA", 6: "APSP_E_NCCL", 7: "APSP_E_NOMEM", 8: "APSP_E_POISONED", 9: "APSP_E_UNSUPPORTED",
 }
 (OPT_FORCE_PATH, OPT_THETA, OPT_TAU, OPT_MAX_ROUNDS, OPT_ROW_DELTA, OPT_SEMIRING, OPT_FW16, OPT_MIRROR8,
- OPT_MIRROR, OPT_FUSED) = range(10)
+ OPT_MIRROR, OPT_FUSED, OPT_HEAVY) = range(11)
 
 # exported symbols (tests check the library exports every one of them)
 SYMBOLS = [

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -51,7 +52,7 @@ struct Plan {
       off_pcol, off_ocol, off_ocnt, off_gprow, off_gpcol, off_glb, off_gfull,
       off_srow, off_scol, off_slid, off_slw, off_wnext, off_slscr, off_panel, off_pt, off_anyrow, off_qsend, off_qcol,
       off_qids, off_qdsv, off_qlab, off_qpred, off_qpath, off_qdone, off_qcnt, off_p16, off_p8, off_mt, off_ptd,
-      off_small, off_qbits, off_qbpred, off_qbout, off_qhit, total;
+      off_small, off_qbits, off_qbpred, off_qbout, off_qhit, off_heavy, off_bigq, total;
   int64_t ldt;   // row stride of the transposed int8 mirror (bytes >= local rows)
   int qcap, qbatch;
   int64_t ldpt;
@@ -92,7 +93,7 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   p.off_slw = take(sizeof(int32_t) * (size_t)cap * kSL);
   p.off_wnext = take(sizeof(int32_t) * (size_t)cap);
   p.off_slscr = take(kSLScratch);
-  p.off_panel = take(world > 1 ? sizeof(int32_t) * (size_t)kTile * p.ld : 256);
+  p.off_panel = take(world > 1 ? 2 * sizeof(int32_t) * (size_t)kTile * p.ld : 256);   // two receive buffers
   // transposed pivot column panel for the FW phase-3 kernel (kTile x ldpt)
   p.ldpt = round_up(world > 1 ? round_up(cdiv(cap, world), kTile) : cap, kTile);
   p.off_pt = take(sizeof(int32_t) * (size_t)kTile * p.ldpt);
@@ -126,6 +127,9 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   p.ldt = round_up(rows_max, 128);
   p.off_mt = take((size_t)cap * p.ldt);       // its transpose (column j of D = row j)
   p.off_ptd = take(sizeof(uint32_t) * (size_t)kTile * kTile);
+  // heavy rows of the sparse recompute (one GPU): the set, then kHeavy rows of X keys
+  p.off_heavy = take(256 + sizeof(int32_t) * (size_t)kHeavy * p.ld);
+  p.off_bigq = take(sizeof(int32_t) * (size_t)p.ocap);   // the rounds' long-frontier pair queue (one GPU)
   p.off_small = take(64 * 1024);
   p.total = o;
   return p;
@@ -153,6 +157,8 @@ struct apsp_handle {
   cudaStream_t st;
   cudaStream_t st2 = nullptr;    // side stream: shortlist upkeep overlapped with the D passes
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_row = nullptr;
+  cudaStream_t stc = nullptr;    // sharded FW: panel broadcasts (look-ahead), world > 1
+  cudaEvent_t ev_pan = nullptr, ev_bc = nullptr;
   int rank, world;
   Comm* comm = nullptr;          // world > 1: NCCL or in-process group (comm.h)
   // options
@@ -168,6 +174,7 @@ struct apsp_handle {
   int mirror_level = 16;         // width of the mirror: 8 or 16 bits
   int mirror8 = 1;               // APSP_OPT_MIRROR8: try the int8 width at each build
   int use_mirror = 1;            // APSP_OPT_MIRROR: 0 = no mirror, the streams read D (4 B/entry)
+  int heavy_min = 0;             // APSP_OPT_HEAVY: 0 = max(512, n/8), -1 = off
   int fused = 0;                 // APSP_OPT_FUSED: detection + phase A in one pass (fused.cu; off:
                                  // measured slower than the separate kernels)
   bool mirror8_failed = false;   // an int8 build found a distance >= 0x7F: int16 from then on
@@ -187,6 +194,12 @@ struct apsp_handle {
   // profiling (apsp_profile_*)
   struct ProfRec { int cls; cudaEvent_t a, b; double work; };
   bool prof_on = false;
+  // one GPU: captured FW pivot loops, keyed by (variant, n); a key is captured
+  // the second time it runs (fw_graph)
+  struct FwGraph { cudaGraphExec_t exec; int64_t launches; };
+  std::map<uint64_t, FwGraph> fw_graphs;
+  cudaStream_t stcap = nullptr;  // capture stream (the caller's may be the legacy default stream)
+  std::vector<uint64_t> fw_seen;
   std::vector<ProfRec> prof_pending;
   std::vector<cudaEvent_t> ev_pool;
   double prof_ms[APSP_K_COUNT] = {};
@@ -247,7 +260,9 @@ struct apsp_handle {
   template <typename T> T* slw() { return reinterpret_cast<T*>(ws + plan.off_slw); }
   template <typename T> T* wnext() { return reinterpret_cast<T*>(ws + plan.off_wnext); }
   void* slscr() { return ws + plan.off_slscr; }
-  template <typename T> T* panel() { return reinterpret_cast<T*>(ws + plan.off_panel); }
+  template <typename T> T* panel(int b = 0) {
+    return reinterpret_cast<T*>(ws + plan.off_panel + (size_t)b * sizeof(int32_t) * kTile * plan.ld);
+  }
   template <typename T> T* pt() { return reinterpret_cast<T*>(ws + plan.off_pt); }
   template <typename T> T* qsend() { return reinterpret_cast<T*>(ws + plan.off_qsend); }
   template <typename T> T* qcol() { return reinterpret_cast<T*>(ws + plan.off_qcol); }
@@ -274,6 +289,13 @@ struct apsp_handle {
   unsigned* mirror_flag() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 396); }
   unsigned* pass1_uncertain() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 400); }
   unsigned* mirror_epoch_word() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 472); }
+  unsigned* validate_done() { return reinterpret_cast<unsigned*>(ws + plan.off_small + 476); }   // block counter
+  int* coop_rounds_word() { return reinterpret_cast<int*>(ws + plan.off_small + 480); }
+  int* coop_total_word() { return reinterpret_cast<int*>(ws + plan.off_small + 484); }
+  int* heavy_set() { return reinterpret_cast<int*>(ws + plan.off_heavy); }
+  int* bigq() { return reinterpret_cast<int*>(ws + plan.off_bigq); }
+  int* bigq_ctr() { return reinterpret_cast<int*>(ws + plan.off_small + 488); }   // 4 ints
+  int* heavy_x() { return reinterpret_cast<int*>(ws + plan.off_heavy + 256); }
   alignas(64) unsigned char tmap8[128];   // CUtensorMap of the int8 mirror (detection's TMA)
   bool tmap8_ok = false;
   const void* tmap8_ptr() const { return tmap8_ok ? tmap8 : nullptr; }
@@ -501,6 +523,121 @@ apsp_status ensure_mirror(apsp_handle* h) {
   return (h->mirror_built && !stale8) ? APSP_OK : mirror_rebuild<T>(h);
 }
 
+// One GPU: the pivot loop of a blocked FW is a fixed launch sequence for a
+// given (variant, n) over the handle's fixed buffers — captured into a CUDA
+// graph the second time it runs and replayed after that (one launch instead
+// of ~4 per pivot block).  Not under the per-kernel profile (its events would
+// be captured too) and never when sharded (the loop holds collectives).
+constexpr size_t kFwGraphs = 8;
+template <typename Body>
+apsp_status fw_graph(apsp_handle* h, uint64_t key, Body body) {
+  if (h->prof_on || h->world > 1) return body();
+  auto it = h->fw_graphs.find(key);
+  if (it == h->fw_graphs.end()) {
+    if (std::find(h->fw_seen.begin(), h->fw_seen.end(), key) == h->fw_seen.end()) {
+      if (h->fw_seen.size() >= 64) h->fw_seen.erase(h->fw_seen.begin());
+      h->fw_seen.push_back(key);
+      return body();   // first run of this key: plain launches
+    }
+    if (h->fw_graphs.size() >= kFwGraphs) {   // bounded cache: drop one
+      cudaGraphExecDestroy(h->fw_graphs.begin()->second.exec);
+      h->fw_graphs.erase(h->fw_graphs.begin());
+    }
+    const int64_t l0 = h->launches;
+    // captured on a stream of its own (capturing the legacy default stream is
+    // not allowed): the body enqueues on h->st, swapped for the capture; the
+    // graph is then launched on the caller's stream
+    if (!h->stcap) CKR(cudaStreamCreateWithFlags(&h->stcap, cudaStreamNonBlocking));
+    cudaStream_t user = h->st;
+    h->st = h->stcap;
+    cudaError_t eb = cudaStreamBeginCapture(h->st, cudaStreamCaptureModeRelaxed);
+    const apsp_status s = eb == cudaSuccess ? body() : APSP_OK;
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = eb == cudaSuccess ? cudaStreamEndCapture(h->st, &g) : eb;
+    h->st = user;
+    if (s != APSP_OK) {
+      if (g) cudaGraphDestroy(g);
+      return s;
+    }
+    CKR(e);
+    cudaGraphExec_t ex = nullptr;
+    const cudaError_t e2 = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    CKR(e2);
+    it = h->fw_graphs.emplace(key, apsp_handle::FwGraph{ex, h->launches - l0}).first;
+    h->launches = l0;   // counted when replayed
+  }
+  CKR(cudaGraphLaunch(it->second.exec, h->st));
+  h->launches += it->second.launches;
+  return APSP_OK;
+}
+
+// Sharded blocked FW (world > 1) with look-ahead: the owner of pivot block
+// K+1 first relaxes that block's rows through pivot K, closes it (diagonal +
+// row panel) and broadcasts it on the comm stream, while the rest of pivot
+// K's phase 3 runs on the compute stream; receivers alternate between two
+// panel buffers.  close(K0, kb) -> the owner's panel (on h->st);
+// phase3(K0, kb, P, lo, hi, skip_ti) relaxes local rows [lo, hi) through
+// pivot block K0 with panel P (skipping row tile skip_ti of that range);
+// recv(b) = receive buffer b; words = panel elements per row.
+template <typename E, typename Close, typename Phase3, typename Recv>
+apsp_status fw_sharded(apsp_handle* h, int64_t n, int64_t m, size_t words, ncclDataType_t dt, Close close,
+                       Phase3 phase3, Recv recv) {
+  const int64_t T = kTile;
+  auto bcast = [&](E* P, int64_t K0, int kb) -> apsp_status {
+    CKR(cudaEventRecord(h->ev_pan, h->st));   // panel closed / receive buffer free
+    CKR(cudaStreamWaitEvent(h->stc, h->ev_pan, 0));
+    NK(h->comm->bcast(P, (size_t)kb * words, dt, h->owner(K0), h->stc));
+    CKR(cudaEventRecord(h->ev_bc, h->stc));
+    return APSP_OK;
+  };
+  E* P = nullptr;
+  {
+    const int kb0 = (int)std::min<int64_t>(T, n);
+    if (h->local(0)) {
+      apsp_status s = close(int64_t(0), kb0, &P);
+      if (s != APSP_OK) return s;
+    } else {
+      P = recv(0);
+    }
+    apsp_status s = bcast(P, 0, kb0);
+    if (s != APSP_OK) return s;
+  }
+  for (int64_t K0 = 0, kbi = 0; K0 < n; K0 += T, ++kbi) {
+    const int kb = (int)std::min<int64_t>(T, n - K0);
+    const bool own = h->local(K0);
+    const int skip_ti = own ? (int)((K0 - h->row0) / T) : -1;
+    CKR(cudaStreamWaitEvent(h->st, h->ev_bc, 0));   // panel K in place everywhere
+    E* P1 = nullptr;
+    const int64_t K1 = K0 + T;
+    apsp_status s = APSP_OK;
+    if (K1 < n) {
+      const int kb1 = (int)std::min<int64_t>(T, n - K1);
+      const bool own1 = h->local(K1);
+      const int64_t l1 = K1 - h->row0;
+      if (own1) {   // look-ahead: block K+1's rows through pivot K, then close it
+        s = phase3(K0, kb, P, l1, std::min<int64_t>(l1 + T, m), -1);
+        if (s == APSP_OK) s = close(K1, kb1, &P1);
+      } else {
+        P1 = recv((int)((kbi + 1) & 1));
+      }
+      if (s == APSP_OK) s = bcast(P1, K1, kb1);
+      if (s != APSP_OK) return s;
+      if (own1) {   // the rest of pivot K's phase 3, around block K+1
+        s = phase3(K0, kb, P, 0, l1, skip_ti);
+        if (s == APSP_OK) s = phase3(K0, kb, P, std::min<int64_t>(l1 + T, m), m, -1);
+      } else {
+        s = phase3(K0, kb, P, 0, m, skip_ti);
+      }
+    } else {
+      s = phase3(K0, kb, P, 0, m, skip_ti);
+    }
+    if (s != APSP_OK) return s;
+    P = P1;
+  }
+  return APSP_OK;
+}
+
 // int16x2 blocked FW (fw.cu) over the packed copy of this rank's rows, with the
 // same pivot schedule and panel broadcast as fw_impl_elem.  Sets *saturated
 // (summed over ranks) when some entry reached 0x3FFF: D then holds the exact
@@ -512,33 +649,55 @@ apsp_status fw16_impl(apsp_handle* h, int64_t skip, bool* saturated) {
   uint32_t* P = h->p16();
   uint32_t* PT = h->pt<uint32_t>();
   CK(p16_from_d32(h->Dl<int32_t>(), ld, m, n, P, h->st));
-  for (int64_t K0 = 0; K0 < n; K0 += kTile) {
-    const int kb = (int)std::min<int64_t>(kTile, n - K0);
-    const bool own = h->local(K0);
-    const int64_t lk = K0 - h->row0;
-    uint32_t* panel;
-    if (own) {
-      uint32_t* rowK = P + lk * (ld / 2);
+  if (h->world > 1) {
+    const int64_t lw = ld / 2;   // words per packed row
+    auto close = [&](int64_t K0, int kb, uint32_t** out) -> apsp_status {
+      uint32_t* rowK = P + (K0 - h->row0) * lw;
       PK(APSP_K_FW_DIAG, (double)kb * kb * kb, p16_diag(rowK + K0 / 2, ld, kb, h->st));
       CK(p16_transpose_rep(rowK, ld, kb, K0, kb, h->ptd(), kTile, h->st));
-      PK(APSP_K_FW_PANEL, (double)kb * kb * (n - kb),
-         p16_tile3(rowK, ld, h->ptd(), kTile, rowK, kb, n, kb, -1, h->st));
-      panel = rowK;
-    } else {
-      panel = h->panel<uint32_t>();
-    }
-    if (h->world > 1)
-      NK(h->comm->bcast(panel, (size_t)kb * (ld / 2), ncclUint32, h->owner(K0), h->st));
-    const int skip_ti = own ? (int)(lk / kTile) : -1;
-    if (m > 0) {
-      const double mo = (double)(m - (own ? kb : 0));
-      CK(p16_transpose_rep(P, ld, m, K0, kb, PT, h->plan.ldpt, h->st));   // old column panel
+      PK(APSP_K_FW_PANEL, (double)kb * kb * (n - kb), p16_tile3(rowK, ld, h->ptd(), kTile, rowK, kb, n, kb, -1, h->st));
+      *out = rowK;
+      return APSP_OK;
+    };
+    auto phase3 = [&](int64_t K0, int kb, uint32_t* panel, int64_t lo, int64_t hi, int skip_ti) -> apsp_status {
+      if (hi <= lo) return APSP_OK;
+      uint32_t* Pr = P + lo * lw;
+      const int64_t rows = hi - lo;
+      const double mo = (double)(rows - (skip_ti >= 0 ? kb : 0));
+      CK(p16_transpose_rep(Pr, ld, rows, K0, kb, PT, h->plan.ldpt, h->st));   // old column panel
       PK(APSP_K_FW_PANEL, mo * kb * kb,
-         p16_tile3(P + K0 / 2, ld, PT, h->plan.ldpt, panel + K0 / 2, m, kb, kb, skip_ti, h->st));
-      CK(p16_transpose_rep(P, ld, m, K0, kb, PT, h->plan.ldpt, h->st));   // updated column panel
+         p16_tile3(Pr + K0 / 2, ld, PT, h->plan.ldpt, panel + K0 / 2, rows, kb, kb, skip_ti, h->st));
+      CK(p16_transpose_rep(Pr, ld, rows, K0, kb, PT, h->plan.ldpt, h->st));   // updated column panel
       PK(APSP_K_FW_TILE, mo * (double)(n - kb) * kb,
-         p16_tile3(P, ld, PT, h->plan.ldpt, panel, m, n, kb, skip_ti, h->st));
-    }
+         p16_tile3(Pr, ld, PT, h->plan.ldpt, panel, rows, n, kb, skip_ti, h->st));
+      return APSP_OK;
+    };
+    auto recv = [&](int b) { return h->panel<uint32_t>(b); };
+    apsp_status s = fw_sharded<uint32_t>(h, n, m, (size_t)lw, ncclUint32, close, phase3, recv);
+    if (s != APSP_OK) return s;
+  }
+  if (h->world == 1) {   // every row local: no panel exchange
+    auto loop = [&]() -> apsp_status {
+      for (int64_t K0 = 0; K0 < n; K0 += kTile) {
+        const int kb = (int)std::min<int64_t>(kTile, n - K0);
+        uint32_t* rowK = P + K0 * (ld / 2);
+        PK(APSP_K_FW_DIAG, (double)kb * kb * kb, p16_diag(rowK + K0 / 2, ld, kb, h->st));
+        CK(p16_transpose_rep(rowK, ld, kb, K0, kb, h->ptd(), kTile, h->st));
+        PK(APSP_K_FW_PANEL, (double)kb * kb * (n - kb),
+           p16_tile3(rowK, ld, h->ptd(), kTile, rowK, kb, n, kb, -1, h->st));
+        const int skip_ti = (int)(K0 / kTile);
+        const double mo = (double)(m - kb);
+        CK(p16_transpose_rep(P, ld, m, K0, kb, PT, h->plan.ldpt, h->st));   // old column panel
+        PK(APSP_K_FW_PANEL, mo * kb * kb,
+           p16_tile3(P + K0 / 2, ld, PT, h->plan.ldpt, rowK + K0 / 2, m, kb, kb, skip_ti, h->st));
+        CK(p16_transpose_rep(P, ld, m, K0, kb, PT, h->plan.ldpt, h->st));   // updated column panel
+        PK(APSP_K_FW_TILE, mo * (double)(n - kb) * kb,
+           p16_tile3(P, ld, PT, h->plan.ldpt, rowK, m, n, kb, skip_ti, h->st));
+      }
+      return APSP_OK;
+    };
+    apsp_status s = fw_graph(h, (uint64_t)n << 8 | 1u, loop);
+    if (s != APSP_OK) return s;
   }
   CKR(cudaMemsetAsync(h->fw16_flag(), 0, sizeof(unsigned), h->st));
   CK(p16_to_d32(P, ld, m, n, h->row0, skip, h->Dl<int32_t>(), h->fw16_flag(), h->st));
@@ -593,31 +752,42 @@ apsp_status fw_impl_elem(apsp_handle* h) {
   Rows r = h->active();
   const int64_t m = r.hi - r.lo;   // local active rows (local row 0 = global row0)
   T* D = h->Dl<T>();
-  for (int64_t K0 = 0; K0 < n; K0 += kTile) {
-    const int kb = (int)std::min<int64_t>(kTile, n - K0);
-    const bool own = h->local(K0);
-    const int64_t lk = K0 - h->row0;    // local row of the pivot block (if own)
-    T* P;
-    if (own) {
-      T* rowK = D + lk * ld;
+  if (h->world > 1) {
+    auto close = [&](int64_t K0, int kb, T** out) -> apsp_status {
+      T* rowK = D + (K0 - h->row0) * ld;
       PK(APSP_K_FW_DIAG, (double)kb * kb * kb, fw_diag<T>(rowK + K0, ld, kb, h->sr, h->st));
       PK(APSP_K_FW_PANEL, (double)kb * kb * (n - kb), fw_row_panel<T>(rowK, ld, K0, kb, n, h->sr, h->st));
-      P = rowK;
-    } else {
-      P = h->panel<T>();
-    }
-    if (h->world > 1) {
-      NK(h->comm->bcast(P, (size_t)kb * ld, nccl_type<T>(), h->owner(K0), h->st));
-    }
-    const int skip_ti = own ? (int)(lk / kTile) : -1;
-    if (m > 0) {
-      const double mo = (double)(m - (own ? kb : 0));   // rows outside the pivot block
-      PK(APSP_K_FW_PANEL, mo * kb * kb, fw_col_panel<T>(D, ld, m, K0, kb, P + K0, ld, skip_ti, h->sr, h->st));
+      *out = rowK;
+      return APSP_OK;
+    };
+    auto phase3 = [&](int64_t K0, int kb, T* P, int64_t lo, int64_t hi, int skip_ti) -> apsp_status {
+      if (hi <= lo) return APSP_OK;
+      T* Dr = D + lo * ld;
+      const int64_t rows = hi - lo;
+      const double mo = (double)(rows - (skip_ti >= 0 ? kb : 0));
+      PK(APSP_K_FW_PANEL, mo * kb * kb, fw_col_panel<T>(Dr, ld, rows, K0, kb, P + K0, ld, skip_ti, h->sr, h->st));
       PK(APSP_K_FW_TILE, mo * (double)(n - kb) * kb,
-         fw_rest_pt<T>(D, ld, m, n, K0, kb, P, ld, skip_ti, h->pt<T>(), h->plan.ldpt, h->sr, h->st));
-    }
+         fw_rest_pt<T>(Dr, ld, rows, n, K0, kb, P, ld, skip_ti, h->pt<T>(), h->plan.ldpt, h->sr, h->st));
+      return APSP_OK;
+    };
+    auto recv = [&](int b) { return h->panel<T>(b); };
+    return fw_sharded<T>(h, n, m, (size_t)ld, nccl_type<T>(), close, phase3, recv);
   }
-  return APSP_OK;
+  auto loop = [&]() -> apsp_status {   // one GPU: every row local
+    for (int64_t K0 = 0; K0 < n; K0 += kTile) {
+      const int kb = (int)std::min<int64_t>(kTile, n - K0);
+      T* rowK = D + K0 * ld;
+      PK(APSP_K_FW_DIAG, (double)kb * kb * kb, fw_diag<T>(rowK + K0, ld, kb, h->sr, h->st));
+      PK(APSP_K_FW_PANEL, (double)kb * kb * (n - kb), fw_row_panel<T>(rowK, ld, K0, kb, n, h->sr, h->st));
+      const int skip_ti = (int)(K0 / kTile);
+      const double mo = (double)(m - kb);   // rows outside the pivot block
+      PK(APSP_K_FW_PANEL, mo * kb * kb, fw_col_panel<T>(D, ld, m, K0, kb, rowK + K0, ld, skip_ti, h->sr, h->st));
+      PK(APSP_K_FW_TILE, mo * (double)(n - kb) * kb,
+         fw_rest_pt<T>(D, ld, m, n, K0, kb, rowK, ld, skip_ti, h->pt<T>(), h->plan.ldpt, h->sr, h->st));
+    }
+    return APSP_OK;
+  };
+  return fw_graph(h, (uint64_t)n << 8 | (std::is_same<T, float>::value ? 2u : 4u) | (uint64_t)h->sr << 3, loop);
 }
 
 // Cold start (a1): D := W, then blocked FW.
@@ -665,6 +835,8 @@ ZeroSet recompute_zero_set(apsp_handle* h) {
   for (int q = 0; q < 4; ++q) z.add(h->chg(q), h->cap + 1);
   z.add(h->anyflag(), 1);
   z.add(h->anyrow(), h->cap);   // the rounds' per-row open minima (keys)
+  z.add(h->heavy_set(), 1);     // no heavy rows selected
+  z.add(h->bigq_ctr(), 4);      // the rounds' queue counters
   return z;
 }
 
@@ -721,6 +893,9 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   // a batch changed nothing: its total, read with the counters.
   int rounds = 0;
   int* fcol[2] = {h->prow(), h->pcol()};
+  // one GPU: the rounds run in one cooperative kernel (sparse_rounds_coop);
+  // sharded: batches of single-round launches with a flag all-reduce between
+  const bool coop = h->world == 1;
   int* last_total = h->anyflag();   // no round enqueued: 0
   auto enqueue_rounds = [&](int batch) -> apsp_status {
     for (int b = 0; b < batch; ++b, ++rounds) {
@@ -764,8 +939,27 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     // rounds over the open entries of each row, a first batch of 4
     // the first batch is enqueued blind: as many rounds as the previous
     // recompute needed (at least 2: round 1 finding nothing proves convergence)
-    apsp_status s = enqueue_rounds(std::min(std::max(2, h->rounds_hint), h->max_rounds));
-    if (s != APSP_OK) return s;
+    if (coop) {   // every round in one cooperative launch, to convergence (no host round trips)
+      // rows with >= max(512, n/8) open pairs skip the rounds and are resolved
+      // from the other rows afterwards (heavy_rows)
+      if (h->heavy_min >= 0)
+        CK(heavy_select(h->ocnt(), r.hi - r.lo,
+                        h->heavy_min > 0 ? h->heavy_min : (int)std::max<int64_t>(512, n / 8), h->heavy_set(), h->st));
+      RoundBufs rb{h->chg(0),      h->cap + 32,     h->cap,    {fcol[0], fcol[1]}, h->coop_rounds_word(),
+                   h->coop_total_word(), h->heavy_set(), h->bigq(), h->bigq_ctr()};
+      PK(APSP_K_SPARSE_R, 0.0,
+         sparse_rounds_coop<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->gprow(), h->gpcol(), h->glb<T>(),
+                               ocap, h->rowoff(), h->ocnt(), h->ocol(), rb, 0, h->max_rounds, h->anyflag(), h->sr,
+                               h->ctr(), h->st, reinterpret_cast<unsigned*>(h->anyrow()), h->wmin<T>(),
+                               h->mirror<T>()));
+      PK(APSP_K_SPARSE_R, 0.0,
+         heavy_rows<T>(h->Dl<T>(), h->ld, n, h->WT<T>(), h->ld, h->heavy_set(), h->heavy_x(), h->ld,
+                       removal ? skip : -1, h->sr, h->st, h->mirror<T>()));
+      last_total = h->coop_total_word();
+    } else {
+      apsp_status s = enqueue_rounds(std::min(std::max(2, h->rounds_hint), h->max_rounds));
+      if (s != APSP_OK) return s;
+    }
   }
 
   if (removal && !try_sparse) {
@@ -776,7 +970,8 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   long long* hv = reinterpret_cast<long long*>(h->host_small);
   unsigned* hmf = reinterpret_cast<unsigned*>(h->host_small) + 12;
   if (h->world == 1) {   // packed straight into mapped host memory
-    CK(pack_to_host(h->ctr(), last_total, h->mirror_flag(), h->host_small_dev, h->st));
+    CK(pack_to_host(h->ctr(), last_total, h->mirror_flag(), h->host_small_dev, h->st,
+                    coop && try_sparse ? h->coop_rounds_word() : nullptr));
   } else {
     long long* v = reinterpret_cast<long long*>(h->small());
     CK(pack_counters(h->ctr(), last_total, v, h->st));   // total rows ovf1 ovf2 changed | maxrow
@@ -789,6 +984,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   }
   CKR(cudaStreamSynchronize(h->st));
   h->mirror_hint = (*hmf & 1u) == 0u;
+  if (coop && try_sparse) rounds = (int)reinterpret_cast<unsigned*>(h->host_small)[14];
   const int64_t total = hv[0], rows = hv[1], maxrow = hv[5];
   const bool overflow = hv[2] != 0 || hv[3] != 0;   // a list overflowed on some rank
   bool changed = hv[4] != 0;
@@ -805,7 +1001,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   // rounds until no entry changes (rarely more than the first batch); later
   // batches double (a round whose frontier is empty costs one small launch)
   int batch = std::max(2, rounds);
-  while (!dense && changed && rounds < h->max_rounds) {
+  while (!coop && !dense && changed && rounds < h->max_rounds) {
     batch *= 2;
     apsp_status s = enqueue_rounds(std::min(batch, h->max_rounds - rounds));
     if (s != APSP_OK) return s;
@@ -853,13 +1049,18 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   T* iw = h->vec<T>(1);
   T* col = h->vec<T>(2);
   T* row = h->vec<T>(3);
+  // (the scratch words start reset: at creation, then by each add's last
+  // kernel, addnode_write, or on a rejected call below)
   const AddScratch as = h->add_scratch();
-  CK(add_init(as, &h->ctr()->err, h->wmin_dev(), h->st));
+  // both vectors in one launch; its last block writes the host's read (the
+  // validation flag, the smallest weight, the mirror flag) to mapped memory
   CK(validate_vec<T>(reinterpret_cast<const T*>(out_w), nullptr, n, ld, ow, &h->ctr()->err, h->wmin_dev(),
                      h->st, reinterpret_cast<const T*>(in_w),
-                     h->directed ? nullptr : reinterpret_cast<const T*>(out_w), iw,   // both vectors, one launch
+                     h->directed ? nullptr : reinterpret_cast<const T*>(out_w), iw,
                      std::is_same<T, int32_t>::value ? as.argmin_out : nullptr,
-                     std::is_same<T, int32_t>::value ? as.in_min : nullptr));
+                     std::is_same<T, int32_t>::value ? as.in_min : nullptr,
+                     ValidateReadback{reinterpret_cast<unsigned*>(h->host_small_dev), h->validate_done(),
+                                      h->mirror_flag()}));
   // the new row from the few rows that can attain it (one GPU, int8 mirror
   // valid): on the side stream, launched before the validation read so it
   // overlaps the host round trip (it writes scratch only; a rejected call
@@ -884,17 +1085,11 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
     }
   }
   unsigned* herr = reinterpret_cast<unsigned*>(h->host_small);
-  {
-    ReadSet rs{};
-    rs.add(&h->ctr()->err, sizeof(unsigned));
-    rs.add(h->wmin_dev(), sizeof(unsigned));
-    rs.add(h->mirror_flag(), sizeof(unsigned));
-    CK(readback(rs, h->host_small_dev, h->st));
-  }
   CKR(cudaStreamSynchronize(h->st));
   h->mirror_hint = (herr[2] & 1u) == 0u;
   if (*herr) {
     if (srow) CKR(cudaStreamSynchronize(h->st2));   // the scratch is free again
+    CK(add_init(as, &h->ctr()->err, h->wmin_dev(), h->st));   // reset for the next add
     return fail(h, APSP_E_INVAL, "add_node: %s",
                 (*herr & 2) ? "undirected graph needs out_w == in_w" : "negative or NaN weight");
   }
@@ -970,7 +1165,7 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
      rank1<T>(h->Dl<T>(), ld, r, n, ceff, row, nullptr, nullptr, h->rank1_bytes(), h->sr, h->mirror<T>(),
               h->st, mirror8_known_valid(h) ? 0 : 1));
   CK(addnode_write<T>(h->Dl<T>(), ld, r, n, x, h->local(x) ? 1 : 0, col, row, h->WT<T>(), ld, ow,
-                      iw, h->mirror<T>(), h->st));
+                      iw, h->mirror<T>(), h->st, as, &h->ctr()->err, h->wmin_dev()));
   // (addnode_write mirrored the new row / column)
   CKR(cudaStreamWaitEvent(h->st, h->ev_join, 0));   // shortlist upkeep (side stream) done
   h->n = n + 1;
@@ -1442,12 +1637,17 @@ namespace {
 
 // Frees everything a handle owns (never the caller's memory).
 void release_handle(apsp_handle* h) {
+  for (auto& g : h->fw_graphs) cudaGraphExecDestroy(g.second.exec);
+  if (h->stcap) cudaStreamDestroy(h->stcap);
   for (auto e : h->ev_pool) cudaEventDestroy(e);
   for (auto& r : h->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   if (h->st2) { cudaStreamSynchronize(h->st2); cudaStreamDestroy(h->st2); }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->ev_row) cudaEventDestroy(h->ev_row);
+  if (h->stc) { cudaStreamSynchronize(h->stc); cudaStreamDestroy(h->stc); }
+  if (h->ev_pan) cudaEventDestroy(h->ev_pan);
+  if (h->ev_bc) cudaEventDestroy(h->ev_bc);
   delete h->comm;
   if (h->host_small) cudaFreeHost(h->host_small);
   delete h;
@@ -1500,6 +1700,12 @@ apsp_status create_impl(apsp_handle** out, apsp_dtype dtype, int directed, int64
     delete h;
     return APSP_E_CUDA;
   }
+  if (world > 1 && (cudaStreamCreateWithFlags(&h->stc, cudaStreamNonBlocking) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&h->ev_pan, cudaEventDisableTiming) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&h->ev_bc, cudaEventDisableTiming) != cudaSuccess)) {
+    release_handle(h);
+    return APSP_E_CUDA;
+  }
   if (world > 1) {
     int err = 0;
     h->comm = group ? make_local_comm(group, rank) : make_nccl_comm(nccl_id, world, rank, &err);
@@ -1513,6 +1719,7 @@ apsp_status create_impl(apsp_handle** out, apsp_dtype dtype, int directed, int64
     using T = decltype(z);
     CKR(cudaMemsetAsync(h->ws + h->plan.off_small, 0, 512, h->st));   // counters, flags
     CKR(cudaMemsetAsync(h->mirror_flag(), 0xff, sizeof(unsigned), h->st));   // no mirror yet
+    CKR(cudaMemsetAsync(h->heavy_x(), 0x7f, sizeof(int32_t) * (size_t)kHeavy * h->ld, h->st));   // X: "INF"
     CK(fill<T>(h->WT<T>(), (int64_t)cap * h->ld, Tr<T>::inf(), h->st));
     CKR(cudaMemsetAsync(&h->ctr()->err, 0, sizeof(unsigned), h->st));
     CKR(cudaMemsetAsync(h->wmin_dev(), 0xff, sizeof(unsigned), h->st));
@@ -1530,6 +1737,7 @@ apsp_status create_impl(apsp_handle** out, apsp_dtype dtype, int directed, int64
     CKR(cudaStreamSynchronize(h->st));
     if (*herr) return fail(h, APSP_E_INVAL, "create: W has %s", (*herr & 4) ? "a nonzero diagonal" : "a negative/NaN weight");
     h->wmin_bits = herr[1];
+    CK(add_init(h->add_scratch(), &h->ctr()->err, h->wmin_dev(), h->st));   // the first add's scratch
     return APSP_OK;
   });
   if (s != APSP_OK) {
@@ -1627,6 +1835,10 @@ apsp_status apsp_set_option(apsp_handle* h, apsp_option opt, double value) {
     case APSP_OPT_FUSED:
       if (value != 0 && value != 1) return APSP_E_INVAL;
       h->fused = (int)value;
+      return APSP_OK;
+    case APSP_OPT_HEAVY:
+      if (!(value >= -1) || value != (double)(int64_t)value || value > 1e9) return APSP_E_INVAL;
+      h->heavy_min = (int)value;
       return APSP_OK;
     case APSP_OPT_ROW_DELTA:
       if (!(value >= 0) || value > 1) return APSP_E_INVAL;

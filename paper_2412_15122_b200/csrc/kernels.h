@@ -76,12 +76,20 @@ struct Rows {
   int64_t lo, hi, row0;
 };
 
+// validate_vec's optional read for the host: the last block writes host[0] =
+// *err, host[1] = *wmin_bits, host[2] = *mflag (mapped host memory); done is
+// a device counter left at 0
+struct ValidateReadback {
+  unsigned* host;
+  unsigned* done;
+  const unsigned* mflag;
+};
 template <typename T>
 // (inb, in2b, outb): an optional second vector validated in the same launch
 cudaError_t validate_vec(const T* in, const T* in2, int64_t n, int64_t npad, T* out,
                          unsigned int* err, unsigned* wmin_bits, cudaStream_t st, const T* inb = nullptr,
                          const T* in2b = nullptr, T* outb = nullptr, unsigned long long* argmin0 = nullptr,
-                         unsigned* min1 = nullptr);
+                         unsigned* min1 = nullptr, ValidateReadback rb = ValidateReadback{nullptr, nullptr, nullptr});
 template <typename T>
 cudaError_t transpose_in(const T* W, int64_t ldw, int64_t n, T* WT, int64_t ldt, unsigned int* err,
                          unsigned* wmin_bits, cudaStream_t st);
@@ -130,10 +138,12 @@ template <typename T>
 cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, const T* c2,
                   const T* rv2, unsigned long long* bytes_read, int sr, Mirror M, cudaStream_t st,
                   int twin = 1);
+// (it also resets the add's scratch words — as, *err, *wmin — for the next add)
 template <typename T>
 cudaError_t addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xlocal,
                           const T* col, const T* row, T* WT, int64_t ldw, const T* ow,
-                          const T* iw, Mirror M, cudaStream_t st);
+                          const T* iw, Mirror M, cudaStream_t st, const AddScratch& as, unsigned* err,
+                          unsigned* wmin);
 // mode 0: mark rows with flags (anyrow); 1: append the need_update_list
 // (pairs to prow/pcol, rowcnt, ctr->total/overflow; plb unused); 2: reset
 // flagged entries to W' in place
@@ -220,6 +230,32 @@ cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw
                         const int* gprow, const int* gpcol, const T* glb, const unsigned char* gfull,
                         int64_t nopen, int sr, const DetectCounters* dc, cudaStream_t st,
                         Mirror M = Mirror{nullptr, nullptr, nullptr});
+// The sparse rounds' buffers: per-round frontier counts chg + k * stride
+// (k = round % 4; the total at [cap]), frontier lists fcol[round & 1]; the
+// cooperative kernel reports rounds run and the last round's total.
+struct RoundBufs {
+  int* chg; int64_t stride; int64_t cap;
+  int* fcol[2];
+  int* rounds_run; int* last_total;
+  const int* heavy;   // heavy rows the rounds skip (heavy_select's set), or null
+  int* bigq;          // queue of long-frontier pairs (capacity: the open-list size)
+  int* bigq_ctr;      // 4 ints: (tail, head) per round parity; zero on entry
+};
+// heavy rows (one GPU): hs[0] = rows selected, hs[1..kHeavy]
+// their ids (hs[0] zeroed with the counters); x = kHeavy rows of ldx keys,
+// 0x7F-filled at creation and reset by heavy_rows after each use
+constexpr int kHeavy = 32;
+cudaError_t heavy_select(const int* ocnt, int64_t rows, int thr, int* hs, cudaStream_t st);
+template <typename T>
+cudaError_t heavy_rows(T* D, int64_t ld, int64_t n, const T* WT, int64_t ldw, const int* hs, int* x, int64_t ldx,
+                       int64_t skip, int sr, cudaStream_t st, Mirror M);
+// rounds r0 .. r1 - 1 in one cooperative launch (grid barriers between rounds),
+// stopping at convergence
+template <typename T>
+cudaError_t sparse_rounds_coop(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, const int* gprow,
+                               const int* gpcol, const T* glb, int64_t nopen, const int64_t* rowoff, const int* ocnt,
+                               const int* ocol, const RoundBufs& rb, int r0, int r1, int* any, int sr,
+                               const DetectCounters* dc, cudaStream_t st, unsigned* rowkey, T wmin, Mirror M);
 template <typename T>
 cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw,
                          const int* gprow, const int* gpcol, const T* glb, int64_t nopen,
@@ -332,7 +368,7 @@ cudaError_t update_prep(const T* D, int64_t ld, Rows r, int64_t col, T add, T* c
                         cudaStream_t st);
 // the counters pack_counters packs, plus the mirror flag, into mapped host memory
 cudaError_t pack_to_host(const DetectCounters* c, const int* any, const unsigned* mflag, void* host_dev,
-                         cudaStream_t st);
+                         cudaStream_t st, const int* rounds = nullptr /* -> host word 14 */);
 double microbench(int kind, void* buf, size_t bytes, cudaStream_t st);   // microbench.cu
 int num_sms();
 // ---------------- fused.cu ----------------

@@ -23,6 +23,8 @@
 // own row until no entry changes.  A fixpoint of these upper bounds is the
 // exact distance.  Rows read only their own D row and the
 // read-only WT / shortlists, so rows never race and no grid sync is needed.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "mirror.cuh"
@@ -664,11 +666,6 @@ cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const 
 // stops at the first batch whose bound reaches lb (certified); after
 // kPhaseABatches batches the pair is left open for A2 / B / the rounds.
 constexpr int kPhaseABatches = 9;   // sorted positions 0-71
-static int pa_tune(const char* name, int dflt) {   // measurement override (read once)
-  const char* v = getenv(name);
-  const int x = v ? atoi(v) : 0;
-  return x > 0 ? x : dflt;
-}
 #ifndef PA_MINB
 #define PA_MINB 4   // 4 CTAs per SM (64 registers, no spills): latency-bound, occupancy wins
 #endif
@@ -812,7 +809,9 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_aq(T* D, int64_t 
     if (M.m8 && (*(volatile unsigned*)M.flag & 1u) == 0u) M8 = M.m8;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  constexpr int64_t CH = 32 * kPAChunk;
+  // chunk: up to 32 * kPAChunk pairs, fewer when the list would leave warps
+  // idle (a multiple of 32, >= 32: every lane starts with a pair)
+  const int64_t CH = min((int64_t)(32 * kPAChunk), max((int64_t)32, ((npairs + nw - 1) / nw + 31) / 32 * 32));
   for (int64_t c0 = wid * CH; c0 < npairs; c0 += nw * CH) {
     const int64_t cend = c0 + CH < npairs ? c0 + CH : npairs;
     int64_t next = c0;   // warp-uniform
@@ -949,8 +948,11 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
       k_sparse_phase_a<T, SRV, TWOV><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, srow, scol,   \
                                                            npairs, c1, r1, c2, r2, tau, ol, ctr, M, nb, list); \
   } while (0)
-  static const int nb = std::min(kSL / 8, pa_tune("APSP_TUNE_PA_BATCHES", kPhaseABatches));
-  static const bool queue = pa_tune("APSP_TUNE_PA_QUEUE", 1) == 1;   // 2: the one-pair-per-lane kernel
+  constexpr int nb = std::min(kSL / 8, kPhaseABatches);
+#ifndef PA_QUEUE
+#define PA_QUEUE 1   // 0: the one-pair-per-lane kernel (measured slower)
+#endif
+  constexpr bool queue = PA_QUEUE == 1;
   const bool two = c2 != nullptr;
   if (sr) { if (two) PA(1, true); else PA(1, false); }
   else { if (two) PA(0, true); else PA(0, false); }
@@ -961,6 +963,9 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
 // ---------------------------------------------------------------------------
 // phase B: full scan (*) for open pairs marked 2, early exit at the lower bound
 // ---------------------------------------------------------------------------
+// One CTA per pair: the scan of a row is a latency chain (one warp per pair
+// took ~1 us per 64 vectors: a few pairs at n = 65536 ran 0.3 ms), so all 8
+// warps split it, with a block-wide early-exit test every 4 steps.
 template <typename T, int SR>
 __global__ void __launch_bounds__(256) k_sparse_full(T* D, int64_t ld, int64_t row0,
                                                      const T* __restrict__ WT, int64_t ldw,
@@ -969,23 +974,22 @@ __global__ void __launch_bounds__(256) k_sparse_full(T* D, int64_t ld, int64_t r
                                                      const T* __restrict__ glb,
                                                      const unsigned char* __restrict__ gfull,
                                                      int64_t nopen, const DetectCounters* dc, Mirror M) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ T wm[8];
   unsigned mbits = 0;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t n4 = (n + 3) / 4;
   nopen = device_count(dc, nopen, 1);
   const T I = Tr<T>::inf();
-  for (int64_t p = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); p < nopen;
-       p += nw) {
-    if (gfull[p] != 2) continue;
+  for (int64_t p = blockIdx.x; p < nopen; p += gridDim.x) {
+    if (gfull[p] != 2) continue;   // block-uniform
     const int64_t i = gprow[p], j = gpcol[p];
     const T lb = glb[p];
     T* Drow = D + (i - row0) * ld;
     const T* Wrow = WT + j * ldw;
     T acc = I;
-    // warp-uniform trip count: the early-exit test below shuffles across lanes
-    for (int64_t base = 0, iter = 1; base < n4; base += 64, ++iter) {
-      const int64_t q0 = base + lane, q1 = base + 32 + lane;
+    // block-uniform trip count: the early-exit test below synchronises the CTA
+    for (int64_t base = 0, iter = 1; base < n4; base += 512, ++iter) {
+      const int64_t q0 = base + threadIdx.x, q1 = base + 256 + threadIdx.x;
       Vec4<T> d0{I, I, I, I}, w0{I, I, I, I}, d1{I, I, I, I}, w1{I, I, I, I};
       if (q0 < n4) {
         d0 = mask_tail<T>(ld4_cg<T>(Drow + 4 * q0), 4 * q0, n);
@@ -999,16 +1003,31 @@ __global__ void __launch_bounds__(256) k_sparse_full(T* D, int64_t ld, int64_t r
       acc = Tr<T, SR>::relax(acc, d0.z, w0.z); acc = Tr<T, SR>::relax(acc, d0.w, w0.w);
       acc = Tr<T, SR>::relax(acc, d1.x, w1.x); acc = Tr<T, SR>::relax(acc, d1.y, w1.y);
       acc = Tr<T, SR>::relax(acc, d1.z, w1.z); acc = Tr<T, SR>::relax(acc, d1.w, w1.w);
-      if ((iter & 7) == 0 && Tr<T>::at_lb(warp_min<T>(acc), lb)) break;   // reached the lower bound
-    }
-    acc = warp_min<T>(acc);
-    if (lane == 0) {
-      T old = Drow[j];
-      if (acc < old) {
-        Drow[j] = acc;
-        if (M.m || M.m8) mbits |= mput(M, (i - row0) * ld + j, acc);
+      if ((iter & 3) == 0 && base + 512 < n4) {   // reached the lower bound?
+        const T m = warp_min<T>(acc);
+        if (lane == 0) wm[warp] = m;
+        __syncthreads();
+        T b = wm[0];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) b = Tr<T>::mn(b, wm[w]);
+        __syncthreads();
+        if (Tr<T>::at_lb(b, lb)) break;
       }
     }
+    acc = warp_min<T>(acc);
+    if (lane == 0) wm[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      T b = wm[0];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) b = Tr<T>::mn(b, wm[w]);
+      const T old = Drow[j];
+      if (b < old) {
+        Drow[j] = b;
+        if (M.m || M.m8) mbits |= mput(M, (i - row0) * ld + j, b);
+      }
+    }
+    __syncthreads();   // wm is reused by the next pair
   }
   if (M.m || M.m8) mirror_post(M, mbits);
 }
@@ -1017,7 +1036,7 @@ cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw
                         const int* gprow, const int* gpcol, const T* glb, const unsigned char* gfull,
                         int64_t nopen, int sr, const DetectCounters* dc, cudaStream_t st, Mirror M) {
   if (nopen <= 0) return cudaSuccess;
-  int grid = (int)std::min<int64_t>(cdiv(nopen, 8), (int64_t)num_sms() * 8);
+  int grid = (int)std::min<int64_t>(nopen, (int64_t)num_sms() * 8);
   if (sr)
     k_sparse_full<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, n, gprow, gpcol, glb, gfull, nopen, dc, M);
   else
@@ -1062,6 +1081,155 @@ cudaError_t open_rowmin(const T* D, int64_t ld, int64_t row0, const int* gprow, 
   return cudaGetLastError();
 }
 
+// One round (see the rounds' description at recompute(), apsp_warm.cu): each
+// open pair (i, j) of a row whose entries changed last round is relaxed
+// through those entries; a lower value is written and becomes part of the
+// next round's frontier.
+constexpr int kRoundLocal = 16;   // frontier length a single lane relaxes on its own
+// The whole warp relaxes pair (i, j) (current value cur) through the cnt
+// frontier entries of row i; a lower value is written and joins the next
+// round's frontier.
+template <typename T, int SR>
+__device__ __forceinline__ unsigned round_pair_warp(T* D, int64_t ld, int64_t row0, const T* __restrict__ WT,
+                                                    int64_t ldw, const int64_t* __restrict__ rowoff,
+                                                    const int* fcol_in, int* fcnt_out, int* ftot_out, int* fcol_out,
+                                                    int* any, unsigned* rowkey, const Mirror& M, int64_t pi,
+                                                    int64_t pj, int pc, T pcur, int lane) {
+  unsigned mbits = 0;
+  T* Drow = D + (pi - row0) * ld;
+  const T* Wrow = WT + pj * ldw;
+  const int* fl = fcol_in + rowoff[pi];
+  T acc = Tr<T>::inf();
+  int t = lane;
+  for (; t + 32 < pc; t += 64) {   // two gathers in flight per lane
+    const int64_t m0 = *(volatile const int*)(fl + t), m1 = *(volatile const int*)(fl + t + 32);
+    const T d0 = *(volatile T*)(Drow + m0), d1 = *(volatile T*)(Drow + m1);
+    const T w0 = Wrow[m0], w1 = Wrow[m1];
+    acc = Tr<T, SR>::relax(Tr<T, SR>::relax(acc, d0, w0), d1, w1);
+  }
+  if (t < pc) {
+    const int64_t m = *(volatile const int*)(fl + t);
+    acc = Tr<T, SR>::relax(acc, *(volatile T*)(Drow + m), Wrow[m]);
+  }
+  acc = warp_min<T>(acc);
+  if (lane == 0 && acc < pcur) {
+    Drow[pj] = acc;
+    if (M.m || M.m8) mbits |= mput(M, (pi - row0) * ld + pj, acc);
+    fcol_out[rowoff[pi] + atomicAdd(fcnt_out + pi, 1)] = (int)pj;   // j changed: next round's frontier
+    atomicAdd(ftot_out, 1);
+    if (rowkey) atomicMax(rowkey + pi, open_key<T>(acc));
+    *any = 1;
+  }
+  return mbits;
+}
+
+// One round over the open pairs: each lane screens one pair of its warp's 32
+// (row changed last round, not heavy, not at its bound, not provably final);
+// a pair whose row's frontier is short is relaxed by its lane alone, a long
+// one by the whole warp — right away, or (bigq != null) appended to a queue
+// that every warp of the grid drains after a barrier (round_big_drain), so a
+// few long rows do not serialise on the warps that happen to hold them.
+template <typename T, int SR>
+__device__ __forceinline__ unsigned sparse_round_body(T* D, int64_t ld, int64_t row0, const T* __restrict__ WT,
+                                                      int64_t ldw, const int* __restrict__ gprow,
+                                                      const int* __restrict__ gpcol, const T* __restrict__ glb,
+                                                      int64_t nopen, const int64_t* __restrict__ rowoff,
+                                                      const int* fcnt_in, const int* fcol_in, int* fcnt_out,
+                                                      int* ftot_out, int* fcol_out, int* any, unsigned* rowkey,
+                                                      T wmin, const Mirror& M, const int* hrow = nullptr,
+                                                      int hc = 0, int* bigq = nullptr, int* bigq_tail = nullptr) {
+  unsigned mbits = 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t p0 = (blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; p0 < nopen;
+       p0 += nw * 32) {
+    const int64_t p = p0 + lane;
+    int i = 0, j = 0, cnt = 0;
+    T cur = Tr<T>::inf();
+    bool need = false;
+    if (p < nopen) {
+      i = gprow[p];
+      cnt = *(volatile const int*)(fcnt_in + i);   // entries of row i changed last round
+      bool heavy = false;   // a heavy row: resolved after the rounds (heavy_rows)
+      for (int q = 0; q < hc; ++q) heavy |= hrow[q] == i;
+      if (cnt != 0 && !heavy) {
+        j = gpcol[p];
+        cur = *(volatile T*)(D + (int64_t)(i - row0) * ld + j);   // only this pair's warp writes it
+        // at its lower bound: final; or no open entry of the row can lower
+        // it: every one is >= the row's smallest open value and every
+        // weight >= wmin
+        need = !Tr<T>::at_lb(cur, glb[p]) &&
+               !(rowkey && cur <= Tr<T, SR>::add(open_min<T>(*(volatile unsigned*)(rowkey + i)), wmin));
+      }
+    }
+    const bool local = need && cnt <= kRoundLocal;
+    if (local) {
+      T* Drow = D + (int64_t)(i - row0) * ld;
+      const T* Wrow = WT + (int64_t)j * ldw;
+      const int* fl = fcol_in + rowoff[i];
+      T acc = Tr<T>::inf();
+      for (int t = 0; t < cnt; ++t) {
+        const int64_t m = *(volatile const int*)(fl + t);
+        acc = Tr<T, SR>::relax(acc, *(volatile T*)(Drow + m), Wrow[m]);
+      }
+      if (acc < cur) {
+        Drow[j] = acc;
+        if (M.m || M.m8) mbits |= mput(M, (int64_t)(i - row0) * ld + j, acc);
+        fcol_out[rowoff[i] + atomicAdd(fcnt_out + i, 1)] = j;   // j changed: next round's frontier
+        atomicAdd(ftot_out, 1);
+        if (rowkey) atomicMax(rowkey + i, open_key<T>(acc));
+        *any = 1;
+      }
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, need && !local);
+    if (bigq) {
+      if (todo) {   // one atomic per warp
+        int base = 0;
+        if (lane == 0) base = atomicAdd(bigq_tail, __popc(todo));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (need && !local) bigq[base + __popc(todo & ((1u << lane) - 1))] = (int)p;
+      }
+      continue;
+    }
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int64_t pi = __shfl_sync(0xffffffffu, i, src), pj = __shfl_sync(0xffffffffu, j, src);
+      const int pc = __shfl_sync(0xffffffffu, cnt, src);
+      const T pcur = __shfl_sync(0xffffffffu, cur, src);
+      mbits |= round_pair_warp<T, SR>(D, ld, row0, WT, ldw, rowoff, fcol_in, fcnt_out, ftot_out, fcol_out, any,
+                                      rowkey, M, pi, pj, pc, pcur, lane);
+    }
+  }
+  return mbits;
+}
+
+// Drains the queue of long-frontier pairs sparse_round_body appended (after
+// a grid barrier): each warp takes the next pair with one atomic.
+template <typename T, int SR>
+__device__ __forceinline__ unsigned round_big_drain(T* D, int64_t ld, int64_t row0, const T* __restrict__ WT,
+                                                    int64_t ldw, const int* __restrict__ gprow,
+                                                    const int* __restrict__ gpcol, const int64_t* __restrict__ rowoff,
+                                                    const int* fcnt_in, const int* fcol_in, int* fcnt_out,
+                                                    int* ftot_out, int* fcol_out, int* any, unsigned* rowkey,
+                                                    const Mirror& M, const int* bigq, int tail, int* head) {
+  unsigned mbits = 0;
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    int k = 0;
+    if (lane == 0) k = atomicAdd(head, 1);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    if (k >= tail) break;
+    const int64_t p = bigq[k];
+    const int64_t i = gprow[p], j = gpcol[p];
+    const int cnt = *(volatile const int*)(fcnt_in + i);
+    const T cur = *(volatile T*)(D + (i - row0) * ld + j);
+    mbits |= round_pair_warp<T, SR>(D, ld, row0, WT, ldw, rowoff, fcol_in, fcnt_out, ftot_out, fcol_out, any,
+                                    rowkey, M, i, j, cnt, cur, lane);
+  }
+  return mbits;
+}
+
 template <typename T, int SR>
 __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t row0,
                                                       const T* __restrict__ WT, int64_t ldw,
@@ -1075,51 +1243,89 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
                                                       int* fcnt_out, int* ftot_out, int* fcol_out, int* any,
                                                       const DetectCounters* dc, unsigned* rowkey, T wmin,
                                                       Mirror M) {
-  unsigned mbits = 0;
   // an empty frontier (nothing changed last round): the round is a no-op
   if (ftot_in && *(volatile const int*)ftot_in == 0) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   nopen = device_count(dc, nopen, 1);
-  for (int64_t p = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); p < nopen;
-       p += nw) {
-    const int64_t i = gprow[p];
-    const int cnt = fcnt_in[i];
-    if (cnt == 0) continue;   // nothing in row i changed last round
-    const int64_t j = gpcol[p];
-    T* Drow = D + (i - row0) * ld;
-    T cur = Tr<T>::inf();
-    if (lane == 0) cur = *(volatile T*)(Drow + j);
-    cur = __shfl_sync(0xffffffffu, cur, 0);  // one value for the whole warp (others may write)
-    if (Tr<T>::at_lb(cur, glb[p])) continue;   // already at its lower bound: final
-    // no open entry of the row can lower it: every one is >= the row's
-    // smallest open value and every weight >= wmin
-    if (rowkey && cur <= Tr<T, SR>::add(open_min<T>(rowkey[i]), wmin)) continue;
-    const T* Wrow = WT + j * ldw;
-    const int* fl = fcol_in + rowoff[i];
-    T acc = Tr<T>::inf();
-    int t = lane;
-    for (; t + 32 < cnt; t += 64) {   // two gathers in flight per lane
-      const int64_t m0 = fl[t], m1 = fl[t + 32];
-      const T d0 = *(volatile T*)(Drow + m0), d1 = *(volatile T*)(Drow + m1);
-      const T w0 = Wrow[m0], w1 = Wrow[m1];
-      acc = Tr<T, SR>::relax(Tr<T, SR>::relax(acc, d0, w0), d1, w1);
+  const unsigned mbits = sparse_round_body<T, SR>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff, fcnt_in,
+                                                  fcol_in, fcnt_out, ftot_out, fcol_out, any, rowkey, wmin, M);
+  if (M.m || M.m8) mirror_post(M, mbits);
+}
+
+// Rounds r0 .. r1 - 1 in ONE cooperative launch, a grid-wide barrier between
+// rounds, stopping after the first round that changes nothing: no host round
+// trip per batch of rounds.  Buffers as the one-round kernel's: frontier
+// counts per round in chg[round % 4] (their totals at [cap]; rounds 0-3
+// zeroed by the caller, later ones here), frontier lists alternating between
+// fcol[0] / fcol[1]; round 0 reads the open lists (ocnt / ocol).  *rounds_run
+// receives the number of rounds executed; *last_total the last round's total.
+template <typename T, int SR>
+__global__ void __launch_bounds__(256) k_sparse_rounds_coop(T* D, int64_t ld, int64_t row0, const T* __restrict__ WT,
+                                                            int64_t ldw, const int* __restrict__ gprow,
+                                                            const int* __restrict__ gpcol, const T* __restrict__ glb,
+                                                            int64_t nopen, const int64_t* __restrict__ rowoff,
+                                                            const int* ocnt, const int* ocol, RoundBufs rb, int r0,
+                                                            int r1, int* any, const DetectCounters* dc,
+                                                            unsigned* rowkey, T wmin, Mirror M) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  nopen = device_count(dc, nopen, 1);
+  __shared__ int hrow[kHeavy];
+  const int hc = rb.heavy ? min(*(volatile const int*)rb.heavy, kHeavy) : 0;
+  if (threadIdx.x < hc) hrow[threadIdx.x] = rb.heavy[1 + threadIdx.x];
+  __syncthreads();
+  unsigned mbits = 0;
+  int round = r0;
+  for (; round < r1; ++round) {
+    const int o = round & 3, oi = (round + 3) & 3;
+    int* chg_o = rb.chg + (int64_t)o * rb.stride;
+    if (round >= 4) {   // this round's counts start at zero
+      for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e <= rb.cap; e += (int64_t)gridDim.x * blockDim.x)
+        chg_o[e] = 0;
+      grid.sync();
     }
-    if (t < cnt) {
-      const int64_t m = fl[t];
-      acc = Tr<T, SR>::relax(acc, *(volatile T*)(Drow + m), Wrow[m]);
-    }
-    acc = warp_min<T>(acc);
-    if (lane == 0 && acc < cur) {
-      Drow[j] = acc;
-      if (M.m || M.m8) mbits |= mput(M, (i - row0) * ld + j, acc);
-      fcol_out[rowoff[i] + atomicAdd(fcnt_out + i, 1)] = (int)j;   // j changed: next round's frontier
-      atomicAdd(ftot_out, 1);
-      if (rowkey) atomicMax(rowkey + i, open_key<T>(acc));
-      *any = 1;
+    const int* fin_c = round == 0 ? ocnt : rb.chg + (int64_t)oi * rb.stride;
+    const int* fin_l = round == 0 ? ocol : rb.fcol[(round & 1) ^ 1];
+    // the previous round changed nothing: converged (grid-uniform after the barrier)
+    if (round > 0 && *(volatile const int*)(fin_c + rb.cap) == 0) break;
+    // this round's queue counters (tail, head) at bq[2 (round & 1)]; the other
+    // pair is reset for the next round (nobody uses it now)
+    int* bq = rb.bigq_ctr + 2 * (round & 1);
+    if (blockIdx.x == 0 && threadIdx.x < 2) rb.bigq_ctr[2 * ((round + 1) & 1) + threadIdx.x] = 0;
+    mbits |= sparse_round_body<T, SR>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff, fin_c, fin_l, chg_o,
+                                      chg_o + rb.cap, rb.fcol[round & 1], any, rowkey, wmin, M, hrow, hc, rb.bigq,
+                                      bq);
+    grid.sync();
+    const int tail = *(volatile int*)bq;
+    if (tail > 0) {   // grid-uniform
+      mbits |= round_big_drain<T, SR>(D, ld, row0, WT, ldw, gprow, gpcol, rowoff, fin_c, fin_l, chg_o, chg_o + rb.cap,
+                                      rb.fcol[round & 1], any, rowkey, M, rb.bigq, tail, bq + 1);
+      grid.sync();
     }
   }
   if (M.m || M.m8) mirror_post(M, mbits);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *rb.rounds_run = round - r0;
+    // the last round that ran (or the one that found nothing): its total
+    const int last = round > r0 ? round - 1 : r0;
+    *rb.last_total = rb.chg[(int64_t)(last & 3) * rb.stride + rb.cap];
+  }
+}
+template <typename T>
+cudaError_t sparse_rounds_coop(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, const int* gprow,
+                               const int* gpcol, const T* glb, int64_t nopen, const int64_t* rowoff, const int* ocnt,
+                               const int* ocol, const RoundBufs& rb, int r0, int r1, int* any, int sr,
+                               const DetectCounters* dc, cudaStream_t st, unsigned* rowkey, T wmin, Mirror M) {
+  auto kern = sr ? k_sparse_rounds_coop<T, 1> : k_sparse_rounds_coop<T, 0>;
+  static int per_sm[2] = {0, 0};
+  int& bps = per_sm[sr ? 1 : 0];
+  if (!bps) {
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0));
+    if (bps <= 0) return cudaErrorInvalidConfiguration;
+  }
+  const int grid = std::min(bps, 2) * num_sms();
+  void* args[] = {&D, &ld, &row0, &WT, &ldw, &gprow, &gpcol, &glb, &nopen, &rowoff, &ocnt, &ocol,
+                  const_cast<RoundBufs*>(&rb), &r0, &r1, &any, &dc, &rowkey, &wmin, &M};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, 256, args, 0, st);
 }
 template <typename T>
 cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw,
@@ -1131,7 +1337,7 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
   // round 0 relaxes every open pair through its row's open entries; later
   // rounds only the pairs whose row changed (often none: a small grid keeps
   // the no-op round cheap)
-  int grid = (int)std::min<int64_t>(cdiv(nopen, 8), (int64_t)num_sms() * (ftot_in ? 2 : 8));
+  int grid = (int)std::min<int64_t>(cdiv(nopen, 256), (int64_t)num_sms() * (ftot_in ? 2 : 8));
   if (sr)
     k_sparse_round<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff,
                                                fcnt_in, ftot_in, fcol_in, fcnt_out, ftot_out, fcol_out, any,
@@ -1143,7 +1349,209 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// heavy rows (one GPU): a row with many open pairs is a large
+// single-source problem for the rounds, whose cost per round is the row's open
+// pairs x its frontier.  Its row of D' is taken instead from the other rows,
+// final once the rounds converged (every pair (i, j) of a row is resolved from
+// row i alone, so excluding the heavy rows does not delay the others): with H
+// the heavy rows and
+//   X_h[j] = min over m not in H of  W'[h][m] + D'[m][j]          (first hop)
+//   C      = shortest paths inside H over the edges W' between heavy nodes
+// every shortest h -> j path leaves H after a prefix inside H (at h', via a
+// first hop to a node outside H) or stays inside H (j in H), so
+//   D'[h][j] = min( min_h' C[h][h'] + X_h'[j],  C[h][j] if j in H ).
+// ---------------------------------------------------------------------------
+// rows with at least thr open pairs (the first kHeavy found)
+__global__ void k_heavy_select(const int* __restrict__ ocnt, int64_t rows, int thr, int* hs) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+    if (ocnt[i] >= thr) {
+      const int s = atomicAdd(hs, 1);
+      if (s < kHeavy) hs[1 + s] = (int)i;
+    }
+}
+cudaError_t heavy_select(const int* ocnt, int64_t rows, int thr, int* hs, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  k_heavy_select<<<(int)std::min<int64_t>(cdiv(rows, 256), 2 * num_sms()), 256, 0, st>>>(ocnt, rows, thr, hs);
+  return cudaGetLastError();
+}
+
+// X keys: atomicMin on the value's order-preserving bits (values >= 0); the
+// buffer holds "INF or above" between recomputes, clamped when read
+template <typename T>
+__device__ __forceinline__ T heavy_xval(int k) {
+  if (Tr<T>::kFloat) {
+    const float f = k >= 0x7F800000 ? __builtin_huge_valf() : __int_as_float(k);
+    return (T)f;
+  }
+  return (T)min(k, (int)Tr<T>::inf());
+}
+template <typename T>
+__device__ __forceinline__ int heavy_xkey(T v) {
+  int k;
+  memcpy(&k, &v, 4);
+  return k;
+}
+
+constexpr int kHxSlab = 32;   // rows m per staging step
+constexpr int kHxGroup = 8;   // heavy rows per X block (blockIdx.z: the group)
+// X_h[j] for a group of 8 selected rows h.  A block owns a 128-column stripe
+// (lane: 4 columns) and a range of rows m; its 8 warps take every 8th row,
+// the weights W'[h][m] of 32 rows at a time staged in shared memory; the
+// warps' partial minima are reduced in shared memory, then one atomicMin per
+// (h, column) per block.
+template <typename T, int SR>
+__global__ void __launch_bounds__(256) k_heavy_x(const T* __restrict__ D, int64_t ld, int64_t n,
+                                                 const T* __restrict__ WT, int64_t ldw, const int* __restrict__ hs,
+                                                 int* x, int64_t ldx, int64_t skip, int64_t slab) {
+  const int hc = min(hs[0], kHeavy);
+  const int g0 = blockIdx.z * kHxGroup;
+  if (g0 >= hc) return;
+  const int gc = min(kHxGroup, hc - g0);   // rows of this group
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int hrow[kHeavy];
+  __shared__ T w[kHxSlab][kHxGroup];
+  __shared__ T red[8][kHxGroup][128];
+  if (threadIdx.x < hc) hrow[threadIdx.x] = hs[1 + threadIdx.x];
+  __syncthreads();
+  const T I = Tr<T>::inf();
+  const int64_t c0 = blockIdx.x * 128 + 4 * lane;   // this lane's columns c0 .. c0+3
+  const int64_t m0 = blockIdx.y * slab, m1 = min(n, m0 + slab);
+  T acc[kHxGroup][4];
+#pragma unroll
+  for (int k = 0; k < kHxGroup; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[k][e] = I;
+  // thread (r, k) holds W'[h_k][m] of row m = b + r of the next stage
+  // (prefetched one stage ahead: the gathers overlap the D loads)
+  const int wr = threadIdx.x / kHxGroup, wk = threadIdx.x % kHxGroup;
+  auto wload = [&](int64_t b) -> T {
+    const int64_t m = b + wr;
+    bool out = m < m1 && m != skip && wk < gc;
+    for (int t = 0; t < hc; ++t) out &= hrow[t] != (int)m;   // m outside H
+    return out ? WT[m * ldw + hrow[g0 + wk]] : I;             // W'[h][m] (WT row m: in-edges of m)
+  };
+  T wnext = wload(m0);
+  for (int64_t b = m0; b < m1; b += kHxSlab) {
+    __syncthreads();
+    w[wr][wk] = wnext;
+    __syncthreads();
+    if (b + kHxSlab < m1) wnext = wload(b + kHxSlab);
+    if (c0 >= n) continue;
+    Vec4<T> d[kHxSlab / 8];
+#pragma unroll
+    for (int rr = 0; rr < kHxSlab / 8; ++rr) {
+      const int64_t m = b + rr * 8 + warp;
+      d[rr] = m < m1 ? mask_tail<T>(ld4<T>(D + m * ld + c0), c0, n) : Vec4<T>{I, I, I, I};
+    }
+#pragma unroll
+    for (int rr = 0; rr < kHxSlab / 8; ++rr) {
+      const int r = rr * 8 + warp;
+#pragma unroll
+      for (int k = 0; k < kHxGroup; ++k) {
+        if (k >= gc) break;
+        const T wv = w[r][k];
+        acc[k][0] = Tr<T, SR>::relax(acc[k][0], wv, d[rr].x);
+        acc[k][1] = Tr<T, SR>::relax(acc[k][1], wv, d[rr].y);
+        acc[k][2] = Tr<T, SR>::relax(acc[k][2], wv, d[rr].z);
+        acc[k][3] = Tr<T, SR>::relax(acc[k][3], wv, d[rr].w);
+      }
+    }
+  }
+  // reduce the 8 warps' partials, then one atomic per (h, column)
+#pragma unroll
+  for (int k = 0; k < kHxGroup; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) red[warp][k][4 * lane + e] = acc[k][e];
+  __syncthreads();
+  for (int o = threadIdx.x; o < kHxGroup * 128; o += blockDim.x) {
+    const int k = o / 128, cc = o % 128;
+    const int64_t j = blockIdx.x * 128 + cc;
+    if (k >= gc || j >= n) continue;
+    T v = red[0][k][cc];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) v = Tr<T>::mn(v, red[q][k][cc]);
+    if (v < I) atomicMin(x + (g0 + k) * ldx + j, heavy_xkey<T>(Tr<T>::sat(v)));
+  }
+}
+
+// D[h][j] := min(D[h][j], min_h' C[h][h'] + X_h'[j], C[h][j] if j in H); resets X
+template <typename T, int SR>
+__global__ void __launch_bounds__(256) k_heavy_fix(T* D, int64_t ld, int64_t n, const T* __restrict__ WT,
+                                                   int64_t ldw, const int* __restrict__ hs, int* x, int64_t ldx,
+                                                   int64_t skip, Mirror M) {
+  const int hc = min(hs[0], kHeavy);
+  if (hc == 0) return;
+  __shared__ int hrow[kHeavy];
+  __shared__ T C[kHeavy][kHeavy];
+  const T I = Tr<T>::inf();
+  if (threadIdx.x < hc) hrow[threadIdx.x] = hs[1 + threadIdx.x];
+  __syncthreads();
+  for (int e = threadIdx.x; e < hc * hc; e += blockDim.x) {
+    const int a = e / hc, b = e % hc;
+    C[a][b] = a == b ? T(0) : WT[(int64_t)hrow[b] * ldw + hrow[a]];   // W'[h_a][h_b]
+  }
+  // Floyd–Warshall inside H, in place (row and column k do not change in step k)
+  for (int k = 0; k < hc; ++k) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < hc * hc; e += blockDim.x) {
+      const int a = e / hc, b = e % hc;
+      C[a][b] = Tr<T>::sat(Tr<T, SR>::relax(C[a][b], C[a][k], C[k][b]));
+    }
+  }
+  __syncthreads();
+  unsigned mbits = 0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    T xb[kHeavy];
+#pragma unroll
+    for (int b = 0; b < kHeavy; ++b) {
+      if (b >= hc) break;
+      xb[b] = heavy_xval<T>(x[b * ldx + j]);
+      x[b * ldx + j] = 0x7F7F7F7F;   // INF again for the next recompute
+    }
+    if (j == skip) continue;
+    for (int a = 0; a < hc; ++a) {
+      T v = I;
+#pragma unroll
+      for (int b = 0; b < kHeavy; ++b) {
+        if (b >= hc) break;
+        v = Tr<T, SR>::relax(v, C[a][b], xb[b]);
+        if (hrow[b] == (int)j) v = Tr<T>::mn(v, C[a][b]);
+      }
+      v = Tr<T>::sat(v);
+      T* dp = D + (int64_t)hrow[a] * ld + j;
+      if (v < *dp) {
+        *dp = v;
+        if (M.m || M.m8) mbits |= mput(M, (int64_t)hrow[a] * ld + j, v);
+      }
+    }
+  }
+  if (M.m || M.m8) mirror_post(M, mbits);
+}
+
+template <typename T>
+cudaError_t heavy_rows(T* D, int64_t ld, int64_t n, const T* WT, int64_t ldw, const int* hs, int* x, int64_t ldx,
+                       int64_t skip, int sr, cudaStream_t st, Mirror M) {
+  if (n <= 0) return cudaSuccess;
+  const int gx = (int)cdiv(n, 128);   // 128-column stripes
+  // about 4 blocks per SM per group, row ranges of whole staging steps
+  const int64_t want = std::max<int64_t>(1, (int64_t)4 * num_sms() / gx);
+  const int64_t slab = cdiv(cdiv(n, want), kHxSlab) * kHxSlab;
+  const dim3 grid(gx, (unsigned)cdiv(n, slab), kHeavy / kHxGroup);
+  const int gf = (int)std::min<int64_t>(cdiv(n, 256), 2 * num_sms());
+  if (sr) {
+    k_heavy_x<T, 1><<<grid, 256, 0, st>>>(D, ld, n, WT, ldw, hs, x, ldx, skip, slab);
+    k_heavy_fix<T, 1><<<gf, 256, 0, st>>>(D, ld, n, WT, ldw, hs, x, ldx, skip, M);
+  } else {
+    k_heavy_x<T, 0><<<grid, 256, 0, st>>>(D, ld, n, WT, ldw, hs, x, ldx, skip, slab);
+    k_heavy_fix<T, 0><<<gf, 256, 0, st>>>(D, ld, n, WT, ldw, hs, x, ldx, skip, M);
+  }
+  return cudaGetLastError();
+}
+
 #define INST(T)                                                                                   \
+  template cudaError_t heavy_rows<T>(T*, int64_t, int64_t, const T*, int64_t, const int*, int*, int64_t, \
+                                     int64_t, int, cudaStream_t, Mirror);                          \
   template cudaError_t shortlist_build<T>(const T*, int64_t, int64_t, const int*, int64_t, int64_t, \
                                           int*, T*, T*, cudaStream_t);                            \
   template cudaError_t shortlist_add_bound<T>(int*, T*, T*, const T*, int64_t, int64_t,            \
@@ -1166,6 +1574,10 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
                                       int64_t, int, const DetectCounters*, cudaStream_t, Mirror);         \
   template cudaError_t open_rowmin<T>(const T*, int64_t, int64_t, const int*, const int*, int64_t,      \
                                       unsigned*, const DetectCounters*, cudaStream_t);             \
+  template cudaError_t sparse_rounds_coop<T>(T*, int64_t, int64_t, const T*, int64_t, const int*, const int*, \
+                                             const T*, int64_t, const int64_t*, const int*, const int*,      \
+                                             const RoundBufs&, int, int, int*, int, const DetectCounters*,    \
+                                             cudaStream_t, unsigned*, T, Mirror);                               \
   template cudaError_t sparse_round<T>(T*, int64_t, int64_t, const T*, int64_t, const int*,        \
                                        const int*, const T*, int64_t, const int64_t*, const int*,  \
                                        const int*, const int*, int*, int*, int*, int*, int,        \

@@ -72,7 +72,7 @@ __device__ __forceinline__ void wmin_fold(unsigned* wmin_bits, T v, bool valid) 
 template <typename T>
 __global__ void k_validate_vec(const T* in, const T* in2, int64_t n, int64_t npad, T* out,
                                unsigned int* err, unsigned* wmin_bits, const T* inb, const T* in2b,
-                               T* outb, unsigned long long* argmin0, unsigned* min1) {
+                               T* outb, unsigned long long* argmin0, unsigned* min1, ValidateReadback rb) {
   if (blockIdx.y == 1) { in = inb; in2 = in2b; out = outb; }   // the second vector of a pair
   // (argmin0: (value << 32 | index) of the first vector's minimum; min1: the
   // second vector's minimum — int32 add-node shortcut, values >= 0)
@@ -113,14 +113,31 @@ __global__ void k_validate_vec(const T* in, const T* in2, int64_t n, int64_t npa
     m1 = __reduce_min_sync(0xffffffffu, m1);
     if ((threadIdx.x & 31) == 0 && m1 != ~0u) atomicMin(min1, m1);
   }
+  if (rb.host) {   // the last block to finish writes the host's read (err, wmin, mirror flag)
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(rb.done, 1u) == gridDim.x * gridDim.y - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      __threadfence();
+      rb.host[0] = *(volatile unsigned*)err;
+      rb.host[1] = *(volatile unsigned*)wmin_bits;
+      rb.host[2] = rb.mflag ? *(volatile const unsigned*)rb.mflag : 0u;
+      *rb.done = 0u;
+      __threadfence_system();
+    }
+  }
 }
 template <typename T>
 cudaError_t validate_vec(const T* in, const T* in2, int64_t n, int64_t npad, T* out,
                          unsigned int* err, unsigned* wmin_bits, cudaStream_t st, const T* inb,
-                         const T* in2b, T* outb, unsigned long long* argmin0, unsigned* min1) {
+                         const T* in2b, T* outb, unsigned long long* argmin0, unsigned* min1, ValidateReadback rb) {
   const int grid = (int)std::min<int64_t>(cdiv(npad, 256), 4 * num_sms());
   k_validate_vec<T><<<dim3(grid, inb ? 2 : 1), 256, 0, st>>>(in, in2, n, npad, out, err, wmin_bits, inb, in2b,
-                                                            outb, argmin0, min1);
+                                                            outb, argmin0, min1, rb);
   return cudaGetLastError();
 }
 
@@ -298,14 +315,26 @@ struct Tiling {
   int64_t slab;     // rows per slab
   int64_t warps;
 };
-// Tuning override for the streaming tilings (warps per SM the grid targets),
-// from the environment (callers keep it in a static: read once); used only
-// to measure alternatives.
-static int tune_wps(const char* name, int dflt) {
-  const char* v = getenv(name);
-  const int x = v ? atoi(v) : 0;
-  return x > 0 ? x : dflt;
-}
+// Streaming tilings: warps per SM each grid targets (measured; compile-time
+// so that scripts/sweep*.sh can rebuild variants with -D)
+#ifndef ADDCOL_DELTA
+#define ADDCOL_DELTA 2     // add: S1 = {t : in[t] <= min in + ADDCOL_DELTA}
+#endif
+#ifndef P8_WPS
+#define P8_WPS 144         // add pass 1, int8 mirror
+#endif
+#ifndef P1_WPS
+#define P1_WPS 16          // add pass 1, int16 mirror
+#endif
+#ifndef R8_WPS
+#define R8_WPS 16          // rank-1, int8 mirror: one wave at 2 CTAs (16 warps) per SM
+#endif
+#ifndef DET_WPS
+#define DET_WPS 192        // detection, int32 / int16
+#endif
+#ifndef DET8_WPS
+#define DET8_WPS 128       // detection, int8 mirror
+#endif
 
 static Tiling make_tiling(int64_t n, int64_t rows, int max_slabs, int chunk_vec = CHUNK_VEC,
                           int warps_per_sm = 32) {
@@ -314,7 +343,9 @@ static Tiling make_tiling(int64_t n, int64_t rows, int max_slabs, int chunk_vec 
   t.nchunk = (int)cdiv(t.n4, chunk_vec);
   int64_t target = (int64_t)num_sms() * warps_per_sm;
   int64_t ns = std::max<int64_t>(1, target / t.nchunk);
-  ns = std::min<int64_t>(ns, std::max<int64_t>(1, rows));
+  // at least 16 rows per slab: a warp's ring setup and pivot loads are
+  // amortised over its rows (small n made 2-row slabs: BJ.c2's detection)
+  ns = std::min<int64_t>(ns, std::max<int64_t>(1, rows / 16));
   ns = std::min<int64_t>(ns, max_slabs);
   t.nslab = (int)ns;
   t.slab = cdiv(std::max<int64_t>(rows, 1), t.nslab);
@@ -1141,7 +1172,7 @@ cudaError_t addcol_g(const AddScratch& a, Rows r, const uint8_t* m8, int64_t ld,
                      int32_t* ceff, int32_t* mprime, int* fb_list, int32_t wmin, cudaStream_t st,
                      const uint8_t* mt, int64_t ldt) {
   const int g = (int)std::min<int64_t>(cdiv(n, 256), 2 * num_sms());
-  static const int delta = tune_wps("APSP_TUNE_ADDCOL_DELTA", 2);   // th = min in + delta (measured)
+  constexpr int delta = ADDCOL_DELTA;   // th = min in + delta (measured)
   k_addcol_sets<<<g, 256, 0, st>>>(a, iw, ow, tflag, n, delta, ulist, uaux, uaux + limit, limit);
   CUDA_TRY(cudaGetLastError());
   if (r.hi > r.lo && mt && limit <= kAddColMax && ((r.lo - r.row0) & 3) == 0 && (ldt & 3) == 0) {
@@ -1297,7 +1328,7 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
                           int* nslab_out, int max_slabs, int sr, Mirror M, const unsigned* uncertain,
                           int packed, cudaStream_t st, int colp, const unsigned* full) {
   const bool p8 = packed && !sr && M.m8 != nullptr;   // int8 mirror: 512-column chunks
-  static const int wps8 = tune_wps("APSP_TUNE_P8_WPS", 144), wps16 = tune_wps("APSP_TUNE_P1_WPS", 16);
+  constexpr int wps8 = P8_WPS, wps16 = P1_WPS;
   Tiling tl = p8 ? make_tiling(n, r.hi - r.lo, max_slabs, 128, wps8)
                  : make_tiling(n, r.hi - r.lo, max_slabs, P1_VEC, wps16);
   *nchunk_out = tl.nchunk;
@@ -1583,6 +1614,9 @@ __global__ void __launch_bounds__(256, 3) k_rank1(T* __restrict__ D, int64_t ld,
 // The int32 k_rank1 launched after it exits while the mirror is still valid;
 // if this pass wrote a distance >= 0x7F (mirror now off) the int32 pass runs
 // too — harmless, the update is idempotent.
+constexpr int kR8S = 4;   // rank-1 on the int8 mirror: ring stages (one 1 KB row each)
+using R8Ring = WarpRing<kR8S, 1, 1024>;
+constexpr int kR8Smem = 8 * (R8Ring::kBytes + kR8S * (int)sizeof(R1Meta));
 template <bool TWO>
 __global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, int64_t ld, Rows r, int64_t n,
                                                      Tiling tl, const int32_t* __restrict__ c,
@@ -1622,101 +1656,107 @@ __global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, in
     r2[q] = a;
     if (TWO) r2b[q] = b;
   }
-  const bool ok0 = g0 < n, ok1 = g0 + 512 < n;
   int64_t rows_read = 0;
   unsigned mbits = 0;
-  for (int64_t ib = i_lo; ib < i_hi; ib += 32) {
-    const int64_t il = ib + lane;
-    const int32_t cl = il < i_hi ? c[il] : I;
-    const int32_t cl2 = TWO ? (il < i_hi ? c2[il] : I) : I;
-    unsigned live = __ballot_sync(0xffffffffu, cl < I || (TWO && cl2 < I));   // rows that can change
-    while (live) {
-      constexpr int kR8 = 4;   // up to 4 live rows at a time: their loads fly together
-      int bs[kR8];
-      uint4 wv[kR8][2];
+  // the rows that can change (c[i] or c2[i] finite: LiveRows, one ballot per
+  // 32 rows, the next group's c loaded ahead) stream through a per-warp TMA
+  // ring: lane 0 bulk-copies the chunk's 1024 mirror bytes of each live row,
+  // kR8S - 1 rows ahead of the warp; the row id and its c values travel with
+  // the stage (R1Meta)
+  extern __shared__ __align__(128) uint8_t r8_raw[];
+  R8Ring ring;
+  const int warp = threadIdx.x >> 5;
+  ring.init(r8_raw + warp * R8Ring::kBytes, lane);
+  R1Meta* meta = reinterpret_cast<R1Meta*>(r8_raw + 8 * R8Ring::kBytes) + warp * kR8S;
+  const uint8_t* mchunk = M.m8 + (int64_t)chunk * 1024 - r.row0 * ld;   // + i * ld: row i's chunk
+  const unsigned cbytes = (unsigned)((min((int64_t)1024, n - (int64_t)chunk * 1024) + 15) & ~15);
+  LiveRows<int32_t, TWO> it;
+  it.init(c, c2, i_lo, i_hi, lane);
+  int issued = 0;
+  auto produce = [&]() {
+    int32_t ci, ci2;
+    const int64_t i = it.next(lane, &ci, &ci2);
+    if (i < 0) return;
+    if (lane == 0) meta[issued % kR8S] = R1Meta{i, ci, ci2};
+    ring.issue(issued, cbytes, lane, [&](int) { return mchunk + i * ld; });
+    ++issued;
+  };
+  for (int k = 0; k < kR8S - 1; ++k) produce();
+  for (int st = 0; st < issued; ++st) {
+    produce();
+    ring.wait(st);
+    const R1Meta mt = meta[st % kR8S];
+    const int64_t i = mt.i;
+    const int32_t ci = mt.c, ci2 = TWO ? mt.c2 : I;
+    const uint4* srow = reinterpret_cast<const uint4*>(ring.row(st, 0));
+    const uint4 wv[2] = {srow[lane], srow[32 + lane]};
+    ++rows_read;
+    int32_t* drow = D + (i - r.row0) * ld;
+    uint8_t* mrow = M.m8 + (i - r.row0) * ld;
 #pragma unroll
-      for (int t = 0; t < kR8; ++t) {
-        bs[t] = live ? __ffs(live) - 1 : -1;
-        if (live) live &= live - 1;
-        const uint8_t* mrow = M.m8 + (ib + max(bs[t], 0) - r.row0) * ld;
-        const bool v = bs[t] >= 0;
-        wv[t][0] = (v && ok0) ? mload8(reinterpret_cast<const uint16_t*>(mrow + g0)) : make_uint4(0, 0, 0, 0);
-        wv[t][1] = (v && ok1) ? mload8(reinterpret_cast<const uint16_t*>(mrow + g0 + 512)) : make_uint4(0, 0, 0, 0);
-      }
+    for (int g = 0; g < 2; ++g) {
+      const int64_t jg = g0 + 512 * g;
+      if (jg >= n) continue;
+      const uint4 wb = wv[g];
+      if (!has_inf) {
+        const uint32_t cw = (uint32_t)sat16(ci) * 0x10001u, cw2 = (uint32_t)sat16(ci2) * 0x10001u;
+        const uint4 lo = widen8(make_uint2(wb.x, wb.y)), hi = widen8(make_uint2(wb.z, wb.w));
+        const uint32_t d[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+        uint32_t o[8], diff = 0;
 #pragma unroll
-      for (int t = 0; t < kR8; ++t) {
-        if (bs[t] < 0) break;   // warp-uniform
-        const int64_t i = ib + bs[t];
-        const int32_t ci = __shfl_sync(0xffffffffu, cl, bs[t]);
-        const int32_t ci2 = TWO ? __shfl_sync(0xffffffffu, cl2, bs[t]) : I;
-        ++rows_read;
-        int32_t* drow = D + (i - r.row0) * ld;
-        uint8_t* mrow = M.m8 + (i - r.row0) * ld;
+        for (int q = 0; q < 8; ++q) {
+          o[q] = __viaddmin_s16x2(cw, r2[8 * g + q], d[q]);
+          if (TWO) o[q] = __viaddmin_s16x2(cw2, r2b[8 * g + q], o[q]);
+          diff |= o[q] ^ d[q];
+        }
+        if (!diff) continue;
+        if (jg + 16 <= n) {   // rewrite the half: 64 bytes of D, 16 mirror bytes
+          int4* dst = reinterpret_cast<int4*>(drow + jg);
+          uint32_t mw[4];
+          uint32_t big = 0;
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          const int64_t jg = g0 + 512 * g;
-          const uint4 wb = wv[t][g];
-          if (!has_inf) {
-            const uint32_t cw = (uint32_t)sat16(ci) * 0x10001u, cw2 = (uint32_t)sat16(ci2) * 0x10001u;
-            const uint4 lo = widen8(make_uint2(wb.x, wb.y)), hi = widen8(make_uint2(wb.z, wb.w));
-            const uint32_t d[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-            uint32_t o[8], diff = 0;
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t a = o[2 * q], b = o[2 * q + 1];
+            dst[q] = make_int4((int)(a & 0xFFFFu), (int)(a >> 16), (int)(b & 0xFFFFu), (int)(b >> 16));
+            const uint32_t sa = __vmins2(a, 0x007F007Fu), sb = __vmins2(b, 0x007F007Fu);   // sat8
+            mw[q] = __byte_perm(sa, sb, 0x6420);
+            big |= __vcmpgeu2(a, 0x007F007Fu) | __vcmpgeu2(b, 0x007F007Fu);
+          }
+          *reinterpret_cast<uint4*>(mrow + jg) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+          if (big) mbits |= kMirrorOff;   // a distance >= 0x7F: the int8 mirror is no longer exact
+          if (M.mt) {   // the changed bytes into the transposed copy
+            const uint32_t ow[4] = {wb.x, wb.y, wb.z, wb.w};
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              o[q] = __viaddmin_s16x2(cw, r2[8 * g + q], d[q]);
-              if (TWO) o[q] = __viaddmin_s16x2(cw2, r2b[8 * g + q], o[q]);
-              diff |= o[q] ^ d[q];
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t x = mw[q] ^ ow[q];
+              if (!x) continue;
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if ((x >> (8 * e)) & 0xFFu) mput_t(M, i - r.row0, jg + 4 * q + e, (uint8_t)(mw[q] >> (8 * e)));
             }
-            if (!diff) continue;
-            if (jg + 16 <= n) {   // rewrite the half: 64 bytes of D, 16 mirror bytes
-              int4* dst = reinterpret_cast<int4*>(drow + jg);
-              uint32_t mw[4];
-              uint32_t big = 0;
+          }
+        } else {   // the row's ragged end: element stores below n
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const uint32_t a = o[2 * q], b = o[2 * q + 1];
-                dst[q] = make_int4((int)(a & 0xFFFFu), (int)(a >> 16), (int)(b & 0xFFFFu), (int)(b >> 16));
-                const uint32_t sa = __vmins2(a, 0x007F007Fu), sb = __vmins2(b, 0x007F007Fu);   // sat8
-                mw[q] = __byte_perm(sa, sb, 0x6420);
-                big |= __vcmpgeu2(a, 0x007F007Fu) | __vcmpgeu2(b, 0x007F007Fu);
-              }
-              *reinterpret_cast<uint4*>(mrow + jg) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
-              if (big) mbits |= kMirrorOff;   // a distance >= 0x7F: the int8 mirror is no longer exact
-              if (M.mt) {   // the changed bytes into the transposed copy
-                const uint32_t ow[4] = {wb.x, wb.y, wb.z, wb.w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const uint32_t x = mw[q] ^ ow[q];
-                  if (!x) continue;
-#pragma unroll
-                  for (int e = 0; e < 4; ++e)
-                    if ((x >> (8 * e)) & 0xFFu) mput_t(M, i - r.row0, jg + 4 * q + e, (uint8_t)(mw[q] >> (8 * e)));
-                }
-              }
-            } else {   // the row's ragged end: element stores below n
-#pragma unroll
-              for (int e = 0; e < 16; ++e)
-                if (jg + e < n) {
-                  const int32_t v = (int32_t)((o[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
-                  drow[jg + e] = v;
-                  mbits |= mput(M, (i - r.row0) * ld + jg + e, v);
-                }
+          for (int e = 0; e < 16; ++e)
+            if (jg + e < n) {
+              const int32_t v = (int32_t)((o[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
+              drow[jg + e] = v;
+              mbits |= mput(M, (i - r.row0) * ld + jg + e, v);
             }
-          } else {   // INF entries present: exact int32 per entry
-            const uint32_t wd[4] = {wb.x, wb.y, wb.z, wb.w};
+        }
+      } else {   // INF entries present: exact int32 per entry
+        const uint32_t wd[4] = {wb.x, wb.y, wb.z, wb.w};
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const int64_t j = jg + e;
-              if (j >= n) break;
-              const int32_t d8 = (int32_t)((wd[e >> 2] >> (8 * (e & 3))) & 0xFFu);
-              const int32_t dv = d8 == kSat8i ? I : d8;
-              int32_t nv = min(I, ci + rv[j]);
-              if (TWO) nv = min(nv, min(I, ci2 + rv2[j]));
-              if (nv < dv) {
-                drow[j] = nv;
-                mbits |= mput(M, (i - r.row0) * ld + j, nv);
-              }
-            }
+        for (int e = 0; e < 16; ++e) {
+          const int64_t j = jg + e;
+          if (j >= n) break;
+          const int32_t d8 = (int32_t)((wd[e >> 2] >> (8 * (e & 3))) & 0xFFu);
+          const int32_t dv = d8 == kSat8i ? I : d8;
+          int32_t nv = min(I, ci + rv[j]);
+          if (TWO) nv = min(nv, min(I, ci2 + rv2[j]));
+          if (nv < dv) {
+            drow[j] = nv;
+            mbits |= mput(M, (i - r.row0) * ld + j, nv);
           }
         }
       }
@@ -1745,13 +1785,20 @@ cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, 
   int grid = (int)cdiv(tl.warps, 8);
   if constexpr (std::is_same<T, int32_t>::value) {
     if (!sr && M.m8) {   // the int8 twin first (the int32 kernel then exits while M stays valid)
-      static const int wps = tune_wps("APSP_TUNE_R8_WPS", 16);   // (measured: 16 -> 29 us, 32 -> 32 us at BJ.c4)
+      constexpr int wps = R8_WPS;   // one wave at 2 CTAs (16 warps) per SM
       const Tiling t8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256, wps);
       const int g8 = (int)cdiv(t8.warps, 8);
+      static const cudaError_t attr8 = [] {
+        cudaError_t e = cudaFuncSetAttribute(k_rank1_p8<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kR8Smem);
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(k_rank1_p8<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kR8Smem);
+        return e;
+      }();
+      CUDA_TRY(attr8);
       if (c2)
-        k_rank1_p8<true><<<g8, 256, 0, st>>>(D, ld, r, n, t8, c, rv, c2, rv2, bytes_read, M);
+        k_rank1_p8<true><<<g8, 256, kR8Smem, st>>>(D, ld, r, n, t8, c, rv, c2, rv2, bytes_read, M);
       else
-        k_rank1_p8<false><<<g8, 256, 0, st>>>(D, ld, r, n, t8, c, rv, nullptr, nullptr, bytes_read, M);
+        k_rank1_p8<false><<<g8, 256, kR8Smem, st>>>(D, ld, r, n, t8, c, rv, nullptr, nullptr, bytes_read, M);
       if (!twin) return cudaGetLastError();
     }
   }
@@ -1783,11 +1830,19 @@ cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, 
 }
 
 // new node's column / row into D, its edges into WT
+__device__ __forceinline__ void add_scratch_reset(const AddScratch& a, unsigned* err, unsigned* wmin) {
+  *a.argmin_out = ~0ull; *a.in_min = ~0u; *a.s_count = 0; *a.u_count = 0; *a.th2 = 0x7F7F7F7F;
+  *a.fb_count = 0; *a.rmax = 0; *a.ufull = 0u; *a.rfull = 0u;
+  *err = 0u; *wmin = ~0u;
+}
 template <typename T>
 __global__ void k_addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xlocal,
                                 const T* col, const T* row, T* WT, int64_t ldw, const T* ow,
-                                const T* iw, Mirror M) {
+                                const T* iw, Mirror M, AddScratch as, unsigned* err, unsigned* wmin) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // the add's scratch words were last read by the kernels before this one:
+  // reset them for the next add (instead of a launch of its own then)
+  if (tid == 0 && as.argmin_out) add_scratch_reset(as, err, wmin);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const bool mir = has_mirror(M);   // the new row / column go to the mirror as well
   unsigned mbits = 0;
@@ -1816,9 +1871,10 @@ __global__ void k_addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, 
 template <typename T>
 cudaError_t addnode_write(T* D, int64_t ld, Rows r, int64_t n, int64_t x, int xlocal,
                           const T* col, const T* row, T* WT, int64_t ldw, const T* ow,
-                          const T* iw, Mirror M, cudaStream_t st) {
+                          const T* iw, Mirror M, cudaStream_t st, const AddScratch& as, unsigned* err,
+                          unsigned* wmin) {
   int grid = (int)std::min<int64_t>(cdiv(n, 256), 4 * num_sms());
-  k_addnode_write<T><<<grid, 256, 0, st>>>(D, ld, r, n, x, xlocal, col, row, WT, ldw, ow, iw, M);
+  k_addnode_write<T><<<grid, 256, 0, st>>>(D, ld, r, n, x, xlocal, col, row, WT, ldw, ow, iw, M, as, err, wmin);
   return cudaGetLastError();
 }
 
@@ -2410,7 +2466,7 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
                    int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr, const T* WT,
                    int64_t ldw, int sr, Mirror M, cudaStream_t st, const void* tmap8) {
   if (r.hi <= r.lo) return cudaSuccess;
-  static const int wps = tune_wps("APSP_TUNE_DET_WPS", 192), wps8 = tune_wps("APSP_TUNE_DET8_WPS", 128);
+  constexpr int wps = DET_WPS, wps8 = DET8_WPS;
   Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20, DS_VEC, wps);   // (measured best)
   if (tl.slab >= (1 << 26)) return cudaErrorInvalidValue;   // MODE-1 queue packing
   if (mode == 0) CUDA_TRY(cudaMemsetAsync(anyrow + r.lo, 0, sizeof(int) * (size_t)(r.hi - r.lo), st));
@@ -2692,7 +2748,8 @@ cudaError_t pack_counters(const DetectCounters* c, const int* any, long long* v,
 // one GPU: the same six words straight into mapped host memory, plus the
 // mirror flag after them (host[12] as unsigned) — the update's one host read
 __global__ void k_pack_to_host(const DetectCounters* c, const int* any, const unsigned* mflag,
-                               volatile long long* host) {
+                               volatile long long* host, const int* rounds) {
+  if (rounds) reinterpret_cast<volatile unsigned*>(host)[14] = (unsigned)*rounds;
   host[0] = (long long)c->total;
   host[1] = (long long)c->rows;
   host[2] = (c->overflow & 1u) ? 1 : 0;
@@ -2703,8 +2760,8 @@ __global__ void k_pack_to_host(const DetectCounters* c, const int* any, const un
   __threadfence_system();
 }
 cudaError_t pack_to_host(const DetectCounters* c, const int* any, const unsigned* mflag, void* host_dev,
-                         cudaStream_t st) {
-  k_pack_to_host<<<1, 1, 0, st>>>(c, any, mflag, reinterpret_cast<volatile long long*>(host_dev));
+                         cudaStream_t st, const int* rounds) {
+  k_pack_to_host<<<1, 1, 0, st>>>(c, any, mflag, reinterpret_cast<volatile long long*>(host_dev), rounds);
   return cudaGetLastError();
 }
 
@@ -2799,7 +2856,8 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
 
 #define INST(T)                                                                                   \
   template cudaError_t validate_vec<T>(const T*, const T*, int64_t, int64_t, T*, unsigned int*, unsigned*,    \
-                                       cudaStream_t, const T*, const T*, T*, unsigned long long*, unsigned*);                                             \
+                                       cudaStream_t, const T*, const T*, T*, unsigned long long*, unsigned*, \
+                                       ValidateReadback);                                          \
   template cudaError_t transpose_in<T>(const T*, int64_t, int64_t, T*, int64_t, unsigned int*,     \
                                        unsigned*, cudaStream_t);                                  \
   template cudaError_t fill<T>(T*, int64_t, T, cudaStream_t);                                      \
@@ -2819,7 +2877,8 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
   template cudaError_t rank1<T>(T*, int64_t, Rows, int64_t, const T*, const T*, const T*,          \
                                 const T*, unsigned long long*, int, Mirror, cudaStream_t, int);        \
   template cudaError_t addnode_write<T>(T*, int64_t, Rows, int64_t, int64_t, int, const T*,        \
-                                        const T*, T*, int64_t, const T*, const T*, Mirror, cudaStream_t); \
+                                        const T*, T*, int64_t, const T*, const T*, Mirror, cudaStream_t, \
+                                        const AddScratch&, unsigned*, unsigned*);                  \
   template cudaError_t detect<T>(T*, int64_t, Rows, int64_t, int64_t, const T*, const T*,          \
                                  const T*, const T*, float, int, int*, int*, int*, int*, T*,      \
                                  int64_t, DetectCounters*, const T*, int64_t, int, Mirror,        \

@@ -147,6 +147,10 @@ def c5():
     t1, info = timed(lambda: h.update_edge(u, v, int(W[u, v]) * 10))
     emit("c5", "increase_x10_random", [t1], n, {"info": info.as_dict(), "mirror_width": h.mirror_width})
     vt = tight_in(W, u)
+    u0 = (u + 1) % n   # an untimed tight increase first (the kernels' first launch loads them)
+    v0 = tight_in(W, u0)
+    h.update_edge(u0, v0, int(W[u0, v0]) * 10)
+    W[u0, v0] = W[u0, v0] * 10
     t2, info = timed(lambda: h.update_edge(u, vt, int(W[u, vt]) * 10))
     emit("c5", "increase_x10_tight", [t2], n, {"info": info.as_dict(), "mirror_width": h.mirror_width})
     s, tt = synth.query_pairs(spec.seed, n, 1024)

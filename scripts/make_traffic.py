@@ -13,9 +13,10 @@ import sys
 
 CLASS_OF = [   # (kernel-name prefix, class) — first match wins
     ("k_detect_p8", "detect"), ("k_detect_p16", "detect"), ("k_detect_stream", "detect"),
-    ("k_addcol_gather", "add_pass1"), ("k_addnode_pass1_p8", "add_pass1"), ("k_addnode_pass1_p16", "add_pass1"),
-    ("k_rank1", "rank1"), ("k_sparse_phase_a", "sparse0"), ("k_sparse_round", "sparse_r"),
-    ("k_query_scan", "query"), ("fw_tile3_kernel", "fw_tile"),
+    ("k_addcol_mt", "add_pass1"), ("k_addcol_gather", "add_pass1"), ("k_addnode_pass1_p8", "add_pass1"),
+    ("k_addnode_pass1_p16", "add_pass1"),
+    ("k_rank1_p8", "rank1"), ("k_rank1", "rank1"), ("k_sparse_phase_aq", "sparse0"), ("k_sparse_phase_a", "sparse0"),
+    ("k_sparse_round", "sparse_r"), ("k_query_scan", "query"), ("fw_tile3_kernel", "fw_tile"),
 ]
 
 

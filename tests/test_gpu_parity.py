@@ -1164,3 +1164,67 @@ def test_query_candidate_set_beyond_scratch(lib):
     assert d == 5 and path == list(range(10, 16))
     with pytest.raises(lib.ApspError):   # path_cap too small: E_RANGE, needed length reported
         h.query(0, n - 1, path_cap=100)
+
+
+# ------------------------------------------------------------------ heavy rows (§4.6)
+@pytest.mark.parametrize("dtype,directed,semiring", [
+    (np.int32, True, 0), (np.float32, False, 0), (np.int32, False, 1), (np.float32, True, 1)])
+def test_heavy_rows_forced_sequence(lib, rng, dtype, directed, semiring):
+    """APSP_OPT_HEAVY = 1: up to 32 rows with any open pair skip the frontier
+    rounds and are resolved from the other rows (X pass + closure inside the
+    heavy set) — every removal and tight increase of a mixed sequence, int32
+    bit-exact / fp32 1e-5 vs the oracle, shortest path and minimax."""
+    n = 260
+    W = random_graph(rng, n, directed=directed, lo=1, hi=9, dtype=dtype, density=0.5)
+    hg = synth.HostGraph(W, directed)
+    h = lib.WarmAPSP(torch.from_numpy(W), directed=directed, cold_start=False,
+                     semiring="minimax" if semiring else "shortest")
+    h.set_option(lib._lib.OPT_HEAVY, 1)
+    h.set_option(0, 1)   # the sparse path
+    h.cold_fw()
+    ref = oracle.fw_minimax if semiring else oracle.fw
+    for t in range(10):
+        if t % 2 == 0:
+            k = int(rng.integers(hg.n))
+            _, info = h.remove_node(k)
+            hg.remove_node(k)
+        else:
+            D = ref(hg.W)
+            u, v = _tight_edge(hg.W, D, rng, directed)
+            w = hg.W[u, v] * (3 if dtype == np.int32 else np.float32(3))
+            if semiring and w == hg.W[u, v]:
+                w = hg.W[u, v] + 5
+            info = h.update_edge(u, v, w)
+            hg.set_edge(u, v, w)
+        assert_parity(getD(h), ref(hg.W))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.int32])
+def test_heavy_rows_default_threshold(lib, dtype):
+    """The default threshold (max(512, n/8) open pairs): an undirected complete
+    graph, the cheapest edge of a node raised x10 leaves thousands of open
+    pairs in that node's row — resolved by the heavy-row pass, equal to the
+    oracle; and to the same update with heavy rows off."""
+    spec = dataclasses.replace(synth.C2, n=1100) if dtype == np.float32 else \
+        dataclasses.replace(synth.C4, n=1100, directed=False)
+    W = synth.graph(spec)
+    if dtype == np.int32:
+        W = np.minimum(W, W.T)
+    hgs = []
+    outs = []
+    for heavy in (0, -1):
+        h = make(lib, W, directed=False)
+        h.set_option(lib._lib.OPT_HEAVY, heavy)
+        hg = synth.HostGraph(W, False)
+        for u in (3, 4):
+            row = hg.W[u].astype(np.float64)
+            row[u] = np.inf
+            v = int(np.argmin(row))
+            w = hg.W[u, v] * (10 if dtype == np.int32 else np.float32(10))
+            info = h.update_edge(u, v, w)
+            hg.set_edge(u, v, w)
+            assert info.path == 2
+        outs.append(getD(h))
+        hgs.append(hg)
+    assert_parity(outs[0], oracle.fw(hgs[0].W))
+    assert np.array_equal(outs[0], outs[1]) if dtype == np.int32 else True

@@ -177,7 +177,12 @@ def test_sharded_updates_equal_oracle(P, world, cap, n, directed, dtype):
     infos1 = [apply(h1, op) for op in ops]
     d1b, _, l1b, _ = h1.query_batch(qs, qt, path_cap=128)
     torch.cuda.synchronize()
-    assert infos1 == res[0][1], "sharded update statistics differ from world 1"
+    # (the number of sparse rounds is an implementation detail: one GPU runs
+    # them in one cooperative launch up to convergence, sharded handles in
+    # batches — everything else must agree)
+    def strip(infos):
+        return [None if i is None else {k: v for k, v in i.items() if k != "rounds"} for i in infos]
+    assert strip(infos1) == strip(res[0][1]), "sharded update statistics differ from world 1"
     assert np.array_equal(d1b.cpu().numpy(), res[0][2])
     assert np.array_equal(l1b.cpu().numpy(), res[0][4])
     h1.close()

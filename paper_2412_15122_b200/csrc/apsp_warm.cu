@@ -171,6 +171,7 @@ struct apsp_handle {
   int last_fw16 = 0;             // 1: the last FW ran packed, 2: it fell back to int32
   bool mirror_built = false;     // the mirror was built (or invalidated) from D
   bool mirror_hint = false;      // last observed mirror state was "valid" (profile accounting only)
+  bool mirror_fresh = false;     // no kernel that can write a new value ran since that observation
   int mirror_level = 16;         // width of the mirror: 8 or 16 bits
   int mirror8 = 1;               // APSP_OPT_MIRROR8: try the int8 width at each build
   int use_mirror = 1;            // APSP_OPT_MIRROR: 0 = no mirror, the streams read D (4 B/entry)
@@ -233,7 +234,13 @@ struct apsp_handle {
     e = cudaMemcpy(&rb, rank1_bytes(), sizeof rb, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return e;
     prof_work[APSP_K_RANK1] += (double)rb;
-    return cudaMemset(rank1_bytes(), 0, sizeof rb);
+    e = cudaMemset(rank1_bytes(), 0, sizeof rb);
+    if (e != cudaSuccess) return e;
+    unsigned long long cb = 0;   // the add's column pass (k_addcol_mt)
+    e = cudaMemcpy(&cb, add_scratch().work, sizeof cb, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return e;
+    prof_work[APSP_K_ADD_PASS1] += (double)cb;
+    return cudaMemset(add_scratch().work, 0, sizeof cb);
   }
 
   template <typename T> T* WT() { return reinterpret_cast<T*>(ws + plan.off_wt); }
@@ -307,7 +314,8 @@ struct apsp_handle {
                       reinterpret_cast<int*>(b + 408), reinterpret_cast<int*>(b + 412),
                       reinterpret_cast<int*>(b + 416), reinterpret_cast<int*>(b + 420),
                       reinterpret_cast<int*>(b + 424), reinterpret_cast<int*>(b + 428),
-                      reinterpret_cast<unsigned*>(b + 432), reinterpret_cast<unsigned*>(b + 436)};
+                      reinterpret_cast<unsigned*>(b + 432), reinterpret_cast<unsigned*>(b + 436),
+                      reinterpret_cast<unsigned long long*>(b + 456)};
   }
   // saturated mirror of D (kernels.h), int32 handles only: int8 (own buffer)
   // or int16 (in the packed-FW buffer), the width picked at the last build
@@ -478,6 +486,7 @@ apsp_status mirror8_settle(apsp_handle* h, bool* need16) {
   CKR(cudaMemcpyAsync(hf, h->mirror_flag(), sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
   CKR(cudaStreamSynchronize(h->st));
   *need16 = (*hf & 1u) != 0u;
+  h->mirror_fresh = true;
   if (*need16) {
     h->mirror8_failed = true;
     h->mirror_level = 16;
@@ -802,8 +811,13 @@ apsp_status cold_fw_impl(apsp_handle* h) {
 // c1/r1 (and c2/r2 when undirected increase) must be set up by the caller.
 // The int8 mirror is valid as of this update's host read of its flag (valid
 // only where no kernel that writes D/the mirror ran since that read).
-inline bool mirror8_known_valid(const apsp_handle* h) {
+// (the last observation only, possibly stale: for speculative work that is
+// re-checked after the next host read)
+inline bool mirror8_hint(const apsp_handle* h) {
   return h->mirror_built && h->mirror_level == 8 && h->mirror_hint && h->sr == 0;
+}
+inline bool mirror8_known_valid(const apsp_handle* h) {
+  return h->mirror_built && h->mirror_level == 8 && h->mirror_hint && h->mirror_fresh && h->sr == 0;
 }
 
 // Removal of node k: SL upkeep (drop k's entries, node n-1 takes slot k) on
@@ -839,6 +853,11 @@ ZeroSet recompute_zero_set(apsp_handle* h) {
   z.add(h->bigq_ctr(), 4);      // the rounds' queue counters
   return z;
 }
+
+// Phase A's algorithmic bytes per listed pair: the list entry (8), the first
+// two shortlist entries of column j (ids + weights, 16), their D entries on
+// the int8 mirror (2) and pivot values (8)
+constexpr double kPhaseABytes = 34.0;
 
 // prepped: the counters were zeroed — and for a removal WT tombstoned — by the
 // update's first launch (update_prep, one GPU)
@@ -877,7 +896,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     PK(APSP_K_DETECT, h->stream_bytes<T>() * (double)(r.hi - r.lo) * (double)n,
        detect<T>(h->Dl<T>(), h->ld, r, n, skip, c1, r1, c2, r2, h->tau, 1, nullptr, h->rowcnt(),
                  h->srow(), h->scol(), nullptr, lcap, h->ctr(), h->WT<T>(), h->ld, h->sr,
-                 h->mirror<T>(), h->st, h->tmap8_ptr()));
+                 h->mirror<T>(), h->st, h->tmap8_ptr(), !mirror8_known_valid(h)));
     PK(APSP_K_EMIT, 0.0, detect_lists(r, h->rowcnt(), h->rowoff(), h->ctr(), h->st));
     // (prepped: WT was tombstoned by update_prep; D's row and column of the
     // removed node are only read again by the dense path, which tombstones
@@ -941,20 +960,16 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     // recompute needed (at least 2: round 1 finding nothing proves convergence)
     if (coop) {   // every round in one cooperative launch, to convergence (no host round trips)
       // rows with >= max(512, n/8) open pairs skip the rounds and are resolved
-      // from the other rows afterwards (heavy_rows)
-      if (h->heavy_min >= 0)
-        CK(heavy_select(h->ocnt(), r.hi - r.lo,
-                        h->heavy_min > 0 ? h->heavy_min : (int)std::max<int64_t>(512, n / 8), h->heavy_set(), h->st));
+      // from the other rows afterwards, inside the same launch
       RoundBufs rb{h->chg(0),      h->cap + 32,     h->cap,    {fcol[0], fcol[1]}, h->coop_rounds_word(),
-                   h->coop_total_word(), h->heavy_set(), h->bigq(), h->bigq_ctr()};
+                   h->coop_total_word(), h->bigq(), h->bigq_ctr(), h->heavy_set(), h->heavy_x(), h->ld,
+                   h->heavy_min < 0 ? 0 : (h->heavy_min > 0 ? h->heavy_min : (int)std::max<int64_t>(512, n / 8)),
+                   r.hi - r.lo, n, removal ? skip : -1};
       PK(APSP_K_SPARSE_R, 0.0,
          sparse_rounds_coop<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->gprow(), h->gpcol(), h->glb<T>(),
                                ocap, h->rowoff(), h->ocnt(), h->ocol(), rb, 0, h->max_rounds, h->anyflag(), h->sr,
                                h->ctr(), h->st, reinterpret_cast<unsigned*>(h->anyrow()), h->wmin<T>(),
                                h->mirror<T>()));
-      PK(APSP_K_SPARSE_R, 0.0,
-         heavy_rows<T>(h->Dl<T>(), h->ld, n, h->WT<T>(), h->ld, h->heavy_set(), h->heavy_x(), h->ld,
-                       removal ? skip : -1, h->sr, h->st, h->mirror<T>()));
       last_total = h->coop_total_word();
     } else {
       apsp_status s = enqueue_rounds(std::min(std::max(2, h->rounds_hint), h->max_rounds));
@@ -984,8 +999,15 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   }
   CKR(cudaStreamSynchronize(h->st));
   h->mirror_hint = (*hmf & 1u) == 0u;
+  h->mirror_fresh = true;
   if (coop && try_sparse) rounds = (int)reinterpret_cast<unsigned*>(h->host_small)[14];
   const int64_t total = hv[0], rows = hv[1], maxrow = hv[5];
+  if (h->prof_on && try_sparse)   // phase A's algorithmic bytes, now that |A| is known
+    for (auto it = h->prof_pending.rbegin(); it != h->prof_pending.rend(); ++it)
+      if (it->cls == APSP_K_SPARSE0) {
+        it->work = kPhaseABytes * (double)total;
+        break;
+      }
   const bool overflow = hv[2] != 0 || hv[3] != 0;   // a list overflowed on some rank
   bool changed = hv[4] != 0;
   if (info) {
@@ -1070,7 +1092,7 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   // (small graphs: the one streaming pass costs less than the shortcuts' extra launches)
   if constexpr (std::is_same<T, int32_t>::value)
     srow = h->world == 1 && n >= kAddShortcutMinN && n < (int64_t(1) << 24) && h->plan.maxchunk >= 2 &&
-           2 * kAddColLimit <= ld && mirror8_known_valid(h);   // (k_addrow packs t in 24 bits)
+           2 * kAddColLimit <= ld && mirror8_hint(h);   // (k_addrow packs t in 24 bits)
   if constexpr (std::is_same<T, int32_t>::value) {
     if (srow) {
       CKR(cudaEventRecord(h->ev_fork, h->st));
@@ -1087,6 +1109,7 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   unsigned* herr = reinterpret_cast<unsigned*>(h->host_small);
   CKR(cudaStreamSynchronize(h->st));
   h->mirror_hint = (herr[2] & 1u) == 0u;
+  h->mirror_fresh = true;
   if (*herr) {
     if (srow) CKR(cudaStreamSynchronize(h->st2));   // the scratch is free again
     CK(add_init(as, &h->ctr()->err, h->wmin_dev(), h->st));   // reset for the next add
@@ -1164,6 +1187,7 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   PK(APSP_K_RANK1, 0.0,   // work: bytes actually read, counted on the device
      rank1<T>(h->Dl<T>(), ld, r, n, ceff, row, nullptr, nullptr, h->rank1_bytes(), h->sr, h->mirror<T>(),
               h->st, mirror8_known_valid(h) ? 0 : 1));
+  h->mirror_fresh = false;   // rank-1 and the new row / column may write values >= 0x7F
   CK(addnode_write<T>(h->Dl<T>(), ld, r, n, x, h->local(x) ? 1 : 0, col, row, h->WT<T>(), ld, ow,
                       iw, h->mirror<T>(), h->st, as, &h->ctr()->err, h->wmin_dev()));
   // (addnode_write mirrored the new row / column)
@@ -1279,6 +1303,7 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
     PK(APSP_K_RANK1, 0.0,   // work: bytes actually read, counted on the device
        rank1<T>(h->Dl<T>(), ld, r, n, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, h->rank1_bytes(),
                 h->sr, h->mirror<T>(), h->st));
+    h->mirror_fresh = false;   // rank-1 may write values >= 0x7F
     CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
     CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
     if (info) info->path = 1;

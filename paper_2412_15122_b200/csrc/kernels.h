@@ -115,6 +115,7 @@ cudaError_t addnode_pass1(const T* D, int64_t ld, Rows r, int64_t n, const T* ow
 struct AddScratch {
   unsigned long long* argmin_out; unsigned* in_min; int* s_count; int* u_count; int* th2; int* fb_count;
   int* rmax; int* rb; unsigned* ufull; unsigned* rfull;
+  unsigned long long* work;   // cumulative algorithmic bytes of the column pass (profile)
 };
 cudaError_t add_init(const AddScratch& a, unsigned* err, unsigned* wmin, cudaStream_t st);
 cudaError_t addrow_s(const AddScratch& a, const int32_t* ow, int64_t n, const uint8_t* m8, int64_t ld, int64_t row0,
@@ -152,7 +153,8 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
                    const T* c2, const T* r2, float tau, int mode, int* anyrow, int* rowcnt,
                    int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr, const T* WT,
                    int64_t ldw, int sr, Mirror M, cudaStream_t st,
-                   const void* tmap8 = nullptr /* host CUtensorMap of the int8 mirror (detect8_tensor_map) */);
+                   const void* tmap8 = nullptr /* host CUtensorMap of the int8 mirror (detect8_tensor_map) */,
+                   bool twin = true /* false: the host knows the int8 mirror is valid, no int32 twin launch */);
 // The 2-D tensor map the int8 detection's TMA copies use: the int8 mirror m8
 // as a uint32 tensor of `rows` x ld / 4 words (row stride ld bytes), boxes of
 // 256 words x the kernel's rows per stage.  out: 128-byte CUtensorMap.
@@ -237,18 +239,17 @@ struct RoundBufs {
   int* chg; int64_t stride; int64_t cap;
   int* fcol[2];
   int* rounds_run; int* last_total;
-  const int* heavy;   // heavy rows the rounds skip (heavy_select's set), or null
   int* bigq;          // queue of long-frontier pairs (capacity: the open-list size)
   int* bigq_ctr;      // 4 ints: (tail, head) per round parity; zero on entry
+  // heavy rows: selected at the start (>= heavy_thr open
+  // pairs, at most kHeavy; heavy_thr 0: none), skipped by the rounds, then
+  // resolved from the other rows.  heavy[0] = rows selected (zero on entry),
+  // heavy[1..kHeavy] their ids; heavy_x = kHeavy rows of ldx keys, 0x7F-filled
+  // at creation and reset after each use
+  int* heavy; int* heavy_x; int64_t ldx; int heavy_thr;
+  int64_t rows, n, skip;   // local rows (one GPU: all), nodes, removed node or -1
 };
-// heavy rows (one GPU): hs[0] = rows selected, hs[1..kHeavy]
-// their ids (hs[0] zeroed with the counters); x = kHeavy rows of ldx keys,
-// 0x7F-filled at creation and reset by heavy_rows after each use
 constexpr int kHeavy = 32;
-cudaError_t heavy_select(const int* ocnt, int64_t rows, int thr, int* hs, cudaStream_t st);
-template <typename T>
-cudaError_t heavy_rows(T* D, int64_t ld, int64_t n, const T* WT, int64_t ldw, const int* hs, int* x, int64_t ldx,
-                       int64_t skip, int sr, cudaStream_t st, Mirror M);
 // rounds r0 .. r1 - 1 in one cooperative launch (grid barriers between rounds),
 // stopping at convergence
 template <typename T>

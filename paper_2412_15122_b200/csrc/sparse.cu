@@ -1085,6 +1085,166 @@ cudaError_t open_rowmin(const T* D, int64_t ld, int64_t row0, const int* gprow, 
 // open pair (i, j) of a row whose entries changed last round is relaxed
 // through those entries; a lower value is written and becomes part of the
 // next round's frontier.
+// ---------------------------------------------------------------------------
+// heavy rows (one GPU; DESIGN.md §4.6): a row with many open pairs is a large
+// single-source problem for the rounds, whose cost per round is the row's open
+// pairs x its frontier.  Its row of D' is taken instead from the other rows,
+// final once the rounds converged (every pair (i, j) of a row is resolved from
+// row i alone, so excluding the heavy rows does not delay the others): with H
+// the heavy rows and
+//   X_h[j] = min over m not in H of  W'[h][m] + D'[m][j]          (first hop)
+//   C      = shortest paths inside H over the edges W' between heavy nodes
+// every shortest h -> j path leaves H after a prefix inside H (at h', via a
+// first hop to a node outside H) or stays inside H (j in H), so
+//   D'[h][j] = min( min_h' C[h][h'] + X_h'[j],  C[h][j] if j in H ).
+// ---------------------------------------------------------------------------
+// X keys: atomicMin on the value's order-preserving bits (values >= 0); the
+// buffer holds "INF or above" between recomputes, clamped when read
+template <typename T>
+__device__ __forceinline__ T heavy_xval(int k) {
+  if (Tr<T>::kFloat) {
+    const float f = k >= 0x7F800000 ? __builtin_huge_valf() : __int_as_float(k);
+    return (T)f;
+  }
+  return (T)min(k, (int)Tr<T>::inf());
+}
+template <typename T>
+__device__ __forceinline__ int heavy_xkey(T v) {
+  int k;
+  memcpy(&k, &v, 4);
+  return k;
+}
+
+constexpr int kHxSlab = 32;   // rows m per staging step
+constexpr int kHxGroup = 8;   // heavy rows per X work item
+// Shared memory of the heavy-row phases (inside the cooperative rounds kernel)
+template <typename T>
+struct HeavySmem {
+  int hrow[kHeavy];
+  T w[kHxSlab][kHxGroup];
+  T red[8][kHxGroup][128];
+  T C[kHeavy][kHeavy];
+};
+// X_h[j] for the group of 8 selected rows starting at g0, over a 128-column
+// stripe and the rows m in [m0, m1): the 8 warps take every 8th row, the
+// weights W'[h][m] of 32 rows at a time staged in shared memory (prefetched
+// one stage ahead); the warps' partial minima are reduced in shared memory,
+// then one atomicMin per (h, column).  Every thread of the block calls it.
+template <typename T, int SR>
+__device__ void heavy_x_item(const T* __restrict__ D, int64_t ld, int64_t n, const T* __restrict__ WT, int64_t ldw,
+                             int hc, int g0, int64_t stripe, int64_t m0, int64_t m1, int* x, int64_t ldx,
+                             int64_t skip, HeavySmem<T>& sm) {
+  const int gc = min(kHxGroup, hc - g0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const T I = Tr<T>::inf();
+  const int64_t c0 = stripe * 128 + 4 * lane;   // this lane's columns c0 .. c0+3
+  T acc[kHxGroup][4];
+#pragma unroll
+  for (int k = 0; k < kHxGroup; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[k][e] = I;
+  const int wr = threadIdx.x / kHxGroup, wk = threadIdx.x % kHxGroup;
+  auto wload = [&](int64_t b) -> T {
+    const int64_t m = b + wr;
+    bool out = m < m1 && m != skip && wk < gc;
+    for (int t = 0; t < hc; ++t) out &= sm.hrow[t] != (int)m;   // m outside H
+    return out ? WT[m * ldw + sm.hrow[g0 + wk]] : I;             // W'[h][m] (WT row m: in-edges of m)
+  };
+  T wnext = wload(m0);
+  for (int64_t b = m0; b < m1; b += kHxSlab) {
+    __syncthreads();
+    sm.w[wr][wk] = wnext;
+    __syncthreads();
+    if (b + kHxSlab < m1) wnext = wload(b + kHxSlab);
+    if (c0 >= n) continue;
+    Vec4<T> d[kHxSlab / 8];
+#pragma unroll
+    for (int rr = 0; rr < kHxSlab / 8; ++rr) {
+      const int64_t m = b + rr * 8 + warp;
+      d[rr] = m < m1 ? mask_tail<T>(ld4<T>(D + m * ld + c0), c0, n) : Vec4<T>{I, I, I, I};
+    }
+#pragma unroll
+    for (int rr = 0; rr < kHxSlab / 8; ++rr) {
+      const int r = rr * 8 + warp;
+#pragma unroll
+      for (int k = 0; k < kHxGroup; ++k) {
+        if (k >= gc) break;
+        const T wv = sm.w[r][k];
+        acc[k][0] = Tr<T, SR>::relax(acc[k][0], wv, d[rr].x);
+        acc[k][1] = Tr<T, SR>::relax(acc[k][1], wv, d[rr].y);
+        acc[k][2] = Tr<T, SR>::relax(acc[k][2], wv, d[rr].z);
+        acc[k][3] = Tr<T, SR>::relax(acc[k][3], wv, d[rr].w);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kHxGroup; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sm.red[warp][k][4 * lane + e] = acc[k][e];
+  __syncthreads();
+  for (int o = threadIdx.x; o < kHxGroup * 128; o += blockDim.x) {
+    const int k = o / 128, cc = o % 128;
+    const int64_t j = stripe * 128 + cc;
+    if (k >= gc || j >= n) continue;
+    T v = sm.red[0][k][cc];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) v = Tr<T>::mn(v, sm.red[q][k][cc]);
+    if (v < I) atomicMin(x + (g0 + k) * ldx + j, heavy_xkey<T>(Tr<T>::sat(v)));
+  }
+}
+
+// The heavy rows' closure C (shortest paths inside H over W'), in shared
+// memory; every thread of the block calls it.
+template <typename T, int SR>
+__device__ void heavy_closure(const T* __restrict__ WT, int64_t ldw, int hc, HeavySmem<T>& sm) {
+  for (int e = threadIdx.x; e < hc * hc; e += blockDim.x) {
+    const int a = e / hc, b = e % hc;
+    sm.C[a][b] = a == b ? T(0) : WT[(int64_t)sm.hrow[b] * ldw + sm.hrow[a]];   // W'[h_a][h_b]
+  }
+  // Floyd–Warshall inside H, in place (row and column k do not change in step k)
+  for (int k = 0; k < hc; ++k) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < hc * hc; e += blockDim.x) {
+      const int a = e / hc, b = e % hc;
+      sm.C[a][b] = Tr<T>::sat(Tr<T, SR>::relax(sm.C[a][b], sm.C[a][k], sm.C[k][b]));
+    }
+  }
+  __syncthreads();
+}
+
+// D[h][j] := min(D[h][j], min_h' C[h][h'] + X_h'[j], C[h][j] if j in H) for
+// column j; resets X_h'[j] to "INF" for the next recompute
+template <typename T, int SR>
+__device__ __forceinline__ unsigned heavy_fix_col(T* D, int64_t ld, int64_t j, int hc, int* x, int64_t ldx,
+                                                  int64_t skip, const Mirror& M, const HeavySmem<T>& sm) {
+  unsigned mbits = 0;
+  T xb[kHeavy];
+#pragma unroll
+  for (int b = 0; b < kHeavy; ++b) {
+    if (b >= hc) break;
+    xb[b] = heavy_xval<T>(x[b * ldx + j]);
+    x[b * ldx + j] = 0x7F7F7F7F;
+  }
+  if (j == skip) return 0u;
+  for (int a = 0; a < hc; ++a) {
+    T v = Tr<T>::inf();
+#pragma unroll
+    for (int b = 0; b < kHeavy; ++b) {
+      if (b >= hc) break;
+      v = Tr<T, SR>::relax(v, sm.C[a][b], xb[b]);
+      if (sm.hrow[b] == (int)j) v = Tr<T>::mn(v, sm.C[a][b]);
+    }
+    v = Tr<T>::sat(v);
+    T* dp = D + (int64_t)sm.hrow[a] * ld + j;
+    if (v < *dp) {
+      *dp = v;
+      if (M.m || M.m8) mbits |= mput(M, (int64_t)sm.hrow[a] * ld + j, v);
+    }
+  }
+  return mbits;
+}
+
 constexpr int kRoundLocal = 16;   // frontier length a single lane relaxes on its own
 // The whole warp relaxes pair (i, j) (current value cur) through the cnt
 // frontier entries of row i; a lower value is written and joins the next
@@ -1269,9 +1429,19 @@ __global__ void __launch_bounds__(256) k_sparse_rounds_coop(T* D, int64_t ld, in
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   nopen = device_count(dc, nopen, 1);
-  __shared__ int hrow[kHeavy];
-  const int hc = rb.heavy ? min(*(volatile const int*)rb.heavy, kHeavy) : 0;
-  if (threadIdx.x < hc) hrow[threadIdx.x] = rb.heavy[1 + threadIdx.x];
+  __shared__ HeavySmem<T> sm;
+  int* hrow = sm.hrow;
+  if (rb.heavy_thr > 0) {   // heavy rows: >= heavy_thr open pairs (the first kHeavy found)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rb.rows;
+         i += (int64_t)gridDim.x * blockDim.x)
+      if (ocnt[i] >= rb.heavy_thr) {
+        const int s = atomicAdd(rb.heavy, 1);
+        if (s < kHeavy) rb.heavy[1 + s] = (int)i;
+      }
+    grid.sync();
+  }
+  const int hc = rb.heavy_thr > 0 ? min(*(volatile const int*)rb.heavy, kHeavy) : 0;
+  if (threadIdx.x < hc) hrow[threadIdx.x] = *(volatile const int*)(rb.heavy + 1 + threadIdx.x);
   __syncthreads();
   unsigned mbits = 0;
   int round = r0;
@@ -1301,6 +1471,25 @@ __global__ void __launch_bounds__(256) k_sparse_rounds_coop(T* D, int64_t ld, in
                                       rb.fcol[round & 1], any, rowkey, M, rb.bigq, tail, bq + 1);
       grid.sync();
     }
+  }
+  if (hc > 0) {   // the heavy rows, from the other rows (final once the rounds converged)
+    const int64_t n = rb.n;
+    const int64_t gx = (n + 127) / 128;
+    const int ng = (hc + kHxGroup - 1) / kHxGroup;
+    const int64_t ny = max((int64_t)1, 2 * (int64_t)gridDim.x / (gx * ng));
+    const int64_t slab = ((n + ny - 1) / ny + kHxSlab - 1) / kHxSlab * kHxSlab;
+    const int64_t items = gx * ng * ((n + slab - 1) / slab);
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+      const int64_t stripe = it % gx, rest = it / gx;
+      const int g = (int)(rest % ng);
+      const int64_t m0 = (rest / ng) * slab;
+      heavy_x_item<T, SR>(D, ld, n, WT, ldw, hc, g * kHxGroup, stripe, m0, min(n, m0 + slab), rb.heavy_x, rb.ldx,
+                          rb.skip, sm);
+    }
+    grid.sync();
+    heavy_closure<T, SR>(WT, ldw, hc, sm);
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+      mbits |= heavy_fix_col<T, SR>(D, ld, j, hc, rb.heavy_x, rb.ldx, rb.skip, M, sm);
   }
   if (M.m || M.m8) mirror_post(M, mbits);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1349,209 +1538,7 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------------------
-// heavy rows (one GPU; DESIGN.md §4.6): a row with many open pairs is a large
-// single-source problem for the rounds, whose cost per round is the row's open
-// pairs x its frontier.  Its row of D' is taken instead from the other rows,
-// final once the rounds converged (every pair (i, j) of a row is resolved from
-// row i alone, so excluding the heavy rows does not delay the others): with H
-// the heavy rows and
-//   X_h[j] = min over m not in H of  W'[h][m] + D'[m][j]          (first hop)
-//   C      = shortest paths inside H over the edges W' between heavy nodes
-// every shortest h -> j path leaves H after a prefix inside H (at h', via a
-// first hop to a node outside H) or stays inside H (j in H), so
-//   D'[h][j] = min( min_h' C[h][h'] + X_h'[j],  C[h][j] if j in H ).
-// ---------------------------------------------------------------------------
-// rows with at least thr open pairs (the first kHeavy found)
-__global__ void k_heavy_select(const int* __restrict__ ocnt, int64_t rows, int thr, int* hs) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
-    if (ocnt[i] >= thr) {
-      const int s = atomicAdd(hs, 1);
-      if (s < kHeavy) hs[1 + s] = (int)i;
-    }
-}
-cudaError_t heavy_select(const int* ocnt, int64_t rows, int thr, int* hs, cudaStream_t st) {
-  if (rows <= 0) return cudaSuccess;
-  k_heavy_select<<<(int)std::min<int64_t>(cdiv(rows, 256), 2 * num_sms()), 256, 0, st>>>(ocnt, rows, thr, hs);
-  return cudaGetLastError();
-}
-
-// X keys: atomicMin on the value's order-preserving bits (values >= 0); the
-// buffer holds "INF or above" between recomputes, clamped when read
-template <typename T>
-__device__ __forceinline__ T heavy_xval(int k) {
-  if (Tr<T>::kFloat) {
-    const float f = k >= 0x7F800000 ? __builtin_huge_valf() : __int_as_float(k);
-    return (T)f;
-  }
-  return (T)min(k, (int)Tr<T>::inf());
-}
-template <typename T>
-__device__ __forceinline__ int heavy_xkey(T v) {
-  int k;
-  memcpy(&k, &v, 4);
-  return k;
-}
-
-constexpr int kHxSlab = 32;   // rows m per staging step
-constexpr int kHxGroup = 8;   // heavy rows per X block (blockIdx.z: the group)
-// X_h[j] for a group of 8 selected rows h.  A block owns a 128-column stripe
-// (lane: 4 columns) and a range of rows m; its 8 warps take every 8th row,
-// the weights W'[h][m] of 32 rows at a time staged in shared memory; the
-// warps' partial minima are reduced in shared memory, then one atomicMin per
-// (h, column) per block.
-template <typename T, int SR>
-__global__ void __launch_bounds__(256) k_heavy_x(const T* __restrict__ D, int64_t ld, int64_t n,
-                                                 const T* __restrict__ WT, int64_t ldw, const int* __restrict__ hs,
-                                                 int* x, int64_t ldx, int64_t skip, int64_t slab) {
-  const int hc = min(hs[0], kHeavy);
-  const int g0 = blockIdx.z * kHxGroup;
-  if (g0 >= hc) return;
-  const int gc = min(kHxGroup, hc - g0);   // rows of this group
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ int hrow[kHeavy];
-  __shared__ T w[kHxSlab][kHxGroup];
-  __shared__ T red[8][kHxGroup][128];
-  if (threadIdx.x < hc) hrow[threadIdx.x] = hs[1 + threadIdx.x];
-  __syncthreads();
-  const T I = Tr<T>::inf();
-  const int64_t c0 = blockIdx.x * 128 + 4 * lane;   // this lane's columns c0 .. c0+3
-  const int64_t m0 = blockIdx.y * slab, m1 = min(n, m0 + slab);
-  T acc[kHxGroup][4];
-#pragma unroll
-  for (int k = 0; k < kHxGroup; ++k)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) acc[k][e] = I;
-  // thread (r, k) holds W'[h_k][m] of row m = b + r of the next stage
-  // (prefetched one stage ahead: the gathers overlap the D loads)
-  const int wr = threadIdx.x / kHxGroup, wk = threadIdx.x % kHxGroup;
-  auto wload = [&](int64_t b) -> T {
-    const int64_t m = b + wr;
-    bool out = m < m1 && m != skip && wk < gc;
-    for (int t = 0; t < hc; ++t) out &= hrow[t] != (int)m;   // m outside H
-    return out ? WT[m * ldw + hrow[g0 + wk]] : I;             // W'[h][m] (WT row m: in-edges of m)
-  };
-  T wnext = wload(m0);
-  for (int64_t b = m0; b < m1; b += kHxSlab) {
-    __syncthreads();
-    w[wr][wk] = wnext;
-    __syncthreads();
-    if (b + kHxSlab < m1) wnext = wload(b + kHxSlab);
-    if (c0 >= n) continue;
-    Vec4<T> d[kHxSlab / 8];
-#pragma unroll
-    for (int rr = 0; rr < kHxSlab / 8; ++rr) {
-      const int64_t m = b + rr * 8 + warp;
-      d[rr] = m < m1 ? mask_tail<T>(ld4<T>(D + m * ld + c0), c0, n) : Vec4<T>{I, I, I, I};
-    }
-#pragma unroll
-    for (int rr = 0; rr < kHxSlab / 8; ++rr) {
-      const int r = rr * 8 + warp;
-#pragma unroll
-      for (int k = 0; k < kHxGroup; ++k) {
-        if (k >= gc) break;
-        const T wv = w[r][k];
-        acc[k][0] = Tr<T, SR>::relax(acc[k][0], wv, d[rr].x);
-        acc[k][1] = Tr<T, SR>::relax(acc[k][1], wv, d[rr].y);
-        acc[k][2] = Tr<T, SR>::relax(acc[k][2], wv, d[rr].z);
-        acc[k][3] = Tr<T, SR>::relax(acc[k][3], wv, d[rr].w);
-      }
-    }
-  }
-  // reduce the 8 warps' partials, then one atomic per (h, column)
-#pragma unroll
-  for (int k = 0; k < kHxGroup; ++k)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) red[warp][k][4 * lane + e] = acc[k][e];
-  __syncthreads();
-  for (int o = threadIdx.x; o < kHxGroup * 128; o += blockDim.x) {
-    const int k = o / 128, cc = o % 128;
-    const int64_t j = blockIdx.x * 128 + cc;
-    if (k >= gc || j >= n) continue;
-    T v = red[0][k][cc];
-#pragma unroll
-    for (int q = 1; q < 8; ++q) v = Tr<T>::mn(v, red[q][k][cc]);
-    if (v < I) atomicMin(x + (g0 + k) * ldx + j, heavy_xkey<T>(Tr<T>::sat(v)));
-  }
-}
-
-// D[h][j] := min(D[h][j], min_h' C[h][h'] + X_h'[j], C[h][j] if j in H); resets X
-template <typename T, int SR>
-__global__ void __launch_bounds__(256) k_heavy_fix(T* D, int64_t ld, int64_t n, const T* __restrict__ WT,
-                                                   int64_t ldw, const int* __restrict__ hs, int* x, int64_t ldx,
-                                                   int64_t skip, Mirror M) {
-  const int hc = min(hs[0], kHeavy);
-  if (hc == 0) return;
-  __shared__ int hrow[kHeavy];
-  __shared__ T C[kHeavy][kHeavy];
-  const T I = Tr<T>::inf();
-  if (threadIdx.x < hc) hrow[threadIdx.x] = hs[1 + threadIdx.x];
-  __syncthreads();
-  for (int e = threadIdx.x; e < hc * hc; e += blockDim.x) {
-    const int a = e / hc, b = e % hc;
-    C[a][b] = a == b ? T(0) : WT[(int64_t)hrow[b] * ldw + hrow[a]];   // W'[h_a][h_b]
-  }
-  // Floyd–Warshall inside H, in place (row and column k do not change in step k)
-  for (int k = 0; k < hc; ++k) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < hc * hc; e += blockDim.x) {
-      const int a = e / hc, b = e % hc;
-      C[a][b] = Tr<T>::sat(Tr<T, SR>::relax(C[a][b], C[a][k], C[k][b]));
-    }
-  }
-  __syncthreads();
-  unsigned mbits = 0;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-    T xb[kHeavy];
-#pragma unroll
-    for (int b = 0; b < kHeavy; ++b) {
-      if (b >= hc) break;
-      xb[b] = heavy_xval<T>(x[b * ldx + j]);
-      x[b * ldx + j] = 0x7F7F7F7F;   // INF again for the next recompute
-    }
-    if (j == skip) continue;
-    for (int a = 0; a < hc; ++a) {
-      T v = I;
-#pragma unroll
-      for (int b = 0; b < kHeavy; ++b) {
-        if (b >= hc) break;
-        v = Tr<T, SR>::relax(v, C[a][b], xb[b]);
-        if (hrow[b] == (int)j) v = Tr<T>::mn(v, C[a][b]);
-      }
-      v = Tr<T>::sat(v);
-      T* dp = D + (int64_t)hrow[a] * ld + j;
-      if (v < *dp) {
-        *dp = v;
-        if (M.m || M.m8) mbits |= mput(M, (int64_t)hrow[a] * ld + j, v);
-      }
-    }
-  }
-  if (M.m || M.m8) mirror_post(M, mbits);
-}
-
-template <typename T>
-cudaError_t heavy_rows(T* D, int64_t ld, int64_t n, const T* WT, int64_t ldw, const int* hs, int* x, int64_t ldx,
-                       int64_t skip, int sr, cudaStream_t st, Mirror M) {
-  if (n <= 0) return cudaSuccess;
-  const int gx = (int)cdiv(n, 128);   // 128-column stripes
-  // about 4 blocks per SM per group, row ranges of whole staging steps
-  const int64_t want = std::max<int64_t>(1, (int64_t)4 * num_sms() / gx);
-  const int64_t slab = cdiv(cdiv(n, want), kHxSlab) * kHxSlab;
-  const dim3 grid(gx, (unsigned)cdiv(n, slab), kHeavy / kHxGroup);
-  const int gf = (int)std::min<int64_t>(cdiv(n, 256), 2 * num_sms());
-  if (sr) {
-    k_heavy_x<T, 1><<<grid, 256, 0, st>>>(D, ld, n, WT, ldw, hs, x, ldx, skip, slab);
-    k_heavy_fix<T, 1><<<gf, 256, 0, st>>>(D, ld, n, WT, ldw, hs, x, ldx, skip, M);
-  } else {
-    k_heavy_x<T, 0><<<grid, 256, 0, st>>>(D, ld, n, WT, ldw, hs, x, ldx, skip, slab);
-    k_heavy_fix<T, 0><<<gf, 256, 0, st>>>(D, ld, n, WT, ldw, hs, x, ldx, skip, M);
-  }
-  return cudaGetLastError();
-}
-
 #define INST(T)                                                                                   \
-  template cudaError_t heavy_rows<T>(T*, int64_t, int64_t, const T*, int64_t, const int*, int*, int64_t, \
-                                     int64_t, int, cudaStream_t, Mirror);                          \
   template cudaError_t shortlist_build<T>(const T*, int64_t, int64_t, const int*, int64_t, int64_t, \
                                           int*, T*, T*, cudaStream_t);                            \
   template cudaError_t shortlist_add_bound<T>(int*, T*, T*, const T*, int64_t, int64_t,            \

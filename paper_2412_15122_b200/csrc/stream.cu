@@ -1082,6 +1082,8 @@ __global__ void __launch_bounds__(kACQ * kACY) k_addcol_mt(AddScratch a, Rows r,
   __syncthreads();
   const int32_t I = APSP_INF_I32_DEV;
   const int64_t m = r.hi - r.lo, lbase = r.lo - r.row0;   // local rows [lbase, lbase + m)
+  // algorithmic bytes (profile): |U| rows of MT over the local rows + U's triples
+  if (a.work && blockIdx.x == 0 && tid == 0) atomicAdd(a.work, (unsigned long long)(cnt * (m + 12)));
   // thread (x, y): rows lbase + 4 (256 blockIdx.x / 4 + x) + [0, 4), U entries y, y + kACY, ...
   const int64_t q = (int64_t)blockIdx.x * kACQ + threadIdx.x;
   const int64_t l0 = lbase + 4 * q;
@@ -2323,10 +2325,14 @@ __global__ void k_detect_rows(Rows r, const int* __restrict__ rowcnt, int64_t* r
 // 256 words x kD8R rows) fills a stage — kD8R KB per copy (one 1 KB bulk copy
 // per row was bound by the TMA engine's per-copy cost: 4.7 TB/s, against
 // 7.0 TB/s for 2 KB copies, scripts/tma_probe.cu).
+// Stages: 3, or 4 for n >= kD8DeepN — measured: at n = 32768 (55-row slabs)
+// the fourth stage slowed the pass (225 -> 265 us), at n = 65536 (222-row
+// slabs) it sped it up 1.7x (1053 -> 606 us, 4.3 -> 7.1 TB/s; scripts/sweep*.sh)
 constexpr int kD8R = D8_R, kD8S = D8_S;   // ring: rows per stage, stages
-using D8Ring = WarpRing<kD8S, kD8R, 1024>;
-constexpr int kD8Smem = 8 * D8Ring::kBytes;
-template <typename T, bool TWO, int MODE>
+constexpr int64_t kD8DeepN = 49152;
+template <int S> using D8Ring = WarpRing<S, kD8R, 1024>;
+template <int S> constexpr int d8_smem() { return 8 * D8Ring<S>::kBytes; }
+template <typename T, bool TWO, int MODE, int S>
 __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, int64_t n, int64_t skip, Tiling tl,
                                                       const T* __restrict__ c1, const T* __restrict__ r1,
                                                       const T* __restrict__ c2, const T* __restrict__ r2,
@@ -2366,8 +2372,8 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
     if (TWO) rw2[q] = b;
   }
   extern __shared__ __align__(128) uint8_t dring_raw[];
-  D8Ring ring;
-  ring.init(dring_raw + (threadIdx.x >> 5) * D8Ring::kBytes, lane);
+  D8Ring<S> ring;
+  ring.init(dring_raw + (threadIdx.x >> 5) * D8Ring<S>::kBytes, lane);
   // tensor coordinates: (word column, local row)
   const int cw0 = chunk * 256, rl0 = (int)(i_lo - r.row0);
   const int nst = (rows + kD8R - 1) / kD8R;
@@ -2375,10 +2381,10 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
     if (st < nst) ring.issue_box(st, &tm, cw0, rl0 + st * kD8R, lane);
   };
 #pragma unroll
-  for (int st = 0; st < kD8S - 1; ++st) issue(st);
+  for (int st = 0; st < S - 1; ++st) issue(st);
   uint32_t cl = 0, cl2 = 0;
   for (int st = 0; st < nst; ++st) {
-    issue(st + kD8S - 1);
+    issue(st + S - 1);
     ring.wait(st);
 #pragma unroll
     for (int h = 0; h < kD8R; ++h) {
@@ -2464,7 +2470,7 @@ template <typename T>
 cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c1, const T* r1,
                    const T* c2, const T* r2, float tau, int mode, int* anyrow, int* rowcnt,
                    int* prow, int* pcol, T* plb, int64_t lcap, DetectCounters* ctr, const T* WT,
-                   int64_t ldw, int sr, Mirror M, cudaStream_t st, const void* tmap8) {
+                   int64_t ldw, int sr, Mirror M, cudaStream_t st, const void* tmap8, bool twin) {
   if (r.hi <= r.lo) return cudaSuccess;
   constexpr int wps = DET_WPS, wps8 = DET8_WPS;
   Tiling tl = make_tiling(n, r.hi - r.lo, 1 << 20, DS_VEC, wps);   // (measured best)
@@ -2482,18 +2488,26 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
 #define LAUNCH(TWO, SR, MODE)                                                                    \
   do {                                                                                           \
     if (SR == 0 && MODE != 2 && M.m8) {                                                          \
-      auto kp8 = k_detect_p8<T, TWO, (MODE == 2 ? 0 : MODE)>;                                    \
-      static const cudaError_t attr =                                                            \
-          cudaFuncSetAttribute(kp8, cudaFuncAttributeMaxDynamicSharedMemorySize, kD8Smem);        \
-      CUDA_TRY(attr);                                                                            \
       if (!tmap8) return cudaErrorInvalidValue;                                                  \
-      kp8<<<g8, 256, kD8Smem, st>>>(r, ld, n, skip, tl8, c1, r1, c2, r2, o,                      \
-                                   *reinterpret_cast<const CUtensorMap*>(tmap8));                \
+      const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(tmap8);                      \
+      if (n >= kD8DeepN) {                                                                       \
+        auto kp8 = k_detect_p8<T, TWO, (MODE == 2 ? 0 : MODE), kD8S + 1>;                        \
+        static const cudaError_t attr = cudaFuncSetAttribute(                                    \
+            kp8, cudaFuncAttributeMaxDynamicSharedMemorySize, d8_smem<kD8S + 1>());              \
+        CUDA_TRY(attr);                                                                          \
+        kp8<<<g8, 256, d8_smem<kD8S + 1>(), st>>>(r, ld, n, skip, tl8, c1, r1, c2, r2, o, tm);  \
+      } else {                                                                                   \
+        auto kp8 = k_detect_p8<T, TWO, (MODE == 2 ? 0 : MODE), kD8S>;                            \
+        static const cudaError_t attr = cudaFuncSetAttribute(                                    \
+            kp8, cudaFuncAttributeMaxDynamicSharedMemorySize, d8_smem<kD8S>());                  \
+        CUDA_TRY(attr);                                                                          \
+        kp8<<<g8, 256, d8_smem<kD8S>(), st>>>(r, ld, n, skip, tl8, c1, r1, c2, r2, o, tm);      \
+      }                                                                                          \
     }                                                                                            \
     else if (SR == 0 && MODE != 2 && M.m)                                                        \
       k_detect_p16<T, TWO, (MODE == 2 ? 0 : MODE)><<<g, 256, 0, st>>>(D, ld, r, n, skip, tl,   \
                                                                           c1, r1, c2, r2, tau, o); \
-    {                                                                                            \
+    if (twin || !(SR == 0 && MODE != 2 && M.m8)) {                                               \
       auto kds = k_detect_stream<T, TWO, SR, MODE>;                                              \
       static const cudaError_t attr2 =                                                           \
           cudaFuncSetAttribute(kds, cudaFuncAttributeMaxDynamicSharedMemorySize, kDSSmem);        \
@@ -2882,7 +2896,7 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
   template cudaError_t detect<T>(T*, int64_t, Rows, int64_t, int64_t, const T*, const T*,          \
                                  const T*, const T*, float, int, int*, int*, int*, int*, T*,      \
                                  int64_t, DetectCounters*, const T*, int64_t, int, Mirror,        \
-                                 cudaStream_t, const void*);                                      \
+                                 cudaStream_t, const void*, bool);                                \
   template cudaError_t min_with_w<T>(T*, int64_t, Rows, int64_t, const T*, int64_t, cudaStream_t);  \
   template cudaError_t reset_pairs<T>(T*, int64_t, int64_t, const T*, int64_t, const int*,         \
                                       const int*, const DetectCounters*, int64_t, cudaStream_t);  \

@@ -265,8 +265,8 @@ def main():
 
     spec = dataclasses.replace(synth.C4, n=args.n, seed=args.seed)
     n0 = spec.n
-    # warm-up, timed, e2e and profiled steps each consume their own updates
-    steps_total = (args.warmup + 2 * args.steps + (0 if args.no_e2e else args.steps) +
+    # warm-up, timed, per-update-timing, e2e and profiled steps each consume their own updates
+    steps_total = (args.warmup + 3 * args.steps + (0 if args.no_e2e else args.steps) +
                    (0 if args.no_int32 else args.steps))
     cap = n0 + UPDATES_PER_STEP + 4 * steps_total
     t_setup = time.perf_counter()
@@ -316,16 +316,22 @@ def main():
             dvecs[up.t] = (torch.from_numpy(up.out_w).to(dev), torch.from_numpy(up.in_w).to(dev))
     setup_s = time.perf_counter() - t_setup
 
-    per_update = []   # (kind, ms, n_after, info)
+    per_update = []   # (kind, ms, n_after, info): the per-update-timing pass
+    timed_n = []      # n_after of every update of the timed region
 
-    def run_step(s, record):
+    def run_step(s, mode="plain"):
+        """One step's 64 updates through the C ABI.  mode "timed": nothing but
+        the library calls (n_after kept for the metric); "events": CUDA events
+        around every call (the per-type breakdown); "plain": the calls only."""
+        events = mode == "events"
         ups = seq[s * UPDATES_PER_STEP:(s + 1) * UPDATES_PER_STEP]
         evs = []
         infos = []
         for up in ups:
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
+            if events:
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
             if up.kind == "add":
                 o, i = dvecs[up.t]
                 _, info = L.apsp_add_node(h.h, o.data_ptr(), i.data_ptr())
@@ -333,16 +339,19 @@ def main():
                 _, info = L.apsp_remove_node(h.h, up.k)
             else:
                 info = L.apsp_update_edge(h.h, up.u, up.v, float(up.w_new))
-            b.record(stream)
-            evs.append((a, b))
+            if events:
+                b.record(stream)
+                evs.append((a, b))
             infos.append((up.kind, info))
-        if record:
+        if mode == "timed":
+            timed_n.extend(info.n_after for _, info in infos)
+        if events:
             torch.cuda.synchronize(dev)
             for (a, b), (kind, info) in zip(evs, infos):
                 per_update.append((kind, a.elapsed_time(b), info.n_after, info.as_dict()))
 
     for s in range(args.warmup):
-        run_step(s, False)
+        run_step(s)
     torch.cuda.synchronize(dev)
 
     # ---------------- timed region (device-resident inputs)
@@ -356,7 +365,7 @@ def main():
     t0.record(stream)
     torch.cuda.nvtx.range_push("timed")   # (ncu --nvtx --nvtx-include "timed/": the timed region's launches)
     for s in range(args.warmup, args.warmup + args.steps):
-        run_step(s, True)
+        run_step(s, "timed")
     torch.cuda.nvtx.range_pop()
     t1.record(stream)
     barrier()
@@ -365,14 +374,20 @@ def main():
     clocks = clk.stop(gpu_index=None) if rank == 0 else None
 
 
-    entries = sum(na * na for _, _, na, _ in per_update)
+    entries = sum(na * na for na in timed_n)
     value = entries / (total_ms / 1e3)
     ms_per_step = total_ms / args.steps
+
+    # ---------------- per-update times (CUDA events around every call): the
+    # per-type breakdown, on the next K steps (not the timed region)
+    s_pu = args.warmup + args.steps
+    for s in range(s_pu, s_pu + args.steps):
+        run_step(s, "events")
 
     # ---------------- e2e: public API with host buffers, copies inside the timed region
     e2e = None
     if not args.no_e2e:
-        s_lo = args.warmup + args.steps
+        s_lo = args.warmup + 2 * args.steps
         pinned = {}
         for up in seq[s_lo * UPDATES_PER_STEP:]:
             if up.kind == "add":
@@ -418,9 +433,9 @@ def main():
     p0 = torch.cuda.Event(enable_timing=True)
     p1 = torch.cuda.Event(enable_timing=True)
     p0.record(stream)
-    s_prof = args.warmup + args.steps + (0 if args.no_e2e else args.steps)
+    s_prof = args.warmup + 2 * args.steps + (0 if args.no_e2e else args.steps)
     for s in range(s_prof, s_prof + args.steps):
-        run_step(s, False)
+        run_step(s)
     p1.record(stream)
     barrier()
     prof_total_ms = max_over_ranks(p0.elapsed_time(p1))
@@ -435,13 +450,13 @@ def main():
     if not args.no_int32:
         L.apsp_set_option(h.h, L.OPT_MIRROR, 0)
         s32 = s_prof + args.steps
-        run_step(s32, False)     # the first update after the switch drops the mirror
+        run_step(s32)     # the first update after the switch drops the mirror
         torch.cuda.synchronize(dev)
         L.apsp_profile_reset(h.h)
         L.apsp_profile_enable(h.h, True)
         barrier()
         for s in range(s32 + 1, s32 + args.steps):
-            run_step(s, False)
+            run_step(s)
         barrier()
         L.apsp_profile_enable(h.h, False)
         prof32 = L.apsp_profile_read(h.h)

@@ -170,8 +170,9 @@ struct apsp_handle {
   int fw16 = 1;                  // int16x2 FW when exact (int32 shortest path, one GPU)
   int last_fw16 = 0;             // 1: the last FW ran packed, 2: it fell back to int32
   bool mirror_built = false;     // the mirror was built (or invalidated) from D
-  bool mirror_hint = false;      // last observed mirror state was "valid" (profile accounting only)
+  bool mirror_hint = false;      // last host read of the mirror flag said "valid" (gates the shortcuts / twins; see mirror_fresh)
   bool mirror_fresh = false;     // no kernel that can write a new value ran since that observation
+  bool sl_join = false;          // shortlist upkeep pending on st2: join (ev_join) before reading them
   int mirror_level = 16;         // width of the mirror: 8 or 16 bits
   int mirror8 = 1;               // APSP_OPT_MIRROR8: try the int8 width at each build
   int use_mirror = 1;            // APSP_OPT_MIRROR: 0 = no mirror, the streams read D (4 B/entry)
@@ -875,7 +876,15 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   // the result is still exact.
   const bool try_sparse = h->force_path != 2;
   const bool fused = use_fused<T>(h, c2 != nullptr) && try_sparse;
+  auto sl_join = [&]() -> apsp_status {   // the side stream's shortlist upkeep (update_edge)
+    if (h->sl_join) {
+      CKR(cudaStreamWaitEvent(h->st, h->ev_join, 0));
+      h->sl_join = false;
+    }
+    return APSP_OK;
+  };
   if (fused) {
+    { apsp_status sj = sl_join(); if (sj != APSP_OK) return sj; }
     // detection + phase A in one pass over the int8 mirror (fused.cu); the
     // pairs it could not buffer get the stand-alone phase A below
     PK(APSP_K_DETECT, (double)(r.hi - r.lo) * (double)n,
@@ -934,6 +943,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   if (try_sparse) {
     // A: every listed entry rewritten with a walk length of G' (stale entries
     // skipped by the detection predicate), certified where it reaches lb
+    { apsp_status sj = sl_join(); if (sj != APSP_OK) return sj; }
     if (!fused)
     PK(APSP_K_SPARSE0, 0.0,
        sparse_phase_a<T>(h->Dl<T>(), h->ld, r, h->slid(), h->slw<T>(), h->rowoff(), h->srow(), h->scol(),
@@ -981,6 +991,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     apsp_status s2 = fork_shortlist_remove<T>(h, skip);
     if (s2 != APSP_OK) return s2;
   }
+  { apsp_status sj = sl_join(); if (sj != APSP_OK) return sj; }   // (forced dense: joined here)
   // ---- the one host read of this update: counters (summed over ranks) ----
   long long* hv = reinterpret_cast<long long*>(h->host_small);
   unsigned* hmf = reinterpret_cast<unsigned*>(h->host_small) + 12;
@@ -1090,17 +1101,17 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
   // invalidated the shortcuts are dropped)
   bool srow = false;
   // (small graphs: the one streaming pass costs less than the shortcuts' extra launches)
-  if constexpr (std::is_same<T, int32_t>::value)
-    srow = h->world == 1 && n >= kAddShortcutMinN && n < (int64_t(1) << 24) && h->plan.maxchunk >= 2 &&
-           2 * kAddColLimit <= ld && mirror8_hint(h);   // (k_addrow packs t in 24 bits)
+  const bool shortcut_shape = std::is_same<T, int32_t>::value && n >= kAddShortcutMinN && n < (int64_t(1) << 24) &&
+                              h->plan.maxchunk >= 2 && 2 * kAddColLimit <= ld;   // (k_addrow packs t in 24 bits)
   if constexpr (std::is_same<T, int32_t>::value) {
+    srow = h->world == 1 && shortcut_shape && mirror8_hint(h);
     if (srow) {
       CKR(cudaEventRecord(h->ev_fork, h->st));
       CKR(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
       // scratch: the (value, minimiser) row, the minimiser flags and U's in /
       // out lists live in the pass-1 partial buffer (4 ld words: unused unless
       // the gathers fall back to pass 1, which runs after they are consumed)
-      CK2(addrow_s(as, ow, n, h->mirror<T>().m8, ld, h->row0, row, ld, reinterpret_cast<int*>(h->vec<T>(5)),
+      CK2(addrow_s(as, ow, n, h->mirror<T>().m8, ld, h->row0, h->rows, row, ld, reinterpret_cast<int*>(h->vec<T>(5)),
                    reinterpret_cast<unsigned long long*>(h->rowpart<T>()),
                    reinterpret_cast<int*>(h->rowpart<T>()) + 2 * ld, h->st2));
       CKR(cudaEventRecord(h->ev_row, h->st2));
@@ -1122,6 +1133,30 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
     // last host read: no shortcuts; the row chain's scratch must be free first
     srow = false;
     CKR(cudaStreamWaitEvent(h->st, h->ev_row, 0));
+  }
+  if constexpr (std::is_same<T, int32_t>::value) {
+    if (h->world > 1 && shortcut_shape) {
+      // sharded: every rank must take the same path (collectives inside), so
+      // the ranks agree on their mirrors first; then the new row from the
+      // rows that can attain it, each rank over its own rows of S
+      int* agree = reinterpret_cast<int*>(h->small() + 2048);
+      CKR(cudaMemsetAsync(agree, mirror8_known_valid(h) ? 1 : 0, sizeof(int), h->st));
+      NK(h->comm->allreduce(agree, 1, ncclInt32, ncclMin, h->st));
+      CKR(cudaMemcpyAsync(h->host_small, agree, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+      CKR(cudaStreamSynchronize(h->st));
+      srow = *reinterpret_cast<int*>(h->host_small) != 0;
+      if (srow) {
+        const uint8_t* m8 = h->mirror<T>().m8;
+        int* slist = reinterpret_cast<int*>(h->vec<T>(5));
+        auto* packed = reinterpret_cast<unsigned long long*>(h->rowpart<T>());
+        int* tflag = reinterpret_cast<int*>(h->rowpart<T>()) + 2 * ld;
+        CK(addrow_s(as, ow, n, m8, ld, h->row0, h->rows, row, ld, slist, packed, tflag, h->st, 1));
+        NK(h->comm->allreduce(as.rmax, 1, ncclInt32, ncclMax, h->st));
+        CK(addrow_s(as, ow, n, m8, ld, h->row0, h->rows, row, ld, slist, packed, tflag, h->st, 2));
+        NK(h->comm->allreduce(packed, (size_t)ld, ncclUint64, ncclMin, h->st));
+        CK(addrow_s(as, ow, n, m8, ld, h->row0, h->rows, row, ld, slist, packed, tflag, h->st, 3));
+      }
+    }
   }
   // shortlist upkeep needs only the validated edge vectors: it runs on the
   // side stream while pass 1 / rank-1 stream D (joined before returning)
@@ -1145,8 +1180,8 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
     if (!srow) CKR(cudaMemsetAsync(unc, 0, sizeof(unsigned), h->st));   // (the gather path never reads it)
     const unsigned* cfull = nullptr;
     if constexpr (std::is_same<T, int32_t>::value) {
-      if (srow) {   // the new row first (side stream), then col / the skip bound by gathers
-        CKR(cudaStreamWaitEvent(h->st, h->ev_row, 0));
+      if (srow) {   // the new row first (side stream; sharded: done above), then col / the skip bound by gathers
+        if (h->world == 1) CKR(cudaStreamWaitEvent(h->st, h->ev_row, 0));
         PK(APSP_K_ADD_PASS1, 0.0,
            addcol_g(as, r, h->mirror<T>().m8, ld, n, iw, ow, reinterpret_cast<int*>(h->rowpart<T>()) + 2 * ld,
                     reinterpret_cast<int*>(h->vec<T>(5)), reinterpret_cast<int*>(h->rowpart<T>()) + 3 * ld,
@@ -1181,7 +1216,7 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
     CK(addnode_finish<T>(h->rowpart<T>(), rowpartM, nchunk, h->colpart<T>(), nslab, ld, r, n, ld, col,
                          ceff, row, try_packed ? 2 : 0, h->mirror<T>(), unc, h->st));
   }
-  if (h->world > 1)
+  if (h->world > 1 && !srow)   // (the shortcut's row is already complete)
     NK(h->comm->allreduce(row, (size_t)ld, nccl_type<T>(), ncclMin, h->st));
   // rows with ceff[i] = INF provably do not change and are not read at all
   PK(APSP_K_RANK1, 0.0,   // work: bytes actually read, counted on the device
@@ -1333,9 +1368,14 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
     s = snap_pivots<T>(h, v, w_old, c2, u, r2);
     if (s != APSP_OK) return s;
   }
-  // W' (WT and the shortlists) before the recompute reads them
+  // W' before the recompute reads it: WT here, the shortlists on the side
+  // stream (recompute joins it before its first shortlist reader)
   CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
-  CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
+  CKR(cudaEventRecord(h->ev_fork, h->st));
+  CKR(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
+  CK2(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st2));
+  CKR(cudaEventRecord(h->ev_join, h->st2));
+  h->sl_join = true;
   {   // the detection pass reads the mirror (early exits and decreases do not)
     apsp_status ms = ensure_mirror<T>(h);
     if (ms != APSP_OK) return ms;
@@ -1745,6 +1785,7 @@ apsp_status create_impl(apsp_handle** out, apsp_dtype dtype, int directed, int64
     CKR(cudaMemsetAsync(h->ws + h->plan.off_small, 0, 512, h->st));   // counters, flags
     CKR(cudaMemsetAsync(h->mirror_flag(), 0xff, sizeof(unsigned), h->st));   // no mirror yet
     CKR(cudaMemsetAsync(h->heavy_x(), 0x7f, sizeof(int32_t) * (size_t)kHeavy * h->ld, h->st));   // X: "INF"
+    CKR(cudaMemsetAsync(h->slscr(), 0, 256 + sizeof(int) * (size_t)kSLBins, h->st));   // SL(x) selection state
     CK(fill<T>(h->WT<T>(), (int64_t)cap * h->ld, Tr<T>::inf(), h->st));
     CKR(cudaMemsetAsync(&h->ctr()->err, 0, sizeof(unsigned), h->st));
     CKR(cudaMemsetAsync(h->wmin_dev(), 0xff, sizeof(unsigned), h->st));

@@ -118,9 +118,14 @@ struct AddScratch {
   unsigned long long* work;   // cumulative algorithmic bytes of the column pass (profile)
 };
 cudaError_t add_init(const AddScratch& a, unsigned* err, unsigned* wmin, cudaStream_t st);
+// The new row of an add from the rows that can attain it.  stage 0: all of
+// it (one GPU); sharded: stage 1 (this rank's part of the bound, into
+// *a.rmax: all-reduce(max) it), stage 2 (S and the partial row over this
+// rank's rows of S, into `packed`: all-reduce(min) it as uint64), stage 3
+// (the row and the minimiser flags from `packed`)
 cudaError_t addrow_s(const AddScratch& a, const int32_t* ow, int64_t n, const uint8_t* m8, int64_t ld, int64_t row0,
-                     int32_t* row, int64_t npad, int* slist, unsigned long long* packed, int* tflag,
-                     cudaStream_t st);
+                     int64_t rows, int32_t* row, int64_t npad, int* slist, unsigned long long* packed, int* tflag,
+                     cudaStream_t st, int stage = 0);
 // *a.ufull = 1 when |U| exceeded `limit`: pass 1 + the finish kernel compute col instead
 cudaError_t addcol_g(const AddScratch& a, Rows r, const uint8_t* m8, int64_t ld, int64_t n, const int32_t* iw,
                      const int32_t* ow, const int* tflag, int* ulist, int* uaux /* 2 * limit */, int limit,
@@ -199,7 +204,11 @@ cudaError_t shortlist_swap(int* SLid, T* SLw, T* wnext, int64_t n, int64_t p, in
 constexpr int kSLK = 16;              // shortlist entries per lane
 constexpr int kSL = 32 * kSLK;        // shortlist entries per node
 constexpr int kSLG = 32;              // shortlist_build_one: partial lists (CTAs) at most
-constexpr size_t kSLScratch = (size_t)kSLG * kSL * 8 + (size_t)kSLG * 4;   // its scratch bytes
+// its scratch: [control 256 B | histogram kSLBins ints | the sort path's lists]
+// (control and histogram zero between calls: zeroed at creation, reset by the
+// kernels that used them)
+constexpr int kSLBins = 4096;
+constexpr size_t kSLScratch = 256 + (size_t)kSLBins * 4 + (size_t)kSLG * kSL * 8 + (size_t)kSLG * 4;
 template <typename T>
 cudaError_t shortlist_build(const T* WT, int64_t ldw, int64_t n, const int* rows, int64_t r0,
                             int64_t r1, int* SLid, T* SLw, T* wnext, cudaStream_t st);

@@ -232,7 +232,8 @@ __device__ __forceinline__ T sl_block_min(T v, T* red) {
 }
 template <typename T>
 __global__ void __launch_bounds__(kSLC) k_sl_one_part(const T* __restrict__ row, int64_t n, int64_t j,
-                                                      T* cw_out, int* ci_out, T* rej_out) {
+                                                      T* cw_out, int* ci_out, T* rej_out, const int* gate) {
+  if (*(volatile const int*)gate == 0) return;   // the selection path did it
   __shared__ T cw[kSLC], rw[kSL];
   __shared__ int ci[kSLC], ri[kSL];
   __shared__ T red[32];
@@ -284,7 +285,8 @@ __global__ void __launch_bounds__(kSLC) k_sl_one_part(const T* __restrict__ row,
 template <typename T>
 __global__ void __launch_bounds__(kSLC) k_sl_one_merge(const T* __restrict__ cw_in, const int* __restrict__ ci_in,
                                                        const T* __restrict__ rej_in, int G, int Gp, int64_t j,
-                                                       int* SLid, T* SLw, T* wnext) {
+                                                       int* SLid, T* SLw, T* wnext, int* gate) {
+  if (*(volatile const int*)gate == 0) return;   // the selection path did it
   extern __shared__ __align__(16) unsigned char sm_raw[];
   T* w = reinterpret_cast<T*>(sm_raw);
   int* id = reinterpret_cast<int*>(sm_raw + sizeof(T) * (size_t)Gp * kSL);
@@ -315,18 +317,186 @@ __global__ void __launch_bounds__(kSLC) k_sl_one_merge(const T* __restrict__ cw_
     SLw[j * kSL + tid] = w[tid];
   }
   rej = sl_block_min<T>(rej, red);
-  if (tid == 0) wnext[j] = rej;
+  if (tid == 0) {
+    wnext[j] = rej;
+    *gate = 0;   // reset for the next call
+  }
 }
+
+// The selection path (round 2): a histogram of the weights' order-preserving
+// 32-bit keys on a log scale (keys < 128 exact, above that 128 bins per power
+// of two) finds the bin b* holding the kSL-th smallest entry; one CTA then
+// collects every entry in bins <= b* (if at most kSelCap of them), sorts them
+// by (weight, id) and keeps the first kSL; wnext = the smallest weight left
+// out (a collected entry past kSL, or the smallest entry above b*).  Exactly
+// the sort path's result; that path runs instead when bin b* is too full.
+constexpr int kSelCap = 4096;
+__device__ __forceinline__ int sl_bin(uint32_t k) {
+  if (k < 128u) return (int)k;
+  const int e = 31 - __clz(k);                         // >= 7
+  return (e - 6) * 128 + (int)((k >> (e - 7)) & 127u);   // < (31 - 6) * 128 + 128 = 3328
+}
+template <typename T>
+__device__ __forceinline__ uint32_t sl_key32(T w) {
+  uint32_t k;
+  memcpy(&k, &w, 4);   // int32 >= 0 and IEEE floats >= 0 order like their bits
+  return k;
+}
+template <typename T>
+__global__ void __launch_bounds__(256) k_sl_hist(const T* __restrict__ row, int64_t n, int64_t j, int* hist) {
+  __shared__ int h[kSLBins];
+  for (int b = threadIdx.x; b < kSLBins; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const T x = row[e];
+    if (e != j && Tr<T>::fin(x)) atomicAdd(&h[sl_bin(sl_key32<T>(x))], 1);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kSLBins; b += blockDim.x)
+    if (h[b]) atomicAdd(hist + b, h[b]);
+}
+template <typename T>
+__global__ void __launch_bounds__(1024) k_sl_select(const T* __restrict__ row, int64_t n, int64_t j, int* hist,
+                                                    int* gate, int* SLid, T* SLw, T* wnext) {
+  extern __shared__ __align__(16) unsigned long long keys[];   // kSelCap
+  __shared__ int cum[1024];
+  __shared__ int s_b, s_c;
+  __shared__ unsigned long long s_out;
+  const int tid = threadIdx.x;
+  // per thread 4 consecutive bins: inclusive scan of the bin counts
+  int c4[4], tot = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) { c4[q] = hist[4 * tid + q]; hist[4 * tid + q] = 0; tot += c4[q]; }
+  cum[tid] = tot;
+  if (tid == 0) { s_b = kSLBins - 1; s_c = 0; s_out = ~0ull; }
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {   // Hillis-Steele scan
+    const int v = tid >= o ? cum[tid - o] : 0;
+    __syncthreads();
+    cum[tid] += v;
+    __syncthreads();
+  }
+  const int total = cum[1023];
+  const int want = min(total, kSL);
+  {   // the first bin whose inclusive count reaches `want`
+    int run = cum[tid] - tot;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int before = run;
+      run += c4[q];
+      if (want > 0 && before < want && run >= want) { s_b = 4 * tid + q; s_c = run; }
+    }
+  }
+  __syncthreads();
+  const int bstar = want > 0 ? s_b : -1, cnt = want > 0 ? s_c : 0;
+  if (cnt > kSelCap) {   // bin b* too full: the sort path (gated kernels after this one)
+    if (tid == 0) *gate = 1;
+    return;
+  }
+  __syncthreads();
+  if (tid == 0) s_c = 0;
+  __syncthreads();
+  // collect the entries of bins <= b*; the smallest entry above b* for wnext
+  unsigned long long out = ~0ull;
+  for (int64_t e0 = 0; e0 < n; e0 += 8 * (int64_t)blockDim.x) {   // 8 loads in flight per thread
+    T x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t e = e0 + q * (int64_t)blockDim.x + tid;
+      x[q] = e < n ? row[e] : Tr<T>::inf();
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t e = e0 + q * (int64_t)blockDim.x + tid;
+      if (e >= n || e == j || !Tr<T>::fin(x[q])) continue;
+      const uint32_t k = sl_key32<T>(x[q]);
+      const unsigned long long key = (unsigned long long)k << 32 | (unsigned)e;
+      if (sl_bin(k) <= bstar) keys[atomicAdd(&s_c, 1)] = key;
+      else out = min(out, key);
+    }
+  }
+  atomicMin(&s_out, out);
+  __syncthreads();
+  int P = 1;
+  while (P < cnt) P <<= 1;
+  if (P <= 1024) {   // one key per thread: strides < 32 by shuffles, the rest through shared memory
+    unsigned long long x = tid < cnt ? keys[tid] : ~0ull;
+    for (int k = 2; k <= 1024; k <<= 1)   // bitonic sort, ascending (weight, id)
+      for (int jj = k >> 1; jj > 0; jj >>= 1) {
+        unsigned long long y;
+        if (jj >= 32) {
+          __syncthreads();
+          keys[tid] = x;
+          __syncthreads();
+          y = keys[tid ^ jj];
+        } else {
+          y = __shfl_xor_sync(0xffffffffu, x, jj);
+        }
+        const bool up = (tid & k) == 0, lo = (tid & jj) == 0;
+        x = (up == lo) ? min(x, y) : max(x, y);
+      }
+    __syncthreads();
+    keys[tid] = x;
+    __syncthreads();
+  } else {
+    for (int e = cnt + tid; e < P; e += blockDim.x) keys[e] = ~0ull;
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)   // bitonic sort, ascending (weight, id)
+      for (int jj = k >> 1; jj > 0; jj >>= 1) {
+        for (int i = tid; i < P; i += blockDim.x) {
+          const int l = i ^ jj;
+          if (l > i) {
+            const unsigned long long a = keys[i], b = keys[l];
+            if (((i & k) == 0) == (a > b)) { keys[i] = b; keys[l] = a; }
+          }
+        }
+        __syncthreads();
+      }
+  }
+  for (int i = tid; i < kSL; i += blockDim.x) {
+    const unsigned long long key = i < cnt ? keys[i] : ~0ull;
+    T w;
+    const uint32_t k = (uint32_t)(key >> 32);
+    memcpy(&w, &k, 4);
+    SLid[j * kSL + i] = key == ~0ull ? -1 : (int)(key & 0xFFFFFFFFull);
+    SLw[j * kSL + i] = key == ~0ull ? Tr<T>::inf() : w;
+  }
+  if (tid == 0) {
+    const unsigned long long left = min(cnt > kSL ? keys[kSL] : ~0ull, s_out);
+    T w = Tr<T>::inf();
+    if (left != ~0ull) {
+      const uint32_t k = (uint32_t)(left >> 32);
+      memcpy(&w, &k, 4);
+    }
+    wnext[j] = w;
+  }
+}
+
 template <typename T>
 cudaError_t shortlist_build_one(const T* WT, int64_t ldw, int64_t n, int64_t j, int* SLid, T* SLw,
                                 T* wnext, void* scratch, cudaStream_t st) {
   const int G = (int)std::max<int64_t>(1, std::min<int64_t>(kSLG, cdiv(n, kSLC)));
   int Gp = 1;
   while (Gp < G) Gp <<= 1;
-  T* cw = reinterpret_cast<T*>(scratch);
+  int* gate = reinterpret_cast<int*>(scratch);                      // control word 0
+  int* hist = reinterpret_cast<int*>(static_cast<char*>(scratch) + 256);
+  T* cw = reinterpret_cast<T*>(hist + kSLBins);
   int* ci = reinterpret_cast<int*>(cw + (size_t)kSLG * kSL);
   T* rj = reinterpret_cast<T*>(ci + (size_t)kSLG * kSL);
-  k_sl_one_part<T><<<G, kSLC, 0, st>>>(WT + j * ldw, n, j, cw, ci, rj);
+  const T* row = WT + j * ldw;
+  k_sl_hist<T><<<(int)std::min<int64_t>(cdiv(n, 1024), 2 * num_sms()), 256, 0, st>>>(row, n, j, hist);
+  CUDA_TRY(cudaGetLastError());
+  static bool attr_sel = false;
+  if (!attr_sel) {
+    CUDA_TRY(cudaFuncSetAttribute(k_sl_select<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(8 * kSelCap)));
+    CUDA_TRY(cudaFuncSetAttribute(k_sl_select<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(8 * kSelCap)));
+    attr_sel = true;
+  }
+  k_sl_select<T><<<1, 1024, 8 * kSelCap, st>>>(row, n, j, hist, gate, SLid, SLw, wnext);
+  CUDA_TRY(cudaGetLastError());
+  k_sl_one_part<T><<<G, kSLC, 0, st>>>(row, n, j, cw, ci, rj, gate);
   CUDA_TRY(cudaGetLastError());
   const size_t smem = (sizeof(T) + sizeof(int)) * (size_t)Gp * kSL;
   static bool attr = false;
@@ -337,7 +507,7 @@ cudaError_t shortlist_build_one(const T* WT, int64_t ldw, int64_t n, int64_t j, 
                                   (int)((sizeof(float) + sizeof(int)) * (size_t)kSLG * kSL)));
     attr = true;
   }
-  k_sl_one_merge<T><<<1, kSLC, smem, st>>>(cw, ci, rj, G, Gp, j, SLid, SLw, wnext);
+  k_sl_one_merge<T><<<1, kSLC, smem, st>>>(cw, ci, rj, G, Gp, j, SLid, SLw, wnext, gate);
   return cudaGetLastError();
 }
 

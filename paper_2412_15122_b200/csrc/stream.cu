@@ -879,19 +879,16 @@ cudaError_t add_init(const AddScratch& a, unsigned* err, unsigned* wmin, cudaStr
   k_add_init<<<1, 1, 0, st>>>(a, err, wmin);
   return cudaGetLastError();
 }
-// Rb = out[t0] + max_j D[t0][j] (t0 = the cheapest out-edge; INF in row t0:
-// every finite out); one CTA reads the 1 KB... n bytes of mirror row t0
+// max_j D[t0][j] (t0 = the cheapest out-edge), on the rank that holds row t0
+// (others keep *rmax = 0; sharded, an all-reduce(max) follows); one CTA
+// reads the n bytes of mirror row t0
 __global__ void __launch_bounds__(1024) k_addrow_bound(AddScratch a, const uint8_t* __restrict__ m8, int64_t ld,
-                                                       int64_t row0, int64_t n) {
+                                                       int64_t row0, int64_t rows, int64_t n) {
   __shared__ int32_t red[32];
   const unsigned long long am = *a.argmin_out;
-  const int32_t I = APSP_INF_I32_DEV;
-  if (am == ~0ull || (int32_t)(am >> 32) >= I) {   // no out-edge: S is empty
-    if (threadIdx.x == 0) *a.rb = -1;
-    return;
-  }
-  const int32_t omin = (int32_t)(am >> 32);
+  if (am == ~0ull || (int32_t)(am >> 32) >= APSP_INF_I32_DEV) return;   // no out-edge: S is empty
   const int64_t t0 = (int64_t)(am & 0xFFFFFFFFull);
+  if (t0 < row0 || t0 >= row0 + rows) return;   // another rank's row
   const uint8_t* mr = m8 + (t0 - row0) * ld;
   int32_t mx = 0;
   for (int64_t j = threadIdx.x; j < n; j += blockDim.x) mx = max(mx, (int32_t)mr[j]);
@@ -900,14 +897,18 @@ __global__ void __launch_bounds__(1024) k_addrow_bound(AddScratch a, const uint8
   __syncthreads();
   if (threadIdx.x < 32) {
     mx = __reduce_max_sync(0xffffffffu, threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0);
-    if (threadIdx.x == 0) *a.rb = mx >= kSat8i ? I - 1 : omin + mx;
+    if (threadIdx.x == 0) *a.rmax = mx;
   }
 }
+// Rb = out[t0] + max_j D[t0][j] (an INF in row t0: every finite out);
 // S = {t : out[t] <= Rb}; the packed (value, minimiser) row := none; the
 // minimiser flags := 0
 __global__ void k_addrow_compact(AddScratch a, const int32_t* __restrict__ ow, int64_t n, int64_t npad, int* slist,
                                  unsigned long long* packed, int* tflag) {
-  const int32_t rb = *a.rb;
+  const unsigned long long am = *a.argmin_out;
+  const int32_t I = APSP_INF_I32_DEV;
+  const int32_t mx = *a.rmax, omin = (int32_t)(am >> 32);
+  const int32_t rb = (am == ~0ull || omin >= I) ? -1 : (mx >= kSat8i ? I - 1 : omin + mx);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < npad; t += (int64_t)gridDim.x * blockDim.x) {
     packed[t] = ~0ull;
     tflag[t] = 0;
@@ -923,7 +924,7 @@ __global__ void k_addrow_compact(AddScratch a, const int32_t* __restrict__ ow, i
 __global__ void __launch_bounds__(256) k_addrow(AddScratch a, const int32_t* __restrict__ ow,
                                                 const int* __restrict__ slist, const int* __restrict__ scount,
                                                 const uint8_t* __restrict__ m8, int64_t ld, int64_t row0,
-                                                int64_t n, unsigned long long* packed) {
+                                                int64_t rows, int64_t n, unsigned long long* packed) {
   const int cnt = *scount;
   const int64_t j0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
   if (j0 >= n) return;
@@ -933,6 +934,7 @@ __global__ void __launch_bounds__(256) k_addrow(AddScratch a, const int32_t* __r
 #pragma unroll 4
   for (int s = s0; s < s1; ++s) {
     const int t = slist[s];
+    if (t < row0 || t >= row0 + rows) continue;   // another rank's row (sharded: all-reduced after)
     const int32_t o = ow[t];
     const unsigned long long lo = (unsigned long long)(((unsigned)min(o - omin, 255) << 24) | (unsigned)t);
     const uint32_t w = *reinterpret_cast<const uint32_t*>(m8 + ((int64_t)t - row0) * ld + j0);
@@ -1194,17 +1196,21 @@ cudaError_t addcol_g(const AddScratch& a, Rows r, const uint8_t* m8, int64_t ld,
 }
 
 cudaError_t addrow_s(const AddScratch& a, const int32_t* ow, int64_t n, const uint8_t* m8, int64_t ld, int64_t row0,
-                     int32_t* row, int64_t npad, int* slist, unsigned long long* packed, int* tflag,
-                     cudaStream_t st) {
-  k_addrow_bound<<<1, 1024, 0, st>>>(a, m8, ld, row0, n);
-  CUDA_TRY(cudaGetLastError());
+                     int64_t rows, int32_t* row, int64_t npad, int* slist, unsigned long long* packed, int* tflag,
+                     cudaStream_t st, int stage) {
   const int g = (int)std::min<int64_t>(cdiv(npad, 256), 2 * num_sms());
-  k_addrow_compact<<<g, 256, 0, st>>>(a, ow, n, npad, slist, packed, tflag);
-  CUDA_TRY(cudaGetLastError());
-  const dim3 grid((unsigned)cdiv(cdiv(n, 4), 256), 16);
-  k_addrow<<<grid, 256, 0, st>>>(a, ow, slist, a.s_count, m8, ld, row0, n, packed);
-  CUDA_TRY(cudaGetLastError());
-  k_addrow_final<<<g, 256, 0, st>>>(packed, npad, row, tflag);
+  if (stage == 0 || stage == 1) {   // the bound's row maximum (rank of t0)
+    k_addrow_bound<<<1, 1024, 0, st>>>(a, m8, ld, row0, rows, n);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (stage == 0 || stage == 2) {   // S, then the partial row over this rank's rows of S
+    k_addrow_compact<<<g, 256, 0, st>>>(a, ow, n, npad, slist, packed, tflag);
+    CUDA_TRY(cudaGetLastError());
+    const dim3 grid((unsigned)cdiv(cdiv(n, 4), 256), 16);
+    k_addrow<<<grid, 256, 0, st>>>(a, ow, slist, a.s_count, m8, ld, row0, rows, n, packed);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (stage == 0 || stage == 3) k_addrow_final<<<g, 256, 0, st>>>(packed, npad, row, tflag);
   return cudaGetLastError();
 }
 

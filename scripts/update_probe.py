@@ -2,7 +2,11 @@
 (n=65536 int32 log-uniform), after a warm-up one, inside the NVTX range
 "probe" (ncu --nvtx --nvtx-include "probe/" lists just its launches).
 
-    python scripts/update_probe.py c2|c5
+    python scripts/update_probe.py c2|c5 [--bench-edge]
+
+--bench-edge: the tight increase scripts/bench_configs.py times (the cheapest
+edge of synth.random_edge(seed, 2)'s tail), after one on the next node.
+Prints each update's time, info and the heavy-row set it selected.
 """
 import os
 import sys
@@ -29,7 +33,11 @@ def tight(u):
     return int(np.argmin(row))
 
 
-for it, u in enumerate((11, 12)):
+us = (11, 12)
+if len(sys.argv) > 2 and sys.argv[2] == "--bench-edge":   # bench_configs.py's tight increase
+    u2, _ = synth.random_edge(spec.seed, 2, synth.HostGraph(W, spec.directed))
+    us = ((u2 + 1) % spec.n, u2)
+for it, u in enumerate(us):
     v = tight(u)
     w = W[u, v] * (10 if W.dtype == np.int32 else np.float32(10))
     if it == 1:

@@ -279,3 +279,60 @@ def test_nccl_transport_loads(P):
     a = P._lib.apsp_nccl_unique_id()
     b = P._lib.apsp_nccl_unique_id()
     assert len(a) == 128 and a != b
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_add_shortcuts(P, world):
+    """The add-node shortcuts on sharded handles (n >= 4096, int8 mirror):
+    the ranks agree on their mirrors, the bound's row maximum and the partial
+    new rows are all-reduced, each rank gathers its own rows' column from
+    its transposed mirror.  Adds (one with every in-edge equally cheap: the
+    gathered column set over its limit, the streaming fallback), a removal in
+    between; the gathered D bit-identical to world 1 after every update and
+    to the oracle's FW at the end."""
+    rng = np.random.default_rng(77 + world)
+    n = 4100
+    cap = n + 8
+    W = random_graph(rng, n, True, density=0.05, lo=1, hi=9)
+    hg = synth.HostGraph(W, True, cap=cap)
+    ops = []
+    for step in range(4):
+        if step == 2:
+            k = int(rng.integers(hg.n))
+            hg.remove_node(k)
+            ops.append(("remove", k))
+            continue
+        o = rng.integers(1, 12, hg.n).astype(np.int32)
+        i = np.full(hg.n, 3, np.int32) if step == 3 else rng.integers(1, 12, hg.n).astype(np.int32)
+        hg.add_node(o, i)
+        ops.append(("add", o, i))
+    g = P._lib.apsp_local_group_create(world)
+
+    def rank(r):
+        st = torch.cuda.Stream()
+        h = P.WarmAPSP(torch.from_numpy(np.ascontiguousarray(W)), directed=True, cap=cap,
+                       device="cuda:0", stream=st, rank=r, world=world, local_group=g)
+        snaps = []
+        for op in ops:
+            apply(h, op)
+            st.synchronize()
+            snaps.append(h.D.cpu().numpy().copy())
+        width = h.mirror_width
+        h.close()
+        return snaps, width
+
+    try:
+        res = run_ranks(world, rank, timeout=600)
+    finally:
+        torch.cuda.synchronize()
+        P._lib.apsp_local_group_destroy(g)
+    assert all(res[r][1] == 8 for r in range(world)), "every rank on the int8 mirror"
+    h1 = P.WarmAPSP(torch.from_numpy(np.ascontiguousarray(W)), directed=True, cap=cap)
+    for j, op in enumerate(ops):
+        apply(h1, op)
+        torch.cuda.synchronize()
+        D1 = h1.D.cpu().numpy()
+        Dj = gather([res[r][0][j] for r in range(world)], D1.shape[0])
+        assert np.array_equal(Dj, D1), f"sharded D differs from world 1 after op {j} {op[0]}"
+    h1.close()
+    assert np.array_equal(Dj, oracle.fw(hg.W[:hg.n, :hg.n]))

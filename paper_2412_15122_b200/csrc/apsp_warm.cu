@@ -38,7 +38,7 @@ constexpr int64_t kTile = 128;       // FW pivot block / row-partition granule
 constexpr int kMaxSlabs = 256;       // add-node column partial slabs
 constexpr int kAddColLimit = 2048;   // columns the add-node gathers may read per row (else the stream)
 constexpr int64_t kAddShortcutMinN = 4096;   // the add-node shortcuts from this n on
-constexpr int64_t kVecs = 8;         // scratch vectors of ld elements
+constexpr int64_t kVecs = 9;         // scratch vectors of ld elements
 constexpr int kQueryChunk = 32;      // sharded queries per column all-gather
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
@@ -301,6 +301,8 @@ struct apsp_handle {
   int* coop_rounds_word() { return reinterpret_cast<int*>(ws + plan.off_small + 480); }
   int* coop_total_word() { return reinterpret_cast<int*>(ws + plan.off_small + 484); }
   int* heavy_set() { return reinterpret_cast<int*>(ws + plan.off_heavy); }
+  // the pivot row snapshot r1 as saturated bytes (update_prep; phase A's stale test)
+  uint8_t* r1_bytes() { return reinterpret_cast<uint8_t*>(vec<int32_t>(8)); }
   int* bigq() { return reinterpret_cast<int*>(ws + plan.off_bigq); }
   int* bigq_ctr() { return reinterpret_cast<int*>(ws + plan.off_small + 488); }   // 4 ints
   int* heavy_x() { return reinterpret_cast<int*>(ws + plan.off_heavy + 256); }
@@ -864,7 +866,8 @@ constexpr double kPhaseABytes = 34.0;
 // update's first launch (update_prep, one GPU)
 template <typename T>
 apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, const T* c2,
-                      const T* r2, bool removal, apsp_update_info* info, bool prepped = false) {
+                      const T* r2, bool removal, apsp_update_info* info, bool prepped = false,
+                      const uint8_t* r1b = nullptr /* r1 as saturated bytes, written by update_prep */) {
   const int64_t n = h->n;
   Rows r = h->active();
   const int64_t lcap = h->plan.lcap, ocap = h->plan.ocap;
@@ -948,7 +951,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     PK(APSP_K_SPARSE0, 0.0,
        sparse_phase_a<T>(h->Dl<T>(), h->ld, r, h->slid(), h->slw<T>(), h->rowoff(), h->srow(), h->scol(),
                          lcap, c1, r1, c2, r2, h->tau, h->ocnt(), h->ocol(), h->gprow(), h->gpcol(),
-                         h->glb<T>(), h->gfull(), ocap, h->ctr(), h->sr, h->mirror<T>(), h->st));
+                         h->glb<T>(), h->gfull(), ocap, h->ctr(), h->sr, h->mirror<T>(), h->st, 0, r1b));
     // A2: whole-shortlist pass over the open pairs, now that certified values are final
     CK(sparse_short<T>(h->Dl<T>(), h->ld, h->row0, h->slid(), h->slw<T>(), h->wnext<T>(), h->gprow(),
                        h->gpcol(), h->glb<T>(), ocap, h->gfull(), 1, h->sr, h->ctr(), h->st, h->mirror<T>(),
@@ -1252,13 +1255,13 @@ apsp_status remove_node_impl(apsp_handle* h, int64_t k, int64_t* moved_from, aps
   const bool prep = h->world == 1;
   if (prep) {   // counters, snapshots t1 = SPD(i, k), t2 = SPD(k, j), WT tombstone: one launch
     CK(update_prep<T>(h->Dl<T>(), ld, r, k, T(0), c1, h->Drow<T>(k), n, ld, r1, recompute_zero_set(h), h->WT<T>(),
-                      ld, k, h->sr, h->st));
+                      ld, k, h->sr, h->st, h->r1_bytes()));
   } else {
     s = snap_pivots<T>(h, k, T(0), c1, k, r1);   // t1 = SPD(i, k), t2 = SPD(k, j)
     if (s != APSP_OK) return s;
   }
   if (info) info->kind = 4;
-  s = recompute<T>(h, k, c1, r1, nullptr, nullptr, true, info, prep);
+  s = recompute<T>(h, k, c1, r1, nullptr, nullptr, true, info, prep, prep ? h->r1_bytes() : nullptr);
   if (s != APSP_OK) return s;
 
   // swap-with-last: node n-1 moves into slot k (Q7)
@@ -1359,7 +1362,7 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
   const bool prep = h->world == 1;
   if (prep) {   // counters and the snapshots D[i][u] + w_old, D[v][j]: one launch
     CK(update_prep<T>(h->Dl<T>(), ld, r, u, w_old, c1, h->Drow<T>(v), n, ld, r1, recompute_zero_set(h), WT, ld,
-                      -1, h->sr, h->st));
+                      -1, h->sr, h->st, h->r1_bytes()));
   } else {
     s = snap_pivots<T>(h, u, w_old, c1, v, r1);   // D[i][u] + w_old, D[v][j]
     if (s != APSP_OK) return s;
@@ -1380,7 +1383,8 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
     apsp_status ms = ensure_mirror<T>(h);
     if (ms != APSP_OK) return ms;
   }
-  return recompute<T>(h, -1, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, false, info, prep);
+  return recompute<T>(h, -1, c1, r1, und ? c2 : nullptr, und ? r2 : nullptr, false, info, prep,
+                      prep ? h->r1_bytes() : nullptr);
 }
 
 // ------------------------------------------------------------------ f1: paper-faithful modify

@@ -235,7 +235,8 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
                            const T* c1, const T* r1, const T* c2, const T* r2, float tau, int* ocnt,
                            int* ocol, int* gprow, int* gpcol, T* glb, unsigned char* gfull, int64_t ocap,
                            DetectCounters* ctr, int sr, Mirror M, cudaStream_t st,
-                           int list = 0 /* 0: the need_update_list, 2: the fused kernel's spills */);
+                           int list = 0 /* 0: the need_update_list, 2: the fused kernel's spills */,
+                           const uint8_t* r1b = nullptr /* r1 as saturated bytes (update_prep), or null */);
 template <typename T>
 cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
                         const int* gprow, const int* gpcol, const T* glb, const unsigned char* gfull,
@@ -375,7 +376,7 @@ cudaError_t zero_set(const ZeroSet& z, cudaStream_t st);
 template <typename T>
 cudaError_t update_prep(const T* D, int64_t ld, Rows r, int64_t col, T add, T* cout, const T* rsrc, int64_t n,
                         int64_t npad, T* rout, const ZeroSet& z, T* WT, int64_t ldw, int64_t tomb, int sr,
-                        cudaStream_t st);
+                        cudaStream_t st, uint8_t* rout8 = nullptr /* + min(rsrc, 0x7F) bytes (int32) */);
 // the counters pack_counters packs, plus the mirror flag, into mapped host memory
 cudaError_t pack_to_host(const DetectCounters* c, const int* any, const unsigned* mflag, void* host_dev,
                          cudaStream_t st, const int* rounds = nullptr /* -> host word 14 */);

@@ -970,13 +970,18 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_aq(T* D, int64_t 
                                                          const T* __restrict__ c2, const T* __restrict__ r2,
                                                          float tau, OpenLists<T> ol,
                                                          const DetectCounters* dc, Mirror M, int nbatch,
-                                                         int list) {
+                                                         int list, const uint8_t* __restrict__ r1b) {
   const int lane = threadIdx.x & 31;
   unsigned mbits = 0;
   npairs = device_count(dc, npairs, list);
   const uint8_t* M8 = nullptr;
   if constexpr (std::is_same<T, int32_t>::value && SR == 0)
     if (M.m8 && (*(volatile unsigned*)M.flag & 1u) == 0u) M8 = M.m8;
+  // with the mirror, the stale test reads r1 as saturated bytes too: exact,
+  // since a byte of 0x7F (r1 >= 0x7F) makes c + r >= 0x7F > every mirrored
+  // d it is compared with (d = 0x7F entries are skipped as INF); a 32 KB row
+  // of bytes stays in L1 where 4-byte values spill to L2
+  const uint8_t* R8 = M8 ? r1b : nullptr;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   // chunk: up to 32 * kPAChunk pairs, fewer when the list would leave warps
@@ -1040,7 +1045,7 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_aq(T* D, int64_t 
           } else {
             dv[q] = m[q] >= 0 ? *(volatile const T*)(Drow + mq) : Tr<T>::inf();
           }
-          rv[q] = r1[mq];
+          rv[q] = R8 ? (T)R8[mq] : r1[mq];
           if (TWO) rv2[q] = r2[mq];
         }
 #pragma unroll
@@ -1104,7 +1109,7 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
                            const int64_t* rowoff, const int* srow, const int* scol, int64_t npairs,
                            const T* c1, const T* r1, const T* c2, const T* r2, float tau, int* ocnt,
                            int* ocol, int* gprow, int* gpcol, T* glb, unsigned char* gfull, int64_t ocap,
-                           DetectCounters* ctr, int sr, Mirror M, cudaStream_t st, int list) {
+                           DetectCounters* ctr, int sr, Mirror M, cudaStream_t st, int list, const uint8_t* r1b) {
   if (npairs <= 0) return cudaSuccess;
   OpenLists<T> ol{ocnt, ocol, rowoff, gprow, gpcol, glb, gfull, ocap, ctr};
   // npairs is the capacity bound (the device count decides): full occupancy
@@ -1113,7 +1118,8 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
   do {                                                                                             \
     if (queue)                                                                                     \
       k_sparse_phase_aq<T, SRV, TWOV><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, srow, scol,  \
-                                                            npairs, c1, r1, c2, r2, tau, ol, ctr, M, nb, list); \
+                                                            npairs, c1, r1, c2, r2, tau, ol, ctr, M, nb, list, \
+                                                            r1b);                                       \
     else                                                                                           \
       k_sparse_phase_a<T, SRV, TWOV><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, srow, scol,   \
                                                            npairs, c1, r1, c2, r2, tau, ol, ctr, M, nb, list); \
@@ -1585,7 +1591,8 @@ __global__ void __launch_bounds__(256) k_sparse_round(T* D, int64_t ld, int64_t 
 // rounds, stopping after the first round that changes nothing: no host round
 // trip per batch of rounds.  Buffers as the one-round kernel's: frontier
 // counts per round in chg[round % 4] (their totals at [cap]; rounds 0-3
-// zeroed by the caller, later ones here), frontier lists alternating between
+// zeroed by the caller, round r + 1's during round r — that buffer was last
+// read in round r - 2 — so no extra barrier), frontier lists alternating between
 // fcol[0] / fcol[1]; round 0 reads the open lists (ocnt / ocol).  *rounds_run
 // receives the number of rounds executed; *last_total the last round's total.
 template <typename T, int SR>
@@ -1618,11 +1625,6 @@ __global__ void __launch_bounds__(256) k_sparse_rounds_coop(T* D, int64_t ld, in
   for (; round < r1; ++round) {
     const int o = round & 3, oi = (round + 3) & 3;
     int* chg_o = rb.chg + (int64_t)o * rb.stride;
-    if (round >= 4) {   // this round's counts start at zero
-      for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e <= rb.cap; e += (int64_t)gridDim.x * blockDim.x)
-        chg_o[e] = 0;
-      grid.sync();
-    }
     const int* fin_c = round == 0 ? ocnt : rb.chg + (int64_t)oi * rb.stride;
     const int* fin_l = round == 0 ? ocol : rb.fcol[(round & 1) ^ 1];
     // the previous round changed nothing: converged (grid-uniform after the barrier)
@@ -1631,6 +1633,11 @@ __global__ void __launch_bounds__(256) k_sparse_rounds_coop(T* D, int64_t ld, in
     // pair is reset for the next round (nobody uses it now)
     int* bq = rb.bigq_ctr + 2 * (round & 1);
     if (blockIdx.x == 0 && threadIdx.x < 2) rb.bigq_ctr[2 * ((round + 1) & 1) + threadIdx.x] = 0;
+    if (round + 1 >= 4) {   // the next round's counts (last read two rounds ago) start at zero
+      int* chg_n = rb.chg + (int64_t)((round + 1) & 3) * rb.stride;
+      for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e <= rb.cap; e += (int64_t)gridDim.x * blockDim.x)
+        chg_n[e] = 0;
+    }
     mbits |= sparse_round_body<T, SR>(D, ld, row0, WT, ldw, gprow, gpcol, glb, nopen, rowoff, fin_c, fin_l, chg_o,
                                       chg_o + rb.cap, rb.fcol[round & 1], any, rowkey, wmin, M, hrow, hc, rb.bigq,
                                       bq);
@@ -1725,7 +1732,7 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
                                          const int*, const int*, int64_t, const T*, const T*,      \
                                          const T*, const T*, float, int*, int*, int*, int*, T*,    \
                                          unsigned char*, int64_t, DetectCounters*, int, Mirror,    \
-                                         cudaStream_t, int);                                       \
+                                         cudaStream_t, int, const uint8_t*);                       \
   template cudaError_t sparse_full<T>(T*, int64_t, int64_t, const T*, int64_t, int64_t,            \
                                       const int*, const int*, const T*, const unsigned char*,      \
                                       int64_t, int, const DetectCounters*, cudaStream_t, Mirror);         \

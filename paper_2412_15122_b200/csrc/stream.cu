@@ -251,7 +251,8 @@ __global__ void k_gather_col_row(const T* D, int64_t ld, Rows r, int64_t col, T 
 // path) — independent writes, one grid-stride pass.
 template <typename T, int SR>
 __global__ void k_update_prep(const T* D, int64_t ld, Rows r, int64_t col, T add, T* cout, const T* rsrc,
-                              int64_t n, int64_t npad, T* rout, ZeroSet z, T* WT, int64_t ldw, int64_t tomb) {
+                              int64_t n, int64_t npad, T* rout, ZeroSet z, T* WT, int64_t ldw, int64_t tomb,
+                              uint8_t* rout8) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int b = 0; b < z.k; ++b)
@@ -259,7 +260,11 @@ __global__ void k_update_prep(const T* D, int64_t ld, Rows r, int64_t col, T add
   for (int64_t i = r.lo + tid; i < r.hi; i += stride)
     cout[i] = Tr<T, SR>::sat(Tr<T, SR>::add(D[(i - r.row0) * ld + col], add));
   if (rsrc)
-    for (int64_t j = tid; j < npad; j += stride) rout[j] = j < n ? rsrc[j] : Tr<T>::inf();
+    for (int64_t j = tid; j < npad; j += stride) {
+      const T v = j < n ? rsrc[j] : Tr<T>::inf();
+      rout[j] = v;
+      if (rout8) rout8[j] = (uint8_t)min((int32_t)v, kSat8i);   // (int32 shortest path only)
+    }
   if (tomb >= 0)
     for (int64_t j = tid; j < n; j += stride) {
       WT[tomb * ldw + j] = (j == tomb) ? T(0) : Tr<T>::inf();
@@ -269,15 +274,18 @@ __global__ void k_update_prep(const T* D, int64_t ld, Rows r, int64_t col, T add
 template <typename T>
 cudaError_t update_prep(const T* D, int64_t ld, Rows r, int64_t col, T add, T* cout, const T* rsrc, int64_t n,
                         int64_t npad, T* rout, const ZeroSet& z, T* WT, int64_t ldw, int64_t tomb, int sr,
-                        cudaStream_t st) {
+                        cudaStream_t st, uint8_t* rout8) {
   if (z.overflow) return cudaErrorInvalidValue;
+  if (Tr<T>::kFloat || sr) rout8 = nullptr;
   int64_t most = std::max<int64_t>(std::max<int64_t>(r.hi - r.lo, npad), 1);
   for (int b = 0; b < z.k; ++b) most = std::max(most, z.n[b]);
   const int grid = (int)std::min<int64_t>(cdiv(most, 256), 4 * num_sms());
   if (sr)
-    k_update_prep<T, 1><<<grid, 256, 0, st>>>(D, ld, r, col, add, cout, rsrc, n, npad, rout, z, WT, ldw, tomb);
+    k_update_prep<T, 1><<<grid, 256, 0, st>>>(D, ld, r, col, add, cout, rsrc, n, npad, rout, z, WT, ldw, tomb,
+                                              rout8);
   else
-    k_update_prep<T, 0><<<grid, 256, 0, st>>>(D, ld, r, col, add, cout, rsrc, n, npad, rout, z, WT, ldw, tomb);
+    k_update_prep<T, 0><<<grid, 256, 0, st>>>(D, ld, r, col, add, cout, rsrc, n, npad, rout, z, WT, ldw, tomb,
+                                              rout8);
   return cudaGetLastError();
 }
 
@@ -1475,34 +1483,40 @@ template <> __device__ __forceinline__ int32_t from_bits32<int32_t>(int32_t b) {
 template <> __device__ __forceinline__ float from_bits32<float>(int32_t b) { return __int_as_float(b); }
 
 // Warp-uniform iterator over the rows i in [lo, hi) that can change in a
-// rank-1 pass (c[i] or c2[i] finite): one ballot per 32 rows, the next group's
-// c values loaded a group ahead.  next() returns the row and its c values.
+// rank-1 pass (c[i] or c2[i] finite): one ballot per 32 rows, the c values of
+// the next kLRAhead groups already in flight (a slab of a few hundred rows
+// with few live ones is otherwise a chain of one load latency per 32 rows).
+// next() returns the row and its c values.
+constexpr int kLRAhead = 4;
 template <typename T, bool TWO>
 struct LiveRows {
   const T* c;
   const T* c2;
-  int64_t g, cur, hi;
+  int64_t g, cur, hi;   // g: the first row of the group in slot 0
   unsigned mask;
-  T nx, nx2, cx, cx2;
-  __device__ __forceinline__ void load(int lane) {
-    const int64_t i = g + lane;
-    nx = i < hi ? c[i] : Tr<T>::inf();
-    nx2 = (TWO && i < hi) ? c2[i] : Tr<T>::inf();
+  T nx[kLRAhead], nx2[kLRAhead], cx, cx2;
+  __device__ __forceinline__ void load(int k, int lane) {
+    const int64_t i = g + 32 * k + lane;
+    nx[k] = i < hi ? c[i] : Tr<T>::inf();
+    nx2[k] = (TWO && i < hi) ? c2[i] : Tr<T>::inf();
   }
   __device__ __forceinline__ void init(const T* c_, const T* c2_, int64_t lo, int64_t hi_, int lane) {
     c = c_; c2 = c2_; g = lo; hi = hi_; mask = 0u; cur = lo;
-    if (g < hi) load(lane);
+#pragma unroll
+    for (int k = 0; k < kLRAhead; ++k) load(k, lane);
   }
   // -1 at the end; *ci / *ci2 = c[i] / c2[i] (warp-uniform)
   __device__ __forceinline__ int64_t next(int lane, T* ci, T* ci2) {
     while (mask == 0u) {
       if (g >= hi) return -1;
-      mask = __ballot_sync(0xffffffffu, Tr<T>::fin(nx) || (TWO && Tr<T>::fin(nx2)));
+      mask = __ballot_sync(0xffffffffu, Tr<T>::fin(nx[0]) || (TWO && Tr<T>::fin(nx2[0])));
       cur = g;
-      cx = nx;
-      cx2 = nx2;
+      cx = nx[0];
+      cx2 = nx2[0];
+#pragma unroll
+      for (int k = 0; k + 1 < kLRAhead; ++k) { nx[k] = nx[k + 1]; nx2[k] = nx2[k + 1]; }
       g += 32;
-      if (g < hi) load(lane);
+      load(kLRAhead - 1, lane);   // the group kLRAhead - 1 after the new slot 0
     }
     const int b = __ffs(mask) - 1;
     mask &= mask - 1u;
@@ -1653,16 +1667,31 @@ __global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, in
   auto colj = [&](int e) -> int64_t { return g0 + (e >> 4) * 512 + (e & 15); };
   uint32_t r2[16], r2b[TWO ? 16 : 1];   // word q: columns colj(2q), colj(2q + 1), saturated at 0x3FFF
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    uint32_t a = 0, b = 0;
+  for (int v = 0; v < 8; ++v) {   // 4 columns colj(4v) .. colj(4v + 3) per 16-byte load
+    const int64_t j0 = colj(4 * v);
+    if (j0 + 3 < n) {
+      const Vec4<int32_t> x = ld4<int32_t>(rv + j0);
+      r2[2 * v] = (uint32_t)sat16(x.x) | (uint32_t)sat16(x.y) << 16;
+      r2[2 * v + 1] = (uint32_t)sat16(x.z) | (uint32_t)sat16(x.w) << 16;
+      if (TWO) {
+        const Vec4<int32_t> y = ld4<int32_t>(rv2 + j0);
+        r2b[2 * v] = (uint32_t)sat16(y.x) | (uint32_t)sat16(y.y) << 16;
+        r2b[2 * v + 1] = (uint32_t)sat16(y.z) | (uint32_t)sat16(y.w) << 16;
+      }
+    } else {
 #pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
-      const int64_t j = colj(2 * q + hf);
-      a |= (uint32_t)(j < n ? sat16(rv[j]) : 0x3FFF) << (16 * hf);
-      if (TWO) b |= (uint32_t)(j < n ? sat16(rv2[j]) : 0x3FFF) << (16 * hf);
+      for (int q = 2 * v; q < 2 * v + 2; ++q) {
+        uint32_t a = 0, b = 0;
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const int64_t j = colj(2 * q + hf);
+          a |= (uint32_t)(j < n ? sat16(rv[j]) : 0x3FFF) << (16 * hf);
+          if (TWO) b |= (uint32_t)(j < n ? sat16(rv2[j]) : 0x3FFF) << (16 * hf);
+        }
+        r2[q] = a;
+        if (TWO) r2b[q] = b;
+      }
     }
-    r2[q] = a;
-    if (TWO) r2b[q] = b;
   }
   int64_t rows_read = 0;
   unsigned mbits = 0;
@@ -2361,22 +2390,7 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
     return (int64_t)chunk * 1024 + 16 * ln + (bit >> 4) * 512 + (bit & 15);
   };
   auto s8 = [](T v) -> uint32_t { return (uint32_t)min((int32_t)v, kSat8i); };
-  uint32_t rw[8], rw2[TWO ? 8 : 1];
-  unsigned vmask = 0;   // bit b <-> column col_of(b, lane): j < n and j != skip
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    uint32_t a = 0, b = 0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int bit = (q >> 2) * 16 + (q & 3) * 4 + e;
-      const int64_t j = g0 + (q >> 2) * 512 + (q & 3) * 4 + e;
-      a |= (j < n ? s8(r1[j]) : (uint32_t)kSat8i) << (8 * e);
-      if (TWO) b |= (j < n ? s8(r2[j]) : (uint32_t)kSat8i) << (8 * e);
-      if (j < n && j != skip) vmask |= 1u << bit;
-    }
-    rw[q] = a;
-    if (TWO) rw2[q] = b;
-  }
+  // the ring first: its copies are in flight while the pivot row is read
   extern __shared__ __align__(128) uint8_t dring_raw[];
   D8Ring<S> ring;
   ring.init(dring_raw + (threadIdx.x >> 5) * D8Ring<S>::kBytes, lane);
@@ -2388,6 +2402,36 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
   };
 #pragma unroll
   for (int st = 0; st < S - 1; ++st) issue(st);
+  // this lane's pivot-row bytes: 16-byte loads where the 4 columns are all < n
+  uint32_t rw[8], rw2[TWO ? 8 : 1];
+  unsigned vmask = 0;   // bit b <-> column col_of(b, lane): j < n and j != skip
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int64_t j0 = g0 + (q >> 2) * 512 + (q & 3) * 4;
+    uint32_t a = 0, b = 0;
+    if (j0 + 3 < n) {
+      const Vec4<T> v = ld4<T>(r1 + j0);
+      a = s8(v.x) | s8(v.y) << 8 | s8(v.z) << 16 | s8(v.w) << 24;
+      if (TWO) {
+        const Vec4<T> v2 = ld4<T>(r2 + j0);
+        b = s8(v2.x) | s8(v2.y) << 8 | s8(v2.z) << 16 | s8(v2.w) << 24;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t j = j0 + e;
+        a |= (j < n ? s8(r1[j]) : (uint32_t)kSat8i) << (8 * e);
+        if (TWO) b |= (j < n ? s8(r2[j]) : (uint32_t)kSat8i) << (8 * e);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t j = j0 + e;
+      if (j < n && j != skip) vmask |= 1u << ((q >> 2) * 16 + (q & 3) * 4 + e);
+    }
+    rw[q] = a;
+    if (TWO) rw2[q] = b;
+  }
   uint32_t cl = 0, cl2 = 0;
   for (int st = 0; st < nst; ++st) {
     issue(st + S - 1);
@@ -2884,7 +2928,7 @@ cudaError_t swap_cols(T* D, int64_t ld, Rows r, int64_t p, int64_t q, cudaStream
   template cudaError_t init_d<T>(T*, int64_t, Rows, int64_t, const T*, int64_t, cudaStream_t);     \
   template cudaError_t gather_col<T>(const T*, int64_t, Rows, int64_t, T, T*, int, cudaStream_t);  \
   template cudaError_t update_prep<T>(const T*, int64_t, Rows, int64_t, T, T*, const T*, int64_t, int64_t, T*, \
-                                      const ZeroSet&, T*, int64_t, int64_t, int, cudaStream_t);   \
+                                      const ZeroSet&, T*, int64_t, int64_t, int, cudaStream_t, uint8_t*); \
   template cudaError_t gather_col_row<T>(const T*, int64_t, Rows, int64_t, T, T*, const T*, int64_t,     \
                                          int64_t, T*, int, cudaStream_t);                               \
   template cudaError_t copy_vec<T>(const T*, int64_t, int64_t, T, T*, cudaStream_t);               \

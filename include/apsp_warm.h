@@ -337,8 +337,8 @@ typedef enum {
   APSP_K_ADD_PASS1 = 3,  /* add-node read pass (new row and column)   work: bytes       */
   APSP_K_RANK1 = 4,      /* rank-1 min-plus relaxation pass           work: bytes read  */
   APSP_K_DETECT = 5,     /* affected-pair detection (streaming pass)  work: bytes       */
-  APSP_K_SPARSE0 = 6,    /* sparse recompute, round 0                 work: bytes       */
-  APSP_K_SPARSE_R = 7,   /* sparse recompute, rounds >= 1             work: bytes       */
+  APSP_K_SPARSE0 = 6,    /* sparse recompute, phase A                 work: bytes       */
+  APSP_K_SPARSE_R = 7,   /* sparse recompute after phase A: A2, B, rounds, heavy rows  work: bytes */
   APSP_K_QUERY = 8,      /* single-pair queries                       work: bytes       */
   APSP_K_OTHER = 9,      /* snapshots, tombstone, swap, small kernels work: bytes       */
   APSP_K_EMIT = 10,      /* detection list: per-row slices, Phi        work: bytes       */

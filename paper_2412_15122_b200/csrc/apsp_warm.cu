@@ -128,7 +128,7 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   p.off_mt = take((size_t)cap * p.ldt);       // its transpose (column j of D = row j)
   p.off_ptd = take(sizeof(uint32_t) * (size_t)kTile * kTile);
   // heavy rows of the sparse recompute (one GPU): the set, then kHeavy rows of X keys
-  p.off_heavy = take(256 + sizeof(int32_t) * (size_t)kHeavy * p.ld);
+  p.off_heavy = take(512 + sizeof(int32_t) * (size_t)kHeavy * p.ld);
   p.off_bigq = take(sizeof(int32_t) * (size_t)p.ocap);   // the rounds' long-frontier pair queue (one GPU)
   p.off_small = take(64 * 1024);
   p.total = o;
@@ -305,7 +305,7 @@ struct apsp_handle {
   uint8_t* r1_bytes() { return reinterpret_cast<uint8_t*>(vec<int32_t>(8)); }
   int* bigq() { return reinterpret_cast<int*>(ws + plan.off_bigq); }
   int* bigq_ctr() { return reinterpret_cast<int*>(ws + plan.off_small + 488); }   // 4 ints
-  int* heavy_x() { return reinterpret_cast<int*>(ws + plan.off_heavy + 256); }
+  int* heavy_x() { return reinterpret_cast<int*>(ws + plan.off_heavy + 512); }
   alignas(64) unsigned char tmap8[128];   // CUtensorMap of the int8 mirror (detection's TMA)
   bool tmap8_ok = false;
   const void* tmap8_ptr() const { return tmap8_ok ? tmap8 : nullptr; }
@@ -852,7 +852,7 @@ ZeroSet recompute_zero_set(apsp_handle* h) {
   for (int q = 0; q < 4; ++q) z.add(h->chg(q), h->cap + 1);
   z.add(h->anyflag(), 1);
   z.add(h->anyrow(), h->cap);   // the rounds' per-row open minima (keys)
-  z.add(h->heavy_set(), 1);     // no heavy rows selected
+  z.add(h->heavy_set(), 2 + 2 * kHeavy);   // heavy rows: count, ids, bounds, pruned-list length
   z.add(h->bigq_ctr(), 4);      // the rounds' queue counters
   return z;
 }
@@ -953,7 +953,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
                          lcap, c1, r1, c2, r2, h->tau, h->ocnt(), h->ocol(), h->gprow(), h->gpcol(),
                          h->glb<T>(), h->gfull(), ocap, h->ctr(), h->sr, h->mirror<T>(), h->st, 0, r1b));
     // A2: whole-shortlist pass over the open pairs, now that certified values are final
-    CK(sparse_short<T>(h->Dl<T>(), h->ld, h->row0, h->slid(), h->slw<T>(), h->wnext<T>(), h->gprow(),
+    PK(APSP_K_SPARSE_R, 0.0, sparse_short<T>(h->Dl<T>(), h->ld, h->row0, h->slid(), h->slw<T>(), h->wnext<T>(), h->gprow(),
                        h->gpcol(), h->glb<T>(), ocap, h->gfull(), 1, h->sr, h->ctr(), h->st, h->mirror<T>(),
                        removal ? skip : -1));
     // the removal's shortlist upkeep needs nothing after A2 (the last reader of

@@ -253,9 +253,10 @@ struct RoundBufs {
   int* bigq_ctr;      // 4 ints: (tail, head) per round parity; zero on entry
   // heavy rows: selected at the start (>= heavy_thr open
   // pairs, at most kHeavy; heavy_thr 0: none), skipped by the rounds, then
-  // resolved from the other rows.  heavy[0] = rows selected (zero on entry),
-  // heavy[1..kHeavy] their ids; heavy_x = kHeavy rows of ldx keys, 0x7F-filled
-  // at creation and reset after each use
+  // resolved from the other rows.  heavy[0] = rows selected, heavy[1..kHeavy]
+  // their ids, heavy[1 + kHeavy + k] row k's bound B_h (key), heavy[1 + 2
+  // kHeavy] the pruned first-hop list's length (all zero on entry); heavy_x =
+  // kHeavy rows of ldx keys, 0x7F-filled at creation and reset after each use
   int* heavy; int* heavy_x; int64_t ldx; int heavy_thr;
   int64_t rows, n, skip;   // local rows (one GPU: all), nodes, removed node or -1
 };

@@ -1309,7 +1309,9 @@ struct HeavySmem {
 template <typename T, int SR>
 __device__ void heavy_x_item(const T* __restrict__ D, int64_t ld, int64_t n, const T* __restrict__ WT, int64_t ldw,
                              int hc, int g0, int64_t stripe, int64_t m0, int64_t m1, int* x, int64_t ldx,
-                             int64_t skip, HeavySmem<T>& sm) {
+                             int64_t skip, HeavySmem<T>& sm, const int* __restrict__ mlist) {
+  // rows m: mlist[m0 .. m1) (the pruned first hops), or m0 .. m1 - 1
+  auto row_at = [&](int64_t q) -> int64_t { return mlist ? (int64_t)mlist[q] : q; };
   const int gc = min(kHxGroup, hc - g0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const T I = Tr<T>::inf();
@@ -1321,8 +1323,9 @@ __device__ void heavy_x_item(const T* __restrict__ D, int64_t ld, int64_t n, con
     for (int e = 0; e < 4; ++e) acc[k][e] = I;
   const int wr = threadIdx.x / kHxGroup, wk = threadIdx.x % kHxGroup;
   auto wload = [&](int64_t b) -> T {
-    const int64_t m = b + wr;
-    bool out = m < m1 && m != skip && wk < gc;
+    if (b + wr >= m1 || wk >= gc) return I;
+    const int64_t m = row_at(b + wr);
+    bool out = m != skip;
     for (int t = 0; t < hc; ++t) out &= sm.hrow[t] != (int)m;   // m outside H
     return out ? WT[m * ldw + sm.hrow[g0 + wk]] : I;             // W'[h][m] (WT row m: in-edges of m)
   };
@@ -1336,8 +1339,8 @@ __device__ void heavy_x_item(const T* __restrict__ D, int64_t ld, int64_t n, con
     Vec4<T> d[kHxSlab / 8];
 #pragma unroll
     for (int rr = 0; rr < kHxSlab / 8; ++rr) {
-      const int64_t m = b + rr * 8 + warp;
-      d[rr] = m < m1 ? mask_tail<T>(ld4<T>(D + m * ld + c0), c0, n) : Vec4<T>{I, I, I, I};
+      const int64_t q = b + rr * 8 + warp;
+      d[rr] = q < m1 ? mask_tail<T>(ld4<T>(D + row_at(q) * ld + c0), c0, n) : Vec4<T>{I, I, I, I};
     }
 #pragma unroll
     for (int rr = 0; rr < kHxSlab / 8; ++rr) {
@@ -1651,17 +1654,43 @@ __global__ void __launch_bounds__(256) k_sparse_rounds_coop(T* D, int64_t ld, in
   }
   if (hc > 0) {   // the heavy rows, from the other rows (final once the rounds converged)
     const int64_t n = rb.n;
+    // Pruning the first hops: D'[h][j] <= B_h = max_j D[h][j] (every entry is
+    // already a walk length of G'), so a first hop m with W'[h][m] > B_h lies
+    // on no shortest h -> j path — only the m with W'[h][m] <= B_h for some
+    // heavy h are read.  B_h as order keys in heavy[1 + kHeavy + k].
+    int* bkey = rb.heavy + 1 + kHeavy;
+    int* nlive = rb.heavy + 1 + 2 * kHeavy;
+    int* mlist = rb.bigq;   // free again: the rounds are over
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)hc * n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      const int k = (int)(e / n);
+      const int64_t j = e - (int64_t)k * n;
+      if (j == rb.skip) continue;
+      int kv = heavy_xkey<T>(D[(int64_t)hrow[k] * ld + j]);
+      kv = __reduce_max_sync(__activemask(), kv);
+      atomicMax(bkey + k, kv);
+    }
+    grid.sync();
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n; m += (int64_t)gridDim.x * blockDim.x) {
+      bool live = false, inh = m == rb.skip;
+      for (int k = 0; k < hc; ++k) inh |= hrow[k] == (int)m;
+      if (!inh)
+        for (int k = 0; k < hc && !live; ++k) live = WT[m * ldw + hrow[k]] <= heavy_xval<T>(bkey[k]);
+      if (live) mlist[atomicAdd(nlive, 1)] = (int)m;
+    }
+    grid.sync();
+    const int64_t nl = *(volatile int*)nlive;
     const int64_t gx = (n + 127) / 128;
     const int ng = (hc + kHxGroup - 1) / kHxGroup;
-    const int64_t ny = max((int64_t)1, 2 * (int64_t)gridDim.x / (gx * ng));
-    const int64_t slab = ((n + ny - 1) / ny + kHxSlab - 1) / kHxSlab * kHxSlab;
-    const int64_t items = gx * ng * ((n + slab - 1) / slab);
+    const int64_t ny = max((int64_t)1, min((nl + kHxSlab - 1) / kHxSlab, 2 * (int64_t)gridDim.x / (gx * ng)));
+    const int64_t slab = ((nl + ny - 1) / ny + kHxSlab - 1) / kHxSlab * kHxSlab;
+    const int64_t items = nl > 0 ? gx * ng * ((nl + slab - 1) / slab) : 0;
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
       const int64_t stripe = it % gx, rest = it / gx;
       const int g = (int)(rest % ng);
       const int64_t m0 = (rest / ng) * slab;
-      heavy_x_item<T, SR>(D, ld, n, WT, ldw, hc, g * kHxGroup, stripe, m0, min(n, m0 + slab), rb.heavy_x, rb.ldx,
-                          rb.skip, sm);
+      heavy_x_item<T, SR>(D, ld, n, WT, ldw, hc, g * kHxGroup, stripe, m0, min(nl, m0 + slab), rb.heavy_x, rb.ldx,
+                          rb.skip, sm, mlist);
     }
     grid.sync();
     heavy_closure<T, SR>(WT, ldw, hc, sm);

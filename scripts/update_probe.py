@@ -58,6 +58,6 @@ for it, u in enumerate(us):
     ru = lambda x: (x + 255) // 256 * 256
     lcap = min(max(h.cap * h.cap // 32, 1 << 20), 1 << 28)
     ocap = max(lcap // 4, 1 << 18)
-    off = ws.numel() - 65536 - ru(4 * ocap) - ru(256 + 4 * 32 * h.ld)   # [heavy | bigq | small]
+    off = ws.numel() - 65536 - ru(4 * ocap) - ru(512 + 4 * 32 * h.ld)   # [heavy | bigq | small]
     hs = ws[off:off + 36].view(torch.int32).cpu().tolist()
     print(cfg, it, round(a.elapsed_time(b), 4), info.as_dict(), "heavy", hs[0], hs[1:1 + min(hs[0], 8)])

@@ -952,22 +952,25 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
        sparse_phase_a<T>(h->Dl<T>(), h->ld, r, h->slid(), h->slw<T>(), h->rowoff(), h->srow(), h->scol(),
                          lcap, c1, r1, c2, r2, h->tau, h->ocnt(), h->ocol(), h->gprow(), h->gpcol(),
                          h->glb<T>(), h->gfull(), ocap, h->ctr(), h->sr, h->mirror<T>(), h->st, 0, r1b));
-    // A2: whole-shortlist pass over the open pairs, now that certified values are final
-    PK(APSP_K_SPARSE_R, 0.0, sparse_short<T>(h->Dl<T>(), h->ld, h->row0, h->slid(), h->slw<T>(), h->wnext<T>(), h->gprow(),
-                       h->gpcol(), h->glb<T>(), ocap, h->gfull(), 1, h->sr, h->ctr(), h->st, h->mirror<T>(),
-                       removal ? skip : -1));
-    // the removal's shortlist upkeep needs nothing after A2 (the last reader of
-    // SL): it runs on the side stream, joined before the update returns
-    if (removal) {
-      apsp_status s2 = fork_shortlist_remove<T>(h, skip);
-      if (s2 != APSP_OK) return s2;
+    if (!coop) {   // (one GPU: A2, B and the row minima run inside the cooperative launch)
+      // A2: whole-shortlist pass over the open pairs, now that certified values are final
+      PK(APSP_K_SPARSE_R, 0.0,
+         sparse_short<T>(h->Dl<T>(), h->ld, h->row0, h->slid(), h->slw<T>(), h->wnext<T>(), h->gprow(),
+                         h->gpcol(), h->glb<T>(), ocap, h->gfull(), 1, h->sr, h->ctr(), h->st, h->mirror<T>(),
+                         removal ? skip : -1));
+      // the removal's shortlist upkeep needs nothing after A2 (the last reader of
+      // SL): it runs on the side stream, joined before the update returns
+      if (removal) {
+        apsp_status s2 = fork_shortlist_remove<T>(h, skip);
+        if (s2 != APSP_OK) return s2;
+      }
+      // B: full O(n) scan for the pairs the shortlist could not settle
+      PK(APSP_K_SPARSE_R, 0.0,
+         sparse_full<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, n, h->gprow(), h->gpcol(),
+                        h->glb<T>(), h->gfull(), ocap, h->sr, h->ctr(), h->st, h->mirror<T>()));
+      CK(open_rowmin<T>(h->Dl<T>(), h->ld, h->row0, h->gprow(), h->gpcol(), ocap,
+                        reinterpret_cast<unsigned*>(h->anyrow()), h->ctr(), h->st));
     }
-    // B: full O(n) scan for the pairs the shortlist could not settle
-    PK(APSP_K_SPARSE_R, 0.0,
-       sparse_full<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, n, h->gprow(), h->gpcol(),
-                      h->glb<T>(), h->gfull(), ocap, h->sr, h->ctr(), h->st, h->mirror<T>()));
-    CK(open_rowmin<T>(h->Dl<T>(), h->ld, h->row0, h->gprow(), h->gpcol(), ocap,
-                      reinterpret_cast<unsigned*>(h->anyrow()), h->ctr(), h->st));
     // rounds over the open entries of each row, a first batch of 4
     // the first batch is enqueued blind: as many rounds as the previous
     // recompute needed (at least 2: round 1 finding nothing proves convergence)
@@ -977,13 +980,18 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
       RoundBufs rb{h->chg(0),      h->cap + 32,     h->cap,    {fcol[0], fcol[1]}, h->coop_rounds_word(),
                    h->coop_total_word(), h->bigq(), h->bigq_ctr(), h->heavy_set(), h->heavy_x(), h->ld,
                    h->heavy_min < 0 ? 0 : (h->heavy_min > 0 ? h->heavy_min : (int)std::max<int64_t>(512, n / 8)),
-                   r.hi - r.lo, n, removal ? skip : -1};
+                   r.hi - r.lo, n, removal ? skip : -1,
+                   1, h->slid(), h->slw<T>(), h->wnext<T>(), h->gfull(), h->host_small_dev, h->mirror_flag()};
       PK(APSP_K_SPARSE_R, 0.0,
          sparse_rounds_coop<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->gprow(), h->gpcol(), h->glb<T>(),
                                ocap, h->rowoff(), h->ocnt(), h->ocol(), rb, 0, h->max_rounds, h->anyflag(), h->sr,
                                h->ctr(), h->st, reinterpret_cast<unsigned*>(h->anyrow()), h->wmin<T>(),
                                h->mirror<T>()));
       last_total = h->coop_total_word();
+      if (removal) {   // the shortlist upkeep after A2, its last reader (inside the launch above)
+        apsp_status s2 = fork_shortlist_remove<T>(h, skip);
+        if (s2 != APSP_OK) return s2;
+      }
     } else {
       apsp_status s = enqueue_rounds(std::min(std::max(2, h->rounds_hint), h->max_rounds));
       if (s != APSP_OK) return s;
@@ -998,9 +1006,10 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   // ---- the one host read of this update: counters (summed over ranks) ----
   long long* hv = reinterpret_cast<long long*>(h->host_small);
   unsigned* hmf = reinterpret_cast<unsigned*>(h->host_small) + 12;
-  if (h->world == 1) {   // packed straight into mapped host memory
-    CK(pack_to_host(h->ctr(), last_total, h->mirror_flag(), h->host_small_dev, h->st,
-                    coop && try_sparse ? h->coop_rounds_word() : nullptr));
+  if (h->world == 1 && coop && try_sparse) {
+    // (the cooperative launch packed the counters into mapped host memory)
+  } else if (h->world == 1) {   // packed straight into mapped host memory
+    CK(pack_to_host(h->ctr(), last_total, h->mirror_flag(), h->host_small_dev, h->st, nullptr));
   } else {
     long long* v = reinterpret_cast<long long*>(h->small());
     CK(pack_counters(h->ctr(), last_total, v, h->st));   // total rows ovf1 ovf2 changed | maxrow

@@ -259,6 +259,12 @@ struct RoundBufs {
   // kHeavy rows of ldx keys, 0x7F-filled at creation and reset after each use
   int* heavy; int* heavy_x; int64_t ldx; int heavy_thr;
   int64_t rows, n, skip;   // local rows (one GPU: all), nodes, removed node or -1
+  // tail = 1 (one GPU): the recompute's tail in this launch — A2 (the whole
+  // shortlists, classifying), B (full scans) and the open rows' minima
+  // before the rounds; the counters packed into mapped host memory after
+  int tail;
+  const int* slid; const void* slw; const void* wnext; unsigned char* gfull;
+  void* host; const unsigned* mflag;
 };
 constexpr int kHeavy = 32;
 // rounds r0 .. r1 - 1 in one cooperative launch (grid barriers between rounds),

@@ -709,8 +709,9 @@ __device__ __forceinline__ int64_t device_count(const DetectCounters* dc, int64_
   return c < cap ? c : cap;
 }
 
+// (the body: every warp of the grid; returns the mirror flag bits it raised)
 template <typename T, int SR>
-__global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t row0,
+__device__ __forceinline__ unsigned sparse_short_body(T* D, int64_t ld, int64_t row0,
                                                       const int* __restrict__ SLid,
                                                       const T* __restrict__ SLw,
                                                       const T* __restrict__ wnext,
@@ -718,8 +719,8 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
                                                       const int* __restrict__ pcol,
                                                       const T* __restrict__ plb, int64_t npairs,
                                                       unsigned char* out, int classify,
-                                                      OpenLists<T> ol, const DetectCounters* dc, Mirror M,
-                                                      int64_t skip) {
+                                                      const OpenLists<T>& ol, const DetectCounters* dc,
+                                                      const Mirror& M, int64_t skip) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   npairs = device_count(dc, npairs, classify ? 1 : 0);
@@ -801,6 +802,21 @@ __global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t 
       if (!classify && st != 0) ol.append(i, j, lb);
     }
   }
+  return mbits;
+}
+template <typename T, int SR>
+__global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t row0,
+                                                      const int* __restrict__ SLid,
+                                                      const T* __restrict__ SLw,
+                                                      const T* __restrict__ wnext,
+                                                      const int* __restrict__ prow,
+                                                      const int* __restrict__ pcol,
+                                                      const T* __restrict__ plb, int64_t npairs,
+                                                      unsigned char* out, int classify,
+                                                      OpenLists<T> ol, const DetectCounters* dc, Mirror M,
+                                                      int64_t skip) {
+  const unsigned mbits = sparse_short_body<T, SR>(D, ld, row0, SLid, SLw, wnext, prow, pcol, plb, npairs, out,
+                                                  classify, ol, dc, M, skip);
   if (M.m || M.m8) mirror_post(M, mbits);
 }
 
@@ -1142,16 +1158,17 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
 // One CTA per pair: the scan of a row is a latency chain (one warp per pair
 // took ~1 us per 64 vectors: a few pairs at n = 65536 ran 0.3 ms), so all 8
 // warps split it, with a block-wide early-exit test every 4 steps.
+// (the body: every CTA of the grid, 256 threads; wm: 8 T of shared memory)
 template <typename T, int SR>
-__global__ void __launch_bounds__(256) k_sparse_full(T* D, int64_t ld, int64_t row0,
+__device__ __forceinline__ unsigned sparse_full_body(T* D, int64_t ld, int64_t row0,
                                                      const T* __restrict__ WT, int64_t ldw,
                                                      int64_t n, const int* __restrict__ gprow,
                                                      const int* __restrict__ gpcol,
                                                      const T* __restrict__ glb,
                                                      const unsigned char* __restrict__ gfull,
-                                                     int64_t nopen, const DetectCounters* dc, Mirror M) {
+                                                     int64_t nopen, const DetectCounters* dc, const Mirror& M,
+                                                     T* wm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ T wm[8];
   unsigned mbits = 0;
   const int64_t n4 = (n + 3) / 4;
   nopen = device_count(dc, nopen, 1);
@@ -1205,6 +1222,18 @@ __global__ void __launch_bounds__(256) k_sparse_full(T* D, int64_t ld, int64_t r
     }
     __syncthreads();   // wm is reused by the next pair
   }
+  return mbits;
+}
+template <typename T, int SR>
+__global__ void __launch_bounds__(256) k_sparse_full(T* D, int64_t ld, int64_t row0,
+                                                     const T* __restrict__ WT, int64_t ldw,
+                                                     int64_t n, const int* __restrict__ gprow,
+                                                     const int* __restrict__ gpcol,
+                                                     const T* __restrict__ glb,
+                                                     const unsigned char* __restrict__ gfull,
+                                                     int64_t nopen, const DetectCounters* dc, Mirror M) {
+  __shared__ T wm[8];
+  const unsigned mbits = sparse_full_body<T, SR>(D, ld, row0, WT, ldw, n, gprow, gpcol, glb, gfull, nopen, dc, M, wm);
   if (M.m || M.m8) mirror_post(M, mbits);
 }
 template <typename T>
@@ -1611,6 +1640,22 @@ __global__ void __launch_bounds__(256) k_sparse_rounds_coop(T* D, int64_t ld, in
   nopen = device_count(dc, nopen, 1);
   __shared__ HeavySmem<T> sm;
   int* hrow = sm.hrow;
+  unsigned mbits = 0;
+  if (rb.tail) {   // A2, then B, then the open rows' minima (each reads the one before)
+    const OpenLists<T> ol{};
+    mbits |= sparse_short_body<T, SR>(D, ld, row0, rb.slid, static_cast<const T*>(rb.slw),
+                                      static_cast<const T*>(rb.wnext), gprow, gpcol, glb, nopen, rb.gfull, 1, ol,
+                                      dc, M, rb.skip);
+    grid.sync();
+    mbits |= sparse_full_body<T, SR>(D, ld, row0, WT, ldw, rb.n, gprow, gpcol, glb, rb.gfull, nopen, dc, M,
+                                     &sm.w[0][0]);
+    grid.sync();
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nopen; p += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i = gprow[p];
+      atomicMax(rowkey + i, open_key<T>(D[(i - row0) * ld + gpcol[p]]));
+    }
+    if (rb.heavy_thr <= 0) grid.sync();   // (else the selection's barrier below)
+  }
   if (rb.heavy_thr > 0) {   // heavy rows: >= heavy_thr open pairs (the first kHeavy found)
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rb.rows;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -1623,7 +1668,6 @@ __global__ void __launch_bounds__(256) k_sparse_rounds_coop(T* D, int64_t ld, in
   const int hc = rb.heavy_thr > 0 ? min(*(volatile const int*)rb.heavy, kHeavy) : 0;
   if (threadIdx.x < hc) hrow[threadIdx.x] = *(volatile const int*)(rb.heavy + 1 + threadIdx.x);
   __syncthreads();
-  unsigned mbits = 0;
   int round = r0;
   for (; round < r1; ++round) {
     const int o = round & 3, oi = (round + 3) & 3;
@@ -1703,6 +1747,21 @@ __global__ void __launch_bounds__(256) k_sparse_rounds_coop(T* D, int64_t ld, in
     // the last round that ran (or the one that found nothing): its total
     const int last = round > r0 ? round - 1 : r0;
     *rb.last_total = rb.chg[(int64_t)(last & 3) * rb.stride + rb.cap];
+  }
+  if (rb.tail) {   // every block's writes and flag bits in place: the host's read
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      volatile long long* host = static_cast<volatile long long*>(rb.host);
+      reinterpret_cast<volatile unsigned*>(host)[14] = (unsigned)*rb.rounds_run;
+      host[0] = (long long)dc->total;
+      host[1] = (long long)dc->rows;
+      host[2] = (dc->overflow & 1u) ? 1 : 0;
+      host[3] = (dc->overflow & 2u) ? 1 : 0;
+      host[4] = *(volatile int*)rb.last_total ? 1 : 0;
+      host[5] = (long long)dc->maxrow;
+      reinterpret_cast<volatile unsigned*>(host)[12] = *(volatile const unsigned*)rb.mflag;
+      __threadfence_system();
+    }
   }
 }
 template <typename T>

@@ -367,6 +367,9 @@ def main():
     for s in range(args.warmup, args.warmup + args.steps):
         run_step(s, "timed")
     torch.cuda.nvtx.range_pop()
+    # (the library's side stream may still hold the last removal's shortlist
+    # upkeep, joined lazily by the next update: drain every stream first)
+    torch.cuda.synchronize(dev)
     t1.record(stream)
     barrier()
     total_ms = max_over_ranks(t0.elapsed_time(t1))
@@ -418,6 +421,7 @@ def main():
             if h.row0 == 0:
                 res_host[:nn].copy_(h.D_local[0, :nn], non_blocking=True)
                 d2h += nn * 4
+        torch.cuda.synchronize(dev)   # (every stream of the handle drained, as above)
         q1.record(stream)
         barrier()
         e2e_ms = max_over_ranks(q0.elapsed_time(q1))
@@ -436,6 +440,7 @@ def main():
     s_prof = args.warmup + 2 * args.steps + (0 if args.no_e2e else args.steps)
     for s in range(s_prof, s_prof + args.steps):
         run_step(s)
+    torch.cuda.synchronize(dev)
     p1.record(stream)
     barrier()
     prof_total_ms = max_over_ranks(p0.elapsed_time(p1))

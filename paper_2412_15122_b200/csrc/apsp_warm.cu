@@ -824,13 +824,24 @@ inline bool mirror8_known_valid(const apsp_handle* h) {
 }
 
 // Removal of node k: SL upkeep (drop k's entries, node n-1 takes slot k) on
-// the side stream; remove_node_impl joins it (ev_join) before returning.
+// the side stream; the next shortlist reader or writer on the compute stream
+// joins it (join_side / recompute's sl_join).
 template <typename T>
 apsp_status fork_shortlist_remove(apsp_handle* h, int64_t k) {
   CKR(cudaEventRecord(h->ev_fork, h->st));
   CKR(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
   CK2(shortlist_remove<T>(h->slid(), h->slw<T>(), h->wnext<T>(), h->n, k, h->n - 1, h->st2));
   CKR(cudaEventRecord(h->ev_join, h->st2));
+  return APSP_OK;
+}
+
+// The compute stream waits for pending shortlist upkeep on the side stream
+// (a removal's, an increase's) before it touches the shortlists itself.
+apsp_status join_side(apsp_handle* h) {
+  if (h->sl_join) {
+    CKR(cudaStreamWaitEvent(h->st, h->ev_join, 0));
+    h->sl_join = false;
+  }
   return APSP_OK;
 }
 
@@ -951,7 +962,8 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
     PK(APSP_K_SPARSE0, 0.0,
        sparse_phase_a<T>(h->Dl<T>(), h->ld, r, h->slid(), h->slw<T>(), h->rowoff(), h->srow(), h->scol(),
                          lcap, c1, r1, c2, r2, h->tau, h->ocnt(), h->ocol(), h->gprow(), h->gpcol(),
-                         h->glb<T>(), h->gfull(), ocap, h->ctr(), h->sr, h->mirror<T>(), h->st, 0, r1b));
+                         h->glb<T>(), h->gfull(), ocap, h->ctr(), h->sr, h->mirror<T>(), h->st, 0, r1b,
+                         h->prow(), h->pcol()));   // (the rounds' frontier buffers: free until the rounds)
     if (!coop) {   // (one GPU: A2, B and the row minima run inside the cooperative launch)
       // A2: whole-shortlist pass over the open pairs, now that certified values are final
       PK(APSP_K_SPARSE_R, 0.0,
@@ -1239,6 +1251,7 @@ apsp_status add_node_impl(apsp_handle* h, const void* out_w, const void* in_w, i
                       iw, h->mirror<T>(), h->st, as, &h->ctr()->err, h->wmin_dev()));
   // (addnode_write mirrored the new row / column)
   CKR(cudaStreamWaitEvent(h->st, h->ev_join, 0));   // shortlist upkeep (side stream) done
+  h->sl_join = false;   // (st2 is in order: this joined any earlier upkeep too)
   h->n = n + 1;
   if (new_index) *new_index = x;
   if (info) {
@@ -1287,7 +1300,10 @@ apsp_status remove_node_impl(apsp_handle* h, int64_t k, int64_t* moved_from, aps
     }
   }
   CK(move_last<T>(h->Dl<T>(), ld, r, n, k, row_copy, h->WT<T>(), ld, h->mirror<T>(), h->st));
-  CKR(cudaStreamWaitEvent(h->st, h->ev_join, 0));   // shortlist upkeep (side stream, forked in recompute)
+  // the shortlist upkeep (side stream, forked in recompute) is joined by the
+  // next reader or writer of the shortlists on the compute stream (join_side,
+  // recompute's sl_join), not here: it overlaps the next update's first kernels
+  h->sl_join = true;
   h->n = n - 1;
   if (moved_from) *moved_from = (k != last) ? last : -1;
   if (info) info->n_after = h->n;
@@ -1337,6 +1353,7 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
     if (!(w_new < duv)) {
       if (info) info->early_exit = 1;
       CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
+      { apsp_status sj = join_side(h); if (sj != APSP_OK) return sj; }
       CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
       return APSP_OK;
     }
@@ -1352,6 +1369,7 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
                 h->sr, h->mirror<T>(), h->st));
     h->mirror_fresh = false;   // rank-1 may write values >= 0x7F
     CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
+    { apsp_status sj = join_side(h); if (sj != APSP_OK) return sj; }
     CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
     if (info) info->path = 1;
     return APSP_OK;
@@ -1364,6 +1382,7 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
   if (!tight) {
     if (info) info->early_exit = 1;
     CK(set_edge<T>(WT, ld, u, v, w_new, h->directed, h->st));
+    { apsp_status sj = join_side(h); if (sj != APSP_OK) return sj; }
     CK(shortlist_set_edge<T>(h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed, h->st));
     return APSP_OK;
   }
@@ -1443,6 +1462,7 @@ apsp_status swap_nodes(apsp_handle* h, int64_t p, int64_t q) {
   CK(swap_vecs<T>(WT + p * ld, WT + q * ld, n, h->st));
   Rows rw{0, n, 0};
   CK(swap_cols<T>(WT, ld, rw, p, q, h->st));
+  { apsp_status sj = join_side(h); if (sj != APSP_OK) return sj; }
   CK(shortlist_swap<T>(h->slid(), h->slw<T>(), h->wnext<T>(), n, p, q, h->st));
   CK(mirror_cross(h->Dl<T>(), ld, h->active(), n, p, p, h->mirror<T>(), h->st));
   CK(mirror_cross(h->Dl<T>(), ld, h->active(), n, q, q, h->mirror<T>(), h->st));
@@ -1605,6 +1625,7 @@ apsp_status query_one(apsp_handle* h, int64_t s, int64_t t, void* dist, int32_t*
 template <typename T>
 apsp_status need_list_impl(apsp_handle* h, int kind, int64_t a, int64_t b, int32_t* rows, int32_t* cols,
                            int64_t cap, int64_t* count) {
+  { apsp_status sj = join_side(h); if (sj != APSP_OK) return sj; }
   {
     apsp_status ms = ensure_mirror<T>(h);
     if (ms != APSP_OK) return ms;

@@ -236,7 +236,8 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
                            int* ocol, int* gprow, int* gpcol, T* glb, unsigned char* gfull, int64_t ocap,
                            DetectCounters* ctr, int sr, Mirror M, cudaStream_t st,
                            int list = 0 /* 0: the need_update_list, 2: the fused kernel's spills */,
-                           const uint8_t* r1b = nullptr /* r1 as saturated bytes (update_prep), or null */);
+                           const uint8_t* r1b = nullptr /* r1 as saturated bytes (update_prep), or null */,
+                           int* crow = nullptr, int* ccol = nullptr /* continuation list of the first step (lcap) */);
 template <typename T>
 cudaError_t sparse_full(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ldw, int64_t n,
                         const int* gprow, const int* gpcol, const T* glb, const unsigned char* gfull,

@@ -646,6 +646,35 @@ struct OpenLists {
   }
 };
 
+// A warp's staging buffer for the global open list: pairs collect in shared
+// memory and go out 32 or more at a time behind ONE atomic on open_total (an
+// atomic per warp step on that one word serialised the whole pass at L2).
+template <typename T>
+struct OpenStage {
+  int i[64], j[64];
+  T lb[64];
+  // every lane of the warp; cnt <= 64 staged pairs
+  __device__ __forceinline__ void flush(int cnt, const OpenLists<T>& ol, int lane) {
+    if (cnt == 0) return;
+    __syncwarp();
+    unsigned long long g0 = 0;
+    if (lane == 0) g0 = atomicAdd(&ol.ctr->open_total, (unsigned long long)cnt);
+    g0 = __shfl_sync(0xffffffffu, g0, 0);
+    for (int e = lane; e < cnt; e += 32) {
+      const unsigned long long s2 = g0 + e;
+      if ((int64_t)s2 < ol.ocap) {
+        ol.gprow[s2] = i[e];
+        ol.gpcol[s2] = j[e];
+        ol.glb[s2] = lb[e];
+        ol.gfull[s2] = 1;
+      } else {
+        atomicOr(&ol.ctr->overflow, 2u);
+      }
+    }
+    __syncwarp();
+  }
+};
+
 // Swap the ids of nodes p and q in every shortlist (rows and entries).
 template <typename T>
 __global__ void k_shortlist_swap(int* SLid, T* SLw, T* wnext, int64_t n, int p, int q) {
@@ -990,6 +1019,9 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_aq(T* D, int64_t 
   const int lane = threadIdx.x & 31;
   unsigned mbits = 0;
   npairs = device_count(dc, npairs, list);
+  __shared__ OpenStage<T> stage_all[8];
+  OpenStage<T>& stg = stage_all[threadIdx.x >> 5];
+  int scnt = 0;   // (warp-uniform) pairs in the warp's stage
   const uint8_t* M8 = nullptr;
   if constexpr (std::is_same<T, int32_t>::value && SR == 0)
     if (M.m8 && (*(volatile unsigned*)M.flag & 1u) == 0u) M8 = M.m8;
@@ -1096,26 +1128,121 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_aq(T* D, int64_t 
       }
       const unsigned bal = __ballot_sync(0xffffffffu, open);
       if (bal) {
-        unsigned long long g0 = 0;
-        if (lane == __ffs(bal) - 1) g0 = atomicAdd(&ol.ctr->open_total, (unsigned long long)__popc(bal));
-        g0 = __shfl_sync(0xffffffffu, g0, __ffs(bal) - 1);
-        if (open) {
+        if (open) {   // the row's open list now; the global list through the warp's stage
           const int s1 = atomicAdd(ol.ocnt + i, 1);
           ol.ocol[ol.rowoff[i] + s1] = j;
-          const unsigned long long s2 = g0 + __popc(bal & ((1u << lane) - 1));
-          if ((int64_t)s2 < ol.ocap) {
-            ol.gprow[s2] = i;
-            ol.gpcol[s2] = j;
-            ol.glb[s2] = lb;
-            ol.gfull[s2] = 1;
-          } else {
-            atomicOr(&ol.ctr->overflow, 2u);
-          }
+          const int sp = scnt + __popc(bal & ((1u << lane) - 1));
+          stg.i[sp] = i;
+          stg.j[sp] = j;
+          stg.lb[sp] = lb;
+        }
+        scnt += __popc(bal);
+        if (scnt >= 32) {
+          stg.flush(scnt, ol, lane);
+          scnt = 0;
         }
       }
     }
   }
+  stg.flush(scnt, ol, lane);
   if (M.m || M.m8) mirror_post(M, mbits);
+}
+
+// Phase A's first step as a separate, write-free pass (int32 shortest path,
+// one pivot term, int8 mirror valid): each pair's two cheapest in-edges of
+// SL(j), against lb = D_old[i][j] = c1[i] + r1[j].  A pair certified here keeps
+// D_old (its new distance, P:173-178 / DESIGN.md §4.6); every other pair goes
+// to the continuation list (crow, ccol; count ctr->spill) that the work-queue
+// kernel then finishes from scratch.  Nothing is written to D, so every
+// gathered D[i][m] is D_old and the detection predicate recognises the stale
+// ones exactly.  A lane takes kA0P pairs at once and issues each level of
+// the chain (pair -> shortlist -> D[i][m]) for all of them together: the
+// chain is three dependent DRAM reads, and the pairs one lane overlaps set the
+// pass's speed (the work-queue kernel holds one pair per lane).
+constexpr int kA0P = 4;
+#ifndef PA_SPLIT
+#define PA_SPLIT 1
+#endif
+__global__ void __launch_bounds__(256, PA_MINB) k_phase_a0(const int* __restrict__ SLid,
+                                                          const int32_t* __restrict__ SLw,
+                                                          const int* __restrict__ srow,
+                                                          const int* __restrict__ scol, int64_t npairs,
+                                                          const int32_t* __restrict__ c1,
+                                                          const int32_t* __restrict__ r1,
+                                                          const uint8_t* __restrict__ r1b, int64_t ld, int64_t row0,
+                                                          Mirror M, int* crow, int* ccol, DetectCounters* dc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  npairs = device_count(dc, npairs, 0);
+  const bool mv = (*(volatile unsigned*)M.flag & 1u) == 0u;   // (CTA-uniform: nothing here writes D)
+  __shared__ unsigned s_cnt[8];
+  __shared__ unsigned long long s_base;
+  // block-stride: every warp of the CTA runs the same iterations, so the
+  // continuation slots are reserved once per CTA and iteration (one atomic)
+  constexpr int kBlk = 8 * 32 * kA0P;
+  for (int64_t b0 = blockIdx.x * (int64_t)kBlk; b0 < npairs; b0 += (int64_t)gridDim.x * kBlk) {
+    const int64_t c0 = b0 + warp * (32 * kA0P);
+    int i[kA0P], j[kA0P];
+    bool ok[kA0P], open[kA0P];
+#pragma unroll
+    for (int q = 0; q < kA0P; ++q) {
+      const int64_t p = c0 + q * 32 + lane;
+      ok[q] = p < npairs;
+      i[q] = ok[q] ? srow[p] : 0;
+      j[q] = ok[q] ? scol[p] : 0;
+    }
+    if (mv) {
+      int2 m[kA0P], w[kA0P];
+      int32_t lb[kA0P], ci[kA0P];
+#pragma unroll
+      for (int q = 0; q < kA0P; ++q) {
+        m[q] = ok[q] ? *reinterpret_cast<const int2*>(SLid + (int64_t)j[q] * kSL) : make_int2(-1, -1);
+        w[q] = ok[q] ? *reinterpret_cast<const int2*>(SLw + (int64_t)j[q] * kSL) : make_int2(0, 0);
+        ci[q] = ok[q] ? c1[i[q]] : 0;
+        lb[q] = ok[q] ? ci[q] + r1[j[q]] : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < kA0P; ++q) {
+        const uint8_t* Mrow = M.m8 + (int64_t)(i[q] - row0) * ld;
+        const int ma = m[q].x >= 0 ? m[q].x : 0, mb = m[q].y >= 0 ? m[q].y : 0;
+        const int32_t da = Mrow[ma], db = Mrow[mb], ra = r1b[ma], rb = r1b[mb];
+        int32_t acc = APSP_INF_I32_DEV;
+        // usable: a finite mirrored entry (0x7F reads as INF) that does not
+        // test tight against the pivot snapshots (a stale D_old, Theorem 4)
+        if (m[q].x >= 0 && da != kSat8i && ci[q] + ra != da) acc = min(acc, da + w[q].x);
+        if (m[q].y >= 0 && db != kSat8i && ci[q] + rb != db) acc = min(acc, db + w[q].y);
+        open[q] = ok[q] && acc > lb[q];
+      }
+    } else {   // the mirror is not valid: every pair to the continuation
+#pragma unroll
+      for (int q = 0; q < kA0P; ++q) open[q] = ok[q];
+    }
+    unsigned bal[kA0P], wcnt = 0;
+#pragma unroll
+    for (int q = 0; q < kA0P; ++q) {
+      bal[q] = __ballot_sync(0xffffffffu, open[q]);
+      wcnt += __popc(bal[q]);
+    }
+    if (lane == 0) s_cnt[warp] = wcnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned tot = 0;
+      for (int w2 = 0; w2 < 8; ++w2) tot += s_cnt[w2];
+      s_base = tot ? atomicAdd(&dc->spill, (unsigned long long)tot) : 0ull;
+    }
+    __syncthreads();
+    unsigned long long pos = s_base;
+    for (int w2 = 0; w2 < warp; ++w2) pos += s_cnt[w2];
+#pragma unroll
+    for (int q = 0; q < kA0P; ++q) {
+      if (open[q]) {
+        const unsigned long long s = pos + __popc(bal[q] & ((1u << lane) - 1));
+        crow[s] = i[q];   // (s < npairs <= the list's capacity)
+        ccol[s] = j[q];
+      }
+      pos += __popc(bal[q]);
+    }
+    __syncthreads();   // (s_cnt / s_base are rewritten by the next iteration)
+  }
 }
 
 // Phase A over the detection list (pairs in append order; every pair reads
@@ -1125,9 +1252,21 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
                            const int64_t* rowoff, const int* srow, const int* scol, int64_t npairs,
                            const T* c1, const T* r1, const T* c2, const T* r2, float tau, int* ocnt,
                            int* ocol, int* gprow, int* gpcol, T* glb, unsigned char* gfull, int64_t ocap,
-                           DetectCounters* ctr, int sr, Mirror M, cudaStream_t st, int list, const uint8_t* r1b) {
+                           DetectCounters* ctr, int sr, Mirror M, cudaStream_t st, int list, const uint8_t* r1b,
+                           int* crow, int* ccol) {
   if (npairs <= 0) return cudaSuccess;
   OpenLists<T> ol{ocnt, ocol, rowoff, gprow, gpcol, glb, gfull, ocap, ctr};
+  // the write-free first step (k_phase_a0), then the work queue over the pairs
+  // it left (list 2)
+  if constexpr (std::is_same<T, int32_t>::value) {
+    if (PA_SPLIT && crow && ccol && r1b && M.m8 && !sr && !c2 && list == 0) {
+      const int g0 = (int)std::min<int64_t>(cdiv(npairs, 32 * kA0P * 8), (int64_t)num_sms() * PA_MINB);   // (256 threads)
+      k_phase_a0<<<g0, 256, 0, st>>>(SLid, SLw, srow, scol, npairs, c1, r1, r1b, ld, r.row0, M, crow, ccol, ctr);
+      srow = crow;
+      scol = ccol;
+      list = 2;
+    }
+  }
   // npairs is the capacity bound (the device count decides): full occupancy
   int grid = (int)std::min<int64_t>(cdiv(npairs, 256), (int64_t)num_sms() * 8);
 #define PA(SRV, TWOV)                                                                              \
@@ -1820,7 +1959,7 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
                                          const int*, const int*, int64_t, const T*, const T*,      \
                                          const T*, const T*, float, int*, int*, int*, int*, T*,    \
                                          unsigned char*, int64_t, DetectCounters*, int, Mirror,    \
-                                         cudaStream_t, int, const uint8_t*);                       \
+                                         cudaStream_t, int, const uint8_t*, int*, int*);           \
   template cudaError_t sparse_full<T>(T*, int64_t, int64_t, const T*, int64_t, int64_t,            \
                                       const int*, const int*, const T*, const unsigned char*,      \
                                       int64_t, int, const DetectCounters*, cudaStream_t, Mirror);         \

@@ -77,7 +77,7 @@ __global__ void k_validate_vec(const T* in, const T* in2, int64_t n, int64_t npa
   // (argmin0: (value << 32 | index) of the first vector's minimum; min1: the
   // second vector's minimum — int32 add-node shortcut, values >= 0)
   unsigned long long am = ~0ull;
-  unsigned m1 = ~0u;
+  unsigned m1 = ~0u, wk = ~0u;
   for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < npad; j0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = j0 + threadIdx.x;
     T v = Tr<T>::inf();
@@ -95,7 +95,7 @@ __global__ void k_validate_vec(const T* in, const T* in2, int64_t n, int64_t npa
         if (!(y2 == v)) atomicOr(err, 2u);             // undirected asymmetry
       }
     }
-    if (wmin_bits) wmin_fold<T>(wmin_bits, v, j < n && v >= T(0) && Tr<T>::fin(v));
+    if (wmin_bits) wk = min(wk, wmin_key<T>(v, j < n && v >= T(0) && Tr<T>::fin(v)));
     if (j < npad) out[j] = v;
     if constexpr (!Tr<T>::kFloat) {
       if (j < n && v >= T(0)) {
@@ -104,14 +104,22 @@ __global__ void k_validate_vec(const T* in, const T* in2, int64_t n, int64_t npa
       }
     }
   }
-  if (argmin0 && blockIdx.y == 0) {
+  // block minima first, then one atomic per block and quantity (per-warp
+  // atomics on the same three words serialised at L2)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) am = min(am, __shfl_xor_sync(0xffffffffu, am, o));
-    if ((threadIdx.x & 31) == 0 && am != ~0ull) atomicMin(argmin0, am);
-  }
-  if (min1 && blockIdx.y == 1) {
-    m1 = __reduce_min_sync(0xffffffffu, m1);
-    if ((threadIdx.x & 31) == 0 && m1 != ~0u) atomicMin(min1, m1);
+  for (int o = 16; o > 0; o >>= 1) am = min(am, __shfl_xor_sync(0xffffffffu, am, o));
+  m1 = __reduce_min_sync(0xffffffffu, m1);
+  wk = __reduce_min_sync(0xffffffffu, wk);
+  __shared__ unsigned long long s_am[32];
+  __shared__ unsigned s_m1[32], s_wk[32];
+  const int wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) { s_am[wid] = am; s_m1[wid] = m1; s_wk[wid] = wk; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < nwarp; ++w) { am = min(am, s_am[w]); m1 = min(m1, s_m1[w]); wk = min(wk, s_wk[w]); }
+    if (argmin0 && blockIdx.y == 0 && am != ~0ull) atomicMin(argmin0, am);
+    if (min1 && blockIdx.y == 1 && m1 != ~0u) atomicMin(min1, m1);
+    if (wmin_bits && wk != ~0u && wk < *(volatile unsigned*)wmin_bits) atomicMin(wmin_bits, wk);
   }
   if (rb.host) {   // the last block to finish writes the host's read (err, wmin, mirror flag)
     __syncthreads();
@@ -1487,7 +1495,10 @@ template <> __device__ __forceinline__ float from_bits32<float>(int32_t b) { ret
 // the next kLRAhead groups already in flight (a slab of a few hundred rows
 // with few live ones is otherwise a chain of one load latency per 32 rows).
 // next() returns the row and its c values.
-constexpr int kLRAhead = 4;
+#ifndef LR_AHEAD
+#define LR_AHEAD 4
+#endif
+constexpr int kLRAhead = LR_AHEAD;
 template <typename T, bool TWO>
 struct LiveRows {
   const T* c;
@@ -1636,7 +1647,10 @@ __global__ void __launch_bounds__(256, 3) k_rank1(T* __restrict__ D, int64_t ld,
 // The int32 k_rank1 launched after it exits while the mirror is still valid;
 // if this pass wrote a distance >= 0x7F (mirror now off) the int32 pass runs
 // too — harmless, the update is idempotent.
-constexpr int kR8S = 4;   // rank-1 on the int8 mirror: ring stages (one 1 KB row each)
+#ifndef R8_S
+#define R8_S 4
+#endif
+constexpr int kR8S = R8_S;   // rank-1 on the int8 mirror: ring stages (one 1 KB row each)
 using R8Ring = WarpRing<kR8S, 1, 1024>;
 constexpr int kR8Smem = 8 * (R8Ring::kBytes + kR8S * (int)sizeof(R1Meta));
 template <bool TWO>
@@ -1988,6 +2002,57 @@ using DetectQueue = DetectQueueT<unsigned short>;
 template <typename T, typename WT, typename ColOf>
 __device__ __forceinline__ void detect_flush_q(const DetectQueueT<WT>& Q, int cnt, int64_t i_lo,
                                                const DetectOut<T>& o, int lane, ColOf col_of);
+// The final flush of a CTA's warps together: one atomic on the list cursor per
+// CTA instead of one per warp (every warp of a launch ends with a flush: one
+// hot word serialised ~20K atomics per pass).  Every thread of the CTA calls
+// it (cnt = 0 for a warp without work).
+template <typename T, typename WT, typename ColOf>
+__device__ __forceinline__ void detect_flush_q_cta(const DetectQueueT<WT>& Q, int cnt, int64_t i_lo,
+                                                   const DetectOut<T>& o, int lane, ColOf col_of) {
+  __shared__ unsigned s_tot[32];
+  __shared__ unsigned long long s_base[32];
+  __syncwarp();
+  int mine = 0;
+  for (int e = lane; e < cnt; e += 32) mine += __popcll((unsigned long long)Q.w[e]);
+  int incl = mine;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  if (lane == 31) s_tot[warp] = (unsigned)incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long sum = 0;
+    for (int w = 0; w < nwarps; ++w) {
+      s_base[w] = sum;
+      sum += s_tot[w];
+    }
+    const unsigned long long b0 = sum ? atomicAdd(&o.ctr->total, sum) : 0ull;
+    if (sum && (int64_t)(b0 + sum) > o.lcap) atomicOr(&o.ctr->overflow, 1u);
+    for (int w = 0; w < nwarps; ++w) s_base[w] += b0;
+  }
+  __syncthreads();
+  int64_t pos = (int64_t)s_base[warp] + incl - mine;
+  for (int e = lane; e < cnt; e += 32) {
+    unsigned long long w = Q.w[e];
+    const unsigned rl = Q.rl[e];
+    const int64_t i = i_lo + (rl >> 5);
+    const int ln = (int)(rl & 31u);
+    while (w) {
+      const int bit = __ffsll(w) - 1;
+      w &= w - 1;
+      const int64_t j = col_of(bit, ln);
+      if (pos < o.lcap) {
+        o.prow[pos] = (int)i;
+        o.pcol[pos] = (int)j;
+      }
+      ++pos;
+    }
+  }
+  __syncwarp();
+}
 template <typename T>
 __device__ __forceinline__ void detect_flush(const DetectQueue& Q, int cnt, int64_t i_lo, int chunk,
                                              bool m16, const DetectOut<T>& o, int lane) {
@@ -2354,6 +2419,12 @@ __global__ void k_detect_rows(Rows r, const int* __restrict__ rowcnt, int64_t* r
 #ifndef D8_MINB
 #define D8_MINB 3
 #endif
+#ifndef D8_VOTE2
+#define D8_VOTE2 1   // one warp vote per ring stage before the per-row votes
+#endif
+#ifndef D8_PF
+#define D8_PF 0   // L2 prefetch distance of the detection ring, in stages beyond the ring (0: off)
+#endif
 // A warp owns a 1024-column chunk of a row slab; lane l the 16-byte groups at
 // 16 l and 512 + 16 l.  Rows arrive through a per-warp TMA ring: one 2-D
 // tensor copy (the mirror as a uint32 tensor of local rows x ld / 4 words, box
@@ -2378,12 +2449,13 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
   DetectQueueT<unsigned>& Q = sq[MODE == 1 ? (threadIdx.x >> 5) : 0];
   int qcnt = 0;
   const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (gw >= tl.warps) return;
+  // (a warp past the last task stays for the CTA's final flush, with no rows)
+  const bool act = gw < tl.warps;
   const int chunk = (int)(gw % tl.nchunk);
   const int slab = (int)(gw / tl.nchunk);
   const int64_t i_lo = r.lo + slab * tl.slab;
   const int64_t i_hi = min(r.hi, i_lo + tl.slab);
-  const int rows = (int)max((int64_t)0, i_hi - i_lo);
+  const int rows = act ? (int)max((int64_t)0, i_hi - i_lo) : 0;
   // this lane's columns: g0 + [0, 16) and g0 + 512 + [0, 16)
   const int64_t g0 = (int64_t)chunk * 1024 + 16 * lane;
   auto col_of = [&](int bit, int ln) -> int64_t {
@@ -2399,9 +2471,12 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
   const int nst = (rows + kD8R - 1) / kD8R;
   auto issue = [&](int st) {
     if (st < nst) ring.issue_box(st, &tm, cw0, rl0 + st * kD8R, lane);
+    if (D8_PF > 0 && lane == 0 && st + D8_PF < nst) tensor2d_prefetch_l2(&tm, cw0, rl0 + (st + D8_PF) * kD8R);
   };
 #pragma unroll
   for (int st = 0; st < S - 1; ++st) issue(st);
+  if (D8_PF > 0 && lane == 0)   // (the stages between the ring's first copies and the first prefetches)
+    for (int st = S - 1; st < D8_PF && st < nst; ++st) tensor2d_prefetch_l2(&tm, cw0, rl0 + st * kD8R);
   // this lane's pivot-row bytes: 16-byte loads where the 4 columns are all < n
   uint32_t rw[8], rw2[TWO ? 8 : 1];
   unsigned vmask = 0;   // bit b <-> column col_of(b, lane): j < n and j != skip
@@ -2436,10 +2511,15 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
   for (int st = 0; st < nst; ++st) {
     issue(st + S - 1);
     ring.wait(st);
+    // the fast test of every row of the stage first, one vote for the stage
+    // (independent chains; most stages have no tight entry in any lane)
+    uint32_t cwv[kD8R], cwv2[kD8R], accv[kD8R], accs = 0;
 #pragma unroll
     for (int h = 0; h < kD8R; ++h) {
       const int rr = st * kD8R + h;
-      if (rr >= rows) break;   // warp-uniform
+      accv[h] = 0;
+      cwv[h] = cwv2[h] = 0;
+      if (rr >= rows) continue;   // warp-uniform
       if ((rr & 31) == 0) {    // the pivot column for the next 32 rows, one per lane (INF on row k)
         const int64_t il = i_lo + rr + lane;
         const bool inr = rr + lane < rows;
@@ -2448,6 +2528,8 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
       }
       const uint32_t cw = __shfl_sync(0xffffffffu, cl, rr & 31);
       const uint32_t cw2 = TWO ? __shfl_sync(0xffffffffu, cl2, rr & 31) : 0u;
+      cwv[h] = cw;
+      cwv2[h] = cw2;
       const uint4* rp = reinterpret_cast<const uint4*>(ring.row(st, h));
       const uint4 w0 = rp[lane], w1 = rp[32 + lane];
       const uint32_t d[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
@@ -2464,6 +2546,18 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
           acc |= (u2 - 0x01010101u) & ~u2;
         }
       }
+      accv[h] = acc;
+      accs |= acc;
+    }
+    if (D8_VOTE2 && !__any_sync(0xffffffffu, (accs & 0x80808080u) != 0u)) continue;
+#pragma unroll
+    for (int h = 0; h < kD8R; ++h) {
+      const int rr = st * kD8R + h;
+      if (rr >= rows) break;   // warp-uniform
+      const uint32_t acc = accv[h], cw = cwv[h], cw2 = cwv2[h];
+      const uint4* rp = reinterpret_cast<const uint4*>(ring.row(st, h));
+      const uint4 w0 = rp[lane], w1 = rp[32 + lane];
+      const uint32_t d[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
       if (!__any_sync(0xffffffffu, (acc & 0x80808080u) != 0u)) continue;
       // some lane has a tight entry in this row: exact per-byte flags of the
       // words that have a zero byte (the test above is exact per word)
@@ -2513,7 +2607,7 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
       }
     }
   }
-  if (MODE == 1) detect_flush_q<T>(Q, qcnt, i_lo, o, lane, col_of);
+  if (MODE == 1) detect_flush_q_cta<T>(Q, qcnt, i_lo, o, lane, col_of);
 }
 
 template <typename T>

@@ -868,6 +868,15 @@ ZeroSet recompute_zero_set(apsp_handle* h) {
   return z;
 }
 
+// One GPU: A2, B and the open rows' minima inside the cooperative rounds
+// launch (1) or as their own launches before it (0: measured faster — the
+// cooperative grid, 2 CTAs per SM, has an eighth of the warps A2's
+// one-warp-per-pair gathers get from a full launch: 90 vs 58 us per BJ.c4 removal)
+#ifndef COOP_TAIL
+#define COOP_TAIL 0
+#endif
+constexpr bool kCoopTail = COOP_TAIL != 0;
+
 // Phase A's algorithmic bytes per listed pair: the list entry (8), the first
 // two shortlist entries of column j (ids + weights, 16), their D entries on
 // the int8 mirror (2) and pivot values (8)
@@ -964,7 +973,7 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
                          lcap, c1, r1, c2, r2, h->tau, h->ocnt(), h->ocol(), h->gprow(), h->gpcol(),
                          h->glb<T>(), h->gfull(), ocap, h->ctr(), h->sr, h->mirror<T>(), h->st, 0, r1b,
                          h->prow(), h->pcol()));   // (the rounds' frontier buffers: free until the rounds)
-    if (!coop) {   // (one GPU: A2, B and the row minima run inside the cooperative launch)
+    if (!coop || !kCoopTail) {   // (kCoopTail: inside the cooperative launch instead)
       // A2: whole-shortlist pass over the open pairs, now that certified values are final
       PK(APSP_K_SPARSE_R, 0.0,
          sparse_short<T>(h->Dl<T>(), h->ld, h->row0, h->slid(), h->slw<T>(), h->wnext<T>(), h->gprow(),
@@ -993,14 +1002,15 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
                    h->coop_total_word(), h->bigq(), h->bigq_ctr(), h->heavy_set(), h->heavy_x(), h->ld,
                    h->heavy_min < 0 ? 0 : (h->heavy_min > 0 ? h->heavy_min : (int)std::max<int64_t>(512, n / 8)),
                    r.hi - r.lo, n, removal ? skip : -1,
-                   1, h->slid(), h->slw<T>(), h->wnext<T>(), h->gfull(), h->host_small_dev, h->mirror_flag()};
+                   kCoopTail ? 1 : 0, h->slid(), h->slw<T>(), h->wnext<T>(), h->gfull(), h->host_small_dev,
+                   h->mirror_flag()};
       PK(APSP_K_SPARSE_R, 0.0,
          sparse_rounds_coop<T>(h->Dl<T>(), h->ld, h->row0, h->WT<T>(), h->ld, h->gprow(), h->gpcol(), h->glb<T>(),
                                ocap, h->rowoff(), h->ocnt(), h->ocol(), rb, 0, h->max_rounds, h->anyflag(), h->sr,
                                h->ctr(), h->st, reinterpret_cast<unsigned*>(h->anyrow()), h->wmin<T>(),
                                h->mirror<T>()));
       last_total = h->coop_total_word();
-      if (removal) {   // the shortlist upkeep after A2, its last reader (inside the launch above)
+      if (removal && kCoopTail) {   // the shortlist upkeep after A2, its last reader (inside the launch above)
         apsp_status s2 = fork_shortlist_remove<T>(h, skip);
         if (s2 != APSP_OK) return s2;
       }
@@ -1018,10 +1028,11 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   // ---- the one host read of this update: counters (summed over ranks) ----
   long long* hv = reinterpret_cast<long long*>(h->host_small);
   unsigned* hmf = reinterpret_cast<unsigned*>(h->host_small) + 12;
-  if (h->world == 1 && coop && try_sparse) {
+  if (h->world == 1 && coop && try_sparse && kCoopTail) {
     // (the cooperative launch packed the counters into mapped host memory)
   } else if (h->world == 1) {   // packed straight into mapped host memory
-    CK(pack_to_host(h->ctr(), last_total, h->mirror_flag(), h->host_small_dev, h->st, nullptr));
+    CK(pack_to_host(h->ctr(), last_total, h->mirror_flag(), h->host_small_dev, h->st,
+                    coop && try_sparse ? h->coop_rounds_word() : nullptr));
   } else {
     long long* v = reinterpret_cast<long long*>(h->small());
     CK(pack_counters(h->ctr(), last_total, v, h->st));   // total rows ovf1 ovf2 changed | maxrow

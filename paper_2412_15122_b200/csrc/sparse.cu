@@ -880,7 +880,10 @@ cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const 
 // Each lane walks SL(j) in ascending weight order, 8 entries per batch, and
 // stops at the first batch whose bound reaches lb (certified); after
 // kPhaseABatches batches the pair is left open for A2 / B / the rounds.
-constexpr int kPhaseABatches = 9;   // sorted positions 0-71
+#ifndef PA_BATCHES
+#define PA_BATCHES 9
+#endif
+constexpr int kPhaseABatches = PA_BATCHES;   // 9: sorted positions 0-71
 #ifndef PA_MINB
 #define PA_MINB 4   // 4 CTAs per SM (64 registers, no spills): latency-bound, occupancy wins
 #endif
@@ -1915,7 +1918,10 @@ cudaError_t sparse_rounds_coop(T* D, int64_t ld, int64_t row0, const T* WT, int6
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0));
     if (bps <= 0) return cudaErrorInvalidConfiguration;
   }
-  const int grid = std::min(bps, 2) * num_sms();
+#ifndef COOP_BPS
+#define COOP_BPS 2
+#endif
+  const int grid = std::min(bps, COOP_BPS) * num_sms();
   void* args[] = {&D, &ld, &row0, &WT, &ldw, &gprow, &gpcol, &glb, &nopen, &rowoff, &ocnt, &ocol,
                   const_cast<RoundBufs*>(&rb), &r0, &r1, &any, &dc, &rowkey, &wmin, &M};
   return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, 256, args, 0, st);

@@ -1638,6 +1638,126 @@ __global__ void __launch_bounds__(256, 3) k_rank1(T* __restrict__ D, int64_t ld,
   (void)rows_read;
   if (has_mirror(M)) mirror_post(M, mbits);
 }
+// This lane's 32 columns of the pivot row (colj(e) = g0 + (e >> 4) * 512 +
+// (e & 15)) as int16x2 words saturated at 0x3FFF (0x3FFF past n)
+template <bool TWO>
+__device__ __forceinline__ void r8_load_pivot(const int32_t* __restrict__ rv, const int32_t* __restrict__ rv2, int64_t n,
+                                              int64_t g0, uint32_t (&r2)[16], uint32_t (&r2b)[TWO ? 16 : 1]) {
+  auto colj = [&](int e) -> int64_t { return g0 + (e >> 4) * 512 + (e & 15); };
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {   // 4 columns colj(4v) .. colj(4v + 3) per 16-byte load
+    const int64_t j0 = colj(4 * v);
+    if (j0 + 3 < n) {
+      const Vec4<int32_t> x = ld4<int32_t>(rv + j0);
+      r2[2 * v] = (uint32_t)sat16(x.x) | (uint32_t)sat16(x.y) << 16;
+      r2[2 * v + 1] = (uint32_t)sat16(x.z) | (uint32_t)sat16(x.w) << 16;
+      if (TWO) {
+        const Vec4<int32_t> y = ld4<int32_t>(rv2 + j0);
+        r2b[2 * v] = (uint32_t)sat16(y.x) | (uint32_t)sat16(y.y) << 16;
+        r2b[2 * v + 1] = (uint32_t)sat16(y.z) | (uint32_t)sat16(y.w) << 16;
+      }
+    } else {
+#pragma unroll
+      for (int q = 2 * v; q < 2 * v + 2; ++q) {
+        uint32_t a = 0, b = 0;
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const int64_t j = colj(2 * q + hf);
+          a |= (uint32_t)(j < n ? sat16(rv[j]) : 0x3FFF) << (16 * hf);
+          if (TWO) b |= (uint32_t)(j < n ? sat16(rv2[j]) : 0x3FFF) << (16 * hf);
+        }
+        r2[q] = a;
+        if (TWO) r2b[q] = b;
+      }
+    }
+  }
+}
+
+// One row chunk of the rank-1 pass on the int8 mirror: lane `lane`'s 2 x 16
+// mirror bytes of row i (wv: columns g0 + [0,16) and g0 + 512 + [0,16)),
+// min(d, c + r) in packed int16x2 (or per entry in int32 when the mirror has
+// INF entries), the changed 16-byte halves written to D, the mirror and MT.
+template <bool TWO>
+__device__ __forceinline__ unsigned r8_apply_row(int32_t* __restrict__ D, int64_t ld, Rows r, int64_t n, Mirror M,
+                                                 int64_t i, int32_t ci, int32_t ci2, const uint4 (&wv)[2], int64_t g0,
+                                                 bool has_inf, const uint32_t (&r2)[16],
+                                                 const uint32_t (&r2b)[TWO ? 16 : 1],
+                                                 const int32_t* __restrict__ rv, const int32_t* __restrict__ rv2) {
+  const int32_t I = APSP_INF_I32_DEV;
+  unsigned mbits = 0;
+  int32_t* drow = D + (i - r.row0) * ld;
+  uint8_t* mrow = M.m8 + (i - r.row0) * ld;
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    const int64_t jg = g0 + 512 * g;
+    if (jg >= n) continue;
+    const uint4 wb = wv[g];
+    if (!has_inf) {
+      const uint32_t cw = (uint32_t)sat16(ci) * 0x10001u, cw2 = (uint32_t)sat16(ci2) * 0x10001u;
+      const uint4 lo = widen8(make_uint2(wb.x, wb.y)), hi = widen8(make_uint2(wb.z, wb.w));
+      const uint32_t d[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+      uint32_t o[8], diff = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        o[q] = __viaddmin_s16x2(cw, r2[8 * g + q], d[q]);
+        if (TWO) o[q] = __viaddmin_s16x2(cw2, r2b[8 * g + q], o[q]);
+        diff |= o[q] ^ d[q];
+      }
+      if (!diff) continue;
+      if (jg + 16 <= n) {   // rewrite the half: 64 bytes of D, 16 mirror bytes
+        int4* dst = reinterpret_cast<int4*>(drow + jg);
+        uint32_t mw[4];
+        uint32_t big = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t a = o[2 * q], b = o[2 * q + 1];
+          dst[q] = make_int4((int)(a & 0xFFFFu), (int)(a >> 16), (int)(b & 0xFFFFu), (int)(b >> 16));
+          const uint32_t sa = __vmins2(a, 0x007F007Fu), sb = __vmins2(b, 0x007F007Fu);   // sat8
+          mw[q] = __byte_perm(sa, sb, 0x6420);
+          big |= __vcmpgeu2(a, 0x007F007Fu) | __vcmpgeu2(b, 0x007F007Fu);
+        }
+        *reinterpret_cast<uint4*>(mrow + jg) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+        if (big) mbits |= kMirrorOff;   // a distance >= 0x7F: the int8 mirror is no longer exact
+        if (M.mt) {   // the changed bytes into the transposed copy
+          const uint32_t ow[4] = {wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t x = mw[q] ^ ow[q];
+            if (!x) continue;
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if ((x >> (8 * e)) & 0xFFu) mput_t(M, i - r.row0, jg + 4 * q + e, (uint8_t)(mw[q] >> (8 * e)));
+          }
+        }
+      } else {   // the row's ragged end: element stores below n
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          if (jg + e < n) {
+            const int32_t v = (int32_t)((o[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
+            drow[jg + e] = v;
+            mbits |= mput(M, (i - r.row0) * ld + jg + e, v);
+          }
+      }
+    } else {   // INF entries present: exact int32 per entry
+      const uint32_t wd[4] = {wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int64_t j = jg + e;
+        if (j >= n) break;
+        const int32_t d8 = (int32_t)((wd[e >> 2] >> (8 * (e & 3))) & 0xFFu);
+        const int32_t dv = d8 == kSat8i ? I : d8;
+        int32_t nv = min(I, ci + rv[j]);
+        if (TWO) nv = min(nv, min(I, ci2 + rv2[j]));
+        if (nv < dv) {
+          drow[j] = nv;
+          mbits |= mput(M, (i - r.row0) * ld + j, nv);
+        }
+      }
+    }
+  }
+  return mbits;
+}
+
 // Rank-1 pass on the int8 mirror (shortest path, int32 D, mirror valid):
 // D[i][j] = min(D[i][j], c[i] + r[j] (, c2[i] + r2[j])).  While the mirror is
 // valid it images D exactly (0x7F = INF), so D itself is never read: a row
@@ -1649,6 +1769,9 @@ __global__ void __launch_bounds__(256, 3) k_rank1(T* __restrict__ D, int64_t ld,
 // too — harmless, the update is idempotent.
 #ifndef R8_S
 #define R8_S 4
+#endif
+#ifndef R8_FENCE
+#define R8_FENCE 1   // generic->async proxy fence before each ring refill
 #endif
 constexpr int kR8S = R8_S;   // rank-1 on the int8 mirror: ring stages (one 1 KB row each)
 using R8Ring = WarpRing<kR8S, 1, 1024>;
@@ -1680,33 +1803,7 @@ __global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, in
   const int64_t g0 = (int64_t)chunk * 1024 + 16 * lane;   // columns g0 + [0,16) and g0 + 512 + [0,16)
   auto colj = [&](int e) -> int64_t { return g0 + (e >> 4) * 512 + (e & 15); };
   uint32_t r2[16], r2b[TWO ? 16 : 1];   // word q: columns colj(2q), colj(2q + 1), saturated at 0x3FFF
-#pragma unroll
-  for (int v = 0; v < 8; ++v) {   // 4 columns colj(4v) .. colj(4v + 3) per 16-byte load
-    const int64_t j0 = colj(4 * v);
-    if (j0 + 3 < n) {
-      const Vec4<int32_t> x = ld4<int32_t>(rv + j0);
-      r2[2 * v] = (uint32_t)sat16(x.x) | (uint32_t)sat16(x.y) << 16;
-      r2[2 * v + 1] = (uint32_t)sat16(x.z) | (uint32_t)sat16(x.w) << 16;
-      if (TWO) {
-        const Vec4<int32_t> y = ld4<int32_t>(rv2 + j0);
-        r2b[2 * v] = (uint32_t)sat16(y.x) | (uint32_t)sat16(y.y) << 16;
-        r2b[2 * v + 1] = (uint32_t)sat16(y.z) | (uint32_t)sat16(y.w) << 16;
-      }
-    } else {
-#pragma unroll
-      for (int q = 2 * v; q < 2 * v + 2; ++q) {
-        uint32_t a = 0, b = 0;
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          const int64_t j = colj(2 * q + hf);
-          a |= (uint32_t)(j < n ? sat16(rv[j]) : 0x3FFF) << (16 * hf);
-          if (TWO) b |= (uint32_t)(j < n ? sat16(rv2[j]) : 0x3FFF) << (16 * hf);
-        }
-        r2[q] = a;
-        if (TWO) r2b[q] = b;
-      }
-    }
-  }
+  r8_load_pivot<TWO>(rv, rv2, n, g0, r2, r2b);
   int64_t rows_read = 0;
   unsigned mbits = 0;
   // the rows that can change (c[i] or c2[i] finite: LiveRows, one ballot per
@@ -1729,7 +1826,8 @@ __global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, in
     const int64_t i = it.next(lane, &ci, &ci2);
     if (i < 0) return;
     if (lane == 0) meta[issued % kR8S] = R1Meta{i, ci, ci2};
-    ring.issue(issued, cbytes, lane, [&](int) { return mchunk + i * ld; });
+    auto src = [&](int) { return mchunk + i * ld; };
+    ring.template issue<decltype(src), R8_FENCE>(issued, cbytes, lane, src);
     ++issued;
   };
   for (int k = 0; k < kR8S - 1; ++k) produce();
@@ -1742,76 +1840,7 @@ __global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, in
     const uint4* srow = reinterpret_cast<const uint4*>(ring.row(st, 0));
     const uint4 wv[2] = {srow[lane], srow[32 + lane]};
     ++rows_read;
-    int32_t* drow = D + (i - r.row0) * ld;
-    uint8_t* mrow = M.m8 + (i - r.row0) * ld;
-#pragma unroll
-    for (int g = 0; g < 2; ++g) {
-      const int64_t jg = g0 + 512 * g;
-      if (jg >= n) continue;
-      const uint4 wb = wv[g];
-      if (!has_inf) {
-        const uint32_t cw = (uint32_t)sat16(ci) * 0x10001u, cw2 = (uint32_t)sat16(ci2) * 0x10001u;
-        const uint4 lo = widen8(make_uint2(wb.x, wb.y)), hi = widen8(make_uint2(wb.z, wb.w));
-        const uint32_t d[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-        uint32_t o[8], diff = 0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          o[q] = __viaddmin_s16x2(cw, r2[8 * g + q], d[q]);
-          if (TWO) o[q] = __viaddmin_s16x2(cw2, r2b[8 * g + q], o[q]);
-          diff |= o[q] ^ d[q];
-        }
-        if (!diff) continue;
-        if (jg + 16 <= n) {   // rewrite the half: 64 bytes of D, 16 mirror bytes
-          int4* dst = reinterpret_cast<int4*>(drow + jg);
-          uint32_t mw[4];
-          uint32_t big = 0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint32_t a = o[2 * q], b = o[2 * q + 1];
-            dst[q] = make_int4((int)(a & 0xFFFFu), (int)(a >> 16), (int)(b & 0xFFFFu), (int)(b >> 16));
-            const uint32_t sa = __vmins2(a, 0x007F007Fu), sb = __vmins2(b, 0x007F007Fu);   // sat8
-            mw[q] = __byte_perm(sa, sb, 0x6420);
-            big |= __vcmpgeu2(a, 0x007F007Fu) | __vcmpgeu2(b, 0x007F007Fu);
-          }
-          *reinterpret_cast<uint4*>(mrow + jg) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
-          if (big) mbits |= kMirrorOff;   // a distance >= 0x7F: the int8 mirror is no longer exact
-          if (M.mt) {   // the changed bytes into the transposed copy
-            const uint32_t ow[4] = {wb.x, wb.y, wb.z, wb.w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint32_t x = mw[q] ^ ow[q];
-              if (!x) continue;
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if ((x >> (8 * e)) & 0xFFu) mput_t(M, i - r.row0, jg + 4 * q + e, (uint8_t)(mw[q] >> (8 * e)));
-            }
-          }
-        } else {   // the row's ragged end: element stores below n
-#pragma unroll
-          for (int e = 0; e < 16; ++e)
-            if (jg + e < n) {
-              const int32_t v = (int32_t)((o[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
-              drow[jg + e] = v;
-              mbits |= mput(M, (i - r.row0) * ld + jg + e, v);
-            }
-        }
-      } else {   // INF entries present: exact int32 per entry
-        const uint32_t wd[4] = {wb.x, wb.y, wb.z, wb.w};
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int64_t j = jg + e;
-          if (j >= n) break;
-          const int32_t d8 = (int32_t)((wd[e >> 2] >> (8 * (e & 3))) & 0xFFu);
-          const int32_t dv = d8 == kSat8i ? I : d8;
-          int32_t nv = min(I, ci + rv[j]);
-          if (TWO) nv = min(nv, min(I, ci2 + rv2[j]));
-          if (nv < dv) {
-            drow[j] = nv;
-            mbits |= mput(M, (i - r.row0) * ld + j, nv);
-          }
-        }
-      }
-    }
+    mbits |= r8_apply_row<TWO>(D, ld, r, n, M, i, ci, ci2, wv, g0, has_inf, r2, r2b, rv, rv2);
   }
   mbits = __reduce_or_sync(0xffffffffu, mbits);
   if (lane == 0 && (mbits & ~*(volatile unsigned*)M.flag)) {
@@ -2419,6 +2448,9 @@ __global__ void k_detect_rows(Rows r, const int* __restrict__ rowcnt, int64_t* r
 #ifndef D8_MINB
 #define D8_MINB 3
 #endif
+#ifndef D8_FENCE
+#define D8_FENCE 1   // generic->async proxy fence before each ring refill
+#endif
 #ifndef D8_VOTE2
 #define D8_VOTE2 1   // one warp vote per ring stage before the per-row votes
 #endif
@@ -2470,7 +2502,7 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
   const int cw0 = chunk * 256, rl0 = (int)(i_lo - r.row0);
   const int nst = (rows + kD8R - 1) / kD8R;
   auto issue = [&](int st) {
-    if (st < nst) ring.issue_box(st, &tm, cw0, rl0 + st * kD8R, lane);
+    if (st < nst) ring.template issue_box<D8_FENCE>(st, &tm, cw0, rl0 + st * kD8R, lane);
     if (D8_PF > 0 && lane == 0 && st + D8_PF < nst) tensor2d_prefetch_l2(&tm, cw0, rl0 + (st + D8_PF) * kD8R);
   };
 #pragma unroll

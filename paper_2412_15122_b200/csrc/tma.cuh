@@ -114,22 +114,26 @@ struct WarpRing {
   }
   // lane 0: refill stage `stage` with rows src(h), h < R, `bytes` each.  The
   // caller's lanes finished reading the slot (the last use of it) before.
-  template <typename Src>
+  template <typename Src, bool kFence = true>
   __device__ __forceinline__ void issue(int stage, unsigned bytes, int lane, Src src) {
     __syncwarp();
     if (lane == 0) {
-      fence_proxy_async();
+      if (kFence) fence_proxy_async();
       uint64_t* b = bar + stage % S;
       mbar_expect_tx(b, R * bytes);
 #pragma unroll
       for (int h = 0; h < R; ++h) bulk_g2s(row(stage, h), src(h), bytes, b);
     }
   }
-  // lane 0: refill stage `stage` with one 2-D tensor box (R rows of CB bytes)
+  // lane 0: refill stage `stage` with one 2-D tensor box (R rows of CB bytes).
+  // kFence = false: no generic->async proxy fence — for a caller whose last
+  // reads of the slot fed a warp vote before this call (the values were in
+  // registers, so the reads are complete before the copy can land)
+  template <bool kFence = true>
   __device__ __forceinline__ void issue_box(int stage, const CUtensorMap* map, int c0, int c1, int lane) {
     __syncwarp();
     if (lane == 0) {
-      fence_proxy_async();
+      if (kFence) fence_proxy_async();
       uint64_t* b = bar + stage % S;
       mbar_expect_tx(b, R * CB);
       tensor2d_g2s(row(stage, 0), map, c0, c1, b);

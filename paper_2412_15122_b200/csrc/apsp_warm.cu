@@ -1028,11 +1028,10 @@ apsp_status recompute(apsp_handle* h, int64_t skip, const T* c1, const T* r1, co
   // ---- the one host read of this update: counters (summed over ranks) ----
   long long* hv = reinterpret_cast<long long*>(h->host_small);
   unsigned* hmf = reinterpret_cast<unsigned*>(h->host_small) + 12;
-  if (h->world == 1 && coop && try_sparse && kCoopTail) {
+  if (h->world == 1 && coop && try_sparse) {
     // (the cooperative launch packed the counters into mapped host memory)
   } else if (h->world == 1) {   // packed straight into mapped host memory
-    CK(pack_to_host(h->ctr(), last_total, h->mirror_flag(), h->host_small_dev, h->st,
-                    coop && try_sparse ? h->coop_rounds_word() : nullptr));
+    CK(pack_to_host(h->ctr(), last_total, h->mirror_flag(), h->host_small_dev, h->st, nullptr));
   } else {
     long long* v = reinterpret_cast<long long*>(h->small());
     CK(pack_counters(h->ctr(), last_total, v, h->st));   // total rows ovf1 ovf2 changed | maxrow

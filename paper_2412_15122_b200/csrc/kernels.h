@@ -265,7 +265,7 @@ struct RoundBufs {
   // before the rounds; the counters packed into mapped host memory after
   int tail;
   const int* slid; const void* slw; const void* wnext; unsigned char* gfull;
-  void* host; const unsigned* mflag;
+  void* host; const unsigned* mflag;   // host: mapped memory for the counters (packed at the end), or null
 };
 constexpr int kHeavy = 32;
 // rounds r0 .. r1 - 1 in one cooperative launch (grid barriers between rounds),

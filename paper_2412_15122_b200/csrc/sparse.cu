@@ -1890,7 +1890,7 @@ __global__ void __launch_bounds__(256) k_sparse_rounds_coop(T* D, int64_t ld, in
     const int last = round > r0 ? round - 1 : r0;
     *rb.last_total = rb.chg[(int64_t)(last & 3) * rb.stride + rb.cap];
   }
-  if (rb.tail) {   // every block's writes and flag bits in place: the host's read
+  if (rb.host) {   // every block's writes and flag bits in place: the host's read
     grid.sync();
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       volatile long long* host = static_cast<volatile long long*>(rb.host);

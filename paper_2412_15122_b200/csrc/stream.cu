@@ -1081,7 +1081,13 @@ __global__ void __launch_bounds__(256) k_addcol_gather(AddScratch a, Rows r, con
 // per row (which cost ~85 B of DRAM each, measured).  U's (t, in[t], out[t])
 // are staged in shared memory.
 constexpr int kAddColMax = 2048;   // |U| limit (= kAddColLimit of the host)
-constexpr int kACQ = 64, kACY = 8;   // row quads per CTA (256 rows), slices of U
+#ifndef ACQ
+#define ACQ 32
+#endif
+#ifndef ACY
+#define ACY 16
+#endif
+constexpr int kACQ = ACQ, kACY = ACY;   // row quads per CTA (4 kACQ rows), slices of U (32 x 16: 64 x 8 was 5 us slower per add)
 __global__ void __launch_bounds__(kACQ * kACY) k_addcol_mt(AddScratch a, Rows r, const uint8_t* __restrict__ mt,
                                                            int64_t ldt, const int* __restrict__ ulist,
                                                            const int* __restrict__ uin, const int* __restrict__ uout,
@@ -1773,8 +1779,13 @@ __device__ __forceinline__ unsigned r8_apply_row(int32_t* __restrict__ D, int64_
 #ifndef R8_FENCE
 #define R8_FENCE 1   // generic->async proxy fence before each ring refill
 #endif
-constexpr int kR8S = R8_S;   // rank-1 on the int8 mirror: ring stages (one 1 KB row each)
-using R8Ring = WarpRing<kR8S, 1, 1024>;
+#ifndef R8_CW
+#define R8_CW 1
+#endif
+// rank-1 on the int8 mirror: ring stages (one row chunk of kR8C KB each;
+// measured at BJ.c4's adds: 1 KB chunks 39 us, 2 KB chunks 55 us per add)
+constexpr int kR8S = R8_S, kR8C = R8_CW;
+using R8Ring = WarpRing<kR8S, 1, 1024 * kR8C>;
 constexpr int kR8Smem = 8 * (R8Ring::kBytes + kR8S * (int)sizeof(R1Meta));
 template <bool TWO>
 __global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, int64_t ld, Rows r, int64_t n,
@@ -1800,10 +1811,12 @@ __global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, in
   const int64_t i_lo = r.lo + slab * tl.slab;
   const int64_t i_hi = min(r.hi, i_lo + tl.slab);
   const int32_t I = APSP_INF_I32_DEV;
-  const int64_t g0 = (int64_t)chunk * 1024 + 16 * lane;   // columns g0 + [0,16) and g0 + 512 + [0,16)
-  auto colj = [&](int e) -> int64_t { return g0 + (e >> 4) * 512 + (e & 15); };
-  uint32_t r2[16], r2b[TWO ? 16 : 1];   // word q: columns colj(2q), colj(2q + 1), saturated at 0x3FFF
-  r8_load_pivot<TWO>(rv, rv2, n, g0, r2, r2b);
+  // chunk: kR8C KB of columns; per KB h, lane owns g0 + 1024 h + [0,16) and
+  // g0 + 1024 h + 512 + [0,16)
+  const int64_t g0 = (int64_t)chunk * 1024 * kR8C + 16 * lane;
+  uint32_t r2[kR8C][16], r2b[kR8C][TWO ? 16 : 1];   // int16x2 pivot words, saturated at 0x3FFF
+#pragma unroll
+  for (int h = 0; h < kR8C; ++h) r8_load_pivot<TWO>(rv, rv2, n, g0 + 1024 * h, r2[h], r2b[h]);
   int64_t rows_read = 0;
   unsigned mbits = 0;
   // the rows that can change (c[i] or c2[i] finite: LiveRows, one ballot per
@@ -1816,8 +1829,9 @@ __global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, in
   const int warp = threadIdx.x >> 5;
   ring.init(r8_raw + warp * R8Ring::kBytes, lane);
   R1Meta* meta = reinterpret_cast<R1Meta*>(r8_raw + 8 * R8Ring::kBytes) + warp * kR8S;
-  const uint8_t* mchunk = M.m8 + (int64_t)chunk * 1024 - r.row0 * ld;   // + i * ld: row i's chunk
-  const unsigned cbytes = (unsigned)((min((int64_t)1024, n - (int64_t)chunk * 1024) + 15) & ~15);
+  const uint8_t* mchunk = M.m8 + (int64_t)chunk * 1024 * kR8C - r.row0 * ld;   // + i * ld: row i's chunk
+  const unsigned cbytes =
+      (unsigned)((min((int64_t)1024 * kR8C, n - (int64_t)chunk * 1024 * kR8C) + 15) & ~15);
   LiveRows<int32_t, TWO> it;
   it.init(c, c2, i_lo, i_hi, lane);
   int issued = 0;
@@ -1838,9 +1852,13 @@ __global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, in
     const int64_t i = mt.i;
     const int32_t ci = mt.c, ci2 = TWO ? mt.c2 : I;
     const uint4* srow = reinterpret_cast<const uint4*>(ring.row(st, 0));
-    const uint4 wv[2] = {srow[lane], srow[32 + lane]};
     ++rows_read;
-    mbits |= r8_apply_row<TWO>(D, ld, r, n, M, i, ci, ci2, wv, g0, has_inf, r2, r2b, rv, rv2);
+#pragma unroll
+    for (int h = 0; h < kR8C; ++h) {
+      if ((int64_t)chunk * 1024 * kR8C + 1024 * h >= n) break;   // (warp-uniform: this KB starts past n)
+      const uint4 wv[2] = {srow[64 * h + lane], srow[64 * h + 32 + lane]};
+      mbits |= r8_apply_row<TWO>(D, ld, r, n, M, i, ci, ci2, wv, g0 + 1024 * h, has_inf, r2[h], r2b[h], rv, rv2);
+    }
   }
   mbits = __reduce_or_sync(0xffffffffu, mbits);
   if (lane == 0 && (mbits & ~*(volatile unsigned*)M.flag)) {
@@ -1851,7 +1869,7 @@ __global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, in
     atomicOr(M.flag, mbits);
   }
   if (bytes_read && lane == 0 && rows_read) {
-    const int64_t cols = min((int64_t)1024, n - (int64_t)chunk * 1024);
+    const int64_t cols = min((int64_t)1024 * kR8C, n - (int64_t)chunk * 1024 * kR8C);
     atomicAdd(bytes_read, (unsigned long long)(rows_read * cols));
   }
 }
@@ -1866,7 +1884,7 @@ cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, 
   if constexpr (std::is_same<T, int32_t>::value) {
     if (!sr && M.m8) {   // the int8 twin first (the int32 kernel then exits while M stays valid)
       constexpr int wps = R8_WPS;   // one wave at 2 CTAs (16 warps) per SM
-      const Tiling t8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256, wps);
+      const Tiling t8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256 * kR8C, wps);
       const int g8 = (int)cdiv(t8.warps, 8);
       static const cudaError_t attr8 = [] {
         cudaError_t e = cudaFuncSetAttribute(k_rank1_p8<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kR8Smem);
@@ -2020,23 +2038,24 @@ struct DetectOut {
 // appends them to the global list with ONE atomic on the list cursor per
 // flush (a single hot address otherwise hit once per (row, chunk) with flags).
 constexpr int DS_Q = 256;   // queued lane words per warp (>= 32: one row always fits)
-template <typename WT>
+template <typename WT, int CAP = DS_Q>
 struct DetectQueueT {
-  unsigned rl[DS_Q];   // (row - slab start) << 5 | lane
-  WT w[DS_Q];          // flag word; its bit -> column mapping belongs to the kernel
+  static constexpr int kCap = CAP;
+  unsigned rl[CAP];   // (row - slab start) << 5 | lane
+  WT w[CAP];          // flag word; its bit -> column mapping belongs to the kernel
 };
 // int32 / int16 readers: bit v*4+c <-> column 4*group_of(m16, chunk, v, lane) + c
 using DetectQueue = DetectQueueT<unsigned short>;
 
-template <typename T, typename WT, typename ColOf>
-__device__ __forceinline__ void detect_flush_q(const DetectQueueT<WT>& Q, int cnt, int64_t i_lo,
+template <typename T, typename WT, int CAP, typename ColOf>
+__device__ __forceinline__ void detect_flush_q(const DetectQueueT<WT, CAP>& Q, int cnt, int64_t i_lo,
                                                const DetectOut<T>& o, int lane, ColOf col_of);
 // The final flush of a CTA's warps together: one atomic on the list cursor per
 // CTA instead of one per warp (every warp of a launch ends with a flush: one
 // hot word serialised ~20K atomics per pass).  Every thread of the CTA calls
 // it (cnt = 0 for a warp without work).
-template <typename T, typename WT, typename ColOf>
-__device__ __forceinline__ void detect_flush_q_cta(const DetectQueueT<WT>& Q, int cnt, int64_t i_lo,
+template <typename T, typename WT, int CAP, typename ColOf>
+__device__ __forceinline__ void detect_flush_q_cta(const DetectQueueT<WT, CAP>& Q, int cnt, int64_t i_lo,
                                                    const DetectOut<T>& o, int lane, ColOf col_of) {
   __shared__ unsigned s_tot[32];
   __shared__ unsigned long long s_base[32];
@@ -2089,8 +2108,8 @@ __device__ __forceinline__ void detect_flush(const DetectQueue& Q, int cnt, int6
     return 4 * group_of(m16, chunk, bit >> 2, ln) + (bit & 3);
   });
 }
-template <typename T, typename WT, typename ColOf>
-__device__ __forceinline__ void detect_flush_q(const DetectQueueT<WT>& Q, int cnt, int64_t i_lo,
+template <typename T, typename WT, int CAP, typename ColOf>
+__device__ __forceinline__ void detect_flush_q(const DetectQueueT<WT, CAP>& Q, int cnt, int64_t i_lo,
                                                const DetectOut<T>& o, int lane, ColOf col_of) {
   if (cnt == 0) return;
   __syncwarp();
@@ -2439,8 +2458,12 @@ __global__ void k_detect_rows(Rows r, const int* __restrict__ rowcnt, int64_t* r
 // 1024 columns of a row: lane l the 16-byte groups at 16 l and 512 + 16 l.
 // Row k (the removed node) is given c = INF: then u >= 0x7F - ... never 0
 // there (its d equals r), and the diagonal is masked in the rare path.
+#ifndef D8_CW
+#define D8_CW 1   // KB of a row per copy (2: 2048 columns per warp, one row per stage —
+                  // measured 218 against 215 us per BJ.c4 detection: no gain)
+#endif
 #ifndef D8_R
-#define D8_R 2
+#define D8_R (D8_CW == 2 ? 1 : 2)
 #endif
 #ifndef D8_S
 #define D8_S 3
@@ -2466,9 +2489,10 @@ __global__ void k_detect_rows(Rows r, const int* __restrict__ rowcnt, int64_t* r
 // Stages: 3, or 4 for n >= kD8DeepN — measured: at n = 32768 (55-row slabs)
 // the fourth stage slowed the pass (225 -> 265 us), at n = 65536 (222-row
 // slabs) it sped it up 1.7x (1053 -> 606 us, 4.3 -> 7.1 TB/s; scripts/sweep*.sh)
-constexpr int kD8R = D8_R, kD8S = D8_S;   // ring: rows per stage, stages
+constexpr int kD8R = D8_R, kD8S = D8_S, kD8C = D8_CW;   // ring: rows per stage, stages; KB per row copy
+using D8Word = std::conditional_t<kD8C == 2, unsigned long long, unsigned>;
 constexpr int64_t kD8DeepN = 49152;
-template <int S> using D8Ring = WarpRing<S, kD8R, 1024>;
+template <int S> using D8Ring = WarpRing<S, kD8R, 1024 * kD8C>;
 template <int S> constexpr int d8_smem() { return 8 * D8Ring<S>::kBytes; }
 template <typename T, bool TWO, int MODE, int S>
 __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, int64_t n, int64_t skip, Tiling tl,
@@ -2476,9 +2500,14 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
                                                       const T* __restrict__ c2, const T* __restrict__ r2,
                                                       DetectOut<T> o, const __grid_constant__ CUtensorMap tm) {
   if (!detect_uses_mirror<T, 0, MODE>(o.M) || o.M.m8 == nullptr) return;
-  __shared__ DetectQueueT<unsigned> sq[MODE == 1 ? 8 : 1];
+  const bool minf = (*(volatile const unsigned*)o.M.flag & kMirrorInf) != 0u;   // some entry is INF (0x7F)
+  using WW = D8Word;   // one flag bit per column of the lane
+  constexpr int NW = 8 * kD8C;   // 4-byte words per lane and row
+  // (64-bit words: half the entries — each covers twice the columns)
+  using DQ = DetectQueueT<WW, kD8C == 2 ? DS_Q / 2 : DS_Q>;
+  __shared__ DQ sq[MODE == 1 ? 8 : 1];
   const int lane = threadIdx.x & 31;
-  DetectQueueT<unsigned>& Q = sq[MODE == 1 ? (threadIdx.x >> 5) : 0];
+  DQ& Q = sq[MODE == 1 ? (threadIdx.x >> 5) : 0];
   int qcnt = 0;
   const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   // (a warp past the last task stays for the CTA's final flush, with no rows)
@@ -2488,17 +2517,17 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
   const int64_t i_lo = r.lo + slab * tl.slab;
   const int64_t i_hi = min(r.hi, i_lo + tl.slab);
   const int rows = act ? (int)max((int64_t)0, i_hi - i_lo) : 0;
-  // this lane's columns: g0 + [0, 16) and g0 + 512 + [0, 16)
-  const int64_t g0 = (int64_t)chunk * 1024 + 16 * lane;
+  // this lane's columns: g0 + 512 g + [0, 16), g < 2 kD8C
+  const int64_t g0 = (int64_t)chunk * 1024 * kD8C + 16 * lane;
   auto col_of = [&](int bit, int ln) -> int64_t {
-    return (int64_t)chunk * 1024 + 16 * ln + (bit >> 4) * 512 + (bit & 15);
+    return (int64_t)chunk * 1024 * kD8C + 16 * ln + (bit >> 4) * 512 + (bit & 15);
   };
   auto s8 = [](T v) -> uint32_t { return (uint32_t)min((int32_t)v, kSat8i); };
   // the ring first: its copies are in flight while the pivot row is read
   extern __shared__ __align__(128) uint8_t dring_raw[];
   D8Ring<S> ring;
   ring.init(dring_raw + (threadIdx.x >> 5) * D8Ring<S>::kBytes, lane);
-  // tensor coordinates: (word column, local row)
+  // tensor coordinates: (element column, local row); 256 elements of 4 kD8C bytes per chunk
   const int cw0 = chunk * 256, rl0 = (int)(i_lo - r.row0);
   const int nst = (rows + kD8R - 1) / kD8R;
   auto issue = [&](int st) {
@@ -2510,10 +2539,10 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
   if (D8_PF > 0 && lane == 0)   // (the stages between the ring's first copies and the first prefetches)
     for (int st = S - 1; st < D8_PF && st < nst; ++st) tensor2d_prefetch_l2(&tm, cw0, rl0 + st * kD8R);
   // this lane's pivot-row bytes: 16-byte loads where the 4 columns are all < n
-  uint32_t rw[8], rw2[TWO ? 8 : 1];
-  unsigned vmask = 0;   // bit b <-> column col_of(b, lane): j < n and j != skip
+  uint32_t rw[NW], rw2[TWO ? NW : 1];
+  WW vmask = 0;   // bit b <-> column col_of(b, lane): j < n and j != skip
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
+  for (int q = 0; q < NW; ++q) {
     const int64_t j0 = g0 + (q >> 2) * 512 + (q & 3) * 4;
     uint32_t a = 0, b = 0;
     if (j0 + 3 < n) {
@@ -2534,7 +2563,7 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int64_t j = j0 + e;
-      if (j < n && j != skip) vmask |= 1u << ((q >> 2) * 16 + (q & 3) * 4 + e);
+      if (j < n && j != skip) vmask |= (WW)1 << ((q >> 2) * 16 + (q & 3) * 4 + e);
     }
     rw[q] = a;
     if (TWO) rw2[q] = b;
@@ -2563,14 +2592,18 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
       cwv[h] = cw;
       cwv2[h] = cw2;
       const uint4* rp = reinterpret_cast<const uint4*>(ring.row(st, h));
-      const uint4 w0 = rp[lane], w1 = rp[32 + lane];
-      const uint32_t d[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+      uint32_t d[NW];
+#pragma unroll
+      for (int g = 0; g < 2 * kD8C; ++g) {
+        const uint4 w = rp[32 * g + lane];
+        d[4 * g] = w.x; d[4 * g + 1] = w.y; d[4 * g + 2] = w.z; d[4 * g + 3] = w.w;
+      }
       // every byte <= 0x7F and D <= c + r: no carries or borrows between
       // bytes; the entry is tight iff its byte of u = c + r - d is 0 (the
       // classic exact zero-byte test: (u - 0x01010101) & ~u)
       uint32_t acc = 0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < NW; ++q) {
         const uint32_t u = cw + rw[q] - d[q];
         acc |= (u - 0x01010101u) & ~u;
         if (TWO) {
@@ -2588,16 +2621,20 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
       if (rr >= rows) break;   // warp-uniform
       const uint32_t acc = accv[h], cw = cwv[h], cw2 = cwv2[h];
       const uint4* rp = reinterpret_cast<const uint4*>(ring.row(st, h));
-      const uint4 w0 = rp[lane], w1 = rp[32 + lane];
-      const uint32_t d[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+      uint32_t d[NW];
+#pragma unroll
+      for (int g = 0; g < 2 * kD8C; ++g) {
+        const uint4 w = rp[32 * g + lane];
+        d[4 * g] = w.x; d[4 * g + 1] = w.y; d[4 * g + 2] = w.z; d[4 * g + 3] = w.w;
+      }
       if (!__any_sync(0xffffffffu, (acc & 0x80808080u) != 0u)) continue;
       // some lane has a tight entry in this row: exact per-byte flags of the
       // words that have a zero byte (the test above is exact per word)
       const int64_t i = i_lo + rr;
-      unsigned word = 0;
+      WW word = 0;
       if (acc & 0x80808080u) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < NW; ++q) {
           const uint32_t u = cw + rw[q] - d[q];
           uint32_t t = (u - 0x01010101u) & ~u;
           const uint32_t u2 = TWO ? cw2 + rw2[q] - d[q] : 0u;
@@ -2606,26 +2643,30 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
             uint32_t z = ~(u | ((u & 0x7F7F7F7Fu) + 0x7F7F7F7Fu)) & 0x80808080u;   // exact zero bytes
             if (TWO) z |= ~(u2 | ((u2 & 0x7F7F7F7Fu) + 0x7F7F7F7Fu)) & 0x80808080u;
             // minus the INF entries (d == 0x7F with c INF and r == 0 tests
-            // tight; INF pairs are never listed, Q5)
-            const uint32_t dq = d[q] ^ 0x7F7F7F7Fu;
-            z &= dq | ((dq & 0x7F7F7F7Fu) + 0x7F7F7F7Fu);
+            // tight; INF pairs are never listed, Q5) — only when
+            // the mirror holds any (its flag's INF bit)
+            if (minf) {
+              const uint32_t dq = d[q] ^ 0x7F7F7F7Fu;
+              z &= dq | ((dq & 0x7F7F7F7Fu) + 0x7F7F7F7Fu);
+            }
             // bytes 0..3 -> bits 4q' .. 4q'+3 of this lane's 16-column half
             const uint32_t nib = ((((z >> 7) & 0x01010101u) * 0x01020408u) >> 24) & 0xFu;
-            word |= nib << ((q >> 2) * 16 + (q & 3) * 4);
+            word |= (WW)nib << ((q >> 2) * 16 + (q & 3) * 4);
           }
         }
         word &= vmask;
         const int64_t di = i - g0;   // the diagonal j == i
-        if (di >= 0 && di < 16) word &= ~(1u << di);
-        else if (di >= 512 && di < 528) word &= ~(1u << (di - 512 + 16));
+#pragma unroll
+        for (int g = 0; g < 2 * kD8C; ++g)
+          if (di >= 512 * g && di < 512 * g + 16) word &= ~((WW)1 << (di - 512 * g + 16 * g));
       }
       if (!__any_sync(0xffffffffu, word != 0)) continue;
       if (MODE == 0) {
         if (lane == 0) o.anyrow[i] = 1;
       } else {
-        const int tot = __reduce_add_sync(0xffffffffu, (unsigned)__popc(word));
+        const int tot = __reduce_add_sync(0xffffffffu, (unsigned)__popcll((unsigned long long)word));
         if (lane == 0) atomicAdd(o.rowcnt + i, tot);
-        if (qcnt + 32 > DS_Q) {
+        if (qcnt + 32 > DQ::kCap) {
           detect_flush_q<T>(Q, qcnt, i_lo, o, lane, col_of);
           qcnt = 0;
         }
@@ -2655,7 +2696,7 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
   DetectOut<T> o{anyrow, rowcnt, prow, pcol, plb, lcap, ctr, WT, ldw, M};
   const int g = (int)cdiv(tl.warps, 8);
   // int8 mirror: 1024-column chunks
-  const Tiling tl8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256, wps8);
+  const Tiling tl8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256 * kD8C, wps8);
   const int g8 = (int)cdiv(tl8.warps, 8);
   // the int32 twin exits when a packed kernel applies (decided on the device):
   // with a mirror it is launched at its residency (2 CTAs per SM) and strides
@@ -2717,11 +2758,13 @@ cudaError_t detect8_tensor_map(void* out, const uint8_t* m8, int64_t ld, int64_t
     encode = reinterpret_cast<Encode>(fn);
   }
   if ((ld & 15) || ((uintptr_t)m8 & 15) || rows < 1) return cudaErrorInvalidValue;
-  const cuuint64_t dims[2] = {(cuuint64_t)(ld / 4), (cuuint64_t)rows};
+  // elements of 4 kD8C bytes, so that a 256-element box row is one chunk row
+  const cuuint64_t dims[2] = {(cuuint64_t)(ld / (4 * kD8C)), (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)ld};   // bytes between rows
   const cuuint32_t box[2] = {256, (cuuint32_t)kD8R};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
+  const CUresult r = encode(reinterpret_cast<CUtensorMap*>(out),
+                            kD8C == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
                             const_cast<uint8_t*>(m8), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -13,7 +13,7 @@ timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-int32 --no-verify
   timeout 900 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-int32 --no-verify --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 timeout 300 python scripts/ncu_probe.py 32768 > gpurun_out/ncu_probe_plain.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_detect_p8|k_sparse_phase_aq|k_sparse_short|k_sparse_rounds_coop|k_addcol_mt|k_addrow|k_rank1_p8|k_query_scan|k_query_solve|k_update_prep" -c 16 -o gpurun_out/hot_full python scripts/ncu_probe.py 32768 > gpurun_out/ncu_hot.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_detect_p8|k_phase_a0|k_sparse_phase_aq|k_sparse_short|k_sparse_full|k_sparse_rounds_coop|k_addcol_mt|k_addrow|k_rank1_p8|k_validate_vec|k_query_scan|k_query_solve|k_update_prep" -c 20 -o gpurun_out/hot_full python scripts/ncu_probe.py 32768 > gpurun_out/ncu_hot.log 2>&1
 python scripts/make_traffic.py gpurun_out/hot_full.ncu-rep > gpurun_out/traffic.json 2> gpurun_out/traffic.err
 python scripts/ncu_summary.py gpurun_out/ncu_hot_kernels.json gpurun_out/hot_full.ncu-rep > gpurun_out/ncu_sum.log 2>&1
 # the 4-byte streams (mirror off) and fp32, n = 32768: detection, pass 1, rank-1

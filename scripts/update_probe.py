@@ -2,7 +2,7 @@
 (n=65536 int32 log-uniform), after a warm-up one, inside the NVTX range
 "probe" (ncu --nvtx --nvtx-include "probe/" lists just its launches).
 
-    python scripts/update_probe.py c2|c5 [--bench-edge]
+    python scripts/update_probe.py c2|c5 [--bench-edge] [--heavy N]
 
 --bench-edge: the tight increase scripts/bench_configs.py times (the cheapest
 edge of synth.random_edge(seed, 2)'s tail), after one on the next node.
@@ -22,6 +22,8 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 spec = synth.CONFIGS[cfg]
 W = synth.graph(spec)
 h = P.WarmAPSP(torch.from_numpy(W), directed=spec.directed)
+if "--heavy" in sys.argv:   # APSP_OPT_HEAVY (0 default, -1 never, else the row threshold)
+    h.set_option(P._lib.OPT_HEAVY, float(sys.argv[sys.argv.index("--heavy") + 1]))
 INF = synth.INF_I32
 
 

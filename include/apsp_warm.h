@@ -284,7 +284,9 @@ apsp_status sp_pair_query(apsp_handle* h, int64_t s, int64_t t, void* dist, int3
 /* Batched form, all arrays on the device: s[q], t[q] -> dist[q],
  * paths[q*path_cap ...], path_lens[q] (-1: path_cap too small, -2: candidate
  * overflow), n_cand[q] (may be NULL).  Asynchronous.  Ids are validated on the
- * device (an out-of-range pair gets path_len -3). */
+ * device (an out-of-range pair gets path_len -3).  One GPU, q > 1024: the
+ * queries run in groups sorted by t (queries sharing a target share column
+ * t's reads); every answer still lands in its own slot. */
 apsp_status sp_pair_query_batch(apsp_handle* h, int32_t q, const int32_t* s, const int32_t* t,
                                 void* dist, int32_t* paths, int32_t path_cap,
                                 int32_t* path_lens, int32_t* n_cand);

@@ -52,7 +52,8 @@ struct Plan {
       off_pcol, off_ocol, off_ocnt, off_gprow, off_gpcol, off_glb, off_gfull,
       off_srow, off_scol, off_slid, off_slw, off_wnext, off_slscr, off_panel, off_pt, off_anyrow, off_qsend, off_qcol,
       off_qids, off_qdsv, off_qlab, off_qpred, off_qpath, off_qdone, off_qcnt, off_p16, off_p8, off_mt, off_ptd,
-      off_small, off_qbits, off_qbpred, off_qbout, off_qhit, off_heavy, off_bigq, total;
+      off_small, off_qbits, off_qbpred, off_qbout, off_qhit, off_heavy, off_bigq, off_qsort, total;
+  size_t qsort_temp = 0;
   int64_t ldt;   // row stride of the transposed int8 mirror (bytes >= local rows)
   int qcap, qbatch;
   int64_t ldpt;
@@ -115,6 +116,9 @@ Plan make_plan(int64_t cap, int world, int64_t ld) {
   p.off_qpath = take(4 * qe);
   p.off_qdone = take(qe);
   p.off_qcnt = take(sizeof(int32_t) * (size_t)p.qbatch);
+  // t-grouped large batches (one GPU): keys, values (in, out) + cub temp
+  p.qsort_temp = world > 1 ? 0 : query_group_temp_bytes();
+  p.off_qsort = take(world > 1 ? 256 : 4 * sizeof(int32_t) * (size_t)kQueryGroup + p.qsort_temp);
   // a single query whose candidate set exceeds qcap (query_big): bitmap,
   // predecessors, [length, path] (one GPU)
   p.off_qbits = take(sizeof(uint32_t) * (size_t)(cap / 32 + 1));
@@ -285,6 +289,10 @@ struct apsp_handle {
     q.cnt = reinterpret_cast<int*>(ws + plan.off_qcnt);
     q.qcap = plan.qcap;
     q.batch = plan.qbatch;
+    if (world == 1 && plan.qsort_temp > 0) {
+      q.sort = reinterpret_cast<int*>(ws + plan.off_qsort);
+      q.sort_temp = plan.qsort_temp;
+    }
     return q;
   }
   int* anyrow() { return reinterpret_cast<int*>(ws + plan.off_anyrow); }
@@ -1329,10 +1337,23 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
   // one GPU: both words straight into the mapped host buffer by one kernel
   T* hv = reinterpret_cast<T*>(h->host_small);
   if (h->world == 1) {
-    ReadSet rs{};
-    rs.add(WT + v * ld + u, sizeof(T));
-    rs.add(h->Drow<T>(u) + v, sizeof(T));
-    CK(readback(rs, h->host_small_dev, h->st));
+    // one warp reads both words and, when the update exits early, applies it
+    // (W and the shortlists) before the host's read — the common case costs
+    // one launch and the read
+    { apsp_status sj = join_side(h); if (sj != APSP_OK) return sj; }
+    CK(edge_early<T>(WT, ld, h->Drow<T>(u), h->slid(), h->slw<T>(), h->wnext<T>(), u, v, w_new, h->directed,
+                     h->tau, h->host_small_dev, h->st));
+    CKR(cudaStreamSynchronize(h->st));
+    if (reinterpret_cast<volatile unsigned*>(h->host_small)[2] != 0u) {
+      const T w_old = hv[0];
+      if (info) {
+        info->n_after = n;
+        info->kind = w_new == w_old ? 0 : (w_new < w_old ? 1 : 2);
+        info->early_exit = 1;
+      }
+      if (w_new != w_old) h->fold_wmin<T>(w_new);
+      return APSP_OK;
+    }
   } else {
     T* dev2 = reinterpret_cast<T*>(h->small());
     CKR(cudaMemcpyAsync(dev2, WT + v * ld + u, sizeof(T), cudaMemcpyDeviceToDevice, h->st));
@@ -1342,8 +1363,8 @@ apsp_status update_edge_impl(apsp_handle* h, int64_t u, int64_t v, T w_new, apsp
     ReadSet rs{};
     rs.add(dev2, 2 * sizeof(T));
     CK(readback(rs, h->host_small_dev, h->st));
+    CKR(cudaStreamSynchronize(h->st));
   }
-  CKR(cudaStreamSynchronize(h->st));
   const T w_old = hv[0], duv = hv[1];
   if (info) info->n_after = n;
   if (w_new == w_old) {

@@ -218,6 +218,10 @@ cudaError_t shortlist_build_one(const T* WT, int64_t ldw, int64_t n, int64_t j, 
 template <typename T>
 cudaError_t shortlist_add_bound(int* SLid, T* SLw, T* wnext, const T* out_w, int64_t n, int64_t x,
                                 cudaStream_t st);
+// one GPU: an edge update's early exits applied on the device (sparse.cu)
+template <typename T>
+cudaError_t edge_early(T* WT, int64_t ldw, const T* Du, int* SLid, T* SLw, T* wnext, int64_t u, int64_t v, T w,
+                       int directed, float tau, void* host_dev, cudaStream_t st);
 template <typename T>
 cudaError_t shortlist_set_edge(int* SLid, T* SLw, T* wnext, int64_t u, int64_t v, T w,
                                int directed, cudaStream_t st);
@@ -300,7 +304,11 @@ struct QueryScratch {
   unsigned char* done;
   int* cnt;             // |C| per slot
   int qcap, batch;
+  int* sort = nullptr;  // t-grouped batches (one GPU): 4 kQueryGroup ints + sort_temp bytes, or null
+  size_t sort_temp = 0;
 };
+constexpr int kQueryGroup = 1 << 16;   // queries per t-sorted group
+size_t query_group_temp_bytes();       // cub temp storage of one group sort
 // One query with a candidate set beyond the batch scratch (one GPU, shortest
 // path): bits (n bits), pred (n ints), cnt (1 int) scratch; out[0] = path
 // length (-2: not found), path (<= cap ids) in out + 1.

@@ -44,6 +44,7 @@
 // data) gives every rank the candidate set, and every rank solves the small
 // graph itself (WT is replicated), so the answer is on every rank without a
 // further exchange.
+#include <cub/device/device_radix_sort.cuh>
 #include "common.cuh"
 #include "kernels.h"
 
@@ -173,12 +174,14 @@ template <typename T, int SR>
 __global__ void __launch_bounds__(32) k_query_solve(
     const T* __restrict__ D, int64_t ld, const T* __restrict__ WT, int64_t ldw, int64_t n, int q,
     const int* __restrict__ S, const int* __restrict__ Tq, const int* __restrict__ cnt,
-    QScratch<T> gs, T* dist, int* paths, int path_cap, int* path_lens, int* ncand, QShard<T> sh) {
+    QScratch<T> gs, T* dist, int* paths, int path_cap, int* path_lens, int* ncand, QShard<T> sh,
+    const int* __restrict__ perm = nullptr /* output slot of query b (t-grouped batches), or null: b */) {
   __shared__ QSolveSmem<T> sm;
   const int lane = threadIdx.x;
   const T I = Tr<T>::inf();
 
   for (int b = blockIdx.x; b < q; b += gridDim.x) {
+    const int ob = perm ? perm[b] : b;   // (scratch is indexed by b, the outputs by ob)
     const int s = S[b], t = Tq[b];
     const bool bad = s < 0 || s >= n || t < 0 || t >= n;
     if (sh.colbuf && !sh.rowbuf) {
@@ -186,34 +189,34 @@ __global__ void __launch_bounds__(32) k_query_solve(
       // every other rank contributes zeros to the all-reduce(sum)
       const bool mine = bad ? sh.row0 == 0 : (s >= sh.row0 && s < sh.row0 + sh.rows);
       if (!mine) {
-        if (lane == 0) { path_lens[b] = 0; if (ncand) ncand[b] = 0; dist[b] = T(0); }
-        for (int c = lane; c < path_cap; c += 32) paths[(int64_t)b * path_cap + c] = 0;
+        if (lane == 0) { path_lens[ob] = 0; if (ncand) ncand[ob] = 0; dist[ob] = T(0); }
+        for (int c = lane; c < path_cap; c += 32) paths[(int64_t)ob * path_cap + c] = 0;
         continue;
       }
-      for (int c = lane; c < path_cap; c += 32) paths[(int64_t)b * path_cap + c] = -1;
+      for (int c = lane; c < path_cap; c += 32) paths[(int64_t)ob * path_cap + c] = -1;
       __syncwarp();
     }
     if (bad) {
-      if (lane == 0) { path_lens[b] = -3; if (ncand) ncand[b] = 0; dist[b] = I; }
+      if (lane == 0) { path_lens[ob] = -3; if (ncand) ncand[ob] = 0; dist[ob] = I; }
       continue;
     }
     const T st = sh.rowbuf ? sh.rowbuf[(int64_t)b * sh.ldr + t] : D[((int64_t)s - sh.row0) * ld + t];
     if (s == t || !Tr<T>::fin(st)) {
       if (lane == 0) {
-        dist[b] = s == t ? T(0) : I;
+        dist[ob] = s == t ? T(0) : I;
         if (s == t) {
-          if (path_cap >= 1) { paths[(int64_t)b * path_cap] = s; path_lens[b] = 1; }
-          else path_lens[b] = -1;
+          if (path_cap >= 1) { paths[(int64_t)ob * path_cap] = s; path_lens[ob] = 1; }
+          else path_lens[ob] = -1;
         } else {
-          path_lens[b] = 0;
+          path_lens[ob] = 0;
         }
-        if (ncand) ncand[b] = s == t ? 1 : 0;
+        if (ncand) ncand[ob] = s == t ? 1 : 0;
       }
       continue;
     }
     const int c = cnt[b];
     if (c > gs.qcap) {
-      if (lane == 0) { path_lens[b] = -2; if (ncand) ncand[b] = c; dist[b] = st; }
+      if (lane == 0) { path_lens[ob] = -2; if (ncand) ncand[ob] = c; dist[ob] = st; }
       continue;
     }
     const int64_t slot = (int64_t)b * gs.qcap;
@@ -239,7 +242,7 @@ __global__ void __launch_bounds__(32) k_query_solve(
     }
     __syncwarp();
     if (is < 0 || it < 0) {   // cannot happen: s and t satisfy the equality
-      if (lane == 0) { path_lens[b] = -2; if (ncand) ncand[b] = c; dist[b] = st; }
+      if (lane == 0) { path_lens[ob] = -2; if (ncand) ncand[ob] = c; dist[ob] = st; }
       continue;
     }
 
@@ -312,12 +315,12 @@ __global__ void __launch_bounds__(32) k_query_solve(
     // ---- output: the path s -> t in original ids ----
     __syncwarp();
     if (lane == 0) {
-      dist[b] = st;
-      if (ncand) ncand[b] = c;
-      path_lens[b] = len < 0 ? -2 : (len > path_cap ? -1 : len);
+      dist[ob] = st;
+      if (ncand) ncand[ob] = c;
+      path_lens[ob] = len < 0 ? -2 : (len > path_cap ? -1 : len);
     }
     if (len > 0 && len <= path_cap) {
-      int* o = paths + (int64_t)b * path_cap;
+      int* o = paths + (int64_t)ob * path_cap;
       for (int x = lane; x < len; x += 32) o[x] = ids[path[len - 1 - x]];
     }
     __syncwarp();
@@ -428,7 +431,7 @@ template <typename T, int SR>
 cudaError_t query_launch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_t n, int q,
                          const int* s, const int* t, T* dist, int* paths, int path_cap,
                          int* path_lens, int* ncand, float tau, cudaStream_t st, QShard<T> sh,
-                         const QueryScratch& qs, T wmin) {
+                         const QueryScratch& qs, T wmin, const int* perm = nullptr) {
   cudaError_t e = cudaMemsetAsync(qs.cnt, 0, sizeof(int) * q, st);
   if (e != cudaSuccess) return e;
   // node chunks: >= 4 CTAs per SM over the whole grid, >= 1 step per CTA
@@ -446,8 +449,31 @@ cudaError_t query_launch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64
   QScratch<T> gs{qs.ids, cand_d, reinterpret_cast<T*>(qs.lab), qs.pred, qs.path, qs.done, qs.qcap};
   const int grid = std::min(q, num_sms() * 16);
   k_query_solve<T, SR><<<grid, 32, 0, st>>>(D, ld, WT, ldw, n, q, s, t, qs.cnt, gs, dist, paths,
-                                            path_cap, path_lens, ncand, sh);
+                                            path_cap, path_lens, ncand, sh, perm);
   return cudaGetLastError();
+}
+
+// t-grouped batches (f3: "very large batches grouped by t"): the
+// queries of a group sorted by t, so that the queries sharing a target run
+// back to back and column t — the scan's expensive read, one sector per
+// entry — comes from L2 after its first reader.  keys/vals: t and the
+// original slot of each query of the group; the solve writes each answer to
+// its original slot (perm).
+__global__ void k_qgroup_init(const int* __restrict__ t, int b0, int c, int* keys, int* vals) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < c; b += gridDim.x * blockDim.x) {
+    keys[b] = t[b0 + b];
+    vals[b] = b0 + b;
+  }
+}
+__global__ void k_qgroup_gather(const int* __restrict__ s, const int* __restrict__ vals, int c, int* s_out) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < c; b += gridDim.x * blockDim.x) s_out[b] = s[vals[b]];
+}
+// bytes of cub temp storage a group sort needs (host query, no launch)
+size_t query_group_temp_bytes() {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int*)nullptr, (int*)nullptr, (const int*)nullptr,
+                                  (int*)nullptr, kQueryGroup, 0, 32);
+  return bytes;
 }
 
 // Gather-free sharded chunk (qc <= qs.batch queries): phases 1 and 2 of f3
@@ -501,6 +527,34 @@ cudaError_t query_batch(const T* D, int64_t ld, const T* WT, int64_t ldw, int64_
                         int64_t rows) {
   if (q <= 0) return cudaSuccess;
   if (colbuf && q > qs.batch) return cudaErrorInvalidValue;   // the host chunks sharded batches
+  if (!colbuf && q > qs.batch && qs.sort) {   // large batch: t-grouped, kQueryGroup queries per sort
+    int* keys_in = qs.sort;
+    int* keys_out = keys_in + kQueryGroup;
+    int* vals_in = keys_out + kQueryGroup;
+    int* vals_out = vals_in + kQueryGroup;
+    void* temp = vals_out + kQueryGroup;
+    int bits = 1;
+    while (bits < 31 && (int64_t(1) << bits) < n) ++bits;
+    for (int g0 = 0; g0 < q; g0 += kQueryGroup) {
+      const int c = std::min(kQueryGroup, q - g0);
+      const int blocks = (c + 255) / 256;
+      k_qgroup_init<<<blocks, 256, 0, st>>>(t, g0, c, keys_in, vals_in);
+      size_t tb = qs.sort_temp;
+      cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, tb, keys_in, keys_out, vals_in, vals_out, c, 0, bits, st);
+      if (e != cudaSuccess) return e;
+      k_qgroup_gather<<<blocks, 256, 0, st>>>(s, vals_out, c, keys_in);   // keys_in := s in t order
+      for (int b0 = 0; b0 < c; b0 += qs.batch) {
+        const int cc = std::min(qs.batch, c - b0);
+        QShard<T> sh{nullptr, 0, 0, 0, cc, nullptr, 0};
+        e = sr ? query_launch<T, 1>(D, ld, WT, ldw, n, cc, keys_in + b0, keys_out + b0, dist, paths, path_cap,
+                                    path_lens, ncand, tau, st, sh, qs, wmin, vals_out + b0)
+               : query_launch<T, 0>(D, ld, WT, ldw, n, cc, keys_in + b0, keys_out + b0, dist, paths, path_cap,
+                                    path_lens, ncand, tau, st, sh, qs, wmin, vals_out + b0);
+        if (e != cudaSuccess) return e;
+      }
+    }
+    return cudaGetLastError();
+  }
   for (int b0 = 0; b0 < q; b0 += qs.batch) {
     const int c = std::min(qs.batch, q - b0);
     QShard<T> sh{colbuf, R, colbuf ? row0 : 0, rows, c, nullptr, 0};

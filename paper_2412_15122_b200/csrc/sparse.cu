@@ -583,6 +583,61 @@ cudaError_t shortlist_set_edge(int* SLid, T* SLw, T* wnext, int64_t u, int64_t v
   return cudaGetLastError();
 }
 
+// An edge update's first step on one GPU, one warp: read
+// W[u][v] and D[u][v]; if the update exits early — same weight, a decrease
+// with w_new >= D[u][v], or an increase of an edge that is not tight — apply
+// it here (W, both directions when undirected, and the shortlist entries),
+// so the host's one read finds it done.  host (mapped): [0] = W[u][v] and
+// [1] = D[u][v] as bits of T, [2] = 1 if applied here.
+template <typename T>
+__global__ void k_edge_early(T* WT, int64_t ldw, const T* Du, int* SLid, T* SLw, T* wnext, int64_t u, int64_t v,
+                             T w, int directed, float tau, unsigned* host) {
+  const int lane = threadIdx.x & 31;
+  const T w_old = WT[v * ldw + u], duv = Du[v];
+  bool early;
+  if (w == w_old) early = true;
+  else if (w < w_old) early = !(w < duv);
+  else if (Tr<T>::kFloat) early = !((double)w_old <= (double)duv * (1.0 + (double)tau));
+  else early = w_old != duv;
+  if (early && w != w_old) {
+    if (lane == 0) {
+      WT[v * ldw + u] = w;
+      if (!directed) WT[u * ldw + v] = w;
+    }
+    __syncwarp();
+    for (int dir = 0; dir < (directed ? 1 : 2); ++dir) {
+      const int64_t a = dir ? v : u, b = dir ? u : v;   // entry a of SL(b)
+      int at = -1;
+#pragma unroll
+      for (int q = 0; q < kSLK; ++q) {
+        const int e = q * 32 + lane;
+        if (SLid[b * kSL + e] == (int)a) at = e;
+      }
+      at = __reduce_max_sync(0xffffffffu, at);
+      if (at >= 0) sl_place_warp<T>(SLid + b * kSL, SLw + b * kSL, at, (int)a, w);
+      else shortlist_insert_warp<T>(SLid, SLw, wnext, b, (int)a, w);
+      __syncwarp();
+    }
+  }
+  if (lane == 0) {
+    unsigned b0, b1;
+    memcpy(&b0, &w_old, sizeof b0);
+    memcpy(&b1, &duv, sizeof b1);
+    volatile unsigned* hv = host;
+    hv[0] = b0;
+    hv[1] = b1;
+    hv[2] = early ? 1u : 0u;
+    __threadfence_system();
+  }
+}
+template <typename T>
+cudaError_t edge_early(T* WT, int64_t ldw, const T* Du, int* SLid, T* SLw, T* wnext, int64_t u, int64_t v, T w,
+                       int directed, float tau, void* host_dev, cudaStream_t st) {
+  k_edge_early<T><<<1, 32, 0, st>>>(WT, ldw, Du, SLid, SLw, wnext, u, v, w, directed, tau,
+                                    reinterpret_cast<unsigned*>(host_dev));
+  return cudaGetLastError();
+}
+
 // Removal of k with node `last` moving into slot k: entries naming k die
 // (weight INF), entries naming `last` are renamed k, row k takes row last.
 template <typename T>
@@ -1958,6 +2013,8 @@ cudaError_t sparse_round(T* D, int64_t ld, int64_t row0, const T* WT, int64_t ld
   template cudaError_t shortlist_set_edge<T>(int*, T*, T*, int64_t, int64_t, T, int, cudaStream_t); \
   template cudaError_t shortlist_swap<T>(int*, T*, T*, int64_t, int64_t, int64_t, cudaStream_t);    \
   template cudaError_t shortlist_remove<T>(int*, T*, T*, int64_t, int64_t, int64_t, cudaStream_t); \
+  template cudaError_t edge_early<T>(T*, int64_t, const T*, int*, T*, T*, int64_t, int64_t, T, int, float, void*, \
+                                     cudaStream_t);                                                  \
   template cudaError_t sparse_short<T>(T*, int64_t, int64_t, const int*, const T*, const T*,       \
                                        const int*, const int*, const T*, int64_t, unsigned char*,  \
                                        int, int, const DetectCounters*, cudaStream_t, Mirror, int64_t);            \

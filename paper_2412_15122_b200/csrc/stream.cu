@@ -143,7 +143,12 @@ template <typename T>
 cudaError_t validate_vec(const T* in, const T* in2, int64_t n, int64_t npad, T* out,
                          unsigned int* err, unsigned* wmin_bits, cudaStream_t st, const T* inb,
                          const T* in2b, T* outb, unsigned long long* argmin0, unsigned* min1, ValidateReadback rb) {
-  const int grid = (int)std::min<int64_t>(cdiv(npad, 256), 4 * num_sms());
+  // 4 entries per thread: fewer blocks behind the block-level atomics and the
+  // last-block read-out (the launch is on the add's critical path)
+#ifndef VALIDATE_EPT
+#define VALIDATE_EPT 4
+#endif
+  const int grid = (int)std::min<int64_t>(cdiv(npad, 256 * VALIDATE_EPT), 4 * num_sms());
   k_validate_vec<T><<<dim3(grid, inb ? 2 : 1), 256, 0, st>>>(in, in2, n, npad, out, err, wmin_bits, inb, in2b,
                                                             outb, argmin0, min1, rb);
   return cudaGetLastError();
@@ -2419,10 +2424,15 @@ __global__ void __launch_bounds__(256, 3) k_detect_p16(T* __restrict__ D, int64_
 // open pairs), Phi (rows with a non-empty list) and max |A_i|.
 __global__ void k_detect_rows(Rows r, const int* __restrict__ rowcnt, int64_t* rowoff,
                               DetectCounters* ctr) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t i0 = r.lo + (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; i0 < r.hi;
-       i0 += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = i0 + lane;
+  // a CTA takes 256 consecutive rows per step: warp scans, then the CTA's
+  // totals behind one atomic per counter (per-warp atomics on the three
+  // counter words serialised at L2)
+  __shared__ int s_tot[8];
+  __shared__ unsigned s_nz[8], s_mx[8];
+  __shared__ unsigned long long s_base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t b0 = r.lo + (int64_t)blockIdx.x * 256; b0 < r.hi; b0 += (int64_t)gridDim.x * 256) {
+    const int64_t i = b0 + threadIdx.x;
     const int c = i < r.hi ? rowcnt[i] : 0;
     int incl = c;
 #pragma unroll
@@ -2430,17 +2440,23 @@ __global__ void k_detect_rows(Rows r, const int* __restrict__ rowcnt, int64_t* r
       const int y = __shfl_up_sync(0xffffffffu, incl, off);
       if (lane >= off) incl += y;
     }
-    const int tot = __shfl_sync(0xffffffffu, incl, 31);
     const unsigned nz = __ballot_sync(0xffffffffu, c > 0);
     const unsigned mx = __reduce_max_sync(0xffffffffu, (unsigned)c);
-    unsigned long long base = 0;
-    if (lane == 0 && tot) {
-      base = atomicAdd(&ctr->rowbase, (unsigned long long)tot);
-      atomicAdd(&ctr->rows, (unsigned)__popc(nz));
-      atomicMax(&ctr->maxrow, mx);
+    if (lane == 31) { s_tot[warp] = incl; s_nz[warp] = (unsigned)__popc(nz); s_mx[warp] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long tot = 0;
+      unsigned rows = 0, m = 0;
+      for (int w = 0; w < 8; ++w) { tot += s_tot[w]; rows += s_nz[w]; m = max(m, s_mx[w]); }
+      s_base = tot ? atomicAdd(&ctr->rowbase, (unsigned long long)tot) : 0ull;
+      if (rows) atomicAdd(&ctr->rows, rows);
+      if (m) atomicMax(&ctr->maxrow, m);
     }
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (c > 0) rowoff[i] = (int64_t)base + incl - c;
+    __syncthreads();
+    long long before = 0;
+    for (int w = 0; w < warp; ++w) before += s_tot[w];
+    if (c > 0) rowoff[i] = (int64_t)(s_base + before) + incl - c;
+    __syncthreads();   // (the shared words are rewritten next step)
   }
 }
 

@@ -163,6 +163,17 @@ def c5():
                                            "mean_candidates": nc})
     t4, _ = timed(lambda: h.query(int(s[0]), int(tt[0])))
     emit("c5", "query_single", [t4], n)
+    # a large batch (t-grouped: 16384 queries over 256 targets, f3)
+    s2, t2q = synth.query_pairs(spec.seed + 1, n, 16384)
+    t2q = t2q[np.arange(16384) % 256]   # 64 queries per target
+    sd2, td2 = torch.from_numpy(s2).cuda(), torch.from_numpy(np.ascontiguousarray(t2q)).cuda()
+    ms2 = []
+    for rep in range(3):
+        t5, res2 = timed(lambda: h.query_batch(sd2, td2, path_cap=16))
+        ms2.append(t5)
+    emit("c5", "query_batch_16384_grouped", ms2, n, {"queries_per_s": 16384 / (statistics.median(ms2) / 1e3),
+                                                    "targets": 256,
+                                                    "mean_candidates": res2[3].float().mean().item()})
 
 
 def c4f1():

@@ -519,6 +519,29 @@ def test_query_batch_matches_single(lib, rng):
         _check_path(W, D, int(s[q]), int(t[q]), dist[q], p)
 
 
+def test_query_large_batch_grouped_by_t(lib, rng):
+    """A batch beyond one launch pair (1024 queries) runs t-grouped (f3: the
+    queries sorted by target, answers written back to their own slots):
+    3000 queries over 40 targets, every answer vs the oracle's D and a valid
+    shortest path; the same pairs one by one give the same paths' lengths."""
+    spec = dataclasses.replace(synth.C5, n=400)
+    W = synth.graph(spec)
+    h = make(lib, W)
+    D = oracle.fw(W)
+    q = 3000
+    s = rng.integers(0, 400, q).astype(np.int32)
+    t = rng.choice(rng.permutation(400)[:40], q).astype(np.int32)
+    dist, paths, lens, nc = h.query_batch(s, t, path_cap=64)
+    dist, paths, lens, nc = dist.cpu().numpy(), paths.cpu().numpy(), lens.cpu().numpy(), nc.cpu().numpy()
+    for k in range(q):
+        assert dist[k] == D[s[k], t[k]], k
+        p = paths[k, : lens[k]].tolist()
+        _check_path(W, D, int(s[k]), int(t[k]), dist[k], p)
+    for k in rng.choice(q, 20, replace=False):
+        d1, p1, n1 = h.query(int(s[k]), int(t[k]), path_cap=64)
+        assert d1 == dist[k] and len(p1) == lens[k] and n1 == nc[k]
+
+
 def test_query_fp32_and_cycle(lib):
     spec = dataclasses.replace(synth.C2, n=256)
     W = synth.graph(spec)
@@ -645,6 +668,33 @@ def test_row_delta_gate_paper_definition1(lib, rng):
         hg.remove_node(k)
         assert ia.cost == ib.cost and ia.cost > 0.01
         assert ia.path == 3 and ib.path == 2
+        Da = getD(a)
+        assert np.array_equal(Da, getD(b))
+        assert_parity(Da, oracle.fw(hg.W))
+
+
+@pytest.mark.parametrize("opt,value", [(1, 1e-9), (3, 1)])
+def test_removal_gate_theta_and_rounds(lib, rng, opt, value):
+    """The pair-level gate (APSP_OPT_THETA: dense iff |A| > theta n^2) and an
+    exhausted round budget (APSP_OPT_MAX_ROUNDS) both send a removal to the
+    dense path after the sparse kernels ran; the swap-with-last that one GPU
+    enqueues before the host's read must then stand aside (it is gated on
+    the device by the same decision) — results equal the oracle and the
+    default handle's, for a removal of an inner node, the first and the last."""
+    n = 240
+    W = random_graph(rng, n, True, 1.0, lo=1, hi=100)
+    a = make(lib, W)
+    b = make(lib, W)
+    a.set_option(opt, value)
+    b.set_option(1, 0.9)   # b: the sparse path (|A| <= 0.9 n^2)
+    hg = synth.HostGraph(W, True)
+    for k in (5, 0, n - 3):
+        _, ia = a.remove_node(k)
+        _, ib = b.remove_node(k)
+        hg.remove_node(k)
+        assert ib.path == 2
+        if opt == 1:
+            assert ia.path == 3
         Da = getD(a)
         assert np.array_equal(Da, getD(b))
         assert_parity(Da, oracle.fw(hg.W))

@@ -1063,8 +1063,11 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_a(T* D, int64_t l
 // many steps as its slowest lane (ncu: ~6 batches per 32 pairs where the
 // average pair needs ~1.3); here a warp runs ~sum(steps)/32.
 constexpr int kPAChunk = 8;   // pairs per warp chunk = 32 * kPAChunk
+#ifndef PA_WPC
+#define PA_WPC 8   // warps per CTA of the work-queue kernel
+#endif
 template <typename T, int SR, bool TWO>
-__global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_aq(T* D, int64_t ld, int64_t row0,
+__global__ void __launch_bounds__(32 * PA_WPC, PA_MINB * 8 / PA_WPC) k_sparse_phase_aq(T* D, int64_t ld, int64_t row0,
                                                          const int* __restrict__ SLid,
                                                          const T* __restrict__ SLw,
                                                          const int* __restrict__ srow,
@@ -1077,7 +1080,7 @@ __global__ void __launch_bounds__(256, PA_MINB) k_sparse_phase_aq(T* D, int64_t 
   const int lane = threadIdx.x & 31;
   unsigned mbits = 0;
   npairs = device_count(dc, npairs, list);
-  __shared__ OpenStage<T> stage_all[8];
+  __shared__ OpenStage<T> stage_all[PA_WPC];
   OpenStage<T>& stg = stage_all[threadIdx.x >> 5];
   int scnt = 0;   // (warp-uniform) pairs in the warp's stage
   const uint8_t* M8 = nullptr;
@@ -1330,7 +1333,7 @@ cudaError_t sparse_phase_a(T* D, int64_t ld, Rows r, const int* SLid, const T* S
 #define PA(SRV, TWOV)                                                                              \
   do {                                                                                             \
     if (queue)                                                                                     \
-      k_sparse_phase_aq<T, SRV, TWOV><<<grid, 256, 0, st>>>(D, ld, r.row0, SLid, SLw, srow, scol,  \
+      k_sparse_phase_aq<T, SRV, TWOV><<<grid * (8 / PA_WPC), 32 * PA_WPC, 0, st>>>(D, ld, r.row0, SLid, SLw, srow, scol,  \
                                                             npairs, c1, r1, c2, r2, tau, ol, ctr, M, nb, list, \
                                                             r1b);                                       \
     else                                                                                           \

@@ -1791,9 +1791,12 @@ __device__ __forceinline__ unsigned r8_apply_row(int32_t* __restrict__ D, int64_
 // measured at BJ.c4's adds: 1 KB chunks 39 us, 2 KB chunks 55 us per add)
 constexpr int kR8S = R8_S, kR8C = R8_CW;
 using R8Ring = WarpRing<kR8S, 1, 1024 * kR8C>;
-constexpr int kR8Smem = 8 * (R8Ring::kBytes + kR8S * (int)sizeof(R1Meta));
+#ifndef R8_WPC
+#define R8_WPC 8   // warps per CTA
+#endif
+constexpr int kR8Smem = R8_WPC * (R8Ring::kBytes + kR8S * (int)sizeof(R1Meta));
 template <bool TWO>
-__global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, int64_t ld, Rows r, int64_t n,
+__global__ void __launch_bounds__(32 * R8_WPC, 16 / R8_WPC) k_rank1_p8(int32_t* __restrict__ D, int64_t ld, Rows r, int64_t n,
                                                      Tiling tl, const int32_t* __restrict__ c,
                                                      const int32_t* __restrict__ rv, const int32_t* __restrict__ c2,
                                                      const int32_t* __restrict__ rv2,
@@ -1833,7 +1836,7 @@ __global__ void __launch_bounds__(256, 2) k_rank1_p8(int32_t* __restrict__ D, in
   R8Ring ring;
   const int warp = threadIdx.x >> 5;
   ring.init(r8_raw + warp * R8Ring::kBytes, lane);
-  R1Meta* meta = reinterpret_cast<R1Meta*>(r8_raw + 8 * R8Ring::kBytes) + warp * kR8S;
+  R1Meta* meta = reinterpret_cast<R1Meta*>(r8_raw + R8_WPC * R8Ring::kBytes) + warp * kR8S;
   const uint8_t* mchunk = M.m8 + (int64_t)chunk * 1024 * kR8C - r.row0 * ld;   // + i * ld: row i's chunk
   const unsigned cbytes =
       (unsigned)((min((int64_t)1024 * kR8C, n - (int64_t)chunk * 1024 * kR8C) + 15) & ~15);
@@ -1890,7 +1893,7 @@ cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, 
     if (!sr && M.m8) {   // the int8 twin first (the int32 kernel then exits while M stays valid)
       constexpr int wps = R8_WPS;   // one wave at 2 CTAs (16 warps) per SM
       const Tiling t8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256 * kR8C, wps);
-      const int g8 = (int)cdiv(t8.warps, 8);
+      const int g8 = (int)cdiv(t8.warps, R8_WPC);
       static const cudaError_t attr8 = [] {
         cudaError_t e = cudaFuncSetAttribute(k_rank1_p8<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kR8Smem);
         if (e == cudaSuccess)
@@ -1899,9 +1902,9 @@ cudaError_t rank1(T* D, int64_t ld, Rows r, int64_t n, const T* c, const T* rv, 
       }();
       CUDA_TRY(attr8);
       if (c2)
-        k_rank1_p8<true><<<g8, 256, kR8Smem, st>>>(D, ld, r, n, t8, c, rv, c2, rv2, bytes_read, M);
+        k_rank1_p8<true><<<g8, 32 * R8_WPC, kR8Smem, st>>>(D, ld, r, n, t8, c, rv, c2, rv2, bytes_read, M);
       else
-        k_rank1_p8<false><<<g8, 256, kR8Smem, st>>>(D, ld, r, n, t8, c, rv, nullptr, nullptr, bytes_read, M);
+        k_rank1_p8<false><<<g8, 32 * R8_WPC, kR8Smem, st>>>(D, ld, r, n, t8, c, rv, nullptr, nullptr, bytes_read, M);
       if (!twin) return cudaGetLastError();
     }
   }
@@ -2496,6 +2499,13 @@ __global__ void k_detect_rows(Rows r, const int* __restrict__ rowcnt, int64_t* r
 #ifndef D8_PF
 #define D8_PF 0   // L2 prefetch distance of the detection ring, in stages beyond the ring (0: off)
 #endif
+#ifndef D8_WPC
+#define D8_WPC 1   // warps per CTA of the int8 detection: 1 = no CTA barrier, each warp flushes its own list
+                   // (BJ.c4: 218 -> 198 us per detection against 8 warps sharing one flush)
+#endif
+#ifndef D8_STRIDE
+#define D8_STRIDE 0   // 1: one resident wave of warps, each striding over row pairs (see below)
+#endif
 // A warp owns a 1024-column chunk of a row slab; lane l the 16-byte groups at
 // 16 l and 512 + 16 l.  Rows arrive through a per-warp TMA ring: one 2-D
 // tensor copy (the mirror as a uint32 tensor of local rows x ld / 4 words, box
@@ -2509,9 +2519,9 @@ constexpr int kD8R = D8_R, kD8S = D8_S, kD8C = D8_CW;   // ring: rows per stage,
 using D8Word = std::conditional_t<kD8C == 2, unsigned long long, unsigned>;
 constexpr int64_t kD8DeepN = 49152;
 template <int S> using D8Ring = WarpRing<S, kD8R, 1024 * kD8C>;
-template <int S> constexpr int d8_smem() { return 8 * D8Ring<S>::kBytes; }
+template <int S> constexpr int d8_smem() { return D8_WPC * D8Ring<S>::kBytes; }
 template <typename T, bool TWO, int MODE, int S>
-__global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, int64_t n, int64_t skip, Tiling tl,
+__global__ void __launch_bounds__(32 * D8_WPC, D8_MINB * 8 / D8_WPC) k_detect_p8(Rows r, int64_t ld, int64_t n, int64_t skip, Tiling tl,
                                                       const T* __restrict__ c1, const T* __restrict__ r1,
                                                       const T* __restrict__ c2, const T* __restrict__ r2,
                                                       DetectOut<T> o, const __grid_constant__ CUtensorMap tm) {
@@ -2521,7 +2531,7 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
   constexpr int NW = 8 * kD8C;   // 4-byte words per lane and row
   // (64-bit words: half the entries — each covers twice the columns)
   using DQ = DetectQueueT<WW, kD8C == 2 ? DS_Q / 2 : DS_Q>;
-  __shared__ DQ sq[MODE == 1 ? 8 : 1];
+  __shared__ DQ sq[MODE == 1 ? D8_WPC : 1];
   const int lane = threadIdx.x & 31;
   DQ& Q = sq[MODE == 1 ? (threadIdx.x >> 5) : 0];
   int qcnt = 0;
@@ -2530,9 +2540,22 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
   const bool act = gw < tl.warps;
   const int chunk = (int)(gw % tl.nchunk);
   const int slab = (int)(gw / tl.nchunk);
-  const int64_t i_lo = r.lo + slab * tl.slab;
-  const int64_t i_hi = min(r.hi, i_lo + tl.slab);
-  const int rows = act ? (int)max((int64_t)0, i_hi - i_lo) : 0;
+  // D8_STRIDE = 0: warp (slab, chunk) takes the tl.slab consecutive rows of
+  // its slab, several waves of CTAs per launch.  D8_STRIDE = 1: one resident
+  // wave, tl.slab (= G) warps per chunk; the warp with slab index s takes the
+  // row groups s, s + G, s + 2G, ... of kD8R rows — every warp streams the
+  // same number of groups (+-1), so a CTA's warps reach the final flush
+  // together and no CTA is retired and relaunched mid-pass (ncu showed the
+  // barrier of that flush as the top stall of the slab tiling).
+  const int64_t i_lo = D8_STRIDE ? r.lo : r.lo + slab * tl.slab;   // (queue rows are relative to it)
+  const int64_t i_hi = D8_STRIDE ? r.hi : min(r.hi, i_lo + tl.slab);
+  const int64_t ngrp = (r.hi - r.lo + kD8R - 1) / kD8R;
+  const int rows = !act ? 0 : D8_STRIDE ? (int)(slab < ngrp ? ((ngrp - 1 - slab) / tl.slab + 1) * kD8R : 0)
+                                        : (int)max((int64_t)0, i_hi - i_lo);
+  // the first row of the warp's stage q
+  auto stage_row = [&](int q) -> int64_t {
+    return D8_STRIDE ? r.lo + kD8R * ((int64_t)slab + (int64_t)q * tl.slab) : i_lo + (int64_t)q * kD8R;
+  };
   // this lane's columns: g0 + 512 g + [0, 16), g < 2 kD8C
   const int64_t g0 = (int64_t)chunk * 1024 * kD8C + 16 * lane;
   auto col_of = [&](int bit, int ln) -> int64_t {
@@ -2544,16 +2567,17 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
   D8Ring<S> ring;
   ring.init(dring_raw + (threadIdx.x >> 5) * D8Ring<S>::kBytes, lane);
   // tensor coordinates: (element column, local row); 256 elements of 4 kD8C bytes per chunk
-  const int cw0 = chunk * 256, rl0 = (int)(i_lo - r.row0);
+  const int cw0 = chunk * 256;
   const int nst = (rows + kD8R - 1) / kD8R;
   auto issue = [&](int st) {
-    if (st < nst) ring.template issue_box<D8_FENCE>(st, &tm, cw0, rl0 + st * kD8R, lane);
-    if (D8_PF > 0 && lane == 0 && st + D8_PF < nst) tensor2d_prefetch_l2(&tm, cw0, rl0 + (st + D8_PF) * kD8R);
+    if (st < nst) ring.template issue_box<D8_FENCE>(st, &tm, cw0, (int)(stage_row(st) - r.row0), lane);
+    if (D8_PF > 0 && lane == 0 && st + D8_PF < nst)
+      tensor2d_prefetch_l2(&tm, cw0, (int)(stage_row(st + D8_PF) - r.row0));
   };
 #pragma unroll
   for (int st = 0; st < S - 1; ++st) issue(st);
   if (D8_PF > 0 && lane == 0)   // (the stages between the ring's first copies and the first prefetches)
-    for (int st = S - 1; st < D8_PF && st < nst; ++st) tensor2d_prefetch_l2(&tm, cw0, rl0 + st * kD8R);
+    for (int st = S - 1; st < D8_PF && st < nst; ++st) tensor2d_prefetch_l2(&tm, cw0, (int)(stage_row(st) - r.row0));
   // this lane's pivot-row bytes: 16-byte loads where the 4 columns are all < n
   uint32_t rw[NW], rw2[TWO ? NW : 1];
   WW vmask = 0;   // bit b <-> column col_of(b, lane): j < n and j != skip
@@ -2596,10 +2620,10 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
       const int rr = st * kD8R + h;
       accv[h] = 0;
       cwv[h] = cwv2[h] = 0;
-      if (rr >= rows) continue;   // warp-uniform
+      if (stage_row(st) + h >= i_hi) continue;   // warp-uniform
       if ((rr & 31) == 0) {    // the pivot column for the next 32 rows, one per lane (INF on row k)
-        const int64_t il = i_lo + rr + lane;
-        const bool inr = rr + lane < rows;
+        const int64_t il = stage_row(st + lane / kD8R) + lane % kD8R;
+        const bool inr = rr + lane < rows && il < i_hi;
         cl = (inr && il != skip) ? s8(c1[il]) * 0x01010101u : 0x7F7F7F7Fu;
         if (TWO) cl2 = (inr && il != skip) ? s8(c2[il]) * 0x01010101u : 0x7F7F7F7Fu;
       }
@@ -2633,8 +2657,8 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
     if (D8_VOTE2 && !__any_sync(0xffffffffu, (accs & 0x80808080u) != 0u)) continue;
 #pragma unroll
     for (int h = 0; h < kD8R; ++h) {
-      const int rr = st * kD8R + h;
-      if (rr >= rows) break;   // warp-uniform
+      const int64_t i = stage_row(st) + h;
+      if (i >= i_hi) break;   // warp-uniform
       const uint32_t acc = accv[h], cw = cwv[h], cw2 = cwv2[h];
       const uint4* rp = reinterpret_cast<const uint4*>(ring.row(st, h));
       uint32_t d[NW];
@@ -2646,7 +2670,6 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
       if (!__any_sync(0xffffffffu, (acc & 0x80808080u) != 0u)) continue;
       // some lane has a tight entry in this row: exact per-byte flags of the
       // words that have a zero byte (the test above is exact per word)
-      const int64_t i = i_lo + rr;
       WW word = 0;
       if (acc & 0x80808080u) {
 #pragma unroll
@@ -2696,7 +2719,10 @@ __global__ void __launch_bounds__(256, D8_MINB) k_detect_p8(Rows r, int64_t ld, 
       }
     }
   }
-  if (MODE == 1) detect_flush_q_cta<T>(Q, qcnt, i_lo, o, lane, col_of);
+  if (MODE == 1) {
+    if (D8_WPC == 1) detect_flush_q<T>(Q, qcnt, i_lo, o, lane, col_of);
+    else detect_flush_q_cta<T>(Q, qcnt, i_lo, o, lane, col_of);
+  }
 }
 
 template <typename T>
@@ -2712,8 +2738,15 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
   DetectOut<T> o{anyrow, rowcnt, prow, pcol, plb, lcap, ctr, WT, ldw, M};
   const int g = (int)cdiv(tl.warps, 8);
   // int8 mirror: 1024-column chunks
-  const Tiling tl8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256 * kD8C, wps8);
-  const int g8 = (int)cdiv(tl8.warps, 8);
+  Tiling tl8 = make_tiling(n, r.hi - r.lo, 1 << 20, 256 * kD8C, wps8);
+  if (D8_STRIDE) {   // one resident wave: G warps per chunk, each striding over row groups
+    const int64_t ngrp = cdiv(r.hi - r.lo, kD8R);
+    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(ngrp, (int64_t)num_sms() * D8_MINB * 8 / tl8.nchunk));
+    tl8.nslab = (int)G;
+    tl8.slab = G;
+    tl8.warps = G * tl8.nchunk;
+  }
+  const int g8 = (int)cdiv(tl8.warps, D8_WPC);
   // the int32 twin exits when a packed kernel applies (decided on the device):
   // with a mirror it is launched at its residency (2 CTAs per SM) and strides
   const bool packed = sr == 0 && mode != 2 && (M.m8 || M.m);
@@ -2728,13 +2761,13 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
         static const cudaError_t attr = cudaFuncSetAttribute(                                    \
             kp8, cudaFuncAttributeMaxDynamicSharedMemorySize, d8_smem<kD8S + 1>());              \
         CUDA_TRY(attr);                                                                          \
-        kp8<<<g8, 256, d8_smem<kD8S + 1>(), st>>>(r, ld, n, skip, tl8, c1, r1, c2, r2, o, tm);  \
+        kp8<<<g8, 32 * D8_WPC, d8_smem<kD8S + 1>(), st>>>(r, ld, n, skip, tl8, c1, r1, c2, r2, o, tm);  \
       } else {                                                                                   \
         auto kp8 = k_detect_p8<T, TWO, (MODE == 2 ? 0 : MODE), kD8S>;                            \
         static const cudaError_t attr = cudaFuncSetAttribute(                                    \
             kp8, cudaFuncAttributeMaxDynamicSharedMemorySize, d8_smem<kD8S>());                  \
         CUDA_TRY(attr);                                                                          \
-        kp8<<<g8, 256, d8_smem<kD8S>(), st>>>(r, ld, n, skip, tl8, c1, r1, c2, r2, o, tm);      \
+        kp8<<<g8, 32 * D8_WPC, d8_smem<kD8S>(), st>>>(r, ld, n, skip, tl8, c1, r1, c2, r2, o, tm);      \
       }                                                                                          \
     }                                                                                            \
     else if (SR == 0 && MODE != 2 && M.m)                                                        \

@@ -888,8 +888,11 @@ __device__ __forceinline__ unsigned sparse_short_body(T* D, int64_t ld, int64_t 
   }
   return mbits;
 }
+#ifndef SS_WPC
+#define SS_WPC 8   // warps per CTA of k_sparse_short
+#endif
 template <typename T, int SR>
-__global__ void __launch_bounds__(256) k_sparse_short(T* D, int64_t ld, int64_t row0,
+__global__ void __launch_bounds__(32 * SS_WPC) k_sparse_short(T* D, int64_t ld, int64_t row0,
                                                       const int* __restrict__ SLid,
                                                       const T* __restrict__ SLw,
                                                       const T* __restrict__ wnext,
@@ -913,10 +916,10 @@ cudaError_t sparse_short(T* D, int64_t ld, int64_t row0, const int* SLid, const 
   int grid = (int)std::min<int64_t>(cdiv(npairs, 8), (int64_t)num_sms() * 16);
   OpenLists<T> ol{};
   if (sr)
-    k_sparse_short<T, 1><<<grid, 256, 0, st>>>(D, ld, row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
+    k_sparse_short<T, 1><<<grid * (8 / SS_WPC), 32 * SS_WPC, 0, st>>>(D, ld, row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
                                                out, classify, ol, dc, M, skip);
   else
-    k_sparse_short<T, 0><<<grid, 256, 0, st>>>(D, ld, row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
+    k_sparse_short<T, 0><<<grid * (8 / SS_WPC), 32 * SS_WPC, 0, st>>>(D, ld, row0, SLid, SLw, wnext, prow, pcol, plb, npairs,
                                                out, classify, ol, dc, M, skip);
   return cudaGetLastError();
 }

@@ -2503,6 +2503,9 @@ __global__ void k_detect_rows(Rows r, const int* __restrict__ rowcnt, int64_t* r
 #define D8_WPC 1   // warps per CTA of the int8 detection: 1 = no CTA barrier, each warp flushes its own list
                    // (BJ.c4: 218 -> 198 us per detection against 8 warps sharing one flush)
 #endif
+#ifndef D8_Q
+#define D8_Q 256   // queued lane words per warp (>= 32)
+#endif
 #ifndef D8_STRIDE
 #define D8_STRIDE 0   // 1: one resident wave of warps, each striding over row pairs (see below)
 #endif
@@ -2530,7 +2533,7 @@ __global__ void __launch_bounds__(32 * D8_WPC, D8_MINB * 8 / D8_WPC) k_detect_p8
   using WW = D8Word;   // one flag bit per column of the lane
   constexpr int NW = 8 * kD8C;   // 4-byte words per lane and row
   // (64-bit words: half the entries — each covers twice the columns)
-  using DQ = DetectQueueT<WW, kD8C == 2 ? DS_Q / 2 : DS_Q>;
+  using DQ = DetectQueueT<WW, kD8C == 2 ? D8_Q / 2 : D8_Q>;
   __shared__ DQ sq[MODE == 1 ? D8_WPC : 1];
   const int lane = threadIdx.x & 31;
   DQ& Q = sq[MODE == 1 ? (threadIdx.x >> 5) : 0];

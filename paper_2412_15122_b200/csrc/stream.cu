@@ -2168,17 +2168,20 @@ __device__ __forceinline__ bool detect_uses_mirror(const Mirror& M) {
 
 constexpr int kDSS = 3, kDSR = 2;   // TMA ring of the 4-byte detection stream: stages, rows per stage
 using DSRing = WarpRing<kDSS, kDSR, DS_VEC * 16>;   // 2 KB per row (512 columns)
-constexpr int kDSSmem = 8 * DSRing::kBytes;
+#ifndef DS_WPC
+#define DS_WPC 8   // warps per CTA of k_detect_stream
+#endif
+constexpr int kDSSmem = DS_WPC * DSRing::kBytes;
 
 template <typename T, bool TWO, int SR, int MODE>
-__global__ void __launch_bounds__(256, 2) k_detect_stream(T* __restrict__ D, int64_t ld, Rows r,
+__global__ void __launch_bounds__(32 * DS_WPC, 16 / DS_WPC) k_detect_stream(T* __restrict__ D, int64_t ld, Rows r,
                                                           int64_t n, int64_t skip, Tiling tl,
                                                           const T* __restrict__ c1,
                                                           const T* __restrict__ r1,
                                                           const T* __restrict__ c2,
                                                           const T* __restrict__ r2, float tau,
                                                           DetectOut<T> o) {
-  __shared__ DetectQueue sq[MODE == 1 ? 8 : 1];
+  __shared__ DetectQueue sq[MODE == 1 ? DS_WPC : 1];
   const int lane = threadIdx.x & 31;
   DetectQueue& Q = sq[MODE == 1 ? (threadIdx.x >> 5) : 0];
   int qcnt = 0;   // MODE 1: queued lane words (warp-uniform)
@@ -2781,7 +2784,7 @@ cudaError_t detect(T* D, int64_t ld, Rows r, int64_t n, int64_t skip, const T* c
       static const cudaError_t attr2 =                                                           \
           cudaFuncSetAttribute(kds, cudaFuncAttributeMaxDynamicSharedMemorySize, kDSSmem);        \
       CUDA_TRY(attr2);                                                                           \
-      kds<<<gs, 256, kDSSmem, st>>>(D, ld, r, n, skip, tl, c1, r1, c2, r2, tau, o);              \
+      kds<<<gs * (8 / DS_WPC), 32 * DS_WPC, kDSSmem, st>>>(D, ld, r, n, skip, tl, c1, r1, c2, r2, tau, o);              \
     }                                                                                            \
   } while (0)
 #define BY_MODE(TWO, SR)                 \

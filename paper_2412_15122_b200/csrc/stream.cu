@@ -2169,7 +2169,8 @@ __device__ __forceinline__ bool detect_uses_mirror(const Mirror& M) {
 constexpr int kDSS = 3, kDSR = 2;   // TMA ring of the 4-byte detection stream: stages, rows per stage
 using DSRing = WarpRing<kDSS, kDSR, DS_VEC * 16>;   // 2 KB per row (512 columns)
 #ifndef DS_WPC
-#define DS_WPC 8   // warps per CTA of k_detect_stream
+#define DS_WPC 1   // warps per CTA of k_detect_stream (1: a finished warp frees its slot at once;
+                   // int32 BJ.c4 detection 6.92 -> 7.07 TB/s, profiles/r02_sweep_int32_wpc.txt)
 #endif
 constexpr int kDSSmem = DS_WPC * DSRing::kBytes;
 

@@ -488,12 +488,15 @@ def main():
     dom = max(cls_ms, key=cls_ms.get)
     ms_d, cnt_d, work_d = prof[dom]
     traffic = None
+    traffic32 = {}
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
-                traffic = json.load(f).get(dom)
+                tj = json.load(f)
+            traffic = tj.get(dom)
             traffic = traffic if isinstance(traffic, (int, float)) else None
+            traffic32 = {k: v for k, v in (tj.get("int32") or {}).items() if isinstance(v, (int, float))}
         except Exception:
             traffic = None
     if dom.startswith("fw"):
@@ -523,7 +526,7 @@ def main():
             ms32, c32, w32 = prof32[d32]
             a32 = w32 / (ms32 / 1e3) / 1e9
             roof32 = {"bound": "hbm", "kernel": d32, "achieved": a32, "peak": hbm_peak, "unit": "GB/s",
-                      "frac": a32 / hbm_peak, "traffic": None, "launches": c32,
+                      "frac": a32 / hbm_peak, "traffic": traffic32.get(d32), "launches": c32,
                       "peak_kind": f"{peak_kind} copy bandwidth",
                       "basis": "int32 D, 4 B per entry read (SURVEY §8(d-4)); APSP_OPT_MIRROR = 0",
                       "classes": {k: {"ms": round(v[0], 3), "launches": v[1],
